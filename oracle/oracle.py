@@ -1,0 +1,293 @@
+# SPDX-License-Identifier: Apache-2.0
+"""TEST INFRASTRUCTURE ONLY -- ctypes binding of the CPU oracle (liboracle.so).
+
+The oracle is the fp64 restatement of the reference hot path (see
+sort_oracle.h). Only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs may import this module, and only as the
+checker / the timed CPU reference -- never as the product path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from typing import Dict, List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+i32p = C.POINTER(C.c_int32)
+i64p = C.POINTER(C.c_int64)
+f64p = C.POINTER(C.c_double)
+f32p = C.POINTER(C.c_float)
+u8p = C.POINTER(C.c_uint8)
+
+
+class OrModelCfg(C.Structure):
+    _fields_ = [
+        ("model_dim", C.c_int), ("item_dim", C.c_int), ("action_dim", C.c_int),
+        ("scene_dim", C.c_int), ("time_dim", C.c_int), ("profile_dim", C.c_int),
+        ("n_items", C.c_int), ("n_actions", C.c_int), ("n_scenes", C.c_int),
+        ("n_time_buckets", C.c_int), ("n_profile_fields", C.c_int),
+        ("profile_vocab", C.c_int * 16), ("special_tokens", C.c_int),
+        ("layers", C.c_int), ("heads", C.c_int), ("ffn_dim", C.c_int),
+        ("qknorm", C.c_int), ("gate", C.c_int), ("rope_theta", C.c_double),
+        ("local_window", C.c_int), ("full_suffix", C.c_int), ("keep", C.c_int * 64),
+        ("keep_specials", C.c_int), ("head_hidden", C.c_int),
+    ]
+
+
+class OrSample(C.Structure):
+    _fields_ = [
+        ("timestamp", C.c_int64), ("n_hist", C.c_int), ("hist_item", i32p),
+        ("hist_action", i32p), ("hist_scene", i32p), ("hist_ts", i64p), ("n_prof", C.c_int),
+        ("profile", i32p), ("n_cand", C.c_int), ("cand_item", i32p),
+    ]
+
+
+class OracleError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"[status {status}] {msg}")
+        self.status = status
+
+
+def build() -> str:
+    src = os.path.join(_HERE, "sort_oracle.cpp")
+    if (not os.path.exists(_LIB_PATH)) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src):
+        subprocess.check_call(["make", "-s", "-C", _HERE])
+    return _LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            build()
+        L = C.CDLL(_LIB_PATH)
+        L.oracle_last_error.restype = C.c_char_p
+        L.oracle_mask_visible_count.restype = C.c_int64
+        L.oracle_model_create.argtypes = [C.POINTER(OrModelCfg), C.POINTER(C.c_void_p)]
+        L.oracle_model_destroy.argtypes = [C.c_void_p]
+        L.oracle_model_set_param.argtypes = [C.c_void_p, C.c_char_p, f64p, C.c_int, C.c_int]
+        L.oracle_tokenize.argtypes = [C.c_void_p, C.POINTER(OrSample), f64p, i32p, i32p, i32p,
+                                      i32p, i32p]
+        L.oracle_model_forward.argtypes = [C.c_void_p, C.POINTER(OrSample), f64p, f64p]
+        L.oracle_model_forward_batch.argtypes = [C.c_void_p, C.POINTER(OrSample), C.c_int,
+                                                 C.c_int, f64p]
+        L.oracle_model_layer_meta.argtypes = [C.c_void_p, C.POINTER(OrSample), i32p, i64p, i32p,
+                                              i32p]
+        L.oracle_attention_forward.argtypes = [C.c_void_p, C.c_int, f64p, C.c_int, i32p, C.c_int,
+                                               u8p, i32p, f64p]
+        L.oracle_time_bucket.argtypes = [C.c_int64, C.c_int]
+        _lib = L
+    return _lib
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        raise OracleError(status, lib().oracle_last_error().decode())
+
+
+def _p(a: np.ndarray, t):
+    return a.ctypes.data_as(t)
+
+
+# ------------------------------------------------------------------ free functions
+def time_bucket(delta: int, n_buckets: int) -> int:
+    return lib().oracle_time_bucket(int(delta), int(n_buckets))
+
+
+def build_mask(l_q: int, roles: Sequence[int], pos: Sequence[int], local_window: int,
+               full_suffix: int, query_rows: Optional[Sequence[int]] = None) -> np.ndarray:
+    roles = np.ascontiguousarray(roles, dtype=np.int32)
+    pos = np.ascontiguousarray(pos, dtype=np.int32)
+    l_kv = len(roles)
+    out = np.zeros((l_q, l_kv), dtype=np.uint8)
+    qr = None if query_rows is None else np.ascontiguousarray(query_rows, dtype=np.int32)
+    _check(lib().oracle_build_mask(l_q, l_kv, local_window, full_suffix, _p(roles, i32p),
+                                   _p(pos, i32p), None if qr is None else _p(qr, i32p),
+                                   _p(out, u8p)))
+    return out
+
+
+def geometric_schedule(prefix_len: int, depth: int, target: int) -> List[int]:
+    out = np.zeros(max(depth, 1), dtype=np.int32)
+    _check(lib().oracle_geometric_schedule(prefix_len, depth, target, _p(out, i32p)))
+    return out.tolist()
+
+
+def retained_rows(roles: Sequence[int], keep: int, keep_specials: bool) -> List[int]:
+    roles = np.ascontiguousarray(roles, dtype=np.int32)
+    out = np.zeros(len(roles), dtype=np.int32)
+    n = C.c_int(0)
+    _check(lib().oracle_retained_rows(_p(roles, i32p), len(roles), keep, int(keep_specials),
+                                      _p(out, i32p), C.byref(n)))
+    return out[: n.value].tolist()
+
+
+def prune_queries(x: np.ndarray, n: int) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = np.zeros((n, x.shape[1]))
+    _check(lib().oracle_prune_queries(_p(x, f64p), x.shape[0], x.shape[1], n, _p(out, f64p)))
+    return out
+
+
+def rmsnorm(x: np.ndarray, gain: np.ndarray) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    g = np.ascontiguousarray(gain, dtype=np.float64).reshape(-1)
+    y = np.zeros_like(x)
+    _check(lib().oracle_rmsnorm_forward(_p(x, f64p), x.shape[0], x.shape[1], _p(g, f64p),
+                                        _p(y, f64p), None))
+    return y
+
+
+def rope(x: np.ndarray, pos: Sequence[int], theta: float = 10000.0, inverse=False) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    p = np.ascontiguousarray(pos, dtype=np.int32)
+    y = np.zeros_like(x)
+    lib().oracle_rope_apply.argtypes = [f64p, C.c_int, C.c_int, i32p, C.c_double, C.c_int, f64p]
+    _check(lib().oracle_rope_apply(_p(x, f64p), x.shape[0], x.shape[1], _p(p, i32p), theta,
+                                   int(inverse), _p(y, f64p)))
+    return y
+
+
+def dense_attention(q, k, v, mask, dtype=np.float64) -> np.ndarray:
+    q, k, v, mask = (np.ascontiguousarray(a, dtype=dtype) for a in (q, k, v, mask))
+    out = np.zeros((q.shape[0], v.shape[1]), dtype=dtype)
+    fn = lib().oracle_dense_masked_attention_f64 if dtype == np.float64 else \
+        lib().oracle_dense_masked_attention_f32
+    t = f64p if dtype == np.float64 else f32p
+    _check(fn(_p(q, t), _p(k, t), _p(v, t), _p(mask, t), q.shape[0], k.shape[0], q.shape[1],
+              v.shape[1], _p(out, t)))
+    return out
+
+
+def blockwise_attention(q, k, v, mask, block=16, dtype=np.float64):
+    q, k, v, mask = (np.ascontiguousarray(a, dtype=dtype) for a in (q, k, v, mask))
+    out = np.zeros((q.shape[0], v.shape[1]), dtype=dtype)
+    sk, tot = C.c_int64(0), C.c_int64(0)
+    fn = lib().oracle_blockwise_masked_attention_f64 if dtype == np.float64 else \
+        lib().oracle_blockwise_masked_attention_f32
+    t = f64p if dtype == np.float64 else f32p
+    _check(fn(_p(q, t), _p(k, t), _p(v, t), _p(mask, t), q.shape[0], k.shape[0], q.shape[1],
+              v.shape[1], block, _p(out, t), C.byref(sk), C.byref(tot)))
+    return out, sk.value, tot.value
+
+
+def swishglu(x, w_gate, w_up, w_down) -> np.ndarray:
+    x, wg, wu, wd = (np.ascontiguousarray(a, dtype=np.float64) for a in (x, w_gate, w_up, w_down))
+    out = np.zeros((x.shape[0], wd.shape[1]))
+    _check(lib().oracle_swishglu(_p(x, f64p), x.shape[0], x.shape[1], wg.shape[1], _p(wg, f64p),
+                                 _p(wu, f64p), _p(wd, f64p), _p(out, f64p)))
+    return out
+
+
+# ------------------------------------------------------------------ model
+class _SampleHold:
+    """Keeps the numpy buffers alive while an OrSample points into them."""
+
+    def __init__(self, batch: Dict[str, np.ndarray], b: int):
+        self.arrs = {
+            "hist_item": np.ascontiguousarray(batch["hist_item"][b], dtype=np.int32),
+            "hist_action": np.ascontiguousarray(batch["hist_action"][b], dtype=np.int32),
+            "hist_scene": np.ascontiguousarray(batch["hist_scene"][b], dtype=np.int32),
+            "hist_ts": np.ascontiguousarray(batch["hist_ts"][b], dtype=np.int64),
+            "profile": np.ascontiguousarray(batch["profile"][b], dtype=np.int32),
+            "cand_item": np.ascontiguousarray(batch["cand_item"][b], dtype=np.int32),
+        }
+        a = self.arrs
+        self.s = OrSample(int(batch["req_ts"][b]), len(a["hist_item"]), _p(a["hist_item"], i32p),
+                          _p(a["hist_action"], i32p), _p(a["hist_scene"], i32p),
+                          _p(a["hist_ts"], i64p), len(a["profile"]), _p(a["profile"], i32p),
+                          len(a["cand_item"]), _p(a["cand_item"], i32p))
+
+
+class OracleModel:
+    def __init__(self, cfg, params: Dict[str, np.ndarray]):
+        c = OrModelCfg()
+        c.model_dim, c.item_dim, c.action_dim = cfg.model_dim, cfg.item_dim, cfg.action_dim
+        c.scene_dim, c.time_dim, c.profile_dim = cfg.scene_dim, cfg.time_dim, cfg.profile_dim
+        c.n_items, c.n_actions, c.n_scenes = cfg.n_items, cfg.n_actions, cfg.n_scenes
+        c.n_time_buckets, c.n_profile_fields = cfg.n_time_buckets, len(cfg.profile_vocab)
+        for i, v in enumerate(cfg.profile_vocab):
+            c.profile_vocab[i] = v
+        c.special_tokens = int(cfg.special_tokens)
+        c.layers, c.heads, c.ffn_dim = cfg.layers, cfg.heads, cfg.ffn_dim
+        c.qknorm, c.gate, c.rope_theta = int(cfg.qknorm), int(cfg.gate), cfg.rope_theta
+        c.local_window, c.full_suffix = cfg.local_window, cfg.full_suffix
+        for i, k in enumerate(cfg.keep_schedule()):
+            c.keep[i] = k
+        c.keep_specials, c.head_hidden = int(cfg.keep_specials), cfg.head_hidden
+        self.cfg = cfg
+        h = C.c_void_p()
+        _check(lib().oracle_model_create(C.byref(c), C.byref(h)))
+        self.h = h
+        for name, a in params.items():
+            a64 = np.ascontiguousarray(a, dtype=np.float64)
+            _check(lib().oracle_model_set_param(self.h, name.encode(), _p(a64, f64p),
+                                                a64.shape[0], a64.shape[1]))
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.oracle_model_destroy(self.h)
+            self.h = None
+
+    def tokenize(self, batch, b: int = 0):
+        hold = _SampleHold(batch, b)
+        cfg = self.cfg
+        L = (3 if cfg.special_tokens else 0) + hold.s.n_hist + hold.s.n_prof + hold.s.n_cand
+        tokens = np.zeros((L, cfg.model_dim))
+        pos, roles, cidx = (np.zeros(L, np.int32) for _ in range(3))
+        ht = np.zeros(max(hold.s.n_hist, 1), np.int32)
+        n = C.c_int(0)
+        _check(lib().oracle_tokenize(self.h, C.byref(hold.s), _p(tokens, f64p), _p(pos, i32p),
+                                     _p(roles, i32p), _p(cidx, i32p), _p(ht, i32p), C.byref(n)))
+        return {"tokens": tokens, "position_ids": pos, "roles": roles, "candidate_index": cidx,
+                "hist_time": ht[: hold.s.n_hist]}
+
+    def forward(self, batch, b: int = 0):
+        hold = _SampleHold(batch, b)
+        n = hold.s.n_cand
+        probs, logits = np.zeros((n, 3)), np.zeros((n, 3))
+        _check(lib().oracle_model_forward(self.h, C.byref(hold.s), _p(probs, f64p),
+                                          _p(logits, f64p)))
+        return probs, logits
+
+    def forward_batch(self, batch, threads: int = 1, limit: Optional[int] = None) -> np.ndarray:
+        B = batch["req_ts"].shape[0] if limit is None else limit
+        holds = [_SampleHold(batch, b) for b in range(B)]
+        arr = (OrSample * B)(*[h.s for h in holds])
+        total = sum(h.s.n_cand for h in holds)
+        probs = np.zeros((total, 3))
+        _check(lib().oracle_model_forward_batch(self.h, arr, B, threads, _p(probs, f64p)))
+        return probs
+
+    def layer_meta(self, batch, b: int = 0):
+        hold = _SampleHold(batch, b)
+        nl = self.cfg.layers
+        lq = np.zeros(nl, np.int32)
+        vis = np.zeros(nl, np.int64)
+        L = (3 if self.cfg.special_tokens else 0) + hold.s.n_hist + hold.s.n_prof + hold.s.n_cand
+        qr = np.zeros(L * nl, np.int32)
+        tot = C.c_int(0)
+        _check(lib().oracle_model_layer_meta(self.h, C.byref(hold.s), _p(lq, i32p), _p(vis, i64p),
+                                             _p(qr, i32p), C.byref(tot)))
+        rows, off = [], 0
+        for l in range(nl):
+            rows.append(qr[off: off + lq[l]].tolist())
+            off += lq[l]
+        return {"l_q": lq.tolist(), "visible": vis.tolist(), "query_rows": rows}
+
+    def attention(self, layer: int, xn: np.ndarray, query_rows, visible: np.ndarray, pos):
+        xn = np.ascontiguousarray(xn, dtype=np.float64)
+        qr = np.ascontiguousarray(query_rows, dtype=np.int32)
+        vis = np.ascontiguousarray(visible, dtype=np.uint8)
+        p = np.ascontiguousarray(pos, dtype=np.int32)
+        out = np.zeros((len(qr), self.cfg.model_dim))
+        _check(lib().oracle_attention_forward(self.h, layer, _p(xn, f64p), xn.shape[0],
+                                              _p(qr, i32p), len(qr), _p(vis, u8p), _p(p, i32p),
+                                              _p(out, f64p)))
+        return out

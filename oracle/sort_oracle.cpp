@@ -1,0 +1,854 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// TEST INFRASTRUCTURE ONLY -- CPU oracle for the SORT hot path (see sort_oracle.h).
+//
+// fp64 restatement of the reference algorithm, written from its semantics
+// (no Eigen: the reference's Eigen dependency is absent in this image, so the
+// matrix kernels below are plain loops). Each function cites the reference
+// file:line it follows; paths are relative to /root/reference.
+// Parity: pinned only against SPEC.md known-answer examples and SURVEY.md
+// derived counts (tests/test_oracle_kat.py) -- "parity unpinned" at the
+// Eigen GEMM boundary, as DESIGN.md states.
+
+#include "sort_oracle.h"
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_err;
+
+struct ConfigError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct RuntimeFailure : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const ConfigError& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const RuntimeFailure& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
+}
+
+constexpr double kRmsEps = 1e-6;  // norm.hpp:8
+
+// ------------------------------------------------------------------ matrices
+struct M {
+  int r = 0, c = 0;
+  std::vector<double> a;
+  M() = default;
+  M(int rows, int cols) : r(rows), c(cols), a(static_cast<size_t>(rows) * cols, 0.0) {}
+  double* row(int i) { return a.data() + static_cast<size_t>(i) * c; }
+  const double* row(int i) const { return a.data() + static_cast<size_t>(i) * c; }
+  double& operator()(int i, int j) { return a[static_cast<size_t>(i) * c + j]; }
+  double operator()(int i, int j) const { return a[static_cast<size_t>(i) * c + j]; }
+};
+
+// C[M,N] = A[M,K] * B[K,N], row-major, i-k-j order (inner loop contiguous).
+void matmul(const double* A, const double* B, double* C, int Mr, int K, int N) {
+  std::fill(C, C + static_cast<size_t>(Mr) * N, 0.0);
+  constexpr int KB = 128;
+  for (int k0 = 0; k0 < K; k0 += KB) {
+    const int k1 = std::min(K, k0 + KB);
+    for (int i = 0; i < Mr; ++i) {
+      double* c = C + static_cast<size_t>(i) * N;
+      const double* a = A + static_cast<size_t>(i) * K;
+      for (int k = k0; k < k1; ++k) {
+        const double av = a[k];
+        const double* b = B + static_cast<size_t>(k) * N;
+        for (int j = 0; j < N; ++j) c[j] += av * b[j];
+      }
+    }
+  }
+}
+M matmul(const M& A, const M& B) {
+  M C(A.r, B.c);
+  matmul(A.a.data(), B.a.data(), C.a.data(), A.r, A.c, B.c);
+  return C;
+}
+M transpose(const M& A) {
+  M T(A.c, A.r);
+  for (int i = 0; i < A.r; ++i)
+    for (int j = 0; j < A.c; ++j) T(j, i) = A(i, j);
+  return T;
+}
+M cols_of(const M& A, int c0, int n) {
+  M out(A.r, n);
+  for (int i = 0; i < A.r; ++i) std::memcpy(out.row(i), A.row(i) + c0, sizeof(double) * n);
+  return out;
+}
+
+double sigmoid(double x) {  // common.hpp:29-35
+  if (x >= 0.0) return 1.0 / (1.0 + std::exp(-x));
+  const double e = std::exp(x);
+  return e / (1.0 + e);
+}
+double swish(double x) { return x * sigmoid(x); }  // common.hpp:37
+
+// rmsnorm_forward (norm.hpp:17-29): y = x / sqrt(mean(x^2) + eps) * gain.
+void rmsnorm_rows(const double* x, int rows, int cols, const double* gain, double* y,
+                  double* inv_out) {
+  for (int r = 0; r < rows; ++r) {
+    const double* xr = x + static_cast<size_t>(r) * cols;
+    double ss = 0.0;
+    for (int j = 0; j < cols; ++j) ss += xr[j] * xr[j];
+    const double inv = 1.0 / std::sqrt(ss / static_cast<double>(cols) + kRmsEps);
+    if (inv_out) inv_out[r] = inv;
+    double* yr = y + static_cast<size_t>(r) * cols;
+    for (int j = 0; j < cols; ++j) yr[j] = xr[j] * inv * gain[j];
+  }
+}
+M rmsnorm(const M& x, const double* gain) {
+  M y(x.r, x.c);
+  rmsnorm_rows(x.a.data(), x.r, x.c, gain, y.a.data(), nullptr);
+  return y;
+}
+
+// rope_apply (rope.hpp:13-40): interleaved pairs (2j, 2j+1), freq_j = theta^(-2j/dim).
+void rope_rows(const double* x, int rows, int dim, const int* pos, double theta, bool inverse,
+               double* out) {
+  if (dim % 2 != 0) throw ConfigError("rope_apply: head dim must be even");
+  const int np = dim / 2;
+  std::vector<double> freq(np);
+  for (int j = 0; j < np; ++j)
+    freq[j] = std::pow(theta, -2.0 * static_cast<double>(j) / static_cast<double>(dim));
+  for (int r = 0; r < rows; ++r) {
+    const double p = static_cast<double>(pos[r]);
+    const double* xr = x + static_cast<size_t>(r) * dim;
+    double* o = out + static_cast<size_t>(r) * dim;
+    for (int j = 0; j < np; ++j) {
+      const double ang = (inverse ? -p : p) * freq[j];
+      const double cs = std::cos(ang), sn = std::sin(ang);
+      const double x0 = xr[2 * j], x1 = xr[2 * j + 1];
+      o[2 * j] = cs * x0 - sn * x1;
+      o[2 * j + 1] = sn * x0 + cs * x1;
+    }
+  }
+}
+
+// time_bucket (tokenizer.cpp:36-40).
+int time_bucket(int64_t delta, int nb) {
+  const int64_t d = std::max<int64_t>(delta, 0);
+  const int b = static_cast<int>(std::floor(std::log2(1.0 + static_cast<double>(d))));
+  return std::min(b, nb - 1);
+}
+
+// build_mask (mask.cpp:14-76); visible[r*l_kv + c] = 1 where the reference writes 0.0.
+void build_mask(int l_q, int l_kv, int W, int F, const int* roles, const int* pos,
+                const int* query_rows, uint8_t* vis) {
+  if (l_q < 1 || l_kv < l_q) throw ConfigError("MaskSpec: need 1 <= l_q <= l_kv");
+  if (W != -1 && W < 1) throw ConfigError("MaskSpec: local_window must be >= 1 or -1 (unbounded)");
+  if (F < 0) throw ConfigError("MaskSpec: full_suffix must be >= 0");
+  // Prefix length = first candidate's position id, else one past the max position (:28-44).
+  int prefix_positions = 0;
+  bool has_cand = false;
+  for (int i = 0; i < l_kv; ++i) {
+    if (roles[i] == OR_ROLE_CAND) {
+      prefix_positions = pos[i];
+      has_cand = true;
+      break;
+    }
+  }
+  if (!has_cand)
+    for (int i = 0; i < l_kv; ++i) prefix_positions = std::max(prefix_positions, pos[i] + 1);
+
+  std::memset(vis, 0, static_cast<size_t>(l_q) * l_kv);
+  for (int r = 0; r < l_q; ++r) {
+    const int qi = query_rows ? query_rows[r] : (l_kv - l_q) + r;  // suffix overload :78-85
+    if (qi < 0 || qi >= l_kv) throw ConfigError("build_mask: query row out of range");
+    const bool q_cand = roles[qi] == OR_ROLE_CAND;
+    const int q_pos = pos[qi];
+    const bool windowed = !q_cand && W != -1 && q_pos < prefix_positions - F;  // :52-53
+    bool any = false;
+    uint8_t* vr = vis + static_cast<size_t>(r) * l_kv;
+    for (int c = 0; c <= qi && c < l_kv; ++c) {  // causal by kv index (:55)
+      const bool k_cand = roles[c] == OR_ROLE_CAND;
+      if (q_cand) {
+        if (k_cand && c != qi) continue;  // candidate diagonal (:57-60)
+      } else if (k_cand) {
+        continue;  // (:61-62)
+      } else if (windowed) {
+        const int k_pos = pos[c];
+        if (k_pos < q_pos - W + 1 || k_pos > q_pos) continue;  // (:63-66)
+      }
+      vr[c] = 1;
+      any = true;
+    }
+    if (!any) throw ConfigError("build_mask: query row " + std::to_string(r) + " has no visible key");
+  }
+}
+
+// retained_rows (mask.cpp:132-154).
+std::vector<int> retained_rows(const std::vector<int>& roles, int keep, bool keep_specials) {
+  int non_cand = 0;
+  for (int r : roles) non_cand += (r != OR_ROLE_CAND) ? 1 : 0;
+  const int kept = std::min(keep, non_cand);
+  const int drop = non_cand - kept;
+  std::vector<int> out;
+  int seen = 0;
+  for (size_t i = 0; i < roles.size(); ++i) {
+    if (roles[i] == OR_ROLE_CAND) {
+      out.push_back(static_cast<int>(i));
+      continue;
+    }
+    const bool in_suffix = seen >= drop;
+    ++seen;
+    const bool special = roles[i] == OR_ROLE_BOS || roles[i] == OR_ROLE_SEP;
+    if (in_suffix || (keep_specials && special)) out.push_back(static_cast<int>(i));
+  }
+  return out;
+}
+
+// make_geometric_schedule (mask.cpp:97-117).
+std::vector<int> geometric_schedule(int prefix_len, int depth, int target) {
+  if (depth < 1) throw ConfigError("make_geometric_schedule: depth must be >= 1");
+  if (prefix_len < 1) prefix_len = 1;
+  const int final_keep = std::min(target, prefix_len);
+  std::vector<int> keep(depth);
+  if (depth == 1) {
+    keep[0] = final_keep;
+    return keep;
+  }
+  const double ratio = static_cast<double>(final_keep) / static_cast<double>(prefix_len);
+  int prev = prefix_len;
+  for (int l = 0; l < depth; ++l) {
+    const double t = static_cast<double>(l) / static_cast<double>(depth - 1);
+    int k = static_cast<int>(std::lround(prefix_len * std::pow(ratio, t)));
+    k = std::clamp(k, final_keep, prev);
+    keep[l] = k;
+    prev = k;
+  }
+  return keep;
+}
+
+// dense_masked_attention<Scalar> (block_attention.hpp:29-52).
+template <class S>
+void dense_attention(const S* q, const S* k, const S* v, const S* mask, int lq, int lkv, int dk,
+                     int dv, S* out) {
+  const S scale = S(1) / std::sqrt(static_cast<S>(dk));
+  std::vector<S> s(lkv);
+  for (int r = 0; r < lq; ++r) {
+    S m = -std::numeric_limits<S>::infinity();
+    for (int c = 0; c < lkv; ++c) {
+      S acc = 0;
+      for (int j = 0; j < dk; ++j) acc += q[static_cast<size_t>(r) * dk + j] * k[static_cast<size_t>(c) * dk + j];
+      s[c] = acc * scale + mask[static_cast<size_t>(r) * lkv + c];
+      m = std::max(m, s[c]);
+    }
+    if (!(m > -std::numeric_limits<S>::infinity()))
+      throw std::invalid_argument("dense_masked_attention: fully masked query row");
+    S denom = 0;
+    for (int c = 0; c < lkv; ++c) {
+      s[c] = std::exp(s[c] - m);
+      denom += s[c];
+    }
+    S* o = out + static_cast<size_t>(r) * dv;
+    for (int j = 0; j < dv; ++j) o[j] = 0;
+    for (int c = 0; c < lkv; ++c) {
+      const S p = s[c] / denom;
+      for (int j = 0; j < dv; ++j) o[j] += p * v[static_cast<size_t>(c) * dv + j];
+    }
+  }
+}
+
+// blockwise_masked_attention<Scalar> (block_attention.hpp:54-134).
+template <class S>
+void blockwise_attention(const S* q, const S* k, const S* v, const S* mask, int lq, int lkv,
+                         int dk, int dv, int B, S* out, int64_t* skipped, int64_t* total) {
+  if (B < 1) throw std::invalid_argument("blockwise_masked_attention: block >= 1");
+  const S ninf = -std::numeric_limits<S>::infinity();
+  const S scale = S(1) / std::sqrt(static_cast<S>(dk));
+  *skipped = 0;
+  *total = 0;
+  std::vector<S> row_max, row_sum, acc, s, p;
+  for (int q0 = 0; q0 < lq; q0 += B) {
+    const int qn = std::min(B, lq - q0);
+    row_max.assign(qn, ninf);
+    row_sum.assign(qn, 0);
+    acc.assign(static_cast<size_t>(qn) * dv, 0);
+    for (int k0 = 0; k0 < lkv; k0 += B) {
+      const int kn = std::min(B, lkv - k0);
+      ++*total;
+      bool any = false;  // mask preload + validation (:86-99)
+      for (int r = 0; r < qn && !any; ++r)
+        for (int c = 0; c < kn; ++c)
+          if (mask[static_cast<size_t>(q0 + r) * lkv + k0 + c] == S(0)) {
+            any = true;
+            break;
+          }
+      if (!any) {
+        ++*skipped;
+        continue;
+      }
+      s.assign(static_cast<size_t>(qn) * kn, 0);
+      p.assign(static_cast<size_t>(qn) * kn, 0);
+      for (int r = 0; r < qn; ++r)
+        for (int c = 0; c < kn; ++c) {
+          S a = 0;
+          for (int j = 0; j < dk; ++j)
+            a += q[static_cast<size_t>(q0 + r) * dk + j] * k[static_cast<size_t>(k0 + c) * dk + j];
+          s[static_cast<size_t>(r) * kn + c] = a * scale + mask[static_cast<size_t>(q0 + r) * lkv + k0 + c];
+        }
+      for (int r = 0; r < qn; ++r) {  // online softmax (:104-122)
+        S tmax = ninf;
+        for (int c = 0; c < kn; ++c) tmax = std::max(tmax, s[static_cast<size_t>(r) * kn + c]);
+        if (!(tmax > ninf)) continue;  // p row stays zero
+        const S nmax = std::max(row_max[r], tmax);
+        const S corr = row_max[r] > ninf ? std::exp(row_max[r] - nmax) : S(0);
+        row_sum[r] *= corr;
+        for (int j = 0; j < dv; ++j) acc[static_cast<size_t>(r) * dv + j] *= corr;
+        S psum = 0;
+        for (int c = 0; c < kn; ++c) {
+          const S sv = s[static_cast<size_t>(r) * kn + c];
+          const S pv = sv > ninf ? std::exp(sv - nmax) : S(0);
+          p[static_cast<size_t>(r) * kn + c] = pv;
+          psum += pv;
+        }
+        row_sum[r] += psum;
+        row_max[r] = nmax;
+      }
+      for (int r = 0; r < qn; ++r)  // acc += p V (:123)
+        for (int c = 0; c < kn; ++c) {
+          const S pv = p[static_cast<size_t>(r) * kn + c];
+          if (pv == S(0)) continue;
+          for (int j = 0; j < dv; ++j)
+            acc[static_cast<size_t>(r) * dv + j] += pv * v[static_cast<size_t>(k0 + c) * dv + j];
+        }
+    }
+    for (int r = 0; r < qn; ++r) {  // normalise (:126-131)
+      if (!(row_sum[r] > S(0)))
+        throw std::invalid_argument("blockwise_masked_attention: fully masked query row");
+      for (int j = 0; j < dv; ++j)
+        out[static_cast<size_t>(q0 + r) * dv + j] = acc[static_cast<size_t>(r) * dv + j] / row_sum[r];
+    }
+  }
+}
+
+}  // namespace
+
+// ====================================================================== model
+struct OrModel {
+  OrModelCfg cfg;
+  int d = 0, dk = 0, m = 0, dh = 0;
+  std::map<std::string, M> p;
+
+  const M& P(const std::string& name) const {
+    auto it = p.find(name);
+    if (it == p.end()) throw ConfigError("oracle: missing parameter " + name);
+    return it->second;
+  }
+  int hist_width() const {
+    return cfg.item_dim + cfg.action_dim + cfg.scene_dim + cfg.time_dim;  // tokenizer.hpp:46-48
+  }
+};
+
+namespace {
+
+void check_id(int id, int vocab, const char* what) {  // tokenizer.cpp:14-19
+  if (id < 0 || id >= vocab)
+    throw ConfigError(std::string("tokenizer: ") + what + " id " + std::to_string(id) +
+                      " outside vocabulary of size " + std::to_string(vocab));
+}
+
+struct Seq {
+  M tokens;
+  std::vector<int> pos, roles, cand_index, hist_time;
+};
+
+// Tokenizer::tokenize_sample (tokenizer.cpp:144-238).
+Seq tokenize(const OrModel& mdl, const OrSample& s) {
+  const OrModelCfg& c = mdl.cfg;
+  if (s.n_cand <= 0) throw ConfigError("tokenizer: sample has zero candidates");
+  if (s.n_prof != c.n_profile_fields)
+    throw ConfigError("tokenizer: profile has " + std::to_string(s.n_prof) + " fields, expected " +
+                      std::to_string(c.n_profile_fields));
+  const bool st = c.special_tokens != 0;
+  const int nh = s.n_hist, np = s.n_prof, nc = s.n_cand;
+  const int total = (st ? 3 : 0) + nh + np + nc;
+  const int d = mdl.d;
+  Seq q;
+  q.tokens = M(total, d);
+  q.pos.assign(total, 0);
+  q.roles.assign(total, 0);
+  q.cand_index.assign(total, -1);
+  q.hist_time.assign(nh, 0);
+
+  const M& special = mdl.P("tok.special");
+  int row = 0;
+  auto put_special = [&](int srow, int role) {
+    std::memcpy(q.tokens.row(row), special.row(srow), sizeof(double) * d);
+    q.roles[row] = role;
+    ++row;
+  };
+  if (st) put_special(0, OR_ROLE_BOS);
+
+  // History group: gather item|action|scene|time rows (history_concat_row, :95-112).
+  const M& it = mdl.P("tok.item_table");
+  const M& at = mdl.P("tok.action_table");
+  const M& sc = mdl.P("tok.scene_table");
+  const M& tt = mdl.P("tok.time_table");
+  const int hw = mdl.hist_width();
+  M hcat(nh, hw);
+  std::vector<int> hrows(nh);
+  for (int i = 0; i < nh; ++i) {
+    check_id(s.hist_item[i], c.n_items, "item");
+    check_id(s.hist_action[i], c.n_actions, "action");
+    check_id(s.hist_scene[i], c.n_scenes, "scene");
+    const int tb = time_bucket(s.timestamp - s.hist_ts[i], c.n_time_buckets);
+    double* o = hcat.row(i);
+    std::memcpy(o, it.row(s.hist_item[i]), sizeof(double) * c.item_dim);
+    o += c.item_dim;
+    std::memcpy(o, at.row(s.hist_action[i]), sizeof(double) * c.action_dim);
+    o += c.action_dim;
+    std::memcpy(o, sc.row(s.hist_scene[i]), sizeof(double) * c.scene_dim);
+    o += c.scene_dim;
+    std::memcpy(o, tt.row(tb), sizeof(double) * c.time_dim);
+    q.hist_time[i] = tb;
+    hrows[i] = row;
+    q.roles[row] = OR_ROLE_HIST;
+    ++row;
+  }
+  if (st) put_special(1, OR_ROLE_SEP);
+
+  M pcat(np, c.profile_dim);
+  std::vector<int> prows(np);
+  for (int f = 0; f < np; ++f) {
+    const int v = s.profile[f];
+    check_id(v, c.profile_vocab[f], "profile");
+    const M& tab = mdl.P("tok.profile_table." + std::to_string(f));
+    std::memcpy(pcat.row(f), tab.row(v), sizeof(double) * c.profile_dim);
+    prows[f] = row;
+    q.roles[row] = OR_ROLE_PROF;
+    ++row;
+  }
+  if (st) put_special(2, OR_ROLE_SEP);
+
+  M ccat(nc, c.item_dim);
+  std::vector<int> crows(nc);
+  for (int j = 0; j < nc; ++j) {
+    check_id(s.cand_item[j], c.n_items, "item");
+    std::memcpy(ccat.row(j), it.row(s.cand_item[j]), sizeof(double) * c.item_dim);
+    crows[j] = row;
+    q.roles[row] = OR_ROLE_CAND;
+    q.cand_index[row] = j;
+    ++row;
+  }
+
+  // emit_group (:219-232): concat * W + b -> RMSNorm(gain) -> scatter into the sequence.
+  auto emit = [&](const M& cat, const std::vector<int>& rows, const char* w, const char* b,
+                  const char* g) {
+    if (cat.r == 0) return;
+    M proj = matmul(cat, mdl.P(w));
+    const M& bias = mdl.P(b);
+    for (int i = 0; i < proj.r; ++i)
+      for (int j = 0; j < d; ++j) proj(i, j) += bias(0, j);
+    M y = rmsnorm(proj, mdl.P(g).row(0));
+    for (int i = 0; i < y.r; ++i) std::memcpy(q.tokens.row(rows[i]), y.row(i), sizeof(double) * d);
+  };
+  emit(hcat, hrows, "tok.w_hist", "tok.b_hist", "tok.g_hist");
+  emit(pcat, prows, "tok.w_prof", "tok.b_prof", "tok.g_prof");
+  emit(ccat, crows, "tok.w_cand", "tok.b_cand", "tok.g_cand");
+
+  const int prefix = total - nc;  // :234-236
+  for (int i = 0; i < prefix; ++i) q.pos[i] = i;
+  for (int i = prefix; i < total; ++i) q.pos[i] = prefix;
+  return q;
+}
+
+// AttentionLayer::forward (attention.cpp:71-132).
+M attention_forward(const OrModel& mdl, int layer, const M& xn, const std::vector<int>& qrows,
+                    const uint8_t* vis, const std::vector<int>& pos) {
+  const int d = mdl.d, h = mdl.cfg.heads, dk = mdl.dk;
+  const int lq = static_cast<int>(qrows.size());
+  const int lkv = xn.r;
+  if (xn.c != d) throw RuntimeFailure("attention: input width mismatch");
+  const std::string base = "attn." + std::to_string(layer) + ".";
+  M xq(lq, d);
+  std::vector<int> pos_q(lq);
+  for (int i = 0; i < lq; ++i) {
+    std::memcpy(xq.row(i), xn.row(qrows[i]), sizeof(double) * d);  // gather_rows (:10-16)
+    pos_q[i] = pos[qrows[i]];
+  }
+  M q_raw = matmul(xq, mdl.P(base + "wq"));
+  M k_raw = matmul(xn, mdl.P(base + "wk"));
+  M v = matmul(xn, mdl.P(base + "wv"));
+  const double scale = 1.0 / std::sqrt(static_cast<double>(dk));
+  M out_pre(lq, d);
+  std::vector<double> logits(static_cast<size_t>(lq) * lkv);
+  for (int i = 0; i < h; ++i) {
+    M qh = cols_of(q_raw, i * dk, dk), kh = cols_of(k_raw, i * dk, dk);
+    if (mdl.cfg.qknorm) {  // per-head RMSNorm before RoPE (:111-114)
+      qh = rmsnorm(qh, mdl.P(base + "qk_gain_q").row(i));
+      kh = rmsnorm(kh, mdl.P(base + "qk_gain_k").row(i));
+    }
+    M qr(lq, dk), kr(lkv, dk);
+    rope_rows(qh.a.data(), lq, dk, pos_q.data(), mdl.cfg.rope_theta, false, qr.a.data());
+    rope_rows(kh.a.data(), lkv, dk, pos.data(), mdl.cfg.rope_theta, false, kr.a.data());
+    M krT = transpose(kr);
+    matmul(qr.a.data(), krT.a.data(), logits.data(), lq, dk, lkv);
+    // logits*scale + mask, then masked_softmax (:19-30, :118-119)
+    M vh = cols_of(v, i * dk, dk);
+    for (int r = 0; r < lq; ++r) {
+      double* lr = logits.data() + static_cast<size_t>(r) * lkv;
+      const uint8_t* vr = vis + static_cast<size_t>(r) * lkv;
+      double mx = -std::numeric_limits<double>::infinity();
+      for (int c = 0; c < lkv; ++c) {
+        lr[c] = vr[c] ? lr[c] * scale : -std::numeric_limits<double>::infinity();
+        mx = std::max(mx, lr[c]);
+      }
+      if (!(mx > -std::numeric_limits<double>::infinity()))
+        throw RuntimeFailure("attention: fully masked query row");
+      double sum = 0.0;
+      for (int c = 0; c < lkv; ++c) {
+        lr[c] = std::exp(lr[c] - mx);
+        sum += lr[c];
+      }
+      double* o = out_pre.row(r) + i * dk;
+      for (int c = 0; c < lkv; ++c) {
+        const double a = lr[c] / sum;
+        if (a == 0.0) continue;
+        const double* vv = vh.row(c);
+        for (int j = 0; j < dk; ++j) o[j] += a * vv[j];
+      }
+    }
+  }
+  M hcat = out_pre;
+  if (mdl.cfg.gate) {  // sigmoid gate on the gathered rows (:124-127)
+    M g = matmul(xq, mdl.P(base + "wg"));
+    for (size_t t = 0; t < hcat.a.size(); ++t) hcat.a[t] = sigmoid(g.a[t]) * out_pre.a[t];
+  }
+  return matmul(hcat, mdl.P(base + "wo"));  // (:131)
+}
+
+// swishglu_ffn: down(swish(x Wg) * (x Wu)).
+M swishglu(const M& x, const M& wg, const M& wu, const M& wd) {
+  M g = matmul(x, wg), u = matmul(x, wu);
+  for (size_t t = 0; t < g.a.size(); ++t) g.a[t] = swish(g.a[t]) * u.a[t];
+  return matmul(g, wd);
+}
+
+struct LayerTrace {
+  std::vector<int> qrows;
+  int64_t visible = 0;
+};
+
+// model_forward: pre-norm residual blocks over a shrinking
+// residual stream, final RMSNorm, ranking head on candidate rows.
+void model_forward(const OrModel& mdl, const OrSample& s, double* probs, double* logits_out,
+                   std::vector<LayerTrace>* trace) {
+  Seq q = tokenize(mdl, s);
+  M x = q.tokens;
+  std::vector<int> roles = q.roles, pos = q.pos;
+  const OrModelCfg& c = mdl.cfg;
+  const int d = mdl.d;
+  for (int l = 0; l < c.layers; ++l) {
+    const std::string L = std::to_string(l);
+    std::vector<int> qrows = retained_rows(roles, c.keep[l], c.keep_specials != 0);
+    const int lq = static_cast<int>(qrows.size()), lkv = x.r;
+    std::vector<uint8_t> vis(static_cast<size_t>(lq) * lkv);
+    build_mask(lq, lkv, c.local_window, c.full_suffix, roles.data(), pos.data(), qrows.data(),
+               vis.data());
+    if (trace) {
+      LayerTrace t;
+      t.qrows = qrows;
+      for (uint8_t v : vis) t.visible += v;
+      trace->push_back(std::move(t));
+    }
+    M xn = rmsnorm(x, mdl.P("block." + L + ".attn_norm").row(0));
+    M a = attention_forward(mdl, l, xn, qrows, vis.data(), pos);
+    M xr(lq, d);
+    std::vector<int> nroles(lq), npos(lq);
+    for (int i = 0; i < lq; ++i) {
+      const double* src = x.row(qrows[i]);
+      double* dst = xr.row(i);
+      const double* ar = a.row(i);
+      for (int j = 0; j < d; ++j) dst[j] = src[j] + ar[j];  // residual on P(x, L_out)
+      nroles[i] = roles[qrows[i]];
+      npos[i] = pos[qrows[i]];
+    }
+    M xf = rmsnorm(xr, mdl.P("block." + L + ".ffn_norm").row(0));
+    M f = swishglu(xf, mdl.P("ffn." + L + ".w_gate"), mdl.P("ffn." + L + ".w_up"),
+                   mdl.P("ffn." + L + ".w_down"));
+    for (size_t t = 0; t < xr.a.size(); ++t) xr.a[t] += f.a[t];
+    x = std::move(xr);
+    roles = std::move(nroles);
+    pos = std::move(npos);
+  }
+  // Final RMSNorm + head on candidate rows, candidates in order.
+  std::vector<int> crows;
+  for (int i = 0; i < x.r; ++i)
+    if (roles[i] == OR_ROLE_CAND) crows.push_back(i);
+  M xc(static_cast<int>(crows.size()), d);
+  for (size_t i = 0; i < crows.size(); ++i)
+    std::memcpy(xc.row(static_cast<int>(i)), x.row(crows[i]), sizeof(double) * d);
+  M xh = rmsnorm(xc, mdl.P("final_norm.gain").row(0));
+  M hid = matmul(xh, mdl.P("head.w1"));
+  const M& b1 = mdl.P("head.b1");
+  for (int i = 0; i < hid.r; ++i)
+    for (int j = 0; j < hid.c; ++j) hid(i, j) = std::max(0.0, hid(i, j) + b1(0, j));
+  M lo = matmul(hid, mdl.P("head.w2"));
+  const M& b2 = mdl.P("head.b2");
+  for (int i = 0; i < lo.r; ++i)
+    for (int j = 0; j < 3; ++j) {
+      const double z = lo(i, j) + b2(0, j);
+      if (logits_out) logits_out[i * 3 + j] = z;
+      probs[i * 3 + j] = sigmoid(z);
+    }
+}
+
+}  // namespace
+
+// ====================================================================== C API
+extern "C" {
+
+const char* oracle_last_error(void) { return g_err.c_str(); }
+
+int oracle_time_bucket(int64_t delta_seconds, int n_buckets) {
+  return time_bucket(delta_seconds, n_buckets);
+}
+
+int oracle_build_mask(int l_q, int l_kv, int local_window, int full_suffix, const int* roles,
+                      const int* position_ids, const int* query_rows, uint8_t* out_visible) {
+  return guarded([&] {
+    build_mask(l_q, l_kv, local_window, full_suffix, roles, position_ids, query_rows, out_visible);
+  });
+}
+
+int64_t oracle_mask_visible_count(const uint8_t* visible, int64_t n) {  // mask.cpp:87-95
+  int64_t c = 0;
+  for (int64_t i = 0; i < n; ++i) c += visible[i] ? 1 : 0;
+  return c;
+}
+
+int oracle_geometric_schedule(int prefix_len, int depth, int target, int* out_keep) {
+  return guarded([&] {
+    std::vector<int> k = geometric_schedule(prefix_len, depth, target);
+    std::copy(k.begin(), k.end(), out_keep);
+  });
+}
+
+int oracle_full_schedule(int prefix_len, int depth, int* out_keep) {  // mask.cpp:119-123
+  for (int i = 0; i < depth; ++i) out_keep[i] = std::max(prefix_len, 1);
+  return 0;
+}
+
+int oracle_retained_rows(const int* roles, int n, int keep, int keep_specials, int* out_rows,
+                         int* out_n) {
+  std::vector<int> r(roles, roles + n);
+  std::vector<int> o = retained_rows(r, keep, keep_specials != 0);
+  std::copy(o.begin(), o.end(), out_rows);
+  *out_n = static_cast<int>(o.size());
+  return 0;
+}
+
+int oracle_prune_queries(const double* x, int rows, int cols, int n, double* out) {
+  return guarded([&] {  // mask.cpp:125-130
+    if (n < 1 || n > rows) throw ConfigError("prune_queries: n must be in [1, rows]");
+    std::memcpy(out, x + static_cast<size_t>(rows - n) * cols, sizeof(double) * n * cols);
+  });
+}
+
+int oracle_rmsnorm_forward(const double* x, int rows, int cols, const double* gain, double* y,
+                           double* inv_rms) {
+  rmsnorm_rows(x, rows, cols, gain, y, inv_rms);
+  return 0;
+}
+
+// rmsnorm_backward (norm.hpp:32-45), with dgain accumulated into the row it belongs to.
+int oracle_rmsnorm_backward(const double* dy, const double* x, const double* inv_rms, int rows,
+                            int cols, const double* gain, double* dgain, double* dx) {
+  for (int r = 0; r < rows; ++r) {
+    const double inv = inv_rms[r];
+    const double* xr = x + static_cast<size_t>(r) * cols;
+    const double* dyr = dy + static_cast<size_t>(r) * cols;
+    double proj = 0.0;
+    for (int j = 0; j < cols; ++j) {
+      const double xh = xr[j] * inv;
+      dgain[j] += dyr[j] * xh;
+      proj += dyr[j] * gain[j] * xh;
+    }
+    proj /= static_cast<double>(cols);
+    double* o = dx + static_cast<size_t>(r) * cols;
+    for (int j = 0; j < cols; ++j) o[j] = (dyr[j] * gain[j] - proj * xr[j] * inv) * inv;
+  }
+  return 0;
+}
+
+int oracle_rope_apply(const double* x, int rows, int dim, const int* position_ids, double theta,
+                      int inverse, double* out) {
+  return guarded([&] { rope_rows(x, rows, dim, position_ids, theta, inverse != 0, out); });
+}
+
+int oracle_dense_masked_attention_f64(const double* q, const double* k, const double* v,
+                                      const double* mask, int l_q, int l_kv, int dk, int dv,
+                                      double* out) {
+  return guarded([&] { dense_attention<double>(q, k, v, mask, l_q, l_kv, dk, dv, out); });
+}
+int oracle_dense_masked_attention_f32(const float* q, const float* k, const float* v,
+                                      const float* mask, int l_q, int l_kv, int dk, int dv,
+                                      float* out) {
+  return guarded([&] { dense_attention<float>(q, k, v, mask, l_q, l_kv, dk, dv, out); });
+}
+int oracle_blockwise_masked_attention_f64(const double* q, const double* k, const double* v,
+                                          const double* mask, int l_q, int l_kv, int dk, int dv,
+                                          int block, double* out, int64_t* skipped,
+                                          int64_t* total) {
+  return guarded([&] {
+    blockwise_attention<double>(q, k, v, mask, l_q, l_kv, dk, dv, block, out, skipped, total);
+  });
+}
+int oracle_blockwise_masked_attention_f32(const float* q, const float* k, const float* v,
+                                          const float* mask, int l_q, int l_kv, int dk, int dv,
+                                          int block, float* out, int64_t* skipped,
+                                          int64_t* total) {
+  return guarded([&] {
+    blockwise_attention<float>(q, k, v, mask, l_q, l_kv, dk, dv, block, out, skipped, total);
+  });
+}
+
+int oracle_swishglu(const double* x, int rows, int d, int m, const double* w_gate,
+                    const double* w_up, const double* w_down, double* out) {
+  M X(rows, d), G(d, m), U(d, m), D(m, d);
+  std::memcpy(X.a.data(), x, sizeof(double) * rows * d);
+  std::memcpy(G.a.data(), w_gate, sizeof(double) * d * m);
+  std::memcpy(U.a.data(), w_up, sizeof(double) * d * m);
+  std::memcpy(D.a.data(), w_down, sizeof(double) * m * d);
+  M y = swishglu(X, G, U, D);
+  std::memcpy(out, y.a.data(), sizeof(double) * rows * d);
+  return 0;
+}
+
+int oracle_model_create(const OrModelCfg* cfg, OrModel** out) {
+  return guarded([&] {
+    auto* m = new OrModel;
+    m->cfg = *cfg;
+    m->d = cfg->model_dim;
+    if (cfg->heads < 1 || m->d % cfg->heads != 0)
+      throw ConfigError("attention: model_dim must be a positive multiple of heads");
+    m->dk = m->d / cfg->heads;
+    if (m->dk % 2 != 0) throw ConfigError("attention: head dim must be even for the rotary transform");
+    m->m = cfg->ffn_dim;
+    m->dh = cfg->head_hidden > 0 ? cfg->head_hidden : m->d;
+    std::vector<int> keep(cfg->keep, cfg->keep + cfg->layers);
+    for (size_t i = 0; i + 1 < keep.size(); ++i)  // PruneSchedule::validate (mask.hpp:51-60)
+      if (keep[i + 1] > keep[i]) throw ConfigError("PruneSchedule: keep counts must be non-increasing");
+    for (int k : keep)
+      if (k < 1) throw ConfigError("PruneSchedule: keep counts must be >= 1");
+    *out = m;
+  });
+}
+
+void oracle_model_destroy(OrModel* m) { delete m; }
+
+int oracle_model_set_param(OrModel* m, const char* name, const double* data, int rows, int cols) {
+  return guarded([&] {
+    M t(rows, cols);
+    std::memcpy(t.a.data(), data, sizeof(double) * rows * cols);
+    m->p[name] = std::move(t);
+  });
+}
+
+int oracle_tokenize(const OrModel* m, const OrSample* s, double* tokens, int* position_ids,
+                    int* roles, int* candidate_index, int* hist_time, int* out_len) {
+  return guarded([&] {
+    Seq q = tokenize(*m, *s);
+    const int L = q.tokens.r;
+    *out_len = L;
+    if (tokens) std::memcpy(tokens, q.tokens.a.data(), sizeof(double) * L * m->d);
+    if (position_ids) std::copy(q.pos.begin(), q.pos.end(), position_ids);
+    if (roles) std::copy(q.roles.begin(), q.roles.end(), roles);
+    if (candidate_index) std::copy(q.cand_index.begin(), q.cand_index.end(), candidate_index);
+    if (hist_time) std::copy(q.hist_time.begin(), q.hist_time.end(), hist_time);
+  });
+}
+
+int oracle_attention_forward(const OrModel* m, int layer, const double* xn, int l_in,
+                             const int* query_rows, int l_q, const uint8_t* visible,
+                             const int* position_ids, double* out) {
+  return guarded([&] {
+    M X(l_in, m->d);
+    std::memcpy(X.a.data(), xn, sizeof(double) * l_in * m->d);
+    std::vector<int> qr(query_rows, query_rows + l_q), pos(position_ids, position_ids + l_in);
+    M y = attention_forward(*m, layer, X, qr, visible, pos);
+    std::memcpy(out, y.a.data(), sizeof(double) * l_q * m->d);
+  });
+}
+
+int oracle_model_forward(const OrModel* m, const OrSample* s, double* probs, double* logits) {
+  return guarded([&] { model_forward(*m, *s, probs, logits, nullptr); });
+}
+
+int oracle_model_layer_meta(const OrModel* m, const OrSample* s, int* l_q, int64_t* visible,
+                            int* query_rows_concat, int* total_rows) {
+  return guarded([&] {
+    std::vector<LayerTrace> tr;
+    std::vector<double> probs(static_cast<size_t>(s->n_cand) * 3);
+    model_forward(*m, *s, probs.data(), nullptr, &tr);
+    int off = 0;
+    for (size_t l = 0; l < tr.size(); ++l) {
+      l_q[l] = static_cast<int>(tr[l].qrows.size());
+      visible[l] = tr[l].visible;
+      if (query_rows_concat) std::copy(tr[l].qrows.begin(), tr[l].qrows.end(), query_rows_concat + off);
+      off += l_q[l];
+    }
+    *total_rows = off;
+  });
+}
+
+int oracle_model_forward_batch(const OrModel* m, const OrSample* samples, int B, int threads,
+                               double* probs) {
+  std::vector<size_t> off(B + 1, 0);
+  for (int b = 0; b < B; ++b) off[b + 1] = off[b] + static_cast<size_t>(samples[b].n_cand) * 3;
+  std::atomic<int> next{0};
+  std::atomic<int> status{0};
+  std::string first_err;
+  std::mutex mu;
+  auto worker = [&] {
+    for (;;) {
+      const int b = next.fetch_add(1);
+      if (b >= B) break;
+      try {
+        model_forward(*m, samples[b], probs + off[b], nullptr, nullptr);
+      } catch (const ConfigError& e) {
+        std::lock_guard<std::mutex> lk(mu);
+        int z = 0;
+        if (status.compare_exchange_strong(z, 1)) first_err = e.what();
+      } catch (const std::exception& e) {
+        std::lock_guard<std::mutex> lk(mu);
+        int z = 0;
+        if (status.compare_exchange_strong(z, 2)) first_err = e.what();
+      }
+    }
+  };
+  threads = std::max(1, threads);
+  std::vector<std::thread> pool;
+  for (int t = 1; t < threads; ++t) pool.emplace_back(worker);
+  worker();
+  for (auto& t : pool) t.join();
+  if (status.load() != 0) g_err = first_err;
+  return status.load();
+}
+
+}  // extern "C"

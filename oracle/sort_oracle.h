@@ -1,0 +1,141 @@
+/* SPDX-License-Identifier: Apache-2.0
+ *
+ * TEST INFRASTRUCTURE ONLY -- the CPU oracle for the SORT hot path.
+ *
+ * A plain fp64 CPU restatement of the reference's algorithm
+ * (/root/reference/proj, C++20 + Eigen, fp64). It exists so that tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference leg
+ * can CHECK the CUDA path and time the reference algorithm on host cores.
+ * Nothing in the product (paper_2603_03988_b200/) links, loads or calls it.
+ *
+ * Parity status: the reference cannot be built here (Eigen3 absent, its
+ * src/tools/tests CMake dirs missing, attention.cpp:152,180-183,194 do not
+ * compile), so this restatement is pinned against every known-answer example
+ * in SPEC.md plus the derived counts in SURVEY.md section 8 -- the reference ships
+ * no tests or golden vectors. Bit-level claims are made for the integer
+ * artifacts (time buckets, positions, roles, masks, schedules, retained rows).
+ *
+ * All functions return 0 on success, 1 for a ConfigError (common.hpp:17-21)
+ * and 2 for a RuntimeFailure (common.hpp:23-27); oracle_last_error() gives
+ * the message (thread-local).
+ */
+#ifndef SORT_ORACLE_H_
+#define SORT_ORACLE_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Role ids follow rankformer::Role (tokenizer.hpp:13). */
+enum { OR_ROLE_BOS = 0, OR_ROLE_HIST = 1, OR_ROLE_SEP = 2, OR_ROLE_PROF = 3, OR_ROLE_CAND = 4 };
+
+typedef struct {
+  /* TokenizerConfig (tokenizer.hpp:31-56) without side-feature groups. */
+  int model_dim, item_dim, action_dim, scene_dim, time_dim, profile_dim;
+  int n_items, n_actions, n_scenes, n_time_buckets;
+  int n_profile_fields;
+  int profile_vocab[16];
+  int special_tokens;
+  /* Block stack + AttentionSettings (attention.hpp:13-29). */
+  int layers, heads, ffn_dim;
+  int qknorm, gate;
+  double rope_theta;
+  /* MaskSpec (mask.hpp:15-31) + PruneSchedule (mask.hpp:48-61). */
+  int local_window, full_suffix;
+  int keep[64];
+  int keep_specials;
+  int head_hidden; /* ranking head d -> d_h; 0 means d */
+} OrModelCfg;
+
+/* One request (RequestSample, data.hpp:32-38) with no side features. */
+typedef struct {
+  int64_t timestamp;
+  int n_hist;
+  const int32_t* hist_item;
+  const int32_t* hist_action;
+  const int32_t* hist_scene;
+  const int64_t* hist_ts;
+  int n_prof;
+  const int32_t* profile;
+  int n_cand;
+  const int32_t* cand_item;
+} OrSample;
+
+const char* oracle_last_error(void);
+
+/* --- integer rules ---------------------------------------------------- */
+int oracle_time_bucket(int64_t delta_seconds, int n_buckets);
+int oracle_build_mask(int l_q, int l_kv, int local_window, int full_suffix, const int* roles,
+                      const int* position_ids, const int* query_rows /* NULL = suffix */,
+                      uint8_t* out_visible /* l_q*l_kv */);
+int64_t oracle_mask_visible_count(const uint8_t* visible, int64_t n);
+int oracle_geometric_schedule(int prefix_len, int depth, int target, int* out_keep);
+int oracle_full_schedule(int prefix_len, int depth, int* out_keep);
+int oracle_retained_rows(const int* roles, int n, int keep, int keep_specials, int* out_rows,
+                         int* out_n);
+int oracle_prune_queries(const double* x, int rows, int cols, int n, double* out);
+
+/* --- numeric ops (fp64) ------------------------------------------------ */
+int oracle_rmsnorm_forward(const double* x, int rows, int cols, const double* gain, double* y,
+                           double* inv_rms /* may be NULL */);
+int oracle_rmsnorm_backward(const double* dy, const double* x, const double* inv_rms, int rows,
+                            int cols, const double* gain, double* dgain_accum, double* dx);
+int oracle_rope_apply(const double* x, int rows, int dim, const int* position_ids, double theta,
+                      int inverse, double* out);
+int oracle_dense_masked_attention_f64(const double* q, const double* k, const double* v,
+                                      const double* mask, int l_q, int l_kv, int dk, int dv,
+                                      double* out);
+int oracle_dense_masked_attention_f32(const float* q, const float* k, const float* v,
+                                      const float* mask, int l_q, int l_kv, int dk, int dv,
+                                      float* out);
+int oracle_blockwise_masked_attention_f64(const double* q, const double* k, const double* v,
+                                          const double* mask, int l_q, int l_kv, int dk, int dv,
+                                          int block, double* out, int64_t* skipped,
+                                          int64_t* total);
+int oracle_blockwise_masked_attention_f32(const float* q, const float* k, const float* v,
+                                          const float* mask, int l_q, int l_kv, int dk, int dv,
+                                          int block, float* out, int64_t* skipped,
+                                          int64_t* total);
+int oracle_swishglu(const double* x, int rows, int d, int m, const double* w_gate,
+                    const double* w_up, const double* w_down, double* out);
+
+/* --- model ------------------------------------------------------------- */
+typedef struct OrModel OrModel;
+int oracle_model_create(const OrModelCfg* cfg, OrModel** out);
+void oracle_model_destroy(OrModel* m);
+/* Parameter names follow the reference (tokenizer.cpp:45-63, attention.cpp:37-46)
+ * plus spec-named block.<l>.attn_norm / block.<l>.ffn_norm / ffn.<l>.w_gate|w_up|w_down /
+ * final_norm.gain / head.w1|b1|w2|b2. Row-major [rows, cols]. */
+int oracle_model_set_param(OrModel* m, const char* name, const double* data, int rows, int cols);
+
+/* Tokenize one request (Tokenizer::tokenize_sample, tokenizer.cpp:144-238). */
+int oracle_tokenize(const OrModel* m, const OrSample* s, double* tokens /* L*d */,
+                    int* position_ids, int* roles, int* candidate_index,
+                    int* hist_time /* n_hist */, int* out_len);
+
+/* Attention layer l (AttentionLayer::forward, attention.cpp:71-132). */
+int oracle_attention_forward(const OrModel* m, int layer, const double* xn, int l_in,
+                             const int* query_rows, int l_q, const uint8_t* visible,
+                             const int* position_ids, double* out /* l_q*d */);
+
+/* Full forward of one request: probabilities [n_cand*3] (click, cart, purchase),
+ * optionally the pre-sigmoid logits [n_cand*3]. */
+int oracle_model_forward(const OrModel* m, const OrSample* s, double* probs, double* logits);
+
+/* Per-layer structural artifacts of one request: for each layer l,
+ * l_q[l], visible count[l], and query_rows concatenated. */
+int oracle_model_layer_meta(const OrModel* m, const OrSample* s, int* l_q, int64_t* visible,
+                            int* query_rows_concat, int* total_rows);
+
+/* Batched forward over B requests on `threads` host threads (one request per
+ * thread at a time, the reference's concurrency model: params.hpp:12-14). */
+int oracle_model_forward_batch(const OrModel* m, const OrSample* samples, int B, int threads,
+                               double* probs /* sum(n_cand)*3 */);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SORT_ORACLE_H_ */
