@@ -1,0 +1,174 @@
+/* SPDX-License-Identifier: Apache-2.0
+ *
+ * sort_b200.h -- C ABI of libsort_b200.so, the B200-native (sm_100a) SORT
+ * ranking-transformer block path (arXiv 2603.03988).
+ *
+ * This is the drop-in boundary for the reference's C++ hot-path API
+ * (/root/reference/proj/include/rankformer/ headers). Plain pointers and sizes
+ * only; no CUDA/torch types. Each entry point names the reference interface
+ * it replaces. A C++ binding with the reference's rankformer:: names lives
+ * in include/rankformer/sort_gpu.hpp; the ctypes binding used by the tests is
+ * paper_2603_03988_b200/runtime.py; INTEGRATION.md shows both.
+ *
+ * Conventions:
+ *   - Every function returns int status: 0 = ok, 1 = config/input error
+ *     (rankformer::ConfigError, common.hpp:17-21; CLI exit 1), 2 = runtime
+ *     failure (rankformer::RuntimeFailure, common.hpp:23-27; CLI exit 2).
+ *     sort_last_error() returns the thread-local message of the last failure.
+ *   - A handle binds one CUDA device and one stream, owns device weights and
+ *     workspace; calls on one handle are serialised by the caller (one handle
+ *     per GPU, each driven by its own host thread -- the reference's
+ *     "pure const forward, many threads" model, params.hpp:12-14).
+ *   - Host buffers are caller-owned. Device-side range checks (OOV ids,
+ *     tokenizer.cpp:14-19) raise a device flag that becomes status 1; an
+ *     out-of-vocabulary id is never read out of bounds.
+ *   - All requests of one batch share n_hist / n_cand (the batched path is
+ *     planned per geometry); ragged batches are issued as several calls.
+ */
+#ifndef SORT_B200_H_
+#define SORT_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SORT_OK 0
+#define SORT_CONFIG_ERROR 1
+#define SORT_RUNTIME_FAILURE 2
+
+#define SORT_MAX_PROFILE_FIELDS 16
+#define SORT_MAX_LAYERS 64
+
+/* Role ids: rankformer::Role (tokenizer.hpp:13). */
+#define SORT_ROLE_BOS 0
+#define SORT_ROLE_HIST 1
+#define SORT_ROLE_SEP 2
+#define SORT_ROLE_PROF 3
+#define SORT_ROLE_CAND 4
+
+typedef struct SortHandle_* SortHandle;
+
+/* Model + batch geometry. Fields mirror TokenizerConfig (tokenizer.hpp:31-56),
+ * AttentionSettings (attention.hpp:13-29), MaskSpec (mask.hpp:15-31),
+ * PruneSchedule (mask.hpp:48-61) and the spec's ModelConfig. */
+typedef struct {
+  int32_t model_dim, heads, layers, ffn_dim, head_hidden; /* head_hidden 0 -> model_dim */
+  int32_t item_dim, action_dim, scene_dim, time_dim, profile_dim;
+  int32_t n_items, n_actions, n_scenes, n_time_buckets;
+  int32_t n_profile_fields;
+  int32_t profile_vocab[SORT_MAX_PROFILE_FIELDS];
+  int32_t special_tokens, qknorm, gate;
+  double rope_theta;
+  int32_t local_window; /* -1 = unbounded */
+  int32_t full_suffix;
+  int32_t keep[SORT_MAX_LAYERS]; /* per-layer non-candidate keep counts */
+  int32_t keep_specials;
+  int32_t max_batch, n_hist, n_cand; /* batch geometry the workspace is planned for */
+} SortConfig;
+
+/* A batch of requests in structure-of-arrays form (RequestSample, data.hpp:32-38,
+ * without side features). Row-major [batch, n] arrays. */
+typedef struct {
+  int32_t batch;
+  const int32_t* hist_item;   /* [batch, n_hist] */
+  const int32_t* hist_action; /* [batch, n_hist] */
+  const int32_t* hist_scene;  /* [batch, n_hist] */
+  const int64_t* hist_ts;     /* [batch, n_hist] */
+  const int64_t* req_ts;      /* [batch] */
+  const int32_t* profile;     /* [batch, n_profile_fields] */
+  const int32_t* cand_item;   /* [batch, n_cand] */
+} SortBatch;
+
+const char* sort_last_error(void);
+int sort_version(void);
+
+/* ---------------------------------------------------------------- lifetime */
+/* Replaces constructing Tokenizer + AttentionLayer x depth (tokenizer.cpp:42-64,
+ * attention.cpp:34-47) and the spec's model assembly. */
+int sort_create(const SortConfig* cfg, int device, SortHandle* out);
+int sort_destroy(SortHandle h);
+/* cudaStream_t passed as void* (NULL = the handle's own stream). */
+int sort_set_stream(SortHandle h, void* stream);
+
+/* Named parameters in the reference's [rows, cols] row-major orientation
+ * (Parameter::value, params.hpp:15-25). Names: tok.* (tokenizer.cpp:45-63),
+ * attn.<l>.{wq,wk,wv,wo,wg,qk_gain_q,qk_gain_k} (attention.cpp:37-46), and the
+ * spec-named block.<l>.{attn_norm,ffn_norm}, ffn.<l>.{w_gate,w_up,w_down},
+ * final_norm.gain, head.{w1,b1,w2,b2}. Values are converted to the device
+ * layout (bf16 K-major tensors, fp32 head) by sort_finalize_params. */
+int sort_load_param(SortHandle h, const char* name, const float* data, int64_t rows, int64_t cols);
+int sort_finalize_params(SortHandle h);
+
+/* ---------------------------------------------------------------- forward */
+/* model_forward over a batch: scores[b, j, 0..2] =
+ * {p_click, p_cart, p_purchase} for candidate j of request b. When
+ * inputs_on_device != 0 the SortBatch pointers are device pointers; when
+ * scores_on_device != 0 `scores` is a device pointer. Synchronous unless
+ * both are device pointers (then it only enqueues on the handle's stream;
+ * call sort_sync to collect the status of device-side checks). */
+int sort_forward(SortHandle h, const SortBatch* batch, int inputs_on_device, float* scores,
+                 int scores_on_device);
+int sort_sync(SortHandle h);
+
+/* Same as sort_forward but also returns the pre-sigmoid logits [batch, n_cand, 3]. */
+int sort_forward_logits(SortHandle h, const SortBatch* batch, float* probs, float* logits);
+
+/* ---------------------------------------------------------------- parity ops */
+/* Tokenizer::tokenize_sample (tokenizer.hpp:84) over a batch, host buffers:
+ * tokens [batch, L, d] (fp32 copy of the bf16 tokens), hist_time [batch, n_hist]
+ * (the time-bucket part of TokenizerCache, tokenizer.hpp:68). position_ids / roles /
+ * candidate_index [L] are the (batch-uniform) sequence structure. Any output may be NULL. */
+int sort_tokenize(SortHandle h, const SortBatch* batch, float* tokens, int32_t* hist_time,
+                  int32_t* position_ids, int32_t* roles, int32_t* candidate_index);
+
+/* Structural plan of layer `layer` (build_mask + retained_rows, mask.hpp:36-76):
+ * l_q/l_kv, the retained query rows (kv-index space), and the compact mask of each
+ * query row: visible = [lo, hi] U {self} (self = -1 for non-candidates), plus the
+ * number of visible entries (mask_visible_count, mask.hpp:44) and the attention
+ * kernel's 128x128 tile census (issued / total). Arrays sized >= l_q; may be NULL. */
+int sort_layer_plan(SortHandle h, int layer, int32_t* l_q, int32_t* l_kv, int32_t* query_rows,
+                    int32_t* lo, int32_t* hi, int32_t* self_idx, int64_t* visible,
+                    int64_t* tiles_issued, int64_t* tiles_total);
+
+/* AttentionLayer::forward (attention.hpp:58-59) of layer `layer` composed with the
+ * pre-norm that feeds it: out = Attn_l(RMSNorm(x; block.<l>.attn_norm)),
+ * for a batch of layer inputs x [batch, l_kv, d] (host fp32), using the layer's plan
+ * for query rows / mask / positions. out: [batch, l_q, d] host fp32. */
+int sort_attention_forward(SortHandle h, int layer, int32_t batch, const float* x, float* out);
+
+/* blockwise_masked_attention (block_attention.hpp:58-62) at the kernel's tile size on
+ * one (q, k, v) problem per head of a batch: q [nh, l_q, dk], k/v [nh, l_kv, dk] (host fp32,
+ * rounded to bf16 on upload), visibility given in compact form (lo/hi/self per query row,
+ * shared by all nh problems). out [nh, l_q, dk]; skipped/total 128x128 tiles per problem. */
+int sort_block_attention(int32_t nh, int32_t l_q, int32_t l_kv, int32_t dk, const float* q,
+                         const float* k, const float* v, const int32_t* lo, const int32_t* hi,
+                         const int32_t* self_idx, float* out, int64_t* skipped, int64_t* total);
+
+/* ---------------------------------------------------------------- host planner */
+/* Host-only integer rules (no GPU needed): time_bucket (tokenizer.cpp:36-40),
+ * make_geometric_schedule (mask.cpp:97-117), retained_rows (mask.cpp:132-154) and the
+ * compact form of build_mask (mask.cpp:14-76). */
+int sort_time_bucket(int64_t delta_seconds, int32_t n_buckets);
+int sort_geometric_schedule(int32_t prefix_len, int32_t depth, int32_t target, int32_t* keep);
+int sort_retained_rows(const int32_t* roles, int32_t n, int32_t keep, int32_t keep_specials,
+                       int32_t* rows, int32_t* n_rows);
+int sort_mask_intervals(int32_t l_q, int32_t l_kv, int32_t local_window, int32_t full_suffix,
+                        const int32_t* roles, const int32_t* position_ids,
+                        const int32_t* query_rows, int32_t* lo, int32_t* hi, int32_t* self_idx);
+
+/* ---------------------------------------------------------------- instrumentation */
+/* Number of CUDA kernels one sort_forward launches, and per-stage device times (ms) of
+ * the last sort_forward when timing was enabled with sort_enable_stage_timing(h, 1).
+ * stage_names is a ';'-separated list written into names (cap bytes). */
+int sort_kernel_count(SortHandle h, int32_t* launches);
+int sort_enable_stage_timing(SortHandle h, int enable);
+int sort_stage_times(SortHandle h, float* ms, int32_t cap, int32_t* n, char* names,
+                     int32_t names_cap);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SORT_B200_H_ */

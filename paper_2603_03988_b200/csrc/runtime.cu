@@ -1,0 +1,937 @@
+// SPDX-License-Identifier: Apache-2.0
+// libsort_b200.so: handle, device weights/workspace, forward orchestration and the
+// C ABI declared in include/sort_b200.h.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/sort_b200.h"
+#include "attention.cuh"
+#include "epilogues.cuh"
+#include "gemm.cuh"
+#include "misc.cuh"
+#include "plan.hpp"
+#include "tma_host.hpp"
+#include "tokenizer.cuh"
+
+namespace sortk {
+
+thread_local std::string g_last_error;
+
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess)                                                                 \
+      throw RuntimeFailure(std::string(#x) + " failed: " + cudaGetErrorString(e_));        \
+  } while (0)
+
+static inline __nv_bfloat16 f2bf(float x) { return __float2bfloat16_rn(x); }
+
+struct HostParam {
+  std::vector<float> v;
+  int64_t rows = 0, cols = 0;
+};
+
+struct LayerDev {
+  int4* rowmeta = nullptr;
+  int32_t *tile_off = nullptr, *tile_code = nullptr, *qtile_order = nullptr;
+  int32_t *pos_q = nullptr, *pos_kv = nullptr, *query_rows = nullptr;
+  __nv_bfloat16 *w_qgkv = nullptr, *w_o = nullptr, *w_up = nullptr, *w_down = nullptr;
+  float *gain_q = nullptr, *gain_k = nullptr;
+  int in_buf = 0, q_buf = 0;
+  int Rq = 0, Rkv = 0, Rkv_pad = 0;
+  int bn_full = 0, bn_half = 0, bn_up = 0;
+  CUtensorMap tmA_in, tmA_q, tmB_qgkv, tmB_qg, tmB_kv, tmA_hg, tmB_o, tmB_up, tmA_hid, tmB_down;
+  CUtensorMap tmQ, tmK, tmV;
+};
+
+struct Handle {
+  SortConfig cfg{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  Plan plan;
+  int d = 0, H = 0, dk = 0, m = 0, dh = 0, L0 = 0, Bmax = 0, num_sms = 148;
+  std::map<std::string, HostParam> host;
+  bool finalized = false;
+  // device weights
+  __nv_bfloat16 *item = nullptr, *action = nullptr, *scene = nullptr, *time = nullptr,
+                *prof = nullptr, *special = nullptr;
+  __nv_bfloat16* tok_wt[3] = {nullptr, nullptr, nullptr};
+  float* tok_b[3] = {nullptr, nullptr, nullptr};
+  float* tok_g[3] = {nullptr, nullptr, nullptr};
+  int prof_off[SORT_MAX_PROFILE_FIELDS] = {0};
+  float2* rope = nullptr;
+  float *head_gain = nullptr, *head_w1 = nullptr, *head_b1 = nullptr, *head_w2 = nullptr,
+        *head_b2 = nullptr;
+  std::vector<LayerDev> layers;
+  // workspace
+  __nv_bfloat16* X[2] = {nullptr, nullptr};
+  float* SS[2] = {nullptr, nullptr};
+  __nv_bfloat16 *Qb = nullptr, *Kb = nullptr, *Vt = nullptr, *Gb = nullptr, *Hg = nullptr,
+                *hid = nullptr;
+  float *probs = nullptr, *logits = nullptr;
+  int32_t* err = nullptr;
+  int32_t* hist_time = nullptr;
+  int32_t *in_item = nullptr, *in_action = nullptr, *in_scene = nullptr, *in_prof = nullptr,
+          *in_cand = nullptr;
+  int64_t *in_ts = nullptr, *in_req = nullptr;
+  std::vector<void*> allocs;
+  // instrumentation
+  bool timing = false;
+  std::vector<cudaEvent_t> events;
+  std::vector<std::string> stage_names;
+  std::vector<float> stage_ms;
+  int launches = 0;
+
+  template <class T>
+  T* dalloc(size_t n) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    CK(cudaMalloc(&p, n * sizeof(T)));
+    allocs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  template <class T>
+  T* upload(const std::vector<T>& h) {
+    T* p = dalloc<T>(h.size());
+    CK(cudaMemcpy(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return p;
+  }
+  ~Handle() {
+    if (device >= 0) cudaSetDevice(device);
+    for (void* p : allocs) cudaFree(p);
+    for (auto e : events) cudaEventDestroy(e);
+    if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+};
+
+// ------------------------------------------------------------------ params
+static const HostParam& need_param(Handle& h, const std::string& name, int64_t rows, int64_t cols) {
+  auto it = h.host.find(name);
+  if (it == h.host.end()) throw ConfigError("missing parameter " + name);
+  if (it->second.rows != rows || it->second.cols != cols)
+    throw ConfigError("parameter " + name + " has shape [" + std::to_string(it->second.rows) + ", " +
+                      std::to_string(it->second.cols) + "], expected [" + std::to_string(rows) +
+                      ", " + std::to_string(cols) + "]");
+  return it->second;
+}
+
+static std::vector<__nv_bfloat16> to_bf16(const std::vector<float>& v) {
+  std::vector<__nv_bfloat16> o(v.size());
+  for (size_t i = 0; i < v.size(); ++i) o[i] = f2bf(v[i]);
+  return o;
+}
+
+// W [K, N] (reference [in, out]) -> W^T [N, Kpad] bf16, optionally scaling input row k by g[k].
+static std::vector<__nv_bfloat16> transpose_bf16(const HostParam& w, int Kpad, const float* g) {
+  const int K = static_cast<int>(w.rows), N = static_cast<int>(w.cols);
+  std::vector<__nv_bfloat16> o(static_cast<size_t>(N) * Kpad, f2bf(0.f));
+  for (int k = 0; k < K; ++k)
+    for (int n = 0; n < N; ++n) o[static_cast<size_t>(n) * Kpad + k] = f2bf(w.v[static_cast<size_t>(k) * N + n] * (g ? g[k] : 1.f));
+  return o;
+}
+
+static void finalize(Handle& h) {
+  const SortConfig& c = h.cfg;
+  const int d = h.d, m = h.m, H = h.H, dk = h.dk;
+  // ---- tokenizer tables and projections (tokenizer.cpp:45-63)
+  h.item = h.upload(to_bf16(need_param(h, "tok.item_table", c.n_items, c.item_dim).v));
+  h.action = h.upload(to_bf16(need_param(h, "tok.action_table", c.n_actions, c.action_dim).v));
+  h.scene = h.upload(to_bf16(need_param(h, "tok.scene_table", c.n_scenes, c.scene_dim).v));
+  h.time = h.upload(to_bf16(need_param(h, "tok.time_table", c.n_time_buckets, c.time_dim).v));
+  {
+    std::vector<float> all;
+    int off = 0;
+    for (int f = 0; f < c.n_profile_fields; ++f) {
+      const HostParam& t = need_param(h, "tok.profile_table." + std::to_string(f), c.profile_vocab[f], c.profile_dim);
+      h.prof_off[f] = off;
+      off += c.profile_vocab[f];
+      all.insert(all.end(), t.v.begin(), t.v.end());
+    }
+    if (all.empty()) all.assign(8, 0.f);
+    h.prof = h.upload(to_bf16(all));
+  }
+  h.special = h.upload(to_bf16(need_param(h, "tok.special", 3, d).v));
+  const int hw = c.item_dim + c.action_dim + c.scene_dim + c.time_dim;
+  const char* gw[3] = {"tok.w_hist", "tok.w_cand", "tok.w_prof"};
+  const char* gb[3] = {"tok.b_hist", "tok.b_cand", "tok.b_prof"};
+  const char* gg[3] = {"tok.g_hist", "tok.g_cand", "tok.g_prof"};
+  const int gk[3] = {hw, c.item_dim, c.profile_dim};
+  for (int g = 0; g < 3; ++g) {
+    h.tok_wt[g] = h.upload(transpose_bf16(need_param(h, gw[g], gk[g], d), 64, nullptr));
+    h.tok_b[g] = h.upload(need_param(h, gb[g], 1, d).v);
+    h.tok_g[g] = h.upload(need_param(h, gg[g], 1, d).v);
+  }
+  // ---- RoPE table in fp64 (rope.hpp:23-38), stored fp32 (cos, sin)
+  {
+    std::vector<float2> tab(static_cast<size_t>(h.plan.max_pos + 1) * (dk / 2));
+    for (int p = 0; p <= h.plan.max_pos; ++p)
+      for (int j = 0; j < dk / 2; ++j) {
+        const double freq = std::pow(c.rope_theta, -2.0 * j / static_cast<double>(dk));
+        const double ang = static_cast<double>(p) * freq;
+        tab[static_cast<size_t>(p) * (dk / 2) + j] = make_float2(static_cast<float>(std::cos(ang)), static_cast<float>(std::sin(ang)));
+      }
+    h.rope = h.upload(tab);
+  }
+  // ---- workspace
+  const size_t rows_max = static_cast<size_t>(h.Bmax) * h.L0;
+  for (int i = 0; i < 2; ++i) {
+    h.X[i] = h.dalloc<__nv_bfloat16>(rows_max * d);
+    h.SS[i] = h.dalloc<float>(rows_max);
+  }
+  h.Qb = h.dalloc<__nv_bfloat16>(rows_max * d);
+  h.Kb = h.dalloc<__nv_bfloat16>(rows_max * d);
+  const int Rkv_pad_max = (h.L0 + 7) / 8 * 8;
+  const size_t vt_elems = static_cast<size_t>(h.Bmax) * H * dk * Rkv_pad_max;
+  h.Vt = h.dalloc<__nv_bfloat16>(vt_elems);
+  CK(cudaMemset(h.Vt, 0, vt_elems * sizeof(__nv_bfloat16)));
+  h.Gb = h.dalloc<__nv_bfloat16>(rows_max * d);
+  h.Hg = h.dalloc<__nv_bfloat16>(rows_max * d);
+  h.hid = h.dalloc<__nv_bfloat16>(rows_max * m);
+  h.probs = h.dalloc<float>(static_cast<size_t>(h.Bmax) * c.n_cand * 3);
+  h.logits = h.dalloc<float>(static_cast<size_t>(h.Bmax) * c.n_cand * 3);
+  h.err = h.dalloc<int32_t>(4);
+  h.hist_time = h.dalloc<int32_t>(static_cast<size_t>(h.Bmax) * std::max(c.n_hist, 1));
+  const size_t BH_ = static_cast<size_t>(h.Bmax) * std::max(c.n_hist, 1);
+  h.in_item = h.dalloc<int32_t>(BH_);
+  h.in_action = h.dalloc<int32_t>(BH_);
+  h.in_scene = h.dalloc<int32_t>(BH_);
+  h.in_ts = h.dalloc<int64_t>(BH_);
+  h.in_req = h.dalloc<int64_t>(h.Bmax);
+  h.in_prof = h.dalloc<int32_t>(static_cast<size_t>(h.Bmax) * std::max(c.n_profile_fields, 1));
+  h.in_cand = h.dalloc<int32_t>(static_cast<size_t>(h.Bmax) * c.n_cand);
+
+  // ---- per-layer weights, plan arrays and TMA descriptors
+  int cur = 0;
+  h.layers.resize(c.layers);
+  for (int l = 0; l < c.layers; ++l) {
+    const LayerPlan& lp = h.plan.layers[l];
+    LayerDev& L = h.layers[l];
+    const std::string a = "attn." + std::to_string(l) + ".";
+    const std::string bk = "block." + std::to_string(l) + ".";
+    const std::string f = "ffn." + std::to_string(l) + ".";
+    const HostParam& ga = need_param(h, bk + "attn_norm", 1, d);
+    const HostParam& gf = need_param(h, bk + "ffn_norm", 1, d);
+    {  // [Q | G | K | V]^T with the attention pre-norm gain folded into the input rows
+      std::vector<__nv_bfloat16> w(static_cast<size_t>(4) * d * d);
+      const char* order[4] = {"wq", "wg", "wk", "wv"};
+      for (int s = 0; s < 4; ++s) {
+        std::vector<__nv_bfloat16> t = transpose_bf16(need_param(h, a + order[s], d, d), d, ga.v.data());
+        std::copy(t.begin(), t.end(), w.begin() + static_cast<size_t>(s) * d * d);
+      }
+      L.w_qgkv = h.upload(w);
+    }
+    L.w_o = h.upload(transpose_bf16(need_param(h, a + "wo", d, d), d, nullptr));
+    {  // SwishGLU up: interleave 32-column blocks [gate_j | up_j], ffn pre-norm gain folded
+      const HostParam& wg = need_param(h, f + "w_gate", d, m);
+      const HostParam& wu = need_param(h, f + "w_up", d, m);
+      std::vector<__nv_bfloat16> w(static_cast<size_t>(2) * m * d);
+      for (int j = 0; j < m / 32; ++j)
+        for (int i = 0; i < 64; ++i) {
+          const HostParam& src = i < 32 ? wg : wu;
+          const int col = 32 * j + (i & 31);
+          const size_t row = static_cast<size_t>(64 * j + i);
+          for (int k = 0; k < d; ++k) w[row * d + k] = f2bf(src.v[static_cast<size_t>(k) * m + col] * gf.v[k]);
+        }
+      L.w_up = h.upload(w);
+    }
+    L.w_down = h.upload(transpose_bf16(need_param(h, f + "w_down", m, d), m, nullptr));
+    L.gain_q = h.upload(need_param(h, a + "qk_gain_q", H, dk).v);
+    L.gain_k = h.upload(need_param(h, a + "qk_gain_k", H, dk).v);
+    // plan arrays
+    std::vector<int4> meta(static_cast<size_t>(lp.n_qtiles) * 128, make_int4(0, -1, -1, 0));
+    for (int r = 0; r < lp.l_q; ++r) meta[r] = make_int4(lp.lo[r], lp.hi[r], lp.self_idx[r], 0);
+    L.rowmeta = h.upload(meta);
+    L.tile_off = h.upload(lp.tile_off);
+    L.tile_code = h.upload(lp.tile_code.empty() ? std::vector<int32_t>{0} : lp.tile_code);
+    L.qtile_order = h.upload(lp.qtile_order);
+    L.pos_q = h.upload(lp.pos_q);
+    L.pos_kv = h.upload(lp.pos_kv);
+    L.query_rows = h.upload(lp.query_rows);
+    L.Rq = lp.l_q;
+    L.Rkv = lp.l_kv;
+    L.Rkv_pad = (lp.l_kv + 7) / 8 * 8;
+    L.in_buf = cur;
+    L.q_buf = lp.q_identity ? cur : 1 - cur;
+    cur = L.q_buf;
+    // GEMM tile widths
+    L.bn_full = std::min(256, 4 * d);
+    L.bn_half = std::min(256, 2 * d);
+    L.bn_up = 0;
+    for (int bn = 256; bn >= 64; bn -= 64)
+      if ((2 * m) % bn == 0) {
+        L.bn_up = bn;
+        break;
+      }
+    if (!L.bn_up) throw ConfigError("unsupported ffn_dim: 2*ffn_dim must be divisible by 64");
+    // TMA descriptors (sized for max_batch; launches use the call's batch)
+    const uint64_t Mkv = static_cast<uint64_t>(h.Bmax) * L.Rkv, Mq = static_cast<uint64_t>(h.Bmax) * L.Rq;
+    L.tmA_in = make_tmap_2d(h.X[L.in_buf], Mkv, d, d, 128, 64, 128);
+    L.tmA_q = make_tmap_2d(h.X[L.q_buf], Mq, d, d, 128, 64, 128);
+    L.tmB_qgkv = make_tmap_2d(L.w_qgkv, 4 * d, d, d, L.bn_full, 64, 128);
+    L.tmB_qg = make_tmap_2d(L.w_qgkv, 2 * d, d, d, L.bn_half, 64, 128);
+    L.tmB_kv = make_tmap_2d(L.w_qgkv + static_cast<size_t>(2) * d * d, 2 * d, d, d, L.bn_half, 64, 128);
+    L.tmA_hg = make_tmap_2d(h.Hg, Mq, d, d, 128, 64, 128);
+    L.tmB_o = make_tmap_2d(L.w_o, d, d, d, d, 64, 128);
+    L.tmB_up = make_tmap_2d(L.w_up, 2 * m, d, d, L.bn_up, 64, 128);
+    L.tmA_hid = make_tmap_2d(h.hid, Mq, m, m, 128, 64, 128);
+    L.tmB_down = make_tmap_2d(L.w_down, d, m, m, d, 64, 128);
+    {
+      const uint64_t BH = static_cast<uint64_t>(h.Bmax) * H;
+      uint64_t dq[3] = {static_cast<uint64_t>(dk), static_cast<uint64_t>(L.Rq), BH};
+      uint64_t sq[2] = {static_cast<uint64_t>(dk) * 2, static_cast<uint64_t>(L.Rq) * dk * 2};
+      uint32_t bq[3] = {static_cast<uint32_t>(dk), 128, 1};
+      L.tmQ = make_tmap_bf16(h.Qb, 3, dq, sq, bq, dk * 2);
+      uint64_t dkd[3] = {static_cast<uint64_t>(dk), static_cast<uint64_t>(L.Rkv), BH};
+      uint64_t skd[2] = {static_cast<uint64_t>(dk) * 2, static_cast<uint64_t>(L.Rkv) * dk * 2};
+      L.tmK = make_tmap_bf16(h.Kb, 3, dkd, skd, bq, dk * 2);
+      uint64_t dv[3] = {static_cast<uint64_t>(L.Rkv_pad), static_cast<uint64_t>(dk), BH};
+      uint64_t sv[2] = {static_cast<uint64_t>(L.Rkv_pad) * 2, static_cast<uint64_t>(L.Rkv_pad) * dk * 2};
+      uint32_t bv[3] = {64, static_cast<uint32_t>(dk), 1};
+      L.tmV = make_tmap_bf16(h.Vt, 3, dv, sv, bv, 128);
+    }
+  }
+  // ---- head (fp32)
+  h.head_gain = h.upload(need_param(h, "final_norm.gain", 1, d).v);
+  h.head_w1 = h.upload(need_param(h, "head.w1", d, h.dh).v);
+  h.head_b1 = h.upload(need_param(h, "head.b1", 1, h.dh).v);
+  h.head_w2 = h.upload(need_param(h, "head.w2", h.dh, 3).v);
+  h.head_b2 = h.upload(need_param(h, "head.b2", 1, 3).v);
+  h.host.clear();  // device copies are authoritative from here on
+  h.finalized = true;
+}
+
+// ------------------------------------------------------------------ launches
+static void check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw RuntimeFailure(std::string(what) + " launch failed: " + cudaGetErrorString(e));
+}
+
+template <class Epi>
+static void launch_gemm(Handle& h, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K,
+                        int BN, const Epi& epi) {
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_gemm_bf16<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(kGemmSmemBytes)));
+    attr = true;
+  }
+  if (N % BN) throw RuntimeFailure("gemm: N not divisible by BN");
+  const int tiles = ((M + kGemmBM - 1) / kGemmBM) * (N / BN);
+  const int grid = std::min(tiles, h.num_sms);
+  k_gemm_bf16<Epi><<<grid, kGemmThreads, kGemmSmemBytes, h.stream>>>(A, B, M, N, K, BN, epi);
+  check_launch("gemm");
+  ++h.launches;
+}
+
+template <int DK>
+static void launch_attention_dk(Handle& h, const LayerDev& L, const LayerPlan& lp, int B) {
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_attention<DK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(AttnSmem<DK>::kTotal)));
+    attr = true;
+  }
+  AttnArgs a;
+  a.rowmeta = L.rowmeta;
+  a.tile_off = L.tile_off;
+  a.tile_code = L.tile_code;
+  a.qtile_order = L.qtile_order;
+  a.g = h.Gb;
+  a.out = h.Hg;
+  a.BH = B * h.H;
+  a.H = h.H;
+  a.Rq = L.Rq;
+  a.d = h.d;
+  a.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(DK)));
+  const int grid = lp.n_qtiles * B * h.H;
+  k_attention<DK><<<grid, kAttnThreads, AttnSmem<DK>::kTotal, h.stream>>>(L.tmQ, L.tmK, L.tmV, a);
+  check_launch("attention");
+  ++h.launches;
+}
+
+static void launch_attention(Handle& h, const LayerDev& L, const LayerPlan& lp, int B) {
+  switch (h.dk) {
+    case 16: launch_attention_dk<16>(h, L, lp, B); break;
+    case 32: launch_attention_dk<32>(h, L, lp, B); break;
+    case 64: launch_attention_dk<64>(h, L, lp, B); break;
+    default: throw ConfigError("unsupported head dim");
+  }
+}
+
+template <int DK>
+static void launch_qkvg_dk(Handle& h, const LayerDev& L, const CUtensorMap& A, const CUtensorMap& Bm,
+                           int M, int N, int BN, int R, const int* sec, const float* ss,
+                           const int32_t* pos) {
+  EpiQKVG<DK> e;
+  e.d = h.d;
+  e.H = h.H;
+  e.R = R;
+  for (int i = 0; i < 4; ++i) e.sec[i] = sec[i];
+  e.inv_d = 1.f / static_cast<float>(h.d);
+  e.ss = ss;
+  e.gain_q = L.gain_q;
+  e.gain_k = L.gain_k;
+  e.rope = h.rope;
+  e.pos = pos;
+  e.q = h.Qb;
+  e.k = h.Kb;
+  e.vt = h.Vt;
+  e.g = h.Gb;
+  e.Rq = L.Rq;
+  e.Rkv = L.Rkv;
+  e.Rkv_pad = L.Rkv_pad;
+  launch_gemm(h, A, Bm, M, N, h.d, BN, e);
+}
+
+static void launch_qkvg(Handle& h, const LayerDev& L, const CUtensorMap& A, const CUtensorMap& Bm,
+                        int M, int N, int BN, int R, const int* sec, const float* ss, const int32_t* pos) {
+  switch (h.dk) {
+    case 16: launch_qkvg_dk<16>(h, L, A, Bm, M, N, BN, R, sec, ss, pos); break;
+    case 32: launch_qkvg_dk<32>(h, L, A, Bm, M, N, BN, R, sec, ss, pos); break;
+    case 64: launch_qkvg_dk<64>(h, L, A, Bm, M, N, BN, R, sec, ss, pos); break;
+    default: throw ConfigError("unsupported head dim");
+  }
+}
+
+static void stage_mark(Handle& h, const std::string& name) {
+  if (!h.timing) return;
+  cudaEvent_t e;
+  CK(cudaEventCreate(&e));
+  CK(cudaEventRecord(e, h.stream));
+  h.events.push_back(e);
+  h.stage_names.push_back(name);
+}
+
+static void run_tokenizer(Handle& h, int B) {
+  const SortConfig& c = h.cfg;
+  TokParams p{};
+  p.item_tab = h.item;
+  p.action_tab = h.action;
+  p.scene_tab = h.scene;
+  p.time_tab = h.time;
+  p.prof_tab = h.prof;
+  p.special = h.special;
+  for (int f = 0; f < c.n_profile_fields; ++f) {
+    p.prof_row_off[f] = h.prof_off[f];
+    p.prof_vocab[f] = c.profile_vocab[f];
+  }
+  for (int g = 0; g < 3; ++g) {
+    p.wt[g] = h.tok_wt[g];
+    p.bias[g] = h.tok_b[g];
+    p.gain[g] = h.tok_g[g];
+  }
+  p.hist_item = h.in_item;
+  p.hist_action = h.in_action;
+  p.hist_scene = h.in_scene;
+  p.hist_ts = h.in_ts;
+  p.req_ts = h.in_req;
+  p.profile = h.in_prof;
+  p.cand_item = h.in_cand;
+  p.x = h.X[0];
+  p.ss = h.SS[0];
+  p.hist_time = h.hist_time;
+  p.err = h.err;
+  p.B = B;
+  p.H = c.n_hist;
+  p.P = c.n_profile_fields;
+  p.N = c.n_cand;
+  p.L = h.L0;
+  p.d = h.d;
+  p.item_dim = c.item_dim;
+  p.action_dim = c.action_dim;
+  p.scene_dim = c.scene_dim;
+  p.time_dim = c.time_dim;
+  p.prof_dim = c.profile_dim;
+  p.n_items = c.n_items;
+  p.n_actions = c.n_actions;
+  p.n_scenes = c.n_scenes;
+  p.n_tb = c.n_time_buckets;
+  p.special_tokens = c.special_tokens;
+  p.tiles_hist = (B * c.n_hist + 127) / 128;
+  p.tiles_cand = (B * c.n_cand + 127) / 128;
+  p.tiles_prof = (B * c.n_profile_fields + 127) / 128;
+  static size_t attr_bytes = 0;
+  const size_t smem = tok_smem_bytes(h.d);
+  if (smem > attr_bytes) {
+    CK(cudaFuncSetAttribute(k_tokenize, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    attr_bytes = smem;
+  }
+  const int tiles = p.tiles_hist + p.tiles_cand + p.tiles_prof;
+  const int grid = std::max(1, std::min(tiles, 2 * h.num_sms));
+  k_tokenize<<<grid, kTokThreads, smem, h.stream>>>(p);
+  check_launch("tokenizer");
+  ++h.launches;
+}
+
+// One SORT block. out_attn_only: write Attn(...) instead of the residual
+// stream (op-level parity entry point).
+static void run_layer(Handle& h, int l, int B, bool attn_only = false) {
+  const LayerDev& L = h.layers[l];
+  const LayerPlan& lp = h.plan.layers[l];
+  const int d = h.d;
+  __nv_bfloat16* Xin = h.X[L.in_buf];
+  float* SSin = h.SS[L.in_buf];
+  __nv_bfloat16* Xq = h.X[L.q_buf];
+  float* SSq = h.SS[L.q_buf];
+  if (lp.q_identity) {
+    const int sec[4] = {kSecQ, kSecG, kSecK, kSecV};
+    launch_qkvg(h, L, L.tmA_in, L.tmB_qgkv, B * L.Rkv, 4 * d, L.bn_full, L.Rkv, sec, SSin, L.pos_kv);
+  } else {
+    const int rows = B * L.Rq;
+    k_gather_rows<<<(rows + 7) / 8, 256, 0, h.stream>>>(Xin, SSin, Xq, SSq, L.query_rows, B, L.Rkv, L.Rq, d);
+    check_launch("gather");
+    ++h.launches;
+    const int sec_kv[4] = {kSecK, kSecV, 0, 0};
+    launch_qkvg(h, L, L.tmA_in, L.tmB_kv, B * L.Rkv, 2 * d, L.bn_half, L.Rkv, sec_kv, SSin, L.pos_kv);
+    const int sec_qg[4] = {kSecQ, kSecG, 0, 0};
+    launch_qkvg(h, L, L.tmA_q, L.tmB_qg, B * L.Rq, 2 * d, L.bn_half, L.Rq, sec_qg, SSq, L.pos_q);
+  }
+  stage_mark(h, "L" + std::to_string(l) + ".qkvg");
+  launch_attention(h, L, lp, B);
+  stage_mark(h, "L" + std::to_string(l) + ".attention");
+  EpiResid eo;
+  eo.resid = attn_only ? nullptr : Xq;
+  eo.out = attn_only ? h.Qb : Xq;  // Q buffer is dead after attention
+  eo.ss_out = SSq;
+  eo.d = d;
+  eo.ss_atomic = 0;
+  launch_gemm(h, L.tmA_hg, L.tmB_o, B * L.Rq, d, d, d, eo);
+  stage_mark(h, "L" + std::to_string(l) + ".wo");
+  if (attn_only) return;
+  EpiSwiGLU eu;
+  eu.ss = SSq;
+  eu.inv_d = 1.f / static_cast<float>(d);
+  eu.hidden = h.hid;
+  eu.m = h.m;
+  launch_gemm(h, L.tmA_q, L.tmB_up, B * L.Rq, 2 * h.m, d, L.bn_up, eu);
+  stage_mark(h, "L" + std::to_string(l) + ".ffn_up");
+  EpiResid ed;
+  ed.resid = Xq;
+  ed.out = Xq;
+  ed.ss_out = SSq;
+  ed.d = d;
+  ed.ss_atomic = 0;
+  launch_gemm(h, L.tmA_hid, L.tmB_down, B * L.Rq, d, h.m, d, ed);
+  stage_mark(h, "L" + std::to_string(l) + ".ffn_down");
+}
+
+static void upload_batch(Handle& h, const SortBatch* b, bool on_device) {
+  const SortConfig& c = h.cfg;
+  const int B = b->batch;
+  if (B < 1 || B > h.Bmax) throw ConfigError("batch size must be in [1, max_batch]");
+  const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  const size_t nh = static_cast<size_t>(B) * c.n_hist;
+  auto cp = [&](void* dst, const void* src, size_t bytes) {
+    if (bytes == 0) return;
+    if (!src) throw ConfigError("batch array is null");
+    CK(cudaMemcpyAsync(dst, src, bytes, kind, h.stream));
+  };
+  cp(h.in_item, b->hist_item, nh * 4);
+  cp(h.in_action, b->hist_action, nh * 4);
+  cp(h.in_scene, b->hist_scene, nh * 4);
+  cp(h.in_ts, b->hist_ts, nh * 8);
+  cp(h.in_req, b->req_ts, static_cast<size_t>(B) * 8);
+  cp(h.in_prof, b->profile, static_cast<size_t>(B) * c.n_profile_fields * 4);
+  cp(h.in_cand, b->cand_item, static_cast<size_t>(B) * c.n_cand * 4);
+}
+
+static void begin_timing(Handle& h) {
+  for (auto e : h.events) cudaEventDestroy(e);
+  h.events.clear();
+  h.stage_names.clear();
+  h.launches = 0;
+  stage_mark(h, "start");
+}
+
+static void forward_device(Handle& h, int B) {
+  CK(cudaMemsetAsync(h.err, 0, 4 * sizeof(int32_t), h.stream));
+  run_tokenizer(h, B);
+  stage_mark(h, "tokenizer");
+  for (int l = 0; l < h.cfg.layers; ++l) run_layer(h, l, B);
+  const LayerDev& last = h.layers.back();
+  const int total = B * h.cfg.n_cand;
+  const size_t hsmem = static_cast<size_t>(kHeadRows) * (h.d + h.dh) * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_head, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+    attr = true;
+  }
+  k_head<<<(total + kHeadRows - 1) / kHeadRows, kHeadThreads, hsmem, h.stream>>>(
+      h.X[last.q_buf], h.SS[last.q_buf], last.Rq, h.cfg.n_cand, total, h.d, h.dh, h.head_gain,
+      h.head_w1, h.head_b1, h.head_w2, h.head_b2, h.probs, h.logits);
+  check_launch("head");
+  ++h.launches;
+  stage_mark(h, "head");
+}
+
+static void collect_status(Handle& h) {
+  int32_t err[4];
+  CK(cudaMemcpyAsync(err, h.err, sizeof(err), cudaMemcpyDeviceToHost, h.stream));
+  CK(cudaStreamSynchronize(h.stream));
+  if (h.timing && h.events.size() > 1) {
+    h.stage_ms.clear();
+    for (size_t i = 1; i < h.events.size(); ++i) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, h.events[i - 1], h.events[i]));
+      h.stage_ms.push_back(ms);
+    }
+  }
+  if (err[0] & kErrOOV) throw ConfigError("tokenizer: id outside vocabulary (device check)");
+}
+
+static Handle* H_(SortHandle p) {
+  if (!p) throw ConfigError("null handle");
+  Handle* h = reinterpret_cast<Handle*>(p);
+  CK(cudaSetDevice(h->device));
+  return h;
+}
+
+static Handle* ready(SortHandle p) {
+  Handle* h = H_(p);
+  if (!h->finalized) throw ConfigError("parameters not finalized (call sort_finalize_params)");
+  return h;
+}
+
+template <class F>
+static int api(F&& f) {
+  try {
+    f();
+    return SORT_OK;
+  } catch (const ConfigError& e) {
+    g_last_error = e.what();
+    return SORT_CONFIG_ERROR;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return SORT_RUNTIME_FAILURE;
+  }
+}
+
+// ------------------------------------------------------------------ op-level helpers
+static std::vector<float> bf16_to_f32(const std::vector<__nv_bfloat16>& v) {
+  std::vector<float> o(v.size());
+  for (size_t i = 0; i < v.size(); ++i) o[i] = __bfloat162float(v[i]);
+  return o;
+}
+
+}  // namespace sortk
+
+using namespace sortk;
+
+// ======================================================================= C ABI
+extern "C" {
+
+const char* sort_last_error(void) { return g_last_error.c_str(); }
+int sort_version(void) { return 1; }
+
+int sort_create(const SortConfig* cfg, int device, SortHandle* out) {
+  return api([&] {
+    if (!cfg || !out) throw ConfigError("null argument");
+    auto h = std::make_unique<Handle>();
+    h->cfg = *cfg;
+    h->device = device;
+    h->plan = make_plan(*cfg);
+    h->d = cfg->model_dim;
+    h->H = cfg->heads;
+    h->dk = cfg->model_dim / cfg->heads;
+    h->m = cfg->ffn_dim;
+    h->dh = cfg->head_hidden > 0 ? cfg->head_hidden : cfg->model_dim;
+    if (h->dh % 32 || h->dh > 1024) throw ConfigError("unsupported head_hidden");
+    h->L0 = h->plan.L0;
+    h->Bmax = cfg->max_batch;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw RuntimeFailure("no CUDA device available (libsort_b200 has no CPU path)");
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) throw RuntimeFailure("libsort_b200 requires an sm_100 (Blackwell) GPU");
+    h->num_sms = prop.multiProcessorCount;
+    CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    h->own_stream = true;
+    *out = reinterpret_cast<SortHandle>(h.release());
+  });
+}
+
+int sort_destroy(SortHandle p) {
+  return api([&] { delete reinterpret_cast<Handle*>(p); });
+}
+
+int sort_set_stream(SortHandle p, void* stream) {
+  return api([&] {
+    Handle* h = H_(p);
+    if (stream) {
+      if (h->own_stream) CK(cudaStreamDestroy(h->stream));
+      h->stream = static_cast<cudaStream_t>(stream);
+      h->own_stream = false;
+    }
+  });
+}
+
+int sort_load_param(SortHandle p, const char* name, const float* data, int64_t rows, int64_t cols) {
+  return api([&] {
+    Handle* h = reinterpret_cast<Handle*>(p);
+    if (!h || !name || !data) throw ConfigError("null argument");
+    if (h->finalized) throw ConfigError("parameters already finalized");
+    HostParam hp;
+    hp.rows = rows;
+    hp.cols = cols;
+    hp.v.assign(data, data + rows * cols);
+    h->host[name] = std::move(hp);
+  });
+}
+
+int sort_finalize_params(SortHandle p) {
+  return api([&] {
+    Handle* h = H_(p);
+    if (h->finalized) return;
+    finalize(*h);
+  });
+}
+
+int sort_forward(SortHandle p, const SortBatch* batch, int inputs_on_device, float* scores,
+                 int scores_on_device) {
+  return api([&] {
+    Handle* h = ready(p);
+    if (!batch || !scores) throw ConfigError("null argument");
+    begin_timing(*h);
+    upload_batch(*h, batch, inputs_on_device != 0);
+    forward_device(*h, batch->batch);
+    const size_t bytes = static_cast<size_t>(batch->batch) * h->cfg.n_cand * 3 * sizeof(float);
+    CK(cudaMemcpyAsync(scores, h->probs, bytes,
+                       scores_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->stream));
+    if (!(inputs_on_device && scores_on_device)) collect_status(*h);
+  });
+}
+
+int sort_sync(SortHandle p) {
+  return api([&] { collect_status(*ready(p)); });
+}
+
+int sort_forward_logits(SortHandle p, const SortBatch* batch, float* probs, float* logits) {
+  return api([&] {
+    Handle* h = ready(p);
+    if (!batch || !probs) throw ConfigError("null argument");
+    begin_timing(*h);
+    upload_batch(*h, batch, false);
+    forward_device(*h, batch->batch);
+    const size_t bytes = static_cast<size_t>(batch->batch) * h->cfg.n_cand * 3 * sizeof(float);
+    CK(cudaMemcpyAsync(probs, h->probs, bytes, cudaMemcpyDeviceToHost, h->stream));
+    if (logits) CK(cudaMemcpyAsync(logits, h->logits, bytes, cudaMemcpyDeviceToHost, h->stream));
+    collect_status(*h);
+  });
+}
+
+int sort_tokenize(SortHandle p, const SortBatch* batch, float* tokens, int32_t* hist_time,
+                  int32_t* position_ids, int32_t* roles, int32_t* candidate_index) {
+  return api([&] {
+    Handle* h = ready(p);
+    if (!batch) throw ConfigError("null argument");
+    begin_timing(*h);
+    upload_batch(*h, batch, false);
+    CK(cudaMemsetAsync(h->err, 0, 4 * sizeof(int32_t), h->stream));
+    run_tokenizer(*h, batch->batch);
+    const int B = batch->batch;
+    std::vector<__nv_bfloat16> xb(static_cast<size_t>(B) * h->L0 * h->d);
+    CK(cudaMemcpyAsync(xb.data(), h->X[0], xb.size() * 2, cudaMemcpyDeviceToHost, h->stream));
+    if (hist_time && h->cfg.n_hist)
+      CK(cudaMemcpyAsync(hist_time, h->hist_time, static_cast<size_t>(B) * h->cfg.n_hist * 4,
+                         cudaMemcpyDeviceToHost, h->stream));
+    collect_status(*h);
+    if (tokens) {
+      std::vector<float> f = bf16_to_f32(xb);
+      std::memcpy(tokens, f.data(), f.size() * sizeof(float));
+    }
+    const Plan& P = h->plan;
+    if (position_ids) std::copy(P.pos0.begin(), P.pos0.end(), position_ids);
+    if (roles) std::copy(P.roles0.begin(), P.roles0.end(), roles);
+    if (candidate_index) std::copy(P.cand_index0.begin(), P.cand_index0.end(), candidate_index);
+  });
+}
+
+int sort_layer_plan(SortHandle p, int layer, int32_t* l_q, int32_t* l_kv, int32_t* query_rows,
+                    int32_t* lo, int32_t* hi, int32_t* self_idx, int64_t* visible,
+                    int64_t* tiles_issued, int64_t* tiles_total) {
+  return api([&] {
+    Handle* h = reinterpret_cast<Handle*>(p);
+    if (!h) throw ConfigError("null handle");
+    if (layer < 0 || layer >= h->cfg.layers) throw ConfigError("layer out of range");
+    const LayerPlan& lp = h->plan.layers[layer];
+    if (l_q) *l_q = lp.l_q;
+    if (l_kv) *l_kv = lp.l_kv;
+    if (query_rows) std::copy(lp.query_rows.begin(), lp.query_rows.end(), query_rows);
+    if (lo) std::copy(lp.lo.begin(), lp.lo.end(), lo);
+    if (hi) std::copy(lp.hi.begin(), lp.hi.end(), hi);
+    if (self_idx) std::copy(lp.self_idx.begin(), lp.self_idx.end(), self_idx);
+    if (visible) *visible = lp.visible;
+    if (tiles_issued) *tiles_issued = lp.tiles_issued;
+    if (tiles_total) *tiles_total = lp.tiles_total;
+  });
+}
+
+int sort_attention_forward(SortHandle p, int layer, int32_t batch, const float* x, float* out) {
+  return api([&] {
+    Handle* h = ready(p);
+    if (layer < 0 || layer >= h->cfg.layers) throw ConfigError("layer out of range");
+    if (batch < 1 || batch > h->Bmax) throw ConfigError("batch out of range");
+    const LayerDev& L = h->layers[layer];
+    const size_t n_in = static_cast<size_t>(batch) * L.Rkv * h->d;
+    std::vector<__nv_bfloat16> xb(n_in);
+    std::vector<float> ss(static_cast<size_t>(batch) * L.Rkv, 0.f);
+    for (size_t i = 0; i < n_in; ++i) {
+      xb[i] = f2bf(x[i]);
+      const float f = __bfloat162float(xb[i]);
+      ss[i / h->d] += f * f;
+    }
+    begin_timing(*h);
+    CK(cudaMemcpyAsync(h->X[L.in_buf], xb.data(), n_in * 2, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(h->SS[L.in_buf], ss.data(), ss.size() * 4, cudaMemcpyHostToDevice, h->stream));
+    run_layer(*h, layer, batch, /*attn_only=*/true);
+    const size_t n_out = static_cast<size_t>(batch) * L.Rq * h->d;
+    std::vector<__nv_bfloat16> ob(n_out);
+    CK(cudaMemcpyAsync(ob.data(), h->Qb, n_out * 2, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    for (size_t i = 0; i < n_out; ++i) out[i] = __bfloat162float(ob[i]);
+  });
+}
+
+int sort_block_attention(int32_t nh, int32_t l_q, int32_t l_kv, int32_t dk, const float* q,
+                         const float* k, const float* v, const int32_t* lo, const int32_t* hi,
+                         const int32_t* self_idx, float* out, int64_t* skipped, int64_t* total) {
+  return api([&] {
+    if (nh < 1 || l_q < 1 || l_kv < 1) throw ConfigError("block_attention: bad shape");
+    if (dk != 16 && dk != 32 && dk != 64) throw ConfigError("block_attention: dk must be 16/32/64");
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    Handle h;
+    h.device = dev;
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major != 10) throw RuntimeFailure("requires an sm_100 GPU");
+    h.num_sms = prop.multiProcessorCount;
+    CK(cudaStreamCreateWithFlags(&h.stream, cudaStreamNonBlocking));
+    h.own_stream = true;
+    h.d = dk;  // one head per "request": out rows are [nh * l_q, dk]
+    h.H = 1;
+    h.dk = dk;
+    LayerPlan lp;
+    lp.l_q = l_q;
+    lp.l_kv = l_kv;
+    lp.lo.assign(lo, lo + l_q);
+    lp.hi.assign(hi, hi + l_q);
+    lp.self_idx.assign(self_idx, self_idx + l_q);
+    build_tiles(lp);
+    LayerDev L;
+    L.Rq = l_q;
+    L.Rkv = l_kv;
+    L.Rkv_pad = (l_kv + 7) / 8 * 8;
+    std::vector<int4> meta(static_cast<size_t>(lp.n_qtiles) * 128, make_int4(0, -1, -1, 0));
+    for (int r = 0; r < l_q; ++r) meta[r] = make_int4(lo[r], hi[r], self_idx[r], 0);
+    L.rowmeta = h.upload(meta);
+    L.tile_off = h.upload(lp.tile_off);
+    L.tile_code = h.upload(lp.tile_code.empty() ? std::vector<int32_t>{0} : lp.tile_code);
+    L.qtile_order = h.upload(lp.qtile_order);
+    auto up = [&](const float* src, size_t n) {
+      std::vector<__nv_bfloat16> b(n);
+      for (size_t i = 0; i < n; ++i) b[i] = f2bf(src[i]);
+      return h.upload(b);
+    };
+    h.Qb = up(q, static_cast<size_t>(nh) * l_q * dk);
+    h.Kb = up(k, static_cast<size_t>(nh) * l_kv * dk);
+    std::vector<__nv_bfloat16> vt(static_cast<size_t>(nh) * dk * L.Rkv_pad, f2bf(0.f));
+    for (int b = 0; b < nh; ++b)
+      for (int c = 0; c < l_kv; ++c)
+        for (int i = 0; i < dk; ++i)
+          vt[(static_cast<size_t>(b) * dk + i) * L.Rkv_pad + c] = f2bf(v[(static_cast<size_t>(b) * l_kv + c) * dk + i]);
+    h.Vt = h.upload(vt);
+    h.Gb = h.upload(std::vector<__nv_bfloat16>(static_cast<size_t>(nh) * l_q * dk, f2bf(1.f)));
+    h.Hg = h.dalloc<__nv_bfloat16>(static_cast<size_t>(nh) * l_q * dk);
+    uint64_t dq[3] = {static_cast<uint64_t>(dk), static_cast<uint64_t>(l_q), static_cast<uint64_t>(nh)};
+    uint64_t sq[2] = {static_cast<uint64_t>(dk) * 2, static_cast<uint64_t>(l_q) * dk * 2};
+    uint32_t bq[3] = {static_cast<uint32_t>(dk), 128, 1};
+    L.tmQ = make_tmap_bf16(h.Qb, 3, dq, sq, bq, dk * 2);
+    uint64_t dkd[3] = {static_cast<uint64_t>(dk), static_cast<uint64_t>(l_kv), static_cast<uint64_t>(nh)};
+    uint64_t skd[2] = {static_cast<uint64_t>(dk) * 2, static_cast<uint64_t>(l_kv) * dk * 2};
+    L.tmK = make_tmap_bf16(h.Kb, 3, dkd, skd, bq, dk * 2);
+    uint64_t dv[3] = {static_cast<uint64_t>(L.Rkv_pad), static_cast<uint64_t>(dk), static_cast<uint64_t>(nh)};
+    uint64_t sv[2] = {static_cast<uint64_t>(L.Rkv_pad) * 2, static_cast<uint64_t>(L.Rkv_pad) * dk * 2};
+    uint32_t bv[3] = {64, static_cast<uint32_t>(dk), 1};
+    L.tmV = make_tmap_bf16(h.Vt, 3, dv, sv, bv, 128);
+    launch_attention(h, L, lp, nh);
+    std::vector<__nv_bfloat16> ob(static_cast<size_t>(nh) * l_q * dk);
+    CK(cudaMemcpyAsync(ob.data(), h.Hg, ob.size() * 2, cudaMemcpyDeviceToHost, h.stream));
+    CK(cudaStreamSynchronize(h.stream));
+    for (size_t i = 0; i < ob.size(); ++i) out[i] = __bfloat162float(ob[i]);
+    if (skipped) *skipped = lp.tiles_total - lp.tiles_issued;
+    if (total) *total = lp.tiles_total;
+  });
+}
+
+int sort_time_bucket(int64_t delta_seconds, int32_t n_buckets) {
+  return time_bucket_int(delta_seconds, n_buckets);
+}
+
+int sort_geometric_schedule(int32_t prefix_len, int32_t depth, int32_t target, int32_t* keep) {
+  return api([&] {
+    std::vector<int32_t> k = geometric_schedule(prefix_len, depth, target);
+    std::copy(k.begin(), k.end(), keep);
+  });
+}
+
+int sort_retained_rows(const int32_t* roles, int32_t n, int32_t keep, int32_t keep_specials,
+                       int32_t* rows, int32_t* n_rows) {
+  return api([&] {
+    std::vector<int32_t> r(roles, roles + n);
+    std::vector<int32_t> o = retained_rows(r, keep, keep_specials != 0);
+    std::copy(o.begin(), o.end(), rows);
+    *n_rows = static_cast<int32_t>(o.size());
+  });
+}
+
+int sort_mask_intervals(int32_t l_q, int32_t l_kv, int32_t local_window, int32_t full_suffix,
+                        const int32_t* roles, const int32_t* position_ids, const int32_t* query_rows,
+                        int32_t* lo, int32_t* hi, int32_t* self_idx) {
+  return api([&] {
+    mask_intervals(l_q, l_kv, local_window, full_suffix, roles, position_ids, query_rows, lo, hi, self_idx);
+  });
+}
+
+int sort_kernel_count(SortHandle p, int32_t* launches) {
+  return api([&] {
+    Handle* h = reinterpret_cast<Handle*>(p);
+    if (!h || !launches) throw ConfigError("null argument");
+    *launches = h->launches;
+  });
+}
+
+int sort_enable_stage_timing(SortHandle p, int enable) {
+  return api([&] {
+    Handle* h = reinterpret_cast<Handle*>(p);
+    if (!h) throw ConfigError("null handle");
+    h->timing = enable != 0;
+  });
+}
+
+int sort_stage_times(SortHandle p, float* ms, int32_t cap, int32_t* n, char* names, int32_t names_cap) {
+  return api([&] {
+    Handle* h = reinterpret_cast<Handle*>(p);
+    if (!h) throw ConfigError("null handle");
+    const int cnt = static_cast<int>(std::min<size_t>(h->stage_ms.size(), static_cast<size_t>(cap)));
+    for (int i = 0; i < cnt; ++i) ms[i] = h->stage_ms[i];
+    *n = cnt;
+    std::string s;
+    for (int i = 0; i < cnt; ++i) s += (i ? ";" : "") + h->stage_names[i + 1];
+    if (names && names_cap > 0) {
+      std::strncpy(names, s.c_str(), static_cast<size_t>(names_cap) - 1);
+      names[names_cap - 1] = 0;
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,269 @@
+// SPDX-License-Identifier: Apache-2.0
+// K1: feature tokenizer -- Tokenizer::tokenize_sample (tokenizer.cpp:144-238) for a
+// whole batch in one persistent kernel.
+//
+// Each 128-row tile belongs to one token group (history / candidate / profile):
+//   1. gather: one thread per token row issues 16-byte vector loads of the
+//      embedding rows (item | action | scene | time for history, tokenizer.cpp:95-112;
+//      item for candidates, :114-127; profile_table[f] for profile fields, :196-205)
+//      straight into the SW128 K-major A-operand layout in shared memory (K padded
+//      to 64 with zeros). Ids are range-checked (check_id, :14-19): an
+//      out-of-vocabulary id raises the device error flag and reads row 0 instead.
+//   2. one tcgen05.mma chain (M=128, N=d, K=64) projects the tile against the
+//      group's W^T (resident in smem) into TMEM.
+//   3. epilogue (thread <-> row): + bias, RMSNorm with the group gain (norm.hpp:17-29,
+//      emit_group :220-229), bf16 token row + its fp32 sum of squares (the
+//      next pre-norm's statistic) written to the row's place in the sequence.
+// BOS/SEP rows copy the special table (:171-176). Positions/roles are batch-uniform
+// and live in the host plan.
+#pragma once
+
+#include "ptx.cuh"
+
+namespace sortk {
+
+struct TokParams {
+  // tables (bf16, row-major)
+  const __nv_bfloat16* item_tab;
+  const __nv_bfloat16* action_tab;
+  const __nv_bfloat16* scene_tab;
+  const __nv_bfloat16* time_tab;
+  const __nv_bfloat16* prof_tab;  // all profile tables concatenated
+  const __nv_bfloat16* special;   // [3, d]
+  int prof_row_off[SORT_MAX_PROFILE_FIELDS];
+  int prof_vocab[SORT_MAX_PROFILE_FIELDS];
+  // per-group projection W^T [d, 64] bf16 (K-major, zero padded) + bias/gain fp32 [d]
+  const __nv_bfloat16* wt[3];
+  const float* bias[3];
+  const float* gain[3];
+  // inputs (device)
+  const int32_t* hist_item;
+  const int32_t* hist_action;
+  const int32_t* hist_scene;
+  const int64_t* hist_ts;
+  const int64_t* req_ts;
+  const int32_t* profile;
+  const int32_t* cand_item;
+  // outputs
+  __nv_bfloat16* x;      // [B, L, d]
+  float* ss;             // [B, L] sum of squares of the bf16 token row
+  int32_t* hist_time;    // [B, H] or null
+  int32_t* err;          // device error flags
+  // geometry
+  int B, H, P, N, L, d;
+  int item_dim, action_dim, scene_dim, time_dim, prof_dim;
+  int n_items, n_actions, n_scenes, n_tb;
+  int special_tokens;
+  int tiles_hist, tiles_cand, tiles_prof;
+};
+
+enum : int { kGroupHist = 0, kGroupCand = 1, kGroupProf = 2 };
+constexpr int kTokThreads = 128;
+constexpr int kErrOOV = 1;
+
+__device__ __forceinline__ int tok_time_bucket(int64_t delta, int nb) {
+  // time_bucket (tokenizer.cpp:36-40) in exact integer form (valid for nb <= 48).
+  const unsigned long long d = delta > 0 ? static_cast<unsigned long long>(delta) : 0ull;
+  const int b = 63 - __clzll(static_cast<long long>(d + 1ull));
+  return b < nb - 1 ? b : nb - 1;
+}
+
+// Copy `n8` 16-byte chunks from src into the swizzled A row starting at chunk c0.
+__device__ __forceinline__ void tok_put(uint8_t* arow, int r, int c0, const __nv_bfloat16* src, int n8) {
+  const int4* s = reinterpret_cast<const int4*>(src);
+#pragma unroll 4
+  for (int i = 0; i < n8; ++i) {
+    const int c = c0 + i;
+    *reinterpret_cast<int4*>(arow + ((c ^ (r & 7)) << 4)) = __ldg(s + i);
+  }
+}
+
+__global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  const int d = p.d;
+  uint8_t* sW = smem;                       // [d rows x 128 B] SW128
+  uint8_t* sA = smem + d * 128;             // [128 rows x 128 B] SW128
+  float* sBias = reinterpret_cast<float*>(sA + 128 * 128);
+  float* sGain = sBias + d;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sGain + d);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const uint32_t tcols = d <= 32 ? 32 : (d <= 64 ? 64 : (d <= 128 ? 128 : 256));
+  if (t == 0) {
+    mbar_init(bar, 1);
+    mbar_fence_init();
+  }
+  if (warp == 0) tmem_alloc(tslot, tcols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t idesc = umma_idesc_bf16(128, d);
+
+  const int n_tiles = p.tiles_hist + p.tiles_cand + p.tiles_prof;
+  const int st = p.special_tokens ? 1 : 0;
+  const int off_hist = st, off_prof = st + p.H + st, off_cand = off_prof + p.P + st;
+  int cur_group = -1;
+  uint32_t phase = 0;
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    int group, e0, count;
+    if (tile < p.tiles_hist) {
+      group = kGroupHist; e0 = tile * 128; count = p.B * p.H;
+    } else if (tile < p.tiles_hist + p.tiles_cand) {
+      group = kGroupCand; e0 = (tile - p.tiles_hist) * 128; count = p.B * p.N;
+    } else {
+      group = kGroupProf; e0 = (tile - p.tiles_hist - p.tiles_cand) * 128; count = p.B * p.P;
+    }
+    if (group != cur_group) {  // (re)load this group's W^T, bias and gain
+      __syncthreads();
+      const int4* w = reinterpret_cast<const int4*>(p.wt[group]);
+      for (int i = t; i < d * 8; i += kTokThreads) {
+        const int n = i >> 3, c = i & 7;
+        *reinterpret_cast<int4*>(sW + n * 128 + ((c ^ (n & 7)) << 4)) = __ldg(w + i);
+      }
+      for (int i = t; i < d; i += kTokThreads) {
+        sBias[i] = p.bias[group][i];
+        sGain[i] = p.gain[group][i];
+      }
+      cur_group = group;
+    }
+    // ---- 1. gather this thread's row into the swizzled A tile
+    const int e = e0 + t;
+    const bool valid = e < count;
+    uint8_t* arow = sA + t * 128;
+    int out_row = -1;
+    int nchunks = 0;
+    if (valid) {
+      if (group == kGroupHist) {
+        const int b = e / p.H, i = e - b * p.H;
+        int item = p.hist_item[e], act = p.hist_action[e], sc = p.hist_scene[e];
+        const int tb = tok_time_bucket(p.req_ts[b] - p.hist_ts[e], p.n_tb);
+        if (static_cast<unsigned>(item) >= static_cast<unsigned>(p.n_items) ||
+            static_cast<unsigned>(act) >= static_cast<unsigned>(p.n_actions) ||
+            static_cast<unsigned>(sc) >= static_cast<unsigned>(p.n_scenes)) {
+          atomicOr(p.err, kErrOOV);
+          item = static_cast<unsigned>(item) < static_cast<unsigned>(p.n_items) ? item : 0;
+          act = static_cast<unsigned>(act) < static_cast<unsigned>(p.n_actions) ? act : 0;
+          sc = static_cast<unsigned>(sc) < static_cast<unsigned>(p.n_scenes) ? sc : 0;
+        }
+        if (p.hist_time) p.hist_time[e] = tb;
+        int c = 0;
+        tok_put(arow, t, c, p.item_tab + static_cast<size_t>(item) * p.item_dim, p.item_dim >> 3);
+        c += p.item_dim >> 3;
+        tok_put(arow, t, c, p.action_tab + static_cast<size_t>(act) * p.action_dim, p.action_dim >> 3);
+        c += p.action_dim >> 3;
+        tok_put(arow, t, c, p.scene_tab + static_cast<size_t>(sc) * p.scene_dim, p.scene_dim >> 3);
+        c += p.scene_dim >> 3;
+        tok_put(arow, t, c, p.time_tab + static_cast<size_t>(tb) * p.time_dim, p.time_dim >> 3);
+        nchunks = c + (p.time_dim >> 3);
+        out_row = b * p.L + off_hist + i;
+      } else if (group == kGroupCand) {
+        const int b = e / p.N, j = e - b * p.N;
+        int item = p.cand_item[e];
+        if (static_cast<unsigned>(item) >= static_cast<unsigned>(p.n_items)) {
+          atomicOr(p.err, kErrOOV);
+          item = 0;
+        }
+        tok_put(arow, t, 0, p.item_tab + static_cast<size_t>(item) * p.item_dim, p.item_dim >> 3);
+        nchunks = p.item_dim >> 3;
+        out_row = b * p.L + off_cand + j;
+      } else {
+        const int b = e / p.P, f = e - b * p.P;
+        int v = p.profile[e];
+        if (static_cast<unsigned>(v) >= static_cast<unsigned>(p.prof_vocab[f])) {
+          atomicOr(p.err, kErrOOV);
+          v = 0;
+        }
+        tok_put(arow, t, 0, p.prof_tab + static_cast<size_t>(p.prof_row_off[f] + v) * p.prof_dim,
+                p.prof_dim >> 3);
+        nchunks = p.prof_dim >> 3;
+        out_row = b * p.L + off_prof + f;
+      }
+    }
+    for (int c = nchunks; c < 8; ++c)
+      *reinterpret_cast<int4*>(arow + ((c ^ (t & 7)) << 4)) = make_int4(0, 0, 0, 0);
+    fence_proxy_async_smem();
+    __syncthreads();
+    // ---- 2. projection on the tensor cores
+    if (t == 0) {
+      tc_fence_after();
+      const uint32_t a0 = smem_u32(sA), b0 = smem_u32(sW);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        mma_bf16_ss(tmem, umma_sdesc_kmajor(a0 + k * 32, 128), umma_sdesc_kmajor(b0 + k * 32, 128),
+                    idesc, k > 0 ? 1u : 0u);
+      mma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    // ---- 3. epilogue: bias + RMSNorm(gain) -> bf16 row + sum of squares
+    const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    float ss = 0.f;
+    for (int c = 0; c < d; c += 16) {
+      uint32_t r[16];
+      tmem_ld_32x32b_x16(trow + c, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float v = __uint_as_float(r[i]) + sBias[c + i];
+        ss += v * v;
+      }
+    }
+    const float inv = rsqrtf(ss / static_cast<float>(d) + 1e-6f);
+    float ss_out = 0.f;
+    for (int c = 0; c < d; c += 16) {
+      uint32_t r[16];
+      tmem_ld_32x32b_x16(trow + c, r);
+      tmem_ld_wait();
+      uint32_t packed[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float y0 = (__uint_as_float(r[2 * i]) + sBias[c + 2 * i]) * inv * sGain[c + 2 * i];
+        const float y1 = (__uint_as_float(r[2 * i + 1]) + sBias[c + 2 * i + 1]) * inv * sGain[c + 2 * i + 1];
+        packed[i] = pack_bf16x2(y0, y1);
+        const __nv_bfloat162 q = *reinterpret_cast<__nv_bfloat162*>(&packed[i]);
+        const float q0 = __bfloat162float(q.x), q1 = __bfloat162float(q.y);
+        ss_out += q0 * q0 + q1 * q1;
+      }
+      if (valid) {
+        int4* dst = reinterpret_cast<int4*>(p.x + static_cast<size_t>(out_row) * d + c);
+        dst[0] = make_int4(packed[0], packed[1], packed[2], packed[3]);
+        dst[1] = make_int4(packed[4], packed[5], packed[6], packed[7]);
+      }
+    }
+    if (valid) p.ss[out_row] = ss_out;
+    tc_fence_before();
+    __syncthreads();
+  }
+  // ---- BOS / SEP rows: raw special-table rows (tokenizer.cpp:171-176), one warp per row.
+  if (p.special_tokens) {
+    const int nwarps = gridDim.x * (kTokThreads / 32);
+    for (int w = blockIdx.x * (kTokThreads / 32) + warp; w < p.B * 3; w += nwarps) {
+      const int b = w / 3, k = w - b * 3;
+      const int row = b * p.L + (k == 0 ? 0 : (k == 1 ? 1 + p.H : 2 + p.H + p.P));
+      float ss = 0.f;
+      for (int c = lane; c < d; c += 32) {
+        const __nv_bfloat16 v = p.special[k * d + c];
+        p.x[static_cast<size_t>(row) * d + c] = v;
+        const float f = __bfloat162float(v);
+        ss += f * f;
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (lane == 0) p.ss[row] = ss;
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, tcols);
+  }
+}
+
+inline size_t tok_smem_bytes(int d) { return 1024 + d * 128 + 128 * 128 + 2 * d * 4 + 16; }
+
+}  // namespace sortk

@@ -1,0 +1,296 @@
+# SPDX-License-Identifier: Apache-2.0
+"""ctypes binding of libsort_b200.so (include/sort_b200.h).
+
+Mirrors the reference's operator API for the hot path with the same names and
+error behaviour: config/input problems raise :class:`ConfigError` (status 1,
+rankformer::ConfigError), runtime failures raise :class:`RuntimeFailure`
+(status 2). There is no CPU fallback: if the library is missing or no sm_100
+GPU is present, construction fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Dict, Optional
+
+import numpy as np
+
+from .config import ConfigError, RuntimeFailure, SortConfig
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libsort_b200.so")
+
+i32p = C.POINTER(C.c_int32)
+i64p = C.POINTER(C.c_int64)
+f32p = C.POINTER(C.c_float)
+
+
+class CSortConfig(C.Structure):
+    _fields_ = [
+        ("model_dim", C.c_int32), ("heads", C.c_int32), ("layers", C.c_int32),
+        ("ffn_dim", C.c_int32), ("head_hidden", C.c_int32),
+        ("item_dim", C.c_int32), ("action_dim", C.c_int32), ("scene_dim", C.c_int32),
+        ("time_dim", C.c_int32), ("profile_dim", C.c_int32),
+        ("n_items", C.c_int32), ("n_actions", C.c_int32), ("n_scenes", C.c_int32),
+        ("n_time_buckets", C.c_int32), ("n_profile_fields", C.c_int32),
+        ("profile_vocab", C.c_int32 * 16),
+        ("special_tokens", C.c_int32), ("qknorm", C.c_int32), ("gate", C.c_int32),
+        ("rope_theta", C.c_double), ("local_window", C.c_int32), ("full_suffix", C.c_int32),
+        ("keep", C.c_int32 * 64), ("keep_specials", C.c_int32),
+        ("max_batch", C.c_int32), ("n_hist", C.c_int32), ("n_cand", C.c_int32),
+    ]
+
+
+class CSortBatch(C.Structure):
+    _fields_ = [
+        ("batch", C.c_int32), ("hist_item", C.c_void_p), ("hist_action", C.c_void_p),
+        ("hist_scene", C.c_void_p), ("hist_ts", C.c_void_p), ("req_ts", C.c_void_p),
+        ("profile", C.c_void_p), ("cand_item", C.c_void_p),
+    ]
+
+
+EXPORTS = [
+    "sort_last_error", "sort_version", "sort_create", "sort_destroy", "sort_set_stream",
+    "sort_load_param", "sort_finalize_params", "sort_forward", "sort_sync", "sort_forward_logits",
+    "sort_tokenize", "sort_layer_plan", "sort_attention_forward", "sort_block_attention",
+    "sort_time_bucket", "sort_geometric_schedule", "sort_retained_rows", "sort_mask_intervals",
+    "sort_kernel_count", "sort_enable_stage_timing", "sort_stage_times",
+]
+
+_lib = None
+
+
+def lib():
+    """Load the CUDA library (raises if it was not built -- no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeFailure(f"{LIB_PATH} not built; run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        L.sort_last_error.restype = C.c_char_p
+        L.sort_create.argtypes = [C.POINTER(CSortConfig), C.c_int, C.POINTER(C.c_void_p)]
+        L.sort_destroy.argtypes = [C.c_void_p]
+        L.sort_set_stream.argtypes = [C.c_void_p, C.c_void_p]
+        L.sort_load_param.argtypes = [C.c_void_p, C.c_char_p, f32p, C.c_int64, C.c_int64]
+        L.sort_finalize_params.argtypes = [C.c_void_p]
+        L.sort_forward.argtypes = [C.c_void_p, C.POINTER(CSortBatch), C.c_int, C.c_void_p, C.c_int]
+        L.sort_sync.argtypes = [C.c_void_p]
+        L.sort_forward_logits.argtypes = [C.c_void_p, C.POINTER(CSortBatch), f32p, f32p]
+        L.sort_tokenize.argtypes = [C.c_void_p, C.POINTER(CSortBatch), f32p, i32p, i32p, i32p, i32p]
+        L.sort_layer_plan.argtypes = [C.c_void_p, C.c_int, i32p, i32p, i32p, i32p, i32p, i32p, i64p,
+                                      i64p, i64p]
+        L.sort_attention_forward.argtypes = [C.c_void_p, C.c_int, C.c_int32, f32p, f32p]
+        L.sort_block_attention.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, f32p, f32p,
+                                           f32p, i32p, i32p, i32p, f32p, i64p, i64p]
+        L.sort_time_bucket.argtypes = [C.c_int64, C.c_int32]
+        L.sort_geometric_schedule.argtypes = [C.c_int32, C.c_int32, C.c_int32, i32p]
+        L.sort_retained_rows.argtypes = [i32p, C.c_int32, C.c_int32, C.c_int32, i32p, i32p]
+        L.sort_mask_intervals.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, i32p, i32p,
+                                          i32p, i32p, i32p, i32p]
+        L.sort_kernel_count.argtypes = [C.c_void_p, i32p]
+        L.sort_enable_stage_timing.argtypes = [C.c_void_p, C.c_int]
+        L.sort_stage_times.argtypes = [C.c_void_p, f32p, C.c_int32, i32p, C.c_char_p, C.c_int32]
+        _lib = L
+    return _lib
+
+
+def _check(status: int) -> None:
+    if status == 0:
+        return
+    msg = lib().sort_last_error().decode()
+    if status == 1:
+        raise ConfigError(msg)
+    raise RuntimeFailure(msg)
+
+
+def _p(a: np.ndarray, t):
+    return a.ctypes.data_as(t)
+
+
+def to_c_config(cfg: SortConfig, max_batch: Optional[int] = None) -> CSortConfig:
+    cfg.validate()
+    c = CSortConfig()
+    c.model_dim, c.heads, c.layers, c.ffn_dim = cfg.model_dim, cfg.heads, cfg.layers, cfg.ffn_dim
+    c.head_hidden = cfg.head_hidden
+    c.item_dim, c.action_dim, c.scene_dim = cfg.item_dim, cfg.action_dim, cfg.scene_dim
+    c.time_dim, c.profile_dim = cfg.time_dim, cfg.profile_dim
+    c.n_items, c.n_actions, c.n_scenes = cfg.n_items, cfg.n_actions, cfg.n_scenes
+    c.n_time_buckets, c.n_profile_fields = cfg.n_time_buckets, cfg.n_prof
+    for i, v in enumerate(cfg.profile_vocab):
+        c.profile_vocab[i] = v
+    c.special_tokens, c.qknorm, c.gate = int(cfg.special_tokens), int(cfg.qknorm), int(cfg.gate)
+    c.rope_theta = cfg.rope_theta
+    c.local_window, c.full_suffix = cfg.local_window, cfg.full_suffix
+    for i, k in enumerate(cfg.keep_schedule()):
+        c.keep[i] = k
+    c.keep_specials = int(cfg.keep_specials)
+    c.max_batch = max_batch or cfg.batch
+    c.n_hist, c.n_cand = cfg.n_hist, cfg.n_cand
+    return c
+
+
+# ----------------------------------------------------------------- host planner (no GPU)
+def time_bucket(delta: int, n_buckets: int = 32) -> int:
+    return lib().sort_time_bucket(int(delta), int(n_buckets))
+
+
+def geometric_schedule(prefix_len: int, depth: int, target: int):
+    out = np.zeros(max(depth, 1), np.int32)
+    _check(lib().sort_geometric_schedule(prefix_len, depth, target, _p(out, i32p)))
+    return out.tolist()
+
+
+def retained_rows(roles, keep: int, keep_specials: bool):
+    r = np.ascontiguousarray(roles, np.int32)
+    out = np.zeros(len(r), np.int32)
+    n = C.c_int32(0)
+    _check(lib().sort_retained_rows(_p(r, i32p), len(r), keep, int(keep_specials), _p(out, i32p),
+                                    C.byref(n)))
+    return out[: n.value].tolist()
+
+
+def mask_intervals(roles, pos, query_rows, window: int, full_suffix: int):
+    r = np.ascontiguousarray(roles, np.int32)
+    p = np.ascontiguousarray(pos, np.int32)
+    q = np.ascontiguousarray(query_rows, np.int32)
+    lo, hi, se = (np.zeros(len(q), np.int32) for _ in range(3))
+    _check(lib().sort_mask_intervals(len(q), len(r), window, full_suffix, _p(r, i32p), _p(p, i32p),
+                                     _p(q, i32p), _p(lo, i32p), _p(hi, i32p), _p(se, i32p)))
+    return lo, hi, se
+
+
+def block_attention(q: np.ndarray, k: np.ndarray, v: np.ndarray, lo, hi, self_idx):
+    """blockwise_masked_attention on the GPU kernel: q [nh, lq, dk], k/v [nh, lkv, dk]."""
+    q, k, v = (np.ascontiguousarray(a, np.float32) for a in (q, k, v))
+    nh, lq, dk = q.shape
+    lkv = k.shape[1]
+    lo, hi, se = (np.ascontiguousarray(a, np.int32) for a in (lo, hi, self_idx))
+    out = np.zeros((nh, lq, dk), np.float32)
+    sk, tot = C.c_int64(0), C.c_int64(0)
+    _check(lib().sort_block_attention(nh, lq, lkv, dk, _p(q, f32p), _p(k, f32p), _p(v, f32p),
+                                      _p(lo, i32p), _p(hi, i32p), _p(se, i32p), _p(out, f32p),
+                                      C.byref(sk), C.byref(tot)))
+    return out, sk.value, tot.value
+
+
+# ----------------------------------------------------------------- model handle
+class _BatchHold:
+    KEYS = ("hist_item", "hist_action", "hist_scene", "hist_ts", "req_ts", "profile", "cand_item")
+    DT = {"hist_ts": np.int64, "req_ts": np.int64}
+
+    def __init__(self, batch: Dict[str, np.ndarray]):
+        self.arrs = {k: np.ascontiguousarray(batch[k], dtype=self.DT.get(k, np.int32)) for k in self.KEYS}
+        a = self.arrs
+        self.c = CSortBatch(int(a["req_ts"].shape[0]), *[a[k].ctypes.data for k in self.KEYS])
+
+
+class _DevBatch:
+    """SortBatch of device pointers (torch CUDA tensors) for the device-resident path."""
+
+    def __init__(self, tensors):
+        self.t = tensors
+        self.c = CSortBatch(int(tensors["req_ts"].shape[0]),
+                            *[tensors[k].data_ptr() for k in _BatchHold.KEYS])
+
+
+class SortModel:
+    """One handle per GPU: the batched SORT forward behind the C ABI."""
+
+    def __init__(self, cfg: SortConfig, params: Dict[str, np.ndarray], device: int = 0,
+                 max_batch: Optional[int] = None):
+        self.cfg = cfg
+        self.max_batch = max_batch or cfg.batch
+        h = C.c_void_p()
+        _check(lib().sort_create(C.byref(to_c_config(cfg, self.max_batch)), device, C.byref(h)))
+        self.h = h
+        for name, a in params.items():
+            a32 = np.ascontiguousarray(a, np.float32)
+            if a32.ndim != 2:
+                raise ConfigError(f"parameter {name} must be 2-D")
+            _check(lib().sort_load_param(self.h, name.encode(), _p(a32, f32p), a32.shape[0],
+                                         a32.shape[1]))
+        _check(lib().sort_finalize_params(self.h))
+
+    def close(self):
+        if getattr(self, "h", None) is not None and _lib is not None:
+            _lib.sort_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def set_stream(self, stream_ptr: int):
+        _check(lib().sort_set_stream(self.h, C.c_void_p(stream_ptr)))
+
+    # -- forward (model_forward) ---------------------------------
+    def forward(self, batch: Dict[str, np.ndarray]) -> np.ndarray:
+        hold = _BatchHold(batch)
+        B = hold.c.batch
+        out = np.zeros((B, self.cfg.n_cand, 3), np.float32)
+        _check(lib().sort_forward(self.h, C.byref(hold.c), 0, out.ctypes.data, 0))
+        return out
+
+    def forward_logits(self, batch: Dict[str, np.ndarray]):
+        hold = _BatchHold(batch)
+        B = hold.c.batch
+        probs = np.zeros((B, self.cfg.n_cand, 3), np.float32)
+        logits = np.zeros((B, self.cfg.n_cand, 3), np.float32)
+        _check(lib().sort_forward_logits(self.h, C.byref(hold.c), _p(probs, f32p), _p(logits, f32p)))
+        return probs, logits
+
+    def forward_device(self, dev_batch: "_DevBatch", scores_ptr: int):
+        """Device-resident inputs and outputs: enqueue only (no host sync)."""
+        _check(lib().sort_forward(self.h, C.byref(dev_batch.c), 1, C.c_void_p(scores_ptr), 1))
+
+    def sync(self):
+        _check(lib().sort_sync(self.h))
+
+    # -- parity ops ------------------------------------------------------------
+    def tokenize(self, batch: Dict[str, np.ndarray]):
+        hold = _BatchHold(batch)
+        B, L = hold.c.batch, self.cfg.seq_len
+        tokens = np.zeros((B, L, self.cfg.model_dim), np.float32)
+        ht = np.zeros((B, max(self.cfg.n_hist, 1)), np.int32)
+        pos, roles, cidx = (np.zeros(L, np.int32) for _ in range(3))
+        _check(lib().sort_tokenize(self.h, C.byref(hold.c), _p(tokens, f32p), _p(ht, i32p),
+                                   _p(pos, i32p), _p(roles, i32p), _p(cidx, i32p)))
+        return {"tokens": tokens, "hist_time": ht[:, : self.cfg.n_hist], "position_ids": pos,
+                "roles": roles, "candidate_index": cidx}
+
+    def layer_plan(self, layer: int):
+        L = self.cfg.seq_len
+        lq, lkv = C.c_int32(0), C.c_int32(0)
+        qr, lo, hi, se = (np.zeros(L, np.int32) for _ in range(4))
+        vis, ti, tt = C.c_int64(0), C.c_int64(0), C.c_int64(0)
+        _check(lib().sort_layer_plan(self.h, layer, C.byref(lq), C.byref(lkv), _p(qr, i32p),
+                                     _p(lo, i32p), _p(hi, i32p), _p(se, i32p), C.byref(vis),
+                                     C.byref(ti), C.byref(tt)))
+        n = lq.value
+        return {"l_q": n, "l_kv": lkv.value, "query_rows": qr[:n], "lo": lo[:n], "hi": hi[:n],
+                "self": se[:n], "visible": vis.value, "tiles_issued": ti.value,
+                "tiles_total": tt.value}
+
+    def attention_forward(self, layer: int, x: np.ndarray) -> np.ndarray:
+        x = np.ascontiguousarray(x, np.float32)
+        B = x.shape[0]
+        plan = self.layer_plan(layer)
+        out = np.zeros((B, plan["l_q"], self.cfg.model_dim), np.float32)
+        _check(lib().sort_attention_forward(self.h, layer, B, _p(x, f32p), _p(out, f32p)))
+        return out
+
+    # -- instrumentation -------------------------------------------------------
+    def kernel_count(self) -> int:
+        n = C.c_int32(0)
+        _check(lib().sort_kernel_count(self.h, C.byref(n)))
+        return n.value
+
+    def enable_stage_timing(self, on: bool = True):
+        _check(lib().sort_enable_stage_timing(self.h, int(on)))
+
+    def stage_times(self):
+        ms = np.zeros(256, np.float32)
+        n = C.c_int32(0)
+        names = C.create_string_buffer(8192)
+        _check(lib().sort_stage_times(self.h, _p(ms, f32p), 256, C.byref(n), names, 8192))
+        keys = names.value.decode().split(";") if n.value else []
+        return dict(zip(keys, ms[: n.value].tolist()))
