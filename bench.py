@@ -1,0 +1,348 @@
+# SPDX-License-Identifier: Apache-2.0
+"""SORT-base forward throughput on B200 (BASELINE.json metric: candidates scored/sec and
+tensor-pipe MFU, SORT forward at 1/2/4/8 B200).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one SORT-base forward (tokenizer -> 4 blocks with pruning after layer 2 ->
+fp32 head) over 256 synthetic requests x (1024 history + 64 targets) per GPU. Multi-GPU
+runs are launched with torchrun, one process per GPU; requests shard across ranks with no
+data-path collective (weak scaling, 256 requests per GPU); a barrier + synchronize bracket
+the timed region and the reported time is the max over ranks.
+
+value   : device-resident throughput (inputs already in HBM), CUDA events on the library's
+          stream, L2 flushed (256 MB write) before every timed step, summed over K steps.
+e2e     : the same forward through the C ABI with pinned HOST inputs and a host score
+          buffer (H2D of the batch + D2H of the scores inside the timed region).
+--impl reference: the reference algorithm's CPU implementation (the fp64 oracle restating
+          rankformer::, since the reference itself does not build here -- DESIGN.md) on all
+          host cores, bounded samples of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from paper_2603_03988_b200 import synth  # noqa: E402
+from paper_2603_03988_b200.config import base_config  # noqa: E402
+from paper_2603_03988_b200.flops import forward_flops  # noqa: E402
+
+METRIC = "candidates scored/sec (SORT-base forward)"
+UNIT = "candidates/s"
+REQ_PER_GPU = 256
+
+
+def workload_desc(cfg):
+    return (f"SORT-base: {cfg.layers} layers, d={cfg.model_dim}, {cfg.heads} heads, m={cfg.ffn_dim}, "
+            f"{REQ_PER_GPU} requests/GPU x ({cfg.n_hist} history + {cfg.n_cand} targets), "
+            f"L={cfg.seq_len}, W={cfg.local_window}, F={cfg.full_suffix}, keep={cfg.keep_schedule()}")
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi style clock / throttle sampling during the timed region (NVML)."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    def _run(self):
+        while not self.stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self.stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def cpu_reference_rate(cfg, params, batch, n_req, threads):
+    """Times the CPU reference algorithm (oracle port of rankformer::, fp64, dense masked
+    attention as attention.cpp:118-121) on `n_req` requests over `threads` host threads."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    om = O.OracleModel(cfg, params)
+    t0 = time.perf_counter()
+    om.forward_batch(batch, threads=threads, limit=n_req)
+    dt = time.perf_counter() - t0
+    return n_req * cfg.n_cand / dt, dt
+
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    params = synth.make_params(cfg, seed=5)
+    n_req = max(threads, 8)
+    batch = synth.make_batch(cfg, n_req, seed=1000)
+    for _ in range(args.warmup and 1):  # one untimed warm-up sample (page-in, allocator)
+        cpu_reference_rate(cfg, params, batch, threads, threads)
+    total_c, total_t = 0.0, 0.0
+    for _ in range(args.steps):
+        rate, dt = cpu_reference_rate(cfg, params, batch, n_req, threads)
+        total_c += n_req * cfg.n_cand
+        total_t += dt
+    value = total_c / total_t
+    sample = f"{n_req} SORT-base requests per step ({n_req * cfg.n_cand} candidates), fp64 oracle port"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_t / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": workload_desc(cfg), "parallelism": "host threads"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--requests", type=int, default=REQ_PER_GPU)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-launches", action="store_true",
+                    help="short run for ncu launch lists (no CPU leg, no e2e)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if not args.profile_launches else args.warmup
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = base_config(batch=args.requests)
+
+    import torch
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local) if args.impl == "ours" else None
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    from paper_2603_03988_b200 import runtime as R
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    params = synth.make_params(cfg, seed=5)  # replicated weights (same seed on every rank)
+    model = R.SortModel(cfg, params, device=local, max_batch=args.requests)
+    stream = torch.cuda.Stream(device=dev)
+    model.set_stream(stream.cuda_stream)
+    B = args.requests
+    batch = synth.make_batch(cfg, B, seed=100 + rank)  # this rank's shard of requests
+    dev_batch = {k: torch.from_numpy(v).to(dev) for k, v in batch.items()}
+    dbatch = R._DevBatch(dev_batch)
+    scores = torch.empty((B, cfg.n_cand, 3), dtype=torch.float32, device=dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    # ---------------------------------------------------------------- device-resident timing
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            model.forward_device(dbatch, scores.data_ptr())
+        model.sync()
+        if args.profile_launches:
+            for _ in range(args.steps):
+                model.forward_device(dbatch, scores.data_ptr())
+            model.sync()
+            return
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+        launches_per_step = 0
+        barrier()
+        with ClockSampler(local) as clk:
+            for i in range(args.steps):
+                flush.fill_(float(i))  # evict L2 between timed steps (untimed)
+                starts[i].record(stream)
+                model.forward_device(dbatch, scores.data_ptr())
+                ends[i].record(stream)
+                launches_per_step = model.kernel_count()
+            model.sync()
+            barrier()
+        dev_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
+
+    # ---------------------------------------------------------------- e2e through the C ABI
+    pinned = {k: torch.from_numpy(v).pin_memory() for k, v in batch.items()}
+    host_scores = torch.empty((B, cfg.n_cand, 3), dtype=torch.float32).pin_memory()
+
+    class _PinnedBatch(R._BatchHold):
+        def __init__(self, t):
+            self.t = t
+            self.c = R.CSortBatch(B, *[t[k].data_ptr() for k in R._BatchHold.KEYS])
+
+    pb = _PinnedBatch(pinned)
+    import ctypes
+    h2d = sum(int(v.nbytes) for v in batch.values())
+    d2h = int(host_scores.numel() * 4)
+    for _ in range(2):
+        R._check(R.lib().sort_forward(model.h, ctypes.byref(pb.c), 0,
+                                      ctypes.c_void_p(host_scores.data_ptr()), 0))
+    barrier()
+    e2e_ms = 0.0
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        R._check(R.lib().sort_forward(model.h, ctypes.byref(pb.c), 0,
+                                      ctypes.c_void_p(host_scores.data_ptr()), 0))
+        e2e_ms += (time.perf_counter() - t0) * 1e3
+    barrier()
+
+    # ---------------------------------------------------------------- per-stage breakdown
+    model.enable_stage_timing(True)
+    with torch.cuda.stream(stream):
+        stage_acc = {}
+        for i in range(3):
+            flush.fill_(float(i))
+            model.forward_device(dbatch, scores.data_ptr())
+            model.sync()
+            for k, v in model.stage_times().items():
+                stage_acc[k] = stage_acc.get(k, 0.0) + v / 3
+    model.enable_stage_timing(False)
+
+    t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_ms, e2e_ms = float(t[0]), float(t[1])
+    if rank != 0:
+        dist.destroy_process_group() if dist else None
+        return
+
+    cand_per_step = world * B * cfg.n_cand
+    value = cand_per_step * args.steps / (dev_ms / 1e3)
+    e2e_value = cand_per_step * args.steps / (e2e_ms / 1e3)
+    fl = forward_flops(cfg)
+    peaks, peak_kind = measured_peaks()
+    step_flops = fl["total"] * B
+    mfu = step_flops / (dev_ms / args.steps / 1e3) / (peaks["bf16_tflops"] * 1e12)
+
+    # dominant kernel (largest stage group) -> roofline entry
+    groups = {}
+    for k, v in stage_acc.items():
+        g = k.split(".")[-1]
+        groups[g] = groups.get(g, 0.0) + v
+    per_group_flops = {
+        "attention": fl["attn"] * B, "qkvg": sum(2 * 2 * (L["l_q"] + L["l_kv"]) * cfg.model_dim ** 2
+                                                  for L in fl["layers"]) * B,
+        "wo": sum(2 * L["l_q"] * cfg.model_dim ** 2 for L in fl["layers"]) * B,
+        "ffn_up": sum(2 * 2 * L["l_q"] * cfg.model_dim * cfg.ffn_dim for L in fl["layers"]) * B,
+        "ffn_down": sum(2 * L["l_q"] * cfg.model_dim * cfg.ffn_dim for L in fl["layers"]) * B,
+        "head": fl["head"] * B, "tokenizer": fl["tokenizer"] * B,
+    }
+    dom = max(groups, key=groups.get) if groups else "attention"
+    n_launch = 4 if dom in ("attention", "qkvg", "wo", "ffn_up", "ffn_down") else 1
+    dom_ms = groups.get(dom, 0.0)
+    achieved = per_group_flops.get(dom, 0.0) / (dom_ms / 1e3) / 1e12 if dom_ms else None
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(dom)
+        except Exception:
+            traffic = None
+    roofline = {
+        "kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"],
+        "unit": "TFLOP/s", "frac": (achieved / peaks["bf16_tflops"]) if achieved else None,
+        "traffic": traffic, "peak_kind": f"{peak_kind} (MEASURED_PEAKS.json bf16_tflops)",
+        "launches_per_step": n_launch, "ms_per_step": dom_ms,
+        "algorithmic_flops_per_step": per_group_flops.get(dom),
+        "stage_ms": {k: round(v, 4) for k, v in groups.items()},
+    }
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        n_req = max(threads, 8)
+        cb = synth.make_batch(cfg, n_req, seed=1000)
+        rate, dt = cpu_reference_rate(cfg, params, cb, n_req, threads)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{n_req} SORT-base requests ({n_req * cfg.n_cand} candidates) in "
+                         f"{dt:.1f} s, fp64 oracle port of the reference, one request per thread"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": workload_desc(cfg), "global_batch": world * B,
+                   "requests_per_gpu": B, "seq_len": cfg.seq_len,
+                   "parallelism": f"dp{world} (request-sharded replicas, no forward collective)",
+                   "l2": "flushed (256 MB write) before every timed step",
+                   "weights": "random init (synth.make_params, fan-in), bf16-rounded"},
+        "mfu": mfu, "mfu_peak": f"{peaks['bf16_tflops']} TFLOP/s bf16 ({peak_kind})",
+        "algorithmic_tflop_per_step": step_flops * world / 1e12,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps},
+        "gpu_launches": launches_per_step * args.steps,
+        "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

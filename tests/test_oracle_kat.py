@@ -448,3 +448,18 @@ def test_flops_ratio_band():
     assert abs(ratio - k["derived"]) < 0.005
     # SORT-base "prune after layer 2": 5.456 GFLOP block stack per request
     assert abs(forward_flops(cfg)["block"] / 1e9 - 5.456) < 0.01
+
+
+def test_oracle_reproduces_golden_fixture():
+    """The committed fixture (tests/golden/make_golden.py) is reproduced bit-for-bit."""
+    from golden.make_golden import params_digest, PARAM_SEED
+    fx = np.load(os.path.join(os.path.dirname(__file__), "golden", "tiny_fixture.npz"))
+    cfg = tiny_config()
+    P = synth.make_params(cfg, seed=PARAM_SEED)
+    assert str(fx["params_sha256"]) == params_digest(P)
+    m = O.OracleModel(cfg, P)
+    batch = {k[3:]: fx[k] for k in fx.files if k.startswith("in_")}
+    for i in range(batch["req_ts"].shape[0]):
+        p, lg = m.forward(batch, i)
+        assert np.array_equal(lg, fx["logits"][i])
+        assert np.array_equal(m.tokenize(batch, i)["hist_time"], fx["hist_time"][i])
