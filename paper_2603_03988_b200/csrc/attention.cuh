@@ -56,7 +56,7 @@ struct AttnArgs {
 };
 
 template <int DK>
-__global__ void __launch_bounds__(kAttnThreads, 1)
+__global__ void __launch_bounds__(kAttnThreads, 2)
     k_attention(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
   using S = AttnSmem<DK>;
@@ -156,12 +156,17 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ softmax warps
+    // Two passes over the S row held in TMEM (max, then exp2 + P store) keep only one
+    // 32-column chunk in registers, so two CTAs fit per SM. Each 32-column chunk is
+    // classified warp-uniformly: fully visible for all 32 rows of the warp (no mask
+    // arithmetic), fully masked (skipped: P = 0, no exp), or mixed (per-element mask).
     const int quarter = warp & 3;
     const int r = quarter * 32 + lane;  // row within the q-tile == TMEM lane
     const int4 meta = a.rowmeta[q0 + r];
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     const float NEG_INF = -__int_as_float(0x7f800000);
-    float m = NEG_INF, l = 0.f, alpha_prev = 0.f;
+    const float sl2 = a.scale_log2;
+    float m = NEG_INF, l = 0.f, alpha_prev = 0.f;  // m: running max of raw logits
     float acc[DK];
 #pragma unroll
     for (int i = 0; i < DK; ++i) acc[i] = 0.f;
@@ -169,58 +174,88 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
       const int code = a.tile_code[t_begin + j];
       const int c0 = (code & 0xffff) * 128;
       const bool partial = (code >> 16) != 0;
+      // per-chunk visibility class for this warp: bit cb of full_mask / none_mask
+      uint32_t full_mask = 0xF, none_mask = 0;
+      if (partial) {
+#pragma unroll
+        for (int cb = 0; cb < 4; ++cb) {
+          const int cs = c0 + cb * 32, ce = cs + 31;
+          const bool f = meta.x <= cs && meta.y >= ce;
+          const bool n = (meta.y < cs || meta.x > ce) && !(meta.z >= cs && meta.z <= ce);
+          if (!__all_sync(0xffffffffu, f)) full_mask &= ~(1u << cb);
+          if (__all_sync(0xffffffffu, n)) none_mask |= 1u << cb;
+        }
+      }
       mbar_wait(s_full, j & 1);
       tc_fence_after();
-      float s[128];
+      // pass 1: masked row max of the raw logits
+      float mx = NEG_INF;
 #pragma unroll
       for (int cb = 0; cb < 4; ++cb) {
+        if (none_mask & (1u << cb)) continue;
         uint32_t rr[32];
         tmem_ld_32x32b_x32(tS + lane_off + cb * 32, rr);
         tmem_ld_wait();
+        if (full_mask & (1u << cb)) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) s[cb * 32 + i] = __uint_as_float(rr[i]);
-      }
-      tc_fence_before();
-      mbar_arrive(s_free);
-      float mx = NEG_INF;
-      if (partial) {
+          for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(rr[i]));
+        } else {
+          const int cs = c0 + cb * 32;
 #pragma unroll
-        for (int c = 0; c < 128; ++c) {
-          const int kv = c0 + c;
-          const bool vis = (kv >= meta.x && kv <= meta.y) || kv == meta.z;
-          s[c] = vis ? s[c] * a.scale_log2 : NEG_INF;
-          mx = fmaxf(mx, s[c]);
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < 128; ++c) {
-          s[c] *= a.scale_log2;
-          mx = fmaxf(mx, s[c]);
+          for (int i = 0; i < 32; ++i) {
+            const int kv = cs + i;
+            const bool vis = (kv >= meta.x && kv <= meta.y) || kv == meta.z;
+            mx = fmaxf(mx, vis ? __uint_as_float(rr[i]) : NEG_INF);
+          }
         }
       }
       const float m_new = fmaxf(m, mx);
-      const float m_use = m_new == NEG_INF ? 0.f : m_new;
-      const float alpha = ex2_approx(m - m_use);
-      float rs = 0.f;
+      // exp2 reference point in the scaled domain; 0 while the row has seen nothing yet
+      const float ms = m_new == NEG_INF ? 0.f : m_new * sl2;
+      const float alpha = ex2_approx(m * sl2 - ms);  // m = -inf -> 0
+      // pass 2: p = 2^(s*scale*log2e - ms), bf16 P into the SW128 A-operand layout
+      float2 rs2 = make_float2(0.f, 0.f);
+      const float2 sl2v = make_float2(sl2, sl2), nms = make_float2(-ms, -ms);
       uint8_t* prow = smem + S::oP + (j & 1) * S::kPBytes + r * 128;
 #pragma unroll
-      for (int ch = 0; ch < 16; ++ch) {
-        uint32_t w[4];
+      for (int cb = 0; cb < 4; ++cb) {
+        uint32_t w[16];
+        if (none_mask & (1u << cb)) {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float p0 = ex2_approx(s[ch * 8 + 2 * e] - m_use);
-          const float p1 = ex2_approx(s[ch * 8 + 2 * e + 1] - m_use);
-          rs += p0 + p1;
-          w[e] = pack_bf16x2(p0, p1);
+          for (int i = 0; i < 16; ++i) w[i] = 0u;
+        } else {
+          uint32_t rr[32];
+          tmem_ld_32x32b_x32(tS + lane_off + cb * 32, rr);
+          tmem_ld_wait();
+          const bool fullc = (full_mask & (1u << cb)) != 0;
+          const int cs = c0 + cb * 32;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float2 x = ffma2(make_float2(__uint_as_float(rr[2 * i]), __uint_as_float(rr[2 * i + 1])),
+                             sl2v, nms);
+            if (!fullc) {
+              const int kv = cs + 2 * i;
+              if (!((kv >= meta.x && kv <= meta.y) || kv == meta.z)) x.x = NEG_INF;
+              if (!((kv + 1 >= meta.x && kv + 1 <= meta.y) || kv + 1 == meta.z)) x.y = NEG_INF;
+            }
+            const float p0 = ex2_approx(x.x), p1 = ex2_approx(x.y);
+            rs2 = fadd2(rs2, make_float2(p0, p1));
+            w[i] = pack_bf16x2(p0, p1);
+          }
         }
-        const int atom = ch >> 3, cc = ch & 7;
-        *reinterpret_cast<int4*>(prow + atom * 16384 + ((cc ^ (r & 7)) << 4)) =
-            make_int4(w[0], w[1], w[2], w[3]);
+#pragma unroll
+        for (int h4 = 0; h4 < 4; ++h4) {
+          const int ch = cb * 4 + h4;  // 16-byte chunk index 0..15 along the 128 kv columns
+          const int atom = ch >> 3, cc = ch & 7;
+          *reinterpret_cast<int4*>(prow + atom * 16384 + ((cc ^ (r & 7)) << 4)) =
+              make_int4(w[4 * h4], w[4 * h4 + 1], w[4 * h4 + 2], w[4 * h4 + 3]);
+        }
       }
-      l = l * alpha + rs;
+      tc_fence_before();
+      mbar_arrive(s_free);  // S fully consumed: the next QK^T may overwrite it
+      l = l * alpha + (rs2.x + rs2.y);
       m = m_new;
       fence_proxy_async_smem();
-      tc_fence_before();
       mbar_arrive(&p_full[j & 1]);
       if (j > 0) {  // deferred: acc <- acc * alpha_{j-1} + O_{j-1}
         const int pb = (j - 1) & 1;
@@ -228,8 +263,14 @@ __global__ void __launch_bounds__(kAttnThreads, 1)
         tc_fence_after();
         float o[DK];
         tmem_row_chunk<DK>(tO0 + pb * DK + lane_off, o);
+        const float2 av = make_float2(alpha_prev, alpha_prev);
 #pragma unroll
-        for (int i = 0; i < DK; ++i) acc[i] = acc[i] * alpha_prev + o[i];
+        for (int i = 0; i < DK; i += 2) {
+          const float2 rr2 = ffma2(make_float2(acc[i], acc[i + 1]), av, make_float2(o[i], o[i + 1]));
+          acc[i] = rr2.x;
+          acc[i + 1] = rr2.y;
+        }
+        tc_fence_before();
       }
       alpha_prev = alpha;
     }

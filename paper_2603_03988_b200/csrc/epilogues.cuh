@@ -1,6 +1,12 @@
 // SPDX-License-Identifier: Apache-2.0
 // Fused GEMM epilogues of the SORT block (thread <-> accumulator row).
 //
+// Interface used by k_gemm_bf16:
+//   prologue(smem, tid, nthreads)  once per CTA, before the role split (fill scratch smem)
+//   run(smem, wait, tbase, row, n0, c0, c1, valid)
+//       issue this row's global prefetches, call wait() (accumulator ready), then consume
+//       accumulator columns [c0, c1) of the tile (absolute columns n0 + c).
+//
 // Pre-norm folding: RMSNorm(x; g) W = diag(1/rms(x)) x (diag(g) W). The gain is
 // folded into the bf16 weight rows at load time and 1/rms is applied here from
 // the row's fp32 sum of squares, written by whichever kernel produced x.
@@ -10,8 +16,8 @@
 
 namespace sortk {
 
-__device__ __forceinline__ float row_inv_rms(const float* ss, int row, float inv_d) {
-  return rsqrtf(ss[row] * inv_d + 1e-6f);  // norm.hpp:23-24 (eps = kRmsEps, norm.hpp:8)
+__device__ __forceinline__ float row_inv_rms(float ss, float inv_d) {
+  return rsqrtf(ss * inv_d + 1e-6f);  // norm.hpp:23-24 (eps = kRmsEps, norm.hpp:8)
 }
 
 __device__ __forceinline__ void store_bf16_row(__nv_bfloat16* dst, const float* v, int n) {
@@ -21,6 +27,11 @@ __device__ __forceinline__ void store_bf16_row(__nv_bfloat16* dst, const float* 
                        pack_bf16x2(v[i + 4], v[i + 5]), pack_bf16x2(v[i + 6], v[i + 7]));
     *reinterpret_cast<int4*>(dst + i) = w;
   }
+}
+
+__device__ __forceinline__ float fast_sigmoid(float x) {
+  // 1 / (1 + e^-x): saturates cleanly to 0 / 1 (e^-x -> inf gives 0), no branch divergence.
+  return __frcp_rn(1.f + __expf(-x));
 }
 
 // ---------------------------------------------------------------------------
@@ -35,8 +46,8 @@ enum : int { kSecQ = 0, kSecK = 1, kSecV = 2, kSecG = 3 };
 template <int DK>
 struct EpiQKVG {
   static constexpr int kChunk = DK;
-  int d, H, R;  // R: rows per request of the A operand
-  int sec[4];
+  int d, H, R;      // R: rows per request of the A operand
+  int sec_packed;   // section of column block i (of width d) in bits [4i, 4i+4)
   float inv_d;
   const float* ss;
   const float* gain_q;  // [H*DK]
@@ -49,35 +60,51 @@ struct EpiQKVG {
   __nv_bfloat16* g;
   int Rq, Rkv, Rkv_pad;
 
-  template <int C>
-  __device__ __forceinline__ void run(uint32_t tbase, int row, int n0, int BN, bool valid) const {
+  __device__ __forceinline__ void prologue(uint8_t* smem, int tid, int nthreads) const {
+    float* sg = reinterpret_cast<float*>(smem);
+    for (int i = tid; i < H * DK; i += nthreads) {
+      sg[i] = gain_q[i];
+      sg[H * DK + i] = gain_k[i];
+    }
+  }
+
+  template <class Wait>
+  __device__ __forceinline__ void run(uint8_t* smem, Wait&& wait, uint32_t tbase, int row, int n0,
+                                      int c0, int c1, bool valid) const {
+    const float* sg = reinterpret_cast<const float*>(smem);
     const int b = row / R, r = row - b * R;
-    const float inv = valid ? row_inv_rms(ss, row, inv_d) : 0.f;
-    for (int c = 0; c < BN; c += DK) {
+    // Sections are d columns wide and BN divides 4d, so a tile's chunks may span sections;
+    // prefetch what any Q/K chunk of this row needs (1/rms, this position's cos/sin).
+    float inv = 0.f;
+    float2 cs[DK / 2];
+    if (valid) {
+      inv = row_inv_rms(ss[row], inv_d);
+      const float2* rp = rope + static_cast<size_t>(pos[r]) * (DK / 2);
+#pragma unroll
+      for (int j = 0; j < DK / 2; ++j) cs[j] = __ldg(rp + j);
+    }
+    wait();
+    for (int c = c0; c < c1; c += DK) {
       float v[DK];
       tmem_row_chunk<DK>(tbase + c, v);
       if (!valid) continue;
       const int col = n0 + c;
       const int si = col / d;
-      const int s = sec[si];
+      const int s = (sec_packed >> (4 * si)) & 0xF;
       const int head = (col - si * d) / DK;
 #pragma unroll
       for (int i = 0; i < DK; ++i) v[i] *= inv;
       if (s == kSecQ || s == kSecK) {
         float m = 0.f;
 #pragma unroll
-        for (int i = 0; i < DK; ++i) m += v[i] * v[i];
+        for (int i = 0; i < DK; ++i) m = fmaf(v[i], v[i], m);
         const float qi = rsqrtf(m * (1.f / DK) + 1e-6f);
-        const float* gn = (s == kSecQ ? gain_q : gain_k) + head * DK;
-#pragma unroll
-        for (int i = 0; i < DK; ++i) v[i] = v[i] * qi * __ldg(gn + i);
-        const float2* cs = rope + static_cast<size_t>(pos[r]) * (DK / 2);
+        const float* gn = sg + (s == kSecQ ? 0 : H * DK) + head * DK;
 #pragma unroll
         for (int j = 0; j < DK / 2; ++j) {
-          const float2 t = __ldg(cs + j);
-          const float x0 = v[2 * j], x1 = v[2 * j + 1];
-          v[2 * j] = t.x * x0 - t.y * x1;
-          v[2 * j + 1] = t.y * x0 + t.x * x1;
+          const float x0 = v[2 * j] * qi * gn[2 * j], x1 = v[2 * j + 1] * qi * gn[2 * j + 1];
+          v[2 * j] = cs[j].x * x0 - cs[j].y * x1;
+          v[2 * j + 1] = cs[j].y * x0 + cs[j].x * x1;
         }
         __nv_bfloat16* dst =
             s == kSecQ ? q + (static_cast<size_t>(b * H + head) * Rq + r) * DK
@@ -89,7 +116,7 @@ struct EpiQKVG {
         for (int i = 0; i < DK; ++i) dst[static_cast<size_t>(i) * Rkv_pad] = __float2bfloat16_rn(v[i]);
       } else {
 #pragma unroll
-        for (int i = 0; i < DK; ++i) v[i] = sigmoidf_stable(v[i]);
+        for (int i = 0; i < DK; ++i) v[i] = fast_sigmoid(v[i]);
         store_bf16_row(g + static_cast<size_t>(row) * d + head * DK, v, DK);
       }
     }
@@ -100,47 +127,62 @@ struct EpiQKVG {
 // Residual epilogue: out = resid + acc (bf16, may alias resid -- each element is
 // read and written by the same thread) and the new row's sum of squares.
 // Used for x <- P(x, L_out) + Attn(...) Wo (attention.cpp:131) and
-// x <- x + FFN(...).
+// x <- x + FFN(...). The residual half-row (<= 128 columns) is
+// prefetched into registers before the accumulator wait.
 struct EpiResid {
   static constexpr int kChunk = 32;
   const __nv_bfloat16* resid;
   __nv_bfloat16* out;
   float* ss_out;
   int d;
-  int ss_atomic;
+  int ss_atomic;  // several column tiles per row -> partial sums combined atomically
 
-  template <int C>
-  __device__ __forceinline__ void run(uint32_t tbase, int row, int n0, int BN, bool valid) const {
+  __device__ __forceinline__ void prologue(uint8_t*, int, int) const {}
+
+  template <class Wait>
+  __device__ __forceinline__ void run(uint8_t*, Wait&& wait, uint32_t tbase, int row, int n0,
+                                      int c0, int c1, bool valid) const {
+    int4 rv[16];  // up to 128 columns
+    const int nq = (c1 - c0) / 8;
+    if (valid && resid) {
+      const int4* rp = reinterpret_cast<const int4*>(resid + static_cast<size_t>(row) * d + n0 + c0);
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (i < nq) rv[i] = rp[i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) rv[i] = make_int4(0, 0, 0, 0);
+    }
+    wait();
     float ss = 0.f;
-    for (int c = 0; c < BN; c += 32) {
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      const int c = c0 + cc * 32;
+      if (c >= c1) break;
       float v[32];
       tmem_row_chunk<32>(tbase + c, v);
       if (!valid) continue;
-      const size_t off = static_cast<size_t>(row) * d + n0 + c;
-      const int4* rp = reinterpret_cast<const int4*>(resid + off);
       int4 o[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        int4 rv = resid ? rp[q] : make_int4(0, 0, 0, 0);
-        const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&rv);
+      for (int qd = 0; qd < 4; ++qd) {
+        const int4 r4 = rv[cc * 4 + qd];
+        const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&r4);
         uint32_t w[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const float2 f = __bfloat1622float2(r2[e]);
-          w[e] = pack_bf16x2(f.x + v[q * 8 + 2 * e], f.y + v[q * 8 + 2 * e + 1]);
+          w[e] = pack_bf16x2(f.x + v[qd * 8 + 2 * e], f.y + v[qd * 8 + 2 * e + 1]);
           const float2 y = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&w[e]));
-          ss += y.x * y.x + y.y * y.y;
+          ss = fmaf(y.x, y.x, fmaf(y.y, y.y, ss));
         }
-        o[q] = make_int4(w[0], w[1], w[2], w[3]);
+        o[qd] = make_int4(w[0], w[1], w[2], w[3]);
       }
-      int4* op = reinterpret_cast<int4*>(out + off);
+      int4* op = reinterpret_cast<int4*>(out + static_cast<size_t>(row) * d + n0 + c);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) op[q] = o[q];
+      for (int qd = 0; qd < 4; ++qd) op[qd] = o[qd];
     }
-    if (valid) {
-      if (ss_atomic) atomicAdd(ss_out + row, ss);
-      else ss_out[row] = ss;
-    }
+    // two half-row epilogue warps (and possibly several column tiles) contribute
+    if (valid) atomicAdd(ss_out + row, ss);
   }
 };
 
@@ -155,10 +197,14 @@ struct EpiSwiGLU {
   __nv_bfloat16* hidden;
   int m;
 
-  template <int C>
-  __device__ __forceinline__ void run(uint32_t tbase, int row, int n0, int BN, bool valid) const {
-    const float inv = valid ? row_inv_rms(ss, row, inv_d) : 0.f;
-    for (int c = 0; c < BN; c += 64) {
+  __device__ __forceinline__ void prologue(uint8_t*, int, int) const {}
+
+  template <class Wait>
+  __device__ __forceinline__ void run(uint8_t*, Wait&& wait, uint32_t tbase, int row, int n0,
+                                      int c0, int c1, bool valid) const {
+    const float inv = valid ? row_inv_rms(ss[row], inv_d) : 0.f;
+    wait();
+    for (int c = c0; c < c1; c += 64) {
       float v[64];
       tmem_row_chunk<64>(tbase + c, v);
       if (!valid) continue;
@@ -166,7 +212,7 @@ struct EpiSwiGLU {
 #pragma unroll
       for (int i = 0; i < 32; ++i) {
         const float gt = v[i] * inv, up = v[32 + i] * inv;
-        h[i] = gt / (1.f + __expf(-gt)) * up;  // swish(x) = x * sigmoid(x) (common.hpp:37)
+        h[i] = gt * up * fast_sigmoid(gt);  // swish(x) = x * sigmoid(x) (common.hpp:37)
       }
       store_bf16_row(hidden + static_cast<size_t>(row) * m + (n0 + c) / 2, h, 32);
     }

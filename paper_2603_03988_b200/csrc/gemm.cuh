@@ -7,14 +7,18 @@
 // Q/K/V/G projection (attention.cpp:93-95,125), the output projection with the
 // residual add (attention.cpp:131 + SPEC.md:375), and both halves of the
 // SwishGLU FFN. What differs between them is only the
-// epilogue, which is a template functor applied to 128-row x kChunk-column
-// slices of the accumulator after tcgen05.ld.
+// epilogue, a template functor that consumes 128-row x kChunk-column slices of
+// the accumulator after tcgen05.ld.
 //
-// Roles (256 threads, 1 CTA per SM):
-//   warp 0      TMA producer   (A tile 128x64, B tile BNx64 per stage, SW128)
-//   warp 1      MMA issuer     (one thread; 4 x tcgen05.mma K=16 per stage)
-//   warp 2      TMEM allocator (2 accumulator stages x 256 columns)
-//   warps 4..7  epilogue       (thread <-> accumulator row; TMEM lane quarter = warp % 4)
+// Roles (384 threads, 1 CTA per SM):
+//   warp 0       TMA producer   (A tile 128x64, B tile BNx64 per stage, SW128)
+//   warp 1       MMA issuer     (one thread; 4 x tcgen05.mma K=16 per stage)
+//   warp 2       TMEM allocator (2 accumulator stages x 256 columns)
+//   warps 4..11  epilogue       (thread <-> accumulator row; TMEM lane quarter = warp % 4;
+//                                warps 4-7 take the first half of the tile's column chunks,
+//                                warps 8-11 the second half)
+// Tiles are walked m-major with every CTA cycling through all n-tiles, so
+// epilogues with different per-section cost (e.g. Q/K vs V) balance across SMs.
 #pragma once
 
 #include "ptx.cuh"
@@ -25,11 +29,20 @@ constexpr int kGemmBM = 128;
 constexpr int kGemmBK = 64;
 constexpr int kGemmStages = 4;
 constexpr int kGemmMaxBN = 256;
-constexpr int kGemmThreads = 256;
+constexpr int kGemmEpiWarps = 8;
+constexpr int kGemmThreads = 128 + 32 * kGemmEpiWarps;
 constexpr uint32_t kGemmABytes = kGemmBM * kGemmBK * 2;     // 16 KB
 constexpr uint32_t kGemmBBytes = kGemmMaxBN * kGemmBK * 2;  // 32 KB
+constexpr uint32_t kGemmEpiSmem = 8192;                     // per-kernel epilogue scratch
 constexpr size_t kGemmSmemBytes =
-    1024 + kGemmStages * (kGemmABytes + kGemmBBytes) + 8 * (2 * kGemmStages + 4) + 16;
+    1024 + kGemmStages * (kGemmABytes + kGemmBBytes) + kGemmEpiSmem + 8 * (2 * kGemmStages + 4) + 16;
+
+// Tile t of the CTA-strided walk -> (m block, n block). Consecutive tiles of one CTA
+// advance n fastest so each CTA sees every n-tile (section) in turn.
+__device__ __forceinline__ void gemm_tile_coords(int tile, int num_n, int& mb, int& nb) {
+  mb = tile / num_n;
+  nb = tile - mb * num_n;
+}
 
 template <class Epi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
@@ -40,7 +53,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + kGemmStages * kGemmABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + kGemmStages * kGemmBBytes);
+  uint8_t* sEpi = sB + kGemmStages * kGemmBBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + kGemmEpiSmem);
   uint64_t* empty = full + kGemmStages;
   uint64_t* tfull = empty + kGemmStages;
   uint64_t* tempty = tfull + 2;
@@ -62,11 +76,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);
+      mbar_init(&tempty[i], 32 * kGemmEpiWarps);
     }
     mbar_fence_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
+  epi.prologue(sEpi, threadIdx.x, kGemmThreads);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -78,13 +93,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m0 = (tile / num_n) * kGemmBM;
-        const int n0 = (tile % num_n) * BN;
+        int mb, nb;
+        gemm_tile_coords(tile, num_n, mb, nb);
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           mbar_arrive_expect_tx(&full[s], stage_bytes);
-          tma_load_2d(sA + s * kGemmABytes, &tmA, &full[s], kb * kGemmBK, m0);
-          tma_load_2d(sB + s * kGemmBBytes, &tmB, &full[s], kb * kGemmBK, n0);
+          tma_load_2d(sA + s * kGemmABytes, &tmA, &full[s], kb * kGemmBK, mb * kGemmBM);
+          tma_load_2d(sB + s * kGemmBBytes, &tmB, &full[s], kb * kGemmBK, nb * BN);
           if (++s == kGemmStages) {
             s = 0;
             ph ^= 1;
@@ -124,18 +139,25 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else if (warp >= 4) {
-    const int q = warp & 3;
+    const int e = warp - 4;
+    const int q = e & 3;     // == warp % 4: the TMEM lane quarter this warp may access
+    const int half = e >> 2;
+    const int n_chunks = BN / Epi::kChunk;
+    const int split = (n_chunks + 1) >> 1;
+    const int c_begin = half ? split : 0, c_end = half ? n_chunks : split;
     int t = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
       const int acc = t & 1;
       const uint32_t acc_ph = (t >> 1) & 1;
-      const int m0 = (tile / num_n) * kGemmBM;
-      const int n0 = (tile % num_n) * BN;
-      mbar_wait(&tfull[acc], acc_ph);
-      tc_fence_after();
-      const int row = m0 + q * 32 + lane;
+      int mb, nb;
+      gemm_tile_coords(tile, num_n, mb, nb);
+      const int row = mb * kGemmBM + q * 32 + lane;
       const uint32_t tbase = tmem + acc * 256 + (static_cast<uint32_t>(q * 32) << 16);
-      epi.template run<Epi::kChunk>(tbase, row, n0, BN, row < M);
+      auto wait = [&]() {
+        mbar_wait(&tfull[acc], acc_ph);
+        tc_fence_after();
+      };
+      epi.run(sEpi, wait, tbase, row, nb * BN, c_begin * Epi::kChunk, c_end * Epi::kChunk, row < M);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
@@ -177,19 +199,12 @@ __device__ __forceinline__ void tmem_row_chunk(uint32_t taddr, float (&v)[kChunk
   }
 }
 
-// Convenience base: iterate the tile's columns in kChunk slices and call
-// Derived::chunk(row, col, v) for valid rows.
-template <class Derived, int kChunk_>
-struct ChunkedEpilogue {
-  static constexpr int kChunk = kChunk_;
-  template <int C>
-  __device__ __forceinline__ void run(uint32_t tbase, int row, int n0, int BN, bool valid) const {
-    for (int c = 0; c < BN; c += C) {
-      float v[C];
-      tmem_row_chunk<C>(tbase + c, v);
-      if (valid) static_cast<const Derived*>(this)->chunk(row, n0 + c, v);
-    }
-  }
-};
+// Grid size for the persistent GEMM: at most one CTA per SM, and never a multiple of the
+// n-tile count (so the CTA-strided tile walk rotates every CTA through all sections).
+inline int gemm_grid(int tiles, int num_n, int sms) {
+  int g = tiles < sms ? tiles : sms;
+  if (g == sms && num_n > 1 && g % num_n == 0) --g;
+  return g > 0 ? g : 1;
+}
 
 }  // namespace sortk

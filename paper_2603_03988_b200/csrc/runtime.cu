@@ -324,7 +324,7 @@ static void launch_gemm(Handle& h, const CUtensorMap& A, const CUtensorMap& B, i
   }
   if (N % BN) throw RuntimeFailure("gemm: N not divisible by BN");
   const int tiles = ((M + kGemmBM - 1) / kGemmBM) * (N / BN);
-  const int grid = std::min(tiles, h.num_sms);
+  const int grid = gemm_grid(tiles, N / BN, h.num_sms);
   k_gemm_bf16<Epi><<<grid, kGemmThreads, kGemmSmemBytes, h.stream>>>(A, B, M, N, K, BN, epi);
   check_launch("gemm");
   ++h.launches;
@@ -373,7 +373,7 @@ static void launch_qkvg_dk(Handle& h, const LayerDev& L, const CUtensorMap& A, c
   e.d = h.d;
   e.H = h.H;
   e.R = R;
-  for (int i = 0; i < 4; ++i) e.sec[i] = sec[i];
+  e.sec_packed = sec[0] | (sec[1] << 4) | (sec[2] << 8) | (sec[3] << 12);
   e.inv_d = 1.f / static_cast<float>(h.d);
   e.ss = ss;
   e.gain_q = L.gain_q;
@@ -496,6 +496,7 @@ static void run_layer(Handle& h, int l, int B, bool attn_only = false) {
   stage_mark(h, "L" + std::to_string(l) + ".qkvg");
   launch_attention(h, L, lp, B);
   stage_mark(h, "L" + std::to_string(l) + ".attention");
+  CK(cudaMemsetAsync(SSq, 0, static_cast<size_t>(B) * L.Rq * sizeof(float), h.stream));
   EpiResid eo;
   eo.resid = attn_only ? nullptr : Xq;
   eo.out = attn_only ? h.Qb : Xq;  // Q buffer is dead after attention
@@ -512,6 +513,7 @@ static void run_layer(Handle& h, int l, int B, bool attn_only = false) {
   eu.m = h.m;
   launch_gemm(h, L.tmA_q, L.tmB_up, B * L.Rq, 2 * h.m, d, L.bn_up, eu);
   stage_mark(h, "L" + std::to_string(l) + ".ffn_up");
+  CK(cudaMemsetAsync(SSq, 0, static_cast<size_t>(B) * L.Rq * sizeof(float), h.stream));
   EpiResid ed;
   ed.resid = Xq;
   ed.out = Xq;

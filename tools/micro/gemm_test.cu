@@ -10,11 +10,19 @@
 
 using namespace sortk;
 
-struct StoreF32 : ChunkedEpilogue<StoreF32, 32> {
+struct StoreF32 {
+  static constexpr int kChunk = 32;
   float* C;
   int ldc;
-  __device__ void chunk(int row, int col, const float (&v)[32]) const {
-    for (int i = 0; i < 32; ++i) C[(size_t)row * ldc + col + i] = v[i];
+  __device__ void prologue(uint8_t*, int, int) const {}
+  template <class Wait>
+  __device__ void run(uint8_t*, Wait&& wait, uint32_t tbase, int row, int n0, int c0, int c1, bool valid) const {
+    wait();
+    for (int c = c0; c < c1; c += 32) {
+      float v[32];
+      tmem_row_chunk<32>(tbase + c, v);
+      if (valid) for (int i = 0; i < 32; ++i) C[(size_t)row * ldc + n0 + c + i] = v[i];
+    }
   }
 };
 
@@ -37,7 +45,7 @@ static int run(int M, int N, int K, int BN) {
   auto kfn = k_gemm_bf16<StoreF32>;
   cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmemBytes);
   int tiles = ((M + 127) / 128) * (N / BN);
-  int grid = tiles < 148 ? tiles : 148;
+  int grid = gemm_grid(tiles, N / BN, 148);
   kfn<<<grid, kGemmThreads, kGemmSmemBytes>>>(tA, tB, M, N, K, BN, epi);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { printf("CUDA error %s\n", cudaGetErrorString(e)); return 1; }
