@@ -1,25 +1,32 @@
 // SPDX-License-Identifier: Apache-2.0
 // K3: structured local-window attention with query pruning, on tcgen05.
 //
-// One CTA computes one (request b, head h, 128-row q-tile) output block of
+// One work item = one (request b, head h, 128-row q-tile) output block of
 //   O = softmax(Q K^T / sqrt(dk) + M) V        (attention.cpp:118-121)
-// followed by the sigmoid gate G (attention.cpp:124-127), visiting ONLY the
-// 128-column kv tiles that hold a visible entry (the block-skip rule of
-// blockwise_masked_attention, block_attention.hpp:86-99, decided analytically by
-// the host plan). Inside partial tiles the mask is evaluated per element from the
-// compact row form visible(r, c) = lo_r <= c <= hi_r || c == self_r
-// (build_mask, mask.cpp:47-74). Masked logits are -inf before the row max, so no
-// 0 * NaN can arise and candidate rows never see another candidate (exact isolation).
+// followed by the sigmoid gate G (attention.cpp:124-127). Only the 128-column kv
+// tiles holding a visible entry are visited (the block-skip rule of
+// blockwise_masked_attention, block_attention.hpp:86-99, decided analytically by the
+// host plan). Inside partial tiles the mask is evaluated from the compact row form
+// visible(r, c) = lo_r <= c <= hi_r || c == self_r (build_mask, mask.cpp:47-74); masked
+// entries never enter the exponent, so candidate rows never see another candidate
+// (exact isolation) and no 0 * NaN can arise.
 //
-// Roles (192 threads):
-//   warp 0      TMA: Q tile once; K tile (128 x dk) and V^T tile (dk x 128) per kv tile,
-//               double-buffered
-//   warp 1      MMA: S = Q K^T (M=128, N=128, K=dk) into TMEM; O_j = P_j V_j (M=128,
-//               N=dk, K=128) into one of two TMEM O buffers
-//   warps 2..5  softmax: thread <-> query row; tcgen05.ld of S, online softmax with
-//               exp2 (streaming-softmax recurrence of block_attention.hpp:104-122),
-//               P written bf16 into the SW128 A-operand layout in smem; the rescaled
-//               accumulation of O_{j-1} is deferred one tile so PV overlaps softmax.
+// Softmax reference point. With QKNorm (attention.cpp:111-114) every q/k row has norm
+// <= sqrt(dk) * max|gain| (RMSNorm output, then a RoPE rotation), so every logit obeys
+// |s| <= B = sqrt(dk) * max|g_q| * max|g_k| ("bounded logits"). When
+// B < kFixedRefMax the kernel uses the FIXED reference exp(s - B) instead of the running
+// row max: softmax is shift-invariant, no rescaling of O is ever needed, PV accumulates
+// straight into one TMEM accumulator across kv tiles, and 2^(-2B log2 e) stays a
+// normal fp32/bf16 number. Otherwise (unbounded logits, e.g. the op-level
+// sort_block_attention entry) the online-max path with a deferred O rescale is used
+// (streaming-softmax recurrence of block_attention.hpp:104-122).
+//
+// Roles (192 threads, persistent, 2 CTAs per SM):
+//   warp 0      TMA: Q tile per item (double-buffered), K tile (128 x dk) and V^T tile
+//               (dk x 128) per kv tile (double-buffered); runs ahead across items
+//   warp 1      MMA: S = Q K^T (M=128, N=128, K=dk) into TMEM; P V (M=128, N=dk, K=128)
+//   warps 2..5  softmax: thread <-> query row; tcgen05.ld of S, exp2 on MUFU, P written
+//               bf16 into the SW128 A-operand layout in smem; gate + store at item end
 #pragma once
 
 #include "gemm.cuh"
@@ -27,6 +34,7 @@
 namespace sortk {
 
 constexpr int kAttnThreads = 192;
+constexpr float kFixedRefMax = 40.f;  // 2^(-2*40*log2 e) ~ 2e-35 > FLT_MIN
 
 template <int DK>
 struct AttnSmem {
@@ -34,14 +42,16 @@ struct AttnSmem {
   static constexpr uint32_t kKBytes = 128 * DK * 2;
   static constexpr uint32_t kVBytes = DK * 128 * 2;  // two [DK x 64] SW128 boxes
   static constexpr uint32_t kPBytes = 128 * 128 * 2;
-  static constexpr uint32_t oQ = 0;
-  static constexpr uint32_t oK = oQ + ((kQBytes + 1023) / 1024) * 1024;
-  static constexpr uint32_t oV = oK + 2 * ((kKBytes + 1023) / 1024) * 1024;
-  static constexpr uint32_t oP = oV + 2 * ((kVBytes + 1023) / 1024) * 1024;
-  static constexpr uint32_t oBar = oP + 2 * kPBytes;
+  static constexpr uint32_t kQStride = ((kQBytes + 1023) / 1024) * 1024;
   static constexpr uint32_t kKStride = ((kKBytes + 1023) / 1024) * 1024;
   static constexpr uint32_t kVStride = ((kVBytes + 1023) / 1024) * 1024;
-  static constexpr uint32_t kTotal = oBar + 16 * 8 + 16 + 1024;
+  static constexpr uint32_t oQ = 0;
+  static constexpr uint32_t oK = oQ + 2 * kQStride;
+  static constexpr uint32_t oV = oK + 2 * kKStride;
+  static constexpr uint32_t oP = oV + 2 * kVStride;
+  static constexpr uint32_t oBar = oP + kPBytes;
+  static constexpr uint32_t oTiles = oBar + 32 * 8;  // int32 tile tables follow
+  static constexpr uint32_t bytes(int n_tile_ints) { return oTiles + 4u * n_tile_ints + 1024; }
 };
 
 struct AttnArgs {
@@ -51,11 +61,12 @@ struct AttnArgs {
   const int32_t* qtile_order; // heavy first
   const __nv_bfloat16* g;     // [B*Rq, d] sigmoid gate
   __nv_bfloat16* out;         // [B*Rq, d]
-  int BH, H, Rq, d;
-  float scale_log2;
+  int BH, H, Rq, d, n_qtiles, n_codes;
+  float scale_log2;           // log2(e) / sqrt(dk)
+  float ref_log2;             // fixed-reference mode: B * scale_log2
 };
 
-template <int DK>
+template <int DK, bool kFixed>
 __global__ void __launch_bounds__(kAttnThreads, 2)
     k_attention(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
@@ -64,35 +75,43 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::oBar);
-  uint64_t* q_full = bars + 0;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
-  uint64_t* s_full = bars + 5;
-  uint64_t* s_free = bars + 6;
-  uint64_t* p_full = bars + 7;    // [2]
-  uint64_t* o_full = bars + 9;    // [2]
+  uint64_t* q_full = bars + 0;    // [2]
+  uint64_t* q_empty = bars + 2;   // [2]
+  uint64_t* kv_full = bars + 4;   // [2]
+  uint64_t* kv_empty = bars + 6;  // [2]
+  uint64_t* s_full = bars + 8;
+  uint64_t* s_free = bars + 9;
+  uint64_t* p_full = bars + 10;
+  uint64_t* p_empty = bars + 11;
+  uint64_t* o_full = bars + 12;   // [2]
+  uint64_t* o_empty = bars + 14;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 16);
+  int32_t* s_off = reinterpret_cast<int32_t*>(smem + S::oTiles);
+  int32_t* s_order = s_off + (a.n_qtiles + 1);
+  int32_t* s_code = s_order + a.n_qtiles;
 
   const int warp = warp_id(), lane = lane_id();
-  const int rank = blockIdx.x / a.BH;
-  const int bh = blockIdx.x - rank * a.BH;
-  const int qt = a.qtile_order[rank];
-  const int q0 = qt * 128;
-  const int t_begin = a.tile_off[qt], n_t = a.tile_off[qt + 1] - t_begin;
+  const int n_items = a.n_qtiles * a.BH;
 
+  for (int i = threadIdx.x; i <= a.n_qtiles; i += kAttnThreads) s_off[i] = a.tile_off[i];
+  for (int i = threadIdx.x; i < a.n_qtiles; i += kAttnThreads) s_order[i] = a.qtile_order[i];
+  for (int i = threadIdx.x; i < a.n_codes; i += kAttnThreads) s_code[i] = a.tile_code[i];
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
     tma_prefetch_desc(&tmV);
-    mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
-      mbar_init(&p_full[i], 128);
       mbar_init(&o_full[i], 1);
     }
     mbar_init(s_full, 1);
     mbar_init(s_free, 128);
+    mbar_init(p_full, 128);
+    mbar_init(p_empty, 1);
+    mbar_init(o_empty, 128);
     mbar_fence_init();
   }
   if (warp == 1) tmem_alloc(tslot, 256);
@@ -100,23 +119,34 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  const uint32_t tS = tmem;                 // 128 columns
-  const uint32_t tO0 = tmem + 128;          // 2 x DK columns
+  const uint32_t tS = tmem;          // 128 columns of S
+  const uint32_t tO0 = tmem + 128;   // O accumulator(s): 1 (fixed) or 2 (online) x DK columns
 
+  // Work item i -> (q-tile of rank i / BH, heaviest first; request*head bh = i % BH).
+  // Every role walks the same item/tile sequence; `g` counts kv tiles across items so
+  // barrier phases and the K/V double buffer run on seamlessly between items.
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, S::kQBytes);
-      tma_load_3d(smem + S::oQ, &tmQ, q_full, 0, q0, bh);
-      for (int j = 0; j < n_t; ++j) {
-        const int st = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
-        const int kv0 = (a.tile_code[t_begin + j] & 0xffff) * 128;
-        mbar_wait(&kv_empty[st], ph ^ 1);
-        mbar_arrive_expect_tx(&kv_full[st], S::kKBytes + S::kVBytes);
-        tma_load_3d(smem + S::oK + st * S::kKStride, &tmK, &kv_full[st], 0, kv0, bh);
-        uint8_t* vdst = smem + S::oV + st * S::kVStride;
-        tma_load_3d(vdst, &tmV, &kv_full[st], kv0, 0, bh);
-        tma_load_3d(vdst + DK * 128, &tmV, &kv_full[st], kv0 + 64, 0, bh);
+      int g = 0, li = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++li) {
+        const int rank = it / a.BH, bh = it - rank * a.BH;
+        const int qt = s_order[rank];
+        const int t_begin = s_off[qt], n_t = s_off[qt + 1] - t_begin;
+        const int qb = li & 1;
+        mbar_wait_sleep(&q_empty[qb], ((li >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&q_full[qb], S::kQBytes);
+        tma_load_3d(smem + S::oQ + qb * S::kQStride, &tmQ, &q_full[qb], 0, qt * 128, bh);
+        for (int j = 0; j < n_t; ++j, ++g) {
+          const int st = g & 1;
+          const uint32_t ph = (g >> 1) & 1;
+          const int kv0 = (s_code[t_begin + j] & 0xffff) * 128;
+          mbar_wait_sleep(&kv_empty[st], ph ^ 1);
+          mbar_arrive_expect_tx(&kv_full[st], S::kKBytes + S::kVBytes);
+          tma_load_3d(smem + S::oK + st * S::kKStride, &tmK, &kv_full[st], 0, kv0, bh);
+          uint8_t* vdst = smem + S::oV + st * S::kVStride;
+          tma_load_3d(vdst, &tmV, &kv_full[st], kv0, 0, bh);
+          tma_load_3d(vdst + DK * 128, &tmV, &kv_full[st], kv0 + 64, 0, bh);
+        }
       }
     }
   } else if (warp == 1) {
@@ -124,180 +154,231 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
       const uint32_t id_s = umma_idesc_bf16(128, 128);
       const uint32_t id_o = umma_idesc_bf16(128, DK);
       constexpr uint32_t qsw = DK * 2;  // Q/K rows are DK*2 bytes = the swizzle span
-      mbar_wait(q_full, 0);
-      const uint32_t sq = smem_u32(smem + S::oQ);
-      for (int j = 0; j < n_t; ++j) {
-        const int st = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
-        mbar_wait(&kv_full[st], ph);
-        mbar_wait(s_free, (j & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t sk = smem_u32(smem + S::oK + st * S::kKStride);
+      const uint32_t sp = smem_u32(smem + S::oP);
+      int g = 0, li = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++li) {
+        const int rank = it / a.BH;
+        const int qt = s_order[rank];
+        const int n_t = s_off[qt + 1] - s_off[qt];
+        const int qb = li & 1;
+        mbar_wait_sleep(&q_full[qb], (li >> 1) & 1);
+        const uint32_t sq = smem_u32(smem + S::oQ + qb * S::kQStride);
+        for (int j = 0; j < n_t; ++j, ++g) {
+          const int st = g & 1;
+          mbar_wait_sleep(&kv_full[st], (g >> 1) & 1);
+          mbar_wait_sleep(s_free, (g & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t sk = smem_u32(smem + S::oK + st * S::kKStride);
 #pragma unroll
-        for (int k = 0; k < DK / 16; ++k)
-          mma_bf16_ss(tS, umma_sdesc_kmajor(sq + k * 32, qsw), umma_sdesc_kmajor(sk + k * 32, qsw),
-                      id_s, k > 0 ? 1u : 0u);
-        mma_commit(s_full);
-        const int pb = j & 1;
-        mbar_wait(&p_full[pb], (j >> 1) & 1);
-        tc_fence_after();
-        const uint32_t sp = smem_u32(smem + S::oP + pb * S::kPBytes);
-        const uint32_t sv = smem_u32(smem + S::oV + st * S::kVStride);
+          for (int k = 0; k < DK / 16; ++k)
+            mma_bf16_ss(tS, umma_sdesc_kmajor(sq + k * 32, qsw), umma_sdesc_kmajor(sk + k * 32, qsw),
+                        id_s, k > 0 ? 1u : 0u);
+          mma_commit(s_full);
+          if (j == n_t - 1) mma_commit(&q_empty[qb]);
+          mbar_wait_sleep(p_full, g & 1);
+          tc_fence_after();
+          uint32_t tO;
+          if constexpr (kFixed) {
+            if (j == 0) {  // the previous item's O has been read out
+              mbar_wait_sleep(o_empty, (li & 1) ^ 1);
+              tc_fence_after();
+            }
+            tO = tO0;
+          } else {
+            tO = tO0 + (g & 1) * DK;
+          }
+          const uint32_t sv = smem_u32(smem + S::oV + st * S::kVStride);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t pa = sp + (kk >> 2) * 16384 + (kk & 3) * 32;
-          const uint32_t va = sv + (kk >> 2) * (DK * 128) + (kk & 3) * 32;
-          mma_bf16_ss(tO0 + pb * DK, umma_sdesc_kmajor(pa, 128), umma_sdesc_kmajor(va, 128), id_o,
-                      kk > 0 ? 1u : 0u);
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t pa = sp + (kk >> 2) * 16384 + (kk & 3) * 32;
+            const uint32_t va = sv + (kk >> 2) * (DK * 128) + (kk & 3) * 32;
+            const uint32_t accum = kFixed ? ((j | kk) != 0) : (kk != 0);
+            mma_bf16_ss(tO, umma_sdesc_kmajor(pa, 128), umma_sdesc_kmajor(va, 128), id_o, accum);
+          }
+          mma_commit(p_empty);
+          mma_commit(&kv_empty[st]);
+          if constexpr (kFixed) {
+            if (j == n_t - 1) mma_commit(&o_full[0]);
+          } else {
+            mma_commit(&o_full[g & 1]);
+          }
         }
-        mma_commit(&o_full[pb]);
-        mma_commit(&kv_empty[st]);
       }
     }
   } else {
     // ------------------------------------------------------------ softmax warps
-    // Two passes over the S row held in TMEM (max, then exp2 + P store) keep only one
-    // 32-column chunk in registers, so two CTAs fit per SM. Each 32-column chunk is
-    // classified warp-uniformly: fully visible for all 32 rows of the warp (no mask
-    // arithmetic), fully masked (skipped: P = 0, no exp), or mixed (per-element mask).
+    // Each 32-column chunk of a partial tile is classified warp-uniformly: fully visible
+    // for all 32 rows of the warp (no mask arithmetic), fully masked (skipped: P = 0, no
+    // exp, no TMEM read), or mixed (per-element mask).
     const int quarter = warp & 3;
     const int r = quarter * 32 + lane;  // row within the q-tile == TMEM lane
-    const int4 meta = a.rowmeta[q0 + r];
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     const float NEG_INF = -__int_as_float(0x7f800000);
     const float sl2 = a.scale_log2;
-    float m = NEG_INF, l = 0.f, alpha_prev = 0.f;  // m: running max of raw logits
-    float acc[DK];
+    const float2 sl2v = make_float2(sl2, sl2);
+    uint8_t* prow = smem + S::oP + r * 128;
+    int g = 0, li = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++li) {
+      const int rank = it / a.BH, bh = it - rank * a.BH;
+      const int qt = s_order[rank];
+      const int q0 = qt * 128;
+      const int t_begin = s_off[qt], n_t = s_off[qt + 1] - t_begin;
+      const int4 meta = a.rowmeta[q0 + r];
+      const int qrow = q0 + r;
+      const int b = bh / a.H, hh = bh - b * a.H;
+      const size_t off = static_cast<size_t>(b * a.Rq + qrow) * a.d + hh * DK;
+      int4 gate[DK / 8];  // prefetch the gate row early
+      if (qrow < a.Rq) {
 #pragma unroll
-    for (int i = 0; i < DK; ++i) acc[i] = 0.f;
-    for (int j = 0; j < n_t; ++j) {
-      const int code = a.tile_code[t_begin + j];
-      const int c0 = (code & 0xffff) * 128;
-      const bool partial = (code >> 16) != 0;
-      // per-chunk visibility class for this warp: bit cb of full_mask / none_mask
-      uint32_t full_mask = 0xF, none_mask = 0;
-      if (partial) {
+        for (int i = 0; i < DK / 8; ++i) gate[i] = reinterpret_cast<const int4*>(a.g + off)[i];
+      }
+      float m = NEG_INF, alpha_prev = 0.f;  // online mode only
+      float2 lsum[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                        make_float2(0.f, 0.f)};
+      float acc[kFixed ? 1 : DK];
+#pragma unroll
+      for (int i = 0; i < (kFixed ? 1 : DK); ++i) acc[i] = 0.f;
+      for (int j = 0; j < n_t; ++j, ++g) {
+        const int code = s_code[t_begin + j];
+        const int c0 = (code & 0xffff) * 128;
+        uint32_t full_mask = 0xF, none_mask = 0;
+        if ((code >> 16) != 0) {
+#pragma unroll
+          for (int cb = 0; cb < 4; ++cb) {
+            const int cs = c0 + cb * 32, ce = cs + 31;
+            const bool f = meta.x <= cs && meta.y >= ce;
+            const bool n = (meta.y < cs || meta.x > ce) && !(meta.z >= cs && meta.z <= ce);
+            if (!__all_sync(0xffffffffu, f)) full_mask &= ~(1u << cb);
+            if (__all_sync(0xffffffffu, n)) none_mask |= 1u << cb;
+          }
+        }
+        mbar_wait(s_full, g & 1);
+        tc_fence_after();
+        float ref;  // exp2 reference in the scaled domain
+        float alpha = 1.f, m_new = m;
+        if constexpr (kFixed) {
+          ref = a.ref_log2;
+        } else {
+          float mx4[4] = {NEG_INF, NEG_INF, NEG_INF, NEG_INF};
+#pragma unroll
+          for (int cb = 0; cb < 4; ++cb) {
+            if (none_mask & (1u << cb)) continue;
+            uint32_t rr[32];
+            tmem_ld_32x32b_x32(tS + lane_off + cb * 32, rr);
+            tmem_ld_wait();
+            const int cs = c0 + cb * 32;
+            const bool fullc = (full_mask & (1u << cb)) != 0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const int kv = cs + i;
+              const bool vis = fullc || (kv >= meta.x && kv <= meta.y) || kv == meta.z;
+              mx4[i & 3] = fmaxf(mx4[i & 3], vis ? __uint_as_float(rr[i]) : NEG_INF);
+            }
+          }
+          m_new = fmaxf(m, fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])));
+          ref = m_new == NEG_INF ? 0.f : m_new * sl2;
+          alpha = ex2_approx(m * sl2 - ref);  // m = -inf -> 0
+#pragma unroll
+          for (int u = 0; u < 4; ++u) lsum[u] = make_float2(lsum[u].x * alpha, lsum[u].y * alpha);
+        }
+        const float2 nref = make_float2(-ref, -ref);
+        mbar_wait(p_empty, (g & 1) ^ 1);  // PV of the previous tile has consumed P
 #pragma unroll
         for (int cb = 0; cb < 4; ++cb) {
-          const int cs = c0 + cb * 32, ce = cs + 31;
-          const bool f = meta.x <= cs && meta.y >= ce;
-          const bool n = (meta.y < cs || meta.x > ce) && !(meta.z >= cs && meta.z <= ce);
-          if (!__all_sync(0xffffffffu, f)) full_mask &= ~(1u << cb);
-          if (__all_sync(0xffffffffu, n)) none_mask |= 1u << cb;
-        }
-      }
-      mbar_wait(s_full, j & 1);
-      tc_fence_after();
-      // pass 1: masked row max of the raw logits
-      float mx = NEG_INF;
+          uint32_t w[16];
+          if (none_mask & (1u << cb)) {
 #pragma unroll
-      for (int cb = 0; cb < 4; ++cb) {
-        if (none_mask & (1u << cb)) continue;
-        uint32_t rr[32];
-        tmem_ld_32x32b_x32(tS + lane_off + cb * 32, rr);
-        tmem_ld_wait();
-        if (full_mask & (1u << cb)) {
+            for (int i = 0; i < 16; ++i) w[i] = 0u;
+          } else {
+            uint32_t rr[32];
+            tmem_ld_32x32b_x32(tS + lane_off + cb * 32, rr);
+            tmem_ld_wait();
+            const bool fullc = (full_mask & (1u << cb)) != 0;
+            const int cs = c0 + cb * 32;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(rr[i]));
-        } else {
-          const int cs = c0 + cb * 32;
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int kv = cs + i;
-            const bool vis = (kv >= meta.x && kv <= meta.y) || kv == meta.z;
-            mx = fmaxf(mx, vis ? __uint_as_float(rr[i]) : NEG_INF);
-          }
-        }
-      }
-      const float m_new = fmaxf(m, mx);
-      // exp2 reference point in the scaled domain; 0 while the row has seen nothing yet
-      const float ms = m_new == NEG_INF ? 0.f : m_new * sl2;
-      const float alpha = ex2_approx(m * sl2 - ms);  // m = -inf -> 0
-      // pass 2: p = 2^(s*scale*log2e - ms), bf16 P into the SW128 A-operand layout
-      float2 rs2 = make_float2(0.f, 0.f);
-      const float2 sl2v = make_float2(sl2, sl2), nms = make_float2(-ms, -ms);
-      uint8_t* prow = smem + S::oP + (j & 1) * S::kPBytes + r * 128;
-#pragma unroll
-      for (int cb = 0; cb < 4; ++cb) {
-        uint32_t w[16];
-        if (none_mask & (1u << cb)) {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) w[i] = 0u;
-        } else {
-          uint32_t rr[32];
-          tmem_ld_32x32b_x32(tS + lane_off + cb * 32, rr);
-          tmem_ld_wait();
-          const bool fullc = (full_mask & (1u << cb)) != 0;
-          const int cs = c0 + cb * 32;
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            float2 x = ffma2(make_float2(__uint_as_float(rr[2 * i]), __uint_as_float(rr[2 * i + 1])),
-                             sl2v, nms);
-            if (!fullc) {
-              const int kv = cs + 2 * i;
-              if (!((kv >= meta.x && kv <= meta.y) || kv == meta.z)) x.x = NEG_INF;
-              if (!((kv + 1 >= meta.x && kv + 1 <= meta.y) || kv + 1 == meta.z)) x.y = NEG_INF;
+            for (int i = 0; i < 16; ++i) {
+              float2 x = ffma2(make_float2(__uint_as_float(rr[2 * i]), __uint_as_float(rr[2 * i + 1])),
+                               sl2v, nref);
+              if (!fullc) {
+                const int kv = cs + 2 * i;
+                if (!((kv >= meta.x && kv <= meta.y) || kv == meta.z)) x.x = NEG_INF;
+                if (!((kv + 1 >= meta.x && kv + 1 <= meta.y) || kv + 1 == meta.z)) x.y = NEG_INF;
+              }
+              const float2 p = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+              lsum[i & 3] = fadd2(lsum[i & 3], p);
+              w[i] = pack_bf16x2(p.x, p.y);
             }
-            const float p0 = ex2_approx(x.x), p1 = ex2_approx(x.y);
-            rs2 = fadd2(rs2, make_float2(p0, p1));
-            w[i] = pack_bf16x2(p0, p1);
           }
-        }
 #pragma unroll
-        for (int h4 = 0; h4 < 4; ++h4) {
-          const int ch = cb * 4 + h4;  // 16-byte chunk index 0..15 along the 128 kv columns
-          const int atom = ch >> 3, cc = ch & 7;
-          *reinterpret_cast<int4*>(prow + atom * 16384 + ((cc ^ (r & 7)) << 4)) =
-              make_int4(w[4 * h4], w[4 * h4 + 1], w[4 * h4 + 2], w[4 * h4 + 3]);
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(s_free);  // S fully consumed: the next QK^T may overwrite it
-      l = l * alpha + (rs2.x + rs2.y);
-      m = m_new;
-      fence_proxy_async_smem();
-      mbar_arrive(&p_full[j & 1]);
-      if (j > 0) {  // deferred: acc <- acc * alpha_{j-1} + O_{j-1}
-        const int pb = (j - 1) & 1;
-        mbar_wait(&o_full[pb], ((j - 1) >> 1) & 1);
-        tc_fence_after();
-        float o[DK];
-        tmem_row_chunk<DK>(tO0 + pb * DK + lane_off, o);
-        const float2 av = make_float2(alpha_prev, alpha_prev);
-#pragma unroll
-        for (int i = 0; i < DK; i += 2) {
-          const float2 rr2 = ffma2(make_float2(acc[i], acc[i + 1]), av, make_float2(o[i], o[i + 1]));
-          acc[i] = rr2.x;
-          acc[i + 1] = rr2.y;
+          for (int h4 = 0; h4 < 4; ++h4) {
+            const int ch = cb * 4 + h4;  // 16-byte chunk index 0..15 along the 128 kv columns
+            const int atom = ch >> 3, cc = ch & 7;
+            *reinterpret_cast<int4*>(prow + atom * 16384 + ((cc ^ (r & 7)) << 4)) =
+                make_int4(w[4 * h4], w[4 * h4 + 1], w[4 * h4 + 2], w[4 * h4 + 3]);
+          }
         }
         tc_fence_before();
+        mbar_arrive(s_free);  // S fully consumed: the next QK^T may overwrite it
+        fence_proxy_async_smem();
+        mbar_arrive(p_full);
+        if constexpr (!kFixed) {
+          m = m_new;
+          if (j > 0) {  // deferred: acc <- acc * alpha_{j-1} + O_{j-1}
+            const int pb = (g - 1) & 1;
+            mbar_wait(&o_full[pb], ((g - 1) >> 1) & 1);
+            tc_fence_after();
+            float o[DK];
+            tmem_row_chunk<DK>(tO0 + pb * DK + lane_off, o);
+            tc_fence_before();
+            const float2 av = make_float2(alpha_prev, alpha_prev);
+#pragma unroll
+            for (int i = 0; i < DK; i += 2) {
+              const float2 t2 = ffma2(make_float2(acc[i], acc[i + 1]), av, make_float2(o[i], o[i + 1]));
+              acc[i] = t2.x;
+              acc[i + 1] = t2.y;
+            }
+          }
+          alpha_prev = alpha;
+        }
       }
-      alpha_prev = alpha;
-    }
-    if (n_t > 0) {
-      const int pb = (n_t - 1) & 1;
-      mbar_wait(&o_full[pb], ((n_t - 1) >> 1) & 1);
-      tc_fence_after();
+      // ---- item epilogue: O / l * gate -> bf16
       float o[DK];
-      tmem_row_chunk<DK>(tO0 + pb * DK + lane_off, o);
 #pragma unroll
-      for (int i = 0; i < DK; ++i) acc[i] = acc[i] * alpha_prev + o[i];
-    }
-    const int qrow = q0 + r;
-    if (qrow < a.Rq) {
-      const int b = bh / a.H, h = bh - b * a.H;
-      const size_t off = static_cast<size_t>(b * a.Rq + qrow) * a.d + h * DK;
-      const float invl = 1.f / l;
-      const __nv_bfloat16* gp = a.g + off;
-      float y[DK];
+      for (int i = 0; i < DK; ++i) o[i] = 0.f;
+      if constexpr (kFixed) {
+        mbar_wait(&o_full[0], li & 1);
+        tc_fence_after();
+        tmem_row_chunk<DK>(tO0 + lane_off, o);
+        tc_fence_before();
+        mbar_arrive(o_empty);
+      } else {
+        if (n_t > 0) {
+          const int pb = (g - 1) & 1;
+          mbar_wait(&o_full[pb], ((g - 1) >> 1) & 1);
+          tc_fence_after();
+          tmem_row_chunk<DK>(tO0 + pb * DK + lane_off, o);
+          tc_fence_before();
 #pragma unroll
-      for (int i = 0; i < DK; ++i) y[i] = acc[i] * invl * __bfloat162float(gp[i]);
-      for (int i = 0; i < DK; i += 8) {
-        int4 w = make_int4(pack_bf16x2(y[i], y[i + 1]), pack_bf16x2(y[i + 2], y[i + 3]),
-                           pack_bf16x2(y[i + 4], y[i + 5]), pack_bf16x2(y[i + 6], y[i + 7]));
-        *reinterpret_cast<int4*>(a.out + off + i) = w;
+          for (int i = 0; i < DK; ++i) o[i] = acc[i] * alpha_prev + o[i];
+        }
       }
-    }
+      const float l = (lsum[0].x + lsum[0].y) + (lsum[1].x + lsum[1].y) +
+                      (lsum[2].x + lsum[2].y) + (lsum[3].x + lsum[3].y);
+      if (qrow < a.Rq) {
+        const float invl = 1.f / l;
+#pragma unroll
+        for (int i = 0; i < DK / 8; ++i) {
+          const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gate[i]);
+          uint32_t w[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 gf = __bfloat1622float2(g2[e]);
+            w[e] = pack_bf16x2(o[8 * i + 2 * e] * invl * gf.x, o[8 * i + 2 * e + 1] * invl * gf.y);
+          }
+          reinterpret_cast<int4*>(a.out + off)[i] = make_int4(w[0], w[1], w[2], w[3]);
+        }
+      }
+    }  // item loop
   }
   tc_fence_before();
   __syncthreads();

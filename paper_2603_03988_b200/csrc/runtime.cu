@@ -46,6 +46,7 @@ struct LayerDev {
   int in_buf = 0, q_buf = 0;
   int Rq = 0, Rkv = 0, Rkv_pad = 0;
   int bn_full = 0, bn_half = 0, bn_up = 0;
+  float logit_bound = 0.f;  // QKNorm logit bound (0 = unknown -> online-max softmax)
   CUtensorMap tmA_in, tmA_q, tmB_qgkv, tmB_qg, tmB_kv, tmA_hg, tmB_o, tmB_up, tmA_hid, tmB_down;
   CUtensorMap tmQ, tmK, tmV;
 };
@@ -242,8 +243,18 @@ static void finalize(Handle& h) {
       L.w_up = h.upload(w);
     }
     L.w_down = h.upload(transpose_bf16(need_param(h, f + "w_down", m, d), m, nullptr));
-    L.gain_q = h.upload(need_param(h, a + "qk_gain_q", H, dk).v);
-    L.gain_k = h.upload(need_param(h, a + "qk_gain_k", H, dk).v);
+    {
+      const HostParam& gq = need_param(h, a + "qk_gain_q", H, dk);
+      const HostParam& gk = need_param(h, a + "qk_gain_k", H, dk);
+      L.gain_q = h.upload(gq.v);
+      L.gain_k = h.upload(gk.v);
+      // |q.k| / sqrt(dk) <= sqrt(dk) * max|g_q| * max|g_k| for every head (QKNorm + RoPE
+      // rotation); 2% margin for the bf16 rounding of q and k.
+      float mq = 0.f, mk = 0.f;
+      for (float v : gq.v) mq = std::max(mq, std::fabs(v));
+      for (float v : gk.v) mk = std::max(mk, std::fabs(v));
+      L.logit_bound = 1.02f * std::sqrt(static_cast<float>(dk)) * mq * mk + 1e-3f;
+    }
     // plan arrays
     std::vector<int4> meta(static_cast<size_t>(lp.n_qtiles) * 128, make_int4(0, -1, -1, 0));
     for (int r = 0; r < lp.l_q; ++r) meta[r] = make_int4(lp.lo[r], lp.hi[r], lp.self_idx[r], 0);
@@ -330,13 +341,15 @@ static void launch_gemm(Handle& h, const CUtensorMap& A, const CUtensorMap& B, i
   ++h.launches;
 }
 
-template <int DK>
+template <int DK, bool kFixed>
 static void launch_attention_dk(Handle& h, const LayerDev& L, const LayerPlan& lp, int B) {
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(k_attention<DK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(AttnSmem<DK>::kTotal)));
-    attr = true;
+  static size_t attr_bytes = 0;
+  const int n_codes = static_cast<int>(lp.tile_code.size());
+  const size_t smem = AttnSmem<DK>::bytes(2 * lp.n_qtiles + 1 + n_codes);
+  if (smem > attr_bytes) {
+    CK(cudaFuncSetAttribute(k_attention<DK, kFixed>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(smem)));
+    attr_bytes = smem;
   }
   AttnArgs a;
   a.rowmeta = L.rowmeta;
@@ -349,18 +362,25 @@ static void launch_attention_dk(Handle& h, const LayerDev& L, const LayerPlan& l
   a.H = h.H;
   a.Rq = L.Rq;
   a.d = h.d;
+  a.n_qtiles = lp.n_qtiles;
+  a.n_codes = n_codes;
   a.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(DK)));
-  const int grid = lp.n_qtiles * B * h.H;
-  k_attention<DK><<<grid, kAttnThreads, AttnSmem<DK>::kTotal, h.stream>>>(L.tmQ, L.tmK, L.tmV, a);
+  a.ref_log2 = L.logit_bound * a.scale_log2;
+  const int grid = std::min(lp.n_qtiles * B * h.H, 2 * h.num_sms);
+  k_attention<DK, kFixed><<<grid, kAttnThreads, smem, h.stream>>>(L.tmQ, L.tmK, L.tmV, a);
   check_launch("attention");
   ++h.launches;
 }
 
 static void launch_attention(Handle& h, const LayerDev& L, const LayerPlan& lp, int B) {
-  switch (h.dk) {
-    case 16: launch_attention_dk<16>(h, L, lp, B); break;
-    case 32: launch_attention_dk<32>(h, L, lp, B); break;
-    case 64: launch_attention_dk<64>(h, L, lp, B); break;
+  const bool fixed = L.logit_bound > 0.f && L.logit_bound < kFixedRefMax;
+  switch (h.dk * 2 + (fixed ? 1 : 0)) {
+    case 32: launch_attention_dk<16, false>(h, L, lp, B); break;
+    case 33: launch_attention_dk<16, true>(h, L, lp, B); break;
+    case 64: launch_attention_dk<32, false>(h, L, lp, B); break;
+    case 65: launch_attention_dk<32, true>(h, L, lp, B); break;
+    case 128: launch_attention_dk<64, false>(h, L, lp, B); break;
+    case 129: launch_attention_dk<64, true>(h, L, lp, B); break;
     default: throw ConfigError("unsupported head dim");
   }
 }
