@@ -66,6 +66,15 @@ struct AttnArgs {
   float ref_log2;             // fixed-reference mode: B * scale_log2
 };
 
+// Visibility of columns [cs, cs+32) for a row with compact mask (lo, hi, self), as bits.
+__device__ __forceinline__ uint32_t chunk_vis_bits(int cs, int lo, int hi, int self_idx) {
+  const int a = max(lo - cs, 0), b = min(hi - cs, 31);
+  uint32_t bits = b >= a ? ((2u << b) - (1u << a)) : 0u;  // (2u << 31) wraps to 0: still exact
+  const int so = self_idx - cs;
+  if (so >= 0 && so < 32) bits |= 1u << so;
+  return bits;
+}
+
 template <int DK, bool kFixed>
 __global__ void __launch_bounds__(kAttnThreads, 2)
     k_attention(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -266,13 +275,14 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
             uint32_t rr[32];
             tmem_ld_32x32b_x32(tS + lane_off + cb * 32, rr);
             tmem_ld_wait();
-            const int cs = c0 + cb * 32;
-            const bool fullc = (full_mask & (1u << cb)) != 0;
+            if (full_mask & (1u << cb)) {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) {
-              const int kv = cs + i;
-              const bool vis = fullc || (kv >= meta.x && kv <= meta.y) || kv == meta.z;
-              mx4[i & 3] = fmaxf(mx4[i & 3], vis ? __uint_as_float(rr[i]) : NEG_INF);
+              for (int i = 0; i < 32; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], __uint_as_float(rr[i]));
+            } else {
+              const uint32_t bits = chunk_vis_bits(c0 + cb * 32, meta.x, meta.y, meta.z);
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                mx4[i & 3] = fmaxf(mx4[i & 3], (bits >> i) & 1u ? __uint_as_float(rr[i]) : NEG_INF);
             }
           }
           m_new = fmaxf(m, fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])));
@@ -293,20 +303,27 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
             uint32_t rr[32];
             tmem_ld_32x32b_x32(tS + lane_off + cb * 32, rr);
             tmem_ld_wait();
-            const bool fullc = (full_mask & (1u << cb)) != 0;
-            const int cs = c0 + cb * 32;
+            if (full_mask & (1u << cb)) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              float2 x = ffma2(make_float2(__uint_as_float(rr[2 * i]), __uint_as_float(rr[2 * i + 1])),
-                               sl2v, nref);
-              if (!fullc) {
-                const int kv = cs + 2 * i;
-                if (!((kv >= meta.x && kv <= meta.y) || kv == meta.z)) x.x = NEG_INF;
-                if (!((kv + 1 >= meta.x && kv + 1 <= meta.y) || kv + 1 == meta.z)) x.y = NEG_INF;
+              for (int i = 0; i < 16; ++i) {
+                const float2 x = ffma2(make_float2(__uint_as_float(rr[2 * i]), __uint_as_float(rr[2 * i + 1])),
+                                       sl2v, nref);
+                const float2 p = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+                lsum[i & 3] = fadd2(lsum[i & 3], p);
+                w[i] = pack_bf16x2(p.x, p.y);
               }
-              const float2 p = make_float2(ex2_approx(x.x), ex2_approx(x.y));
-              lsum[i & 3] = fadd2(lsum[i & 3], p);
-              w[i] = pack_bf16x2(p.x, p.y);
+            } else {
+              const uint32_t bits = chunk_vis_bits(c0 + cb * 32, meta.x, meta.y, meta.z);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                float2 x = ffma2(make_float2(__uint_as_float(rr[2 * i]), __uint_as_float(rr[2 * i + 1])),
+                                 sl2v, nref);
+                x.x = (bits >> (2 * i)) & 1u ? x.x : NEG_INF;
+                x.y = (bits >> (2 * i + 1)) & 1u ? x.y : NEG_INF;
+                const float2 p = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+                lsum[i & 3] = fadd2(lsum[i & 3], p);
+                w[i] = pack_bf16x2(p.x, p.y);
+              }
             }
           }
 #pragma unroll
