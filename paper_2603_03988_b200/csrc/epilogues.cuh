@@ -3,9 +3,10 @@
 //
 // Interface used by k_gemm_bf16:
 //   prologue(smem, tid, nthreads)  once per CTA, before the role split (fill scratch smem)
-//   run(smem, wait, tbase, row, n0, c0, c1, valid)
+//   run(smem, wait, tbase, row, n0, c0, c1, valid, part, nparts)
 //       issue this row's global prefetches, call wait() (accumulator ready), then consume
-//       accumulator columns [c0, c1) of the tile (absolute columns n0 + c).
+//       accumulator columns [c0, c1) of the tile (absolute columns n0 + c). `part` numbers
+//       the (n-slice, column half) this thread covers out of `nparts` per row.
 //
 // Pre-norm folding: RMSNorm(x; g) W = diag(1/rms(x)) x (diag(g) W). The gain is
 // folded into the bf16 weight rows at load time and 1/rms is applied here from
@@ -16,6 +17,13 @@
 
 namespace sortk {
 
+// Row statistics: each residual-stream row carries its sum of squares as kSSParts partial
+// sums written by distinct epilogue threads; they are combined in a fixed order so the
+// result (and everything downstream) is bitwise deterministic.
+__device__ __forceinline__ float row_ss(const float4* ss, int row) {
+  const float4 p = ss[row];
+  return (p.x + p.y) + (p.z + p.w);
+}
 __device__ __forceinline__ float row_inv_rms(float ss, float inv_d) {
   return rsqrtf(ss * inv_d + 1e-6f);  // norm.hpp:23-24 (eps = kRmsEps, norm.hpp:8)
 }
@@ -30,8 +38,8 @@ __device__ __forceinline__ void store_bf16_row(__nv_bfloat16* dst, const float* 
 }
 
 __device__ __forceinline__ float fast_sigmoid(float x) {
-  // 1 / (1 + e^-x): saturates cleanly to 0 / 1 (e^-x -> inf gives 0), no branch divergence.
-  return __frcp_rn(1.f + __expf(-x));
+  // sigma(x) = (1 + tanh(x/2)) / 2: one MUFU op, saturates cleanly, no branch divergence.
+  return fmaf(0.5f, tanh_approx(0.5f * x), 0.5f);
 }
 
 // ---------------------------------------------------------------------------
@@ -46,10 +54,14 @@ enum : int { kSecQ = 0, kSecK = 1, kSecV = 2, kSecG = 3 };
 template <int DK>
 struct EpiQKVG {
   static constexpr int kChunk = DK;
+  static constexpr int kMaxParts = 1 << 30;  // does not produce row statistics
   int d, H, R;      // R: rows per request of the A operand
-  int sec_packed;   // section of column block i (of width d) in bits [4i, 4i+4)
+  // Column chunk ci (= col / DK) of this GEMM's N dimension -> section / head. The host
+  // interleaves the weight rows head by head ([Q_h V_h K_h G_h] ...) so every n-slice,
+  // and each half of it, carries the same epilogue work.
+  uint8_t csec[64], chead[64];
   float inv_d;
-  const float* ss;
+  const float4* ss;
   const float* gain_q;  // [H*DK]
   const float* gain_k;
   const float2* rope;   // [(max_pos+1) * DK/2] (cos, sin)
@@ -70,7 +82,7 @@ struct EpiQKVG {
 
   template <class Wait>
   __device__ __forceinline__ void run(uint8_t* smem, Wait&& wait, uint32_t tbase, int row, int n0,
-                                      int c0, int c1, bool valid) const {
+                                      int c0, int c1, bool valid, int, int) const {
     const float* sg = reinterpret_cast<const float*>(smem);
     const int b = row / R, r = row - b * R;
     // Sections are d columns wide and BN divides 4d, so a tile's chunks may span sections;
@@ -78,7 +90,7 @@ struct EpiQKVG {
     float inv = 0.f;
     float2 cs[DK / 2];
     if (valid) {
-      inv = row_inv_rms(ss[row], inv_d);
+      inv = row_inv_rms(row_ss(ss, row), inv_d);
       const float2* rp = rope + static_cast<size_t>(pos[r]) * (DK / 2);
 #pragma unroll
       for (int j = 0; j < DK / 2; ++j) cs[j] = __ldg(rp + j);
@@ -88,10 +100,9 @@ struct EpiQKVG {
       float v[DK];
       tmem_row_chunk<DK>(tbase + c, v);
       if (!valid) continue;
-      const int col = n0 + c;
-      const int si = col / d;
-      const int s = (sec_packed >> (4 * si)) & 0xF;
-      const int head = (col - si * d) / DK;
+      const int ci = (n0 + c) / DK;
+      const int s = csec[ci];
+      const int head = chead[ci];
 #pragma unroll
       for (int i = 0; i < DK; ++i) v[i] *= inv;
       if (s == kSecQ || s == kSecK) {
@@ -131,17 +142,17 @@ struct EpiQKVG {
 // prefetched into registers before the accumulator wait.
 struct EpiResid {
   static constexpr int kChunk = 32;
+  static constexpr int kMaxParts = 4;
   const __nv_bfloat16* resid;
   __nv_bfloat16* out;
-  float* ss_out;
+  float* ss_out;   // [rows, 4] partial sums of squares
   int d;
-  int ss_atomic;  // several column tiles per row -> partial sums combined atomically
 
   __device__ __forceinline__ void prologue(uint8_t*, int, int) const {}
 
   template <class Wait>
   __device__ __forceinline__ void run(uint8_t*, Wait&& wait, uint32_t tbase, int row, int n0,
-                                      int c0, int c1, bool valid) const {
+                                      int c0, int c1, bool valid, int part, int nparts) const {
     int4 rv[16];  // up to 128 columns
     const int nq = (c1 - c0) / 8;
     if (valid && resid) {
@@ -181,8 +192,13 @@ struct EpiResid {
 #pragma unroll
       for (int qd = 0; qd < 4; ++qd) op[qd] = o[qd];
     }
-    // two half-row epilogue warps (and possibly several column tiles) contribute
-    if (valid) atomicAdd(ss_out + row, ss);
+    // this thread's partial sum goes to its own slot; part 0 clears the unused slots
+    if (valid) {
+      float* o = ss_out + static_cast<size_t>(row) * 4;
+      o[part] = ss;
+      if (part == 0)
+        for (int k = nparts; k < 4; ++k) o[k] = 0.f;
+    }
   }
 };
 
@@ -192,7 +208,8 @@ struct EpiResid {
 // hidden units: h = swish(g/rms) * (u/rms) -> bf16 hidden [M, m].
 struct EpiSwiGLU {
   static constexpr int kChunk = 64;
-  const float* ss;
+  static constexpr int kMaxParts = 1 << 30;
+  const float4* ss;
   float inv_d;
   __nv_bfloat16* hidden;
   int m;
@@ -201,8 +218,8 @@ struct EpiSwiGLU {
 
   template <class Wait>
   __device__ __forceinline__ void run(uint8_t*, Wait&& wait, uint32_t tbase, int row, int n0,
-                                      int c0, int c1, bool valid) const {
-    const float inv = valid ? row_inv_rms(ss[row], inv_d) : 0.f;
+                                      int c0, int c1, bool valid, int, int) const {
+    const float inv = valid ? row_inv_rms(row_ss(ss, row), inv_d) : 0.f;
     wait();
     for (int c = c0; c < c1; c += 64) {
       float v[64];

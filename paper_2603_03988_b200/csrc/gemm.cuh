@@ -11,14 +11,13 @@
 // the accumulator after tcgen05.ld.
 //
 // Roles (384 threads, 1 CTA per SM):
-//   warp 0       TMA producer   (A tile 128x64, B tile BNx64 per stage, SW128)
+//   warp 0       TMA producer   (weight slice once, then A tiles 128x64 per stage, SW128)
 //   warp 1       MMA issuer     (one thread; 4 x tcgen05.mma K=16 per stage)
 //   warp 2       TMEM allocator (2 accumulator stages x 256 columns)
 //   warps 4..11  epilogue       (thread <-> accumulator row; TMEM lane quarter = warp % 4;
 //                                warps 4-7 take the first half of the tile's column chunks,
 //                                warps 8-11 the second half)
-// Tiles are walked m-major with every CTA cycling through all n-tiles, so
-// epilogues with different per-section cost (e.g. Q/K vs V) balance across SMs.
+// The weight slice of a CTA stays resident in shared memory (weight-stationary).
 #pragma once
 
 #include "ptx.cuh"
@@ -27,50 +26,69 @@ namespace sortk {
 
 constexpr int kGemmBM = 128;
 constexpr int kGemmBK = 64;
-constexpr int kGemmStages = 4;
-constexpr int kGemmMaxBN = 256;
 constexpr int kGemmEpiWarps = 8;
 constexpr int kGemmThreads = 128 + 32 * kGemmEpiWarps;
-constexpr uint32_t kGemmABytes = kGemmBM * kGemmBK * 2;     // 16 KB
-constexpr uint32_t kGemmBBytes = kGemmMaxBN * kGemmBK * 2;  // 32 KB
-constexpr uint32_t kGemmEpiSmem = 8192;                     // per-kernel epilogue scratch
-constexpr size_t kGemmSmemBytes =
-    1024 + kGemmStages * (kGemmABytes + kGemmBBytes) + kGemmEpiSmem + 8 * (2 * kGemmStages + 4) + 16;
+constexpr uint32_t kGemmABytes = kGemmBM * kGemmBK * 2;  // 16 KB per A stage
+constexpr uint32_t kGemmEpiSmem = 8192;                  // per-kernel epilogue scratch
+constexpr uint32_t kGemmSmemMax = 227 * 1024;
 
-// Tile t of the CTA-strided walk -> (m block, n block). Consecutive tiles of one CTA
-// advance n fastest so each CTA sees every n-tile (section) in turn.
-__device__ __forceinline__ void gemm_tile_coords(int tile, int num_n, int& mb, int& nb) {
-  mb = tile / num_n;
-  nb = tile - mb * num_n;
+// Shared-memory plan of one weight-stationary GEMM launch.
+struct GemmPlan {
+  int BN, num_k, a_stages;
+  uint32_t b_bytes, smem_bytes;
+};
+
+__host__ __device__ inline GemmPlan gemm_plan(int K, int BN) {
+  GemmPlan p;
+  p.BN = BN;
+  p.num_k = (K + kGemmBK - 1) / kGemmBK;
+  p.b_bytes = static_cast<uint32_t>(BN) * kGemmBK * 2 * p.num_k;
+  const uint32_t fixed = 1024 + p.b_bytes + kGemmEpiSmem + 256;
+  int st = fixed < kGemmSmemMax ? static_cast<int>((kGemmSmemMax - fixed) / kGemmABytes) : 0;
+  p.a_stages = st > 8 ? 8 : st;
+  p.smem_bytes = fixed + p.a_stages * kGemmABytes;
+  return p;
 }
 
+// Weight-stationary persistent GEMM. CTA c owns the BN-wide weight slice nb = c % num_n
+// (loaded into smem once by TMA) and streams the A tiles of m-blocks c / num_n,
+// c / num_n + G / num_n, ... through an a_stages-deep TMA ring. Only A moves per tile,
+// which keeps the L2 -> SM traffic at ~32 B/clk/SM for K = 256 instead of re-reading
+// the weights for every 128-row tile.
 template <class Epi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm_bf16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                int M, int N, int K, int BN, Epi epi) {
+                int M, int N, int K, int BN, int a_stages, Epi epi) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + kGemmStages * kGemmABytes;
-  uint8_t* sEpi = sB + kGemmStages * kGemmBBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sEpi + kGemmEpiSmem);
-  uint64_t* empty = full + kGemmStages;
-  uint64_t* tfull = empty + kGemmStages;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int num_k = (K + kGemmBK - 1) / kGemmBK;
+  const uint32_t b_box = static_cast<uint32_t>(BN) * kGemmBK * 2;
+  uint8_t* sB = smem;
+  uint8_t* sA = sB + b_box * num_k;
+  uint8_t* sEpi = sA + a_stages * kGemmABytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + kGemmEpiSmem);
+  uint64_t* full = bars;             // [a_stages <= 8]
+  uint64_t* empty = bars + 8;        // [8]
+  uint64_t* tfull = bars + 16;       // [2]
+  uint64_t* tempty = bars + 18;      // [2]
+  uint64_t* b_full = bars + 20;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 21);
 
   const int warp = warp_id();
   const int lane = lane_id();
   const int num_m = (M + kGemmBM - 1) / kGemmBM;
   const int num_n = N / BN;
-  const int num_tiles = num_m * num_n;
-  const int num_k = (K + kGemmBK - 1) / kGemmBK;
+  const int nb = blockIdx.x % num_n;
+  const int m_first = blockIdx.x / num_n;
+  const int m_step = gridDim.x / num_n;
+  // residual epilogues keep one sum-of-squares slot per (n-slice, half): at most 4
+  if (num_n > 2 && threadIdx.x == 0 && blockIdx.x == 0 && Epi::kMaxParts < num_n * 2) __trap();
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    for (int s = 0; s < kGemmStages; ++s) {
+    for (int s = 0; s < a_stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -78,6 +96,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 32 * kGemmEpiWarps);
     }
+    mbar_init(b_full, 1);
     mbar_fence_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
@@ -89,18 +108,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint32_t stage_bytes = kGemmABytes + static_cast<uint32_t>(BN) * kGemmBK * 2;
+      mbar_arrive_expect_tx(b_full, b_box * num_k);
+      for (int kb = 0; kb < num_k; ++kb)
+        tma_load_2d(sB + kb * b_box, &tmB, b_full, kb * kGemmBK, nb * BN);
       int s = 0;
       uint32_t ph = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        int mb, nb;
-        gemm_tile_coords(tile, num_n, mb, nb);
+      for (int mb = m_first; mb < num_m; mb += m_step) {
         for (int kb = 0; kb < num_k; ++kb) {
-          mbar_wait(&empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&full[s], stage_bytes);
+          mbar_wait_sleep(&empty[s], ph ^ 1);
+          mbar_arrive_expect_tx(&full[s], kGemmABytes);
           tma_load_2d(sA + s * kGemmABytes, &tmA, &full[s], kb * kGemmBK, mb * kGemmBM);
-          tma_load_2d(sB + s * kGemmBBytes, &tmB, &full[s], kb * kGemmBK, nb * BN);
-          if (++s == kGemmStages) {
+          if (++s == a_stages) {
             s = 0;
             ph ^= 1;
           }
@@ -110,27 +128,29 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       const uint32_t idesc = umma_idesc_bf16(kGemmBM, BN);
+      const uint32_t b0 = smem_u32(sB);
+      mbar_wait_sleep(b_full, 0);
       int s = 0;
       uint32_t ph = 0;
       int t = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
+      for (int mb = m_first; mb < num_m; mb += m_step, ++t) {
         const int acc = t & 1;
         const uint32_t acc_ph = (t >> 1) & 1;
-        mbar_wait(&tempty[acc], acc_ph ^ 1);
+        mbar_wait_sleep(&tempty[acc], acc_ph ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * 256;
         for (int kb = 0; kb < num_k; ++kb) {
-          mbar_wait(&full[s], ph);
+          mbar_wait_sleep(&full[s], ph);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + s * kGemmABytes);
-          const uint32_t b0 = smem_u32(sB + s * kGemmBBytes);
+          const uint32_t bk = b0 + kb * b_box;
 #pragma unroll
           for (int k = 0; k < kGemmBK / 16; ++k) {
-            mma_bf16_ss(d, umma_sdesc_kmajor(a0 + k * 32, 128), umma_sdesc_kmajor(b0 + k * 32, 128),
+            mma_bf16_ss(d, umma_sdesc_kmajor(a0 + k * 32, 128), umma_sdesc_kmajor(bk + k * 32, 128),
                         idesc, (kb | k) != 0 ? 1u : 0u);
           }
           mma_commit(&empty[s]);
-          if (++s == kGemmStages) {
+          if (++s == a_stages) {
             s = 0;
             ph ^= 1;
           }
@@ -146,18 +166,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int split = (n_chunks + 1) >> 1;
     const int c_begin = half ? split : 0, c_end = half ? n_chunks : split;
     int t = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++t) {
+    for (int mb = m_first; mb < num_m; mb += m_step, ++t) {
       const int acc = t & 1;
       const uint32_t acc_ph = (t >> 1) & 1;
-      int mb, nb;
-      gemm_tile_coords(tile, num_n, mb, nb);
       const int row = mb * kGemmBM + q * 32 + lane;
       const uint32_t tbase = tmem + acc * 256 + (static_cast<uint32_t>(q * 32) << 16);
       auto wait = [&]() {
         mbar_wait(&tfull[acc], acc_ph);
         tc_fence_after();
       };
-      epi.run(sEpi, wait, tbase, row, nb * BN, c_begin * Epi::kChunk, c_end * Epi::kChunk, row < M);
+      epi.run(sEpi, wait, tbase, row, nb * BN, c_begin * Epi::kChunk, c_end * Epi::kChunk, row < M,
+              nb * 2 + half, num_n * 2);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
     }
@@ -199,12 +218,13 @@ __device__ __forceinline__ void tmem_row_chunk(uint32_t taddr, float (&v)[kChunk
   }
 }
 
-// Grid size for the persistent GEMM: at most one CTA per SM, and never a multiple of the
-// n-tile count (so the CTA-strided tile walk rotates every CTA through all sections).
-inline int gemm_grid(int tiles, int num_n, int sms) {
-  int g = tiles < sms ? tiles : sms;
-  if (g == sms && num_n > 1 && g % num_n == 0) --g;
-  return g > 0 ? g : 1;
+// Grid of the weight-stationary GEMM: a multiple of the n-slice count (CTA c -> slice
+// c % num_n), at most one CTA per SM and no more than the tiles available.
+inline int gemm_grid(int num_m, int num_n, int sms) {
+  int per_slice = sms / num_n;
+  if (per_slice < 1) per_slice = 1;
+  if (per_slice > num_m) per_slice = num_m;
+  return per_slice * num_n;
 }
 
 }  // namespace sortk

@@ -9,8 +9,8 @@ namespace sortk {
 // P(x, L_out) generalised to retained rows (prune_queries / retained_rows,
 // mask.cpp:125-154): dst[b, i] = src[b, rows[i]] plus the row's sum of squares.
 // One warp per destination row, 16-byte vector copies.
-__global__ void k_gather_rows(const __nv_bfloat16* __restrict__ src, const float* __restrict__ ss_src,
-                              __nv_bfloat16* __restrict__ dst, float* __restrict__ ss_dst,
+__global__ void k_gather_rows(const __nv_bfloat16* __restrict__ src, const float4* __restrict__ ss_src,
+                              __nv_bfloat16* __restrict__ dst, float4* __restrict__ ss_dst,
                               const int32_t* __restrict__ rows, int B, int Rsrc, int Rdst, int d) {
   const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -30,7 +30,7 @@ constexpr int kHeadRows = 32;
 constexpr int kHeadThreads = 256;
 
 __global__ void __launch_bounds__(kHeadThreads)
-    k_head(const __nv_bfloat16* __restrict__ x, const float* __restrict__ ss, int R, int N, int total,
+    k_head(const __nv_bfloat16* __restrict__ x, const float4* __restrict__ ss, int R, int N, int total,
            int d, int dh, const float* __restrict__ gain, const float* __restrict__ w1,
            const float* __restrict__ b1, const float* __restrict__ w2, const float* __restrict__ b2,
            float* __restrict__ probs, float* __restrict__ logits) {
@@ -44,7 +44,8 @@ __global__ void __launch_bounds__(kHeadThreads)
     if (e < total) {
       const int b = e / N, j = e - b * N;
       const size_t row = static_cast<size_t>(b) * R + (R - N) + j;
-      const float inv = rsqrtf(ss[row] / static_cast<float>(d) + 1e-6f);
+      const float4 sp = ss[row];
+      const float inv = rsqrtf(((sp.x + sp.y) + (sp.z + sp.w)) / static_cast<float>(d) + 1e-6f);
       for (int c = lane; c < d; c += 32) xs[rr * d + c] = __bfloat162float(x[row * d + c]) * inv * gain[c];
     } else {
       for (int c = lane; c < d; c += 32) xs[rr * d + c] = 0.f;

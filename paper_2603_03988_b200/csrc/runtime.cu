@@ -41,13 +41,14 @@ struct LayerDev {
   int4* rowmeta = nullptr;
   int32_t *tile_off = nullptr, *tile_code = nullptr, *qtile_order = nullptr;
   int32_t *pos_q = nullptr, *pos_kv = nullptr, *query_rows = nullptr;
-  __nv_bfloat16 *w_qgkv = nullptr, *w_o = nullptr, *w_up = nullptr, *w_down = nullptr;
+  __nv_bfloat16 *w_all = nullptr, *w_kv = nullptr, *w_qg = nullptr, *w_o = nullptr,
+                *w_up = nullptr, *w_down = nullptr;
   float *gain_q = nullptr, *gain_k = nullptr;
   int in_buf = 0, q_buf = 0;
   int Rq = 0, Rkv = 0, Rkv_pad = 0;
-  int bn_full = 0, bn_half = 0, bn_up = 0;
+  int bn_full = 0, bn_half = 0, bn_up = 0, bn_o = 0, bn_down = 0;
   float logit_bound = 0.f;  // QKNorm logit bound (0 = unknown -> online-max softmax)
-  CUtensorMap tmA_in, tmA_q, tmB_qgkv, tmB_qg, tmB_kv, tmA_hg, tmB_o, tmB_up, tmA_hid, tmB_down;
+  CUtensorMap tmA_in, tmA_q, tmB_all, tmB_qg, tmB_kv, tmA_hg, tmB_o, tmB_up, tmA_hid, tmB_down;
   CUtensorMap tmQ, tmK, tmV;
 };
 
@@ -73,7 +74,7 @@ struct Handle {
   std::vector<LayerDev> layers;
   // workspace
   __nv_bfloat16* X[2] = {nullptr, nullptr};
-  float* SS[2] = {nullptr, nullptr};
+  float4* SS[2] = {nullptr, nullptr};  // per-row sum-of-squares partials
   __nv_bfloat16 *Qb = nullptr, *Kb = nullptr, *Vt = nullptr, *Gb = nullptr, *Hg = nullptr,
                 *hid = nullptr;
   float *probs = nullptr, *logits = nullptr;
@@ -184,7 +185,7 @@ static void finalize(Handle& h) {
   const size_t rows_max = static_cast<size_t>(h.Bmax) * h.L0;
   for (int i = 0; i < 2; ++i) {
     h.X[i] = h.dalloc<__nv_bfloat16>(rows_max * d);
-    h.SS[i] = h.dalloc<float>(rows_max);
+    h.SS[i] = h.dalloc<float4>(rows_max);
   }
   h.Qb = h.dalloc<__nv_bfloat16>(rows_max * d);
   h.Kb = h.dalloc<__nv_bfloat16>(rows_max * d);
@@ -219,14 +220,23 @@ static void finalize(Handle& h) {
     const std::string f = "ffn." + std::to_string(l) + ".";
     const HostParam& ga = need_param(h, bk + "attn_norm", 1, d);
     const HostParam& gf = need_param(h, bk + "ffn_norm", 1, d);
-    {  // [Q | G | K | V]^T with the attention pre-norm gain folded into the input rows
-      std::vector<__nv_bfloat16> w(static_cast<size_t>(4) * d * d);
-      const char* order[4] = {"wq", "wg", "wk", "wv"};
-      for (int s = 0; s < 4; ++s) {
-        std::vector<__nv_bfloat16> t = transpose_bf16(need_param(h, a + order[s], d, d), d, ga.v.data());
-        std::copy(t.begin(), t.end(), w.begin() + static_cast<size_t>(s) * d * d);
-      }
-      L.w_qgkv = h.upload(w);
+    {  // Q/K/V/G projections: W^T rows interleaved head by head in section order `order`,
+       // attention pre-norm gain folded into the input rows.
+      const std::string names[4] = {"wq", "wk", "wv", "wg"};  // kSecQ, kSecK, kSecV, kSecG
+      std::vector<__nv_bfloat16> t[4];
+      for (int sct = 0; sct < 4; ++sct) t[sct] = transpose_bf16(need_param(h, a + names[sct], d, d), d, ga.v.data());
+      auto build = [&](const std::vector<int>& order) {
+        std::vector<__nv_bfloat16> w;
+        w.reserve(order.size() * static_cast<size_t>(d) * d);
+        for (int hd = 0; hd < H; ++hd)
+          for (int sct : order)
+            w.insert(w.end(), t[sct].begin() + static_cast<size_t>(hd) * dk * d,
+                     t[sct].begin() + static_cast<size_t>(hd + 1) * dk * d);
+        return h.upload(w);
+      };
+      L.w_all = build({kSecQ, kSecV, kSecK, kSecG});
+      L.w_kv = build({kSecK, kSecV});
+      L.w_qg = build({kSecQ, kSecG});
     }
     L.w_o = h.upload(transpose_bf16(need_param(h, a + "wo", d, d), d, nullptr));
     {  // SwishGLU up: interleave 32-column blocks [gate_j | up_j], ffn pre-norm gain folded
@@ -271,28 +281,29 @@ static void finalize(Handle& h) {
     L.in_buf = cur;
     L.q_buf = lp.q_identity ? cur : 1 - cur;
     cur = L.q_buf;
-    // GEMM tile widths
-    L.bn_full = std::min(256, 4 * d);
-    L.bn_half = std::min(256, 2 * d);
-    L.bn_up = 0;
-    for (int bn = 256; bn >= 64; bn -= 64)
-      if ((2 * m) % bn == 0) {
-        L.bn_up = bn;
-        break;
-      }
-    if (!L.bn_up) throw ConfigError("unsupported ffn_dim: 2*ffn_dim must be divisible by 64");
+    // GEMM tile widths (weight-stationary: BN x K weight slice resident in smem)
+    auto pick_bn = [&](int N, int K, int chunk) {
+      for (int bn = 256; bn >= chunk; bn /= 2)
+        if (N % bn == 0 && bn % chunk == 0 && gemm_plan(K, bn).a_stages >= 2) return bn;
+      throw ConfigError("unsupported GEMM shape N=" + std::to_string(N) + " K=" + std::to_string(K));
+    };
+    L.bn_full = pick_bn(4 * d, d, 4 * dk);
+    L.bn_half = pick_bn(2 * d, d, 2 * dk);
+    L.bn_o = pick_bn(d, d, 32);
+    L.bn_up = pick_bn(2 * m, d, 64);
+    L.bn_down = pick_bn(d, m, 32);
     // TMA descriptors (sized for max_batch; launches use the call's batch)
     const uint64_t Mkv = static_cast<uint64_t>(h.Bmax) * L.Rkv, Mq = static_cast<uint64_t>(h.Bmax) * L.Rq;
     L.tmA_in = make_tmap_2d(h.X[L.in_buf], Mkv, d, d, 128, 64, 128);
     L.tmA_q = make_tmap_2d(h.X[L.q_buf], Mq, d, d, 128, 64, 128);
-    L.tmB_qgkv = make_tmap_2d(L.w_qgkv, 4 * d, d, d, L.bn_full, 64, 128);
-    L.tmB_qg = make_tmap_2d(L.w_qgkv, 2 * d, d, d, L.bn_half, 64, 128);
-    L.tmB_kv = make_tmap_2d(L.w_qgkv + static_cast<size_t>(2) * d * d, 2 * d, d, d, L.bn_half, 64, 128);
+    L.tmB_all = make_tmap_2d(L.w_all, 4 * d, d, d, L.bn_full, 64, 128);
+    L.tmB_qg = make_tmap_2d(L.w_qg, 2 * d, d, d, L.bn_half, 64, 128);
+    L.tmB_kv = make_tmap_2d(L.w_kv, 2 * d, d, d, L.bn_half, 64, 128);
     L.tmA_hg = make_tmap_2d(h.Hg, Mq, d, d, 128, 64, 128);
-    L.tmB_o = make_tmap_2d(L.w_o, d, d, d, d, 64, 128);
+    L.tmB_o = make_tmap_2d(L.w_o, d, d, d, L.bn_o, 64, 128);
     L.tmB_up = make_tmap_2d(L.w_up, 2 * m, d, d, L.bn_up, 64, 128);
     L.tmA_hid = make_tmap_2d(h.hid, Mq, m, m, 128, 64, 128);
-    L.tmB_down = make_tmap_2d(L.w_down, d, m, m, d, 64, 128);
+    L.tmB_down = make_tmap_2d(L.w_down, d, m, m, L.bn_down, 64, 128);
     {
       const uint64_t BH = static_cast<uint64_t>(h.Bmax) * H;
       uint64_t dq[3] = {static_cast<uint64_t>(dk), static_cast<uint64_t>(L.Rq), BH};
@@ -327,16 +338,17 @@ static void check_launch(const char* what) {
 template <class Epi>
 static void launch_gemm(Handle& h, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K,
                         int BN, const Epi& epi) {
-  static bool attr = false;
-  if (!attr) {
+  static uint32_t attr_bytes = 0;
+  const GemmPlan gp = gemm_plan(K, BN);
+  if (N % BN || gp.a_stages < 2) throw RuntimeFailure("gemm: unsupported tile plan");
+  if (gp.smem_bytes > attr_bytes) {
     CK(cudaFuncSetAttribute(k_gemm_bf16<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(kGemmSmemBytes)));
-    attr = true;
+                            static_cast<int>(gp.smem_bytes)));
+    attr_bytes = gp.smem_bytes;
   }
-  if (N % BN) throw RuntimeFailure("gemm: N not divisible by BN");
-  const int tiles = ((M + kGemmBM - 1) / kGemmBM) * (N / BN);
-  const int grid = gemm_grid(tiles, N / BN, h.num_sms);
-  k_gemm_bf16<Epi><<<grid, kGemmThreads, kGemmSmemBytes, h.stream>>>(A, B, M, N, K, BN, epi);
+  const int num_m = (M + kGemmBM - 1) / kGemmBM;
+  const int grid = gemm_grid(num_m, N / BN, h.num_sms);
+  k_gemm_bf16<Epi><<<grid, kGemmThreads, gp.smem_bytes, h.stream>>>(A, B, M, N, K, BN, gp.a_stages, epi);
   check_launch("gemm");
   ++h.launches;
 }
@@ -387,13 +399,17 @@ static void launch_attention(Handle& h, const LayerDev& L, const LayerPlan& lp, 
 
 template <int DK>
 static void launch_qkvg_dk(Handle& h, const LayerDev& L, const CUtensorMap& A, const CUtensorMap& Bm,
-                           int M, int N, int BN, int R, const int* sec, const float* ss,
+                           int M, int N, int BN, int R, const std::vector<int>& order, const float4* ss,
                            const int32_t* pos) {
   EpiQKVG<DK> e;
   e.d = h.d;
   e.H = h.H;
   e.R = R;
-  e.sec_packed = sec[0] | (sec[1] << 4) | (sec[2] << 8) | (sec[3] << 12);
+  const int ns = static_cast<int>(order.size());
+  for (int ci = 0; ci < N / DK && ci < 64; ++ci) {
+    e.csec[ci] = static_cast<uint8_t>(order[ci % ns]);
+    e.chead[ci] = static_cast<uint8_t>(ci / ns);
+  }
   e.inv_d = 1.f / static_cast<float>(h.d);
   e.ss = ss;
   e.gain_q = L.gain_q;
@@ -411,7 +427,9 @@ static void launch_qkvg_dk(Handle& h, const LayerDev& L, const CUtensorMap& A, c
 }
 
 static void launch_qkvg(Handle& h, const LayerDev& L, const CUtensorMap& A, const CUtensorMap& Bm,
-                        int M, int N, int BN, int R, const int* sec, const float* ss, const int32_t* pos) {
+                        int M, int N, int BN, int R, const std::vector<int>& sec, const float4* ss,
+                        const int32_t* pos) {
+  if (N / h.dk > 64) throw ConfigError("unsupported: more than 64 head chunks per projection");
   switch (h.dk) {
     case 16: launch_qkvg_dk<16>(h, L, A, Bm, M, N, BN, R, sec, ss, pos); break;
     case 32: launch_qkvg_dk<32>(h, L, A, Bm, M, N, BN, R, sec, ss, pos); break;
@@ -497,33 +515,30 @@ static void run_layer(Handle& h, int l, int B, bool attn_only = false) {
   const LayerPlan& lp = h.plan.layers[l];
   const int d = h.d;
   __nv_bfloat16* Xin = h.X[L.in_buf];
-  float* SSin = h.SS[L.in_buf];
+  float4* SSin = h.SS[L.in_buf];
   __nv_bfloat16* Xq = h.X[L.q_buf];
-  float* SSq = h.SS[L.q_buf];
+  float4* SSq = h.SS[L.q_buf];
   if (lp.q_identity) {
-    const int sec[4] = {kSecQ, kSecG, kSecK, kSecV};
-    launch_qkvg(h, L, L.tmA_in, L.tmB_qgkv, B * L.Rkv, 4 * d, L.bn_full, L.Rkv, sec, SSin, L.pos_kv);
+    launch_qkvg(h, L, L.tmA_in, L.tmB_all, B * L.Rkv, 4 * d, L.bn_full, L.Rkv,
+                {kSecQ, kSecV, kSecK, kSecG}, SSin, L.pos_kv);
   } else {
     const int rows = B * L.Rq;
     k_gather_rows<<<(rows + 7) / 8, 256, 0, h.stream>>>(Xin, SSin, Xq, SSq, L.query_rows, B, L.Rkv, L.Rq, d);
     check_launch("gather");
     ++h.launches;
-    const int sec_kv[4] = {kSecK, kSecV, 0, 0};
-    launch_qkvg(h, L, L.tmA_in, L.tmB_kv, B * L.Rkv, 2 * d, L.bn_half, L.Rkv, sec_kv, SSin, L.pos_kv);
-    const int sec_qg[4] = {kSecQ, kSecG, 0, 0};
-    launch_qkvg(h, L, L.tmA_q, L.tmB_qg, B * L.Rq, 2 * d, L.bn_half, L.Rq, sec_qg, SSq, L.pos_q);
+    launch_qkvg(h, L, L.tmA_in, L.tmB_kv, B * L.Rkv, 2 * d, L.bn_half, L.Rkv, {kSecK, kSecV}, SSin,
+                L.pos_kv);
+    launch_qkvg(h, L, L.tmA_q, L.tmB_qg, B * L.Rq, 2 * d, L.bn_half, L.Rq, {kSecQ, kSecG}, SSq, L.pos_q);
   }
   stage_mark(h, "L" + std::to_string(l) + ".qkvg");
   launch_attention(h, L, lp, B);
   stage_mark(h, "L" + std::to_string(l) + ".attention");
-  CK(cudaMemsetAsync(SSq, 0, static_cast<size_t>(B) * L.Rq * sizeof(float), h.stream));
   EpiResid eo;
   eo.resid = attn_only ? nullptr : Xq;
   eo.out = attn_only ? h.Qb : Xq;  // Q buffer is dead after attention
-  eo.ss_out = SSq;
+  eo.ss_out = reinterpret_cast<float*>(SSq);
   eo.d = d;
-  eo.ss_atomic = 0;
-  launch_gemm(h, L.tmA_hg, L.tmB_o, B * L.Rq, d, d, d, eo);
+  launch_gemm(h, L.tmA_hg, L.tmB_o, B * L.Rq, d, d, L.bn_o, eo);
   stage_mark(h, "L" + std::to_string(l) + ".wo");
   if (attn_only) return;
   EpiSwiGLU eu;
@@ -533,14 +548,12 @@ static void run_layer(Handle& h, int l, int B, bool attn_only = false) {
   eu.m = h.m;
   launch_gemm(h, L.tmA_q, L.tmB_up, B * L.Rq, 2 * h.m, d, L.bn_up, eu);
   stage_mark(h, "L" + std::to_string(l) + ".ffn_up");
-  CK(cudaMemsetAsync(SSq, 0, static_cast<size_t>(B) * L.Rq * sizeof(float), h.stream));
   EpiResid ed;
   ed.resid = Xq;
   ed.out = Xq;
-  ed.ss_out = SSq;
+  ed.ss_out = reinterpret_cast<float*>(SSq);
   ed.d = d;
-  ed.ss_atomic = 0;
-  launch_gemm(h, L.tmA_hid, L.tmB_down, B * L.Rq, d, h.m, d, ed);
+  launch_gemm(h, L.tmA_hid, L.tmB_down, B * L.Rq, d, h.m, L.bn_down, ed);
   stage_mark(h, "L" + std::to_string(l) + ".ffn_down");
 }
 
@@ -805,15 +818,15 @@ int sort_attention_forward(SortHandle p, int layer, int32_t batch, const float* 
     const LayerDev& L = h->layers[layer];
     const size_t n_in = static_cast<size_t>(batch) * L.Rkv * h->d;
     std::vector<__nv_bfloat16> xb(n_in);
-    std::vector<float> ss(static_cast<size_t>(batch) * L.Rkv, 0.f);
+    std::vector<float4> ss(static_cast<size_t>(batch) * L.Rkv, make_float4(0.f, 0.f, 0.f, 0.f));
     for (size_t i = 0; i < n_in; ++i) {
       xb[i] = f2bf(x[i]);
       const float f = __bfloat162float(xb[i]);
-      ss[i / h->d] += f * f;
+      ss[i / h->d].x += f * f;
     }
     begin_timing(*h);
     CK(cudaMemcpyAsync(h->X[L.in_buf], xb.data(), n_in * 2, cudaMemcpyHostToDevice, h->stream));
-    CK(cudaMemcpyAsync(h->SS[L.in_buf], ss.data(), ss.size() * 4, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(h->SS[L.in_buf], ss.data(), ss.size() * sizeof(float4), cudaMemcpyHostToDevice, h->stream));
     run_layer(*h, layer, batch, /*attn_only=*/true);
     const size_t n_out = static_cast<size_t>(batch) * L.Rq * h->d;
     std::vector<__nv_bfloat16> ob(n_out);

@@ -46,7 +46,7 @@ struct TokParams {
   const int32_t* cand_item;
   // outputs
   __nv_bfloat16* x;      // [B, L, d]
-  float* ss;             // [B, L] sum of squares of the bf16 token row
+  float4* ss;            // [B, L] sum of squares of the bf16 token row (slot 0 of 4)
   int32_t* hist_time;    // [B, H] or null
   int32_t* err;          // device error flags
   // geometry
@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
         dst[1] = make_int4(packed[4], packed[5], packed[6], packed[7]);
       }
     }
-    if (valid) p.ss[out_row] = ss_out;
+    if (valid) p.ss[out_row] = make_float4(ss_out, 0.f, 0.f, 0.f);
     tc_fence_before();
     __syncthreads();
   }
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
       }
 #pragma unroll
       for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-      if (lane == 0) p.ss[row] = ss;
+      if (lane == 0) p.ss[row] = make_float4(ss, 0.f, 0.f, 0.f);
     }
   }
   __syncthreads();

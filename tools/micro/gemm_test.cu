@@ -12,11 +12,12 @@ using namespace sortk;
 
 struct StoreF32 {
   static constexpr int kChunk = 32;
+  static constexpr int kMaxParts = 1 << 30;
   float* C;
   int ldc;
   __device__ void prologue(uint8_t*, int, int) const {}
   template <class Wait>
-  __device__ void run(uint8_t*, Wait&& wait, uint32_t tbase, int row, int n0, int c0, int c1, bool valid) const {
+  __device__ void run(uint8_t*, Wait&& wait, uint32_t tbase, int row, int n0, int c0, int c1, bool valid, int, int) const {
     wait();
     for (int c = c0; c < c1; c += 32) {
       float v[32];
@@ -43,10 +44,10 @@ static int run(int M, int N, int K, int BN) {
   CUtensorMap tB = make_tmap_2d(dB, N, K, K, BN, 64, 128);
   StoreF32 epi; epi.C = dC; epi.ldc = N;
   auto kfn = k_gemm_bf16<StoreF32>;
-  cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmemBytes);
-  int tiles = ((M + 127) / 128) * (N / BN);
-  int grid = gemm_grid(tiles, N / BN, 148);
-  kfn<<<grid, kGemmThreads, kGemmSmemBytes>>>(tA, tB, M, N, K, BN, epi);
+  GemmPlan gp = gemm_plan(K, BN);
+  cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gp.smem_bytes);
+  int grid = gemm_grid((M + 127) / 128, N / BN, 148);
+  kfn<<<grid, kGemmThreads, gp.smem_bytes>>>(tA, tB, M, N, K, BN, gp.a_stages, epi);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { printf("CUDA error %s\n", cudaGetErrorString(e)); return 1; }
   std::vector<float> hC((size_t)M * N);
@@ -61,7 +62,7 @@ static int run(int M, int N, int K, int BN) {
   // timing at this shape
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  for (int it = 0; it < 10; ++it) kfn<<<grid, kGemmThreads, kGemmSmemBytes>>>(tA, tB, M, N, K, BN, epi);
+  for (int it = 0; it < 10; ++it) kfn<<<grid, kGemmThreads, gp.smem_bytes>>>(tA, tB, M, N, K, BN, gp.a_stages, epi);
   cudaEventRecord(e1); cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= 10;
   printf("GEMM M=%d N=%d K=%d BN=%d maxerr=%.3g %s  %.3f ms  %.1f TFLOP/s\n", M, N, K, BN, maxerr,
@@ -76,8 +77,10 @@ int main() {
   fails += run(300, 512, 256, 256);
   fails += run(128, 160, 160, 160);
   fails += run(1000, 1280, 256, 256);
-  fails += run(257, 256, 640, 256);
+  fails += run(257, 256, 640, 128);
   fails += run(513, 128, 256, 128);
+  fails += run(70000, 1024, 256, 256);
+  fails += run(20000, 256, 640, 128);
   printf(fails ? "SOME FAILED\n" : "ALL PASS\n");
   return fails;
 }
