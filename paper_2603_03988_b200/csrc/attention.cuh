@@ -21,19 +21,19 @@
 // sort_block_attention entry) the online-max path with a deferred O rescale is used
 // (streaming-softmax recurrence of block_attention.hpp:104-122).
 //
-// Roles (192 threads, persistent, 2 CTAs per SM):
+// Roles (320 threads, persistent, 2 CTAs per SM):
 //   warp 0      TMA: Q tile per item (double-buffered), K tile (128 x dk) and V^T tile
 //               (dk x 128) per kv tile (double-buffered); runs ahead across items
 //   warp 1      MMA: S = Q K^T (M=128, N=128, K=dk) into TMEM; P V (M=128, N=dk, K=128)
-//   warps 2..5  softmax: thread <-> query row; tcgen05.ld of S, exp2 on MUFU, P written
-//               bf16 into the SW128 A-operand layout in smem; gate + store at item end
+//   warps 2..9  softmax: thread <-> (query row, S half); tcgen05.ld of S, exp2 on MUFU, P
+//               written bf16 into the SW128 A-operand layout in smem; gate + store at item end
 #pragma once
 
 #include "gemm.cuh"
 
 namespace sortk {
 
-constexpr int kAttnThreads = 192;
+constexpr int kAttnThreads = 320;
 constexpr float kFixedRefMax = 40.f;  // 2^(-2*40*log2 e) ~ 2e-35 > FLT_MIN
 
 template <int DK>
@@ -50,7 +50,8 @@ struct AttnSmem {
   static constexpr uint32_t oV = oK + 2 * kKStride;
   static constexpr uint32_t oP = oV + 2 * kVStride;
   static constexpr uint32_t oBar = oP + kPBytes;
-  static constexpr uint32_t oTiles = oBar + 32 * 8;  // int32 tile tables follow
+  static constexpr uint32_t oRed = oBar + 32 * 8;      // softmax cross-warp reduction scratch
+  static constexpr uint32_t oTiles = oRed + 3 * 1024;  // int32 tile tables follow
   static constexpr uint32_t bytes(int n_tile_ints) { return oTiles + 4u * n_tile_ints + 1024; }
 };
 
@@ -88,13 +89,13 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   uint64_t* q_empty = bars + 2;   // [2]
   uint64_t* kv_full = bars + 4;   // [2]
   uint64_t* kv_empty = bars + 6;  // [2]
-  uint64_t* s_full = bars + 8;
-  uint64_t* s_free = bars + 9;
-  uint64_t* p_full = bars + 10;
-  uint64_t* p_empty = bars + 11;
-  uint64_t* o_full = bars + 12;   // [2]
-  uint64_t* o_empty = bars + 14;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint64_t* s_full = bars + 8;    // [2] halves: columns [0,64) and [64,128) of S
+  uint64_t* s_free = bars + 10;   // [2]
+  uint64_t* p_full = bars + 12;
+  uint64_t* p_empty = bars + 13;
+  uint64_t* o_full = bars + 14;   // [2]
+  uint64_t* o_empty = bars + 16;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 18);
   int32_t* s_off = reinterpret_cast<int32_t*>(smem + S::oTiles);
   int32_t* s_order = s_off + (a.n_qtiles + 1);
   int32_t* s_code = s_order + a.n_qtiles;
@@ -115,12 +116,12 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
       mbar_init(&o_full[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 128);
     }
-    mbar_init(s_full, 1);
-    mbar_init(s_free, 128);
-    mbar_init(p_full, 128);
+    mbar_init(p_full, 256);
     mbar_init(p_empty, 1);
-    mbar_init(o_empty, 128);
+    mbar_init(o_empty, 256);
     mbar_fence_init();
   }
   if (warp == 1) tmem_alloc(tslot, 256);
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t id_s = umma_idesc_bf16(128, 128);
+      const uint32_t id_s = umma_idesc_bf16(128, 64);
       const uint32_t id_o = umma_idesc_bf16(128, DK);
       constexpr uint32_t qsw = DK * 2;  // Q/K rows are DK*2 bytes = the swizzle span
       const uint32_t sp = smem_u32(smem + S::oP);
@@ -175,14 +176,19 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
         for (int j = 0; j < n_t; ++j, ++g) {
           const int st = g & 1;
           mbar_wait_sleep(&kv_full[st], (g >> 1) & 1);
-          mbar_wait_sleep(s_free, (g & 1) ^ 1);
-          tc_fence_after();
           const uint32_t sk = smem_u32(smem + S::oK + st * S::kKStride);
+          // S = Q K^T in two N=64 halves, each issued as soon as the softmax has drained
+          // the same half of the previous tile.
 #pragma unroll
-          for (int k = 0; k < DK / 16; ++k)
-            mma_bf16_ss(tS, umma_sdesc_kmajor(sq + k * 32, qsw), umma_sdesc_kmajor(sk + k * 32, qsw),
-                        id_s, k > 0 ? 1u : 0u);
-          mma_commit(s_full);
+          for (int hf = 0; hf < 2; ++hf) {
+            mbar_wait_sleep(&s_free[hf], (g & 1) ^ 1);
+            tc_fence_after();
+#pragma unroll
+            for (int k = 0; k < DK / 16; ++k)
+              mma_bf16_ss(tS + hf * 64, umma_sdesc_kmajor(sq + k * 32, qsw),
+                          umma_sdesc_kmajor(sk + hf * 64 * DK * 2 + k * 32, qsw), id_s, k > 0 ? 1u : 0u);
+            mma_commit(&s_full[hf]);
+          }
           if (j == n_t - 1) mma_commit(&q_empty[qb]);
           mbar_wait_sleep(p_full, g & 1);
           tc_fence_after();
@@ -216,16 +222,23 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
     }
   } else {
     // ------------------------------------------------------------ softmax warps
-    // Each 32-column chunk of a partial tile is classified warp-uniformly: fully visible
-    // for all 32 rows of the warp (no mask arithmetic), fully masked (skipped: P = 0, no
-    // exp, no TMEM read), or mixed (per-element mask).
+    // Eight warps: warp pair (w, w+4) shares TMEM lane quarter w % 4 (query rows) and
+    // splits each kv tile by S half: half hf = (warp - 2) / 4 owns columns [64hf, 64hf+64)
+    // and, at item end, output columns [hf*DK/2, (hf+1)*DK/2). With the fixed reference
+    // the halves are independent until the row sums are combined (lo + hi, fixed order).
+    // Each 32-column chunk is classified warp-uniformly: fully visible for all 32 rows of
+    // the warp (no mask arithmetic), fully masked (skipped: P = 0, no exp, no TMEM read),
+    // or mixed (per-element mask from a visibility bitmask).
     const int quarter = warp & 3;
+    const int hf = (warp - 2) >> 2;
     const int r = quarter * 32 + lane;  // row within the q-tile == TMEM lane
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
     const float NEG_INF = -__int_as_float(0x7f800000);
     const float sl2 = a.scale_log2;
     const float2 sl2v = make_float2(sl2, sl2);
-    uint8_t* prow = smem + S::oP + r * 128;
+    uint8_t* prow = smem + S::oP + hf * 16384 + r * 128;  // this half's SW128 atom of the P row
+    float* s_red = reinterpret_cast<float*>(smem + S::oRed);  // [2][2][128] maxima, [2][128] sums
+    constexpr int DH = DK / 2;
     int g = 0, li = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++li) {
       const int rank = it / a.BH, bh = it - rank * a.BH;
@@ -233,27 +246,18 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
       const int q0 = qt * 128;
       const int t_begin = s_off[qt], n_t = s_off[qt + 1] - t_begin;
       const int4 meta = a.rowmeta[q0 + r];
-      const int qrow = q0 + r;
-      const int b = bh / a.H, hh = bh - b * a.H;
-      const size_t off = static_cast<size_t>(b * a.Rq + qrow) * a.d + hh * DK;
-      int4 gate[DK / 8];  // prefetch the gate row early
-      if (qrow < a.Rq) {
-#pragma unroll
-        for (int i = 0; i < DK / 8; ++i) gate[i] = reinterpret_cast<const int4*>(a.g + off)[i];
-      }
       float m = NEG_INF, alpha_prev = 0.f;  // online mode only
-      float2 lsum[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                        make_float2(0.f, 0.f)};
-      float acc[kFixed ? 1 : DK];
+      float2 lsum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      float acc[kFixed ? 1 : DH];
 #pragma unroll
-      for (int i = 0; i < (kFixed ? 1 : DK); ++i) acc[i] = 0.f;
+      for (int i = 0; i < (kFixed ? 1 : DH); ++i) acc[i] = 0.f;
       for (int j = 0; j < n_t; ++j, ++g) {
         const int code = s_code[t_begin + j];
-        const int c0 = (code & 0xffff) * 128;
-        uint32_t full_mask = 0xF, none_mask = 0;
+        const int c0 = (code & 0xffff) * 128 + hf * 64;  // first kv column of this half
+        uint32_t full_mask = 0x3, none_mask = 0;
         if ((code >> 16) != 0) {
 #pragma unroll
-          for (int cb = 0; cb < 4; ++cb) {
+          for (int cb = 0; cb < 2; ++cb) {
             const int cs = c0 + cb * 32, ce = cs + 31;
             const bool f = meta.x <= cs && meta.y >= ce;
             const bool n = (meta.y < cs || meta.x > ce) && !(meta.z >= cs && meta.z <= ce);
@@ -261,7 +265,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
             if (__all_sync(0xffffffffu, n)) none_mask |= 1u << cb;
           }
         }
-        mbar_wait(s_full, g & 1);
+        mbar_wait(&s_full[hf], g & 1);
         tc_fence_after();
         float ref;  // exp2 reference in the scaled domain
         float alpha = 1.f, m_new = m;
@@ -270,10 +274,10 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
         } else {
           float mx4[4] = {NEG_INF, NEG_INF, NEG_INF, NEG_INF};
 #pragma unroll
-          for (int cb = 0; cb < 4; ++cb) {
+          for (int cb = 0; cb < 2; ++cb) {
             if (none_mask & (1u << cb)) continue;
             uint32_t rr[32];
-            tmem_ld_32x32b_x32(tS + lane_off + cb * 32, rr);
+            tmem_ld_32x32b_x32(tS + lane_off + hf * 64 + cb * 32, rr);
             tmem_ld_wait();
             if (full_mask & (1u << cb)) {
 #pragma unroll
@@ -285,23 +289,27 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
                 mx4[i & 3] = fmaxf(mx4[i & 3], (bits >> i) & 1u ? __uint_as_float(rr[i]) : NEG_INF);
             }
           }
-          m_new = fmaxf(m, fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])));
+          // combine the two halves' maxima (double-buffered slot by tile parity)
+          float* slot = s_red + (g & 1) * 256;
+          slot[hf * 128 + r] = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+          named_bar_sync(1 + quarter, 64);
+          m_new = fmaxf(m, fmaxf(slot[r], slot[128 + r]));
           ref = m_new == NEG_INF ? 0.f : m_new * sl2;
           alpha = ex2_approx(m * sl2 - ref);  // m = -inf -> 0
 #pragma unroll
-          for (int u = 0; u < 4; ++u) lsum[u] = make_float2(lsum[u].x * alpha, lsum[u].y * alpha);
+          for (int u = 0; u < 2; ++u) lsum[u] = make_float2(lsum[u].x * alpha, lsum[u].y * alpha);
         }
         const float2 nref = make_float2(-ref, -ref);
         mbar_wait(p_empty, (g & 1) ^ 1);  // PV of the previous tile has consumed P
 #pragma unroll
-        for (int cb = 0; cb < 4; ++cb) {
+        for (int cb = 0; cb < 2; ++cb) {
           uint32_t w[16];
           if (none_mask & (1u << cb)) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) w[i] = 0u;
           } else {
             uint32_t rr[32];
-            tmem_ld_32x32b_x32(tS + lane_off + cb * 32, rr);
+            tmem_ld_32x32b_x32(tS + lane_off + hf * 64 + cb * 32, rr);
             tmem_ld_wait();
             if (full_mask & (1u << cb)) {
 #pragma unroll
@@ -309,7 +317,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
                 const float2 x = ffma2(make_float2(__uint_as_float(rr[2 * i]), __uint_as_float(rr[2 * i + 1])),
                                        sl2v, nref);
                 const float2 p = make_float2(ex2_approx(x.x), ex2_approx(x.y));
-                lsum[i & 3] = fadd2(lsum[i & 3], p);
+                lsum[i & 1] = fadd2(lsum[i & 1], p);
                 w[i] = pack_bf16x2(p.x, p.y);
               }
             } else {
@@ -321,51 +329,53 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
                 x.x = (bits >> (2 * i)) & 1u ? x.x : NEG_INF;
                 x.y = (bits >> (2 * i + 1)) & 1u ? x.y : NEG_INF;
                 const float2 p = make_float2(ex2_approx(x.x), ex2_approx(x.y));
-                lsum[i & 3] = fadd2(lsum[i & 3], p);
+                lsum[i & 1] = fadd2(lsum[i & 1], p);
                 w[i] = pack_bf16x2(p.x, p.y);
               }
             }
           }
 #pragma unroll
           for (int h4 = 0; h4 < 4; ++h4) {
-            const int ch = cb * 4 + h4;  // 16-byte chunk index 0..15 along the 128 kv columns
-            const int atom = ch >> 3, cc = ch & 7;
-            *reinterpret_cast<int4*>(prow + atom * 16384 + ((cc ^ (r & 7)) << 4)) =
+            const int cc = cb * 4 + h4;  // 16-byte chunk index 0..7 within this half's atom
+            *reinterpret_cast<int4*>(prow + ((cc ^ (r & 7)) << 4)) =
                 make_int4(w[4 * h4], w[4 * h4 + 1], w[4 * h4 + 2], w[4 * h4 + 3]);
           }
         }
         tc_fence_before();
-        mbar_arrive(s_free);  // S fully consumed: the next QK^T may overwrite it
+        mbar_arrive(&s_free[hf]);  // this half of S consumed: next QK^T half may overwrite it
         fence_proxy_async_smem();
         mbar_arrive(p_full);
         if constexpr (!kFixed) {
           m = m_new;
-          if (j > 0) {  // deferred: acc <- acc * alpha_{j-1} + O_{j-1}
+          if (j > 0) {  // deferred: acc <- acc * alpha_{j-1} + O_{j-1} (this warp's DK/2 columns)
             const int pb = (g - 1) & 1;
             mbar_wait(&o_full[pb], ((g - 1) >> 1) & 1);
             tc_fence_after();
-            float o[DK];
-            tmem_row_chunk<DK>(tO0 + pb * DK + lane_off, o);
+            float o[DH];
+            tmem_row_chunk<DH>(tO0 + pb * DK + hf * DH + lane_off, o);
             tc_fence_before();
-            const float2 av = make_float2(alpha_prev, alpha_prev);
 #pragma unroll
-            for (int i = 0; i < DK; i += 2) {
-              const float2 t2 = ffma2(make_float2(acc[i], acc[i + 1]), av, make_float2(o[i], o[i + 1]));
-              acc[i] = t2.x;
-              acc[i + 1] = t2.y;
-            }
+            for (int i = 0; i < DH; ++i) acc[i] = fmaf(acc[i], alpha_prev, o[i]);
           }
           alpha_prev = alpha;
         }
       }
-      // ---- item epilogue: O / l * gate -> bf16
-      float o[DK];
+      // ---- item epilogue: O / l * gate -> bf16, this warp's DK/2 output columns
+      const int qrow = q0 + r;
+      const int b = bh / a.H, hh = bh - b * a.H;
+      const size_t off = static_cast<size_t>(b * a.Rq + qrow) * a.d + hh * DK + hf * DH;
+      int4 gate[DH / 8];
+      if (qrow < a.Rq) {
 #pragma unroll
-      for (int i = 0; i < DK; ++i) o[i] = 0.f;
+        for (int i = 0; i < DH / 8; ++i) gate[i] = reinterpret_cast<const int4*>(a.g + off)[i];
+      }
+      float o[DH];
+#pragma unroll
+      for (int i = 0; i < DH; ++i) o[i] = 0.f;
       if constexpr (kFixed) {
         mbar_wait(&o_full[0], li & 1);
         tc_fence_after();
-        tmem_row_chunk<DK>(tO0 + lane_off, o);
+        tmem_row_chunk<DH>(tO0 + hf * DH + lane_off, o);
         tc_fence_before();
         mbar_arrive(o_empty);
       } else {
@@ -373,18 +383,21 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
           const int pb = (g - 1) & 1;
           mbar_wait(&o_full[pb], ((g - 1) >> 1) & 1);
           tc_fence_after();
-          tmem_row_chunk<DK>(tO0 + pb * DK + lane_off, o);
+          tmem_row_chunk<DH>(tO0 + pb * DK + hf * DH + lane_off, o);
           tc_fence_before();
 #pragma unroll
-          for (int i = 0; i < DK; ++i) o[i] = acc[i] * alpha_prev + o[i];
+          for (int i = 0; i < DH; ++i) o[i] = fmaf(acc[i], alpha_prev, o[i]);
         }
       }
-      const float l = (lsum[0].x + lsum[0].y) + (lsum[1].x + lsum[1].y) +
-                      (lsum[2].x + lsum[2].y) + (lsum[3].x + lsum[3].y);
+      float* sl = s_red + 512;  // [2][128] partial row sums
+      sl[hf * 128 + r] = (lsum[0].x + lsum[0].y) + (lsum[1].x + lsum[1].y);
+      named_bar_sync(1 + quarter, 64);
+      const float l = sl[r] + sl[128 + r];
+      named_bar_sync(1 + quarter, 64);  // both partners read before the next item overwrites
       if (qrow < a.Rq) {
         const float invl = 1.f / l;
 #pragma unroll
-        for (int i = 0; i < DK / 8; ++i) {
+        for (int i = 0; i < DH / 8; ++i) {
           const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gate[i]);
           uint32_t w[4];
 #pragma unroll

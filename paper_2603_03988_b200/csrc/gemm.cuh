@@ -191,7 +191,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 // Loads kChunk accumulator columns [c, c+kChunk) of this thread's row as fp32.
 template <int kChunk>
 __device__ __forceinline__ void tmem_row_chunk(uint32_t taddr, float (&v)[kChunk]) {
-  if constexpr (kChunk == 16) {
+  if constexpr (kChunk == 8) {
+    uint32_t r[8];
+    tmem_ld_32x32b_x8(taddr, r);
+    tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+  } else if constexpr (kChunk == 16) {
     uint32_t r[16];
     tmem_ld_32x32b_x16(taddr, r);
     tmem_ld_wait();
@@ -204,7 +210,7 @@ __device__ __forceinline__ void tmem_row_chunk(uint32_t taddr, float (&v)[kChunk
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
   } else {
-    static_assert(kChunk == 64, "chunk must be 16, 32 or 64");
+    static_assert(kChunk == 64, "chunk must be 8, 16, 32 or 64");
     uint32_t r[32];
     tmem_ld_32x32b_x32(taddr, r);
     uint32_t r2[32];
