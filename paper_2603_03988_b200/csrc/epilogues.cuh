@@ -83,14 +83,17 @@ struct EpiQKVG {
   template <class Wait>
   __device__ __forceinline__ void run(uint8_t* smem, Wait&& wait, uint32_t tbase, int row, int n0,
                                       int c0, int c1, bool valid, int, int) const {
-    const float* sg = reinterpret_cast<const float*>(smem);
+    const uint32_t sg = smem_u32(smem);
     const int b = row / R, r = row - b * R;
-    // Sections are d columns wide and BN divides 4d, so a tile's chunks may span sections;
-    // prefetch what any Q/K chunk of this row needs (1/rms, this position's cos/sin).
-    float inv = 0.f;
+    // Per-row prefetch before the accumulator wait: 1/rms of the input row and the cos/sin
+    // of this row's position (shared by every Q/K head chunk of the row).
+    float inv = 0.f, eps_eff = 0.f;
     float2 cs[DK / 2];
     if (valid) {
-      inv = row_inv_rms(row_ss(ss, row), inv_d);
+      const float ssum = row_ss(ss, row);
+      inv = row_inv_rms(ssum, inv_d);
+      // QKNorm of v = inv * acc: v * rsqrt(mean(v^2) + eps) = acc * rsqrt(mean(acc^2) + eps / inv^2)
+      eps_eff = 1e-6f * (ssum * inv_d + 1e-6f);
       const float2* rp = rope + static_cast<size_t>(pos[r]) * (DK / 2);
 #pragma unroll
       for (int j = 0; j < DK / 2; ++j) cs[j] = __ldg(rp + j);
@@ -103,19 +106,30 @@ struct EpiQKVG {
       const int ci = (n0 + c) / DK;
       const int s = csec[ci];
       const int head = chead[ci];
-#pragma unroll
-      for (int i = 0; i < DK; ++i) v[i] *= inv;
       if (s == kSecQ || s == kSecK) {
-        float m = 0.f;
-#pragma unroll
-        for (int i = 0; i < DK; ++i) m = fmaf(v[i], v[i], m);
-        const float qi = rsqrtf(m * (1.f / DK) + 1e-6f);
-        const float* gn = sg + (s == kSecQ ? 0 : H * DK) + head * DK;
+        float2 m2 = make_float2(0.f, 0.f);
 #pragma unroll
         for (int j = 0; j < DK / 2; ++j) {
-          const float x0 = v[2 * j] * qi * gn[2 * j], x1 = v[2 * j + 1] * qi * gn[2 * j + 1];
-          v[2 * j] = cs[j].x * x0 - cs[j].y * x1;
-          v[2 * j + 1] = cs[j].y * x0 + cs[j].x * x1;
+          const float2 x = make_float2(v[2 * j], v[2 * j + 1]);
+          m2 = ffma2(x, x, m2);
+        }
+        const float qi = rsqrtf((m2.x + m2.y) * (1.f / DK) + eps_eff);
+        const float2 qi2 = make_float2(qi, qi);
+        const uint32_t gaddr = sg + ((s == kSecQ ? 0 : H * DK) + head * DK) * 4;
+#pragma unroll
+        for (int j4 = 0; j4 < DK / 4; ++j4) {
+          const float4 g4 = lds_f32x4(gaddr + j4 * 16);
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int j = 2 * j4 + u;
+            const float2 x = fmul2(fmul2(make_float2(v[2 * j], v[2 * j + 1]), qi2),
+                                   u ? make_float2(g4.z, g4.w) : make_float2(g4.x, g4.y));
+            // (o0, o1) = (c, s) * x0 + (-s, c) * x1   (rope.hpp:35-36)
+            const float2 o = ffma2(make_float2(-cs[j].y, cs[j].x), make_float2(x.y, x.y),
+                                   fmul2(cs[j], make_float2(x.x, x.x)));
+            v[2 * j] = o.x;
+            v[2 * j + 1] = o.y;
+          }
         }
         __nv_bfloat16* dst =
             s == kSecQ ? q + (static_cast<size_t>(b * H + head) * Rq + r) * DK
@@ -124,10 +138,11 @@ struct EpiQKVG {
       } else if (s == kSecV) {
         __nv_bfloat16* dst = vt + static_cast<size_t>(b * H + head) * DK * Rkv_pad + r;
 #pragma unroll
-        for (int i = 0; i < DK; ++i) dst[static_cast<size_t>(i) * Rkv_pad] = __float2bfloat16_rn(v[i]);
+        for (int i = 0; i < DK; ++i) dst[static_cast<size_t>(i) * Rkv_pad] = __float2bfloat16_rn(v[i] * inv);
       } else {
+        const float hinv = 0.5f * inv;
 #pragma unroll
-        for (int i = 0; i < DK; ++i) v[i] = fast_sigmoid(v[i]);
+        for (int i = 0; i < DK; ++i) v[i] = fmaf(0.5f, tanh_approx(hinv * v[i]), 0.5f);
         store_bf16_row(g + static_cast<size_t>(row) * d + head * DK, v, DK);
       }
     }

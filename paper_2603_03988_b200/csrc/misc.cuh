@@ -25,18 +25,22 @@ __global__ void k_gather_rows(const __nv_bfloat16* __restrict__ src, const float
 
 // Final RMSNorm + ranking head on candidate rows, fp32 (
 // PAPER.md:243 keeps the head in fp32): h = relu(xn W1 + b1), z = h W2 + b2,
-// p = sigmoid(z) for {click, cart, purchase}. 32 candidate rows per CTA.
-constexpr int kHeadRows = 32;
+// p = sigmoid(z) for {click, cart, purchase}.
+// 64 candidate rows per CTA, 256 threads: warp w owns rows [8w, 8w+8), lane l owns hidden
+// columns {l, l+32, ...} (CPT = dh/32 of them), so each thread keeps an 8 x CPT register
+// tile; xn is staged transposed in smem (broadcast reads), W1 streams coalesced from L2.
+// The 3 logits are reduced across the 32 lanes with shuffles in a fixed order.
+constexpr int kHeadRows = 64;
 constexpr int kHeadThreads = 256;
 
+template <int CPT>
 __global__ void __launch_bounds__(kHeadThreads)
     k_head(const __nv_bfloat16* __restrict__ x, const float4* __restrict__ ss, int R, int N, int total,
-           int d, int dh, const float* __restrict__ gain, const float* __restrict__ w1,
+           int d, const float* __restrict__ gain, const float* __restrict__ w1,
            const float* __restrict__ b1, const float* __restrict__ w2, const float* __restrict__ b2,
            float* __restrict__ probs, float* __restrict__ logits) {
-  extern __shared__ float hsm[];
-  float* xs = hsm;                  // [32][d]
-  float* hs = hsm + kHeadRows * d;  // [32][dh]
+  constexpr int dh = CPT * 32;
+  extern __shared__ float xs[];  // [d][kHeadRows] transposed normalised rows
   const int e0 = blockIdx.x * kHeadRows;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   for (int rr = warp; rr < kHeadRows; rr += kHeadThreads / 32) {
@@ -46,47 +50,67 @@ __global__ void __launch_bounds__(kHeadThreads)
       const size_t row = static_cast<size_t>(b) * R + (R - N) + j;
       const float4 sp = ss[row];
       const float inv = rsqrtf(((sp.x + sp.y) + (sp.z + sp.w)) / static_cast<float>(d) + 1e-6f);
-      for (int c = lane; c < d; c += 32) xs[rr * d + c] = __bfloat162float(x[row * d + c]) * inv * gain[c];
+      for (int c = lane; c < d; c += 32) xs[c * kHeadRows + rr] = __bfloat162float(x[row * d + c]) * inv * gain[c];
     } else {
-      for (int c = lane; c < d; c += 32) xs[rr * d + c] = 0.f;
+      for (int c = lane; c < d; c += 32) xs[c * kHeadRows + rr] = 0.f;
     }
   }
   __syncthreads();
-  for (int c = t; c < dh; c += kHeadThreads) {
-    float acc[kHeadRows];
+  float acc[8][CPT];
 #pragma unroll
-    for (int r = 0; r < kHeadRows; ++r) acc[r] = 0.f;
-    for (int k = 0; k < d; ++k) {
-      const float w = __ldg(w1 + static_cast<size_t>(k) * dh + c);
+  for (int r = 0; r < 8; ++r)
 #pragma unroll
-      for (int r = 0; r < kHeadRows; ++r) acc[r] = fmaf(xs[r * d + k], w, acc[r]);
-    }
-    const float bb = b1[c];
+    for (int c = 0; c < CPT; ++c) acc[r][c] = 0.f;
+  const float* xw = xs + warp * 8;
+#pragma unroll 4
+  for (int k = 0; k < d; ++k) {
+    const float4 xa = *reinterpret_cast<const float4*>(xw + k * kHeadRows);
+    const float4 xb = *reinterpret_cast<const float4*>(xw + k * kHeadRows + 4);
+    const float xr[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+    float wv[CPT];
 #pragma unroll
-    for (int r = 0; r < kHeadRows; ++r) hs[r * dh + c] = fmaxf(acc[r] + bb, 0.f);
+    for (int c = 0; c < CPT; ++c) wv[c] = __ldg(w1 + static_cast<size_t>(k) * dh + c * 32 + lane);
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) acc[r][c] = fmaf(xr[r], wv[c], acc[r][c]);
   }
-  __syncthreads();
-  for (int rr = warp; rr < kHeadRows; rr += kHeadThreads / 32) {
-    const int e = e0 + rr;
-    float z0 = 0.f, z1 = 0.f, z2 = 0.f;
-    for (int c = lane; c < dh; c += 32) {
-      const float h = hs[rr * dh + c];
-      z0 = fmaf(h, w2[c * 3 + 0], z0);
-      z1 = fmaf(h, w2[c * 3 + 1], z1);
-      z2 = fmaf(h, w2[c * 3 + 2], z2);
-    }
+  float z[8][3];
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      z0 += __shfl_xor_sync(0xffffffffu, z0, o);
-      z1 += __shfl_xor_sync(0xffffffffu, z1, o);
-      z2 += __shfl_xor_sync(0xffffffffu, z2, o);
+  for (int r = 0; r < 8; ++r) z[r][0] = z[r][1] = z[r][2] = 0.f;
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) {
+    const int col = c * 32 + lane;
+    const float bb = b1[col];
+    const float wa = w2[col * 3 + 0], wb = w2[col * 3 + 1], wc = w2[col * 3 + 2];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const float hv = fmaxf(acc[r][c] + bb, 0.f);
+      z[r][0] = fmaf(hv, wa, z[r][0]);
+      z[r][1] = fmaf(hv, wb, z[r][1]);
+      z[r][2] = fmaf(hv, wc, z[r][2]);
     }
-    if (lane == 0 && e < total) {
-      const float z[3] = {z0 + b2[0], z1 + b2[1], z2 + b2[2]};
+  }
+#pragma unroll
+  for (int r = 0; r < 8; ++r)
+#pragma unroll
+    for (int o = 0; o < 3; ++o)
+#pragma unroll
+      for (int sft = 16; sft; sft >>= 1) z[r][o] += __shfl_xor_sync(0xffffffffu, z[r][o], sft);
+  if (lane < 8) {
+    float zz[3];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+      if (r == lane)
+#pragma unroll
+        for (int o = 0; o < 3; ++o) zz[o] = z[r][o];
+    const int e = e0 + warp * 8 + lane;
+    if (e < total) {
       for (int o = 0; o < 3; ++o) {
-        if (logits) logits[e * 3 + o] = z[o];
+        const float v = zz[o] + b2[o];
+        if (logits) logits[e * 3 + o] = v;
         // rankformer::sigmoid branch structure (common.hpp:29-35) in fp32
-        probs[e * 3 + o] = z[o] >= 0.f ? 1.f / (1.f + expf(-z[o])) : expf(z[o]) / (1.f + expf(z[o]));
+        probs[e * 3 + o] = v >= 0.f ? 1.f / (1.f + expf(-v)) : expf(v) / (1.f + expf(v));
       }
     }
   }

@@ -592,15 +592,29 @@ static void forward_device(Handle& h, int B) {
   for (int l = 0; l < h.cfg.layers; ++l) run_layer(h, l, B);
   const LayerDev& last = h.layers.back();
   const int total = B * h.cfg.n_cand;
-  const size_t hsmem = static_cast<size_t>(kHeadRows) * (h.d + h.dh) * sizeof(float);
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(k_head, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-    attr = true;
+  const size_t hsmem = static_cast<size_t>(kHeadRows) * h.d * sizeof(float);
+  const int hgrid = (total + kHeadRows - 1) / kHeadRows;
+  const LayerDev& lst = last;
+#define SORT_HEAD(CPT)                                                                          \
+  case CPT: {                                                                                   \
+    static bool attr = false;                                                                   \
+    if (!attr) {                                                                                \
+      CK(cudaFuncSetAttribute(k_head<CPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024)); \
+      attr = true;                                                                              \
+    }                                                                                           \
+    k_head<CPT><<<hgrid, kHeadThreads, hsmem, h.stream>>>(                                      \
+        h.X[lst.q_buf], h.SS[lst.q_buf], lst.Rq, h.cfg.n_cand, total, h.d, h.head_gain,         \
+        h.head_w1, h.head_b1, h.head_w2, h.head_b2, h.probs, h.logits);                         \
+    break;                                                                                      \
   }
-  k_head<<<(total + kHeadRows - 1) / kHeadRows, kHeadThreads, hsmem, h.stream>>>(
-      h.X[last.q_buf], h.SS[last.q_buf], last.Rq, h.cfg.n_cand, total, h.d, h.dh, h.head_gain,
-      h.head_w1, h.head_b1, h.head_w2, h.head_b2, h.probs, h.logits);
+  switch (h.dh / 32) {
+    SORT_HEAD(1)
+    SORT_HEAD(2)
+    SORT_HEAD(4)
+    SORT_HEAD(8)
+    default: throw ConfigError("unsupported head_hidden (must be 32, 64, 128 or 256)");
+  }
+#undef SORT_HEAD
   check_launch("head");
   ++h.launches;
   stage_mark(h, "head");
@@ -677,7 +691,8 @@ int sort_create(const SortConfig* cfg, int device, SortHandle* out) {
     h->dk = cfg->model_dim / cfg->heads;
     h->m = cfg->ffn_dim;
     h->dh = cfg->head_hidden > 0 ? cfg->head_hidden : cfg->model_dim;
-    if (h->dh % 32 || h->dh > 1024) throw ConfigError("unsupported head_hidden");
+    if (h->dh != 32 && h->dh != 64 && h->dh != 128 && h->dh != 256)
+      throw ConfigError("unsupported head_hidden (must be 32, 64, 128 or 256)");
     h->L0 = h->plan.L0;
     h->Bmax = cfg->max_batch;
     int ndev = 0;
