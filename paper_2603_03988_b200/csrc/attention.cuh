@@ -22,8 +22,8 @@
 // (streaming-softmax recurrence of block_attention.hpp:104-122).
 //
 // Roles (320 threads, persistent, 2 CTAs per SM):
-//   warp 0      TMA: Q tile per item (double-buffered), K tile (128 x dk) and V^T tile
-//               (dk x 128) per kv tile (double-buffered); runs ahead across items
+//   warp 0      TMA: Q tile per item (double-buffered), K and V tiles (128 x dk each)
+//               per kv tile (double-buffered); runs ahead across items
 //   warp 1      MMA: S = Q K^T (M=128, N=128, K=dk) into TMEM; P V (M=128, N=dk, K=128)
 //   warps 2..9  softmax: thread <-> (query row, S half); tcgen05.ld of S, exp2 on MUFU, P
 //               written bf16 into the SW128 A-operand layout in smem; gate + store at item end
@@ -40,7 +40,7 @@ template <int DK>
 struct AttnSmem {
   static constexpr uint32_t kQBytes = 128 * DK * 2;
   static constexpr uint32_t kKBytes = 128 * DK * 2;
-  static constexpr uint32_t kVBytes = DK * 128 * 2;  // two [DK x 64] SW128 boxes
+  static constexpr uint32_t kVBytes = 128 * DK * 2;  // V tile row-major [128 kv x DK], like K
   static constexpr uint32_t kPBytes = 128 * 128 * 2;
   static constexpr uint32_t kQStride = ((kQBytes + 1023) / 1024) * 1024;
   static constexpr uint32_t kKStride = ((kKBytes + 1023) / 1024) * 1024;
@@ -153,16 +153,15 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
           mbar_wait_sleep(&kv_empty[st], ph ^ 1);
           mbar_arrive_expect_tx(&kv_full[st], S::kKBytes + S::kVBytes);
           tma_load_3d(smem + S::oK + st * S::kKStride, &tmK, &kv_full[st], 0, kv0, bh);
-          uint8_t* vdst = smem + S::oV + st * S::kVStride;
-          tma_load_3d(vdst, &tmV, &kv_full[st], kv0, 0, bh);
-          tma_load_3d(vdst + DK * 128, &tmV, &kv_full[st], kv0 + 64, 0, bh);
+          tma_load_3d(smem + S::oV + st * S::kVStride, &tmV, &kv_full[st], 0, kv0, bh);
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       const uint32_t id_s = umma_idesc_bf16(128, 64);
-      const uint32_t id_o = umma_idesc_bf16(128, DK);
+      // PV: A = P (K-major), B = V tile read MN-major (dk contiguous): idesc bit 16.
+      const uint32_t id_o = umma_idesc_bf16(128, DK) | (1u << 16);
       constexpr uint32_t qsw = DK * 2;  // Q/K rows are DK*2 bytes = the swizzle span
       const uint32_t sp = smem_u32(smem + S::oP);
       int g = 0, li = 0;
@@ -206,9 +205,10 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const uint32_t pa = sp + (kk >> 2) * 16384 + (kk & 3) * 32;
-            const uint32_t va = sv + (kk >> 2) * (DK * 128) + (kk & 3) * 32;
+            // MN-major swizzled V: 8-row groups SBO = 8 * DK * 2 bytes apart; K = 16 rows per MMA
+            const uint32_t va = sv + kk * 16 * (DK * 2);
             const uint32_t accum = kFixed ? ((j | kk) != 0) : (kk != 0);
-            mma_bf16_ss(tO, umma_sdesc_kmajor(pa, 128), umma_sdesc_kmajor(va, 128), id_o, accum);
+            mma_bf16_ss(tO, umma_sdesc_kmajor(pa, 128), umma_sdesc_kmajor(va, qsw), id_o, accum);
           }
           mma_commit(p_empty);
           mma_commit(&kv_empty[st]);

@@ -47,7 +47,7 @@ __device__ __forceinline__ float fast_sigmoid(float x) {
 // Column chunk = one head of one section. Q,K: 1/rms -> QKNorm (per-head RMSNorm
 // with gain, :111-114) -> interleaved RoPE at the row's ORIGINAL position
 // (rope.hpp:27-38, cos/sin from an fp64 host table) -> bf16 [B*H, R, DK].
-// V: -> bf16 V^T [B*H, DK, Rkv_pad] (the K-major B operand of PV).
+// V: -> bf16 [B*H, R, DK] like K (read MN-major as the B operand of PV).
 // G: -> sigmoid (:125-126) -> bf16 [B*R, d].
 enum : int { kSecQ = 0, kSecK = 1, kSecV = 2, kSecG = 3 };
 
@@ -68,9 +68,9 @@ struct EpiQKVG {
   const int32_t* pos;   // [R]
   __nv_bfloat16* q;
   __nv_bfloat16* k;
-  __nv_bfloat16* vt;
+  __nv_bfloat16* v;
   __nv_bfloat16* g;
-  int Rq, Rkv, Rkv_pad;
+  int Rq, Rkv;
 
   __device__ __forceinline__ void prologue(uint8_t* smem, int tid, int nthreads) const {
     float* sg = reinterpret_cast<float*>(smem);
@@ -136,9 +136,9 @@ struct EpiQKVG {
                        : k + (static_cast<size_t>(b * H + head) * Rkv + r) * DK;
         store_bf16_row(dst, v, DK);
       } else if (s == kSecV) {
-        __nv_bfloat16* dst = vt + static_cast<size_t>(b * H + head) * DK * Rkv_pad + r;
 #pragma unroll
-        for (int i = 0; i < DK; ++i) dst[static_cast<size_t>(i) * Rkv_pad] = __float2bfloat16_rn(v[i] * inv);
+        for (int i = 0; i < DK; ++i) v[i] *= inv;
+        store_bf16_row(this->v + (static_cast<size_t>(b * H + head) * Rkv + r) * DK, v, DK);
       } else {
         const float hinv = 0.5f * inv;
 #pragma unroll

@@ -45,7 +45,7 @@ struct LayerDev {
                 *w_up = nullptr, *w_down = nullptr;
   float *gain_q = nullptr, *gain_k = nullptr;
   int in_buf = 0, q_buf = 0;
-  int Rq = 0, Rkv = 0, Rkv_pad = 0;
+  int Rq = 0, Rkv = 0;
   int bn_full = 0, bn_half = 0, bn_up = 0, bn_o = 0, bn_down = 0;
   float logit_bound = 0.f;  // QKNorm logit bound (0 = unknown -> online-max softmax)
   CUtensorMap tmA_in, tmA_q, tmB_all, tmB_qg, tmB_kv, tmA_hg, tmB_o, tmB_up, tmA_hid, tmB_down;
@@ -75,7 +75,7 @@ struct Handle {
   // workspace
   __nv_bfloat16* X[2] = {nullptr, nullptr};
   float4* SS[2] = {nullptr, nullptr};  // per-row sum-of-squares partials
-  __nv_bfloat16 *Qb = nullptr, *Kb = nullptr, *Vt = nullptr, *Gb = nullptr, *Hg = nullptr,
+  __nv_bfloat16 *Qb = nullptr, *Kb = nullptr, *Vb = nullptr, *Gb = nullptr, *Hg = nullptr,
                 *hid = nullptr;
   float *probs = nullptr, *logits = nullptr;
   int32_t* err = nullptr;
@@ -189,10 +189,7 @@ static void finalize(Handle& h) {
   }
   h.Qb = h.dalloc<__nv_bfloat16>(rows_max * d);
   h.Kb = h.dalloc<__nv_bfloat16>(rows_max * d);
-  const int Rkv_pad_max = (h.L0 + 7) / 8 * 8;
-  const size_t vt_elems = static_cast<size_t>(h.Bmax) * H * dk * Rkv_pad_max;
-  h.Vt = h.dalloc<__nv_bfloat16>(vt_elems);
-  CK(cudaMemset(h.Vt, 0, vt_elems * sizeof(__nv_bfloat16)));
+  h.Vb = h.dalloc<__nv_bfloat16>(rows_max * d);
   h.Gb = h.dalloc<__nv_bfloat16>(rows_max * d);
   h.Hg = h.dalloc<__nv_bfloat16>(rows_max * d);
   h.hid = h.dalloc<__nv_bfloat16>(rows_max * m);
@@ -277,7 +274,6 @@ static void finalize(Handle& h) {
     L.query_rows = h.upload(lp.query_rows);
     L.Rq = lp.l_q;
     L.Rkv = lp.l_kv;
-    L.Rkv_pad = (lp.l_kv + 7) / 8 * 8;
     L.in_buf = cur;
     L.q_buf = lp.q_identity ? cur : 1 - cur;
     cur = L.q_buf;
@@ -313,10 +309,7 @@ static void finalize(Handle& h) {
       uint64_t dkd[3] = {static_cast<uint64_t>(dk), static_cast<uint64_t>(L.Rkv), BH};
       uint64_t skd[2] = {static_cast<uint64_t>(dk) * 2, static_cast<uint64_t>(L.Rkv) * dk * 2};
       L.tmK = make_tmap_bf16(h.Kb, 3, dkd, skd, bq, dk * 2);
-      uint64_t dv[3] = {static_cast<uint64_t>(L.Rkv_pad), static_cast<uint64_t>(dk), BH};
-      uint64_t sv[2] = {static_cast<uint64_t>(L.Rkv_pad) * 2, static_cast<uint64_t>(L.Rkv_pad) * dk * 2};
-      uint32_t bv[3] = {64, static_cast<uint32_t>(dk), 1};
-      L.tmV = make_tmap_bf16(h.Vt, 3, dv, sv, bv, 128);
+      L.tmV = make_tmap_bf16(h.Vb, 3, dkd, skd, bq, dk * 2);
     }
   }
   // ---- head (fp32)
@@ -418,11 +411,10 @@ static void launch_qkvg_dk(Handle& h, const LayerDev& L, const CUtensorMap& A, c
   e.pos = pos;
   e.q = h.Qb;
   e.k = h.Kb;
-  e.vt = h.Vt;
+  e.v = h.Vb;
   e.g = h.Gb;
   e.Rq = L.Rq;
   e.Rkv = L.Rkv;
-  e.Rkv_pad = L.Rkv_pad;
   launch_gemm(h, A, Bm, M, N, h.d, BN, e);
 }
 
@@ -880,7 +872,6 @@ int sort_block_attention(int32_t nh, int32_t l_q, int32_t l_kv, int32_t dk, cons
     LayerDev L;
     L.Rq = l_q;
     L.Rkv = l_kv;
-    L.Rkv_pad = (l_kv + 7) / 8 * 8;
     std::vector<int4> meta(static_cast<size_t>(lp.n_qtiles) * 128, make_int4(0, -1, -1, 0));
     for (int r = 0; r < l_q; ++r) meta[r] = make_int4(lo[r], hi[r], self_idx[r], 0);
     L.rowmeta = h.upload(meta);
@@ -894,12 +885,7 @@ int sort_block_attention(int32_t nh, int32_t l_q, int32_t l_kv, int32_t dk, cons
     };
     h.Qb = up(q, static_cast<size_t>(nh) * l_q * dk);
     h.Kb = up(k, static_cast<size_t>(nh) * l_kv * dk);
-    std::vector<__nv_bfloat16> vt(static_cast<size_t>(nh) * dk * L.Rkv_pad, f2bf(0.f));
-    for (int b = 0; b < nh; ++b)
-      for (int c = 0; c < l_kv; ++c)
-        for (int i = 0; i < dk; ++i)
-          vt[(static_cast<size_t>(b) * dk + i) * L.Rkv_pad + c] = f2bf(v[(static_cast<size_t>(b) * l_kv + c) * dk + i]);
-    h.Vt = h.upload(vt);
+    h.Vb = up(v, static_cast<size_t>(nh) * l_kv * dk);
     h.Gb = h.upload(std::vector<__nv_bfloat16>(static_cast<size_t>(nh) * l_q * dk, f2bf(1.f)));
     h.Hg = h.dalloc<__nv_bfloat16>(static_cast<size_t>(nh) * l_q * dk);
     uint64_t dq[3] = {static_cast<uint64_t>(dk), static_cast<uint64_t>(l_q), static_cast<uint64_t>(nh)};
@@ -909,10 +895,7 @@ int sort_block_attention(int32_t nh, int32_t l_q, int32_t l_kv, int32_t dk, cons
     uint64_t dkd[3] = {static_cast<uint64_t>(dk), static_cast<uint64_t>(l_kv), static_cast<uint64_t>(nh)};
     uint64_t skd[2] = {static_cast<uint64_t>(dk) * 2, static_cast<uint64_t>(l_kv) * dk * 2};
     L.tmK = make_tmap_bf16(h.Kb, 3, dkd, skd, bq, dk * 2);
-    uint64_t dv[3] = {static_cast<uint64_t>(L.Rkv_pad), static_cast<uint64_t>(dk), static_cast<uint64_t>(nh)};
-    uint64_t sv[2] = {static_cast<uint64_t>(L.Rkv_pad) * 2, static_cast<uint64_t>(L.Rkv_pad) * dk * 2};
-    uint32_t bv[3] = {64, static_cast<uint32_t>(dk), 1};
-    L.tmV = make_tmap_bf16(h.Vt, 3, dv, sv, bv, 128);
+    L.tmV = make_tmap_bf16(h.Vb, 3, dkd, skd, bq, dk * 2);
     launch_attention(h, L, lp, nh);
     std::vector<__nv_bfloat16> ob(static_cast<size_t>(nh) * l_q * dk);
     CK(cudaMemcpyAsync(ob.data(), h.Hg, ob.size() * 2, cudaMemcpyDeviceToHost, h.stream));
