@@ -3,8 +3,9 @@
 //
 // Interface used by k_gemm_bf16:
 //   prologue(smem, tid, nthreads)  once per CTA, before the role split (fill scratch smem)
-//   run(smem, wait, tbase, row, n0, c0, c1, valid, part, nparts)
-//       issue this row's global prefetches, call wait() (accumulator ready), then consume
+//   run(smem, side, wait, tbase, row, n0, c0, c1, valid, part, nparts)
+//       issue this row's global prefetches, call wait() (accumulator + side data ready), then
+//       read the tile's per-row side data from `side` (see kSide in gemm.cuh) and consume
 //       accumulator columns [c0, c1) of the tile (absolute columns n0 + c). `part` numbers
 //       the (n-slice, column half) this thread covers out of `nparts` per row.
 //
@@ -24,6 +25,23 @@ __device__ __forceinline__ float row_ss(const float4* ss, int row) {
   const float4 p = ss[row];
   return (p.x + p.y) + (p.z + p.w);
 }
+// Row statistics of tile row `lrow` from the side buffer (TMA-staged copy of the float4 row).
+__device__ __forceinline__ float side_row_ss(const uint8_t* side, int lrow) {
+  const float4 p = lds_f32x4(smem_u32(side + lrow * 16));
+  return (p.x + p.y) + (p.z + p.w);
+}
+// 16-byte chunk j of tile row `lrow` of a TMA-swizzled fp32 side table with `floats`
+// floats per row (boxes of <= 32 floats, swizzle span = box row bytes).
+template <int floats>
+__device__ __forceinline__ float4 side_row_chunk(const uint8_t* base, int lrow, int j) {
+  constexpr int bf = floats < 32 ? floats : 32;  // floats per box row
+  constexpr int S = bf * 4;                      // box row bytes == swizzle span
+  constexpr int per = S / 16;                    // 16-byte chunks per box row
+  const int box = j / per, jj = j % per;
+  const int sw = ((lrow * S) >> 7) & (per - 1);
+  return lds_f32x4(smem_u32(base + box * 128 * S + lrow * S + ((jj ^ sw) << 4)));
+}
+
 __device__ __forceinline__ float row_inv_rms(float ss, float inv_d) {
   return rsqrtf(ss * inv_d + 1e-6f);  // norm.hpp:23-24 (eps = kRmsEps, norm.hpp:8)
 }
@@ -55,17 +73,16 @@ template <int DK>
 struct EpiQKVG {
   static constexpr int kChunk = DK;
   static constexpr int kMaxParts = 1 << 30;  // does not produce row statistics
+  static constexpr int kSide = 3;            // row statistics + RoPE rows
+  static constexpr int kRopeFloats = DK;     // DK/2 (cos, sin) pairs
   int d, H, R;      // R: rows per request of the A operand
   // Column chunk ci (= col / DK) of this GEMM's N dimension -> section / head. The host
   // interleaves the weight rows head by head ([Q_h V_h K_h G_h] ...) so every n-slice,
   // and each half of it, carries the same epilogue work.
   uint8_t csec[64], chead[64];
   float inv_d;
-  const float4* ss;
   const float* gain_q;  // [H*DK]
   const float* gain_k;
-  const float2* rope;   // [(max_pos+1) * DK/2] (cos, sin)
-  const int32_t* pos;   // [R]
   __nv_bfloat16* q;
   __nv_bfloat16* k;
   __nv_bfloat16* v;
@@ -81,24 +98,28 @@ struct EpiQKVG {
   }
 
   template <class Wait>
-  __device__ __forceinline__ void run(uint8_t* smem, Wait&& wait, uint32_t tbase, int row, int n0,
-                                      int c0, int c1, bool valid, int, int) const {
+  __device__ __forceinline__ void run(uint8_t* smem, uint8_t* side, Wait&& wait, uint32_t tbase,
+                                      int row, int n0, int c0, int c1, bool valid, int, int) const {
     const uint32_t sg = smem_u32(smem);
     const int b = row / R, r = row - b * R;
-    // Per-row prefetch before the accumulator wait: 1/rms of the input row and the cos/sin
-    // of this row's position (shared by every Q/K head chunk of the row).
-    float inv = 0.f, eps_eff = 0.f;
-    float2 cs[DK / 2];
-    if (valid) {
-      const float ssum = row_ss(ss, row);
-      inv = row_inv_rms(ssum, inv_d);
-      // QKNorm of v = inv * acc: v * rsqrt(mean(v^2) + eps) = acc * rsqrt(mean(acc^2) + eps / inv^2)
-      eps_eff = 1e-6f * (ssum * inv_d + 1e-6f);
-      const float2* rp = rope + static_cast<size_t>(pos[r]) * (DK / 2);
-#pragma unroll
-      for (int j = 0; j < DK / 2; ++j) cs[j] = __ldg(rp + j);
-    }
+    const int lrow = row & (kGemmBM - 1);
     wait();
+    // Per-row side data (staged by the TMA producer): the input row's statistics -> 1/rms,
+    // and the cos/sin pairs of the row's position (shared by every Q/K head of the row).
+    const float ssum = side_row_ss(side, lrow);
+    const float inv = row_inv_rms(ssum, inv_d);
+    // QKNorm of v = inv * acc: v * rsqrt(mean(v^2) + eps) = acc * rsqrt(mean(acc^2) + eps / inv^2)
+    const float eps_eff = 1e-6f * (ssum * inv_d + 1e-6f);
+    float2 cs[DK / 2];
+    {
+      const uint8_t* rb = side + kSideStatBytes;
+#pragma unroll
+      for (int j = 0; j < DK / 4; ++j) {
+        const float4 t4 = side_row_chunk<DK>(rb, lrow, j);
+        cs[2 * j] = make_float2(t4.x, t4.y);
+        cs[2 * j + 1] = make_float2(t4.z, t4.w);
+      }
+    }
     for (int c = c0; c < c1; c += DK) {
       float v[DK];
       tmem_row_chunk<DK>(tbase + c, v);
@@ -158,6 +179,8 @@ struct EpiQKVG {
 struct EpiResid {
   static constexpr int kChunk = 32;
   static constexpr int kMaxParts = 4;
+  static constexpr int kSide = 0;
+  static constexpr int kRopeFloats = 0;
   const __nv_bfloat16* resid;
   __nv_bfloat16* out;
   float* ss_out;   // [rows, 4] partial sums of squares
@@ -166,8 +189,8 @@ struct EpiResid {
   __device__ __forceinline__ void prologue(uint8_t*, int, int) const {}
 
   template <class Wait>
-  __device__ __forceinline__ void run(uint8_t*, Wait&& wait, uint32_t tbase, int row, int n0,
-                                      int c0, int c1, bool valid, int part, int nparts) const {
+  __device__ __forceinline__ void run(uint8_t*, uint8_t*, Wait&& wait, uint32_t tbase, int row,
+                                      int n0, int c0, int c1, bool valid, int part, int nparts) const {
     int4 rv[16];  // up to 128 columns
     const int nq = (c1 - c0) / 8;
     if (valid && resid) {
@@ -224,7 +247,8 @@ struct EpiResid {
 struct EpiSwiGLU {
   static constexpr int kChunk = 64;
   static constexpr int kMaxParts = 1 << 30;
-  const float4* ss;
+  static constexpr int kSide = 1;  // row statistics
+  static constexpr int kRopeFloats = 0;
   float inv_d;
   __nv_bfloat16* hidden;
   int m;
@@ -232,10 +256,10 @@ struct EpiSwiGLU {
   __device__ __forceinline__ void prologue(uint8_t*, int, int) const {}
 
   template <class Wait>
-  __device__ __forceinline__ void run(uint8_t*, Wait&& wait, uint32_t tbase, int row, int n0,
-                                      int c0, int c1, bool valid, int, int) const {
-    const float inv = valid ? row_inv_rms(row_ss(ss, row), inv_d) : 0.f;
+  __device__ __forceinline__ void run(uint8_t*, uint8_t* side, Wait&& wait, uint32_t tbase, int row,
+                                      int n0, int c0, int c1, bool valid, int, int) const {
     wait();
+    const float inv = row_inv_rms(side_row_ss(side, row & (kGemmBM - 1)), inv_d);
     for (int c = c0; c < c1; c += 64) {
       float v[64];
       tmem_row_chunk<64>(tbase + c, v);

@@ -11,7 +11,8 @@
 // the accumulator after tcgen05.ld.
 //
 // Roles (384 threads, 1 CTA per SM):
-//   warp 0       TMA producer   (weight slice once, then A tiles 128x64 per stage, SW128)
+//   warp 0       TMA producer   (weight slice once, then per tile: the epilogue's per-row side
+//                                data (row statistics, RoPE rows) and the A tiles 128x64, SW128)
 //   warp 1       MMA issuer     (one thread; 4 x tcgen05.mma K=16 per stage)
 //   warp 2       TMEM allocator (2 accumulator stages x 256 columns)
 //   warps 4..11  epilogue       (thread <-> accumulator row; TMEM lane quarter = warp % 4;
@@ -32,18 +33,29 @@ constexpr uint32_t kGemmABytes = kGemmBM * kGemmBK * 2;  // 16 KB per A stage
 constexpr uint32_t kGemmEpiSmem = 8192;                  // per-kernel epilogue scratch
 constexpr uint32_t kGemmSmemMax = 227 * 1024;
 
+// Per-row side data streamed by the TMA producer next to each A tile (double-buffered):
+//   bit 0  row statistics: float4 per row (sum-of-squares partials)     128 x 16 B
+//   bit 1  RoPE rows: kRopeFloats fp32 per row (cos/sin pairs of the row's position)
+// Epilogues declare `kSide` and `kRopeFloats`; side_bytes() is one buffer.
+constexpr uint32_t kSideStatBytes = 128 * 16;
+__host__ __device__ constexpr uint32_t side_bytes(int side, int rope_floats) {
+  return side == 0 ? 0u
+                   : (((side & 1) ? kSideStatBytes : 0u) + ((side & 2) ? 128u * rope_floats * 4u : 0u) +
+                      1023u) / 1024u * 1024u;
+}
+
 // Shared-memory plan of one weight-stationary GEMM launch.
 struct GemmPlan {
   int BN, num_k, a_stages;
   uint32_t b_bytes, smem_bytes;
 };
 
-__host__ __device__ inline GemmPlan gemm_plan(int K, int BN) {
+__host__ __device__ inline GemmPlan gemm_plan(int K, int BN, uint32_t side_buf_bytes = 0) {
   GemmPlan p;
   p.BN = BN;
   p.num_k = (K + kGemmBK - 1) / kGemmBK;
   p.b_bytes = static_cast<uint32_t>(BN) * kGemmBK * 2 * p.num_k;
-  const uint32_t fixed = 1024 + p.b_bytes + kGemmEpiSmem + 256;
+  const uint32_t fixed = 1024 + p.b_bytes + kGemmEpiSmem + 2 * side_buf_bytes + 256;
   int st = fixed < kGemmSmemMax ? static_cast<int>((kGemmSmemMax - fixed) / kGemmABytes) : 0;
   p.a_stages = st > 8 ? 8 : st;
   p.smem_bytes = fixed + p.a_stages * kGemmABytes;
@@ -58,7 +70,12 @@ __host__ __device__ inline GemmPlan gemm_plan(int K, int BN) {
 template <class Epi>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm_bf16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmR,
                 int M, int N, int K, int BN, int a_stages, Epi epi) {
+  constexpr int kSide = Epi::kSide;
+  constexpr uint32_t kSideBuf = side_bytes(Epi::kSide, Epi::kRopeFloats);
+  constexpr int kRopeBoxFloats = Epi::kRopeFloats < 32 ? Epi::kRopeFloats : 32;
+  constexpr int kRopeBoxes = Epi::kRopeFloats / (kRopeBoxFloats > 0 ? kRopeBoxFloats : 1);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -67,13 +84,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint8_t* sB = smem;
   uint8_t* sA = sB + b_box * num_k;
   uint8_t* sEpi = sA + a_stages * kGemmABytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + kGemmEpiSmem);
+  uint8_t* sSide = sEpi + kGemmEpiSmem;  // 2 x kSideBuf (1024-aligned)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sSide + 2 * kSideBuf);
   uint64_t* full = bars;             // [a_stages <= 8]
   uint64_t* empty = bars + 8;        // [8]
   uint64_t* tfull = bars + 16;       // [2]
   uint64_t* tempty = bars + 18;      // [2]
   uint64_t* b_full = bars + 20;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 21);
+  uint64_t* side_full = bars + 21;   // [2]
+  uint64_t* side_empty = bars + 23;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 25);
 
   const int warp = warp_id();
   const int lane = lane_id();
@@ -88,6 +108,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
+    if constexpr (kSide & 1) tma_prefetch_desc(&tmS);
+    if constexpr (kSide & 2) tma_prefetch_desc(&tmR);
     for (int s = 0; s < a_stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -97,6 +119,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_init(&tempty[i], 32 * kGemmEpiWarps);
     }
     mbar_init(b_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&side_full[i], 1);
+      mbar_init(&side_empty[i], 32 * kGemmEpiWarps);
+    }
     mbar_fence_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, 512);
@@ -113,7 +139,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         tma_load_2d(sB + kb * b_box, &tmB, b_full, kb * kGemmBK, nb * BN);
       int s = 0;
       uint32_t ph = 0;
-      for (int mb = m_first; mb < num_m; mb += m_step) {
+      int t = 0;
+      for (int mb = m_first; mb < num_m; mb += m_step, ++t) {
+        if constexpr (kSide != 0) {  // this tile's per-row side data
+          const int sb = t & 1;
+          uint8_t* dst = sSide + sb * kSideBuf;
+          mbar_wait_sleep(&side_empty[sb], ((t >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&side_full[sb], ((kSide & 1) ? kSideStatBytes : 0u) +
+                                                    ((kSide & 2) ? 128u * Epi::kRopeFloats * 4u : 0u));
+          if constexpr (kSide & 1) tma_load_2d(dst, &tmS, &side_full[sb], 0, mb * kGemmBM);
+          if constexpr (kSide & 2) {
+#pragma unroll
+            for (int bx = 0; bx < kRopeBoxes; ++bx)
+              tma_load_2d(dst + ((kSide & 1) ? kSideStatBytes : 0u) + bx * 128 * kRopeBoxFloats * 4, &tmR,
+                          &side_full[sb], bx * kRopeBoxFloats, mb * kGemmBM);
+          }
+        }
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait_sleep(&empty[s], ph ^ 1);
           mbar_arrive_expect_tx(&full[s], kGemmABytes);
@@ -171,14 +212,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint32_t acc_ph = (t >> 1) & 1;
       const int row = mb * kGemmBM + q * 32 + lane;
       const uint32_t tbase = tmem + acc * 256 + (static_cast<uint32_t>(q * 32) << 16);
+      uint8_t* side = sSide + acc * kSideBuf;
       auto wait = [&]() {
+        if constexpr (kSide != 0) mbar_wait(&side_full[acc], acc_ph);
         mbar_wait(&tfull[acc], acc_ph);
         tc_fence_after();
       };
-      epi.run(sEpi, wait, tbase, row, nb * BN, c_begin * Epi::kChunk, c_end * Epi::kChunk, row < M,
-              nb * 2 + half, num_n * 2);
+      epi.run(sEpi, side, wait, tbase, row, nb * BN, c_begin * Epi::kChunk, c_end * Epi::kChunk,
+              row < M, nb * 2 + half, num_n * 2);
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
+      if constexpr (kSide != 0) mbar_arrive(&side_empty[acc]);
     }
   }
   __syncthreads();

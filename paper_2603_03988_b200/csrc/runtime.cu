@@ -50,6 +50,7 @@ struct LayerDev {
   float logit_bound = 0.f;  // QKNorm logit bound (0 = unknown -> online-max softmax)
   CUtensorMap tmA_in, tmA_q, tmB_all, tmB_qg, tmB_kv, tmA_hg, tmB_o, tmB_up, tmA_hid, tmB_down;
   CUtensorMap tmQ, tmK, tmV;
+  CUtensorMap tmRopeKV, tmRopeQ;  // per-row RoPE side tables for the K/V rows and the Q rows
 };
 
 struct Handle {
@@ -75,6 +76,8 @@ struct Handle {
   // workspace
   __nv_bfloat16* X[2] = {nullptr, nullptr};
   float4* SS[2] = {nullptr, nullptr};  // per-row sum-of-squares partials
+  CUtensorMap tmSS[2];                 // the same rows as a TMA side stream (128-row boxes)
+  std::map<std::pair<int, std::vector<int32_t>>, CUtensorMap> rope_tables;
   __nv_bfloat16 *Qb = nullptr, *Kb = nullptr, *Vb = nullptr, *Gb = nullptr, *Hg = nullptr,
                 *hid = nullptr;
   float *probs = nullptr, *logits = nullptr;
@@ -139,6 +142,30 @@ static std::vector<__nv_bfloat16> transpose_bf16(const HostParam& w, int Kpad, c
   return o;
 }
 
+// Per-row RoPE side table for a GEMM over B x R rows whose row r sits at position pos[r]:
+// row b*R + r holds the (cos, sin) pairs of pos[r] (rope.hpp:23-38, fp64 -> fp32), so the
+// TMA producer can stage a tile's rows next to its A tile. Shared by GEMMs with equal (R, pos).
+static const CUtensorMap& rope_table(Handle& h, int R, const std::vector<int32_t>& pos) {
+  auto key = std::make_pair(R, pos);
+  auto it = h.rope_tables.find(key);
+  if (it != h.rope_tables.end()) return it->second;
+  const int dk = h.dk;
+  std::vector<float> one(static_cast<size_t>(R) * dk);
+  for (int r = 0; r < R; ++r)
+    for (int j = 0; j < dk / 2; ++j) {
+      const double freq = std::pow(h.cfg.rope_theta, -2.0 * j / static_cast<double>(dk));
+      const double ang = static_cast<double>(pos[r]) * freq;
+      one[static_cast<size_t>(r) * dk + 2 * j] = static_cast<float>(std::cos(ang));
+      one[static_cast<size_t>(r) * dk + 2 * j + 1] = static_cast<float>(std::sin(ang));
+    }
+  const size_t rows = static_cast<size_t>(h.Bmax) * R;
+  float* dev = h.dalloc<float>(rows * dk);
+  for (int b = 0; b < h.Bmax; ++b)
+    CK(cudaMemcpy(dev + static_cast<size_t>(b) * R * dk, one.data(), one.size() * 4, cudaMemcpyHostToDevice));
+  const int box = std::min(dk, 32);
+  return h.rope_tables[key] = make_tmap_2d_f32(dev, rows, dk, 128, box, box * 4);
+}
+
 static void finalize(Handle& h) {
   const SortConfig& c = h.cfg;
   const int d = h.d, m = h.m, H = h.H, dk = h.dk;
@@ -186,6 +213,7 @@ static void finalize(Handle& h) {
   for (int i = 0; i < 2; ++i) {
     h.X[i] = h.dalloc<__nv_bfloat16>(rows_max * d);
     h.SS[i] = h.dalloc<float4>(rows_max);
+    h.tmSS[i] = make_tmap_2d_f32(h.SS[i], rows_max, 4, 128, 4, 0);
   }
   h.Qb = h.dalloc<__nv_bfloat16>(rows_max * d);
   h.Kb = h.dalloc<__nv_bfloat16>(rows_max * d);
@@ -278,15 +306,16 @@ static void finalize(Handle& h) {
     L.q_buf = lp.q_identity ? cur : 1 - cur;
     cur = L.q_buf;
     // GEMM tile widths (weight-stationary: BN x K weight slice resident in smem)
-    auto pick_bn = [&](int N, int K, int chunk) {
+    auto pick_bn = [&](int N, int K, int chunk, uint32_t side = 0) {
       for (int bn = 256; bn >= chunk; bn /= 2)
-        if (N % bn == 0 && bn % chunk == 0 && gemm_plan(K, bn).a_stages >= 2) return bn;
+        if (N % bn == 0 && bn % chunk == 0 && gemm_plan(K, bn, side).a_stages >= 2) return bn;
       throw ConfigError("unsupported GEMM shape N=" + std::to_string(N) + " K=" + std::to_string(K));
     };
-    L.bn_full = pick_bn(4 * d, d, 4 * dk);
-    L.bn_half = pick_bn(2 * d, d, 2 * dk);
+    const uint32_t qkvg_side = side_bytes(3, dk);
+    L.bn_full = pick_bn(4 * d, d, 4 * dk, qkvg_side);
+    L.bn_half = pick_bn(2 * d, d, 2 * dk, qkvg_side);
     L.bn_o = pick_bn(d, d, 32);
-    L.bn_up = pick_bn(2 * m, d, 64);
+    L.bn_up = pick_bn(2 * m, d, 64, side_bytes(1, 0));
     L.bn_down = pick_bn(d, m, 32);
     // TMA descriptors (sized for max_batch; launches use the call's batch)
     const uint64_t Mkv = static_cast<uint64_t>(h.Bmax) * L.Rkv, Mq = static_cast<uint64_t>(h.Bmax) * L.Rq;
@@ -298,6 +327,8 @@ static void finalize(Handle& h) {
     L.tmA_hg = make_tmap_2d(h.Hg, Mq, d, d, 128, 64, 128);
     L.tmB_o = make_tmap_2d(L.w_o, d, d, d, L.bn_o, 64, 128);
     L.tmB_up = make_tmap_2d(L.w_up, 2 * m, d, d, L.bn_up, 64, 128);
+    L.tmRopeKV = rope_table(h, L.Rkv, lp.pos_kv);
+    L.tmRopeQ = rope_table(h, L.Rq, lp.pos_q);
     L.tmA_hid = make_tmap_2d(h.hid, Mq, m, m, 128, 64, 128);
     L.tmB_down = make_tmap_2d(L.w_down, d, m, m, L.bn_down, 64, 128);
     {
@@ -330,10 +361,13 @@ static void check_launch(const char* what) {
 
 template <class Epi>
 static void launch_gemm(Handle& h, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K,
-                        int BN, const Epi& epi) {
+                        int BN, const Epi& epi, const CUtensorMap* side_stats = nullptr,
+                        const CUtensorMap* side_rope = nullptr) {
   static uint32_t attr_bytes = 0;
-  const GemmPlan gp = gemm_plan(K, BN);
+  const GemmPlan gp = gemm_plan(K, BN, side_bytes(Epi::kSide, Epi::kRopeFloats));
   if (N % BN || gp.a_stages < 2) throw RuntimeFailure("gemm: unsupported tile plan");
+  if (((Epi::kSide & 1) && !side_stats) || ((Epi::kSide & 2) && !side_rope))
+    throw RuntimeFailure("gemm: epilogue side data missing");
   if (gp.smem_bytes > attr_bytes) {
     CK(cudaFuncSetAttribute(k_gemm_bf16<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(gp.smem_bytes)));
@@ -341,7 +375,8 @@ static void launch_gemm(Handle& h, const CUtensorMap& A, const CUtensorMap& B, i
   }
   const int num_m = (M + kGemmBM - 1) / kGemmBM;
   const int grid = gemm_grid(num_m, N / BN, h.num_sms);
-  k_gemm_bf16<Epi><<<grid, kGemmThreads, gp.smem_bytes, h.stream>>>(A, B, M, N, K, BN, gp.a_stages, epi);
+  k_gemm_bf16<Epi><<<grid, kGemmThreads, gp.smem_bytes, h.stream>>>(
+      A, B, side_stats ? *side_stats : A, side_rope ? *side_rope : A, M, N, K, BN, gp.a_stages, epi);
   check_launch("gemm");
   ++h.launches;
 }
@@ -392,8 +427,8 @@ static void launch_attention(Handle& h, const LayerDev& L, const LayerPlan& lp, 
 
 template <int DK>
 static void launch_qkvg_dk(Handle& h, const LayerDev& L, const CUtensorMap& A, const CUtensorMap& Bm,
-                           int M, int N, int BN, int R, const std::vector<int>& order, const float4* ss,
-                           const int32_t* pos) {
+                           int M, int N, int BN, int R, const std::vector<int>& order,
+                           const CUtensorMap& tmS, const CUtensorMap& tmR) {
   EpiQKVG<DK> e;
   e.d = h.d;
   e.H = h.H;
@@ -404,28 +439,25 @@ static void launch_qkvg_dk(Handle& h, const LayerDev& L, const CUtensorMap& A, c
     e.chead[ci] = static_cast<uint8_t>(ci / ns);
   }
   e.inv_d = 1.f / static_cast<float>(h.d);
-  e.ss = ss;
   e.gain_q = L.gain_q;
   e.gain_k = L.gain_k;
-  e.rope = h.rope;
-  e.pos = pos;
   e.q = h.Qb;
   e.k = h.Kb;
   e.v = h.Vb;
   e.g = h.Gb;
   e.Rq = L.Rq;
   e.Rkv = L.Rkv;
-  launch_gemm(h, A, Bm, M, N, h.d, BN, e);
+  launch_gemm(h, A, Bm, M, N, h.d, BN, e, &tmS, &tmR);
 }
 
 static void launch_qkvg(Handle& h, const LayerDev& L, const CUtensorMap& A, const CUtensorMap& Bm,
-                        int M, int N, int BN, int R, const std::vector<int>& sec, const float4* ss,
-                        const int32_t* pos) {
+                        int M, int N, int BN, int R, const std::vector<int>& sec,
+                        const CUtensorMap& tmS, const CUtensorMap& tmR) {
   if (N / h.dk > 64) throw ConfigError("unsupported: more than 64 head chunks per projection");
   switch (h.dk) {
-    case 16: launch_qkvg_dk<16>(h, L, A, Bm, M, N, BN, R, sec, ss, pos); break;
-    case 32: launch_qkvg_dk<32>(h, L, A, Bm, M, N, BN, R, sec, ss, pos); break;
-    case 64: launch_qkvg_dk<64>(h, L, A, Bm, M, N, BN, R, sec, ss, pos); break;
+    case 16: launch_qkvg_dk<16>(h, L, A, Bm, M, N, BN, R, sec, tmS, tmR); break;
+    case 32: launch_qkvg_dk<32>(h, L, A, Bm, M, N, BN, R, sec, tmS, tmR); break;
+    case 64: launch_qkvg_dk<64>(h, L, A, Bm, M, N, BN, R, sec, tmS, tmR); break;
     default: throw ConfigError("unsupported head dim");
   }
 }
@@ -512,15 +544,16 @@ static void run_layer(Handle& h, int l, int B, bool attn_only = false) {
   float4* SSq = h.SS[L.q_buf];
   if (lp.q_identity) {
     launch_qkvg(h, L, L.tmA_in, L.tmB_all, B * L.Rkv, 4 * d, L.bn_full, L.Rkv,
-                {kSecQ, kSecV, kSecK, kSecG}, SSin, L.pos_kv);
+                {kSecQ, kSecV, kSecK, kSecG}, h.tmSS[L.in_buf], L.tmRopeKV);
   } else {
     const int rows = B * L.Rq;
     k_gather_rows<<<(rows + 7) / 8, 256, 0, h.stream>>>(Xin, SSin, Xq, SSq, L.query_rows, B, L.Rkv, L.Rq, d);
     check_launch("gather");
     ++h.launches;
-    launch_qkvg(h, L, L.tmA_in, L.tmB_kv, B * L.Rkv, 2 * d, L.bn_half, L.Rkv, {kSecK, kSecV}, SSin,
-                L.pos_kv);
-    launch_qkvg(h, L, L.tmA_q, L.tmB_qg, B * L.Rq, 2 * d, L.bn_half, L.Rq, {kSecQ, kSecG}, SSq, L.pos_q);
+    launch_qkvg(h, L, L.tmA_in, L.tmB_kv, B * L.Rkv, 2 * d, L.bn_half, L.Rkv, {kSecK, kSecV},
+                h.tmSS[L.in_buf], L.tmRopeKV);
+    launch_qkvg(h, L, L.tmA_q, L.tmB_qg, B * L.Rq, 2 * d, L.bn_half, L.Rq, {kSecQ, kSecG},
+                h.tmSS[L.q_buf], L.tmRopeQ);
   }
   stage_mark(h, "L" + std::to_string(l) + ".qkvg");
   launch_attention(h, L, lp, B);
@@ -534,11 +567,10 @@ static void run_layer(Handle& h, int l, int B, bool attn_only = false) {
   stage_mark(h, "L" + std::to_string(l) + ".wo");
   if (attn_only) return;
   EpiSwiGLU eu;
-  eu.ss = SSq;
   eu.inv_d = 1.f / static_cast<float>(d);
   eu.hidden = h.hid;
   eu.m = h.m;
-  launch_gemm(h, L.tmA_q, L.tmB_up, B * L.Rq, 2 * h.m, d, L.bn_up, eu);
+  launch_gemm(h, L.tmA_q, L.tmB_up, B * L.Rq, 2 * h.m, d, L.bn_up, eu, &h.tmSS[L.q_buf]);
   stage_mark(h, "L" + std::to_string(l) + ".ffn_up");
   EpiResid ed;
   ed.resid = Xq;

@@ -38,14 +38,13 @@ inline CUtensorMapSwizzle tma_swizzle(int bytes) {
   }
 }
 
-// bf16 tensor of rank 2..3, dims[0] innermost (contiguous). strides_bytes has
+// Tensor of rank 2..3, dims[0] innermost (contiguous). strides_bytes has
 // rank-1 entries (stride of dims[1], dims[2]).
-inline CUtensorMap make_tmap_bf16(const void* base, int rank, const uint64_t* dims,
-                                  const uint64_t* strides_bytes, const uint32_t* box,
-                                  int swizzle_bytes) {
+inline CUtensorMap make_tmap(CUtensorMapDataType dt, const void* base, int rank, const uint64_t* dims,
+                             const uint64_t* strides_bytes, const uint32_t* box, int swizzle_bytes) {
   CUtensorMap m;
   uint32_t elem_strides[3] = {1, 1, 1};
-  CUresult r = tma_encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base),
+  CUresult r = tma_encode_fn()(&m, dt, rank, const_cast<void*>(base),
                                dims, strides_bytes, box, elem_strides,
                                CU_TENSOR_MAP_INTERLEAVE_NONE, tma_swizzle(swizzle_bytes),
                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -54,6 +53,21 @@ inline CUtensorMap make_tmap_bf16(const void* base, int rank, const uint64_t* di
     throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
   }
   return m;
+}
+
+inline CUtensorMap make_tmap_bf16(const void* base, int rank, const uint64_t* dims,
+                                  const uint64_t* strides_bytes, const uint32_t* box,
+                                  int swizzle_bytes) {
+  return make_tmap(CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, base, rank, dims, strides_bytes, box, swizzle_bytes);
+}
+
+// Row-major [rows, cols] fp32 matrix, box = [box_rows, box_cols].
+inline CUtensorMap make_tmap_2d_f32(const void* base, uint64_t rows, uint64_t cols,
+                                    uint32_t box_rows, uint32_t box_cols, int swizzle_bytes) {
+  uint64_t dims[2] = {cols, rows};
+  uint64_t strides[1] = {cols * 4};
+  uint32_t box[2] = {box_cols, box_rows};
+  return make_tmap(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, base, 2, dims, strides, box, swizzle_bytes);
 }
 
 // Row-major [rows, cols] bf16 matrix with row pitch `ld` elements; box = [box_rows, box_cols].

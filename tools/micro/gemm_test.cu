@@ -13,11 +13,13 @@ using namespace sortk;
 struct StoreF32 {
   static constexpr int kChunk = 32;
   static constexpr int kMaxParts = 1 << 30;
+  static constexpr int kSide = 0;
+  static constexpr int kRopeFloats = 0;
   float* C;
   int ldc;
   __device__ void prologue(uint8_t*, int, int) const {}
   template <class Wait>
-  __device__ void run(uint8_t*, Wait&& wait, uint32_t tbase, int row, int n0, int c0, int c1, bool valid, int, int) const {
+  __device__ void run(uint8_t*, uint8_t*, Wait&& wait, uint32_t tbase, int row, int n0, int c0, int c1, bool valid, int, int) const {
     wait();
     for (int c = c0; c < c1; c += 32) {
       float v[32];
@@ -47,7 +49,7 @@ static int run(int M, int N, int K, int BN) {
   GemmPlan gp = gemm_plan(K, BN);
   cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gp.smem_bytes);
   int grid = gemm_grid((M + 127) / 128, N / BN, 148);
-  kfn<<<grid, kGemmThreads, gp.smem_bytes>>>(tA, tB, M, N, K, BN, gp.a_stages, epi);
+  kfn<<<grid, kGemmThreads, gp.smem_bytes>>>(tA, tB, tA, tA, M, N, K, BN, gp.a_stages, epi);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { printf("CUDA error %s\n", cudaGetErrorString(e)); return 1; }
   std::vector<float> hC((size_t)M * N);
@@ -62,7 +64,7 @@ static int run(int M, int N, int K, int BN) {
   // timing at this shape
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  for (int it = 0; it < 10; ++it) kfn<<<grid, kGemmThreads, gp.smem_bytes>>>(tA, tB, M, N, K, BN, gp.a_stages, epi);
+  for (int it = 0; it < 10; ++it) kfn<<<grid, kGemmThreads, gp.smem_bytes>>>(tA, tB, tA, tA, M, N, K, BN, gp.a_stages, epi);
   cudaEventRecord(e1); cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= 10;
   printf("GEMM M=%d N=%d K=%d BN=%d maxerr=%.3g %s  %.3f ms  %.1f TFLOP/s\n", M, N, K, BN, maxerr,
