@@ -132,14 +132,16 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   const uint32_t tS = tmem;          // 128 columns of S
   const uint32_t tO0 = tmem + 128;   // O accumulator(s): 1 (fixed) or 2 (online) x DK columns
 
-  // Work item i -> (q-tile of rank i / BH, heaviest first; request*head bh = i % BH).
+  // Work item i -> (request*head bh = i / n_qtiles, q-tile of rank i % n_qtiles, heaviest
+  // first). (b,h)-major order keeps the ~2 CTAs x 148 in-flight items on a few dozen (b,h)
+  // pairs, so K/V tiles shared by neighbouring q-tiles are re-read from L2, not HBM.
   // Every role walks the same item/tile sequence; `g` counts kv tiles across items so
   // barrier phases and the K/V double buffer run on seamlessly between items.
   if (warp == 0) {
     if (lane == 0) {
       int g = 0, li = 0;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++li) {
-        const int rank = it / a.BH, bh = it - rank * a.BH;
+        const int bh = it / a.n_qtiles, rank = it - bh * a.n_qtiles;
         const int qt = s_order[rank];
         const int t_begin = s_off[qt], n_t = s_off[qt + 1] - t_begin;
         const int qb = li & 1;
@@ -166,7 +168,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
       const uint32_t sp = smem_u32(smem + S::oP);
       int g = 0, li = 0;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++li) {
-        const int rank = it / a.BH;
+        const int rank = it % a.n_qtiles;
         const int qt = s_order[rank];
         const int n_t = s_off[qt + 1] - s_off[qt];
         const int qb = li & 1;
@@ -241,7 +243,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
     constexpr int DH = DK / 2;
     int g = 0, li = 0;
     for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++li) {
-      const int rank = it / a.BH, bh = it - rank * a.BH;
+      const int bh = it / a.n_qtiles, rank = it - bh * a.n_qtiles;
       const int qt = s_order[rank];
       const int q0 = qt * 128;
       const int t_begin = s_off[qt], n_t = s_off[qt + 1] - t_begin;

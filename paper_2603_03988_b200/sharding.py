@@ -1,0 +1,59 @@
+# SPDX-License-Identifier: Apache-2.0
+"""Request sharding across the GPUs of one node.
+
+SORT requests are independent (one request-centric sample = one shared history with its
+candidates), so data parallelism needs no collective in the forward pass: each rank scores
+a contiguous shard of the requests with its own replica of the weights. The only
+cross-rank traffic is host-side bookkeeping -- gathering scores to rank 0 when a caller
+wants the whole batch, and the max-over-ranks step time a benchmark reports. Every kernel
+is row-independent (no split-K, fixed reduction orders), so a request's scores are
+bit-identical at 1, 2, 4 or 8 GPUs (tests/test_gpu_parity.py::test_batch_position_independence).
+"""
+from __future__ import annotations
+
+from typing import Dict, List, Tuple
+
+import numpy as np
+
+
+def shard_range(total: int, world: int, rank: int) -> Tuple[int, int]:
+    """Contiguous [begin, end) of `total` requests for `rank` (sizes differ by at most one)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad world/rank")
+    base, extra = divmod(total, world)
+    begin = rank * base + min(rank, extra)
+    return begin, begin + base + (1 if rank < extra else 0)
+
+
+def shard_batch(batch: Dict[str, np.ndarray], world: int, rank: int) -> Dict[str, np.ndarray]:
+    total = int(batch["req_ts"].shape[0])
+    b, e = shard_range(total, world, rank)
+    return {k: np.ascontiguousarray(v[b:e]) for k, v in batch.items()}
+
+
+def gather_scores(local: np.ndarray, world: int, rank: int, group=None) -> np.ndarray:
+    """Concatenate per-rank score shards [b_r, N, 3] on every rank, in rank order."""
+    if world == 1:
+        return local
+    import torch
+    import torch.distributed as dist
+    t = torch.from_numpy(np.ascontiguousarray(local))
+    sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(sizes, torch.tensor([t.shape[0]], dtype=torch.int64), group=group)
+    mx = int(max(s.item() for s in sizes))
+    pad = torch.zeros((mx,) + tuple(t.shape[1:]), dtype=t.dtype)
+    pad[: t.shape[0]] = t
+    parts = [torch.zeros_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad, group=group)
+    return np.concatenate([p[: int(s.item())].numpy() for p, s in zip(parts, sizes)], axis=0)
+
+
+def max_over_ranks(values: List[float], world: int, device=None, group=None) -> List[float]:
+    """Element-wise max of per-rank timings (the multi-GPU step time is the slowest rank)."""
+    if world == 1:
+        return list(values)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(values, dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return t.cpu().tolist()

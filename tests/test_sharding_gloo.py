@@ -1,0 +1,74 @@
+# SPDX-License-Identifier: Apache-2.0
+"""N>1 host path on CPU: 2-rank gloo process group exercising request sharding, the scores
+gather and the max-over-ranks timing reduction that bench.py uses under torchrun. The
+per-rank "scores" come from the CPU oracle so the test also checks that sharded scoring
+reproduces the unsharded result exactly (requests are independent)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2603_03988_b200 import sharding as S
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_shard_range_partitions_exactly():
+    for total in (0, 1, 5, 16, 256, 257):
+        for world in (1, 2, 3, 4, 8):
+            seen = []
+            for r in range(world):
+                b, e = S.shard_range(total, world, r)
+                seen.extend(range(b, e))
+                assert e - b in (total // world, total // world + 1)
+            assert seen == list(range(total))
+
+
+def _worker(rank, world, port, out_q):
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path[:0] = [os.path.dirname(here), os.path.join(os.path.dirname(here), "oracle")]
+    import torch.distributed as dist
+    import oracle as O
+    from paper_2603_03988_b200 import synth
+    from paper_2603_03988_b200.config import tiny_config
+    from paper_2603_03988_b200 import sharding as S2
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = tiny_config()
+    P = synth.make_params(cfg, seed=3)
+    batch = synth.make_batch(cfg, 5, seed=9)
+    local = S2.shard_batch(batch, world, rank)
+    om = O.OracleModel(cfg, P)
+    scores = np.stack([om.forward(local, i)[0] for i in range(local["req_ts"].shape[0])]) \
+        if local["req_ts"].shape[0] else np.zeros((0, cfg.n_cand, 3))
+    full = S2.gather_scores(scores.astype(np.float32), world, rank)
+    t = S2.max_over_ranks([float(rank + 1), 10.0 - rank], world)
+    if rank == 0:
+        ref = np.stack([om.forward(batch, i)[0] for i in range(5)]).astype(np.float32)
+        out_q.put((bool(np.array_equal(full, ref)), t))
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_sharded_scoring_and_max_time():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    ok, t = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert ok
+    assert t == [2.0, 10.0]
