@@ -24,9 +24,10 @@
 // Roles (320 threads, persistent, 2 CTAs per SM):
 //   warp 0      TMA: Q tile per item (double-buffered), K and V tiles (128 x dk each)
 //               per kv tile (double-buffered); runs ahead across items
-//   warp 1      MMA: S = Q K^T (M=128, N=128, K=dk) into TMEM; P V (M=128, N=dk, K=128)
+//   warp 1      MMA: S = Q K^T (M=128, N=128, K=dk) into TMEM, one tile ahead; O += P V
+//               with P read from TMEM (M=128, N=dk, K=128)
 //   warps 2..9  softmax: thread <-> (query row, S half); tcgen05.ld of S, exp2 on MUFU, P
-//               written bf16 into the SW128 A-operand layout in smem; gate + store at item end
+//               written back to TMEM as bf16 (tcgen05.st); gate + store at item end
 #pragma once
 
 #include "gemm.cuh"
@@ -41,7 +42,6 @@ struct AttnSmem {
   static constexpr uint32_t kQBytes = 128 * DK * 2;
   static constexpr uint32_t kKBytes = 128 * DK * 2;
   static constexpr uint32_t kVBytes = 128 * DK * 2;  // V tile row-major [128 kv x DK], like K
-  static constexpr uint32_t kPBytes = 128 * 128 * 2;
   static constexpr uint32_t kQStride = ((kQBytes + 1023) / 1024) * 1024;
   static constexpr uint32_t kKStride = ((kKBytes + 1023) / 1024) * 1024;
   static constexpr uint32_t kVStride = ((kVBytes + 1023) / 1024) * 1024;
@@ -49,7 +49,7 @@ struct AttnSmem {
   static constexpr uint32_t oK = oQ + 2 * kQStride;
   static constexpr uint32_t oV = oK + 2 * kKStride;
   static constexpr uint32_t oP = oV + 2 * kVStride;
-  static constexpr uint32_t oBar = oP + kPBytes;
+  static constexpr uint32_t oBar = oP;  // P lives in TMEM
   static constexpr uint32_t oRed = oBar + 32 * 8;      // softmax cross-warp reduction scratch
   static constexpr uint32_t oTiles = oRed + 3 * 1024;  // int32 tile tables follow
   static constexpr uint32_t bytes(int n_tile_ints) { return oTiles + 4u * n_tile_ints + 1024; }
@@ -129,8 +129,9 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  const uint32_t tS = tmem;          // 128 columns of S
-  const uint32_t tO0 = tmem + 128;   // O accumulator(s): 1 (fixed) or 2 (online) x DK columns
+  const uint32_t tS = tmem;          // [0, 128): S (fp32)
+  const uint32_t tP = tmem + 128;    // [128, 192): P (bf16 pairs), the A operand of PV
+  const uint32_t tO0 = tmem + 192;   // O accumulator(s): 1 (fixed) or 2 (online) x DK columns
 
   // Work item i -> (request*head bh = i / n_qtiles, q-tile of rank i % n_qtiles, heaviest
   // first). (b,h)-major order keeps the ~2 CTAs x 148 in-flight items on a few dozen (b,h)
@@ -161,65 +162,82 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
     }
   } else if (warp == 1) {
     if (lane == 0) {
+      // MMA issue order per kv tile g: wait P(g) -> issue S(g+1) = Q K^T (lookahead, may belong
+      // to the next item) -> issue O += P(g) V(g). The softmax of tile g+1 therefore never
+      // waits behind PV(g); P sits in its own TMEM columns so both can be in flight.
       const uint32_t id_s = umma_idesc_bf16(128, 64);
-      // PV: A = P (K-major), B = V tile read MN-major (dk contiguous): idesc bit 16.
+      // PV: A = P from TMEM (K-major), B = V tile read MN-major (dk contiguous): idesc bit 16.
       const uint32_t id_o = umma_idesc_bf16(128, DK) | (1u << 16);
-      constexpr uint32_t qsw = DK * 2;  // Q/K rows are DK*2 bytes = the swizzle span
-      const uint32_t sp = smem_u32(smem + S::oP);
-      int g = 0, li = 0;
-      for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++li) {
-        const int rank = it % a.n_qtiles;
-        const int qt = s_order[rank];
-        const int n_t = s_off[qt + 1] - s_off[qt];
-        const int qb = li & 1;
-        mbar_wait_sleep(&q_full[qb], (li >> 1) & 1);
-        const uint32_t sq = smem_u32(smem + S::oQ + qb * S::kQStride);
-        for (int j = 0; j < n_t; ++j, ++g) {
-          const int st = g & 1;
-          mbar_wait_sleep(&kv_full[st], (g >> 1) & 1);
-          const uint32_t sk = smem_u32(smem + S::oK + st * S::kKStride);
-          // S = Q K^T in two N=64 halves, each issued as soon as the softmax has drained
-          // the same half of the previous tile.
+      constexpr uint32_t qsw = DK * 2;  // Q/K/V rows are DK*2 bytes = the swizzle span
+      struct Cur {
+        int it, li, j, n_t, g;
+      };
+      auto tiles_of = [&](int it) {
+        const int qt = s_order[it % a.n_qtiles];
+        return s_off[qt + 1] - s_off[qt];
+      };
+      auto issue_s = [&](const Cur& c) {  // S(c.g) in two N=64 halves
+        const int st = c.g & 1;
+        if (c.j == 0) mbar_wait_sleep(&q_full[c.li & 1], (c.li >> 1) & 1);
+        mbar_wait_sleep(&kv_full[st], (c.g >> 1) & 1);
+        const uint32_t sq = smem_u32(smem + S::oQ + (c.li & 1) * S::kQStride);
+        const uint32_t sk = smem_u32(smem + S::oK + st * S::kKStride);
 #pragma unroll
-          for (int hf = 0; hf < 2; ++hf) {
-            mbar_wait_sleep(&s_free[hf], (g & 1) ^ 1);
-            tc_fence_after();
-#pragma unroll
-            for (int k = 0; k < DK / 16; ++k)
-              mma_bf16_ss(tS + hf * 64, umma_sdesc_kmajor(sq + k * 32, qsw),
-                          umma_sdesc_kmajor(sk + hf * 64 * DK * 2 + k * 32, qsw), id_s, k > 0 ? 1u : 0u);
-            mma_commit(&s_full[hf]);
-          }
-          if (j == n_t - 1) mma_commit(&q_empty[qb]);
-          mbar_wait_sleep(p_full, g & 1);
+        for (int hf = 0; hf < 2; ++hf) {
+          mbar_wait_sleep(&s_free[hf], (c.g & 1) ^ 1);
           tc_fence_after();
-          uint32_t tO;
-          if constexpr (kFixed) {
-            if (j == 0) {  // the previous item's O has been read out
-              mbar_wait_sleep(o_empty, (li & 1) ^ 1);
-              tc_fence_after();
-            }
-            tO = tO0;
-          } else {
-            tO = tO0 + (g & 1) * DK;
-          }
-          const uint32_t sv = smem_u32(smem + S::oV + st * S::kVStride);
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint32_t pa = sp + (kk >> 2) * 16384 + (kk & 3) * 32;
-            // MN-major swizzled V: 8-row groups SBO = 8 * DK * 2 bytes apart; K = 16 rows per MMA
-            const uint32_t va = sv + kk * 16 * (DK * 2);
-            const uint32_t accum = kFixed ? ((j | kk) != 0) : (kk != 0);
-            mma_bf16_ss(tO, umma_sdesc_kmajor(pa, 128), umma_sdesc_kmajor(va, qsw), id_o, accum);
-          }
-          mma_commit(p_empty);
-          mma_commit(&kv_empty[st]);
-          if constexpr (kFixed) {
-            if (j == n_t - 1) mma_commit(&o_full[0]);
-          } else {
-            mma_commit(&o_full[g & 1]);
-          }
+          for (int k = 0; k < DK / 16; ++k)
+            mma_bf16_ss(tS + hf * 64, umma_sdesc_kmajor(sq + k * 32, qsw),
+                        umma_sdesc_kmajor(sk + hf * 64 * DK * 2 + k * 32, qsw), id_s, k > 0 ? 1u : 0u);
+          mma_commit(&s_full[hf]);
         }
+        if (c.j == c.n_t - 1) mma_commit(&q_empty[c.li & 1]);
+      };
+      auto next = [&](Cur c) {
+        ++c.g;
+        if (++c.j == c.n_t) {
+          c.j = 0;
+          ++c.li;
+          c.it += gridDim.x;
+          c.n_t = c.it < n_items ? tiles_of(c.it) : 0;
+        }
+        return c;
+      };
+      Cur cur{static_cast<int>(blockIdx.x), 0, 0, 0, 0};
+      cur.n_t = cur.it < n_items ? tiles_of(cur.it) : 0;
+      if (cur.it < n_items) issue_s(cur);
+      while (cur.it < n_items) {
+        mbar_wait_sleep(p_full, cur.g & 1);  // P(g) written (and S(g) fully read)
+        tc_fence_after();
+        const Cur nx = next(cur);
+        if (nx.it < n_items) issue_s(nx);
+        uint32_t tO;
+        if constexpr (kFixed) {
+          if (cur.j == 0) {  // the previous item's O has been read out
+            mbar_wait_sleep(o_empty, (cur.li & 1) ^ 1);
+            tc_fence_after();
+          }
+          tO = tO0;
+        } else {
+          tO = tO0 + (cur.g & 1) * DK;
+        }
+        const uint32_t sv = smem_u32(smem + S::oV + (cur.g & 1) * S::kVStride);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          // MN-major swizzled V: 8-row groups SBO = 8 * DK * 2 bytes apart; K = 16 rows per MMA
+          const uint32_t va = sv + kk * 16 * (DK * 2);
+          const uint32_t accum = kFixed ? ((cur.j | kk) != 0) : (kk != 0);
+          mma_bf16_ts(tO, tP + kk * 8, umma_sdesc_kmajor(va, qsw), id_o, accum);
+        }
+        mma_commit(p_empty);
+        mma_commit(&kv_empty[cur.g & 1]);
+        if constexpr (kFixed) {
+          if (cur.j == cur.n_t - 1) mma_commit(&o_full[0]);
+        } else {
+          mma_commit(&o_full[cur.g & 1]);
+        }
+        cur = nx;
       }
     }
   } else {
@@ -238,7 +256,6 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
     const float NEG_INF = -__int_as_float(0x7f800000);
     const float sl2 = a.scale_log2;
     const float2 sl2v = make_float2(sl2, sl2);
-    uint8_t* prow = smem + S::oP + hf * 16384 + r * 128;  // this half's SW128 atom of the P row
     float* s_red = reinterpret_cast<float*>(smem + S::oRed);  // [2][2][128] maxima, [2][128] sums
     constexpr int DH = DK / 2;
     int g = 0, li = 0;
@@ -302,7 +319,6 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
           for (int u = 0; u < 2; ++u) lsum[u] = make_float2(lsum[u].x * alpha, lsum[u].y * alpha);
         }
         const float2 nref = make_float2(-ref, -ref);
-        mbar_wait(p_empty, (g & 1) ^ 1);  // PV of the previous tile has consumed P
 #pragma unroll
         for (int cb = 0; cb < 2; ++cb) {
           uint32_t w[16];
@@ -336,16 +352,16 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
               }
             }
           }
-#pragma unroll
-          for (int h4 = 0; h4 < 4; ++h4) {
-            const int cc = cb * 4 + h4;  // 16-byte chunk index 0..7 within this half's atom
-            *reinterpret_cast<int4*>(prow + ((cc ^ (r & 7)) << 4)) =
-                make_int4(w[4 * h4], w[4 * h4 + 1], w[4 * h4 + 2], w[4 * h4 + 3]);
+          if (cb == 0) {  // PV of the previous tile has consumed P
+            mbar_wait(p_empty, (g & 1) ^ 1);
+            tc_fence_after();
           }
+          // P columns [hf*64 + cb*32, +32) -> 16 packed bf16x2 TMEM columns of this row
+          tmem_st_32x32b_x16(tP + lane_off + hf * 32 + cb * 16, w);
         }
+        tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&s_free[hf]);  // this half of S consumed: next QK^T half may overwrite it
-        fence_proxy_async_smem();
         mbar_arrive(p_full);
         if constexpr (!kFixed) {
           m = m_new;
