@@ -58,7 +58,7 @@ struct AttnSmem {
 struct AttnArgs {
   const int4* rowmeta;        // [n_qtiles*128] {lo, hi, self, 0} in kv-index space
   const int32_t* tile_off;    // [n_qtiles+1]
-  const int32_t* tile_code;   // kv_tile | partial << 16
+  const int2* tile_code;      // {kv_tile, warp chunk classes} (plan.hpp)
   const int32_t* qtile_order; // heavy first
   const __nv_bfloat16* g;     // [B*Rq, d] sigmoid gate
   __nv_bfloat16* out;         // [B*Rq, d]
@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 18);
   int32_t* s_off = reinterpret_cast<int32_t*>(smem + S::oTiles);
   int32_t* s_order = s_off + (a.n_qtiles + 1);
-  int32_t* s_code = s_order + a.n_qtiles;
+  int2* s_code = reinterpret_cast<int2*>(s_order + a.n_qtiles + 1);  // 2n+2 ints: 8-byte aligned
 
   const int warp = warp_id(), lane = lane_id();
   const int n_items = a.n_qtiles * a.BH;
@@ -106,6 +106,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   for (int i = threadIdx.x; i <= a.n_qtiles; i += kAttnThreads) s_off[i] = a.tile_off[i];
   for (int i = threadIdx.x; i < a.n_qtiles; i += kAttnThreads) s_order[i] = a.qtile_order[i];
   for (int i = threadIdx.x; i < a.n_codes; i += kAttnThreads) s_code[i] = a.tile_code[i];
+  static_assert(sizeof(int2) == 8, "tile code pairs");
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
         for (int j = 0; j < n_t; ++j, ++g) {
           const int st = g & 1;
           const uint32_t ph = (g >> 1) & 1;
-          const int kv0 = (s_code[t_begin + j] & 0xffff) * 128;
+          const int kv0 = s_code[t_begin + j].x * 128;
           mbar_wait_sleep(&kv_empty[st], ph ^ 1);
           mbar_arrive_expect_tx(&kv_full[st], S::kKBytes + S::kVBytes);
           tma_load_3d(smem + S::oK + st * S::kKStride, &tmK, &kv_full[st], 0, kv0, bh);
@@ -271,20 +272,13 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
 #pragma unroll
       for (int i = 0; i < (kFixed ? 1 : DH); ++i) acc[i] = 0.f;
       for (int j = 0; j < n_t; ++j, ++g) {
-        const int code = s_code[t_begin + j];
-        const int c0 = (code & 0xffff) * 128 + hf * 64;  // first kv column of this half
-        uint32_t full_mask = 0x3, none_mask = 0;
-        if ((code >> 16) != 0) {
-#pragma unroll
-          for (int cb = 0; cb < 2; ++cb) {
-            const int cs = c0 + cb * 32, ce = cs + 31;
-            const bool f = meta.x <= cs && meta.y >= ce;
-            const bool n = (meta.y < cs || meta.x > ce) && !(meta.z >= cs && meta.z <= ce);
-            if (!__all_sync(0xffffffffu, f)) full_mask &= ~(1u << cb);
-            if (__all_sync(0xffffffffu, n)) none_mask |= 1u << cb;
-          }
-        }
-        mbar_wait(&s_full[hf], g & 1);
+        const int2 code = s_code[t_begin + j];
+        const int c0 = code.x * 128 + hf * 64;  // first kv column of this half
+        // this warp's two 32-column chunks: classes from the host plan (full / none / mixed)
+        const uint32_t cls = static_cast<uint32_t>(code.y) >> (2 * (4 * quarter + 2 * hf));
+        const uint32_t full_mask = (cls & 1u) | ((cls >> 1) & 2u);
+        const uint32_t none_mask = ((cls >> 1) & 1u) | ((cls >> 2) & 2u);
+        mbar_wait_sleep(&s_full[hf], g & 1);
         tc_fence_after();
         float ref;  // exp2 reference in the scaled domain
         float alpha = 1.f, m_new = m;
@@ -353,7 +347,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
             }
           }
           if (cb == 0) {  // PV of the previous tile has consumed P
-            mbar_wait(p_empty, (g & 1) ^ 1);
+            mbar_wait_sleep(p_empty, (g & 1) ^ 1);
             tc_fence_after();
           }
           // P columns [hf*64 + cb*32, +32) -> 16 packed bf16x2 TMEM columns of this row
@@ -391,7 +385,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
 #pragma unroll
       for (int i = 0; i < DH; ++i) o[i] = 0.f;
       if constexpr (kFixed) {
-        mbar_wait(&o_full[0], li & 1);
+        mbar_wait_sleep(&o_full[0], li & 1);
         tc_fence_after();
         tmem_row_chunk<DH>(tO0 + hf * DH + lane_off, o);
         tc_fence_before();

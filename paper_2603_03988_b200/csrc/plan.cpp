@@ -127,22 +127,38 @@ void build_tiles(LayerPlan& p) {
   p.tile_off.assign(1, 0);
   p.tile_code.clear();
   p.tiles_total = static_cast<int64_t>(p.n_qtiles) * n_kv;
+  int64_t issued = 0;
   for (int t = 0; t < p.n_qtiles; ++t) {
     const int r0 = t * T, r1 = std::min(p.l_q, r0 + T);
     for (int u = 0; u < n_kv; ++u) {
       const int c0 = u * T, c1 = std::min(p.l_kv, c0 + T);  // [c0, c1)
-      bool any = false, full = (c1 - c0) == T;
-      for (int r = r0; r < r1; ++r) {
-        const bool hit = (p.lo[r] <= c1 - 1 && p.hi[r] >= c0) ||
-                         (p.self_idx[r] >= c0 && p.self_idx[r] < c1);
-        any = any || hit;
-        if (!(p.lo[r] <= c0 && p.hi[r] >= c1 - 1)) full = false;
-      }
-      if (any) p.tile_code.push_back(u | ((full ? 0 : 1) << 16));
+      bool any = false;
+      for (int r = r0; r < r1; ++r)
+        any = any || (p.lo[r] <= c1 - 1 && p.hi[r] >= c0) || (p.self_idx[r] >= c0 && p.self_idx[r] < c1);
+      if (!any) continue;
+      // warp-level chunk classes: rows [r0 + 32q, +32) x columns [c0 + 32c, +32)
+      uint32_t cls = 0;
+      for (int q = 0; q < 4; ++q)
+        for (int c = 0; c < 4; ++c) {
+          const int cs = c0 + 32 * c, ce = cs + 31;
+          bool full = ce < p.l_kv, none = true;
+          for (int r = r0 + 32 * q; r < std::min(r1, r0 + 32 * q + 32); ++r) {
+            const bool sees_all = p.lo[r] <= cs && p.hi[r] >= ce;
+            const bool sees_any = (p.lo[r] <= ce && p.hi[r] >= cs) || (p.self_idx[r] >= cs && p.self_idx[r] <= ce);
+            full = full && sees_all;
+            none = none && !sees_any;
+          }
+          const int ci = 4 * q + c;
+          if (none) cls |= 2u << (2 * ci);  // rows that do not exist count as "none"
+          else if (full) cls |= 1u << (2 * ci);
+        }
+      p.tile_code.push_back(u);
+      p.tile_code.push_back(static_cast<int32_t>(cls));
+      ++issued;
     }
-    p.tile_off.push_back(static_cast<int32_t>(p.tile_code.size()));
+    p.tile_off.push_back(static_cast<int32_t>(issued));
   }
-  p.tiles_issued = static_cast<int64_t>(p.tile_code.size());
+  p.tiles_issued = issued;
   p.qtile_order.resize(p.n_qtiles);
   std::iota(p.qtile_order.begin(), p.qtile_order.end(), 0);
   std::stable_sort(p.qtile_order.begin(), p.qtile_order.end(), [&](int a, int b) {

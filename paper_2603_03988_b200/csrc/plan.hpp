@@ -31,7 +31,9 @@ struct LayerPlan {
   // attention tile lists (q-tiles of kAttnTile rows x kv-tiles of kAttnTile cols)
   int n_qtiles = 0;
   std::vector<int32_t> tile_off;    // [n_qtiles + 1]
-  std::vector<int32_t> tile_code;   // kv_tile | (partial << 16)
+  std::vector<int32_t> tile_code;   // pairs {kv_tile, chunk classes}: for row quarter q and
+                                    // 32-column chunk c, bit 2(4q+c) = fully visible to every
+                                    // valid row, bit 2(4q+c)+1 = visible to none
   std::vector<int32_t> qtile_order; // q-tiles, heaviest first
   int64_t tiles_issued = 0, tiles_total = 0;
 };

@@ -295,7 +295,7 @@ static void finalize(Handle& h) {
     for (int r = 0; r < lp.l_q; ++r) meta[r] = make_int4(lp.lo[r], lp.hi[r], lp.self_idx[r], 0);
     L.rowmeta = h.upload(meta);
     L.tile_off = h.upload(lp.tile_off);
-    L.tile_code = h.upload(lp.tile_code.empty() ? std::vector<int32_t>{0} : lp.tile_code);
+    L.tile_code = h.upload(lp.tile_code.empty() ? std::vector<int32_t>{0, 0} : lp.tile_code);
     L.qtile_order = h.upload(lp.qtile_order);
     L.pos_q = h.upload(lp.pos_q);
     L.pos_kv = h.upload(lp.pos_kv);
@@ -384,8 +384,8 @@ static void launch_gemm(Handle& h, const CUtensorMap& A, const CUtensorMap& B, i
 template <int DK, bool kFixed>
 static void launch_attention_dk(Handle& h, const LayerDev& L, const LayerPlan& lp, int B) {
   static size_t attr_bytes = 0;
-  const int n_codes = static_cast<int>(lp.tile_code.size());
-  const size_t smem = AttnSmem<DK>::bytes(2 * lp.n_qtiles + 1 + n_codes);
+  const int n_codes = static_cast<int>(lp.tile_code.size()) / 2;  // {kv_tile, classes} pairs
+  const size_t smem = AttnSmem<DK>::bytes(2 * lp.n_qtiles + 2 + 2 * n_codes);
   if (smem > attr_bytes) {
     CK(cudaFuncSetAttribute(k_attention<DK, kFixed>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(smem)));
@@ -394,7 +394,7 @@ static void launch_attention_dk(Handle& h, const LayerDev& L, const LayerPlan& l
   AttnArgs a;
   a.rowmeta = L.rowmeta;
   a.tile_off = L.tile_off;
-  a.tile_code = L.tile_code;
+  a.tile_code = reinterpret_cast<const int2*>(L.tile_code);
   a.qtile_order = L.qtile_order;
   a.g = h.Gb;
   a.out = h.Hg;
@@ -908,7 +908,7 @@ int sort_block_attention(int32_t nh, int32_t l_q, int32_t l_kv, int32_t dk, cons
     for (int r = 0; r < l_q; ++r) meta[r] = make_int4(lo[r], hi[r], self_idx[r], 0);
     L.rowmeta = h.upload(meta);
     L.tile_off = h.upload(lp.tile_off);
-    L.tile_code = h.upload(lp.tile_code.empty() ? std::vector<int32_t>{0} : lp.tile_code);
+    L.tile_code = h.upload(lp.tile_code.empty() ? std::vector<int32_t>{0, 0} : lp.tile_code);
     L.qtile_order = h.upload(lp.qtile_order);
     auto up = [&](const float* src, size_t n) {
       std::vector<__nv_bfloat16> b(n);
