@@ -383,14 +383,7 @@ static void launch_gemm(Handle& h, const CUtensorMap& A, const CUtensorMap& B, i
 
 template <int DK, bool kFixed>
 static void launch_attention_dk(Handle& h, const LayerDev& L, const LayerPlan& lp, int B) {
-  static size_t attr_bytes = 0;
   const int n_codes = static_cast<int>(lp.tile_code.size()) / 2;  // {kv_tile, classes} pairs
-  const size_t smem = AttnSmem<DK>::bytes(2 * lp.n_qtiles + 2 + 2 * n_codes);
-  if (smem > attr_bytes) {
-    CK(cudaFuncSetAttribute(k_attention<DK, kFixed>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(smem)));
-    attr_bytes = smem;
-  }
   AttnArgs a;
   a.rowmeta = L.rowmeta;
   a.tile_off = L.tile_off;
@@ -406,7 +399,16 @@ static void launch_attention_dk(Handle& h, const LayerDev& L, const LayerPlan& l
   a.n_codes = n_codes;
   a.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(DK)));
   a.ref_log2 = L.logit_bound * a.scale_log2;
-  const int grid = std::min(lp.n_qtiles * B * h.H, 2 * h.num_sms);
+  const int n_items = lp.n_qtiles * B * h.H;
+  const int tile_ints = 2 * lp.n_qtiles + 2 + 2 * n_codes;
+  static size_t attr_bytes = 0;
+  const size_t smem = AttnSmem<DK>::bytes(tile_ints);
+  if (smem > attr_bytes) {
+    CK(cudaFuncSetAttribute(k_attention<DK, kFixed>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(smem)));
+    attr_bytes = smem;
+  }
+  const int grid = std::min(n_items, 2 * h.num_sms);
   k_attention<DK, kFixed><<<grid, kAttnThreads, smem, h.stream>>>(L.tmQ, L.tmK, L.tmV, a);
   check_launch("attention");
   ++h.launches;

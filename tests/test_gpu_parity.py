@@ -5,7 +5,8 @@ committed golden fixture.
 Bars:
 * integer artifacts -- time buckets, positions, roles, candidate index, retained rows,
   per-layer masks and visible counts -- bit-exact;
-* candidate isolation -- exact zero diff; candidate permutation / batch position -- bit-identical;
+* candidate isolation -- exact zero diff; batch position (=> 1 vs N GPUs) -- bit-identical;
+  candidate permutation -- within PERM_ABS_TOL (self-term summation position, see the test);
 * floating point: bf16 compute vs the fp64 oracle fed the same bf16-rounded weights.
   Tolerances are stated per test: TOKEN_TOL, LOGIT_MAX_ABS, LOGIT_REL_L2.
 """
@@ -219,7 +220,14 @@ def test_candidate_isolation_exact(base):
     assert not np.array_equal(p0[:, 5], p1[:, 5])
 
 
-def test_candidate_permutation_bit_identical(base):
+PERM_ABS_TOL = 5e-3  # one bf16 ulp flip of an activation after a reordered fp32 sum
+
+
+def test_candidate_permutation(base):
+    """permuting candidates permutes the outputs. Not bit-exact (nor is the fp64
+    reference under Eigen): a candidate's self column moves inside the last kv tile, which
+    changes the fp32 summation position of that one term; when the fp32 attention output sits
+    on a bf16 rounding boundary that flips one ulp downstream. Most candidates stay exact."""
     cfg, P, gm, _ = base
     b = synth.make_batch(cfg, 1, seed=42)
     p0 = gm.forward(b)
@@ -227,7 +235,9 @@ def test_candidate_permutation_bit_identical(base):
     b2 = {k: v.copy() for k, v in b.items()}
     b2["cand_item"][0] = b["cand_item"][0][perm]
     p1 = gm.forward(b2)
-    assert np.array_equal(p1[0], p0[0][perm])
+    d = np.abs(p1[0] - p0[0][perm])
+    assert d.max() < PERM_ABS_TOL
+    assert np.median(d) < 1e-6
 
 
 def test_batch_position_independence(base):
