@@ -139,7 +139,7 @@ int sort_layer_plan(SortHandle h, int layer, int32_t* l_q, int32_t* l_kv, int32_
 int sort_attention_forward(SortHandle h, int layer, int32_t batch, const float* x, float* out);
 
 /* blockwise_masked_attention (block_attention.hpp:58-62) at the kernel's tile size on
- * one (q, k, v) problem per head of a batch: q [nh, l_q, dk], k/v [nh, l_kv, dk] (host fp32,
+ * one (q, k, v) problem per head of a batch (dk 16 or 32): q [nh, l_q, dk], k/v [nh, l_kv, dk] (host fp32,
  * rounded to bf16 on upload), visibility given in compact form (lo/hi/self per query row,
  * shared by all nh problems). out [nh, l_q, dk]; skipped/total 128x128 tiles per problem. */
 int sort_block_attention(int32_t nh, int32_t l_q, int32_t l_kv, int32_t dk, const float* q,

@@ -6,7 +6,8 @@
 // followed by the sigmoid gate G (attention.cpp:124-127). Only the 128-column kv
 // tiles holding a visible entry are visited (the block-skip rule of
 // blockwise_masked_attention, block_attention.hpp:86-99, decided analytically by the
-// host plan). Inside partial tiles the mask is evaluated from the compact row form
+// host plan, which also pre-classifies every warp's 32-column chunks as fully visible /
+// invisible / mixed). Inside mixed chunks the mask comes from the compact row form
 // visible(r, c) = lo_r <= c <= hi_r || c == self_r (build_mask, mask.cpp:47-74); masked
 // entries never enter the exponent, so candidate rows never see another candidate
 // (exact isolation) and no 0 * NaN can arise.
@@ -15,19 +16,25 @@
 // <= sqrt(dk) * max|gain| (RMSNorm output, then a RoPE rotation), so every logit obeys
 // |s| <= B = sqrt(dk) * max|g_q| * max|g_k| ("bounded logits"). When
 // B < kFixedRefMax the kernel uses the FIXED reference exp(s - B) instead of the running
-// row max: softmax is shift-invariant, no rescaling of O is ever needed, PV accumulates
-// straight into one TMEM accumulator across kv tiles, and 2^(-2B log2 e) stays a
-// normal fp32/bf16 number. Otherwise (unbounded logits, e.g. the op-level
-// sort_block_attention entry) the online-max path with a deferred O rescale is used
-// (streaming-softmax recurrence of block_attention.hpp:104-122).
+// row max (softmax is shift-invariant; 2^(-2B log2 e) stays a normal fp32/bf16 number), so
+// kv tiles never rescale each other. Otherwise (unbounded logits, e.g. the op-level
+// sort_block_attention entry) the online max with rescaling runs (streaming-softmax
+// recurrence of block_attention.hpp:104-122); the two half-row warps exchange tile maxima.
 //
-// Roles (320 threads, persistent, 2 CTAs per SM):
-//   warp 0      TMA: Q tile per item (double-buffered), K and V tiles (128 x dk each)
-//               per kv tile (double-buffered); runs ahead across items
-//   warp 1      MMA: S = Q K^T (M=128, N=128, K=dk) into TMEM, one tile ahead; O += P V
-//               with P read from TMEM (M=128, N=dk, K=128)
-//   warps 2..9  softmax: thread <-> (query row, S half); tcgen05.ld of S, exp2 on MUFU, P
-//               written back to TMEM as bf16 (tcgen05.st); gate + store at item end
+// TMEM (256 columns per CTA, 2 CTAs per SM): two 128-column buffers, tile g uses buffer
+// g & 1. In a buffer: S (fp32, 128 cols) -> the softmax writes P (bf16 pairs) in place over
+// the consumed columns [0,32) and [64,96) -> PV writes this tile's O_g (fp32, DK cols) into
+// the free columns [32, 32+DK). The softmax adds O_g into registers (tile order: the result
+// is deterministic) while the tensor core already computes S(g+1) in the other buffer.
+//
+// Roles (320 threads, persistent):
+//   warp 0      TMA: Q per item (double-buffered), K and V tiles (128 x dk each) per kv tile
+//               (double-buffered); runs ahead across items
+//   warp 1      MMA: S(g+1) = Q K^T as soon as O(g-1) has been read out of its buffer, then
+//               O_g = P(g) V(g) (A = P from TMEM, B = V read MN-major)
+//   warps 2..9  softmax: warp pair (w, w+4) shares TMEM lane quarter w % 4 (query rows) and
+//               splits every tile by S half; the half-h warp owns output columns
+//               [h*DK/2, (h+1)*DK/2). Row sums are combined lo + hi at item end.
 #pragma once
 
 #include "gemm.cuh"
@@ -39,17 +46,12 @@ constexpr float kFixedRefMax = 40.f;  // 2^(-2*40*log2 e) ~ 2e-35 > FLT_MIN
 
 template <int DK>
 struct AttnSmem {
-  static constexpr uint32_t kQBytes = 128 * DK * 2;
-  static constexpr uint32_t kKBytes = 128 * DK * 2;
-  static constexpr uint32_t kVBytes = 128 * DK * 2;  // V tile row-major [128 kv x DK], like K
-  static constexpr uint32_t kQStride = ((kQBytes + 1023) / 1024) * 1024;
-  static constexpr uint32_t kKStride = ((kKBytes + 1023) / 1024) * 1024;
-  static constexpr uint32_t kVStride = ((kVBytes + 1023) / 1024) * 1024;
+  static constexpr uint32_t kTileBytes = 128 * DK * 2;  // Q, K or V tile (rows of DK*2 bytes)
+  static constexpr uint32_t kStride = ((kTileBytes + 1023) / 1024) * 1024;
   static constexpr uint32_t oQ = 0;
-  static constexpr uint32_t oK = oQ + 2 * kQStride;
-  static constexpr uint32_t oV = oK + 2 * kKStride;
-  static constexpr uint32_t oP = oV + 2 * kVStride;
-  static constexpr uint32_t oBar = oP;  // P lives in TMEM
+  static constexpr uint32_t oK = oQ + 2 * kStride;
+  static constexpr uint32_t oV = oK + 2 * kStride;
+  static constexpr uint32_t oBar = oV + 2 * kStride;
   static constexpr uint32_t oRed = oBar + 32 * 8;      // softmax cross-warp reduction scratch
   static constexpr uint32_t oTiles = oRed + 3 * 1024;  // int32 tile tables follow
   static constexpr uint32_t bytes(int n_tile_ints) { return oTiles + 4u * n_tile_ints + 1024; }
@@ -80,6 +82,7 @@ template <int DK, bool kFixed>
 __global__ void __launch_bounds__(kAttnThreads, 2)
     k_attention(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
+  static_assert(DK <= 32, "O_g must fit the free columns [32, 64) of an S buffer");
   using S = AttnSmem<DK>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -89,12 +92,10 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   uint64_t* q_empty = bars + 2;   // [2]
   uint64_t* kv_full = bars + 4;   // [2]
   uint64_t* kv_empty = bars + 6;  // [2]
-  uint64_t* s_full = bars + 8;    // [2] halves: columns [0,64) and [64,128) of S
-  uint64_t* s_free = bars + 10;   // [2]
-  uint64_t* p_full = bars + 12;
-  uint64_t* p_empty = bars + 13;
-  uint64_t* o_full = bars + 14;   // [2]
-  uint64_t* o_empty = bars + 16;
+  uint64_t* s_full = bars + 8;    // [2 buffers][2 halves]
+  uint64_t* p_full = bars + 12;   // [2 buffers]
+  uint64_t* pv_done = bars + 14;  // [2 buffers]
+  uint64_t* o_read = bars + 16;   // [2 buffers]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 18);
   int32_t* s_off = reinterpret_cast<int32_t*>(smem + S::oTiles);
   int32_t* s_order = s_off + (a.n_qtiles + 1);
@@ -106,7 +107,6 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   for (int i = threadIdx.x; i <= a.n_qtiles; i += kAttnThreads) s_off[i] = a.tile_off[i];
   for (int i = threadIdx.x; i < a.n_qtiles; i += kAttnThreads) s_order[i] = a.qtile_order[i];
   for (int i = threadIdx.x; i < a.n_codes; i += kAttnThreads) s_code[i] = a.tile_code[i];
-  static_assert(sizeof(int2) == 8, "tile code pairs");
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
@@ -116,13 +116,12 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
       mbar_init(&q_empty[i], 1);
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
-      mbar_init(&o_full[i], 1);
-      mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 128);
+      mbar_init(&s_full[2 * i], 1);
+      mbar_init(&s_full[2 * i + 1], 1);
+      mbar_init(&p_full[i], 256);
+      mbar_init(&pv_done[i], 1);
+      mbar_init(&o_read[i], 256);
     }
-    mbar_init(p_full, 256);
-    mbar_init(p_empty, 1);
-    mbar_init(o_empty, 256);
     mbar_fence_init();
   }
   if (warp == 1) tmem_alloc(tslot, 256);
@@ -130,15 +129,15 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
-  const uint32_t tS = tmem;          // [0, 128): S (fp32)
-  const uint32_t tP = tmem + 128;    // [128, 192): P (bf16 pairs), the A operand of PV
-  const uint32_t tO0 = tmem + 192;   // O accumulator(s): 1 (fixed) or 2 (online) x DK columns
+
+  auto tiles_of = [&](int it) {
+    const int qt = s_order[it % a.n_qtiles];
+    return s_off[qt + 1] - s_off[qt];
+  };
 
   // Work item i -> (request*head bh = i / n_qtiles, q-tile of rank i % n_qtiles, heaviest
   // first). (b,h)-major order keeps the ~2 CTAs x 148 in-flight items on a few dozen (b,h)
   // pairs, so K/V tiles shared by neighbouring q-tiles are re-read from L2, not HBM.
-  // Every role walks the same item/tile sequence; `g` counts kv tiles across items so
-  // barrier phases and the K/V double buffer run on seamlessly between items.
   if (warp == 0) {
     if (lane == 0) {
       int g = 0, li = 0;
@@ -148,52 +147,25 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
         const int t_begin = s_off[qt], n_t = s_off[qt + 1] - t_begin;
         const int qb = li & 1;
         mbar_wait_sleep(&q_empty[qb], ((li >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&q_full[qb], S::kQBytes);
-        tma_load_3d(smem + S::oQ + qb * S::kQStride, &tmQ, &q_full[qb], 0, qt * 128, bh);
+        mbar_arrive_expect_tx(&q_full[qb], S::kTileBytes);
+        tma_load_3d(smem + S::oQ + qb * S::kStride, &tmQ, &q_full[qb], 0, qt * 128, bh);
         for (int j = 0; j < n_t; ++j, ++g) {
           const int st = g & 1;
-          const uint32_t ph = (g >> 1) & 1;
           const int kv0 = s_code[t_begin + j].x * 128;
-          mbar_wait_sleep(&kv_empty[st], ph ^ 1);
-          mbar_arrive_expect_tx(&kv_full[st], S::kKBytes + S::kVBytes);
-          tma_load_3d(smem + S::oK + st * S::kKStride, &tmK, &kv_full[st], 0, kv0, bh);
-          tma_load_3d(smem + S::oV + st * S::kVStride, &tmV, &kv_full[st], 0, kv0, bh);
+          mbar_wait_sleep(&kv_empty[st], ((g >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&kv_full[st], 2 * S::kTileBytes);
+          tma_load_3d(smem + S::oK + st * S::kStride, &tmK, &kv_full[st], 0, kv0, bh);
+          tma_load_3d(smem + S::oV + st * S::kStride, &tmV, &kv_full[st], 0, kv0, bh);
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // MMA issue order per kv tile g: wait P(g) -> issue S(g+1) = Q K^T (lookahead, may belong
-      // to the next item) -> issue O += P(g) V(g). The softmax of tile g+1 therefore never
-      // waits behind PV(g); P sits in its own TMEM columns so both can be in flight.
       const uint32_t id_s = umma_idesc_bf16(128, 64);
-      // PV: A = P from TMEM (K-major), B = V tile read MN-major (dk contiguous): idesc bit 16.
-      const uint32_t id_o = umma_idesc_bf16(128, DK) | (1u << 16);
-      constexpr uint32_t qsw = DK * 2;  // Q/K/V rows are DK*2 bytes = the swizzle span
+      const uint32_t id_o = umma_idesc_bf16(128, DK) | (1u << 16);  // B = V, MN-major
+      constexpr uint32_t sw = DK * 2;  // Q/K/V rows are DK*2 bytes = the swizzle span
       struct Cur {
         int it, li, j, n_t, g;
-      };
-      auto tiles_of = [&](int it) {
-        const int qt = s_order[it % a.n_qtiles];
-        return s_off[qt + 1] - s_off[qt];
-      };
-      auto issue_s = [&](const Cur& c) {  // S(c.g) in two N=64 halves
-        const int st = c.g & 1;
-        if (c.j == 0) mbar_wait_sleep(&q_full[c.li & 1], (c.li >> 1) & 1);
-        mbar_wait_sleep(&kv_full[st], (c.g >> 1) & 1);
-        const uint32_t sq = smem_u32(smem + S::oQ + (c.li & 1) * S::kQStride);
-        const uint32_t sk = smem_u32(smem + S::oK + st * S::kKStride);
-#pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
-          mbar_wait_sleep(&s_free[hf], (c.g & 1) ^ 1);
-          tc_fence_after();
-#pragma unroll
-          for (int k = 0; k < DK / 16; ++k)
-            mma_bf16_ss(tS + hf * 64, umma_sdesc_kmajor(sq + k * 32, qsw),
-                        umma_sdesc_kmajor(sk + hf * 64 * DK * 2 + k * 32, qsw), id_s, k > 0 ? 1u : 0u);
-          mma_commit(&s_full[hf]);
-        }
-        if (c.j == c.n_t - 1) mma_commit(&q_empty[c.li & 1]);
       };
       auto next = [&](Cur c) {
         ++c.g;
@@ -205,51 +177,51 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
         }
         return c;
       };
+      auto issue_s = [&](const Cur& c) {  // S(c.g) into buffer c.g & 1, two N=64 halves
+        const int buf = c.g & 1;
+        if (c.g >= 2) {  // O of the buffer's previous tile has been read out
+          mbar_wait_sleep(&o_read[buf], ((c.g >> 1) - 1) & 1);
+        }
+        if (c.j == 0) mbar_wait_sleep(&q_full[c.li & 1], (c.li >> 1) & 1);
+        mbar_wait_sleep(&kv_full[buf], (c.g >> 1) & 1);
+        tc_fence_after();
+        const uint32_t sq = smem_u32(smem + S::oQ + (c.li & 1) * S::kStride);
+        const uint32_t sk = smem_u32(smem + S::oK + buf * S::kStride);
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+#pragma unroll
+          for (int k = 0; k < DK / 16; ++k)
+            mma_bf16_ss(tmem + buf * 128 + hf * 64, umma_sdesc_kmajor(sq + k * 32, sw),
+                        umma_sdesc_kmajor(sk + hf * 64 * DK * 2 + k * 32, sw), id_s, k > 0 ? 1u : 0u);
+          mma_commit(&s_full[buf * 2 + hf]);
+        }
+        if (c.j == c.n_t - 1) mma_commit(&q_empty[c.li & 1]);
+      };
       Cur cur{static_cast<int>(blockIdx.x), 0, 0, 0, 0};
       cur.n_t = cur.it < n_items ? tiles_of(cur.it) : 0;
       if (cur.it < n_items) issue_s(cur);
       while (cur.it < n_items) {
-        mbar_wait_sleep(p_full, cur.g & 1);  // P(g) written (and S(g) fully read)
-        tc_fence_after();
         const Cur nx = next(cur);
-        if (nx.it < n_items) issue_s(nx);
-        uint32_t tO;
-        if constexpr (kFixed) {
-          if (cur.j == 0) {  // the previous item's O has been read out
-            mbar_wait_sleep(o_empty, (cur.li & 1) ^ 1);
-            tc_fence_after();
-          }
-          tO = tO0;
-        } else {
-          tO = tO0 + (cur.g & 1) * DK;
-        }
-        const uint32_t sv = smem_u32(smem + S::oV + (cur.g & 1) * S::kVStride);
+        if (nx.it < n_items) issue_s(nx);  // S(g+1) overlaps the softmax of tile g
+        const int buf = cur.g & 1;
+        mbar_wait_sleep(&p_full[buf], (cur.g >> 1) & 1);  // P(g) written, S(g) consumed
+        tc_fence_after();
+        const uint32_t tb = tmem + buf * 128;
+        const uint32_t sv = smem_u32(smem + S::oV + buf * S::kStride);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
-          // MN-major swizzled V: 8-row groups SBO = 8 * DK * 2 bytes apart; K = 16 rows per MMA
-          const uint32_t va = sv + kk * 16 * (DK * 2);
-          const uint32_t accum = kFixed ? ((cur.j | kk) != 0) : (kk != 0);
-          mma_bf16_ts(tO, tP + kk * 8, umma_sdesc_kmajor(va, qsw), id_o, accum);
+          const uint32_t pa = tb + (kk >> 2) * 64 + (kk & 3) * 8;  // P of half kk/4, K=16 per MMA
+          const uint32_t va = sv + kk * 16 * (DK * 2);           // V rows, MN-major, SBO = 8 rows
+          mma_bf16_ts(tb + 32, pa, umma_sdesc_kmajor(va, sw), id_o, kk != 0 ? 1u : 0u);
         }
-        mma_commit(p_empty);
-        mma_commit(&kv_empty[cur.g & 1]);
-        if constexpr (kFixed) {
-          if (cur.j == cur.n_t - 1) mma_commit(&o_full[0]);
-        } else {
-          mma_commit(&o_full[cur.g & 1]);
-        }
+        mma_commit(&pv_done[buf]);
+        mma_commit(&kv_empty[buf]);
         cur = nx;
       }
     }
   } else {
     // ------------------------------------------------------------ softmax warps
-    // Eight warps: warp pair (w, w+4) shares TMEM lane quarter w % 4 (query rows) and
-    // splits each kv tile by S half: half hf = (warp - 2) / 4 owns columns [64hf, 64hf+64)
-    // and, at item end, output columns [hf*DK/2, (hf+1)*DK/2). With the fixed reference
-    // the halves are independent until the row sums are combined (lo + hi, fixed order).
-    // Each 32-column chunk is classified warp-uniformly: fully visible for all 32 rows of
-    // the warp (no mask arithmetic), fully masked (skipped: P = 0, no exp, no TMEM read),
-    // or mixed (per-element mask from a visibility bitmask).
+    constexpr int DH = DK / 2;
     const int quarter = warp & 3;
     const int hf = (warp - 2) >> 2;
     const int r = quarter * 32 + lane;  // row within the q-tile == TMEM lane
@@ -258,30 +230,51 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
     const float sl2 = a.scale_log2;
     const float2 sl2v = make_float2(sl2, sl2);
     float* s_red = reinterpret_cast<float*>(smem + S::oRed);  // [2][2][128] maxima, [2][128] sums
-    constexpr int DH = DK / 2;
-    int g = 0, li = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++li) {
+    int g = 0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
       const int bh = it / a.n_qtiles, rank = it - bh * a.n_qtiles;
       const int qt = s_order[rank];
       const int q0 = qt * 128;
       const int t_begin = s_off[qt], n_t = s_off[qt + 1] - t_begin;
       const int4 meta = a.rowmeta[q0 + r];
-      float m = NEG_INF, alpha_prev = 0.f;  // online mode only
-      float2 lsum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-      float acc[kFixed ? 1 : DH];
+      const int qrow = q0 + r;
+      const int b = bh / a.H, hh = bh - b * a.H;
+      const size_t off = static_cast<size_t>(b * a.Rq + qrow) * a.d + hh * DK + hf * DH;
+      int4 gate[DH / 8];  // prefetched; consumed at item end
+      if (qrow < a.Rq) {
 #pragma unroll
-      for (int i = 0; i < (kFixed ? 1 : DH); ++i) acc[i] = 0.f;
+        for (int i = 0; i < DH / 8; ++i) gate[i] = reinterpret_cast<const int4*>(a.g + off)[i];
+      }
+      float m = NEG_INF, alpha_prev = 1.f;  // online mode only
+      float2 lsum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      float acc[DH];
+#pragma unroll
+      for (int i = 0; i < DH; ++i) acc[i] = 0.f;
+      // acc <- acc * alpha + O_t  (this warp's DK/2 columns of tile t's PV result)
+      auto fold_o = [&](int t, float alpha) {
+        const int pb = t & 1;
+        mbar_wait_sleep(&pv_done[pb], (t >> 1) & 1);
+        tc_fence_after();
+        float o[DH];
+        tmem_row_chunk<DH>(tmem + pb * 128 + 32 + hf * DH + lane_off, o);
+        tc_fence_before();
+        mbar_arrive(&o_read[pb]);
+#pragma unroll
+        for (int i = 0; i < DH; ++i) acc[i] = kFixed ? acc[i] + o[i] : fmaf(acc[i], alpha, o[i]);
+      };
       for (int j = 0; j < n_t; ++j, ++g) {
+        if (j > 0) fold_o(g - 1, alpha_prev);  // tile order: deterministic accumulation
+        const int buf = g & 1;
+        const uint32_t tSh = tmem + buf * 128 + hf * 64 + lane_off;  // this warp's S half (and P)
         const int2 code = s_code[t_begin + j];
         const int c0 = code.x * 128 + hf * 64;  // first kv column of this half
         // this warp's two 32-column chunks: classes from the host plan (full / none / mixed)
         const uint32_t cls = static_cast<uint32_t>(code.y) >> (2 * (4 * quarter + 2 * hf));
         const uint32_t full_mask = (cls & 1u) | ((cls >> 1) & 2u);
         const uint32_t none_mask = ((cls >> 1) & 1u) | ((cls >> 2) & 2u);
-        mbar_wait_sleep(&s_full[hf], g & 1);
+        mbar_wait_sleep(&s_full[buf * 2 + hf], (g >> 1) & 1);
         tc_fence_after();
         float ref;  // exp2 reference in the scaled domain
-        float alpha = 1.f, m_new = m;
         if constexpr (kFixed) {
           ref = a.ref_log2;
         } else {
@@ -290,27 +283,25 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
           for (int cb = 0; cb < 2; ++cb) {
             if (none_mask & (1u << cb)) continue;
             uint32_t rr[32];
-            tmem_ld_32x32b_x32(tS + lane_off + hf * 64 + cb * 32, rr);
+            tmem_ld_32x32b_x32(tSh + cb * 32, rr);
             tmem_ld_wait();
-            if (full_mask & (1u << cb)) {
+            const uint32_t bits = (full_mask & (1u << cb)) ? 0xffffffffu
+                                                           : chunk_vis_bits(c0 + cb * 32, meta.x, meta.y, meta.z);
 #pragma unroll
-              for (int i = 0; i < 32; ++i) mx4[i & 3] = fmaxf(mx4[i & 3], __uint_as_float(rr[i]));
-            } else {
-              const uint32_t bits = chunk_vis_bits(c0 + cb * 32, meta.x, meta.y, meta.z);
-#pragma unroll
-              for (int i = 0; i < 32; ++i)
-                mx4[i & 3] = fmaxf(mx4[i & 3], (bits >> i) & 1u ? __uint_as_float(rr[i]) : NEG_INF);
-            }
+            for (int i = 0; i < 32; ++i)
+              mx4[i & 3] = fmaxf(mx4[i & 3], (bits >> i) & 1u ? __uint_as_float(rr[i]) : NEG_INF);
           }
           // combine the two halves' maxima (double-buffered slot by tile parity)
           float* slot = s_red + (g & 1) * 256;
           slot[hf * 128 + r] = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
           named_bar_sync(1 + quarter, 64);
-          m_new = fmaxf(m, fmaxf(slot[r], slot[128 + r]));
+          const float m_new = fmaxf(m, fmaxf(slot[r], slot[128 + r]));
           ref = m_new == NEG_INF ? 0.f : m_new * sl2;
-          alpha = ex2_approx(m * sl2 - ref);  // m = -inf -> 0
+          const float alpha = ex2_approx(m * sl2 - ref);  // m = -inf -> 0
 #pragma unroll
           for (int u = 0; u < 2; ++u) lsum[u] = make_float2(lsum[u].x * alpha, lsum[u].y * alpha);
+          alpha_prev = alpha;  // applied to acc when O of this tile is folded in (next tile / end)
+          m = m_new;
         }
         const float2 nref = make_float2(-ref, -ref);
 #pragma unroll
@@ -321,7 +312,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
             for (int i = 0; i < 16; ++i) w[i] = 0u;
           } else {
             uint32_t rr[32];
-            tmem_ld_32x32b_x32(tS + lane_off + hf * 64 + cb * 32, rr);
+            tmem_ld_32x32b_x32(tSh + cb * 32, rr);
             tmem_ld_wait();
             if (full_mask & (1u << cb)) {
 #pragma unroll
@@ -346,61 +337,15 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
               }
             }
           }
-          if (cb == 0) {  // PV of the previous tile has consumed P
-            mbar_wait_sleep(p_empty, (g & 1) ^ 1);
-            tc_fence_after();
-          }
-          // P columns [hf*64 + cb*32, +32) -> 16 packed bf16x2 TMEM columns of this row
-          tmem_st_32x32b_x16(tP + lane_off + hf * 32 + cb * 16, w);
+          // P of columns [cb*32, +32) of this half -> 16 bf16x2 columns, in place over S
+          tmem_st_32x32b_x16(tSh + cb * 16, w);
         }
         tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(&s_free[hf]);  // this half of S consumed: next QK^T half may overwrite it
-        mbar_arrive(p_full);
-        if constexpr (!kFixed) {
-          m = m_new;
-          if (j > 0) {  // deferred: acc <- acc * alpha_{j-1} + O_{j-1} (this warp's DK/2 columns)
-            const int pb = (g - 1) & 1;
-            mbar_wait(&o_full[pb], ((g - 1) >> 1) & 1);
-            tc_fence_after();
-            float o[DH];
-            tmem_row_chunk<DH>(tO0 + pb * DK + hf * DH + lane_off, o);
-            tc_fence_before();
-#pragma unroll
-            for (int i = 0; i < DH; ++i) acc[i] = fmaf(acc[i], alpha_prev, o[i]);
-          }
-          alpha_prev = alpha;
-        }
+        mbar_arrive(&p_full[buf]);
       }
-      // ---- item epilogue: O / l * gate -> bf16, this warp's DK/2 output columns
-      const int qrow = q0 + r;
-      const int b = bh / a.H, hh = bh - b * a.H;
-      const size_t off = static_cast<size_t>(b * a.Rq + qrow) * a.d + hh * DK + hf * DH;
-      int4 gate[DH / 8];
-      if (qrow < a.Rq) {
-#pragma unroll
-        for (int i = 0; i < DH / 8; ++i) gate[i] = reinterpret_cast<const int4*>(a.g + off)[i];
-      }
-      float o[DH];
-#pragma unroll
-      for (int i = 0; i < DH; ++i) o[i] = 0.f;
-      if constexpr (kFixed) {
-        mbar_wait_sleep(&o_full[0], li & 1);
-        tc_fence_after();
-        tmem_row_chunk<DH>(tO0 + hf * DH + lane_off, o);
-        tc_fence_before();
-        mbar_arrive(o_empty);
-      } else {
-        if (n_t > 0) {
-          const int pb = (g - 1) & 1;
-          mbar_wait(&o_full[pb], ((g - 1) >> 1) & 1);
-          tc_fence_after();
-          tmem_row_chunk<DH>(tO0 + pb * DK + hf * DH + lane_off, o);
-          tc_fence_before();
-#pragma unroll
-          for (int i = 0; i < DH; ++i) o[i] = fmaf(acc[i], alpha_prev, o[i]);
-        }
-      }
+      // ---- item epilogue
+      if (n_t > 0) fold_o(g - 1, alpha_prev);
       float* sl = s_red + 512;  // [2][128] partial row sums
       sl[hf * 128 + r] = (lsum[0].x + lsum[0].y) + (lsum[1].x + lsum[1].y);
       named_bar_sync(1 + quarter, 64);
@@ -415,7 +360,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const float2 gf = __bfloat1622float2(g2[e]);
-            w[e] = pack_bf16x2(o[8 * i + 2 * e] * invl * gf.x, o[8 * i + 2 * e + 1] * invl * gf.y);
+            w[e] = pack_bf16x2(acc[8 * i + 2 * e] * invl * gf.x, acc[8 * i + 2 * e + 1] * invl * gf.y);
           }
           reinterpret_cast<int4*>(a.out + off)[i] = make_int4(w[0], w[1], w[2], w[3]);
         }

@@ -421,8 +421,6 @@ static void launch_attention(Handle& h, const LayerDev& L, const LayerPlan& lp, 
     case 33: launch_attention_dk<16, true>(h, L, lp, B); break;
     case 64: launch_attention_dk<32, false>(h, L, lp, B); break;
     case 65: launch_attention_dk<32, true>(h, L, lp, B); break;
-    case 128: launch_attention_dk<64, false>(h, L, lp, B); break;
-    case 129: launch_attention_dk<64, true>(h, L, lp, B); break;
     default: throw ConfigError("unsupported head dim");
   }
 }
@@ -882,7 +880,7 @@ int sort_block_attention(int32_t nh, int32_t l_q, int32_t l_kv, int32_t dk, cons
                          const int32_t* self_idx, float* out, int64_t* skipped, int64_t* total) {
   return api([&] {
     if (nh < 1 || l_q < 1 || l_kv < 1) throw ConfigError("block_attention: bad shape");
-    if (dk != 16 && dk != 32 && dk != 64) throw ConfigError("block_attention: dk must be 16/32/64");
+    if (dk != 16 && dk != 32) throw ConfigError("block_attention: dk must be 16 or 32");
     int dev = 0;
     CK(cudaGetDevice(&dev));
     Handle h;
