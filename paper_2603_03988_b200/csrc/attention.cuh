@@ -53,7 +53,8 @@ struct AttnSmem {
   static constexpr uint32_t oV = oK + 2 * kStride;
   static constexpr uint32_t oBar = oV + 2 * kStride;
   static constexpr uint32_t oRed = oBar + 32 * 8;      // softmax cross-warp reduction scratch
-  static constexpr uint32_t oTiles = oRed + 3 * 1024;  // int32 tile tables follow
+  static constexpr uint32_t oGate = oRed + 3 * 1024;   // [2 halves][128 rows][DK/2] bf16 gate rows
+  static constexpr uint32_t oTiles = oGate + 128 * DK * 2;  // int32 tile tables follow
   static constexpr uint32_t bytes(int n_tile_ints) { return oTiles + 4u * n_tile_ints + 1024; }
 };
 
@@ -240,12 +241,14 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
       const int qrow = q0 + r;
       const int b = bh / a.H, hh = bh - b * a.H;
       const size_t off = static_cast<size_t>(b * a.Rq + qrow) * a.d + hh * DK + hf * DH;
-      int4 gate[DH / 8];  // prefetched; consumed at item end
+      // gate row prefetched into smem (async, no registers held across the item)
+      uint8_t* gslot = smem + S::oGate + (hf * 128 + r) * (DH * 2);
       if (qrow < a.Rq) {
 #pragma unroll
-        for (int i = 0; i < DH / 8; ++i) gate[i] = reinterpret_cast<const int4*>(a.g + off)[i];
+        for (int i = 0; i < DH / 8; ++i) cp_async_16(gslot + 16 * i, a.g + off + 8 * i);
       }
-      float m = NEG_INF, alpha_prev = 1.f;  // online mode only
+      cp_async_commit();
+      float m = NEG_INF, alpha_prev = 1.f, alpha_prev_fold = 1.f;  // online mode only
       float2 lsum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
       float acc[DH];
 #pragma unroll
@@ -263,7 +266,6 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
         for (int i = 0; i < DH; ++i) acc[i] = kFixed ? acc[i] + o[i] : fmaf(acc[i], alpha, o[i]);
       };
       for (int j = 0; j < n_t; ++j, ++g) {
-        if (j > 0) fold_o(g - 1, alpha_prev);  // tile order: deterministic accumulation
         const int buf = g & 1;
         const uint32_t tSh = tmem + buf * 128 + hf * 64 + lane_off;  // this warp's S half (and P)
         const int2 code = s_code[t_begin + j];
@@ -300,6 +302,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
           const float alpha = ex2_approx(m * sl2 - ref);  // m = -inf -> 0
 #pragma unroll
           for (int u = 0; u < 2; ++u) lsum[u] = make_float2(lsum[u].x * alpha, lsum[u].y * alpha);
+          alpha_prev_fold = alpha_prev;  // alpha of tile g-1, used by the fold inside this tile
           alpha_prev = alpha;  // applied to acc when O of this tile is folded in (next tile / end)
           m = m_new;
         }
@@ -339,6 +342,9 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
           }
           // P of columns [cb*32, +32) of this half -> 16 bf16x2 columns, in place over S
           tmem_st_32x32b_x16(tSh + cb * 16, w);
+          // Fold O of the previous tile between the two chunks: its PV has had a full chunk
+          // to finish, and releasing its buffer now still gives QK^T(g+1) half a tile of lead.
+          if (cb == 0 && j > 0) fold_o(g - 1, alpha_prev_fold);
         }
         tmem_st_wait();
         tc_fence_before();
@@ -351,11 +357,13 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
       named_bar_sync(1 + quarter, 64);
       const float l = sl[r] + sl[128 + r];
       named_bar_sync(1 + quarter, 64);  // both partners read before the next item overwrites
+      cp_async_wait_all();
       if (qrow < a.Rq) {
         const float invl = 1.f / l;
 #pragma unroll
         for (int i = 0; i < DH / 8; ++i) {
-          const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gate[i]);
+          const int4 gv = *reinterpret_cast<const int4*>(gslot + 16 * i);
+          const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gv);
           uint32_t w[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
