@@ -107,16 +107,28 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def cpu_reference_rate(cfg, params, batch, n_req, threads):
-    """Times the CPU reference algorithm (oracle port of rankformer::, fp64, dense masked
-    attention as attention.cpp:118-121) on `n_req` requests over `threads` host threads."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as O
-    om = O.OracleModel(cfg, params)
-    t0 = time.perf_counter()
-    om.forward_batch(batch, threads=threads, limit=n_req)
-    dt = time.perf_counter() - t0
-    return n_req * cfg.n_cand / dt, dt
+class CpuReference:
+    """The CPU reference algorithm (fp64 oracle port of rankformer::, dense masked attention as
+    attention.cpp:118-121), one request per host thread.
+
+    A sample is time-bounded: chunks of `threads` requests are scored until at least
+    `min_requests` requests and `target_s` seconds of work are done."""
+
+    def __init__(self, cfg, params, threads):
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+        self.cfg, self.threads = cfg, threads
+        self.om = O.OracleModel(cfg, params)
+        self.batch = synth.make_batch(cfg, threads, seed=1000)
+
+    def sample(self, target_s, min_requests):
+        n, t0 = 0, time.perf_counter()
+        while True:
+            self.om.forward_batch(self.batch, threads=self.threads)
+            n += self.threads
+            dt = time.perf_counter() - t0
+            if dt >= target_s and n >= min_requests:
+                return n * self.cfg.n_cand / dt, dt, n
 
 
 def run_reference(args, cfg, rank, world):
@@ -124,17 +136,20 @@ def run_reference(args, cfg, rank, world):
         return
     threads = os.cpu_count() or 1
     params = synth.make_params(cfg, seed=5)
-    n_req = max(threads, 8)
-    batch = synth.make_batch(cfg, n_req, seed=1000)
-    for _ in range(args.warmup and 1):  # one untimed warm-up sample (page-in, allocator)
-        cpu_reference_rate(cfg, params, batch, threads, threads)
-    total_c, total_t = 0.0, 0.0
+    ref = CpuReference(cfg, params, threads)
+    # each step is a bounded sample so that --steps K --warmup W ends within ~3 minutes
+    per_step = min(20.0, max(1.0, 150.0 / max(1, args.steps + min(args.warmup, 1))))
+    if args.warmup:
+        ref.sample(0.0, threads)  # one untimed warm-up chunk (page-in, allocator)
+    total_c, total_t, total_r = 0.0, 0.0, 0
     for _ in range(args.steps):
-        rate, dt = cpu_reference_rate(cfg, params, batch, n_req, threads)
-        total_c += n_req * cfg.n_cand
+        rate, dt, n = ref.sample(per_step, 1)
+        total_c += n * cfg.n_cand
         total_t += dt
+        total_r += n
     value = total_c / total_t
-    sample = f"{n_req} SORT-base requests per step ({n_req * cfg.n_cand} candidates), fp64 oracle port"
+    sample = (f"{total_r} SORT-base requests over {args.steps} steps ({int(total_c)} candidates, "
+              f"{total_t:.1f} s), fp64 oracle port, one request per thread")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_t / args.steps * 1e3,
@@ -155,6 +170,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--requests", type=int, default=REQ_PER_GPU)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="minimum length of the CPU-baseline sample (>= 32 requests)")
     ap.add_argument("--profile-launches", action="store_true",
                     help="short run for ncu launch lists (no CPU leg, no e2e)")
     args = ap.parse_args()
@@ -316,9 +333,8 @@ def main():
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        n_req = max(threads, 8)
-        cb = synth.make_batch(cfg, n_req, seed=1000)
-        rate, dt = cpu_reference_rate(cfg, params, cb, n_req, threads)
+        ref = CpuReference(cfg, params, threads)
+        rate, dt, n_req = ref.sample(args.cpu_seconds, 32)
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
                "sample": f"{n_req} SORT-base requests ({n_req * cfg.n_cand} candidates) in "
                          f"{dt:.1f} s, fp64 oracle port of the reference, one request per thread"}

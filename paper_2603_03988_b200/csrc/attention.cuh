@@ -29,7 +29,7 @@
 //
 // Roles (320 threads, persistent):
 //   warp 0      TMA: Q per item (double-buffered), K and V tiles (128 x dk each) per kv tile
-//               (double-buffered); runs ahead across items
+//               (kKvStages-deep ring); runs ahead across items
 //   warp 1      MMA: S(g+1) = Q K^T as soon as O(g-1) has been read out of its buffer, then
 //               O_g = P(g) V(g) (A = P from TMEM, B = V read MN-major)
 //   warps 2..9  softmax: warp pair (w, w+4) shares TMEM lane quarter w % 4 (query rows) and
@@ -43,6 +43,7 @@ namespace sortk {
 
 constexpr int kAttnThreads = 320;
 constexpr float kFixedRefMax = 40.f;  // 2^(-2*40*log2 e) ~ 2e-35 > FLT_MIN
+constexpr int kKvStages = 4;         // K/V tile ring depth: loads run ~3 tiles ahead of PV
 
 template <int DK>
 struct AttnSmem {
@@ -50,11 +51,11 @@ struct AttnSmem {
   static constexpr uint32_t kStride = ((kTileBytes + 1023) / 1024) * 1024;
   static constexpr uint32_t oQ = 0;
   static constexpr uint32_t oK = oQ + 2 * kStride;
-  static constexpr uint32_t oV = oK + 2 * kStride;
-  static constexpr uint32_t oBar = oV + 2 * kStride;
+  static constexpr uint32_t oV = oK + kKvStages * kStride;
+  static constexpr uint32_t oBar = oV + kKvStages * kStride;
   static constexpr uint32_t oRed = oBar + 32 * 8;      // softmax cross-warp reduction scratch
-  static constexpr uint32_t oGate = oRed + 3 * 1024;   // [2 halves][128 rows][DK/2] bf16 gate rows
-  static constexpr uint32_t oTiles = oGate + 128 * DK * 2;  // int32 tile tables follow
+  static constexpr uint32_t oGate = oRed + 3 * 1024;   // [2 items][2 halves][128 rows][DK/2] bf16
+  static constexpr uint32_t oTiles = oGate + 2 * 128 * DK * 2;  // int32 tile tables follow
   static constexpr uint32_t bytes(int n_tile_ints) { return oTiles + 4u * n_tile_ints + 1024; }
 };
 
@@ -91,13 +92,13 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::oBar);
   uint64_t* q_full = bars + 0;    // [2]
   uint64_t* q_empty = bars + 2;   // [2]
-  uint64_t* kv_full = bars + 4;   // [2]
-  uint64_t* kv_empty = bars + 6;  // [2]
-  uint64_t* s_full = bars + 8;    // [2 buffers][2 halves]
-  uint64_t* p_full = bars + 12;   // [2 buffers]
-  uint64_t* pv_done = bars + 14;  // [2 buffers]
-  uint64_t* o_read = bars + 16;   // [2 buffers]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 18);
+  uint64_t* s_full = bars + 4;    // [2 buffers][2 halves]
+  uint64_t* p_full = bars + 8;    // [2 buffers]
+  uint64_t* pv_done = bars + 10;  // [2 buffers]
+  uint64_t* o_read = bars + 12;   // [2 buffers]
+  uint64_t* kv_full = bars + 14;  // [kKvStages]
+  uint64_t* kv_empty = kv_full + kKvStages;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(kv_empty + kKvStages);
   int32_t* s_off = reinterpret_cast<int32_t*>(smem + S::oTiles);
   int32_t* s_order = s_off + (a.n_qtiles + 1);
   int2* s_code = reinterpret_cast<int2*>(s_order + a.n_qtiles + 1);  // 2n+2 ints: 8-byte aligned
@@ -115,13 +116,15 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
       mbar_init(&s_full[2 * i], 1);
       mbar_init(&s_full[2 * i + 1], 1);
       mbar_init(&p_full[i], 256);
       mbar_init(&pv_done[i], 1);
       mbar_init(&o_read[i], 256);
+    }
+    for (int i = 0; i < kKvStages; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
     }
     mbar_fence_init();
   }
@@ -151,9 +154,9 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
         mbar_arrive_expect_tx(&q_full[qb], S::kTileBytes);
         tma_load_3d(smem + S::oQ + qb * S::kStride, &tmQ, &q_full[qb], 0, qt * 128, bh);
         for (int j = 0; j < n_t; ++j, ++g) {
-          const int st = g & 1;
+          const int st = g % kKvStages;
           const int kv0 = s_code[t_begin + j].x * 128;
-          mbar_wait_sleep(&kv_empty[st], ((g >> 1) & 1) ^ 1);
+          mbar_wait_sleep(&kv_empty[st], ((g / kKvStages) & 1) ^ 1);
           mbar_arrive_expect_tx(&kv_full[st], 2 * S::kTileBytes);
           tma_load_3d(smem + S::oK + st * S::kStride, &tmK, &kv_full[st], 0, kv0, bh);
           tma_load_3d(smem + S::oV + st * S::kStride, &tmV, &kv_full[st], 0, kv0, bh);
@@ -184,10 +187,11 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
           mbar_wait_sleep(&o_read[buf], ((c.g >> 1) - 1) & 1);
         }
         if (c.j == 0) mbar_wait_sleep(&q_full[c.li & 1], (c.li >> 1) & 1);
-        mbar_wait_sleep(&kv_full[buf], (c.g >> 1) & 1);
+        const int st = c.g % kKvStages;
+        mbar_wait_sleep(&kv_full[st], (c.g / kKvStages) & 1);
         tc_fence_after();
         const uint32_t sq = smem_u32(smem + S::oQ + (c.li & 1) * S::kStride);
-        const uint32_t sk = smem_u32(smem + S::oK + buf * S::kStride);
+        const uint32_t sk = smem_u32(smem + S::oK + st * S::kStride);
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
 #pragma unroll
@@ -208,7 +212,8 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
         mbar_wait_sleep(&p_full[buf], (cur.g >> 1) & 1);  // P(g) written, S(g) consumed
         tc_fence_after();
         const uint32_t tb = tmem + buf * 128;
-        const uint32_t sv = smem_u32(smem + S::oV + buf * S::kStride);
+        const int st = cur.g % kKvStages;
+        const uint32_t sv = smem_u32(smem + S::oV + st * S::kStride);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t pa = tb + (kk >> 2) * 64 + (kk & 3) * 8;  // P of half kk/4, K=16 per MMA
@@ -216,7 +221,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
           mma_bf16_ts(tb + 32, pa, umma_sdesc_kmajor(va, sw), id_o, kk != 0 ? 1u : 0u);
         }
         mma_commit(&pv_done[buf]);
-        mma_commit(&kv_empty[buf]);
+        mma_commit(&kv_empty[st]);
         cur = nx;
       }
     }
@@ -231,8 +236,57 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
     const float sl2 = a.scale_log2;
     const float2 sl2v = make_float2(sl2, sl2);
     float* s_red = reinterpret_cast<float*>(smem + S::oRed);  // [2][2][128] maxima, [2][128] sums
-    int g = 0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    int g = 0, li = 0;
+    float m = NEG_INF, alpha_prev = 1.f, alpha_prev_fold = 1.f;  // online mode only
+    float2 lsum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+    float acc[DH];
+#pragma unroll
+    for (int i = 0; i < DH; ++i) acc[i] = 0.f;
+    // the previous item, finished while the next item's first tile is in flight
+    bool p_valid = false;
+    size_t p_off = 0;
+    float p_lsum = 0.f;
+    // acc <- acc * alpha + O_t  (this warp's DK/2 columns of tile t's PV result)
+    auto fold_o = [&](int t, float alpha) {
+      const int pb = t & 1;
+      mbar_wait_sleep(&pv_done[pb], (t >> 1) & 1);
+      tc_fence_after();
+      float o[DH];
+      tmem_row_chunk<DH>(tmem + pb * 128 + 32 + hf * DH + lane_off, o);
+      tc_fence_before();
+      mbar_arrive(&o_read[pb]);
+#pragma unroll
+      for (int i = 0; i < DH; ++i) acc[i] = kFixed ? acc[i] + o[i] : fmaf(acc[i], alpha, o[i]);
+    };
+    // fold the item's last O (tile t), combine the half-row sums, gate, store, clear acc
+    auto finish_item = [&](int t, float alpha, int pli, bool gate_pending) {
+      fold_o(t, alpha);
+      float* sl = s_red + 512;  // [2][128] partial row sums
+      sl[hf * 128 + r] = p_lsum;
+      named_bar_sync(1 + quarter, 64);
+      const float l = sl[r] + sl[128 + r];
+      named_bar_sync(1 + quarter, 64);  // both partners read before the next item overwrites
+      if (gate_pending) cp_async_wait_1(); else cp_async_wait_all();
+      if (p_valid) {
+        const uint8_t* gs = smem + S::oGate + ((pli & 1) * 256 + hf * 128 + r) * (DH * 2);
+        const float invl = 1.f / l;
+#pragma unroll
+        for (int i = 0; i < DH / 8; ++i) {
+          const int4 gv = *reinterpret_cast<const int4*>(gs + 16 * i);
+          const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gv);
+          uint32_t w[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 gf = __bfloat1622float2(g2[e]);
+            w[e] = pack_bf16x2(acc[8 * i + 2 * e] * invl * gf.x, acc[8 * i + 2 * e + 1] * invl * gf.y);
+          }
+          reinterpret_cast<int4*>(a.out + p_off)[i] = make_int4(w[0], w[1], w[2], w[3]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < DH; ++i) acc[i] = 0.f;
+    };
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x, ++li) {
       const int bh = it / a.n_qtiles, rank = it - bh * a.n_qtiles;
       const int qt = s_order[rank];
       const int q0 = qt * 128;
@@ -241,30 +295,20 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
       const int qrow = q0 + r;
       const int b = bh / a.H, hh = bh - b * a.H;
       const size_t off = static_cast<size_t>(b * a.Rq + qrow) * a.d + hh * DK + hf * DH;
-      // gate row prefetched into smem (async, no registers held across the item)
-      uint8_t* gslot = smem + S::oGate + (hf * 128 + r) * (DH * 2);
+      // gate row prefetched into smem (async; slot by item parity, the previous item's
+      // gate is still unread until its epilogue runs inside this item's first tile)
+      uint8_t* gslot = smem + S::oGate + ((li & 1) * 256 + hf * 128 + r) * (DH * 2);
       if (qrow < a.Rq) {
 #pragma unroll
         for (int i = 0; i < DH / 8; ++i) cp_async_16(gslot + 16 * i, a.g + off + 8 * i);
       }
       cp_async_commit();
-      float m = NEG_INF, alpha_prev = 1.f, alpha_prev_fold = 1.f;  // online mode only
-      float2 lsum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-      float acc[DH];
-#pragma unroll
-      for (int i = 0; i < DH; ++i) acc[i] = 0.f;
-      // acc <- acc * alpha + O_t  (this warp's DK/2 columns of tile t's PV result)
-      auto fold_o = [&](int t, float alpha) {
-        const int pb = t & 1;
-        mbar_wait_sleep(&pv_done[pb], (t >> 1) & 1);
-        tc_fence_after();
-        float o[DH];
-        tmem_row_chunk<DH>(tmem + pb * 128 + 32 + hf * DH + lane_off, o);
-        tc_fence_before();
-        mbar_arrive(&o_read[pb]);
-#pragma unroll
-        for (int i = 0; i < DH; ++i) acc[i] = kFixed ? acc[i] + o[i] : fmaf(acc[i], alpha, o[i]);
-      };
+      const bool has_prev = li > 0;
+      if (has_prev) {  // this item's row sums start from zero; keep the previous item's
+        p_lsum = (lsum[0].x + lsum[0].y) + (lsum[1].x + lsum[1].y);
+        lsum[0] = lsum[1] = make_float2(0.f, 0.f);
+      }
+      m = NEG_INF;
       for (int j = 0; j < n_t; ++j, ++g) {
         const int buf = g & 1;
         const uint32_t tSh = tmem + buf * 128 + hf * 64 + lane_off;  // this warp's S half (and P)
@@ -344,36 +388,26 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
           tmem_st_32x32b_x16(tSh + cb * 16, w);
           // Fold O of the previous tile between the two chunks: its PV has had a full chunk
           // to finish, and releasing its buffer now still gives QK^T(g+1) half a tile of lead.
-          if (cb == 0 && j > 0) fold_o(g - 1, alpha_prev_fold);
+          // On an item's first tile that O is the previous item's last: finish that item here.
+          if (cb == 0) {
+            if (j > 0) {
+              fold_o(g - 1, alpha_prev_fold);
+            } else if (has_prev) {
+              finish_item(g - 1, alpha_prev_fold, li - 1, true);
+            }
+          }
         }
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&p_full[buf]);
       }
-      // ---- item epilogue
-      if (n_t > 0) fold_o(g - 1, alpha_prev);
-      float* sl = s_red + 512;  // [2][128] partial row sums
-      sl[hf * 128 + r] = (lsum[0].x + lsum[0].y) + (lsum[1].x + lsum[1].y);
-      named_bar_sync(1 + quarter, 64);
-      const float l = sl[r] + sl[128 + r];
-      named_bar_sync(1 + quarter, 64);  // both partners read before the next item overwrites
-      cp_async_wait_all();
-      if (qrow < a.Rq) {
-        const float invl = 1.f / l;
-#pragma unroll
-        for (int i = 0; i < DH / 8; ++i) {
-          const int4 gv = *reinterpret_cast<const int4*>(gslot + 16 * i);
-          const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gv);
-          uint32_t w[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 gf = __bfloat1622float2(g2[e]);
-            w[e] = pack_bf16x2(acc[8 * i + 2 * e] * invl * gf.x, acc[8 * i + 2 * e + 1] * invl * gf.y);
-          }
-          reinterpret_cast<int4*>(a.out + off)[i] = make_int4(w[0], w[1], w[2], w[3]);
-        }
-      }
+      p_valid = qrow < a.Rq;
+      p_off = off;
     }  // item loop
+    if (li > 0) {  // the last item
+      p_lsum = (lsum[0].x + lsum[0].y) + (lsum[1].x + lsum[1].y);
+      finish_item(g - 1, alpha_prev, li - 1, false);
+    }
   }
   tc_fence_before();
   __syncthreads();
