@@ -87,8 +87,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   static_assert(DK <= 32, "O_g must fit the free columns [32, 64) of an S buffer");
   using S = AttnSmem<DK>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* smem = align_smem_1k(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::oBar);
   uint64_t* q_full = bars + 0;    // [2]
   uint64_t* q_empty = bars + 2;   // [2]
@@ -184,11 +183,11 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
       auto issue_s = [&](const Cur& c) {  // S(c.g) into buffer c.g & 1, two N=64 halves
         const int buf = c.g & 1;
         if (c.g >= 2) {  // O of the buffer's previous tile has been read out
-          mbar_wait_sleep(&o_read[buf], ((c.g >> 1) - 1) & 1);
+          mbar_wait(&o_read[buf], ((c.g >> 1) - 1) & 1);
         }
-        if (c.j == 0) mbar_wait_sleep(&q_full[c.li & 1], (c.li >> 1) & 1);
+        if (c.j == 0) mbar_wait(&q_full[c.li & 1], (c.li >> 1) & 1);
         const int st = c.g % kKvStages;
-        mbar_wait_sleep(&kv_full[st], (c.g / kKvStages) & 1);
+        mbar_wait(&kv_full[st], (c.g / kKvStages) & 1);
         tc_fence_after();
         const uint32_t sq = smem_u32(smem + S::oQ + (c.li & 1) * S::kStride);
         const uint32_t sk = smem_u32(smem + S::oK + st * S::kStride);
@@ -209,7 +208,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
         const Cur nx = next(cur);
         if (nx.it < n_items) issue_s(nx);  // S(g+1) overlaps the softmax of tile g
         const int buf = cur.g & 1;
-        mbar_wait_sleep(&p_full[buf], (cur.g >> 1) & 1);  // P(g) written, S(g) consumed
+        mbar_wait(&p_full[buf], (cur.g >> 1) & 1);  // P(g) written, S(g) consumed
         tc_fence_after();
         const uint32_t tb = tmem + buf * 128;
         const int st = cur.g % kKvStages;

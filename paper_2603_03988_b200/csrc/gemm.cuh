@@ -77,8 +77,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   constexpr int kRopeBoxFloats = Epi::kRopeFloats < 32 ? Epi::kRopeFloats : 32;
   constexpr int kRopeBoxes = Epi::kRopeFloats / (kRopeBoxFloats > 0 ? kRopeBoxFloats : 1);
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* smem = align_smem_1k(smem_raw);
   const int num_k = (K + kGemmBK - 1) / kGemmBK;
   const uint32_t b_box = static_cast<uint32_t>(BN) * kGemmBK * 2;
   uint8_t* sB = smem;

@@ -68,6 +68,13 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
   }
 }
 
+// 1024-byte aligned view of the dynamic smem window. Pointer arithmetic on the
+// __shared__ array itself (not an integer round trip) keeps the shared address space
+// visible to the compiler, so accesses through it lower to LDS/STS, not generic LD/ST.
+__device__ __forceinline__ uint8_t* align_smem_1k(uint8_t* smem_raw) {
+  return smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+}
+
 // ---------------------------------------------------------------- fences
 // Generic-proxy smem writes (st.shared) -> visible to the async proxy (MMA/TMA).
 __device__ __forceinline__ void fence_proxy_async_smem() {

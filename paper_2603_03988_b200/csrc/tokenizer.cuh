@@ -80,8 +80,7 @@ __device__ __forceinline__ void tok_put(uint8_t* arow, int r, int c0, const __nv
 
 __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* smem = align_smem_1k(smem_raw);
   const int d = p.d;
   uint8_t* sW = smem;                       // [d rows x 128 B] SW128
   uint8_t* sA = smem + d * 128;             // [128 rows x 128 B] SW128
