@@ -166,6 +166,11 @@ int sort_kernel_count(SortHandle h, int32_t* launches);
 int sort_enable_stage_timing(SortHandle h, int enable);
 int sort_stage_times(SortHandle h, float* ms, int32_t cap, int32_t* n, char* names,
                      int32_t names_cap);
+/* Kernel-selection knobs for A/B tests (no reference counterpart; defaults are the fastest
+ * path): "fused_tail" (1 = one k_block_tail launch per block for Wo + residual + SwishGLU FFN
+ * + residual where the shape allows it, 0 = the three separate GEMMs). Status 1 on an
+ * unknown name. */
+int sort_set_option(SortHandle h, const char* name, int32_t value);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,387 @@
+// SPDX-License-Identifier: Apache-2.0
+// Fused SORT block tail on tcgen05: everything of one block after the attention core,
+//
+//   x1 = P(x, L_out) + (G . O) Wo                         (attention.cpp:124-131)
+//   x2 = x1 + down( swish(RMSN(x1) W_gate) * RMSN(x1) W_up )
+//
+// in ONE persistent kernel per 128-row tile, so neither x1 nor the m-wide FFN hidden
+// activation ever touches HBM: per row the kernel reads the gated attention output and the
+// residual (2 x 2d bytes) and writes x2 plus its row statistics (2d + 16 bytes), where the
+// unfused Wo / up / down GEMM chain moves 2d + 2d + 2d + 2m + 2d + 2m + 2d + 2d bytes.
+//
+// Per tile (d = 256, m = 640; TMEM = 512 columns):
+//   Wo     D[0,256)      = Hg (128 x d, smem, TMA) . Wo^T                 4 weight stages
+//   E1     x1 = bf16(x + D) -> smem (SW128 K-major: the A operand of the up projection),
+//          sum(x1^2) per row (fixed-order halves -> deterministic 1/rms)
+//   for hidden chunk j = 0 .. m/64-1:
+//     up   U[j&1] (128 cols) = x1 . Wup_j^T     ([gate 32 | up 32] x 2 blocks, 2 stages)
+//     E2   h = swish(g/rms) * (u/rms) -> bf16 pairs written IN PLACE into U[j&1] (TMEM)
+//     down D[0,256) += h (A operand from TMEM) . Wdown_j^T                  1 stage
+//   E3     x2 = bf16(x1 + D) -> HBM, row statistics (sum of squares partials)
+//
+// Weights stream through a 3-deep ring of 32 KB stages from L2 (the whole layer's weights
+// are 1.1 MB and stay L2-resident); the rounding points (x1, h, x2 in bf16, fp32 MMA
+// accumulation in the same K order) are those of the unfused kernels, so both paths give
+// bit-identical activations.
+//
+// Roles (384 threads, 1 CTA per SM): warp 0 TMA, warp 1 MMA (one thread), warp 2 TMEM
+// allocator, warps 4..11 epilogue (TMEM lane quarter = warp % 4; warps 4-7 own the first
+// half of every row's columns, warps 8-11 the second half).
+#pragma once
+
+#include "epilogues.cuh"
+
+namespace sortk {
+
+constexpr int kTailThreads = 384;
+constexpr int kTailStages = 3;
+constexpr uint32_t kTailStageBytes = 32768;
+
+template <int D>
+struct TailSmem {
+  static constexpr uint32_t kTileBytes = 128u * D * 2;  // 128 rows x D bf16 (D/64 K-blocks)
+  static constexpr uint32_t oHg = 0;
+  static constexpr uint32_t oX1 = oHg + kTileBytes;
+  static constexpr uint32_t oW = oX1 + kTileBytes;
+  static constexpr uint32_t oSS = oW + kTailStages * kTailStageBytes;  // [2][128] fp32
+  static constexpr uint32_t oBar = oSS + 1024;
+  static constexpr uint32_t bytes = oBar + 256 + 1024;  // + alignment slack
+};
+
+struct TailArgs {
+  const __nv_bfloat16* resid;  // [M, D] residual rows P(x, L_out) (may alias out)
+  __nv_bfloat16* out;          // [M, D]
+  float* ss_out;               // [M, 4] sum-of-squares partials of out
+  int M, m;                    // rows, FFN hidden width
+  float inv_d;
+};
+
+__device__ __forceinline__ void sts_v4(uint32_t addr, int4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ int4 lds_v4(uint32_t addr) {
+  int4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
+// Byte offset of the 16-byte chunk (row r, column chunk c16 of 8 bf16) of a 128-row tile
+// stored as K-blocks of 64 columns in the TMA SWIZZLE_128B layout (UMMA K-major SW128).
+__device__ __forceinline__ uint32_t sw128_off(int r, int c16) {
+  return static_cast<uint32_t>((c16 >> 3) * 16384 + r * 128 + (((c16 & 7) ^ (r & 7)) << 4));
+}
+
+template <int D>
+__global__ void __launch_bounds__(kTailThreads, 1)
+    k_block_tail(const __grid_constant__ CUtensorMap tmHg, const __grid_constant__ CUtensorMap tmWo,
+                 const __grid_constant__ CUtensorMap tmWup, const __grid_constant__ CUtensorMap tmWdown,
+                 const TailArgs a) {
+  static_assert(D == 128 || D == 256, "block tail: model dim 128 or 256");
+  using S = TailSmem<D>;
+  constexpr uint32_t kKB = D / 64;              // K-blocks of the Hg / x1 tiles
+  constexpr uint32_t kWoStage = D * 128u;       // one K-block of Wo^T: D rows x 64 K
+  constexpr uint32_t kDownStage = D * 128u;     // Wdown_j^T: D rows x 64 K
+  constexpr uint32_t kUpBox = 128u * 128u;      // 128 rows x 64 K of the interleaved W_up
+  constexpr int kCols = D / 2;                  // accumulator columns per epilogue thread
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1k(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::oBar);
+  uint64_t* w_full = bars;                 // [3]
+  uint64_t* w_empty = bars + 3;            // [3]
+  uint64_t* hg_full = bars + 6;
+  uint64_t* hg_empty = bars + 7;
+  uint64_t* d_full = bars + 8;             // D1 ready, then D2 ready (two phases per tile)
+  uint64_t* d_empty = bars + 9;
+  uint64_t* x1_full = bars + 10;
+  uint64_t* u_full = bars + 11;            // [2]
+  uint64_t* h_full = bars + 13;            // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 16);
+
+  const int warp = warp_id(), lane = lane_id();
+  const int num_m = (a.M + 127) / 128;
+  const int n_chunks = a.m / 64;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmHg);
+    tma_prefetch_desc(&tmWo);
+    tma_prefetch_desc(&tmWup);
+    tma_prefetch_desc(&tmWdown);
+    for (int s = 0; s < kTailStages; ++s) {
+      mbar_init(&w_full[s], 1);
+      mbar_init(&w_empty[s], 1);
+    }
+    mbar_init(hg_full, 1);
+    mbar_init(hg_empty, 1);
+    mbar_init(d_full, 1);
+    mbar_init(d_empty, 256);
+    mbar_init(x1_full, 256);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&u_full[i], 1);
+      mbar_init(&h_full[i], 256);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 2) tmem_alloc(tslot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      auto stage = [&](uint32_t bytes) -> uint8_t* {
+        mbar_wait_sleep(&w_empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&w_full[s], bytes);
+        return smem + S::oW + s * kTailStageBytes;
+      };
+      auto advance = [&]() {
+        if (++s == kTailStages) {
+          s = 0;
+          ph ^= 1;
+        }
+      };
+      auto load_hg = [&](int mb, int t) {
+        mbar_wait_sleep(hg_empty, (t & 1) ^ 1);
+        mbar_arrive_expect_tx(hg_full, S::kTileBytes);
+        for (uint32_t kb = 0; kb < kKB; ++kb)
+          tma_load_2d(smem + S::oHg + kb * 16384, &tmHg, hg_full, kb * 64, mb * 128);
+      };
+      int t = 0;
+      if (static_cast<int>(blockIdx.x) < num_m) load_hg(blockIdx.x, 0);
+      for (int mb = blockIdx.x; mb < num_m; mb += gridDim.x, ++t) {
+        for (uint32_t kb = 0; kb < kKB; ++kb) {  // Wo^T K-blocks
+          uint8_t* dst = stage(kWoStage);
+          tma_load_2d(dst, &tmWo, &w_full[s], kb * 64, 0);
+          advance();
+        }
+        // the next tile's attention rows, as soon as this tile's Wo MMAs released the buffer
+        if (mb + static_cast<int>(gridDim.x) < num_m) load_hg(mb + gridDim.x, t + 1);
+        auto up = [&](int j) {
+          for (int p = 0; p < static_cast<int>(kKB) / 2; ++p) {
+            uint8_t* dst = stage(2 * kUpBox);
+            tma_load_2d(dst, &tmWup, &w_full[s], (2 * p) * 64, j * 128);
+            tma_load_2d(dst + kUpBox, &tmWup, &w_full[s], (2 * p + 1) * 64, j * 128);
+            advance();
+          }
+        };
+        up(0);
+        if (n_chunks > 1) up(1);
+        for (int j = 0; j < n_chunks; ++j) {
+          uint8_t* dst = stage(kDownStage);
+          tma_load_2d(dst, &tmWdown, &w_full[s], j * 64, 0);
+          advance();
+          if (j + 2 < n_chunks) up(j + 2);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t id_d = umma_idesc_bf16(128, D);
+      const uint32_t id_u = umma_idesc_bf16(128, 128);
+      const uint32_t hg0 = smem_u32(smem + S::oHg), x10 = smem_u32(smem + S::oX1);
+      const uint32_t w0 = smem_u32(smem + S::oW);
+      int s = 0;
+      uint32_t ph = 0;
+      auto wait_stage = [&]() -> uint32_t {
+        mbar_wait(&w_full[s], ph);
+        tc_fence_after();
+        return w0 + s * kTailStageBytes;
+      };
+      auto release_stage = [&]() {
+        mma_commit(&w_empty[s]);
+        if (++s == kTailStages) {
+          s = 0;
+          ph ^= 1;
+        }
+      };
+      int t = 0, c = 0;  // tile, global hidden-chunk counter (phases of u_full / h_full)
+      for (int mb = blockIdx.x; mb < num_m; mb += gridDim.x, ++t) {
+        mbar_wait_sleep(hg_full, t & 1);
+        mbar_wait_sleep(d_empty, (t & 1) ^ 1);  // E3 of the previous tile drained D
+        tc_fence_after();
+        for (uint32_t kb = 0; kb < kKB; ++kb) {
+          const uint32_t b = wait_stage();
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            mma_bf16_ss(tmem, umma_sdesc_kmajor(hg0 + kb * 16384 + k * 32, 128),
+                        umma_sdesc_kmajor(b + k * 32, 128), id_d, (kb | k) != 0 ? 1u : 0u);
+          release_stage();
+        }
+        mma_commit(hg_empty);
+        mma_commit(d_full);
+        mbar_wait(x1_full, t & 1);  // x1 in smem, D drained by E1
+        tc_fence_after();
+        auto up = [&](int j) {
+          const uint32_t u = tmem + 256 + (j & 1) * 128;
+          for (uint32_t p = 0; p < kKB / 2; ++p) {
+            const uint32_t b = wait_stage();
+#pragma unroll
+            for (uint32_t kh = 0; kh < 2; ++kh) {
+              const uint32_t kb = 2 * p + kh;
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                mma_bf16_ss(u, umma_sdesc_kmajor(x10 + kb * 16384 + k * 32, 128),
+                            umma_sdesc_kmajor(b + kh * kUpBox + k * 32, 128), id_u, (kb | k) != 0 ? 1u : 0u);
+            }
+            release_stage();
+          }
+          mma_commit(&u_full[j & 1]);
+        };
+        up(0);
+        if (n_chunks > 1) up(1);
+        for (int j = 0; j < n_chunks; ++j, ++c) {
+          const int hb = c & 1;
+          mbar_wait(&h_full[hb], (c >> 1) & 1);  // E2 wrote h_j over U[j&1]
+          tc_fence_after();
+          const uint32_t hbase = tmem + 256 + hb * 128;
+          const uint32_t b = wait_stage();
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            mma_bf16_ts(tmem, hbase + (k >> 1) * 64 + (k & 1) * 8, umma_sdesc_kmajor(b + k * 32, 128), id_d,
+                        (j | k) != 0 ? 1u : 0u);
+          release_stage();
+          if (j + 2 < n_chunks) up(j + 2);  // in-order tensor pipe: reads of h_j precede
+        }
+        mma_commit(d_full);
+      }
+    }
+  } else if (warp >= 4) {
+    const int e = warp - 4;
+    const int q = e & 3, hf = e >> 2;
+    const int r = q * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    const uint32_t tD = tmem + lane_off + hf * kCols;
+    const uint32_t x1s = smem_u32(smem + S::oX1);
+    float* s_ss = reinterpret_cast<float*>(smem + S::oSS);
+    int t = 0, c = 0;
+    uint32_t dph = 0;
+    for (int mb = blockIdx.x; mb < num_m; mb += gridDim.x, ++t) {
+      const int row = mb * 128 + r;
+      const bool valid = row < a.M;
+      int4 rv[kCols / 8];
+      if (valid) {
+        const int4* rp = reinterpret_cast<const int4*>(a.resid + static_cast<size_t>(row) * D + hf * kCols);
+#pragma unroll
+        for (int i = 0; i < kCols / 8; ++i) rv[i] = rp[i];
+      } else {
+#pragma unroll
+        for (int i = 0; i < kCols / 8; ++i) rv[i] = make_int4(0, 0, 0, 0);
+      }
+      // ---- E1: x1 = bf16(resid + Wo acc) -> smem A tile; sum of squares
+      mbar_wait(d_full, dph);
+      dph ^= 1;
+      tc_fence_after();
+      float ss = 0.f;
+#pragma unroll
+      for (int cc = 0; cc < kCols / 32; ++cc) {
+        float v[32];
+        tmem_row_chunk<32>(tD + cc * 32, v);
+#pragma unroll
+        for (int qd = 0; qd < 4; ++qd) {
+          const int4 r4 = rv[cc * 4 + qd];
+          const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&r4);
+          uint32_t w[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float2 f = __bfloat1622float2(r2[k]);
+            w[k] = pack_bf16x2(f.x + v[qd * 8 + 2 * k], f.y + v[qd * 8 + 2 * k + 1]);
+            const float2 y = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&w[k]));
+            ss = fmaf(y.x, y.x, fmaf(y.y, y.y, ss));
+          }
+          sts_v4(x1s + sw128_off(r, (hf * kCols + cc * 32) / 8 + qd), make_int4(w[0], w[1], w[2], w[3]));
+        }
+      }
+      s_ss[hf * 128 + r] = ss;
+      named_bar_sync(1 + q, 64);
+      const float ss1 = s_ss[r] + s_ss[128 + r];
+      const float inv = row_inv_rms(ss1, a.inv_d);
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(x1_full);
+      // ---- E2 per hidden chunk: h = swish(g/rms) * (u/rms), bf16 pairs in place in TMEM
+      for (int j = 0; j < n_chunks; ++j, ++c) {
+        const int ub = c & 1;
+        mbar_wait(&u_full[ub], (c >> 1) & 1);
+        tc_fence_after();
+        const uint32_t tu = tmem + lane_off + 256 + ub * 128 + hf * 64;
+        float v[64];
+        tmem_row_chunk<64>(tu, v);
+        uint32_t hw[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          float hh[2];
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const float gt = v[2 * i + k] * inv, up = v[32 + 2 * i + k] * inv;
+            hh[k] = gt * up * fast_sigmoid(gt);  // swish(x) = x * sigmoid(x) (common.hpp:37)
+          }
+          hw[i] = pack_bf16x2(hh[0], hh[1]);
+        }
+        tmem_st_32x32b_x16(tu, hw);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&h_full[ub]);
+      }
+      // ---- E3: x2 = bf16(x1 + down acc) -> HBM, row statistics
+      mbar_wait(d_full, dph);
+      dph ^= 1;
+      tc_fence_after();
+      // one partial per 64 columns, each summed in column order: the partition the unfused
+      // down-projection epilogue (BN = 128, two halves) writes, so row statistics match it bitwise
+      float ss2[kCols / 64];
+#pragma unroll
+      for (int i = 0; i < kCols / 64; ++i) ss2[i] = 0.f;
+#pragma unroll
+      for (int cc = 0; cc < kCols / 32; ++cc) {
+        float v[32];
+        tmem_row_chunk<32>(tD + cc * 32, v);
+        int4 o[4];
+#pragma unroll
+        for (int qd = 0; qd < 4; ++qd) {
+          const int4 x4 = lds_v4(x1s + sw128_off(r, (hf * kCols + cc * 32) / 8 + qd));
+          const __nv_bfloat162* x2p = reinterpret_cast<const __nv_bfloat162*>(&x4);
+          uint32_t w[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float2 f = __bfloat1622float2(x2p[k]);
+            w[k] = pack_bf16x2(f.x + v[qd * 8 + 2 * k], f.y + v[qd * 8 + 2 * k + 1]);
+            const float2 y = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&w[k]));
+            ss2[cc >> 1] = fmaf(y.x, y.x, fmaf(y.y, y.y, ss2[cc >> 1]));
+          }
+          o[qd] = make_int4(w[0], w[1], w[2], w[3]);
+        }
+        if (valid) {
+          int4* op = reinterpret_cast<int4*>(a.out + static_cast<size_t>(row) * D + hf * kCols + cc * 32);
+#pragma unroll
+          for (int qd = 0; qd < 4; ++qd) op[qd] = o[qd];
+        }
+      }
+      if (valid) {
+        float* so = a.ss_out + static_cast<size_t>(row) * 4;
+        if constexpr (D == 256) {
+          so[2 * hf] = ss2[0];
+          so[2 * hf + 1] = ss2[1];
+        } else {
+          so[hf] = ss2[0];
+          if (hf == 0) so[2] = so[3] = 0.f;
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(d_empty);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace sortk

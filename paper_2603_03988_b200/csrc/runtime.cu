@@ -12,6 +12,7 @@
 
 #include "../../include/sort_b200.h"
 #include "attention.cuh"
+#include "block_tail.cuh"
 #include "epilogues.cuh"
 #include "gemm.cuh"
 #include "misc.cuh"
@@ -51,6 +52,7 @@ struct LayerDev {
   CUtensorMap tmA_in, tmA_q, tmB_all, tmB_qg, tmB_kv, tmA_hg, tmB_o, tmB_up, tmA_hid, tmB_down;
   CUtensorMap tmQ, tmK, tmV;
   CUtensorMap tmRopeKV, tmRopeQ;  // per-row RoPE side tables for the K/V rows and the Q rows
+  CUtensorMap tmWo_t, tmWup_t, tmWdown_t;  // k_block_tail weight stages
 };
 
 struct Handle {
@@ -62,6 +64,7 @@ struct Handle {
   int d = 0, H = 0, dk = 0, m = 0, dh = 0, L0 = 0, Bmax = 0, num_sms = 148;
   std::map<std::string, HostParam> host;
   bool finalized = false;
+  bool fused_tail = true;  // sort_set_option("fused_tail")
   // device weights
   __nv_bfloat16 *item = nullptr, *action = nullptr, *scene = nullptr, *time = nullptr,
                 *prof = nullptr, *special = nullptr;
@@ -164,6 +167,11 @@ static const CUtensorMap& rope_table(Handle& h, int R, const std::vector<int32_t
     CK(cudaMemcpy(dev + static_cast<size_t>(b) * R * dk, one.data(), one.size() * 4, cudaMemcpyHostToDevice));
   const int box = std::min(dk, 32);
   return h.rope_tables[key] = make_tmap_2d_f32(dev, rows, dk, 128, box, box * 4);
+}
+
+// Shapes the fused block tail covers (TMEM: d accumulator + 2 x 128 hidden-chunk columns).
+static bool tail_supported(const Handle& h) {
+  return (h.d == 128 || h.d == 256) && h.m % 64 == 0 && h.m >= 64;
 }
 
 static void finalize(Handle& h) {
@@ -331,6 +339,11 @@ static void finalize(Handle& h) {
     L.tmRopeQ = rope_table(h, L.Rq, lp.pos_q);
     L.tmA_hid = make_tmap_2d(h.hid, Mq, m, m, 128, 64, 128);
     L.tmB_down = make_tmap_2d(L.w_down, d, m, m, L.bn_down, 64, 128);
+    if (tail_supported(h)) {
+      L.tmWo_t = make_tmap_2d(L.w_o, d, d, d, d, 64, 128);
+      L.tmWup_t = make_tmap_2d(L.w_up, 2 * m, d, d, 128, 64, 128);
+      L.tmWdown_t = make_tmap_2d(L.w_down, d, m, m, d, 64, 128);
+    }
     {
       const uint64_t BH = static_cast<uint64_t>(h.Bmax) * H;
       uint64_t dq[3] = {static_cast<uint64_t>(dk), static_cast<uint64_t>(L.Rq), BH};
@@ -462,6 +475,29 @@ static void launch_qkvg(Handle& h, const LayerDev& L, const CUtensorMap& A, cons
   }
 }
 
+template <int D>
+static void launch_tail_d(Handle& h, const LayerDev& L, __nv_bfloat16* Xq, float4* SSq, int M) {
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_block_tail<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(TailSmem<D>::bytes)));
+    attr = true;
+  }
+  TailArgs ta;
+  ta.resid = Xq;
+  ta.out = Xq;
+  ta.ss_out = reinterpret_cast<float*>(SSq);
+  ta.M = M;
+  ta.m = h.m;
+  ta.inv_d = 1.f / static_cast<float>(h.d);
+  const int num_m = (M + 127) / 128;
+  const int grid = std::min(num_m, h.num_sms);
+  k_block_tail<D><<<grid, kTailThreads, TailSmem<D>::bytes, h.stream>>>(L.tmA_hg, L.tmWo_t, L.tmWup_t,
+                                                                        L.tmWdown_t, ta);
+  check_launch("block_tail");
+  ++h.launches;
+}
+
 static void stage_mark(Handle& h, const std::string& name) {
   if (!h.timing) return;
   cudaEvent_t e;
@@ -558,6 +594,12 @@ static void run_layer(Handle& h, int l, int B, bool attn_only = false) {
   stage_mark(h, "L" + std::to_string(l) + ".qkvg");
   launch_attention(h, L, lp, B);
   stage_mark(h, "L" + std::to_string(l) + ".attention");
+  if (!attn_only && h.fused_tail && tail_supported(h)) {
+    if (d == 256) launch_tail_d<256>(h, L, Xq, SSq, B * L.Rq);
+    else launch_tail_d<128>(h, L, Xq, SSq, B * L.Rq);
+    stage_mark(h, "L" + std::to_string(l) + ".tail");
+    return;
+  }
   EpiResid eo;
   eo.resid = attn_only ? nullptr : Xq;
   eo.out = attn_only ? h.Qb : Xq;  // Q buffer is dead after attention
@@ -980,6 +1022,18 @@ int sort_enable_stage_timing(SortHandle p, int enable) {
     Handle* h = reinterpret_cast<Handle*>(p);
     if (!h) throw ConfigError("null handle");
     h->timing = enable != 0;
+  });
+}
+
+int sort_set_option(SortHandle p, const char* name, int32_t value) {
+  return api([&] {
+    Handle* h = reinterpret_cast<Handle*>(p);
+    if (!h || !name) throw ConfigError("null argument");
+    if (std::strcmp(name, "fused_tail") == 0) {
+      h->fused_tail = value != 0;
+    } else {
+      throw ConfigError(std::string("unknown option ") + name);
+    }
   });
 }
 

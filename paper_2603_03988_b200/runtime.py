@@ -54,7 +54,7 @@ EXPORTS = [
     "sort_load_param", "sort_finalize_params", "sort_forward", "sort_sync", "sort_forward_logits",
     "sort_tokenize", "sort_layer_plan", "sort_attention_forward", "sort_block_attention",
     "sort_time_bucket", "sort_geometric_schedule", "sort_retained_rows", "sort_mask_intervals",
-    "sort_kernel_count", "sort_enable_stage_timing", "sort_stage_times",
+    "sort_kernel_count", "sort_enable_stage_timing", "sort_stage_times", "sort_set_option",
 ]
 
 _lib = None
@@ -89,6 +89,7 @@ def lib():
                                           i32p, i32p, i32p, i32p]
         L.sort_kernel_count.argtypes = [C.c_void_p, i32p]
         L.sort_enable_stage_timing.argtypes = [C.c_void_p, C.c_int]
+        L.sort_set_option.argtypes = [C.c_void_p, C.c_char_p, C.c_int32]
         L.sort_stage_times.argtypes = [C.c_void_p, f32p, C.c_int32, i32p, C.c_char_p, C.c_int32]
         _lib = L
     return _lib
@@ -283,6 +284,11 @@ class SortModel:
         n = C.c_int32(0)
         _check(lib().sort_kernel_count(self.h, C.byref(n)))
         return n.value
+
+    def set_option(self, name: str, value: int):
+        """Kernel-selection knob (sort_set_option), e.g. ("fused_tail", 0) for the unfused
+        Wo / FFN GEMM chain."""
+        _check(lib().sort_set_option(self.h, name.encode(), int(value)))
 
     def enable_stage_timing(self, on: bool = True):
         _check(lib().sort_enable_stage_timing(self.h, int(on)))

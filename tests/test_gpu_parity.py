@@ -259,3 +259,38 @@ def test_all_zero_params_give_half(tiny):
     gm = R.SortModel(cfg, P, max_batch=1)
     p = gm.forward(synth.make_batch(cfg, 1, seed=1))
     assert np.all(p == 0.5)
+
+
+# ----------------------------------------------------------------------- fused block tail
+def test_fused_tail_bit_identical_to_unfused(base):
+    """k_block_tail (Wo + residual + SwishGLU FFN + residual in one kernel, x1 and the hidden
+    activation on chip) keeps the unfused GEMM chain's rounding points and K order, so the
+    logits are bitwise equal; B = 3 leaves a partial last 128-row tile in every layer."""
+    cfg, P, gm, _ = base
+    b = synth.make_batch(cfg, 3, seed=51)
+    p_f, z_f = gm.forward_logits(b)
+    gm.set_option("fused_tail", 0)
+    try:
+        p_u, z_u = gm.forward_logits(b)
+    finally:
+        gm.set_option("fused_tail", 1)
+    assert np.array_equal(z_f, z_u)
+    assert np.array_equal(p_f, p_u)
+
+
+def test_fused_tail_d128_vs_oracle():
+    cfg = base_config(model_dim=128, heads=4, ffn_dim=320, n_hist=300, n_cand=20,
+                      n_items=5000)
+    cfg.keep = [cfg.prefix_len, 128, 128, 64]
+    P = synth.make_params(cfg, seed=17)
+    gm, om = R.SortModel(cfg, P, max_batch=3), O.OracleModel(cfg, P)
+    b = synth.make_batch(cfg, 3, seed=18)
+    _, logits = gm.forward_logits(b)
+    ref = np.stack([om.forward(b, i)[1] for i in range(3)])
+    assert np.max(np.abs(logits - ref)) < LOGIT_MAX_ABS
+    assert rel_l2(logits, ref) < LOGIT_REL_L2
+
+
+def test_unknown_option_is_config_error(tiny):
+    with pytest.raises(R.ConfigError):
+        tiny[2].set_option("no_such_knob", 1)
