@@ -79,6 +79,7 @@ template <int D>
 __global__ void __launch_bounds__(kTailThreads, 1)
     k_block_tail(const __grid_constant__ CUtensorMap tmHg, const __grid_constant__ CUtensorMap tmWo,
                  const __grid_constant__ CUtensorMap tmWup, const __grid_constant__ CUtensorMap tmWdown,
+                 const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmOut,
                  const TailArgs a) {
   static_assert(D == 128 || D == 256, "block tail: model dim 128 or 256");
   using S = TailSmem<D>;
@@ -94,12 +95,15 @@ __global__ void __launch_bounds__(kTailThreads, 1)
   uint64_t* w_empty = bars + 3;            // [3]
   uint64_t* hg_full = bars + 6;
   uint64_t* hg_empty = bars + 7;
-  uint64_t* d_full = bars + 8;             // D1 ready, then D2 ready (two phases per tile)
+  uint64_t* d_full = bars + 8;             // down-projection accumulator ready
   uint64_t* d_empty = bars + 9;
   uint64_t* x1_full = bars + 10;
   uint64_t* u_full = bars + 11;            // [2]
   uint64_t* h_full = bars + 13;            // [2]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint64_t* wo_full = bars + 15;           // Wo accumulator (in the U columns) ready
+  uint64_t* res_full = bars + 16;          // residual tile landed in the x1 buffer (TMA)
+  uint64_t* x2_full = bars + 17;           // x2 written over x1 in smem, ready to store
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 18);
 
   const int warp = warp_id(), lane = lane_id();
   const int num_m = (a.M + 127) / 128;
@@ -110,6 +114,8 @@ __global__ void __launch_bounds__(kTailThreads, 1)
     tma_prefetch_desc(&tmWo);
     tma_prefetch_desc(&tmWup);
     tma_prefetch_desc(&tmWdown);
+    tma_prefetch_desc(&tmX);
+    tma_prefetch_desc(&tmOut);
     for (int s = 0; s < kTailStages; ++s) {
       mbar_init(&w_full[s], 1);
       mbar_init(&w_empty[s], 1);
@@ -117,6 +123,9 @@ __global__ void __launch_bounds__(kTailThreads, 1)
     mbar_init(hg_full, 1);
     mbar_init(hg_empty, 1);
     mbar_init(d_full, 1);
+    mbar_init(wo_full, 1);
+    mbar_init(res_full, 1);
+    mbar_init(x2_full, 256);
     mbar_init(d_empty, 256);
     mbar_init(x1_full, 256);
     for (int i = 0; i < 2; ++i) {
@@ -160,8 +169,12 @@ __global__ void __launch_bounds__(kTailThreads, 1)
           tma_load_2d(dst, &tmWo, &w_full[s], kb * 64, 0);
           advance();
         }
-        // the next tile's attention rows, as soon as this tile's Wo MMAs released the buffer
-        if (mb + static_cast<int>(gridDim.x) < num_m) load_hg(mb + gridDim.x, t + 1);
+        // the next tile's attention rows, as soon as this tile's Wo MMAs released the buffer,
+        // and its residual rows into L2 (the epilogue reads them a whole tile later)
+        if (mb + static_cast<int>(gridDim.x) < num_m) {
+          load_hg(mb + gridDim.x, t + 1);
+          for (uint32_t kb = 0; kb < kKB; ++kb) tma_prefetch_l2_2d(&tmX, kb * 64, (mb + gridDim.x) * 128);
+        }
         auto up = [&](int j) {
           for (int p = 0; p < static_cast<int>(kKB) / 2; ++p) {
             uint8_t* dst = stage(2 * kUpBox);
@@ -202,20 +215,21 @@ __global__ void __launch_bounds__(kTailThreads, 1)
       };
       int t = 0, c = 0;  // tile, global hidden-chunk counter (phases of u_full / h_full)
       for (int mb = blockIdx.x; mb < num_m; mb += gridDim.x, ++t) {
+        // Wo accumulates into the U columns [256, 256 + D): free once the previous tile's
+        // last down MMA was issued (in-order pipe), so it overlaps that tile's E3 drain of D
         mbar_wait_sleep(hg_full, t & 1);
-        mbar_wait_sleep(d_empty, (t & 1) ^ 1);  // E3 of the previous tile drained D
         tc_fence_after();
         for (uint32_t kb = 0; kb < kKB; ++kb) {
           const uint32_t b = wait_stage();
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            mma_bf16_ss(tmem, umma_sdesc_kmajor(hg0 + kb * 16384 + k * 32, 128),
+            mma_bf16_ss(tmem + 256, umma_sdesc_kmajor(hg0 + kb * 16384 + k * 32, 128),
                         umma_sdesc_kmajor(b + k * 32, 128), id_d, (kb | k) != 0 ? 1u : 0u);
           release_stage();
         }
         mma_commit(hg_empty);
-        mma_commit(d_full);
-        mbar_wait(x1_full, t & 1);  // x1 in smem, D drained by E1
+        mma_commit(wo_full);
+        mbar_wait(x1_full, t & 1);  // x1 in smem, Wo accumulator drained by E1
         tc_fence_after();
         auto up = [&](int j) {
           const uint32_t u = tmem + 256 + (j & 1) * 128;
@@ -238,6 +252,7 @@ __global__ void __launch_bounds__(kTailThreads, 1)
         for (int j = 0; j < n_chunks; ++j, ++c) {
           const int hb = c & 1;
           mbar_wait(&h_full[hb], (c >> 1) & 1);  // E2 wrote h_j over U[j&1]
+          if (j == 0) mbar_wait(d_empty, (t & 1) ^ 1);  // E3 of the previous tile drained D
           tc_fence_after();
           const uint32_t hbase = tmem + 256 + hb * 128;
           const uint32_t b = wait_stage();
@@ -251,6 +266,32 @@ __global__ void __launch_bounds__(kTailThreads, 1)
         mma_commit(d_full);
       }
     }
+  } else if (warp == 3) {
+    // I/O: the x1 buffer cycles residual tile (TMA load) -> x1 (E1, in place) -> x2 (E3, in
+    // place) -> TMA store; the next tile's residual lands once the store has read the buffer.
+    if (lane == 0) {
+      int t = 0;
+      for (int mb = blockIdx.x; mb < num_m; mb += gridDim.x, ++t) {
+        if (t > 0) {
+          mbar_wait_sleep(x2_full, (t - 1) & 1);
+          for (uint32_t kb = 0; kb < kKB; ++kb)
+            tma_store_2d(&tmOut, smem + S::oX1 + kb * 16384, kb * 64, (mb - gridDim.x) * 128);
+          bulk_commit();
+          bulk_wait_read0();
+        }
+        mbar_arrive_expect_tx(res_full, S::kTileBytes);
+        for (uint32_t kb = 0; kb < kKB; ++kb)
+          tma_load_2d(smem + S::oX1 + kb * 16384, &tmX, res_full, kb * 64, mb * 128);
+      }
+      if (t > 0) {
+        mbar_wait_sleep(x2_full, (t - 1) & 1);
+        for (uint32_t kb = 0; kb < kKB; ++kb)
+          tma_store_2d(&tmOut, smem + S::oX1 + kb * 16384, kb * 64,
+                       (blockIdx.x + (t - 1) * gridDim.x) * 128);
+        bulk_commit();
+        bulk_wait0();
+      }
+    }
   } else if (warp >= 4) {
     const int e = warp - 4;
     const int q = e & 3, hf = e >> 2;
@@ -260,31 +301,22 @@ __global__ void __launch_bounds__(kTailThreads, 1)
     const uint32_t x1s = smem_u32(smem + S::oX1);
     float* s_ss = reinterpret_cast<float*>(smem + S::oSS);
     int t = 0, c = 0;
-    uint32_t dph = 0;
     for (int mb = blockIdx.x; mb < num_m; mb += gridDim.x, ++t) {
       const int row = mb * 128 + r;
       const bool valid = row < a.M;
-      int4 rv[kCols / 8];
-      if (valid) {
-        const int4* rp = reinterpret_cast<const int4*>(a.resid + static_cast<size_t>(row) * D + hf * kCols);
-#pragma unroll
-        for (int i = 0; i < kCols / 8; ++i) rv[i] = rp[i];
-      } else {
-#pragma unroll
-        for (int i = 0; i < kCols / 8; ++i) rv[i] = make_int4(0, 0, 0, 0);
-      }
-      // ---- E1: x1 = bf16(resid + Wo acc) -> smem A tile; sum of squares
-      mbar_wait(d_full, dph);
-      dph ^= 1;
+      // ---- E1: x1 = bf16(resid + Wo acc) -> smem A tile (in place over the residual tile)
+      mbar_wait(res_full, t & 1);
+      mbar_wait(wo_full, t & 1);
       tc_fence_after();
       float ss = 0.f;
 #pragma unroll
       for (int cc = 0; cc < kCols / 32; ++cc) {
         float v[32];
-        tmem_row_chunk<32>(tD + cc * 32, v);
+        tmem_row_chunk<32>(tmem + lane_off + 256 + hf * kCols + cc * 32, v);
 #pragma unroll
         for (int qd = 0; qd < 4; ++qd) {
-          const int4 r4 = rv[cc * 4 + qd];
+          const uint32_t adr = x1s + sw128_off(r, (hf * kCols + cc * 32) / 8 + qd);
+          const int4 r4 = lds_v4(adr);
           const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&r4);
           uint32_t w[4];
 #pragma unroll
@@ -294,7 +326,7 @@ __global__ void __launch_bounds__(kTailThreads, 1)
             const float2 y = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&w[k]));
             ss = fmaf(y.x, y.x, fmaf(y.y, y.y, ss));
           }
-          sts_v4(x1s + sw128_off(r, (hf * kCols + cc * 32) / 8 + qd), make_int4(w[0], w[1], w[2], w[3]));
+          sts_v4(adr, make_int4(w[0], w[1], w[2], w[3]));
         }
       }
       s_ss[hf * 128 + r] = ss;
@@ -329,8 +361,7 @@ __global__ void __launch_bounds__(kTailThreads, 1)
         mbar_arrive(&h_full[ub]);
       }
       // ---- E3: x2 = bf16(x1 + down acc) -> HBM, row statistics
-      mbar_wait(d_full, dph);
-      dph ^= 1;
+      mbar_wait(d_full, t & 1);
       tc_fence_after();
       // one partial per 64 columns, each summed in column order: the partition the unfused
       // down-projection epilogue (BN = 128, two halves) writes, so row statistics match it bitwise
@@ -341,10 +372,10 @@ __global__ void __launch_bounds__(kTailThreads, 1)
       for (int cc = 0; cc < kCols / 32; ++cc) {
         float v[32];
         tmem_row_chunk<32>(tD + cc * 32, v);
-        int4 o[4];
 #pragma unroll
         for (int qd = 0; qd < 4; ++qd) {
-          const int4 x4 = lds_v4(x1s + sw128_off(r, (hf * kCols + cc * 32) / 8 + qd));
+          const uint32_t adr = x1s + sw128_off(r, (hf * kCols + cc * 32) / 8 + qd);
+          const int4 x4 = lds_v4(adr);
           const __nv_bfloat162* x2p = reinterpret_cast<const __nv_bfloat162*>(&x4);
           uint32_t w[4];
 #pragma unroll
@@ -354,19 +385,15 @@ __global__ void __launch_bounds__(kTailThreads, 1)
             const float2 y = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&w[k]));
             ss2[cc >> 1] = fmaf(y.x, y.x, fmaf(y.y, y.y, ss2[cc >> 1]));
           }
-          o[qd] = make_int4(w[0], w[1], w[2], w[3]);
-        }
-        if (valid) {
-          int4* op = reinterpret_cast<int4*>(a.out + static_cast<size_t>(row) * D + hf * kCols + cc * 32);
-#pragma unroll
-          for (int qd = 0; qd < 4; ++qd) op[qd] = o[qd];
+          sts_v4(adr, make_int4(w[0], w[1], w[2], w[3]));
         }
       }
+      fence_proxy_async_smem();  // x2 tile -> TMA store (async proxy)
+      mbar_arrive(x2_full);
       if (valid) {
         float* so = a.ss_out + static_cast<size_t>(row) * 4;
         if constexpr (D == 256) {
-          so[2 * hf] = ss2[0];
-          so[2 * hf + 1] = ss2[1];
+          *reinterpret_cast<float2*>(so + 2 * hf) = make_float2(ss2[0], ss2[1]);
         } else {
           so[hf] = ss2[0];
           if (hf == 0) so[2] = so[3] = 0.f;

@@ -493,7 +493,7 @@ static void launch_tail_d(Handle& h, const LayerDev& L, __nv_bfloat16* Xq, float
   const int num_m = (M + 127) / 128;
   const int grid = std::min(num_m, h.num_sms);
   k_block_tail<D><<<grid, kTailThreads, TailSmem<D>::bytes, h.stream>>>(L.tmA_hg, L.tmWo_t, L.tmWup_t,
-                                                                        L.tmWdown_t, ta);
+                                                                        L.tmWdown_t, L.tmA_q, L.tmA_q, ta);
   check_launch("block_tail");
   ++h.launches;
 }
