@@ -40,19 +40,16 @@ constexpr uint32_t kTailStageBytes = 32768;
 template <int D>
 struct TailSmem {
   static constexpr uint32_t kTileBytes = 128u * D * 2;  // 128 rows x D bf16 (D/64 K-blocks)
-  static constexpr uint32_t oHg = 0;
-  static constexpr uint32_t oX1 = oHg + kTileBytes;
-  static constexpr uint32_t oW = oX1 + kTileBytes;
+  static constexpr uint32_t oX = 0;                     // two tile buffers (tile t uses t & 1)
+  static constexpr uint32_t oW = oX + 2 * kTileBytes;
   static constexpr uint32_t oSS = oW + kTailStages * kTailStageBytes;  // [2][128] fp32
   static constexpr uint32_t oBar = oSS + 1024;
   static constexpr uint32_t bytes = oBar + 256 + 1024;  // + alignment slack
 };
 
 struct TailArgs {
-  const __nv_bfloat16* resid;  // [M, D] residual rows P(x, L_out) (may alias out)
-  __nv_bfloat16* out;          // [M, D]
-  float* ss_out;               // [M, 4] sum-of-squares partials of out
-  int M, m;                    // rows, FFN hidden width
+  float* ss_out;  // [M, 4] sum-of-squares partials of the output rows
+  int M, m;       // rows, FFN hidden width
   float inv_d;
 };
 
@@ -75,6 +72,11 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int c16) {
   return static_cast<uint32_t>((c16 >> 3) * 16384 + r * 128 + (((c16 & 7) ^ (r & 7)) << 4));
 }
 
+// Tile buffer life cycle (buffer t & 1, 64 KB, SW128 K-major):
+//   Hg(t) (TMA, io warp) -> Wo MMAs -> residual rows of t (TMA, io warp) -> x1 (E1, in place)
+//   -> up MMAs -> x2 (E3, in place) -> TMA store (io warp) -> Hg(t + 2)
+// The other buffer meanwhile drains tile t-1 and prefetches Hg(t+1), so the previous tile's
+// drain overlaps this tile's Wo MMAs and nothing waits on a store.
 template <int D>
 __global__ void __launch_bounds__(kTailThreads, 1)
     k_block_tail(const __grid_constant__ CUtensorMap tmHg, const __grid_constant__ CUtensorMap tmWo,
@@ -83,7 +85,7 @@ __global__ void __launch_bounds__(kTailThreads, 1)
                  const TailArgs a) {
   static_assert(D == 128 || D == 256, "block tail: model dim 128 or 256");
   using S = TailSmem<D>;
-  constexpr uint32_t kKB = D / 64;              // K-blocks of the Hg / x1 tiles
+  constexpr uint32_t kKB = D / 64;              // K-blocks of a tile buffer
   constexpr uint32_t kWoStage = D * 128u;       // one K-block of Wo^T: D rows x 64 K
   constexpr uint32_t kDownStage = D * 128u;     // Wdown_j^T: D rows x 64 K
   constexpr uint32_t kUpBox = 128u * 128u;      // 128 rows x 64 K of the interleaved W_up
@@ -91,23 +93,23 @@ __global__ void __launch_bounds__(kTailThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem_1k(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::oBar);
-  uint64_t* w_full = bars;                 // [3]
-  uint64_t* w_empty = bars + 3;            // [3]
-  uint64_t* hg_full = bars + 6;
-  uint64_t* hg_empty = bars + 7;
-  uint64_t* d_full = bars + 8;             // down-projection accumulator ready
-  uint64_t* d_empty = bars + 9;
-  uint64_t* x1_full = bars + 10;
-  uint64_t* u_full = bars + 11;            // [2]
-  uint64_t* h_full = bars + 13;            // [2]
-  uint64_t* wo_full = bars + 15;           // Wo accumulator (in the U columns) ready
-  uint64_t* res_full = bars + 16;          // residual tile landed in the x1 buffer (TMA)
-  uint64_t* x2_full = bars + 17;           // x2 written over x1 in smem, ready to store
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 18);
+  uint64_t* w_full = bars;        // [3] weight ring
+  uint64_t* w_empty = bars + 3;   // [3]
+  uint64_t* hg_full = bars + 6;   // Hg(t) landed (one phase per tile)
+  uint64_t* wo_full = bars + 7;   // Wo accumulator (U columns) ready, Hg(t) consumed
+  uint64_t* res_full = bars + 8;  // residual rows of t landed over Hg(t)
+  uint64_t* x1_full = bars + 9;   // x1 in smem, Wo accumulator drained
+  uint64_t* u_full = bars + 10;   // [2] up-projection chunk accumulators
+  uint64_t* h_full = bars + 12;   // [2] SwiGLU output written over them
+  uint64_t* d_full = bars + 14;   // down-projection accumulator ready
+  uint64_t* d_empty = bars + 15;  // ... drained by E3
+  uint64_t* x2_full = bars + 16;  // x2 over x1 in smem, ready to store
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 17);
 
   const int warp = warp_id(), lane = lane_id();
   const int num_m = (a.M + 127) / 128;
   const int n_chunks = a.m / 64;
+  auto xbuf = [&](int t) { return smem + S::oX + (t & 1) * S::kTileBytes; };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmHg);
@@ -121,17 +123,16 @@ __global__ void __launch_bounds__(kTailThreads, 1)
       mbar_init(&w_empty[s], 1);
     }
     mbar_init(hg_full, 1);
-    mbar_init(hg_empty, 1);
-    mbar_init(d_full, 1);
     mbar_init(wo_full, 1);
     mbar_init(res_full, 1);
-    mbar_init(x2_full, 256);
-    mbar_init(d_empty, 256);
     mbar_init(x1_full, 256);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&u_full[i], 1);
       mbar_init(&h_full[i], 256);
     }
+    mbar_init(d_full, 1);
+    mbar_init(d_empty, 256);
+    mbar_init(x2_full, 256);
     mbar_fence_init();
   }
   if (warp == 2) tmem_alloc(tslot, 512);
@@ -141,6 +142,7 @@ __global__ void __launch_bounds__(kTailThreads, 1)
   const uint32_t tmem = *tslot;
 
   if (warp == 0) {
+    // ---------------------------------------------------------------- weight stream
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
@@ -155,34 +157,20 @@ __global__ void __launch_bounds__(kTailThreads, 1)
           ph ^= 1;
         }
       };
-      auto load_hg = [&](int mb, int t) {
-        mbar_wait_sleep(hg_empty, (t & 1) ^ 1);
-        mbar_arrive_expect_tx(hg_full, S::kTileBytes);
-        for (uint32_t kb = 0; kb < kKB; ++kb)
-          tma_load_2d(smem + S::oHg + kb * 16384, &tmHg, hg_full, kb * 64, mb * 128);
+      auto up = [&](int j) {
+        for (int p = 0; p < static_cast<int>(kKB) / 2; ++p) {
+          uint8_t* dst = stage(2 * kUpBox);
+          tma_load_2d(dst, &tmWup, &w_full[s], (2 * p) * 64, j * 128);
+          tma_load_2d(dst + kUpBox, &tmWup, &w_full[s], (2 * p + 1) * 64, j * 128);
+          advance();
+        }
       };
-      int t = 0;
-      if (static_cast<int>(blockIdx.x) < num_m) load_hg(blockIdx.x, 0);
-      for (int mb = blockIdx.x; mb < num_m; mb += gridDim.x, ++t) {
+      for (int mb = blockIdx.x; mb < num_m; mb += gridDim.x) {
         for (uint32_t kb = 0; kb < kKB; ++kb) {  // Wo^T K-blocks
           uint8_t* dst = stage(kWoStage);
           tma_load_2d(dst, &tmWo, &w_full[s], kb * 64, 0);
           advance();
         }
-        // the next tile's attention rows, as soon as this tile's Wo MMAs released the buffer,
-        // and its residual rows into L2 (the epilogue reads them a whole tile later)
-        if (mb + static_cast<int>(gridDim.x) < num_m) {
-          load_hg(mb + gridDim.x, t + 1);
-          for (uint32_t kb = 0; kb < kKB; ++kb) tma_prefetch_l2_2d(&tmX, kb * 64, (mb + gridDim.x) * 128);
-        }
-        auto up = [&](int j) {
-          for (int p = 0; p < static_cast<int>(kKB) / 2; ++p) {
-            uint8_t* dst = stage(2 * kUpBox);
-            tma_load_2d(dst, &tmWup, &w_full[s], (2 * p) * 64, j * 128);
-            tma_load_2d(dst + kUpBox, &tmWup, &w_full[s], (2 * p + 1) * 64, j * 128);
-            advance();
-          }
-        };
         up(0);
         if (n_chunks > 1) up(1);
         for (int j = 0; j < n_chunks; ++j) {
@@ -194,10 +182,10 @@ __global__ void __launch_bounds__(kTailThreads, 1)
       }
     }
   } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
     if (lane == 0) {
       const uint32_t id_d = umma_idesc_bf16(128, D);
       const uint32_t id_u = umma_idesc_bf16(128, 128);
-      const uint32_t hg0 = smem_u32(smem + S::oHg), x10 = smem_u32(smem + S::oX1);
       const uint32_t w0 = smem_u32(smem + S::oW);
       int s = 0;
       uint32_t ph = 0;
@@ -215,6 +203,7 @@ __global__ void __launch_bounds__(kTailThreads, 1)
       };
       int t = 0, c = 0;  // tile, global hidden-chunk counter (phases of u_full / h_full)
       for (int mb = blockIdx.x; mb < num_m; mb += gridDim.x, ++t) {
+        const uint32_t xb = smem_u32(xbuf(t));
         // Wo accumulates into the U columns [256, 256 + D): free once the previous tile's
         // last down MMA was issued (in-order pipe), so it overlaps that tile's E3 drain of D
         mbar_wait_sleep(hg_full, t & 1);
@@ -223,11 +212,10 @@ __global__ void __launch_bounds__(kTailThreads, 1)
           const uint32_t b = wait_stage();
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            mma_bf16_ss(tmem + 256, umma_sdesc_kmajor(hg0 + kb * 16384 + k * 32, 128),
+            mma_bf16_ss(tmem + 256, umma_sdesc_kmajor(xb + kb * 16384 + k * 32, 128),
                         umma_sdesc_kmajor(b + k * 32, 128), id_d, (kb | k) != 0 ? 1u : 0u);
           release_stage();
         }
-        mma_commit(hg_empty);
         mma_commit(wo_full);
         mbar_wait(x1_full, t & 1);  // x1 in smem, Wo accumulator drained by E1
         tc_fence_after();
@@ -240,7 +228,7 @@ __global__ void __launch_bounds__(kTailThreads, 1)
               const uint32_t kb = 2 * p + kh;
 #pragma unroll
               for (int k = 0; k < 4; ++k)
-                mma_bf16_ss(u, umma_sdesc_kmajor(x10 + kb * 16384 + k * 32, 128),
+                mma_bf16_ss(u, umma_sdesc_kmajor(xb + kb * 16384 + k * 32, 128),
                             umma_sdesc_kmajor(b + kh * kUpBox + k * 32, 128), id_u, (kb | k) != 0 ? 1u : 0u);
             }
             release_stage();
@@ -267,46 +255,55 @@ __global__ void __launch_bounds__(kTailThreads, 1)
       }
     }
   } else if (warp == 3) {
-    // I/O: the x1 buffer cycles residual tile (TMA load) -> x1 (E1, in place) -> x2 (E3, in
-    // place) -> TMA store; the next tile's residual lands once the store has read the buffer.
+    // ---------------------------------------------------------------- tile I/O (TMA)
     if (lane == 0) {
+      auto load_hg = [&](int mb, int t) {
+        mbar_arrive_expect_tx(hg_full, S::kTileBytes);
+        for (uint32_t kb = 0; kb < kKB; ++kb)
+          tma_load_2d(xbuf(t) + kb * 16384, &tmHg, hg_full, kb * 64, mb * 128);
+      };
+      auto store_x2 = [&](int mb, int t) {
+        mbar_wait_sleep(x2_full, t & 1);
+        for (uint32_t kb = 0; kb < kKB; ++kb) tma_store_2d(&tmOut, xbuf(t) + kb * 16384, kb * 64, mb * 128);
+        bulk_commit();
+      };
       int t = 0;
+      if (static_cast<int>(blockIdx.x) < num_m) load_hg(blockIdx.x, 0);
       for (int mb = blockIdx.x; mb < num_m; mb += gridDim.x, ++t) {
+        const int next = mb + gridDim.x;
+        if (next < num_m)  // residual rows of t+1 into L2 ahead of their TMA load
+          for (uint32_t kb = 0; kb < kKB; ++kb) tma_prefetch_l2_2d(&tmX, kb * 64, next * 128);
+        // residual rows of t over the consumed Hg(t)
+        mbar_wait_sleep(wo_full, t & 1);
+        mbar_arrive_expect_tx(res_full, S::kTileBytes);
+        for (uint32_t kb = 0; kb < kKB; ++kb) tma_load_2d(xbuf(t) + kb * 16384, &tmX, res_full, kb * 64, mb * 128);
+        // drain tile t-1 from the other buffer, then prefetch Hg(t+1) into it
         if (t > 0) {
-          mbar_wait_sleep(x2_full, (t - 1) & 1);
-          for (uint32_t kb = 0; kb < kKB; ++kb)
-            tma_store_2d(&tmOut, smem + S::oX1 + kb * 16384, kb * 64, (mb - gridDim.x) * 128);
-          bulk_commit();
+          store_x2(mb - gridDim.x, t - 1);
           bulk_wait_read0();
         }
-        mbar_arrive_expect_tx(res_full, S::kTileBytes);
-        for (uint32_t kb = 0; kb < kKB; ++kb)
-          tma_load_2d(smem + S::oX1 + kb * 16384, &tmX, res_full, kb * 64, mb * 128);
+        if (next < num_m) load_hg(next, t + 1);
       }
       if (t > 0) {
-        mbar_wait_sleep(x2_full, (t - 1) & 1);
-        for (uint32_t kb = 0; kb < kKB; ++kb)
-          tma_store_2d(&tmOut, smem + S::oX1 + kb * 16384, kb * 64,
-                       (blockIdx.x + (t - 1) * gridDim.x) * 128);
-        bulk_commit();
+        store_x2(blockIdx.x + (t - 1) * gridDim.x, t - 1);
         bulk_wait0();
       }
     }
   } else if (warp >= 4) {
+    // ---------------------------------------------------------------- epilogue warps
     const int e = warp - 4;
     const int q = e & 3, hf = e >> 2;
     const int r = q * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
     const uint32_t tD = tmem + lane_off + hf * kCols;
-    const uint32_t x1s = smem_u32(smem + S::oX1);
     float* s_ss = reinterpret_cast<float*>(smem + S::oSS);
     int t = 0, c = 0;
     for (int mb = blockIdx.x; mb < num_m; mb += gridDim.x, ++t) {
       const int row = mb * 128 + r;
-      const bool valid = row < a.M;
-      // ---- E1: x1 = bf16(resid + Wo acc) -> smem A tile (in place over the residual tile)
-      mbar_wait(res_full, t & 1);
+      const uint32_t xs = smem_u32(xbuf(t));
+      // ---- E1: x1 = bf16(resid + Wo acc) in place over the residual tile; sum of squares
       mbar_wait(wo_full, t & 1);
+      mbar_wait(res_full, t & 1);
       tc_fence_after();
       float ss = 0.f;
 #pragma unroll
@@ -315,7 +312,7 @@ __global__ void __launch_bounds__(kTailThreads, 1)
         tmem_row_chunk<32>(tmem + lane_off + 256 + hf * kCols + cc * 32, v);
 #pragma unroll
         for (int qd = 0; qd < 4; ++qd) {
-          const uint32_t adr = x1s + sw128_off(r, (hf * kCols + cc * 32) / 8 + qd);
+          const uint32_t adr = xs + sw128_off(r, (hf * kCols + cc * 32) / 8 + qd);
           const int4 r4 = lds_v4(adr);
           const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&r4);
           uint32_t w[4];
@@ -360,7 +357,7 @@ __global__ void __launch_bounds__(kTailThreads, 1)
         tc_fence_before();
         mbar_arrive(&h_full[ub]);
       }
-      // ---- E3: x2 = bf16(x1 + down acc) -> HBM, row statistics
+      // ---- E3: x2 = bf16(x1 + down acc) in place -> TMA store; row statistics
       mbar_wait(d_full, t & 1);
       tc_fence_after();
       // one partial per 64 columns, each summed in column order: the partition the unfused
@@ -374,7 +371,7 @@ __global__ void __launch_bounds__(kTailThreads, 1)
         tmem_row_chunk<32>(tD + cc * 32, v);
 #pragma unroll
         for (int qd = 0; qd < 4; ++qd) {
-          const uint32_t adr = x1s + sw128_off(r, (hf * kCols + cc * 32) / 8 + qd);
+          const uint32_t adr = xs + sw128_off(r, (hf * kCols + cc * 32) / 8 + qd);
           const int4 x4 = lds_v4(adr);
           const __nv_bfloat162* x2p = reinterpret_cast<const __nv_bfloat162*>(&x4);
           uint32_t w[4];
@@ -388,9 +385,11 @@ __global__ void __launch_bounds__(kTailThreads, 1)
           sts_v4(adr, make_int4(w[0], w[1], w[2], w[3]));
         }
       }
+      tc_fence_before();
+      mbar_arrive(d_empty);
       fence_proxy_async_smem();  // x2 tile -> TMA store (async proxy)
       mbar_arrive(x2_full);
-      if (valid) {
+      if (row < a.M) {
         float* so = a.ss_out + static_cast<size_t>(row) * 4;
         if constexpr (D == 256) {
           *reinterpret_cast<float2*>(so + 2 * hf) = make_float2(ss2[0], ss2[1]);
@@ -399,8 +398,6 @@ __global__ void __launch_bounds__(kTailThreads, 1)
           if (hf == 0) so[2] = so[3] = 0.f;
         }
       }
-      tc_fence_before();
-      mbar_arrive(d_empty);
     }
   }
   tc_fence_before();

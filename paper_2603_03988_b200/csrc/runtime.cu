@@ -484,8 +484,6 @@ static void launch_tail_d(Handle& h, const LayerDev& L, __nv_bfloat16* Xq, float
     attr = true;
   }
   TailArgs ta;
-  ta.resid = Xq;
-  ta.out = Xq;
   ta.ss_out = reinterpret_cast<float*>(SSq);
   ta.M = M;
   ta.m = h.m;
