@@ -97,14 +97,15 @@ __global__ void __launch_bounds__(kTailThreads, 1)
   uint64_t* w_empty = bars + 3;   // [3]
   uint64_t* hg_full = bars + 6;   // Hg(t) landed (one phase per tile)
   uint64_t* wo_full = bars + 7;   // Wo accumulator (U columns) ready, Hg(t) consumed
-  uint64_t* res_full = bars + 8;  // residual rows of t landed over Hg(t)
-  uint64_t* x1_full = bars + 9;   // x1 in smem, Wo accumulator drained
+  uint64_t* hg_kb = bars + 18;    // [4] Hg(t) K-block kb consumed by the Wo MMAs
+  uint64_t* res_full = bars + 22; // [4] residual K-block kb of t landed over Hg(t)
+  uint64_t* x1_kb = bars + 26;    // [4] x1 K-block kb in smem (its Wo accumulator columns read)
   uint64_t* u_full = bars + 10;   // [2] up-projection chunk accumulators
   uint64_t* h_full = bars + 12;   // [2] SwiGLU output written over them
   uint64_t* d_full = bars + 14;   // down-projection accumulator ready
   uint64_t* d_empty = bars + 15;  // ... drained by E3
   uint64_t* x2_full = bars + 16;  // x2 over x1 in smem, ready to store
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 17);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 30);
 
   const int warp = warp_id(), lane = lane_id();
   const int num_m = (a.M + 127) / 128;
@@ -124,8 +125,11 @@ __global__ void __launch_bounds__(kTailThreads, 1)
     }
     mbar_init(hg_full, 1);
     mbar_init(wo_full, 1);
-    mbar_init(res_full, 1);
-    mbar_init(x1_full, 256);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&hg_kb[i], 1);
+      mbar_init(&res_full[i], 1);
+      mbar_init(&x1_kb[i], 128);
+    }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&u_full[i], 1);
       mbar_init(&h_full[i], 256);
@@ -215,9 +219,13 @@ __global__ void __launch_bounds__(kTailThreads, 1)
             mma_bf16_ss(tmem + 256, umma_sdesc_kmajor(xb + kb * 16384 + k * 32, 128),
                         umma_sdesc_kmajor(b + k * 32, 128), id_d, (kb | k) != 0 ? 1u : 0u);
           release_stage();
+          mma_commit(&hg_kb[kb]);  // the residual K-block may overwrite it now
         }
         mma_commit(wo_full);
-        mbar_wait(x1_full, t & 1);  // x1 in smem, Wo accumulator drained by E1
+        // up(0) overwrites the Wo accumulator columns of K-blocks 0 and 1 (U0): both must have
+        // been read; later K-blocks of x1 are waited for one by one (E1 runs a K-block ahead)
+        mbar_wait(&x1_kb[0], t & 1);
+        mbar_wait(&x1_kb[1], t & 1);
         tc_fence_after();
         auto up = [&](int j) {
           const uint32_t u = tmem + 256 + (j & 1) * 128;
@@ -226,6 +234,10 @@ __global__ void __launch_bounds__(kTailThreads, 1)
 #pragma unroll
             for (uint32_t kh = 0; kh < 2; ++kh) {
               const uint32_t kb = 2 * p + kh;
+              if (j == 0 && kb >= 2) {
+                mbar_wait(&x1_kb[kb], t & 1);
+                tc_fence_after();
+              }
 #pragma unroll
               for (int k = 0; k < 4; ++k)
                 mma_bf16_ss(u, umma_sdesc_kmajor(xb + kb * 16384 + k * 32, 128),
@@ -274,9 +286,11 @@ __global__ void __launch_bounds__(kTailThreads, 1)
         if (next < num_m)  // residual rows of t+1 into L2 ahead of their TMA load
           for (uint32_t kb = 0; kb < kKB; ++kb) tma_prefetch_l2_2d(&tmX, kb * 64, next * 128);
         // residual rows of t over the consumed Hg(t)
-        mbar_wait_sleep(wo_full, t & 1);
-        mbar_arrive_expect_tx(res_full, S::kTileBytes);
-        for (uint32_t kb = 0; kb < kKB; ++kb) tma_load_2d(xbuf(t) + kb * 16384, &tmX, res_full, kb * 64, mb * 128);
+        for (uint32_t kb = 0; kb < kKB; ++kb) {
+          mbar_wait_sleep(&hg_kb[kb], t & 1);
+          mbar_arrive_expect_tx(&res_full[kb], 16384);
+          tma_load_2d(xbuf(t) + kb * 16384, &tmX, &res_full[kb], kb * 64, mb * 128);
+        }
         // drain tile t-1 from the other buffer, then prefetch Hg(t+1) into it
         if (t > 0) {
           store_x2(mb - gridDim.x, t - 1);
@@ -301,38 +315,59 @@ __global__ void __launch_bounds__(kTailThreads, 1)
     for (int mb = blockIdx.x; mb < num_m; mb += gridDim.x, ++t) {
       const int row = mb * 128 + r;
       const uint32_t xs = smem_u32(xbuf(t));
-      // ---- E1: x1 = bf16(resid + Wo acc) in place over the residual tile; sum of squares
+      // ---- E1: x1 = bf16(resid + Wo acc) in place over the residual tile, one K-block per
+      // pass (half hf takes K-blocks hf, hf + 2, ...), so the up MMAs start after the first
+      // pass; per-64-column sums of squares, combined as (s0 + s1) + (s2 + s3) like the
+      // unfused residual epilogue's row statistics
       mbar_wait(wo_full, t & 1);
-      mbar_wait(res_full, t & 1);
       tc_fence_after();
-      float ss = 0.f;
+      float ssb[kKB / 2];
 #pragma unroll
-      for (int cc = 0; cc < kCols / 32; ++cc) {
-        float v[32];
-        tmem_row_chunk<32>(tmem + lane_off + 256 + hf * kCols + cc * 32, v);
+      for (int p = 0; p < static_cast<int>(kKB) / 2; ++p) {
+        const int kb = 2 * p + hf;
+        mbar_wait(&res_full[kb], t & 1);
+        float ss = 0.f;
 #pragma unroll
-        for (int qd = 0; qd < 4; ++qd) {
-          const uint32_t adr = xs + sw128_off(r, (hf * kCols + cc * 32) / 8 + qd);
-          const int4 r4 = lds_v4(adr);
-          const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&r4);
-          uint32_t w[4];
+        for (int cc = 0; cc < 2; ++cc) {
+          float v[32];
+          tmem_row_chunk<32>(tmem + lane_off + 256 + kb * 64 + cc * 32, v);
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const float2 f = __bfloat1622float2(r2[k]);
-            w[k] = pack_bf16x2(f.x + v[qd * 8 + 2 * k], f.y + v[qd * 8 + 2 * k + 1]);
-            const float2 y = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&w[k]));
-            ss = fmaf(y.x, y.x, fmaf(y.y, y.y, ss));
+          for (int qd = 0; qd < 4; ++qd) {
+            const uint32_t adr = xs + sw128_off(r, kb * 8 + cc * 4 + qd);
+            const int4 r4 = lds_v4(adr);
+            const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&r4);
+            uint32_t w[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float2 f = __bfloat1622float2(r2[k]);
+              w[k] = pack_bf16x2(f.x + v[qd * 8 + 2 * k], f.y + v[qd * 8 + 2 * k + 1]);
+              const float2 y = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&w[k]));
+              ss = fmaf(y.x, y.x, fmaf(y.y, y.y, ss));
+            }
+            sts_v4(adr, make_int4(w[0], w[1], w[2], w[3]));
           }
-          sts_v4(adr, make_int4(w[0], w[1], w[2], w[3]));
         }
+        ssb[p] = ss;
+        fence_proxy_async_smem();
+        tc_fence_before();
+        mbar_arrive(&x1_kb[kb]);
       }
-      s_ss[hf * 128 + r] = ss;
-      named_bar_sync(1 + q, 64);
-      const float ss1 = s_ss[r] + s_ss[128 + r];
+      float ss1;
+      if constexpr (kKB == 4) {  // hf 0 holds s0, s2; hf 1 holds s1, s3
+        s_ss[hf * 128 + r] = hf == 0 ? ssb[1] : ssb[0];
+        named_bar_sync(1 + q, 64);
+        const float o = s_ss[(1 - hf) * 128 + r];
+        const float pair = hf == 0 ? ssb[0] + o : o + ssb[1];  // s0 + s1 | s2 + s3
+        named_bar_sync(1 + q, 64);
+        s_ss[hf * 128 + r] = pair;
+        named_bar_sync(1 + q, 64);
+        ss1 = s_ss[r] + s_ss[128 + r];
+      } else {
+        s_ss[hf * 128 + r] = ssb[0];
+        named_bar_sync(1 + q, 64);
+        ss1 = s_ss[r] + s_ss[128 + r];
+      }
       const float inv = row_inv_rms(ss1, a.inv_d);
-      fence_proxy_async_smem();
-      tc_fence_before();
-      mbar_arrive(x1_full);
       // ---- E2 per hidden chunk: h = swish(g/rms) * (u/rms), bf16 pairs in place in TMEM
       for (int j = 0; j < n_chunks; ++j, ++c) {
         const int ub = c & 1;

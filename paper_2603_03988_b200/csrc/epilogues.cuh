@@ -203,7 +203,9 @@ struct EpiResid {
       for (int i = 0; i < 16; ++i) rv[i] = make_int4(0, 0, 0, 0);
     }
     wait();
-    float ss = 0.f;
+    // sum of squares per 64-column block of the row (slot = block index), each summed in
+    // column order; spans narrower than 64 columns (d = 64) fall back to one slot per part
+    float ssb[2] = {0.f, 0.f};
 #pragma unroll
     for (int cc = 0; cc < 4; ++cc) {
       const int c = c0 + cc * 32;
@@ -222,7 +224,7 @@ struct EpiResid {
           const float2 f = __bfloat1622float2(r2[e]);
           w[e] = pack_bf16x2(f.x + v[qd * 8 + 2 * e], f.y + v[qd * 8 + 2 * e + 1]);
           const float2 y = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&w[e]));
-          ss = fmaf(y.x, y.x, fmaf(y.y, y.y, ss));
+          ssb[cc >> 1] = fmaf(y.x, y.x, fmaf(y.y, y.y, ssb[cc >> 1]));
         }
         o[qd] = make_int4(w[0], w[1], w[2], w[3]);
       }
@@ -230,12 +232,18 @@ struct EpiResid {
 #pragma unroll
       for (int qd = 0; qd < 4; ++qd) op[qd] = o[qd];
     }
-    // this thread's partial sum goes to its own slot; part 0 clears the unused slots
     if (valid) {
       float* o = ss_out + static_cast<size_t>(row) * 4;
-      o[part] = ss;
-      if (part == 0)
-        for (int k = nparts; k < 4; ++k) o[k] = 0.f;
+      if (c1 - c0 >= 64) {
+        const int b0 = (n0 + c0) / 64;
+        for (int i = 0; i < (c1 - c0) / 64; ++i) o[b0 + i] = ssb[i];
+        if (b0 == 0)
+          for (int k = d / 64; k < 4; ++k) o[k] = 0.f;
+      } else {
+        o[part] = ssb[0];
+        if (part == 0)
+          for (int k = nparts; k < 4; ++k) o[k] = 0.f;
+      }
     }
   }
 };
