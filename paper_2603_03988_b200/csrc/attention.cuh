@@ -269,17 +269,23 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
       if (p_valid) {
         const uint8_t* gs = smem + S::oGate + ((pli & 1) * 256 + hf * 128 + r) * (DH * 2);
         const float invl = 1.f / l;
+        uint32_t w[DH / 2];
 #pragma unroll
         for (int i = 0; i < DH / 8; ++i) {
           const int4 gv = *reinterpret_cast<const int4*>(gs + 16 * i);
           const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gv);
-          uint32_t w[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const float2 gf = __bfloat1622float2(g2[e]);
-            w[e] = pack_bf16x2(acc[8 * i + 2 * e] * invl * gf.x, acc[8 * i + 2 * e + 1] * invl * gf.y);
+            w[4 * i + e] = pack_bf16x2(acc[8 * i + 2 * e] * invl * gf.x, acc[8 * i + 2 * e + 1] * invl * gf.y);
           }
-          reinterpret_cast<int4*>(a.out + p_off)[i] = make_int4(w[0], w[1], w[2], w[3]);
+        }
+        if constexpr (DH == 16) {
+          stg256(a.out + p_off, w);  // the warp half's 32-byte output sector
+        } else {
+#pragma unroll
+          for (int i = 0; i < DH / 8; ++i)
+            reinterpret_cast<int4*>(a.out + p_off)[i] = make_int4(w[4 * i], w[4 * i + 1], w[4 * i + 2], w[4 * i + 3]);
         }
       }
 #pragma unroll

@@ -47,7 +47,16 @@ __device__ __forceinline__ float row_inv_rms(float ss, float inv_d) {
 }
 
 __device__ __forceinline__ void store_bf16_row(__nv_bfloat16* dst, const float* v, int n) {
-  // n multiple of 8; dst 16-byte aligned
+  // n multiple of 16 -> 32-byte sector stores (dst 32-byte aligned); else 16-byte stores
+  if (n % 16 == 0) {
+    for (int i = 0; i < n; i += 16) {
+      uint32_t w[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) w[k] = pack_bf16x2(v[i + 2 * k], v[i + 2 * k + 1]);
+      stg256(dst + i, w);
+    }
+    return;
+  }
   for (int i = 0; i < n; i += 8) {
     int4 w = make_int4(pack_bf16x2(v[i], v[i + 1]), pack_bf16x2(v[i + 2], v[i + 3]),
                        pack_bf16x2(v[i + 4], v[i + 5]), pack_bf16x2(v[i + 6], v[i + 7]));
@@ -228,9 +237,15 @@ struct EpiResid {
         }
         o[qd] = make_int4(w[0], w[1], w[2], w[3]);
       }
-      int4* op = reinterpret_cast<int4*>(out + static_cast<size_t>(row) * d + n0 + c);
+      uint8_t* op = reinterpret_cast<uint8_t*>(out + static_cast<size_t>(row) * d + n0 + c);
 #pragma unroll
-      for (int qd = 0; qd < 4; ++qd) op[qd] = o[qd];
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const uint32_t w8[8] = {static_cast<uint32_t>(o[2 * h2].x), static_cast<uint32_t>(o[2 * h2].y),
+                                static_cast<uint32_t>(o[2 * h2].z), static_cast<uint32_t>(o[2 * h2].w),
+                                static_cast<uint32_t>(o[2 * h2 + 1].x), static_cast<uint32_t>(o[2 * h2 + 1].y),
+                                static_cast<uint32_t>(o[2 * h2 + 1].z), static_cast<uint32_t>(o[2 * h2 + 1].w)};
+        stg256(op + 32 * h2, w8);
+      }
     }
     if (valid) {
       float* o = ss_out + static_cast<size_t>(row) * 4;
