@@ -105,17 +105,97 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
   const int n_tiles = p.tiles_hist + p.tiles_cand + p.tiles_prof;
   const int st = p.special_tokens ? 1 : 0;
   const int off_hist = st, off_prof = st + p.H + st, off_cand = off_prof + p.P + st;
+  auto group_of = [&](int tile, int& e0, int& count) {
+    if (tile < p.tiles_hist) {
+      e0 = tile * 128; count = p.B * p.H;
+      return static_cast<int>(kGroupHist);
+    }
+    if (tile < p.tiles_hist + p.tiles_cand) {
+      e0 = (tile - p.tiles_hist) * 128; count = p.B * p.N;
+      return static_cast<int>(kGroupCand);
+    }
+    e0 = (tile - p.tiles_hist - p.tiles_cand) * 128; count = p.B * p.P;
+    return static_cast<int>(kGroupProf);
+  };
+  // ---- gather of one token row into registers: up to 8 16-byte chunks of the concatenated
+  // embedding rows (K padded to 64 with zeros). Issued one tile ahead, so the dependent
+  // id -> row loads of tile i+1 are in flight while tile i's MMA and epilogue run.
+  struct Row {
+    int4 c[8];
+    int out_row;
+  };
+  auto gather = [&](int tile, Row& g) {
+    g.out_row = -1;
+    const __nv_bfloat16* src[4] = {nullptr, nullptr, nullptr, nullptr};
+    int n8[4] = {0, 0, 0, 0};
+    if (tile < n_tiles) {
+      int e0, count;
+      const int group = group_of(tile, e0, count);
+      const int e = e0 + t;
+      if (e < count) {
+        if (group == kGroupHist) {
+          const int b = e / p.H, i = e - b * p.H;
+          int item = p.hist_item[e], act = p.hist_action[e], sc = p.hist_scene[e];
+          const int tb = tok_time_bucket(p.req_ts[b] - p.hist_ts[e], p.n_tb);
+          if (static_cast<unsigned>(item) >= static_cast<unsigned>(p.n_items) ||
+              static_cast<unsigned>(act) >= static_cast<unsigned>(p.n_actions) ||
+              static_cast<unsigned>(sc) >= static_cast<unsigned>(p.n_scenes)) {
+            atomicOr(p.err, kErrOOV);
+            item = static_cast<unsigned>(item) < static_cast<unsigned>(p.n_items) ? item : 0;
+            act = static_cast<unsigned>(act) < static_cast<unsigned>(p.n_actions) ? act : 0;
+            sc = static_cast<unsigned>(sc) < static_cast<unsigned>(p.n_scenes) ? sc : 0;
+          }
+          if (p.hist_time) p.hist_time[e] = tb;
+          src[0] = p.item_tab + static_cast<size_t>(item) * p.item_dim;
+          src[1] = p.action_tab + static_cast<size_t>(act) * p.action_dim;
+          src[2] = p.scene_tab + static_cast<size_t>(sc) * p.scene_dim;
+          src[3] = p.time_tab + static_cast<size_t>(tb) * p.time_dim;
+          n8[0] = p.item_dim >> 3;
+          n8[1] = p.action_dim >> 3;
+          n8[2] = p.scene_dim >> 3;
+          n8[3] = p.time_dim >> 3;
+          g.out_row = b * p.L + off_hist + i;
+        } else if (group == kGroupCand) {
+          const int b = e / p.N, j = e - b * p.N;
+          int item = p.cand_item[e];
+          if (static_cast<unsigned>(item) >= static_cast<unsigned>(p.n_items)) {
+            atomicOr(p.err, kErrOOV);
+            item = 0;
+          }
+          src[0] = p.item_tab + static_cast<size_t>(item) * p.item_dim;
+          n8[0] = p.item_dim >> 3;
+          g.out_row = b * p.L + off_cand + j;
+        } else {
+          const int b = e / p.P, f = e - b * p.P;
+          int v = p.profile[e];
+          if (static_cast<unsigned>(v) >= static_cast<unsigned>(p.prof_vocab[f])) {
+            atomicOr(p.err, kErrOOV);
+            v = 0;
+          }
+          src[0] = p.prof_tab + static_cast<size_t>(p.prof_row_off[f] + v) * p.prof_dim;
+          n8[0] = p.prof_dim >> 3;
+          g.out_row = b * p.L + off_prof + f;
+        }
+      }
+    }
+    // chunk c of the concatenated row -> (segment, offset); static register indexing
+    int seg = 0, base = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      while (seg < 4 && c - base >= n8[seg]) {
+        base += n8[seg];
+        ++seg;
+      }
+      g.c[c] = seg < 4 ? __ldg(reinterpret_cast<const int4*>(src[seg]) + (c - base)) : make_int4(0, 0, 0, 0);
+    }
+  };
   int cur_group = -1;
   uint32_t phase = 0;
+  Row g;
+  gather(blockIdx.x, g);
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    int group, e0, count;
-    if (tile < p.tiles_hist) {
-      group = kGroupHist; e0 = tile * 128; count = p.B * p.H;
-    } else if (tile < p.tiles_hist + p.tiles_cand) {
-      group = kGroupCand; e0 = (tile - p.tiles_hist) * 128; count = p.B * p.N;
-    } else {
-      group = kGroupProf; e0 = (tile - p.tiles_hist - p.tiles_cand) * 128; count = p.B * p.P;
-    }
+    int e0, count;
+    const int group = group_of(tile, e0, count);
     if (group != cur_group) {  // (re)load this group's W^T, bias and gain
       __syncthreads();
       const int4* w = reinterpret_cast<const int4*>(p.wt[group]);
@@ -129,61 +209,12 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
       }
       cur_group = group;
     }
-    // ---- 1. gather this thread's row into the swizzled A tile
-    const int e = e0 + t;
-    const bool valid = e < count;
+    // ---- 1. this thread's gathered row -> the swizzled A tile
     uint8_t* arow = sA + t * 128;
-    int out_row = -1;
-    int nchunks = 0;
-    if (valid) {
-      if (group == kGroupHist) {
-        const int b = e / p.H, i = e - b * p.H;
-        int item = p.hist_item[e], act = p.hist_action[e], sc = p.hist_scene[e];
-        const int tb = tok_time_bucket(p.req_ts[b] - p.hist_ts[e], p.n_tb);
-        if (static_cast<unsigned>(item) >= static_cast<unsigned>(p.n_items) ||
-            static_cast<unsigned>(act) >= static_cast<unsigned>(p.n_actions) ||
-            static_cast<unsigned>(sc) >= static_cast<unsigned>(p.n_scenes)) {
-          atomicOr(p.err, kErrOOV);
-          item = static_cast<unsigned>(item) < static_cast<unsigned>(p.n_items) ? item : 0;
-          act = static_cast<unsigned>(act) < static_cast<unsigned>(p.n_actions) ? act : 0;
-          sc = static_cast<unsigned>(sc) < static_cast<unsigned>(p.n_scenes) ? sc : 0;
-        }
-        if (p.hist_time) p.hist_time[e] = tb;
-        int c = 0;
-        tok_put(arow, t, c, p.item_tab + static_cast<size_t>(item) * p.item_dim, p.item_dim >> 3);
-        c += p.item_dim >> 3;
-        tok_put(arow, t, c, p.action_tab + static_cast<size_t>(act) * p.action_dim, p.action_dim >> 3);
-        c += p.action_dim >> 3;
-        tok_put(arow, t, c, p.scene_tab + static_cast<size_t>(sc) * p.scene_dim, p.scene_dim >> 3);
-        c += p.scene_dim >> 3;
-        tok_put(arow, t, c, p.time_tab + static_cast<size_t>(tb) * p.time_dim, p.time_dim >> 3);
-        nchunks = c + (p.time_dim >> 3);
-        out_row = b * p.L + off_hist + i;
-      } else if (group == kGroupCand) {
-        const int b = e / p.N, j = e - b * p.N;
-        int item = p.cand_item[e];
-        if (static_cast<unsigned>(item) >= static_cast<unsigned>(p.n_items)) {
-          atomicOr(p.err, kErrOOV);
-          item = 0;
-        }
-        tok_put(arow, t, 0, p.item_tab + static_cast<size_t>(item) * p.item_dim, p.item_dim >> 3);
-        nchunks = p.item_dim >> 3;
-        out_row = b * p.L + off_cand + j;
-      } else {
-        const int b = e / p.P, f = e - b * p.P;
-        int v = p.profile[e];
-        if (static_cast<unsigned>(v) >= static_cast<unsigned>(p.prof_vocab[f])) {
-          atomicOr(p.err, kErrOOV);
-          v = 0;
-        }
-        tok_put(arow, t, 0, p.prof_tab + static_cast<size_t>(p.prof_row_off[f] + v) * p.prof_dim,
-                p.prof_dim >> 3);
-        nchunks = p.prof_dim >> 3;
-        out_row = b * p.L + off_prof + f;
-      }
-    }
-    for (int c = nchunks; c < 8; ++c)
-      *reinterpret_cast<int4*>(arow + ((c ^ (t & 7)) << 4)) = make_int4(0, 0, 0, 0);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) *reinterpret_cast<int4*>(arow + ((c ^ (t & 7)) << 4)) = g.c[c];
+    const int out_row = g.out_row;
+    const bool valid = out_row >= 0;
     fence_proxy_async_smem();
     __syncthreads();
     // ---- 2. projection on the tensor cores
@@ -196,6 +227,7 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
                     idesc, k > 0 ? 1u : 0u);
       mma_commit(bar);
     }
+    gather(tile + gridDim.x, g);  // next tile's rows in flight during this tile's epilogue
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_fence_after();
@@ -228,11 +260,7 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
         const float q0 = __bfloat162float(q.x), q1 = __bfloat162float(q.y);
         ss_out += q0 * q0 + q1 * q1;
       }
-      if (valid) {
-        int4* dst = reinterpret_cast<int4*>(p.x + static_cast<size_t>(out_row) * d + c);
-        dst[0] = make_int4(packed[0], packed[1], packed[2], packed[3]);
-        dst[1] = make_int4(packed[4], packed[5], packed[6], packed[7]);
-      }
+      if (valid) stg256(p.x + static_cast<size_t>(out_row) * d + c, packed);
     }
     if (valid) p.ss[out_row] = make_float4(ss_out, 0.f, 0.f, 0.f);
     tc_fence_before();
