@@ -82,6 +82,10 @@ def lib():
         L.oracle_attention_forward.argtypes = [C.c_void_p, C.c_int, f64p, C.c_int, i32p, C.c_int,
                                                u8p, i32p, f64p]
         L.oracle_time_bucket.argtypes = [C.c_int64, C.c_int]
+        L.oracle_model_backward.argtypes = [C.c_void_p, C.POINTER(OrSample), f64p, f64p,
+                                            C.POINTER(C.c_void_p)]
+        L.oracle_grads_get.argtypes = [C.c_void_p, C.c_char_p, f64p, i32p, i32p]
+        L.oracle_grads_destroy.argtypes = [C.c_void_p]
         _lib = L
     return _lib
 
@@ -291,3 +295,29 @@ class OracleModel:
                                               _p(qr, i32p), len(qr), _p(vis, u8p), _p(p, i32p),
                                               _p(out, f64p)))
         return out
+
+    def backward(self, batch, b: int, dlogits: np.ndarray, names):
+        """fp64 backward of forward(batch, b) given dL/dlogits [n_cand, 3]: returns
+        ({name: gradient} for the requested parameter names, dtokens [L, d])."""
+        hold = _SampleHold(batch, b)
+        cfg = self.cfg
+        L = (3 if cfg.special_tokens else 0) + hold.s.n_hist + hold.s.n_prof + hold.s.n_cand
+        dz = np.ascontiguousarray(dlogits, dtype=np.float64)
+        dtok = np.zeros((L, cfg.model_dim))
+        g = C.c_void_p()
+        _check(lib().oracle_model_backward(self.h, C.byref(hold.s), _p(dz, f64p), _p(dtok, f64p),
+                                           C.byref(g)))
+        out = {}
+        try:
+            for name in names:
+                r, c = C.c_int32(0), C.c_int32(0)
+                _check(lib().oracle_grads_get(g, name.encode(), None, C.byref(r), C.byref(c)))
+                a = np.zeros((max(r.value, 1), max(c.value, 1)))
+                if r.value:
+                    _check(lib().oracle_grads_get(g, name.encode(), _p(a, f64p), None, None))
+                    out[name] = a
+                else:
+                    out[name] = None
+        finally:
+            lib().oracle_grads_destroy(g)
+        return out, dtok

@@ -618,6 +618,270 @@ void model_forward(const OrModel& mdl, const OrSample& s, double* probs, double*
     }
 }
 
+// ====================================================================== backward
+// Training-mode backward of the whole scoring path for one request, fp64: head -> final
+// RMSNorm -> blocks (FFN, pre-norms, residuals, pruning scatter) -> attention layers
+// (AttentionLayer::backward, attention.cpp:134-202, with the intended math: the gate
+// path's d(xq) added to the query path, QKNorm gains indexed per head) -> dtokens.
+// rmsnorm_backward follows norm.hpp:32-45.
+using Grads = std::map<std::string, M>;
+
+M& grad_of(Grads& g, const OrModel& mdl, const std::string& name) {
+  auto it = g.find(name);
+  if (it == g.end()) {
+    const M& p = mdl.P(name);
+    it = g.emplace(name, M(p.r, p.c)).first;
+  }
+  return it->second;
+}
+
+// y = x * inv * gain (per row); returns dx, accumulates dgain (norm.hpp:32-45)
+M rmsnorm_backward(const M& dy, const M& x, const double* gain, double* dgain) {
+  M dx(x.r, x.c);
+  for (int r = 0; r < x.r; ++r) {
+    const double* xr = x.row(r);
+    double ss = 0.0;
+    for (int j = 0; j < x.c; ++j) ss += xr[j] * xr[j];
+    const double inv = 1.0 / std::sqrt(ss / static_cast<double>(x.c) + kRmsEps);
+    double proj = 0.0;
+    for (int j = 0; j < x.c; ++j) {
+      const double xh = xr[j] * inv;
+      dgain[j] += dy(r, j) * xh;
+      proj += dy(r, j) * gain[j] * xh;
+    }
+    proj /= static_cast<double>(x.c);
+    for (int j = 0; j < x.c; ++j) dx(r, j) = (dy(r, j) * gain[j] - proj * xr[j] * inv) * inv;
+  }
+  return dx;
+}
+
+M matmul_tn(const M& A, const M& B) { return matmul(transpose(A), B); }  // A^T B
+M matmul_nt(const M& A, const M& B) { return matmul(A, transpose(B)); }  // A B^T
+void add_into(M& a, const M& b) {
+  for (size_t t = 0; t < a.a.size(); ++t) a.a[t] += b.a[t];
+}
+
+// AttentionLayer::backward (attention.cpp:134-202): returns d(xn) [l_kv, d].
+M attention_backward(const OrModel& mdl, int layer, const M& xn, const std::vector<int>& qrows,
+                     const uint8_t* vis, const std::vector<int>& pos, const M& dout, Grads& G) {
+  const int d = mdl.d, h = mdl.cfg.heads, dk = mdl.dk;
+  const int lq = static_cast<int>(qrows.size()), lkv = xn.r;
+  const std::string base = "attn." + std::to_string(layer) + ".";
+  const double scale = 1.0 / std::sqrt(static_cast<double>(dk));
+  // ---- forward with caches (attention.cpp:71-132)
+  M xq(lq, d);
+  std::vector<int> pos_q(lq);
+  for (int i = 0; i < lq; ++i) {
+    std::memcpy(xq.row(i), xn.row(qrows[i]), sizeof(double) * d);
+    pos_q[i] = pos[qrows[i]];
+  }
+  const M& Wq = mdl.P(base + "wq");
+  const M& Wk = mdl.P(base + "wk");
+  const M& Wv = mdl.P(base + "wv");
+  const M& Wo = mdl.P(base + "wo");
+  M q_raw = matmul(xq, Wq), k_raw = matmul(xn, Wk), v = matmul(xn, Wv);
+  M out_pre(lq, d);
+  std::vector<M> attn(h), q_rot(h), k_rot(h);
+  for (int i = 0; i < h; ++i) {
+    M qh = cols_of(q_raw, i * dk, dk), kh = cols_of(k_raw, i * dk, dk);
+    if (mdl.cfg.qknorm) {
+      qh = rmsnorm(qh, mdl.P(base + "qk_gain_q").row(i));
+      kh = rmsnorm(kh, mdl.P(base + "qk_gain_k").row(i));
+    }
+    q_rot[i] = M(lq, dk);
+    k_rot[i] = M(lkv, dk);
+    rope_rows(qh.a.data(), lq, dk, pos_q.data(), mdl.cfg.rope_theta, false, q_rot[i].a.data());
+    rope_rows(kh.a.data(), lkv, dk, pos.data(), mdl.cfg.rope_theta, false, k_rot[i].a.data());
+    M& a = attn[i] = M(lq, lkv);
+    matmul(q_rot[i].a.data(), transpose(k_rot[i]).a.data(), a.a.data(), lq, dk, lkv);
+    for (int r = 0; r < lq; ++r) {
+      double* ar = a.row(r);
+      const uint8_t* vr = vis + static_cast<size_t>(r) * lkv;
+      double mx = -std::numeric_limits<double>::infinity();
+      for (int c = 0; c < lkv; ++c) {
+        ar[c] = vr[c] ? ar[c] * scale : -std::numeric_limits<double>::infinity();
+        mx = std::max(mx, ar[c]);
+      }
+      double sum = 0.0;
+      for (int c = 0; c < lkv; ++c) {
+        ar[c] = vr[c] ? std::exp(ar[c] - mx) : 0.0;
+        sum += ar[c];
+      }
+      for (int c = 0; c < lkv; ++c) ar[c] /= sum;
+    }
+    M oh = matmul(a, cols_of(v, i * dk, dk));
+    for (int r = 0; r < lq; ++r) std::memcpy(out_pre.row(r) + i * dk, oh.row(r), sizeof(double) * dk);
+  }
+  M gsig(lq, d), hcat = out_pre;
+  if (mdl.cfg.gate) {
+    M graw = matmul(xq, mdl.P(base + "wg"));
+    for (size_t t = 0; t < gsig.a.size(); ++t) {
+      gsig.a[t] = sigmoid(graw.a[t]);
+      hcat.a[t] = gsig.a[t] * out_pre.a[t];
+    }
+  }
+  // ---- backward (attention.cpp:134-202)
+  add_into(grad_of(G, mdl, base + "wo"), matmul_tn(hcat, dout));
+  M dh = matmul_nt(dout, Wo);
+  M dpre = dh, dxq(lq, d);
+  if (mdl.cfg.gate) {
+    M dgraw(lq, d);
+    for (size_t t = 0; t < dh.a.size(); ++t) {
+      dpre.a[t] = dh.a[t] * gsig.a[t];
+      dgraw.a[t] = dh.a[t] * out_pre.a[t] * gsig.a[t] * (1.0 - gsig.a[t]);
+    }
+    add_into(grad_of(G, mdl, base + "wg"), matmul_tn(xq, dgraw));
+    dxq = matmul_nt(dgraw, mdl.P(base + "wg"));
+  }
+  M dq_raw(lq, d), dk_raw(lkv, d), dv(lkv, d);
+  for (int i = 0; i < h; ++i) {
+    const M& a = attn[i];
+    M dO = cols_of(dpre, i * dk, dk);
+    M da = matmul_nt(dO, cols_of(v, i * dk, dk));
+    M dvh = matmul_tn(a, dO);
+    M ds(lq, lkv);
+    for (int r = 0; r < lq; ++r) {
+      double dot = 0.0;
+      for (int c = 0; c < lkv; ++c) dot += da(r, c) * a(r, c);
+      for (int c = 0; c < lkv; ++c) ds(r, c) = a(r, c) * (da(r, c) - dot);
+    }
+    M dq_rot = matmul(ds, k_rot[i]), dk_rot = matmul_tn(ds, q_rot[i]);
+    for (double& t : dq_rot.a) t *= scale;
+    for (double& t : dk_rot.a) t *= scale;
+    M dq(lq, dk), dkk(lkv, dk);
+    rope_rows(dq_rot.a.data(), lq, dk, pos_q.data(), mdl.cfg.rope_theta, true, dq.a.data());
+    rope_rows(dk_rot.a.data(), lkv, dk, pos.data(), mdl.cfg.rope_theta, true, dkk.a.data());
+    if (mdl.cfg.qknorm) {
+      M& gq = grad_of(G, mdl, base + "qk_gain_q");
+      M& gk = grad_of(G, mdl, base + "qk_gain_k");
+      dq = rmsnorm_backward(dq, cols_of(q_raw, i * dk, dk), mdl.P(base + "qk_gain_q").row(i), gq.row(i));
+      dkk = rmsnorm_backward(dkk, cols_of(k_raw, i * dk, dk), mdl.P(base + "qk_gain_k").row(i), gk.row(i));
+    }
+    for (int r = 0; r < lq; ++r) std::memcpy(dq_raw.row(r) + i * dk, dq.row(r), sizeof(double) * dk);
+    for (int r = 0; r < lkv; ++r) {
+      std::memcpy(dk_raw.row(r) + i * dk, dkk.row(r), sizeof(double) * dk);
+      std::memcpy(dv.row(r) + i * dk, dvh.row(r), sizeof(double) * dk);
+    }
+  }
+  add_into(grad_of(G, mdl, base + "wq"), matmul_tn(xq, dq_raw));
+  add_into(grad_of(G, mdl, base + "wk"), matmul_tn(xn, dk_raw));
+  add_into(grad_of(G, mdl, base + "wv"), matmul_tn(xn, dv));
+  add_into(dxq, matmul_nt(dq_raw, Wq));
+  M dxn = matmul_nt(dk_raw, Wk);
+  add_into(dxn, matmul_nt(dv, Wv));
+  for (int i = 0; i < lq; ++i)
+    for (int j = 0; j < d; ++j) dxn(qrows[i], j) += dxq(i, j);
+  return dxn;
+}
+
+// Backward of model_forward for one request given dL/dlogits [n_cand, 3]; returns dtokens.
+M model_backward(const OrModel& mdl, const OrSample& s, const double* dlogits, Grads& G) {
+  Seq q = tokenize(mdl, s);
+  const OrModelCfg& c = mdl.cfg;
+  const int d = mdl.d;
+  struct Saved {
+    M x, xr;
+    std::vector<int> qrows, roles, pos;
+    std::vector<uint8_t> vis;
+  };
+  std::vector<Saved> sv(c.layers);
+  M x = q.tokens;
+  std::vector<int> roles = q.roles, pos = q.pos;
+  for (int l = 0; l < c.layers; ++l) {
+    const std::string L = std::to_string(l);
+    Saved& S = sv[l];
+    S.x = x;
+    S.roles = roles;
+    S.pos = pos;
+    S.qrows = retained_rows(roles, c.keep[l], c.keep_specials != 0);
+    const int lq = static_cast<int>(S.qrows.size()), lkv = x.r;
+    S.vis.assign(static_cast<size_t>(lq) * lkv, 0);
+    build_mask(lq, lkv, c.local_window, c.full_suffix, roles.data(), pos.data(), S.qrows.data(), S.vis.data());
+    M xn = rmsnorm(x, mdl.P("block." + L + ".attn_norm").row(0));
+    M a = attention_forward(mdl, l, xn, S.qrows, S.vis.data(), pos);
+    M xr(lq, d);
+    std::vector<int> nroles(lq), npos(lq);
+    for (int i = 0; i < lq; ++i) {
+      for (int j = 0; j < d; ++j) xr(i, j) = x(S.qrows[i], j) + a(i, j);
+      nroles[i] = roles[S.qrows[i]];
+      npos[i] = pos[S.qrows[i]];
+    }
+    S.xr = xr;
+    M xf = rmsnorm(xr, mdl.P("block." + L + ".ffn_norm").row(0));
+    M f = swishglu(xf, mdl.P("ffn." + L + ".w_gate"), mdl.P("ffn." + L + ".w_up"), mdl.P("ffn." + L + ".w_down"));
+    add_into(xr, f);
+    x = std::move(xr);
+    roles = std::move(nroles);
+    pos = std::move(npos);
+  }
+  // ---- head backward
+  std::vector<int> crows;
+  for (int i = 0; i < x.r; ++i)
+    if (roles[i] == OR_ROLE_CAND) crows.push_back(i);
+  const int nc = static_cast<int>(crows.size());
+  M xc(nc, d);
+  for (int i = 0; i < nc; ++i) std::memcpy(xc.row(i), x.row(crows[i]), sizeof(double) * d);
+  const double* gfin = mdl.P("final_norm.gain").row(0);
+  M xh = rmsnorm(xc, gfin);
+  M hid = matmul(xh, mdl.P("head.w1"));
+  const M& b1 = mdl.P("head.b1");
+  for (int i = 0; i < hid.r; ++i)
+    for (int j = 0; j < hid.c; ++j) hid(i, j) = std::max(0.0, hid(i, j) + b1(0, j));
+  M dz(nc, 3);
+  std::memcpy(dz.a.data(), dlogits, sizeof(double) * nc * 3);
+  add_into(grad_of(G, mdl, "head.w2"), matmul_tn(hid, dz));
+  M& gb2 = grad_of(G, mdl, "head.b2");
+  for (int i = 0; i < nc; ++i)
+    for (int j = 0; j < 3; ++j) gb2(0, j) += dz(i, j);
+  M dhid = matmul_nt(dz, mdl.P("head.w2"));
+  for (size_t t = 0; t < dhid.a.size(); ++t)
+    if (hid.a[t] <= 0.0) dhid.a[t] = 0.0;  // ReLU (the subgradient 0 at 0)
+  add_into(grad_of(G, mdl, "head.w1"), matmul_tn(xh, dhid));
+  M& gb1 = grad_of(G, mdl, "head.b1");
+  for (int i = 0; i < nc; ++i)
+    for (int j = 0; j < dhid.c; ++j) gb1(0, j) += dhid(i, j);
+  M dxh = matmul_nt(dhid, mdl.P("head.w1"));
+  M dxc = rmsnorm_backward(dxh, xc, gfin, grad_of(G, mdl, "final_norm.gain").row(0));
+  M dx(x.r, d);
+  for (int i = 0; i < nc; ++i) std::memcpy(dx.row(crows[i]), dxc.row(i), sizeof(double) * d);
+  // ---- blocks in reverse
+  for (int l = c.layers - 1; l >= 0; --l) {
+    const std::string L = std::to_string(l);
+    const Saved& S = sv[l];
+    const int lq = static_cast<int>(S.qrows.size());
+    // FFN: x_out = xr + down(swish(xf Wg) * (xf Wu)), xf = RMSN(xr)
+    const double* gf = mdl.P("block." + L + ".ffn_norm").row(0);
+    M xf = rmsnorm(S.xr, gf);
+    const M& Wg = mdl.P("ffn." + L + ".w_gate");
+    const M& Wu = mdl.P("ffn." + L + ".w_up");
+    const M& Wd = mdl.P("ffn." + L + ".w_down");
+    M gp = matmul(xf, Wg), up = matmul(xf, Wu), z(gp.r, gp.c);
+    for (size_t t = 0; t < z.a.size(); ++t) z.a[t] = swish(gp.a[t]) * up.a[t];
+    add_into(grad_of(G, mdl, "ffn." + L + ".w_down"), matmul_tn(z, dx));
+    M dz2 = matmul_nt(dx, Wd), dgp(gp.r, gp.c), dup(gp.r, gp.c);
+    for (size_t t = 0; t < z.a.size(); ++t) {
+      const double sg = sigmoid(gp.a[t]);
+      dup.a[t] = dz2.a[t] * gp.a[t] * sg;
+      dgp.a[t] = dz2.a[t] * up.a[t] * sg * (1.0 + gp.a[t] * (1.0 - sg));
+    }
+    add_into(grad_of(G, mdl, "ffn." + L + ".w_gate"), matmul_tn(xf, dgp));
+    add_into(grad_of(G, mdl, "ffn." + L + ".w_up"), matmul_tn(xf, dup));
+    M dxf = matmul_nt(dgp, Wg);
+    add_into(dxf, matmul_nt(dup, Wu));
+    M dxr = dx;
+    add_into(dxr, rmsnorm_backward(dxf, S.xr, gf, grad_of(G, mdl, "block." + L + ".ffn_norm").row(0)));
+    // attention: xr = P(x, L_out) + Attn(RMSN(x))
+    const double* ga = mdl.P("block." + L + ".attn_norm").row(0);
+    M xn = rmsnorm(S.x, ga);
+    M dxn = attention_backward(mdl, l, xn, S.qrows, S.vis.data(), S.pos, dxr, G);
+    M dxin = rmsnorm_backward(dxn, S.x, ga, grad_of(G, mdl, "block." + L + ".attn_norm").row(0));
+    for (int i = 0; i < lq; ++i)
+      for (int j = 0; j < d; ++j) dxin(S.qrows[i], j) += dxr(i, j);
+    dx = std::move(dxin);
+  }
+  return dx;
+}
+
 }  // namespace
 
 // ====================================================================== C API
@@ -851,4 +1115,39 @@ int oracle_model_forward_batch(const OrModel* m, const OrSample* samples, int B,
   return status.load();
 }
 
+
+struct OrGrads {
+  Grads g;
+};
+
+int oracle_model_backward(const OrModel* m, const OrSample* s, const double* dlogits,
+                          double* dtokens, OrGrads** out) {
+  return guarded([&] {
+    auto* G = new OrGrads;
+    try {
+      M dx = model_backward(*m, *s, dlogits, G->g);
+      if (dtokens) std::memcpy(dtokens, dx.a.data(), sizeof(double) * dx.a.size());
+    } catch (...) {
+      delete G;
+      throw;
+    }
+    *out = G;
+  });
+}
+
+int oracle_grads_get(const OrGrads* g, const char* name, double* out, int* rows, int* cols) {
+  return guarded([&] {
+    auto it = g->g.find(name);
+    if (it == g->g.end()) {  // parameter not on the differentiated path: zero gradient
+      if (rows) *rows = 0;
+      if (cols) *cols = 0;
+      return;
+    }
+    if (rows) *rows = it->second.r;
+    if (cols) *cols = it->second.c;
+    if (out) std::memcpy(out, it->second.a.data(), sizeof(double) * it->second.a.size());
+  });
+}
+
+void oracle_grads_destroy(OrGrads* g) { delete g; }
 }  // extern "C"

@@ -134,6 +134,18 @@ int oracle_model_layer_meta(const OrModel* m, const OrSample* s, int* l_q, int64
 int oracle_model_forward_batch(const OrModel* m, const OrSample* samples, int B, int threads,
                                double* probs /* sum(n_cand)*3 */);
 
+/* --- training backward (fp64) ------------------------------------------ */
+/* Backward of oracle_model_forward for one request given dL/dlogits [n_cand*3]: the head,
+ * final RMSNorm, every block (SwishGLU FFN, pre-norms, residuals, pruning scatter) and
+ * AttentionLayer::backward (attention.cpp:134-202, intended math). dtokens [L*d] may be NULL.
+ * Gradients are returned by parameter name (oracle_grads_get; rows = cols = 0 for a
+ * parameter off the differentiated path, e.g. the tokenizer tables). */
+typedef struct OrGrads OrGrads;
+int oracle_model_backward(const OrModel* m, const OrSample* s, const double* dlogits,
+                          double* dtokens, OrGrads** out);
+int oracle_grads_get(const OrGrads* g, const char* name, double* out, int* rows, int* cols);
+void oracle_grads_destroy(OrGrads* g);
+
 #ifdef __cplusplus
 }
 #endif

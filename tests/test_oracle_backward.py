@@ -1,0 +1,60 @@
+# SPDX-License-Identifier: Apache-2.0
+"""The fp64 oracle's training backward (AttentionLayer::backward, attention.cpp:134-202, with
+the intended math; rmsnorm_backward, norm.hpp:32-45; the spec's SwishGLU FFN / pre-norm
+blocks / ranking head) pinned by central finite differences of the
+oracle's own forward, as SPEC.md:411 prescribes. CPU only."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2603_03988_b200 import synth
+from paper_2603_03988_b200.config import tiny_config
+
+FD_EPS = 1e-5
+FD_REL_TOL = 1e-6   # fp64 central differences on an O(1) loss
+
+
+@pytest.fixture(scope="module")
+def setup():
+    # pruning after layer 0, windowed + full-causal rows, specials kept
+    cfg = tiny_config(n_hist=40, n_cand=5, keep=[46, 20], local_window=8, full_suffix=6)
+    P = {k: v.astype(np.float64) for k, v in synth.make_params(cfg, seed=3).items()}
+    b = synth.make_batch(cfg, 1, seed=4)
+    W = np.random.default_rng(0).normal(size=(cfg.n_cand, 3))
+    return cfg, P, b, W
+
+
+def _loss(cfg, P, b, W):
+    _, z = O.OracleModel(cfg, P).forward(b, 0)
+    return float((W * z).sum())
+
+
+def _fd(cfg, P, b, W, name, idx):
+    Pp = dict(P); Pp[name] = P[name].copy(); Pp[name][idx] += FD_EPS
+    Pm = dict(P); Pm[name] = P[name].copy(); Pm[name][idx] -= FD_EPS
+    return (_loss(cfg, Pp, b, W) - _loss(cfg, Pm, b, W)) / (2 * FD_EPS)
+
+
+def test_param_grads_match_finite_differences(setup):
+    cfg, P, b, W = setup
+    names = [n for n in P if not n.startswith("tok.")]
+    g, _ = O.OracleModel(cfg, P).backward(b, 0, W, names)
+    rng = np.random.default_rng(1)
+    for n in names:
+        assert g[n] is not None and g[n].shape == P[n].shape, n
+        for _ in range(2):
+            idx = tuple(int(rng.integers(0, s)) for s in P[n].shape)
+            fd = _fd(cfg, P, b, W, n, idx)
+            an = g[n][idx]
+            assert abs(fd - an) <= FD_REL_TOL * max(1.0, abs(fd)) + 1e-9, (n, idx, fd, an)
+
+
+def test_dtokens_match_finite_differences(setup):
+    """Special rows enter the sequence raw (tokenizer.cpp:171-176), so d loss / d special[k]
+    equals dtokens at that special token's row (BOS = row 0, first SEP = row 1 + H)."""
+    cfg, P, b, W = setup
+    _, dt = O.OracleModel(cfg, P).backward(b, 0, W, [])
+    for k, row in ((0, 0), (1, 1 + cfg.n_hist)):
+        for j in (0, 7, cfg.model_dim - 1):
+            fd = _fd(cfg, P, b, W, "tok.special", (k, j))
+            assert abs(fd - dt[row, j]) <= FD_REL_TOL * max(1.0, abs(fd)) + 1e-9, (k, j)
