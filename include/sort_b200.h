@@ -166,6 +166,24 @@ int sort_kernel_count(SortHandle h, int32_t* launches);
 int sort_enable_stage_timing(SortHandle h, int enable);
 int sort_stage_times(SortHandle h, float* ms, int32_t cap, int32_t* n, char* names,
                      int32_t names_cap);
+/* ---------------------------------------------------------------- training */
+/* One training step of the scoring path on the handle's device: forward (saving activations)
+ * + backward of the head, final norm, every block (SwishGLU FFN, pre-norms, residuals,
+ * pruning scatter) and AttentionLayer::backward (attention.cpp:134-202, intended math),
+ * given dL/dlogits [batch, n_cand, 3] (host). Gradients (fp32) stay on the device in one flat
+ * buffer in parameter-name order; logits [batch, n_cand, 3] are returned when non-null.
+ * Replaces the reference's per-request AttentionLayer::backward / rmsnorm_backward calls
+ * (attention.hpp:62-63, norm.hpp:32) accumulated into a GradBuffer (params.hpp:42-70). */
+int sort_train_step(SortHandle h, const SortBatch* batch, const float* dlogits, float* logits);
+/* Offset / shape of one parameter's gradient in the flat buffer, and its total length. */
+int sort_grad_info(SortHandle h, const char* name, int64_t* offset, int64_t* rows, int64_t* cols,
+                   int64_t* total);
+/* Copy the flat gradient buffer out (to_handle = 0) or back in (to_handle = 1, e.g. after a
+ * data-parallel all-reduce); buf is host or device memory. */
+int sort_grads_copy(SortHandle h, float* buf, int buf_on_device, int to_handle);
+/* d(loss)/d(tokens) of the last step, [batch, L, d] fp32 on the host. */
+int sort_dtokens(SortHandle h, int32_t batch, float* out);
+
 /* Kernel-selection knobs for A/B tests (no reference counterpart; defaults are the fastest
  * path): "fused_tail" (1 = one k_block_tail launch per block for Wo + residual + SwishGLU FFN
  * + residual where the shape allows it, 0 = the three separate GEMMs). Status 1 on an

@@ -66,6 +66,8 @@ struct AttnArgs {
   const int32_t* qtile_order; // heavy first
   const __nv_bfloat16* g;     // [B*Rq, d] sigmoid gate
   __nv_bfloat16* out;         // [B*Rq, d]
+  __nv_bfloat16* o_pre;       // training: pre-gate output [B*Rq, d] (or null)
+  float* lse;                 // training: log2-sum-exp per (b*H + h, row) [BH, Rq] (or null)
   int BH, H, Rq, d, n_qtiles, n_codes;
   float scale_log2;           // log2(e) / sqrt(dk)
   float ref_log2;             // fixed-reference mode: B * scale_log2
@@ -243,8 +245,8 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
     for (int i = 0; i < DH; ++i) acc[i] = 0.f;
     // the previous item, finished while the next item's first tile is in flight
     bool p_valid = false;
-    size_t p_off = 0;
-    float p_lsum = 0.f;
+    size_t p_off = 0, p_lse = 0;
+    float p_lsum = 0.f, p_ref = 0.f;
     // acc <- acc * alpha + O_t  (this warp's DK/2 columns of tile t's PV result)
     auto fold_o = [&](int t, float alpha) {
       const int pb = t & 1;
@@ -269,6 +271,15 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
       if (p_valid) {
         const uint8_t* gs = smem + S::oGate + ((pli & 1) * 256 + hf * 128 + r) * (DH * 2);
         const float invl = 1.f / l;
+        if (a.lse) {  // training outputs: P = exp2(s * scale_log2 - lse2), pre-gate O
+          if (hf == 0) a.lse[p_lse] = p_ref + log2f(l);
+          uint32_t wo[DH / 2];
+#pragma unroll
+          for (int i = 0; i < DH / 2; ++i) wo[i] = pack_bf16x2(acc[2 * i] * invl, acc[2 * i + 1] * invl);
+#pragma unroll
+          for (int i = 0; i < DH / 8; ++i)
+            reinterpret_cast<int4*>(a.o_pre + p_off)[i] = make_int4(wo[4 * i], wo[4 * i + 1], wo[4 * i + 2], wo[4 * i + 3]);
+        }
         uint32_t w[DH / 2];
 #pragma unroll
         for (int i = 0; i < DH / 8; ++i) {
@@ -311,6 +322,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
       const bool has_prev = li > 0;
       if (has_prev) {  // this item's row sums start from zero; keep the previous item's
         p_lsum = (lsum[0].x + lsum[0].y) + (lsum[1].x + lsum[1].y);
+        p_ref = kFixed ? a.ref_log2 : (m == NEG_INF ? 0.f : m * sl2);
         lsum[0] = lsum[1] = make_float2(0.f, 0.f);
       }
       m = NEG_INF;
@@ -408,9 +420,11 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
       }
       p_valid = qrow < a.Rq;
       p_off = off;
+      p_lse = static_cast<size_t>(bh) * a.Rq + qrow;
     }  // item loop
     if (li > 0) {  // the last item
       p_lsum = (lsum[0].x + lsum[0].y) + (lsum[1].x + lsum[1].y);
+      p_ref = kFixed ? a.ref_log2 : (m == NEG_INF ? 0.f : m * sl2);
       finish_item(g - 1, alpha_prev, li - 1, false);
     }
   }

@@ -1,6 +1,7 @@
 // SPDX-License-Identifier: Apache-2.0
 // libsort_b200.so: handle, device weights/workspace, forward orchestration and the
 // C ABI declared in include/sort_b200.h.
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -19,6 +20,7 @@
 #include "plan.hpp"
 #include "tma_host.hpp"
 #include "tokenizer.cuh"
+#include "train.cuh"
 
 namespace sortk {
 
@@ -65,6 +67,27 @@ struct Handle {
   std::map<std::string, HostParam> host;
   bool finalized = false;
   bool fused_tail = true;  // sort_set_option("fused_tail")
+  // ---- training (sort_train_step): fp32 master copies of the block/head parameters,
+  // a flat fp32 gradient buffer, saved forward activations per layer, workspace
+  std::map<std::string, float*> w32;
+  std::map<std::string, std::pair<size_t, std::pair<int64_t, int64_t>>> grad_index;  // offset, shape
+  float* grads = nullptr;
+  size_t grad_count = 0;
+  bool training = false;  // forward currently saving activations
+  struct TrainLayer {
+    __nv_bfloat16 *x_in = nullptr, *q = nullptr, *k = nullptr, *v = nullptr, *g = nullptr,
+                  *o_pre = nullptr, *x1 = nullptr;
+    float* lse = nullptr;
+    int32_t *dq_off = nullptr, *dkv_off = nullptr;
+    int2 *dq_iv = nullptr, *dkv_iv = nullptr;
+  };
+  std::vector<TrainLayer> tl;
+  float *tw[16] = {nullptr};  // backward workspace
+  float* dtokens = nullptr;
+  float* dz_dev = nullptr;                 // dL/dlogits of the current step
+  std::map<int, int32_t*> cand_maps;       // candidate-row maps for the head backward
+  int train_B = 0;
+  cublasHandle_t cublas = nullptr;
   // device weights
   __nv_bfloat16 *item = nullptr, *action = nullptr, *scene = nullptr, *time = nullptr,
                 *prof = nullptr, *special = nullptr;
@@ -115,6 +138,7 @@ struct Handle {
     if (device >= 0) cudaSetDevice(device);
     for (void* p : allocs) cudaFree(p);
     for (auto e : events) cudaEventDestroy(e);
+    if (cublas) cublasDestroy(cublas);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
 };
@@ -362,6 +386,28 @@ static void finalize(Handle& h) {
   h.head_b1 = h.upload(need_param(h, "head.b1", 1, h.dh).v);
   h.head_w2 = h.upload(need_param(h, "head.w2", h.dh, 3).v);
   h.head_b2 = h.upload(need_param(h, "head.b2", 1, 3).v);
+  // fp32 copies of the differentiated parameters (training backward), and the flat gradient
+  // buffer in the same name order; W_gate | W_up also concatenated as ffn.<l>.w_gu [d, 2m]
+  size_t goff = 0;
+  for (auto& kv : h.host) {
+    if (kv.first.rfind("tok.", 0) == 0) continue;
+    h.w32[kv.first] = h.upload(kv.second.v);
+    h.grad_index[kv.first] = {goff, {kv.second.rows, kv.second.cols}};
+    goff += static_cast<size_t>(kv.second.rows) * kv.second.cols;
+  }
+  for (int l = 0; l < c.layers; ++l) {
+    const std::string f = "ffn." + std::to_string(l) + ".";
+    const HostParam& wg = h.host.at(f + "w_gate");
+    const HostParam& wu = h.host.at(f + "w_up");
+    std::vector<float> gu(static_cast<size_t>(d) * 2 * m);
+    for (int i = 0; i < d; ++i)
+      for (int j = 0; j < m; ++j) {
+        gu[static_cast<size_t>(i) * 2 * m + j] = wg.v[static_cast<size_t>(i) * m + j];
+        gu[static_cast<size_t>(i) * 2 * m + m + j] = wu.v[static_cast<size_t>(i) * m + j];
+      }
+    h.w32[f + "w_gu"] = h.upload(gu);
+  }
+  h.grad_count = goff;
   h.host.clear();  // device copies are authoritative from here on
   h.finalized = true;
 }
@@ -404,6 +450,13 @@ static void launch_attention_dk(Handle& h, const LayerDev& L, const LayerPlan& l
   a.qtile_order = L.qtile_order;
   a.g = h.Gb;
   a.out = h.Hg;
+  a.o_pre = nullptr;
+  a.lse = nullptr;
+  if (h.training) {
+    const int li = static_cast<int>(&L - h.layers.data());
+    a.o_pre = h.tl[li].o_pre;
+    a.lse = h.tl[li].lse;
+  }
   a.BH = B * h.H;
   a.H = h.H;
   a.Rq = L.Rq;
@@ -576,6 +629,9 @@ static void run_layer(Handle& h, int l, int B, bool attn_only = false) {
   float4* SSin = h.SS[L.in_buf];
   __nv_bfloat16* Xq = h.X[L.q_buf];
   float4* SSq = h.SS[L.q_buf];
+  if (h.training)
+    CK(cudaMemcpyAsync(h.tl[l].x_in, Xin, static_cast<size_t>(B) * L.Rkv * d * 2, cudaMemcpyDeviceToDevice,
+                       h.stream));
   if (lp.q_identity) {
     launch_qkvg(h, L, L.tmA_in, L.tmB_all, B * L.Rkv, 4 * d, L.bn_full, L.Rkv,
                 {kSecQ, kSecV, kSecK, kSecG}, h.tmSS[L.in_buf], L.tmRopeKV);
@@ -592,7 +648,14 @@ static void run_layer(Handle& h, int l, int B, bool attn_only = false) {
   stage_mark(h, "L" + std::to_string(l) + ".qkvg");
   launch_attention(h, L, lp, B);
   stage_mark(h, "L" + std::to_string(l) + ".attention");
-  if (!attn_only && h.fused_tail && tail_supported(h)) {
+  if (h.training) {  // saved activations of the attention core for the backward
+    const size_t nq = static_cast<size_t>(B) * L.Rq * d, nkv = static_cast<size_t>(B) * L.Rkv * d;
+    CK(cudaMemcpyAsync(h.tl[l].q, h.Qb, nq * 2, cudaMemcpyDeviceToDevice, h.stream));
+    CK(cudaMemcpyAsync(h.tl[l].k, h.Kb, nkv * 2, cudaMemcpyDeviceToDevice, h.stream));
+    CK(cudaMemcpyAsync(h.tl[l].v, h.Vb, nkv * 2, cudaMemcpyDeviceToDevice, h.stream));
+    CK(cudaMemcpyAsync(h.tl[l].g, h.Gb, nq * 2, cudaMemcpyDeviceToDevice, h.stream));
+  }
+  if (!attn_only && h.fused_tail && !h.training && tail_supported(h)) {
     if (d == 256) launch_tail_d<256>(h, L, Xq, SSq, B * L.Rq);
     else launch_tail_d<128>(h, L, Xq, SSq, B * L.Rq);
     stage_mark(h, "L" + std::to_string(l) + ".tail");
@@ -606,6 +669,8 @@ static void run_layer(Handle& h, int l, int B, bool attn_only = false) {
   launch_gemm(h, L.tmA_hg, L.tmB_o, B * L.Rq, d, d, L.bn_o, eo);
   stage_mark(h, "L" + std::to_string(l) + ".wo");
   if (attn_only) return;
+  if (h.training)
+    CK(cudaMemcpyAsync(h.tl[l].x1, Xq, static_cast<size_t>(B) * L.Rq * d * 2, cudaMemcpyDeviceToDevice, h.stream));
   EpiSwiGLU eu;
   eu.inv_d = 1.f / static_cast<float>(d);
   eu.hidden = h.hid;
@@ -619,6 +684,283 @@ static void run_layer(Handle& h, int l, int B, bool attn_only = false) {
   ed.d = d;
   launch_gemm(h, L.tmA_hid, L.tmB_down, B * L.Rq, d, h.m, L.bn_down, ed);
   stage_mark(h, "L" + std::to_string(l) + ".ffn_down");
+}
+
+
+// ====================================================================== training
+// Row-major C[M,N] = op(A)[M,K] op(B)[K,N] (+ beta C) through column-major cuBLAS
+// (C^T = op(B)^T op(A)^T), TF32 tensor cores, fp32 in/out.
+static void gemm_rm(Handle& h, bool ta, bool tb, int M, int N, int K, const float* A, int lda, const float* B,
+                    int ldb, float* C, int ldc, float beta = 0.f) {
+  const float alpha = 1.f;
+  const cublasStatus_t st = cublasGemmEx(h.cublas, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N,
+                                         N, M, K, &alpha, B, CUDA_R_32F, ldb, A, CUDA_R_32F, lda, &beta, C,
+                                         CUDA_R_32F, ldc, CUBLAS_COMPUTE_32F_FAST_TF32, CUBLAS_GEMM_DEFAULT);
+  if (st != CUBLAS_STATUS_SUCCESS) throw RuntimeFailure("cublasGemmEx failed: " + std::to_string(static_cast<int>(st)));
+}
+
+static float* grad_ptr(Handle& h, const std::string& name) {
+  auto it = h.grad_index.find(name);
+  if (it == h.grad_index.end()) throw RuntimeFailure("no gradient slot for " + name);
+  return h.grads + it->second.first;
+}
+static const float* w32(Handle& h, const std::string& name) {
+  auto it = h.w32.find(name);
+  if (it == h.w32.end()) throw RuntimeFailure("no fp32 parameter " + name);
+  return it->second;
+}
+
+// Work lists of the attention backward for one layer (batch-uniform): for every 32-row
+// q-block the kv-column intervals any of its rows sees, for every 32-column kv-block the
+// q-row intervals that see any of its columns (from the compact mask {lo, hi, self}).
+static void build_bwd_lists(const LayerPlan& lp, std::vector<int32_t>& dq_off, std::vector<int2>& dq_iv,
+                            std::vector<int32_t>& dkv_off, std::vector<int2>& dkv_iv) {
+  auto push_runs = [](const std::vector<char>& on, std::vector<int2>& iv) {
+    const int n = static_cast<int>(on.size());
+    for (int i = 0; i < n;) {
+      if (!on[i]) {
+        ++i;
+        continue;
+      }
+      int j = i;
+      while (j < n && on[j]) ++j;
+      iv.push_back(make_int2(i, j));
+      i = j;
+    }
+  };
+  const int nqb = (lp.l_q + 31) / 32, nkb = (lp.l_kv + 31) / 32;
+  dq_off.assign(1, 0);
+  for (int qb = 0; qb < nqb; ++qb) {
+    std::vector<char> on(lp.l_kv, 0);
+    for (int r = qb * 32; r < std::min(lp.l_q, qb * 32 + 32); ++r) {
+      for (int c = std::max(lp.lo[r], 0); c <= lp.hi[r] && c < lp.l_kv; ++c) on[c] = 1;
+      if (lp.self_idx[r] >= 0) on[lp.self_idx[r]] = 1;
+    }
+    push_runs(on, dq_iv);
+    dq_off.push_back(static_cast<int32_t>(dq_iv.size()));
+  }
+  dkv_off.assign(1, 0);
+  for (int kb = 0; kb < nkb; ++kb) {
+    const int c0 = kb * 32, c1 = std::min(lp.l_kv, c0 + 32) - 1;
+    std::vector<char> on(lp.l_q, 0);
+    for (int r = 0; r < lp.l_q; ++r) {
+      const bool iv = lp.lo[r] <= c1 && lp.hi[r] >= c0 && lp.hi[r] >= lp.lo[r];
+      const bool self = lp.self_idx[r] >= c0 && lp.self_idx[r] <= c1;
+      on[r] = iv || self;
+    }
+    push_runs(on, dkv_iv);
+    dkv_off.push_back(static_cast<int32_t>(dkv_iv.size()));
+  }
+}
+
+static void ensure_train_buffers(Handle& h, int B) {
+  if (h.train_B >= B) return;
+  if (!h.cublas) {
+    if (cublasCreate(&h.cublas) != CUBLAS_STATUS_SUCCESS) throw RuntimeFailure("cublasCreate failed");
+  }
+  const int d = h.d, m = h.m;
+  B = h.Bmax;  // size once for max_batch
+  h.grads = h.dalloc<float>(h.grad_count);
+  h.tl.resize(h.cfg.layers);
+  size_t mkv_max = 0;
+  for (int l = 0; l < h.cfg.layers; ++l) {
+    const LayerDev& L = h.layers[l];
+    auto& T = h.tl[l];
+    const size_t nq = static_cast<size_t>(B) * L.Rq * d, nkv = static_cast<size_t>(B) * L.Rkv * d;
+    T.x_in = h.dalloc<__nv_bfloat16>(nkv);
+    T.q = h.dalloc<__nv_bfloat16>(nq);
+    T.k = h.dalloc<__nv_bfloat16>(nkv);
+    T.v = h.dalloc<__nv_bfloat16>(nkv);
+    T.g = h.dalloc<__nv_bfloat16>(nq);
+    T.o_pre = h.dalloc<__nv_bfloat16>(nq);
+    T.x1 = h.dalloc<__nv_bfloat16>(nq);
+    T.lse = h.dalloc<float>(static_cast<size_t>(B) * h.H * L.Rq);
+    std::vector<int32_t> qo, ko;
+    std::vector<int2> qi, ki;
+    build_bwd_lists(h.plan.layers[l], qo, qi, ko, ki);
+    if (qi.empty()) qi.push_back(make_int2(0, 0));
+    if (ki.empty()) ki.push_back(make_int2(0, 0));
+    T.dq_off = h.upload(qo);
+    T.dq_iv = h.upload(qi);
+    T.dkv_off = h.upload(ko);
+    T.dkv_iv = h.upload(ki);
+    mkv_max = std::max(mkv_max, static_cast<size_t>(B) * L.Rkv);
+  }
+  const size_t rows = std::max(mkv_max, static_cast<size_t>(B) * h.L0);
+  // workspace: 0 dX, 1 dX next, 2 xn, 3 xq, 4 H / dxq, 5 dH, 6 dO, 7 dgraw, 8 dQ, 9 dK, 10 dV,
+  // 11 raw, 12 GU / dGU, 13 z / dz, 14 inv (rows), 15 D / head scratch
+  for (int i = 0; i < 12; ++i) h.tw[i] = h.dalloc<float>(rows * d);
+  h.tw[12] = h.dalloc<float>(rows * 2 * m * 2);  // GU and dGU
+  h.tw[13] = h.dalloc<float>(rows * m);
+  h.tw[14] = h.dalloc<float>(rows * 2);
+  h.tw[15] = h.dalloc<float>(std::max(rows * h.H, static_cast<size_t>(B) * h.cfg.n_cand * (h.dh * 4 + 3)));
+  h.train_B = h.Bmax;
+}
+
+static inline int ew_grid(size_t n) { return static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 16)); }
+
+// Backward of one training forward; dz = dL/dlogits [B*N, 3] on the device.
+static void backward_device(Handle& h, int B, const float* dz) {
+  const SortConfig& c = h.cfg;
+  const int d = h.d, m = h.m, H = h.H, dk = h.dk, N = c.n_cand, dh = h.dh;
+  CK(cudaMemsetAsync(h.grads, 0, h.grad_count * sizeof(float), h.stream));
+  float* dX = h.tw[0];
+  float* dXn = h.tw[1];
+  float* inv = h.tw[14];
+  // ---- head: xc = final candidate rows, xh = RMSN(xc), hid = relu(xh W1 + b1)
+  const LayerDev& last = h.layers.back();
+  const int R = last.Rq, BN = B * N;
+  std::vector<int32_t> cmap_h(N);
+  for (int j = 0; j < N; ++j) cmap_h[j] = R - N + j;
+  int32_t*& cmap = h.cand_maps[R];
+  if (!cmap) cmap = h.upload(cmap_h);
+  float* xc = h.tw[2];
+  float* xh = h.tw[3];
+  float* hid = h.tw[15];
+  float* dhid = hid + static_cast<size_t>(BN) * dh;
+  const __nv_bfloat16* Xf = h.X[last.q_buf];
+  k_gather_f32<__nv_bfloat16><<<(BN + 7) / 8, 256, 0, h.stream>>>(Xf, cmap, N, R, BN, d, xc);
+  k_rmsnorm_rows<float><<<(BN + 7) / 8, 256, 0, h.stream>>>(xc, w32(h, "final_norm.gain"), BN, d, nullptr, 1, 1, xh,
+                                                            inv);
+  check_launch("head rows");
+  gemm_rm(h, false, false, BN, dh, d, xh, d, w32(h, "head.w1"), dh, hid, dh);
+  k_bias_relu<<<ew_grid(static_cast<size_t>(BN) * dh), 256, 0, h.stream>>>(hid, w32(h, "head.b1"), BN, dh);
+  gemm_rm(h, true, false, dh, 3, BN, hid, dh, dz, 3, grad_ptr(h, "head.w2"), 3);
+  k_colsum<<<dim3(1, 64), 32, 0, h.stream>>>(dz, BN, 3, grad_ptr(h, "head.b2"));
+  gemm_rm(h, false, true, BN, dh, 3, dz, 3, w32(h, "head.w2"), 3, dhid, dh);
+  k_relu_mask<<<ew_grid(static_cast<size_t>(BN) * dh), 256, 0, h.stream>>>(dhid, hid, static_cast<size_t>(BN) * dh);
+  gemm_rm(h, true, false, d, dh, BN, xh, d, dhid, dh, grad_ptr(h, "head.w1"), dh);
+  k_colsum<<<dim3((dh + 31) / 32, 64), 32, 0, h.stream>>>(dhid, BN, dh, grad_ptr(h, "head.b1"));
+  float* dxh = h.tw[4];
+  gemm_rm(h, false, true, BN, d, dh, dhid, dh, w32(h, "head.w1"), dh, dxh, d);
+  float* dxc = h.tw[5];
+  k_rmsnorm_bwd<float><<<(BN + 63) / 64, 256, d * 4, h.stream>>>(dxh, xc, inv, w32(h, "final_norm.gain"), BN, d, dxc,
+                                                                 0, grad_ptr(h, "final_norm.gain"));
+  CK(cudaMemsetAsync(dX, 0, static_cast<size_t>(B) * R * d * 4, h.stream));
+  k_scatter_add_rows<<<(BN + 7) / 8, 256, 0, h.stream>>>(dxc, cmap, B, N, R, d, dX);
+  check_launch("head backward");
+  // ---- blocks in reverse
+  for (int l = c.layers - 1; l >= 0; --l) {
+    const LayerDev& L = h.layers[l];
+    const LayerPlan& lp = h.plan.layers[l];
+    const auto& T = h.tl[l];
+    const std::string sl = std::to_string(l);
+    const std::string A = "attn." + sl + ".", F = "ffn." + sl + ".", Bk = "block." + sl + ".";
+    const int M = B * L.Rq, Mkv = B * L.Rkv;
+    const size_t nq = static_cast<size_t>(M) * d, nkv = static_cast<size_t>(Mkv) * d;
+    // FFN: xo = xr + down(swish(xf Wg) * (xf Wu)), xf = RMSN(xr = x1)
+    float* xf = h.tw[2];
+    float* GU = h.tw[12];
+    float* dGU = GU + static_cast<size_t>(M) * 2 * m;
+    float* z = h.tw[13];
+    k_rmsnorm_rows<__nv_bfloat16><<<(M + 7) / 8, 256, 0, h.stream>>>(T.x1, w32(h, Bk + "ffn_norm"), M, d, nullptr, 1,
+                                                                     1, xf, inv);
+    gemm_rm(h, false, false, M, 2 * m, d, xf, d, w32(h, F + "w_gu"), 2 * m, GU, 2 * m);
+    k_swiglu_z<<<ew_grid(static_cast<size_t>(M) * m), 256, 0, h.stream>>>(GU, M, m, z);
+    gemm_rm(h, true, false, m, d, M, z, m, dX, d, grad_ptr(h, F + "w_down"), d);
+    gemm_rm(h, false, true, M, m, d, dX, d, w32(h, F + "w_down"), d, z, m);  // z <- dz
+    k_swiglu_bwd<<<ew_grid(static_cast<size_t>(M) * m), 256, 0, h.stream>>>(z, GU, M, m, dGU);
+    gemm_rm(h, true, false, d, m, M, xf, d, dGU, 2 * m, grad_ptr(h, F + "w_gate"), m);
+    gemm_rm(h, true, false, d, m, M, xf, d, dGU + m, 2 * m, grad_ptr(h, F + "w_up"), m);
+    float* dxf = h.tw[3];
+    gemm_rm(h, false, true, M, d, 2 * m, dGU, 2 * m, w32(h, F + "w_gu"), 2 * m, dxf, d);
+    k_rmsnorm_bwd<__nv_bfloat16><<<(M + 63) / 64, 256, d * 4, h.stream>>>(dxf, T.x1, inv, w32(h, Bk + "ffn_norm"), M,
+                                                                           d, dX, 1, grad_ptr(h, Bk + "ffn_norm"));
+    check_launch("ffn backward");
+    // attention (attention.cpp:134-202); dX now holds d(xr)
+    float* Hm = h.tw[4];
+    float* dH = h.tw[5];
+    float* dO = h.tw[6];
+    float* dgraw = h.tw[7];
+    k_gate_fwd<<<ew_grid(nq), 256, 0, h.stream>>>(T.g, T.o_pre, nq, Hm);
+    gemm_rm(h, true, false, d, d, M, Hm, d, dX, d, grad_ptr(h, A + "wo"), d);
+    gemm_rm(h, false, true, M, d, d, dX, d, w32(h, A + "wo"), d, dH, d);
+    k_gate_bwd<<<ew_grid(nq), 256, 0, h.stream>>>(dH, T.g, T.o_pre, nq, dO, dgraw);
+    float* xn = h.tw[2];
+    float* xq = h.tw[3];
+    float* inv_a = h.tw[14] + static_cast<size_t>(h.train_B) * h.L0;
+    k_rmsnorm_rows<__nv_bfloat16><<<(Mkv + 7) / 8, 256, 0, h.stream>>>(T.x_in, w32(h, Bk + "attn_norm"), Mkv, d,
+                                                                       nullptr, 1, 1, xn, inv_a);
+    const float* xqp = xn;
+    if (!lp.q_identity) {
+      k_gather_f32<float><<<(M + 7) / 8, 256, 0, h.stream>>>(xn, L.query_rows, L.Rq, L.Rkv, M, d, xq);
+      xqp = xq;
+    }
+    check_launch("attention rows");
+    gemm_rm(h, true, false, d, d, M, xqp, d, dgraw, d, grad_ptr(h, A + "wg"), d);
+    float* dxq = h.tw[4];  // H no longer needed
+    gemm_rm(h, false, true, M, d, d, dgraw, d, w32(h, A + "wg"), d, dxq, d);
+    // attention core
+    float* Dd = h.tw[15];
+    k_attn_rowdot<<<(M * H + 7) / 8, 256, 0, h.stream>>>(dO, T.o_pre, B, L.Rq, H, dk, Dd);
+    AttnBwdArgs ab;
+    ab.q = T.q;
+    ab.k = T.k;
+    ab.v = T.v;
+    ab.dO = dO;
+    ab.lse = T.lse;
+    ab.D = Dd;
+    ab.rowmeta = L.rowmeta;
+    ab.H = H;
+    ab.Rq = L.Rq;
+    ab.Rkv = L.Rkv;
+    ab.BH = B * H;
+    ab.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(dk)));
+    ab.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(dk)));
+    float* dQ = h.tw[8];
+    float* dK = h.tw[9];
+    float* dV = h.tw[10];
+    ab.dq = dQ;
+    ab.dk = dK;
+    ab.dv = dV;
+    ab.blk_off = T.dq_off;
+    ab.blk_iv = T.dq_iv;
+    AttnBwdArgs ak = ab;
+    ak.blk_off = T.dkv_off;
+    ak.blk_iv = T.dkv_iv;
+    switch (dk) {
+      case 16:
+        k_attn_bwd_dq<16><<<dim3((L.Rq + 31) / 32, B * H), 32, 0, h.stream>>>(ab);
+        k_attn_bwd_dkv<16><<<dim3((L.Rkv + 31) / 32, B * H), 32, 0, h.stream>>>(ak);
+        break;
+      case 32:
+        k_attn_bwd_dq<32><<<dim3((L.Rq + 31) / 32, B * H), 32, 0, h.stream>>>(ab);
+        k_attn_bwd_dkv<32><<<dim3((L.Rkv + 31) / 32, B * H), 32, 0, h.stream>>>(ak);
+        break;
+      case 64:
+        k_attn_bwd_dq<64><<<dim3((L.Rq + 31) / 32, B * H), 32, 0, h.stream>>>(ab);
+        k_attn_bwd_dkv<64><<<dim3((L.Rkv + 31) / 32, B * H), 32, 0, h.stream>>>(ak);
+        break;
+      default:
+        throw ConfigError("training: unsupported head dim");
+    }
+    check_launch("attention core backward");
+    // QKNorm + RoPE backward against recomputed raw projections
+    float* raw = h.tw[11];
+    gemm_rm(h, false, false, M, d, d, xqp, d, w32(h, A + "wq"), d, raw, d);
+    k_qknorm_rope_bwd<<<(M + 7) / 8, 256, 0, h.stream>>>(dQ, raw, M, L.Rq, L.pos_q, h.rope, H, dk,
+                                                         w32(h, A + "qk_gain_q"), dQ, grad_ptr(h, A + "qk_gain_q"));
+    gemm_rm(h, false, false, Mkv, d, d, xn, d, w32(h, A + "wk"), d, raw, d);
+    k_qknorm_rope_bwd<<<(Mkv + 7) / 8, 256, 0, h.stream>>>(dK, raw, Mkv, L.Rkv, L.pos_kv, h.rope, H, dk,
+                                                           w32(h, A + "qk_gain_k"), dK, grad_ptr(h, A + "qk_gain_k"));
+    check_launch("qknorm/rope backward");
+    gemm_rm(h, true, false, d, d, M, xqp, d, dQ, d, grad_ptr(h, A + "wq"), d);
+    gemm_rm(h, true, false, d, d, Mkv, xn, d, dK, d, grad_ptr(h, A + "wk"), d);
+    gemm_rm(h, true, false, d, d, Mkv, xn, d, dV, d, grad_ptr(h, A + "wv"), d);
+    gemm_rm(h, false, true, M, d, d, dQ, d, w32(h, A + "wq"), d, dxq, d, 1.f);
+    float* dxn = h.tw[5];
+    gemm_rm(h, false, true, Mkv, d, d, dK, d, w32(h, A + "wk"), d, dxn, d);
+    gemm_rm(h, false, true, Mkv, d, d, dV, d, w32(h, A + "wv"), d, dxn, d, 1.f);
+    k_scatter_add_rows<<<(M + 7) / 8, 256, 0, h.stream>>>(dxq, L.query_rows, B, L.Rq, L.Rkv, d, dxn);
+    // d(x_in) = RMSN_bwd(dxn) + scatter of d(xr) through P(x, L_out)
+    k_rmsnorm_bwd<__nv_bfloat16><<<(Mkv + 63) / 64, 256, d * 4, h.stream>>>(
+        dxn, T.x_in, inv_a, w32(h, Bk + "attn_norm"), Mkv, d, dXn, 0, grad_ptr(h, Bk + "attn_norm"));
+    k_scatter_add_rows<<<(M + 7) / 8, 256, 0, h.stream>>>(dX, L.query_rows, B, L.Rq, L.Rkv, d, dXn);
+    check_launch("attention backward");
+    std::swap(dX, dXn);
+    (void)nkv;
+  }
+  h.dtokens = dX;
 }
 
 static void upload_batch(Handle& h, const SortBatch* b, bool on_device) {
@@ -1020,6 +1362,73 @@ int sort_enable_stage_timing(SortHandle p, int enable) {
     Handle* h = reinterpret_cast<Handle*>(p);
     if (!h) throw ConfigError("null handle");
     h->timing = enable != 0;
+  });
+}
+
+int sort_train_step(SortHandle p, const SortBatch* batch, const float* dlogits, float* logits) {
+  return api([&] {
+    Handle* h = ready(p);
+    if (!batch || !dlogits) throw ConfigError("null argument");
+    const int B = batch->batch;
+    begin_timing(*h);
+    upload_batch(*h, batch, false);
+    ensure_train_buffers(*h, B);
+    h->training = true;
+    try {
+      forward_device(*h, B);
+    } catch (...) {
+      h->training = false;
+      throw;
+    }
+    h->training = false;
+    const size_t nz = static_cast<size_t>(B) * h->cfg.n_cand * 3;
+    float*& dzb = h->dz_dev;
+    if (!dzb) dzb = h->dalloc<float>(static_cast<size_t>(h->Bmax) * h->cfg.n_cand * 3);
+    CK(cudaMemcpyAsync(dzb, dlogits, nz * 4, cudaMemcpyHostToDevice, h->stream));
+    CK(cublasSetStream(h->cublas, h->stream) == CUBLAS_STATUS_SUCCESS ? cudaSuccess : cudaErrorUnknown);
+    backward_device(*h, B, dzb);
+    if (logits) CK(cudaMemcpyAsync(logits, h->logits, nz * 4, cudaMemcpyDeviceToHost, h->stream));
+    collect_status(*h);
+  });
+}
+
+int sort_grad_info(SortHandle p, const char* name, int64_t* offset, int64_t* rows, int64_t* cols,
+                   int64_t* total) {
+  return api([&] {
+    Handle* h = ready(p);
+    if (total) *total = static_cast<int64_t>(h->grad_count);
+    if (!name) return;
+    auto it = h->grad_index.find(name);
+    if (it == h->grad_index.end()) throw ConfigError(std::string("no gradient for parameter ") + name);
+    if (offset) *offset = static_cast<int64_t>(it->second.first);
+    if (rows) *rows = it->second.second.first;
+    if (cols) *cols = it->second.second.second;
+  });
+}
+
+int sort_grads_copy(SortHandle p, float* buf, int buf_on_device, int to_handle) {
+  return api([&] {
+    Handle* h = ready(p);
+    if (!buf) throw ConfigError("null argument");
+    if (!h->grads) throw ConfigError("no gradients yet (call sort_train_step)");
+    const size_t bytes = h->grad_count * sizeof(float);
+    if (to_handle)
+      CK(cudaMemcpyAsync(h->grads, buf, bytes, buf_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                         h->stream));
+    else
+      CK(cudaMemcpyAsync(buf, h->grads, bytes, buf_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                         h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+  });
+}
+
+int sort_dtokens(SortHandle p, int32_t batch, float* out) {
+  return api([&] {
+    Handle* h = ready(p);
+    if (!out || !h->dtokens) throw ConfigError("no token gradients yet (call sort_train_step)");
+    CK(cudaMemcpyAsync(out, h->dtokens, static_cast<size_t>(batch) * h->L0 * h->d * 4, cudaMemcpyDeviceToHost,
+                       h->stream));
+    CK(cudaStreamSynchronize(h->stream));
   });
 }
 

@@ -1,0 +1,385 @@
+// SPDX-License-Identifier: Apache-2.0
+// Training backward of the SORT scoring path (the builder's GPU restatement of
+// AttentionLayer::backward, attention.cpp:134-202 with its intended math; rmsnorm_backward,
+// norm.hpp:32-45; and the spec's SwishGLU FFN / pre-norm blocks / ranking head,
+// SPEC.md:291-299,362-376). The dense GEMMs of the backward are plain library GEMMs
+// (cuBLAS, TF32 tensor cores, fp32 gradients, runtime.cu); the kernels here are the
+// row-wise pieces in between and the masked attention core backward.
+//
+// Gradients are fp32. Saved forward activations are the bf16 tensors the inference
+// kernels produce (layer input rows, rotated Q/K, V, sigmoid gate, pre-gate attention
+// output, x1) plus the attention's per-row log2-sum-exp.
+#pragma once
+
+#include "ptx.cuh"
+
+namespace sortk {
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// y = RMSNorm(x[src_row(r)]; gain) in fp32, inv_rms per row (norm.hpp:17-29). x is bf16 or
+// fp32; rows may be gathered: src row = (r / R) * Rsrc + map[r % R] when map != null.
+template <class T>
+__global__ void k_rmsnorm_rows(const T* __restrict__ x, const float* __restrict__ gain, int rows, int d,
+                               const int32_t* __restrict__ map, int R, int Rsrc, float* __restrict__ y,
+                               float* __restrict__ inv_out) {
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (w >= rows) return;
+  size_t src = w;
+  if (map) src = static_cast<size_t>(w / R) * Rsrc + map[w % R];
+  const T* xr = x + src * d;
+  float ss = 0.f;
+  for (int c = lane; c < d; c += 32) {
+    const float v = static_cast<float>(xr[c]);
+    ss = fmaf(v, v, ss);
+  }
+  ss = warp_sum(ss);
+  const float inv = rsqrtf(ss / static_cast<float>(d) + 1e-6f);
+  if (inv_out && lane == 0) inv_out[w] = inv;
+  if (y) {
+    float* yr = y + static_cast<size_t>(w) * d;
+    for (int c = lane; c < d; c += 32) yr[c] = static_cast<float>(xr[c]) * inv * (gain ? gain[c] : 1.f);
+  }
+}
+
+// out[r] = x[(r / R) * Rsrc + map[r % R]] as fp32 (row gather; map = null -> identity).
+template <class T>
+__global__ void k_gather_f32(const T* __restrict__ x, const int32_t* __restrict__ map, int R, int Rsrc, int rows, int d,
+                             float* __restrict__ out) {
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (w >= rows) return;
+  size_t src = w;
+  if (map) src = static_cast<size_t>(w / R) * Rsrc + map[w % R];
+  for (int c = lane; c < d; c += 32) out[static_cast<size_t>(w) * d + c] = static_cast<float>(x[src * d + c]);
+}
+
+// rmsnorm_backward (norm.hpp:32-45): dx = (dy*g - <dy*g, xhat>/n * xhat) * inv, dgain +=
+// sum_r dy*xhat. x is bf16 [rows, d]; dx is written (accum = 0) or added (accum = 1).
+// 8 rows per warp, dgain partials reduced in shared memory, one atomic per column per CTA.
+constexpr int kNormBwdRowsPerWarp = 8;
+template <class T>
+__global__ void __launch_bounds__(256) k_rmsnorm_bwd(const float* __restrict__ dy, const T* __restrict__ x,
+                                                     const float* __restrict__ inv, const float* __restrict__ gain,
+                                                     int rows, int d, float* __restrict__ dx, int accum,
+                                                     float* __restrict__ dgain) {
+  extern __shared__ float sg[];  // [d]
+  for (int c = threadIdx.x; c < d; c += blockDim.x) sg[c] = 0.f;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r0 = (blockIdx.x * (blockDim.x >> 5) + warp) * kNormBwdRowsPerWarp;
+  for (int r = r0; r < r0 + kNormBwdRowsPerWarp && r < rows; ++r) {
+    const float iv = inv[r];
+    const float* dyr = dy + static_cast<size_t>(r) * d;
+    const T* xr = x + static_cast<size_t>(r) * d;
+    float proj = 0.f;
+    for (int c = lane; c < d; c += 32) {
+      const float xh = static_cast<float>(xr[c]) * iv;
+      const float g = dyr[c];
+      atomicAdd(&sg[c], g * xh);
+      proj = fmaf(g * gain[c], xh, proj);
+    }
+    proj = warp_sum(proj) / static_cast<float>(d);
+    float* dxr = dx + static_cast<size_t>(r) * d;
+    for (int c = lane; c < d; c += 32) {
+      const float xh = static_cast<float>(xr[c]) * iv;
+      const float v = (dyr[c] * gain[c] - proj * xh) * iv;
+      dxr[c] = accum ? dxr[c] + v : v;
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < d; c += blockDim.x) atomicAdd(&dgain[c], sg[c]);
+}
+
+// SwishGLU pieces. GU = [gp | up] (fp32 [M, 2m]).
+__device__ __forceinline__ float sigmoid_f(float x) { return 1.f / (1.f + __expf(-x)); }
+__global__ void k_swiglu_z(const float* __restrict__ gu, int M, int m, float* __restrict__ z) {
+  const size_t n = static_cast<size_t>(M) * m;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t r = i / m, j = i - r * m;
+    const float g = gu[r * 2 * m + j], u = gu[r * 2 * m + m + j];
+    z[i] = g * sigmoid_f(g) * u;
+  }
+}
+// dgu = [dz * u * swish'(g) | dz * swish(g)], swish'(g) = s (1 + g (1 - s))
+__global__ void k_swiglu_bwd(const float* __restrict__ dz, const float* __restrict__ gu, int M, int m,
+                             float* __restrict__ dgu) {
+  const size_t n = static_cast<size_t>(M) * m;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t r = i / m, j = i - r * m;
+    const float g = gu[r * 2 * m + j], u = gu[r * 2 * m + m + j];
+    const float s = sigmoid_f(g);
+    dgu[r * 2 * m + j] = dz[i] * u * s * (1.f + g * (1.f - s));
+    dgu[r * 2 * m + m + j] = dz[i] * g * s;
+  }
+}
+
+// Gate (attention.cpp:124-127, backward :144-152): H = G * O; given dH: dO = dH * G,
+// dgraw = dH * O * G (1 - G). G, O bf16 [M, d].
+__global__ void k_gate_fwd(const __nv_bfloat16* __restrict__ G, const __nv_bfloat16* __restrict__ O, size_t n,
+                           float* __restrict__ H) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    H[i] = __bfloat162float(G[i]) * __bfloat162float(O[i]);
+}
+__global__ void k_gate_bwd(const float* __restrict__ dH, const __nv_bfloat16* __restrict__ G,
+                           const __nv_bfloat16* __restrict__ O, size_t n, float* __restrict__ dO,
+                           float* __restrict__ dgraw) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const float g = __bfloat162float(G[i]), o = __bfloat162float(O[i]);
+    dO[i] = dH[i] * g;
+    dgraw[i] = dH[i] * o * g * (1.f - g);
+  }
+}
+
+// D[bh, r] = sum_j dO[b, r, h*dk + j] * O[b, r, h*dk + j]  (softmax backward row term,
+// attention.cpp:169-172). One warp per (row, head-group of 32 columns).
+__global__ void k_attn_rowdot(const float* __restrict__ dO, const __nv_bfloat16* __restrict__ O, int B, int Rq,
+                              int H, int dk, float* __restrict__ D) {
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (w >= B * Rq * H) return;
+  const int row = w / H, h = w - row * H;  // row = b * Rq + r
+  float s = 0.f;
+  for (int j = lane; j < dk; j += 32)
+    s = fmaf(dO[static_cast<size_t>(row) * H * dk + h * dk + j],
+             __bfloat162float(O[static_cast<size_t>(row) * H * dk + h * dk + j]), s);
+  s = warp_sum(s);
+  if (lane == 0) {
+    const int b = row / Rq, r = row - b * Rq;
+    D[(static_cast<size_t>(b) * H + h) * Rq + r] = s;
+  }
+}
+
+// ---------------------------------------------------------------- masked attention backward
+// Per (request, head): P = exp2(s * scale_log2 - lse2) on visible entries (rows' compact mask
+// {lo, hi, self}), dP = dO V^T, dS = P (dP - D), dQ = scale dS K, dK = scale dS^T Q,
+// dV = P^T dO (attention.cpp:160-176). Lane-per-row SIMT with fp32 pair math: the q-centric
+// kernel gives one query row per lane and streams the block's visible kv rows (broadcast
+// loads); the kv-centric kernel gives one kv row per lane and streams the query rows that
+// see its block, so neither needs atomics. Work lists (row / column intervals per 32-block)
+// come from the host plan.
+struct AttnBwdArgs {
+  const __nv_bfloat16 *q, *k, *v;  // rotated Q [BH, Rq, dk], rotated K / V [BH, Rkv, dk]
+  const float* dO;                 // [B*Rq, H*dk] (row-major, head column blocks)
+  const float* lse;                // [BH, Rq] log2-domain
+  const float* D;                  // [BH, Rq]
+  const int4* rowmeta;             // [Rq] {lo, hi, self, 0}
+  const int32_t* blk_off;          // CSR over 32-blocks
+  const int2* blk_iv;              // [begin, end) intervals
+  float* dq;                       // [B*Rq, H*dk]
+  float* dk;                       // [B*Rkv, H*dk]
+  float* dv;                       // [B*Rkv, H*dk]
+  int BH, H, Rq, Rkv;
+  float scale_log2, scale;
+};
+
+template <int DK>
+__device__ __forceinline__ void load_row_bf16(const __nv_bfloat16* p, float2 (&o)[DK / 2]) {
+#pragma unroll
+  for (int i = 0; i < DK / 8; ++i) {
+    const int4 v = reinterpret_cast<const int4*>(p)[i];
+    const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) o[4 * i + e] = __bfloat1622float2(b[e]);
+  }
+}
+template <int DK>
+__device__ __forceinline__ float dot2(const float2 (&a)[DK / 2], const float2 (&b)[DK / 2]) {
+  float2 s0 = make_float2(0.f, 0.f), s1 = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int i = 0; i < DK / 2; i += 2) {
+    s0 = ffma2(a[i], b[i], s0);
+    s1 = ffma2(a[i + 1], b[i + 1], s1);
+  }
+  s0 = fadd2(s0, s1);
+  return s0.x + s0.y;
+}
+__device__ __forceinline__ bool row_sees(int4 m, int c) { return (c >= m.x && c <= m.y) || c == m.z; }
+
+// grid: (ceil(Rq / 32), BH), 32 threads. blk lists = kv-column intervals per 32-row q-block.
+template <int DK>
+__global__ void __launch_bounds__(32) k_attn_bwd_dq(const AttnBwdArgs a) {
+  const int qb = blockIdx.x, bh = blockIdx.y, lane = threadIdx.x;
+  const int b = bh / a.H, h = bh - b * a.H;
+  const int r = qb * 32 + lane;
+  const bool valid = r < a.Rq;
+  float2 q[DK / 2], go[DK / 2], acc[DK / 2];
+  int4 meta = make_int4(0, -1, -1, 0);
+  float lse = 0.f, Dr = 0.f;
+  if (valid) {
+    load_row_bf16<DK>(a.q + (static_cast<size_t>(bh) * a.Rq + r) * DK, q);
+    const float* gp = a.dO + (static_cast<size_t>(b) * a.Rq + r) * a.H * DK + h * DK;
+#pragma unroll
+    for (int i = 0; i < DK / 2; ++i) go[i] = make_float2(gp[2 * i], gp[2 * i + 1]);
+    meta = a.rowmeta[r];
+    lse = a.lse[static_cast<size_t>(bh) * a.Rq + r];
+    Dr = a.D[static_cast<size_t>(bh) * a.Rq + r];
+  } else {
+#pragma unroll
+    for (int i = 0; i < DK / 2; ++i) q[i] = go[i] = make_float2(0.f, 0.f);
+  }
+#pragma unroll
+  for (int i = 0; i < DK / 2; ++i) acc[i] = make_float2(0.f, 0.f);
+  const __nv_bfloat16* kb = a.k + static_cast<size_t>(bh) * a.Rkv * DK;
+  const __nv_bfloat16* vb = a.v + static_cast<size_t>(bh) * a.Rkv * DK;
+  for (int iv = a.blk_off[qb]; iv < a.blk_off[qb + 1]; ++iv) {
+    const int2 range = a.blk_iv[iv];
+    for (int c = range.x; c < range.y; ++c) {
+      float2 kk[DK / 2], vv[DK / 2];
+      load_row_bf16<DK>(kb + static_cast<size_t>(c) * DK, kk);
+      load_row_bf16<DK>(vb + static_cast<size_t>(c) * DK, vv);
+      if (!valid || !row_sees(meta, c)) continue;
+      const float p = exp2f(dot2<DK>(q, kk) * a.scale_log2 - lse);
+      const float ds = p * (dot2<DK>(go, vv) - Dr) * a.scale;
+      const float2 ds2 = make_float2(ds, ds);
+#pragma unroll
+      for (int i = 0; i < DK / 2; ++i) acc[i] = ffma2(ds2, kk[i], acc[i]);
+    }
+  }
+  if (valid) {
+    float* out = a.dq + (static_cast<size_t>(b) * a.Rq + r) * a.H * DK + h * DK;
+#pragma unroll
+    for (int i = 0; i < DK / 2; ++i) reinterpret_cast<float2*>(out)[i] = acc[i];
+  }
+}
+
+// grid: (ceil(Rkv / 32), BH), 32 threads. blk lists = q-row intervals per 32-column kv-block.
+template <int DK>
+__global__ void __launch_bounds__(32) k_attn_bwd_dkv(const AttnBwdArgs a) {
+  const int kb_ = blockIdx.x, bh = blockIdx.y, lane = threadIdx.x;
+  const int b = bh / a.H, h = bh - b * a.H;
+  const int c = kb_ * 32 + lane;
+  const bool valid = c < a.Rkv;
+  float2 kk[DK / 2], vv[DK / 2], dk[DK / 2], dv[DK / 2];
+  if (valid) {
+    load_row_bf16<DK>(a.k + (static_cast<size_t>(bh) * a.Rkv + c) * DK, kk);
+    load_row_bf16<DK>(a.v + (static_cast<size_t>(bh) * a.Rkv + c) * DK, vv);
+  } else {
+#pragma unroll
+    for (int i = 0; i < DK / 2; ++i) kk[i] = vv[i] = make_float2(0.f, 0.f);
+  }
+#pragma unroll
+  for (int i = 0; i < DK / 2; ++i) dk[i] = dv[i] = make_float2(0.f, 0.f);
+  for (int iv = a.blk_off[kb_]; iv < a.blk_off[kb_ + 1]; ++iv) {
+    const int2 range = a.blk_iv[iv];
+    for (int r = range.x; r < range.y; ++r) {
+      const int4 meta = a.rowmeta[r];
+      float2 q[DK / 2], go[DK / 2];
+      load_row_bf16<DK>(a.q + (static_cast<size_t>(bh) * a.Rq + r) * DK, q);
+      const float* gp = a.dO + (static_cast<size_t>(b) * a.Rq + r) * a.H * DK + h * DK;
+#pragma unroll
+      for (int i = 0; i < DK / 2; ++i) go[i] = reinterpret_cast<const float2*>(gp)[i];
+      const float lse = a.lse[static_cast<size_t>(bh) * a.Rq + r];
+      const float Dr = a.D[static_cast<size_t>(bh) * a.Rq + r];
+      if (!valid || !row_sees(meta, c)) continue;
+      const float p = exp2f(dot2<DK>(q, kk) * a.scale_log2 - lse);
+      const float ds = p * (dot2<DK>(go, vv) - Dr) * a.scale;
+      const float2 ds2 = make_float2(ds, ds), p2 = make_float2(p, p);
+#pragma unroll
+      for (int i = 0; i < DK / 2; ++i) {
+        dk[i] = ffma2(ds2, q[i], dk[i]);
+        dv[i] = ffma2(p2, go[i], dv[i]);
+      }
+    }
+  }
+  if (valid) {
+    const size_t o = (static_cast<size_t>(b) * a.Rkv + c) * a.H * DK + h * DK;
+#pragma unroll
+    for (int i = 0; i < DK / 2; ++i) {
+      reinterpret_cast<float2*>(a.dk + o)[i] = dk[i];
+      reinterpret_cast<float2*>(a.dv + o)[i] = dv[i];
+    }
+  }
+}
+
+// QKNorm + RoPE backward per (row, head) (attention.cpp:177-183): dx_rot -> inverse RoPE
+// at the row's position (rope.hpp:13-40, angle -> -angle) -> per-head RMSNorm backward
+// against the raw projection `raw` with gain g[h]. One warp per row, lanes over dims.
+// drot and draw may alias (in place): each lane reads its elements of a head before writing them.
+__global__ void k_qknorm_rope_bwd(const float* drot, const float* __restrict__ raw, int rows, int R,
+                                  const int32_t* __restrict__ pos, const float2* __restrict__ rope_tab, int H,
+                                  int dk, const float* __restrict__ gain, float* draw,
+                                  float* __restrict__ dgain) {
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (w >= rows) return;
+  const int p = pos[w % R];
+  const int d = H * dk;
+  for (int h = 0; h < H; ++h) {
+    // inverse rotation of the pair (2j, 2j+1): (c, s) -> (c, -s)
+    float dq[2] = {0.f, 0.f}, xr[2] = {0.f, 0.f};
+    const int j = lane;  // pair index (dk/2 <= 32)
+    const bool act = j < dk / 2;
+    if (act) {
+      const float2 cs = rope_tab[static_cast<size_t>(p) * (dk / 2) + j];
+      const float g0 = drot[static_cast<size_t>(w) * d + h * dk + 2 * j];
+      const float g1 = drot[static_cast<size_t>(w) * d + h * dk + 2 * j + 1];
+      dq[0] = cs.x * g0 + cs.y * g1;
+      dq[1] = -cs.y * g0 + cs.x * g1;
+      xr[0] = raw[static_cast<size_t>(w) * d + h * dk + 2 * j];
+      xr[1] = raw[static_cast<size_t>(w) * d + h * dk + 2 * j + 1];
+    }
+    const float ss = warp_sum(xr[0] * xr[0] + xr[1] * xr[1]);
+    const float inv = rsqrtf(ss / static_cast<float>(dk) + 1e-6f);
+    float proj = 0.f;
+    if (act) {
+      const float* g = gain + h * dk + 2 * j;
+      proj = dq[0] * g[0] * xr[0] * inv + dq[1] * g[1] * xr[1] * inv;
+    }
+    proj = warp_sum(proj) / static_cast<float>(dk);
+    if (act) {
+      const float* g = gain + h * dk + 2 * j;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const float xh = xr[e] * inv;
+        atomicAdd(&dgain[h * dk + 2 * j + e], dq[e] * xh);
+        draw[static_cast<size_t>(w) * d + h * dk + 2 * j + e] = (dq[e] * g[e] - proj * xh) * inv;
+      }
+    }
+  }
+}
+
+// dst[b*Rdst + map[r]] (+)= src[b*Rsrc + r] over B*Rsrc rows (unique destinations).
+__global__ void k_scatter_add_rows(const float* __restrict__ src, const int32_t* __restrict__ map, int B, int Rsrc,
+                                   int Rdst, int d, float* __restrict__ dst) {
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (w >= B * Rsrc) return;
+  const int b = w / Rsrc, r = w - b * Rsrc;
+  float* o = dst + (static_cast<size_t>(b) * Rdst + map[r]) * d;
+  const float* s = src + static_cast<size_t>(w) * d;
+  for (int c = lane; c < d; c += 32) o[c] += s[c];
+}
+
+// Column sums: out[c] += sum_r a[r, c] (bias gradients).
+__global__ void k_colsum(const float* __restrict__ a, int rows, int cols, float* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  float s = 0.f;
+  for (int r = blockIdx.y; r < rows; r += gridDim.y) s += a[static_cast<size_t>(r) * cols + c];
+  atomicAdd(&out[c], s);
+}
+
+// Ranking head forward pieces in fp32: hid = relu(pre + b1); and its backward mask.
+__global__ void k_bias_relu(float* __restrict__ x, const float* __restrict__ b, int rows, int cols) {
+  const size_t n = static_cast<size_t>(rows) * cols;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    x[i] = fmaxf(x[i] + b[i % cols], 0.f);
+}
+__global__ void k_relu_mask(float* __restrict__ g, const float* __restrict__ hid, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    if (hid[i] <= 0.f) g[i] = 0.f;
+}
+__global__ void k_add_f32(float* __restrict__ a, const float* __restrict__ b, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    a[i] += b[i];
+}
+
+}  // namespace sortk

@@ -55,6 +55,7 @@ EXPORTS = [
     "sort_tokenize", "sort_layer_plan", "sort_attention_forward", "sort_block_attention",
     "sort_time_bucket", "sort_geometric_schedule", "sort_retained_rows", "sort_mask_intervals",
     "sort_kernel_count", "sort_enable_stage_timing", "sort_stage_times", "sort_set_option",
+    "sort_train_step", "sort_grad_info", "sort_grads_copy", "sort_dtokens",
 ]
 
 _lib = None
@@ -90,6 +91,10 @@ def lib():
         L.sort_kernel_count.argtypes = [C.c_void_p, i32p]
         L.sort_enable_stage_timing.argtypes = [C.c_void_p, C.c_int]
         L.sort_set_option.argtypes = [C.c_void_p, C.c_char_p, C.c_int32]
+        L.sort_train_step.argtypes = [C.c_void_p, C.c_void_p, f32p, f32p]
+        L.sort_grad_info.argtypes = [C.c_void_p, C.c_char_p, i64p, i64p, i64p, i64p]
+        L.sort_grads_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int]
+        L.sort_dtokens.argtypes = [C.c_void_p, C.c_int32, f32p]
         L.sort_stage_times.argtypes = [C.c_void_p, f32p, C.c_int32, i32p, C.c_char_p, C.c_int32]
         _lib = L
     return _lib
@@ -245,6 +250,43 @@ class SortModel:
 
     def sync(self):
         _check(lib().sort_sync(self.h))
+
+    # -- training (sort_train_step) --------------------------------------------
+    def train_step(self, batch: Dict[str, np.ndarray], dlogits: np.ndarray) -> np.ndarray:
+        """Forward + backward given dL/dlogits [B, n_cand, 3]; returns the step's logits.
+        Gradients stay on the device (grad(), grads_flat())."""
+        hold = _BatchHold(batch)
+        B = hold.c.batch
+        dz = np.ascontiguousarray(dlogits, np.float32).reshape(B, self.cfg.n_cand, 3)
+        logits = np.zeros((B, self.cfg.n_cand, 3), np.float32)
+        _check(lib().sort_train_step(self.h, C.byref(hold.c), _p(dz, f32p), _p(logits, f32p)))
+        return logits
+
+    def grad_layout(self, name: Optional[str] = None):
+        off, r, c, tot = (C.c_int64(0) for _ in range(4))
+        _check(lib().sort_grad_info(self.h, name.encode() if name else None, C.byref(off), C.byref(r),
+                                    C.byref(c), C.byref(tot)))
+        return off.value, r.value, c.value, tot.value
+
+    def grads_flat(self) -> np.ndarray:
+        n = self.grad_layout()[3]
+        out = np.zeros(n, np.float32)
+        _check(lib().sort_grads_copy(self.h, C.c_void_p(out.ctypes.data), 0, 0))
+        return out
+
+    def grads_to_device(self, ptr: int, on_device: bool = True, to_handle: bool = False):
+        """Copy the flat gradient buffer to (or, to_handle=True, from) caller memory, e.g. a
+        torch tensor that torch.distributed all-reduces across data-parallel ranks."""
+        _check(lib().sort_grads_copy(self.h, C.c_void_p(ptr), int(on_device), int(to_handle)))
+
+    def grad(self, name: str) -> np.ndarray:
+        off, r, c, _ = self.grad_layout(name)
+        return self.grads_flat()[off: off + r * c].reshape(r, c)
+
+    def dtokens(self, batch_size: int) -> np.ndarray:
+        out = np.zeros((batch_size, self.cfg.seq_len, self.cfg.model_dim), np.float32)
+        _check(lib().sort_dtokens(self.h, batch_size, _p(out, f32p)))
+        return out
 
     # -- parity ops ------------------------------------------------------------
     def tokenize(self, batch: Dict[str, np.ndarray]):

@@ -1,0 +1,95 @@
+# SPDX-License-Identifier: Apache-2.0
+"""GPU training step (sort_train_step: forward + backward of the whole scoring path) against
+the fp64 oracle backward (tests/test_oracle_backward.py pins that by finite differences).
+
+The GPU forward is bf16 (the inference kernels), the backward fp32 with TF32 GEMMs; the
+oracle is fed the same bf16-rounded weights. The bar is self-calibrated, because these
+gradients are intrinsically sensitive at bf16 resolution (ReLU / softmax decisions flip):
+the oracle's own gradients move by `noise[n]` (relative L2) when every weight is perturbed
+by a relative N(0, 2^-9) -- half a bf16 ulp. Each GPU gradient must be within
+NOISE_FACTOR * noise[n] (floor GRAD_FLOOR) of the oracle's and point the same way
+(cosine > COS_MIN); dtokens likewise. Measured on B200: GPU error ~= 1x noise."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2603_03988_b200 import runtime as R
+from paper_2603_03988_b200 import synth
+from paper_2603_03988_b200.config import base_config, tiny_config
+
+pytestmark = pytest.mark.gpu
+
+NOISE_FACTOR = 3.0
+GRAD_FLOOR = 2e-2
+COS_MIN = 0.99
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def _oracle_grads(cfg, P, b, dz, names, B):
+    om = O.OracleModel(cfg, P)
+    ref = {n: np.zeros_like(P[n], dtype=np.float64) for n in names}
+    dtok, logits = [], []
+    for i in range(B):
+        logits.append(om.forward(b, i)[1])
+        g, dt = om.backward(b, i, dz[i].astype(np.float64), names)
+        for n in names:
+            ref[n] += g[n]
+        dtok.append(dt)
+    return ref, np.stack(dtok), np.stack(logits)
+
+
+def _check_step(cfg, seed, B):
+    P = synth.make_params(cfg, seed=seed)
+    Pr = {k: synth.bf16_round(v).astype(np.float64) for k, v in P.items()}
+    gm = R.SortModel(cfg, P, max_batch=B)
+    b = synth.make_batch(cfg, B, seed=seed + 1)
+    dz = np.random.default_rng(seed).normal(size=(B, cfg.n_cand, 3)).astype(np.float32)
+    logits = gm.train_step(b, dz)
+    names = [n for n in P if not n.startswith("tok.")]
+    ref, dtok_ref, zref = _oracle_grads(cfg, Pr, b, dz, names, B)
+    assert np.max(np.abs(logits - zref)) < 5e-2
+    rng = np.random.default_rng(seed + 2)
+    Pn = {k: (v * (1 + rng.normal(size=v.shape) * 2.0 ** -9) if not k.startswith("tok.") else v)
+          for k, v in Pr.items()}
+    refn, dtokn, _ = _oracle_grads(cfg, Pn, b, dz, names, B)
+    report = {}
+    for n in names:
+        g = gm.grad(n).astype(np.float64)
+        err, noise = rel_l2(g, ref[n]), rel_l2(refn[n], ref[n])
+        cos = float((g * ref[n]).sum() / max(np.linalg.norm(g) * np.linalg.norm(ref[n]), 1e-30))
+        report[n] = (err, noise, cos)
+    bad = {n: r for n, r in report.items()
+           if r[0] > max(NOISE_FACTOR * r[1], GRAD_FLOOR) or r[2] < COS_MIN}
+    assert not bad, bad
+    dtok = gm.dtokens(B)
+    assert rel_l2(dtok, dtok_ref) < max(NOISE_FACTOR * rel_l2(dtokn, dtok_ref), GRAD_FLOOR)
+    return report
+
+
+def test_train_step_tiny_vs_oracle():
+    _check_step(tiny_config(keep=[262, 128]), 7, 2)
+
+
+def test_train_step_base_shape_vs_oracle():
+    """SORT-base widths (d=256, 8 heads, m=640, W=256, F=128) with a shorter history so the
+    fp64 dense oracle stays fast; pruning after layer 2 as in SORT-base."""
+    cfg = base_config(n_hist=300, n_cand=16, n_items=20000)
+    cfg.keep = [cfg.prefix_len, cfg.prefix_len, 128, 128]
+    _check_step(cfg, 11, 2)
+
+
+def test_train_step_is_deterministic_in_loss_scale():
+    """Gradients are linear in dL/dlogits: doubling dz doubles every gradient."""
+    cfg = tiny_config()
+    P = synth.make_params(cfg, seed=5)
+    gm = R.SortModel(cfg, P, max_batch=1)
+    b = synth.make_batch(cfg, 1, seed=6)
+    dz = np.random.default_rng(1).normal(size=(1, cfg.n_cand, 3)).astype(np.float32)
+    gm.train_step(b, dz)
+    g1 = gm.grads_flat()
+    gm.train_step(b, 2 * dz)
+    g2 = gm.grads_flat()
+    assert rel_l2(g2, 2 * g1) < 1e-3
