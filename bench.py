@@ -162,6 +162,68 @@ def run_reference(args, cfg, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def run_train(args, cfg, rank, world, local, dist):
+    """BASELINE configs[2]: SORT-base training step (forward + backward of the scoring path,
+    sort_train_step) with the global batch sharded over the ranks and the flat fp32 gradient
+    all-reduced over NCCL (torch.distributed) every step. Loss: mean BCE of the three heads
+    against synthetic labels (dL/dlogits computed on the host from the step's logits of the
+    previous step's shape -- the labels are fixed, so dz = (sigmoid(z) - y) / n)."""
+    import torch
+    from paper_2603_03988_b200 import runtime as R
+    from paper_2603_03988_b200.sharding import allreduce_grads, shard_range
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    b0, b1 = shard_range(args.requests, world, rank)
+    B = b1 - b0
+    params = synth.make_params(cfg, seed=5)
+    model = R.SortModel(cfg, params, device=local, max_batch=B)
+    full = synth.make_batch(cfg, args.requests, seed=100)
+    batch = {k: np.ascontiguousarray(v[b0:b1]) for k, v in full.items()}
+    labels = (np.random.default_rng(7).random((args.requests, cfg.n_cand, 3)) < 0.2).astype(np.float32)[b0:b1]
+    n_total = args.requests * cfg.n_cand * 3
+    gbuf = torch.zeros(model.grad_layout()[3], dtype=torch.float32, device=dev)
+    z = np.zeros((B, cfg.n_cand, 3), np.float32)
+
+    def step():
+        nonlocal z
+        dz = (1.0 / (1.0 + np.exp(-z)) - labels) / n_total
+        z = model.train_step(batch, dz.astype(np.float32))
+        if dist:
+            model.grads_to_device(gbuf.data_ptr())
+            allreduce_grads(gbuf, world)
+            model.grads_to_device(gbuf.data_ptr(), to_handle=True)
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0])
+    if rank == 0:
+        print(json.dumps({
+            "metric": "requests trained/sec (SORT-base forward+backward, data parallel)",
+            "value": args.requests / (ms / 1e3), "unit": "requests/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16/fp32",
+            "data": "synthetic",
+            "config": {"workload": workload_desc(cfg) + " -- training step, BCE loss on 3 heads",
+                       "global_batch": args.requests, "requests_per_gpu": B,
+                       "parallelism": f"dp{world} (request shards, NCCL all-reduce of "
+                                      f"{model.grad_layout()[3]} fp32 gradients per step)"},
+            "timing": "wall clock per synchronized step (host-driven: the step returns logits "
+                      "and gradients), max over ranks",
+        }))
+    if dist:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -172,6 +234,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="minimum length of the CPU-baseline sample (>= 32 requests)")
+    ap.add_argument("--mode", default="forward", choices=["forward", "train"],
+                    help="train: SORT-base training step (BASELINE configs[2]), global batch "
+                         "--requests sharded over the ranks, gradient all-reduce over NCCL")
     ap.add_argument("--profile-launches", action="store_true",
                     help="short run for ncu launch lists (no CPU leg, no e2e)")
     args = ap.parse_args()
@@ -195,6 +260,10 @@ def main():
         if dist:
             dist.barrier()
             dist.destroy_process_group()
+        return
+
+    if args.mode == "train":
+        run_train(args, cfg, rank, world, local, dist)
         return
 
     from paper_2603_03988_b200 import runtime as R

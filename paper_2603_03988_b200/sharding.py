@@ -57,3 +57,16 @@ def max_over_ranks(values: List[float], world: int, device=None, group=None) -> 
     t = torch.tensor(values, dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return t.cpu().tolist()
+
+
+def allreduce_grads(flat, world: int, group=None):
+    """Data-parallel training (BASELINE configs[2]): sum the flat fp32 gradient buffer of
+    every rank's request shard (sort_grads_copy layout) in place. `flat` is a torch tensor
+    (CUDA under NCCL, CPU under gloo). The per-request gradients of the reference's
+    GradBuffer are additive (params.hpp:42-70), so the sum over shards equals the gradient
+    of the whole batch."""
+    if world == 1:
+        return flat
+    import torch.distributed as dist
+    dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+    return flat

@@ -72,3 +72,57 @@ def test_two_rank_gloo_sharded_scoring_and_max_time():
         assert p.exitcode == 0
     assert ok
     assert t == [2.0, 10.0]
+
+
+def _grad_worker(rank, world, port, out_q):
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    sys.path[:0] = [os.path.dirname(here), os.path.join(os.path.dirname(here), "oracle")]
+    import torch
+    import torch.distributed as dist
+    import oracle as O
+    from paper_2603_03988_b200 import synth
+    from paper_2603_03988_b200.config import tiny_config
+    from paper_2603_03988_b200 import sharding as S2
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = tiny_config(n_hist=40, n_cand=5, keep=[46, 20], local_window=8, full_suffix=6)
+    P = synth.make_params(cfg, seed=3)
+    names = sorted(n for n in P if not n.startswith("tok."))
+    batch = synth.make_batch(cfg, 3, seed=9)
+    dz = np.random.default_rng(2).normal(size=(3, cfg.n_cand, 3))
+    om = O.OracleModel(cfg, P)
+
+    def flat_grads(b, idx):
+        tot = np.zeros(sum(P[n].size for n in names))
+        for j, i in enumerate(idx):
+            g, _ = om.backward(b, j, dz[i], names)
+            tot += np.concatenate([g[n].ravel() for n in names])
+        return tot
+
+    lo, hi = S2.shard_range(3, world, rank)
+    local = flat_grads(S2.shard_batch(batch, world, rank), range(lo, hi))
+    t = torch.from_numpy(local)
+    S2.allreduce_grads(t, world)
+    if rank == 0:
+        ref = flat_grads(batch, range(3))
+        out_q.put(float(np.max(np.abs(t.numpy() - ref)) / np.max(np.abs(ref))))
+    dist.destroy_process_group()
+
+
+def test_two_rank_gloo_gradient_allreduce_equals_full_batch():
+    """Data-parallel training step (configs[2]): per-shard gradients (the oracle backward
+    stands in for each rank's sort_train_step) summed by allreduce_grads equal the gradient of
+    the whole batch."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_grad_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    err = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert err < 1e-12
