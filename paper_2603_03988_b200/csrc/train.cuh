@@ -203,8 +203,11 @@ __device__ __forceinline__ float dot2(const float2 (&a)[DK / 2], const float2 (&
 __device__ __forceinline__ bool row_sees(int4 m, int c) { return (c >= m.x && c <= m.y) || c == m.z; }
 
 // grid: (ceil(Rq / 32), BH), 32 threads. blk lists = kv-column intervals per 32-row q-block.
+// kv rows are staged 32 at a time in shared memory by coalesced warp loads and read back
+// as broadcasts.
 template <int DK>
 __global__ void __launch_bounds__(32) k_attn_bwd_dq(const AttnBwdArgs a) {
+  __shared__ int4 sk[32][DK / 8], sv[32][DK / 8];
   const int qb = blockIdx.x, bh = blockIdx.y, lane = threadIdx.x;
   const int b = bh / a.H, h = bh - b * a.H;
   const int r = qb * 32 + lane;
@@ -216,7 +219,7 @@ __global__ void __launch_bounds__(32) k_attn_bwd_dq(const AttnBwdArgs a) {
     load_row_bf16<DK>(a.q + (static_cast<size_t>(bh) * a.Rq + r) * DK, q);
     const float* gp = a.dO + (static_cast<size_t>(b) * a.Rq + r) * a.H * DK + h * DK;
 #pragma unroll
-    for (int i = 0; i < DK / 2; ++i) go[i] = make_float2(gp[2 * i], gp[2 * i + 1]);
+    for (int i = 0; i < DK / 2; ++i) go[i] = reinterpret_cast<const float2*>(gp)[i];
     meta = a.rowmeta[r];
     lse = a.lse[static_cast<size_t>(bh) * a.Rq + r];
     Dr = a.D[static_cast<size_t>(bh) * a.Rq + r];
@@ -226,20 +229,33 @@ __global__ void __launch_bounds__(32) k_attn_bwd_dq(const AttnBwdArgs a) {
   }
 #pragma unroll
   for (int i = 0; i < DK / 2; ++i) acc[i] = make_float2(0.f, 0.f);
-  const __nv_bfloat16* kb = a.k + static_cast<size_t>(bh) * a.Rkv * DK;
-  const __nv_bfloat16* vb = a.v + static_cast<size_t>(bh) * a.Rkv * DK;
+  const int4* kb = reinterpret_cast<const int4*>(a.k + static_cast<size_t>(bh) * a.Rkv * DK);
+  const int4* vb = reinterpret_cast<const int4*>(a.v + static_cast<size_t>(bh) * a.Rkv * DK);
   for (int iv = a.blk_off[qb]; iv < a.blk_off[qb + 1]; ++iv) {
     const int2 range = a.blk_iv[iv];
-    for (int c = range.x; c < range.y; ++c) {
-      float2 kk[DK / 2], vv[DK / 2];
-      load_row_bf16<DK>(kb + static_cast<size_t>(c) * DK, kk);
-      load_row_bf16<DK>(vb + static_cast<size_t>(c) * DK, vv);
-      if (!valid || !row_sees(meta, c)) continue;
-      const float p = exp2f(dot2<DK>(q, kk) * a.scale_log2 - lse);
-      const float ds = p * (dot2<DK>(go, vv) - Dr) * a.scale;
-      const float2 ds2 = make_float2(ds, ds);
+    for (int c0 = range.x; c0 < range.y; c0 += 32) {
+      const int n = min(32, range.y - c0);
+      __syncwarp();
+      if (lane < n) {
 #pragma unroll
-      for (int i = 0; i < DK / 2; ++i) acc[i] = ffma2(ds2, kk[i], acc[i]);
+        for (int i = 0; i < DK / 8; ++i) {
+          sk[lane][i] = kb[static_cast<size_t>(c0 + lane) * (DK / 8) + i];
+          sv[lane][i] = vb[static_cast<size_t>(c0 + lane) * (DK / 8) + i];
+        }
+      }
+      __syncwarp();
+      for (int jj = 0; jj < n; ++jj) {
+        const int c = c0 + jj;
+        float2 kk[DK / 2], vv[DK / 2];
+        load_row_bf16<DK>(reinterpret_cast<const __nv_bfloat16*>(sk[jj]), kk);
+        load_row_bf16<DK>(reinterpret_cast<const __nv_bfloat16*>(sv[jj]), vv);
+        if (!valid || !row_sees(meta, c)) continue;
+        const float p = exp2f(dot2<DK>(q, kk) * a.scale_log2 - lse);
+        const float ds = p * (dot2<DK>(go, vv) - Dr) * a.scale;
+        const float2 ds2 = make_float2(ds, ds);
+#pragma unroll
+        for (int i = 0; i < DK / 2; ++i) acc[i] = ffma2(ds2, kk[i], acc[i]);
+      }
     }
   }
   if (valid) {
@@ -250,8 +266,13 @@ __global__ void __launch_bounds__(32) k_attn_bwd_dq(const AttnBwdArgs a) {
 }
 
 // grid: (ceil(Rkv / 32), BH), 32 threads. blk lists = q-row intervals per 32-column kv-block.
+// Query rows (Q, dO, lse, D, mask row) are staged 32 at a time in shared memory.
 template <int DK>
 __global__ void __launch_bounds__(32) k_attn_bwd_dkv(const AttnBwdArgs a) {
+  __shared__ int4 sq[32][DK / 8];
+  __shared__ float4 sdo[32][DK / 4];
+  __shared__ int4 smeta[32];
+  __shared__ float2 sld[32];
   const int kb_ = blockIdx.x, bh = blockIdx.y, lane = threadIdx.x;
   const int b = bh / a.H, h = bh - b * a.H;
   const int c = kb_ * 32 + lane;
@@ -266,25 +287,42 @@ __global__ void __launch_bounds__(32) k_attn_bwd_dkv(const AttnBwdArgs a) {
   }
 #pragma unroll
   for (int i = 0; i < DK / 2; ++i) dk[i] = dv[i] = make_float2(0.f, 0.f);
+  const int4* qb = reinterpret_cast<const int4*>(a.q + static_cast<size_t>(bh) * a.Rq * DK);
   for (int iv = a.blk_off[kb_]; iv < a.blk_off[kb_ + 1]; ++iv) {
     const int2 range = a.blk_iv[iv];
-    for (int r = range.x; r < range.y; ++r) {
-      const int4 meta = a.rowmeta[r];
-      float2 q[DK / 2], go[DK / 2];
-      load_row_bf16<DK>(a.q + (static_cast<size_t>(bh) * a.Rq + r) * DK, q);
-      const float* gp = a.dO + (static_cast<size_t>(b) * a.Rq + r) * a.H * DK + h * DK;
+    for (int r0 = range.x; r0 < range.y; r0 += 32) {
+      const int n = min(32, range.y - r0);
+      __syncwarp();
+      if (lane < n) {
+        const int r = r0 + lane;
 #pragma unroll
-      for (int i = 0; i < DK / 2; ++i) go[i] = reinterpret_cast<const float2*>(gp)[i];
-      const float lse = a.lse[static_cast<size_t>(bh) * a.Rq + r];
-      const float Dr = a.D[static_cast<size_t>(bh) * a.Rq + r];
-      if (!valid || !row_sees(meta, c)) continue;
-      const float p = exp2f(dot2<DK>(q, kk) * a.scale_log2 - lse);
-      const float ds = p * (dot2<DK>(go, vv) - Dr) * a.scale;
-      const float2 ds2 = make_float2(ds, ds), p2 = make_float2(p, p);
+        for (int i = 0; i < DK / 8; ++i) sq[lane][i] = qb[static_cast<size_t>(r) * (DK / 8) + i];
+        const float4* gp = reinterpret_cast<const float4*>(a.dO + (static_cast<size_t>(b) * a.Rq + r) * a.H * DK + h * DK);
 #pragma unroll
-      for (int i = 0; i < DK / 2; ++i) {
-        dk[i] = ffma2(ds2, q[i], dk[i]);
-        dv[i] = ffma2(p2, go[i], dv[i]);
+        for (int i = 0; i < DK / 4; ++i) sdo[lane][i] = gp[i];
+        smeta[lane] = a.rowmeta[r];
+        sld[lane] = make_float2(a.lse[static_cast<size_t>(bh) * a.Rq + r], a.D[static_cast<size_t>(bh) * a.Rq + r]);
+      }
+      __syncwarp();
+      for (int jj = 0; jj < n; ++jj) {
+        if (!valid || !row_sees(smeta[jj], c)) continue;
+        float2 q[DK / 2], go[DK / 2];
+        load_row_bf16<DK>(reinterpret_cast<const __nv_bfloat16*>(sq[jj]), q);
+#pragma unroll
+        for (int i = 0; i < DK / 4; ++i) {
+          const float4 t = sdo[jj][i];
+          go[2 * i] = make_float2(t.x, t.y);
+          go[2 * i + 1] = make_float2(t.z, t.w);
+        }
+        const float2 ld = sld[jj];
+        const float p = exp2f(dot2<DK>(q, kk) * a.scale_log2 - ld.x);
+        const float ds = p * (dot2<DK>(go, vv) - ld.y) * a.scale;
+        const float2 ds2 = make_float2(ds, ds), p2 = make_float2(p, p);
+#pragma unroll
+        for (int i = 0; i < DK / 2; ++i) {
+          dk[i] = ffma2(ds2, q[i], dk[i]);
+          dv[i] = ffma2(p2, go[i], dv[i]);
+        }
       }
     }
   }
@@ -300,48 +338,52 @@ __global__ void __launch_bounds__(32) k_attn_bwd_dkv(const AttnBwdArgs a) {
 
 // QKNorm + RoPE backward per (row, head) (attention.cpp:177-183): dx_rot -> inverse RoPE
 // at the row's position (rope.hpp:13-40, angle -> -angle) -> per-head RMSNorm backward
-// against the raw projection `raw` with gain g[h]. One warp per row, lanes over dims.
+// against the raw projection `raw` with gain g[h]. Each warp takes kQkRowsPerWarp rows,
+// lanes over rotation pairs; the gain gradient is reduced in shared memory per CTA.
 // drot and draw may alias (in place): each lane reads its elements of a head before writing them.
-__global__ void k_qknorm_rope_bwd(const float* drot, const float* __restrict__ raw, int rows, int R,
-                                  const int32_t* __restrict__ pos, const float2* __restrict__ rope_tab, int H,
-                                  int dk, const float* __restrict__ gain, float* draw,
-                                  float* __restrict__ dgain) {
-  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (w >= rows) return;
-  const int p = pos[w % R];
+constexpr int kQkRowsPerWarp = 8;
+__global__ void __launch_bounds__(256) k_qknorm_rope_bwd(const float* drot, const float* __restrict__ raw, int rows,
+                                                         int R, const int32_t* __restrict__ pos,
+                                                         const float2* __restrict__ rope_tab, int H, int dk,
+                                                         const float* __restrict__ gain, float* draw,
+                                                         float* __restrict__ dgain) {
+  extern __shared__ float sg[];  // [H * dk]
   const int d = H * dk;
-  for (int h = 0; h < H; ++h) {
-    // inverse rotation of the pair (2j, 2j+1): (c, s) -> (c, -s)
-    float dq[2] = {0.f, 0.f}, xr[2] = {0.f, 0.f};
-    const int j = lane;  // pair index (dk/2 <= 32)
-    const bool act = j < dk / 2;
-    if (act) {
-      const float2 cs = rope_tab[static_cast<size_t>(p) * (dk / 2) + j];
-      const float g0 = drot[static_cast<size_t>(w) * d + h * dk + 2 * j];
-      const float g1 = drot[static_cast<size_t>(w) * d + h * dk + 2 * j + 1];
-      dq[0] = cs.x * g0 + cs.y * g1;
-      dq[1] = -cs.y * g0 + cs.x * g1;
-      xr[0] = raw[static_cast<size_t>(w) * d + h * dk + 2 * j];
-      xr[1] = raw[static_cast<size_t>(w) * d + h * dk + 2 * j + 1];
-    }
-    const float ss = warp_sum(xr[0] * xr[0] + xr[1] * xr[1]);
-    const float inv = rsqrtf(ss / static_cast<float>(dk) + 1e-6f);
-    float proj = 0.f;
-    if (act) {
-      const float* g = gain + h * dk + 2 * j;
-      proj = dq[0] * g[0] * xr[0] * inv + dq[1] * g[1] * xr[1] * inv;
-    }
-    proj = warp_sum(proj) / static_cast<float>(dk);
-    if (act) {
-      const float* g = gain + h * dk + 2 * j;
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const float xh = xr[e] * inv;
-        atomicAdd(&dgain[h * dk + 2 * j + e], dq[e] * xh);
-        draw[static_cast<size_t>(w) * d + h * dk + 2 * j + e] = (dq[e] * g[e] - proj * xh) * inv;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) sg[c] = 0.f;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = lane;  // rotation pair (dk/2 <= 32)
+  const bool act = j < dk / 2;
+  const int r0 = (blockIdx.x * (blockDim.x >> 5) + warp) * kQkRowsPerWarp;
+  for (int w = r0; w < r0 + kQkRowsPerWarp && w < rows; ++w) {
+    const int p = pos[w % R];
+    const float2 cs = act ? rope_tab[static_cast<size_t>(p) * (dk / 2) + j] : make_float2(1.f, 0.f);
+    for (int h = 0; h < H; ++h) {
+      float dq[2] = {0.f, 0.f}, xr[2] = {0.f, 0.f};
+      const size_t o = static_cast<size_t>(w) * d + h * dk + 2 * j;
+      if (act) {
+        const float2 g = *reinterpret_cast<const float2*>(drot + o);
+        dq[0] = cs.x * g.x + cs.y * g.y;  // inverse rotation of the pair (2j, 2j+1)
+        dq[1] = -cs.y * g.x + cs.x * g.y;
+        const float2 x = *reinterpret_cast<const float2*>(raw + o);
+        xr[0] = x.x;
+        xr[1] = x.y;
+      }
+      const float ss = warp_sum(xr[0] * xr[0] + xr[1] * xr[1]);
+      const float inv = rsqrtf(ss / static_cast<float>(dk) + 1e-6f);
+      const float g0 = act ? gain[h * dk + 2 * j] : 0.f, g1 = act ? gain[h * dk + 2 * j + 1] : 0.f;
+      const float proj = warp_sum(dq[0] * g0 * xr[0] * inv + dq[1] * g1 * xr[1] * inv) / static_cast<float>(dk);
+      if (act) {
+        const float xh0 = xr[0] * inv, xh1 = xr[1] * inv;
+        atomicAdd(&sg[h * dk + 2 * j], dq[0] * xh0);
+        atomicAdd(&sg[h * dk + 2 * j + 1], dq[1] * xh1);
+        *reinterpret_cast<float2*>(draw + o) =
+            make_float2((dq[0] * g0 - proj * xh0) * inv, (dq[1] * g1 - proj * xh1) * inv);
       }
     }
   }
+  __syncthreads();
+  for (int c = threadIdx.x; c < d; c += blockDim.x) atomicAdd(&dgain[c], sg[c]);
 }
 
 // dst[b*Rdst + map[r]] (+)= src[b*Rsrc + r] over B*Rsrc rows (unique destinations).
