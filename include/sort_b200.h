@@ -184,6 +184,21 @@ int sort_grads_copy(SortHandle h, float* buf, int buf_on_device, int to_handle);
 /* d(loss)/d(tokens) of the last step, [batch, L, d] fp32 on the host. */
 int sort_dtokens(SortHandle h, int32_t batch, float* out);
 
+/* ---------------------------------------------------------------- row-sharded item table */
+/* Embedding-heavy configuration (item table larger than one GPU should hold, row-sharded
+ * over the ranks): the caller exchanges the batch's unique item ids with the owning ranks
+ * (all-to-all), each owner gathers its rows with sort_gather_rows, the rows come back and
+ * form a batch-local table; sort_set_item_table makes the tokenizer read item rows from it
+ * (ids in the batch are then indices into it) until it is reset with rows = NULL.
+ * Replaces the Eigen row copies of history_concat_row / candidate_concat_row
+ * (tokenizer.cpp:95-127) against a table the process does not own. rows: device bf16
+ * [n_rows, item_dim]. */
+int sort_set_item_table(SortHandle h, const void* rows, int64_t n_rows);
+/* out[i] = table[ids[i]] (device pointers; row_bytes a multiple of 16) on `stream`; status 1
+ * if an id is outside [0, n_rows). */
+int sort_gather_rows(const void* table, int64_t n_rows, int32_t row_bytes, const int64_t* ids,
+                     int64_t n, void* out, void* stream);
+
 /* Kernel-selection knobs for A/B tests (no reference counterpart; defaults are the fastest
  * path): "fused_tail" (1 = one k_block_tail launch per block for Wo + residual + SwishGLU FFN
  * + residual where the shape allows it, 0 = the three separate GEMMs). Status 1 on an

@@ -23,6 +23,27 @@ __global__ void k_gather_rows(const __nv_bfloat16* __restrict__ src, const float
   if (lane == 0) ss_dst[w] = ss_src[s];
 }
 
+// Local step of the row-sharded embedding lookup (embedding-heavy):
+// out[i] = table[ids[i]] for the ids this rank owns (already shard-local), 16-byte vectors,
+// consecutive threads on consecutive chunks of a row (coalesced 64-byte item rows).
+// Out-of-range ids set *err and read row 0 (check_id, tokenizer.cpp:14-19).
+__global__ void k_gather_table_rows(const int4* __restrict__ table, int64_t n_rows, int chunks,
+                                    const int64_t* __restrict__ ids, int64_t n, int4* __restrict__ out,
+                                    int32_t* err) {
+  const int64_t total = n * chunks;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = t / chunks;
+    const int c = static_cast<int>(t - i * chunks);
+    int64_t id = ids[i];
+    if (id < 0 || id >= n_rows) {
+      atomicOr(err, 1);
+      id = 0;
+    }
+    out[t] = __ldg(table + id * chunks + c);
+  }
+}
+
 // Final RMSNorm + ranking head on candidate rows, fp32 (
 // PAPER.md:243 keeps the head in fp32): h = relu(xn W1 + b1), z = h W2 + b2,
 // p = sigmoid(z) for {click, cart, purchase}.

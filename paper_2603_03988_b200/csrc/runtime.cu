@@ -67,6 +67,10 @@ struct Handle {
   std::map<std::string, HostParam> host;
   bool finalized = false;
   bool fused_tail = true;  // sort_set_option("fused_tail")
+  // row-sharded item table (sort_set_item_table): the batch's item rows, gathered from the
+  // owning ranks, replace the handle's table for the following calls
+  const __nv_bfloat16* item_ext = nullptr;
+  int64_t item_ext_rows = 0;
   // ---- training (sort_train_step): fp32 master copies of the block/head parameters,
   // a flat fp32 gradient buffer, saved forward activations per layer, workspace
   std::map<std::string, float*> w32;
@@ -561,7 +565,7 @@ static void stage_mark(Handle& h, const std::string& name) {
 static void run_tokenizer(Handle& h, int B) {
   const SortConfig& c = h.cfg;
   TokParams p{};
-  p.item_tab = h.item;
+  p.item_tab = h.item_ext ? h.item_ext : h.item;
   p.action_tab = h.action;
   p.scene_tab = h.scene;
   p.time_tab = h.time;
@@ -598,7 +602,7 @@ static void run_tokenizer(Handle& h, int B) {
   p.scene_dim = c.scene_dim;
   p.time_dim = c.time_dim;
   p.prof_dim = c.profile_dim;
-  p.n_items = c.n_items;
+  p.n_items = h.item_ext ? static_cast<int>(h.item_ext_rows) : c.n_items;
   p.n_actions = c.n_actions;
   p.n_scenes = c.n_scenes;
   p.n_tb = c.n_time_buckets;
@@ -1430,6 +1434,39 @@ int sort_dtokens(SortHandle p, int32_t batch, float* out) {
     CK(cudaMemcpyAsync(out, h->dtokens, static_cast<size_t>(batch) * h->L0 * h->d * 4, cudaMemcpyDeviceToHost,
                        h->stream));
     CK(cudaStreamSynchronize(h->stream));
+  });
+}
+
+int sort_set_item_table(SortHandle p, const void* rows, int64_t n_rows) {
+  return api([&] {
+    Handle* h = reinterpret_cast<Handle*>(p);
+    if (!h) throw ConfigError("null handle");
+    if (rows && (n_rows < 1 || n_rows > INT32_MAX)) throw ConfigError("item table rows out of range");
+    h->item_ext = static_cast<const __nv_bfloat16*>(rows);
+    h->item_ext_rows = rows ? n_rows : 0;
+  });
+}
+
+int sort_gather_rows(const void* table, int64_t n_rows, int32_t row_bytes, const int64_t* ids, int64_t n,
+                     void* out, void* stream) {
+  return api([&] {
+    if (!table || !ids || !out) throw ConfigError("null argument");
+    if (row_bytes <= 0 || row_bytes % 16) throw ConfigError("row_bytes must be a positive multiple of 16");
+    if (n == 0) return;
+    int32_t* err = nullptr;
+    CK(cudaMallocAsync(reinterpret_cast<void**>(&err), 4, static_cast<cudaStream_t>(stream)));
+    CK(cudaMemsetAsync(err, 0, 4, static_cast<cudaStream_t>(stream)));
+    const int chunks = row_bytes / 16;
+    const int64_t threads = n * chunks;
+    const int grid = static_cast<int>(std::min<int64_t>((threads + 255) / 256, 148 * 32));
+    k_gather_table_rows<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const int4*>(table), n_rows, chunks, ids, n, static_cast<int4*>(out), err);
+    check_launch("gather rows");
+    int32_t herr = 0;
+    CK(cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, static_cast<cudaStream_t>(stream)));
+    CK(cudaFreeAsync(err, static_cast<cudaStream_t>(stream)));
+    CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    if (herr) throw ConfigError("gather rows: id outside the table shard");
   });
 }
 

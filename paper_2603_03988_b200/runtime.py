@@ -56,6 +56,7 @@ EXPORTS = [
     "sort_time_bucket", "sort_geometric_schedule", "sort_retained_rows", "sort_mask_intervals",
     "sort_kernel_count", "sort_enable_stage_timing", "sort_stage_times", "sort_set_option",
     "sort_train_step", "sort_grad_info", "sort_grads_copy", "sort_dtokens",
+    "sort_set_item_table", "sort_gather_rows",
 ]
 
 _lib = None
@@ -95,6 +96,9 @@ def lib():
         L.sort_grad_info.argtypes = [C.c_void_p, C.c_char_p, i64p, i64p, i64p, i64p]
         L.sort_grads_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int]
         L.sort_dtokens.argtypes = [C.c_void_p, C.c_int32, f32p]
+        L.sort_set_item_table.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
+        L.sort_gather_rows.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int64,
+                                       C.c_void_p, C.c_void_p]
         L.sort_stage_times.argtypes = [C.c_void_p, f32p, C.c_int32, i32p, C.c_char_p, C.c_int32]
         _lib = L
     return _lib
@@ -251,6 +255,12 @@ class SortModel:
     def sync(self):
         _check(lib().sort_sync(self.h))
 
+    # -- row-sharded item table --------------------------------------------------
+    def set_item_table(self, ptr: int, n_rows: int):
+        """Batch-local item rows (device bf16 [n_rows, item_dim]) for the next calls; ptr=0
+        restores the handle's own table."""
+        _check(lib().sort_set_item_table(self.h, C.c_void_p(ptr) if ptr else None, int(n_rows)))
+
     # -- training (sort_train_step) --------------------------------------------
     def train_step(self, batch: Dict[str, np.ndarray], dlogits: np.ndarray) -> np.ndarray:
         """Forward + backward given dL/dlogits [B, n_cand, 3]; returns the step's logits.
@@ -342,3 +352,11 @@ class SortModel:
         _check(lib().sort_stage_times(self.h, _p(ms, f32p), 256, C.byref(n), names, 8192))
         keys = names.value.decode().split(";") if n.value else []
         return dict(zip(keys, ms[: n.value].tolist()))
+
+
+def gather_rows(table_ptr: int, n_rows: int, row_bytes: int, ids_ptr: int, n: int, out_ptr: int,
+                stream_ptr: int = 0) -> None:
+    """out[i] = table[ids[i]] on the device (the owner-local step of a sharded lookup)."""
+    _check(lib().sort_gather_rows(C.c_void_p(table_ptr), int(n_rows), int(row_bytes),
+                                  C.c_void_p(ids_ptr), int(n), C.c_void_p(out_ptr),
+                                  C.c_void_p(stream_ptr) if stream_ptr else None))

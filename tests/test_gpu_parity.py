@@ -294,3 +294,48 @@ def test_fused_tail_d128_vs_oracle():
 def test_unknown_option_is_config_error(tiny):
     with pytest.raises(R.ConfigError):
         tiny[2].set_option("no_such_knob", 1)
+
+
+# ----------------------------------------------------------------------- row-sharded item table
+def test_batch_local_item_table_bit_identical(base):
+    """Embedding-heavy path (configs[4]) on one GPU: the batch's unique item rows gathered by
+    the CUDA gather kernel into a batch-local table (ShardedItemTable, world = 1) and fed with
+    remapped ids through sort_set_item_table give bit-identical scores to the full table."""
+    import torch
+    from paper_2603_03988_b200.sharding import ShardedItemTable
+    cfg, P, gm, _ = base
+    b = synth.make_batch(cfg, 3, seed=61)
+    ref = gm.forward(b)
+    dev = torch.device("cuda", 0)
+    table = torch.from_numpy(synth.bf16_round(P["tok.item_table"])).to(dev).to(torch.bfloat16)
+    tb = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in b.items()}
+    rows, mapped = ShardedItemTable(table, cfg.n_items, 0, 1).lookup(tb)
+    assert rows.shape[0] == len(np.unique(np.concatenate([b["hist_item"].ravel(), b["cand_item"].ravel()])))
+    gm.set_item_table(rows.data_ptr(), rows.shape[0])
+    try:
+        out = gm.forward({k: v.cpu().numpy() for k, v in mapped.items()})
+    finally:
+        gm.set_item_table(0, 0)
+    assert np.array_equal(out, ref)
+    bad = {k: v.cpu().numpy() for k, v in mapped.items()}
+    bad["cand_item"][0, 0] = rows.shape[0]  # outside the batch-local table
+    gm.set_item_table(rows.data_ptr(), rows.shape[0])
+    try:
+        with pytest.raises(R.ConfigError):
+            gm.forward(bad)
+    finally:
+        gm.set_item_table(0, 0)
+
+
+def test_gather_rows_kernel_and_range_check():
+    import torch
+    dev = torch.device("cuda", 0)
+    t = torch.randn(1000, 32, device=dev).to(torch.bfloat16)
+    ids = torch.tensor([5, 999, 0, 5, 123], dtype=torch.int64, device=dev)
+    out = torch.empty(5, 32, dtype=torch.bfloat16, device=dev)
+    R.gather_rows(t.data_ptr(), 1000, 64, ids.data_ptr(), 5, out.data_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(out, t[ids])
+    ids[1] = 1000
+    with pytest.raises(R.ConfigError):
+        R.gather_rows(t.data_ptr(), 1000, 64, ids.data_ptr(), 5, out.data_ptr())
