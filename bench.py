@@ -224,6 +224,72 @@ def run_train(args, cfg, rank, world, local, dist):
         dist.destroy_process_group()
 
 
+def run_embed(args, cfg, rank, world, local, dist):
+    """BASELINE configs[4]: SORT-base scoring whose item table (--table-rows x item_dim bf16,
+    6.4 GB at 100M rows) is row-sharded over the ranks. Per step and rank: dedupe the shard's
+    256 requests' item ids, all-to-all ids to their owners, owner-side CUDA gather, all-to-all
+    rows back, batch-local table -> sort_set_item_table -> SORT-base forward."""
+    import torch
+    from paper_2603_03988_b200 import runtime as R
+    from paper_2603_03988_b200.sharding import ShardedItemTable
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    rows_per_rank = (args.table_rows + world - 1) // world
+    g = torch.Generator(device=dev)
+    g.manual_seed(1000 + rank)
+    shard = (torch.randn((rows_per_rank, cfg.item_dim), generator=g, device=dev) * 0.1).to(torch.bfloat16)
+    small = base_config(batch=args.requests, n_items=1024)  # the handle's own table is unused
+    model = R.SortModel(small, synth.make_params(small, seed=5), device=local, max_batch=args.requests)
+    stream = torch.cuda.Stream(device=dev)
+    model.set_stream(stream.cuda_stream)
+    rng = np.random.default_rng(100 + rank)
+    B = args.requests
+    batch = synth.make_batch(small, B, seed=100 + rank)
+    batch["hist_item"] = rng.integers(0, args.table_rows, size=batch["hist_item"].shape, dtype=np.int64).astype(np.int32)
+    batch["cand_item"] = np.stack([rng.choice(args.table_rows, size=cfg.n_cand, replace=False)
+                                   for _ in range(B)]).astype(np.int32)
+    tb = {k: torch.from_numpy(v).to(dev) for k, v in batch.items()}
+    table = ShardedItemTable(shard, rows_per_rank, rank, world, stream_ptr=stream.cuda_stream)
+    scores = torch.empty((B, cfg.n_cand, 3), dtype=torch.float32, device=dev)
+    n_unique = []
+
+    def step():
+        with torch.cuda.stream(stream):
+            rows, mapped = table.lookup(tb)
+            n_unique.append(rows.shape[0])
+            model.set_item_table(rows.data_ptr(), rows.shape[0])
+            model.forward_device(R._DevBatch(mapped), scores.data_ptr())
+            model.sync()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0])
+    if rank == 0:
+        print(json.dumps({
+            "metric": "candidates scored/sec (SORT-base forward, row-sharded 100M-row item table)",
+            "value": world * B * cfg.n_cand / (ms / 1e3), "unit": "candidates/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": workload_desc(cfg) + f" -- item table {args.table_rows} x "
+                                                        f"{cfg.item_dim} bf16 row-sharded over {world} rank(s)",
+                       "requests_per_gpu": B, "unique_items_per_step": int(np.mean(n_unique)),
+                       "parallelism": f"dp{world} + row-sharded table, NCCL all-to-all of ids/rows"},
+            "timing": "wall clock per synchronized step (lookup has host-visible sizes), max over ranks",
+        }))
+    if dist:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -234,9 +300,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="minimum length of the CPU-baseline sample (>= 32 requests)")
-    ap.add_argument("--mode", default="forward", choices=["forward", "train"],
+    ap.add_argument("--mode", default="forward", choices=["forward", "train", "embed"],
                     help="train: SORT-base training step (BASELINE configs[2]), global batch "
-                         "--requests sharded over the ranks, gradient all-reduce over NCCL")
+                         "--requests sharded over the ranks, gradient all-reduce over NCCL; "
+                         "embed: BASELINE configs[4], 100M-row item table row-sharded over the "
+                         "ranks, all-to-all tokenization feeding SORT-base")
+    ap.add_argument("--table-rows", type=int, default=100_000_000)
     ap.add_argument("--profile-launches", action="store_true",
                     help="short run for ncu launch lists (no CPU leg, no e2e)")
     args = ap.parse_args()
@@ -264,6 +333,9 @@ def main():
 
     if args.mode == "train":
         run_train(args, cfg, rank, world, local, dist)
+        return
+    if args.mode == "embed":
+        run_embed(args, cfg, rank, world, local, dist)
         return
 
     from paper_2603_03988_b200 import runtime as R
