@@ -9,8 +9,8 @@ set -u
 TAG=${1:-r01}
 OUT=gpurun_out
 mkdir -p $OUT
-PER_STEP=24   # kernels per SORT-base forward (tokenizer, 4 x {qkvg.., attention, wo, ffn_up,
-              # ffn_down}, gather at the pruning layer, head)
+PER_STEP=16   # kernels per SORT-base forward (tokenizer, 4 x {qkvg(s), attention, block tail},
+              # gather at the pruning layer, head)
 W=3
 ncu --metrics gpu__time_duration.sum --clock-control none -s $((PER_STEP * W)) -c $((PER_STEP * 2)) \
     --csv --log-file $OUT/launches_$TAG.csv \

@@ -33,6 +33,8 @@ def stage_of(name, index_in_step, pruned_seen):
         return "gather"
     if "k_attention" in name:
         return "attention"
+    if "k_block_tail" in name:
+        return "tail"
     if "EpiQKVG" in name:
         return "qkvg"
     if "EpiSwiGLU" in name:
