@@ -82,11 +82,21 @@ __device__ __forceinline__ uint32_t chunk_vis_bits(int cs, int lo, int hi, int s
   return bits;
 }
 
+// TMEM plan: DK <= 32 keeps O_g in the free columns of its S buffer (256 columns, 2 CTAs per
+// SM); DK = 64 (SORT-large) gives O_g its own 64-column buffers after the two S buffers (512
+// columns, 1 CTA per SM).
+template <int DK>
+struct AttnTmem {
+  static constexpr uint32_t kCols = DK <= 32 ? 256 : 512;
+  static constexpr int kCtasPerSm = DK <= 32 ? 2 : 1;
+  __device__ static constexpr uint32_t o_col(int buf) { return DK <= 32 ? buf * 128 + 32 : 256 + buf * DK; }
+};
+
 template <int DK, bool kFixed>
-__global__ void __launch_bounds__(kAttnThreads, 2)
+__global__ void __launch_bounds__(kAttnThreads, AttnTmem<DK>::kCtasPerSm)
     k_attention(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
-  static_assert(DK <= 32, "O_g must fit the free columns [32, 64) of an S buffer");
+  static_assert(DK == 16 || DK == 32 || DK == 64, "head dim 16, 32 or 64");
   using S = AttnSmem<DK>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem_1k(smem_raw);
@@ -129,7 +139,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
     }
     mbar_fence_init();
   }
-  if (warp == 1) tmem_alloc(tslot, 256);
+  if (warp == 1) tmem_alloc(tslot, AttnTmem<DK>::kCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -219,7 +229,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t pa = tb + (kk >> 2) * 64 + (kk & 3) * 8;  // P of half kk/4, K=16 per MMA
           const uint32_t va = sv + kk * 16 * (DK * 2);           // V rows, MN-major, SBO = 8 rows
-          mma_bf16_ts(tb + 32, pa, umma_sdesc_kmajor(va, sw), id_o, kk != 0 ? 1u : 0u);
+          mma_bf16_ts(tmem + AttnTmem<DK>::o_col(buf), pa, umma_sdesc_kmajor(va, sw), id_o, kk != 0 ? 1u : 0u);
         }
         mma_commit(&pv_done[buf]);
         mma_commit(&kv_empty[st]);
@@ -253,7 +263,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
       mbar_wait_sleep(&pv_done[pb], (t >> 1) & 1);
       tc_fence_after();
       float o[DH];
-      tmem_row_chunk<DH>(tmem + pb * 128 + 32 + hf * DH + lane_off, o);
+      tmem_row_chunk<DH>(tmem + AttnTmem<DK>::o_col(pb) + hf * DH + lane_off, o);
       tc_fence_before();
       mbar_arrive(&o_read[pb]);
 #pragma unroll
@@ -432,7 +442,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, 256);
+    tmem_dealloc(tmem, AttnTmem<DK>::kCols);
   }
 }
 

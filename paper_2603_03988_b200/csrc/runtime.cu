@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -349,6 +350,7 @@ static void finalize(Handle& h) {
     };
     const uint32_t qkvg_side = side_bytes(3, dk);
     L.bn_full = pick_bn(4 * d, d, 4 * dk, qkvg_side);
+    if (const char* e = std::getenv("SORT_QKVG_BN")) L.bn_full = std::min(L.bn_full, std::atoi(e));  // experiment
     L.bn_half = pick_bn(2 * d, d, 2 * dk, qkvg_side);
     L.bn_o = pick_bn(d, d, 32);
     L.bn_up = pick_bn(2 * m, d, 64, side_bytes(1, 0));
@@ -478,7 +480,7 @@ static void launch_attention_dk(Handle& h, const LayerDev& L, const LayerPlan& l
                             static_cast<int>(smem)));
     attr_bytes = smem;
   }
-  const int grid = std::min(n_items, 2 * h.num_sms);
+  const int grid = std::min(n_items, AttnTmem<DK>::kCtasPerSm * h.num_sms);
   k_attention<DK, kFixed><<<grid, kAttnThreads, smem, h.stream>>>(L.tmQ, L.tmK, L.tmV, a);
   check_launch("attention");
   ++h.launches;
@@ -491,6 +493,8 @@ static void launch_attention(Handle& h, const LayerDev& L, const LayerPlan& lp, 
     case 33: launch_attention_dk<16, true>(h, L, lp, B); break;
     case 64: launch_attention_dk<32, false>(h, L, lp, B); break;
     case 65: launch_attention_dk<32, true>(h, L, lp, B); break;
+    case 128: launch_attention_dk<64, false>(h, L, lp, B); break;
+    case 129: launch_attention_dk<64, true>(h, L, lp, B); break;
     default: throw ConfigError("unsupported head dim");
   }
 }
@@ -1267,7 +1271,7 @@ int sort_block_attention(int32_t nh, int32_t l_q, int32_t l_kv, int32_t dk, cons
                          const int32_t* self_idx, float* out, int64_t* skipped, int64_t* total) {
   return api([&] {
     if (nh < 1 || l_q < 1 || l_kv < 1) throw ConfigError("block_attention: bad shape");
-    if (dk != 16 && dk != 32) throw ConfigError("block_attention: dk must be 16 or 32");
+    if (dk != 16 && dk != 32 && dk != 64) throw ConfigError("block_attention: dk must be 16, 32 or 64");
     int dev = 0;
     CK(cudaGetDevice(&dev));
     Handle h;

@@ -137,7 +137,7 @@ def test_layer_masks_bit_exact(which, tiny, base):
 
 
 # ----------------------------------------------------------------------- attention operator
-@pytest.mark.parametrize("dk", [16, 32])
+@pytest.mark.parametrize("dk", [16, 32, 64])
 def test_block_attention_vs_dense_oracle(dk):
     rng = np.random.default_rng(dk)
     cases = [(128, 128, -1, 0, 0), (300, 300, 64, 0, 0), (70, 1094, -1, 0, 0),
