@@ -290,6 +290,61 @@ def run_embed(args, cfg, rank, world, local, dist):
         dist.destroy_process_group()
 
 
+def run_large(args, rank, world, local, dist):
+    """BASELINE configs[3]: SORT-large (12 layers, d=1024, 16 heads, 4096 history, W=256,
+    128 targets, geometric pruning) forward, 8 requests per GPU, requests sharded over the
+    ranks (weak scaling). Generic path: TF32 library GEMMs + the tcgen05 attention core."""
+    import torch
+    from paper_2603_03988_b200 import runtime as R
+    from paper_2603_03988_b200.config import large_config
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    B = 8
+    cfg = large_config(batch=B)
+    model = R.SortModel(cfg, synth.make_params(cfg, seed=5), device=local, max_batch=B)
+    stream = torch.cuda.Stream(device=dev)
+    model.set_stream(stream.cuda_stream)
+    batch = synth.make_batch(cfg, B, seed=200 + rank)
+    dbatch = R._DevBatch({k: torch.from_numpy(v).to(dev) for k, v in batch.items()})
+    scores = torch.empty((B, cfg.n_cand, 3), dtype=torch.float32, device=dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            model.forward_device(dbatch, scores.data_ptr())
+        model.sync()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        if dist:
+            dist.barrier()
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            ev[i][0].record(stream)
+            model.forward_device(dbatch, scores.data_ptr())
+            ev[i][1].record(stream)
+        model.sync()
+    ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0])
+    fl = forward_flops(cfg)
+    peaks, _ = measured_peaks()
+    if rank == 0:
+        print(json.dumps({
+            "metric": "candidates scored/sec (SORT-large forward)", "value": world * B * cfg.n_cand / (ms / 1e3),
+            "unit": "candidates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "tf32 GEMMs / bf16 attention", "data": "synthetic",
+            "mfu_vs_bf16_peak": fl["total"] * B / (ms / 1e3) / (peaks["bf16_tflops"] * 1e12),
+            "algorithmic_tflop_per_step": fl["total"] * B / 1e12,
+            "config": {"workload": f"SORT-large: {cfg.layers} layers, d={cfg.model_dim}, {cfg.heads} heads, "
+                                   f"m={cfg.ffn_dim}, {B} requests/GPU x ({cfg.n_hist} history + {cfg.n_cand} "
+                                   f"targets), L={cfg.seq_len}, W={cfg.local_window}, keep={cfg.keep_schedule()}",
+                       "requests_per_gpu": B, "l2": "flushed (256 MB write) before every timed step"},
+        }))
+    if dist:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -300,7 +355,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="minimum length of the CPU-baseline sample (>= 32 requests)")
-    ap.add_argument("--mode", default="forward", choices=["forward", "train", "embed"],
+    ap.add_argument("--mode", default="forward", choices=["forward", "train", "embed", "large"],
                     help="train: SORT-base training step (BASELINE configs[2]), global batch "
                          "--requests sharded over the ranks, gradient all-reduce over NCCL; "
                          "embed: BASELINE configs[4], 100M-row item table row-sharded over the "
@@ -336,6 +391,9 @@ def main():
         return
     if args.mode == "embed":
         run_embed(args, cfg, rank, world, local, dist)
+        return
+    if args.mode == "large":
+        run_large(args, rank, world, local, dist)
         return
 
     from paper_2603_03988_b200 import runtime as R

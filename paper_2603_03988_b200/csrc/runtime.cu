@@ -5,7 +5,6 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
-#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -22,6 +21,7 @@
 #include "tma_host.hpp"
 #include "tokenizer.cuh"
 #include "train.cuh"
+#include "generic.cuh"
 
 namespace sortk {
 
@@ -68,6 +68,7 @@ struct Handle {
   std::map<std::string, HostParam> host;
   bool finalized = false;
   bool fused_tail = true;  // sort_set_option("fused_tail")
+  bool generic = false;    // d > 256 (SORT-large): projections through the generic path
   // row-sharded item table (sort_set_item_table): the batch's item rows, gathered from the
   // owning ranks, replace the handle's table for the following calls
   const __nv_bfloat16* item_ext = nullptr;
@@ -90,6 +91,11 @@ struct Handle {
   float *tw[16] = {nullptr};  // backward workspace
   float* dtokens = nullptr;
   float* dz_dev = nullptr;                 // dL/dlogits of the current step
+  // generic (d > 256) forward: fp32 residual stream and workspace
+  float* gX[2] = {nullptr, nullptr};
+  float* gw[10] = {nullptr};
+  int32_t* g_rows = nullptr;
+  int gX_final = 0;
   std::map<int, int32_t*> cand_maps;       // candidate-row maps for the head backward
   int train_B = 0;
   cublasHandle_t cublas = nullptr;
@@ -230,7 +236,7 @@ static void finalize(Handle& h) {
   const char* gg[3] = {"tok.g_hist", "tok.g_cand", "tok.g_prof"};
   const int gk[3] = {hw, c.item_dim, c.profile_dim};
   for (int g = 0; g < 3; ++g) {
-    h.tok_wt[g] = h.upload(transpose_bf16(need_param(h, gw[g], gk[g], d), 64, nullptr));
+    if (!h.generic) h.tok_wt[g] = h.upload(transpose_bf16(need_param(h, gw[g], gk[g], d), 64, nullptr));
     h.tok_b[g] = h.upload(need_param(h, gb[g], 1, d).v);
     h.tok_g[g] = h.upload(need_param(h, gg[g], 1, d).v);
   }
@@ -282,8 +288,8 @@ static void finalize(Handle& h) {
     const std::string f = "ffn." + std::to_string(l) + ".";
     const HostParam& ga = need_param(h, bk + "attn_norm", 1, d);
     const HostParam& gf = need_param(h, bk + "ffn_norm", 1, d);
-    {  // Q/K/V/G projections: W^T rows interleaved head by head in section order `order`,
-       // attention pre-norm gain folded into the input rows.
+    if (!h.generic) {  // Q/K/V/G projections: W^T rows interleaved head by head in section
+                       // order `order`, attention pre-norm gain folded into the input rows.
       const std::string names[4] = {"wq", "wk", "wv", "wg"};  // kSecQ, kSecK, kSecV, kSecG
       std::vector<__nv_bfloat16> t[4];
       for (int sct = 0; sct < 4; ++sct) t[sct] = transpose_bf16(need_param(h, a + names[sct], d, d), d, ga.v.data());
@@ -300,8 +306,8 @@ static void finalize(Handle& h) {
       L.w_kv = build({kSecK, kSecV});
       L.w_qg = build({kSecQ, kSecG});
     }
-    L.w_o = h.upload(transpose_bf16(need_param(h, a + "wo", d, d), d, nullptr));
-    {  // SwishGLU up: interleave 32-column blocks [gate_j | up_j], ffn pre-norm gain folded
+    if (!h.generic) L.w_o = h.upload(transpose_bf16(need_param(h, a + "wo", d, d), d, nullptr));
+    if (!h.generic) {  // SwishGLU up: interleave 32-column blocks [gate_j | up_j], ffn pre-norm gain folded
       const HostParam& wg = need_param(h, f + "w_gate", d, m);
       const HostParam& wu = need_param(h, f + "w_up", d, m);
       std::vector<__nv_bfloat16> w(static_cast<size_t>(2) * m * d);
@@ -314,7 +320,7 @@ static void finalize(Handle& h) {
         }
       L.w_up = h.upload(w);
     }
-    L.w_down = h.upload(transpose_bf16(need_param(h, f + "w_down", m, d), m, nullptr));
+    if (!h.generic) L.w_down = h.upload(transpose_bf16(need_param(h, f + "w_down", m, d), m, nullptr));
     {
       const HostParam& gq = need_param(h, a + "qk_gain_q", H, dk);
       const HostParam& gk = need_param(h, a + "qk_gain_k", H, dk);
@@ -342,6 +348,7 @@ static void finalize(Handle& h) {
     L.in_buf = cur;
     L.q_buf = lp.q_identity ? cur : 1 - cur;
     cur = L.q_buf;
+    if (!h.generic) {
     // GEMM tile widths (weight-stationary: BN x K weight slice resident in smem)
     auto pick_bn = [&](int N, int K, int chunk, uint32_t side = 0) {
       for (int bn = 256; bn >= chunk; bn /= 2)
@@ -350,7 +357,6 @@ static void finalize(Handle& h) {
     };
     const uint32_t qkvg_side = side_bytes(3, dk);
     L.bn_full = pick_bn(4 * d, d, 4 * dk, qkvg_side);
-    if (const char* e = std::getenv("SORT_QKVG_BN")) L.bn_full = std::min(L.bn_full, std::atoi(e));  // experiment
     L.bn_half = pick_bn(2 * d, d, 2 * dk, qkvg_side);
     L.bn_o = pick_bn(d, d, 32);
     L.bn_up = pick_bn(2 * m, d, 64, side_bytes(1, 0));
@@ -374,6 +380,7 @@ static void finalize(Handle& h) {
       L.tmWup_t = make_tmap_2d(L.w_up, 2 * m, d, d, 128, 64, 128);
       L.tmWdown_t = make_tmap_2d(L.w_down, d, m, m, d, 64, 128);
     }
+    }  // !generic
     {
       const uint64_t BH = static_cast<uint64_t>(h.Bmax) * H;
       uint64_t dq[3] = {static_cast<uint64_t>(dk), static_cast<uint64_t>(L.Rq), BH};
@@ -396,7 +403,10 @@ static void finalize(Handle& h) {
   // buffer in the same name order; W_gate | W_up also concatenated as ffn.<l>.w_gu [d, 2m]
   size_t goff = 0;
   for (auto& kv : h.host) {
-    if (kv.first.rfind("tok.", 0) == 0) continue;
+    if (kv.first.rfind("tok.", 0) == 0) {  // tokenizer projections (generic path), not tables
+      if (kv.first.find("table") == std::string::npos) h.w32[kv.first] = h.upload(kv.second.v);
+      continue;
+    }
     h.w32[kv.first] = h.upload(kv.second.v);
     h.grad_index[kv.first] = {goff, {kv.second.rows, kv.second.cols}};
     goff += static_cast<size_t>(kv.second.rows) * kv.second.cols;
@@ -566,7 +576,7 @@ static void stage_mark(Handle& h, const std::string& name) {
   h.stage_names.push_back(name);
 }
 
-static void run_tokenizer(Handle& h, int B) {
+static TokParams tok_params(Handle& h, int B) {
   const SortConfig& c = h.cfg;
   TokParams p{};
   p.item_tab = h.item_ext ? h.item_ext : h.item;
@@ -614,6 +624,11 @@ static void run_tokenizer(Handle& h, int B) {
   p.tiles_hist = (B * c.n_hist + 127) / 128;
   p.tiles_cand = (B * c.n_cand + 127) / 128;
   p.tiles_prof = (B * c.n_profile_fields + 127) / 128;
+  return p;
+}
+
+static void run_tokenizer(Handle& h, int B) {
+  const TokParams p = tok_params(h, B);
   static size_t attr_bytes = 0;
   const size_t smem = tok_smem_bytes(h.d);
   if (smem > attr_bytes) {
@@ -972,6 +987,122 @@ static void backward_device(Handle& h, int B, const float* dz) {
   h.dtokens = dX;
 }
 
+
+// ====================================================================== generic forward (d > 256)
+static void ensure_generic_buffers(Handle& h) {
+  if (h.gX[0]) return;
+  if (!h.cublas && cublasCreate(&h.cublas) != CUBLAS_STATUS_SUCCESS) throw RuntimeFailure("cublasCreate failed");
+  const size_t rows = static_cast<size_t>(h.Bmax) * h.L0;
+  const int d = h.d, m = h.m;
+  for (int i = 0; i < 2; ++i) h.gX[i] = h.dalloc<float>(rows * d);
+  // 0 xn, 1 xq / xf, 2 Qr / a, 3 Kr, 4 Vr, 5 Gr, 6 GU [rows, 2m], 7 z [rows, m], 8 tokenizer
+  // concat rows [rows, 64], 9 head scratch
+  for (int i = 0; i < 6; ++i) h.gw[i] = h.dalloc<float>(rows * d);
+  h.gw[6] = h.dalloc<float>(rows * 2 * m);
+  h.gw[7] = h.dalloc<float>(rows * m);
+  h.gw[8] = h.dalloc<float>(rows * 64);
+  h.gw[9] = h.dalloc<float>(static_cast<size_t>(h.Bmax) * h.cfg.n_cand * (2 * d + h.dh + 4));
+  h.g_rows = h.dalloc<int32_t>(rows);
+}
+
+static inline int warp_rows_grid(int rows) { return (rows + 7) / 8; }
+
+static void forward_generic(Handle& h, int B) {
+  ensure_generic_buffers(h);
+  CK(cublasSetStream(h.cublas, h.stream) == CUBLAS_STATUS_SUCCESS ? cudaSuccess : cudaErrorUnknown);
+  const SortConfig& c = h.cfg;
+  const int d = h.d, m = h.m, H = h.H, dk = h.dk, N = c.n_cand;
+  CK(cudaMemsetAsync(h.err, 0, 4 * sizeof(int32_t), h.stream));
+  // ---- tokenizer: gather -> projection -> bias + RMSNorm (tokenizer.cpp:144-238)
+  const TokParams tp = tok_params(h, B);
+  float* X = h.gX[0];
+  const int gcount[3] = {B * c.n_hist, B * N, B * c.n_profile_fields};
+  const int gK[3] = {c.item_dim + c.action_dim + c.scene_dim + c.time_dim, c.item_dim, c.profile_dim};
+  const char* gname[3] = {"hist", "cand", "prof"};
+  for (int g = 0; g < 3; ++g) {
+    if (gcount[g] == 0) continue;
+    k_tok_concat<<<warp_rows_grid(gcount[g]), 256, 0, h.stream>>>(tp, g, gK[g], h.gw[8], h.g_rows);
+    gemm_rm(h, false, false, gcount[g], d, gK[g], h.gw[8], gK[g], w32(h, std::string("tok.w_") + gname[g]), d,
+            h.gw[0], d);
+    k_tok_finish<<<warp_rows_grid(gcount[g]), 256, 0, h.stream>>>(h.gw[0], w32(h, std::string("tok.b_") + gname[g]),
+                                                                w32(h, std::string("tok.g_") + gname[g]), h.g_rows,
+                                                                gcount[g], d, X);
+  }
+  if (c.special_tokens)
+    k_tok_specials<<<warp_rows_grid(B * 3), 256, 0, h.stream>>>(w32(h, "tok.special"), B, h.L0, c.n_hist,
+                                                               c.n_profile_fields, d, X);
+  check_launch("generic tokenizer");
+  stage_mark(h, "tokenizer");
+  // ---- blocks
+  int cur = 0;
+  for (int l = 0; l < c.layers; ++l) {
+    const LayerDev& L = h.layers[l];
+    const LayerPlan& lp = h.plan.layers[l];
+    const std::string sl = std::to_string(l);
+    const std::string A = "attn." + sl + ".", F = "ffn." + sl + ".", Bk = "block." + sl + ".";
+    const int M = B * L.Rq, Mkv = B * L.Rkv;
+    float* x = h.gX[cur];
+    float* xo = h.gX[1 - cur];
+    float* xn = h.gw[0];
+    float* xq = h.gw[1];
+    k_rmsnorm_rows<float><<<warp_rows_grid(Mkv), 256, 0, h.stream>>>(x, w32(h, Bk + "attn_norm"), Mkv, d, nullptr, 1,
+                                                                     1, xn, nullptr);
+    const float* xqp = xn;
+    if (!lp.q_identity) {
+      k_gather_f32<float><<<warp_rows_grid(M), 256, 0, h.stream>>>(xn, L.query_rows, L.Rq, L.Rkv, M, d, xq);
+      xqp = xq;
+    }
+    gemm_rm(h, false, false, M, d, d, xqp, d, w32(h, A + "wq"), d, h.gw[2], d);
+    gemm_rm(h, false, false, M, d, d, xqp, d, w32(h, A + "wg"), d, h.gw[5], d);
+    gemm_rm(h, false, false, Mkv, d, d, xn, d, w32(h, A + "wk"), d, h.gw[3], d);
+    gemm_rm(h, false, false, Mkv, d, d, xn, d, w32(h, A + "wv"), d, h.gw[4], d);
+    k_qkv_prep<<<warp_rows_grid(M), 256, 0, h.stream>>>(h.gw[2], M, L.Rq, H, dk, 0, L.pos_q, h.rope, L.gain_q, h.Qb);
+    k_qkv_prep<<<warp_rows_grid(Mkv), 256, 0, h.stream>>>(h.gw[3], Mkv, L.Rkv, H, dk, 1, L.pos_kv, h.rope, L.gain_k,
+                                                          h.Kb);
+    k_qkv_prep<<<warp_rows_grid(Mkv), 256, 0, h.stream>>>(h.gw[4], Mkv, L.Rkv, H, dk, 2, L.pos_kv, h.rope, nullptr,
+                                                          h.Vb);
+    k_qkv_prep<<<warp_rows_grid(M), 256, 0, h.stream>>>(h.gw[5], M, L.Rq, H, dk, 3, nullptr, nullptr, nullptr, h.Gb);
+    check_launch("generic projections");
+    stage_mark(h, "L" + sl + ".qkvg");
+    launch_attention(h, L, lp, B);  // tcgen05 core; writes the gated output to h.Hg
+    stage_mark(h, "L" + sl + ".attention");
+    const size_t nq = static_cast<size_t>(M) * d;
+    k_bf16_to_f32<<<ew_grid(nq), 256, 0, h.stream>>>(h.Hg, nq, h.gw[3]);
+    gemm_rm(h, false, false, M, d, d, h.gw[3], d, w32(h, A + "wo"), d, h.gw[2], d);
+    k_residual_gather<<<warp_rows_grid(M), 256, 0, h.stream>>>(x, L.query_rows, L.Rq, L.Rkv, h.gw[2], M, d, xo);
+    // SwishGLU FFN on RMSN(x1) + residual
+    float* xf = h.gw[1];
+    k_rmsnorm_rows<float><<<warp_rows_grid(M), 256, 0, h.stream>>>(xo, w32(h, Bk + "ffn_norm"), M, d, nullptr, 1, 1,
+                                                                   xf, nullptr);
+    gemm_rm(h, false, false, M, 2 * m, d, xf, d, w32(h, F + "w_gu"), 2 * m, h.gw[6], 2 * m);
+    k_swiglu_z<<<ew_grid(static_cast<size_t>(M) * m), 256, 0, h.stream>>>(h.gw[6], M, m, h.gw[7]);
+    gemm_rm(h, false, false, M, d, m, h.gw[7], m, w32(h, F + "w_down"), d, xo, d, 1.f);
+    check_launch("generic block tail");
+    stage_mark(h, "L" + sl + ".tail");
+    cur = 1 - cur;
+  }
+  h.gX_final = cur;
+  // ---- final RMSNorm + head on the candidate rows
+  const LayerDev& last = h.layers.back();
+  const int R = last.Rq, BN = B * N;
+  std::vector<int32_t> cmap_h(N);
+  for (int j = 0; j < N; ++j) cmap_h[j] = R - N + j;
+  int32_t*& cmap = h.cand_maps[R];
+  if (!cmap) cmap = h.upload(cmap_h);
+  float* xh = h.gw[9];
+  float* hid = xh + static_cast<size_t>(BN) * d;
+  float* lo = hid + static_cast<size_t>(BN) * h.dh;
+  k_gather_f32<float><<<warp_rows_grid(BN), 256, 0, h.stream>>>(h.gX[cur], cmap, N, R, BN, d, h.gw[0]);
+  k_rmsnorm_rows<float><<<warp_rows_grid(BN), 256, 0, h.stream>>>(h.gw[0], w32(h, "final_norm.gain"), BN, d, nullptr,
+                                                                  1, 1, xh, nullptr);
+  gemm_rm(h, false, false, BN, h.dh, d, xh, d, w32(h, "head.w1"), h.dh, hid, h.dh);
+  k_bias_relu<<<ew_grid(static_cast<size_t>(BN) * h.dh), 256, 0, h.stream>>>(hid, w32(h, "head.b1"), BN, h.dh);
+  gemm_rm(h, false, false, BN, 3, h.dh, hid, h.dh, w32(h, "head.w2"), 3, lo, 3);
+  k_head_out<<<(BN * 3 + 255) / 256, 256, 0, h.stream>>>(lo, w32(h, "head.b2"), BN, h.logits, h.probs);
+  check_launch("generic head");
+  stage_mark(h, "head");
+}
+
 static void upload_batch(Handle& h, const SortBatch* b, bool on_device) {
   const SortConfig& c = h.cfg;
   const int B = b->batch;
@@ -1001,6 +1132,11 @@ static void begin_timing(Handle& h) {
 }
 
 static void forward_device(Handle& h, int B) {
+  if (h.generic) {
+    if (h.training) throw ConfigError("training step: model_dim > 256 is not supported in this build");
+    forward_generic(h, B);
+    return;
+  }
   CK(cudaMemsetAsync(h.err, 0, 4 * sizeof(int32_t), h.stream));
   run_tokenizer(h, B);
   stage_mark(h, "tokenizer");
@@ -1106,7 +1242,8 @@ int sort_create(const SortConfig* cfg, int device, SortHandle* out) {
     h->dk = cfg->model_dim / cfg->heads;
     h->m = cfg->ffn_dim;
     h->dh = cfg->head_hidden > 0 ? cfg->head_hidden : cfg->model_dim;
-    if (h->dh != 32 && h->dh != 64 && h->dh != 128 && h->dh != 256)
+    h->generic = cfg->model_dim > 256;
+    if (!h->generic && h->dh != 32 && h->dh != 64 && h->dh != 128 && h->dh != 256)
       throw ConfigError("unsupported head_hidden (must be 32, 64, 128 or 256)");
     h->L0 = h->plan.L0;
     h->Bmax = cfg->max_batch;
@@ -1201,9 +1338,12 @@ int sort_tokenize(SortHandle p, const SortBatch* batch, float* tokens, int32_t* 
     begin_timing(*h);
     upload_batch(*h, batch, false);
     CK(cudaMemsetAsync(h->err, 0, 4 * sizeof(int32_t), h->stream));
-    run_tokenizer(*h, batch->batch);
     const int B = batch->batch;
     std::vector<__nv_bfloat16> xb(static_cast<size_t>(B) * h->L0 * h->d);
+    if (h->generic) {
+      throw ConfigError("sort_tokenize: model_dim > 256 tokens are only produced inside sort_forward");
+    }
+    run_tokenizer(*h, batch->batch);
     CK(cudaMemcpyAsync(xb.data(), h->X[0], xb.size() * 2, cudaMemcpyDeviceToHost, h->stream));
     if (hist_time && h->cfg.n_hist)
       CK(cudaMemcpyAsync(hist_time, h->hist_time, static_cast<size_t>(B) * h->cfg.n_hist * 4,

@@ -339,3 +339,27 @@ def test_gather_rows_kernel_and_range_check():
     ids[1] = 1000
     with pytest.raises(R.ConfigError):
         R.gather_rows(t.data_ptr(), 1000, 64, ids.data_ptr(), 5, out.data_ptr())
+
+
+# ----------------------------------------------------------------------- SORT-large widths
+def test_large_widths_vs_oracle():
+    """SORT-large widths (d = 1024, 16 heads of 64, m = 2560, W = 256, geometric pruning) on
+    the generic path (library GEMMs + the tcgen05 attention core at head dim 64), with a short
+    history so the fp64 dense oracle stays fast."""
+    from paper_2603_03988_b200.config import large_config
+    cfg = large_config(layers=2, n_hist=200, n_cand=16, n_items=20000)
+    cfg.keep = [cfg.prefix_len, 128]
+    P = synth.make_params(cfg, seed=23)
+    gm = R.SortModel(cfg, P, max_batch=2)
+    om = O.OracleModel(cfg, {k: synth.bf16_round(v) for k, v in P.items()})
+    b = synth.make_batch(cfg, 2, seed=24)
+    probs, logits = gm.forward_logits(b)
+    ref = np.stack([om.forward(b, i)[1] for i in range(2)])
+    assert np.max(np.abs(logits - ref)) < LOGIT_MAX_ABS
+    assert rel_l2(logits, ref) < LOGIT_REL_L2
+    # candidate isolation holds on the generic path too
+    b2 = {k: v.copy() for k, v in b.items()}
+    b2["cand_item"][:, 3] = (b["cand_item"][:, 3] + 11) % cfg.n_items
+    p2 = gm.forward(b2)
+    others = [j for j in range(cfg.n_cand) if j != 3]
+    assert np.array_equal(p2[:, others], probs[:, others])
