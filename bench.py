@@ -293,7 +293,7 @@ def run_embed(args, cfg, rank, world, local, dist):
 def run_large(args, rank, world, local, dist):
     """BASELINE configs[3]: SORT-large (12 layers, d=1024, 16 heads, 4096 history, W=256,
     128 targets, geometric pruning) forward, 8 requests per GPU, requests sharded over the
-    ranks (weak scaling). Generic path: TF32 library GEMMs + the tcgen05 attention core."""
+    ranks (weak scaling). Generic path: bf16 library GEMMs + the tcgen05 attention core."""
     import torch
     from paper_2603_03988_b200 import runtime as R
     from paper_2603_03988_b200.config import large_config
@@ -333,7 +333,7 @@ def run_large(args, rank, world, local, dist):
             "metric": "candidates scored/sec (SORT-large forward)", "value": world * B * cfg.n_cand / (ms / 1e3),
             "unit": "candidates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "tf32 GEMMs / bf16 attention", "data": "synthetic",
+            "dtype": "bf16 (fp32 accumulation and residual stream)", "data": "synthetic",
             "mfu_vs_bf16_peak": fl["total"] * B / (ms / 1e3) / (peaks["bf16_tflops"] * 1e12),
             "algorithmic_tflop_per_step": fl["total"] * B / 1e12,
             "config": {"workload": f"SORT-large: {cfg.layers} layers, d={cfg.model_dim}, {cfg.heads} heads, "

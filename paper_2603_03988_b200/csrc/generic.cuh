@@ -3,7 +3,8 @@
 //
 // The SORT-base kernels keep a whole weight slice resident in shared memory and the whole
 // d-wide row in one TMEM tile; at d = 1024 neither fits. This path runs the projections as
-// plain library GEMMs (cuBLAS TF32, fp32 activations) around row kernels, and the attention
+// plain library GEMMs (cuBLAS, bf16 operands, fp32 accumulation and fp32 residual stream)
+// around row kernels, and the attention
 // core on the same tcgen05 kernel as SORT-base (head dim 64). The row kernels restate the
 // reference operations: tokenizer gather/projection/RMSNorm (tokenizer.cpp:95-238), QKNorm +
 // RoPE + sigmoid gate (attention.cpp:93-127), residuals and SwishGLU,
@@ -15,10 +16,10 @@
 
 namespace sortk {
 
-// One token row of a group -> its fp32 concat row [K] (history: item | action | scene | time;
+// One token row of a group -> its bf16 concat row [K] (history: item | action | scene | time;
 // candidate: item; profile: the field's table row) and its row in the sequence.
 // group 0 = history (e over B*H), 1 = candidates (B*N), 2 = profile (B*P).
-__global__ void k_tok_concat(const TokParams p, int group, int K, float* __restrict__ out,
+__global__ void k_tok_concat(const TokParams p, int group, int K, __nv_bfloat16* __restrict__ out,
                              int32_t* __restrict__ out_row) {
   const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   const int count = group == 0 ? p.B * p.H : (group == 1 ? p.B * p.N : p.B * p.P);
@@ -74,7 +75,7 @@ __global__ void k_tok_concat(const TokParams p, int group, int K, float* __restr
   for (int k = lane; k < K; k += 32) {
     int s = 0, base = 0;
     while (s < 3 && k - base >= len[s]) base += len[s++];
-    out[static_cast<size_t>(w) * K + k] = __bfloat162float(src[s][k - base]);
+    out[static_cast<size_t>(w) * K + k] = src[s][k - base];
   }
   if (lane == 0) out_row[w] = row;
 }
@@ -155,6 +156,11 @@ __global__ void k_residual_gather(const float* __restrict__ x, const int32_t* __
     out[static_cast<size_t>(w) * d + c] = x[src * d + c] + a[static_cast<size_t>(w) * d + c];
 }
 
+__global__ void k_f32_to_bf16(const float* __restrict__ x, size_t n, __nv_bfloat16* __restrict__ y) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    y[i] = __float2bfloat16_rn(x[i]);
+}
 __global__ void k_bf16_to_f32(const __nv_bfloat16* __restrict__ x, size_t n, float* __restrict__ y) {
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x)

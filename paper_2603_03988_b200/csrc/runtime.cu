@@ -76,6 +76,7 @@ struct Handle {
   // ---- training (sort_train_step): fp32 master copies of the block/head parameters,
   // a flat fp32 gradient buffer, saved forward activations per layer, workspace
   std::map<std::string, float*> w32;
+  std::map<std::string, __nv_bfloat16*> w16;  // bf16 copies for the generic path's GEMMs
   std::map<std::string, std::pair<size_t, std::pair<int64_t, int64_t>>> grad_index;  // offset, shape
   float* grads = nullptr;
   size_t grad_count = 0;
@@ -722,6 +723,16 @@ static void gemm_rm(Handle& h, bool ta, bool tb, int M, int N, int K, const floa
   if (st != CUBLAS_STATUS_SUCCESS) throw RuntimeFailure("cublasGemmEx failed: " + std::to_string(static_cast<int>(st)));
 }
 
+// Row-major C[M,N] (fp32, + beta C) = A[M,K] (bf16) . B[K,N] (bf16), fp32 accumulation.
+static void gemm_rm_bf16(Handle& h, int M, int N, int K, const __nv_bfloat16* A, int lda, const __nv_bfloat16* B,
+                         int ldb, float* C, int ldc, float beta = 0.f) {
+  const float alpha = 1.f;
+  const cublasStatus_t st = cublasGemmEx(h.cublas, CUBLAS_OP_N, CUBLAS_OP_N, N, M, K, &alpha, B, CUDA_R_16BF, ldb, A,
+                                         CUDA_R_16BF, lda, &beta, C, CUDA_R_32F, ldc, CUBLAS_COMPUTE_32F,
+                                         CUBLAS_GEMM_DEFAULT);
+  if (st != CUBLAS_STATUS_SUCCESS) throw RuntimeFailure("cublasGemmEx (bf16) failed: " + std::to_string(static_cast<int>(st)));
+}
+
 static float* grad_ptr(Handle& h, const std::string& name) {
   auto it = h.grad_index.find(name);
   if (it == h.grad_index.end()) throw RuntimeFailure("no gradient slot for " + name);
@@ -1007,6 +1018,27 @@ static void ensure_generic_buffers(Handle& h) {
 
 static inline int warp_rows_grid(int rows) { return (rows + 7) / 8; }
 
+static const __nv_bfloat16* w16(Handle& h, const std::string& name) {
+  auto it = h.w16.find(name);
+  if (it != h.w16.end()) return it->second;
+  auto src = h.w32.find(name);
+  if (src == h.w32.end()) throw RuntimeFailure("no parameter " + name);
+  size_t n = 0;
+  if (auto g = h.grad_index.find(name); g != h.grad_index.end())
+    n = static_cast<size_t>(g->second.second.first) * g->second.second.second;
+  else if (name.rfind("tok.w_", 0) == 0)
+    n = static_cast<size_t>(name == "tok.w_hist" ? h.cfg.item_dim + h.cfg.action_dim + h.cfg.scene_dim + h.cfg.time_dim
+                            : name == "tok.w_cand" ? h.cfg.item_dim : h.cfg.profile_dim) * h.d;
+  else if (name.size() > 5 && name.compare(name.size() - 5, 5, ".w_gu") == 0)
+    n = static_cast<size_t>(h.d) * 2 * h.m;
+  else
+    throw RuntimeFailure("no size for parameter " + name);
+  __nv_bfloat16* dst = h.dalloc<__nv_bfloat16>(n);
+  k_f32_to_bf16<<<ew_grid(n), 256, 0, h.stream>>>(src->second, n, dst);
+  check_launch("weight cast");
+  return h.w16[name] = dst;
+}
+
 static void forward_generic(Handle& h, int B) {
   ensure_generic_buffers(h);
   CK(cublasSetStream(h.cublas, h.stream) == CUBLAS_STATUS_SUCCESS ? cudaSuccess : cudaErrorUnknown);
@@ -1021,9 +1053,9 @@ static void forward_generic(Handle& h, int B) {
   const char* gname[3] = {"hist", "cand", "prof"};
   for (int g = 0; g < 3; ++g) {
     if (gcount[g] == 0) continue;
-    k_tok_concat<<<warp_rows_grid(gcount[g]), 256, 0, h.stream>>>(tp, g, gK[g], h.gw[8], h.g_rows);
-    gemm_rm(h, false, false, gcount[g], d, gK[g], h.gw[8], gK[g], w32(h, std::string("tok.w_") + gname[g]), d,
-            h.gw[0], d);
+    __nv_bfloat16* cat = reinterpret_cast<__nv_bfloat16*>(h.gw[8]);
+    k_tok_concat<<<warp_rows_grid(gcount[g]), 256, 0, h.stream>>>(tp, g, gK[g], cat, h.g_rows);
+    gemm_rm_bf16(h, gcount[g], d, gK[g], cat, gK[g], w16(h, std::string("tok.w_") + gname[g]), d, h.gw[0], d);
     k_tok_finish<<<warp_rows_grid(gcount[g]), 256, 0, h.stream>>>(h.gw[0], w32(h, std::string("tok.b_") + gname[g]),
                                                                 w32(h, std::string("tok.g_") + gname[g]), h.g_rows,
                                                                 gcount[g], d, X);
@@ -1043,19 +1075,20 @@ static void forward_generic(Handle& h, int B) {
     const int M = B * L.Rq, Mkv = B * L.Rkv;
     float* x = h.gX[cur];
     float* xo = h.gX[1 - cur];
-    float* xn = h.gw[0];
-    float* xq = h.gw[1];
-    k_rmsnorm_rows<float><<<warp_rows_grid(Mkv), 256, 0, h.stream>>>(x, w32(h, Bk + "attn_norm"), Mkv, d, nullptr, 1,
-                                                                     1, xn, nullptr);
-    const float* xqp = xn;
+    __nv_bfloat16* xn = reinterpret_cast<__nv_bfloat16*>(h.gw[0]);
+    __nv_bfloat16* xq = reinterpret_cast<__nv_bfloat16*>(h.gw[1]);
+    k_rmsnorm_rows<float, __nv_bfloat16><<<warp_rows_grid(Mkv), 256, 0, h.stream>>>(
+        x, w32(h, Bk + "attn_norm"), Mkv, d, nullptr, 1, 1, xn, nullptr);
+    const __nv_bfloat16* xqp = xn;
     if (!lp.q_identity) {
-      k_gather_f32<float><<<warp_rows_grid(M), 256, 0, h.stream>>>(xn, L.query_rows, L.Rq, L.Rkv, M, d, xq);
+      k_gather_f32<__nv_bfloat16, __nv_bfloat16><<<warp_rows_grid(M), 256, 0, h.stream>>>(xn, L.query_rows, L.Rq,
+                                                                                          L.Rkv, M, d, xq);
       xqp = xq;
     }
-    gemm_rm(h, false, false, M, d, d, xqp, d, w32(h, A + "wq"), d, h.gw[2], d);
-    gemm_rm(h, false, false, M, d, d, xqp, d, w32(h, A + "wg"), d, h.gw[5], d);
-    gemm_rm(h, false, false, Mkv, d, d, xn, d, w32(h, A + "wk"), d, h.gw[3], d);
-    gemm_rm(h, false, false, Mkv, d, d, xn, d, w32(h, A + "wv"), d, h.gw[4], d);
+    gemm_rm_bf16(h, M, d, d, xqp, d, w16(h, A + "wq"), d, h.gw[2], d);
+    gemm_rm_bf16(h, M, d, d, xqp, d, w16(h, A + "wg"), d, h.gw[5], d);
+    gemm_rm_bf16(h, Mkv, d, d, xn, d, w16(h, A + "wk"), d, h.gw[3], d);
+    gemm_rm_bf16(h, Mkv, d, d, xn, d, w16(h, A + "wv"), d, h.gw[4], d);
     k_qkv_prep<<<warp_rows_grid(M), 256, 0, h.stream>>>(h.gw[2], M, L.Rq, H, dk, 0, L.pos_q, h.rope, L.gain_q, h.Qb);
     k_qkv_prep<<<warp_rows_grid(Mkv), 256, 0, h.stream>>>(h.gw[3], Mkv, L.Rkv, H, dk, 1, L.pos_kv, h.rope, L.gain_k,
                                                           h.Kb);
@@ -1066,17 +1099,16 @@ static void forward_generic(Handle& h, int B) {
     stage_mark(h, "L" + sl + ".qkvg");
     launch_attention(h, L, lp, B);  // tcgen05 core; writes the gated output to h.Hg
     stage_mark(h, "L" + sl + ".attention");
-    const size_t nq = static_cast<size_t>(M) * d;
-    k_bf16_to_f32<<<ew_grid(nq), 256, 0, h.stream>>>(h.Hg, nq, h.gw[3]);
-    gemm_rm(h, false, false, M, d, d, h.gw[3], d, w32(h, A + "wo"), d, h.gw[2], d);
+    gemm_rm_bf16(h, M, d, d, h.Hg, d, w16(h, A + "wo"), d, h.gw[2], d);
     k_residual_gather<<<warp_rows_grid(M), 256, 0, h.stream>>>(x, L.query_rows, L.Rq, L.Rkv, h.gw[2], M, d, xo);
     // SwishGLU FFN on RMSN(x1) + residual
-    float* xf = h.gw[1];
-    k_rmsnorm_rows<float><<<warp_rows_grid(M), 256, 0, h.stream>>>(xo, w32(h, Bk + "ffn_norm"), M, d, nullptr, 1, 1,
-                                                                   xf, nullptr);
-    gemm_rm(h, false, false, M, 2 * m, d, xf, d, w32(h, F + "w_gu"), 2 * m, h.gw[6], 2 * m);
-    k_swiglu_z<<<ew_grid(static_cast<size_t>(M) * m), 256, 0, h.stream>>>(h.gw[6], M, m, h.gw[7]);
-    gemm_rm(h, false, false, M, d, m, h.gw[7], m, w32(h, F + "w_down"), d, xo, d, 1.f);
+    __nv_bfloat16* xf = reinterpret_cast<__nv_bfloat16*>(h.gw[1]);
+    k_rmsnorm_rows<float, __nv_bfloat16><<<warp_rows_grid(M), 256, 0, h.stream>>>(
+        xo, w32(h, Bk + "ffn_norm"), M, d, nullptr, 1, 1, xf, nullptr);
+    gemm_rm_bf16(h, M, 2 * m, d, xf, d, w16(h, F + "w_gu"), 2 * m, h.gw[6], 2 * m);
+    __nv_bfloat16* z = reinterpret_cast<__nv_bfloat16*>(h.gw[7]);
+    k_swiglu_z<__nv_bfloat16><<<ew_grid(static_cast<size_t>(M) * m), 256, 0, h.stream>>>(h.gw[6], M, m, z);
+    gemm_rm_bf16(h, M, d, m, z, m, w16(h, F + "w_down"), d, xo, d, 1.f);
     check_launch("generic block tail");
     stage_mark(h, "L" + sl + ".tail");
     cur = 1 - cur;

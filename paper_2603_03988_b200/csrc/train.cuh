@@ -23,9 +23,12 @@ __device__ __forceinline__ float warp_sum(float v) {
 
 // y = RMSNorm(x[src_row(r)]; gain) in fp32, inv_rms per row (norm.hpp:17-29). x is bf16 or
 // fp32; rows may be gathered: src row = (r / R) * Rsrc + map[r % R] when map != null.
-template <class T>
+__device__ __forceinline__ void store_as(float* p, float v) { *p = v; }
+__device__ __forceinline__ void store_as(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+
+template <class T, class O = float>
 __global__ void k_rmsnorm_rows(const T* __restrict__ x, const float* __restrict__ gain, int rows, int d,
-                               const int32_t* __restrict__ map, int R, int Rsrc, float* __restrict__ y,
+                               const int32_t* __restrict__ map, int R, int Rsrc, O* __restrict__ y,
                                float* __restrict__ inv_out) {
   const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (w >= rows) return;
@@ -41,20 +44,20 @@ __global__ void k_rmsnorm_rows(const T* __restrict__ x, const float* __restrict_
   const float inv = rsqrtf(ss / static_cast<float>(d) + 1e-6f);
   if (inv_out && lane == 0) inv_out[w] = inv;
   if (y) {
-    float* yr = y + static_cast<size_t>(w) * d;
-    for (int c = lane; c < d; c += 32) yr[c] = static_cast<float>(xr[c]) * inv * (gain ? gain[c] : 1.f);
+    O* yr = y + static_cast<size_t>(w) * d;
+    for (int c = lane; c < d; c += 32) store_as(yr + c, static_cast<float>(xr[c]) * inv * (gain ? gain[c] : 1.f));
   }
 }
 
 // out[r] = x[(r / R) * Rsrc + map[r % R]] as fp32 (row gather; map = null -> identity).
-template <class T>
+template <class T, class O = float>
 __global__ void k_gather_f32(const T* __restrict__ x, const int32_t* __restrict__ map, int R, int Rsrc, int rows, int d,
-                             float* __restrict__ out) {
+                             O* __restrict__ out) {
   const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (w >= rows) return;
   size_t src = w;
   if (map) src = static_cast<size_t>(w / R) * Rsrc + map[w % R];
-  for (int c = lane; c < d; c += 32) out[static_cast<size_t>(w) * d + c] = static_cast<float>(x[src * d + c]);
+  for (int c = lane; c < d; c += 32) store_as(out + static_cast<size_t>(w) * d + c, static_cast<float>(x[src * d + c]));
 }
 
 // rmsnorm_backward (norm.hpp:32-45): dx = (dy*g - <dy*g, xhat>/n * xhat) * inv, dgain +=
@@ -96,13 +99,14 @@ __global__ void __launch_bounds__(256) k_rmsnorm_bwd(const float* __restrict__ d
 
 // SwishGLU pieces. GU = [gp | up] (fp32 [M, 2m]).
 __device__ __forceinline__ float sigmoid_f(float x) { return 1.f / (1.f + __expf(-x)); }
-__global__ void k_swiglu_z(const float* __restrict__ gu, int M, int m, float* __restrict__ z) {
+template <class O = float>
+__global__ void k_swiglu_z(const float* __restrict__ gu, int M, int m, O* __restrict__ z) {
   const size_t n = static_cast<size_t>(M) * m;
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
     const size_t r = i / m, j = i - r * m;
     const float g = gu[r * 2 * m + j], u = gu[r * 2 * m + m + j];
-    z[i] = g * sigmoid_f(g) * u;
+    store_as(z + i, g * sigmoid_f(g) * u);
   }
 }
 // dgu = [dz * u * swish'(g) | dz * swish(g)], swish'(g) = s (1 + g (1 - s))
