@@ -31,7 +31,9 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    cmd = [NVCC, *FLAGS, *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB + ".tmp", "-lcudart", "-lcublas"]
+    extra = os.environ.get("SORT_NVCC_EXTRA", "").split()  # experiments only (e.g. -DSORT_ATTN_POLY_EVERY=2)
+    cmd = [NVCC, *FLAGS, *extra, *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB + ".tmp", "-lcudart",
+           "-lcublas"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)

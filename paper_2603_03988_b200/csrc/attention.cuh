@@ -43,7 +43,11 @@ namespace sortk {
 
 constexpr int kAttnThreads = 320;
 constexpr float kFixedRefMax = 40.f;  // 2^(-2*40*log2 e) ~ 2e-35 > FLT_MIN
-constexpr int kKvStages = 4;         // K/V tile ring depth: loads run ~3 tiles ahead of PV
+constexpr int kKvStages = 4;
+#ifndef SORT_ATTN_POLY_EVERY
+#define SORT_ATTN_POLY_EVERY 3
+#endif
+constexpr int kPolyEvery = SORT_ATTN_POLY_EVERY;  // exp2 offload ratio in fully visible chunks         // K/V tile ring depth: loads run ~3 tiles ahead of PV
 
 template <int DK>
 struct AttnSmem {
@@ -393,7 +397,10 @@ __global__ void __launch_bounds__(kAttnThreads, AttnTmem<DK>::kCtasPerSm)
               for (int i = 0; i < 16; ++i) {
                 const float2 x = ffma2(make_float2(__uint_as_float(rr[2 * i]), __uint_as_float(rr[2 * i + 1])),
                                        sl2v, nref);
-                const float2 p = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+                // every kPolyEvery-th pair on the FMA pipe, the rest on MUFU
+                const float2 p = (kPolyEvery > 0 && i % kPolyEvery == kPolyEvery - 1)
+                                     ? ex2_poly2(x)
+                                     : make_float2(ex2_approx(x.x), ex2_approx(x.y));
                 lsum[i & 1] = fadd2(lsum[i & 1], p);
                 w[i] = pack_bf16x2(p.x, p.y);
               }

@@ -299,6 +299,24 @@ __device__ __forceinline__ float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x for a pair on the FMA pipe (FA4-style MUFU offload): round-to-nearest split x = j + f
+// (|f| <= 1/2) through the 1.5 * 2^23 magic add, 2^f by a degree-3 minimax polynomial
+// (rel. error < 7.5e-5, well below the bf16 rounding of P), exponent added to the bits. x is
+// clamped to [-126, 0] (inputs are <= 0 here).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 t = fadd2(x, make_float2(12582912.f, 12582912.f));  // j in the low mantissa bits
+  const float2 j = fadd2(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = fadd2(x, make_float2(-j.x, -j.y));
+  float2 p = ffma2(make_float2(5.5171616e-2f, 5.5171616e-2f), f, make_float2(2.4261117e-1f, 2.4261117e-1f));
+  p = ffma2(p, f, make_float2(6.9326103e-1f, 6.9326103e-1f));
+  p = ffma2(p, f, make_float2(9.9992806e-1f, 9.9992806e-1f));
+  const int jx = __float_as_int(t.x) - 0x4B400000, jy = __float_as_int(t.y) - 0x4B400000;
+  return make_float2(__int_as_float(__float_as_int(p.x) + (jx << 23)),
+                     __int_as_float(__float_as_int(p.y) + (jy << 23)));
+}
+
 __device__ __forceinline__ float tanh_approx(float x) {
   float y;
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
