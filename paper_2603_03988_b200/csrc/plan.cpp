@@ -189,8 +189,8 @@ void validate_config(const SortConfig& c) {
   need(dk % 2 == 0, "attention: head dim must be even for the rotary transform");
   // B200 kernel geometry
   need(dk == 16 || dk == 32 || dk == 64, "unsupported: head dim must be 16, 32 or 64 in this build");
-  need(c.model_dim % 32 == 0 && (c.model_dim <= 256 || (c.model_dim % 64 == 0 && c.model_dim <= 2048)),
-       "unsupported: model_dim must be a multiple of 32 <= 256, or of 64 <= 2048 (generic path)");
+  need(c.model_dim % 64 == 0 && c.model_dim <= 2048,
+       "unsupported: model_dim must be a multiple of 64 and <= 2048 (> 256: generic path)");
   need(c.item_dim % 8 == 0 && c.action_dim % 8 == 0 && c.scene_dim % 8 == 0 &&
            c.time_dim % 8 == 0 && c.profile_dim % 8 == 0,
        "unsupported: embedding dims must be multiples of 8");

@@ -231,36 +231,50 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_fence_after();
-    // ---- 3. epilogue: bias + RMSNorm(gain) -> bf16 row + sum of squares
+    // ---- 3. epilogue: bias + RMSNorm(gain) -> bf16 row + sum of squares. 64 accumulator
+    // columns per TMEM round trip (two x32 loads, one wait); bias / gain as float4 LDS.
     const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    const uint32_t sb = smem_u32(sBias), sgn = smem_u32(sGain);
     float ss = 0.f;
-    for (int c = 0; c < d; c += 16) {
-      uint32_t r[16];
-      tmem_ld_32x32b_x16(trow + c, r);
+    for (int c = 0; c < d; c += 64) {
+      uint32_t r[64];
+      tmem_ld_32x32b_x32(trow + c, *reinterpret_cast<uint32_t(*)[32]>(r));
+      tmem_ld_32x32b_x32(trow + c + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
       tmem_ld_wait();
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const float v = __uint_as_float(r[i]) + sBias[c + i];
-        ss += v * v;
+      for (int i = 0; i < 64; i += 4) {
+        const float4 bv = lds_f32x4(sb + (c + i) * 4);
+        const float v0 = __uint_as_float(r[i]) + bv.x, v1 = __uint_as_float(r[i + 1]) + bv.y;
+        const float v2 = __uint_as_float(r[i + 2]) + bv.z, v3 = __uint_as_float(r[i + 3]) + bv.w;
+        ss += v0 * v0 + v1 * v1 + v2 * v2 + v3 * v3;
       }
     }
     const float inv = rsqrtf(ss / static_cast<float>(d) + 1e-6f);
     float ss_out = 0.f;
-    for (int c = 0; c < d; c += 16) {
-      uint32_t r[16];
-      tmem_ld_32x32b_x16(trow + c, r);
+    for (int c = 0; c < d; c += 64) {
+      uint32_t r[64];
+      tmem_ld_32x32b_x32(trow + c, *reinterpret_cast<uint32_t(*)[32]>(r));
+      tmem_ld_32x32b_x32(trow + c + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
       tmem_ld_wait();
-      uint32_t packed[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float y0 = (__uint_as_float(r[2 * i]) + sBias[c + 2 * i]) * inv * sGain[c + 2 * i];
-        const float y1 = (__uint_as_float(r[2 * i + 1]) + sBias[c + 2 * i + 1]) * inv * sGain[c + 2 * i + 1];
-        packed[i] = pack_bf16x2(y0, y1);
-        const __nv_bfloat162 q = *reinterpret_cast<__nv_bfloat162*>(&packed[i]);
-        const float q0 = __bfloat162float(q.x), q1 = __bfloat162float(q.y);
-        ss_out += q0 * q0 + q1 * q1;
+      for (int q16 = 0; q16 < 4; ++q16) {
+        uint32_t packed[8];
+#pragma unroll
+        for (int i = 0; i < 16; i += 4) {
+          const int k = q16 * 16 + i;
+          const float4 bv = lds_f32x4(sb + (c + k) * 4), gv = lds_f32x4(sgn + (c + k) * 4);
+          const float y0 = (__uint_as_float(r[k]) + bv.x) * inv * gv.x;
+          const float y1 = (__uint_as_float(r[k + 1]) + bv.y) * inv * gv.y;
+          const float y2 = (__uint_as_float(r[k + 2]) + bv.z) * inv * gv.z;
+          const float y3 = (__uint_as_float(r[k + 3]) + bv.w) * inv * gv.w;
+          packed[i / 2] = pack_bf16x2(y0, y1);
+          packed[i / 2 + 1] = pack_bf16x2(y2, y3);
+          const float2 q0 = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&packed[i / 2]));
+          const float2 q1 = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&packed[i / 2 + 1]));
+          ss_out += q0.x * q0.x + q0.y * q0.y + q1.x * q1.x + q1.y * q1.y;
+        }
+        if (valid) stg256(p.x + static_cast<size_t>(out_row) * d + c + q16 * 16, packed);
       }
-      if (valid) stg256(p.x + static_cast<size_t>(out_row) * d + c, packed);
     }
     if (valid) p.ss[out_row] = make_float4(ss_out, 0.f, 0.f, 0.f);
     tc_fence_before();
