@@ -774,6 +774,75 @@ M attention_backward(const OrModel& mdl, int layer, const M& xn, const std::vect
   return dxn;
 }
 
+// Tokenizer::backward (tokenizer.cpp:286-352) for one request: per group
+// dproj = rmsnorm_backward(dtokens[group rows]) -> dW = concat^T dproj, db = colsum(dproj),
+// d(concat) = dproj W^T scattered into the feature tables; special rows take dtokens raw.
+// The item table is treated as frozen (SPEC.md transfer+freeze; tokenizer.cpp:315-317,
+// 346-352 skip frozen tables), so no item-table gradient is produced.
+void tokenizer_backward(const OrModel& mdl, const OrSample& s, const M& dtok, Grads& G) {
+  const OrModelCfg& c = mdl.cfg;
+  const bool st = c.special_tokens != 0;
+  const int nh = s.n_hist, np = s.n_prof, nc = s.n_cand, d = mdl.d;
+  if (st) {
+    M& gs = grad_of(G, mdl, "tok.special");
+    const int srow[3] = {0, 1 + nh, 2 + nh + np};
+    for (int k = 0; k < 3; ++k)
+      for (int j = 0; j < d; ++j) gs(k, j) += dtok(srow[k], j);
+  }
+  auto group = [&](const M& cat, int row0, const char* w, const char* b, const char* g) -> M {
+    const int n = cat.r;
+    M dy(n, d);
+    for (int i = 0; i < n; ++i) std::memcpy(dy.row(i), dtok.row(row0 + i), sizeof(double) * d);
+    M proj = matmul(cat, mdl.P(w));
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < d; ++j) proj(i, j) += mdl.P(b)(0, j);
+    M dproj = rmsnorm_backward(dy, proj, mdl.P(g).row(0), grad_of(G, mdl, g).row(0));
+    add_into(grad_of(G, mdl, w), matmul_tn(cat, dproj));
+    M& gb = grad_of(G, mdl, b);
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < d; ++j) gb(0, j) += dproj(i, j);
+    return matmul_nt(dproj, mdl.P(w));
+  };
+  const M& it = mdl.P("tok.item_table");
+  if (nh > 0) {
+    M hcat(nh, mdl.hist_width());
+    for (int i = 0; i < nh; ++i) {
+      double* o = hcat.row(i);
+      std::memcpy(o, it.row(s.hist_item[i]), sizeof(double) * c.item_dim);
+      std::memcpy(o + c.item_dim, mdl.P("tok.action_table").row(s.hist_action[i]), sizeof(double) * c.action_dim);
+      std::memcpy(o + c.item_dim + c.action_dim, mdl.P("tok.scene_table").row(s.hist_scene[i]),
+                  sizeof(double) * c.scene_dim);
+      const int tb = time_bucket(s.timestamp - s.hist_ts[i], c.n_time_buckets);
+      std::memcpy(o + c.item_dim + c.action_dim + c.scene_dim, mdl.P("tok.time_table").row(tb),
+                  sizeof(double) * c.time_dim);
+    }
+    M dc = group(hcat, st ? 1 : 0, "tok.w_hist", "tok.b_hist", "tok.g_hist");
+    M& ga = grad_of(G, mdl, "tok.action_table");
+    M& gsn = grad_of(G, mdl, "tok.scene_table");
+    M& gt = grad_of(G, mdl, "tok.time_table");
+    for (int i = 0; i < nh; ++i) {
+      const int tb = time_bucket(s.timestamp - s.hist_ts[i], c.n_time_buckets);
+      for (int j = 0; j < c.action_dim; ++j) ga(s.hist_action[i], j) += dc(i, c.item_dim + j);
+      for (int j = 0; j < c.scene_dim; ++j) gsn(s.hist_scene[i], j) += dc(i, c.item_dim + c.action_dim + j);
+      for (int j = 0; j < c.time_dim; ++j) gt(tb, j) += dc(i, c.item_dim + c.action_dim + c.scene_dim + j);
+    }
+  }
+  if (np > 0) {
+    M pcat(np, c.profile_dim);
+    for (int f = 0; f < np; ++f)
+      std::memcpy(pcat.row(f), mdl.P("tok.profile_table." + std::to_string(f)).row(s.profile[f]),
+                  sizeof(double) * c.profile_dim);
+    M dc = group(pcat, (st ? 2 : 0) + nh, "tok.w_prof", "tok.b_prof", "tok.g_prof");
+    for (int f = 0; f < np; ++f) {
+      M& gp = grad_of(G, mdl, "tok.profile_table." + std::to_string(f));
+      for (int j = 0; j < c.profile_dim; ++j) gp(s.profile[f], j) += dc(f, j);
+    }
+  }
+  M ccat(nc, c.item_dim);
+  for (int j = 0; j < nc; ++j) std::memcpy(ccat.row(j), it.row(s.cand_item[j]), sizeof(double) * c.item_dim);
+  group(ccat, (st ? 3 : 0) + nh + np, "tok.w_cand", "tok.b_cand", "tok.g_cand");
+}
+
 // Backward of model_forward for one request given dL/dlogits [n_cand, 3]; returns dtokens.
 M model_backward(const OrModel& mdl, const OrSample& s, const double* dlogits, Grads& G) {
   Seq q = tokenize(mdl, s);
@@ -879,6 +948,7 @@ M model_backward(const OrModel& mdl, const OrSample& s, const double* dlogits, G
       for (int j = 0; j < d; ++j) dxin(S.qrows[i], j) += dxr(i, j);
     dx = std::move(dxin);
   }
+  tokenizer_backward(mdl, s, dx, G);
   return dx;
 }
 

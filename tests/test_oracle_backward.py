@@ -49,6 +49,28 @@ def test_param_grads_match_finite_differences(setup):
             assert abs(fd - an) <= FD_REL_TOL * max(1.0, abs(fd)) + 1e-9, (n, idx, fd, an)
 
 
+def test_tokenizer_grads_match_finite_differences(setup):
+    """Tokenizer::backward (tokenizer.cpp:286-352): projections, biases, gains, specials and the
+    feature tables (the item table is frozen: no gradient)."""
+    cfg, P, b, W = setup
+    names = [n for n in P if n.startswith("tok.")]
+    g, _ = O.OracleModel(cfg, P).backward(b, 0, W, names)
+    assert g["tok.item_table"] is None
+    rng = np.random.default_rng(4)
+    used = {"tok.action_table": b["hist_action"][0], "tok.scene_table": b["hist_scene"][0]}
+    for n in names:
+        if n == "tok.item_table":
+            continue
+        assert g[n] is not None and g[n].shape == P[n].shape, n
+        for _ in range(2):
+            if n in used:  # probe a row the request actually uses
+                idx = (int(rng.choice(used[n])), int(rng.integers(0, P[n].shape[1])))
+            else:
+                idx = tuple(int(rng.integers(0, s)) for s in P[n].shape)
+            fd = _fd(cfg, P, b, W, n, idx)
+            assert abs(fd - g[n][idx]) <= FD_REL_TOL * max(1.0, abs(fd)) + 1e-9, (n, idx, fd, g[n][idx])
+
+
 def test_dtokens_match_finite_differences(setup):
     """Special rows enter the sequence raw (tokenizer.cpp:171-176), so d loss / d special[k]
     equals dtokens at that special token's row (BOS = row 0, first SEP = row 1 + H)."""
