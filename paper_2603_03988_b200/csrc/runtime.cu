@@ -79,6 +79,9 @@ struct Handle {
   std::map<std::string, __nv_bfloat16*> w16;  // bf16 copies for the generic path's GEMMs
   std::map<std::string, std::pair<size_t, std::pair<int64_t, int64_t>>> grad_index;  // offset, shape
   float* grads = nullptr;
+  float* master = nullptr;                 // fp32 master parameters (grad_index layout)
+  float *adam_m = nullptr, *adam_v = nullptr;
+  int adam_t = 0;
   size_t grad_count = 0;
   bool training = false;  // forward currently saving activations
   struct TrainLayer {
@@ -92,6 +95,7 @@ struct Handle {
   float *tw[16] = {nullptr};  // backward workspace
   float* dtokens = nullptr;
   float* dz_dev = nullptr;                 // dL/dlogits of the current step
+  int32_t* t_rows = nullptr;               // tokenizer backward: token row of each group row
   // generic (d > 256) forward: fp32 residual stream and workspace
   float* gX[2] = {nullptr, nullptr};
   float* gw[10] = {nullptr};
@@ -402,15 +406,19 @@ static void finalize(Handle& h) {
   h.head_b2 = h.upload(need_param(h, "head.b2", 1, 3).v);
   // fp32 copies of the differentiated parameters (training backward), and the flat gradient
   // buffer in the same name order; W_gate | W_up also concatenated as ffn.<l>.w_gu [d, 2m]
+  // Trainable parameters: every tensor except the (frozen) item table, one flat fp32 master
+  // buffer in name order; the gradient buffer and the AdamW moments share its layout.
   size_t goff = 0;
   for (auto& kv : h.host) {
-    if (kv.first.rfind("tok.", 0) == 0) {  // tokenizer projections (generic path), not tables
-      if (kv.first.find("table") == std::string::npos) h.w32[kv.first] = h.upload(kv.second.v);
-      continue;
-    }
-    h.w32[kv.first] = h.upload(kv.second.v);
+    if (kv.first == "tok.item_table") continue;
     h.grad_index[kv.first] = {goff, {kv.second.rows, kv.second.cols}};
     goff += static_cast<size_t>(kv.second.rows) * kv.second.cols;
+  }
+  h.master = h.dalloc<float>(std::max<size_t>(goff, 1));
+  for (auto& kv : h.grad_index) {
+    const HostParam& hp = h.host.at(kv.first);
+    CK(cudaMemcpy(h.master + kv.second.first, hp.v.data(), hp.v.size() * 4, cudaMemcpyHostToDevice));
+    h.w32[kv.first] = h.master + kv.second.first;
   }
   for (int l = 0; l < c.layers; ++l) {
     const std::string f = "ffn." + std::to_string(l) + ".";
@@ -795,6 +803,7 @@ static void ensure_train_buffers(Handle& h, int B) {
   const int d = h.d, m = h.m;
   B = h.Bmax;  // size once for max_batch
   h.grads = h.dalloc<float>(h.grad_count);
+  h.t_rows = h.dalloc<int32_t>(static_cast<size_t>(h.Bmax) * h.L0);
   h.tl.resize(h.cfg.layers);
   size_t mkv_max = 0;
   for (int l = 0; l < h.cfg.layers; ++l) {
@@ -831,6 +840,7 @@ static void ensure_train_buffers(Handle& h, int B) {
   h.train_B = h.Bmax;
 }
 
+static inline int warp_rows_grid(int rows) { return (rows + 7) / 8; }
 static inline int ew_grid(size_t n) { return static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 16)); }
 
 // Backward of one training forward; dz = dL/dlogits [B*N, 3] on the device.
@@ -996,6 +1006,65 @@ static void backward_device(Handle& h, int B, const float* dz) {
     (void)nkv;
   }
   h.dtokens = dX;
+  // ---- Tokenizer::backward (tokenizer.cpp:286-352); the item table is frozen
+  const TokParams tp = tok_params(h, B);
+  const int gcount[3] = {B * c.n_hist, B * N, B * c.n_profile_fields};
+  const int gK[3] = {c.item_dim + c.action_dim + c.scene_dim + c.time_dim, c.item_dim, c.profile_dim};
+  const char* gname[3] = {"hist", "cand", "prof"};
+  __nv_bfloat16* catb = reinterpret_cast<__nv_bfloat16*>(h.tw[13]);
+  float* catf = h.tw[12];
+  float* y = h.tw[2];
+  float* dy = h.tw[3];
+  float* dproj = h.tw[4];
+  float* dcat = h.tw[5];
+  for (int g = 0; g < 3; ++g) {
+    const int n = gcount[g], K = gK[g];
+    if (n == 0) continue;
+    const std::string W = std::string("tok.w_") + gname[g];
+    k_tok_concat<<<warp_rows_grid(n), 256, 0, h.stream>>>(tp, g, K, catb, h.t_rows);
+    k_bf16_to_f32<<<ew_grid(static_cast<size_t>(n) * K), 256, 0, h.stream>>>(catb, static_cast<size_t>(n) * K, catf);
+    gemm_rm(h, false, false, n, d, K, catf, K, w32(h, W), d, y, d);
+    k_bias_add<<<ew_grid(static_cast<size_t>(n) * d), 256, 0, h.stream>>>(y, w32(h, std::string("tok.b_") + gname[g]),
+                                                                         n, d);
+    k_rmsnorm_rows<float><<<warp_rows_grid(n), 256, 0, h.stream>>>(y, nullptr, n, d, nullptr, 1, 1,
+                                                                   static_cast<float*>(nullptr), inv);
+    k_gather_f32<float><<<warp_rows_grid(n), 256, 0, h.stream>>>(dX, h.t_rows, n, 0, n, d, dy);
+    k_rmsnorm_bwd<float><<<(n + 63) / 64, 256, d * 4, h.stream>>>(dy, y, inv, w32(h, std::string("tok.g_") + gname[g]), n,
+                                                                  d, dproj, 0, grad_ptr(h, std::string("tok.g_") + gname[g]));
+    gemm_rm(h, true, false, K, d, n, catf, K, dproj, d, grad_ptr(h, W), d);
+    k_colsum<<<dim3((d + 31) / 32, 64), 32, 0, h.stream>>>(dproj, n, d, grad_ptr(h, std::string("tok.b_") + gname[g]));
+    if (g == 1) continue;  // candidates gather only the frozen item table
+    gemm_rm(h, false, true, n, K, d, dproj, d, w32(h, W), d, dcat, K);
+    TokTableGrads tg{};
+    int tsize = 0;
+    if (g == 0) {
+      tg.action = grad_ptr(h, "tok.action_table");
+      tg.scene = grad_ptr(h, "tok.scene_table");
+      tg.time = grad_ptr(h, "tok.time_table");
+      tsize = c.n_actions * c.action_dim + c.n_scenes * c.scene_dim + c.n_time_buckets * c.time_dim;
+    } else {
+      for (int f = 0; f < c.n_profile_fields; ++f) {
+        tg.prof[f] = grad_ptr(h, "tok.profile_table." + std::to_string(f));
+        tsize += c.profile_vocab[f] * c.profile_dim;
+      }
+    }
+    if (tsize * 4 > 200 * 1024) throw ConfigError("training: feature tables too large for the scatter kernel");
+    int* pvd = nullptr;
+    if (g == 2) {
+      int32_t*& pvd_h = h.cand_maps[-1];  // profile vocab sizes (device), cached
+      if (!pvd_h) pvd_h = h.upload(std::vector<int32_t>(c.profile_vocab, c.profile_vocab + std::max(c.n_profile_fields, 1)));
+      pvd = pvd_h;
+    }
+    if (tsize * 4 > 48 * 1024)
+      CK(cudaFuncSetAttribute(k_tok_table_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, tsize * 4));
+    k_tok_table_scatter<<<std::min(148 * 2, (n + 7) / 8), 256, tsize * 4, h.stream>>>(
+        dcat, g == 0 ? 0 : 1, n, K, h.in_action, h.in_scene, h.hist_time, h.in_prof, c.n_profile_fields, c.item_dim,
+        c.action_dim, c.scene_dim, c.time_dim, c.n_actions, c.n_scenes, c.n_time_buckets, pvd, c.profile_dim, tg);
+  }
+  if (c.special_tokens)
+    k_special_grad<<<(3 * d + 255) / 256, 256, 0, h.stream>>>(dX, B, h.L0, c.n_hist, c.n_profile_fields, d,
+                                                              grad_ptr(h, "tok.special"));
+  check_launch("tokenizer backward");
 }
 
 
@@ -1015,8 +1084,6 @@ static void ensure_generic_buffers(Handle& h) {
   h.gw[9] = h.dalloc<float>(static_cast<size_t>(h.Bmax) * h.cfg.n_cand * (2 * d + h.dh + 4));
   h.g_rows = h.dalloc<int32_t>(rows);
 }
-
-static inline int warp_rows_grid(int rows) { return (rows + 7) / 8; }
 
 static const __nv_bfloat16* w16(Handle& h, const std::string& name) {
   auto it = h.w16.find(name);

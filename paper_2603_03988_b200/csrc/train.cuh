@@ -410,6 +410,89 @@ __global__ void k_colsum(const float* __restrict__ a, int rows, int cols, float*
   atomicAdd(&out[c], s);
 }
 
+// ---------------------------------------------------------------- tokenizer backward
+// (Tokenizer::backward, tokenizer.cpp:286-352): d(concat) rows scattered into the small
+// feature tables. History: [item | action | scene | time] (item frozen, skipped); profile:
+// the field's table. Per-CTA shared-memory accumulation (the tables have a few hundred
+// entries that every row hits), one global atomic per entry per CTA.
+struct TokTableGrads {
+  float* action;  // [n_actions, action_dim]
+  float* scene;   // [n_scenes, scene_dim]
+  float* time;    // [n_tb, time_dim]
+  float* prof[SORT_MAX_PROFILE_FIELDS];  // per field [vocab_f, prof_dim]
+};
+__global__ void __launch_bounds__(256) k_tok_table_scatter(const float* __restrict__ dcat, int group, int n, int K,
+                                                           const int32_t* __restrict__ hist_action,
+                                                           const int32_t* __restrict__ hist_scene,
+                                                           const int32_t* __restrict__ hist_time,
+                                                           const int32_t* __restrict__ profile, int P, int item_dim,
+                                                           int action_dim, int scene_dim, int time_dim, int n_actions,
+                                                           int n_scenes, int n_tb, const int* __restrict__ prof_vocab,
+                                                           int prof_dim, TokTableGrads g) {
+  extern __shared__ float acc[];
+  int total = 0;
+  int prof_off[SORT_MAX_PROFILE_FIELDS] = {0};
+  if (group == 0) {
+    total = n_actions * action_dim + n_scenes * scene_dim + n_tb * time_dim;
+  } else {
+    for (int f = 0; f < P; ++f) {
+      prof_off[f] = total;
+      total += prof_vocab[f] * prof_dim;
+    }
+  }
+  for (int i = threadIdx.x; i < total; i += blockDim.x) acc[i] = 0.f;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int r = blockIdx.x * 8 + warp; r < n; r += gridDim.x * 8) {
+    const float* row = dcat + static_cast<size_t>(r) * K;
+    if (group == 0) {
+      const int a = hist_action[r], sc = hist_scene[r], tb = hist_time[r];
+      for (int j = lane; j < action_dim; j += 32) atomicAdd(&acc[a * action_dim + j], row[item_dim + j]);
+      for (int j = lane; j < scene_dim; j += 32)
+        atomicAdd(&acc[n_actions * action_dim + sc * scene_dim + j], row[item_dim + action_dim + j]);
+      for (int j = lane; j < time_dim; j += 32)
+        atomicAdd(&acc[n_actions * action_dim + n_scenes * scene_dim + tb * time_dim + j],
+                  row[item_dim + action_dim + scene_dim + j]);
+    } else {
+      const int f = r % P, v = profile[r];
+      for (int j = lane; j < prof_dim; j += 32) atomicAdd(&acc[prof_off[f] + v * prof_dim + j], row[j]);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < total; i += blockDim.x) {
+    if (acc[i] == 0.f) continue;
+    if (group == 0) {
+      const int na = n_actions * action_dim, ns = n_scenes * scene_dim;
+      if (i < na) atomicAdd(&g.action[i], acc[i]);
+      else if (i < na + ns) atomicAdd(&g.scene[i - na], acc[i]);
+      else atomicAdd(&g.time[i - na - ns], acc[i]);
+    } else {
+      int f = 0;
+      while (f + 1 < P && i >= prof_off[f + 1]) ++f;
+      atomicAdd(&g.prof[f][i - prof_off[f]], acc[i]);
+    }
+  }
+}
+
+// d(special table) rows: BOS = row 0, SEPs = rows 1 + H and 2 + H + P of every request.
+__global__ void k_special_grad(const float* __restrict__ dX, int B, int L, int H, int P, int d,
+                               float* __restrict__ gspecial) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 3 * d) return;
+  const int k = i / d, c = i - k * d;
+  const int row = k == 0 ? 0 : (k == 1 ? 1 + H : 2 + H + P);
+  float s = 0.f;
+  for (int b = 0; b < B; ++b) s += dX[(static_cast<size_t>(b) * L + row) * d + c];
+  gspecial[i] += s;
+}
+
+__global__ void k_bias_add(float* __restrict__ x, const float* __restrict__ b, int rows, int cols) {
+  const size_t n = static_cast<size_t>(rows) * cols;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    x[i] += b[i % cols];
+}
+
 // Ranking head forward pieces in fp32: hid = relu(pre + b1); and its backward mask.
 __global__ void k_bias_relu(float* __restrict__ x, const float* __restrict__ b, int rows, int cols) {
   const size_t n = static_cast<size_t>(rows) * cols;

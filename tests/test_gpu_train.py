@@ -5,10 +5,11 @@ the fp64 oracle backward (tests/test_oracle_backward.py pins that by finite diff
 The GPU forward is bf16 (the inference kernels), the backward fp32 with TF32 GEMMs; the
 oracle is fed the same bf16-rounded weights. The bar is self-calibrated, because these
 gradients are intrinsically sensitive at bf16 resolution (ReLU / softmax decisions flip):
-the oracle's own gradients move by `noise[n]` (relative L2) when every weight is perturbed
-by a relative N(0, 2^-9) -- half a bf16 ulp. Each GPU gradient must be within
-NOISE_FACTOR * noise[n] (floor GRAD_FLOOR) of the oracle's and point the same way
-(cosine > COS_MIN); dtokens likewise. Measured on B200: GPU error ~= 1x noise."""
+the oracle's own gradients move by `noise[n]` (relative L2, the larger of NOISE_SAMPLES
+draws) when every trainable weight is perturbed by a relative N(0, 2^-8) -- one bf16 ulp,
+the resolution the GPU forward computes its activations at. Each GPU gradient must be
+within NOISE_FACTOR * noise[n] (floor GRAD_FLOOR) of the oracle's and point the same way
+(cosine > COS_MIN); dtokens likewise. Measured on B200: GPU error ~= 0.5-1.5x noise."""
 import numpy as np
 import pytest
 
@@ -20,6 +21,7 @@ from paper_2603_03988_b200.config import base_config, tiny_config
 pytestmark = pytest.mark.gpu
 
 NOISE_FACTOR = 3.0
+NOISE_SAMPLES = 2
 GRAD_FLOOR = 2e-2
 COS_MIN = 0.99
 
@@ -48,24 +50,30 @@ def _check_step(cfg, seed, B):
     b = synth.make_batch(cfg, B, seed=seed + 1)
     dz = np.random.default_rng(seed).normal(size=(B, cfg.n_cand, 3)).astype(np.float32)
     logits = gm.train_step(b, dz)
-    names = [n for n in P if not n.startswith("tok.")]
+    names = [n for n in P if n != "tok.item_table"]  # the item table is frozen
     ref, dtok_ref, zref = _oracle_grads(cfg, Pr, b, dz, names, B)
     assert np.max(np.abs(logits - zref)) < 5e-2
     rng = np.random.default_rng(seed + 2)
-    Pn = {k: (v * (1 + rng.normal(size=v.shape) * 2.0 ** -9) if not k.startswith("tok.") else v)
-          for k, v in Pr.items()}
-    refn, dtokn, _ = _oracle_grads(cfg, Pn, b, dz, names, B)
+    noise = {n: 0.0 for n in names}
+    dtok_noise = 0.0
+    for _ in range(NOISE_SAMPLES):
+        Pn = {k: (v * (1 + rng.normal(size=v.shape) * 2.0 ** -8) if k != "tok.item_table" else v)
+              for k, v in Pr.items()}
+        refn, dtokn, _ = _oracle_grads(cfg, Pn, b, dz, names, B)
+        for n in names:
+            noise[n] = max(noise[n], rel_l2(refn[n], ref[n]))
+        dtok_noise = max(dtok_noise, rel_l2(dtokn, dtok_ref))
     report = {}
     for n in names:
         g = gm.grad(n).astype(np.float64)
-        err, noise = rel_l2(g, ref[n]), rel_l2(refn[n], ref[n])
+        err = rel_l2(g, ref[n])
         cos = float((g * ref[n]).sum() / max(np.linalg.norm(g) * np.linalg.norm(ref[n]), 1e-30))
-        report[n] = (err, noise, cos)
+        report[n] = (err, noise[n], cos)
     bad = {n: r for n, r in report.items()
            if r[0] > max(NOISE_FACTOR * r[1], GRAD_FLOOR) or r[2] < COS_MIN}
     assert not bad, bad
     dtok = gm.dtokens(B)
-    assert rel_l2(dtok, dtok_ref) < max(NOISE_FACTOR * rel_l2(dtokn, dtok_ref), GRAD_FLOOR)
+    assert rel_l2(dtok, dtok_ref) < max(NOISE_FACTOR * dtok_noise, GRAD_FLOOR)
     return report
 
 
