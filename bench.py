@@ -166,8 +166,9 @@ def run_train(args, cfg, rank, world, local, dist):
     """BASELINE configs[2]: SORT-base training step (forward + backward of the scoring path,
     sort_train_step) with the global batch sharded over the ranks and the flat fp32 gradient
     all-reduced over NCCL (torch.distributed) every step. Loss: mean BCE of the three heads
-    against synthetic labels (dL/dlogits computed on the host from the step's logits of the
-    previous step's shape -- the labels are fixed, so dz = (sigmoid(z) - y) / n)."""
+    against synthetic labels;
+    ranking loss and dL/dlogits computed on the device, AdamW step on the
+    fp32 masters and the bf16 inference weights rebuilt on the device every step."""
     import torch
     from paper_2603_03988_b200 import runtime as R
     from paper_2603_03988_b200.sharding import allreduce_grads, shard_range
@@ -180,18 +181,18 @@ def run_train(args, cfg, rank, world, local, dist):
     full = synth.make_batch(cfg, args.requests, seed=100)
     batch = {k: np.ascontiguousarray(v[b0:b1]) for k, v in full.items()}
     labels = (np.random.default_rng(7).random((args.requests, cfg.n_cand, 3)) < 0.2).astype(np.float32)[b0:b1]
-    n_total = args.requests * cfg.n_cand * 3
     gbuf = torch.zeros(model.grad_layout()[3], dtype=torch.float32, device=dev)
-    z = np.zeros((B, cfg.n_cand, 3), np.float32)
+    # per-rank mean BCE scaled by 1/world: the all-reduced sum is the global-batch mean
+    w_obj = np.array([1.0, 0.5, 0.5], np.float32) / world
+    losses = []
 
     def step():
-        nonlocal z
-        dz = (1.0 / (1.0 + np.exp(-z)) - labels) / n_total
-        z = model.train_step(batch, dz.astype(np.float32))
+        losses.append(model.train_step_bce(batch, labels, w_obj))  # fwd + loss + bwd on device
         if dist:
             model.grads_to_device(gbuf.data_ptr())
             allreduce_grads(gbuf, world)
             model.grads_to_device(gbuf.data_ptr(), to_handle=True)
+        model.adamw_step(lr=2e-4)  # PAPER.md:4.1.3 base lr, beta (0.9, 0.99), wd 0.01
         torch.cuda.synchronize(dev)
 
     for _ in range(args.warmup):
@@ -208,12 +209,13 @@ def run_train(args, cfg, rank, world, local, dist):
     ms = float(t[0])
     if rank == 0:
         print(json.dumps({
-            "metric": "requests trained/sec (SORT-base forward+backward, data parallel)",
+            "metric": "requests trained/sec (SORT-base forward+backward+AdamW, data parallel)",
             "value": args.requests / (ms / 1e3), "unit": "requests/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16/fp32",
             "data": "synthetic",
-            "config": {"workload": workload_desc(cfg) + " -- training step, BCE loss on 3 heads",
+            "loss_first_last": [losses[0], losses[-1]],
+            "config": {"workload": workload_desc(cfg) + " -- training step, weighted BCE on 3 heads, AdamW",
                        "global_batch": args.requests, "requests_per_gpu": B,
                        "parallelism": f"dp{world} (request shards, NCCL all-reduce of "
                                       f"{model.grad_layout()[3]} fp32 gradients per step)"},

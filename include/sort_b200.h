@@ -175,6 +175,17 @@ int sort_stage_times(SortHandle h, float* ms, int32_t cap, int32_t* n, char* nam
  * Replaces the reference's per-request AttentionLayer::backward / rmsnorm_backward calls
  * (attention.hpp:62-63, norm.hpp:32) accumulated into a GradBuffer (params.hpp:42-70). */
 int sort_train_step(SortHandle h, const SortBatch* batch, const float* dlogits, float* logits);
+/* Training step with the ranking loss on the device: L = sum_obj w_obj *
+ * mean BCE over candidates (labels [batch, n_cand, 3] host; obj_weights NULL = (1, .5, .5),
+ * SPEC.md:416); dL/dlogits never leaves the GPU. *loss receives L. */
+int sort_train_step_bce(SortHandle h, const SortBatch* batch, const float* labels,
+                        const float* obj_weights, float* loss);
+/* adamw_step over every trainable parameter (the item table is frozen), then
+ * the bf16 inference weights are rebuilt from the fp32 masters on the device. Status 2 names
+ * the parameter on a non-finite gradient. */
+int sort_adamw_step(SortHandle h, float lr, float beta1, float beta2, float eps, float weight_decay);
+/* Current fp32 master value of a trainable parameter (host copy, reference shape). */
+int sort_get_param(SortHandle h, const char* name, float* out);
 /* Offset / shape of one parameter's gradient in the flat buffer, and its total length. */
 int sort_grad_info(SortHandle h, const char* name, int64_t* offset, int64_t* rows, int64_t* cols,
                    int64_t* total);

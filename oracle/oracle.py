@@ -321,3 +321,26 @@ class OracleModel:
         finally:
             lib().oracle_grads_destroy(g)
         return out, dtok
+
+
+# ------------------------------------------------------------------ training references (numpy)
+def bce_loss(logits: np.ndarray, labels: np.ndarray, weights=(1.0, 0.5, 0.5), eps: float = 1e-7):
+    """total_loss (SPEC.md:381-389): sum_obj w_obj * mean BCE over candidates, eps-clamped logs;
+    returns (loss, dL/dlogits)."""
+    z = np.asarray(logits, np.float64).reshape(-1, 3)
+    y = np.asarray(labels, np.float64).reshape(-1, 3)
+    w = np.asarray(weights, np.float64)
+    p = 1.0 / (1.0 + np.exp(-z))
+    pc = np.clip(p, eps, 1 - eps)
+    n = z.shape[0]
+    loss = float((w * -(y * np.log(pc) + (1 - y) * np.log(1 - pc))).sum() / n)
+    return loss, (w * (p - y) / n).reshape(np.shape(logits))
+
+
+def adamw(p, g, m, v, t, lr, b1=0.9, b2=0.99, eps=1e-8, wd=0.01):
+    """adamw_step: bias-corrected moments, decoupled weight decay. Returns
+    (p', m', v')."""
+    m = b1 * m + (1 - b1) * g
+    v = b2 * v + (1 - b2) * g * g
+    mh, vh = m / (1 - b1 ** t), v / (1 - b2 ** t)
+    return p - lr * wd * p - lr * mh / (np.sqrt(vh) + eps), m, v

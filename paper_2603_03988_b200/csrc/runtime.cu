@@ -433,6 +433,22 @@ static void finalize(Handle& h) {
     h.w32[f + "w_gu"] = h.upload(gu);
   }
   h.grad_count = goff;
+  // fp32 parameters the inference kernels read directly now live in the master buffer, so
+  // an optimizer step updates them in place
+  h.head_gain = h.w32["final_norm.gain"];
+  h.head_w1 = h.w32["head.w1"];
+  h.head_b1 = h.w32["head.b1"];
+  h.head_w2 = h.w32["head.w2"];
+  h.head_b2 = h.w32["head.b2"];
+  const char* gnames[3] = {"hist", "cand", "prof"};
+  for (int g = 0; g < 3; ++g) {
+    h.tok_b[g] = h.w32[std::string("tok.b_") + gnames[g]];
+    h.tok_g[g] = h.w32[std::string("tok.g_") + gnames[g]];
+  }
+  for (int l = 0; l < c.layers; ++l) {
+    h.layers[l].gain_q = h.w32["attn." + std::to_string(l) + ".qk_gain_q"];
+    h.layers[l].gain_k = h.w32["attn." + std::to_string(l) + ".qk_gain_k"];
+  }
   h.host.clear();  // device copies are authoritative from here on
   h.finalized = true;
 }
@@ -1202,6 +1218,60 @@ static void forward_generic(Handle& h, int B) {
   stage_mark(h, "head");
 }
 
+// Rebuild the bf16 inference weights (and the derived fp32 W_gate|W_up) from the masters,
+// and the per-layer QKNorm logit bounds from the updated gains.
+static void repack_weights(Handle& h) {
+  const SortConfig& c = h.cfg;
+  const int d = h.d, m = h.m, H = h.H, dk = h.dk;
+  auto grid = [](size_t n) { return static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 32)); };
+  auto cast = [&](const std::string& name, __nv_bfloat16* dst, size_t n) {
+    k_cast_bf16<<<grid(n), 256, 0, h.stream>>>(h.w32.at(name), n, dst);
+  };
+  cast("tok.action_table", h.action, static_cast<size_t>(c.n_actions) * c.action_dim);
+  cast("tok.scene_table", h.scene, static_cast<size_t>(c.n_scenes) * c.scene_dim);
+  cast("tok.time_table", h.time, static_cast<size_t>(c.n_time_buckets) * c.time_dim);
+  for (int f = 0; f < c.n_profile_fields; ++f)
+    cast("tok.profile_table." + std::to_string(f), h.prof + static_cast<size_t>(h.prof_off[f]) * c.profile_dim,
+         static_cast<size_t>(c.profile_vocab[f]) * c.profile_dim);
+  cast("tok.special", h.special, static_cast<size_t>(3) * d);
+  const int gk[3] = {c.item_dim + c.action_dim + c.scene_dim + c.time_dim, c.item_dim, c.profile_dim};
+  const char* gw[3] = {"tok.w_hist", "tok.w_cand", "tok.w_prof"};
+  for (int g = 0; g < 3; ++g)
+    if (h.tok_wt[g])
+      k_repack_t<<<grid(static_cast<size_t>(d) * 64), 256, 0, h.stream>>>(h.w32.at(gw[g]), nullptr, gk[g], d, 64,
+                                                                       h.tok_wt[g]);
+  for (int l = 0; l < c.layers; ++l) {
+    LayerDev& L = h.layers[l];
+    const std::string a = "attn." + std::to_string(l) + ".", f = "ffn." + std::to_string(l) + ".",
+                      bk = "block." + std::to_string(l) + ".";
+    QkvgSrc src{{h.w32.at(a + "wq"), h.w32.at(a + "wk"), h.w32.at(a + "wv"), h.w32.at(a + "wg")}};
+    const float* ga = h.w32.at(bk + "attn_norm");
+    k_repack_qkvg<<<grid(static_cast<size_t>(4) * d * d), 256, 0, h.stream>>>(
+        src, ga, make_int4(kSecQ, kSecV, kSecK, kSecG), 4, H, dk, d, L.w_all);
+    k_repack_qkvg<<<grid(static_cast<size_t>(2) * d * d), 256, 0, h.stream>>>(src, ga, make_int4(kSecK, kSecV, 0, 0),
+                                                                             2, H, dk, d, L.w_kv);
+    k_repack_qkvg<<<grid(static_cast<size_t>(2) * d * d), 256, 0, h.stream>>>(src, ga, make_int4(kSecQ, kSecG, 0, 0),
+                                                                             2, H, dk, d, L.w_qg);
+    k_repack_t<<<grid(static_cast<size_t>(d) * d), 256, 0, h.stream>>>(h.w32.at(a + "wo"), nullptr, d, d, d, L.w_o);
+    k_repack_up<<<grid(static_cast<size_t>(2) * m * d), 256, 0, h.stream>>>(h.w32.at(f + "w_gate"), h.w32.at(f + "w_up"),
+                                                                         h.w32.at(bk + "ffn_norm"), d, m, L.w_up);
+    k_repack_t<<<grid(static_cast<size_t>(d) * m), 256, 0, h.stream>>>(h.w32.at(f + "w_down"), nullptr, m, d, m,
+                                                                    L.w_down);
+    k_concat_gu<<<grid(static_cast<size_t>(d) * 2 * m), 256, 0, h.stream>>>(h.w32.at(f + "w_gate"), h.w32.at(f + "w_up"),
+                                                                          d, m, h.w32.at(f + "w_gu"));
+    std::vector<float> gq(static_cast<size_t>(H) * dk), gkv(static_cast<size_t>(H) * dk);
+    CK(cudaMemcpyAsync(gq.data(), L.gain_q, gq.size() * 4, cudaMemcpyDeviceToHost, h.stream));
+    CK(cudaMemcpyAsync(gkv.data(), L.gain_k, gkv.size() * 4, cudaMemcpyDeviceToHost, h.stream));
+    CK(cudaStreamSynchronize(h.stream));
+    float mq = 0.f, mk = 0.f;
+    for (float v : gq) mq = std::max(mq, std::fabs(v));
+    for (float v : gkv) mk = std::max(mk, std::fabs(v));
+    L.logit_bound = 1.02f * std::sqrt(static_cast<float>(dk)) * mq * mk + 1e-3f;
+  }
+  check_launch("weight repack");
+  h.w16.clear();  // generic-path bf16 copies are rebuilt on next use
+}
+
 static void upload_batch(Handle& h, const SortBatch* b, bool on_device) {
   const SortConfig& c = h.cfg;
   const int B = b->batch;
@@ -1637,6 +1707,92 @@ int sort_train_step(SortHandle p, const SortBatch* batch, const float* dlogits, 
     backward_device(*h, B, dzb);
     if (logits) CK(cudaMemcpyAsync(logits, h->logits, nz * 4, cudaMemcpyDeviceToHost, h->stream));
     collect_status(*h);
+  });
+}
+
+int sort_train_step_bce(SortHandle p, const SortBatch* batch, const float* labels, const float* obj_weights,
+                        float* loss) {
+  return api([&] {
+    Handle* h = ready(p);
+    if (!batch || !labels) throw ConfigError("null argument");
+    if (h->generic) throw ConfigError("training step: model_dim > 256 is not supported in this build");
+    const int B = batch->batch;
+    begin_timing(*h);
+    upload_batch(*h, batch, false);
+    ensure_train_buffers(*h, B);
+    h->training = true;
+    try {
+      forward_device(*h, B);
+    } catch (...) {
+      h->training = false;
+      throw;
+    }
+    h->training = false;
+    const int n = B * h->cfg.n_cand;
+    float*& dzb = h->dz_dev;
+    if (!dzb) dzb = h->dalloc<float>(static_cast<size_t>(h->Bmax) * h->cfg.n_cand * 3 + 1);
+    float* lab = h->tw[15];  // scratch until the attention backward
+    CK(cudaMemcpyAsync(lab, labels, static_cast<size_t>(n) * 3 * 4, cudaMemcpyHostToDevice, h->stream));
+    const float w0 = obj_weights ? obj_weights[0] : 1.f, w1 = obj_weights ? obj_weights[1] : 0.5f,
+                w2 = obj_weights ? obj_weights[2] : 0.5f;  // SPEC.md:416 defaults
+    float* dloss = dzb + static_cast<size_t>(h->Bmax) * h->cfg.n_cand * 3;
+    k_bce<<<1, 256, 0, h->stream>>>(h->logits, lab, n, w0, w1, w2, dzb, dloss);
+    check_launch("bce");
+    float hl = 0.f;
+    CK(cudaMemcpyAsync(&hl, dloss, 4, cudaMemcpyDeviceToHost, h->stream));
+    CK(cublasSetStream(h->cublas, h->stream) == CUBLAS_STATUS_SUCCESS ? cudaSuccess : cudaErrorUnknown);
+    backward_device(*h, B, dzb);
+    collect_status(*h);
+    if (loss) *loss = hl;
+  });
+}
+
+int sort_adamw_step(SortHandle p, float lr, float beta1, float beta2, float eps, float weight_decay) {
+  return api([&] {
+    Handle* h = ready(p);
+    if (!h->grads) throw ConfigError("no gradients yet (call sort_train_step)");
+    if (h->generic) throw ConfigError("training step: model_dim > 256 is not supported in this build");
+    if (!h->adam_m) {
+      h->adam_m = h->dalloc<float>(h->grad_count);
+      h->adam_v = h->dalloc<float>(h->grad_count);
+      CK(cudaMemsetAsync(h->adam_m, 0, h->grad_count * 4, h->stream));
+      CK(cudaMemsetAsync(h->adam_v, 0, h->grad_count * 4, h->stream));
+    }
+    ++h->adam_t;
+    const float bc1 = 1.f - std::pow(beta1, static_cast<float>(h->adam_t));
+    const float bc2 = 1.f - std::pow(beta2, static_cast<float>(h->adam_t));
+    unsigned long long* bad = reinterpret_cast<unsigned long long*>(h->dz_dev ? h->tw[14] : nullptr);
+    if (!bad) throw ConfigError("no gradients yet (call sort_train_step)");
+    const unsigned long long none = ~0ull;
+    CK(cudaMemcpyAsync(bad, &none, 8, cudaMemcpyHostToDevice, h->stream));
+    k_adamw<<<static_cast<int>(std::min<size_t>((h->grad_count + 255) / 256, 148 * 32)), 256, 0, h->stream>>>(
+        h->master, h->grads, h->adam_m, h->adam_v, h->grad_count, lr, beta1, beta2, eps, weight_decay, bc1, bc2, bad);
+    check_launch("adamw");
+    unsigned long long hb = 0;
+    CK(cudaMemcpyAsync(&hb, bad, 8, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (hb != none) {
+      const size_t idx = static_cast<size_t>(hb - 1);
+      std::string name = "?";
+      for (auto& kv : h->grad_index)
+        if (idx >= kv.second.first &&
+            idx < kv.second.first + static_cast<size_t>(kv.second.second.first) * kv.second.second.second)
+          name = kv.first;
+      throw RuntimeFailure("adamw_step: non-finite gradient in parameter " + name);
+    }
+    repack_weights(*h);
+  });
+}
+
+int sort_get_param(SortHandle p, const char* name, float* out) {
+  return api([&] {
+    Handle* h = ready(p);
+    if (!name || !out) throw ConfigError("null argument");
+    auto it = h->grad_index.find(name);
+    if (it == h->grad_index.end()) throw ConfigError(std::string("no trainable parameter ") + name);
+    const size_t n = static_cast<size_t>(it->second.second.first) * it->second.second.second;
+    CK(cudaMemcpyAsync(out, h->master + it->second.first, n * 4, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
   });
 }
 

@@ -493,6 +493,111 @@ __global__ void k_bias_add(float* __restrict__ x, const float* __restrict__ b, i
     x[i] += b[i % cols];
 }
 
+// ---------------------------------------------------------------- optimizer step
+// adamw_step: bias-corrected moments, decoupled weight decay, over the
+// flat master buffer (every trainable tensor; the frozen item table is not in it).
+// Non-finite gradients set *bad to (index + 1) of the first one seen (host names it).
+__global__ void k_adamw(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
+                        float* __restrict__ v, size_t n, float lr, float b1, float b2, float eps, float wd,
+                        float bc1, float bc2, unsigned long long* bad) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const float gi = g[i];
+    if (!isfinite(gi)) {
+      atomicMin(bad, static_cast<unsigned long long>(i) + 1ull);
+      continue;
+    }
+    const float mi = b1 * m[i] + (1.f - b1) * gi;
+    const float vi = b2 * v[i] + (1.f - b2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    const float mh = mi / bc1, vh = vi / bc2;
+    p[i] = p[i] - lr * wd * p[i] - lr * (mh / (sqrtf(vh) + eps));
+  }
+}
+
+// Ranking loss: L = sum_obj w_obj * mean over candidates of BCE(p, y) with
+// eps-clamped logs; dL/dz = w_obj (p - y) / n. One block, fixed-order reduction.
+__global__ void k_bce(const float* __restrict__ logits, const float* __restrict__ labels, int n,
+                      float w0, float w1, float w2, float* __restrict__ dz, float* __restrict__ loss) {
+  __shared__ float red[256];
+  float acc = 0.f;
+  const float w[3] = {w0, w1, w2};
+  for (int i = threadIdx.x; i < n * 3; i += blockDim.x) {
+    const int o = i % 3;
+    const float p = sigmoidf_stable(logits[i]), y = labels[i];
+    const float pc = fminf(fmaxf(p, 1e-7f), 1.f - 1e-7f);
+    acc += w[o] * -(y * logf(pc) + (1.f - y) * logf(1.f - pc));
+    dz[i] = w[o] * (p - y) / static_cast<float>(n);
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *loss = red[0] / static_cast<float>(n);
+}
+
+// ---------------------------------------------------------------- weight repacking
+// After an optimizer step the inference kernels' bf16 weights are rebuilt from the fp32
+// masters with the transforms finalize() applies on the host: W^T (K-major), pre-norm gain
+// folded into the input rows, QKVG rows interleaved head by head in `order`, SwishGLU up rows
+// interleaved in 32-column [gate | up] blocks.
+struct QkvgSrc {
+  const float* w[4];  // kSecQ, kSecK, kSecV, kSecG  ([d, d], [in, out])
+};
+__global__ void k_repack_qkvg(QkvgSrc src, const float* __restrict__ gain, int4 order, int n_sec, int H, int dk,
+                              int d, __nv_bfloat16* __restrict__ out) {
+  const size_t n = static_cast<size_t>(n_sec) * d * d;
+  const int ord[4] = {order.x, order.y, order.z, order.w};
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(i % d);
+    const int row = static_cast<int>(i / d);
+    const int hd = row / (n_sec * dk), rem = row - hd * n_sec * dk;
+    const int sec = ord[rem / dk], j = rem % dk;
+    out[i] = __float2bfloat16_rn(src.w[sec][static_cast<size_t>(k) * d + hd * dk + j] * gain[k]);
+  }
+}
+// out[n, k] = bf16(W[k, n] * (gain ? gain[k] : 1)) for W [K, N]; out row pitch Kpad (zeros past K).
+__global__ void k_repack_t(const float* __restrict__ W, const float* __restrict__ gain, int K, int N, int Kpad,
+                           __nv_bfloat16* __restrict__ out) {
+  const size_t n = static_cast<size_t>(N) * Kpad;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(i % Kpad), c = static_cast<int>(i / Kpad);
+    out[i] = k < K ? __float2bfloat16_rn(W[static_cast<size_t>(k) * N + c] * (gain ? gain[k] : 1.f))
+                   : __float2bfloat16_rn(0.f);
+  }
+}
+__global__ void k_repack_up(const float* __restrict__ wg, const float* __restrict__ wu, const float* __restrict__ gain,
+                            int d, int m, __nv_bfloat16* __restrict__ out) {
+  const size_t n = static_cast<size_t>(2) * m * d;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(i % d), row = static_cast<int>(i / d);
+    const int j = row / 64, r = row % 64;
+    const float* src = r < 32 ? wg : wu;
+    out[i] = __float2bfloat16_rn(src[static_cast<size_t>(k) * m + 32 * j + (r & 31)] * gain[k]);
+  }
+}
+__global__ void k_concat_gu(const float* __restrict__ wg, const float* __restrict__ wu, int d, int m,
+                            float* __restrict__ out) {
+  const size_t n = static_cast<size_t>(d) * 2 * m;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t r = i / (2 * m);
+    const int c = static_cast<int>(i % (2 * m));
+    out[i] = c < m ? wg[r * m + c] : wu[r * m + c - m];
+  }
+}
+__global__ void k_cast_bf16(const float* __restrict__ x, size_t n, __nv_bfloat16* __restrict__ y) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    y[i] = __float2bfloat16_rn(x[i]);
+}
+
 // Ranking head forward pieces in fp32: hid = relu(pre + b1); and its backward mask.
 __global__ void k_bias_relu(float* __restrict__ x, const float* __restrict__ b, int rows, int cols) {
   const size_t n = static_cast<size_t>(rows) * cols;

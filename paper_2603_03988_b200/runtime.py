@@ -56,7 +56,8 @@ EXPORTS = [
     "sort_time_bucket", "sort_geometric_schedule", "sort_retained_rows", "sort_mask_intervals",
     "sort_kernel_count", "sort_enable_stage_timing", "sort_stage_times", "sort_set_option",
     "sort_train_step", "sort_grad_info", "sort_grads_copy", "sort_dtokens",
-    "sort_set_item_table", "sort_gather_rows",
+    "sort_set_item_table", "sort_gather_rows", "sort_train_step_bce", "sort_adamw_step",
+    "sort_get_param",
 ]
 
 _lib = None
@@ -97,6 +98,9 @@ def lib():
         L.sort_grads_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int]
         L.sort_dtokens.argtypes = [C.c_void_p, C.c_int32, f32p]
         L.sort_set_item_table.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
+        L.sort_train_step_bce.argtypes = [C.c_void_p, C.c_void_p, f32p, f32p, f32p]
+        L.sort_adamw_step.argtypes = [C.c_void_p, C.c_float, C.c_float, C.c_float, C.c_float, C.c_float]
+        L.sort_get_param.argtypes = [C.c_void_p, C.c_char_p, f32p]
         L.sort_gather_rows.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int64,
                                        C.c_void_p, C.c_void_p]
         L.sort_stage_times.argtypes = [C.c_void_p, f32p, C.c_int32, i32p, C.c_char_p, C.c_int32]
@@ -271,6 +275,30 @@ class SortModel:
         logits = np.zeros((B, self.cfg.n_cand, 3), np.float32)
         _check(lib().sort_train_step(self.h, C.byref(hold.c), _p(dz, f32p), _p(logits, f32p)))
         return logits
+
+    def train_step_bce(self, batch: Dict[str, np.ndarray], labels: np.ndarray,
+                       obj_weights=(1.0, 0.5, 0.5)) -> float:
+        """Forward + ranking loss (weighted mean BCE of click / cart /
+        purchase, labels [B, n_cand, 3]) + backward, all on the device; returns the loss."""
+        hold = _BatchHold(batch)
+        lab = np.ascontiguousarray(labels, np.float32)
+        w = np.ascontiguousarray(obj_weights, np.float32)
+        loss = C.c_float(0.0)
+        _check(lib().sort_train_step_bce(self.h, C.byref(hold.c), _p(lab, f32p), _p(w, f32p),
+                                         C.byref(loss)))
+        return float(loss.value)
+
+    def adamw_step(self, lr: float, beta1: float = 0.9, beta2: float = 0.99, eps: float = 1e-8,
+                   weight_decay: float = 0.01):
+        """adamw_step (paper defaults beta = (0.9, 0.99), wd = 0.01) on the fp32
+        masters, then the bf16 inference weights are rebuilt on the device."""
+        _check(lib().sort_adamw_step(self.h, lr, beta1, beta2, eps, weight_decay))
+
+    def get_param(self, name: str) -> np.ndarray:
+        _, r, c, _ = self.grad_layout(name)
+        out = np.zeros((r, c), np.float32)
+        _check(lib().sort_get_param(self.h, name.encode(), _p(out, f32p)))
+        return out
 
     def grad_layout(self, name: Optional[str] = None):
         off, r, c, tot = (C.c_int64(0) for _ in range(4))

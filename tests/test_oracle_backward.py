@@ -80,3 +80,25 @@ def test_dtokens_match_finite_differences(setup):
         for j in (0, 7, cfg.model_dim - 1):
             fd = _fd(cfg, P, b, W, "tok.special", (k, j))
             assert abs(fd - dt[row, j]) <= FD_REL_TOL * max(1.0, abs(fd)) + 1e-9, (k, j)
+
+
+# ----------------------------------------------------------------------- loss / optimizer KATs
+def test_bce_loss_spec_examples():
+    """SPEC.md:386-389."""
+    z = np.zeros((4, 3))
+    loss, _ = O.bce_loss(z, np.ones((4, 3)), weights=(1.0, 0.0, 0.0))
+    assert abs(loss - np.log(2)) < 1e-12                       # p = 0.5 -> ln 2
+    z = np.full((1, 3), np.log(0.9 / 0.1))                     # p = 0.9
+    loss, dz = O.bce_loss(z, np.ones((1, 3)), weights=(1.0, 0.0, 0.0))
+    assert abs(loss - 0.10536051565782628) < 1e-12             # -ln 0.9
+    assert abs(dz[0, 0] - (0.9 - 1.0)) < 1e-12 and dz[0, 1] == 0.0
+
+
+def test_adamw_spec_examples():
+    """SPEC.md:453-456."""
+    p, m, v = O.adamw(np.array([1.0]), np.array([0.0]), 0.0, 0.0, 1, lr=0.1, wd=0.0)
+    assert p[0] == 1.0                                          # zero grad, zero wd
+    p, _, _ = O.adamw(np.array([1.0]), np.array([1.0]), 0.0, 0.0, 1, lr=0.1, wd=0.0)
+    assert abs(p[0] - (1 - 0.1 / (1 + 1e-8))) < 1e-12          # ~0.9
+    p, _, _ = O.adamw(np.array([2.0]), np.array([0.0]), 0.0, 0.0, 1, lr=0.1, wd=0.01)
+    assert abs(p[0] - 2.0 * (1 - 0.001)) < 1e-12               # decay only
