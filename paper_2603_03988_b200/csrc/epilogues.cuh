@@ -30,16 +30,20 @@ __device__ __forceinline__ float side_row_ss(const uint8_t* side, int lrow) {
   const float4 p = lds_f32x4(smem_u32(side + lrow * 16));
   return (p.x + p.y) + (p.z + p.w);
 }
-// 16-byte chunk j of tile row `lrow` of a TMA-swizzled fp32 side table with `floats`
-// floats per row (boxes of <= 32 floats, swizzle span = box row bytes).
-template <int floats>
-__device__ __forceinline__ float4 side_row_chunk(const uint8_t* base, int lrow, int j) {
-  constexpr int bf = floats < 32 ? floats : 32;  // floats per box row
-  constexpr int S = bf * 4;                      // box row bytes == swizzle span
-  constexpr int per = S / 16;                    // 16-byte chunks per box row
+// 16-byte chunk j (8 fp16) of tile row `lrow` of a TMA-swizzled fp16 side table with
+// `halfs` values per row (boxes of <= 64 fp16, swizzle span = box row bytes).
+template <int halfs>
+__device__ __forceinline__ uint4 side_row_chunk_h(const uint8_t* base, int lrow, int j) {
+  constexpr int bh = halfs < 64 ? halfs : 64;  // fp16 per box row
+  constexpr int S = bh * 2;                    // box row bytes == swizzle span
+  constexpr int per = S / 16;                  // 16-byte chunks per box row
   const int box = j / per, jj = j % per;
   const int sw = ((lrow * S) >> 7) & (per - 1);
-  return lds_f32x4(smem_u32(base + box * 128 * S + lrow * S + ((jj ^ sw) << 4)));
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(smem_u32(base + box * 128 * S + lrow * S + ((jj ^ sw) << 4))));
+  return v;
 }
 
 __device__ __forceinline__ float row_inv_rms(float ss, float inv_d) {
@@ -123,10 +127,11 @@ struct EpiQKVG {
     {
       const uint8_t* rb = side + kSideStatBytes;
 #pragma unroll
-      for (int j = 0; j < DK / 4; ++j) {
-        const float4 t4 = side_row_chunk<DK>(rb, lrow, j);
-        cs[2 * j] = make_float2(t4.x, t4.y);
-        cs[2 * j + 1] = make_float2(t4.z, t4.w);
+      for (int j = 0; j < DK / 8; ++j) {
+        const uint4 t = side_row_chunk_h<DK>(rb, lrow, j);
+        const uint32_t w[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) cs[4 * j + e] = __half22float2(*reinterpret_cast<const __half2*>(&w[e]));
       }
     }
     for (int c = c0; c < c1; c += DK) {

@@ -30,17 +30,18 @@ constexpr int kGemmBK = 64;
 constexpr int kGemmEpiWarps = 8;
 constexpr int kGemmThreads = 128 + 32 * kGemmEpiWarps;
 constexpr uint32_t kGemmABytes = kGemmBM * kGemmBK * 2;  // 16 KB per A stage
-constexpr uint32_t kGemmEpiSmem = 8192;                  // per-kernel epilogue scratch
+constexpr uint32_t kGemmEpiSmem = 2048;                  // per-kernel epilogue scratch (QKNorm gains)
 constexpr uint32_t kGemmSmemMax = 227 * 1024;
 
 // Per-row side data streamed by the TMA producer next to each A tile (double-buffered):
 //   bit 0  row statistics: float4 per row (sum-of-squares partials)     128 x 16 B
-//   bit 1  RoPE rows: kRopeFloats fp32 per row (cos/sin pairs of the row's position)
+//   bit 1  RoPE rows: kRopeFloats fp16 per row (cos/sin pairs of the row's position, fp64 on
+//          the host -> fp16: 2^-11 relative, finer than the bf16 Q/K they rotate)
 // Epilogues declare `kSide` and `kRopeFloats`; side_bytes() is one buffer.
 constexpr uint32_t kSideStatBytes = 128 * 16;
 __host__ __device__ constexpr uint32_t side_bytes(int side, int rope_floats) {
   return side == 0 ? 0u
-                   : (((side & 1) ? kSideStatBytes : 0u) + ((side & 2) ? 128u * rope_floats * 4u : 0u) +
+                   : (((side & 1) ? kSideStatBytes : 0u) + ((side & 2) ? 128u * rope_floats * 2u : 0u) +
                       1023u) / 1024u * 1024u;
 }
 
@@ -74,7 +75,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 int M, int N, int K, int BN, int a_stages, Epi epi) {
   constexpr int kSide = Epi::kSide;
   constexpr uint32_t kSideBuf = side_bytes(Epi::kSide, Epi::kRopeFloats);
-  constexpr int kRopeBoxFloats = Epi::kRopeFloats < 32 ? Epi::kRopeFloats : 32;
+  constexpr int kRopeBoxFloats = Epi::kRopeFloats < 64 ? Epi::kRopeFloats : 64;  // fp16 per box row
   constexpr int kRopeBoxes = Epi::kRopeFloats / (kRopeBoxFloats > 0 ? kRopeBoxFloats : 1);
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem_1k(smem_raw);
@@ -145,12 +146,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           uint8_t* dst = sSide + sb * kSideBuf;
           mbar_wait_sleep(&side_empty[sb], ((t >> 1) & 1) ^ 1);
           mbar_arrive_expect_tx(&side_full[sb], ((kSide & 1) ? kSideStatBytes : 0u) +
-                                                    ((kSide & 2) ? 128u * Epi::kRopeFloats * 4u : 0u));
+                                                    ((kSide & 2) ? 128u * Epi::kRopeFloats * 2u : 0u));
           if constexpr (kSide & 1) tma_load_2d(dst, &tmS, &side_full[sb], 0, mb * kGemmBM);
           if constexpr (kSide & 2) {
 #pragma unroll
             for (int bx = 0; bx < kRopeBoxes; ++bx)
-              tma_load_2d(dst + ((kSide & 1) ? kSideStatBytes : 0u) + bx * 128 * kRopeBoxFloats * 4, &tmR,
+              tma_load_2d(dst + ((kSide & 1) ? kSideStatBytes : 0u) + bx * 128 * kRopeBoxFloats * 2, &tmR,
                           &side_full[sb], bx * kRopeBoxFloats, mb * kGemmBM);
           }
         }

@@ -193,20 +193,23 @@ static const CUtensorMap& rope_table(Handle& h, int R, const std::vector<int32_t
   auto it = h.rope_tables.find(key);
   if (it != h.rope_tables.end()) return it->second;
   const int dk = h.dk;
-  std::vector<float> one(static_cast<size_t>(R) * dk);
+  std::vector<__half> one(static_cast<size_t>(R) * dk);
   for (int r = 0; r < R; ++r)
     for (int j = 0; j < dk / 2; ++j) {
       const double freq = std::pow(h.cfg.rope_theta, -2.0 * j / static_cast<double>(dk));
       const double ang = static_cast<double>(pos[r]) * freq;
-      one[static_cast<size_t>(r) * dk + 2 * j] = static_cast<float>(std::cos(ang));
-      one[static_cast<size_t>(r) * dk + 2 * j + 1] = static_cast<float>(std::sin(ang));
+      one[static_cast<size_t>(r) * dk + 2 * j] = __float2half_rn(static_cast<float>(std::cos(ang)));
+      one[static_cast<size_t>(r) * dk + 2 * j + 1] = __float2half_rn(static_cast<float>(std::sin(ang)));
     }
   const size_t rows = static_cast<size_t>(h.Bmax) * R;
-  float* dev = h.dalloc<float>(rows * dk);
+  __half* dev = h.dalloc<__half>(rows * dk);
   for (int b = 0; b < h.Bmax; ++b)
-    CK(cudaMemcpy(dev + static_cast<size_t>(b) * R * dk, one.data(), one.size() * 4, cudaMemcpyHostToDevice));
-  const int box = std::min(dk, 32);
-  return h.rope_tables[key] = make_tmap_2d_f32(dev, rows, dk, 128, box, box * 4);
+    CK(cudaMemcpy(dev + static_cast<size_t>(b) * R * dk, one.data(), one.size() * 2, cudaMemcpyHostToDevice));
+  const uint32_t box = static_cast<uint32_t>(std::min(dk, 64));
+  uint64_t dims[2] = {static_cast<uint64_t>(dk), rows};
+  uint64_t strides[1] = {static_cast<uint64_t>(dk) * 2};
+  uint32_t bx[2] = {box, 128};
+  return h.rope_tables[key] = make_tmap(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, dev, 2, dims, strides, bx, box * 2);
 }
 
 // Shapes the fused block tail covers (TMEM: d accumulator + 2 x 128 hidden-chunk columns).
