@@ -44,7 +44,7 @@ struct TailSmem {
   static constexpr uint32_t oW = oX + 2 * kTileBytes;
   static constexpr uint32_t oSS = oW + kTailStages * kTailStageBytes;  // [2][128] fp32
   static constexpr uint32_t oBar = oSS + 1024;
-  static constexpr uint32_t bytes = oBar + 256 + 1024;  // + alignment slack
+  static constexpr uint32_t bytes = oBar + 320 + 1024;  // + alignment slack
 };
 
 struct TailArgs {
@@ -66,6 +66,60 @@ __device__ __forceinline__ int4 lds_v4(uint32_t addr) {
                : "memory");
   return v;
 }
+// ---- CTA-pair (cta_group::2) helpers: the pair computes 256-row tiles, CTA rank r owning
+// rows [128 r, 128 r + 128); weights are split by N (each CTA loads half of every stage) and
+// one thread of the leader (rank 0) issues M = 256 MMAs reading both CTAs' shared memory.
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+// arrive on the mbarrier at shared::cluster address `caddr` (possibly in the peer CTA) with
+// the default .release.cta semantics: a .cluster-scope release would fence (MEMBAR) every
+// epilogue thread's outstanding global stores at each hand-off (ncu: membar the top stall);
+// the producers' own fences (tcgen05.fence::before_thread_sync, fence.proxy.async) order
+// the TMEM / shared-memory data the leader's MMA reads.
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t caddr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+}
+// TMA load into this CTA's smem completing on an mbarrier that may live in the peer CTA
+__device__ __forceinline__ void tma_load_2d_2sm(void* dst, const CUtensorMap* m, uint32_t bar_caddr, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(bar_caddr)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_bf16_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_bf16_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_commit_both(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+
 // Byte offset of the 16-byte chunk (row r, column chunk c16 of 8 bf16) of a 128-row tile
 // stored as K-blocks of 64 columns in the TMA SWIZZLE_128B layout (UMMA K-major SW128).
 __device__ __forceinline__ uint32_t sw128_off(int r, int c16) {
@@ -77,7 +131,7 @@ __device__ __forceinline__ uint32_t sw128_off(int r, int c16) {
 //   -> up MMAs -> x2 (E3, in place) -> TMA store (io warp) -> Hg(t + 2)
 // The other buffer meanwhile drains tile t-1 and prefetches Hg(t+1), so the previous tile's
 // drain overlaps this tile's Wo MMAs and nothing waits on a store.
-template <int D>
+template <int D, bool kPair>
 __global__ void __launch_bounds__(kTailThreads, 1)
     k_block_tail(const __grid_constant__ CUtensorMap tmHg, const __grid_constant__ CUtensorMap tmWo,
                  const __grid_constant__ CUtensorMap tmWup, const __grid_constant__ CUtensorMap tmWdown,
@@ -85,31 +139,55 @@ __global__ void __launch_bounds__(kTailThreads, 1)
                  const TailArgs a) {
   static_assert(D == 128 || D == 256, "block tail: model dim 128 or 256");
   using S = TailSmem<D>;
+  constexpr uint32_t kNcta = kPair ? 2 : 1;     // weights split by N over the pair
+  constexpr int kStages = kPair ? 2 * kTailStages : kTailStages;
+  constexpr uint32_t kStageBytes = kTailStageBytes / kNcta;
   constexpr uint32_t kKB = D / 64;              // K-blocks of a tile buffer
-  constexpr uint32_t kWoStage = D * 128u;       // one K-block of Wo^T: D rows x 64 K
-  constexpr uint32_t kDownStage = D * 128u;     // Wdown_j^T: D rows x 64 K
-  constexpr uint32_t kUpBox = 128u * 128u;      // 128 rows x 64 K of the interleaved W_up
+  constexpr uint32_t kWoStage = D * 128u / kNcta;    // one K-block of Wo^T: D/ncta rows x 64 K
+  constexpr uint32_t kDownStage = D * 128u / kNcta;  // Wdown_j^T: D/ncta rows x 64 K
+  constexpr uint32_t kUpBox = 128u * 128u / kNcta;   // 128/ncta rows x 64 K of the interleaved W_up
   constexpr int kCols = D / 2;                  // accumulator columns per epilogue thread
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem_1k(smem_raw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::oBar);
-  uint64_t* w_full = bars;        // [3] weight ring
-  uint64_t* w_empty = bars + 3;   // [3]
-  uint64_t* hg_full = bars + 6;   // Hg(t) landed (one phase per tile)
-  uint64_t* wo_full = bars + 7;   // Wo accumulator (U columns) ready, Hg(t) consumed
-  uint64_t* hg_kb = bars + 18;    // [4] Hg(t) K-block kb consumed by the Wo MMAs
-  uint64_t* res_full = bars + 22; // [4] residual K-block kb of t landed over Hg(t)
-  uint64_t* x1_kb = bars + 26;    // [4] x1 K-block kb in smem (its Wo accumulator columns read)
-  uint64_t* u_full = bars + 10;   // [2] up-projection chunk accumulators
-  uint64_t* h_full = bars + 12;   // [2] SwiGLU output written over them
-  uint64_t* d_full = bars + 14;   // down-projection accumulator ready
-  uint64_t* d_empty = bars + 15;  // ... drained by E3
-  uint64_t* x2_full = bars + 16;  // x2 over x1 in smem, ready to store
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 30);
+  uint64_t* w_full = bars;        // [6] weight ring (3 stages single-CTA, 6 half stages as a pair)
+  uint64_t* w_empty = bars + 6;   // [6]
+  uint64_t* hg_full = bars + 12;  // Hg(t) landed (one phase per tile)
+  uint64_t* wo_full = bars + 13;  // Wo accumulator (U columns) ready, Hg(t) consumed
+  uint64_t* u_full = bars + 14;   // [2] up-projection chunk accumulators
+  uint64_t* h_full = bars + 16;   // [2] SwiGLU output written over them
+  uint64_t* d_full = bars + 18;   // down-projection accumulator ready
+  uint64_t* d_empty = bars + 19;  // ... drained by E3
+  uint64_t* x2_full = bars + 20;  // x2 over x1 in smem, ready to store
+  uint64_t* hg_kb = bars + 21;    // [4] Hg(t) K-block kb consumed by the Wo MMAs
+  uint64_t* res_full = bars + 25; // [4] residual K-block kb of t landed over Hg(t)
+  uint64_t* x1_kb = bars + 29;    // [4] x1 K-block kb in smem (its Wo accumulator columns read)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 33);
 
   const int warp = warp_id(), lane = lane_id();
-  const int num_m = (a.M + 127) / 128;
+  // work unit = one 128-row tile, or one 256-row tile of the pair (rank r: rows 128 r ...)
+  const uint32_t rank = kPair ? cluster_rank() : 0u;
+  const int unit0 = kPair ? static_cast<int>(blockIdx.x) / 2 : static_cast<int>(blockIdx.x);
+  const int ustep = kPair ? static_cast<int>(gridDim.x) / 2 : static_cast<int>(gridDim.x);
+  const int num_m = kPair ? (a.M + 255) / 256 : (a.M + 127) / 128;
+  auto tile_row0 = [&](int u) { return (u * static_cast<int>(kNcta) + static_cast<int>(rank)) * 128; };
   const int n_chunks = a.m / 64;
+  // mbarriers the leader's MMA issuer waits on: the peer CTA's threads arrive there remotely
+  auto leader = [&](uint64_t* bar) { return kPair ? map_to_rank(smem_u32(bar), 0) : smem_u32(bar); };
+  auto arrive_leader = [&](uint64_t* bar) {
+    if constexpr (kPair) {
+      mbar_arrive_cluster(map_to_rank(smem_u32(bar), 0));
+    } else {
+      mbar_arrive(bar);
+    }
+  };
+  auto commit = [&](uint64_t* bar) {
+    if constexpr (kPair) {
+      mma2_commit_both(bar);
+    } else {
+      mma_commit(bar);
+    }
+  };
   auto xbuf = [&](int t) { return smem + S::oX + (t & 1) * S::kTileBytes; };
 
   if (warp == 0 && lane == 0) {
@@ -119,7 +197,7 @@ __global__ void __launch_bounds__(kTailThreads, 1)
     tma_prefetch_desc(&tmWdown);
     tma_prefetch_desc(&tmX);
     tma_prefetch_desc(&tmOut);
-    for (int s = 0; s < kTailStages; ++s) {
+    for (int s = 0; s < kStages; ++s) {
       mbar_init(&w_full[s], 1);
       mbar_init(&w_empty[s], 1);
     }
@@ -128,20 +206,33 @@ __global__ void __launch_bounds__(kTailThreads, 1)
     for (int i = 0; i < 4; ++i) {
       mbar_init(&hg_kb[i], 1);
       mbar_init(&res_full[i], 1);
-      mbar_init(&x1_kb[i], 128);
+      mbar_init(&x1_kb[i], 128 * kNcta);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&u_full[i], 1);
-      mbar_init(&h_full[i], 256);
+      mbar_init(&h_full[i], 256 * kNcta);
     }
     mbar_init(d_full, 1);
-    mbar_init(d_empty, 256);
+    mbar_init(d_empty, 256 * kNcta);
     mbar_init(x2_full, 256);
     mbar_fence_init();
   }
-  if (warp == 2) tmem_alloc(tslot, 512);
+  if (warp == 2) {
+    if constexpr (kPair) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                   "r"(512u)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      tmem_alloc(tslot, 512);
+    }
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair) {
+    cluster_sync_all();  // barrier inits of both CTAs visible before any remote arrive / TMA
+  } else {
+    __syncthreads();
+  }
   tc_fence_after();
   const uint32_t tmem = *tslot;
 
@@ -150,36 +241,47 @@ __global__ void __launch_bounds__(kTailThreads, 1)
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
+      // each stage: this CTA's share (the N-rows rank * N/ncta ...) of one weight K-block;
+      // as a pair, both CTAs' loads complete on the leader's w_full
       auto stage = [&](uint32_t bytes) -> uint8_t* {
         mbar_wait_sleep(&w_empty[s], ph ^ 1);
-        mbar_arrive_expect_tx(&w_full[s], bytes);
-        return smem + S::oW + s * kTailStageBytes;
+        if (rank == 0) mbar_arrive_expect_tx(&w_full[s], bytes * kNcta);
+        return smem + S::oW + s * kStageBytes;
+      };
+      auto load = [&](void* dst, const CUtensorMap* m, int c0, int c1) {
+        if constexpr (kPair) {
+          tma_load_2d_2sm(dst, m, leader(&w_full[s]), c0, c1);
+        } else {
+          tma_load_2d(dst, m, &w_full[s], c0, c1);
+        }
       };
       auto advance = [&]() {
-        if (++s == kTailStages) {
+        if (++s == kStages) {
           s = 0;
           ph ^= 1;
         }
       };
+      const int nro = static_cast<int>(rank) * (D / static_cast<int>(kNcta));    // Wo / Wdown rows
+      const int nru = static_cast<int>(rank) * (128 / static_cast<int>(kNcta));  // W_up chunk rows
       auto up = [&](int j) {
         for (int p = 0; p < static_cast<int>(kKB) / 2; ++p) {
           uint8_t* dst = stage(2 * kUpBox);
-          tma_load_2d(dst, &tmWup, &w_full[s], (2 * p) * 64, j * 128);
-          tma_load_2d(dst + kUpBox, &tmWup, &w_full[s], (2 * p + 1) * 64, j * 128);
+          load(dst, &tmWup, (2 * p) * 64, j * 128 + nru);
+          load(dst + kUpBox, &tmWup, (2 * p + 1) * 64, j * 128 + nru);
           advance();
         }
       };
-      for (int mb = blockIdx.x; mb < num_m; mb += gridDim.x) {
+      for (int u = unit0; u < num_m; u += ustep) {
         for (uint32_t kb = 0; kb < kKB; ++kb) {  // Wo^T K-blocks
           uint8_t* dst = stage(kWoStage);
-          tma_load_2d(dst, &tmWo, &w_full[s], kb * 64, 0);
+          load(dst, &tmWo, kb * 64, nro);
           advance();
         }
         up(0);
         if (n_chunks > 1) up(1);
         for (int j = 0; j < n_chunks; ++j) {
           uint8_t* dst = stage(kDownStage);
-          tma_load_2d(dst, &tmWdown, &w_full[s], j * 64, 0);
+          load(dst, &tmWdown, j * 64, nro);
           advance();
           if (j + 2 < n_chunks) up(j + 2);
         }
@@ -187,26 +289,40 @@ __global__ void __launch_bounds__(kTailThreads, 1)
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
-      const uint32_t id_d = umma_idesc_bf16(128, D);
-      const uint32_t id_u = umma_idesc_bf16(128, 128);
+    if (lane == 0 && rank == 0) {
+      const uint32_t id_d = umma_idesc_bf16(128 * kNcta, D);
+      const uint32_t id_u = umma_idesc_bf16(128 * kNcta, 128);
       const uint32_t w0 = smem_u32(smem + S::oW);
+      auto mma_ss = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+        if constexpr (kPair) {
+          mma2_bf16_ss(d, a, b, idesc, acc);
+        } else {
+          mma_bf16_ss(d, a, b, idesc, acc);
+        }
+      };
+      auto mma_ts = [&](uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+        if constexpr (kPair) {
+          mma2_bf16_ts(d, a, b, idesc, acc);
+        } else {
+          mma_bf16_ts(d, a, b, idesc, acc);
+        }
+      };
       int s = 0;
       uint32_t ph = 0;
       auto wait_stage = [&]() -> uint32_t {
         mbar_wait(&w_full[s], ph);
         tc_fence_after();
-        return w0 + s * kTailStageBytes;
+        return w0 + s * kStageBytes;
       };
       auto release_stage = [&]() {
-        mma_commit(&w_empty[s]);
-        if (++s == kTailStages) {
+        commit(&w_empty[s]);
+        if (++s == kStages) {
           s = 0;
           ph ^= 1;
         }
       };
       int t = 0, c = 0;  // tile, global hidden-chunk counter (phases of u_full / h_full)
-      for (int mb = blockIdx.x; mb < num_m; mb += gridDim.x, ++t) {
+      for (int u = unit0; u < num_m; u += ustep, ++t) {
         const uint32_t xb = smem_u32(xbuf(t));
         // Wo accumulates into the U columns [256, 256 + D): free once the previous tile's
         // last down MMA was issued (in-order pipe), so it overlaps that tile's E3 drain of D
@@ -216,12 +332,12 @@ __global__ void __launch_bounds__(kTailThreads, 1)
           const uint32_t b = wait_stage();
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            mma_bf16_ss(tmem + 256, umma_sdesc_kmajor(xb + kb * 16384 + k * 32, 128),
-                        umma_sdesc_kmajor(b + k * 32, 128), id_d, (kb | k) != 0 ? 1u : 0u);
+            mma_ss(tmem + 256, umma_sdesc_kmajor(xb + kb * 16384 + k * 32, 128),
+                   umma_sdesc_kmajor(b + k * 32, 128), id_d, (kb | k) != 0 ? 1u : 0u);
           release_stage();
-          mma_commit(&hg_kb[kb]);  // the residual K-block may overwrite it now
+          commit(&hg_kb[kb]);  // the residual K-block may overwrite it now
         }
-        mma_commit(wo_full);
+        commit(wo_full);
         // up(0) overwrites the Wo accumulator columns of K-blocks 0 and 1 (U0): both must have
         // been read; later K-blocks of x1 are waited for one by one (E1 runs a K-block ahead)
         mbar_wait(&x1_kb[0], t & 1);
@@ -240,12 +356,12 @@ __global__ void __launch_bounds__(kTailThreads, 1)
               }
 #pragma unroll
               for (int k = 0; k < 4; ++k)
-                mma_bf16_ss(u, umma_sdesc_kmajor(xb + kb * 16384 + k * 32, 128),
-                            umma_sdesc_kmajor(b + kh * kUpBox + k * 32, 128), id_u, (kb | k) != 0 ? 1u : 0u);
+                mma_ss(u, umma_sdesc_kmajor(xb + kb * 16384 + k * 32, 128),
+                       umma_sdesc_kmajor(b + kh * kUpBox + k * 32, 128), id_u, (kb | k) != 0 ? 1u : 0u);
             }
             release_stage();
           }
-          mma_commit(&u_full[j & 1]);
+          commit(&u_full[j & 1]);
         };
         up(0);
         if (n_chunks > 1) up(1);
@@ -258,48 +374,54 @@ __global__ void __launch_bounds__(kTailThreads, 1)
           const uint32_t b = wait_stage();
 #pragma unroll
           for (int k = 0; k < 4; ++k)
-            mma_bf16_ts(tmem, hbase + (k >> 1) * 64 + (k & 1) * 8, umma_sdesc_kmajor(b + k * 32, 128), id_d,
-                        (j | k) != 0 ? 1u : 0u);
+            mma_ts(tmem, hbase + (k >> 1) * 64 + (k & 1) * 8, umma_sdesc_kmajor(b + k * 32, 128), id_d,
+                   (j | k) != 0 ? 1u : 0u);
           release_stage();
           if (j + 2 < n_chunks) up(j + 2);  // in-order tensor pipe: reads of h_j precede
         }
-        mma_commit(d_full);
+        commit(d_full);
       }
     }
   } else if (warp == 3) {
     // ---------------------------------------------------------------- tile I/O (TMA)
     if (lane == 0) {
-      auto load_hg = [&](int mb, int t) {
-        mbar_arrive_expect_tx(hg_full, S::kTileBytes);
-        for (uint32_t kb = 0; kb < kKB; ++kb)
-          tma_load_2d(xbuf(t) + kb * 16384, &tmHg, hg_full, kb * 64, mb * 128);
+      // Hg rows of this CTA; as a pair both CTAs' loads complete on the leader's hg_full
+      auto load_hg = [&](int u, int t) {
+        if (rank == 0) mbar_arrive_expect_tx(hg_full, S::kTileBytes * kNcta);
+        for (uint32_t kb = 0; kb < kKB; ++kb) {
+          if constexpr (kPair) {
+            tma_load_2d_2sm(xbuf(t) + kb * 16384, &tmHg, leader(hg_full), kb * 64, tile_row0(u));
+          } else {
+            tma_load_2d(xbuf(t) + kb * 16384, &tmHg, hg_full, kb * 64, tile_row0(u));
+          }
+        }
       };
-      auto store_x2 = [&](int mb, int t) {
+      auto store_x2 = [&](int u, int t) {
         mbar_wait_sleep(x2_full, t & 1);
-        for (uint32_t kb = 0; kb < kKB; ++kb) tma_store_2d(&tmOut, xbuf(t) + kb * 16384, kb * 64, mb * 128);
+        for (uint32_t kb = 0; kb < kKB; ++kb) tma_store_2d(&tmOut, xbuf(t) + kb * 16384, kb * 64, tile_row0(u));
         bulk_commit();
       };
       int t = 0;
-      if (static_cast<int>(blockIdx.x) < num_m) load_hg(blockIdx.x, 0);
-      for (int mb = blockIdx.x; mb < num_m; mb += gridDim.x, ++t) {
-        const int next = mb + gridDim.x;
+      if (unit0 < num_m) load_hg(unit0, 0);
+      for (int u = unit0; u < num_m; u += ustep, ++t) {
+        const int next = u + ustep;
         if (next < num_m)  // residual rows of t+1 into L2 ahead of their TMA load
-          for (uint32_t kb = 0; kb < kKB; ++kb) tma_prefetch_l2_2d(&tmX, kb * 64, next * 128);
+          for (uint32_t kb = 0; kb < kKB; ++kb) tma_prefetch_l2_2d(&tmX, kb * 64, tile_row0(next));
         // residual rows of t over the consumed Hg(t)
         for (uint32_t kb = 0; kb < kKB; ++kb) {
           mbar_wait_sleep(&hg_kb[kb], t & 1);
           mbar_arrive_expect_tx(&res_full[kb], 16384);
-          tma_load_2d(xbuf(t) + kb * 16384, &tmX, &res_full[kb], kb * 64, mb * 128);
+          tma_load_2d(xbuf(t) + kb * 16384, &tmX, &res_full[kb], kb * 64, tile_row0(u));
         }
         // drain tile t-1 from the other buffer, then prefetch Hg(t+1) into it
         if (t > 0) {
-          store_x2(mb - gridDim.x, t - 1);
+          store_x2(u - ustep, t - 1);
           bulk_wait_read0();
         }
         if (next < num_m) load_hg(next, t + 1);
       }
       if (t > 0) {
-        store_x2(blockIdx.x + (t - 1) * gridDim.x, t - 1);
+        store_x2(unit0 + (t - 1) * ustep, t - 1);
         bulk_wait0();
       }
     }
@@ -312,8 +434,8 @@ __global__ void __launch_bounds__(kTailThreads, 1)
     const uint32_t tD = tmem + lane_off + hf * kCols;
     float* s_ss = reinterpret_cast<float*>(smem + S::oSS);
     int t = 0, c = 0;
-    for (int mb = blockIdx.x; mb < num_m; mb += gridDim.x, ++t) {
-      const int row = mb * 128 + r;
+    for (int u = unit0; u < num_m; u += ustep, ++t) {
+      const int row = tile_row0(u) + r;
       const uint32_t xs = smem_u32(xbuf(t));
       // ---- E1: x1 = bf16(resid + Wo acc) in place over the residual tile, one K-block per
       // pass (half hf takes K-blocks hf, hf + 2, ...), so the up MMAs start after the first
@@ -350,7 +472,7 @@ __global__ void __launch_bounds__(kTailThreads, 1)
         ssb[p] = ss;
         fence_proxy_async_smem();
         tc_fence_before();
-        mbar_arrive(&x1_kb[kb]);
+        arrive_leader(&x1_kb[kb]);
       }
       float ss1;
       if constexpr (kKB == 4) {  // hf 0 holds s0, s2; hf 1 holds s1, s3
@@ -390,7 +512,7 @@ __global__ void __launch_bounds__(kTailThreads, 1)
         tmem_st_32x32b_x16(tu, hw);
         tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(&h_full[ub]);
+        arrive_leader(&h_full[ub]);
       }
       // ---- E3: x2 = bf16(x1 + down acc) in place -> TMA store; row statistics
       mbar_wait(d_full, t & 1);
@@ -421,7 +543,7 @@ __global__ void __launch_bounds__(kTailThreads, 1)
         }
       }
       tc_fence_before();
-      mbar_arrive(d_empty);
+      arrive_leader(d_empty);
       fence_proxy_async_smem();  // x2 tile -> TMA store (async proxy)
       mbar_arrive(x2_full);
       if (row < a.M) {
@@ -436,10 +558,18 @@ __global__ void __launch_bounds__(kTailThreads, 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair) {
+    cluster_sync_all();  // the peer's remote arrives and MMAs on our TMEM are done
+  } else {
+    __syncthreads();
+  }
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem, 512);
+    if constexpr (kPair) {
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u) : "memory");
+    } else {
+      tmem_dealloc(tmem, 512);
+    }
   }
 }
 

@@ -56,6 +56,7 @@ struct LayerDev {
   CUtensorMap tmQ, tmK, tmV;
   CUtensorMap tmRopeKV, tmRopeQ;  // per-row RoPE side tables for the K/V rows and the Q rows
   CUtensorMap tmWo_t, tmWup_t, tmWdown_t;  // k_block_tail weight stages
+  CUtensorMap tmWo_p, tmWup_p, tmWdown_p;  // ... as a CTA pair (each CTA loads half the rows)
 };
 
 struct Handle {
@@ -68,6 +69,7 @@ struct Handle {
   std::map<std::string, HostParam> host;
   bool finalized = false;
   bool fused_tail = true;  // sort_set_option("fused_tail")
+  bool tail_pair = false;  // sort_set_option("tail_pair"): block tail as CTA pairs (cta_group::2)
   bool generic = false;    // d > 256 (SORT-large): projections through the generic path
   // row-sharded item table (sort_set_item_table): the batch's item rows, gathered from the
   // owning ranks, replace the handle's table for the following calls
@@ -387,6 +389,9 @@ static void finalize(Handle& h) {
       L.tmWo_t = make_tmap_2d(L.w_o, d, d, d, d, 64, 128);
       L.tmWup_t = make_tmap_2d(L.w_up, 2 * m, d, d, 128, 64, 128);
       L.tmWdown_t = make_tmap_2d(L.w_down, d, m, m, d, 64, 128);
+      L.tmWo_p = make_tmap_2d(L.w_o, d, d, d, d / 2, 64, 128);
+      L.tmWup_p = make_tmap_2d(L.w_up, 2 * m, d, d, 64, 64, 128);
+      L.tmWdown_p = make_tmap_2d(L.w_down, d, m, m, d / 2, 64, 128);
     }
     }  // !generic
     {
@@ -574,11 +579,11 @@ static void launch_qkvg(Handle& h, const LayerDev& L, const CUtensorMap& A, cons
   }
 }
 
-template <int D>
-static void launch_tail_d(Handle& h, const LayerDev& L, __nv_bfloat16* Xq, float4* SSq, int M) {
+template <int D, bool kPair>
+static void launch_tail_dp(Handle& h, const LayerDev& L, float4* SSq, int M) {
   static bool attr = false;
   if (!attr) {
-    CK(cudaFuncSetAttribute(k_block_tail<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(k_block_tail<D, kPair>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(TailSmem<D>::bytes)));
     attr = true;
   }
@@ -587,12 +592,40 @@ static void launch_tail_d(Handle& h, const LayerDev& L, __nv_bfloat16* Xq, float
   ta.M = M;
   ta.m = h.m;
   ta.inv_d = 1.f / static_cast<float>(h.d);
-  const int num_m = (M + 127) / 128;
-  const int grid = std::min(num_m, h.num_sms);
-  k_block_tail<D><<<grid, kTailThreads, TailSmem<D>::bytes, h.stream>>>(L.tmA_hg, L.tmWo_t, L.tmWup_t,
-                                                                        L.tmWdown_t, L.tmA_q, L.tmA_q, ta);
+  if constexpr (kPair) {
+    const int units = (M + 255) / 256;
+    const int pairs = std::min(units, h.num_sms / 2);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(kTailThreads);
+    cfg.dynamicSmemBytes = TailSmem<D>::bytes;
+    cfg.stream = h.stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, k_block_tail<D, true>, L.tmA_hg, L.tmWo_p, L.tmWup_p, L.tmWdown_p, L.tmA_q, L.tmA_q,
+                          ta));
+  } else {
+    const int num_m = (M + 127) / 128;
+    const int grid = std::min(num_m, h.num_sms);
+    k_block_tail<D, false><<<grid, kTailThreads, TailSmem<D>::bytes, h.stream>>>(L.tmA_hg, L.tmWo_t, L.tmWup_t,
+                                                                                L.tmWdown_t, L.tmA_q, L.tmA_q, ta);
+  }
   check_launch("block_tail");
   ++h.launches;
+}
+
+template <int D>
+static void launch_tail_d(Handle& h, const LayerDev& L, __nv_bfloat16*, float4* SSq, int M) {
+  if (h.tail_pair) {
+    launch_tail_dp<D, true>(h, L, SSq, M);
+  } else {
+    launch_tail_dp<D, false>(h, L, SSq, M);
+  }
 }
 
 static void stage_mark(Handle& h, const std::string& name) {
@@ -1878,6 +1911,8 @@ int sort_set_option(SortHandle p, const char* name, int32_t value) {
     if (!h || !name) throw ConfigError("null argument");
     if (std::strcmp(name, "fused_tail") == 0) {
       h->fused_tail = value != 0;
+    } else if (std::strcmp(name, "tail_pair") == 0) {
+      h->tail_pair = value != 0;
     } else {
       throw ConfigError(std::string("unknown option ") + name);
     }

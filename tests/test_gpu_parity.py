@@ -268,13 +268,18 @@ def test_fused_tail_bit_identical_to_unfused(base):
     logits are bitwise equal; B = 3 leaves a partial last 128-row tile in every layer."""
     cfg, P, gm, _ = base
     b = synth.make_batch(cfg, 3, seed=51)
-    p_f, z_f = gm.forward_logits(b)
+    p_f, z_f = gm.forward_logits(b)          # default: single-CTA block tail
+    gm.set_option("tail_pair", 1)
+    try:
+        p_s, z_s = gm.forward_logits(b)      # CTA-pair (cta_group::2) block tail
+    finally:
+        gm.set_option("tail_pair", 0)
     gm.set_option("fused_tail", 0)
     try:
-        p_u, z_u = gm.forward_logits(b)
+        p_u, z_u = gm.forward_logits(b)      # unfused Wo / up / down GEMM chain
     finally:
         gm.set_option("fused_tail", 1)
-    assert np.array_equal(z_f, z_u)
+    assert np.array_equal(z_f, z_u) and np.array_equal(z_s, z_u)
     assert np.array_equal(p_f, p_u)
 
 
