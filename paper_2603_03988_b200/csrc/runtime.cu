@@ -70,6 +70,7 @@ struct Handle {
   bool finalized = false;
   bool fused_tail = true;  // sort_set_option("fused_tail")
   bool tail_pair = false;  // sort_set_option("tail_pair"): block tail as CTA pairs (cta_group::2)
+  bool attn_bwd_mma = true; // sort_set_option("attn_bwd_mma"): tensor-core attention backward
   bool generic = false;    // d > 256 (SORT-large): projections through the generic path
   // row-sharded item table (sort_set_item_table): the batch's item rows, gathered from the
   // owning ranks, replace the handle's table for the following calls
@@ -92,6 +93,7 @@ struct Handle {
     float* lse = nullptr;
     int32_t *dq_off = nullptr, *dkv_off = nullptr;
     int2 *dq_iv = nullptr, *dkv_iv = nullptr;
+    int32_t *qb_off = nullptr, *qb_list = nullptr;  // tensor-core backward: q blocks per kv block
   };
   std::vector<TrainLayer> tl;
   float *tw[16] = {nullptr};  // backward workspace
@@ -879,6 +881,24 @@ static void ensure_train_buffers(Handle& h, int B) {
     T.dq_iv = h.upload(qi);
     T.dkv_off = h.upload(ko);
     T.dkv_iv = h.upload(ki);
+    {  // 64-row q blocks that see each 64-column kv block (k_attn_bwd_mma)
+      const LayerPlan& lp = h.plan.layers[l];
+      std::vector<int32_t> off(1, 0), lst;
+      for (int c0 = 0; c0 < lp.l_kv; c0 += 64) {
+        const int c1 = std::min(lp.l_kv, c0 + 64) - 1;
+        for (int qb = 0; qb * 64 < lp.l_q; ++qb) {
+          bool any = false;
+          for (int r = qb * 64; r < std::min(lp.l_q, qb * 64 + 64) && !any; ++r)
+            any = (lp.hi[r] >= lp.lo[r] && lp.lo[r] <= c1 && lp.hi[r] >= c0) ||
+                  (lp.self_idx[r] >= c0 && lp.self_idx[r] <= c1);
+          if (any) lst.push_back(qb);
+        }
+        off.push_back(static_cast<int32_t>(lst.size()));
+      }
+      if (lst.empty()) lst.push_back(0);
+      T.qb_off = h.upload(off);
+      T.qb_list = h.upload(lst);
+    }
     mkv_max = std::max(mkv_max, static_cast<size_t>(B) * L.Rkv);
   }
   const size_t rows = std::max(mkv_max, static_cast<size_t>(B) * h.L0);
@@ -1014,21 +1034,50 @@ static void backward_device(Handle& h, int B, const float* dz) {
     AttnBwdArgs ak = ab;
     ak.blk_off = T.dkv_off;
     ak.blk_iv = T.dkv_iv;
-    switch (dk) {
-      case 16:
-        k_attn_bwd_dq<16><<<dim3((L.Rq + 31) / 32, B * H), 32, 0, h.stream>>>(ab);
-        k_attn_bwd_dkv<16><<<dim3((L.Rkv + 31) / 32, B * H), 32, 0, h.stream>>>(ak);
-        break;
-      case 32:
-        k_attn_bwd_dq<32><<<dim3((L.Rq + 31) / 32, B * H), 32, 0, h.stream>>>(ab);
-        k_attn_bwd_dkv<32><<<dim3((L.Rkv + 31) / 32, B * H), 32, 0, h.stream>>>(ak);
-        break;
-      case 64:
-        k_attn_bwd_dq<64><<<dim3((L.Rq + 31) / 32, B * H), 32, 0, h.stream>>>(ab);
-        k_attn_bwd_dkv<64><<<dim3((L.Rkv + 31) / 32, B * H), 32, 0, h.stream>>>(ak);
-        break;
-      default:
-        throw ConfigError("training: unsupported head dim");
+    if (h.attn_bwd_mma) {
+      AttnBwdMmaArgs am;
+      am.q = T.q;
+      am.k = T.k;
+      am.v = T.v;
+      am.dO = dO;
+      am.lse = T.lse;
+      am.D = Dd;
+      am.rowmeta = L.rowmeta;
+      am.qb_off = T.qb_off;
+      am.qb_list = T.qb_list;
+      am.dq = dQ;
+      am.dk = dK;
+      am.dv = dV;
+      am.H = H;
+      am.Rq = L.Rq;
+      am.Rkv = L.Rkv;
+      am.scale = ab.scale;
+      am.scale_log2 = ab.scale_log2;
+      CK(cudaMemsetAsync(dQ, 0, static_cast<size_t>(M) * d * 4, h.stream));
+      const dim3 grid((L.Rkv + 63) / 64, B * H);
+      switch (dk) {
+        case 16: k_attn_bwd_mma<16><<<grid, 128, 0, h.stream>>>(am); break;
+        case 32: k_attn_bwd_mma<32><<<grid, 128, 0, h.stream>>>(am); break;
+        case 64: k_attn_bwd_mma<64><<<grid, 128, 0, h.stream>>>(am); break;
+        default: throw ConfigError("training: unsupported head dim");
+      }
+    } else {
+      switch (dk) {
+        case 16:
+          k_attn_bwd_dq<16><<<dim3((L.Rq + 31) / 32, B * H), 32, 0, h.stream>>>(ab);
+          k_attn_bwd_dkv<16><<<dim3((L.Rkv + 31) / 32, B * H), 32, 0, h.stream>>>(ak);
+          break;
+        case 32:
+          k_attn_bwd_dq<32><<<dim3((L.Rq + 31) / 32, B * H), 32, 0, h.stream>>>(ab);
+          k_attn_bwd_dkv<32><<<dim3((L.Rkv + 31) / 32, B * H), 32, 0, h.stream>>>(ak);
+          break;
+        case 64:
+          k_attn_bwd_dq<64><<<dim3((L.Rq + 31) / 32, B * H), 32, 0, h.stream>>>(ab);
+          k_attn_bwd_dkv<64><<<dim3((L.Rkv + 31) / 32, B * H), 32, 0, h.stream>>>(ak);
+          break;
+        default:
+          throw ConfigError("training: unsupported head dim");
+      }
     }
     check_launch("attention core backward");
     // QKNorm + RoPE backward against recomputed raw projections
@@ -1913,6 +1962,8 @@ int sort_set_option(SortHandle p, const char* name, int32_t value) {
       h->fused_tail = value != 0;
     } else if (std::strcmp(name, "tail_pair") == 0) {
       h->tail_pair = value != 0;
+    } else if (std::strcmp(name, "attn_bwd_mma") == 0) {
+      h->attn_bwd_mma = value != 0;
     } else {
       throw ConfigError(std::string("unknown option ") + name);
     }

@@ -340,6 +340,208 @@ __global__ void __launch_bounds__(32) k_attn_bwd_dkv(const AttnBwdArgs a) {
   }
 }
 
+// ---------------------------------------------------------------- tensor-core attention backward
+// FlashAttention-2-style backward on bf16 mma.sync (m16n8k16, fp32 accumulation), one CTA per
+// (request*head, 64-row kv block), 4 warps of 16 kv rows each. For every 64-row q block that
+// sees the kv block (host list): S^T = K Q^T, P^T = exp2(S^T log2e/sqrt(dk) - lse) masked by the
+// compact rows {lo, hi, self}, dP^T = V dO^T, dS^T = P^T (dP^T - D); dV += P^T dO and
+// dK += dS^T Q stay in registers across q blocks; dQ += dS K goes through dS^T in shared
+// memory and fp32 atomics (several kv blocks contribute to a q block).
+struct AttnBwdMmaArgs {
+  const __nv_bfloat16 *q, *k, *v;  // [BH, Rq, DK], [BH, Rkv, DK], [BH, Rkv, DK]
+  const float* dO;                 // [B*Rq, H*DK]
+  const float* lse;                // [BH, Rq]
+  const float* D;                  // [BH, Rq]
+  const int4* rowmeta;             // [Rq]
+  const int32_t* qb_off;           // CSR over 64-row kv blocks -> 64-row q blocks
+  const int32_t* qb_list;
+  float *dq, *dk, *dv;             // dq zeroed by the caller; dk/dv written
+  int H, Rq, Rkv;
+  float scale_log2, scale;
+};
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int DK>
+__global__ void __launch_bounds__(128) k_attn_bwd_mma(const AttnBwdMmaArgs a) {
+  constexpr int LD = DK + 8;  // padded bf16 row (conflict-free ldmatrix)
+  constexpr int LDS = 64 + 8;
+  constexpr int NT = DK / 8;  // n-tiles of the dK / dV / dQ accumulators
+  constexpr int KS = DK / 16; // k-steps of S^T and dP^T
+  __shared__ __align__(16) __nv_bfloat16 sK[64 * LD], sV[64 * LD], sQ[64 * LD], sO[64 * LD];
+  __shared__ __align__(16) __nv_bfloat16 sS[64 * LDS];  // dS^T [kv][q]
+  __shared__ float sL[64], sD[64];
+  __shared__ int4 sM[64];
+  const int kvb = blockIdx.x, bh = blockIdx.y;
+  const int b = bh / a.H, h = bh - b * a.H;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int c0 = kvb * 64;
+  for (int i = tid; i < 64 * (DK / 8); i += 128) {  // K, V rows of the block (zero past Rkv)
+    const int r = i / (DK / 8), cc = i % (DK / 8);
+    int4 kv = make_int4(0, 0, 0, 0), vv = kv;
+    if (c0 + r < a.Rkv) {
+      kv = reinterpret_cast<const int4*>(a.k + (static_cast<size_t>(bh) * a.Rkv + c0 + r) * DK)[cc];
+      vv = reinterpret_cast<const int4*>(a.v + (static_cast<size_t>(bh) * a.Rkv + c0 + r) * DK)[cc];
+    }
+    *reinterpret_cast<int4*>(sK + r * LD + cc * 8) = kv;
+    *reinterpret_cast<int4*>(sV + r * LD + cc * 8) = vv;
+  }
+  float dk[NT][4], dv[NT][4];
+#pragma unroll
+  for (int n = 0; n < NT; ++n)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) dk[n][e] = dv[n][e] = 0.f;
+  const uint32_t sKa = smem_u32(sK), sVa = smem_u32(sV), sQa = smem_u32(sQ), sOa = smem_u32(sO), sSa = smem_u32(sS);
+  const int kv_lo = c0 + warp * 16 + g;  // this thread's two kv rows: kv_lo, kv_lo + 8
+  for (int it = a.qb_off[kvb]; it < a.qb_off[kvb + 1]; ++it) {
+    const int r0 = a.qb_list[it] * 64;
+    __syncthreads();  // previous iteration done with sQ / sO / sS
+    for (int i = tid; i < 64 * (DK / 8); i += 128) {
+      const int r = i / (DK / 8), cc = i % (DK / 8);
+      int4 qv = make_int4(0, 0, 0, 0);
+      uint32_t ov[4] = {0u, 0u, 0u, 0u};
+      if (r0 + r < a.Rq) {
+        qv = reinterpret_cast<const int4*>(a.q + (static_cast<size_t>(bh) * a.Rq + r0 + r) * DK)[cc];
+        const float* gp = a.dO + (static_cast<size_t>(b) * a.Rq + r0 + r) * a.H * DK + h * DK + cc * 8;
+        const float4 x0 = reinterpret_cast<const float4*>(gp)[0], x1 = reinterpret_cast<const float4*>(gp)[1];
+        ov[0] = pack_bf16x2(x0.x, x0.y);
+        ov[1] = pack_bf16x2(x0.z, x0.w);
+        ov[2] = pack_bf16x2(x1.x, x1.y);
+        ov[3] = pack_bf16x2(x1.z, x1.w);
+      }
+      *reinterpret_cast<int4*>(sQ + r * LD + cc * 8) = qv;
+      *reinterpret_cast<int4*>(sO + r * LD + cc * 8) = make_int4(ov[0], ov[1], ov[2], ov[3]);
+    }
+    for (int i = tid; i < 64; i += 128) {
+      const bool ok = r0 + i < a.Rq;
+      sL[i] = ok ? a.lse[static_cast<size_t>(bh) * a.Rq + r0 + i] : 0.f;
+      sD[i] = ok ? a.D[static_cast<size_t>(bh) * a.Rq + r0 + i] : 0.f;
+      sM[i] = ok ? a.rowmeta[r0 + i] : make_int4(0, -1, -1, 0);
+    }
+    __syncthreads();
+    // S^T and dP^T: [16 kv (this warp) x 64 q]
+    float st[8][4], dp[8][4];
+#pragma unroll
+    for (int n = 0; n < 8; ++n)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) st[n][e] = dp[n][e] = 0.f;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      uint32_t ak[4], av[4];
+      const int arow = warp * 16 + (lane & 15), acol = ks * 16 + (lane >> 4) * 8;
+      ldsm_x4(sKa + (arow * LD + acol) * 2, ak);
+      ldsm_x4(sVa + (arow * LD + acol) * 2, av);
+#pragma unroll
+      for (int np = 0; np < 4; ++np) {  // pairs of q n-tiles
+        uint32_t bq[4], bo[4];
+        const int brow = np * 16 + (lane & 7) + ((lane >> 4) << 3), bcol = ks * 16 + ((lane >> 3) & 1) * 8;
+        ldsm_x4(sQa + (brow * LD + bcol) * 2, bq);
+        ldsm_x4(sOa + (brow * LD + bcol) * 2, bo);
+        mma16816(st[2 * np], ak, bq[0], bq[1]);
+        mma16816(st[2 * np + 1], ak, bq[2], bq[3]);
+        mma16816(dp[2 * np], av, bo[0], bo[1]);
+        mma16816(dp[2 * np + 1], av, bo[2], bo[3]);
+      }
+    }
+    // P^T, dS^T as bf16 A fragments: C n-tiles 2s, 2s+1 form the k-slice s
+    uint32_t pa[4][4], sa[4][4];
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      float p[4], ds[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int q = n * 8 + 2 * t4 + (e & 1);
+        const int kv = kv_lo + ((e >> 1) << 3);
+        const int4 m = sM[q];
+        const bool vis = kv < a.Rkv && ((kv >= m.x && kv <= m.y) || kv == m.z);
+        p[e] = vis ? exp2f(st[n][e] * a.scale_log2 - sL[q]) : 0.f;
+        ds[e] = p[e] * (dp[n][e] - sD[q]);
+      }
+      const int s = n >> 1, hi = n & 1;
+      // A fragment regs: {rows g, k 0-7}, {rows g+8, k 0-7}, {rows g, k 8-15}, {rows g+8, k 8-15}
+      pa[s][hi * 2 + 0] = pack_bf16x2(p[0], p[1]);
+      pa[s][hi * 2 + 1] = pack_bf16x2(p[2], p[3]);
+      sa[s][hi * 2 + 0] = pack_bf16x2(ds[0], ds[1]);
+      sa[s][hi * 2 + 1] = pack_bf16x2(ds[2], ds[3]);
+      const int kl = warp * 16 + g;  // dS^T (bf16) rows kv (local), cols q, for the dQ product
+      *reinterpret_cast<uint32_t*>(sS + kl * LDS + n * 8 + 2 * t4) = sa[s][hi * 2 + 0];
+      *reinterpret_cast<uint32_t*>(sS + (kl + 8) * LDS + n * 8 + 2 * t4) = sa[s][hi * 2 + 1];
+    }
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {  // k = q
+#pragma unroll
+      for (int np = 0; np < NT / 2; ++np) {  // pairs of dk n-tiles; B from [q][dk] rows -> .trans
+        uint32_t bo[4], bq[4];
+        const int brow = s * 16 + (lane & 15), bcol = np * 16 + (lane >> 4) * 8;
+        ldsm_x4_t(sOa + (brow * LD + bcol) * 2, bo);
+        ldsm_x4_t(sQa + (brow * LD + bcol) * 2, bq);
+        mma16816(dv[2 * np], pa[s], bo[0], bo[1]);
+        mma16816(dv[2 * np + 1], pa[s], bo[2], bo[3]);
+        mma16816(dk[2 * np], sa[s], bq[0], bq[1]);
+        mma16816(dk[2 * np + 1], sa[s], bq[2], bq[3]);
+      }
+    }
+    __syncthreads();  // dS^T of all warps in smem
+    // dQ rows [16 w, 16 w + 16) of the q block = dS (q x 64 kv) . K (64 kv x DK)
+    float dq[NT][4];
+#pragma unroll
+    for (int n = 0; n < NT; ++n)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) dq[n][e] = 0.f;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {  // k = kv
+      uint32_t as[4];
+      const int arow = s * 16 + (lane & 7) + ((lane >> 4) << 3), acol = warp * 16 + ((lane >> 3) & 1) * 8;
+      ldsm_x4_t(sSa + (arow * LDS + acol) * 2, as);
+#pragma unroll
+      for (int np = 0; np < NT / 2; ++np) {
+        uint32_t bk[4];
+        const int brow = s * 16 + (lane & 15), bcol = np * 16 + (lane >> 4) * 8;
+        ldsm_x4_t(sKa + (brow * LD + bcol) * 2, bk);
+        mma16816(dq[2 * np], as, bk[0], bk[1]);
+        mma16816(dq[2 * np + 1], as, bk[2], bk[3]);
+      }
+    }
+#pragma unroll
+    for (int n = 0; n < NT; ++n)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int q = r0 + warp * 16 + g + ((e >> 1) << 3);
+        if (q < a.Rq)
+          atomicAdd(a.dq + (static_cast<size_t>(b) * a.Rq + q) * a.H * DK + h * DK + n * 8 + 2 * t4 + (e & 1),
+                    dq[n][e] * a.scale);
+      }
+  }
+#pragma unroll
+  for (int n = 0; n < NT; ++n)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int kv = kv_lo + ((e >> 1) << 3);
+      if (kv < a.Rkv) {
+        const size_t o = (static_cast<size_t>(b) * a.Rkv + kv) * a.H * DK + h * DK + n * 8 + 2 * t4 + (e & 1);
+        a.dk[o] = dk[n][e] * a.scale;
+        a.dv[o] = dv[n][e];
+      }
+    }
+}
+
 // QKNorm + RoPE backward per (row, head) (attention.cpp:177-183): dx_rot -> inverse RoPE
 // at the row's position (rope.hpp:13-40, angle -> -angle) -> per-head RMSNorm backward
 // against the raw projection `raw` with gain g[h]. Each warp takes kQkRowsPerWarp rows,

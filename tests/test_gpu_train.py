@@ -133,3 +133,23 @@ def test_bce_adamw_step_and_weight_repack():
     p_dev = gm.forward(b)
     p_host = fresh.forward(b)
     assert np.array_equal(p_dev, p_host)
+
+
+def test_tensor_core_and_simt_attention_backward_agree():
+    """k_attn_bwd_mma (bf16 mma.sync, dS/P rounded to bf16) against the fp32 SIMT kernels
+    (k_attn_bwd_dq / k_attn_bwd_dkv) on the same saved activations: every gradient within
+    bf16 resolution."""
+    cfg = tiny_config(keep=[262, 128])
+    P = synth.make_params(cfg, seed=12)
+    gm = R.SortModel(cfg, P, max_batch=2)
+    b = synth.make_batch(cfg, 2, seed=13)
+    dz = np.random.default_rng(4).normal(size=(2, cfg.n_cand, 3)).astype(np.float32)
+    gm.train_step(b, dz)
+    g_mma = gm.grads_flat()
+    gm.set_option("attn_bwd_mma", 0)
+    try:
+        gm.train_step(b, dz)
+        g_simt = gm.grads_flat()
+    finally:
+        gm.set_option("attn_bwd_mma", 1)
+    assert rel_l2(g_mma, g_simt) < 1e-2
