@@ -946,7 +946,8 @@ static void backward_device(Handle& h, int B, const float* dz) {
   gemm_rm(h, false, true, BN, dh, 3, dz, 3, w32(h, "head.w2"), 3, dhid, dh);
   k_relu_mask<<<ew_grid(static_cast<size_t>(BN) * dh), 256, 0, h.stream>>>(dhid, hid, static_cast<size_t>(BN) * dh);
   gemm_rm(h, true, false, d, dh, BN, xh, d, dhid, dh, grad_ptr(h, "head.w1"), dh);
-  k_colsum<<<dim3((dh + 31) / 32, 64), 32, 0, h.stream>>>(dhid, BN, dh, grad_ptr(h, "head.b1"));
+  k_colsum<<<dim3((dh + 31) / 32, std::min(1024, (BN + 63) / 64)), 32, 0, h.stream>>>(dhid, BN, dh,
+                                                                                    grad_ptr(h, "head.b1"));
   float* dxh = h.tw[4];
   gemm_rm(h, false, true, BN, d, dh, dhid, dh, w32(h, "head.w1"), dh, dxh, d);
   float* dxc = h.tw[5];
@@ -972,10 +973,10 @@ static void backward_device(Handle& h, int B, const float* dz) {
     k_rmsnorm_rows<__nv_bfloat16><<<(M + 7) / 8, 256, 0, h.stream>>>(T.x1, w32(h, Bk + "ffn_norm"), M, d, nullptr, 1,
                                                                      1, xf, inv);
     gemm_rm(h, false, false, M, 2 * m, d, xf, d, w32(h, F + "w_gu"), 2 * m, GU, 2 * m);
-    k_swiglu_z<<<ew_grid(static_cast<size_t>(M) * m), 256, 0, h.stream>>>(GU, M, m, z);
+    k_swiglu_z<<<std::min(M, 148 * 16), 256, 0, h.stream>>>(GU, M, m, z);
     gemm_rm(h, true, false, m, d, M, z, m, dX, d, grad_ptr(h, F + "w_down"), d);
     gemm_rm(h, false, true, M, m, d, dX, d, w32(h, F + "w_down"), d, z, m);  // z <- dz
-    k_swiglu_bwd<<<ew_grid(static_cast<size_t>(M) * m), 256, 0, h.stream>>>(z, GU, M, m, dGU);
+    k_swiglu_bwd<<<std::min(M, 148 * 16), 256, 0, h.stream>>>(z, GU, M, m, dGU);
     gemm_rm(h, true, false, d, m, M, xf, d, dGU, 2 * m, grad_ptr(h, F + "w_gate"), m);
     gemm_rm(h, true, false, d, m, M, xf, d, dGU + m, 2 * m, grad_ptr(h, F + "w_up"), m);
     float* dxf = h.tw[3];
@@ -1133,7 +1134,8 @@ static void backward_device(Handle& h, int B, const float* dz) {
     k_rmsnorm_bwd<float><<<(n + 63) / 64, 256, d * 4, h.stream>>>(dy, y, inv, w32(h, std::string("tok.g_") + gname[g]), n,
                                                                   d, dproj, 0, grad_ptr(h, std::string("tok.g_") + gname[g]));
     gemm_rm(h, true, false, K, d, n, catf, K, dproj, d, grad_ptr(h, W), d);
-    k_colsum<<<dim3((d + 31) / 32, 64), 32, 0, h.stream>>>(dproj, n, d, grad_ptr(h, std::string("tok.b_") + gname[g]));
+    k_colsum<<<dim3((d + 31) / 32, std::min(1024, (n + 63) / 64)), 32, 0, h.stream>>>(
+        dproj, n, d, grad_ptr(h, std::string("tok.b_") + gname[g]));
     if (g == 1) continue;  // candidates gather only the frozen item table
     gemm_rm(h, false, true, n, K, d, dproj, d, w32(h, W), d, dcat, K);
     TokTableGrads tg{};
@@ -1275,7 +1277,7 @@ static void forward_generic(Handle& h, int B) {
         xo, w32(h, Bk + "ffn_norm"), M, d, nullptr, 1, 1, xf, nullptr);
     gemm_rm_bf16(h, M, 2 * m, d, xf, d, w16(h, F + "w_gu"), 2 * m, h.gw[6], 2 * m);
     __nv_bfloat16* z = reinterpret_cast<__nv_bfloat16*>(h.gw[7]);
-    k_swiglu_z<__nv_bfloat16><<<ew_grid(static_cast<size_t>(M) * m), 256, 0, h.stream>>>(h.gw[6], M, m, z);
+    k_swiglu_z<__nv_bfloat16><<<std::min(M, 148 * 16), 256, 0, h.stream>>>(h.gw[6], M, m, z);
     gemm_rm_bf16(h, M, d, m, z, m, w16(h, F + "w_down"), d, xo, d, 1.f);
     check_launch("generic block tail");
     stage_mark(h, "L" + sl + ".tail");

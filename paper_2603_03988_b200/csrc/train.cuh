@@ -74,12 +74,26 @@ __global__ void __launch_bounds__(256) k_rmsnorm_bwd(const float* __restrict__ d
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r0 = (blockIdx.x * (blockDim.x >> 5) + warp) * kNormBwdRowsPerWarp;
+  constexpr int kMaxCols = 8;  // register-held dgain partials for d <= 256; larger d spill to smem atomics
+  float gacc[kMaxCols];
+#pragma unroll
+  for (int i = 0; i < kMaxCols; ++i) gacc[i] = 0.f;
   for (int r = r0; r < r0 + kNormBwdRowsPerWarp && r < rows; ++r) {
     const float iv = inv[r];
     const float* dyr = dy + static_cast<size_t>(r) * d;
     const T* xr = x + static_cast<size_t>(r) * d;
     float proj = 0.f;
-    for (int c = lane; c < d; c += 32) {
+#pragma unroll
+    for (int i = 0; i < kMaxCols; ++i) {
+      const int c = lane + 32 * i;
+      if (c < d) {
+        const float xh = static_cast<float>(xr[c]) * iv;
+        const float g = dyr[c];
+        gacc[i] = fmaf(g, xh, gacc[i]);
+        proj = fmaf(g * gain[c], xh, proj);
+      }
+    }
+    for (int c = lane + 32 * kMaxCols; c < d; c += 32) {
       const float xh = static_cast<float>(xr[c]) * iv;
       const float g = dyr[c];
       atomicAdd(&sg[c], g * xh);
@@ -93,6 +107,9 @@ __global__ void __launch_bounds__(256) k_rmsnorm_bwd(const float* __restrict__ d
       dxr[c] = accum ? dxr[c] + v : v;
     }
   }
+#pragma unroll
+  for (int i = 0; i < kMaxCols; ++i)
+    if (lane + 32 * i < d) atomicAdd(&sg[lane + 32 * i], gacc[i]);
   __syncthreads();
   for (int c = threadIdx.x; c < d; c += blockDim.x) atomicAdd(&dgain[c], sg[c]);
 }
@@ -101,25 +118,29 @@ __global__ void __launch_bounds__(256) k_rmsnorm_bwd(const float* __restrict__ d
 __device__ __forceinline__ float sigmoid_f(float x) { return 1.f / (1.f + __expf(-x)); }
 template <class O = float>
 __global__ void k_swiglu_z(const float* __restrict__ gu, int M, int m, O* __restrict__ z) {
-  const size_t n = static_cast<size_t>(M) * m;
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const size_t r = i / m, j = i - r * m;
-    const float g = gu[r * 2 * m + j], u = gu[r * 2 * m + m + j];
-    store_as(z + i, g * sigmoid_f(g) * u);
+  // block-rows x columns (no 64-bit division per element)
+  for (int r = blockIdx.x; r < M; r += gridDim.x) {
+    const float* gr = gu + static_cast<size_t>(r) * 2 * m;
+    O* zr = z + static_cast<size_t>(r) * m;
+    for (int j = threadIdx.x; j < m; j += blockDim.x) {
+      const float g = gr[j], u = gr[m + j];
+      store_as(zr + j, g * sigmoid_f(g) * u);
+    }
   }
 }
 // dgu = [dz * u * swish'(g) | dz * swish(g)], swish'(g) = s (1 + g (1 - s))
 __global__ void k_swiglu_bwd(const float* __restrict__ dz, const float* __restrict__ gu, int M, int m,
                              float* __restrict__ dgu) {
-  const size_t n = static_cast<size_t>(M) * m;
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const size_t r = i / m, j = i - r * m;
-    const float g = gu[r * 2 * m + j], u = gu[r * 2 * m + m + j];
-    const float s = sigmoid_f(g);
-    dgu[r * 2 * m + j] = dz[i] * u * s * (1.f + g * (1.f - s));
-    dgu[r * 2 * m + m + j] = dz[i] * g * s;
+  for (int r = blockIdx.x; r < M; r += gridDim.x) {
+    const float* gr = gu + static_cast<size_t>(r) * 2 * m;
+    const float* dzr = dz + static_cast<size_t>(r) * m;
+    float* o = dgu + static_cast<size_t>(r) * 2 * m;
+    for (int j = threadIdx.x; j < m; j += blockDim.x) {
+      const float g = gr[j], u = gr[m + j], dzv = dzr[j];
+      const float s = sigmoid_f(g);
+      o[j] = dzv * u * s * (1.f + g * (1.f - s));
+      o[m + j] = dzv * g * s;
+    }
   }
 }
 
@@ -561,10 +582,16 @@ __global__ void __launch_bounds__(256) k_qknorm_rope_bwd(const float* drot, cons
   const int j = lane;  // rotation pair (dk/2 <= 32)
   const bool act = j < dk / 2;
   const int r0 = (blockIdx.x * (blockDim.x >> 5) + warp) * kQkRowsPerWarp;
+  constexpr int kMaxH = 16;  // register-held gain partials (2 per head)
+  float gq[kMaxH][2];
+#pragma unroll
+  for (int i = 0; i < kMaxH; ++i) gq[i][0] = gq[i][1] = 0.f;
   for (int w = r0; w < r0 + kQkRowsPerWarp && w < rows; ++w) {
     const int p = pos[w % R];
     const float2 cs = act ? rope_tab[static_cast<size_t>(p) * (dk / 2) + j] : make_float2(1.f, 0.f);
-    for (int h = 0; h < H; ++h) {
+#pragma unroll
+    for (int h = 0; h < kMaxH; ++h) {
+      if (h >= H) break;
       float dq[2] = {0.f, 0.f}, xr[2] = {0.f, 0.f};
       const size_t o = static_cast<size_t>(w) * d + h * dk + 2 * j;
       if (act) {
@@ -581,13 +608,19 @@ __global__ void __launch_bounds__(256) k_qknorm_rope_bwd(const float* drot, cons
       const float proj = warp_sum(dq[0] * g0 * xr[0] * inv + dq[1] * g1 * xr[1] * inv) / static_cast<float>(dk);
       if (act) {
         const float xh0 = xr[0] * inv, xh1 = xr[1] * inv;
-        atomicAdd(&sg[h * dk + 2 * j], dq[0] * xh0);
-        atomicAdd(&sg[h * dk + 2 * j + 1], dq[1] * xh1);
+        gq[h][0] = fmaf(dq[0], xh0, gq[h][0]);
+        gq[h][1] = fmaf(dq[1], xh1, gq[h][1]);
         *reinterpret_cast<float2*>(draw + o) =
             make_float2((dq[0] * g0 - proj * xh0) * inv, (dq[1] * g1 - proj * xh1) * inv);
       }
     }
   }
+#pragma unroll
+  for (int h = 0; h < kMaxH; ++h)
+    if (h < H && act) {
+      atomicAdd(&sg[h * dk + 2 * j], gq[h][0]);
+      atomicAdd(&sg[h * dk + 2 * j + 1], gq[h][1]);
+    }
   __syncthreads();
   for (int c = threadIdx.x; c < d; c += blockDim.x) atomicAdd(&dgain[c], sg[c]);
 }
