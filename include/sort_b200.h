@@ -214,7 +214,9 @@ int sort_gather_rows(const void* table, int64_t n_rows, int32_t row_bytes, const
  * path): "fused_tail" (1 = one k_block_tail launch per block for Wo + residual + SwishGLU FFN
  * + residual where the shape allows it, 0 = the three separate GEMMs); "tail_pair" (1 = run
  * that kernel as CTA pairs with cta_group::2 MMAs, M = 256 per pair and the weights split by
- * N; 0 = single CTA, the default: measured faster on B200). Status 1 on an unknown name. */
+ * N; 0 = single CTA, the default: measured faster on B200); "qkvg_pair" (the QKVG projection
+ * GEMM as CTA pairs, default 0 for the same reason); "attn_bwd_mma" (1 = tensor-core
+ * attention backward, the default; 0 = the fp32 SIMT kernels). Status 1 on an unknown name. */
 int sort_set_option(SortHandle h, const char* name, int32_t value);
 
 #ifdef __cplusplus

@@ -51,11 +51,11 @@ struct GemmPlan {
   uint32_t b_bytes, smem_bytes;
 };
 
-__host__ __device__ inline GemmPlan gemm_plan(int K, int BN, uint32_t side_buf_bytes = 0) {
+__host__ __device__ inline GemmPlan gemm_plan(int K, int BN, uint32_t side_buf_bytes = 0, int ncta = 1) {
   GemmPlan p;
   p.BN = BN;
   p.num_k = (K + kGemmBK - 1) / kGemmBK;
-  p.b_bytes = static_cast<uint32_t>(BN) * kGemmBK * 2 * p.num_k;
+  p.b_bytes = static_cast<uint32_t>(BN / ncta) * kGemmBK * 2 * p.num_k;  // this CTA's weight share
   const uint32_t fixed = 1024 + p.b_bytes + kGemmEpiSmem + 2 * side_buf_bytes + 256;
   int st = fixed < kGemmSmemMax ? static_cast<int>((kGemmSmemMax - fixed) / kGemmABytes) : 0;
   p.a_stages = st > 8 ? 8 : st;
@@ -68,11 +68,15 @@ __host__ __device__ inline GemmPlan gemm_plan(int K, int BN, uint32_t side_buf_b
 // c / num_n + G / num_n, ... through an a_stages-deep TMA ring. Only A moves per tile,
 // which keeps the L2 -> SM traffic at ~32 B/clk/SM for K = 256 instead of re-reading
 // the weights for every 128-row tile.
-template <class Epi>
+// kPair: the CTA-pair form (tcgen05 cta_group::2): a cluster of 2 CTAs owns the slice, each
+// CTA holding half of its weight rows (BN/2 x K) and streaming its own 128 rows of every
+// 256-row m-block; the leader issues M = 256 MMAs.
+template <class Epi, bool kPair = false>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm_bf16(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmR,
                 int M, int N, int K, int BN, int a_stages, Epi epi) {
+  constexpr int kNcta = kPair ? 2 : 1;
   constexpr int kSide = Epi::kSide;
   constexpr uint32_t kSideBuf = side_bytes(Epi::kSide, Epi::kRopeFloats);
   constexpr int kRopeBoxFloats = Epi::kRopeFloats < 64 ? Epi::kRopeFloats : 64;  // fp16 per box row
@@ -80,7 +84,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem_1k(smem_raw);
   const int num_k = (K + kGemmBK - 1) / kGemmBK;
-  const uint32_t b_box = static_cast<uint32_t>(BN) * kGemmBK * 2;
+  const uint32_t b_box = static_cast<uint32_t>(BN / kNcta) * kGemmBK * 2;
   uint8_t* sB = smem;
   uint8_t* sA = sB + b_box * num_k;
   uint8_t* sEpi = sA + a_stages * kGemmABytes;
@@ -97,11 +101,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   const int warp = warp_id();
   const int lane = lane_id();
-  const int num_m = (M + kGemmBM - 1) / kGemmBM;
+  const uint32_t rank = kPair ? cluster_rank() : 0u;
+  const int unit = kPair ? static_cast<int>(blockIdx.x) / 2 : static_cast<int>(blockIdx.x);
+  const int units = kPair ? static_cast<int>(gridDim.x) / 2 : static_cast<int>(gridDim.x);
+  const int num_m = (M + kGemmBM * kNcta - 1) / (kGemmBM * kNcta);  // m-blocks of 128 (256 as a pair)
   const int num_n = N / BN;
-  const int nb = blockIdx.x % num_n;
-  const int m_first = blockIdx.x / num_n;
-  const int m_step = gridDim.x / num_n;
+  const int nb = unit % num_n;
+  const int m_first = unit / num_n;
+  const int m_step = units / num_n;
+  auto mrow0 = [&](int mb) { return (mb * kNcta + static_cast<int>(rank)) * kGemmBM; };
   // residual epilogues keep one sum-of-squares slot per (n-slice, half): at most 4
   if (num_n > 2 && threadIdx.x == 0 && blockIdx.x == 0 && Epi::kMaxParts < num_n * 2) __trap();
 
@@ -116,7 +124,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 32 * kGemmEpiWarps);
+      mbar_init(&tempty[i], 32 * kGemmEpiWarps * kNcta);
     }
     mbar_init(b_full, 1);
     for (int i = 0; i < 2; ++i) {
@@ -125,18 +133,39 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     mbar_fence_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  if (warp == 2) {
+    if constexpr (kPair) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(512u)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      tmem_alloc(tmem_slot, 512);
+    }
+  }
   epi.prologue(sEpi, threadIdx.x, kGemmThreads);
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair) {
+    cluster_sync_all();
+  } else {
+    __syncthreads();
+  }
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // TMA into this CTA's smem completing on the (leader's, as a pair) barrier
+  auto load_ab = [&](void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
+    if constexpr (kPair) {
+      tma_load_2d_2sm(dst, m, map_to_rank(smem_u32(bar), 0), c0, c1);
+    } else {
+      tma_load_2d(dst, m, bar, c0, c1);
+    }
+  };
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(b_full, b_box * num_k);
+      if (rank == 0) mbar_arrive_expect_tx(b_full, b_box * num_k * kNcta);
       for (int kb = 0; kb < num_k; ++kb)
-        tma_load_2d(sB + kb * b_box, &tmB, b_full, kb * kGemmBK, nb * BN);
+        load_ab(sB + kb * b_box, &tmB, b_full, kb * kGemmBK, nb * BN + static_cast<int>(rank) * (BN / kNcta));
       int s = 0;
       uint32_t ph = 0;
       int t = 0;
@@ -147,18 +176,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           mbar_wait_sleep(&side_empty[sb], ((t >> 1) & 1) ^ 1);
           mbar_arrive_expect_tx(&side_full[sb], ((kSide & 1) ? kSideStatBytes : 0u) +
                                                     ((kSide & 2) ? 128u * Epi::kRopeFloats * 2u : 0u));
-          if constexpr (kSide & 1) tma_load_2d(dst, &tmS, &side_full[sb], 0, mb * kGemmBM);
+          if constexpr (kSide & 1) tma_load_2d(dst, &tmS, &side_full[sb], 0, mrow0(mb));
           if constexpr (kSide & 2) {
 #pragma unroll
             for (int bx = 0; bx < kRopeBoxes; ++bx)
               tma_load_2d(dst + ((kSide & 1) ? kSideStatBytes : 0u) + bx * 128 * kRopeBoxFloats * 2, &tmR,
-                          &side_full[sb], bx * kRopeBoxFloats, mb * kGemmBM);
+                          &side_full[sb], bx * kRopeBoxFloats, mrow0(mb));
           }
         }
         for (int kb = 0; kb < num_k; ++kb) {
           mbar_wait_sleep(&empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&full[s], kGemmABytes);
-          tma_load_2d(sA + s * kGemmABytes, &tmA, &full[s], kb * kGemmBK, mb * kGemmBM);
+          if (rank == 0) mbar_arrive_expect_tx(&full[s], kGemmABytes * kNcta);
+          load_ab(sA + s * kGemmABytes, &tmA, &full[s], kb * kGemmBK, mrow0(mb));
           if (++s == a_stages) {
             s = 0;
             ph ^= 1;
@@ -167,8 +196,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t idesc = umma_idesc_bf16(kGemmBM, BN);
+    if (lane == 0 && rank == 0) {
+      const uint32_t idesc = umma_idesc_bf16(kGemmBM * kNcta, BN);
       const uint32_t b0 = smem_u32(sB);
       mbar_wait_sleep(b_full, 0);
       int s = 0;
@@ -187,16 +216,29 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const uint32_t bk = b0 + kb * b_box;
 #pragma unroll
           for (int k = 0; k < kGemmBK / 16; ++k) {
-            mma_bf16_ss(d, umma_sdesc_kmajor(a0 + k * 32, 128), umma_sdesc_kmajor(bk + k * 32, 128),
-                        idesc, (kb | k) != 0 ? 1u : 0u);
+            if constexpr (kPair) {
+              mma2_bf16_ss(d, umma_sdesc_kmajor(a0 + k * 32, 128), umma_sdesc_kmajor(bk + k * 32, 128), idesc,
+                           (kb | k) != 0 ? 1u : 0u);
+            } else {
+              mma_bf16_ss(d, umma_sdesc_kmajor(a0 + k * 32, 128), umma_sdesc_kmajor(bk + k * 32, 128),
+                          idesc, (kb | k) != 0 ? 1u : 0u);
+            }
           }
-          mma_commit(&empty[s]);
+          if constexpr (kPair) {
+            mma2_commit_both(&empty[s]);
+          } else {
+            mma_commit(&empty[s]);
+          }
           if (++s == a_stages) {
             s = 0;
             ph ^= 1;
           }
         }
-        mma_commit(&tfull[acc]);
+        if constexpr (kPair) {
+          mma2_commit_both(&tfull[acc]);
+        } else {
+          mma_commit(&tfull[acc]);
+        }
       }
     }
   } else if (warp >= 4) {
@@ -210,7 +252,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int mb = m_first; mb < num_m; mb += m_step, ++t) {
       const int acc = t & 1;
       const uint32_t acc_ph = (t >> 1) & 1;
-      const int row = mb * kGemmBM + q * 32 + lane;
+      const int row = mrow0(mb) + q * 32 + lane;
       const uint32_t tbase = tmem + acc * 256 + (static_cast<uint32_t>(q * 32) << 16);
       uint8_t* side = sSide + acc * kSideBuf;
       auto wait = [&]() {
@@ -221,14 +263,27 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       epi.run(sEpi, side, wait, tbase, row, nb * BN, c_begin * Epi::kChunk, c_end * Epi::kChunk,
               row < M, nb * 2 + half, num_n * 2);
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      if constexpr (kPair) {
+        mbar_arrive_cluster(map_to_rank(smem_u32(&tempty[acc]), 0));
+      } else {
+        mbar_arrive(&tempty[acc]);
+      }
       if constexpr (kSide != 0) mbar_arrive(&side_empty[acc]);
     }
   }
-  __syncthreads();
+  tc_fence_before();
+  if constexpr (kPair) {
+    cluster_sync_all();
+  } else {
+    __syncthreads();
+  }
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem, 512);
+    if constexpr (kPair) {
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u) : "memory");
+    } else {
+      tmem_dealloc(tmem, 512);
+    }
   }
 }
 

@@ -57,6 +57,7 @@ struct LayerDev {
   CUtensorMap tmRopeKV, tmRopeQ;  // per-row RoPE side tables for the K/V rows and the Q rows
   CUtensorMap tmWo_t, tmWup_t, tmWdown_t;  // k_block_tail weight stages
   CUtensorMap tmWo_p, tmWup_p, tmWdown_p;  // ... as a CTA pair (each CTA loads half the rows)
+  CUtensorMap tmB_all_p, tmB_kv_p, tmB_qg_p;  // QKVG weight slices as a CTA pair (BN/2 rows)
 };
 
 struct Handle {
@@ -71,6 +72,7 @@ struct Handle {
   bool fused_tail = true;  // sort_set_option("fused_tail")
   bool tail_pair = false;  // sort_set_option("tail_pair"): block tail as CTA pairs (cta_group::2)
   bool attn_bwd_mma = true; // sort_set_option("attn_bwd_mma"): tensor-core attention backward
+  bool qkvg_pair = false;   // sort_set_option("qkvg_pair"): QKVG projection as CTA pairs
   bool generic = false;    // d > 256 (SORT-large): projections through the generic path
   // row-sharded item table (sort_set_item_table): the batch's item rows, gathered from the
   // owning ranks, replace the handle's table for the following calls
@@ -380,6 +382,9 @@ static void finalize(Handle& h) {
     L.tmB_all = make_tmap_2d(L.w_all, 4 * d, d, d, L.bn_full, 64, 128);
     L.tmB_qg = make_tmap_2d(L.w_qg, 2 * d, d, d, L.bn_half, 64, 128);
     L.tmB_kv = make_tmap_2d(L.w_kv, 2 * d, d, d, L.bn_half, 64, 128);
+    L.tmB_all_p = make_tmap_2d(L.w_all, 4 * d, d, d, L.bn_full / 2, 64, 128);
+    L.tmB_qg_p = make_tmap_2d(L.w_qg, 2 * d, d, d, L.bn_half / 2, 64, 128);
+    L.tmB_kv_p = make_tmap_2d(L.w_kv, 2 * d, d, d, L.bn_half / 2, 64, 128);
     L.tmA_hg = make_tmap_2d(h.Hg, Mq, d, d, 128, 64, 128);
     L.tmB_o = make_tmap_2d(L.w_o, d, d, d, L.bn_o, 64, 128);
     L.tmB_up = make_tmap_2d(L.w_up, 2 * m, d, d, L.bn_up, 64, 128);
@@ -491,6 +496,39 @@ static void launch_gemm(Handle& h, const CUtensorMap& A, const CUtensorMap& B, i
   ++h.launches;
 }
 
+// The same GEMM as CTA pairs (cluster of 2, tcgen05 cta_group::2); B is the pair map whose
+// box holds BN/2 weight rows.
+template <class Epi>
+static void launch_gemm_pair(Handle& h, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K, int BN,
+                             const Epi& epi, const CUtensorMap* side_stats, const CUtensorMap* side_rope) {
+  static uint32_t attr_bytes = 0;
+  const GemmPlan gp = gemm_plan(K, BN, side_bytes(Epi::kSide, Epi::kRopeFloats), 2);
+  if (N % BN || gp.a_stages < 2) throw RuntimeFailure("gemm: unsupported tile plan");
+  if (gp.smem_bytes > attr_bytes) {
+    CK(cudaFuncSetAttribute(k_gemm_bf16<Epi, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(gp.smem_bytes)));
+    attr_bytes = gp.smem_bytes;
+  }
+  const int num_m2 = (M + 2 * kGemmBM - 1) / (2 * kGemmBM);
+  const int units = gemm_grid(num_m2, N / BN, h.num_sms / 2);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * units);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = gp.smem_bytes;
+  cfg.stream = h.stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, k_gemm_bf16<Epi, true>, A, B, side_stats ? *side_stats : A,
+                        side_rope ? *side_rope : A, M, N, K, BN, gp.a_stages, epi));
+  check_launch("gemm (pair)");
+  ++h.launches;
+}
+
 template <int DK, bool kFixed>
 static void launch_attention_dk(Handle& h, const LayerDev& L, const LayerPlan& lp, int B) {
   const int n_codes = static_cast<int>(lp.tile_code.size()) / 2;  // {kv_tile, classes} pairs
@@ -547,7 +585,7 @@ static void launch_attention(Handle& h, const LayerDev& L, const LayerPlan& lp, 
 template <int DK>
 static void launch_qkvg_dk(Handle& h, const LayerDev& L, const CUtensorMap& A, const CUtensorMap& Bm,
                            int M, int N, int BN, int R, const std::vector<int>& order,
-                           const CUtensorMap& tmS, const CUtensorMap& tmR) {
+                           const CUtensorMap& tmS, const CUtensorMap& tmR, const CUtensorMap* Bpair) {
   EpiQKVG<DK> e;
   e.d = h.d;
   e.H = h.H;
@@ -566,17 +604,20 @@ static void launch_qkvg_dk(Handle& h, const LayerDev& L, const CUtensorMap& A, c
   e.g = h.Gb;
   e.Rq = L.Rq;
   e.Rkv = L.Rkv;
-  launch_gemm(h, A, Bm, M, N, h.d, BN, e, &tmS, &tmR);
+  if (Bpair && h.qkvg_pair)
+    launch_gemm_pair(h, A, *Bpair, M, N, h.d, BN, e, &tmS, &tmR);
+  else
+    launch_gemm(h, A, Bm, M, N, h.d, BN, e, &tmS, &tmR);
 }
 
 static void launch_qkvg(Handle& h, const LayerDev& L, const CUtensorMap& A, const CUtensorMap& Bm,
                         int M, int N, int BN, int R, const std::vector<int>& sec,
-                        const CUtensorMap& tmS, const CUtensorMap& tmR) {
+                        const CUtensorMap& tmS, const CUtensorMap& tmR, const CUtensorMap* Bpair = nullptr) {
   if (N / h.dk > 64) throw ConfigError("unsupported: more than 64 head chunks per projection");
   switch (h.dk) {
-    case 16: launch_qkvg_dk<16>(h, L, A, Bm, M, N, BN, R, sec, tmS, tmR); break;
-    case 32: launch_qkvg_dk<32>(h, L, A, Bm, M, N, BN, R, sec, tmS, tmR); break;
-    case 64: launch_qkvg_dk<64>(h, L, A, Bm, M, N, BN, R, sec, tmS, tmR); break;
+    case 16: launch_qkvg_dk<16>(h, L, A, Bm, M, N, BN, R, sec, tmS, tmR, Bpair); break;
+    case 32: launch_qkvg_dk<32>(h, L, A, Bm, M, N, BN, R, sec, tmS, tmR, Bpair); break;
+    case 64: launch_qkvg_dk<64>(h, L, A, Bm, M, N, BN, R, sec, tmS, tmR, Bpair); break;
     default: throw ConfigError("unsupported head dim");
   }
 }
@@ -720,16 +761,16 @@ static void run_layer(Handle& h, int l, int B, bool attn_only = false) {
                        h.stream));
   if (lp.q_identity) {
     launch_qkvg(h, L, L.tmA_in, L.tmB_all, B * L.Rkv, 4 * d, L.bn_full, L.Rkv,
-                {kSecQ, kSecV, kSecK, kSecG}, h.tmSS[L.in_buf], L.tmRopeKV);
+                {kSecQ, kSecV, kSecK, kSecG}, h.tmSS[L.in_buf], L.tmRopeKV, &L.tmB_all_p);
   } else {
     const int rows = B * L.Rq;
     k_gather_rows<<<(rows + 7) / 8, 256, 0, h.stream>>>(Xin, SSin, Xq, SSq, L.query_rows, B, L.Rkv, L.Rq, d);
     check_launch("gather");
     ++h.launches;
     launch_qkvg(h, L, L.tmA_in, L.tmB_kv, B * L.Rkv, 2 * d, L.bn_half, L.Rkv, {kSecK, kSecV},
-                h.tmSS[L.in_buf], L.tmRopeKV);
+                h.tmSS[L.in_buf], L.tmRopeKV, &L.tmB_kv_p);
     launch_qkvg(h, L, L.tmA_q, L.tmB_qg, B * L.Rq, 2 * d, L.bn_half, L.Rq, {kSecQ, kSecG},
-                h.tmSS[L.q_buf], L.tmRopeQ);
+                h.tmSS[L.q_buf], L.tmRopeQ, &L.tmB_qg_p);
   }
   stage_mark(h, "L" + std::to_string(l) + ".qkvg");
   launch_attention(h, L, lp, B);
@@ -1966,6 +2007,8 @@ int sort_set_option(SortHandle p, const char* name, int32_t value) {
       h->tail_pair = value != 0;
     } else if (std::strcmp(name, "attn_bwd_mma") == 0) {
       h->attn_bwd_mma = value != 0;
+    } else if (std::strcmp(name, "qkvg_pair") == 0) {
+      h->qkvg_pair = value != 0;
     } else {
       throw ConfigError(std::string("unknown option ") + name);
     }

@@ -279,8 +279,17 @@ def test_fused_tail_bit_identical_to_unfused(base):
         p_u, z_u = gm.forward_logits(b)      # unfused Wo / up / down GEMM chain
     finally:
         gm.set_option("fused_tail", 1)
-    assert np.array_equal(z_f, z_u) and np.array_equal(z_s, z_u)
+    gm.set_option("qkvg_pair", 1 - gm_qkvg_default(gm))
+    try:
+        p_q, z_q = gm.forward_logits(b)      # QKVG projection with the other CTA form
+    finally:
+        gm.set_option("qkvg_pair", gm_qkvg_default(gm))
+    assert np.array_equal(z_f, z_u) and np.array_equal(z_s, z_u) and np.array_equal(z_q, z_u)
     assert np.array_equal(p_f, p_u)
+
+
+def gm_qkvg_default(gm):
+    return 0  # sort_set_option("qkvg_pair") default (runtime.cu)
 
 
 def test_fused_tail_d128_vs_oracle():
