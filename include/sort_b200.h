@@ -210,6 +210,21 @@ int sort_set_item_table(SortHandle h, const void* rows, int64_t n_rows);
 int sort_gather_rows(const void* table, int64_t n_rows, int32_t row_bytes, const int64_t* ids,
                      int64_t n, void* out, void* stream);
 
+/* ---------------------------------------------------------------- request ingest */
+/* The reference's JSONL dataset (schema "rankformer.dataset" v1, read_dataset,
+ * dataset_io.cpp:58-162) parsed on the host with its validation rules; errors are status 1
+ * with "dataset line N, field 'F': what" (DatasetFormatError). Batches are packed into
+ * pinned SoA arrays owned by the dataset (valid until the next sort_dataset_batch call):
+ * records [first, first + count) must all have n_hist events, n_cand candidates and
+ * n_profile_fields profile values (one handle serves one geometry). labels [count, n_cand,
+ * 3] (click, cart, purchase) and request_ids [count] are optional. */
+typedef struct SortDataset_* SortDataset;
+int sort_dataset_open(const char* path, SortDataset* out);
+void sort_dataset_close(SortDataset d);
+int64_t sort_dataset_size(SortDataset d);
+int sort_dataset_batch(SortDataset d, int64_t first, int32_t count, int32_t n_hist, int32_t n_cand,
+                       int32_t n_profile_fields, SortBatch* batch, float* labels, int64_t* request_ids);
+
 /* Kernel-selection knobs for A/B tests (no reference counterpart; defaults are the fastest
  * path): "fused_tail" (1 = one k_block_tail launch per block for Wo + residual + SwishGLU FFN
  * + residual where the shape allows it, 0 = the three separate GEMMs); "tail_pair" (1 = run

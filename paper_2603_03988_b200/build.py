@@ -10,7 +10,7 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsort_b200.so")
-SOURCES = ["runtime.cu", "plan.cpp"]
+SOURCES = ["runtime.cu", "plan.cpp", "dataset.cpp"]
 HEADERS = ["ptx.cuh", "gemm.cuh", "epilogues.cuh", "attention.cuh", "tokenizer.cuh", "misc.cuh",
            "block_tail.cuh", "train.cuh",
            "plan.hpp", "tma_host.hpp"]

@@ -57,7 +57,8 @@ EXPORTS = [
     "sort_kernel_count", "sort_enable_stage_timing", "sort_stage_times", "sort_set_option",
     "sort_train_step", "sort_grad_info", "sort_grads_copy", "sort_dtokens",
     "sort_set_item_table", "sort_gather_rows", "sort_train_step_bce", "sort_adamw_step",
-    "sort_get_param",
+    "sort_get_param", "sort_dataset_open", "sort_dataset_close", "sort_dataset_size",
+    "sort_dataset_batch",
 ]
 
 _lib = None
@@ -101,6 +102,12 @@ def lib():
         L.sort_train_step_bce.argtypes = [C.c_void_p, C.c_void_p, f32p, f32p, f32p]
         L.sort_adamw_step.argtypes = [C.c_void_p, C.c_float, C.c_float, C.c_float, C.c_float, C.c_float]
         L.sort_get_param.argtypes = [C.c_void_p, C.c_char_p, f32p]
+        L.sort_dataset_open.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+        L.sort_dataset_close.argtypes = [C.c_void_p]
+        L.sort_dataset_size.argtypes = [C.c_void_p]
+        L.sort_dataset_size.restype = C.c_int64
+        L.sort_dataset_batch.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                         C.POINTER(CSortBatch), f32p, i64p]
         L.sort_gather_rows.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int64,
                                        C.c_void_p, C.c_void_p]
         L.sort_stage_times.argtypes = [C.c_void_p, f32p, C.c_int32, i32p, C.c_char_p, C.c_int32]
@@ -388,3 +395,70 @@ def gather_rows(table_ptr: int, n_rows: int, row_bytes: int, ids_ptr: int, n: in
     _check(lib().sort_gather_rows(C.c_void_p(table_ptr), int(n_rows), int(row_bytes),
                                   C.c_void_p(ids_ptr), int(n), C.c_void_p(out_ptr),
                                   C.c_void_p(stream_ptr) if stream_ptr else None))
+
+
+class Dataset:
+    """The reference's JSONL dataset (schema "rankformer.dataset" v1, read_dataset,
+    dataset_io.cpp:58-162) parsed by the library's host reader into pinned SoA batches."""
+
+    def __init__(self, path: str):
+        h = C.c_void_p()
+        _check(lib().sort_dataset_open(path.encode(), C.byref(h)))
+        self.h = h
+
+    def __len__(self) -> int:
+        return int(lib().sort_dataset_size(self.h))
+
+    def close(self):
+        if getattr(self, "h", None) is not None and _lib is not None:
+            _lib.sort_dataset_close(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def batch(self, first: int, count: int, cfg: SortConfig):
+        """(SortBatch over the dataset's pinned arrays, labels [count, n_cand, 3], request ids,
+        numpy views of the arrays). The arrays stay valid until the next batch() call."""
+        cb = CSortBatch()
+        labels = np.zeros((count, cfg.n_cand, 3), np.float32)
+        ids = np.zeros(count, np.int64)
+        P = len(cfg.profile_vocab)
+        _check(lib().sort_dataset_batch(self.h, first, count, cfg.n_hist, cfg.n_cand, P, C.byref(cb),
+                                        _p(labels, f32p), _p(ids, i64p)))
+
+        def view(ptr, shape, dt):
+            n = int(np.prod(shape))
+            ct = C.c_int64 if dt == np.int64 else C.c_int32
+            return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(ct)), shape=(n,)).reshape(shape).view(dt)
+
+        arrs = {"hist_item": view(cb.hist_item, (count, cfg.n_hist), np.int32),
+                "hist_action": view(cb.hist_action, (count, cfg.n_hist), np.int32),
+                "hist_scene": view(cb.hist_scene, (count, cfg.n_hist), np.int32),
+                "hist_ts": view(cb.hist_ts, (count, cfg.n_hist), np.int64),
+                "req_ts": view(cb.req_ts, (count,), np.int64),
+                "profile": view(cb.profile, (count, P), np.int32),
+                "cand_item": view(cb.cand_item, (count, cfg.n_cand), np.int32)}
+        return cb, labels, ids, arrs
+
+
+def write_dataset(path: str, batch: Dict[str, np.ndarray], labels: Optional[np.ndarray] = None,
+                  request_ids=None) -> None:
+    """write_dataset (dataset_io.cpp:14-56) for a SoA batch: header line + one JSON record per
+    request (history events [item, action, ts, scene], candidates [item, click, cart,
+    purchase, side])."""
+    import json
+    B = int(batch["req_ts"].shape[0])
+    with open(path, "w") as f:
+        f.write(json.dumps({"schema": "rankformer.dataset", "version": 1, "records": B}) + "\n")
+        for b in range(B):
+            hist = [[int(batch["hist_item"][b, i]), int(batch["hist_action"][b, i]), int(batch["hist_ts"][b, i]),
+                     int(batch["hist_scene"][b, i])] for i in range(batch["hist_item"].shape[1])]
+            cands = []
+            for j in range(batch["cand_item"].shape[1]):
+                lab = [0, 0, 0] if labels is None else [int(x) for x in labels[b, j]]
+                cands.append([int(batch["cand_item"][b, j]), lab[0], lab[1], lab[2], []])
+            rec = {"request_id": int(request_ids[b]) if request_ids is not None else b,
+                   "ts": int(batch["req_ts"][b]), "profile": [int(x) for x in batch["profile"][b]],
+                   "history": hist, "candidates": cands}
+            f.write(json.dumps(rec) + "\n")

@@ -377,3 +377,18 @@ def test_large_widths_vs_oracle():
     p2 = gm.forward(b2)
     others = [j for j in range(cfg.n_cand) if j != 3]
     assert np.array_equal(p2[:, others], probs[:, others])
+
+
+def test_jsonl_ingest_forward_bit_identical(tiny, tmp_path):
+    """Requests read from the reference's JSONL format (sort_dataset_batch, pinned SoA) score
+    bit-identically to the same requests passed as arrays."""
+    import ctypes
+    cfg, P, gm, _ = tiny
+    b = synth.make_batch(cfg, 3, seed=71)
+    path = str(tmp_path / "req.jsonl")
+    R.write_dataset(path, b)
+    ds = R.Dataset(path)
+    cb, _, _, _ = ds.batch(0, 3, cfg)
+    out = np.zeros((3, cfg.n_cand, 3), np.float32)
+    R._check(R.lib().sort_forward(gm.h, ctypes.byref(cb), 0, out.ctypes.data, 0))
+    assert np.array_equal(out, gm.forward(b))
