@@ -29,7 +29,7 @@ def built():
 
 def test_library_exports_every_header_symbol():
     hdr = open(os.path.join(ROOT, "include", "sort_b200.h")).read()
-    declared = set(re.findall(r"^(?:int|const char\*)\s+(sort_\w+)\(", hdr, flags=re.M))
+    declared = set(re.findall(r"^(?:int|int64_t|void|const char\*)\s+(sort_\w+)\(", hdr, flags=re.M))
     assert len(declared) >= 20
     lib = ctypes.CDLL(R.LIB_PATH)
     for name in sorted(declared):
