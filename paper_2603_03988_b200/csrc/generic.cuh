@@ -109,40 +109,145 @@ __global__ void k_tok_specials(const float* __restrict__ special, int B, int L, 
 
 // Per row and head: Q/K -> per-head RMSNorm with gain (attention.cpp:111-114) -> interleaved
 // RoPE at the row's position (rope.hpp:27-38) -> bf16 head-major [B*H, R, dk]; V -> bf16
-// head-major; G -> sigmoid -> bf16 [rows, d]. One warp per row; lane j owns pair j.
-__global__ void k_qkv_prep(const float* __restrict__ raw, int rows, int R, int H, int dk, int kind,
+// head-major; G -> sigmoid -> bf16 [rows, d]. Input: the bf16 projection [rows, d]. One warp per
+// row; each lane owns 8 contiguous elements (16-byte loads/stores) of chunk c = lane + 32 i, so a
+// head spans dk / 8 aligned lanes and its sum of squares is a 1-3 step shuffle reduction.
+template <int kV>
+__global__ void k_qkv_prep(const __nv_bfloat16* __restrict__ raw, int rows, int R, int H, int dk, int kind,
                            const int32_t* __restrict__ pos, const float2* __restrict__ rope_tab,
                            const float* __restrict__ gain, __nv_bfloat16* __restrict__ out) {
-  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (w >= rows) return;
-  const int d = H * dk, b = w / R, r = w - b * R;
-  const float* xr = raw + static_cast<size_t>(w) * d;
-  if (kind == 3) {  // gate
-    for (int c = lane; c < d; c += 32)
-      out[static_cast<size_t>(w) * d + c] = __float2bfloat16_rn(1.f / (1.f + __expf(-xr[c])));
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const int d = H * dk, d8 = d >> 3, b = row / R, r = row - b * R;
+  const int e = (lane * 8) & (dk - 1);  // offset inside the head (same for every chunk: 256 % dk == 0)
+  const int4* src = reinterpret_cast<const int4*>(raw + static_cast<size_t>(row) * d);
+  int4 v[kV];
+#pragma unroll
+  for (int i = 0; i < kV; ++i) {
+    const int c = lane + 32 * i;
+    v[i] = c < d8 ? src[c] : make_int4(0, 0, 0, 0);
+  }
+  if (kind == 3) {  // gate: row-major [rows, d]
+    int4* dst = reinterpret_cast<int4*>(out + static_cast<size_t>(row) * d);
+#pragma unroll
+    for (int i = 0; i < kV; ++i) {
+      const int c = lane + 32 * i;
+      if (c >= d8) continue;
+      const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&v[i]);
+      uint32_t o[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 x = __bfloat1622float2(x2[k]);
+        o[k] = pack_bf16x2(1.f / (1.f + __expf(-x.x)), 1.f / (1.f + __expf(-x.y)));
+      }
+      dst[c] = make_int4(o[0], o[1], o[2], o[3]);
+    }
     return;
   }
-  const int p = pos[r];
-  const bool act = lane < dk / 2;
-  for (int h = 0; h < H; ++h) {
-    float x0 = 0.f, x1 = 0.f;
-    if (act) {
-      x0 = xr[h * dk + 2 * lane];
-      x1 = xr[h * dk + 2 * lane + 1];
+  const size_t head0 = static_cast<size_t>(b) * H;
+  if (kind == 2) {  // V: layout change only
+#pragma unroll
+    for (int i = 0; i < kV; ++i) {
+      const int c = lane + 32 * i;
+      if (c >= d8) continue;
+      const int h = (c * 8) / dk;
+      *reinterpret_cast<int4*>(out + ((head0 + h) * R + r) * dk + e) = v[i];
     }
-    __nv_bfloat16* o = out + ((static_cast<size_t>(b) * H + h) * R + r) * dk;
-    if (kind == 2) {  // V
-      if (act) *reinterpret_cast<__nv_bfloat162*>(o + 2 * lane) = __floats2bfloat162_rn(x0, x1);
-      continue;
+    return;
+  }
+  float4 cs[2];  // the lane's 4 (cos, sin) pairs
+  {
+    const float4* t = reinterpret_cast<const float4*>(rope_tab + static_cast<size_t>(pos[r]) * (dk / 2) + e / 2);
+    cs[0] = t[0];
+    cs[1] = t[1];
+  }
+  const float* csf = reinterpret_cast<const float*>(cs);
+  float ss[kV];
+#pragma unroll
+  for (int i = 0; i < kV; ++i) {
+    const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&v[i]);
+    float t = 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 x = __bfloat1622float2(x2[k]);
+      t = fmaf(x.x, x.x, fmaf(x.y, x.y, t));
     }
-    const float inv = rsqrtf(warp_sum(x0 * x0 + x1 * x1) / static_cast<float>(dk) + 1e-6f);
-    if (act) {
-      x0 *= inv * gain[h * dk + 2 * lane];
-      x1 *= inv * gain[h * dk + 2 * lane + 1];
-      const float2 cs = rope_tab[static_cast<size_t>(p) * (dk / 2) + lane];
-      *reinterpret_cast<__nv_bfloat162*>(o + 2 * lane) =
-          __floats2bfloat162_rn(cs.x * x0 - cs.y * x1, cs.y * x0 + cs.x * x1);
+    ss[i] = t;
+  }
+  for (int o = dk / 16; o; o >>= 1)
+#pragma unroll
+    for (int i = 0; i < kV; ++i) ss[i] += __shfl_xor_sync(0xffffffffu, ss[i], o);
+#pragma unroll
+  for (int i = 0; i < kV; ++i) {
+    const int c = lane + 32 * i;
+    if (c >= d8) continue;
+    const int h = (c * 8) / dk;
+    const float inv = rsqrtf(ss[i] / static_cast<float>(dk) + 1e-6f);
+    const float4* g4 = reinterpret_cast<const float4*>(gain + c * 8);
+    const float4 ga = g4[0], gb = g4[1];
+    const float g[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+    const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&v[i]);
+    uint32_t o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 x = __bfloat1622float2(x2[k]);
+      const float x0 = x.x * inv * g[2 * k], x1 = x.y * inv * g[2 * k + 1];
+      const float cc = csf[2 * k], sn = csf[2 * k + 1];
+      o[k] = pack_bf16x2(cc * x0 - sn * x1, sn * x0 + cc * x1);
     }
+    *reinterpret_cast<int4*>(out + ((head0 + h) * R + r) * dk + e) = make_int4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+// Row RMSNorm with gain to bf16, optionally on a residual sum first (the block's two
+// pre-norms, and the attention residual on P(x, L_out)):
+//   v = x[(r / R) * Rsrc + map[r % R]] (+ a[r]);  xo[r] = v (if xo);  y[r] = bf16(v * rsqrt(mean v^2 + eps) * gain)
+// One warp per row, lane owns float4 j = lane + 32 v (v < kV); d % 4 == 0, d <= 128 kV.
+template <int kV>
+__global__ void k_resid_rmsnorm(const float* __restrict__ x, const int32_t* __restrict__ map, int R, int Rsrc,
+                                const float* __restrict__ a, const float* __restrict__ gain, int rows, int d,
+                                float* __restrict__ xo, __nv_bfloat16* __restrict__ y) {
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (w >= rows) return;
+  size_t src = w;
+  if (map) src = static_cast<size_t>(w / R) * Rsrc + map[w % R];
+  const int d4 = d >> 2;
+  const float4* xr = reinterpret_cast<const float4*>(x + src * d);
+  const float4* ar = a ? reinterpret_cast<const float4*>(a + static_cast<size_t>(w) * d) : nullptr;
+  float4 v[kV];
+#pragma unroll
+  for (int i = 0; i < kV; ++i) {
+    const int j = lane + 32 * i;
+    v[i] = j < d4 ? xr[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  if (ar) {
+#pragma unroll
+    for (int i = 0; i < kV; ++i) {
+      const int j = lane + 32 * i;
+      if (j < d4) {
+        const float4 t = ar[j];
+        v[i].x += t.x;
+        v[i].y += t.y;
+        v[i].z += t.z;
+        v[i].w += t.w;
+      }
+    }
+  }
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < kV; ++i) ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+  const float inv = rsqrtf(warp_sum(ss) / static_cast<float>(d) + 1e-6f);
+  float4* xor_ = xo ? reinterpret_cast<float4*>(xo + static_cast<size_t>(w) * d) : nullptr;
+  uint2* yr = reinterpret_cast<uint2*>(y + static_cast<size_t>(w) * d);
+  const float4* g4 = reinterpret_cast<const float4*>(gain);
+#pragma unroll
+  for (int i = 0; i < kV; ++i) {
+    const int j = lane + 32 * i;
+    if (j >= d4) continue;
+    if (xor_) xor_[j] = v[i];
+    const float4 g = g4[j];
+    yr[j] = make_uint2(pack_bf16x2(v[i].x * inv * g.x, v[i].y * inv * g.y),
+                       pack_bf16x2(v[i].z * inv * g.z, v[i].w * inv * g.w));
   }
 }
 

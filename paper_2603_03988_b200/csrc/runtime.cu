@@ -828,12 +828,44 @@ static void gemm_rm(Handle& h, bool ta, bool tb, int M, int N, int K, const floa
 
 // Row-major C[M,N] (fp32, + beta C) = A[M,K] (bf16) . B[K,N] (bf16), fp32 accumulation.
 static void gemm_rm_bf16(Handle& h, int M, int N, int K, const __nv_bfloat16* A, int lda, const __nv_bfloat16* B,
-                         int ldb, float* C, int ldc, float beta = 0.f) {
+                         int ldb, void* C, int ldc, float beta = 0.f, bool c_bf16 = false) {
   const float alpha = 1.f;
   const cublasStatus_t st = cublasGemmEx(h.cublas, CUBLAS_OP_N, CUBLAS_OP_N, N, M, K, &alpha, B, CUDA_R_16BF, ldb, A,
-                                         CUDA_R_16BF, lda, &beta, C, CUDA_R_32F, ldc, CUBLAS_COMPUTE_32F,
-                                         CUBLAS_GEMM_DEFAULT);
+                                         CUDA_R_16BF, lda, &beta, C, c_bf16 ? CUDA_R_16BF : CUDA_R_32F, ldc,
+                                         CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
   if (st != CUBLAS_STATUS_SUCCESS) throw RuntimeFailure("cublasGemmEx (bf16) failed: " + std::to_string(static_cast<int>(st)));
+}
+
+static inline int warp_rows_grid(int rows) { return (rows + 7) / 8; }
+static inline int ew_grid(size_t n) { return static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 16)); }
+
+// generic-path row RMSNorm (optionally after the gathered residual add), see k_resid_rmsnorm
+static void resid_rmsnorm(Handle& h, const float* x, const int32_t* map, int R, int Rsrc, const float* a,
+                          const float* gain, int rows, int d, float* xo, __nv_bfloat16* y) {
+  const int g = warp_rows_grid(rows);
+  if (d <= 256)
+    k_resid_rmsnorm<2><<<g, 256, 0, h.stream>>>(x, map, R, Rsrc, a, gain, rows, d, xo, y);
+  else if (d <= 512)
+    k_resid_rmsnorm<4><<<g, 256, 0, h.stream>>>(x, map, R, Rsrc, a, gain, rows, d, xo, y);
+  else if (d <= 1024)
+    k_resid_rmsnorm<8><<<g, 256, 0, h.stream>>>(x, map, R, Rsrc, a, gain, rows, d, xo, y);
+  else
+    k_resid_rmsnorm<16><<<g, 256, 0, h.stream>>>(x, map, R, Rsrc, a, gain, rows, d, xo, y);
+}
+
+// generic-path per-head Q/K/V/G preparation, see k_qkv_prep (d = H dk <= 2048)
+static void qkv_prep(Handle& h, const __nv_bfloat16* raw, int rows, int R, int H, int dk, int kind,
+                     const int32_t* pos, const float* gain, __nv_bfloat16* out) {
+  const int g = warp_rows_grid(rows), d = H * dk;
+  const float2* rope = h.rope;
+  if (d <= 256)
+    k_qkv_prep<1><<<g, 256, 0, h.stream>>>(raw, rows, R, H, dk, kind, pos, rope, gain, out);
+  else if (d <= 512)
+    k_qkv_prep<2><<<g, 256, 0, h.stream>>>(raw, rows, R, H, dk, kind, pos, rope, gain, out);
+  else if (d <= 1024)
+    k_qkv_prep<4><<<g, 256, 0, h.stream>>>(raw, rows, R, H, dk, kind, pos, rope, gain, out);
+  else
+    k_qkv_prep<8><<<g, 256, 0, h.stream>>>(raw, rows, R, H, dk, kind, pos, rope, gain, out);
 }
 
 static float* grad_ptr(Handle& h, const std::string& name) {
@@ -953,8 +985,6 @@ static void ensure_train_buffers(Handle& h, int B) {
   h.train_B = h.Bmax;
 }
 
-static inline int warp_rows_grid(int rows) { return (rows + 7) / 8; }
-static inline int ew_grid(size_t n) { return static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 16)); }
 
 // Backward of one training forward; dz = dL/dlogits [B*N, 3] on the device.
 static void backward_device(Handle& h, int B, const float* dz) {
@@ -1288,37 +1318,38 @@ static void forward_generic(Handle& h, int B) {
     float* xo = h.gX[1 - cur];
     __nv_bfloat16* xn = reinterpret_cast<__nv_bfloat16*>(h.gw[0]);
     __nv_bfloat16* xq = reinterpret_cast<__nv_bfloat16*>(h.gw[1]);
-    k_rmsnorm_rows<float, __nv_bfloat16><<<warp_rows_grid(Mkv), 256, 0, h.stream>>>(
-        x, w32(h, Bk + "attn_norm"), Mkv, d, nullptr, 1, 1, xn, nullptr);
+    resid_rmsnorm(h, x, nullptr, 1, 1, nullptr, w32(h, Bk + "attn_norm"), Mkv, d, nullptr, xn);
     const __nv_bfloat16* xqp = xn;
     if (!lp.q_identity) {
       k_gather_f32<__nv_bfloat16, __nv_bfloat16><<<warp_rows_grid(M), 256, 0, h.stream>>>(xn, L.query_rows, L.Rq,
                                                                                           L.Rkv, M, d, xq);
       xqp = xq;
     }
-    gemm_rm_bf16(h, M, d, d, xqp, d, w16(h, A + "wq"), d, h.gw[2], d);
-    gemm_rm_bf16(h, M, d, d, xqp, d, w16(h, A + "wg"), d, h.gw[5], d);
-    gemm_rm_bf16(h, Mkv, d, d, xn, d, w16(h, A + "wk"), d, h.gw[3], d);
-    gemm_rm_bf16(h, Mkv, d, d, xn, d, w16(h, A + "wv"), d, h.gw[4], d);
-    k_qkv_prep<<<warp_rows_grid(M), 256, 0, h.stream>>>(h.gw[2], M, L.Rq, H, dk, 0, L.pos_q, h.rope, L.gain_q, h.Qb);
-    k_qkv_prep<<<warp_rows_grid(Mkv), 256, 0, h.stream>>>(h.gw[3], Mkv, L.Rkv, H, dk, 1, L.pos_kv, h.rope, L.gain_k,
-                                                          h.Kb);
-    k_qkv_prep<<<warp_rows_grid(Mkv), 256, 0, h.stream>>>(h.gw[4], Mkv, L.Rkv, H, dk, 2, L.pos_kv, h.rope, nullptr,
-                                                          h.Vb);
-    k_qkv_prep<<<warp_rows_grid(M), 256, 0, h.stream>>>(h.gw[5], M, L.Rq, H, dk, 3, nullptr, nullptr, nullptr, h.Gb);
+    // bf16 projection outputs (fp32 accumulation), consumed by the per-head prep
+    __nv_bfloat16* pq = reinterpret_cast<__nv_bfloat16*>(h.gw[2]);
+    __nv_bfloat16* pk = reinterpret_cast<__nv_bfloat16*>(h.gw[3]);
+    __nv_bfloat16* pv = reinterpret_cast<__nv_bfloat16*>(h.gw[4]);
+    __nv_bfloat16* pg = reinterpret_cast<__nv_bfloat16*>(h.gw[5]);
+    gemm_rm_bf16(h, M, d, d, xqp, d, w16(h, A + "wq"), d, pq, d, 0.f, true);
+    gemm_rm_bf16(h, M, d, d, xqp, d, w16(h, A + "wg"), d, pg, d, 0.f, true);
+    gemm_rm_bf16(h, Mkv, d, d, xn, d, w16(h, A + "wk"), d, pk, d, 0.f, true);
+    gemm_rm_bf16(h, Mkv, d, d, xn, d, w16(h, A + "wv"), d, pv, d, 0.f, true);
+    qkv_prep(h, pq, M, L.Rq, H, dk, 0, L.pos_q, L.gain_q, h.Qb);
+    qkv_prep(h, pk, Mkv, L.Rkv, H, dk, 1, L.pos_kv, L.gain_k, h.Kb);
+    qkv_prep(h, pv, Mkv, L.Rkv, H, dk, 2, nullptr, nullptr, h.Vb);
+    qkv_prep(h, pg, M, L.Rq, H, dk, 3, nullptr, nullptr, h.Gb);
     check_launch("generic projections");
     stage_mark(h, "L" + sl + ".qkvg");
     launch_attention(h, L, lp, B);  // tcgen05 core; writes the gated output to h.Hg
     stage_mark(h, "L" + sl + ".attention");
     gemm_rm_bf16(h, M, d, d, h.Hg, d, w16(h, A + "wo"), d, h.gw[2], d);
-    k_residual_gather<<<warp_rows_grid(M), 256, 0, h.stream>>>(x, L.query_rows, L.Rq, L.Rkv, h.gw[2], M, d, xo);
-    // SwishGLU FFN on RMSN(x1) + residual
+    // x1 = P(x) + attn (kept fp32 in xo), then RMSN(x1) -> bf16 FFN input, in one pass
     __nv_bfloat16* xf = reinterpret_cast<__nv_bfloat16*>(h.gw[1]);
-    k_rmsnorm_rows<float, __nv_bfloat16><<<warp_rows_grid(M), 256, 0, h.stream>>>(
-        xo, w32(h, Bk + "ffn_norm"), M, d, nullptr, 1, 1, xf, nullptr);
-    gemm_rm_bf16(h, M, 2 * m, d, xf, d, w16(h, F + "w_gu"), 2 * m, h.gw[6], 2 * m);
+    resid_rmsnorm(h, x, L.query_rows, L.Rq, L.Rkv, h.gw[2], w32(h, Bk + "ffn_norm"), M, d, xo, xf);
+    __nv_bfloat16* gu = reinterpret_cast<__nv_bfloat16*>(h.gw[6]);  // bf16 [gate | up] pre-activations
+    gemm_rm_bf16(h, M, 2 * m, d, xf, d, w16(h, F + "w_gu"), 2 * m, gu, 2 * m, 0.f, true);
     __nv_bfloat16* z = reinterpret_cast<__nv_bfloat16*>(h.gw[7]);
-    k_swiglu_z<__nv_bfloat16><<<std::min(M, 148 * 16), 256, 0, h.stream>>>(h.gw[6], M, m, z);
+    k_swiglu_z<__nv_bfloat16, __nv_bfloat16><<<std::min(M, 148 * 16), 256, 0, h.stream>>>(gu, M, m, z);
     gemm_rm_bf16(h, M, d, m, z, m, w16(h, F + "w_down"), d, xo, d, 1.f);
     check_launch("generic block tail");
     stage_mark(h, "L" + sl + ".tail");

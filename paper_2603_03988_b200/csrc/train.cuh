@@ -116,15 +116,37 @@ __global__ void __launch_bounds__(256) k_rmsnorm_bwd(const float* __restrict__ d
 
 // SwishGLU pieces. GU = [gp | up] (fp32 [M, 2m]).
 __device__ __forceinline__ float sigmoid_f(float x) { return 1.f / (1.f + __expf(-x)); }
-template <class O = float>
-__global__ void k_swiglu_z(const float* __restrict__ gu, int M, int m, O* __restrict__ z) {
+template <class O = float, class I = float>
+__global__ void k_swiglu_z(const I* __restrict__ gu, int M, int m, O* __restrict__ z) {
   // block-rows x columns (no 64-bit division per element)
   for (int r = blockIdx.x; r < M; r += gridDim.x) {
-    const float* gr = gu + static_cast<size_t>(r) * 2 * m;
+    const I* gr = gu + static_cast<size_t>(r) * 2 * m;
     O* zr = z + static_cast<size_t>(r) * m;
     for (int j = threadIdx.x; j < m; j += blockDim.x) {
-      const float g = gr[j], u = gr[m + j];
+      const float g = static_cast<float>(gr[j]), u = static_cast<float>(gr[m + j]);
       store_as(zr + j, g * sigmoid_f(g) * u);
+    }
+  }
+}
+// bf16 -> bf16 form with 16-byte vectors (m % 8 == 0): the HBM-bound case of the generic path
+template <>
+__global__ void k_swiglu_z<__nv_bfloat16, __nv_bfloat16>(const __nv_bfloat16* __restrict__ gu, int M, int m,
+                                                         __nv_bfloat16* __restrict__ z) {
+  const int m8 = m / 8;
+  for (int r = blockIdx.x; r < M; r += gridDim.x) {
+    const int4* gr = reinterpret_cast<const int4*>(gu + static_cast<size_t>(r) * 2 * m);
+    int4* zr = reinterpret_cast<int4*>(z + static_cast<size_t>(r) * m);
+    for (int j = threadIdx.x; j < m8; j += blockDim.x) {
+      const int4 gv = gr[j], uv = gr[m8 + j];
+      const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gv);
+      const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&uv);
+      uint32_t o[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 g = __bfloat1622float2(g2[e]), u = __bfloat1622float2(u2[e]);
+        o[e] = pack_bf16x2(g.x * sigmoid_f(g.x) * u.x, g.y * sigmoid_f(g.y) * u.y);
+      }
+      zr[j] = make_int4(o[0], o[1], o[2], o[3]);
     }
   }
 }
