@@ -37,6 +37,8 @@ class OrModelCfg(C.Structure):
         ("qknorm", C.c_int), ("gate", C.c_int), ("rope_theta", C.c_double),
         ("local_window", C.c_int), ("full_suffix", C.c_int), ("keep", C.c_int * 64),
         ("keep_specials", C.c_int), ("head_hidden", C.c_int),
+        ("moe_experts", C.c_int), ("moe_topk", C.c_int), ("moe_shared", C.c_int),
+        ("moe_ffn_dim", C.c_int),
     ]
 
 
@@ -86,6 +88,13 @@ def lib():
                                             C.POINTER(C.c_void_p)]
         L.oracle_grads_get.argtypes = [C.c_void_p, C.c_char_p, f64p, i32p, i32p]
         L.oracle_grads_destroy.argtypes = [C.c_void_p]
+        L.oracle_model_forward_moe.argtypes = [C.c_void_p, C.POINTER(OrSample), i32p, f64p, f64p,
+                                               i32p, f64p]
+        L.oracle_moe_route.argtypes = [f64p, C.c_int, C.c_int, C.c_int, C.c_int, f64p, f64p, i32p,
+                                       f64p, f64p]
+        L.oracle_moe_ffn.argtypes = [f64p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                     f64p, f64p, f64p, f64p, f64p, i32p, f64p, i32p, f64p]
+        L.oracle_moe_update_bias.argtypes = [i64p, C.c_int, C.c_double, f64p]
         _lib = L
     return _lib
 
@@ -189,6 +198,53 @@ def swishglu(x, w_gate, w_up, w_down) -> np.ndarray:
     return out
 
 
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def moe_route(x, router, bias, k: int):
+    """route_topk, DeepSeek style: (sel [rows, k], w [rows, k], margin [rows])."""
+    x, router = _f64(x), _f64(router)
+    E = router.shape[1]
+    b = _f64(np.zeros(E) if bias is None else bias).reshape(-1)
+    sel = np.zeros((x.shape[0], k), np.int32)
+    w = np.zeros((x.shape[0], k))
+    mg = np.zeros(x.shape[0])
+    _check(lib().oracle_moe_route(_p(x, f64p), x.shape[0], x.shape[1], E, k, _p(router, f64p),
+                                  _p(b, f64p), _p(sel, i32p), _p(w, f64p), _p(mg, f64p)))
+    return sel, w, mg
+
+
+def moe_ffn(x, router, bias, k: int, w_gate, w_up, w_down, shared: int = 0, forced=None):
+    """moe_forward (SPEC.md:316-324). w_gate/w_up [E+shared, d, m], w_down [E+shared, m, d],
+    shared expert last. Returns (out [rows, d], sel [rows, k], w [rows, k])."""
+    x, router = _f64(x), _f64(router)
+    E = router.shape[1]
+    wg, wu, wd = _f64(w_gate), _f64(w_up), _f64(w_down)
+    b = _f64(np.zeros(E) if bias is None else bias).reshape(-1)
+    rows, d = x.shape
+    m = wg.shape[2]
+    out = np.zeros((rows, d))
+    sel = np.zeros((rows, k), np.int32)
+    w = np.zeros((rows, k))
+    fp = None
+    if forced is not None:
+        forced = np.ascontiguousarray(forced, dtype=np.int32)
+        fp = _p(forced, i32p)
+    _check(lib().oracle_moe_ffn(_p(x, f64p), rows, d, m, E, k, shared, _p(router, f64p), _p(b, f64p),
+                                _p(wg, f64p), _p(wu, f64p), _p(wd, f64p), fp, _p(out, f64p),
+                                _p(sel, i32p), _p(w, f64p)))
+    return out, sel, w
+
+
+def moe_update_bias(load, bias, gamma: float = 1e-3) -> np.ndarray:
+    """update_balance, DeepSeek style: returns the new bias vector."""
+    ld = np.ascontiguousarray(load, dtype=np.int64)
+    b = _f64(bias).copy()
+    _check(lib().oracle_moe_update_bias(_p(ld, i64p), len(ld), gamma, _p(b, f64p)))
+    return b
+
+
 # ------------------------------------------------------------------ model
 class _SampleHold:
     """Keeps the numpy buffers alive while an OrSample points into them."""
@@ -225,6 +281,10 @@ class OracleModel:
         for i, k in enumerate(cfg.keep_schedule()):
             c.keep[i] = k
         c.keep_specials, c.head_hidden = int(cfg.keep_specials), cfg.head_hidden
+        c.moe_experts = getattr(cfg, "moe_experts", 0)
+        c.moe_topk = getattr(cfg, "moe_topk", 1)
+        c.moe_shared = getattr(cfg, "moe_shared", 0)
+        c.moe_ffn_dim = getattr(cfg, "moe_ffn_dim", 0)
         self.cfg = cfg
         h = C.c_void_p()
         _check(lib().oracle_model_create(C.byref(c), C.byref(h)))
@@ -259,6 +319,31 @@ class OracleModel:
         _check(lib().oracle_model_forward(self.h, C.byref(hold.s), _p(probs, f64p),
                                           _p(logits, f64p)))
         return probs, logits
+
+    def forward_moe(self, batch, b: int = 0, forced=None):
+        """Forward with MoE routing control: forced = list (per layer) of [l_q, k] expert ids or
+        None. Returns (probs, logits, sel per layer, margin per layer)."""
+        hold = _SampleHold(batch, b)
+        n = hold.s.n_cand
+        lq = self.layer_meta(batch, b)["l_q"]
+        k = self.cfg.moe_topk
+        tot = int(sum(lq))
+        probs, logits = np.zeros((n, 3)), np.zeros((n, 3))
+        sel = np.zeros(tot * k, np.int32)
+        mg = np.zeros(tot)
+        fp = None
+        if forced is not None:
+            fa = np.ascontiguousarray(np.concatenate([np.asarray(f, np.int32).reshape(-1) for f in forced]))
+            assert fa.size == tot * k
+            fp = _p(fa, i32p)
+        _check(lib().oracle_model_forward_moe(self.h, C.byref(hold.s), fp, _p(probs, f64p),
+                                              _p(logits, f64p), _p(sel, i32p), _p(mg, f64p)))
+        sels, mgs, o = [], [], 0
+        for q in lq:
+            sels.append(sel[o * k:(o + q) * k].reshape(q, k))
+            mgs.append(mg[o:o + q])
+            o += q
+        return probs, logits, sels, mgs
 
     def forward_batch(self, batch, threads: int = 1, limit: Optional[int] = None) -> np.ndarray:
         B = batch["req_ts"].shape[0] if limit is None else limit

@@ -554,10 +554,114 @@ struct LayerTrace {
   int64_t visible = 0;
 };
 
+// ====================================================================== MoE FFN
+// DeepSeek-style mixture of SwishGLU experts: sigmoid gate
+// scores, selection by score + bias (auxiliary-loss-free balancing; the bias never enters the
+// combine weights, SPEC.md "Bias-neutral combine"), ties broken toward the lower expert index,
+// weights renormalised over the selected experts, one always-on shared expert (weight 1).
+struct MoeRouting {
+  std::vector<int> sel;        // [rows, k], descending biased score
+  std::vector<double> w;       // [rows, k]
+  std::vector<double> margin;  // [rows]
+};
+
+void moe_route(const M& x, const M& router, const double* bias, int k, const int* forced, MoeRouting& R) {
+  const int rows = x.r, E = router.c;
+  if (k < 1 || k > E) throw ConfigError("moe: need 1 <= k <= E");
+  R.sel.assign(static_cast<size_t>(rows) * k, 0);
+  R.w.assign(static_cast<size_t>(rows) * k, 0.0);
+  R.margin.assign(rows, 0.0);
+  M logit = matmul(x, router);
+  std::vector<double> sc(E), bs(E);
+  std::vector<int> order(E);
+  for (int i = 0; i < rows; ++i) {
+    for (int e = 0; e < E; ++e) {
+      sc[e] = sigmoid(logit(i, e));
+      bs[e] = sc[e] + (bias ? bias[e] : 0.0);
+      order[e] = e;
+    }
+    // descending biased score, lower index first on ties (a stable sort of the identity order)
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return bs[a] > bs[b]; });
+    R.margin[i] = k < E ? bs[order[k - 1]] - bs[order[k]] : std::numeric_limits<double>::infinity();
+    double tot = 0.0;
+    for (int j = 0; j < k; ++j) {
+      int e = order[j];
+      if (forced) {
+        e = forced[static_cast<size_t>(i) * k + j];
+        if (e < 0 || e >= E) throw ConfigError("moe: forced expert id out of range");
+      }
+      R.sel[static_cast<size_t>(i) * k + j] = e;
+      tot += sc[e];
+    }
+    for (int j = 0; j < k; ++j) {
+      const int e = R.sel[static_cast<size_t>(i) * k + j];
+      R.w[static_cast<size_t>(i) * k + j] = sc[e] / tot;
+    }
+  }
+}
+
+// Rows of x routed to each expert run through that expert's SwishGLU and are added back with
+// their combine weight; the shared expert sees every row with weight 1.
+M moe_ffn(const M& x, const M& router, const double* bias, int k, int shared,
+          const std::vector<const M*>& wg, const std::vector<const M*>& wu, const std::vector<const M*>& wd,
+          const int* forced, MoeRouting& R) {
+  const int rows = x.r, d = x.c, E = router.c;
+  moe_route(x, router, bias, k, forced, R);
+  M out(rows, d);
+  for (int e = 0; e < E + shared; ++e) {
+    std::vector<int> rid;
+    std::vector<double> rw;
+    for (int i = 0; i < rows; ++i) {
+      if (e == E) {
+        rid.push_back(i);
+        rw.push_back(1.0);
+        continue;
+      }
+      for (int j = 0; j < k; ++j)
+        if (R.sel[static_cast<size_t>(i) * k + j] == e) {
+          rid.push_back(i);
+          rw.push_back(R.w[static_cast<size_t>(i) * k + j]);
+        }
+    }
+    if (rid.empty()) continue;
+    M xs(static_cast<int>(rid.size()), d);
+    for (size_t t = 0; t < rid.size(); ++t) std::memcpy(xs.row(static_cast<int>(t)), x.row(rid[t]), sizeof(double) * d);
+    M y = swishglu(xs, *wg[e], *wu[e], *wd[e]);
+    for (size_t t = 0; t < rid.size(); ++t) {
+      double* o = out.row(rid[t]);
+      const double* yr = y.row(static_cast<int>(t));
+      for (int c = 0; c < d; ++c) o[c] += rw[t] * yr[c];
+    }
+  }
+  return out;
+}
+
+M model_moe_ffn(const OrModel& mdl, int l, const M& xf, const int* forced, MoeRouting& R) {
+  const OrModelCfg& c = mdl.cfg;
+  const std::string F = "ffn." + std::to_string(l) + ".";
+  std::vector<const M*> wg, wu, wd;
+  for (int e = 0; e < c.moe_experts + c.moe_shared; ++e) {
+    const std::string X = e < c.moe_experts ? F + "expert." + std::to_string(e) + "." : F + "shared.";
+    wg.push_back(&mdl.P(X + "w_gate"));
+    wu.push_back(&mdl.P(X + "w_up"));
+    wd.push_back(&mdl.P(X + "w_down"));
+  }
+  const M& b = mdl.P(F + "router_bias");
+  return moe_ffn(xf, mdl.P(F + "router"), b.row(0), c.moe_topk, c.moe_shared, wg, wu, wd, forced, R);
+}
+
+// MoE routing control of one model_forward (see oracle_model_forward_moe).
+struct MoeCtl {
+  const int* forced = nullptr;
+  int* out_sel = nullptr;
+  double* out_margin = nullptr;
+};
+
 // model_forward: pre-norm residual blocks over a shrinking
 // residual stream, final RMSNorm, ranking head on candidate rows.
 void model_forward(const OrModel& mdl, const OrSample& s, double* probs, double* logits_out,
-                   std::vector<LayerTrace>* trace) {
+                   std::vector<LayerTrace>* trace, MoeCtl* moe = nullptr) {
+  size_t moe_off = 0, moe_row_off = 0;
   Seq q = tokenize(mdl, s);
   M x = q.tokens;
   std::vector<int> roles = q.roles, pos = q.pos;
@@ -589,8 +693,17 @@ void model_forward(const OrModel& mdl, const OrSample& s, double* probs, double*
       npos[i] = pos[qrows[i]];
     }
     M xf = rmsnorm(xr, mdl.P("block." + L + ".ffn_norm").row(0));
-    M f = swishglu(xf, mdl.P("ffn." + L + ".w_gate"), mdl.P("ffn." + L + ".w_up"),
-                   mdl.P("ffn." + L + ".w_down"));
+    M f;
+    if (c.moe_experts > 0) {  // DeepSeek-style MoE FFN
+      MoeRouting R;
+      f = model_moe_ffn(mdl, l, xf, moe && moe->forced ? moe->forced + moe_off : nullptr, R);
+      if (moe && moe->out_sel) std::copy(R.sel.begin(), R.sel.end(), moe->out_sel + moe_off);
+      if (moe && moe->out_margin) std::copy(R.margin.begin(), R.margin.end(), moe->out_margin + moe_row_off);
+      moe_off += R.sel.size();
+      moe_row_off += R.margin.size();
+    } else {
+      f = swishglu(xf, mdl.P("ffn." + L + ".w_gate"), mdl.P("ffn." + L + ".w_up"), mdl.P("ffn." + L + ".w_down"));
+    }
     for (size_t t = 0; t < xr.a.size(); ++t) xr.a[t] += f.a[t];
     x = std::move(xr);
     roles = std::move(nroles);
@@ -845,6 +958,7 @@ void tokenizer_backward(const OrModel& mdl, const OrSample& s, const M& dtok, Gr
 
 // Backward of model_forward for one request given dL/dlogits [n_cand, 3]; returns dtokens.
 M model_backward(const OrModel& mdl, const OrSample& s, const double* dlogits, Grads& G) {
+  if (mdl.cfg.moe_experts > 0) throw ConfigError("oracle: backward of the MoE FFN is not implemented");
   Seq q = tokenize(mdl, s);
   const OrModelCfg& c = mdl.cfg;
   const int d = mdl.d;
@@ -1074,6 +1188,70 @@ int oracle_swishglu(const double* x, int rows, int d, int m, const double* w_gat
   return 0;
 }
 
+int oracle_model_forward_moe(const OrModel* m, const OrSample* s, const int* forced_sel, double* probs,
+                             double* logits, int* out_sel, double* out_margin) {
+  return guarded([&] {
+    MoeCtl ctl;
+    ctl.forced = forced_sel;
+    ctl.out_sel = out_sel;
+    ctl.out_margin = out_margin;
+    model_forward(*m, *s, probs, logits, nullptr, &ctl);
+  });
+}
+
+int oracle_moe_route(const double* x, int rows, int d, int n_experts, int k, const double* router,
+                     const double* bias, int* sel, double* w, double* margin) {
+  return guarded([&] {
+    M X(rows, d), Rt(d, n_experts);
+    std::memcpy(X.a.data(), x, sizeof(double) * rows * d);
+    std::memcpy(Rt.a.data(), router, sizeof(double) * d * n_experts);
+    MoeRouting R;
+    moe_route(X, Rt, bias, k, nullptr, R);
+    std::copy(R.sel.begin(), R.sel.end(), sel);
+    std::copy(R.w.begin(), R.w.end(), w);
+    if (margin) std::copy(R.margin.begin(), R.margin.end(), margin);
+  });
+}
+
+int oracle_moe_ffn(const double* x, int rows, int d, int m, int n_experts, int k, int shared,
+                   const double* router, const double* bias, const double* w_gate, const double* w_up,
+                   const double* w_down, const int* forced_sel, double* out, int* sel, double* w) {
+  return guarded([&] {
+    if (shared != 0 && shared != 1) throw ConfigError("moe: shared must be 0 or 1");
+    M X(rows, d), Rt(d, n_experts);
+    std::memcpy(X.a.data(), x, sizeof(double) * rows * d);
+    std::memcpy(Rt.a.data(), router, sizeof(double) * d * n_experts);
+    const int n = n_experts + shared;
+    std::vector<M> G(n, M(d, m)), U(n, M(d, m)), D(n, M(m, d));
+    std::vector<const M*> pg, pu, pd;
+    for (int e = 0; e < n; ++e) {
+      std::memcpy(G[e].a.data(), w_gate + static_cast<size_t>(e) * d * m, sizeof(double) * d * m);
+      std::memcpy(U[e].a.data(), w_up + static_cast<size_t>(e) * d * m, sizeof(double) * d * m);
+      std::memcpy(D[e].a.data(), w_down + static_cast<size_t>(e) * m * d, sizeof(double) * m * d);
+      pg.push_back(&G[e]);
+      pu.push_back(&U[e]);
+      pd.push_back(&D[e]);
+    }
+    MoeRouting R;
+    M y = moe_ffn(X, Rt, bias, k, shared, pg, pu, pd, forced_sel, R);
+    std::memcpy(out, y.a.data(), sizeof(double) * rows * d);
+    if (sel) std::copy(R.sel.begin(), R.sel.end(), sel);
+    if (w) std::copy(R.w.begin(), R.w.end(), w);
+  });
+}
+
+int oracle_moe_update_bias(const int64_t* load, int n_experts, double gamma, double* bias) {
+  return guarded([&] {
+    double mean = 0.0;
+    for (int e = 0; e < n_experts; ++e) mean += static_cast<double>(load[e]);
+    mean /= n_experts;
+    for (int e = 0; e < n_experts; ++e) {
+      const double dlt = static_cast<double>(load[e]) - mean;
+      bias[e] -= gamma * (dlt > 0 ? 1.0 : (dlt < 0 ? -1.0 : 0.0));
+    }
+  });
+}
+
 int oracle_model_create(const OrModelCfg* cfg, OrModel** out) {
   return guarded([&] {
     auto* m = new OrModel;
@@ -1090,6 +1268,10 @@ int oracle_model_create(const OrModelCfg* cfg, OrModel** out) {
       if (keep[i + 1] > keep[i]) throw ConfigError("PruneSchedule: keep counts must be non-increasing");
     for (int k : keep)
       if (k < 1) throw ConfigError("PruneSchedule: keep counts must be >= 1");
+    if (cfg->moe_experts < 0 ||
+        (cfg->moe_experts > 0 && (cfg->moe_topk < 1 || cfg->moe_topk > cfg->moe_experts ||
+                                  (cfg->moe_shared != 0 && cfg->moe_shared != 1) || cfg->moe_ffn_dim < 1)))
+      throw ConfigError("moe: need 1 <= topk <= experts, shared in {0, 1}, expert ffn dim >= 1");
     *out = m;
   });
 }

@@ -47,6 +47,10 @@ typedef struct {
   int keep[64];
   int keep_specials;
   int head_hidden; /* ranking head d -> d_h; 0 means d */
+  /* DeepSeek-style MoE FFN: moe_experts routed experts (0 = dense
+   * SwishGLU), moe_topk active per token, moe_shared always-on shared experts (0/1),
+   * moe_ffn_dim intermediate size of every expert. */
+  int moe_experts, moe_topk, moe_shared, moe_ffn_dim;
 } OrModelCfg;
 
 /* One request (RequestSample, data.hpp:32-38) with no side features. */
@@ -123,6 +127,29 @@ int oracle_attention_forward(const OrModel* m, int layer, const double* xn, int 
 /* Full forward of one request: probabilities [n_cand*3] (click, cart, purchase),
  * optionally the pre-sigmoid logits [n_cand*3]. */
 int oracle_model_forward(const OrModel* m, const OrSample* s, double* probs, double* logits);
+
+/* Full forward with MoE routing control: forced_sel (NULL = route) holds, layer after layer,
+ * l_q[l] x moe_topk expert ids to use instead of the oracle's own selection (combine weights
+ * still come from the oracle's raw scores of those experts); out_sel (same layout) receives
+ * the selection used and out_margin (l_q[l] per layer) the gap between the k-th and
+ * (k+1)-th biased score (+inf when k == E). Any of the three may be NULL. */
+int oracle_model_forward_moe(const OrModel* m, const OrSample* s, const int* forced_sel, double* probs,
+                             double* logits, int* out_sel, double* out_margin);
+
+/* --- MoE FFN operators -------------------------------- */
+/* route_topk, DeepSeek style: s_e = sigmoid(x . router[:, e]); selection = top-k of s_e + bias_e
+ * in descending order, ties -> lower index; weights w_j = s_{e_j} / sum_j s_{e_j} (bias never
+ * enters the weights). router [d, E] row-major. sel/w [rows, k]; margin [rows] (may be NULL). */
+int oracle_moe_route(const double* x, int rows, int d, int n_experts, int k, const double* router,
+                     const double* bias, int* sel, double* w, double* margin);
+/* moe_forward: out = sum_{shared} swishglu_s(x) + sum_j w_j swishglu_{e_j}(x). Expert weights
+ * stacked over (n_experts + shared) experts, shared last: w_gate/w_up [n, d, m], w_down [n, m, d].
+ * forced_sel [rows, k] or NULL. */
+int oracle_moe_ffn(const double* x, int rows, int d, int m, int n_experts, int k, int shared,
+                   const double* router, const double* bias, const double* w_gate, const double* w_up,
+                   const double* w_down, const int* forced_sel, double* out, int* sel, double* w);
+/* update_balance, DeepSeek style: bias_e -= gamma * sign(load_e - mean load). */
+int oracle_moe_update_bias(const int64_t* load, int n_experts, double gamma, double* bias);
 
 /* Per-layer structural artifacts of one request: for each layer l,
  * l_q[l], visible count[l], and query_rows concatenated. */

@@ -72,6 +72,11 @@ class SortConfig:
     qknorm: bool = True
     gate: bool = True
     rope_theta: float = 10000.0
+    # DeepSeek-style MoE FFN; moe_experts = 0 -> dense SwishGLU
+    moe_experts: int = 0
+    moe_topk: int = 1
+    moe_shared: int = 1
+    moe_ffn_dim: int = 0
     # mask / pruning
     local_window: int = 32
     full_suffix: int = 128

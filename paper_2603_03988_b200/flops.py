@@ -22,7 +22,11 @@ def forward_flops(cfg: SortConfig) -> dict:
     for p in layer_plans(cfg):
         lp = 2 * (3 * p.l_q * d * d + 2 * p.l_kv * d * d)   # Q, G, O on queries; K, V on kv rows
         la = 4 * dk * h * p.visible                          # QK^T + PV over visible entries
-        lf = 2 * 3 * p.l_q * d * m                           # gate, up, down
+        if cfg.moe_experts > 0:  # activated experts only (k routed + shared) + fp32 router
+            lf = 2 * 3 * p.l_q * d * cfg.moe_ffn_dim * (cfg.moe_topk + cfg.moe_shared) \
+                + 2 * p.l_q * d * cfg.moe_experts
+        else:
+            lf = 2 * 3 * p.l_q * d * m                       # gate, up, down
         layers.append({"proj": lp, "attn": la, "ffn": lf, "visible_per_head": p.visible,
                        "l_q": p.l_q, "l_kv": p.l_kv})
         proj, attn, ffn = proj + lp, attn + la, ffn + lf

@@ -86,9 +86,19 @@ def param_shapes(cfg: SortConfig) -> Dict[str, tuple]:
         s[f"attn.{l}.qk_gain_k"] = (cfg.heads, cfg.head_dim)
         s[f"block.{l}.attn_norm"] = (1, d)
         s[f"block.{l}.ffn_norm"] = (1, d)
-        s[f"ffn.{l}.w_gate"] = (d, m)
-        s[f"ffn.{l}.w_up"] = (d, m)
-        s[f"ffn.{l}.w_down"] = (m, d)
+        if cfg.moe_experts > 0:
+            E, me = cfg.moe_experts, cfg.moe_ffn_dim
+            s[f"ffn.{l}.router"] = (d, E)
+            s[f"ffn.{l}.router_bias"] = (1, E)
+            names = [f"expert.{e}" for e in range(E)] + (["shared"] if cfg.moe_shared else [])
+            for x in names:
+                s[f"ffn.{l}.{x}.w_gate"] = (d, me)
+                s[f"ffn.{l}.{x}.w_up"] = (d, me)
+                s[f"ffn.{l}.{x}.w_down"] = (me, d)
+        else:
+            s[f"ffn.{l}.w_gate"] = (d, m)
+            s[f"ffn.{l}.w_up"] = (d, m)
+            s[f"ffn.{l}.w_down"] = (m, d)
     return s
 
 
@@ -109,6 +119,8 @@ def make_params(cfg: SortConfig, seed: int = 7, init: str = "fanin") -> Dict[str
         elif leaf.startswith("g_") or leaf in ("attn_norm", "ffn_norm", "gain") \
                 or leaf.startswith("qk_gain"):
             a = 1.0 + 0.1 * rng.normal(size=(r, c))
+        elif leaf == "router_bias":  # balancing state; small and non-trivial for parity
+            a = 0.05 * rng.normal(size=(r, c))
         elif leaf.startswith("b"):
             a = 0.1 * rng.normal(size=(r, c))
         else:
