@@ -66,6 +66,12 @@ typedef struct {
   int32_t keep[SORT_MAX_LAYERS]; /* per-layer non-candidate keep counts */
   int32_t keep_specials;
   int32_t max_batch, n_hist, n_cand; /* batch geometry the workspace is planned for */
+  /* DeepSeek-style MoE FFN in every block instead of the dense SwishGLU:
+   * moe_experts routed experts (0 = dense FFN), moe_topk active per token, moe_shared
+   * always-on shared experts (0 or 1), moe_ffn_dim intermediate size of every expert.
+   * Parameters ffn.<l>.router [d, E], ffn.<l>.router_bias [1, E],
+   * ffn.<l>.expert.<e>.w_gate|w_up [d, m_e] / w_down [m_e, d], ffn.<l>.shared.* likewise. */
+  int32_t moe_experts, moe_topk, moe_shared, moe_ffn_dim;
 } SortConfig;
 
 /* A batch of requests in structure-of-arrays form (RequestSample, data.hpp:32-38,
@@ -233,6 +239,23 @@ int sort_dataset_batch(SortDataset d, int64_t first, int32_t count, int32_t n_hi
  * GEMM as CTA pairs, default 0 for the same reason); "attn_bwd_mma" (1 = tensor-core
  * attention backward, the default; 0 = the fp32 SIMT kernels). Status 1 on an unknown name. */
 int sort_set_option(SortHandle h, const char* name, int32_t value);
+
+/* ---- MoE FFN (config fields moe_*) ------------------------------------
+ * Routing of layer `layer` in the last forward: sel/weights [rows, moe_topk] host buffers
+ * (either may be NULL), rows = batch * l_q(layer) in the forward's row order; selection in
+ * descending biased score, weights = renormalised raw sigmoid scores (route_topk,
+ * SPEC.md:305-315). */
+int sort_moe_routing(SortHandle h, int layer, int32_t* sel, float* weights);
+/* Expert-load histogram [moe_experts] of layer `layer` in the last forward (update_balance
+ * input). */
+int sort_moe_load(SortHandle h, int layer, int64_t* load);
+/* update_balance, DeepSeek style, on every layer from the last forward's loads:
+ * router_bias_e -= gamma * sign(load_e - mean load) (gamma = 1e-3 default). */
+int sort_moe_update_bias(SortHandle h, double gamma);
+/* Op-level entry (moe_forward, SPEC.md:316-324 inside the block residual):
+ * out = x + MoE(RMSNorm(x; block.<layer>.ffn_norm)) for `rows` host rows [rows, d], x rounded
+ * to bf16 first (the residual stream's type), out read back from bf16. */
+int sort_moe_forward(SortHandle h, int layer, const float* x, int rows, float* out);
 
 #ifdef __cplusplus
 }

@@ -142,6 +142,15 @@ def base_config(**kw) -> SortConfig:
     return dataclasses.replace(c, **kw)
 
 
+def base_moe_config(**kw) -> SortConfig:
+    """SURVEY.md section 8(f) "next 1": SORT-base with the DeepSeek-style MoE FFN at the paper's
+    best sparsity 1/8: 8 routed experts, top-1, one shared expert, expert width
+    ffn_dim / 2 = 320 so the activated FFN width (shared + routed) equals the dense 640 (the
+    spec's sizing rule)."""
+    c = base_config(moe_experts=8, moe_topk=1, moe_shared=1, moe_ffn_dim=320)
+    return dataclasses.replace(c, **kw)
+
+
 def large_config(**kw) -> SortConfig:
     """BASELINE.json configs[3]: SORT-large, 12 layers, d=1024, 16 heads, 4096 history,
     W=256, 128 targets, geometric schedule (mask.cpp:97-117)."""

@@ -21,9 +21,24 @@
 // The weight slice of a CTA stays resident in shared memory (weight-stationary).
 #pragma once
 
+#include <type_traits>
+
 #include "ptx.cuh"
 
 namespace sortk {
+
+// Grouped mode (MoE experts): an epilogue declaring `kGrouped = true` carries
+//   const int32_t* tile_group;  // group (expert) of every 128-row m-block
+//   const int32_t* num_tiles;   // number of m-blocks (device-side, written by the router)
+//   int group_n;                // weight rows per group in the stacked B operand
+// The A rows of each group are contiguous and padded to 128, so an m-block belongs to one
+// group; B stacks the groups' [N, K] weights. A CTA keeps two weight slices resident and
+// reloads one whenever its next m-block belongs to a new group (the next group's slice
+// streams in while the MMA still works on the current one).
+template <class E, class = void>
+struct is_grouped : std::false_type {};
+template <class E>
+struct is_grouped<E, std::void_t<decltype(E::kGrouped)>> : std::bool_constant<E::kGrouped> {};
 
 constexpr int kGemmBM = 128;
 constexpr int kGemmBK = 64;
@@ -51,12 +66,13 @@ struct GemmPlan {
   uint32_t b_bytes, smem_bytes;
 };
 
-__host__ __device__ inline GemmPlan gemm_plan(int K, int BN, uint32_t side_buf_bytes = 0, int ncta = 1) {
+__host__ __device__ inline GemmPlan gemm_plan(int K, int BN, uint32_t side_buf_bytes = 0, int ncta = 1,
+                                              int b_bufs = 1) {
   GemmPlan p;
   p.BN = BN;
   p.num_k = (K + kGemmBK - 1) / kGemmBK;
   p.b_bytes = static_cast<uint32_t>(BN / ncta) * kGemmBK * 2 * p.num_k;  // this CTA's weight share
-  const uint32_t fixed = 1024 + p.b_bytes + kGemmEpiSmem + 2 * side_buf_bytes + 256;
+  const uint32_t fixed = 1024 + b_bufs * p.b_bytes + kGemmEpiSmem + 2 * side_buf_bytes + 256;
   int st = fixed < kGemmSmemMax ? static_cast<int>((kGemmSmemMax - fixed) / kGemmABytes) : 0;
   p.a_stages = st > 8 ? 8 : st;
   p.smem_bytes = fixed + p.a_stages * kGemmABytes;
@@ -77,6 +93,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmR,
                 int M, int N, int K, int BN, int a_stages, Epi epi) {
   constexpr int kNcta = kPair ? 2 : 1;
+  constexpr bool kGroup = is_grouped<Epi>::value;
+  static_assert(!(kGroup && kPair), "grouped GEMM runs as single CTAs");
   constexpr int kSide = Epi::kSide;
   constexpr uint32_t kSideBuf = side_bytes(Epi::kSide, Epi::kRopeFloats);
   constexpr int kRopeBoxFloats = Epi::kRopeFloats < 64 ? Epi::kRopeFloats : 64;  // fp16 per box row
@@ -85,8 +103,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint8_t* smem = align_smem_1k(smem_raw);
   const int num_k = (K + kGemmBK - 1) / kGemmBK;
   const uint32_t b_box = static_cast<uint32_t>(BN / kNcta) * kGemmBK * 2;
+  const uint32_t b_slice = b_box * num_k;  // one resident weight slice
   uint8_t* sB = smem;
-  uint8_t* sA = sB + b_box * num_k;
+  uint8_t* sA = sB + b_slice * (kGroup ? 2 : 1);
   uint8_t* sEpi = sA + a_stages * kGemmABytes;
   uint8_t* sSide = sEpi + kGemmEpiSmem;  // 2 x kSideBuf (1024-aligned)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sSide + 2 * kSideBuf);
@@ -97,14 +116,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* b_full = bars + 20;
   uint64_t* side_full = bars + 21;   // [2]
   uint64_t* side_empty = bars + 23;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 25);
+  uint64_t* gb_full = bars + 25;   // [2] grouped: weight slice slot s loaded
+  uint64_t* gb_empty = bars + 27;  // [2] grouped: weight slice slot s released by the MMA
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 29);
 
   const int warp = warp_id();
   const int lane = lane_id();
   const uint32_t rank = kPair ? cluster_rank() : 0u;
   const int unit = kPair ? static_cast<int>(blockIdx.x) / 2 : static_cast<int>(blockIdx.x);
   const int units = kPair ? static_cast<int>(gridDim.x) / 2 : static_cast<int>(gridDim.x);
-  const int num_m = (M + kGemmBM * kNcta - 1) / (kGemmBM * kNcta);  // m-blocks of 128 (256 as a pair)
+  int num_m = (M + kGemmBM * kNcta - 1) / (kGemmBM * kNcta);  // m-blocks of 128 (256 as a pair)
+  if constexpr (kGroup) num_m = *epi.num_tiles;
   const int num_n = N / BN;
   const int nb = unit % num_n;
   const int m_first = unit / num_n;
@@ -130,6 +152,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&side_full[i], 1);
       mbar_init(&side_empty[i], 32 * kGemmEpiWarps);
+      mbar_init(&gb_full[i], 1);
+      mbar_init(&gb_empty[i], 1);
     }
     mbar_fence_init();
   }
@@ -163,13 +187,29 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      if (rank == 0) mbar_arrive_expect_tx(b_full, b_box * num_k * kNcta);
-      for (int kb = 0; kb < num_k; ++kb)
-        load_ab(sB + kb * b_box, &tmB, b_full, kb * kGemmBK, nb * BN + static_cast<int>(rank) * (BN / kNcta));
+      if constexpr (!kGroup) {
+        if (rank == 0) mbar_arrive_expect_tx(b_full, b_box * num_k * kNcta);
+        for (int kb = 0; kb < num_k; ++kb)
+          load_ab(sB + kb * b_box, &tmB, b_full, kb * kGemmBK, nb * BN + static_cast<int>(rank) * (BN / kNcta));
+      }
       int s = 0;
       uint32_t ph = 0;
       int t = 0;
+      int cur_g = -1, n_loads = 0;
       for (int mb = m_first; mb < num_m; mb += m_step, ++t) {
+        if constexpr (kGroup) {  // this m-block's group weights: reload on a group change
+          const int g = epi.tile_group[mb];
+          if (g != cur_g) {
+            const int slot = n_loads & 1;
+            if (n_loads >= 2) mbar_wait_sleep(&gb_empty[slot], ((n_loads >> 1) - 1) & 1);
+            mbar_arrive_expect_tx(&gb_full[slot], b_slice);
+            for (int kb = 0; kb < num_k; ++kb)
+              tma_load_2d(sB + slot * b_slice + kb * b_box, &tmB, &gb_full[slot], kb * kGemmBK,
+                          g * epi.group_n + nb * BN);
+            cur_g = g;
+            ++n_loads;
+          }
+        }
         if constexpr (kSide != 0) {  // this tile's per-row side data
           const int sb = t & 1;
           uint8_t* dst = sSide + sb * kSideBuf;
@@ -198,12 +238,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
       const uint32_t idesc = umma_idesc_bf16(kGemmBM * kNcta, BN);
-      const uint32_t b0 = smem_u32(sB);
-      mbar_wait_sleep(b_full, 0);
+      uint32_t b0 = smem_u32(sB);
+      if constexpr (!kGroup) mbar_wait_sleep(b_full, 0);
       int s = 0;
       uint32_t ph = 0;
       int t = 0;
+      int cur_g = -1, n_loads = 0;
       for (int mb = m_first; mb < num_m; mb += m_step, ++t) {
+        if constexpr (kGroup) {
+          const int g = epi.tile_group[mb];
+          if (g != cur_g) {
+            if (n_loads > 0) mma_commit(&gb_empty[(n_loads - 1) & 1]);  // previous slice free once its MMAs retire
+            const int slot = n_loads & 1;
+            mbar_wait_sleep(&gb_full[slot], (n_loads >> 1) & 1);
+            b0 = smem_u32(sB + slot * b_slice);
+            cur_g = g;
+            ++n_loads;
+          }
+        }
         const int acc = t & 1;
         const uint32_t acc_ph = (t >> 1) & 1;
         mbar_wait_sleep(&tempty[acc], acc_ph ^ 1);

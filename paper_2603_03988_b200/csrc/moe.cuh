@@ -1,0 +1,365 @@
+// SPDX-License-Identifier: Apache-2.0
+// DeepSeek-style MoE FFN on the SORT-base residual stream.
+//
+//   x1 [T, d] bf16 (after the attention residual)
+//   -> k_moe_route    fp32 RMSNorm(x1; ffn_norm), router logits z = xf . W_r (fp32),
+//                     s = sigmoid(z), top-k of s + bias (ties -> lower index), w = s / sum_sel s,
+//                     per-expert token counts
+//   -> k_moe_plan     expert segments padded to 128 rows, m-block -> expert list
+//   -> k_moe_scatter  bf16 RMSNorm rows into their expert segments (shared expert: every row)
+//   -> grouped tcgen05 GEMM [gate | up] with the SwishGLU epilogue -> h [P, m_e]
+//   -> grouped tcgen05 GEMM down, epilogue scales by the combine weight -> y [P, d] fp32
+//   -> k_moe_combine  x1 + y_shared + sum_j y_j (fixed order) -> bf16 residual + row statistics
+// Every row's arithmetic is independent of where the scatter put it, so the output is
+// deterministic even though segment order within an expert follows atomic arrival.
+#pragma once
+
+#include "epilogues.cuh"
+#include "gemm.cuh"
+#include "train.cuh"
+
+namespace sortk {
+
+constexpr int kErrMoeNonFinite = 2;  // err[0] bit; err[1] = 1 + first offending token
+constexpr int kMoeMaxExperts = 64;
+constexpr int kMoeMaxK = 8;
+
+// ---------------------------------------------------------------------------------- router
+// One warp per token (grid-stride), lane owns 8 contiguous columns (d <= 256, d % 8 == 0).
+__global__ void __launch_bounds__(256) k_moe_route(const __nv_bfloat16* __restrict__ x, int T, int d,
+                                                   const float* __restrict__ gain, const float* __restrict__ router,
+                                                   const float* __restrict__ bias, int E, int k,
+                                                   int32_t* __restrict__ sel, float* __restrict__ wgt,
+                                                   float* __restrict__ inv_out, int32_t* __restrict__ counts,
+                                                   int32_t* __restrict__ err) {
+  extern __shared__ float smem_f[];
+  float* wr = smem_f;  // router transposed [E][d]
+  __shared__ int hist[kMoeMaxExperts];
+  for (int i = threadIdx.x; i < d * E; i += blockDim.x) {
+    const int c = i / E, e = i - c * E;
+    wr[e * d + c] = router[i];
+  }
+  for (int i = threadIdx.x; i < E; i += blockDim.x) hist[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int c0 = lane * 8;
+  const bool act = c0 < d;
+  float g[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) g[i] = act ? gain[c0 + i] : 0.f;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  for (int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < T; t += warps) {
+    float v[8];
+    if (act) {
+      const int4 raw = *reinterpret_cast<const int4*>(x + static_cast<size_t>(t) * d + c0);
+      const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(p2[i]);
+        v[2 * i] = f.x;
+        v[2 * i + 1] = f.y;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = 0.f;
+    }
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ss = fmaf(v[i], v[i], ss);
+    const float inv = rsqrtf(warp_sum(ss) / static_cast<float>(d) + 1e-6f);  // norm.hpp:23-24
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] *= inv * g[i];
+    // router scores in fp32; after the butterfly every lane holds every expert's score
+    float best_b[kMoeMaxK], best_s[kMoeMaxK];
+    int best_e[kMoeMaxK];
+#pragma unroll
+    for (int j = 0; j < kMoeMaxK; ++j) {
+      best_b[j] = -INFINITY;
+      best_s[j] = 0.f;
+      best_e[j] = -1;
+    }
+    for (int e = 0; e < E; ++e) {
+      float z = 0.f;
+      if (act) {
+        const float4 a = *reinterpret_cast<const float4*>(wr + e * d + c0);
+        const float4 b = *reinterpret_cast<const float4*>(wr + e * d + c0 + 4);
+        z = v[0] * a.x + v[1] * a.y + v[2] * a.z + v[3] * a.w + v[4] * b.x + v[5] * b.y + v[6] * b.z + v[7] * b.w;
+      }
+      z = warp_sum(z);
+      const float sc = 1.f / (1.f + expf(-z));  // sigmoid gate
+      const float bs = sc + bias[e];
+      // insert into the running top-k (descending biased score; strict > keeps the lower
+      // index ahead on ties since experts arrive in ascending order)
+      if (bs > best_b[k - 1]) {
+        int j = k - 1;
+        while (j > 0 && bs > best_b[j - 1]) {
+          best_b[j] = best_b[j - 1];
+          best_s[j] = best_s[j - 1];
+          best_e[j] = best_e[j - 1];
+          --j;
+        }
+        best_b[j] = bs;
+        best_s[j] = sc;
+        best_e[j] = e;
+      }
+    }
+    if (lane == 0) {
+      float tot = 0.f;
+      for (int j = 0; j < k; ++j) {
+        if (best_e[j] < 0) {  // non-finite router score: flag it, keep indices in range
+          atomicOr(err, kErrMoeNonFinite);
+          atomicCAS(err + 1, 0, t + 1);
+          best_e[j] = 0;
+          best_s[j] = 1.f;
+        }
+        tot += best_s[j];
+      }
+      for (int j = 0; j < k; ++j) {
+        sel[static_cast<size_t>(t) * k + j] = best_e[j];
+        wgt[static_cast<size_t>(t) * k + j] = best_s[j] / tot;
+        atomicAdd(&hist[best_e[j]], 1);
+      }
+      inv_out[t] = inv;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < E; i += blockDim.x)
+    if (hist[i]) atomicAdd(&counts[i], hist[i]);
+}
+
+// ------------------------------------------------------------------------------------ plan
+// One block: group g (E routed + shared) gets rows [off[g], off[g] + 128 * ceil(count / 128));
+// its m-blocks are listed in tile_group; padding rows get tok_of = -1. cursors reset.
+__global__ void k_moe_plan(const int32_t* __restrict__ counts, int E, int shared, int T, int32_t* __restrict__ off,
+                           int32_t* __restrict__ cursor, int32_t* __restrict__ tile_group,
+                           int32_t* __restrict__ num_tiles, int32_t* __restrict__ tok_of) {
+  __shared__ int s_off[kMoeMaxExperts + 2], s_cnt[kMoeMaxExperts + 1];
+  const int G = E + shared;
+  if (threadIdx.x == 0) {
+    int o = 0;
+    for (int g = 0; g < G; ++g) {
+      const int c = g < E ? counts[g] : T;
+      s_cnt[g] = c;
+      s_off[g] = o;
+      o += (c + 127) / 128 * 128;
+    }
+    s_off[G] = o;
+    *num_tiles = o / 128;
+  }
+  __syncthreads();
+  for (int g = threadIdx.x; g < G; g += blockDim.x) {
+    off[g] = s_off[g];
+    cursor[g] = 0;
+  }
+  for (int g = 0; g < G; ++g) {
+    const int t0 = s_off[g] / 128, t1 = s_off[g + 1] / 128;
+    for (int i = t0 + threadIdx.x; i < t1; i += blockDim.x) tile_group[i] = g;
+    for (int r = s_off[g] + s_cnt[g] + threadIdx.x; r < s_off[g + 1]; r += blockDim.x) tok_of[r] = -1;
+  }
+}
+
+// --------------------------------------------------------------------------------- scatter
+// A warp takes 32 tokens: positions come from one warp-aggregated atomic per (slot, expert),
+// then the warp writes each token's normalised bf16 row into its k (+ shared) segments.
+__global__ void __launch_bounds__(256) k_moe_scatter(const __nv_bfloat16* __restrict__ x, int T, int d,
+                                                     const float* __restrict__ gain, const float* __restrict__ inv,
+                                                     const int32_t* __restrict__ sel, const float* __restrict__ wgt,
+                                                     int E, int k, int shared, const int32_t* __restrict__ off,
+                                                     int32_t* __restrict__ cursor, __nv_bfloat16* __restrict__ xs,
+                                                     int32_t* __restrict__ tok_of, float* __restrict__ w_of,
+                                                     int32_t* __restrict__ slot_pos) {
+  const int lane = threadIdx.x & 31;
+  const int S = k + shared;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  const int c0 = lane * 8;
+  const bool act = c0 < d;
+  float g[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) g[i] = act ? gain[c0 + i] : 0.f;
+  for (int base = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < T; base += warps * 32) {
+    const int t = base + lane;
+    const bool tv = t < T;
+    int pos[kMoeMaxK + 1];
+    for (int j = 0; j < k; ++j) {
+      const int e = tv ? sel[static_cast<size_t>(t) * k + j] : -1 - lane;  // invalid lanes never match
+      const unsigned peers = __match_any_sync(0xffffffffu, e);
+      const int leader = __ffs(peers) - 1;
+      int b = 0;
+      if (lane == leader && tv) b = atomicAdd(&cursor[e], __popc(peers));
+      b = __shfl_sync(0xffffffffu, b, leader);
+      pos[j] = tv ? off[e] + b + __popc(peers & ((1u << lane) - 1u)) : 0;
+    }
+    if (shared) pos[k] = off[E] + t;
+    if (tv) {
+      for (int j = 0; j < S; ++j) {
+        tok_of[pos[j]] = t;
+        w_of[pos[j]] = j < k ? wgt[static_cast<size_t>(t) * k + j] : 1.f;
+        slot_pos[static_cast<size_t>(t) * S + j] = pos[j];
+      }
+    }
+    // rows: token by token, the whole warp moves one d-wide row (16 B per lane)
+    const int n = min(32, T - base);
+    for (int i = 0; i < n; ++i) {
+      const int tt = base + i;
+      int pj[kMoeMaxK + 1];
+      for (int j = 0; j < S; ++j) pj[j] = __shfl_sync(0xffffffffu, pos[j], i);
+      if (!act) continue;
+      const float iv = inv[tt];
+      const int4 raw = *reinterpret_cast<const int4*>(x + static_cast<size_t>(tt) * d + c0);
+      const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+      uint32_t o[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = __bfloat1622float2(p2[q]);
+        o[q] = pack_bf16x2(f.x * iv * g[2 * q], f.y * iv * g[2 * q + 1]);
+      }
+      const int4 ov = make_int4(o[0], o[1], o[2], o[3]);
+      for (int j = 0; j < S; ++j) *reinterpret_cast<int4*>(xs + static_cast<size_t>(pj[j]) * d + c0) = ov;
+    }
+  }
+}
+
+// --------------------------------------------------------------------------------- combine
+// x_out = bf16(x1 + y_shared + sum_j y_j) in place, with the row's sum-of-squares partials
+// per 64-column block (the EpiResid layout the next layer's GEMMs read).
+__global__ void __launch_bounds__(256) k_moe_combine(__nv_bfloat16* __restrict__ x, int T, int d,
+                                                     const float* __restrict__ ys, const int32_t* __restrict__ slot_pos,
+                                                     int k, int shared, float4* __restrict__ ss_out) {
+  const int lane = threadIdx.x & 31;
+  const int S = k + shared;
+  const int c0 = lane * 8;
+  const bool act = c0 < d;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  for (int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < T; t += warps) {
+    float acc[8];
+    __nv_bfloat16* xr = x + static_cast<size_t>(t) * d + c0;
+    if (act) {
+      const int4 raw = *reinterpret_cast<const int4*>(xr);
+      const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = __bfloat1622float2(p2[q]);
+        acc[2 * q] = f.x;
+        acc[2 * q + 1] = f.y;
+      }
+      // shared expert first, then the routed experts in selection order
+      for (int jj = 0; jj < S; ++jj) {
+        const int j = shared ? (jj == 0 ? k : jj - 1) : jj;
+        const float* yr = ys + static_cast<size_t>(slot_pos[static_cast<size_t>(t) * S + j]) * d + c0;
+        const float4 a = *reinterpret_cast<const float4*>(yr);
+        const float4 b = *reinterpret_cast<const float4*>(yr + 4);
+        acc[0] += a.x;
+        acc[1] += a.y;
+        acc[2] += a.z;
+        acc[3] += a.w;
+        acc[4] += b.x;
+        acc[5] += b.y;
+        acc[6] += b.z;
+        acc[7] += b.w;
+      }
+    }
+    float ss = 0.f;
+    if (act) {
+      uint32_t o[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        o[q] = pack_bf16x2(acc[2 * q], acc[2 * q + 1]);
+        const float2 y = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&o[q]));
+        ss = fmaf(y.x, y.x, fmaf(y.y, y.y, ss));
+      }
+      *reinterpret_cast<int4*>(xr) = make_int4(o[0], o[1], o[2], o[3]);
+    }
+    // 64-column blocks = groups of 8 lanes
+    ss += __shfl_xor_sync(0xffffffffu, ss, 4);
+    ss += __shfl_xor_sync(0xffffffffu, ss, 2);
+    ss += __shfl_xor_sync(0xffffffffu, ss, 1);
+    const float s1 = __shfl_sync(0xffffffffu, ss, 8), s2 = __shfl_sync(0xffffffffu, ss, 16),
+                s3 = __shfl_sync(0xffffffffu, ss, 24);
+    if (lane == 0) {
+      const int nb = (d + 63) / 64;
+      ss_out[t] = make_float4(ss, nb > 1 ? s1 : 0.f, nb > 2 ? s2 : 0.f, nb > 3 ? s3 : 0.f);
+    }
+  }
+}
+
+// update_balance (DeepSeek style): bias_e -= gamma * sign(load_e - mean load) per layer.
+__global__ void k_moe_update_bias(const int32_t* __restrict__ counts, int E, float gamma, float* __restrict__ bias) {
+  const int e = threadIdx.x;
+  if (e >= E) return;
+  float mean = 0.f;
+  for (int i = 0; i < E; ++i) mean += static_cast<float>(counts[i]);
+  mean /= static_cast<float>(E);
+  const float dl = static_cast<float>(counts[e]) - mean;
+  bias[e] -= gamma * (dl > 0.f ? 1.f : (dl < 0.f ? -1.f : 0.f));
+}
+
+// ------------------------------------------------------------------------------- epilogues
+// Expert [gate | up] GEMM on normalised rows: the stacked B interleaves 32-column blocks
+// [gate_j | up_j] per expert, so a 64-column chunk holds 32 hidden units: h = swish(g) * u.
+struct EpiMoeGU {
+  static constexpr int kChunk = 64;
+  static constexpr int kMaxParts = 1 << 30;
+  static constexpr int kSide = 0;
+  static constexpr int kRopeFloats = 0;
+  static constexpr bool kGrouped = true;
+  const int32_t* tile_group;
+  const int32_t* num_tiles;
+  int group_n;
+  const int32_t* tok_of;
+  __nv_bfloat16* hidden;
+  int m;
+
+  __device__ __forceinline__ void prologue(uint8_t*, int, int) const {}
+
+  template <class Wait>
+  __device__ __forceinline__ void run(uint8_t*, uint8_t*, Wait&& wait, uint32_t tbase, int row, int n0, int c0,
+                                      int c1, bool valid, int, int) const {
+    const bool live = valid && tok_of[row] >= 0;
+    wait();
+    for (int c = c0; c < c1; c += 64) {
+      float v[64];
+      tmem_row_chunk<64>(tbase + c, v);
+      if (!live) continue;
+      float h[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) h[i] = v[i] * fast_sigmoid(v[i]) * v[32 + i];  // common.hpp:37
+      store_bf16_row(hidden + static_cast<size_t>(row) * m + (n0 + c) / 2, h, 32);
+    }
+  }
+};
+
+// Expert down GEMM: y[row] = w_row * acc (fp32), w = the row's combine weight.
+struct EpiMoeDown {
+  static constexpr int kChunk = 32;
+  static constexpr int kMaxParts = 1 << 30;
+  static constexpr int kSide = 0;
+  static constexpr int kRopeFloats = 0;
+  static constexpr bool kGrouped = true;
+  const int32_t* tile_group;
+  const int32_t* num_tiles;
+  int group_n;
+  const int32_t* tok_of;
+  const float* w_of;
+  float* y;
+  int d;
+
+  __device__ __forceinline__ void prologue(uint8_t*, int, int) const {}
+
+  template <class Wait>
+  __device__ __forceinline__ void run(uint8_t*, uint8_t*, Wait&& wait, uint32_t tbase, int row, int n0, int c0,
+                                      int c1, bool valid, int, int) const {
+    const bool live = valid && tok_of[row] >= 0;
+    const float w = live ? w_of[row] : 0.f;
+    wait();
+    for (int c = c0; c < c1; c += 32) {
+      float v[32];
+      tmem_row_chunk<32>(tbase + c, v);
+      if (!live) continue;
+      float4* o = reinterpret_cast<float4*>(y + static_cast<size_t>(row) * d + n0 + c);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = make_float4(w * v[4 * i], w * v[4 * i + 1], w * v[4 * i + 2], w * v[4 * i + 3]);
+    }
+  }
+};
+
+}  // namespace sortk

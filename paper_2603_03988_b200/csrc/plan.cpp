@@ -209,6 +209,15 @@ void validate_config(const SortConfig& c) {
   for (int l = 0; l < c.layers; ++l) need(c.keep[l] >= 1, "PruneSchedule: keep counts must be >= 1");
   need(c.n_cand >= 1, "tokenizer: sample has zero candidates");
   need(c.n_hist >= 0 && c.max_batch >= 1, "batch geometry");
+  // MoE FFN: SparsityConfig invariants 1 <= k <= E
+  need(c.moe_experts >= 0 && c.moe_experts <= 64, "unsupported: moe_experts must be in [0, 64]");
+  if (c.moe_experts > 0) {
+    need(c.moe_topk >= 1 && c.moe_topk <= c.moe_experts, "SparsityConfig: need 1 <= k <= E");
+    need(c.moe_topk <= 8, "unsupported: moe_topk > 8");
+    need(c.moe_shared == 0 || c.moe_shared == 1, "unsupported: moe_shared must be 0 or 1");
+    need(c.moe_ffn_dim >= 64 && c.moe_ffn_dim % 64 == 0, "unsupported: moe_ffn_dim must be a multiple of 64");
+    need(c.model_dim <= 256, "unsupported: the MoE FFN runs on the tcgen05 path (model_dim <= 256)");
+  }
 }
 
 Plan make_plan(const SortConfig& c) {

@@ -22,6 +22,7 @@
 #include "tokenizer.cuh"
 #include "train.cuh"
 #include "generic.cuh"
+#include "moe.cuh"
 
 namespace sortk {
 
@@ -58,6 +59,15 @@ struct LayerDev {
   CUtensorMap tmWo_t, tmWup_t, tmWdown_t;  // k_block_tail weight stages
   CUtensorMap tmWo_p, tmWup_p, tmWdown_p;  // ... as a CTA pair (each CTA loads half the rows)
   CUtensorMap tmB_all_p, tmB_kv_p, tmB_qg_p;  // QKVG weight slices as a CTA pair (BN/2 rows)
+  // MoE FFN: stacked expert weights (routed experts, then the shared one), router in the
+  // fp32 master buffer, this layer's routing of the last forward
+  __nv_bfloat16 *w_moe_gu = nullptr, *w_moe_down = nullptr;
+  CUtensorMap tmB_moe_gu, tmB_moe_down;
+  int bn_moe_gu = 0, bn_moe_down = 0;
+  const float* router = nullptr;
+  float* router_bias = nullptr;
+  int32_t* moe_sel = nullptr;
+  float* moe_w = nullptr;
 };
 
 struct Handle {
@@ -74,6 +84,15 @@ struct Handle {
   bool attn_bwd_mma = true; // sort_set_option("attn_bwd_mma"): tensor-core attention backward
   bool qkvg_pair = false;   // sort_set_option("qkvg_pair"): QKVG projection as CTA pairs
   bool generic = false;    // d > 256 (SORT-large): projections through the generic path
+  // ---- MoE FFN: routed + shared experts as grouped tcgen05 GEMMs
+  bool moe = false;
+  int moe_E = 0, moe_k = 0, moe_s = 0, moe_m = 0, moe_pmax = 0, moe_tiles_max = 0;
+  __nv_bfloat16 *moe_xs = nullptr, *moe_hs = nullptr;
+  float *moe_ys = nullptr, *moe_inv = nullptr, *moe_wof = nullptr;
+  int32_t *moe_tok = nullptr, *moe_slot = nullptr, *moe_off = nullptr, *moe_cursor = nullptr,
+          *moe_tile_group = nullptr, *moe_ntiles = nullptr, *moe_counts = nullptr;  // counts [layers][E]
+  int moe_rows[SORT_MAX_LAYERS] = {0};  // rows routed per layer in the last forward
+  CUtensorMap tmA_moe_xs, tmA_moe_hs;
   // row-sharded item table (sort_set_item_table): the batch's item rows, gathered from the
   // owning ranks, replace the handle's table for the following calls
   const __nv_bfloat16* item_ext = nullptr;
@@ -220,7 +239,76 @@ static const CUtensorMap& rope_table(Handle& h, int R, const std::vector<int32_t
 
 // Shapes the fused block tail covers (TMEM: d accumulator + 2 x 128 hidden-chunk columns).
 static bool tail_supported(const Handle& h) {
-  return (h.d == 128 || h.d == 256) && h.m % 64 == 0 && h.m >= 64;
+  return !h.moe && (h.d == 128 || h.d == 256) && h.m % 64 == 0 && h.m >= 64;
+}
+
+// MoE layer weights: expert g (routed 0..E-1, then the shared expert) as
+//   [gate | up]: rows g*2m_e .. interleaving 32-column blocks [gate_j | up_j] (W^T, K = d)
+//   down:        rows g*d ..    W_down^T [d, m_e]
+// The expert input is the RMSNorm'd row itself (the router needs it in fp32 anyway), so the
+// ffn_norm gain is applied by the scatter kernel instead of being folded into the weights.
+static void build_moe_layer(Handle& h, int l, LayerDev& L) {
+  const int d = h.d, me = h.moe_m, G = h.moe_E + h.moe_s;
+  const std::string f = "ffn." + std::to_string(l) + ".";
+  need_param(h, f + "router", d, h.moe_E);
+  need_param(h, f + "router_bias", 1, h.moe_E);
+  std::vector<__nv_bfloat16> gu(static_cast<size_t>(G) * 2 * me * d), dn(static_cast<size_t>(G) * d * me);
+  for (int g = 0; g < G; ++g) {
+    const std::string X = g < h.moe_E ? f + "expert." + std::to_string(g) + "." : f + "shared.";
+    const HostParam& wg = need_param(h, X + "w_gate", d, me);
+    const HostParam& wu = need_param(h, X + "w_up", d, me);
+    const HostParam& wd = need_param(h, X + "w_down", me, d);
+    __nv_bfloat16* o = gu.data() + static_cast<size_t>(g) * 2 * me * d;
+    for (int j = 0; j < me / 32; ++j)
+      for (int i = 0; i < 64; ++i) {
+        const HostParam& src = i < 32 ? wg : wu;
+        const int col = 32 * j + (i & 31);
+        const size_t row = static_cast<size_t>(64 * j + i);
+        for (int k = 0; k < d; ++k) o[row * d + k] = f2bf(src.v[static_cast<size_t>(k) * me + col]);
+      }
+    const std::vector<__nv_bfloat16> t = transpose_bf16(wd, me, nullptr);
+    std::copy(t.begin(), t.end(), dn.begin() + static_cast<size_t>(g) * d * me);
+  }
+  L.w_moe_gu = h.upload(gu);
+  L.w_moe_down = h.upload(dn);
+  auto pick = [&](int N, int K, int chunk) {
+    for (int bn = 256; bn >= chunk; bn /= 2)
+      if (N % bn == 0 && bn % chunk == 0 && gemm_plan(K, bn, 0, 1, 2).a_stages >= 2) return bn;
+    throw ConfigError("unsupported MoE GEMM shape N=" + std::to_string(N) + " K=" + std::to_string(K));
+  };
+  L.bn_moe_gu = pick(2 * me, d, 64);
+  L.bn_moe_down = pick(d, me, 32);
+  L.tmB_moe_gu = make_tmap_2d(L.w_moe_gu, static_cast<uint64_t>(G) * 2 * me, d, d, L.bn_moe_gu, 64, 128);
+  L.tmB_moe_down = make_tmap_2d(L.w_moe_down, static_cast<uint64_t>(G) * d, me, me, L.bn_moe_down, 64, 128);
+  const size_t T = static_cast<size_t>(h.Bmax) * h.plan.layers[l].l_q;
+  L.moe_sel = h.dalloc<int32_t>(T * h.moe_k);
+  L.moe_w = h.dalloc<float>(T * h.moe_k);
+}
+
+// Token-major MoE workspace sized for the largest layer: P = T (k + s) rows + per-group padding.
+static void ensure_moe_buffers(Handle& h) {
+  int tq = 0;
+  for (const LayerPlan& lp : h.plan.layers) tq = std::max(tq, lp.l_q);
+  const size_t T = static_cast<size_t>(h.Bmax) * tq;
+  const int G = h.moe_E + h.moe_s, S = h.moe_k + h.moe_s;
+  h.moe_pmax = static_cast<int>(T * S + static_cast<size_t>(G) * 128);
+  h.moe_tiles_max = h.moe_pmax / 128;
+  const size_t P = h.moe_pmax;
+  h.moe_xs = h.dalloc<__nv_bfloat16>(P * h.d);
+  h.moe_hs = h.dalloc<__nv_bfloat16>(P * h.moe_m);
+  h.moe_ys = h.dalloc<float>(P * h.d);
+  h.moe_tok = h.dalloc<int32_t>(P);
+  h.moe_wof = h.dalloc<float>(P);
+  h.moe_slot = h.dalloc<int32_t>(T * S);
+  h.moe_inv = h.dalloc<float>(T);
+  h.moe_off = h.dalloc<int32_t>(G + 1);
+  h.moe_cursor = h.dalloc<int32_t>(G + 1);
+  h.moe_tile_group = h.dalloc<int32_t>(h.moe_tiles_max + 1);
+  h.moe_ntiles = h.dalloc<int32_t>(1);
+  h.moe_counts = h.dalloc<int32_t>(static_cast<size_t>(h.cfg.layers) * h.moe_E);
+  CK(cudaMemset(h.moe_counts, 0, static_cast<size_t>(h.cfg.layers) * h.moe_E * 4));
+  h.tmA_moe_xs = make_tmap_2d(h.moe_xs, P, h.d, h.d, 128, 64, 128);
+  h.tmA_moe_hs = make_tmap_2d(h.moe_hs, P, h.moe_m, h.moe_m, 128, 64, 128);
 }
 
 static void finalize(Handle& h) {
@@ -321,7 +409,8 @@ static void finalize(Handle& h) {
       L.w_qg = build({kSecQ, kSecG});
     }
     if (!h.generic) L.w_o = h.upload(transpose_bf16(need_param(h, a + "wo", d, d), d, nullptr));
-    if (!h.generic) {  // SwishGLU up: interleave 32-column blocks [gate_j | up_j], ffn pre-norm gain folded
+    if (h.moe) build_moe_layer(h, l, L);
+    if (!h.generic && !h.moe) {  // SwishGLU up: interleave 32-column blocks [gate_j | up_j], ffn pre-norm gain folded
       const HostParam& wg = need_param(h, f + "w_gate", d, m);
       const HostParam& wu = need_param(h, f + "w_up", d, m);
       std::vector<__nv_bfloat16> w(static_cast<size_t>(2) * m * d);
@@ -334,7 +423,7 @@ static void finalize(Handle& h) {
         }
       L.w_up = h.upload(w);
     }
-    if (!h.generic) L.w_down = h.upload(transpose_bf16(need_param(h, f + "w_down", m, d), m, nullptr));
+    if (!h.generic && !h.moe) L.w_down = h.upload(transpose_bf16(need_param(h, f + "w_down", m, d), m, nullptr));
     {
       const HostParam& gq = need_param(h, a + "qk_gain_q", H, dk);
       const HostParam& gk = need_param(h, a + "qk_gain_k", H, dk);
@@ -373,8 +462,10 @@ static void finalize(Handle& h) {
     L.bn_full = pick_bn(4 * d, d, 4 * dk, qkvg_side);
     L.bn_half = pick_bn(2 * d, d, 2 * dk, qkvg_side);
     L.bn_o = pick_bn(d, d, 32);
-    L.bn_up = pick_bn(2 * m, d, 64, side_bytes(1, 0));
-    L.bn_down = pick_bn(d, m, 32);
+    if (!h.moe) {
+      L.bn_up = pick_bn(2 * m, d, 64, side_bytes(1, 0));
+      L.bn_down = pick_bn(d, m, 32);
+    }
     // TMA descriptors (sized for max_batch; launches use the call's batch)
     const uint64_t Mkv = static_cast<uint64_t>(h.Bmax) * L.Rkv, Mq = static_cast<uint64_t>(h.Bmax) * L.Rq;
     L.tmA_in = make_tmap_2d(h.X[L.in_buf], Mkv, d, d, 128, 64, 128);
@@ -387,11 +478,11 @@ static void finalize(Handle& h) {
     L.tmB_kv_p = make_tmap_2d(L.w_kv, 2 * d, d, d, L.bn_half / 2, 64, 128);
     L.tmA_hg = make_tmap_2d(h.Hg, Mq, d, d, 128, 64, 128);
     L.tmB_o = make_tmap_2d(L.w_o, d, d, d, L.bn_o, 64, 128);
-    L.tmB_up = make_tmap_2d(L.w_up, 2 * m, d, d, L.bn_up, 64, 128);
+    if (!h.moe) L.tmB_up = make_tmap_2d(L.w_up, 2 * m, d, d, L.bn_up, 64, 128);
     L.tmRopeKV = rope_table(h, L.Rkv, lp.pos_kv);
     L.tmRopeQ = rope_table(h, L.Rq, lp.pos_q);
     L.tmA_hid = make_tmap_2d(h.hid, Mq, m, m, 128, 64, 128);
-    L.tmB_down = make_tmap_2d(L.w_down, d, m, m, L.bn_down, 64, 128);
+    if (!h.moe) L.tmB_down = make_tmap_2d(L.w_down, d, m, m, L.bn_down, 64, 128);
     if (tail_supported(h)) {
       L.tmWo_t = make_tmap_2d(L.w_o, d, d, d, d, 64, 128);
       L.tmWup_t = make_tmap_2d(L.w_up, 2 * m, d, d, 128, 64, 128);
@@ -435,7 +526,7 @@ static void finalize(Handle& h) {
     CK(cudaMemcpy(h.master + kv.second.first, hp.v.data(), hp.v.size() * 4, cudaMemcpyHostToDevice));
     h.w32[kv.first] = h.master + kv.second.first;
   }
-  for (int l = 0; l < c.layers; ++l) {
+  for (int l = 0; l < c.layers && !h.moe; ++l) {
     const std::string f = "ffn." + std::to_string(l) + ".";
     const HostParam& wg = h.host.at(f + "w_gate");
     const HostParam& wu = h.host.at(f + "w_up");
@@ -463,7 +554,12 @@ static void finalize(Handle& h) {
   for (int l = 0; l < c.layers; ++l) {
     h.layers[l].gain_q = h.w32["attn." + std::to_string(l) + ".qk_gain_q"];
     h.layers[l].gain_k = h.w32["attn." + std::to_string(l) + ".qk_gain_k"];
+    if (h.moe) {  // router and balancing bias read (and updated) in the master buffer
+      h.layers[l].router = h.w32["ffn." + std::to_string(l) + ".router"];
+      h.layers[l].router_bias = h.w32["ffn." + std::to_string(l) + ".router_bias"];
+    }
   }
+  if (h.moe) ensure_moe_buffers(h);
   h.host.clear();  // device copies are authoritative from here on
   h.finalized = true;
 }
@@ -493,6 +589,27 @@ static void launch_gemm(Handle& h, const CUtensorMap& A, const CUtensorMap& B, i
   k_gemm_bf16<Epi><<<grid, kGemmThreads, gp.smem_bytes, h.stream>>>(
       A, B, side_stats ? *side_stats : A, side_rope ? *side_rope : A, M, N, K, BN, gp.a_stages, epi);
   check_launch("gemm");
+  ++h.launches;
+}
+
+// Grouped (MoE expert) GEMM: A = expert-sorted rows padded per expert to 128, B = the stacked
+// expert weights; the m-block count and each block's expert are read on the device.
+template <class Epi>
+static void launch_gemm_grouped(Handle& h, const CUtensorMap& A, const CUtensorMap& B, int N, int K, int BN,
+                                const Epi& epi) {
+  static_assert(is_grouped<Epi>::value, "grouped epilogue expected");
+  static uint32_t attr_bytes = 0;
+  const GemmPlan gp = gemm_plan(K, BN, 0, 1, 2);
+  if (N % BN || gp.a_stages < 2) throw RuntimeFailure("grouped gemm: unsupported tile plan");
+  if (gp.smem_bytes > attr_bytes) {
+    CK(cudaFuncSetAttribute(k_gemm_bf16<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(gp.smem_bytes)));
+    attr_bytes = gp.smem_bytes;
+  }
+  const int grid = gemm_grid(h.moe_tiles_max, N / BN, h.num_sms);
+  k_gemm_bf16<Epi><<<grid, kGemmThreads, gp.smem_bytes, h.stream>>>(A, B, A, A, h.moe_pmax, N, K, BN,
+                                                                      gp.a_stages, epi);
+  check_launch("grouped gemm");
   ++h.launches;
 }
 
@@ -746,6 +863,57 @@ static void run_tokenizer(Handle& h, int B) {
   ++h.launches;
 }
 
+// MoE FFN of layer l on the T rows of X (in place): x <- x + MoE(RMSNorm(x)) (SPEC.md:375 with
+// the FFN of SPEC.md:272-351), row statistics refreshed for the next layer. See moe.cuh.
+static void run_moe(Handle& h, int l, __nv_bfloat16* X, float4* SS, int T) {
+  LayerDev& L = h.layers[l];
+  const int d = h.d, E = h.moe_E, k = h.moe_k, S = h.moe_s, me = h.moe_m;
+  if (T * (k + S) + (E + S) * 128 > h.moe_pmax) throw RuntimeFailure("moe: workspace too small");
+  int32_t* counts = h.moe_counts + static_cast<size_t>(l) * E;
+  const float* gain = h.w32.at("block." + std::to_string(l) + ".ffn_norm");
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(k_moe_route, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * kMoeMaxExperts * 4));
+    attr = true;
+  }
+  CK(cudaMemsetAsync(counts, 0, static_cast<size_t>(E) * 4, h.stream));
+  const int rgrid = std::max(1, std::min((T + 7) / 8, h.num_sms * 8));
+  k_moe_route<<<rgrid, 256, static_cast<size_t>(d) * E * 4, h.stream>>>(
+      X, T, d, gain, L.router, L.router_bias, E, k, L.moe_sel, L.moe_w, h.moe_inv, counts, h.err);
+  k_moe_plan<<<1, 256, 0, h.stream>>>(counts, E, S, T, h.moe_off, h.moe_cursor, h.moe_tile_group, h.moe_ntiles,
+                                      h.moe_tok);
+  const int sgrid = std::max(1, std::min((T + 255) / 256, h.num_sms * 8));
+  k_moe_scatter<<<sgrid, 256, 0, h.stream>>>(X, T, d, gain, h.moe_inv, L.moe_sel, L.moe_w, E, k, S, h.moe_off,
+                                             h.moe_cursor, h.moe_xs, h.moe_tok, h.moe_wof, h.moe_slot);
+  check_launch("moe route/plan/scatter");
+  h.launches += 3;
+  stage_mark(h, "L" + std::to_string(l) + ".moe_route");
+  EpiMoeGU eg;
+  eg.tile_group = h.moe_tile_group;
+  eg.num_tiles = h.moe_ntiles;
+  eg.group_n = 2 * me;
+  eg.tok_of = h.moe_tok;
+  eg.hidden = h.moe_hs;
+  eg.m = me;
+  launch_gemm_grouped(h, h.tmA_moe_xs, L.tmB_moe_gu, 2 * me, d, L.bn_moe_gu, eg);
+  EpiMoeDown ed;
+  ed.tile_group = h.moe_tile_group;
+  ed.num_tiles = h.moe_ntiles;
+  ed.group_n = d;
+  ed.tok_of = h.moe_tok;
+  ed.w_of = h.moe_wof;
+  ed.y = h.moe_ys;
+  ed.d = d;
+  launch_gemm_grouped(h, h.tmA_moe_hs, L.tmB_moe_down, d, me, L.bn_moe_down, ed);
+  stage_mark(h, "L" + std::to_string(l) + ".moe_experts");
+  const int cgrid = std::max(1, std::min((T + 7) / 8, h.num_sms * 8));
+  k_moe_combine<<<cgrid, 256, 0, h.stream>>>(X, T, d, h.moe_ys, h.moe_slot, k, S, SS);
+  check_launch("moe combine");
+  ++h.launches;
+  h.moe_rows[l] = T;
+  stage_mark(h, "L" + std::to_string(l) + ".moe_combine");
+}
+
 // One SORT block. out_attn_only: write Attn(...) instead of the residual
 // stream (op-level parity entry point).
 static void run_layer(Handle& h, int l, int B, bool attn_only = false) {
@@ -796,6 +964,10 @@ static void run_layer(Handle& h, int l, int B, bool attn_only = false) {
   launch_gemm(h, L.tmA_hg, L.tmB_o, B * L.Rq, d, d, L.bn_o, eo);
   stage_mark(h, "L" + std::to_string(l) + ".wo");
   if (attn_only) return;
+  if (h.moe) {
+    run_moe(h, l, Xq, SSq, B * L.Rq);
+    return;
+  }
   if (h.training)
     CK(cudaMemcpyAsync(h.tl[l].x1, Xq, static_cast<size_t>(B) * L.Rq * d * 2, cudaMemcpyDeviceToDevice, h.stream));
   EpiSwiGLU eu;
@@ -923,6 +1095,7 @@ static void build_bwd_lists(const LayerPlan& lp, std::vector<int32_t>& dq_off, s
 }
 
 static void ensure_train_buffers(Handle& h, int B) {
+  if (h.moe) throw ConfigError("training step: the MoE FFN backward is not implemented in this build");
   if (h.train_B >= B) return;
   if (!h.cublas) {
     if (cublasCreate(&h.cublas) != CUBLAS_STATUS_SUCCESS) throw RuntimeFailure("cublasCreate failed");
@@ -1512,6 +1685,9 @@ static void collect_status(Handle& h) {
     }
   }
   if (err[0] & kErrOOV) throw ConfigError("tokenizer: id outside vocabulary (device check)");
+  if (err[0] & kErrMoeNonFinite)
+    throw RuntimeFailure("moe: non-finite router score at token row " + std::to_string(err[1] - 1) +
+                         " (device check)");
 }
 
 static Handle* H_(SortHandle p) {
@@ -1571,6 +1747,11 @@ int sort_create(const SortConfig* cfg, int device, SortHandle* out) {
     h->m = cfg->ffn_dim;
     h->dh = cfg->head_hidden > 0 ? cfg->head_hidden : cfg->model_dim;
     h->generic = cfg->model_dim > 256;
+    h->moe = cfg->moe_experts > 0;
+    h->moe_E = cfg->moe_experts;
+    h->moe_k = cfg->moe_topk;
+    h->moe_s = cfg->moe_shared;
+    h->moe_m = cfg->moe_ffn_dim;
     if (!h->generic && h->dh != 32 && h->dh != 64 && h->dh != 128 && h->dh != 256)
       throw ConfigError("unsupported head_hidden (must be 32, 64, 128 or 256)");
     h->L0 = h->plan.L0;
@@ -2025,6 +2206,64 @@ int sort_gather_rows(const void* table, int64_t n_rows, int32_t row_bytes, const
     CK(cudaFreeAsync(err, static_cast<cudaStream_t>(stream)));
     CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
     if (herr) throw ConfigError("gather rows: id outside the table shard");
+  });
+}
+
+int sort_moe_routing(SortHandle p, int layer, int32_t* sel, float* weights) {
+  return api([&] {
+    Handle* h = ready(p);
+    if (!h->moe) throw ConfigError("moe: the model has no MoE FFN");
+    if (layer < 0 || layer >= h->cfg.layers) throw ConfigError("moe: layer out of range");
+    const LayerDev& L = h->layers[layer];
+    const size_t n = static_cast<size_t>(h->moe_rows[layer]) * h->moe_k;
+    if (sel) CK(cudaMemcpyAsync(sel, L.moe_sel, n * 4, cudaMemcpyDeviceToHost, h->stream));
+    if (weights) CK(cudaMemcpyAsync(weights, L.moe_w, n * 4, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+  });
+}
+
+int sort_moe_load(SortHandle p, int layer, int64_t* load) {
+  return api([&] {
+    Handle* h = ready(p);
+    if (!h->moe) throw ConfigError("moe: the model has no MoE FFN");
+    if (layer < 0 || layer >= h->cfg.layers || !load) throw ConfigError("moe: bad argument");
+    std::vector<int32_t> c(h->moe_E);
+    CK(cudaMemcpyAsync(c.data(), h->moe_counts + static_cast<size_t>(layer) * h->moe_E, c.size() * 4,
+                       cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    for (int e = 0; e < h->moe_E; ++e) load[e] = c[e];
+  });
+}
+
+int sort_moe_update_bias(SortHandle p, double gamma) {
+  return api([&] {
+    Handle* h = ready(p);
+    if (!h->moe) throw ConfigError("moe: the model has no MoE FFN");
+    for (int l = 0; l < h->cfg.layers; ++l)
+      k_moe_update_bias<<<1, 64, 0, h->stream>>>(h->moe_counts + static_cast<size_t>(l) * h->moe_E, h->moe_E,
+                                                 static_cast<float>(gamma), h->layers[l].router_bias);
+    check_launch("moe bias update");
+    CK(cudaStreamSynchronize(h->stream));
+  });
+}
+
+int sort_moe_forward(SortHandle p, int layer, const float* x, int rows, float* out) {
+  return api([&] {
+    Handle* h = ready(p);
+    if (!h->moe) throw ConfigError("moe: the model has no MoE FFN");
+    if (layer < 0 || layer >= h->cfg.layers || !x || !out || rows < 0) throw ConfigError("moe: bad argument");
+    const size_t cap = static_cast<size_t>(h->Bmax) * h->plan.layers[layer].l_q;
+    if (static_cast<size_t>(rows) > cap) throw ConfigError("moe: more rows than the layer's workspace");
+    const int d = h->d;
+    std::vector<__nv_bfloat16> xb(static_cast<size_t>(rows) * d);
+    for (size_t i = 0; i < xb.size(); ++i) xb[i] = f2bf(x[i]);
+    __nv_bfloat16* X = h->X[0];
+    CK(cudaMemcpyAsync(X, xb.data(), xb.size() * 2, cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemsetAsync(h->err, 0, 4 * sizeof(int32_t), h->stream));
+    if (rows > 0) run_moe(*h, layer, X, h->SS[0], rows);
+    CK(cudaMemcpyAsync(xb.data(), X, xb.size() * 2, cudaMemcpyDeviceToHost, h->stream));
+    collect_status(*h);
+    for (size_t i = 0; i < xb.size(); ++i) out[i] = __bfloat162float(xb[i]);
   });
 }
 

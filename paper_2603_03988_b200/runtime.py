@@ -38,6 +38,8 @@ class CSortConfig(C.Structure):
         ("rope_theta", C.c_double), ("local_window", C.c_int32), ("full_suffix", C.c_int32),
         ("keep", C.c_int32 * 64), ("keep_specials", C.c_int32),
         ("max_batch", C.c_int32), ("n_hist", C.c_int32), ("n_cand", C.c_int32),
+        ("moe_experts", C.c_int32), ("moe_topk", C.c_int32), ("moe_shared", C.c_int32),
+        ("moe_ffn_dim", C.c_int32),
     ]
 
 
@@ -58,7 +60,8 @@ EXPORTS = [
     "sort_train_step", "sort_grad_info", "sort_grads_copy", "sort_dtokens",
     "sort_set_item_table", "sort_gather_rows", "sort_train_step_bce", "sort_adamw_step",
     "sort_get_param", "sort_dataset_open", "sort_dataset_close", "sort_dataset_size",
-    "sort_dataset_batch",
+    "sort_dataset_batch", "sort_moe_routing", "sort_moe_load", "sort_moe_update_bias",
+    "sort_moe_forward",
 ]
 
 _lib = None
@@ -102,6 +105,10 @@ def lib():
         L.sort_train_step_bce.argtypes = [C.c_void_p, C.c_void_p, f32p, f32p, f32p]
         L.sort_adamw_step.argtypes = [C.c_void_p, C.c_float, C.c_float, C.c_float, C.c_float, C.c_float]
         L.sort_get_param.argtypes = [C.c_void_p, C.c_char_p, f32p]
+        L.sort_moe_routing.argtypes = [C.c_void_p, C.c_int, i32p, f32p]
+        L.sort_moe_load.argtypes = [C.c_void_p, C.c_int, i64p]
+        L.sort_moe_update_bias.argtypes = [C.c_void_p, C.c_double]
+        L.sort_moe_forward.argtypes = [C.c_void_p, C.c_int, f32p, C.c_int, f32p]
         L.sort_dataset_open.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
         L.sort_dataset_close.argtypes = [C.c_void_p]
         L.sort_dataset_size.argtypes = [C.c_void_p]
@@ -147,6 +154,8 @@ def to_c_config(cfg: SortConfig, max_batch: Optional[int] = None) -> CSortConfig
     c.keep_specials = int(cfg.keep_specials)
     c.max_batch = max_batch or cfg.batch
     c.n_hist, c.n_cand = cfg.n_hist, cfg.n_cand
+    c.moe_experts, c.moe_topk = cfg.moe_experts, cfg.moe_topk
+    c.moe_shared, c.moe_ffn_dim = cfg.moe_shared, cfg.moe_ffn_dim
     return c
 
 
@@ -271,6 +280,30 @@ class SortModel:
         """Batch-local item rows (device bf16 [n_rows, item_dim]) for the next calls; ptr=0
         restores the handle's own table."""
         _check(lib().sort_set_item_table(self.h, C.c_void_p(ptr) if ptr else None, int(n_rows)))
+
+    # -- MoE FFN (SPEC.md:272-351) ----------------------------------------------
+    def moe_routing(self, layer: int, rows: int):
+        """(sel [rows, k] int32, weights [rows, k]) of `layer` in the last forward."""
+        k = self.cfg.moe_topk
+        sel = np.zeros((rows, k), np.int32)
+        w = np.zeros((rows, k), np.float32)
+        _check(lib().sort_moe_routing(self.h, layer, _p(sel, i32p), _p(w, f32p)))
+        return sel, w
+
+    def moe_load(self, layer: int) -> np.ndarray:
+        out = np.zeros(self.cfg.moe_experts, np.int64)
+        _check(lib().sort_moe_load(self.h, layer, _p(out, i64p)))
+        return out
+
+    def moe_update_bias(self, gamma: float = 1e-3) -> None:
+        _check(lib().sort_moe_update_bias(self.h, float(gamma)))
+
+    def moe_forward(self, layer: int, x: np.ndarray) -> np.ndarray:
+        """out = x + MoE(RMSNorm(x; ffn_norm)) through the device path (bf16 residual)."""
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        out = np.zeros_like(x)
+        _check(lib().sort_moe_forward(self.h, layer, _p(x, f32p), x.shape[0], _p(out, f32p)))
+        return out
 
     # -- training (sort_train_step) --------------------------------------------
     def train_step(self, batch: Dict[str, np.ndarray], dlogits: np.ndarray) -> np.ndarray:
