@@ -292,17 +292,19 @@ def run_embed(args, cfg, rank, world, local, dist):
         dist.destroy_process_group()
 
 
-def run_large(args, rank, world, local, dist):
+def run_large(args, rank, world, local, dist, moe=False):
     """BASELINE configs[3]: SORT-large (12 layers, d=1024, 16 heads, 4096 history, W=256,
     128 targets, geometric pruning) forward, 8 requests per GPU, requests sharded over the
-    ranks (weak scaling). Generic path: bf16 library GEMMs + the tcgen05 attention core."""
+    ranks (weak scaling). Generic path: bf16 library GEMMs + the tcgen05 attention core.
+    moe=True: SURVEY.md 8(f) "next 1", SORT-base with the DeepSeek-style MoE FFN (8 routed
+    experts, top-1, 1 shared, expert width 320), 256 requests per GPU."""
     import torch
     from paper_2603_03988_b200 import runtime as R
-    from paper_2603_03988_b200.config import large_config
+    from paper_2603_03988_b200.config import base_moe_config, large_config
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    B = 8
-    cfg = large_config(batch=B)
+    B = args.requests if moe else 8
+    cfg = base_moe_config(batch=B) if moe else large_config(batch=B)
     model = R.SortModel(cfg, synth.make_params(cfg, seed=5), device=local, max_batch=B)
     stream = torch.cuda.Stream(device=dev)
     model.set_stream(stream.cuda_stream)
@@ -330,18 +332,29 @@ def run_large(args, rank, world, local, dist):
     ms = float(t[0])
     fl = forward_flops(cfg)
     peaks, _ = measured_peaks()
+    if moe:
+        wl = (f"SORT-base + MoE FFN: {cfg.layers} layers, d={cfg.model_dim}, {cfg.heads} heads, "
+              f"{cfg.moe_experts} routed experts top-{cfg.moe_topk} + {cfg.moe_shared} shared, expert "
+              f"m={cfg.moe_ffn_dim}, {B} requests/GPU x ({cfg.n_hist} history + {cfg.n_cand} targets), "
+              f"keep={cfg.keep_schedule()}")
+        metric = "candidates scored/sec (SORT-base MoE forward)"
+        dtype = "bf16 (fp32 accumulation, fp32 router)"
+    else:
+        wl = (f"SORT-large: {cfg.layers} layers, d={cfg.model_dim}, {cfg.heads} heads, "
+              f"m={cfg.ffn_dim}, {B} requests/GPU x ({cfg.n_hist} history + {cfg.n_cand} "
+              f"targets), L={cfg.seq_len}, W={cfg.local_window}, keep={cfg.keep_schedule()}")
+        metric = "candidates scored/sec (SORT-large forward)"
+        dtype = "bf16 (fp32 accumulation and residual stream)"
     if rank == 0:
         print(json.dumps({
-            "metric": "candidates scored/sec (SORT-large forward)", "value": world * B * cfg.n_cand / (ms / 1e3),
+            "metric": metric, "value": world * B * cfg.n_cand / (ms / 1e3),
             "unit": "candidates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "bf16 (fp32 accumulation and residual stream)", "data": "synthetic",
+            "dtype": dtype, "data": "synthetic",
             "mfu_vs_bf16_peak": fl["total"] * B / (ms / 1e3) / (peaks["bf16_tflops"] * 1e12),
             "algorithmic_tflop_per_step": fl["total"] * B / 1e12,
-            "config": {"workload": f"SORT-large: {cfg.layers} layers, d={cfg.model_dim}, {cfg.heads} heads, "
-                                   f"m={cfg.ffn_dim}, {B} requests/GPU x ({cfg.n_hist} history + {cfg.n_cand} "
-                                   f"targets), L={cfg.seq_len}, W={cfg.local_window}, keep={cfg.keep_schedule()}",
-                       "requests_per_gpu": B, "l2": "flushed (256 MB write) before every timed step"},
+            "config": {"workload": wl, "requests_per_gpu": B,
+                       "l2": "flushed (256 MB write) before every timed step"},
         }))
     if dist:
         dist.destroy_process_group()
@@ -357,7 +370,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="minimum length of the CPU-baseline sample (>= 32 requests)")
-    ap.add_argument("--mode", default="forward", choices=["forward", "train", "embed", "large"],
+    ap.add_argument("--mode", default="forward", choices=["forward", "train", "embed", "large", "moe"],
                     help="train: SORT-base training step (BASELINE configs[2]), global batch "
                          "--requests sharded over the ranks, gradient all-reduce over NCCL; "
                          "embed: BASELINE configs[4], 100M-row item table row-sharded over the "
@@ -394,8 +407,8 @@ def main():
     if args.mode == "embed":
         run_embed(args, cfg, rank, world, local, dist)
         return
-    if args.mode == "large":
-        run_large(args, rank, world, local, dist)
+    if args.mode in ("large", "moe"):
+        run_large(args, rank, world, local, dist, moe=args.mode == "moe")
         return
 
     from paper_2603_03988_b200 import runtime as R

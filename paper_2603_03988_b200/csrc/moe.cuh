@@ -8,7 +8,7 @@
 //   -> k_moe_plan     expert segments padded to 128 rows, m-block -> expert list
 //   -> k_moe_scatter  bf16 RMSNorm rows into their expert segments (shared expert: every row)
 //   -> grouped tcgen05 GEMM [gate | up] with the SwishGLU epilogue -> h [P, m_e]
-//   -> grouped tcgen05 GEMM down, epilogue scales by the combine weight -> y [P, d] fp32
+//   -> grouped tcgen05 GEMM down, epilogue scales by the combine weight -> y [P, d] bf16
 //   -> k_moe_combine  x1 + y_shared + sum_j y_j (fixed order) -> bf16 residual + row statistics
 // Every row's arithmetic is independent of where the scatter put it, so the output is
 // deterministic even though segment order within an expert follows atomic arrival.
@@ -26,6 +26,15 @@ constexpr int kMoeMaxK = 8;
 
 // ---------------------------------------------------------------------------------- router
 // One warp per token (grid-stride), lane owns 8 contiguous columns (d <= 256, d % 8 == 0).
+// Router logits: every lane forms its 8-column partial dot for each expert and parks them in a
+// per-warp smem tile; lane e (and e + 32) then sums expert e's 32 partials and applies the
+// sigmoid. Top-k: k rounds of a warp max over order-preserving integer keys, the lowest lane
+// (= lowest expert index) winning ties via a ballot.
+__device__ __forceinline__ uint32_t float_key(float f) {
+  const uint32_t b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
 __global__ void __launch_bounds__(256) k_moe_route(const __nv_bfloat16* __restrict__ x, int T, int d,
                                                    const float* __restrict__ gain, const float* __restrict__ router,
                                                    const float* __restrict__ bias, int E, int k,
@@ -34,6 +43,8 @@ __global__ void __launch_bounds__(256) k_moe_route(const __nv_bfloat16* __restri
                                                    int32_t* __restrict__ err) {
   extern __shared__ float smem_f[];
   float* wr = smem_f;  // router transposed [E][d]
+  const int stride = E + 1;  // partial tile row pitch (conflict-free column sums)
+  float* part = smem_f + static_cast<size_t>(E) * d + (threadIdx.x >> 5) * 32 * stride;
   __shared__ int hist[kMoeMaxExperts];
   for (int i = threadIdx.x; i < d * E; i += blockDim.x) {
     const int c = i / E, e = i - c * E;
@@ -47,6 +58,8 @@ __global__ void __launch_bounds__(256) k_moe_route(const __nv_bfloat16* __restri
   float g[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) g[i] = act ? gain[c0 + i] : 0.f;
+  const bool own0 = lane < E, own1 = lane + 32 < E;
+  const float b0 = own0 ? bias[lane] : 0.f, b1 = own1 ? bias[lane + 32] : 0.f;
   const int warps = gridDim.x * (blockDim.x >> 5);
   for (int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < T; t += warps) {
     float v[8];
@@ -69,15 +82,6 @@ __global__ void __launch_bounds__(256) k_moe_route(const __nv_bfloat16* __restri
     const float inv = rsqrtf(warp_sum(ss) / static_cast<float>(d) + 1e-6f);  // norm.hpp:23-24
 #pragma unroll
     for (int i = 0; i < 8; ++i) v[i] *= inv * g[i];
-    // router scores in fp32; after the butterfly every lane holds every expert's score
-    float best_b[kMoeMaxK], best_s[kMoeMaxK];
-    int best_e[kMoeMaxK];
-#pragma unroll
-    for (int j = 0; j < kMoeMaxK; ++j) {
-      best_b[j] = -INFINITY;
-      best_s[j] = 0.f;
-      best_e[j] = -1;
-    }
     for (int e = 0; e < E; ++e) {
       float z = 0.f;
       if (act) {
@@ -85,39 +89,54 @@ __global__ void __launch_bounds__(256) k_moe_route(const __nv_bfloat16* __restri
         const float4 b = *reinterpret_cast<const float4*>(wr + e * d + c0 + 4);
         z = v[0] * a.x + v[1] * a.y + v[2] * a.z + v[3] * a.w + v[4] * b.x + v[5] * b.y + v[6] * b.z + v[7] * b.w;
       }
-      z = warp_sum(z);
-      const float sc = 1.f / (1.f + expf(-z));  // sigmoid gate
-      const float bs = sc + bias[e];
-      // insert into the running top-k (descending biased score; strict > keeps the lower
-      // index ahead on ties since experts arrive in ascending order)
-      if (bs > best_b[k - 1]) {
-        int j = k - 1;
-        while (j > 0 && bs > best_b[j - 1]) {
-          best_b[j] = best_b[j - 1];
-          best_s[j] = best_s[j - 1];
-          best_e[j] = best_e[j - 1];
-          --j;
-        }
-        best_b[j] = bs;
-        best_s[j] = sc;
-        best_e[j] = e;
+      part[lane * stride + e] = z;
+    }
+    __syncwarp();
+    float z0 = 0.f, z1 = 0.f;
+    if (own0)
+#pragma unroll 8
+      for (int l = 0; l < 32; ++l) z0 += part[l * stride + lane];
+    if (own1)
+#pragma unroll 8
+      for (int l = 0; l < 32; ++l) z1 += part[l * stride + lane + 32];
+    __syncwarp();
+    // sigmoid gate scores and biased selection keys; a non-finite score
+    // is flagged and never selected
+    const float s0 = 1.f / (1.f + expf(-z0)), s1 = 1.f / (1.f + expf(-z1));
+    const float k0f = s0 + b0, k1f = s1 + b1;
+    bool bad = (own0 && !isfinite(k0f)) || (own1 && !isfinite(k1f));
+    uint32_t key0 = own0 && isfinite(k0f) ? float_key(k0f) : 0u;
+    uint32_t key1 = own1 && isfinite(k1f) ? float_key(k1f) : 0u;
+    if (__any_sync(0xffffffffu, bad) && lane == 0) {
+      atomicOr(err, kErrMoeNonFinite);
+      atomicCAS(err + 1, 0, t + 1);
+    }
+    int my_e[kMoeMaxK];
+    float my_s[kMoeMaxK];
+    float tot = 0.f;
+#pragma unroll
+    for (int j = 0; j < kMoeMaxK; ++j) {
+      if (j >= k) break;
+      const uint32_t best = __reduce_max_sync(0xffffffffu, key0 > key1 ? key0 : key1);
+      const uint32_t lo = __ballot_sync(0xffffffffu, key0 == best);   // experts 0..31 first
+      const uint32_t hi = __ballot_sync(0xffffffffu, key1 == best);
+      const int e = lo ? __ffs(lo) - 1 : (hi ? 32 + __ffs(hi) - 1 : 0);
+      const float sw = __shfl_sync(0xffffffffu, e < 32 ? s0 : s1, e & 31);
+      if (lane == (e & 31)) {
+        if (e < 32) key0 = 0u;
+        else key1 = 0u;
       }
+      my_e[j] = e;
+      my_s[j] = (lo | hi) ? sw : 1.f;
+      tot += my_s[j];
     }
     if (lane == 0) {
-      float tot = 0.f;
-      for (int j = 0; j < k; ++j) {
-        if (best_e[j] < 0) {  // non-finite router score: flag it, keep indices in range
-          atomicOr(err, kErrMoeNonFinite);
-          atomicCAS(err + 1, 0, t + 1);
-          best_e[j] = 0;
-          best_s[j] = 1.f;
-        }
-        tot += best_s[j];
-      }
-      for (int j = 0; j < k; ++j) {
-        sel[static_cast<size_t>(t) * k + j] = best_e[j];
-        wgt[static_cast<size_t>(t) * k + j] = best_s[j] / tot;
-        atomicAdd(&hist[best_e[j]], 1);
+#pragma unroll
+      for (int j = 0; j < kMoeMaxK; ++j) {
+        if (j >= k) break;
+        sel[static_cast<size_t>(t) * k + j] = my_e[j];
+        wgt[static_cast<size_t>(t) * k + j] = my_s[j] / tot;
+        atomicAdd(&hist[my_e[j]], 1);
       }
       inv_out[t] = inv;
     }
@@ -125,6 +144,108 @@ __global__ void __launch_bounds__(256) k_moe_route(const __nv_bfloat16* __restri
   __syncthreads();
   for (int i = threadIdx.x; i < E; i += blockDim.x)
     if (hist[i]) atomicAdd(&counts[i], hist[i]);
+}
+
+// Small-E router (E <= 8): the lane's 8 x 8 router slice lives in registers and the 8 expert
+// partials are reduce-scattered across the warp with 9 shuffles; afterwards lane 4e holds
+// expert e's logit. Same arithmetic contract as k_moe_route.
+__global__ void __launch_bounds__(256) k_moe_route8(const __nv_bfloat16* __restrict__ x, int T, int d,
+                                                    const float* __restrict__ gain,
+                                                    const float* __restrict__ router, const float* __restrict__ bias,
+                                                    int E, int k, int32_t* __restrict__ sel, float* __restrict__ wgt,
+                                                    float* __restrict__ inv_out, int32_t* __restrict__ counts,
+                                                    int32_t* __restrict__ err) {
+  __shared__ int hist[8];
+  if (threadIdx.x < 8) hist[threadIdx.x] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int c0 = lane * 8;
+  const bool act = c0 < d;
+  float g[8], w[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    g[i] = act ? gain[c0 + i] : 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) w[e][i] = act && e < E ? router[static_cast<size_t>(c0 + i) * E + e] : 0.f;
+  }
+  const int my_e = lane >> 2;
+  const bool owner = (lane & 3) == 0 && my_e < E;
+  const float my_b = owner ? bias[my_e] : 0.f;
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  int t = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  int4 nxt = make_int4(0, 0, 0, 0);  // software pipeline: the next row's load is in flight
+  if (act && t < T) nxt = *reinterpret_cast<const int4*>(x + static_cast<size_t>(t) * d + c0);
+  for (; t < T; t += warps) {
+    const int4 raw = nxt;
+    if (act && t + warps < T) nxt = *reinterpret_cast<const int4*>(x + static_cast<size_t>(t + warps) * d + c0);
+    float v[8];
+    {
+      const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(p2[i]);
+        v[2 * i] = f.x;
+        v[2 * i + 1] = f.y;
+      }
+    }
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ss = fmaf(v[i], v[i], ss);
+    const float inv = rsqrtf(warp_sum(ss) / static_cast<float>(d) + 1e-6f);  // norm.hpp:23-24
+    float p[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      float z = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) z = fmaf(v[i] * inv * g[i], w[e][i], z);
+      p[e] = z;
+    }
+    float q[4], r[2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      q[i] = (b4 ? p[i + 4] : p[i]) + __shfl_xor_sync(0xffffffffu, b4 ? p[i] : p[i + 4], 16);
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+      r[i] = (b3 ? q[i + 2] : q[i]) + __shfl_xor_sync(0xffffffffu, b3 ? q[i] : q[i + 2], 8);
+    float z = (b2 ? r[1] : r[0]) + __shfl_xor_sync(0xffffffffu, b2 ? r[0] : r[1], 4);
+    z += __shfl_xor_sync(0xffffffffu, z, 2);
+    z += __shfl_xor_sync(0xffffffffu, z, 1);
+    const float sc = 1.f / (1.f + expf(-z));  // sigmoid gate
+    const float kf = sc + my_b;
+    const bool bad = owner && !isfinite(kf);
+    uint32_t key = owner && !bad ? float_key(kf) : 0u;
+    if (__any_sync(0xffffffffu, bad) && lane == 0) {
+      atomicOr(err, kErrMoeNonFinite);
+      atomicCAS(err + 1, 0, t + 1);
+    }
+    int se[kMoeMaxK];
+    float sw[kMoeMaxK];
+    float tot = 0.f;
+#pragma unroll
+    for (int j = 0; j < kMoeMaxK; ++j) {
+      if (j >= k) break;
+      const uint32_t best = __reduce_max_sync(0xffffffffu, key);
+      const uint32_t m = __ballot_sync(0xffffffffu, key == best && owner);
+      const int wl = m ? __ffs(m) - 1 : 0;  // lowest lane = lowest expert on ties
+      sw[j] = m ? __shfl_sync(0xffffffffu, sc, wl) : 1.f;
+      se[j] = wl >> 2;
+      if (lane == wl) key = 0u;
+      tot += sw[j];
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int j = 0; j < kMoeMaxK; ++j) {
+        if (j >= k) break;
+        sel[static_cast<size_t>(t) * k + j] = se[j];
+        wgt[static_cast<size_t>(t) * k + j] = sw[j] / tot;
+        atomicAdd(&hist[se[j]], 1);
+      }
+      inv_out[t] = inv;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < E && hist[threadIdx.x]) atomicAdd(&counts[threadIdx.x], hist[threadIdx.x]);
 }
 
 // ------------------------------------------------------------------------------------ plan
@@ -223,7 +344,7 @@ __global__ void __launch_bounds__(256) k_moe_scatter(const __nv_bfloat16* __rest
 // x_out = bf16(x1 + y_shared + sum_j y_j) in place, with the row's sum-of-squares partials
 // per 64-column block (the EpiResid layout the next layer's GEMMs read).
 __global__ void __launch_bounds__(256) k_moe_combine(__nv_bfloat16* __restrict__ x, int T, int d,
-                                                     const float* __restrict__ ys, const int32_t* __restrict__ slot_pos,
+                                                     const __nv_bfloat16* __restrict__ ys, const int32_t* __restrict__ slot_pos,
                                                      int k, int shared, float4* __restrict__ ss_out) {
   const int lane = threadIdx.x & 31;
   const int S = k + shared;
@@ -245,17 +366,15 @@ __global__ void __launch_bounds__(256) k_moe_combine(__nv_bfloat16* __restrict__
       // shared expert first, then the routed experts in selection order
       for (int jj = 0; jj < S; ++jj) {
         const int j = shared ? (jj == 0 ? k : jj - 1) : jj;
-        const float* yr = ys + static_cast<size_t>(slot_pos[static_cast<size_t>(t) * S + j]) * d + c0;
-        const float4 a = *reinterpret_cast<const float4*>(yr);
-        const float4 b = *reinterpret_cast<const float4*>(yr + 4);
-        acc[0] += a.x;
-        acc[1] += a.y;
-        acc[2] += a.z;
-        acc[3] += a.w;
-        acc[4] += b.x;
-        acc[5] += b.y;
-        acc[6] += b.z;
-        acc[7] += b.w;
+        const int4 yv = *reinterpret_cast<const int4*>(
+            ys + static_cast<size_t>(slot_pos[static_cast<size_t>(t) * S + j]) * d + c0);
+        const __nv_bfloat162* y2 = reinterpret_cast<const __nv_bfloat162*>(&yv);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 f = __bfloat1622float2(y2[q]);
+          acc[2 * q] += f.x;
+          acc[2 * q + 1] += f.y;
+        }
       }
     }
     float ss = 0.f;
@@ -328,7 +447,7 @@ struct EpiMoeGU {
   }
 };
 
-// Expert down GEMM: y[row] = w_row * acc (fp32), w = the row's combine weight.
+// Expert down GEMM: y[row] = bf16(w_row * acc), w = the row's combine weight.
 struct EpiMoeDown {
   static constexpr int kChunk = 32;
   static constexpr int kMaxParts = 1 << 30;
@@ -340,7 +459,7 @@ struct EpiMoeDown {
   int group_n;
   const int32_t* tok_of;
   const float* w_of;
-  float* y;
+  __nv_bfloat16* y;
   int d;
 
   __device__ __forceinline__ void prologue(uint8_t*, int, int) const {}
@@ -355,9 +474,9 @@ struct EpiMoeDown {
       float v[32];
       tmem_row_chunk<32>(tbase + c, v);
       if (!live) continue;
-      float4* o = reinterpret_cast<float4*>(y + static_cast<size_t>(row) * d + n0 + c);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) o[i] = make_float4(w * v[4 * i], w * v[4 * i + 1], w * v[4 * i + 2], w * v[4 * i + 3]);
+      for (int i = 0; i < 32; ++i) v[i] *= w;
+      store_bf16_row(y + static_cast<size_t>(row) * d + n0 + c, v, 32);
     }
   }
 };

@@ -88,7 +88,8 @@ struct Handle {
   bool moe = false;
   int moe_E = 0, moe_k = 0, moe_s = 0, moe_m = 0, moe_pmax = 0, moe_tiles_max = 0;
   __nv_bfloat16 *moe_xs = nullptr, *moe_hs = nullptr;
-  float *moe_ys = nullptr, *moe_inv = nullptr, *moe_wof = nullptr;
+  __nv_bfloat16* moe_ys = nullptr;
+  float *moe_inv = nullptr, *moe_wof = nullptr;
   int32_t *moe_tok = nullptr, *moe_slot = nullptr, *moe_off = nullptr, *moe_cursor = nullptr,
           *moe_tile_group = nullptr, *moe_ntiles = nullptr, *moe_counts = nullptr;  // counts [layers][E]
   int moe_rows[SORT_MAX_LAYERS] = {0};  // rows routed per layer in the last forward
@@ -296,7 +297,7 @@ static void ensure_moe_buffers(Handle& h) {
   const size_t P = h.moe_pmax;
   h.moe_xs = h.dalloc<__nv_bfloat16>(P * h.d);
   h.moe_hs = h.dalloc<__nv_bfloat16>(P * h.moe_m);
-  h.moe_ys = h.dalloc<float>(P * h.d);
+  h.moe_ys = h.dalloc<__nv_bfloat16>(P * h.d);
   h.moe_tok = h.dalloc<int32_t>(P);
   h.moe_wof = h.dalloc<float>(P);
   h.moe_slot = h.dalloc<int32_t>(T * S);
@@ -873,13 +874,18 @@ static void run_moe(Handle& h, int l, __nv_bfloat16* X, float4* SS, int T) {
   const float* gain = h.w32.at("block." + std::to_string(l) + ".ffn_norm");
   static bool attr = false;
   if (!attr) {
-    CK(cudaFuncSetAttribute(k_moe_route, cudaFuncAttributeMaxDynamicSharedMemorySize, 256 * kMoeMaxExperts * 4));
+    CK(cudaFuncSetAttribute(k_moe_route, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (256 * kMoeMaxExperts + 8 * 32 * (kMoeMaxExperts + 1)) * 4));
     attr = true;
   }
   CK(cudaMemsetAsync(counts, 0, static_cast<size_t>(E) * 4, h.stream));
   const int rgrid = std::max(1, std::min((T + 7) / 8, h.num_sms * 8));
-  k_moe_route<<<rgrid, 256, static_cast<size_t>(d) * E * 4, h.stream>>>(
-      X, T, d, gain, L.router, L.router_bias, E, k, L.moe_sel, L.moe_w, h.moe_inv, counts, h.err);
+  if (E <= 8)  // persistent: 2 resident CTAs per SM (120 registers)
+    k_moe_route8<<<std::max(1, std::min((T + 7) / 8, 2 * h.num_sms)), 256, 0, h.stream>>>(X, T, d, gain, L.router, L.router_bias, E, k, L.moe_sel, L.moe_w,
+                                              h.moe_inv, counts, h.err);
+  else
+    k_moe_route<<<rgrid, 256, (static_cast<size_t>(d) * E + 8 * 32 * (E + 1)) * 4, h.stream>>>(
+        X, T, d, gain, L.router, L.router_bias, E, k, L.moe_sel, L.moe_w, h.moe_inv, counts, h.err);
   k_moe_plan<<<1, 256, 0, h.stream>>>(counts, E, S, T, h.moe_off, h.moe_cursor, h.moe_tile_group, h.moe_ntiles,
                                       h.moe_tok);
   const int sgrid = std::max(1, std::min((T + 255) / 256, h.num_sms * 8));

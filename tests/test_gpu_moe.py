@@ -56,9 +56,11 @@ def rmsnorm(x, g):
     return x / np.sqrt(np.mean(x * x, axis=1, keepdims=True) + 1e-6) * g
 
 
-@pytest.mark.parametrize("which", ["tiny_k2", "base"])
+@pytest.mark.parametrize("which", ["tiny_k2", "tiny_e16_k3", "base"])
 def test_moe_op_vs_oracle(which):
-    cfg = tiny_moe() if which == "tiny_k2" else base_moe_config(batch=2)
+    # E <= 8 runs the register-resident router, E = 16 the shared-memory one
+    cfg = {"tiny_k2": lambda: tiny_moe(), "tiny_e16_k3": lambda: tiny_moe(moe_experts=16, moe_topk=3),
+           "base": lambda: base_moe_config(batch=2)}[which]()
     P = synth.make_params(cfg, seed=21)
     gm = R.SortModel(cfg, P, max_batch=2)
     rng = np.random.default_rng(5)
