@@ -252,7 +252,15 @@ def run_embed(args, cfg, rank, world, local, dist):
                                    for _ in range(B)]).astype(np.int32)
     tb = {k: torch.from_numpy(v).to(dev) for k, v in batch.items()}
     table = ShardedItemTable(shard, rows_per_rank, rank, world, stream_ptr=stream.cuda_stream)
-    scores = torch.empty((B, cfg.n_cand, 3), dtype=torch.float32, device=dev)
+    scores = torch.empty((B, max(cfg.n_cand, 1), 3), dtype=torch.float32, device=dev)
+    lse_t = torch.empty((B, cfg.n_hist), dtype=torch.float32, device=dev)
+    tgt_t = torch.empty((B, cfg.n_hist), dtype=torch.float32, device=dev)
+
+    def step():
+        if pretrain:
+            model.pretrain_forward_device(dbatch, lse_t.data_ptr(), tgt_t.data_ptr())
+        else:
+            model.forward_device(dbatch, scores.data_ptr())
     n_unique = []
 
     def step():
@@ -292,7 +300,7 @@ def run_embed(args, cfg, rank, world, local, dist):
         dist.destroy_process_group()
 
 
-def run_large(args, rank, world, local, dist, moe=False):
+def run_large(args, rank, world, local, dist, moe=False, pretrain=False):
     """BASELINE configs[3]: SORT-large (12 layers, d=1024, 16 heads, 4096 history, W=256,
     128 targets, geometric pruning) forward, 8 requests per GPU, requests sharded over the
     ranks (weak scaling). Generic path: bf16 library GEMMs + the tcgen05 attention core.
@@ -300,21 +308,29 @@ def run_large(args, rank, world, local, dist, moe=False):
     experts, top-1, 1 shared, expert width 320), 256 requests per GPU."""
     import torch
     from paper_2603_03988_b200 import runtime as R
-    from paper_2603_03988_b200.config import base_moe_config, large_config
+    from paper_2603_03988_b200.config import base_moe_config, large_config, pretrain_config
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    B = args.requests if moe else 8
-    cfg = base_moe_config(batch=B) if moe else large_config(batch=B)
+    B = args.requests if moe else (64 if pretrain else 8)
+    cfg = base_moe_config(batch=B) if moe else (pretrain_config(batch=B) if pretrain else large_config(batch=B))
     model = R.SortModel(cfg, synth.make_params(cfg, seed=5), device=local, max_batch=B)
     stream = torch.cuda.Stream(device=dev)
     model.set_stream(stream.cuda_stream)
     batch = synth.make_batch(cfg, B, seed=200 + rank)
     dbatch = R._DevBatch({k: torch.from_numpy(v).to(dev) for k, v in batch.items()})
-    scores = torch.empty((B, cfg.n_cand, 3), dtype=torch.float32, device=dev)
+    scores = torch.empty((B, max(cfg.n_cand, 1), 3), dtype=torch.float32, device=dev)
+    lse_t = torch.empty((B, cfg.n_hist), dtype=torch.float32, device=dev)
+    tgt_t = torch.empty((B, cfg.n_hist), dtype=torch.float32, device=dev)
+
+    def step():
+        if pretrain:
+            model.pretrain_forward_device(dbatch, lse_t.data_ptr(), tgt_t.data_ptr())
+        else:
+            model.forward_device(dbatch, scores.data_ptr())
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
-            model.forward_device(dbatch, scores.data_ptr())
+            step()
         model.sync()
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         if dist:
@@ -322,7 +338,7 @@ def run_large(args, rank, world, local, dist, moe=False):
         for i in range(args.steps):
             flush.fill_(float(i))
             ev[i][0].record(stream)
-            model.forward_device(dbatch, scores.data_ptr())
+            step()
             ev[i][1].record(stream)
         model.sync()
     ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
@@ -332,7 +348,16 @@ def run_large(args, rank, world, local, dist, moe=False):
     ms = float(t[0])
     fl = forward_flops(cfg)
     peaks, _ = measured_peaks()
-    if moe:
+    units = B * cfg.n_cand
+    if pretrain:
+        wl = (f"pre-training (causal next-item, tied full-softmax head): {cfg.layers} layers, d={cfg.model_dim}, "
+              f"{cfg.heads} heads, m={cfg.ffn_dim}, {B} sequences/GPU x {cfg.n_hist} clicks, "
+              f"vocab {cfg.n_items}")
+        metric = "next-item positions scored/sec (pre-training forward + full-softmax CE)"
+        dtype = "bf16 (fp32 accumulation, fp32 log-sum-exp)"
+        units = B * cfg.n_hist
+        ce_flop = 2.0 * B * cfg.seq_len * cfg.n_items * cfg.item_dim
+    elif moe:
         wl = (f"SORT-base + MoE FFN: {cfg.layers} layers, d={cfg.model_dim}, {cfg.heads} heads, "
               f"{cfg.moe_experts} routed experts top-{cfg.moe_topk} + {cfg.moe_shared} shared, expert "
               f"m={cfg.moe_ffn_dim}, {B} requests/GPU x ({cfg.n_hist} history + {cfg.n_cand} targets), "
@@ -347,12 +372,14 @@ def run_large(args, rank, world, local, dist, moe=False):
         dtype = "bf16 (fp32 accumulation and residual stream)"
     if rank == 0:
         print(json.dumps({
-            "metric": metric, "value": world * B * cfg.n_cand / (ms / 1e3),
-            "unit": "candidates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "metric": metric, "value": world * units / (ms / 1e3),
+            "unit": "positions/s" if pretrain else "candidates/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": dtype, "data": "synthetic",
-            "mfu_vs_bf16_peak": fl["total"] * B / (ms / 1e3) / (peaks["bf16_tflops"] * 1e12),
-            "algorithmic_tflop_per_step": fl["total"] * B / 1e12,
+            "mfu_vs_bf16_peak": (fl["block"] * B + (ce_flop if pretrain else fl["total"] * B - fl["block"] * B))
+            / (ms / 1e3) / (peaks["bf16_tflops"] * 1e12),
+            "algorithmic_tflop_per_step": (fl["block"] * B + (ce_flop if pretrain else fl["total"] * B - fl["block"] * B)) / 1e12,
             "config": {"workload": wl, "requests_per_gpu": B,
                        "l2": "flushed (256 MB write) before every timed step"},
         }))
@@ -370,7 +397,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="minimum length of the CPU-baseline sample (>= 32 requests)")
-    ap.add_argument("--mode", default="forward", choices=["forward", "train", "embed", "large", "moe"],
+    ap.add_argument("--mode", default="forward", choices=["forward", "train", "embed", "large", "moe", "pretrain"],
                     help="train: SORT-base training step (BASELINE configs[2]), global batch "
                          "--requests sharded over the ranks, gradient all-reduce over NCCL; "
                          "embed: BASELINE configs[4], 100M-row item table row-sharded over the "
@@ -407,8 +434,8 @@ def main():
     if args.mode == "embed":
         run_embed(args, cfg, rank, world, local, dist)
         return
-    if args.mode in ("large", "moe"):
-        run_large(args, rank, world, local, dist, moe=args.mode == "moe")
+    if args.mode in ("large", "moe", "pretrain"):
+        run_large(args, rank, world, local, dist, moe=args.mode == "moe", pretrain=args.mode == "pretrain")
         return
 
     from paper_2603_03988_b200 import runtime as R
@@ -422,7 +449,15 @@ def main():
     batch = synth.make_batch(cfg, B, seed=100 + rank)  # this rank's shard of requests
     dev_batch = {k: torch.from_numpy(v).to(dev) for k, v in batch.items()}
     dbatch = R._DevBatch(dev_batch)
-    scores = torch.empty((B, cfg.n_cand, 3), dtype=torch.float32, device=dev)
+    scores = torch.empty((B, max(cfg.n_cand, 1), 3), dtype=torch.float32, device=dev)
+    lse_t = torch.empty((B, cfg.n_hist), dtype=torch.float32, device=dev)
+    tgt_t = torch.empty((B, cfg.n_hist), dtype=torch.float32, device=dev)
+
+    def step():
+        if pretrain:
+            model.pretrain_forward_device(dbatch, lse_t.data_ptr(), tgt_t.data_ptr())
+        else:
+            model.forward_device(dbatch, scores.data_ptr())
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
 
     def barrier():

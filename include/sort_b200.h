@@ -72,6 +72,11 @@ typedef struct {
    * Parameters ffn.<l>.router [d, E], ffn.<l>.router_bias [1, E],
    * ffn.<l>.expert.<e>.w_gate|w_up [d, m_e] / w_down [m_e, d], ffn.<l>.shared.* likewise. */
   int32_t moe_experts, moe_topk, moe_shared, moe_ffn_dim;
+  /* 1 = generative pre-training model: sequences are click histories
+   * tokenized as [BOS; clicks] (tokenize_click_sequence, tokenizer.cpp:240-284) with
+   * n_cand = 0 and n_profile_fields = 0, no pruning, and the ranking head replaced by the
+   * tied next-item head (parameter pretrain.proj [d, item_dim]; sort_pretrain_forward). */
+  int32_t pretrain;
 } SortConfig;
 
 /* A batch of requests in structure-of-arrays form (RequestSample, data.hpp:32-38,
@@ -239,6 +244,16 @@ int sort_dataset_batch(SortDataset d, int64_t first, int32_t count, int32_t n_hi
  * GEMM as CTA pairs, default 0 for the same reason); "attn_bwd_mma" (1 = tensor-core
  * attention backward, the default; 0 = the fp32 SIMT kernels). Status 1 on an unknown name. */
 int sort_set_option(SortHandle h, const char* name, int32_t value);
+
+/* ---- pre-training (config field pretrain = 1) ---------------------------------------------
+ * pretrain_forward of a batch of click sequences (hist_* arrays, n_hist
+ * clicks each; req_ts/profile/cand_item unused): for every position t < n_hist of sequence
+ * b, lse[b, t] = log sum_v exp z[v] and target_logit[b, t] = z[click_t.item] with
+ * z = (RMSNorm(x_t; final_norm.gain) . pretrain.proj) . item_table^T over the full vocabulary.
+ * The next-item cross entropy of position t is lse - target_logit. Pointers follow
+ * sort_forward's host/device convention; outputs are [batch, n_hist] fp32. */
+int sort_pretrain_forward(SortHandle h, const SortBatch* batch, int inputs_on_device, float* lse,
+                          float* target_logit, int outputs_on_device);
 
 /* ---- MoE FFN (config fields moe_*) ------------------------------------
  * Routing of layer `layer` in the last forward: sel/weights [rows, moe_topk] host buffers

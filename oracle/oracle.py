@@ -95,6 +95,8 @@ def lib():
         L.oracle_moe_ffn.argtypes = [f64p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                      f64p, f64p, f64p, f64p, f64p, i32p, f64p, i32p, f64p]
         L.oracle_moe_update_bias.argtypes = [i64p, C.c_int, C.c_double, f64p]
+        L.oracle_pretrain_forward.argtypes = [C.c_void_p, C.POINTER(OrSample), f64p, f64p, f64p]
+        L.oracle_tokenize_clicks.argtypes = [C.c_void_p, C.POINTER(OrSample), f64p, i32p]
         _lib = L
     return _lib
 
@@ -319,6 +321,25 @@ class OracleModel:
         _check(lib().oracle_model_forward(self.h, C.byref(hold.s), _p(probs, f64p),
                                           _p(logits, f64p)))
         return probs, logits
+
+    def tokenize_clicks(self, batch, b: int = 0):
+        """tokenize_click_sequence (tokenizer.cpp:240-284) of sequence b's hist_* clicks."""
+        hold = _SampleHold(batch, b)
+        n = hold.s.n_hist
+        tokens = np.zeros((1 + n, self.cfg.model_dim))
+        ht = np.zeros(n, np.int32)
+        _check(lib().oracle_tokenize_clicks(self.h, C.byref(hold.s), _p(tokens, f64p), _p(ht, i32p)))
+        return tokens, ht
+
+    def pretrain_forward(self, batch, b: int = 0):
+        """pretrain_forward: (lse [n], target logit [n], h [1 + n, item_dim])."""
+        hold = _SampleHold(batch, b)
+        n = hold.s.n_hist
+        lse, tgt = np.zeros(n), np.zeros(n)
+        hp = np.zeros((1 + n, self.cfg.item_dim))
+        _check(lib().oracle_pretrain_forward(self.h, C.byref(hold.s), _p(lse, f64p), _p(tgt, f64p),
+                                             _p(hp, f64p)))
+        return lse, tgt, hp
 
     def forward_moe(self, batch, b: int = 0, forced=None):
         """Forward with MoE routing control: forced = list (per layer) of [l_q, k] expert ids or

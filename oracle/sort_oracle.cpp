@@ -659,12 +659,10 @@ struct MoeCtl {
 
 // model_forward: pre-norm residual blocks over a shrinking
 // residual stream, final RMSNorm, ranking head on candidate rows.
-void model_forward(const OrModel& mdl, const OrSample& s, double* probs, double* logits_out,
-                   std::vector<LayerTrace>* trace, MoeCtl* moe = nullptr) {
+// The block stack over x with its roles/positions, shrinking by query pruning.
+void blocks_forward(const OrModel& mdl, M& x, std::vector<int>& roles, std::vector<int>& pos,
+                    std::vector<LayerTrace>* trace, MoeCtl* moe) {
   size_t moe_off = 0, moe_row_off = 0;
-  Seq q = tokenize(mdl, s);
-  M x = q.tokens;
-  std::vector<int> roles = q.roles, pos = q.pos;
   const OrModelCfg& c = mdl.cfg;
   const int d = mdl.d;
   for (int l = 0; l < c.layers; ++l) {
@@ -709,6 +707,15 @@ void model_forward(const OrModel& mdl, const OrSample& s, double* probs, double*
     roles = std::move(nroles);
     pos = std::move(npos);
   }
+}
+
+void model_forward(const OrModel& mdl, const OrSample& s, double* probs, double* logits_out,
+                   std::vector<LayerTrace>* trace, MoeCtl* moe = nullptr) {
+  Seq q = tokenize(mdl, s);
+  M x = q.tokens;
+  std::vector<int> roles = q.roles, pos = q.pos;
+  const int d = mdl.d;
+  blocks_forward(mdl, x, roles, pos, trace, moe);
   // Final RMSNorm + head on candidate rows, candidates in order.
   std::vector<int> crows;
   for (int i = 0; i < x.r; ++i)
@@ -729,6 +736,88 @@ void model_forward(const OrModel& mdl, const OrSample& s, double* probs, double*
       if (logits_out) logits_out[i * 3 + j] = z;
       probs[i * 3 + j] = sigmoid(z);
     }
+}
+
+// ====================================================================== pre-training
+// Tokenizer::tokenize_click_sequence (tokenizer.cpp:240-284): [BOS; one token per click],
+// history projection of item|action|scene|time where the time slice is the bucket of the gap
+// to the previous click (the first click gets the bucket of INT64_MAX/4, :262-270);
+// positions 0..n, roles BOS + HIST.
+Seq tokenize_clicks(const OrModel& mdl, const OrSample& s) {
+  const OrModelCfg& c = mdl.cfg;
+  const int n = s.n_hist, d = mdl.d, total = 1 + n;
+  Seq q;
+  q.tokens = M(total, d);
+  q.pos.resize(total);
+  q.roles.assign(total, OR_ROLE_HIST);
+  q.cand_index.assign(total, -1);
+  q.hist_time.assign(n, 0);
+  std::memcpy(q.tokens.row(0), mdl.P("tok.special").row(0), sizeof(double) * d);
+  q.roles[0] = OR_ROLE_BOS;
+  const M& it = mdl.P("tok.item_table");
+  const M& at = mdl.P("tok.action_table");
+  const M& sc = mdl.P("tok.scene_table");
+  const M& tt = mdl.P("tok.time_table");
+  M cat(n, mdl.hist_width());
+  for (int i = 0; i < n; ++i) {
+    check_id(s.hist_item[i], c.n_items, "item");
+    check_id(s.hist_action[i], c.n_actions, "action");
+    check_id(s.hist_scene[i], c.n_scenes, "scene");
+    const int64_t gap = i == 0 ? std::numeric_limits<int64_t>::max() / 4 : s.hist_ts[i] - s.hist_ts[i - 1];
+    const int tb = time_bucket(gap, c.n_time_buckets);
+    double* o = cat.row(i);
+    std::memcpy(o, it.row(s.hist_item[i]), sizeof(double) * c.item_dim);
+    o += c.item_dim;
+    std::memcpy(o, at.row(s.hist_action[i]), sizeof(double) * c.action_dim);
+    o += c.action_dim;
+    std::memcpy(o, sc.row(s.hist_scene[i]), sizeof(double) * c.scene_dim);
+    o += c.scene_dim;
+    std::memcpy(o, tt.row(tb), sizeof(double) * c.time_dim);
+    q.hist_time[i] = tb;
+  }
+  if (n > 0) {
+    M proj = matmul(cat, mdl.P("tok.w_hist"));
+    const M& b = mdl.P("tok.b_hist");
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < d; ++j) proj(i, j) += b(0, j);
+    M y = rmsnorm(proj, mdl.P("tok.g_hist").row(0));
+    for (int i = 0; i < n; ++i) std::memcpy(q.tokens.row(1 + i), y.row(i), sizeof(double) * d);
+  }
+  for (int i = 0; i < total; ++i) q.pos[i] = i;
+  return q;
+}
+
+// pretrain_forward: the block stack as a causal LM over [BOS; clicks]
+// (no candidates, local window and pruning off by config), final RMSNorm,
+// projection to the item-embedding width (pretrain.proj [d, item_dim], the builder's bridge
+// between d and the table) and tied logits z_t[v] = h_t . item_table[v]. Position t (< n)
+// predicts click t: lse[t] = log sum_v exp z_t[v], target[t] = z_t[click_t].
+void pretrain_forward(const OrModel& mdl, const OrSample& s, double* lse, double* target, double* hproj) {
+  if (s.n_hist < 2) throw ConfigError("pretrain: sequences shorter than 2 clicks are skipped");
+  Seq q = tokenize_clicks(mdl, s);
+  M x = q.tokens;
+  std::vector<int> roles = q.roles, pos = q.pos;
+  blocks_forward(mdl, x, roles, pos, nullptr, nullptr);
+  if (x.r != s.n_hist + 1) throw ConfigError("pretrain: query pruning must be off");
+  M h = matmul(rmsnorm(x, mdl.P("final_norm.gain").row(0)), mdl.P("pretrain.proj"));
+  const M& E = mdl.P("tok.item_table");
+  const int V = E.r, k = E.c;
+  if (h.c != k) throw ConfigError("pretrain: projection width must equal item_dim");
+  std::vector<double> z(V);
+  for (int t = 0; t < s.n_hist; ++t) {
+    double mx = -std::numeric_limits<double>::infinity();
+    for (int v = 0; v < V; ++v) {
+      double a = 0.0;
+      for (int j = 0; j < k; ++j) a += h(t, j) * E(v, j);
+      z[v] = a;
+      mx = std::max(mx, a);
+    }
+    double se = 0.0;
+    for (int v = 0; v < V; ++v) se += std::exp(z[v] - mx);
+    lse[t] = mx + std::log(se);
+    target[t] = z[s.hist_item[t]];
+  }
+  if (hproj) std::memcpy(hproj, h.a.data(), sizeof(double) * h.r * h.c);
 }
 
 // ====================================================================== backward
@@ -1249,6 +1338,18 @@ int oracle_moe_update_bias(const int64_t* load, int n_experts, double gamma, dou
       const double dlt = static_cast<double>(load[e]) - mean;
       bias[e] -= gamma * (dlt > 0 ? 1.0 : (dlt < 0 ? -1.0 : 0.0));
     }
+  });
+}
+
+int oracle_pretrain_forward(const OrModel* m, const OrSample* s, double* lse, double* target, double* hproj) {
+  return guarded([&] { pretrain_forward(*m, *s, lse, target, hproj); });
+}
+
+int oracle_tokenize_clicks(const OrModel* m, const OrSample* s, double* tokens, int* hist_time) {
+  return guarded([&] {
+    Seq q = tokenize_clicks(*m, *s);
+    std::memcpy(tokens, q.tokens.a.data(), sizeof(double) * q.tokens.a.size());
+    if (hist_time) std::copy(q.hist_time.begin(), q.hist_time.end(), hist_time);
   });
 }
 

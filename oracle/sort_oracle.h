@@ -136,6 +136,13 @@ int oracle_model_forward(const OrModel* m, const OrSample* s, double* probs, dou
 int oracle_model_forward_moe(const OrModel* m, const OrSample* s, const int* forced_sel, double* probs,
                              double* logits, int* out_sel, double* out_margin);
 
+/* Pre-training: click sequence = s->hist_* (n_hist clicks; timestamp,
+ * profile and candidates unused). tokens [1 + n, d] (tokenize_click_sequence,
+ * tokenizer.cpp:240-284); forward: lse[t], target[t] (logit of click t) for t < n, hproj
+ * [1 + n, item_dim] the projected hidden rows (may be NULL). */
+int oracle_tokenize_clicks(const OrModel* m, const OrSample* s, double* tokens, int* hist_time);
+int oracle_pretrain_forward(const OrModel* m, const OrSample* s, double* lse, double* target, double* hproj);
+
 /* --- MoE FFN operators -------------------------------- */
 /* route_topk, DeepSeek style: s_e = sigmoid(x . router[:, e]); selection = top-k of s_e + bias_e
  * in descending order, ties -> lower index; weights w_j = s_{e_j} / sum_j s_{e_j} (bias never

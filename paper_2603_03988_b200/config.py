@@ -77,6 +77,8 @@ class SortConfig:
     moe_topk: int = 1
     moe_shared: int = 1
     moe_ffn_dim: int = 0
+    # generative pre-training model: click sequences [BOS; clicks]
+    pretrain: bool = False
     # mask / pruning
     local_window: int = 32
     full_suffix: int = 128
@@ -97,6 +99,8 @@ class SortConfig:
 
     @property
     def seq_len(self) -> int:
+        if self.pretrain:  # [BOS; clicks] (tokenizer.cpp:243)
+            return 1 + self.n_hist
         # L = 1 + H + 1 + |U| + 1 + N (tokenizer.cpp:158-159)
         return (3 if self.special_tokens else 0) + self.n_hist + self.n_prof + self.n_cand
 
@@ -148,6 +152,15 @@ def base_moe_config(**kw) -> SortConfig:
     ffn_dim / 2 = 320 so the activated FFN width (shared + routed) equals the dense 640 (the
     spec's sizing rule)."""
     c = base_config(moe_experts=8, moe_topk=1, moe_shared=1, moe_ffn_dim=320)
+    return dataclasses.replace(c, **kw)
+
+
+def pretrain_config(**kw) -> SortConfig:
+    """SURVEY.md section 8(f) "next 4": the SORT-base block stack as a causal next-item model
+    over click sequences (no candidates, no local window, no pruning),
+    1024 clicks per sequence, 64 sequences, a 65,536-item vocabulary with the full softmax."""
+    c = SortConfig(model_dim=256, heads=8, layers=4, ffn_dim=640, local_window=-1, full_suffix=0,
+                   n_hist=1024, n_cand=0, profile_vocab=[], batch=64, n_items=65536, pretrain=True)
     return dataclasses.replace(c, **kw)
 
 

@@ -207,7 +207,14 @@ void validate_config(const SortConfig& c) {
   for (int l = 0; l + 1 < c.layers; ++l)
     need(c.keep[l + 1] <= c.keep[l], "PruneSchedule: keep counts must be non-increasing");
   for (int l = 0; l < c.layers; ++l) need(c.keep[l] >= 1, "PruneSchedule: keep counts must be >= 1");
-  need(c.n_cand >= 1, "tokenizer: sample has zero candidates");
+  if (c.pretrain) {  // click-sequence model
+    need(c.n_cand == 0 && c.n_profile_fields == 0, "pretrain: sequences have no candidates or profile");
+    need(c.n_hist >= 2, "pretrain: sequences shorter than 2 clicks are skipped");
+    for (int l = 0; l < c.layers; ++l) need(c.keep[l] >= 1 + c.n_hist, "pretrain: query pruning must be off");
+    need(c.moe_experts == 0 && c.model_dim <= 256, "unsupported: pretrain with MoE or model_dim > 256");
+  } else {
+    need(c.n_cand >= 1, "tokenizer: sample has zero candidates");
+  }
   need(c.n_hist >= 0 && c.max_batch >= 1, "batch geometry");
   // MoE FFN: SparsityConfig invariants 1 <= k <= E
   need(c.moe_experts >= 0 && c.moe_experts <= 64, "unsupported: moe_experts must be in [0, 64]");
@@ -228,12 +235,17 @@ Plan make_plan(const SortConfig& c) {
   auto push = [&](int role, int n) {
     for (int i = 0; i < n; ++i) P.roles0.push_back(role);
   };
-  if (st) push(SORT_ROLE_BOS, 1);
-  push(SORT_ROLE_HIST, c.n_hist);
-  if (st) push(SORT_ROLE_SEP, 1);
-  push(SORT_ROLE_PROF, c.n_profile_fields);
-  if (st) push(SORT_ROLE_SEP, 1);
-  push(SORT_ROLE_CAND, c.n_cand);
+  if (c.pretrain) {  // [BOS; clicks] (tokenizer.cpp:243-256)
+    push(SORT_ROLE_BOS, 1);
+    push(SORT_ROLE_HIST, c.n_hist);
+  } else {
+    if (st) push(SORT_ROLE_BOS, 1);
+    push(SORT_ROLE_HIST, c.n_hist);
+    if (st) push(SORT_ROLE_SEP, 1);
+    push(SORT_ROLE_PROF, c.n_profile_fields);
+    if (st) push(SORT_ROLE_SEP, 1);
+    push(SORT_ROLE_CAND, c.n_cand);
+  }
   P.L0 = static_cast<int>(P.roles0.size());
   P.prefix = P.L0 - c.n_cand;
   P.pos0.resize(P.L0);

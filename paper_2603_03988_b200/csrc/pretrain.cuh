@@ -1,0 +1,229 @@
+// SPDX-License-Identifier: Apache-2.0
+// Generative pre-training head: next-item logits tied to the item table.
+//
+//   h_t   = RMSNorm(x_t; final_norm.gain) . pretrain.proj          [T, K]  (K = item_dim)
+//   z_t[v] = h_t . item_table[v]                                    over the full vocabulary
+//   lse_t = log sum_v exp z_t[v],  target_t = z_t[click_t]          (CE_t = lse_t - target_t)
+//
+// k_pretrain_proj: one warp per token row (final norm in fp32, projection from a shared-memory
+//   copy of pretrain.proj, bf16 h_t, the target logit from the bf16 h_t and the target row).
+// k_ce_tied: the [T, K] x [K, V] logit GEMM never reaches HBM: each CTA holds 128 rows of h
+//   as mma.sync A fragments, streams the item table through a cp.async double buffer in
+//   64-item tiles and folds every logit into a per-row online log-sum-exp (exp2 domain), the
+//   way attention folds QK^T without materialising it.
+#pragma once
+
+#include "train.cuh"
+
+namespace sortk {
+
+constexpr int kPreK = 32;          // item_dim of the tied head
+constexpr int kCeRows = 128;       // rows per CTA (4 warps x 32)
+constexpr int kCeItems = 64;       // items per streamed tile
+constexpr int kCePitch = 80;       // smem bytes per item row (64 + 16: conflict-free fragments)
+
+// One warp per row r = b * L + t of the final residual stream.
+__global__ void __launch_bounds__(256) k_pretrain_proj(const __nv_bfloat16* __restrict__ x, int T, int L, int d,
+                                                       const float* __restrict__ gain, const float* __restrict__ proj,
+                                                       const __nv_bfloat16* __restrict__ items,
+                                                       const int32_t* __restrict__ click_item,
+                                                       __nv_bfloat16* __restrict__ hp, float* __restrict__ tgt) {
+  extern __shared__ float smem_f[];
+  float* sW = smem_f;                                        // [d][K]
+  float* sx = smem_f + d * kPreK + (threadIdx.x >> 5) * d;   // this warp's normalised row
+  for (int i = threadIdx.x; i < d * kPreK; i += blockDim.x) sW[i] = proj[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int c0 = lane * 8;
+  const bool act = c0 < d;
+  const int n = L - 1;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < T; r += warps) {
+    float v[8];
+    if (act) {
+      const int4 raw = *reinterpret_cast<const int4*>(x + static_cast<size_t>(r) * d + c0);
+      const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(p2[i]);
+        v[2 * i] = f.x;
+        v[2 * i + 1] = f.y;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = 0.f;
+    }
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ss = fmaf(v[i], v[i], ss);
+    const float inv = rsqrtf(warp_sum(ss) / static_cast<float>(d) + 1e-6f);  // norm.hpp:23-24
+    if (act) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sx[c0 + i] = v[i] * inv * gain[c0 + i];
+    }
+    __syncwarp();
+    float a = 0.f;  // lane j: h_j = sum_c xh[c] W[c][j]
+    for (int c = 0; c < d; ++c) a = fmaf(sx[c], sW[c * kPreK + lane], a);
+    __syncwarp();
+    const __nv_bfloat16 hb = __float2bfloat16_rn(a);
+    hp[static_cast<size_t>(r) * kPreK + lane] = hb;
+    const int b = r / L, t = r - b * L;
+    if (t < n) {  // position t predicts click t
+      const int item = click_item[static_cast<size_t>(b) * n + t];
+      float z = __bfloat162float(hb) * __bfloat162float(items[static_cast<size_t>(item) * kPreK + lane]);
+      z = warp_sum(z);
+      if (lane == 0) tgt[static_cast<size_t>(b) * n + t] = z;
+    }
+  }
+}
+
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool pred) {
+  const uint32_t s = smem_u32(dst);
+  const int n = pred ? 16 : 0;  // src-size 0 -> zero fill
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(src), "r"(n) : "memory");
+}
+
+// lse[b, t] over the full vocabulary for the rows of 128-row block blockIdx.x.
+__global__ void __launch_bounds__(128) k_ce_tied(const __nv_bfloat16* __restrict__ hp, int T, int L,
+                                                 const __nv_bfloat16* __restrict__ items, int V,
+                                                 float* __restrict__ lse) {
+  __shared__ __align__(16) uint8_t sB[2][kCeItems * kCePitch];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  const int row0 = blockIdx.x * kCeRows + warp * 32;
+  // A fragments: 2 m16 tiles x 2 k16 steps (K = 32)
+  uint32_t a[2][2][4];
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r = row0 + mt * 16 + g + ((q & 1) ? 8 : 0);
+        const int k = ks * 16 + 2 * tq + ((q & 2) ? 8 : 0);
+        a[mt][ks][q] = r < T ? *reinterpret_cast<const uint32_t*>(hp + static_cast<size_t>(r) * kPreK + k) : 0u;
+      }
+  const int n_tiles = (V + kCeItems - 1) / kCeItems;
+  auto stage = [&](int tile, int buf) {
+    // 64 items x 64 B = 256 16-byte chunks, 2 per thread
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int ch = threadIdx.x + i * 128;
+      const int it = ch >> 2, part = ch & 3;
+      const int v = tile * kCeItems + it;
+      cp_async16(sB[buf] + it * kCePitch + part * 16,
+                 items + static_cast<size_t>(v < V ? v : 0) * kPreK + part * 8, v < V);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  constexpr float kLog2e = 1.4426950408889634f;
+  float m[4], s[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    m[i] = -INFINITY;
+    s[i] = 0.f;
+  }
+  stage(0, 0);
+  for (int tile = 0; tile < n_tiles; ++tile) {
+    const int buf = tile & 1;
+    if (tile + 1 < n_tiles) {
+      stage(tile + 1, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    float c[2][8][4];
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) c[mt][nt][q] = 0.f;
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      const uint8_t* brow = sB[buf] + (nt * 8 + g) * kCePitch;
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(brow + (ks * 16 + 2 * tq) * 2);
+        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(brow + (ks * 16 + 2 * tq + 8) * 2);
+        mma_bf16_16816(c[0][nt], a[0][ks], b0, b1);
+        mma_bf16_16816(c[1][nt], a[1][ks], b0, b1);
+      }
+    }
+    __syncthreads();  // buffer `buf` is restaged two tiles later
+    // online log-sum-exp (exp2 domain): raw maxima, one FFMA per logit for the argument,
+    // 3 of every 8 column pairs through the FMA-pipe polynomial to offload the MUFU
+    if (tile == n_tiles - 1) {  // vocabulary tail: columns >= V never count
+      const int vbase = tile * kCeItems + 2 * tq;
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt)
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (vbase + nt * 8 + (q & 1) >= V) c[mt][nt][q] = -INFINITY;
+    }
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        const int slot = mt * 2 + hf;
+        float zmax = -INFINITY;
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) zmax = fmaxf(zmax, fmaxf(c[mt][nt][hf * 2], c[mt][nt][hf * 2 + 1]));
+        const float mn = fmaxf(m[slot], zmax);
+        if (mn == -INFINITY) continue;  // no valid column seen yet (V < 64 tails)
+        const float ms = mn * kLog2e;
+        float2 acc = make_float2(m[slot] == -INFINITY ? 0.f : s[slot] * ex2_approx(fmaf(m[slot], kLog2e, -ms)), 0.f);
+#pragma unroll
+        for (int nt = 0; nt < 8; ++nt) {
+          const float2 arg = ffma2(make_float2(c[mt][nt][hf * 2], c[mt][nt][hf * 2 + 1]),
+                                   make_float2(kLog2e, kLog2e), make_float2(-ms, -ms));
+          float2 e;
+          if (nt % 3 == 1) {
+            e = ex2_poly2(arg);
+          } else {
+            e.x = ex2_approx(arg.x);
+            e.y = ex2_approx(arg.y);
+          }
+          acc = fadd2(acc, e);
+        }
+        m[slot] = mn;
+        s[slot] = acc.x + acc.y;
+      }
+  }
+  // combine the 4 threads of a quad (same rows, different columns)
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+      const float mo = __shfl_xor_sync(0xffffffffu, m[i], o), so = __shfl_xor_sync(0xffffffffu, s[i], o);
+      const float mn = fmaxf(m[i], mo);
+      if (mn == -INFINITY) continue;
+      s[i] = (m[i] == -INFINITY ? 0.f : s[i] * ex2_approx((m[i] - mn) * kLog2e)) +
+             (mo == -INFINITY ? 0.f : so * ex2_approx((mo - mn) * kLog2e));
+      m[i] = mn;
+    }
+  }
+  if (tq == 0) {
+    const int n = L - 1;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = row0 + (i >> 1) * 16 + g + ((i & 1) ? 8 : 0);
+      if (r >= T) continue;
+      const int b = r / L, t = r - b * L;
+      if (t < n) lse[static_cast<size_t>(b) * n + t] = m[i] + log2f(s[i]) * 0.6931471805599453f;
+    }
+  }
+}
+
+}  // namespace sortk

@@ -23,6 +23,7 @@
 #include "train.cuh"
 #include "generic.cuh"
 #include "moe.cuh"
+#include "pretrain.cuh"
 
 namespace sortk {
 
@@ -94,6 +95,10 @@ struct Handle {
           *moe_tile_group = nullptr, *moe_ntiles = nullptr, *moe_counts = nullptr;  // counts [layers][E]
   int moe_rows[SORT_MAX_LAYERS] = {0};  // rows routed per layer in the last forward
   CUtensorMap tmA_moe_xs, tmA_moe_hs;
+  // ---- pre-training head
+  const float* pre_proj = nullptr;  // pretrain.proj [d, item_dim] in the master buffer
+  __nv_bfloat16* pre_hp = nullptr;  // projected rows [B * L, item_dim]
+  float *pre_lse = nullptr, *pre_tgt = nullptr;  // [B, n_hist]
   // row-sharded item table (sort_set_item_table): the batch's item rows, gathered from the
   // owning ranks, replace the handle's table for the following calls
   const __nv_bfloat16* item_ext = nullptr;
@@ -506,11 +511,19 @@ static void finalize(Handle& h) {
     }
   }
   // ---- head (fp32)
-  h.head_gain = h.upload(need_param(h, "final_norm.gain", 1, d).v);
-  h.head_w1 = h.upload(need_param(h, "head.w1", d, h.dh).v);
-  h.head_b1 = h.upload(need_param(h, "head.b1", 1, h.dh).v);
-  h.head_w2 = h.upload(need_param(h, "head.w2", h.dh, 3).v);
-  h.head_b2 = h.upload(need_param(h, "head.b2", 1, 3).v);
+  need_param(h, "final_norm.gain", 1, d);
+  if (c.pretrain) {
+    if (c.item_dim != kPreK) throw ConfigError("pretrain: the tied head needs item_dim == 32 in this build");
+    need_param(h, "pretrain.proj", d, c.item_dim);
+    h.pre_hp = h.dalloc<__nv_bfloat16>(static_cast<size_t>(h.Bmax) * h.L0 * kPreK);
+    h.pre_lse = h.dalloc<float>(static_cast<size_t>(h.Bmax) * c.n_hist);
+    h.pre_tgt = h.dalloc<float>(static_cast<size_t>(h.Bmax) * c.n_hist);
+  } else {
+    need_param(h, "head.w1", d, h.dh);
+    need_param(h, "head.b1", 1, h.dh);
+    need_param(h, "head.w2", h.dh, 3);
+    need_param(h, "head.b2", 1, 3);
+  }
   // fp32 copies of the differentiated parameters (training backward), and the flat gradient
   // buffer in the same name order; W_gate | W_up also concatenated as ffn.<l>.w_gu [d, 2m]
   // Trainable parameters: every tensor except the (frozen) item table, one flat fp32 master
@@ -543,6 +556,7 @@ static void finalize(Handle& h) {
   // fp32 parameters the inference kernels read directly now live in the master buffer, so
   // an optimizer step updates them in place
   h.head_gain = h.w32["final_norm.gain"];
+  if (c.pretrain) h.pre_proj = h.w32["pretrain.proj"];
   h.head_w1 = h.w32["head.w1"];
   h.head_b1 = h.w32["head.b1"];
   h.head_w2 = h.w32["head.w2"];
@@ -843,6 +857,7 @@ static TokParams tok_params(Handle& h, int B) {
   p.n_scenes = c.n_scenes;
   p.n_tb = c.n_time_buckets;
   p.special_tokens = c.special_tokens;
+  p.click_seq = c.pretrain;
   p.tiles_hist = (B * c.n_hist + 127) / 128;
   p.tiles_cand = (B * c.n_cand + 127) / 128;
   p.tiles_prof = (B * c.n_profile_fields + 127) / 128;
@@ -1101,6 +1116,7 @@ static void build_bwd_lists(const LayerPlan& lp, std::vector<int32_t>& dq_off, s
 }
 
 static void ensure_train_buffers(Handle& h, int B) {
+  if (h.cfg.pretrain) throw ConfigError("training step: use the ranking model (pretrain backward not in this build)");
   if (h.moe) throw ConfigError("training step: the MoE FFN backward is not implemented in this build");
   if (h.train_B >= B) return;
   if (!h.cublas) {
@@ -1649,6 +1665,24 @@ static void forward_device(Handle& h, int B) {
   stage_mark(h, "tokenizer");
   for (int l = 0; l < h.cfg.layers; ++l) run_layer(h, l, B);
   const LayerDev& last = h.layers.back();
+  if (h.cfg.pretrain) {  // tied next-item head, see pretrain.cuh
+    const int T = B * h.L0;
+    const size_t psmem = (static_cast<size_t>(h.d) * kPreK + 8 * h.d) * sizeof(float);
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(k_pretrain_proj, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+      attr = true;
+    }
+    const __nv_bfloat16* items = h.item_ext ? h.item_ext : h.item;
+    const int V = h.item_ext ? static_cast<int>(h.item_ext_rows) : h.cfg.n_items;
+    k_pretrain_proj<<<std::max(1, std::min((T + 7) / 8, 8 * h.num_sms)), 256, psmem, h.stream>>>(
+        h.X[last.q_buf], T, h.L0, h.d, h.head_gain, h.pre_proj, items, h.in_item, h.pre_hp, h.pre_tgt);
+    k_ce_tied<<<(T + kCeRows - 1) / kCeRows, 128, 0, h.stream>>>(h.pre_hp, T, h.L0, items, V, h.pre_lse);
+    check_launch("pretrain head");
+    h.launches += 2;
+    stage_mark(h, "head");
+    return;
+  }
   const int total = B * h.cfg.n_cand;
   const size_t hsmem = static_cast<size_t>(kHeadRows) * h.d * sizeof(float);
   const int hgrid = (total + kHeadRows - 1) / kHeadRows;
@@ -1817,6 +1851,7 @@ int sort_forward(SortHandle p, const SortBatch* batch, int inputs_on_device, flo
   return api([&] {
     Handle* h = ready(p);
     if (!batch || !scores) throw ConfigError("null argument");
+    if (h->cfg.pretrain) throw ConfigError("pre-training model: use sort_pretrain_forward");
     begin_timing(*h);
     upload_batch(*h, batch, inputs_on_device != 0);
     forward_device(*h, batch->batch);
@@ -2212,6 +2247,23 @@ int sort_gather_rows(const void* table, int64_t n_rows, int32_t row_bytes, const
     CK(cudaFreeAsync(err, static_cast<cudaStream_t>(stream)));
     CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
     if (herr) throw ConfigError("gather rows: id outside the table shard");
+  });
+}
+
+int sort_pretrain_forward(SortHandle p, const SortBatch* batch, int inputs_on_device, float* lse,
+                          float* target_logit, int outputs_on_device) {
+  return api([&] {
+    Handle* h = ready(p);
+    if (!batch || !lse || !target_logit) throw ConfigError("null argument");
+    if (!h->cfg.pretrain) throw ConfigError("sort_pretrain_forward needs a pre-training model (pretrain = 1)");
+    begin_timing(*h);
+    upload_batch(*h, batch, inputs_on_device != 0);
+    forward_device(*h, batch->batch);
+    const size_t bytes = static_cast<size_t>(batch->batch) * h->cfg.n_hist * sizeof(float);
+    const cudaMemcpyKind k = outputs_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    CK(cudaMemcpyAsync(lse, h->pre_lse, bytes, k, h->stream));
+    CK(cudaMemcpyAsync(target_logit, h->pre_tgt, bytes, k, h->stream));
+    if (!(inputs_on_device && outputs_on_device)) collect_status(*h);
   });
 }
 

@@ -54,6 +54,7 @@ struct TokParams {
   int item_dim, action_dim, scene_dim, time_dim, prof_dim;
   int n_items, n_actions, n_scenes, n_tb;
   int special_tokens;
+  int click_seq;  // tokenize_click_sequence (tokenizer.cpp:240-284): [BOS; clicks], gap buckets
   int tiles_hist, tiles_cand, tiles_prof;
 };
 
@@ -103,7 +104,7 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
   const uint32_t idesc = umma_idesc_bf16(128, d);
 
   const int n_tiles = p.tiles_hist + p.tiles_cand + p.tiles_prof;
-  const int st = p.special_tokens ? 1 : 0;
+  const int st = p.special_tokens || p.click_seq ? 1 : 0;
   const int off_hist = st, off_prof = st + p.H + st, off_cand = off_prof + p.P + st;
   auto group_of = [&](int tile, int& e0, int& count) {
     if (tile < p.tiles_hist) {
@@ -136,7 +137,11 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
         if (group == kGroupHist) {
           const int b = e / p.H, i = e - b * p.H;
           int item = p.hist_item[e], act = p.hist_action[e], sc = p.hist_scene[e];
-          const int tb = tok_time_bucket(p.req_ts[b] - p.hist_ts[e], p.n_tb);
+          // click sequences: the gap to the previous click, the first click at INT64_MAX / 4
+          // (tokenizer.cpp:262-270); requests: request time - event time (:95-112)
+          const int64_t delta = p.click_seq ? (i == 0 ? 0x1FFFFFFFFFFFFFFFll : p.hist_ts[e] - p.hist_ts[e - 1])
+                                            : p.req_ts[b] - p.hist_ts[e];
+          const int tb = tok_time_bucket(delta, p.n_tb);
           if (static_cast<unsigned>(item) >= static_cast<unsigned>(p.n_items) ||
               static_cast<unsigned>(act) >= static_cast<unsigned>(p.n_actions) ||
               static_cast<unsigned>(sc) >= static_cast<unsigned>(p.n_scenes)) {
@@ -281,10 +286,11 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
     __syncthreads();
   }
   // ---- BOS / SEP rows: raw special-table rows (tokenizer.cpp:171-176), one warp per row.
-  if (p.special_tokens) {
+  if (p.special_tokens || p.click_seq) {
     const int nwarps = gridDim.x * (kTokThreads / 32);
-    for (int w = blockIdx.x * (kTokThreads / 32) + warp; w < p.B * 3; w += nwarps) {
-      const int b = w / 3, k = w - b * 3;
+    const int per = p.click_seq ? 1 : 3;  // click sequences carry BOS only
+    for (int w = blockIdx.x * (kTokThreads / 32) + warp; w < p.B * per; w += nwarps) {
+      const int b = w / per, k = w - b * per;
       const int row = b * p.L + (k == 0 ? 0 : (k == 1 ? 1 + p.H : 2 + p.H + p.P));
       float ss = 0.f;
       for (int c = lane; c < d; c += 32) {

@@ -26,6 +26,8 @@ from .config import ROLE_BOS, ROLE_CAND, ROLE_HIST, ROLE_PROF, ROLE_SEP, SortCon
 
 
 def sequence_structure(cfg: SortConfig):
+    if cfg.pretrain:  # [BOS; clicks] (tokenize_click_sequence, tokenizer.cpp:243-256)
+        return [ROLE_BOS] + [ROLE_HIST] * cfg.n_hist, list(range(1 + cfg.n_hist))
     roles: List[int] = []
     if cfg.special_tokens:
         roles.append(ROLE_BOS)

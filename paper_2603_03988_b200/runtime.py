@@ -39,7 +39,7 @@ class CSortConfig(C.Structure):
         ("keep", C.c_int32 * 64), ("keep_specials", C.c_int32),
         ("max_batch", C.c_int32), ("n_hist", C.c_int32), ("n_cand", C.c_int32),
         ("moe_experts", C.c_int32), ("moe_topk", C.c_int32), ("moe_shared", C.c_int32),
-        ("moe_ffn_dim", C.c_int32),
+        ("moe_ffn_dim", C.c_int32), ("pretrain", C.c_int32),
     ]
 
 
@@ -61,7 +61,7 @@ EXPORTS = [
     "sort_set_item_table", "sort_gather_rows", "sort_train_step_bce", "sort_adamw_step",
     "sort_get_param", "sort_dataset_open", "sort_dataset_close", "sort_dataset_size",
     "sort_dataset_batch", "sort_moe_routing", "sort_moe_load", "sort_moe_update_bias",
-    "sort_moe_forward",
+    "sort_moe_forward", "sort_pretrain_forward",
 ]
 
 _lib = None
@@ -109,6 +109,7 @@ def lib():
         L.sort_moe_load.argtypes = [C.c_void_p, C.c_int, i64p]
         L.sort_moe_update_bias.argtypes = [C.c_void_p, C.c_double]
         L.sort_moe_forward.argtypes = [C.c_void_p, C.c_int, f32p, C.c_int, f32p]
+        L.sort_pretrain_forward.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int]
         L.sort_dataset_open.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
         L.sort_dataset_close.argtypes = [C.c_void_p]
         L.sort_dataset_size.argtypes = [C.c_void_p]
@@ -156,6 +157,7 @@ def to_c_config(cfg: SortConfig, max_batch: Optional[int] = None) -> CSortConfig
     c.n_hist, c.n_cand = cfg.n_hist, cfg.n_cand
     c.moe_experts, c.moe_topk = cfg.moe_experts, cfg.moe_topk
     c.moe_shared, c.moe_ffn_dim = cfg.moe_shared, cfg.moe_ffn_dim
+    c.pretrain = int(cfg.pretrain)
     return c
 
 
@@ -280,6 +282,21 @@ class SortModel:
         """Batch-local item rows (device bf16 [n_rows, item_dim]) for the next calls; ptr=0
         restores the handle's own table."""
         _check(lib().sort_set_item_table(self.h, C.c_void_p(ptr) if ptr else None, int(n_rows)))
+
+    # -- pre-training (SPEC.md:390-398) -----------------------------------------
+    def pretrain_forward(self, batch: Dict[str, np.ndarray]):
+        """(lse [B, n], target_logit [B, n]) of the tied next-item head; CE = lse - target."""
+        hold = _BatchHold(batch)
+        B, n = hold.c.batch, self.cfg.n_hist
+        lse = np.zeros((B, n), np.float32)
+        tgt = np.zeros((B, n), np.float32)
+        _check(lib().sort_pretrain_forward(self.h, C.byref(hold.c), 0, lse.ctypes.data, tgt.ctypes.data, 0))
+        return lse, tgt
+
+    def pretrain_forward_device(self, dev_batch: "_DevBatch", lse_ptr: int, tgt_ptr: int):
+        """Device-resident inputs and outputs: enqueue only (no host sync)."""
+        _check(lib().sort_pretrain_forward(self.h, C.byref(dev_batch.c), 1, C.c_void_p(lse_ptr),
+                                           C.c_void_p(tgt_ptr), 1))
 
     # -- MoE FFN (SPEC.md:272-351) ----------------------------------------------
     def moe_routing(self, layer: int, rows: int):

@@ -79,6 +79,8 @@ def param_shapes(cfg: SortConfig) -> Dict[str, tuple]:
     }
     for f, v in enumerate(cfg.profile_vocab):
         s[f"tok.profile_table.{f}"] = (v, cfg.profile_dim)
+    if cfg.pretrain:  # tied next-item head: hidden -> item-embedding width
+        s["pretrain.proj"] = (d, cfg.item_dim)
     for l in range(cfg.layers):
         for w in ("wq", "wk", "wv", "wo", "wg"):
             s[f"attn.{l}.{w}"] = (d, d)

@@ -1,0 +1,77 @@
+# SPDX-License-Identifier: Apache-2.0
+"""GPU parity of the pre-training path (SURVEY.md section 8(f) "next 4")
+through the C ABI against the fp64 oracle: click-sequence tokens (gap time buckets bit-exact,
+rows within TOKEN_TOL), per-position log-sum-exp and target logit of the tied next-item head
+(LSE_MAX_ABS, CE_REL_L2), and causality (an edit to click j leaves the log-sum-exp of every
+earlier position bit-identical)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2603_03988_b200 import runtime as R
+from paper_2603_03988_b200 import synth
+from paper_2603_03988_b200.config import pretrain_config
+
+pytestmark = pytest.mark.gpu
+
+TOKEN_TOL = 1.0 / 64   # bf16 token rows, O(1) values
+LSE_REL = 1e-2         # |lse_gpu - lse_ref| <= LSE_REL * max(1, |lse_ref|): bf16 residual stream,
+                       # bf16 projected rows and item table (logits here reach |z| ~ 20)
+CE_REL_L2 = 3e-2       # ||ce_gpu - ce_ref|| / ||ce_ref||, ce = lse - target
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def small(**kw):
+    c = dict(model_dim=64, heads=4, layers=2, ffn_dim=160, n_hist=200, batch=2, n_items=300)
+    c.update(kw)
+    return pretrain_config(**c)
+
+
+@pytest.mark.parametrize("which", ["small", "base"])
+def test_pretrain_vs_oracle(which):
+    cfg = small() if which == "small" else pretrain_config(batch=2, n_hist=512, n_items=20000)
+    B = 2
+    P = synth.make_params(cfg, seed=41)
+    gm = R.SortModel(cfg, P, max_batch=B)
+    om = O.OracleModel(cfg, P)
+    batch = synth.make_batch(cfg, B, seed=42)
+    tk = gm.tokenize(batch)
+    assert tk["position_ids"].tolist() == list(range(cfg.seq_len))
+    assert tk["roles"].tolist() == [0] + [1] * cfg.n_hist
+    lse, tgt = gm.pretrain_forward(batch)
+    for b in range(B):
+        ref_tok, ref_ht = om.tokenize_clicks(batch, b)
+        np.testing.assert_array_equal(tk["hist_time"][b], ref_ht)
+        assert np.max(np.abs(tk["tokens"][b] - ref_tok)) < TOKEN_TOL
+        rl, rt, _ = om.pretrain_forward(batch, b)
+        assert np.all(np.abs(lse[b] - rl) <= LSE_REL * np.maximum(1.0, np.abs(rl)))
+        assert np.all(np.abs(tgt[b] - rt) <= LSE_REL * np.maximum(1.0, np.abs(rl)))
+        assert rel_l2(lse[b] - tgt[b], rl - rt) < CE_REL_L2
+
+
+def test_pretrain_causality_bit_identical():
+    cfg = small()
+    P = synth.make_params(cfg, seed=43)
+    gm = R.SortModel(cfg, P, max_batch=2)
+    batch = synth.make_batch(cfg, 2, seed=44)
+    lse, tgt = gm.pretrain_forward(batch)
+    j = 137
+    b2 = {k: v.copy() for k, v in batch.items()}
+    b2["hist_item"][1, j] = (b2["hist_item"][1, j] + 7) % cfg.n_items
+    lse2, tgt2 = gm.pretrain_forward(b2)
+    np.testing.assert_array_equal(lse2[0], lse[0])            # other sequence untouched
+    np.testing.assert_array_equal(lse2[1, :j + 1], lse[1, :j + 1])
+    np.testing.assert_array_equal(tgt2[1, :j], tgt[1, :j])
+    assert np.abs(lse2[1, j + 1:] - lse[1, j + 1:]).max() > 0
+
+
+def test_pretrain_uniform_vocab_ce_is_ln_v():
+    cfg = small(n_items=100)
+    P = synth.make_params(cfg, seed=45)
+    P["tok.item_table"][:] = P["tok.item_table"][0]
+    gm = R.SortModel(cfg, P, max_batch=1)
+    lse, tgt = gm.pretrain_forward(synth.make_batch(cfg, 1, seed=46))
+    np.testing.assert_allclose(lse - tgt, np.log(100.0), atol=2e-3)
