@@ -19,6 +19,7 @@ namespace sortk {
 
 constexpr int kPreK = 32;          // item_dim of the tied head
 constexpr int kCeRows = 128;       // rows per CTA (4 warps x 32)
+constexpr int kCeThreads = 128;
 constexpr int kCeItems = 64;       // items per streamed tile
 constexpr int kCePitch = 80;       // smem bytes per item row (64 + 16: conflict-free fragments)
 
@@ -62,8 +63,15 @@ __global__ void __launch_bounds__(256) k_pretrain_proj(const __nv_bfloat16* __re
       for (int i = 0; i < 8; ++i) sx[c0 + i] = v[i] * inv * gain[c0 + i];
     }
     __syncwarp();
-    float a = 0.f;  // lane j: h_j = sum_c xh[c] W[c][j]
-    for (int c = 0; c < d; ++c) a = fmaf(sx[c], sW[c * kPreK + lane], a);
+    float a4[4] = {0.f, 0.f, 0.f, 0.f};  // lane j: h_j = sum_c xh[c] W[c][j], 4 independent chains
+    for (int c = 0; c < d; c += 4) {
+      const float4 xv = *reinterpret_cast<const float4*>(sx + c);
+      a4[0] = fmaf(xv.x, sW[(c + 0) * kPreK + lane], a4[0]);
+      a4[1] = fmaf(xv.y, sW[(c + 1) * kPreK + lane], a4[1]);
+      a4[2] = fmaf(xv.z, sW[(c + 2) * kPreK + lane], a4[2]);
+      a4[3] = fmaf(xv.w, sW[(c + 3) * kPreK + lane], a4[3]);
+    }
+    const float a = (a4[0] + a4[1]) + (a4[2] + a4[3]);
     __syncwarp();
     const __nv_bfloat16 hb = __float2bfloat16_rn(a);
     hp[static_cast<size_t>(r) * kPreK + lane] = hb;
@@ -91,16 +99,23 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool pred
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(src), "r"(n) : "memory");
 }
 
-// lse[b, t] over the full vocabulary for the rows of 128-row block blockIdx.x.
-__global__ void __launch_bounds__(128) k_ce_tied(const __nv_bfloat16* __restrict__ hp, int T, int L,
-                                                 const __nv_bfloat16* __restrict__ items, int V,
-                                                 float* __restrict__ lse) {
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// lse[b, t] over the full vocabulary for the rows of 128-row block blockIdx.x. 4 warps x 32 rows
+// (two m16 tiles share every B fragment); B fragments by ldmatrix.x4 (one per 8-item n-tile
+// covering both k16 steps); per row slot an online (max, sum) in natural-log units.
+__global__ void __launch_bounds__(kCeThreads) k_ce_tied(const __nv_bfloat16* __restrict__ hp, int T, int L,
+                                                        const __nv_bfloat16* __restrict__ items, int V,
+                                                        float* __restrict__ lse) {
   __shared__ __align__(16) uint8_t sB[2][kCeItems * kCePitch];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, tq = lane & 3;
   const int row0 = blockIdx.x * kCeRows + warp * 32;
-  // A fragments: 2 m16 tiles x 2 k16 steps (K = 32)
-  uint32_t a[2][2][4];
+  uint32_t a[2][2][4];  // A fragments: 2 m16 tiles x 2 k16 steps (K = 32)
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -116,7 +131,7 @@ __global__ void __launch_bounds__(128) k_ce_tied(const __nv_bfloat16* __restrict
     // 64 items x 64 B = 256 16-byte chunks, 2 per thread
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
-      const int ch = threadIdx.x + i * 128;
+      const int ch = threadIdx.x + i * kCeThreads;
       const int it = ch >> 2, part = ch & 3;
       const int v = tile * kCeItems + it;
       cp_async16(sB[buf] + it * kCePitch + part * 16,
@@ -131,6 +146,8 @@ __global__ void __launch_bounds__(128) k_ce_tied(const __nv_bfloat16* __restrict
     m[i] = -INFINITY;
     s[i] = 0.f;
   }
+  // ldmatrix row address of this lane: matrix lane / 8 = k block, row lane % 8 = item
+  const uint32_t lm_off = static_cast<uint32_t>((lane & 7) * kCePitch + (lane >> 3) * 16);
   stage(0, 0);
   for (int tile = 0; tile < n_tiles; ++tile) {
     const int buf = tile & 1;
@@ -148,20 +165,19 @@ __global__ void __launch_bounds__(128) k_ce_tied(const __nv_bfloat16* __restrict
       for (int nt = 0; nt < 8; ++nt)
 #pragma unroll
         for (int q = 0; q < 4; ++q) c[mt][nt][q] = 0.f;
+    const uint32_t sb = smem_u32(sB[buf]) + lm_off;
 #pragma unroll
     for (int nt = 0; nt < 8; ++nt) {
-      const uint8_t* brow = sB[buf] + (nt * 8 + g) * kCePitch;
-#pragma unroll
-      for (int ks = 0; ks < 2; ++ks) {
-        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(brow + (ks * 16 + 2 * tq) * 2);
-        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(brow + (ks * 16 + 2 * tq + 8) * 2);
-        mma_bf16_16816(c[0][nt], a[0][ks], b0, b1);
-        mma_bf16_16816(c[1][nt], a[1][ks], b0, b1);
-      }
+      uint32_t b[4];
+      asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(b[0]), "=r"(b[1]), "=r"(b[2]), "=r"(b[3])
+                   : "r"(sb + nt * 8 * kCePitch));
+      mma_bf16_16816(c[0][nt], a[0][0], b[0], b[1]);
+      mma_bf16_16816(c[1][nt], a[1][0], b[0], b[1]);
+      mma_bf16_16816(c[0][nt], a[0][1], b[2], b[3]);
+      mma_bf16_16816(c[1][nt], a[1][1], b[2], b[3]);
     }
     __syncthreads();  // buffer `buf` is restaged two tiles later
-    // online log-sum-exp (exp2 domain): raw maxima, one FFMA per logit for the argument,
-    // 3 of every 8 column pairs through the FMA-pipe polynomial to offload the MUFU
     if (tile == n_tiles - 1) {  // vocabulary tail: columns >= V never count
       const int vbase = tile * kCeItems + 2 * tq;
 #pragma unroll
@@ -173,33 +189,40 @@ __global__ void __launch_bounds__(128) k_ce_tied(const __nv_bfloat16* __restrict
             if (vbase + nt * 8 + (q & 1) >= V) c[mt][nt][q] = -INFINITY;
     }
 #pragma unroll
-    for (int mt = 0; mt < 2; ++mt)
+    for (int slot = 0; slot < 4; ++slot) {
+      const int mt = slot >> 1, hf = slot & 1;
+      float z[16];
 #pragma unroll
-      for (int hf = 0; hf < 2; ++hf) {
-        const int slot = mt * 2 + hf;
-        float zmax = -INFINITY;
-#pragma unroll
-        for (int nt = 0; nt < 8; ++nt) zmax = fmaxf(zmax, fmaxf(c[mt][nt][hf * 2], c[mt][nt][hf * 2 + 1]));
-        const float mn = fmaxf(m[slot], zmax);
-        if (mn == -INFINITY) continue;  // no valid column seen yet (V < 64 tails)
-        const float ms = mn * kLog2e;
-        float2 acc = make_float2(m[slot] == -INFINITY ? 0.f : s[slot] * ex2_approx(fmaf(m[slot], kLog2e, -ms)), 0.f);
-#pragma unroll
-        for (int nt = 0; nt < 8; ++nt) {
-          const float2 arg = ffma2(make_float2(c[mt][nt][hf * 2], c[mt][nt][hf * 2 + 1]),
-                                   make_float2(kLog2e, kLog2e), make_float2(-ms, -ms));
-          float2 e;
-          if (nt % 3 == 1) {
-            e = ex2_poly2(arg);
-          } else {
-            e.x = ex2_approx(arg.x);
-            e.y = ex2_approx(arg.y);
-          }
-          acc = fadd2(acc, e);
-        }
-        m[slot] = mn;
-        s[slot] = acc.x + acc.y;
+      for (int nt = 0; nt < 8; ++nt) {
+        z[2 * nt] = c[mt][nt][hf * 2];
+        z[2 * nt + 1] = c[mt][nt][hf * 2 + 1];
       }
+      float mx[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) mx[i] = fmax3(z[4 * i], z[4 * i + 1], fmaxf(z[4 * i + 2], z[4 * i + 3]));
+      const float zmax = fmax3(mx[0], mx[1], fmaxf(mx[2], mx[3]));
+      const float mn = fmaxf(m[slot], zmax);
+      if (mn == -INFINITY) continue;  // no valid column seen yet (V < 64 tails)
+      const float ms = mn * kLog2e;
+      float2 acc0 = make_float2(m[slot] == -INFINITY ? 0.f : s[slot] * ex2_approx(fmaf(m[slot], kLog2e, -ms)), 0.f);
+      float2 acc1 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int nt = 0; nt < 8; ++nt) {
+        const float2 arg = ffma2(make_float2(z[2 * nt], z[2 * nt + 1]), make_float2(kLog2e, kLog2e),
+                                 make_float2(-ms, -ms));
+        float2 e;
+        if (nt == 7) {  // 1 of 8 pairs on the FMA pipe
+          e = ex2_poly2(arg);
+        } else {
+          e.x = ex2_approx(arg.x);
+          e.y = ex2_approx(arg.y);
+        }
+        if (nt & 1) acc1 = fadd2(acc1, e);
+        else acc0 = fadd2(acc0, e);
+      }
+      m[slot] = mn;
+      s[slot] = (acc0.x + acc1.x) + (acc0.y + acc1.y);
+    }
   }
   // combine the 4 threads of a quad (same rows, different columns)
 #pragma unroll

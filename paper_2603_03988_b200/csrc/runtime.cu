@@ -1677,7 +1677,7 @@ static void forward_device(Handle& h, int B) {
     const int V = h.item_ext ? static_cast<int>(h.item_ext_rows) : h.cfg.n_items;
     k_pretrain_proj<<<std::max(1, std::min((T + 7) / 8, 8 * h.num_sms)), 256, psmem, h.stream>>>(
         h.X[last.q_buf], T, h.L0, h.d, h.head_gain, h.pre_proj, items, h.in_item, h.pre_hp, h.pre_tgt);
-    k_ce_tied<<<(T + kCeRows - 1) / kCeRows, 128, 0, h.stream>>>(h.pre_hp, T, h.L0, items, V, h.pre_lse);
+    k_ce_tied<<<(T + kCeRows - 1) / kCeRows, kCeThreads, 0, h.stream>>>(h.pre_hp, T, h.L0, items, V, h.pre_lse);
     check_launch("pretrain head");
     h.launches += 2;
     stage_mark(h, "head");
