@@ -578,6 +578,22 @@ def main():
         "algorithmic_flops_per_step": per_group_flops.get(dom),
         "stage_ms": {k: round(v, 4) for k, v in groups.items()},
     }
+    if dom == "attention" and dom_ms:
+        # the attention core's binding unit is the exp (MUFU), one per visible logit: report
+        # that roofline next to the tensor one (peak: tools/micro/mufu_peak.cu on a B200)
+        mufu = os.path.join(ROOT, "profiles", "mufu_peak.json")
+        mufu_peak = 4.61e12
+        if os.path.exists(mufu):
+            try:
+                mufu_peak = json.loads(open(mufu).readline())["ex2_per_s"]
+            except Exception:
+                pass
+        exps = sum(L["visible_per_head"] for L in fl["layers"]) * cfg.heads * B
+        roofline["exp_roofline"] = {
+            "bound": "mufu", "achieved": exps / (dom_ms / 1e3) / 1e12, "peak": mufu_peak / 1e12,
+            "unit": "Texp/s", "frac": exps / (dom_ms / 1e3) / mufu_peak,
+            "algorithmic_exps_per_step": exps,
+            "peak_kind": "measured (profiles/mufu_peak.json: ex2.approx throughput, 16/clk/SM)"}
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
