@@ -508,14 +508,33 @@ def main():
         R._check(R.lib().sort_forward(model.h, ctypes.byref(pb.c), 0,
                                       ctypes.c_void_p(host_scores.data_ptr()), 0))
     barrier()
-    e2e_ms = 0.0
+    # (a) one synchronous call per step (copy in, forward, copy out, sync), L2 flushed
+    #     outside the timed region
+    e2e_sync_ms = 0.0
     for i in range(args.steps):
         flush.fill_(float(i))
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
         R._check(R.lib().sort_forward(model.h, ctypes.byref(pb.c), 0,
                                       ctypes.c_void_p(host_scores.data_ptr()), 0))
-        e2e_ms += (time.perf_counter() - t0) * 1e3
+        e2e_sync_ms += (time.perf_counter() - t0) * 1e3
+    barrier()
+    # (b) the serving loop: sort_forward_async per step (each step's host->device copy rides
+    #     the copy stream and overlaps the previous step's kernels; scores copied back every
+    #     step), the L2 flush enqueued before every step INSIDE the timed region, one sync at
+    #     the end. This is the e2e value.
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            R._check(R.lib().sort_forward_async(model.h, ctypes.byref(pb.c), host_scores.data_ptr()))
+        model.sync()
+        barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            flush.fill_(float(i))
+            R._check(R.lib().sort_forward_async(model.h, ctypes.byref(pb.c), host_scores.data_ptr()))
+        model.sync()
+        e2e_ms = (time.perf_counter() - t0) * 1e3
     barrier()
 
     # ---------------------------------------------------------------- per-stage breakdown
@@ -530,10 +549,10 @@ def main():
                 stage_acc[k] = stage_acc.get(k, 0.0) + v / 3
     model.enable_stage_timing(False)
 
-    t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([dev_ms, e2e_ms, e2e_sync_ms], dtype=torch.float64, device=dev)
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    dev_ms, e2e_ms = float(t[0]), float(t[1])
+    dev_ms, e2e_ms, e2e_sync_ms = float(t[0]), float(t[1]), float(t[2])
     if rank != 0:
         dist.destroy_process_group() if dist else None
         return
@@ -616,7 +635,9 @@ def main():
         "mfu": mfu, "mfu_peak": f"{peaks['bf16_tflops']} TFLOP/s bf16 ({peak_kind})",
         "algorithmic_tflop_per_step": step_flops * world / 1e12,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps},
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps,
+                "form": "pipelined sort_forward_async loop, L2 flush inside the timed region",
+                "sync_call_ms_per_step": e2e_sync_ms / args.steps},
         "gpu_launches": launches_per_step * args.steps,
         "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
     }

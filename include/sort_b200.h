@@ -121,6 +121,12 @@ int sort_finalize_params(SortHandle h);
  * call sort_sync to collect the status of device-side checks). */
 int sort_forward(SortHandle h, const SortBatch* batch, int inputs_on_device, float* scores,
                  int scores_on_device);
+/* Pipelined serving form of sort_forward with HOST inputs and outputs: enqueue only. The
+ * batch's arrays are copied on the handle's copy stream into one of two device staging slots
+ * (alternating per call), so the next call's host->device copy overlaps this call's kernels;
+ * scores [batch, n_cand, 3] are written back asynchronously. Host buffers should be pinned
+ * and must stay untouched until sort_sync; device-side errors (OOV ids) surface at sort_sync. */
+int sort_forward_async(SortHandle h, const SortBatch* batch, float* scores);
 int sort_sync(SortHandle h);
 
 /* Same as sort_forward but also returns the pre-sigmoid logits [batch, n_cand, 3]. */
@@ -242,7 +248,9 @@ int sort_dataset_batch(SortDataset d, int64_t first, int32_t count, int32_t n_hi
  * that kernel as CTA pairs with cta_group::2 MMAs, M = 256 per pair and the weights split by
  * N; 0 = single CTA, the default: measured faster on B200); "qkvg_pair" (the QKVG projection
  * GEMM as CTA pairs, default 0 for the same reason); "attn_bwd_mma" (1 = tensor-core
- * attention backward, the default; 0 = the fp32 SIMT kernels). Status 1 on an unknown name. */
+ * attention backward, the default; 0 = the fp32 SIMT kernels); "graphs" (1 = replay the
+ * inference forward from a CUDA graph per (batch size, input slot, item table), the default;
+ * 0 = eager launches). Status 1 on an unknown name. */
 int sort_set_option(SortHandle h, const char* name, int32_t value);
 
 /* ---- pre-training (config field pretrain = 1) ---------------------------------------------

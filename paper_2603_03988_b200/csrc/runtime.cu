@@ -9,6 +9,7 @@
 #include <map>
 #include <memory>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/sort_b200.h"
@@ -159,6 +160,29 @@ struct Handle {
   int32_t *in_item = nullptr, *in_action = nullptr, *in_scene = nullptr, *in_prof = nullptr,
           *in_cand = nullptr;
   int64_t *in_ts = nullptr, *in_req = nullptr;
+  // sort_forward_async: two input staging slots filled on a copy stream, so step i+1's
+  // host->device copy overlaps step i's kernels
+  struct InSlot {
+    int32_t *item = nullptr, *action = nullptr, *scene = nullptr, *prof = nullptr, *cand = nullptr;
+    int64_t *ts = nullptr, *req = nullptr;
+  } in_slot[2];
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t slot_copied[2] = {nullptr, nullptr}, slot_free[2] = {nullptr, nullptr};
+  int64_t async_steps = 0;
+  // CUDA graphs of the inference forward, one per (batch, input slot, item table): a replay
+  // is one launch instead of ~160 (sort_set_option("graphs")); dropped whenever weights,
+  // options or logit bounds change
+  bool use_graphs = true;
+  struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    int launches = 0;
+  };
+  std::map<std::tuple<int, const void*, const void*, int64_t>, GraphEntry> graphs;
+  void drop_graphs() {
+    for (auto& kv : graphs)
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    graphs.clear();
+  }
   std::vector<void*> allocs;
   // instrumentation
   bool timing = false;
@@ -183,8 +207,14 @@ struct Handle {
   }
   ~Handle() {
     if (device >= 0) cudaSetDevice(device);
+    drop_graphs();
     for (void* p : allocs) cudaFree(p);
     for (auto e : events) cudaEventDestroy(e);
+    for (int i = 0; i < 2; ++i) {
+      if (slot_copied[i]) cudaEventDestroy(slot_copied[i]);
+      if (slot_free[i]) cudaEventDestroy(slot_free[i]);
+    }
+    if (copy_stream) cudaStreamDestroy(copy_stream);
     if (cublas) cublasDestroy(cublas);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
@@ -384,6 +414,7 @@ static void finalize(Handle& h) {
   h.in_req = h.dalloc<int64_t>(h.Bmax);
   h.in_prof = h.dalloc<int32_t>(static_cast<size_t>(h.Bmax) * std::max(c.n_profile_fields, 1));
   h.in_cand = h.dalloc<int32_t>(static_cast<size_t>(h.Bmax) * c.n_cand);
+  h.in_slot[0] = {h.in_item, h.in_action, h.in_scene, h.in_prof, h.in_cand, h.in_ts, h.in_req};
 
   // ---- per-layer weights, plan arrays and TMA descriptors
   int cur = 0;
@@ -1712,6 +1743,42 @@ static void forward_device(Handle& h, int B) {
   stage_mark(h, "head");
 }
 
+// The inference forward, replayed from a CUDA graph when possible. The first call for a key
+// runs eagerly (kernel attributes, plan checks) and then captures the same enqueue sequence.
+static void forward_run(Handle& h, int B) {
+  if (!h.use_graphs || h.timing || h.training || h.generic || h.stream == nullptr) {
+    forward_device(h, B);
+    return;
+  }
+  const auto key = std::make_tuple(B, static_cast<const void*>(h.in_item), static_cast<const void*>(h.item_ext),
+                                   h.item_ext_rows);
+  auto it = h.graphs.find(key);
+  if (it != h.graphs.end()) {
+    CK(cudaGraphLaunch(it->second.exec, h.stream));
+    h.launches = it->second.launches;
+    return;
+  }
+  forward_device(h, B);
+  const int launches = h.launches;
+  cudaGraph_t g = nullptr;
+  CK(cudaStreamBeginCapture(h.stream, cudaStreamCaptureModeRelaxed));
+  try {
+    forward_device(h, B);
+  } catch (...) {
+    cudaStreamEndCapture(h.stream, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  CK(cudaStreamEndCapture(h.stream, &g));
+  Handle::GraphEntry e;
+  const cudaError_t ie = cudaGraphInstantiate(&e.exec, g, 0);
+  cudaGraphDestroy(g);
+  if (ie != cudaSuccess) throw RuntimeFailure(std::string("cudaGraphInstantiate failed: ") + cudaGetErrorString(ie));
+  e.launches = launches;
+  h.launches = launches;
+  h.graphs[key] = e;
+}
+
 static void collect_status(Handle& h) {
   int32_t err[4];
   CK(cudaMemcpyAsync(err, h.err, sizeof(err), cudaMemcpyDeviceToHost, h.stream));
@@ -1854,11 +1921,70 @@ int sort_forward(SortHandle p, const SortBatch* batch, int inputs_on_device, flo
     if (h->cfg.pretrain) throw ConfigError("pre-training model: use sort_pretrain_forward");
     begin_timing(*h);
     upload_batch(*h, batch, inputs_on_device != 0);
-    forward_device(*h, batch->batch);
+    forward_run(*h, batch->batch);
     const size_t bytes = static_cast<size_t>(batch->batch) * h->cfg.n_cand * 3 * sizeof(float);
     CK(cudaMemcpyAsync(scores, h->probs, bytes,
                        scores_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->stream));
     if (!(inputs_on_device && scores_on_device)) collect_status(*h);
+  });
+}
+
+int sort_forward_async(SortHandle p, const SortBatch* batch, float* scores) {
+  return api([&] {
+    Handle* h = ready(p);
+    if (!batch || !scores) throw ConfigError("null argument");
+    if (h->cfg.pretrain) throw ConfigError("pre-training model: use sort_pretrain_forward");
+    const SortConfig& c = h->cfg;
+    const int B = batch->batch;
+    if (B < 1 || B > h->Bmax) throw ConfigError("batch size must be in [1, max_batch]");
+    if (!h->copy_stream) {
+      CK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+      for (int i = 0; i < 2; ++i) {
+        CK(cudaEventCreateWithFlags(&h->slot_copied[i], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&h->slot_free[i], cudaEventDisableTiming));
+      }
+      const size_t BH_ = static_cast<size_t>(h->Bmax) * std::max(c.n_hist, 1);
+      Handle::InSlot& s1 = h->in_slot[1];
+      s1.item = h->dalloc<int32_t>(BH_);
+      s1.action = h->dalloc<int32_t>(BH_);
+      s1.scene = h->dalloc<int32_t>(BH_);
+      s1.ts = h->dalloc<int64_t>(BH_);
+      s1.req = h->dalloc<int64_t>(h->Bmax);
+      s1.prof = h->dalloc<int32_t>(static_cast<size_t>(h->Bmax) * std::max(c.n_profile_fields, 1));
+      s1.cand = h->dalloc<int32_t>(static_cast<size_t>(h->Bmax) * c.n_cand);
+    }
+    const int k = static_cast<int>(h->async_steps & 1);
+    Handle::InSlot& sl = h->in_slot[k];
+    // the slot's previous reader (the forward two steps back) must be done before overwriting
+    if (h->async_steps >= 2) CK(cudaStreamWaitEvent(h->copy_stream, h->slot_free[k], 0));
+    const size_t nh = static_cast<size_t>(B) * c.n_hist;
+    auto cp = [&](void* dst, const void* src, size_t bytes) {
+      if (bytes == 0) return;
+      if (!src) throw ConfigError("batch array is null");
+      CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, h->copy_stream));
+    };
+    cp(sl.item, batch->hist_item, nh * 4);
+    cp(sl.action, batch->hist_action, nh * 4);
+    cp(sl.scene, batch->hist_scene, nh * 4);
+    cp(sl.ts, batch->hist_ts, nh * 8);
+    cp(sl.req, batch->req_ts, static_cast<size_t>(B) * 8);
+    cp(sl.prof, batch->profile, static_cast<size_t>(B) * c.n_profile_fields * 4);
+    cp(sl.cand, batch->cand_item, static_cast<size_t>(B) * c.n_cand * 4);
+    CK(cudaEventRecord(h->slot_copied[k], h->copy_stream));
+    CK(cudaStreamWaitEvent(h->stream, h->slot_copied[k], 0));
+    h->in_item = sl.item;
+    h->in_action = sl.action;
+    h->in_scene = sl.scene;
+    h->in_ts = sl.ts;
+    h->in_req = sl.req;
+    h->in_prof = sl.prof;
+    h->in_cand = sl.cand;
+    begin_timing(*h);
+    forward_run(*h, B);
+    CK(cudaEventRecord(h->slot_free[k], h->stream));
+    CK(cudaMemcpyAsync(scores, h->probs, static_cast<size_t>(B) * c.n_cand * 3 * sizeof(float),
+                       cudaMemcpyDeviceToHost, h->stream));
+    ++h->async_steps;
   });
 }
 
@@ -2133,6 +2259,7 @@ int sort_adamw_step(SortHandle p, float lr, float beta1, float beta2, float eps,
     Handle* h = ready(p);
     if (!h->grads) throw ConfigError("no gradients yet (call sort_train_step)");
     if (h->generic) throw ConfigError("training step: model_dim > 256 is not supported in this build");
+    h->drop_graphs();  // weights and QKNorm logit bounds (kernel arguments) change
     if (!h->adam_m) {
       h->adam_m = h->dalloc<float>(h->grad_count);
       h->adam_v = h->dalloc<float>(h->grad_count);
@@ -2222,6 +2349,7 @@ int sort_set_item_table(SortHandle p, const void* rows, int64_t n_rows) {
     Handle* h = reinterpret_cast<Handle*>(p);
     if (!h) throw ConfigError("null handle");
     if (rows && (n_rows < 1 || n_rows > INT32_MAX)) throw ConfigError("item table rows out of range");
+    h->drop_graphs();
     h->item_ext = static_cast<const __nv_bfloat16*>(rows);
     h->item_ext_rows = rows ? n_rows : 0;
   });
@@ -2329,7 +2457,10 @@ int sort_set_option(SortHandle p, const char* name, int32_t value) {
   return api([&] {
     Handle* h = reinterpret_cast<Handle*>(p);
     if (!h || !name) throw ConfigError("null argument");
-    if (std::strcmp(name, "fused_tail") == 0) {
+    h->drop_graphs();
+    if (std::strcmp(name, "graphs") == 0) {
+      h->use_graphs = value != 0;
+    } else if (std::strcmp(name, "fused_tail") == 0) {
       h->fused_tail = value != 0;
     } else if (std::strcmp(name, "tail_pair") == 0) {
       h->tail_pair = value != 0;

@@ -61,7 +61,7 @@ EXPORTS = [
     "sort_set_item_table", "sort_gather_rows", "sort_train_step_bce", "sort_adamw_step",
     "sort_get_param", "sort_dataset_open", "sort_dataset_close", "sort_dataset_size",
     "sort_dataset_batch", "sort_moe_routing", "sort_moe_load", "sort_moe_update_bias",
-    "sort_moe_forward", "sort_pretrain_forward",
+    "sort_moe_forward", "sort_pretrain_forward", "sort_forward_async",
 ]
 
 _lib = None
@@ -109,6 +109,7 @@ def lib():
         L.sort_moe_load.argtypes = [C.c_void_p, C.c_int, i64p]
         L.sort_moe_update_bias.argtypes = [C.c_void_p, C.c_double]
         L.sort_moe_forward.argtypes = [C.c_void_p, C.c_int, f32p, C.c_int, f32p]
+        L.sort_forward_async.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.sort_pretrain_forward.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int]
         L.sort_dataset_open.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
         L.sort_dataset_close.argtypes = [C.c_void_p]

@@ -392,3 +392,19 @@ def test_jsonl_ingest_forward_bit_identical(tiny, tmp_path):
     out = np.zeros((3, cfg.n_cand, 3), np.float32)
     R._check(R.lib().sort_forward(gm.h, ctypes.byref(cb), 0, out.ctypes.data, 0))
     assert np.array_equal(out, gm.forward(b))
+
+
+def test_forward_async_pipeline_matches_sync(tiny):
+    """sort_forward_async alternates two input staging slots on a copy stream; a run of
+    different batches enqueued back to back must give exactly the synchronous scores."""
+    import ctypes
+    cfg, P, gm, _ = tiny
+    batches = [synth.make_batch(cfg, 4, seed=300 + i) for i in range(5)]
+    ref = [gm.forward(b) for b in batches]
+    holds = [R._BatchHold(b) for b in batches]
+    outs = [np.zeros((4, cfg.n_cand, 3), np.float32) for _ in batches]
+    for hd, o in zip(holds, outs):
+        R._check(R.lib().sort_forward_async(gm.h, ctypes.byref(hd.c), o.ctypes.data))
+    gm.sync()
+    for o, r in zip(outs, ref):
+        np.testing.assert_array_equal(o, r)
