@@ -14,6 +14,7 @@
 
 #include "../../include/sort_b200.h"
 #include "attention.cuh"
+#include "attention_fixed.cuh"
 #include "block_tail.cuh"
 #include "epilogues.cuh"
 #include "gemm.cuh"
@@ -57,6 +58,7 @@ struct LayerDev {
   float logit_bound = 0.f;  // QKNorm logit bound (0 = unknown -> online-max softmax)
   CUtensorMap tmA_in, tmA_q, tmB_all, tmB_qg, tmB_kv, tmA_hg, tmB_o, tmB_up, tmA_hid, tmB_down;
   CUtensorMap tmQ, tmK, tmV;
+  CUtensorMap tmK64, tmV64;  // 64-row K/V boxes (k_attention_f subtiles)
   CUtensorMap tmRopeKV, tmRopeQ;  // per-row RoPE side tables for the K/V rows and the Q rows
   CUtensorMap tmWo_t, tmWup_t, tmWdown_t;  // k_block_tail weight stages
   CUtensorMap tmWo_p, tmWup_p, tmWdown_p;  // ... as a CTA pair (each CTA loads half the rows)
@@ -85,6 +87,7 @@ struct Handle {
   bool tail_pair = false;  // sort_set_option("tail_pair"): block tail as CTA pairs (cta_group::2)
   bool attn_bwd_mma = true; // sort_set_option("attn_bwd_mma"): tensor-core attention backward
   bool qkvg_pair = false;   // sort_set_option("qkvg_pair"): QKVG projection as CTA pairs
+  bool attn_sub = false;    // sort_set_option("attn_subtiles"): k_attention_f in fixed-reference mode
   bool generic = false;    // d > 256 (SORT-large): projections through the generic path
   // ---- MoE FFN: routed + shared experts as grouped tcgen05 GEMMs
   bool moe = false;
@@ -539,6 +542,9 @@ static void finalize(Handle& h) {
       uint64_t skd[2] = {static_cast<uint64_t>(dk) * 2, static_cast<uint64_t>(L.Rkv) * dk * 2};
       L.tmK = make_tmap_bf16(h.Kb, 3, dkd, skd, bq, dk * 2);
       L.tmV = make_tmap_bf16(h.Vb, 3, dkd, skd, bq, dk * 2);
+      uint32_t b64[3] = {static_cast<uint32_t>(dk), 64, 1};
+      L.tmK64 = make_tmap_bf16(h.Kb, 3, dkd, skd, b64, dk * 2);
+      L.tmV64 = make_tmap_bf16(h.Vb, 3, dkd, skd, b64, dk * 2);
     }
   }
   // ---- head (fp32)
@@ -719,6 +725,22 @@ static void launch_attention_dk(Handle& h, const LayerDev& L, const LayerPlan& l
   a.ref_log2 = L.logit_bound * a.scale_log2;
   const int n_items = lp.n_qtiles * B * h.H;
   const int tile_ints = 2 * lp.n_qtiles + 2 + 2 * n_codes;
+  if constexpr (kFixed) {
+    if (h.attn_sub) {  // fixed reference: 64-column subtiles, O accumulated in TMEM
+      static size_t attr_f = 0;
+      const size_t smem_f = AttnFLayout<DK>::bytes(tile_ints);
+      if (smem_f > attr_f) {
+        CK(cudaFuncSetAttribute(k_attention_f<DK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem_f)));
+        attr_f = smem_f;
+      }
+      const int grid_f = std::min(n_items, 2 * h.num_sms);
+      k_attention_f<DK><<<grid_f, kAttnThreads, smem_f, h.stream>>>(L.tmQ, L.tmK64, L.tmV64, a);
+      check_launch("attention (subtiles)");
+      ++h.launches;
+      return;
+    }
+  }
   static size_t attr_bytes = 0;
   const size_t smem = AttnSmem<DK>::bytes(tile_ints);
   if (smem > attr_bytes) {
@@ -2135,6 +2157,9 @@ int sort_block_attention(int32_t nh, int32_t l_q, int32_t l_kv, int32_t dk, cons
     uint64_t skd[2] = {static_cast<uint64_t>(dk) * 2, static_cast<uint64_t>(l_kv) * dk * 2};
     L.tmK = make_tmap_bf16(h.Kb, 3, dkd, skd, bq, dk * 2);
     L.tmV = make_tmap_bf16(h.Vb, 3, dkd, skd, bq, dk * 2);
+    uint32_t b64[3] = {static_cast<uint32_t>(dk), 64, 1};
+    L.tmK64 = make_tmap_bf16(h.Kb, 3, dkd, skd, b64, dk * 2);
+    L.tmV64 = make_tmap_bf16(h.Vb, 3, dkd, skd, b64, dk * 2);
     launch_attention(h, L, lp, nh);
     std::vector<__nv_bfloat16> ob(static_cast<size_t>(nh) * l_q * dk);
     CK(cudaMemcpyAsync(ob.data(), h.Hg, ob.size() * 2, cudaMemcpyDeviceToHost, h.stream));
@@ -2468,6 +2493,8 @@ int sort_set_option(SortHandle p, const char* name, int32_t value) {
       h->attn_bwd_mma = value != 0;
     } else if (std::strcmp(name, "qkvg_pair") == 0) {
       h->qkvg_pair = value != 0;
+    } else if (std::strcmp(name, "attn_subtiles") == 0) {
+      h->attn_sub = value != 0;
     } else {
       throw ConfigError(std::string("unknown option ") + name);
     }

@@ -408,3 +408,20 @@ def test_forward_async_pipeline_matches_sync(tiny):
     gm.sync()
     for o, r in zip(outs, ref):
         np.testing.assert_array_equal(o, r)
+
+
+@pytest.mark.parametrize("which", ["tiny", "base"])
+def test_subtile_attention_option_matches_default(which, tiny, base):
+    """k_attention_f (64-column subtiles, O accumulated in TMEM; sort_set_option
+    "attn_subtiles") computes the same P = exp2(s - B) in bf16 as k_attention and only sums
+    the P V products in another order: logits agree to fp32 summation noise."""
+    cfg, P, gm, _ = tiny if which == "tiny" else base
+    b = synth.make_batch(cfg, 2, seed=77)
+    _, z0 = gm.forward_logits(b)
+    gm.set_option("attn_subtiles", 1)
+    try:
+        _, z1 = gm.forward_logits(b)
+    finally:
+        gm.set_option("attn_subtiles", 0)
+    assert np.max(np.abs(z1 - z0)) < 2e-2
+    assert rel_l2(z1, z0) < 2e-3
