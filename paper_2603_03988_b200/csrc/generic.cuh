@@ -109,18 +109,18 @@ __global__ void k_tok_specials(const float* __restrict__ special, int B, int L, 
 
 // Per row and head: Q/K -> per-head RMSNorm with gain (attention.cpp:111-114) -> interleaved
 // RoPE at the row's position (rope.hpp:27-38) -> bf16 head-major [B*H, R, dk]; V -> bf16
-// head-major; G -> sigmoid -> bf16 [rows, d]. Input: the bf16 projection [rows, d]. One warp per
+// head-major; G -> sigmoid -> bf16 [rows, d]. Input: the bf16 projection (row stride ld). One warp per
 // row; each lane owns 8 contiguous elements (16-byte loads/stores) of chunk c = lane + 32 i, so a
 // head spans dk / 8 aligned lanes and its sum of squares is a 1-3 step shuffle reduction.
 template <int kV>
-__global__ void k_qkv_prep(const __nv_bfloat16* __restrict__ raw, int rows, int R, int H, int dk, int kind,
+__global__ void k_qkv_prep(const __nv_bfloat16* __restrict__ raw, int ld, int rows, int R, int H, int dk, int kind,
                            const int32_t* __restrict__ pos, const float2* __restrict__ rope_tab,
                            const float* __restrict__ gain, __nv_bfloat16* __restrict__ out) {
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (row >= rows) return;
   const int d = H * dk, d8 = d >> 3, b = row / R, r = row - b * R;
   const int e = (lane * 8) & (dk - 1);  // offset inside the head (same for every chunk: 256 % dk == 0)
-  const int4* src = reinterpret_cast<const int4*>(raw + static_cast<size_t>(row) * d);
+  const int4* src = reinterpret_cast<const int4*>(raw + static_cast<size_t>(row) * ld);
   int4 v[kV];
 #pragma unroll
   for (int i = 0; i < kV; ++i) {

@@ -1100,18 +1100,18 @@ static void resid_rmsnorm(Handle& h, const float* x, const int32_t* map, int R, 
 }
 
 // generic-path per-head Q/K/V/G preparation, see k_qkv_prep (d = H dk <= 2048)
-static void qkv_prep(Handle& h, const __nv_bfloat16* raw, int rows, int R, int H, int dk, int kind,
+static void qkv_prep(Handle& h, const __nv_bfloat16* raw, int ld, int rows, int R, int H, int dk, int kind,
                      const int32_t* pos, const float* gain, __nv_bfloat16* out) {
   const int g = warp_rows_grid(rows), d = H * dk;
   const float2* rope = h.rope;
   if (d <= 256)
-    k_qkv_prep<1><<<g, 256, 0, h.stream>>>(raw, rows, R, H, dk, kind, pos, rope, gain, out);
+    k_qkv_prep<1><<<g, 256, 0, h.stream>>>(raw, ld, rows, R, H, dk, kind, pos, rope, gain, out);
   else if (d <= 512)
-    k_qkv_prep<2><<<g, 256, 0, h.stream>>>(raw, rows, R, H, dk, kind, pos, rope, gain, out);
+    k_qkv_prep<2><<<g, 256, 0, h.stream>>>(raw, ld, rows, R, H, dk, kind, pos, rope, gain, out);
   else if (d <= 1024)
-    k_qkv_prep<4><<<g, 256, 0, h.stream>>>(raw, rows, R, H, dk, kind, pos, rope, gain, out);
+    k_qkv_prep<4><<<g, 256, 0, h.stream>>>(raw, ld, rows, R, H, dk, kind, pos, rope, gain, out);
   else
-    k_qkv_prep<8><<<g, 256, 0, h.stream>>>(raw, rows, R, H, dk, kind, pos, rope, gain, out);
+    k_qkv_prep<8><<<g, 256, 0, h.stream>>>(raw, ld, rows, R, H, dk, kind, pos, rope, gain, out);
 }
 
 static float* grad_ptr(Handle& h, const std::string& name) {
@@ -1528,6 +1528,22 @@ static const __nv_bfloat16* w16(Handle& h, const std::string& name) {
   return h.w16[name] = dst;
 }
 
+// bf16 [K, n * N] row-major weight whose column blocks are the named [K, N] parameters
+// (built once per handle; the generic path's concatenated projections).
+static const __nv_bfloat16* w16_cat(Handle& h, const std::string& key, const std::vector<std::string>& parts) {
+  auto it = h.w16.find(key);
+  if (it != h.w16.end()) return it->second;
+  const auto& gi = h.grad_index.at(parts[0]);
+  const int64_t K = gi.second.first, N = gi.second.second, n = static_cast<int64_t>(parts.size());
+  __nv_bfloat16* dst = h.dalloc<__nv_bfloat16>(static_cast<size_t>(K * N * n));
+  for (int64_t i = 0; i < n; ++i) {
+    const __nv_bfloat16* src = w16(h, parts[i]);
+    CK(cudaMemcpy2DAsync(dst + i * N, static_cast<size_t>(n * N) * 2, src, static_cast<size_t>(N) * 2,
+                         static_cast<size_t>(N) * 2, static_cast<size_t>(K), cudaMemcpyDeviceToDevice, h.stream));
+  }
+  return h.w16[key] = dst;
+}
+
 static void forward_generic(Handle& h, int B) {
   ensure_generic_buffers(h);
   CK(cublasSetStream(h.cublas, h.stream) == CUBLAS_STATUS_SUCCESS ? cudaSuccess : cudaErrorUnknown);
@@ -1573,19 +1589,16 @@ static void forward_generic(Handle& h, int B) {
                                                                                           L.Rkv, M, d, xq);
       xqp = xq;
     }
-    // bf16 projection outputs (fp32 accumulation), consumed by the per-head prep
-    __nv_bfloat16* pq = reinterpret_cast<__nv_bfloat16*>(h.gw[2]);
-    __nv_bfloat16* pk = reinterpret_cast<__nv_bfloat16*>(h.gw[3]);
-    __nv_bfloat16* pv = reinterpret_cast<__nv_bfloat16*>(h.gw[4]);
-    __nv_bfloat16* pg = reinterpret_cast<__nv_bfloat16*>(h.gw[5]);
-    gemm_rm_bf16(h, M, d, d, xqp, d, w16(h, A + "wq"), d, pq, d, 0.f, true);
-    gemm_rm_bf16(h, M, d, d, xqp, d, w16(h, A + "wg"), d, pg, d, 0.f, true);
-    gemm_rm_bf16(h, Mkv, d, d, xn, d, w16(h, A + "wk"), d, pk, d, 0.f, true);
-    gemm_rm_bf16(h, Mkv, d, d, xn, d, w16(h, A + "wv"), d, pv, d, 0.f, true);
-    qkv_prep(h, pq, M, L.Rq, H, dk, 0, L.pos_q, L.gain_q, h.Qb);
-    qkv_prep(h, pk, Mkv, L.Rkv, H, dk, 1, L.pos_kv, L.gain_k, h.Kb);
-    qkv_prep(h, pv, Mkv, L.Rkv, H, dk, 2, nullptr, nullptr, h.Vb);
-    qkv_prep(h, pg, M, L.Rq, H, dk, 3, nullptr, nullptr, h.Gb);
+    // bf16 projection outputs (fp32 accumulation), consumed by the per-head prep: two GEMMs
+    // with column-concatenated weights, [Wq | Wg] on the query rows and [Wk | Wv] on all rows
+    __nv_bfloat16* pqg = reinterpret_cast<__nv_bfloat16*>(h.gw[2]);  // [M, 2d]
+    __nv_bfloat16* pkv = reinterpret_cast<__nv_bfloat16*>(h.gw[3]);  // [Mkv, 2d]
+    gemm_rm_bf16(h, M, 2 * d, d, xqp, d, w16_cat(h, A + "wq|wg", {A + "wq", A + "wg"}), 2 * d, pqg, 2 * d, 0.f, true);
+    gemm_rm_bf16(h, Mkv, 2 * d, d, xn, d, w16_cat(h, A + "wk|wv", {A + "wk", A + "wv"}), 2 * d, pkv, 2 * d, 0.f, true);
+    qkv_prep(h, pqg, 2 * d, M, L.Rq, H, dk, 0, L.pos_q, L.gain_q, h.Qb);
+    qkv_prep(h, pkv, 2 * d, Mkv, L.Rkv, H, dk, 1, L.pos_kv, L.gain_k, h.Kb);
+    qkv_prep(h, pkv + d, 2 * d, Mkv, L.Rkv, H, dk, 2, nullptr, nullptr, h.Vb);
+    qkv_prep(h, pqg + d, 2 * d, M, L.Rq, H, dk, 3, nullptr, nullptr, h.Gb);
     check_launch("generic projections");
     stage_mark(h, "L" + sl + ".qkvg");
     launch_attention(h, L, lp, B);  // tcgen05 core; writes the gated output to h.Hg
