@@ -286,11 +286,21 @@ __global__ void __launch_bounds__(kTailThreads, 1)
         commit(wo_full);
         // up(0) overwrites the Wo accumulator columns of K-blocks 0 and 1 (U0): both must have
         // been read; later K-blocks of x1 are waited for one by one (E1 runs a K-block ahead)
+        // U buffer of hidden chunk j = the global chunk counter's parity (what E2 waits on), so
+        // tiles with an odd chunk count keep the MMA issuer and E2 in step; when up(0) lands in
+        // U1 (odd counter, D = 256) the Wo accumulator columns of K-blocks 2 and 3 must be read too
+        const int cbase = c;
         mbar_wait(&x1_kb[0], t & 1);
         mbar_wait(&x1_kb[1], t & 1);
+        if constexpr (kKB == 4) {
+          if (cbase & 1) {
+            mbar_wait(&x1_kb[2], t & 1);
+            mbar_wait(&x1_kb[3], t & 1);
+          }
+        }
         tc_fence_after();
         auto up = [&](int j) {
-          const uint32_t u = tmem + 256 + (j & 1) * 128;
+          const uint32_t u = tmem + 256 + ((cbase + j) & 1) * 128;
           for (uint32_t p = 0; p < kKB / 2; ++p) {
             const uint32_t b = wait_stage();
 #pragma unroll
@@ -307,7 +317,7 @@ __global__ void __launch_bounds__(kTailThreads, 1)
             }
             release_stage();
           }
-          commit(&u_full[j & 1]);
+          commit(&u_full[(cbase + j) & 1]);
         };
         up(0);
         if (n_chunks > 1) up(1);

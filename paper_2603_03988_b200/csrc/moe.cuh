@@ -14,6 +14,7 @@
 // deterministic even though segment order within an expert follows atomic arrival.
 #pragma once
 
+#include "block_tail.cuh"
 #include "epilogues.cuh"
 #include "gemm.cuh"
 #include "train.cuh"
@@ -480,5 +481,268 @@ struct EpiMoeDown {
     }
   }
 };
+
+
+// ------------------------------------------------------------------ fused expert kernel
+// One persistent kernel per MoE layer for all experts (routed and shared) on the 128-row tiles
+// of the expert-sorted rows, the block-tail structure without Wo (csrc/block_tail.cuh):
+//   x tile (bf16 normalised rows, TMA) -> for hidden chunk j of the tile's expert:
+//     up   U[j&1] = x . [gate_j | up_j]^T   (N = 128: 64 hidden units)
+//     E2   h = swish(g) * u -> bf16 pairs in place in TMEM
+//     down D += h . Wdown_j^T               (A from TMEM)
+//   E3  y = bf16(w_row * D) in place over the x tile -> TMA store
+// so the expert hidden activation never leaves the SM (the grouped-GEMM pair writes and
+// re-reads it: 2 * m_e bytes per routed row). Weights stream through the 3-stage ring from
+// L2 with the tile's expert offset (stacked [G * 2 m_e, d] and [G * d, m_e] K-major).
+template <int D>
+__global__ void __launch_bounds__(kTailThreads, 1)
+    k_moe_expert(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWup,
+                 const __grid_constant__ CUtensorMap tmWdown, const __grid_constant__ CUtensorMap tmY,
+                 const int32_t* __restrict__ tile_group, const int32_t* __restrict__ num_tiles,
+                 const float* __restrict__ w_of, int me) {
+  static_assert(D == 128 || D == 256, "moe expert: model dim 128 or 256");
+  using S = TailSmem<D>;
+  constexpr int kStages = kTailStages;
+  constexpr uint32_t kStageBytes = kTailStageBytes;
+  constexpr uint32_t kKB = D / 64;
+  constexpr uint32_t kDownStage = D * 128u;  // Wdown_j^T: D rows x 64 K
+  constexpr uint32_t kUpBox = 128u * 128u;   // 128 rows x 64 K of the interleaved [gate | up]
+  constexpr int kCols = D / 2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1k(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::oBar);
+  uint64_t* w_full = bars;        // [3]
+  uint64_t* w_empty = bars + 3;   // [3]
+  uint64_t* x_full = bars + 6;    // [2] x tile of buffer b landed
+  uint64_t* u_full = bars + 8;    // [2]
+  uint64_t* h_full = bars + 10;   // [2]
+  uint64_t* d_full = bars + 12;
+  uint64_t* d_empty = bars + 13;
+  uint64_t* y_full = bars + 14;   // [2] y over x in buffer b, ready to store (per buffer: the
+                                  // epilogue cannot complete a buffer's phase twice ahead of the store)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 16);
+  const int warp = warp_id(), lane = lane_id();
+  const int num_m = *num_tiles;
+  const int n_chunks = me / 64;
+  auto xbuf = [&](int t) { return smem + S::oX + (t & 1) * S::kTileBytes; };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmX);
+    tma_prefetch_desc(&tmWup);
+    tma_prefetch_desc(&tmWdown);
+    tma_prefetch_desc(&tmY);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&w_full[s], 1);
+      mbar_init(&w_empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&x_full[i], 1);
+      mbar_init(&u_full[i], 1);
+      mbar_init(&h_full[i], 256);
+    }
+    mbar_init(d_full, 1);
+    mbar_init(d_empty, 256);
+    mbar_init(&y_full[0], 256);
+    mbar_init(&y_full[1], 256);
+    mbar_fence_init();
+  }
+  if (warp == 2) tmem_alloc(tslot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- weight stream
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      auto stage = [&](uint32_t bytes) -> uint8_t* {
+        mbar_wait_sleep(&w_empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&w_full[s], bytes);
+        return smem + S::oW + s * kStageBytes;
+      };
+      auto advance = [&]() {
+        if (++s == kStages) {
+          s = 0;
+          ph ^= 1;
+        }
+      };
+      for (int mb = blockIdx.x; mb < num_m; mb += gridDim.x) {
+        const int e = tile_group[mb];
+        auto up = [&](int j) {
+          for (int p = 0; p < static_cast<int>(kKB) / 2; ++p) {
+            uint8_t* dst = stage(2 * kUpBox);
+            tma_load_2d(dst, &tmWup, &w_full[s], (2 * p) * 64, e * 2 * me + j * 128);
+            tma_load_2d(dst + kUpBox, &tmWup, &w_full[s], (2 * p + 1) * 64, e * 2 * me + j * 128);
+            advance();
+          }
+        };
+        up(0);
+        if (n_chunks > 1) up(1);
+        for (int j = 0; j < n_chunks; ++j) {
+          uint8_t* dst = stage(kDownStage);
+          tma_load_2d(dst, &tmWdown, &w_full[s], j * 64, e * D);
+          advance();
+          if (j + 2 < n_chunks) up(j + 2);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      const uint32_t id_d = umma_idesc_bf16(128, D);
+      const uint32_t id_u = umma_idesc_bf16(128, 128);
+      const uint32_t w0 = smem_u32(smem + S::oW);
+      int s = 0;
+      uint32_t ph = 0;
+      auto wait_stage = [&]() -> uint32_t {
+        mbar_wait(&w_full[s], ph);
+        tc_fence_after();
+        return w0 + s * kStageBytes;
+      };
+      auto release_stage = [&]() {
+        mma_commit(&w_empty[s]);
+        if (++s == kStages) {
+          s = 0;
+          ph ^= 1;
+        }
+      };
+      int t = 0, c = 0;
+      for (int mb = blockIdx.x; mb < num_m; mb += gridDim.x, ++t) {
+        const uint32_t xb = smem_u32(xbuf(t));
+        mbar_wait_sleep(&x_full[t & 1], (t >> 1) & 1);
+        tc_fence_after();
+        // U buffer of hidden chunk j = the global chunk counter's parity (what E2 waits on), so
+        // tiles with an odd chunk count keep the MMA issuer and E2 in step
+        const int cbase = c;
+        auto up = [&](int j) {
+          const uint32_t u = tmem + 256 + ((cbase + j) & 1) * 128;
+          for (uint32_t p = 0; p < kKB / 2; ++p) {
+            const uint32_t b = wait_stage();
+#pragma unroll
+            for (uint32_t kh = 0; kh < 2; ++kh) {
+              const uint32_t kb = 2 * p + kh;
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                mma_bf16_ss(u, umma_sdesc_kmajor(xb + kb * 16384 + k * 32, 128),
+                            umma_sdesc_kmajor(b + kh * kUpBox + k * 32, 128), id_u, (kb | k) != 0 ? 1u : 0u);
+            }
+            release_stage();
+          }
+          mma_commit(&u_full[(cbase + j) & 1]);
+        };
+        up(0);
+        if (n_chunks > 1) up(1);
+        for (int j = 0; j < n_chunks; ++j, ++c) {
+          const int hb = c & 1;
+          mbar_wait(&h_full[hb], (c >> 1) & 1);
+          if (j == 0) mbar_wait(d_empty, (t & 1) ^ 1);  // E3 of the previous tile drained D
+          tc_fence_after();
+          const uint32_t hbase = tmem + 256 + hb * 128;
+          const uint32_t b = wait_stage();
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            mma_bf16_ts(tmem, hbase + (k >> 1) * 64 + (k & 1) * 8, umma_sdesc_kmajor(b + k * 32, 128), id_d,
+                        (j | k) != 0 ? 1u : 0u);
+          release_stage();
+          if (j + 2 < n_chunks) up(j + 2);
+        }
+        mma_commit(d_full);
+      }
+    }
+  } else if (warp == 3) {
+    // ---------------------------------------------------------------- tile I/O (TMA)
+    if (lane == 0) {
+      auto load_x = [&](int mb, int t) {
+        mbar_arrive_expect_tx(&x_full[t & 1], S::kTileBytes);
+        for (uint32_t kb = 0; kb < kKB; ++kb) tma_load_2d(xbuf(t) + kb * 16384, &tmX, &x_full[t & 1], kb * 64, mb * 128);
+      };
+      int t = 0;
+      if (static_cast<int>(blockIdx.x) < num_m) load_x(blockIdx.x, 0);
+      for (int mb = blockIdx.x; mb < num_m; mb += gridDim.x, ++t) {
+        const int next = mb + gridDim.x;
+        if (t > 0) {  // drain tile t-1 from the other buffer, then load x(t+1) into it
+          mbar_wait_sleep(&y_full[(t - 1) & 1], ((t - 1) >> 1) & 1);
+          for (uint32_t kb = 0; kb < kKB; ++kb)
+            tma_store_2d(&tmY, xbuf(t - 1) + kb * 16384, kb * 64, (mb - static_cast<int>(gridDim.x)) * 128);
+          bulk_commit();
+          bulk_wait_read0();
+        }
+        if (next < num_m) load_x(next, t + 1);
+      }
+      if (t > 0) {
+        mbar_wait_sleep(&y_full[(t - 1) & 1], ((t - 1) >> 1) & 1);
+        const int last = static_cast<int>(blockIdx.x) + (t - 1) * static_cast<int>(gridDim.x);
+        for (uint32_t kb = 0; kb < kKB; ++kb) tma_store_2d(&tmY, xbuf(t - 1) + kb * 16384, kb * 64, last * 128);
+        bulk_commit();
+        bulk_wait0();
+      }
+    }
+  } else if (warp >= 4) {
+    // ---------------------------------------------------------------- epilogue warps
+    const int ep = warp - 4;
+    const int q = ep & 3, hf = ep >> 2;
+    const int r = q * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+    const uint32_t tD = tmem + lane_off + hf * kCols;
+    int t = 0, c = 0;
+    for (int mb = blockIdx.x; mb < num_m; mb += gridDim.x, ++t) {
+      const int row = mb * 128 + r;
+      const float w = w_of[row];  // combine weight (garbage on padding rows, never read back)
+      const uint32_t xs = smem_u32(xbuf(t));
+      // ---- E2 per hidden chunk: h = swish(g) * u (input rows are already normalised)
+      for (int j = 0; j < n_chunks; ++j, ++c) {
+        const int ub = c & 1;
+        mbar_wait(&u_full[ub], (c >> 1) & 1);
+        tc_fence_after();
+        const uint32_t tu = tmem + lane_off + 256 + ub * 128 + hf * 64;
+        float v[64];
+        tmem_row_chunk<64>(tu, v);
+        uint32_t hw[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          float hh[2];
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            const float gt = v[2 * i + k], up = v[32 + 2 * i + k];
+            hh[k] = gt * up * fast_sigmoid(gt);  // swish(x) = x * sigmoid(x) (common.hpp:37)
+          }
+          hw[i] = pack_bf16x2(hh[0], hh[1]);
+        }
+        tmem_st_32x32b_x16(tu, hw);
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&h_full[ub]);
+      }
+      // ---- E3: y = bf16(w * D) in place over the x tile -> TMA store
+      mbar_wait(d_full, t & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int cc = 0; cc < kCols / 32; ++cc) {
+        float v[32];
+        tmem_row_chunk<32>(tD + cc * 32, v);
+#pragma unroll
+        for (int qd = 0; qd < 4; ++qd) {
+          const uint32_t adr = xs + sw128_off(r, (hf * kCols + cc * 32) / 8 + qd);
+          sts_v4(adr, make_int4(pack_bf16x2(w * v[qd * 8 + 0], w * v[qd * 8 + 1]),
+                                pack_bf16x2(w * v[qd * 8 + 2], w * v[qd * 8 + 3]),
+                                pack_bf16x2(w * v[qd * 8 + 4], w * v[qd * 8 + 5]),
+                                pack_bf16x2(w * v[qd * 8 + 6], w * v[qd * 8 + 7])));
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(d_empty);
+      fence_proxy_async_smem();
+      mbar_arrive(&y_full[t & 1]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
 
 }  // namespace sortk

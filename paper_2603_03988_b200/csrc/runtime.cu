@@ -67,6 +67,7 @@ struct LayerDev {
   // fp32 master buffer, this layer's routing of the last forward
   __nv_bfloat16 *w_moe_gu = nullptr, *w_moe_down = nullptr;
   CUtensorMap tmB_moe_gu, tmB_moe_down;
+  CUtensorMap tmWup_moe, tmWdown_moe;  // k_moe_expert weight stages (128 x 64 and d x 64 boxes)
   int bn_moe_gu = 0, bn_moe_down = 0;
   const float* router = nullptr;
   float* router_bias = nullptr;
@@ -98,7 +99,8 @@ struct Handle {
   int32_t *moe_tok = nullptr, *moe_slot = nullptr, *moe_off = nullptr, *moe_cursor = nullptr,
           *moe_tile_group = nullptr, *moe_ntiles = nullptr, *moe_counts = nullptr;  // counts [layers][E]
   int moe_rows[SORT_MAX_LAYERS] = {0};  // rows routed per layer in the last forward
-  CUtensorMap tmA_moe_xs, tmA_moe_hs;
+  CUtensorMap tmA_moe_xs, tmA_moe_hs, tmY_moe;
+  bool moe_fused = true;  // sort_set_option("moe_fused"): k_moe_expert instead of the grouped GEMM pair
   // ---- pre-training head
   const float* pre_proj = nullptr;  // pretrain.proj [d, item_dim] in the master buffer
   __nv_bfloat16* pre_hp = nullptr;  // projected rows [B * L, item_dim]
@@ -319,6 +321,8 @@ static void build_moe_layer(Handle& h, int l, LayerDev& L) {
   L.bn_moe_down = pick(d, me, 32);
   L.tmB_moe_gu = make_tmap_2d(L.w_moe_gu, static_cast<uint64_t>(G) * 2 * me, d, d, L.bn_moe_gu, 64, 128);
   L.tmB_moe_down = make_tmap_2d(L.w_moe_down, static_cast<uint64_t>(G) * d, me, me, L.bn_moe_down, 64, 128);
+  L.tmWup_moe = make_tmap_2d(L.w_moe_gu, static_cast<uint64_t>(G) * 2 * me, d, d, 128, 64, 128);
+  L.tmWdown_moe = make_tmap_2d(L.w_moe_down, static_cast<uint64_t>(G) * d, me, me, d, 64, 128);
   const size_t T = static_cast<size_t>(h.Bmax) * h.plan.layers[l].l_q;
   L.moe_sel = h.dalloc<int32_t>(T * h.moe_k);
   L.moe_w = h.dalloc<float>(T * h.moe_k);
@@ -348,6 +352,7 @@ static void ensure_moe_buffers(Handle& h) {
   CK(cudaMemset(h.moe_counts, 0, static_cast<size_t>(h.cfg.layers) * h.moe_E * 4));
   h.tmA_moe_xs = make_tmap_2d(h.moe_xs, P, h.d, h.d, 128, 64, 128);
   h.tmA_moe_hs = make_tmap_2d(h.moe_hs, P, h.moe_m, h.moe_m, 128, 64, 128);
+  h.tmY_moe = make_tmap_2d(h.moe_ys, P, h.d, h.d, 128, 64, 128);
 }
 
 static void finalize(Handle& h) {
@@ -962,6 +967,25 @@ static void run_moe(Handle& h, int l, __nv_bfloat16* X, float4* SS, int T) {
   check_launch("moe route/plan/scatter");
   h.launches += 3;
   stage_mark(h, "L" + std::to_string(l) + ".moe_route");
+  if (h.moe_fused && (d == 128 || d == 256)) {  // hidden chunk stays on chip (moe.cuh)
+    static bool attr = false;
+    if (!attr) {
+      CK(cudaFuncSetAttribute(k_moe_expert<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(TailSmem<256>::bytes)));
+      CK(cudaFuncSetAttribute(k_moe_expert<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(TailSmem<128>::bytes)));
+      attr = true;
+    }
+    const int grid = std::max(1, std::min(h.moe_tiles_max, h.num_sms));
+    if (d == 256)
+      k_moe_expert<256><<<grid, kTailThreads, TailSmem<256>::bytes, h.stream>>>(
+          h.tmA_moe_xs, L.tmWup_moe, L.tmWdown_moe, h.tmY_moe, h.moe_tile_group, h.moe_ntiles, h.moe_wof, me);
+    else
+      k_moe_expert<128><<<grid, kTailThreads, TailSmem<128>::bytes, h.stream>>>(
+          h.tmA_moe_xs, L.tmWup_moe, L.tmWdown_moe, h.tmY_moe, h.moe_tile_group, h.moe_ntiles, h.moe_wof, me);
+    check_launch("moe expert");
+    ++h.launches;
+  } else {
   EpiMoeGU eg;
   eg.tile_group = h.moe_tile_group;
   eg.num_tiles = h.moe_ntiles;
@@ -979,6 +1003,7 @@ static void run_moe(Handle& h, int l, __nv_bfloat16* X, float4* SS, int T) {
   ed.y = h.moe_ys;
   ed.d = d;
   launch_gemm_grouped(h, h.tmA_moe_hs, L.tmB_moe_down, d, me, L.bn_moe_down, ed);
+  }
   stage_mark(h, "L" + std::to_string(l) + ".moe_experts");
   const int cgrid = std::max(1, std::min((T + 7) / 8, h.num_sms * 8));
   k_moe_combine<<<cgrid, 256, 0, h.stream>>>(X, T, d, h.moe_ys, h.moe_slot, k, S, SS);
@@ -2508,6 +2533,8 @@ int sort_set_option(SortHandle p, const char* name, int32_t value) {
       h->qkvg_pair = value != 0;
     } else if (std::strcmp(name, "attn_subtiles") == 0) {
       h->attn_sub = value != 0;
+    } else if (std::strcmp(name, "moe_fused") == 0) {
+      h->moe_fused = value != 0;
     } else {
       throw ConfigError(std::string("unknown option ") + name);
     }
