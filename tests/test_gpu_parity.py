@@ -426,3 +426,18 @@ def test_subtile_attention_option_matches_default(which, tiny, base):
         gm.set_option("attn_subtiles", 0)
     assert np.max(np.abs(z1 - z0)) < LOGIT_MAX_ABS
     assert rel_l2(z1, z0) < LOGIT_REL_L2
+
+
+def test_fused_tail_odd_hidden_chunks_many_tiles():
+    """m = 320 gives 5 hidden chunks per tile (odd), and 64 requests give more 128-row tiles
+    than SMs, so CTAs run several tiles: the U-buffer parity must follow the global chunk
+    counter (regression test); the result stays bitwise equal to the unfused GEMM chain."""
+    cfg = base_config(ffn_dim=320, n_hist=300, n_cand=20, n_items=5000)
+    cfg.keep = [cfg.prefix_len] * 4
+    P = synth.make_params(cfg, seed=19)
+    gm = R.SortModel(cfg, P, max_batch=64)
+    b = synth.make_batch(cfg, 64, seed=20)
+    _, z_f = gm.forward_logits(b)
+    gm.set_option("fused_tail", 0)
+    _, z_u = gm.forward_logits(b)
+    assert np.array_equal(z_f, z_u)
