@@ -28,8 +28,9 @@
 namespace sortk {
 
 // Grouped mode (MoE experts): an epilogue declaring `kGrouped = true` carries
-//   const int32_t* tile_group;  // group (expert) of every 128-row m-block
-//   const int32_t* num_tiles;   // number of m-blocks (device-side, written by the router)
+//   const int32_t* tile_group;  // group (expert) of every listed 128-row tile
+//   const int32_t* tile_mblk;   // its m-block (first row / 128)
+//   const int32_t* num_tiles;   // number of listed tiles (device-side, written by the router)
 //   int group_n;                // weight rows per group in the stacked B operand
 // The A rows of each group are contiguous and padded to 128, so an m-block belongs to one
 // group; B stacks the groups' [N, K] weights. A CTA keeps two weight slices resident and
@@ -131,7 +132,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int nb = unit % num_n;
   const int m_first = unit / num_n;
   const int m_step = units / num_n;
-  auto mrow0 = [&](int mb) { return (mb * kNcta + static_cast<int>(rank)) * kGemmBM; };
+  auto mrow0 = [&](int mb) {
+    if constexpr (kGroup) {
+      return epi.tile_mblk[mb] * kGemmBM;  // grouped: the listed tile's first row
+    } else {
+      return (mb * kNcta + static_cast<int>(rank)) * kGemmBM;
+    }
+  };
   // residual epilogues keep one sum-of-squares slot per (n-slice, half): at most 4
   if (num_n > 2 && threadIdx.x == 0 && blockIdx.x == 0 && Epi::kMaxParts < num_n * 2) __trap();
 

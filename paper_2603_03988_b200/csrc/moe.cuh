@@ -249,34 +249,205 @@ __global__ void __launch_bounds__(256) k_moe_route8(const __nv_bfloat16* __restr
   if (threadIdx.x < E && hist[threadIdx.x]) atomicAdd(&counts[threadIdx.x], hist[threadIdx.x]);
 }
 
+// Routing and scatter in one pass (E <= 8, top-K with K <= 2): a warp routes 32 tokens
+// (the k_moe_route8 arithmetic, results parked in lane i for token i), takes their expert-
+// segment positions with one warp-aggregated atomic per (slot, expert) on the per-expert
+// cursors (which end as the expert loads), then writes each token's normalised bf16 row into
+// its K (+ shared) segments, re-reading the row from L2.
+template <int K>
+__global__ void __launch_bounds__(256) k_moe_route_scatter8(
+    const __nv_bfloat16* __restrict__ x, int T, int d, const float* __restrict__ gain,
+    const float* __restrict__ router, const float* __restrict__ bias, int E, int shared, int Tcap,
+    int32_t* __restrict__ sel, float* __restrict__ wgt, int32_t* __restrict__ cursor,
+    __nv_bfloat16* __restrict__ xs, int32_t* __restrict__ tok_of, float* __restrict__ w_of,
+    int32_t* __restrict__ slot_pos, int32_t* __restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  const int c0 = lane * 8;
+  const bool act = c0 < d;
+  const int S = K + shared;
+  float g[8], w[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    g[i] = act ? gain[c0 + i] : 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) w[e][i] = act && e < E ? router[static_cast<size_t>(c0 + i) * E + e] : 0.f;
+  }
+  const int my_e = lane >> 2;
+  const bool owner = (lane & 3) == 0 && my_e < E;
+  const float my_b = owner ? bias[my_e] : 0.f;
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  for (int base = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < T; base += warps * 32) {
+    const int n = min(32, T - base);
+    int te[K];
+    float tw[K], tinv = 0.f;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      te[j] = 0;
+      tw[j] = 0.f;
+    }
+    // software pipeline: token i + 2's row load is in flight while token i is routed
+    int4 nx0 = make_int4(0, 0, 0, 0), nx1 = make_int4(0, 0, 0, 0);
+    if (act) {
+      nx0 = *reinterpret_cast<const int4*>(x + static_cast<size_t>(base) * d + c0);
+      if (n > 1) nx1 = *reinterpret_cast<const int4*>(x + static_cast<size_t>(base + 1) * d + c0);
+    }
+    for (int i = 0; i < n; ++i) {
+      const int t = base + i;
+      const int4 raw = nx0;
+      nx0 = nx1;
+      if (act && i + 2 < n) nx1 = *reinterpret_cast<const int4*>(x + static_cast<size_t>(t + 2) * d + c0);
+      float v[8];
+      {
+        const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 f = __bfloat1622float2(p2[q]);
+          v[2 * q] = f.x;
+          v[2 * q + 1] = f.y;
+        }
+      }
+      float ss = 0.f;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) ss = fmaf(v[q], v[q], ss);
+      const float inv = rsqrtf(warp_sum(ss) / static_cast<float>(d) + 1e-6f);  // norm.hpp:23-24
+      float p[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        float z = 0.f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) z = fmaf(v[q] * inv * g[q], w[e][q], z);
+        p[e] = z;
+      }
+      float qq[4], rr[2];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        qq[q] = (b4 ? p[q + 4] : p[q]) + __shfl_xor_sync(0xffffffffu, b4 ? p[q] : p[q + 4], 16);
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        rr[q] = (b3 ? qq[q + 2] : qq[q]) + __shfl_xor_sync(0xffffffffu, b3 ? qq[q] : qq[q + 2], 8);
+      float z = (b2 ? rr[1] : rr[0]) + __shfl_xor_sync(0xffffffffu, b2 ? rr[0] : rr[1], 4);
+      z += __shfl_xor_sync(0xffffffffu, z, 2);
+      z += __shfl_xor_sync(0xffffffffu, z, 1);
+      const float sc = 1.f / (1.f + expf(-z));  // sigmoid gate
+      const float kf = sc + my_b;
+      const bool bad = owner && !isfinite(kf);
+      uint32_t key = owner && !bad ? float_key(kf) : 0u;
+      if (__any_sync(0xffffffffu, bad) && lane == 0) {
+        atomicOr(err, kErrMoeNonFinite);
+        atomicCAS(err + 1, 0, t + 1);
+      }
+      int se[K];
+      float sw[K];
+      float tot = 0.f;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const uint32_t best = __reduce_max_sync(0xffffffffu, key);
+        const uint32_t m = __ballot_sync(0xffffffffu, key == best && owner);
+        const int wl = m ? __ffs(m) - 1 : 0;  // lowest lane = lowest expert on ties
+        sw[j] = m ? __shfl_sync(0xffffffffu, sc, wl) : 1.f;
+        se[j] = wl >> 2;
+        if (lane == wl) key = 0u;
+        tot += sw[j];
+      }
+      if (lane == i) {
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          te[j] = se[j];
+          tw[j] = sw[j] / tot;
+        }
+        tinv = inv;
+      }
+    }
+    // expert-segment positions: one atomic per (slot, expert) group of the warp's tokens
+    const bool tv = lane < n;
+    const int t = base + lane;
+    int pos[K + 1];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const int e = tv ? te[j] : -1 - lane;  // inactive lanes never match
+      const unsigned peers = __match_any_sync(0xffffffffu, e);
+      const int leader = __ffs(peers) - 1;
+      int b = 0;
+      if (lane == leader && tv) b = atomicAdd(&cursor[e], __popc(peers));
+      b = __shfl_sync(0xffffffffu, b, leader);
+      pos[j] = tv ? e * Tcap + b + __popc(peers & ((1u << lane) - 1u)) : 0;
+    }
+    pos[K] = E * Tcap + t;  // shared expert: the token's own row of its segment
+    if (tv) {
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        sel[static_cast<size_t>(t) * K + j] = te[j];
+        wgt[static_cast<size_t>(t) * K + j] = tw[j];
+      }
+#pragma unroll
+      for (int j = 0; j <= K; ++j) {
+        if (j == K && !shared) break;
+        tok_of[pos[j]] = t;
+        w_of[pos[j]] = j < K ? tw[j] : 1.f;
+        slot_pos[static_cast<size_t>(t) * S + j] = pos[j];
+      }
+    }
+    // rows: token by token, the whole warp moves one normalised row (16 B per lane)
+    for (int i = 0; i < n; ++i) {
+      int pj[K + 1];
+#pragma unroll
+      for (int j = 0; j <= K; ++j) pj[j] = __shfl_sync(0xffffffffu, pos[j], i);
+      const float iv = __shfl_sync(0xffffffffu, tinv, i);
+      if (!act) continue;
+      const int4 raw = *reinterpret_cast<const int4*>(x + static_cast<size_t>(base + i) * d + c0);
+      const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+      uint32_t o[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = __bfloat1622float2(p2[q]);
+        o[q] = pack_bf16x2(f.x * iv * g[2 * q], f.y * iv * g[2 * q + 1]);
+      }
+      const int4 ov = make_int4(o[0], o[1], o[2], o[3]);
+#pragma unroll
+      for (int j = 0; j <= K; ++j) {
+        if (j == K && !shared) break;
+        *reinterpret_cast<int4*>(xs + static_cast<size_t>(pj[j]) * d + c0) = ov;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------------------------ plan
-// One block: group g (E routed + shared) gets rows [off[g], off[g] + 128 * ceil(count / 128));
-// its m-blocks are listed in tile_group; padding rows get tok_of = -1. cursors reset.
-__global__ void k_moe_plan(const int32_t* __restrict__ counts, int E, int shared, int T, int32_t* __restrict__ off,
-                           int32_t* __restrict__ cursor, int32_t* __restrict__ tile_group,
+// Expert g owns the row segment [g * Tcap, (g + 1) * Tcap) (Tcap = T rounded up to 128; the
+// shared expert's rows are its tokens in order). One block: the segment offsets, the list of
+// 128-row tiles that hold rows (tile k: expert tile_group[k], first row 128 * tile_mblk[k]),
+// padding rows of the last tile marked tok_of = -1, scatter cursors reset.
+__global__ void k_moe_plan(const int32_t* __restrict__ counts, int E, int shared, int T, int Tcap,
+                           int32_t* __restrict__ off, int32_t* __restrict__ cursor,
+                           int32_t* __restrict__ tile_group, int32_t* __restrict__ tile_mblk,
                            int32_t* __restrict__ num_tiles, int32_t* __restrict__ tok_of) {
-  __shared__ int s_off[kMoeMaxExperts + 2], s_cnt[kMoeMaxExperts + 1];
+  __shared__ int s_first[kMoeMaxExperts + 2], s_cnt[kMoeMaxExperts + 1];
   const int G = E + shared;
   if (threadIdx.x == 0) {
-    int o = 0;
+    int k = 0;
     for (int g = 0; g < G; ++g) {
       const int c = g < E ? counts[g] : T;
       s_cnt[g] = c;
-      s_off[g] = o;
-      o += (c + 127) / 128 * 128;
+      s_first[g] = k;
+      k += (c + 127) / 128;
     }
-    s_off[G] = o;
-    *num_tiles = o / 128;
+    s_first[G] = k;
+    *num_tiles = k;
   }
   __syncthreads();
   for (int g = threadIdx.x; g < G; g += blockDim.x) {
-    off[g] = s_off[g];
+    off[g] = g * Tcap;
     cursor[g] = 0;
   }
   for (int g = 0; g < G; ++g) {
-    const int t0 = s_off[g] / 128, t1 = s_off[g + 1] / 128;
-    for (int i = t0 + threadIdx.x; i < t1; i += blockDim.x) tile_group[i] = g;
-    for (int r = s_off[g] + s_cnt[g] + threadIdx.x; r < s_off[g + 1]; r += blockDim.x) tok_of[r] = -1;
+    const int k0 = s_first[g], nk = s_first[g + 1] - k0;
+    for (int i = threadIdx.x; i < nk; i += blockDim.x) {
+      tile_group[k0 + i] = g;
+      tile_mblk[k0 + i] = g * (Tcap / 128) + i;
+    }
+    const int r0 = g * Tcap + s_cnt[g], r1 = g * Tcap + nk * 128;
+    for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) tok_of[r] = -1;
   }
 }
 
@@ -423,6 +594,7 @@ struct EpiMoeGU {
   static constexpr int kRopeFloats = 0;
   static constexpr bool kGrouped = true;
   const int32_t* tile_group;
+  const int32_t* tile_mblk;
   const int32_t* num_tiles;
   int group_n;
   const int32_t* tok_of;
@@ -456,6 +628,7 @@ struct EpiMoeDown {
   static constexpr int kRopeFloats = 0;
   static constexpr bool kGrouped = true;
   const int32_t* tile_group;
+  const int32_t* tile_mblk;
   const int32_t* num_tiles;
   int group_n;
   const int32_t* tok_of;
@@ -498,8 +671,8 @@ template <int D>
 __global__ void __launch_bounds__(kTailThreads, 1)
     k_moe_expert(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmWup,
                  const __grid_constant__ CUtensorMap tmWdown, const __grid_constant__ CUtensorMap tmY,
-                 const int32_t* __restrict__ tile_group, const int32_t* __restrict__ num_tiles,
-                 const float* __restrict__ w_of, int me) {
+                 const int32_t* __restrict__ tile_group, const int32_t* __restrict__ tile_mblk,
+                 const int32_t* __restrict__ num_tiles, const float* __restrict__ w_of, int me) {
   static_assert(D == 128 || D == 256, "moe expert: model dim 128 or 256");
   using S = TailSmem<D>;
   constexpr int kStages = kTailStages;
@@ -656,7 +829,8 @@ __global__ void __launch_bounds__(kTailThreads, 1)
     if (lane == 0) {
       auto load_x = [&](int mb, int t) {
         mbar_arrive_expect_tx(&x_full[t & 1], S::kTileBytes);
-        for (uint32_t kb = 0; kb < kKB; ++kb) tma_load_2d(xbuf(t) + kb * 16384, &tmX, &x_full[t & 1], kb * 64, mb * 128);
+        for (uint32_t kb = 0; kb < kKB; ++kb)
+          tma_load_2d(xbuf(t) + kb * 16384, &tmX, &x_full[t & 1], kb * 64, tile_mblk[mb] * 128);
       };
       int t = 0;
       if (static_cast<int>(blockIdx.x) < num_m) load_x(blockIdx.x, 0);
@@ -665,7 +839,7 @@ __global__ void __launch_bounds__(kTailThreads, 1)
         if (t > 0) {  // drain tile t-1 from the other buffer, then load x(t+1) into it
           mbar_wait_sleep(&y_full[(t - 1) & 1], ((t - 1) >> 1) & 1);
           for (uint32_t kb = 0; kb < kKB; ++kb)
-            tma_store_2d(&tmY, xbuf(t - 1) + kb * 16384, kb * 64, (mb - static_cast<int>(gridDim.x)) * 128);
+            tma_store_2d(&tmY, xbuf(t - 1) + kb * 16384, kb * 64, tile_mblk[mb - static_cast<int>(gridDim.x)] * 128);
           bulk_commit();
           bulk_wait_read0();
         }
@@ -674,7 +848,7 @@ __global__ void __launch_bounds__(kTailThreads, 1)
       if (t > 0) {
         mbar_wait_sleep(&y_full[(t - 1) & 1], ((t - 1) >> 1) & 1);
         const int last = static_cast<int>(blockIdx.x) + (t - 1) * static_cast<int>(gridDim.x);
-        for (uint32_t kb = 0; kb < kKB; ++kb) tma_store_2d(&tmY, xbuf(t - 1) + kb * 16384, kb * 64, last * 128);
+        for (uint32_t kb = 0; kb < kKB; ++kb) tma_store_2d(&tmY, xbuf(t - 1) + kb * 16384, kb * 64, tile_mblk[last] * 128);
         bulk_commit();
         bulk_wait0();
       }
@@ -688,7 +862,7 @@ __global__ void __launch_bounds__(kTailThreads, 1)
     const uint32_t tD = tmem + lane_off + hf * kCols;
     int t = 0, c = 0;
     for (int mb = blockIdx.x; mb < num_m; mb += gridDim.x, ++t) {
-      const int row = mb * 128 + r;
+      const int row = tile_mblk[mb] * 128 + r;
       const float w = w_of[row];  // combine weight (garbage on padding rows, never read back)
       const uint32_t xs = smem_u32(xbuf(t));
       // ---- E2 per hidden chunk: h = swish(g) * u (input rows are already normalised)

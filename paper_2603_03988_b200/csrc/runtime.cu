@@ -97,7 +97,8 @@ struct Handle {
   __nv_bfloat16* moe_ys = nullptr;
   float *moe_inv = nullptr, *moe_wof = nullptr;
   int32_t *moe_tok = nullptr, *moe_slot = nullptr, *moe_off = nullptr, *moe_cursor = nullptr,
-          *moe_tile_group = nullptr, *moe_ntiles = nullptr, *moe_counts = nullptr;  // counts [layers][E]
+          *moe_tile_group = nullptr, *moe_tile_mblk = nullptr, *moe_ntiles = nullptr,
+          *moe_counts = nullptr;  // counts [layers][E]
   int moe_rows[SORT_MAX_LAYERS] = {0};  // rows routed per layer in the last forward
   CUtensorMap tmA_moe_xs, tmA_moe_hs, tmY_moe;
   bool moe_fused = true;  // sort_set_option("moe_fused"): k_moe_expert instead of the grouped GEMM pair
@@ -328,14 +329,17 @@ static void build_moe_layer(Handle& h, int l, LayerDev& L) {
   L.moe_w = h.dalloc<float>(T * h.moe_k);
 }
 
-// Token-major MoE workspace sized for the largest layer: P = T (k + s) rows + per-group padding.
+// MoE workspace sized for the largest layer: expert g owns rows [g Tcap, (g + 1) Tcap) of the
+// expert-sorted buffers (Tcap = the layer's token count rounded up to 128), so routing can
+// place rows before the expert loads are known.
 static void ensure_moe_buffers(Handle& h) {
   int tq = 0;
   for (const LayerPlan& lp : h.plan.layers) tq = std::max(tq, lp.l_q);
   const size_t T = static_cast<size_t>(h.Bmax) * tq;
+  const size_t Tcap = (T + 127) / 128 * 128;
   const int G = h.moe_E + h.moe_s, S = h.moe_k + h.moe_s;
-  h.moe_pmax = static_cast<int>(T * S + static_cast<size_t>(G) * 128);
-  h.moe_tiles_max = h.moe_pmax / 128;
+  h.moe_pmax = static_cast<int>(static_cast<size_t>(G) * Tcap);
+  h.moe_tiles_max = static_cast<int>(T * S / 128 + G + 1);
   const size_t P = h.moe_pmax;
   h.moe_xs = h.dalloc<__nv_bfloat16>(P * h.d);
   h.moe_hs = h.dalloc<__nv_bfloat16>(P * h.moe_m);
@@ -347,6 +351,7 @@ static void ensure_moe_buffers(Handle& h) {
   h.moe_off = h.dalloc<int32_t>(G + 1);
   h.moe_cursor = h.dalloc<int32_t>(G + 1);
   h.moe_tile_group = h.dalloc<int32_t>(h.moe_tiles_max + 1);
+  h.moe_tile_mblk = h.dalloc<int32_t>(h.moe_tiles_max + 1);
   h.moe_ntiles = h.dalloc<int32_t>(1);
   h.moe_counts = h.dalloc<int32_t>(static_cast<size_t>(h.cfg.layers) * h.moe_E);
   CK(cudaMemset(h.moe_counts, 0, static_cast<size_t>(h.cfg.layers) * h.moe_E * 4));
@@ -942,7 +947,9 @@ static void run_tokenizer(Handle& h, int B) {
 static void run_moe(Handle& h, int l, __nv_bfloat16* X, float4* SS, int T) {
   LayerDev& L = h.layers[l];
   const int d = h.d, E = h.moe_E, k = h.moe_k, S = h.moe_s, me = h.moe_m;
-  if (T * (k + S) + (E + S) * 128 > h.moe_pmax) throw RuntimeFailure("moe: workspace too small");
+  const int Tcap = (T + 127) / 128 * 128;
+  if (static_cast<int64_t>(E + S) * Tcap > h.moe_pmax || T * (k + S) / 128 + E + S + 1 > h.moe_tiles_max)
+    throw RuntimeFailure("moe: workspace too small");
   int32_t* counts = h.moe_counts + static_cast<size_t>(l) * E;
   const float* gain = h.w32.at("block." + std::to_string(l) + ".ffn_norm");
   static bool attr = false;
@@ -952,20 +959,36 @@ static void run_moe(Handle& h, int l, __nv_bfloat16* X, float4* SS, int T) {
     attr = true;
   }
   CK(cudaMemsetAsync(counts, 0, static_cast<size_t>(E) * 4, h.stream));
-  const int rgrid = std::max(1, std::min((T + 7) / 8, h.num_sms * 8));
-  if (E <= 8)  // persistent: 2 resident CTAs per SM (120 registers)
-    k_moe_route8<<<std::max(1, std::min((T + 7) / 8, 2 * h.num_sms)), 256, 0, h.stream>>>(X, T, d, gain, L.router, L.router_bias, E, k, L.moe_sel, L.moe_w,
-                                              h.moe_inv, counts, h.err);
-  else
-    k_moe_route<<<rgrid, 256, (static_cast<size_t>(d) * E + 8 * 32 * (E + 1)) * 4, h.stream>>>(
-        X, T, d, gain, L.router, L.router_bias, E, k, L.moe_sel, L.moe_w, h.moe_inv, counts, h.err);
-  k_moe_plan<<<1, 256, 0, h.stream>>>(counts, E, S, T, h.moe_off, h.moe_cursor, h.moe_tile_group, h.moe_ntiles,
-                                      h.moe_tok);
-  const int sgrid = std::max(1, std::min((T + 255) / 256, h.num_sms * 8));
-  k_moe_scatter<<<sgrid, 256, 0, h.stream>>>(X, T, d, gain, h.moe_inv, L.moe_sel, L.moe_w, E, k, S, h.moe_off,
-                                             h.moe_cursor, h.moe_xs, h.moe_tok, h.moe_wof, h.moe_slot);
-  check_launch("moe route/plan/scatter");
-  h.launches += 3;
+  if (E <= 8 && k <= 2) {  // routing and scatter in one pass; the cursors end as the loads
+    const int grid = std::max(1, std::min((T + 255) / 256, 2 * h.num_sms));
+    if (k == 1)
+      k_moe_route_scatter8<1><<<grid, 256, 0, h.stream>>>(X, T, d, gain, L.router, L.router_bias, E, S, Tcap,
+                                                          L.moe_sel, L.moe_w, counts, h.moe_xs, h.moe_tok, h.moe_wof,
+                                                          h.moe_slot, h.err);
+    else
+      k_moe_route_scatter8<2><<<grid, 256, 0, h.stream>>>(X, T, d, gain, L.router, L.router_bias, E, S, Tcap,
+                                                          L.moe_sel, L.moe_w, counts, h.moe_xs, h.moe_tok, h.moe_wof,
+                                                          h.moe_slot, h.err);
+    k_moe_plan<<<1, 256, 0, h.stream>>>(counts, E, S, T, Tcap, h.moe_off, h.moe_cursor, h.moe_tile_group,
+                                        h.moe_tile_mblk, h.moe_ntiles, h.moe_tok);
+    check_launch("moe route+scatter/plan");
+    h.launches += 2;
+  } else {
+    const int rgrid = std::max(1, std::min((T + 7) / 8, h.num_sms * 8));
+    if (E <= 8)  // persistent: 2 resident CTAs per SM (120 registers)
+      k_moe_route8<<<std::max(1, std::min((T + 7) / 8, 2 * h.num_sms)), 256, 0, h.stream>>>(
+          X, T, d, gain, L.router, L.router_bias, E, k, L.moe_sel, L.moe_w, h.moe_inv, counts, h.err);
+    else
+      k_moe_route<<<rgrid, 256, (static_cast<size_t>(d) * E + 8 * 32 * (E + 1)) * 4, h.stream>>>(
+          X, T, d, gain, L.router, L.router_bias, E, k, L.moe_sel, L.moe_w, h.moe_inv, counts, h.err);
+    k_moe_plan<<<1, 256, 0, h.stream>>>(counts, E, S, T, Tcap, h.moe_off, h.moe_cursor, h.moe_tile_group,
+                                        h.moe_tile_mblk, h.moe_ntiles, h.moe_tok);
+    const int sgrid = std::max(1, std::min((T + 255) / 256, h.num_sms * 8));
+    k_moe_scatter<<<sgrid, 256, 0, h.stream>>>(X, T, d, gain, h.moe_inv, L.moe_sel, L.moe_w, E, k, S, h.moe_off,
+                                               h.moe_cursor, h.moe_xs, h.moe_tok, h.moe_wof, h.moe_slot);
+    check_launch("moe route/plan/scatter");
+    h.launches += 3;
+  }
   stage_mark(h, "L" + std::to_string(l) + ".moe_route");
   if (h.moe_fused && (d == 128 || d == 256)) {  // hidden chunk stays on chip (moe.cuh)
     static bool attr = false;
@@ -979,15 +1002,18 @@ static void run_moe(Handle& h, int l, __nv_bfloat16* X, float4* SS, int T) {
     const int grid = std::max(1, std::min(h.moe_tiles_max, h.num_sms));
     if (d == 256)
       k_moe_expert<256><<<grid, kTailThreads, TailSmem<256>::bytes, h.stream>>>(
-          h.tmA_moe_xs, L.tmWup_moe, L.tmWdown_moe, h.tmY_moe, h.moe_tile_group, h.moe_ntiles, h.moe_wof, me);
+          h.tmA_moe_xs, L.tmWup_moe, L.tmWdown_moe, h.tmY_moe, h.moe_tile_group, h.moe_tile_mblk, h.moe_ntiles,
+          h.moe_wof, me);
     else
       k_moe_expert<128><<<grid, kTailThreads, TailSmem<128>::bytes, h.stream>>>(
-          h.tmA_moe_xs, L.tmWup_moe, L.tmWdown_moe, h.tmY_moe, h.moe_tile_group, h.moe_ntiles, h.moe_wof, me);
+          h.tmA_moe_xs, L.tmWup_moe, L.tmWdown_moe, h.tmY_moe, h.moe_tile_group, h.moe_tile_mblk, h.moe_ntiles,
+          h.moe_wof, me);
     check_launch("moe expert");
     ++h.launches;
   } else {
   EpiMoeGU eg;
   eg.tile_group = h.moe_tile_group;
+  eg.tile_mblk = h.moe_tile_mblk;
   eg.num_tiles = h.moe_ntiles;
   eg.group_n = 2 * me;
   eg.tok_of = h.moe_tok;
@@ -996,6 +1022,7 @@ static void run_moe(Handle& h, int l, __nv_bfloat16* X, float4* SS, int T) {
   launch_gemm_grouped(h, h.tmA_moe_xs, L.tmB_moe_gu, 2 * me, d, L.bn_moe_gu, eg);
   EpiMoeDown ed;
   ed.tile_group = h.moe_tile_group;
+  ed.tile_mblk = h.moe_tile_mblk;
   ed.num_tiles = h.moe_ntiles;
   ed.group_n = d;
   ed.tok_of = h.moe_tok;
