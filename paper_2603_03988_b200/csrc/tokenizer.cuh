@@ -59,7 +59,7 @@ struct TokParams {
 };
 
 enum : int { kGroupHist = 0, kGroupCand = 1, kGroupProf = 2 };
-constexpr int kTokThreads = 128;
+constexpr int kTokThreads = 256;  // two threads per token row (gather halves, epilogue column halves)
 constexpr int kErrOOV = 1;
 
 __device__ __forceinline__ int tok_time_bucket(int64_t delta, int nb) {
@@ -89,8 +89,10 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
   float* sGain = sBias + d;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sGain + d);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+  float* sSS = reinterpret_cast<float*>(bar + 2);  // [2 column halves][128 rows] partial sums
 
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int rt = t & 127, hh = t >> 7;  // token row of the tile, which half of it this thread owns
   const uint32_t tcols = d <= 32 ? 32 : (d <= 64 ? 64 : (d <= 128 ? 128 : 256));
   if (t == 0) {
     mbar_init(bar, 1);
@@ -122,7 +124,7 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
   // embedding rows (K padded to 64 with zeros). Issued one tile ahead, so the dependent
   // id -> row loads of tile i+1 are in flight while tile i's MMA and epilogue run.
   struct Row {
-    int4 c[8];
+    int4 c[4];  // chunks [4 hh, 4 hh + 4) of the row
     int out_row;
   };
   auto gather = [&](int tile, Row& g) {
@@ -132,7 +134,7 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
     if (tile < n_tiles) {
       int e0, count;
       const int group = group_of(tile, e0, count);
-      const int e = e0 + t;
+      const int e = e0 + rt;
       if (e < count) {
         if (group == kGroupHist) {
           const int b = e / p.H, i = e - b * p.H;
@@ -150,7 +152,7 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
             act = static_cast<unsigned>(act) < static_cast<unsigned>(p.n_actions) ? act : 0;
             sc = static_cast<unsigned>(sc) < static_cast<unsigned>(p.n_scenes) ? sc : 0;
           }
-          if (p.hist_time) p.hist_time[e] = tb;
+          if (p.hist_time && hh == 0) p.hist_time[e] = tb;
           src[0] = p.item_tab + static_cast<size_t>(item) * p.item_dim;
           src[1] = p.action_tab + static_cast<size_t>(act) * p.action_dim;
           src[2] = p.scene_tab + static_cast<size_t>(sc) * p.scene_dim;
@@ -183,15 +185,14 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
         }
       }
     }
-    // chunk c of the concatenated row -> (segment, offset); static register indexing
-    int seg = 0, base = 0;
+    // chunk c = 4 hh + i of the concatenated row -> (segment, offset), constant-indexed selects
+    const int e1 = n8[0], e2 = e1 + n8[1], e3 = e2 + n8[2], e4 = e3 + n8[3];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      while (seg < 4 && c - base >= n8[seg]) {
-        base += n8[seg];
-        ++seg;
-      }
-      g.c[c] = seg < 4 ? __ldg(reinterpret_cast<const int4*>(src[seg]) + (c - base)) : make_int4(0, 0, 0, 0);
+    for (int i = 0; i < 4; ++i) {
+      const int c = hh * 4 + i;
+      const __nv_bfloat16* sp = c < e1 ? src[0] : (c < e2 ? src[1] : (c < e3 ? src[2] : src[3]));
+      const int o = c < e1 ? c : (c < e2 ? c - e1 : (c < e3 ? c - e2 : c - e3));
+      g.c[i] = c < e4 ? __ldg(reinterpret_cast<const int4*>(sp) + o) : make_int4(0, 0, 0, 0);
     }
   };
   int cur_group = -1;
@@ -215,9 +216,12 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
       cur_group = group;
     }
     // ---- 1. this thread's gathered row -> the swizzled A tile
-    uint8_t* arow = sA + t * 128;
+    uint8_t* arow = sA + rt * 128;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) *reinterpret_cast<int4*>(arow + ((c ^ (t & 7)) << 4)) = g.c[c];
+    for (int i = 0; i < 4; ++i) {
+      const int c = hh * 4 + i;
+      *reinterpret_cast<int4*>(arow + ((c ^ (rt & 7)) << 4)) = g.c[i];
+    }
     const int out_row = g.out_row;
     const bool valid = out_row >= 0;
     fence_proxy_async_smem();
@@ -236,42 +240,47 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_fence_after();
-    // ---- 3. epilogue: bias + RMSNorm(gain) -> bf16 row + sum of squares. 64 accumulator
-    // columns per TMEM round trip (two x32 loads, one wait); bias / gain as float4 LDS.
-    const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    // ---- 3. epilogue: bias + RMSNorm(gain) -> bf16 row + sum of squares. Warp w reads TMEM
+    // lane quarter w % 4 (its 32 rows) and columns [hh * d/2, (hh + 1) * d/2); the two halves
+    // combine their sums of squares through shared memory. 32 accumulator columns per load.
+    const int q = warp & 3, r = q * 32 + lane;
+    const int cb = hh * (d / 2), ce = cb + d / 2;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
     const uint32_t sb = smem_u32(sBias), sgn = smem_u32(sGain);
     float ss = 0.f;
-    for (int c = 0; c < d; c += 64) {
-      uint32_t r[64];
-      tmem_ld_32x32b_x32(trow + c, *reinterpret_cast<uint32_t(*)[32]>(r));
-      tmem_ld_32x32b_x32(trow + c + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+    for (int c = cb; c < ce; c += 32) {
+      uint32_t rv[32];
+      tmem_ld_32x32b_x32(trow + c, rv);
       tmem_ld_wait();
 #pragma unroll
-      for (int i = 0; i < 64; i += 4) {
+      for (int i = 0; i < 32; i += 4) {
         const float4 bv = lds_f32x4(sb + (c + i) * 4);
-        const float v0 = __uint_as_float(r[i]) + bv.x, v1 = __uint_as_float(r[i + 1]) + bv.y;
-        const float v2 = __uint_as_float(r[i + 2]) + bv.z, v3 = __uint_as_float(r[i + 3]) + bv.w;
+        const float v0 = __uint_as_float(rv[i]) + bv.x, v1 = __uint_as_float(rv[i + 1]) + bv.y;
+        const float v2 = __uint_as_float(rv[i + 2]) + bv.z, v3 = __uint_as_float(rv[i + 3]) + bv.w;
         ss += v0 * v0 + v1 * v1 + v2 * v2 + v3 * v3;
       }
     }
-    const float inv = rsqrtf(ss / static_cast<float>(d) + 1e-6f);
+    sSS[hh * 128 + r] = ss;
+    named_bar_sync(1 + q, 64);
+    const float inv = rsqrtf((sSS[r] + sSS[128 + r]) / static_cast<float>(d) + 1e-6f);
+    named_bar_sync(1 + q, 64);  // both halves have read before the sums are overwritten
+    // (thread t gathered tile row t & 127 == q * 32 + lane: out_row / valid are this lane's row)
     float ss_out = 0.f;
-    for (int c = 0; c < d; c += 64) {
-      uint32_t r[64];
-      tmem_ld_32x32b_x32(trow + c, *reinterpret_cast<uint32_t(*)[32]>(r));
-      tmem_ld_32x32b_x32(trow + c + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+    for (int c = cb; c < ce; c += 32) {
+      uint32_t rv[32];
+      tmem_ld_32x32b_x32(trow + c, rv);
       tmem_ld_wait();
 #pragma unroll
-      for (int q16 = 0; q16 < 4; ++q16) {
+      for (int q16 = 0; q16 < 2; ++q16) {
         uint32_t packed[8];
 #pragma unroll
         for (int i = 0; i < 16; i += 4) {
           const int k = q16 * 16 + i;
           const float4 bv = lds_f32x4(sb + (c + k) * 4), gv = lds_f32x4(sgn + (c + k) * 4);
-          const float y0 = (__uint_as_float(r[k]) + bv.x) * inv * gv.x;
-          const float y1 = (__uint_as_float(r[k + 1]) + bv.y) * inv * gv.y;
-          const float y2 = (__uint_as_float(r[k + 2]) + bv.z) * inv * gv.z;
-          const float y3 = (__uint_as_float(r[k + 3]) + bv.w) * inv * gv.w;
+          const float y0 = (__uint_as_float(rv[k]) + bv.x) * inv * gv.x;
+          const float y1 = (__uint_as_float(rv[k + 1]) + bv.y) * inv * gv.y;
+          const float y2 = (__uint_as_float(rv[k + 2]) + bv.z) * inv * gv.z;
+          const float y3 = (__uint_as_float(rv[k + 3]) + bv.w) * inv * gv.w;
           packed[i / 2] = pack_bf16x2(y0, y1);
           packed[i / 2 + 1] = pack_bf16x2(y2, y3);
           const float2 q0 = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&packed[i / 2]));
@@ -281,7 +290,10 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
         if (valid) stg256(p.x + static_cast<size_t>(out_row) * d + c + q16 * 16, packed);
       }
     }
-    if (valid) p.ss[out_row] = make_float4(ss_out, 0.f, 0.f, 0.f);
+    sSS[hh * 128 + r] = ss_out;
+    named_bar_sync(1 + q, 64);
+    if (valid && hh == 0) p.ss[out_row] = make_float4(sSS[r], sSS[128 + r], 0.f, 0.f);
+    named_bar_sync(1 + q, 64);
     tc_fence_before();
     __syncthreads();
   }
@@ -311,6 +323,6 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
   }
 }
 
-inline size_t tok_smem_bytes(int d) { return 1024 + d * 128 + 128 * 128 + 2 * d * 4 + 16; }
+inline size_t tok_smem_bytes(int d) { return 1024 + d * 128 + 128 * 128 + 2 * d * 4 + 16 + 2 * 128 * 4; }
 
 }  // namespace sortk
