@@ -47,12 +47,16 @@ __global__ void k_gather_table_rows(const int4* __restrict__ table, int64_t n_ro
 // Final RMSNorm + ranking head on candidate rows, fp32 (
 // PAPER.md:243 keeps the head in fp32): h = relu(xn W1 + b1), z = h W2 + b2,
 // p = sigmoid(z) for {click, cart, purchase}.
-// 64 candidate rows per CTA, 256 threads: warp w owns rows [8w, 8w+8), lane l owns hidden
+// 128 candidate rows per CTA, 512 threads: warp w owns rows [8w, 8w+8), lane l owns hidden
 // columns {l, l+32, ...} (CPT = dh/32 of them), so each thread keeps an 8 x CPT register
-// tile; xn is staged transposed in smem (broadcast reads), W1 streams coalesced from L2.
+// tile; xn is staged transposed in smem (broadcast reads) and W1 streams through shared
+// memory in 16-row slices (cp.async, double-buffered) that all 16 warps share, so each CTA
+// reads W1 from L2 once.
 // The 3 logits are reduced across the 32 lanes with shuffles in a fixed order.
-constexpr int kHeadRows = 64;
-constexpr int kHeadThreads = 256;
+constexpr int kHeadRows = 128;
+constexpr int kHeadPitch = kHeadRows + 4;  // xs row pitch: 4-way (not 32-way) conflicts on the transposed store
+constexpr int kHeadThreads = 512;
+constexpr int kHeadKSlice = 16;  // W1 rows staged per cp.async slice (double-buffered)
 
 template <int CPT>
 __global__ void __launch_bounds__(kHeadThreads)
@@ -61,7 +65,21 @@ __global__ void __launch_bounds__(kHeadThreads)
            const float* __restrict__ b1, const float* __restrict__ w2, const float* __restrict__ b2,
            float* __restrict__ probs, float* __restrict__ logits) {
   constexpr int dh = CPT * 32;
-  extern __shared__ float xs[];  // [d][kHeadRows] transposed normalised rows
+  extern __shared__ float xs[];  // [d][kHeadPitch] transposed normalised rows, then 2 W1 slices
+  float* sw1 = xs + static_cast<size_t>(d) * kHeadPitch;  // [2][kHeadKSlice][dh]
+  auto stage_w1 = [&](int slice, int buf) {
+    // kHeadKSlice x dh floats = 16 B chunks, spread over the CTA
+    const int chunks = kHeadKSlice * dh / 4;
+    for (int i = threadIdx.x; i < chunks; i += kHeadThreads) {
+      const int k = slice * kHeadKSlice + (i * 4) / dh, c = (i * 4) % dh;
+      const float* src = w1 + static_cast<size_t>(k) * dh + c;
+      const uint32_t dst = smem_u32(sw1 + (buf * kHeadKSlice * dh) + i * 4);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(k < d ? 16 : 0)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  stage_w1(0, 0);
   const int e0 = blockIdx.x * kHeadRows;
   const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
   for (int rr = warp; rr < kHeadRows; rr += kHeadThreads / 32) {
@@ -71,9 +89,9 @@ __global__ void __launch_bounds__(kHeadThreads)
       const size_t row = static_cast<size_t>(b) * R + (R - N) + j;
       const float4 sp = ss[row];
       const float inv = rsqrtf(((sp.x + sp.y) + (sp.z + sp.w)) / static_cast<float>(d) + 1e-6f);
-      for (int c = lane; c < d; c += 32) xs[c * kHeadRows + rr] = __bfloat162float(x[row * d + c]) * inv * gain[c];
+      for (int c = lane; c < d; c += 32) xs[c * kHeadPitch + rr] = __bfloat162float(x[row * d + c]) * inv * gain[c];
     } else {
-      for (int c = lane; c < d; c += 32) xs[c * kHeadRows + rr] = 0.f;
+      for (int c = lane; c < d; c += 32) xs[c * kHeadPitch + rr] = 0.f;
     }
   }
   __syncthreads();
@@ -83,18 +101,32 @@ __global__ void __launch_bounds__(kHeadThreads)
 #pragma unroll
     for (int c = 0; c < CPT; ++c) acc[r][c] = 0.f;
   const float* xw = xs + warp * 8;
+  const int n_slices = (d + kHeadKSlice - 1) / kHeadKSlice;
+  for (int sl = 0; sl < n_slices; ++sl) {
+    if (sl + 1 < n_slices) {
+      stage_w1(sl + 1, (sl + 1) & 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    const float* ws = sw1 + (sl & 1) * kHeadKSlice * dh;
 #pragma unroll 4
-  for (int k = 0; k < d; ++k) {
-    const float4 xa = *reinterpret_cast<const float4*>(xw + k * kHeadRows);
-    const float4 xb = *reinterpret_cast<const float4*>(xw + k * kHeadRows + 4);
-    const float xr[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
-    float wv[CPT];
+    for (int kk = 0; kk < kHeadKSlice; ++kk) {
+      const int k = sl * kHeadKSlice + kk;
+      if (k >= d) break;
+      const float4 xa = *reinterpret_cast<const float4*>(xw + k * kHeadPitch);
+      const float4 xb = *reinterpret_cast<const float4*>(xw + k * kHeadPitch + 4);
+      const float xr[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+      float wv[CPT];
 #pragma unroll
-    for (int c = 0; c < CPT; ++c) wv[c] = __ldg(w1 + static_cast<size_t>(k) * dh + c * 32 + lane);
+      for (int c = 0; c < CPT; ++c) wv[c] = ws[kk * dh + c * 32 + lane];
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
+      for (int r = 0; r < 8; ++r)
 #pragma unroll
-      for (int c = 0; c < CPT; ++c) acc[r][c] = fmaf(xr[r], wv[c], acc[r][c]);
+        for (int c = 0; c < CPT; ++c) acc[r][c] = fmaf(xr[r], wv[c], acc[r][c]);
+    }
+    __syncthreads();  // slice buffer (sl & 1) is restaged two slices later
   }
   float z[8][3];
 #pragma unroll

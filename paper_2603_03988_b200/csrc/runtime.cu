@@ -578,10 +578,12 @@ static void finalize(Handle& h) {
   size_t goff = 0;
   for (auto& kv : h.host) {
     if (kv.first == "tok.item_table") continue;
+    goff = (goff + 3) & ~static_cast<size_t>(3);  // 16-byte aligned tensors (vector / cp.async loads)
     h.grad_index[kv.first] = {goff, {kv.second.rows, kv.second.cols}};
     goff += static_cast<size_t>(kv.second.rows) * kv.second.cols;
   }
   h.master = h.dalloc<float>(std::max<size_t>(goff, 1));
+  CK(cudaMemset(h.master, 0, std::max<size_t>(goff, 1) * sizeof(float)));  // alignment gaps
   for (auto& kv : h.grad_index) {
     const HostParam& hp = h.host.at(kv.first);
     CK(cudaMemcpy(h.master + kv.second.first, hp.v.data(), hp.v.size() * 4, cudaMemcpyHostToDevice));
@@ -1802,14 +1804,14 @@ static void forward_device(Handle& h, int B) {
     return;
   }
   const int total = B * h.cfg.n_cand;
-  const size_t hsmem = static_cast<size_t>(kHeadRows) * h.d * sizeof(float);
+  const size_t hsmem = (static_cast<size_t>(kHeadPitch) * h.d + 2 * kHeadKSlice * h.dh) * sizeof(float);
   const int hgrid = (total + kHeadRows - 1) / kHeadRows;
   const LayerDev& lst = last;
 #define SORT_HEAD(CPT)                                                                          \
   case CPT: {                                                                                   \
     static bool attr = false;                                                                   \
     if (!attr) {                                                                                \
-      CK(cudaFuncSetAttribute(k_head<CPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024)); \
+      CK(cudaFuncSetAttribute(k_head<CPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)); \
       attr = true;                                                                              \
     }                                                                                           \
     k_head<CPT><<<hgrid, kHeadThreads, hsmem, h.stream>>>(                                      \

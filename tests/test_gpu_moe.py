@@ -89,12 +89,14 @@ def test_moe_op_vs_oracle(which):
     assert np.max(np.abs(out - (xb + ref))) < MOE_MAX_ABS
 
 
-@pytest.mark.parametrize("which", ["tiny_k2", "base"])
+@pytest.mark.parametrize("which", ["tiny_k2", "base", "base_grouped"])
 def test_moe_model_vs_oracle_forced_routing(which):
     cfg = tiny_moe() if which == "tiny_k2" else base_moe_config(batch=2)
     B = 2
     P = synth.make_params(cfg, seed=23)
     gm = R.SortModel(cfg, P, max_batch=B)
+    if which == "base_grouped":
+        gm.set_option("moe_fused", 0)  # the grouped [gate|up] / down GEMM pair
     om = O.OracleModel(cfg, P)
     batch = synth.make_batch(cfg, B, seed=31)
     probs, logits = gm.forward_logits(batch)
@@ -153,22 +155,18 @@ def test_fused_expert_kernel_matches_grouped_gemms(which):
     [gate|up] / down GEMM pair (h from smem, N = 128 slices); the tensor core's accumulation
     differs in the last fp32 bits between those MMA shapes, so a few bf16 outputs move by an
     ulp (measured: 9 of 2000 rows, <= 1 ulp). Op level: < 1 % of the elements differ, by at most
-    2^-6 of the largest MoE delta; model logits within the bf16 rel-L2 bar."""
+    2^-6 of the largest MoE delta."""
     cfg = tiny_moe(moe_topk=1) if which == "tiny" else base_moe_config(batch=2)
     P = synth.make_params(cfg, seed=51)
     gm = R.SortModel(cfg, P, max_batch=2)
-    batch = synth.make_batch(cfg, 2, seed=52)
-    p1, z1 = gm.forward_logits(batch)
     rows = min(600, 2 * gm.layer_plan(1)["l_q"])
     x = np.random.default_rng(53).normal(size=(rows, cfg.model_dim)).astype(np.float32)
     y1 = gm.moe_forward(1, x)
     gm.set_option("moe_fused", 0)
-    p0, z0 = gm.forward_logits(batch)
     y0 = gm.moe_forward(1, x)
     gm.set_option("moe_fused", 1)
     delta = y0 - bf16(x)
     assert np.max(np.abs(y1 - y0)) <= 2.0 ** -6 * np.max(np.abs(delta))   # a few bf16 ulps
     assert np.mean(y1 != y0) < 0.01                                       # on a few elements
-    # an ulp in one layer can flip a near-tie routing decision in the next, which moves that
-    # token a lot: at model level only the aggregate bar applies
-    assert rel_l2(z1, z0) < LOGIT_REL_L2
+    # (model level: an ulp in one layer can flip a near-tie routing decision in the next, so
+    # the two paths are each checked against the oracle with forced routing instead)
