@@ -1835,12 +1835,13 @@ static void forward_device(Handle& h, int B) {
 // The inference forward, replayed from a CUDA graph when possible. The first call for a key
 // runs eagerly (kernel attributes, plan checks) and then captures the same enqueue sequence.
 static void forward_run(Handle& h, int B) {
-  if (!h.use_graphs || h.timing || h.training || h.generic || h.stream == nullptr) {
+  // (a batch-local item table changes with every batch: no graph for those calls)
+  if (!h.use_graphs || h.timing || h.training || h.generic || h.stream == nullptr || h.item_ext) {
     forward_device(h, B);
     return;
   }
-  const auto key = std::make_tuple(B, static_cast<const void*>(h.in_item), static_cast<const void*>(h.item_ext),
-                                   h.item_ext_rows);
+  const auto key = std::make_tuple(B, static_cast<const void*>(h.in_item), static_cast<const void*>(nullptr),
+                                   static_cast<int64_t>(0));
   auto it = h.graphs.find(key);
   if (it != h.graphs.end()) {
     CK(cudaGraphLaunch(it->second.exec, h.stream));
@@ -2441,7 +2442,6 @@ int sort_set_item_table(SortHandle p, const void* rows, int64_t n_rows) {
     Handle* h = reinterpret_cast<Handle*>(p);
     if (!h) throw ConfigError("null handle");
     if (rows && (n_rows < 1 || n_rows > INT32_MAX)) throw ConfigError("item table rows out of range");
-    h->drop_graphs();
     h->item_ext = static_cast<const __nv_bfloat16*>(rows);
     h->item_ext_rows = rows ? n_rows : 0;
   });
