@@ -1457,12 +1457,14 @@ static void backward_device(Handle& h, int B, const float* dz) {
     // QKNorm + RoPE backward against recomputed raw projections
     float* raw = h.tw[11];
     gemm_rm(h, false, false, M, d, d, xqp, d, w32(h, A + "wq"), d, raw, d);
-    const int qk_rows = 8 * kQkRowsPerWarp;
-    k_qknorm_rope_bwd<<<(M + qk_rows - 1) / qk_rows, 256, d * 4, h.stream>>>(dQ, raw, M, L.Rq, L.pos_q, h.rope, H, dk,
-                                                         w32(h, A + "qk_gain_q"), dQ, grad_ptr(h, A + "qk_gain_q"));
+    // persistent grid (register-held gain partials per warp, one smem reduction per CTA)
+    const int qk_grid_q = std::max(1, std::min((M + 7) / 8, 4 * h.num_sms));
+    k_qknorm_rope_bwd_v<1><<<qk_grid_q, 256, d * 4, h.stream>>>(dQ, raw, M, L.Rq, L.pos_q, h.rope, H, dk,
+                                                              w32(h, A + "qk_gain_q"), dQ, grad_ptr(h, A + "qk_gain_q"));
     gemm_rm(h, false, false, Mkv, d, d, xn, d, w32(h, A + "wk"), d, raw, d);
-    k_qknorm_rope_bwd<<<(Mkv + qk_rows - 1) / qk_rows, 256, d * 4, h.stream>>>(dK, raw, Mkv, L.Rkv, L.pos_kv, h.rope, H, dk,
-                                                           w32(h, A + "qk_gain_k"), dK, grad_ptr(h, A + "qk_gain_k"));
+    const int qk_grid_k = std::max(1, std::min((Mkv + 7) / 8, 4 * h.num_sms));
+    k_qknorm_rope_bwd_v<1><<<qk_grid_k, 256, d * 4, h.stream>>>(dK, raw, Mkv, L.Rkv, L.pos_kv, h.rope, H, dk,
+                                                              w32(h, A + "qk_gain_k"), dK, grad_ptr(h, A + "qk_gain_k"));
     check_launch("qknorm/rope backward");
     gemm_rm(h, true, false, d, d, M, xqp, d, dQ, d, grad_ptr(h, A + "wq"), d);
     gemm_rm(h, true, false, d, d, Mkv, xn, d, dK, d, grad_ptr(h, A + "wk"), d);

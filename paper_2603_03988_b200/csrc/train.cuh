@@ -647,6 +647,99 @@ __global__ void __launch_bounds__(256) k_qknorm_rope_bwd(const float* drot, cons
   for (int c = threadIdx.x; c < d; c += blockDim.x) atomicAdd(&dgain[c], sg[c]);
 }
 
+// Vectorised form of k_qknorm_rope_bwd (same math): one warp per row, lane owns 8 contiguous
+// elements (4 rotation pairs) of chunk c = lane + 32 i, so a head spans dk / 8 aligned lanes and
+// both per-head reductions are 1-3 shuffle steps; 32-byte loads and stores. Gain-gradient
+// partials stay in registers across the warp's rows (grid-stride), then one shared-memory
+// reduction per CTA. d = H * dk <= 256 * kV.
+template <int kV>
+__global__ void __launch_bounds__(256) k_qknorm_rope_bwd_v(const float* drot, const float* __restrict__ raw,
+                                                           int rows, int R, const int32_t* __restrict__ pos,
+                                                           const float2* __restrict__ rope_tab, int H, int dk,
+                                                           const float* __restrict__ gain, float* draw,
+                                                           float* __restrict__ dgain) {
+  extern __shared__ float sg[];  // [H * dk]
+  const int d = H * dk, d8 = d >> 3;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) sg[c] = 0.f;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int e = (lane * 8) & (dk - 1);  // offset inside the head (same for every chunk: 256 % dk == 0)
+  float g[kV][8], gacc[kV][8];
+#pragma unroll
+  for (int i = 0; i < kV; ++i) {
+    const int c = lane + 32 * i;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      g[i][k] = c < d8 ? gain[c * 8 + k] : 0.f;
+      gacc[i][k] = 0.f;
+    }
+  }
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  for (int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < rows; w += warps) {
+    float cs[8];  // (cos, sin) of the lane's 4 pairs
+    {
+      const float4* t = reinterpret_cast<const float4*>(rope_tab + static_cast<size_t>(pos[w % R]) * (dk / 2) + e / 2);
+      const float4 a = t[0], b = t[1];
+      cs[0] = a.x; cs[1] = a.y; cs[2] = a.z; cs[3] = a.w;
+      cs[4] = b.x; cs[5] = b.y; cs[6] = b.z; cs[7] = b.w;
+    }
+#pragma unroll
+    for (int i = 0; i < kV; ++i) {
+      const int c = lane + 32 * i;
+      const bool act = c < d8;
+      float dq[8], x[8];
+      if (act) {
+        const float4* gp = reinterpret_cast<const float4*>(drot + static_cast<size_t>(w) * d + c * 8);
+        const float4* xp = reinterpret_cast<const float4*>(raw + static_cast<size_t>(w) * d + c * 8);
+        const float4 g0 = gp[0], g1 = gp[1], x0 = xp[0], x1 = xp[1];
+        const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+        x[0] = x0.x; x[1] = x0.y; x[2] = x0.z; x[3] = x0.w;
+        x[4] = x1.x; x[5] = x1.y; x[6] = x1.z; x[7] = x1.w;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {  // inverse rotation of pair q (rope.hpp:13-40, -angle)
+          const float cc = cs[2 * q], sn = cs[2 * q + 1];
+          dq[2 * q] = cc * gg[2 * q] + sn * gg[2 * q + 1];
+          dq[2 * q + 1] = -sn * gg[2 * q] + cc * gg[2 * q + 1];
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) dq[k] = x[k] = 0.f;
+      }
+      float ss = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) ss = fmaf(x[k], x[k], ss);
+      for (int o = dk / 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      const float inv = rsqrtf(ss / static_cast<float>(dk) + 1e-6f);
+      float pr = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) pr = fmaf(dq[k] * g[i][k], x[k] * inv, pr);
+      for (int o = dk / 16; o; o >>= 1) pr += __shfl_xor_sync(0xffffffffu, pr, o);
+      const float proj = pr / static_cast<float>(dk);
+      if (act) {
+        float out[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float xh = x[k] * inv;
+          gacc[i][k] = fmaf(dq[k], xh, gacc[i][k]);
+          out[k] = (dq[k] * g[i][k] - proj * xh) * inv;
+        }
+        float4* op = reinterpret_cast<float4*>(draw + static_cast<size_t>(w) * d + c * 8);
+        op[0] = make_float4(out[0], out[1], out[2], out[3]);
+        op[1] = make_float4(out[4], out[5], out[6], out[7]);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kV; ++i) {
+    const int c = lane + 32 * i;
+    if (c < d8)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) atomicAdd(&sg[c * 8 + k], gacc[i][k]);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < d; c += blockDim.x) atomicAdd(&dgain[c], sg[c]);
+}
+
 // dst[b*Rdst + map[r]] (+)= src[b*Rsrc + r] over B*Rsrc rows (unique destinations).
 __global__ void k_scatter_add_rows(const float* __restrict__ src, const int32_t* __restrict__ map, int B, int Rsrc,
                                    int Rdst, int d, float* __restrict__ dst) {
