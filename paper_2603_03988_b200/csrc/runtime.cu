@@ -131,6 +131,7 @@ struct Handle {
   };
   std::vector<TrainLayer> tl;
   float *tw[16] = {nullptr};  // backward workspace
+  __nv_bfloat16* dO16 = nullptr;  // bf16 copy of dL/d(attention output) for the tensor-core backward
   float* dtokens = nullptr;
   float* dz_dev = nullptr;                 // dL/dlogits of the current step
   int32_t* t_rows = nullptr;               // tokenizer backward: token row of each group row
@@ -1280,6 +1281,7 @@ static void ensure_train_buffers(Handle& h, int B) {
   // workspace: 0 dX, 1 dX next, 2 xn, 3 xq, 4 H / dxq, 5 dH, 6 dO, 7 dgraw, 8 dQ, 9 dK, 10 dV,
   // 11 raw, 12 GU / dGU, 13 z / dz, 14 inv (rows), 15 D / head scratch
   for (int i = 0; i < 12; ++i) h.tw[i] = h.dalloc<float>(rows * d);
+  h.dO16 = h.dalloc<__nv_bfloat16>(rows * d);
   h.tw[12] = h.dalloc<float>(rows * 2 * m * 2);  // GU and dGU
   h.tw[13] = h.dalloc<float>(rows * m);
   h.tw[14] = h.dalloc<float>(rows * 2);
@@ -1365,7 +1367,9 @@ static void backward_device(Handle& h, int B, const float* dz) {
     k_gate_fwd<<<ew_grid(nq), 256, 0, h.stream>>>(T.g, T.o_pre, nq, Hm);
     gemm_rm(h, true, false, d, d, M, Hm, d, dX, d, grad_ptr(h, A + "wo"), d);
     gemm_rm(h, false, true, M, d, d, dX, d, w32(h, A + "wo"), d, dH, d);
-    k_gate_bwd<<<ew_grid(nq), 256, 0, h.stream>>>(dH, T.g, T.o_pre, nq, dO, dgraw);
+    float* Dd = h.tw[15];
+    k_gate_bwd_rows<<<warp_rows_grid(M), 256, 0, h.stream>>>(dH, T.g, T.o_pre, M, L.Rq, H, dk, dO, h.dO16, dgraw,
+                                                             Dd);
     float* xn = h.tw[2];
     float* xq = h.tw[3];
     float* inv_a = h.tw[14] + static_cast<size_t>(h.train_B) * h.L0;
@@ -1381,8 +1385,6 @@ static void backward_device(Handle& h, int B, const float* dz) {
     float* dxq = h.tw[4];  // H no longer needed
     gemm_rm(h, false, true, M, d, d, dgraw, d, w32(h, A + "wg"), d, dxq, d);
     // attention core
-    float* Dd = h.tw[15];
-    k_attn_rowdot<<<(M * H + 7) / 8, 256, 0, h.stream>>>(dO, T.o_pre, B, L.Rq, H, dk, Dd);
     AttnBwdArgs ab;
     ab.q = T.q;
     ab.k = T.k;
@@ -1413,7 +1415,7 @@ static void backward_device(Handle& h, int B, const float* dz) {
       am.q = T.q;
       am.k = T.k;
       am.v = T.v;
-      am.dO = dO;
+      am.dO16 = h.dO16;
       am.lse = T.lse;
       am.D = Dd;
       am.rowmeta = L.rowmeta;

@@ -185,6 +185,51 @@ __global__ void k_gate_bwd(const float* __restrict__ dH, const __nv_bfloat16* __
   }
 }
 
+// Gate backward and the softmax row term in one pass (attention.cpp:124-131, 169-172): per
+// row, dO = dH * g (fp32 and a bf16 copy for the tensor-core backward), d(g_raw) =
+// dH * o * g (1 - g), and D[bh, r] = <dO_head, O_head>. Warp per row, lane owns 8 contiguous
+// columns, a head = dk / 8 lanes (shuffle reduction). d <= 256.
+__global__ void __launch_bounds__(256) k_gate_bwd_rows(const float* __restrict__ dH, const __nv_bfloat16* __restrict__ G,
+                                                       const __nv_bfloat16* __restrict__ O, int rows, int Rq, int H,
+                                                       int dk, float* __restrict__ dO, __nv_bfloat16* __restrict__ dO16,
+                                                       float* __restrict__ dgraw, float* __restrict__ D) {
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (w >= rows) return;
+  const int d = H * dk, c0 = lane * 8;
+  const bool act = c0 < d;
+  float dot = 0.f;
+  if (act) {
+    const size_t o = static_cast<size_t>(w) * d + c0;
+    const float4 h0 = reinterpret_cast<const float4*>(dH + o)[0], h1 = reinterpret_cast<const float4*>(dH + o)[1];
+    const int4 gv = *reinterpret_cast<const int4*>(G + o), ov = *reinterpret_cast<const int4*>(O + o);
+    const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gv);
+    const __nv_bfloat162* o2 = reinterpret_cast<const __nv_bfloat162*>(&ov);
+    const float hh[8] = {h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w};
+    float dov[8], dgr[8];
+    uint32_t pk[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float2 g = __bfloat1622float2(g2[q]), ob = __bfloat1622float2(o2[q]);
+      dov[2 * q] = hh[2 * q] * g.x;
+      dov[2 * q + 1] = hh[2 * q + 1] * g.y;
+      dgr[2 * q] = hh[2 * q] * ob.x * g.x * (1.f - g.x);
+      dgr[2 * q + 1] = hh[2 * q + 1] * ob.y * g.y * (1.f - g.y);
+      dot = fmaf(dov[2 * q], ob.x, fmaf(dov[2 * q + 1], ob.y, dot));
+      pk[q] = pack_bf16x2(dov[2 * q], dov[2 * q + 1]);
+    }
+    reinterpret_cast<float4*>(dO + o)[0] = make_float4(dov[0], dov[1], dov[2], dov[3]);
+    reinterpret_cast<float4*>(dO + o)[1] = make_float4(dov[4], dov[5], dov[6], dov[7]);
+    reinterpret_cast<float4*>(dgraw + o)[0] = make_float4(dgr[0], dgr[1], dgr[2], dgr[3]);
+    reinterpret_cast<float4*>(dgraw + o)[1] = make_float4(dgr[4], dgr[5], dgr[6], dgr[7]);
+    *reinterpret_cast<int4*>(dO16 + o) = make_int4(pk[0], pk[1], pk[2], pk[3]);
+  }
+  for (int off = dk / 16; off; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
+  if (act && (c0 & (dk - 1)) == 0) {
+    const int h = c0 / dk, b = w / Rq, r = w - b * Rq;
+    D[(static_cast<size_t>(b) * H + h) * Rq + r] = dot;
+  }
+}
+
 // D[bh, r] = sum_j dO[b, r, h*dk + j] * O[b, r, h*dk + j]  (softmax backward row term,
 // attention.cpp:169-172). One warp per (row, head-group of 32 columns).
 __global__ void k_attn_rowdot(const float* __restrict__ dO, const __nv_bfloat16* __restrict__ O, int B, int Rq,
@@ -392,7 +437,7 @@ __global__ void __launch_bounds__(32) k_attn_bwd_dkv(const AttnBwdArgs a) {
 // memory and fp32 atomics (several kv blocks contribute to a q block).
 struct AttnBwdMmaArgs {
   const __nv_bfloat16 *q, *k, *v;  // [BH, Rq, DK], [BH, Rkv, DK], [BH, Rkv, DK]
-  const float* dO;                 // [B*Rq, H*DK]
+  const __nv_bfloat16* dO16;       // [B*Rq, H*DK] bf16
   const float* lse;                // [BH, Rq]
   const float* D;                  // [BH, Rq]
   const int4* rowmeta;             // [Rq]
@@ -422,20 +467,52 @@ __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], 
 }
 
 template <int DK>
-__global__ void __launch_bounds__(128) k_attn_bwd_mma(const AttnBwdMmaArgs a) {
+__global__ void __launch_bounds__(128, 4) k_attn_bwd_mma(const AttnBwdMmaArgs a) {
   constexpr int LD = DK + 8;  // padded bf16 row (conflict-free ldmatrix)
   constexpr int LDS = 64 + 8;
   constexpr int NT = DK / 8;  // n-tiles of the dK / dV / dQ accumulators
   constexpr int KS = DK / 16; // k-steps of S^T and dP^T
-  __shared__ __align__(16) __nv_bfloat16 sK[64 * LD], sV[64 * LD], sQ[64 * LD], sO[64 * LD];
+  // Q / dO (bf16) / lse / D / row metadata of a q block, double-buffered: the next q block's
+  // tiles stream in (cp.async) while this one is computed
+  constexpr int NBUF = DK <= 32 ? 2 : 1;  // dk = 64: single-buffered (48 KB static smem)
+  __shared__ __align__(16) __nv_bfloat16 sK[64 * LD], sV[64 * LD], sQb[NBUF][64 * LD], sOb[NBUF][64 * LD];
   __shared__ __align__(16) __nv_bfloat16 sS[64 * LDS];  // dS^T [kv][q]
-  __shared__ float sL[64], sD[64];
-  __shared__ int4 sM[64];
+  __shared__ __align__(16) float sLb[NBUF][64], sDb[NBUF][64];
+  __shared__ __align__(16) int4 sMb[NBUF][64];
   const int kvb = blockIdx.x, bh = blockIdx.y;
   const int b = bh / a.H, h = bh - b * a.H;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t4 = lane & 3;
   const int c0 = kvb * 64;
+  auto cp16 = [](void* dst, const void* src, bool ok) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(ok ? 16 : 0)
+                 : "memory");
+  };
+  auto cp4 = [](void* dst, const void* src, bool ok) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(ok ? 4 : 0)
+                 : "memory");
+  };
+  const int it0 = a.qb_off[kvb], it1 = a.qb_off[kvb + 1];
+  auto stage = [&](int it, int buf) {
+    const int r0 = a.qb_list[it] * 64;
+    for (int i = tid; i < 64 * (DK / 8); i += 128) {
+      const int r = i / (DK / 8), cc = i % (DK / 8);
+      const bool ok = r0 + r < a.Rq;
+      const int rr = ok ? r0 + r : 0;
+      cp16(sQb[buf] + r * LD + cc * 8, a.q + (static_cast<size_t>(bh) * a.Rq + rr) * DK + cc * 8, ok);
+      cp16(sOb[buf] + r * LD + cc * 8, a.dO16 + (static_cast<size_t>(b) * a.Rq + rr) * a.H * DK + h * DK + cc * 8, ok);
+    }
+    for (int i = tid; i < 64; i += 128) {
+      const bool ok = r0 + i < a.Rq;
+      const size_t li = static_cast<size_t>(bh) * a.Rq + (ok ? r0 + i : 0);
+      cp4(&sLb[buf][i], a.lse + li, ok);
+      cp4(&sDb[buf][i], a.D + li, ok);
+      if (ok) cp16(&sMb[buf][i], a.rowmeta + r0 + i, true);
+      else sMb[buf][i] = make_int4(0, -1, -1, 0);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (it0 < it1) stage(it0, 0);
   for (int i = tid; i < 64 * (DK / 8); i += 128) {  // K, V rows of the block (zero past Rkv)
     const int r = i / (DK / 8), cc = i % (DK / 8);
     int4 kv = make_int4(0, 0, 0, 0), vv = kv;
@@ -451,34 +528,28 @@ __global__ void __launch_bounds__(128) k_attn_bwd_mma(const AttnBwdMmaArgs a) {
   for (int n = 0; n < NT; ++n)
 #pragma unroll
     for (int e = 0; e < 4; ++e) dk[n][e] = dv[n][e] = 0.f;
-  const uint32_t sKa = smem_u32(sK), sVa = smem_u32(sV), sQa = smem_u32(sQ), sOa = smem_u32(sO), sSa = smem_u32(sS);
+  const uint32_t sKa = smem_u32(sK), sVa = smem_u32(sV), sSa = smem_u32(sS);
   const int kv_lo = c0 + warp * 16 + g;  // this thread's two kv rows: kv_lo, kv_lo + 8
-  for (int it = a.qb_off[kvb]; it < a.qb_off[kvb + 1]; ++it) {
+  for (int it = it0; it < it1; ++it) {
+    const int buf = (it - it0) % NBUF;
     const int r0 = a.qb_list[it] * 64;
-    __syncthreads();  // previous iteration done with sQ / sO / sS
-    for (int i = tid; i < 64 * (DK / 8); i += 128) {
-      const int r = i / (DK / 8), cc = i % (DK / 8);
-      int4 qv = make_int4(0, 0, 0, 0);
-      uint32_t ov[4] = {0u, 0u, 0u, 0u};
-      if (r0 + r < a.Rq) {
-        qv = reinterpret_cast<const int4*>(a.q + (static_cast<size_t>(bh) * a.Rq + r0 + r) * DK)[cc];
-        const float* gp = a.dO + (static_cast<size_t>(b) * a.Rq + r0 + r) * a.H * DK + h * DK + cc * 8;
-        const float4 x0 = reinterpret_cast<const float4*>(gp)[0], x1 = reinterpret_cast<const float4*>(gp)[1];
-        ov[0] = pack_bf16x2(x0.x, x0.y);
-        ov[1] = pack_bf16x2(x0.z, x0.w);
-        ov[2] = pack_bf16x2(x1.x, x1.y);
-        ov[3] = pack_bf16x2(x1.z, x1.w);
+    __syncthreads();  // previous iteration done with sS and with the other buffer
+    if constexpr (NBUF == 2) {
+      if (it + 1 < it1) {
+        stage(it + 1, buf ^ 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
       }
-      *reinterpret_cast<int4*>(sQ + r * LD + cc * 8) = qv;
-      *reinterpret_cast<int4*>(sO + r * LD + cc * 8) = make_int4(ov[0], ov[1], ov[2], ov[3]);
-    }
-    for (int i = tid; i < 64; i += 128) {
-      const bool ok = r0 + i < a.Rq;
-      sL[i] = ok ? a.lse[static_cast<size_t>(bh) * a.Rq + r0 + i] : 0.f;
-      sD[i] = ok ? a.D[static_cast<size_t>(bh) * a.Rq + r0 + i] : 0.f;
-      sM[i] = ok ? a.rowmeta[r0 + i] : make_int4(0, -1, -1, 0);
+    } else {
+      if (it > it0) stage(it, 0);
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
+    const uint32_t sQa = smem_u32(sQb[buf]), sOa = smem_u32(sOb[buf]);
+    const float* sL = sLb[buf];
+    const float* sD = sDb[buf];
+    const int4* sM = sMb[buf];
     // S^T and dP^T: [16 kv (this warp) x 64 q]
     float st[8][4], dp[8][4];
 #pragma unroll
