@@ -585,7 +585,7 @@ __global__ void __launch_bounds__(128, 4) k_attn_bwd_mma(const AttnBwdMmaArgs a)
         const int kv = kv_lo + ((e >> 1) << 3);
         const int4 m = sM[q];
         const bool vis = kv < a.Rkv && ((kv >= m.x && kv <= m.y) || kv == m.z);
-        p[e] = vis ? exp2f(st[n][e] * a.scale_log2 - sL[q]) : 0.f;
+        p[e] = vis ? ex2_approx(st[n][e] * a.scale_log2 - sL[q]) : 0.f;  // argument <= 0 (P <= 1)
         ds[e] = p[e] * (dp[n][e] - sD[q]);
       }
       const int s = n >> 1, hi = n & 1;
@@ -636,11 +636,14 @@ __global__ void __launch_bounds__(128, 4) k_attn_bwd_mma(const AttnBwdMmaArgs a)
 #pragma unroll
     for (int n = 0; n < NT; ++n)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int q = r0 + warp * 16 + g + ((e >> 1) << 3);
-        if (q < a.Rq)
-          atomicAdd(a.dq + (static_cast<size_t>(b) * a.Rq + q) * a.H * DK + h * DK + n * 8 + 2 * t4 + (e & 1),
-                    dq[n][e] * a.scale);
+      for (int e2 = 0; e2 < 2; ++e2) {  // two adjacent columns per vector reduction
+        const int q = r0 + warp * 16 + g + (e2 << 3);
+        if (q < a.Rq) {
+          float* dst = a.dq + (static_cast<size_t>(b) * a.Rq + q) * a.H * DK + h * DK + n * 8 + 2 * t4;
+          asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(dst), "f"(dq[n][2 * e2] * a.scale),
+                       "f"(dq[n][2 * e2 + 1] * a.scale)
+                       : "memory");
+        }
       }
   }
 #pragma unroll
