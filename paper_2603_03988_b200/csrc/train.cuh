@@ -166,26 +166,15 @@ __global__ void k_swiglu_bwd(const float* __restrict__ dz, const float* __restri
   }
 }
 
-// Gate (attention.cpp:124-127, backward :144-152): H = G * O; given dH: dO = dH * G,
-// dgraw = dH * O * G (1 - G). G, O bf16 [M, d].
+// Gate (attention.cpp:124-127): H = G * O (recomputed for the Wo weight gradient). G, O bf16 [M, d].
 __global__ void k_gate_fwd(const __nv_bfloat16* __restrict__ G, const __nv_bfloat16* __restrict__ O, size_t n,
                            float* __restrict__ H) {
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x)
     H[i] = __bfloat162float(G[i]) * __bfloat162float(O[i]);
 }
-__global__ void k_gate_bwd(const float* __restrict__ dH, const __nv_bfloat16* __restrict__ G,
-                           const __nv_bfloat16* __restrict__ O, size_t n, float* __restrict__ dO,
-                           float* __restrict__ dgraw) {
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const float g = __bfloat162float(G[i]), o = __bfloat162float(O[i]);
-    dO[i] = dH[i] * g;
-    dgraw[i] = dH[i] * o * g * (1.f - g);
-  }
-}
 
-// Gate backward and the softmax row term in one pass (attention.cpp:124-131, 169-172): per
+// Gate backward and the softmax row term in one pass (attention.cpp:124-131, 144-152, 169-172): per
 // row, dO = dH * g (fp32 and a bf16 copy for the tensor-core backward), d(g_raw) =
 // dH * o * g (1 - g), and D[bh, r] = <dO_head, O_head>. Warp per row, lane owns 8 contiguous
 // columns, a head = dk / 8 lanes (shuffle reduction). d <= 256.
@@ -227,24 +216,6 @@ __global__ void __launch_bounds__(256) k_gate_bwd_rows(const float* __restrict__
   if (act && (c0 & (dk - 1)) == 0) {
     const int h = c0 / dk, b = w / Rq, r = w - b * Rq;
     D[(static_cast<size_t>(b) * H + h) * Rq + r] = dot;
-  }
-}
-
-// D[bh, r] = sum_j dO[b, r, h*dk + j] * O[b, r, h*dk + j]  (softmax backward row term,
-// attention.cpp:169-172). One warp per (row, head-group of 32 columns).
-__global__ void k_attn_rowdot(const float* __restrict__ dO, const __nv_bfloat16* __restrict__ O, int B, int Rq,
-                              int H, int dk, float* __restrict__ D) {
-  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (w >= B * Rq * H) return;
-  const int row = w / H, h = w - row * H;  // row = b * Rq + r
-  float s = 0.f;
-  for (int j = lane; j < dk; j += 32)
-    s = fmaf(dO[static_cast<size_t>(row) * H * dk + h * dk + j],
-             __bfloat162float(O[static_cast<size_t>(row) * H * dk + h * dk + j]), s);
-  s = warp_sum(s);
-  if (lane == 0) {
-    const int b = row / Rq, r = row - b * Rq;
-    D[(static_cast<size_t>(b) * H + h) * Rq + r] = s;
   }
 }
 
@@ -659,69 +630,10 @@ __global__ void __launch_bounds__(128, 4) k_attn_bwd_mma(const AttnBwdMmaArgs a)
     }
 }
 
-// QKNorm + RoPE backward per (row, head) (attention.cpp:177-183): dx_rot -> inverse RoPE
-// at the row's position (rope.hpp:13-40, angle -> -angle) -> per-head RMSNorm backward
-// against the raw projection `raw` with gain g[h]. Each warp takes kQkRowsPerWarp rows,
-// lanes over rotation pairs; the gain gradient is reduced in shared memory per CTA.
-// drot and draw may alias (in place): each lane reads its elements of a head before writing them.
-constexpr int kQkRowsPerWarp = 8;
-__global__ void __launch_bounds__(256) k_qknorm_rope_bwd(const float* drot, const float* __restrict__ raw, int rows,
-                                                         int R, const int32_t* __restrict__ pos,
-                                                         const float2* __restrict__ rope_tab, int H, int dk,
-                                                         const float* __restrict__ gain, float* draw,
-                                                         float* __restrict__ dgain) {
-  extern __shared__ float sg[];  // [H * dk]
-  const int d = H * dk;
-  for (int c = threadIdx.x; c < d; c += blockDim.x) sg[c] = 0.f;
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int j = lane;  // rotation pair (dk/2 <= 32)
-  const bool act = j < dk / 2;
-  const int r0 = (blockIdx.x * (blockDim.x >> 5) + warp) * kQkRowsPerWarp;
-  constexpr int kMaxH = 16;  // register-held gain partials (2 per head)
-  float gq[kMaxH][2];
-#pragma unroll
-  for (int i = 0; i < kMaxH; ++i) gq[i][0] = gq[i][1] = 0.f;
-  for (int w = r0; w < r0 + kQkRowsPerWarp && w < rows; ++w) {
-    const int p = pos[w % R];
-    const float2 cs = act ? rope_tab[static_cast<size_t>(p) * (dk / 2) + j] : make_float2(1.f, 0.f);
-#pragma unroll
-    for (int h = 0; h < kMaxH; ++h) {
-      if (h >= H) break;
-      float dq[2] = {0.f, 0.f}, xr[2] = {0.f, 0.f};
-      const size_t o = static_cast<size_t>(w) * d + h * dk + 2 * j;
-      if (act) {
-        const float2 g = *reinterpret_cast<const float2*>(drot + o);
-        dq[0] = cs.x * g.x + cs.y * g.y;  // inverse rotation of the pair (2j, 2j+1)
-        dq[1] = -cs.y * g.x + cs.x * g.y;
-        const float2 x = *reinterpret_cast<const float2*>(raw + o);
-        xr[0] = x.x;
-        xr[1] = x.y;
-      }
-      const float ss = warp_sum(xr[0] * xr[0] + xr[1] * xr[1]);
-      const float inv = rsqrtf(ss / static_cast<float>(dk) + 1e-6f);
-      const float g0 = act ? gain[h * dk + 2 * j] : 0.f, g1 = act ? gain[h * dk + 2 * j + 1] : 0.f;
-      const float proj = warp_sum(dq[0] * g0 * xr[0] * inv + dq[1] * g1 * xr[1] * inv) / static_cast<float>(dk);
-      if (act) {
-        const float xh0 = xr[0] * inv, xh1 = xr[1] * inv;
-        gq[h][0] = fmaf(dq[0], xh0, gq[h][0]);
-        gq[h][1] = fmaf(dq[1], xh1, gq[h][1]);
-        *reinterpret_cast<float2*>(draw + o) =
-            make_float2((dq[0] * g0 - proj * xh0) * inv, (dq[1] * g1 - proj * xh1) * inv);
-      }
-    }
-  }
-#pragma unroll
-  for (int h = 0; h < kMaxH; ++h)
-    if (h < H && act) {
-      atomicAdd(&sg[h * dk + 2 * j], gq[h][0]);
-      atomicAdd(&sg[h * dk + 2 * j + 1], gq[h][1]);
-    }
-  __syncthreads();
-  for (int c = threadIdx.x; c < d; c += blockDim.x) atomicAdd(&dgain[c], sg[c]);
-}
-
-// Vectorised form of k_qknorm_rope_bwd (same math): one warp per row, lane owns 8 contiguous
+// QKNorm + RoPE backward (attention.cpp:177-183): dx_rot -> inverse RoPE at the row's position
+// (rope.hpp:13-40, angle -> -angle) -> per-head RMSNorm backward against the raw projection
+// `raw` with gain g[h]; drot and draw may alias (each lane reads its elements before writing
+// them). One warp per row, lane owns 8 contiguous
 // elements (4 rotation pairs) of chunk c = lane + 32 i, so a head spans dk / 8 aligned lanes and
 // both per-head reductions are 1-3 shuffle steps; 32-byte loads and stores. Gain-gradient
 // partials stay in registers across the warp's rows (grid-stride), then one shared-memory
