@@ -620,12 +620,12 @@ __global__ void __launch_bounds__(128, 4) k_attn_bwd_mma(const AttnBwdMmaArgs a)
 #pragma unroll
   for (int n = 0; n < NT; ++n)
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int kv = kv_lo + ((e >> 1) << 3);
+    for (int e2 = 0; e2 < 2; ++e2) {  // two adjacent columns per store
+      const int kv = kv_lo + (e2 << 3);
       if (kv < a.Rkv) {
-        const size_t o = (static_cast<size_t>(b) * a.Rkv + kv) * a.H * DK + h * DK + n * 8 + 2 * t4 + (e & 1);
-        a.dk[o] = dk[n][e] * a.scale;
-        a.dv[o] = dv[n][e];
+        const size_t o = (static_cast<size_t>(b) * a.Rkv + kv) * a.H * DK + h * DK + n * 8 + 2 * t4;
+        *reinterpret_cast<float2*>(a.dk + o) = make_float2(dk[n][2 * e2] * a.scale, dk[n][2 * e2 + 1] * a.scale);
+        *reinterpret_cast<float2*>(a.dv + o) = make_float2(dv[n][2 * e2], dv[n][2 * e2 + 1]);
       }
     }
 }
