@@ -8,6 +8,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -629,6 +630,25 @@ static void finalize(Handle& h) {
   h.finalized = true;
 }
 
+// cudaFuncSetAttribute is per device: the largest dynamic shared memory set so far is
+// remembered per (device, kernel), so handles on several GPUs in one process all get it.
+static void ensure_smem(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& cur = done[{dev, fn}];
+  if (bytes > cur) {
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+    cur = bytes;
+  }
+}
+template <class F>
+static void ensure_smem(F* fn, size_t bytes) {
+  ensure_smem(reinterpret_cast<const void*>(fn), bytes);
+}
+
 // ------------------------------------------------------------------ launches
 static void check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
@@ -639,16 +659,11 @@ template <class Epi>
 static void launch_gemm(Handle& h, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K,
                         int BN, const Epi& epi, const CUtensorMap* side_stats = nullptr,
                         const CUtensorMap* side_rope = nullptr) {
-  static uint32_t attr_bytes = 0;
   const GemmPlan gp = gemm_plan(K, BN, side_bytes(Epi::kSide, Epi::kRopeFloats));
   if (N % BN || gp.a_stages < 2) throw RuntimeFailure("gemm: unsupported tile plan");
   if (((Epi::kSide & 1) && !side_stats) || ((Epi::kSide & 2) && !side_rope))
     throw RuntimeFailure("gemm: epilogue side data missing");
-  if (gp.smem_bytes > attr_bytes) {
-    CK(cudaFuncSetAttribute(k_gemm_bf16<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(gp.smem_bytes)));
-    attr_bytes = gp.smem_bytes;
-  }
+  ensure_smem(k_gemm_bf16<Epi>, gp.smem_bytes);
   const int num_m = (M + kGemmBM - 1) / kGemmBM;
   const int grid = gemm_grid(num_m, N / BN, h.num_sms);
   k_gemm_bf16<Epi><<<grid, kGemmThreads, gp.smem_bytes, h.stream>>>(
@@ -663,14 +678,9 @@ template <class Epi>
 static void launch_gemm_grouped(Handle& h, const CUtensorMap& A, const CUtensorMap& B, int N, int K, int BN,
                                 const Epi& epi) {
   static_assert(is_grouped<Epi>::value, "grouped epilogue expected");
-  static uint32_t attr_bytes = 0;
   const GemmPlan gp = gemm_plan(K, BN, 0, 1, 2);
   if (N % BN || gp.a_stages < 2) throw RuntimeFailure("grouped gemm: unsupported tile plan");
-  if (gp.smem_bytes > attr_bytes) {
-    CK(cudaFuncSetAttribute(k_gemm_bf16<Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(gp.smem_bytes)));
-    attr_bytes = gp.smem_bytes;
-  }
+  ensure_smem(k_gemm_bf16<Epi>, gp.smem_bytes);
   const int grid = gemm_grid(h.moe_tiles_max, N / BN, h.num_sms);
   k_gemm_bf16<Epi><<<grid, kGemmThreads, gp.smem_bytes, h.stream>>>(A, B, A, A, h.moe_pmax, N, K, BN,
                                                                       gp.a_stages, epi);
@@ -683,14 +693,9 @@ static void launch_gemm_grouped(Handle& h, const CUtensorMap& A, const CUtensorM
 template <class Epi>
 static void launch_gemm_pair(Handle& h, const CUtensorMap& A, const CUtensorMap& B, int M, int N, int K, int BN,
                              const Epi& epi, const CUtensorMap* side_stats, const CUtensorMap* side_rope) {
-  static uint32_t attr_bytes = 0;
   const GemmPlan gp = gemm_plan(K, BN, side_bytes(Epi::kSide, Epi::kRopeFloats), 2);
   if (N % BN || gp.a_stages < 2) throw RuntimeFailure("gemm: unsupported tile plan");
-  if (gp.smem_bytes > attr_bytes) {
-    CK(cudaFuncSetAttribute(k_gemm_bf16<Epi, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(gp.smem_bytes)));
-    attr_bytes = gp.smem_bytes;
-  }
+  ensure_smem(k_gemm_bf16<Epi, true>, gp.smem_bytes);
   const int num_m2 = (M + 2 * kGemmBM - 1) / (2 * kGemmBM);
   const int units = gemm_grid(num_m2, N / BN, h.num_sms / 2);
   cudaLaunchConfig_t cfg = {};
@@ -740,13 +745,8 @@ static void launch_attention_dk(Handle& h, const LayerDev& L, const LayerPlan& l
   const int tile_ints = 2 * lp.n_qtiles + 2 + 2 * n_codes;
   if constexpr (kFixed) {
     if (h.attn_sub) {  // fixed reference: 64-column subtiles, O accumulated in TMEM
-      static size_t attr_f = 0;
       const size_t smem_f = AttnFLayout<DK>::bytes(tile_ints);
-      if (smem_f > attr_f) {
-        CK(cudaFuncSetAttribute(k_attention_f<DK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(smem_f)));
-        attr_f = smem_f;
-      }
+      ensure_smem(k_attention_f<DK>, smem_f);
       const int grid_f = std::min(n_items, 2 * h.num_sms);
       k_attention_f<DK><<<grid_f, kAttnThreads, smem_f, h.stream>>>(L.tmQ, L.tmK64, L.tmV64, a);
       check_launch("attention (subtiles)");
@@ -754,13 +754,8 @@ static void launch_attention_dk(Handle& h, const LayerDev& L, const LayerPlan& l
       return;
     }
   }
-  static size_t attr_bytes = 0;
   const size_t smem = AttnSmem<DK>::bytes(tile_ints);
-  if (smem > attr_bytes) {
-    CK(cudaFuncSetAttribute(k_attention<DK, kFixed>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(smem)));
-    attr_bytes = smem;
-  }
+  ensure_smem(k_attention<DK, kFixed>, smem);
   const int grid = std::min(n_items, AttnTmem<DK>::kCtasPerSm * h.num_sms);
   k_attention<DK, kFixed><<<grid, kAttnThreads, smem, h.stream>>>(L.tmQ, L.tmK, L.tmV, a);
   check_launch("attention");
@@ -822,12 +817,7 @@ static void launch_qkvg(Handle& h, const LayerDev& L, const CUtensorMap& A, cons
 
 template <int D, bool kPair>
 static void launch_tail_dp(Handle& h, const LayerDev& L, float4* SSq, int M) {
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(k_block_tail<D, kPair>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(TailSmem<D>::bytes)));
-    attr = true;
-  }
+  ensure_smem(k_block_tail<D, kPair>, TailSmem<D>::bytes);
   TailArgs ta;
   ta.ss_out = reinterpret_cast<float*>(SSq);
   ta.M = M;
@@ -932,12 +922,8 @@ static TokParams tok_params(Handle& h, int B) {
 
 static void run_tokenizer(Handle& h, int B) {
   const TokParams p = tok_params(h, B);
-  static size_t attr_bytes = 0;
   const size_t smem = tok_smem_bytes(h.d);
-  if (smem > attr_bytes) {
-    CK(cudaFuncSetAttribute(k_tokenize, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    attr_bytes = smem;
-  }
+  ensure_smem(k_tokenize, smem);
   const int tiles = p.tiles_hist + p.tiles_cand + p.tiles_prof;
   const int grid = std::max(1, std::min(tiles, 2 * h.num_sms));
   k_tokenize<<<grid, kTokThreads, smem, h.stream>>>(p);
@@ -955,12 +941,7 @@ static void run_moe(Handle& h, int l, __nv_bfloat16* X, float4* SS, int T) {
     throw RuntimeFailure("moe: workspace too small");
   int32_t* counts = h.moe_counts + static_cast<size_t>(l) * E;
   const float* gain = h.w32.at("block." + std::to_string(l) + ".ffn_norm");
-  static bool attr = false;
-  if (!attr) {
-    CK(cudaFuncSetAttribute(k_moe_route, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (256 * kMoeMaxExperts + 8 * 32 * (kMoeMaxExperts + 1)) * 4));
-    attr = true;
-  }
+  ensure_smem(k_moe_route, (256 * kMoeMaxExperts + 8 * 32 * (kMoeMaxExperts + 1)) * 4);
   CK(cudaMemsetAsync(counts, 0, static_cast<size_t>(E) * 4, h.stream));
   if (E <= 8 && k <= 2) {  // routing and scatter in one pass; the cursors end as the loads
     const int grid = std::max(1, std::min((T + 255) / 256, 2 * h.num_sms));
@@ -994,14 +975,8 @@ static void run_moe(Handle& h, int l, __nv_bfloat16* X, float4* SS, int T) {
   }
   stage_mark(h, "L" + std::to_string(l) + ".moe_route");
   if (h.moe_fused && (d == 128 || d == 256)) {  // hidden chunk stays on chip (moe.cuh)
-    static bool attr = false;
-    if (!attr) {
-      CK(cudaFuncSetAttribute(k_moe_expert<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              static_cast<int>(TailSmem<256>::bytes)));
-      CK(cudaFuncSetAttribute(k_moe_expert<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              static_cast<int>(TailSmem<128>::bytes)));
-      attr = true;
-    }
+    ensure_smem(k_moe_expert<256>, TailSmem<256>::bytes);
+    ensure_smem(k_moe_expert<128>, TailSmem<128>::bytes);
     const int grid = std::max(1, std::min(h.moe_tiles_max, h.num_sms));
     if (d == 256)
       k_moe_expert<256><<<grid, kTailThreads, TailSmem<256>::bytes, h.stream>>>(
@@ -1792,11 +1767,7 @@ static void forward_device(Handle& h, int B) {
   if (h.cfg.pretrain) {  // tied next-item head, see pretrain.cuh
     const int T = B * h.L0;
     const size_t psmem = (static_cast<size_t>(h.d) * kPreK + 8 * h.d) * sizeof(float);
-    static bool attr = false;
-    if (!attr) {
-      CK(cudaFuncSetAttribute(k_pretrain_proj, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-      attr = true;
-    }
+    ensure_smem(k_pretrain_proj, psmem);
     const __nv_bfloat16* items = h.item_ext ? h.item_ext : h.item;
     const int V = h.item_ext ? static_cast<int>(h.item_ext_rows) : h.cfg.n_items;
     k_pretrain_proj<<<std::max(1, std::min((T + 7) / 8, 8 * h.num_sms)), 256, psmem, h.stream>>>(
@@ -1813,11 +1784,7 @@ static void forward_device(Handle& h, int B) {
   const LayerDev& lst = last;
 #define SORT_HEAD(CPT)                                                                          \
   case CPT: {                                                                                   \
-    static bool attr = false;                                                                   \
-    if (!attr) {                                                                                \
-      CK(cudaFuncSetAttribute(k_head<CPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)); \
-      attr = true;                                                                              \
-    }                                                                                           \
+    ensure_smem(k_head<CPT>, hsmem);                                                            \
     k_head<CPT><<<hgrid, kHeadThreads, hsmem, h.stream>>>(                                      \
         h.X[lst.q_buf], h.SS[lst.q_buf], lst.Rq, h.cfg.n_cand, total, h.d, h.head_gain,         \
         h.head_w1, h.head_b1, h.head_w2, h.head_b2, h.probs, h.logits);                         \
