@@ -441,3 +441,27 @@ def test_fused_tail_odd_hidden_chunks_many_tiles():
     gm.set_option("fused_tail", 0)
     _, z_u = gm.forward_logits(b)
     assert np.array_equal(z_f, z_u)
+
+
+def test_two_handles_two_threads(tiny):
+    """One handle per host thread (the C ABI's threading contract): two handles driven
+    concurrently from two threads give exactly the sequential results."""
+    import threading
+    cfg, P, gm, _ = tiny
+    g2 = R.SortModel(cfg, P, max_batch=8)
+    batches = [synth.make_batch(cfg, 4, seed=400 + i) for i in range(6)]
+    ref = [gm.forward(b) for b in batches]
+    out = [[None] * len(batches), [None] * len(batches)]
+
+    def run(model, slot):
+        for i, b in enumerate(batches):
+            out[slot][i] = model.forward(b)
+
+    ts = [threading.Thread(target=run, args=(gm, 0)), threading.Thread(target=run, args=(g2, 1))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for slot in range(2):
+        for o, r in zip(out[slot], ref):
+            np.testing.assert_array_equal(o, r)
