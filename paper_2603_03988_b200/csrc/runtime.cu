@@ -1265,6 +1265,25 @@ static void ensure_train_buffers(Handle& h, int B) {
 }
 
 
+// Row RMSNorm / its backward for the training path: the vectorised kernels when d <= 256.
+template <class T>
+static void rms_rows(Handle& h, const T* x, const float* gain, int rows, int d, float* y, float* inv) {
+  if (d <= 256 && d % 8 == 0)
+    k_rmsnorm_rows_v<T><<<std::max(1, std::min((rows + 7) / 8, 8 * h.num_sms)), 256, 0, h.stream>>>(x, gain, rows, d,
+                                                                                                   y, inv);
+  else
+    k_rmsnorm_rows<T><<<(rows + 7) / 8, 256, 0, h.stream>>>(x, gain, rows, d, nullptr, 1, 1, y, inv);
+}
+template <class T>
+static void rms_bwd(Handle& h, const float* dy, const T* x, const float* inv, const float* gain, int rows, int d,
+                    float* dx, int accum, float* dgain) {
+  if (d <= 256 && d % 8 == 0)
+    k_rmsnorm_bwd_v<T><<<std::max(1, std::min((rows + 7) / 8, 4 * h.num_sms)), 256, d * 4, h.stream>>>(
+        dy, x, inv, gain, rows, d, dx, accum, dgain);
+  else
+    k_rmsnorm_bwd<T><<<(rows + 63) / 64, 256, d * 4, h.stream>>>(dy, x, inv, gain, rows, d, dx, accum, dgain);
+}
+
 // Backward of one training forward; dz = dL/dlogits [B*N, 3] on the device.
 static void backward_device(Handle& h, int B, const float* dz) {
   const SortConfig& c = h.cfg;
@@ -1286,8 +1305,7 @@ static void backward_device(Handle& h, int B, const float* dz) {
   float* dhid = hid + static_cast<size_t>(BN) * dh;
   const __nv_bfloat16* Xf = h.X[last.q_buf];
   k_gather_f32<__nv_bfloat16><<<(BN + 7) / 8, 256, 0, h.stream>>>(Xf, cmap, N, R, BN, d, xc);
-  k_rmsnorm_rows<float><<<(BN + 7) / 8, 256, 0, h.stream>>>(xc, w32(h, "final_norm.gain"), BN, d, nullptr, 1, 1, xh,
-                                                            inv);
+  rms_rows<float>(h, xc, w32(h, "final_norm.gain"), BN, d, xh, inv);
   check_launch("head rows");
   gemm_rm(h, false, false, BN, dh, d, xh, d, w32(h, "head.w1"), dh, hid, dh);
   k_bias_relu<<<ew_grid(static_cast<size_t>(BN) * dh), 256, 0, h.stream>>>(hid, w32(h, "head.b1"), BN, dh);
@@ -1301,8 +1319,7 @@ static void backward_device(Handle& h, int B, const float* dz) {
   float* dxh = h.tw[4];
   gemm_rm(h, false, true, BN, d, dh, dhid, dh, w32(h, "head.w1"), dh, dxh, d);
   float* dxc = h.tw[5];
-  k_rmsnorm_bwd<float><<<(BN + 63) / 64, 256, d * 4, h.stream>>>(dxh, xc, inv, w32(h, "final_norm.gain"), BN, d, dxc,
-                                                                 0, grad_ptr(h, "final_norm.gain"));
+  rms_bwd<float>(h, dxh, xc, inv, w32(h, "final_norm.gain"), BN, d, dxc, 0, grad_ptr(h, "final_norm.gain"));
   CK(cudaMemsetAsync(dX, 0, static_cast<size_t>(B) * R * d * 4, h.stream));
   k_scatter_add_rows<<<(BN + 7) / 8, 256, 0, h.stream>>>(dxc, cmap, B, N, R, d, dX);
   check_launch("head backward");
@@ -1320,8 +1337,7 @@ static void backward_device(Handle& h, int B, const float* dz) {
     float* GU = h.tw[12];
     float* dGU = GU + static_cast<size_t>(M) * 2 * m;
     float* z = h.tw[13];
-    k_rmsnorm_rows<__nv_bfloat16><<<(M + 7) / 8, 256, 0, h.stream>>>(T.x1, w32(h, Bk + "ffn_norm"), M, d, nullptr, 1,
-                                                                     1, xf, inv);
+    rms_rows<__nv_bfloat16>(h, T.x1, w32(h, Bk + "ffn_norm"), M, d, xf, inv);
     gemm_rm(h, false, false, M, 2 * m, d, xf, d, w32(h, F + "w_gu"), 2 * m, GU, 2 * m);
     k_swiglu_z<<<std::min(M, 148 * 16), 256, 0, h.stream>>>(GU, M, m, z);
     gemm_rm(h, true, false, m, d, M, z, m, dX, d, grad_ptr(h, F + "w_down"), d);
@@ -1331,8 +1347,7 @@ static void backward_device(Handle& h, int B, const float* dz) {
     gemm_rm(h, true, false, d, m, M, xf, d, dGU + m, 2 * m, grad_ptr(h, F + "w_up"), m);
     float* dxf = h.tw[3];
     gemm_rm(h, false, true, M, d, 2 * m, dGU, 2 * m, w32(h, F + "w_gu"), 2 * m, dxf, d);
-    k_rmsnorm_bwd<__nv_bfloat16><<<(M + 63) / 64, 256, d * 4, h.stream>>>(dxf, T.x1, inv, w32(h, Bk + "ffn_norm"), M,
-                                                                           d, dX, 1, grad_ptr(h, Bk + "ffn_norm"));
+    rms_bwd<__nv_bfloat16>(h, dxf, T.x1, inv, w32(h, Bk + "ffn_norm"), M, d, dX, 1, grad_ptr(h, Bk + "ffn_norm"));
     check_launch("ffn backward");
     // attention (attention.cpp:134-202); dX now holds d(xr)
     float* Hm = h.tw[4];
@@ -1348,8 +1363,7 @@ static void backward_device(Handle& h, int B, const float* dz) {
     float* xn = h.tw[2];
     float* xq = h.tw[3];
     float* inv_a = h.tw[14] + static_cast<size_t>(h.train_B) * h.L0;
-    k_rmsnorm_rows<__nv_bfloat16><<<(Mkv + 7) / 8, 256, 0, h.stream>>>(T.x_in, w32(h, Bk + "attn_norm"), Mkv, d,
-                                                                       nullptr, 1, 1, xn, inv_a);
+    rms_rows<__nv_bfloat16>(h, T.x_in, w32(h, Bk + "attn_norm"), Mkv, d, xn, inv_a);
     const float* xqp = xn;
     if (!lp.q_identity) {
       k_gather_f32<float><<<(M + 7) / 8, 256, 0, h.stream>>>(xn, L.query_rows, L.Rq, L.Rkv, M, d, xq);
@@ -1452,8 +1466,8 @@ static void backward_device(Handle& h, int B, const float* dz) {
     gemm_rm(h, false, true, Mkv, d, d, dV, d, w32(h, A + "wv"), d, dxn, d, 1.f);
     k_scatter_add_rows<<<(M + 7) / 8, 256, 0, h.stream>>>(dxq, L.query_rows, B, L.Rq, L.Rkv, d, dxn);
     // d(x_in) = RMSN_bwd(dxn) + scatter of d(xr) through P(x, L_out)
-    k_rmsnorm_bwd<__nv_bfloat16><<<(Mkv + 63) / 64, 256, d * 4, h.stream>>>(
-        dxn, T.x_in, inv_a, w32(h, Bk + "attn_norm"), Mkv, d, dXn, 0, grad_ptr(h, Bk + "attn_norm"));
+    rms_bwd<__nv_bfloat16>(h, dxn, T.x_in, inv_a, w32(h, Bk + "attn_norm"), Mkv, d, dXn, 0,
+                           grad_ptr(h, Bk + "attn_norm"));
     k_scatter_add_rows<<<(M + 7) / 8, 256, 0, h.stream>>>(dX, L.query_rows, B, L.Rq, L.Rkv, d, dXn);
     check_launch("attention backward");
     std::swap(dX, dXn);
@@ -1480,11 +1494,10 @@ static void backward_device(Handle& h, int B, const float* dz) {
     gemm_rm(h, false, false, n, d, K, catf, K, w32(h, W), d, y, d);
     k_bias_add<<<ew_grid(static_cast<size_t>(n) * d), 256, 0, h.stream>>>(y, w32(h, std::string("tok.b_") + gname[g]),
                                                                          n, d);
-    k_rmsnorm_rows<float><<<warp_rows_grid(n), 256, 0, h.stream>>>(y, nullptr, n, d, nullptr, 1, 1,
-                                                                   static_cast<float*>(nullptr), inv);
+    rms_rows<float>(h, y, nullptr, n, d, nullptr, inv);
     k_gather_f32<float><<<warp_rows_grid(n), 256, 0, h.stream>>>(dX, h.t_rows, n, 0, n, d, dy);
-    k_rmsnorm_bwd<float><<<(n + 63) / 64, 256, d * 4, h.stream>>>(dy, y, inv, w32(h, std::string("tok.g_") + gname[g]), n,
-                                                                  d, dproj, 0, grad_ptr(h, std::string("tok.g_") + gname[g]));
+    rms_bwd<float>(h, dy, y, inv, w32(h, std::string("tok.g_") + gname[g]), n, d, dproj, 0,
+                   grad_ptr(h, std::string("tok.g_") + gname[g]));
     gemm_rm(h, true, false, K, d, n, catf, K, dproj, d, grad_ptr(h, W), d);
     k_colsum<<<dim3((d + 31) / 32, std::min(1024, (n + 63) / 64)), 32, 0, h.stream>>>(
         dproj, n, d, grad_ptr(h, std::string("tok.b_") + gname[g]));

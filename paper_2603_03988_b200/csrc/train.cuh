@@ -114,6 +114,106 @@ __global__ void __launch_bounds__(256) k_rmsnorm_bwd(const float* __restrict__ d
   for (int c = threadIdx.x; c < d; c += blockDim.x) atomicAdd(&dgain[c], sg[c]);
 }
 
+// Vectorised row forms for d <= 256 (d % 8 == 0): one warp per row, lane owns 8 contiguous
+// columns (32-byte fp32 / 16-byte bf16 accesses), grid-stride over rows.
+__device__ __forceinline__ void load8(const float* p, float (&v)[8]) {
+  const float4 a = reinterpret_cast<const float4*>(p)[0], b = reinterpret_cast<const float4*>(p)[1];
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void load8(const __nv_bfloat16* p, float (&v)[8]) {
+  const int4 r = *reinterpret_cast<const int4*>(p);
+  const __nv_bfloat162* q = reinterpret_cast<const __nv_bfloat162*>(&r);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(q[i]);
+    v[2 * i] = f.x;
+    v[2 * i + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void store8(float* p, const float (&v)[8]) {
+  reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+  reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+
+// y = RMSNorm(x; gain) (fp32 out, gain may be null), inv_rms per row (norm.hpp:17-29).
+template <class T>
+__global__ void __launch_bounds__(256) k_rmsnorm_rows_v(const T* __restrict__ x, const float* __restrict__ gain,
+                                                        int rows, int d, float* __restrict__ y,
+                                                        float* __restrict__ inv_out) {
+  const int lane = threadIdx.x & 31, c0 = lane * 8;
+  const bool act = c0 < d;
+  float g[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) g[k] = act && gain ? gain[c0 + k] : 1.f;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  for (int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < rows; w += warps) {
+    float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (act) load8(x + static_cast<size_t>(w) * d + c0, v);
+    float ss = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) ss = fmaf(v[k], v[k], ss);
+    const float inv = rsqrtf(warp_sum(ss) / static_cast<float>(d) + 1e-6f);
+    if (inv_out && lane == 0) inv_out[w] = inv;
+    if (y && act) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] *= inv * g[k];
+      store8(y + static_cast<size_t>(w) * d + c0, v);
+    }
+  }
+}
+
+// rmsnorm_backward (norm.hpp:32-45), vectorised form of k_rmsnorm_bwd (same math).
+template <class T>
+__global__ void __launch_bounds__(256) k_rmsnorm_bwd_v(const float* __restrict__ dy, const T* __restrict__ x,
+                                                       const float* __restrict__ inv, const float* __restrict__ gain,
+                                                       int rows, int d, float* __restrict__ dx, int accum,
+                                                       float* __restrict__ dgain) {
+  extern __shared__ float sg[];  // [d]
+  for (int c = threadIdx.x; c < d; c += blockDim.x) sg[c] = 0.f;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, c0 = lane * 8;
+  const bool act = c0 < d;
+  float g[8], gacc[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    g[k] = act ? gain[c0 + k] : 0.f;
+    gacc[k] = 0.f;
+  }
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+    const float iv = inv[r];
+    float dyv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, xv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (act) {
+      load8(dy + static_cast<size_t>(r) * d + c0, dyv);
+      load8(x + static_cast<size_t>(r) * d + c0, xv);
+    }
+    float proj = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float xh = xv[k] * iv;
+      gacc[k] = fmaf(dyv[k], xh, gacc[k]);
+      proj = fmaf(dyv[k] * g[k], xh, proj);
+    }
+    proj = warp_sum(proj) / static_cast<float>(d);
+    if (act) {
+      float o[8];
+      float* dxr = dx + static_cast<size_t>(r) * d + c0;
+      if (accum) load8(dxr, o);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float v = (dyv[k] * g[k] - proj * xv[k] * iv) * iv;
+        o[k] = accum ? o[k] + v : v;
+      }
+      store8(dxr, o);
+    }
+  }
+  if (act)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) atomicAdd(&sg[c0 + k], gacc[k]);
+  __syncthreads();
+  for (int c = threadIdx.x; c < d; c += blockDim.x) atomicAdd(&dgain[c], sg[c]);
+}
+
 // SwishGLU pieces. GU = [gp | up] (fp32 [M, 2m]).
 __device__ __forceinline__ float sigmoid_f(float x) { return 1.f / (1.f + __expf(-x)); }
 template <class O = float, class I = float>
@@ -734,7 +834,19 @@ __global__ void k_scatter_add_rows(const float* __restrict__ src, const int32_t*
   const int b = w / Rsrc, r = w - b * Rsrc;
   float* o = dst + (static_cast<size_t>(b) * Rdst + map[r]) * d;
   const float* s = src + static_cast<size_t>(w) * d;
-  for (int c = lane; c < d; c += 32) o[c] += s[c];
+  if ((d & 3) == 0) {  // 16-byte vectors
+    for (int c = lane; c < d / 4; c += 32) {
+      const float4 a = reinterpret_cast<const float4*>(s)[c];
+      float4 t = reinterpret_cast<float4*>(o)[c];
+      t.x += a.x;
+      t.y += a.y;
+      t.z += a.z;
+      t.w += a.w;
+      reinterpret_cast<float4*>(o)[c] = t;
+    }
+  } else {
+    for (int c = lane; c < d; c += 32) o[c] += s[c];
+  }
 }
 
 // Column sums: out[c] += sum_r a[r, c] (bias gradients).
