@@ -129,8 +129,10 @@ struct Handle {
     int32_t *dq_off = nullptr, *dkv_off = nullptr;
     int2 *dq_iv = nullptr, *dkv_iv = nullptr;
     int32_t *qb_off = nullptr, *qb_list = nullptr;  // tensor-core backward: q blocks per kv block
+    CUtensorMap tmQ, tmK, tmV;  // the attention core reads the saved Q / K / V directly
   };
   std::vector<TrainLayer> tl;
+  const TrainLayer* save_to = nullptr;  // training forward: QKVG writes straight into these buffers
   float *tw[16] = {nullptr};  // backward workspace
   __nv_bfloat16* dO16 = nullptr;  // bf16 copy of dL/d(attention output) for the tensor-core backward
   float* dtokens = nullptr;
@@ -724,7 +726,7 @@ static void launch_attention_dk(Handle& h, const LayerDev& L, const LayerPlan& l
   a.tile_off = L.tile_off;
   a.tile_code = reinterpret_cast<const int2*>(L.tile_code);
   a.qtile_order = L.qtile_order;
-  a.g = h.Gb;
+  a.g = h.save_to ? h.save_to->g : h.Gb;
   a.out = h.Hg;
   a.o_pre = nullptr;
   a.lse = nullptr;
@@ -744,7 +746,7 @@ static void launch_attention_dk(Handle& h, const LayerDev& L, const LayerPlan& l
   const int n_items = lp.n_qtiles * B * h.H;
   const int tile_ints = 2 * lp.n_qtiles + 2 + 2 * n_codes;
   if constexpr (kFixed) {
-    if (h.attn_sub) {  // fixed reference: 64-column subtiles, O accumulated in TMEM
+    if (h.attn_sub && !h.save_to) {  // fixed reference: 64-column subtiles, O accumulated in TMEM
       const size_t smem_f = AttnFLayout<DK>::bytes(tile_ints);
       ensure_smem(k_attention_f<DK>, smem_f);
       const int grid_f = std::min(n_items, 2 * h.num_sms);
@@ -757,7 +759,10 @@ static void launch_attention_dk(Handle& h, const LayerDev& L, const LayerPlan& l
   const size_t smem = AttnSmem<DK>::bytes(tile_ints);
   ensure_smem(k_attention<DK, kFixed>, smem);
   const int grid = std::min(n_items, AttnTmem<DK>::kCtasPerSm * h.num_sms);
-  k_attention<DK, kFixed><<<grid, kAttnThreads, smem, h.stream>>>(L.tmQ, L.tmK, L.tmV, a);
+  const CUtensorMap& tq = h.save_to ? h.save_to->tmQ : L.tmQ;
+  const CUtensorMap& tk = h.save_to ? h.save_to->tmK : L.tmK;
+  const CUtensorMap& tv = h.save_to ? h.save_to->tmV : L.tmV;
+  k_attention<DK, kFixed><<<grid, kAttnThreads, smem, h.stream>>>(tq, tk, tv, a);
   check_launch("attention");
   ++h.launches;
 }
@@ -791,10 +796,10 @@ static void launch_qkvg_dk(Handle& h, const LayerDev& L, const CUtensorMap& A, c
   e.inv_d = 1.f / static_cast<float>(h.d);
   e.gain_q = L.gain_q;
   e.gain_k = L.gain_k;
-  e.q = h.Qb;
-  e.k = h.Kb;
-  e.v = h.Vb;
-  e.g = h.Gb;
+  e.q = h.save_to ? h.save_to->q : h.Qb;
+  e.k = h.save_to ? h.save_to->k : h.Kb;
+  e.v = h.save_to ? h.save_to->v : h.Vb;
+  e.g = h.save_to ? h.save_to->g : h.Gb;
   e.Rq = L.Rq;
   e.Rkv = L.Rkv;
   if (Bpair && h.qkvg_pair)
@@ -1028,9 +1033,13 @@ static void run_layer(Handle& h, int l, int B, bool attn_only = false) {
   float4* SSin = h.SS[L.in_buf];
   __nv_bfloat16* Xq = h.X[L.q_buf];
   float4* SSq = h.SS[L.q_buf];
-  if (h.training)
+  if (h.training) {
     CK(cudaMemcpyAsync(h.tl[l].x_in, Xin, static_cast<size_t>(B) * L.Rkv * d * 2, cudaMemcpyDeviceToDevice,
                        h.stream));
+    h.save_to = &h.tl[l];  // the projections and the attention core use the saved buffers
+  } else {
+    h.save_to = nullptr;
+  }
   if (lp.q_identity) {
     launch_qkvg(h, L, L.tmA_in, L.tmB_all, B * L.Rkv, 4 * d, L.bn_full, L.Rkv,
                 {kSecQ, kSecV, kSecK, kSecG}, h.tmSS[L.in_buf], L.tmRopeKV, &L.tmB_all_p);
@@ -1047,13 +1056,7 @@ static void run_layer(Handle& h, int l, int B, bool attn_only = false) {
   stage_mark(h, "L" + std::to_string(l) + ".qkvg");
   launch_attention(h, L, lp, B);
   stage_mark(h, "L" + std::to_string(l) + ".attention");
-  if (h.training) {  // saved activations of the attention core for the backward
-    const size_t nq = static_cast<size_t>(B) * L.Rq * d, nkv = static_cast<size_t>(B) * L.Rkv * d;
-    CK(cudaMemcpyAsync(h.tl[l].q, h.Qb, nq * 2, cudaMemcpyDeviceToDevice, h.stream));
-    CK(cudaMemcpyAsync(h.tl[l].k, h.Kb, nkv * 2, cudaMemcpyDeviceToDevice, h.stream));
-    CK(cudaMemcpyAsync(h.tl[l].v, h.Vb, nkv * 2, cudaMemcpyDeviceToDevice, h.stream));
-    CK(cudaMemcpyAsync(h.tl[l].g, h.Gb, nq * 2, cudaMemcpyDeviceToDevice, h.stream));
-  }
+  h.save_to = nullptr;  // (Q / K / V / G of a training forward went straight to h.tl[l])
   if (!attn_only && h.fused_tail && !h.training && tail_supported(h)) {
     if (d == 256) launch_tail_d<256>(h, L, Xq, SSq, B * L.Rq);
     else launch_tail_d<128>(h, L, Xq, SSq, B * L.Rq);
@@ -1223,6 +1226,18 @@ static void ensure_train_buffers(Handle& h, int B) {
     T.o_pre = h.dalloc<__nv_bfloat16>(nq);
     T.x1 = h.dalloc<__nv_bfloat16>(nq);
     T.lse = h.dalloc<float>(static_cast<size_t>(B) * h.H * L.Rq);
+    {
+      const int dk = h.dk;
+      const uint64_t BH = static_cast<uint64_t>(B) * h.H;
+      uint64_t dq[3] = {static_cast<uint64_t>(dk), static_cast<uint64_t>(L.Rq), BH};
+      uint64_t sq[2] = {static_cast<uint64_t>(dk) * 2, static_cast<uint64_t>(L.Rq) * dk * 2};
+      uint32_t bq[3] = {static_cast<uint32_t>(dk), 128, 1};
+      T.tmQ = make_tmap_bf16(T.q, 3, dq, sq, bq, dk * 2);
+      uint64_t dkd[3] = {static_cast<uint64_t>(dk), static_cast<uint64_t>(L.Rkv), BH};
+      uint64_t skd[2] = {static_cast<uint64_t>(dk) * 2, static_cast<uint64_t>(L.Rkv) * dk * 2};
+      T.tmK = make_tmap_bf16(T.k, 3, dkd, skd, bq, dk * 2);
+      T.tmV = make_tmap_bf16(T.v, 3, dkd, skd, bq, dk * 2);
+    }
     std::vector<int32_t> qo, ko;
     std::vector<int2> qi, ki;
     build_bwd_lists(h.plan.layers[l], qo, qi, ko, ki);
