@@ -51,6 +51,7 @@ struct TailArgs {
   float* ss_out;  // [M, 4] sum-of-squares partials of the output rows
   int M, m;       // rows, FFN hidden width
   float inv_d;
+  __nv_bfloat16* x1_out;  // training: x1 rows also written here (the backward's saved input), or null
 };
 
 __device__ __forceinline__ void sts_v4(uint32_t addr, int4 v) {
@@ -423,6 +424,9 @@ __global__ void __launch_bounds__(kTailThreads, 1)
               ss = fmaf(y.x, y.x, fmaf(y.y, y.y, ss));
             }
             sts_v4(adr, make_int4(w[0], w[1], w[2], w[3]));
+            if (a.x1_out && row < a.M)
+              *reinterpret_cast<int4*>(a.x1_out + static_cast<size_t>(row) * D + kb * 64 + cc * 32 + qd * 8) =
+                  make_int4(w[0], w[1], w[2], w[3]);
           }
         }
         ssb[p] = ss;

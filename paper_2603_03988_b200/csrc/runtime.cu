@@ -821,9 +821,10 @@ static void launch_qkvg(Handle& h, const LayerDev& L, const CUtensorMap& A, cons
 }
 
 template <int D, bool kPair>
-static void launch_tail_dp(Handle& h, const LayerDev& L, float4* SSq, int M) {
+static void launch_tail_dp(Handle& h, const LayerDev& L, float4* SSq, int M, __nv_bfloat16* x1_out) {
   ensure_smem(k_block_tail<D, kPair>, TailSmem<D>::bytes);
   TailArgs ta;
+  ta.x1_out = x1_out;
   ta.ss_out = reinterpret_cast<float*>(SSq);
   ta.M = M;
   ta.m = h.m;
@@ -856,11 +857,12 @@ static void launch_tail_dp(Handle& h, const LayerDev& L, float4* SSq, int M) {
 }
 
 template <int D>
-static void launch_tail_d(Handle& h, const LayerDev& L, __nv_bfloat16*, float4* SSq, int M) {
+static void launch_tail_d(Handle& h, const LayerDev& L, __nv_bfloat16*, float4* SSq, int M,
+                          __nv_bfloat16* x1_out = nullptr) {
   if (h.tail_pair) {
-    launch_tail_dp<D, true>(h, L, SSq, M);
+    launch_tail_dp<D, true>(h, L, SSq, M, x1_out);
   } else {
-    launch_tail_dp<D, false>(h, L, SSq, M);
+    launch_tail_dp<D, false>(h, L, SSq, M, x1_out);
   }
 }
 
@@ -1057,9 +1059,10 @@ static void run_layer(Handle& h, int l, int B, bool attn_only = false) {
   launch_attention(h, L, lp, B);
   stage_mark(h, "L" + std::to_string(l) + ".attention");
   h.save_to = nullptr;  // (Q / K / V / G of a training forward went straight to h.tl[l])
-  if (!attn_only && h.fused_tail && !h.training && tail_supported(h)) {
-    if (d == 256) launch_tail_d<256>(h, L, Xq, SSq, B * L.Rq);
-    else launch_tail_d<128>(h, L, Xq, SSq, B * L.Rq);
+  if (!attn_only && h.fused_tail && tail_supported(h)) {  // training: x1 saved by the kernel
+    __nv_bfloat16* x1_out = h.training ? h.tl[l].x1 : nullptr;
+    if (d == 256) launch_tail_d<256>(h, L, Xq, SSq, B * L.Rq, x1_out);
+    else launch_tail_d<128>(h, L, Xq, SSq, B * L.Rq, x1_out);
     stage_mark(h, "L" + std::to_string(l) + ".tail");
     return;
   }
