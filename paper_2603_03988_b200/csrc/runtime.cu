@@ -115,6 +115,7 @@ struct Handle {
   // a flat fp32 gradient buffer, saved forward activations per layer, workspace
   std::map<std::string, float*> w32;
   std::map<std::string, __nv_bfloat16*> w16;  // bf16 copies for the generic path's GEMMs
+  std::map<std::string, std::pair<__nv_bfloat16*, size_t>> tw16;  // training: bf16 weights of the FFN backward
   std::map<std::string, std::pair<size_t, std::pair<int64_t, int64_t>>> grad_index;  // offset, shape
   float* grads = nullptr;
   float* master = nullptr;                 // fp32 master parameters (grad_index layout)
@@ -1150,6 +1151,18 @@ static void qkv_prep(Handle& h, const __nv_bfloat16* raw, int ld, int rows, int 
     k_qkv_prep<8><<<g, 256, 0, h.stream>>>(raw, ld, rows, R, H, dk, kind, pos, rope, gain, out);
 }
 
+// Row-major C[M,N] (+ beta C) = op(A) op(B) with bf16 operands and fp32 accumulation; C fp32
+// or bf16 (the training FFN backward).
+static void gemm_rm16(Handle& h, bool ta, bool tb, int M, int N, int K, const __nv_bfloat16* A, int lda,
+                      const __nv_bfloat16* B, int ldb, void* C, int ldc, bool c_bf16, float beta = 0.f) {
+  const float alpha = 1.f;
+  const cublasStatus_t st = cublasGemmEx(h.cublas, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N,
+                                         N, M, K, &alpha, B, CUDA_R_16BF, ldb, A, CUDA_R_16BF, lda, &beta, C,
+                                         c_bf16 ? CUDA_R_16BF : CUDA_R_32F, ldc, CUBLAS_COMPUTE_32F,
+                                         CUBLAS_GEMM_DEFAULT);
+  if (st != CUBLAS_STATUS_SUCCESS) throw RuntimeFailure("cublasGemmEx (bf16) failed: " + std::to_string(static_cast<int>(st)));
+}
+
 static float* grad_ptr(Handle& h, const std::string& name) {
   auto it = h.grad_index.find(name);
   if (it == h.grad_index.end()) throw RuntimeFailure("no gradient slot for " + name);
@@ -1159,6 +1172,18 @@ static const float* w32(Handle& h, const std::string& name) {
   auto it = h.w32.find(name);
   if (it == h.w32.end()) throw RuntimeFailure("no fp32 parameter " + name);
   return it->second;
+}
+
+// bf16 copy of an fp32 training weight (`n` elements), refreshed by repack_weights after every
+// optimizer step.
+static const __nv_bfloat16* tw16(Handle& h, const std::string& name, size_t n) {
+  auto it = h.tw16.find(name);
+  if (it != h.tw16.end()) return it->second.first;
+  __nv_bfloat16* dst = h.dalloc<__nv_bfloat16>(n);
+  k_f32_to_bf16<<<ew_grid(n), 256, 0, h.stream>>>(w32(h, name), n, dst);
+  check_launch("training weight cast");
+  h.tw16[name] = {dst, n};
+  return dst;
 }
 
 // Work lists of the attention backward for one layer (batch-uniform): for every 32-row
@@ -1351,20 +1376,31 @@ static void backward_device(Handle& h, int B, const float* dz) {
     const int M = B * L.Rq, Mkv = B * L.Rkv;
     const size_t nq = static_cast<size_t>(M) * d, nkv = static_cast<size_t>(Mkv) * d;
     // FFN: xo = xr + down(swish(xf Wg) * (xf Wu)), xf = RMSN(xr = x1)
-    float* xf = h.tw[2];
-    float* GU = h.tw[12];
-    float* dGU = GU + static_cast<size_t>(M) * 2 * m;
-    float* z = h.tw[13];
-    rms_rows<__nv_bfloat16>(h, T.x1, w32(h, Bk + "ffn_norm"), M, d, xf, inv);
-    gemm_rm(h, false, false, M, 2 * m, d, xf, d, w32(h, F + "w_gu"), 2 * m, GU, 2 * m);
-    k_swiglu_z<<<std::min(M, 148 * 16), 256, 0, h.stream>>>(GU, M, m, z);
-    gemm_rm(h, true, false, m, d, M, z, m, dX, d, grad_ptr(h, F + "w_down"), d);
-    gemm_rm(h, false, true, M, m, d, dX, d, w32(h, F + "w_down"), d, z, m);  // z <- dz
-    k_swiglu_bwd<<<std::min(M, 148 * 16), 256, 0, h.stream>>>(z, GU, M, m, dGU);
-    gemm_rm(h, true, false, d, m, M, xf, d, dGU, 2 * m, grad_ptr(h, F + "w_gate"), m);
-    gemm_rm(h, true, false, d, m, M, xf, d, dGU + m, 2 * m, grad_ptr(h, F + "w_up"), m);
+    // bf16 operands and [M, m] / [M, 2m] intermediates, fp32 accumulation and gradients
+    __nv_bfloat16* xf = reinterpret_cast<__nv_bfloat16*>(h.tw[2]);
+    __nv_bfloat16* GU = reinterpret_cast<__nv_bfloat16*>(h.tw[12]);
+    __nv_bfloat16* dGU = GU + static_cast<size_t>(M) * 2 * m;
+    __nv_bfloat16* z = reinterpret_cast<__nv_bfloat16*>(h.tw[13]);
+    __nv_bfloat16* dX16 = reinterpret_cast<__nv_bfloat16*>(h.tw[3]);
+    const __nv_bfloat16* Wgu = tw16(h, F + "w_gu", static_cast<size_t>(d) * 2 * m);
+    const __nv_bfloat16* Wdn = tw16(h, F + "w_down", static_cast<size_t>(m) * d);
+    if (d <= 256 && d % 8 == 0) {
+      k_rmsnorm_rows_v<__nv_bfloat16, __nv_bfloat16><<<std::max(1, std::min((M + 7) / 8, 8 * h.num_sms)), 256, 0,
+                                                        h.stream>>>(T.x1, w32(h, Bk + "ffn_norm"), M, d, xf, inv);
+    } else {
+      k_rmsnorm_rows<__nv_bfloat16, __nv_bfloat16><<<(M + 7) / 8, 256, 0, h.stream>>>(
+          T.x1, w32(h, Bk + "ffn_norm"), M, d, nullptr, 1, 1, xf, inv);
+    }
+    gemm_rm16(h, false, false, M, 2 * m, d, xf, d, Wgu, 2 * m, GU, 2 * m, true);
+    k_swiglu_z<__nv_bfloat16, __nv_bfloat16><<<std::min(M, 148 * 16), 256, 0, h.stream>>>(GU, M, m, z);
+    k_f32_to_bf16<<<ew_grid(nq), 256, 0, h.stream>>>(dX, nq, dX16);
+    gemm_rm16(h, true, false, m, d, M, z, m, dX16, d, grad_ptr(h, F + "w_down"), d, false);
+    gemm_rm16(h, false, true, M, m, d, dX16, d, Wdn, d, z, m, true);  // z <- dz
+    k_swiglu_bwd16<<<std::min(M, 148 * 16), 256, 0, h.stream>>>(z, GU, M, m, dGU);
+    gemm_rm16(h, true, false, d, m, M, xf, d, dGU, 2 * m, grad_ptr(h, F + "w_gate"), m, false);
+    gemm_rm16(h, true, false, d, m, M, xf, d, dGU + m, 2 * m, grad_ptr(h, F + "w_up"), m, false);
     float* dxf = h.tw[3];
-    gemm_rm(h, false, true, M, d, 2 * m, dGU, 2 * m, w32(h, F + "w_gu"), 2 * m, dxf, d);
+    gemm_rm16(h, false, true, M, d, 2 * m, dGU, 2 * m, Wgu, 2 * m, dxf, d, false);
     rms_bwd<__nv_bfloat16>(h, dxf, T.x1, inv, w32(h, Bk + "ffn_norm"), M, d, dX, 1, grad_ptr(h, Bk + "ffn_norm"));
     check_launch("ffn backward");
     // attention (attention.cpp:134-202); dX now holds d(xr)
@@ -1752,6 +1788,9 @@ static void repack_weights(Handle& h) {
     for (float v : gkv) mk = std::max(mk, std::fabs(v));
     L.logit_bound = 1.02f * std::sqrt(static_cast<float>(dk)) * mq * mk + 1e-3f;
   }
+  for (auto& kv : h.tw16)  // bf16 copies the training backward reads
+    k_f32_to_bf16<<<ew_grid(kv.second.second), 256, 0, h.stream>>>(w32(h, kv.first), kv.second.second,
+                                                                   kv.second.first);
   check_launch("weight repack");
   h.w16.clear();  // generic-path bf16 copies are rebuilt on next use
 }

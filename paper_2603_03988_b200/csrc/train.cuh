@@ -135,10 +135,14 @@ __device__ __forceinline__ void store8(float* p, const float (&v)[8]) {
   reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
 }
 
-// y = RMSNorm(x; gain) (fp32 out, gain may be null), inv_rms per row (norm.hpp:17-29).
-template <class T>
+// y = RMSNorm(x; gain) (fp32 or bf16 out, gain may be null), inv_rms per row (norm.hpp:17-29).
+__device__ __forceinline__ void store8(__nv_bfloat16* p, const float (&v)[8]) {
+  *reinterpret_cast<int4*>(p) = make_int4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]), pack_bf16x2(v[4], v[5]),
+                                          pack_bf16x2(v[6], v[7]));
+}
+template <class T, class O = float>
 __global__ void __launch_bounds__(256) k_rmsnorm_rows_v(const T* __restrict__ x, const float* __restrict__ gain,
-                                                        int rows, int d, float* __restrict__ y,
+                                                        int rows, int d, O* __restrict__ y,
                                                         float* __restrict__ inv_out) {
   const int lane = threadIdx.x & 31, c0 = lane * 8;
   const bool act = c0 < d;
@@ -250,6 +254,34 @@ __global__ void k_swiglu_z<__nv_bfloat16, __nv_bfloat16>(const __nv_bfloat16* __
     }
   }
 }
+// bf16 form of k_swiglu_bwd (16-byte vectors, m % 8 == 0): the training FFN backward keeps its
+// [M, m] / [M, 2m] intermediates in bf16.
+__global__ void k_swiglu_bwd16(const __nv_bfloat16* __restrict__ dz, const __nv_bfloat16* __restrict__ gu, int M,
+                               int m, __nv_bfloat16* __restrict__ dgu) {
+  const int m8 = m / 8;
+  for (int r = blockIdx.x; r < M; r += gridDim.x) {
+    const int4* gr = reinterpret_cast<const int4*>(gu + static_cast<size_t>(r) * 2 * m);
+    const int4* dzr = reinterpret_cast<const int4*>(dz + static_cast<size_t>(r) * m);
+    int4* o = reinterpret_cast<int4*>(dgu + static_cast<size_t>(r) * 2 * m);
+    for (int j = threadIdx.x; j < m8; j += blockDim.x) {
+      const int4 gv = gr[j], uv = gr[m8 + j], dv = dzr[j];
+      const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gv);
+      const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&uv);
+      const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&dv);
+      uint32_t og[4], ou[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 g = __bfloat1622float2(g2[e]), u = __bfloat1622float2(u2[e]), dzv = __bfloat1622float2(d2[e]);
+        const float sx = sigmoid_f(g.x), sy = sigmoid_f(g.y);
+        og[e] = pack_bf16x2(dzv.x * u.x * sx * (1.f + g.x * (1.f - sx)), dzv.y * u.y * sy * (1.f + g.y * (1.f - sy)));
+        ou[e] = pack_bf16x2(dzv.x * g.x * sx, dzv.y * g.y * sy);
+      }
+      o[j] = make_int4(og[0], og[1], og[2], og[3]);
+      o[m8 + j] = make_int4(ou[0], ou[1], ou[2], ou[3]);
+    }
+  }
+}
+
 // dgu = [dz * u * swish'(g) | dz * swish(g)], swish'(g) = s (1 + g (1 - s))
 __global__ void k_swiglu_bwd(const float* __restrict__ dz, const float* __restrict__ gu, int M, int m,
                              float* __restrict__ dgu) {
