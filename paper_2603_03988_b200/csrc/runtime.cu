@@ -1403,30 +1403,47 @@ static void backward_device(Handle& h, int B, const float* dz) {
     gemm_rm16(h, false, true, M, d, 2 * m, dGU, 2 * m, Wgu, 2 * m, dxf, d, false);
     rms_bwd<__nv_bfloat16>(h, dxf, T.x1, inv, w32(h, Bk + "ffn_norm"), M, d, dX, 1, grad_ptr(h, Bk + "ffn_norm"));
     check_launch("ffn backward");
-    // attention (attention.cpp:134-202); dX now holds d(xr)
-    float* Hm = h.tw[4];
+    // attention (attention.cpp:134-202); dX now holds d(xr). GEMM operands in bf16 (fp32
+    // accumulation and gradients): the gated output, d(xr), the normalised rows, d(g_raw),
+    // dQ / dK / dV
+    __nv_bfloat16* Hm = reinterpret_cast<__nv_bfloat16*>(h.tw[4]);
     float* dH = h.tw[5];
     float* dO = h.tw[6];
-    float* dgraw = h.tw[7];
-    k_gate_fwd<<<ew_grid(nq), 256, 0, h.stream>>>(T.g, T.o_pre, nq, Hm);
-    gemm_rm(h, true, false, d, d, M, Hm, d, dX, d, grad_ptr(h, A + "wo"), d);
-    gemm_rm(h, false, true, M, d, d, dX, d, w32(h, A + "wo"), d, dH, d);
+    __nv_bfloat16* dgraw = reinterpret_cast<__nv_bfloat16*>(h.tw[7]);
+    __nv_bfloat16* dXr16 = reinterpret_cast<__nv_bfloat16*>(h.tw[11]);  // d(xr); (raw is recomputed later)
+    const __nv_bfloat16* Wo16 = tw16(h, A + "wo", static_cast<size_t>(d) * d);
+    const __nv_bfloat16* Wg16 = tw16(h, A + "wg", static_cast<size_t>(d) * d);
+    const __nv_bfloat16* Wq16 = tw16(h, A + "wq", static_cast<size_t>(d) * d);
+    const __nv_bfloat16* Wk16 = tw16(h, A + "wk", static_cast<size_t>(d) * d);
+    const __nv_bfloat16* Wv16 = tw16(h, A + "wv", static_cast<size_t>(d) * d);
+    k_gate_fwd<__nv_bfloat16><<<ew_grid(nq), 256, 0, h.stream>>>(T.g, T.o_pre, nq, Hm);
+    k_f32_to_bf16<<<ew_grid(nq), 256, 0, h.stream>>>(dX, nq, dXr16);
+    gemm_rm16(h, true, false, d, d, M, Hm, d, dXr16, d, grad_ptr(h, A + "wo"), d, false);
+    gemm_rm16(h, false, true, M, d, d, dXr16, d, Wo16, d, dH, d, false);
     float* Dd = h.tw[15];
     k_gate_bwd_rows<<<warp_rows_grid(M), 256, 0, h.stream>>>(dH, T.g, T.o_pre, M, L.Rq, H, dk, dO, h.dO16, dgraw,
                                                              Dd);
-    float* xn = h.tw[2];
-    float* xq = h.tw[3];
+    __nv_bfloat16* xn = reinterpret_cast<__nv_bfloat16*>(h.tw[2]);
+    __nv_bfloat16* xq = reinterpret_cast<__nv_bfloat16*>(h.tw[3]);
     float* inv_a = h.tw[14] + static_cast<size_t>(h.train_B) * h.L0;
-    rms_rows<__nv_bfloat16>(h, T.x_in, w32(h, Bk + "attn_norm"), Mkv, d, xn, inv_a);
-    const float* xqp = xn;
+    if (d <= 256 && d % 8 == 0) {
+      k_rmsnorm_rows_v<__nv_bfloat16, __nv_bfloat16><<<std::max(1, std::min((Mkv + 7) / 8, 8 * h.num_sms)), 256, 0,
+                                                        h.stream>>>(T.x_in, w32(h, Bk + "attn_norm"), Mkv, d, xn,
+                                                                    inv_a);
+    } else {
+      k_rmsnorm_rows<__nv_bfloat16, __nv_bfloat16><<<(Mkv + 7) / 8, 256, 0, h.stream>>>(
+          T.x_in, w32(h, Bk + "attn_norm"), Mkv, d, nullptr, 1, 1, xn, inv_a);
+    }
+    const __nv_bfloat16* xqp = xn;
     if (!lp.q_identity) {
-      k_gather_f32<float><<<(M + 7) / 8, 256, 0, h.stream>>>(xn, L.query_rows, L.Rq, L.Rkv, M, d, xq);
+      k_gather_f32<__nv_bfloat16, __nv_bfloat16><<<(M + 7) / 8, 256, 0, h.stream>>>(xn, L.query_rows, L.Rq, L.Rkv,
+                                                                                    M, d, xq);
       xqp = xq;
     }
     check_launch("attention rows");
-    gemm_rm(h, true, false, d, d, M, xqp, d, dgraw, d, grad_ptr(h, A + "wg"), d);
-    float* dxq = h.tw[4];  // H no longer needed
-    gemm_rm(h, false, true, M, d, d, dgraw, d, w32(h, A + "wg"), d, dxq, d);
+    gemm_rm16(h, true, false, d, d, M, xqp, d, dgraw, d, grad_ptr(h, A + "wg"), d, false);
+    float* dxq = h.tw[4];  // (the gated output is no longer needed) -- fp32 [M, d]
+    gemm_rm16(h, false, true, M, d, d, dgraw, d, Wg16, d, dxq, d, false);
     // attention core
     AttnBwdArgs ab;
     ab.q = T.q;
@@ -1501,23 +1518,29 @@ static void backward_device(Handle& h, int B, const float* dz) {
     check_launch("attention core backward");
     // QKNorm + RoPE backward against recomputed raw projections
     float* raw = h.tw[11];
-    gemm_rm(h, false, false, M, d, d, xqp, d, w32(h, A + "wq"), d, raw, d);
+    __nv_bfloat16* dQ16 = reinterpret_cast<__nv_bfloat16*>(h.tw[12]);
+    __nv_bfloat16* dK16 = dQ16 + static_cast<size_t>(h.train_B) * h.L0 * d;
+    __nv_bfloat16* dV16 = dK16 + static_cast<size_t>(h.train_B) * h.L0 * d;
+    gemm_rm16(h, false, false, M, d, d, xqp, d, Wq16, d, raw, d, false);
     // persistent grid (register-held gain partials per warp, one smem reduction per CTA)
     const int qk_grid_q = std::max(1, std::min((M + 7) / 8, 4 * h.num_sms));
     k_qknorm_rope_bwd_v<1><<<qk_grid_q, 256, d * 4, h.stream>>>(dQ, raw, M, L.Rq, L.pos_q, h.rope, H, dk,
-                                                              w32(h, A + "qk_gain_q"), dQ, grad_ptr(h, A + "qk_gain_q"));
-    gemm_rm(h, false, false, Mkv, d, d, xn, d, w32(h, A + "wk"), d, raw, d);
+                                                              w32(h, A + "qk_gain_q"), dQ, grad_ptr(h, A + "qk_gain_q"),
+                                                              dQ16);
+    gemm_rm16(h, false, false, Mkv, d, d, xn, d, Wk16, d, raw, d, false);
     const int qk_grid_k = std::max(1, std::min((Mkv + 7) / 8, 4 * h.num_sms));
     k_qknorm_rope_bwd_v<1><<<qk_grid_k, 256, d * 4, h.stream>>>(dK, raw, Mkv, L.Rkv, L.pos_kv, h.rope, H, dk,
-                                                              w32(h, A + "qk_gain_k"), dK, grad_ptr(h, A + "qk_gain_k"));
+                                                              w32(h, A + "qk_gain_k"), dK, grad_ptr(h, A + "qk_gain_k"),
+                                                              dK16);
+    k_f32_to_bf16<<<ew_grid(nkv), 256, 0, h.stream>>>(dV, nkv, dV16);
     check_launch("qknorm/rope backward");
-    gemm_rm(h, true, false, d, d, M, xqp, d, dQ, d, grad_ptr(h, A + "wq"), d);
-    gemm_rm(h, true, false, d, d, Mkv, xn, d, dK, d, grad_ptr(h, A + "wk"), d);
-    gemm_rm(h, true, false, d, d, Mkv, xn, d, dV, d, grad_ptr(h, A + "wv"), d);
-    gemm_rm(h, false, true, M, d, d, dQ, d, w32(h, A + "wq"), d, dxq, d, 1.f);
+    gemm_rm16(h, true, false, d, d, M, xqp, d, dQ16, d, grad_ptr(h, A + "wq"), d, false);
+    gemm_rm16(h, true, false, d, d, Mkv, xn, d, dK16, d, grad_ptr(h, A + "wk"), d, false);
+    gemm_rm16(h, true, false, d, d, Mkv, xn, d, dV16, d, grad_ptr(h, A + "wv"), d, false);
+    gemm_rm16(h, false, true, M, d, d, dQ16, d, Wq16, d, dxq, d, false, 1.f);
     float* dxn = h.tw[5];
-    gemm_rm(h, false, true, Mkv, d, d, dK, d, w32(h, A + "wk"), d, dxn, d);
-    gemm_rm(h, false, true, Mkv, d, d, dV, d, w32(h, A + "wv"), d, dxn, d, 1.f);
+    gemm_rm16(h, false, true, Mkv, d, d, dK16, d, Wk16, d, dxn, d, false);
+    gemm_rm16(h, false, true, Mkv, d, d, dV16, d, Wv16, d, dxn, d, false, 1.f);
     k_scatter_add_rows<<<(M + 7) / 8, 256, 0, h.stream>>>(dxq, L.query_rows, B, L.Rq, L.Rkv, d, dxn);
     // d(x_in) = RMSN_bwd(dxn) + scatter of d(xr) through P(x, L_out)
     rms_bwd<__nv_bfloat16>(h, dxn, T.x_in, inv_a, w32(h, Bk + "attn_norm"), Mkv, d, dXn, 0,
@@ -1525,7 +1548,6 @@ static void backward_device(Handle& h, int B, const float* dz) {
     k_scatter_add_rows<<<(M + 7) / 8, 256, 0, h.stream>>>(dX, L.query_rows, B, L.Rq, L.Rkv, d, dXn);
     check_launch("attention backward");
     std::swap(dX, dXn);
-    (void)nkv;
   }
   h.dtokens = dX;
   // ---- Tokenizer::backward (tokenizer.cpp:286-352); the item table is frozen

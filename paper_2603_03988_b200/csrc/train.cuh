@@ -299,21 +299,22 @@ __global__ void k_swiglu_bwd(const float* __restrict__ dz, const float* __restri
 }
 
 // Gate (attention.cpp:124-127): H = G * O (recomputed for the Wo weight gradient). G, O bf16 [M, d].
+template <class T = float>
 __global__ void k_gate_fwd(const __nv_bfloat16* __restrict__ G, const __nv_bfloat16* __restrict__ O, size_t n,
-                           float* __restrict__ H) {
+                           T* __restrict__ H) {
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x)
-    H[i] = __bfloat162float(G[i]) * __bfloat162float(O[i]);
+    store_as(H + i, __bfloat162float(G[i]) * __bfloat162float(O[i]));
 }
 
 // Gate backward and the softmax row term in one pass (attention.cpp:124-131, 144-152, 169-172): per
 // row, dO = dH * g (fp32 and a bf16 copy for the tensor-core backward), d(g_raw) =
-// dH * o * g (1 - g), and D[bh, r] = <dO_head, O_head>. Warp per row, lane owns 8 contiguous
+// dH * o * g (1 - g) (bf16: a GEMM operand only), and D[bh, r] = <dO_head, O_head>. Warp per row, lane owns 8 contiguous
 // columns, a head = dk / 8 lanes (shuffle reduction). d <= 256.
 __global__ void __launch_bounds__(256) k_gate_bwd_rows(const float* __restrict__ dH, const __nv_bfloat16* __restrict__ G,
                                                        const __nv_bfloat16* __restrict__ O, int rows, int Rq, int H,
                                                        int dk, float* __restrict__ dO, __nv_bfloat16* __restrict__ dO16,
-                                                       float* __restrict__ dgraw, float* __restrict__ D) {
+                                                       __nv_bfloat16* __restrict__ dgraw, float* __restrict__ D) {
   const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (w >= rows) return;
   const int d = H * dk, c0 = lane * 8;
@@ -340,8 +341,8 @@ __global__ void __launch_bounds__(256) k_gate_bwd_rows(const float* __restrict__
     }
     reinterpret_cast<float4*>(dO + o)[0] = make_float4(dov[0], dov[1], dov[2], dov[3]);
     reinterpret_cast<float4*>(dO + o)[1] = make_float4(dov[4], dov[5], dov[6], dov[7]);
-    reinterpret_cast<float4*>(dgraw + o)[0] = make_float4(dgr[0], dgr[1], dgr[2], dgr[3]);
-    reinterpret_cast<float4*>(dgraw + o)[1] = make_float4(dgr[4], dgr[5], dgr[6], dgr[7]);
+    *reinterpret_cast<int4*>(dgraw + o) = make_int4(pack_bf16x2(dgr[0], dgr[1]), pack_bf16x2(dgr[2], dgr[3]),
+                                                    pack_bf16x2(dgr[4], dgr[5]), pack_bf16x2(dgr[6], dgr[7]));
     *reinterpret_cast<int4*>(dO16 + o) = make_int4(pk[0], pk[1], pk[2], pk[3]);
   }
   for (int off = dk / 16; off; off >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, off);
@@ -775,7 +776,7 @@ __global__ void __launch_bounds__(256) k_qknorm_rope_bwd_v(const float* drot, co
                                                            int rows, int R, const int32_t* __restrict__ pos,
                                                            const float2* __restrict__ rope_tab, int H, int dk,
                                                            const float* __restrict__ gain, float* draw,
-                                                           float* __restrict__ dgain) {
+                                                           float* __restrict__ dgain, __nv_bfloat16* __restrict__ draw16) {
   extern __shared__ float sg[];  // [H * dk]
   const int d = H * dk, d8 = d >> 3;
   for (int c = threadIdx.x; c < d; c += blockDim.x) sg[c] = 0.f;
@@ -844,6 +845,7 @@ __global__ void __launch_bounds__(256) k_qknorm_rope_bwd_v(const float* drot, co
         float4* op = reinterpret_cast<float4*>(draw + static_cast<size_t>(w) * d + c * 8);
         op[0] = make_float4(out[0], out[1], out[2], out[3]);
         op[1] = make_float4(out[4], out[5], out[6], out[7]);
+        if (draw16) store8(draw16 + static_cast<size_t>(w) * d + c * 8, out);
       }
     }
   }
