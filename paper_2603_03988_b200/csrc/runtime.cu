@@ -1319,12 +1319,14 @@ static void rms_rows(Handle& h, const T* x, const float* gain, int rows, int d, 
 }
 template <class T>
 static void rms_bwd(Handle& h, const float* dy, const T* x, const float* inv, const float* gain, int rows, int d,
-                    float* dx, int accum, float* dgain) {
-  if (d <= 256 && d % 8 == 0)
+                    float* dx, int accum, float* dgain, __nv_bfloat16* dx16 = nullptr) {
+  if (d <= 256 && d % 8 == 0) {
     k_rmsnorm_bwd_v<T><<<std::max(1, std::min((rows + 7) / 8, 4 * h.num_sms)), 256, d * 4, h.stream>>>(
-        dy, x, inv, gain, rows, d, dx, accum, dgain);
-  else
+        dy, x, inv, gain, rows, d, dx, accum, dgain, dx16);
+  } else {
     k_rmsnorm_bwd<T><<<(rows + 63) / 64, 256, d * 4, h.stream>>>(dy, x, inv, gain, rows, d, dx, accum, dgain);
+    if (dx16) k_f32_to_bf16<<<ew_grid(static_cast<size_t>(rows) * d), 256, 0, h.stream>>>(dx, static_cast<size_t>(rows) * d, dx16);
+  }
 }
 
 // Backward of one training forward; dz = dL/dlogits [B*N, 3] on the device.
@@ -1401,7 +1403,9 @@ static void backward_device(Handle& h, int B, const float* dz) {
     gemm_rm16(h, true, false, d, m, M, xf, d, dGU + m, 2 * m, grad_ptr(h, F + "w_up"), m, false);
     float* dxf = h.tw[3];
     gemm_rm16(h, false, true, M, d, 2 * m, dGU, 2 * m, Wgu, 2 * m, dxf, d, false);
-    rms_bwd<__nv_bfloat16>(h, dxf, T.x1, inv, w32(h, Bk + "ffn_norm"), M, d, dX, 1, grad_ptr(h, Bk + "ffn_norm"));
+    __nv_bfloat16* dXr16 = reinterpret_cast<__nv_bfloat16*>(h.tw[11]);  // d(xr) in bf16 for the next GEMMs
+    rms_bwd<__nv_bfloat16>(h, dxf, T.x1, inv, w32(h, Bk + "ffn_norm"), M, d, dX, 1, grad_ptr(h, Bk + "ffn_norm"),
+                           dXr16);
     check_launch("ffn backward");
     // attention (attention.cpp:134-202); dX now holds d(xr). GEMM operands in bf16 (fp32
     // accumulation and gradients): the gated output, d(xr), the normalised rows, d(g_raw),
@@ -1410,14 +1414,13 @@ static void backward_device(Handle& h, int B, const float* dz) {
     float* dH = h.tw[5];
     float* dO = h.tw[6];
     __nv_bfloat16* dgraw = reinterpret_cast<__nv_bfloat16*>(h.tw[7]);
-    __nv_bfloat16* dXr16 = reinterpret_cast<__nv_bfloat16*>(h.tw[11]);  // d(xr); (raw is recomputed later)
+
     const __nv_bfloat16* Wo16 = tw16(h, A + "wo", static_cast<size_t>(d) * d);
     const __nv_bfloat16* Wg16 = tw16(h, A + "wg", static_cast<size_t>(d) * d);
     const __nv_bfloat16* Wq16 = tw16(h, A + "wq", static_cast<size_t>(d) * d);
     const __nv_bfloat16* Wk16 = tw16(h, A + "wk", static_cast<size_t>(d) * d);
     const __nv_bfloat16* Wv16 = tw16(h, A + "wv", static_cast<size_t>(d) * d);
     k_gate_fwd<__nv_bfloat16><<<ew_grid(nq), 256, 0, h.stream>>>(T.g, T.o_pre, nq, Hm);
-    k_f32_to_bf16<<<ew_grid(nq), 256, 0, h.stream>>>(dX, nq, dXr16);
     gemm_rm16(h, true, false, d, d, M, Hm, d, dXr16, d, grad_ptr(h, A + "wo"), d, false);
     gemm_rm16(h, false, true, M, d, d, dXr16, d, Wo16, d, dH, d, false);
     float* Dd = h.tw[15];
@@ -1484,6 +1487,7 @@ static void backward_device(Handle& h, int B, const float* dz) {
       am.dq = dQ;
       am.dk = dK;
       am.dv = dV;
+      am.dv16 = reinterpret_cast<__nv_bfloat16*>(h.tw[12]) + 2 * static_cast<size_t>(h.train_B) * h.L0 * d;
       am.H = H;
       am.Rq = L.Rq;
       am.Rkv = L.Rkv;
@@ -1532,7 +1536,7 @@ static void backward_device(Handle& h, int B, const float* dz) {
     k_qknorm_rope_bwd_v<1><<<qk_grid_k, 256, d * 4, h.stream>>>(dK, raw, Mkv, L.Rkv, L.pos_kv, h.rope, H, dk,
                                                               w32(h, A + "qk_gain_k"), dK, grad_ptr(h, A + "qk_gain_k"),
                                                               dK16);
-    k_f32_to_bf16<<<ew_grid(nkv), 256, 0, h.stream>>>(dV, nkv, dV16);
+    if (!h.attn_bwd_mma) k_f32_to_bf16<<<ew_grid(nkv), 256, 0, h.stream>>>(dV, nkv, dV16);  // (SIMT path)
     check_launch("qknorm/rope backward");
     gemm_rm16(h, true, false, d, d, M, xqp, d, dQ16, d, grad_ptr(h, A + "wq"), d, false);
     gemm_rm16(h, true, false, d, d, Mkv, xn, d, dK16, d, grad_ptr(h, A + "wk"), d, false);

@@ -171,7 +171,7 @@ template <class T>
 __global__ void __launch_bounds__(256) k_rmsnorm_bwd_v(const float* __restrict__ dy, const T* __restrict__ x,
                                                        const float* __restrict__ inv, const float* __restrict__ gain,
                                                        int rows, int d, float* __restrict__ dx, int accum,
-                                                       float* __restrict__ dgain) {
+                                                       float* __restrict__ dgain, __nv_bfloat16* __restrict__ dx16) {
   extern __shared__ float sg[];  // [d]
   for (int c = threadIdx.x; c < d; c += blockDim.x) sg[c] = 0.f;
   __syncthreads();
@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(256) k_rmsnorm_bwd_v(const float* __restrict__
         o[k] = accum ? o[k] + v : v;
       }
       store8(dxr, o);
+      if (dx16) store8(dx16 + static_cast<size_t>(r) * d + c0, o);  // bf16 copy (a GEMM operand)
     }
   }
   if (act)
@@ -548,6 +549,7 @@ struct AttnBwdMmaArgs {
   const int32_t* qb_off;           // CSR over 64-row kv blocks -> 64-row q blocks
   const int32_t* qb_list;
   float *dq, *dk, *dv;             // dq zeroed by the caller; dk/dv written
+  __nv_bfloat16* dv16;             // optional bf16 copy of dv (a GEMM operand)
   int H, Rq, Rkv;
   float scale_log2, scale;
 };
@@ -759,6 +761,7 @@ __global__ void __launch_bounds__(128, 4) k_attn_bwd_mma(const AttnBwdMmaArgs a)
         const size_t o = (static_cast<size_t>(b) * a.Rkv + kv) * a.H * DK + h * DK + n * 8 + 2 * t4;
         *reinterpret_cast<float2*>(a.dk + o) = make_float2(dk[n][2 * e2] * a.scale, dk[n][2 * e2 + 1] * a.scale);
         *reinterpret_cast<float2*>(a.dv + o) = make_float2(dv[n][2 * e2], dv[n][2 * e2 + 1]);
+        if (a.dv16) *reinterpret_cast<uint32_t*>(a.dv16 + o) = pack_bf16x2(dv[n][2 * e2], dv[n][2 * e2 + 1]);
       }
     }
 }
