@@ -1394,11 +1394,11 @@ static void backward_device(Handle& h, int B, const float* dz) {
           T.x1, w32(h, Bk + "ffn_norm"), M, d, nullptr, 1, 1, xf, inv);
     }
     gemm_rm16(h, false, false, M, 2 * m, d, xf, d, Wgu, 2 * m, GU, 2 * m, true);
-    k_swiglu_z<__nv_bfloat16, __nv_bfloat16><<<std::min(M, 148 * 16), 256, 0, h.stream>>>(GU, M, m, z);
+    k_swiglu_z<__nv_bfloat16, __nv_bfloat16><<<ew_grid(static_cast<size_t>(M) * m / 8), 256, 0, h.stream>>>(GU, M, m, z);
     k_f32_to_bf16<<<ew_grid(nq), 256, 0, h.stream>>>(dX, nq, dX16);
     gemm_rm16(h, true, false, m, d, M, z, m, dX16, d, grad_ptr(h, F + "w_down"), d, false);
     gemm_rm16(h, false, true, M, m, d, dX16, d, Wdn, d, z, m, true);  // z <- dz
-    k_swiglu_bwd16<<<std::min(M, 148 * 16), 256, 0, h.stream>>>(z, GU, M, m, dGU);
+    k_swiglu_bwd16<<<ew_grid(static_cast<size_t>(M) * m / 8), 256, 0, h.stream>>>(z, GU, M, m, dGU);
     gemm_rm16(h, true, false, d, m, M, xf, d, dGU, 2 * m, grad_ptr(h, F + "w_gate"), m, false);
     gemm_rm16(h, true, false, d, m, M, xf, d, dGU + m, 2 * m, grad_ptr(h, F + "w_up"), m, false);
     float* dxf = h.tw[3];
@@ -1736,7 +1736,7 @@ static void forward_generic(Handle& h, int B) {
     __nv_bfloat16* gu = reinterpret_cast<__nv_bfloat16*>(h.gw[6]);  // bf16 [gate | up] pre-activations
     gemm_rm_bf16(h, M, 2 * m, d, xf, d, w16(h, F + "w_gu"), 2 * m, gu, 2 * m, 0.f, true);
     __nv_bfloat16* z = reinterpret_cast<__nv_bfloat16*>(h.gw[7]);
-    k_swiglu_z<__nv_bfloat16, __nv_bfloat16><<<std::min(M, 148 * 16), 256, 0, h.stream>>>(gu, M, m, z);
+    k_swiglu_z<__nv_bfloat16, __nv_bfloat16><<<ew_grid(static_cast<size_t>(M) * m / 8), 256, 0, h.stream>>>(gu, M, m, z);
     gemm_rm_bf16(h, M, d, m, z, m, w16(h, F + "w_down"), d, xo, d, 1.f);
     check_launch("generic block tail");
     stage_mark(h, "L" + sl + ".tail");

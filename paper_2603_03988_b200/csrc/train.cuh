@@ -233,26 +233,28 @@ __global__ void k_swiglu_z(const I* __restrict__ gu, int M, int m, O* __restrict
     }
   }
 }
-// bf16 -> bf16 form with 16-byte vectors (m % 8 == 0): the HBM-bound case of the generic path
+// bf16 -> bf16 form with 16-byte vectors (m % 8 == 0): the HBM-bound case. The (row, vector)
+// pairs are flattened over the grid so every thread has work whatever m is.
 template <>
 __global__ void k_swiglu_z<__nv_bfloat16, __nv_bfloat16>(const __nv_bfloat16* __restrict__ gu, int M, int m,
                                                          __nv_bfloat16* __restrict__ z) {
   const int m8 = m / 8;
-  for (int r = blockIdx.x; r < M; r += gridDim.x) {
-    const int4* gr = reinterpret_cast<const int4*>(gu + static_cast<size_t>(r) * 2 * m);
-    int4* zr = reinterpret_cast<int4*>(z + static_cast<size_t>(r) * m);
-    for (int j = threadIdx.x; j < m8; j += blockDim.x) {
-      const int4 gv = gr[j], uv = gr[m8 + j];
-      const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gv);
-      const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&uv);
-      uint32_t o[4];
+  const size_t total = static_cast<size_t>(M) * m8;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t r = i / m8;
+    const int j = static_cast<int>(i - r * m8);
+    const int4* gr = reinterpret_cast<const int4*>(gu + r * 2 * m);
+    const int4 gv = gr[j], uv = gr[m8 + j];
+    const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gv);
+    const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&uv);
+    uint32_t o[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 g = __bfloat1622float2(g2[e]), u = __bfloat1622float2(u2[e]);
-        o[e] = pack_bf16x2(g.x * sigmoid_f(g.x) * u.x, g.y * sigmoid_f(g.y) * u.y);
-      }
-      zr[j] = make_int4(o[0], o[1], o[2], o[3]);
+    for (int e = 0; e < 4; ++e) {
+      const float2 g = __bfloat1622float2(g2[e]), u = __bfloat1622float2(u2[e]);
+      o[e] = pack_bf16x2(g.x * sigmoid_f(g.x) * u.x, g.y * sigmoid_f(g.y) * u.y);
     }
+    reinterpret_cast<int4*>(z + r * m)[j] = make_int4(o[0], o[1], o[2], o[3]);
   }
 }
 // bf16 form of k_swiglu_bwd (16-byte vectors, m % 8 == 0): the training FFN backward keeps its
@@ -260,26 +262,27 @@ __global__ void k_swiglu_z<__nv_bfloat16, __nv_bfloat16>(const __nv_bfloat16* __
 __global__ void k_swiglu_bwd16(const __nv_bfloat16* __restrict__ dz, const __nv_bfloat16* __restrict__ gu, int M,
                                int m, __nv_bfloat16* __restrict__ dgu) {
   const int m8 = m / 8;
-  for (int r = blockIdx.x; r < M; r += gridDim.x) {
-    const int4* gr = reinterpret_cast<const int4*>(gu + static_cast<size_t>(r) * 2 * m);
-    const int4* dzr = reinterpret_cast<const int4*>(dz + static_cast<size_t>(r) * m);
-    int4* o = reinterpret_cast<int4*>(dgu + static_cast<size_t>(r) * 2 * m);
-    for (int j = threadIdx.x; j < m8; j += blockDim.x) {
-      const int4 gv = gr[j], uv = gr[m8 + j], dv = dzr[j];
-      const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gv);
-      const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&uv);
-      const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&dv);
-      uint32_t og[4], ou[4];
+  const size_t total = static_cast<size_t>(M) * m8;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t r = i / m8;
+    const int j = static_cast<int>(i - r * m8);
+    const int4* gr = reinterpret_cast<const int4*>(gu + r * 2 * m);
+    const int4 gv = gr[j], uv = gr[m8 + j], dv = reinterpret_cast<const int4*>(dz + r * m)[j];
+    const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gv);
+    const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&uv);
+    const __nv_bfloat162* d2 = reinterpret_cast<const __nv_bfloat162*>(&dv);
+    uint32_t og[4], ou[4];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 g = __bfloat1622float2(g2[e]), u = __bfloat1622float2(u2[e]), dzv = __bfloat1622float2(d2[e]);
-        const float sx = sigmoid_f(g.x), sy = sigmoid_f(g.y);
-        og[e] = pack_bf16x2(dzv.x * u.x * sx * (1.f + g.x * (1.f - sx)), dzv.y * u.y * sy * (1.f + g.y * (1.f - sy)));
-        ou[e] = pack_bf16x2(dzv.x * g.x * sx, dzv.y * g.y * sy);
-      }
-      o[j] = make_int4(og[0], og[1], og[2], og[3]);
-      o[m8 + j] = make_int4(ou[0], ou[1], ou[2], ou[3]);
+    for (int e = 0; e < 4; ++e) {
+      const float2 g = __bfloat1622float2(g2[e]), u = __bfloat1622float2(u2[e]), dzv = __bfloat1622float2(d2[e]);
+      const float sx = sigmoid_f(g.x), sy = sigmoid_f(g.y);
+      og[e] = pack_bf16x2(dzv.x * u.x * sx * (1.f + g.x * (1.f - sx)), dzv.y * u.y * sy * (1.f + g.y * (1.f - sy)));
+      ou[e] = pack_bf16x2(dzv.x * g.x * sx, dzv.y * g.y * sy);
     }
+    int4* o = reinterpret_cast<int4*>(dgu + r * 2 * m);
+    o[j] = make_int4(og[0], og[1], og[2], og[3]);
+    o[m8 + j] = make_int4(ou[0], ou[1], ou[2], ou[3]);
   }
 }
 
