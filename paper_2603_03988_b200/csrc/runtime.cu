@@ -1355,11 +1355,11 @@ static void backward_device(Handle& h, int B, const float* dz) {
   gemm_rm(h, false, false, BN, dh, d, xh, d, w32(h, "head.w1"), dh, hid, dh);
   k_bias_relu<<<ew_grid(static_cast<size_t>(BN) * dh), 256, 0, h.stream>>>(hid, w32(h, "head.b1"), BN, dh);
   gemm_rm(h, true, false, dh, 3, BN, hid, dh, dz, 3, grad_ptr(h, "head.w2"), 3);
-  k_colsum<<<dim3(1, 64), 32, 0, h.stream>>>(dz, BN, 3, grad_ptr(h, "head.b2"));
+  k_colsum<<<dim3(1, 64), dim3(32, 8), 0, h.stream>>>(dz, BN, 3, grad_ptr(h, "head.b2"));
   gemm_rm(h, false, true, BN, dh, 3, dz, 3, w32(h, "head.w2"), 3, dhid, dh);
   k_relu_mask<<<ew_grid(static_cast<size_t>(BN) * dh), 256, 0, h.stream>>>(dhid, hid, static_cast<size_t>(BN) * dh);
   gemm_rm(h, true, false, d, dh, BN, xh, d, dhid, dh, grad_ptr(h, "head.w1"), dh);
-  k_colsum<<<dim3((dh + 31) / 32, std::min(1024, (BN + 63) / 64)), 32, 0, h.stream>>>(dhid, BN, dh,
+  k_colsum<<<dim3((dh + 31) / 32, std::min(148, (BN + 255) / 256)), dim3(32, 8), 0, h.stream>>>(dhid, BN, dh,
                                                                                     grad_ptr(h, "head.b1"));
   float* dxh = h.tw[4];
   gemm_rm(h, false, true, BN, d, dh, dhid, dh, w32(h, "head.w1"), dh, dxh, d);
@@ -1579,7 +1579,7 @@ static void backward_device(Handle& h, int B, const float* dz) {
     rms_bwd<float>(h, dy, y, inv, w32(h, std::string("tok.g_") + gname[g]), n, d, dproj, 0,
                    grad_ptr(h, std::string("tok.g_") + gname[g]));
     gemm_rm(h, true, false, K, d, n, catf, K, dproj, d, grad_ptr(h, W), d);
-    k_colsum<<<dim3((d + 31) / 32, std::min(1024, (n + 63) / 64)), 32, 0, h.stream>>>(
+    k_colsum<<<dim3((d + 31) / 32, std::min(148, (n + 255) / 256)), dim3(32, 8), 0, h.stream>>>(
         dproj, n, d, grad_ptr(h, std::string("tok.b_") + gname[g]));
     if (g == 1) continue;  // candidates gather only the frozen item table
     gemm_rm(h, false, true, n, K, d, dproj, d, w32(h, W), d, dcat, K);

@@ -890,12 +890,26 @@ __global__ void k_scatter_add_rows(const float* __restrict__ src, const int32_t*
 }
 
 // Column sums: out[c] += sum_r a[r, c] (bias gradients).
-__global__ void k_colsum(const float* __restrict__ a, int rows, int cols, float* __restrict__ out) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= cols) return;
-  float s = 0.f;
-  for (int r = blockIdx.y; r < rows; r += gridDim.y) s += a[static_cast<size_t>(r) * cols + c];
-  atomicAdd(&out[c], s);
+// Block (32, 8): 32 columns x 8 row lanes, 4 independent partial sums per thread, the 8 row
+// lanes combined in shared memory, one atomic per column per block.
+__global__ void __launch_bounds__(256) k_colsum(const float* __restrict__ a, int rows, int cols,
+                                                float* __restrict__ out) {
+  __shared__ float red[8][33];
+  const int c = blockIdx.x * 32 + threadIdx.x;
+  const int r0 = blockIdx.y * 8 + threadIdx.y, rs = gridDim.y * 8;
+  float s[4] = {0.f, 0.f, 0.f, 0.f};
+  if (c < cols) {
+    int r = r0, k = 0;
+    for (; r < rows; r += rs, k = (k + 1) & 3) s[k] += a[static_cast<size_t>(r) * cols + c];
+  }
+  red[threadIdx.y][threadIdx.x] = (s[0] + s[1]) + (s[2] + s[3]);
+  __syncthreads();
+  if (threadIdx.y == 0 && c < cols) {
+    float t = 0.f;
+#pragma unroll
+    for (int y = 0; y < 8; ++y) t += red[y][threadIdx.x];
+    atomicAdd(&out[c], t);
+  }
 }
 
 // ---------------------------------------------------------------- tokenizer backward
