@@ -1285,7 +1285,11 @@ static void ensure_train_buffers(Handle& h, int B) {
           for (int r = qb * 64; r < std::min(lp.l_q, qb * 64 + 64) && !any; ++r)
             any = (lp.hi[r] >= lp.lo[r] && lp.lo[r] <= c1 && lp.hi[r] >= c0) ||
                   (lp.self_idx[r] >= c0 && lp.self_idx[r] <= c1);
-          if (any) lst.push_back(qb);
+          if (!any) continue;
+          // every (q, kv) of the 64 x 64 block visible and in range: no per-element mask
+          bool full = qb * 64 + 64 <= lp.l_q && c0 + 64 <= lp.l_kv;
+          for (int r = qb * 64; r < qb * 64 + 64 && full; ++r) full = lp.lo[r] <= c0 && lp.hi[r] >= c1;
+          lst.push_back(full ? (qb | static_cast<int32_t>(0x40000000)) : qb);
         }
         off.push_back(static_cast<int32_t>(lst.size()));
       }

@@ -603,7 +603,7 @@ __global__ void __launch_bounds__(128, 4) k_attn_bwd_mma(const AttnBwdMmaArgs a)
   };
   const int it0 = a.qb_off[kvb], it1 = a.qb_off[kvb + 1];
   auto stage = [&](int it, int buf) {
-    const int r0 = a.qb_list[it] * 64;
+    const int r0 = (a.qb_list[it] & 0x3fffffff) * 64;
     for (int i = tid; i < 64 * (DK / 8); i += 128) {
       const int r = i / (DK / 8), cc = i % (DK / 8);
       const bool ok = r0 + r < a.Rq;
@@ -641,7 +641,9 @@ __global__ void __launch_bounds__(128, 4) k_attn_bwd_mma(const AttnBwdMmaArgs a)
   const int kv_lo = c0 + warp * 16 + g;  // this thread's two kv rows: kv_lo, kv_lo + 8
   for (int it = it0; it < it1; ++it) {
     const int buf = (it - it0) % NBUF;
-    const int r0 = a.qb_list[it] * 64;
+    const int qbe = a.qb_list[it];
+    const int r0 = (qbe & 0x3fffffff) * 64;
+    const bool full = (qbe & 0x40000000) != 0;  // the whole 64 x 64 block is visible (host plan)
     __syncthreads();  // previous iteration done with sS and with the other buffer
     if constexpr (NBUF == 2) {
       if (it + 1 < it1) {
@@ -692,8 +694,11 @@ __global__ void __launch_bounds__(128, 4) k_attn_bwd_mma(const AttnBwdMmaArgs a)
       for (int e = 0; e < 4; ++e) {
         const int q = n * 8 + 2 * t4 + (e & 1);
         const int kv = kv_lo + ((e >> 1) << 3);
-        const int4 m = sM[q];
-        const bool vis = kv < a.Rkv && ((kv >= m.x && kv <= m.y) || kv == m.z);
+        bool vis = true;
+        if (!full) {
+          const int4 m = sM[q];
+          vis = kv < a.Rkv && ((kv >= m.x && kv <= m.y) || kv == m.z);
+        }
         p[e] = vis ? ex2_approx(st[n][e] * a.scale_log2 - sL[q]) : 0.f;  // argument <= 0 (P <= 1)
         ds[e] = p[e] * (dp[n][e] - sD[q]);
       }
