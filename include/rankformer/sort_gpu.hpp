@@ -194,23 +194,80 @@ class Model {
   // model_forward for every request: {p_click, p_cart, p_purchase} per candidate. Requests
   // are packed AoS -> SoA and scored in GPU batches of the planned geometry (n_hist, n_cand);
   // a request with another geometry is a ConfigError (issue it through a Model planned for it).
+  // Batches go through the pipelined serving path (sort_forward_async: each batch's host ->
+  // device copy overlaps the previous batch's kernels), one sync at the end.
   std::vector<std::vector<std::array<float, 3>>> score(const std::vector<RequestSample>& reqs) {
     std::vector<std::vector<std::array<float, 3>>> out(reqs.size());
+    std::vector<Packed> packs;
+    std::vector<std::vector<float>> scores;
+    std::vector<size_t> first;
     for (size_t b0 = 0; b0 < reqs.size(); b0 += static_cast<size_t>(cfg_.max_batch)) {
       const size_t nb = std::min(reqs.size() - b0, static_cast<size_t>(cfg_.max_batch));
-      Packed p = pack(reqs, b0, nb);
-      std::vector<float> scores(nb * static_cast<size_t>(cfg_.n_cand) * 3);
-      check(sort_forward(h_, &p.batch, 0, scores.data(), 0));
+      packs.push_back(pack(reqs, b0, nb));
+      scores.emplace_back(nb * static_cast<size_t>(cfg_.n_cand) * 3);
+      first.push_back(b0);
+    }
+    for (size_t k = 0; k < packs.size(); ++k) {
+      packs[k].batch = bind(packs[k]);  // (vectors moved into the list: re-point the SoA batch)
+      check(sort_forward_async(h_, &packs[k].batch, scores[k].data()));
+    }
+    check(sort_sync(h_));
+    for (size_t k = 0; k < packs.size(); ++k) {
+      const size_t nb = static_cast<size_t>(packs[k].batch.batch);
       for (size_t i = 0; i < nb; ++i) {
-        out[b0 + i].resize(static_cast<size_t>(cfg_.n_cand));
+        auto& o = out[first[k] + i];
+        o.resize(static_cast<size_t>(cfg_.n_cand));
         for (int j = 0; j < cfg_.n_cand; ++j)
-          for (int o = 0; o < 3; ++o)
-            out[b0 + i][static_cast<size_t>(j)][static_cast<size_t>(o)] =
-                scores[(i * static_cast<size_t>(cfg_.n_cand) + static_cast<size_t>(j)) * 3 + static_cast<size_t>(o)];
+          for (int q = 0; q < 3; ++q)
+            o[static_cast<size_t>(j)][static_cast<size_t>(q)] =
+                scores[k][(i * static_cast<size_t>(cfg_.n_cand) + static_cast<size_t>(j)) * 3 + static_cast<size_t>(q)];
       }
     }
     return out;
   }
+
+  // pretrain_forward (cfg.pretrain = 1): for every click sequence of
+  // cfg.n_hist clicks, the next-item cross entropy of each position (lse - target logit).
+  std::vector<std::vector<float>> pretrain_ce(const std::vector<std::vector<ItemEvent>>& seqs) {
+    std::vector<std::vector<float>> out(seqs.size());
+    for (size_t b0 = 0; b0 < seqs.size(); b0 += static_cast<size_t>(cfg_.max_batch)) {
+      const size_t nb = std::min(seqs.size() - b0, static_cast<size_t>(cfg_.max_batch));
+      Packed p;
+      for (size_t i = b0; i < b0 + nb; ++i) {
+        if (static_cast<int>(seqs[i].size()) != cfg_.n_hist)
+          throw ConfigError("click sequence length differs from the planned n_hist");
+        for (const ItemEvent& e : seqs[i]) {
+          p.item.push_back(e.item_id);
+          p.action.push_back(static_cast<int32_t>(e.action_type));
+          p.scene.push_back(e.scene_id);
+          p.ts.push_back(e.timestamp);
+        }
+        p.req.push_back(0);
+      }
+      p.batch = bind(p);
+      p.batch.batch = static_cast<int32_t>(nb);
+      const size_t n = nb * static_cast<size_t>(cfg_.n_hist);
+      std::vector<float> lse(n), tgt(n);
+      check(sort_pretrain_forward(h_, &p.batch, 0, lse.data(), tgt.data(), 0));
+      for (size_t i = 0; i < nb; ++i) {
+        out[b0 + i].resize(static_cast<size_t>(cfg_.n_hist));
+        for (int t = 0; t < cfg_.n_hist; ++t) {
+          const size_t k = i * static_cast<size_t>(cfg_.n_hist) + static_cast<size_t>(t);
+          out[b0 + i][static_cast<size_t>(t)] = lse[k] - tgt[k];
+        }
+      }
+    }
+    return out;
+  }
+
+  // MoE FFN (cfg.moe_experts > 0): expert loads of `layer` in the last
+  // forward, and update_balance (router_bias_e -= gamma * sign(load_e - mean)) on every layer.
+  std::vector<int64_t> moe_load(int layer) {
+    std::vector<int64_t> load(static_cast<size_t>(cfg_.moe_experts));
+    check(sort_moe_load(h_, layer, load.data()));
+    return load;
+  }
+  void moe_update_bias(double gamma = 1e-3) { check(sort_moe_update_bias(h_, gamma)); }
 
   // Tokenizer::tokenize_sample (tokenizer.hpp:84) of one request.
   TokenSequence tokenize_sample(const RequestSample& s) {
@@ -230,6 +287,7 @@ class Model {
   }
 
   int seq_len() const {
+    if (cfg_.pretrain) return 1 + cfg_.n_hist;  // [BOS; clicks]
     return (cfg_.special_tokens ? 3 : 0) + cfg_.n_hist + cfg_.n_profile_fields + cfg_.n_cand;
   }
   SortHandle handle() const { return h_; }
@@ -240,6 +298,18 @@ class Model {
     std::vector<int64_t> ts, req;
     SortBatch batch{};
   };
+  // the SoA batch over a Packed's arrays (after the Packed was moved into a container)
+  static SortBatch bind(const Packed& p) {
+    SortBatch b = p.batch;
+    b.hist_item = p.item.data();
+    b.hist_action = p.action.data();
+    b.hist_scene = p.scene.data();
+    b.hist_ts = p.ts.data();
+    b.req_ts = p.req.data();
+    b.profile = p.prof.data();
+    b.cand_item = p.cand.data();
+    return b;
+  }
   Packed pack(const std::vector<RequestSample>& reqs, size_t b0, size_t nb) const {
     Packed p;
     for (size_t i = b0; i < b0 + nb; ++i) {

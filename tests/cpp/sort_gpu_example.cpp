@@ -68,6 +68,19 @@ int main(int argc, char** argv) {
   if (t.length() != 278 || t.position_ids.back() != 262) { std::puts("tokenize mismatch"); return 1; }
   const float p0 = scores[0][0][0];
   if (!(p0 > 0.f && p0 < 1.f)) { std::puts("bad score"); return 1; }
+  // five requests = three batches of max_batch 2 through the pipelined path: each request's
+  // scores equal its single-request scores
+  std::vector<RequestSample> many;
+  for (int k = 0; k < 5; ++k) {
+    RequestSample r = s;
+    for (auto& cnd : r.candidates) cnd.item_id = (cnd.item_id + 17 * k) % 5000;
+    many.push_back(r);
+  }
+  auto multi = model.score(many);
+  for (int k = 0; k < 5; ++k) {
+    auto single = model.score({many[static_cast<size_t>(k)]});
+    if (single[0] != multi[static_cast<size_t>(k)]) { std::puts("pipelined batch mismatch"); return 1; }
+  }
   s.candidates[3].item_id = 5000;  // OOV -> ConfigError (tokenizer.cpp:14-19)
   threw = false;
   try { model.score({s}); } catch (const ConfigError&) { threw = true; }
