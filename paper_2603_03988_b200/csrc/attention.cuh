@@ -47,6 +47,10 @@ constexpr int kKvStages = 4;
 #ifndef SORT_ATTN_POLY_EVERY
 #define SORT_ATTN_POLY_EVERY 3
 #endif
+#ifndef SORT_ATTN_FOLD_AT
+#define SORT_ATTN_FOLD_AT 1
+#endif
+constexpr int kFoldAt = SORT_ATTN_FOLD_AT;  // where the previous tile's O is folded (see loop)
 constexpr int kPolyEvery = SORT_ATTN_POLY_EVERY;  // exp2 offload ratio in fully visible chunks         // K/V tile ring depth: loads run ~3 tiles ahead of PV
 
 template <int DK>
@@ -382,6 +386,17 @@ __global__ void __launch_bounds__(kAttnThreads, AttnTmem<DK>::kCtasPerSm)
           m = m_new;
         }
         const float2 nref = make_float2(-ref, -ref);
+        // Fold O of the previous tile (kFoldAt: 0 before the first chunk, 1 between the two
+        // chunks, 2 after both). On an item's first tile that O is the previous item's last:
+        // finish that item here.
+        auto fold_prev = [&]() {
+          if (j > 0) {
+            fold_o(g - 1, alpha_prev_fold);
+          } else if (has_prev) {
+            finish_item(g - 1, alpha_prev_fold, li - 1, true);
+          }
+        };
+        if (kFoldAt == 0) fold_prev();
 #pragma unroll
         for (int cb = 0; cb < 2; ++cb) {
           uint32_t w[16];
@@ -420,17 +435,11 @@ __global__ void __launch_bounds__(kAttnThreads, AttnTmem<DK>::kCtasPerSm)
           }
           // P of columns [cb*32, +32) of this half -> 16 bf16x2 columns, in place over S
           tmem_st_32x32b_x16(tSh + cb * 16, w);
-          // Fold O of the previous tile between the two chunks: its PV has had a full chunk
-          // to finish, and releasing its buffer now still gives QK^T(g+1) half a tile of lead.
-          // On an item's first tile that O is the previous item's last: finish that item here.
-          if (cb == 0) {
-            if (j > 0) {
-              fold_o(g - 1, alpha_prev_fold);
-            } else if (has_prev) {
-              finish_item(g - 1, alpha_prev_fold, li - 1, true);
-            }
-          }
+          // Default: fold between the two chunks: its PV has had a full chunk to finish, and
+          // releasing its buffer now still gives QK^T(g+1) half a tile of lead.
+          if (kFoldAt == 1 && cb == 0) fold_prev();
         }
+        if (kFoldAt == 2) fold_prev();
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&p_full[buf]);
