@@ -51,7 +51,15 @@ constexpr int kKvStages = 4;
 #define SORT_ATTN_FOLD_AT 1
 #endif
 constexpr int kFoldAt = SORT_ATTN_FOLD_AT;  // where the previous tile's O is folded (see loop)
-constexpr int kPolyEvery = SORT_ATTN_POLY_EVERY;  // exp2 offload ratio in fully visible chunks         // K/V tile ring depth: loads run ~3 tiles ahead of PV
+#ifndef SORT_ATTN_MMA_ROWSUM
+#define SORT_ATTN_MMA_ROWSUM 0
+#endif
+// Option (default off: measured equal on the same box, tools/ab_rowsum.sh): row sums of P
+// on the tensor core, P * ones[128 x 16] into the tile's free TMEM columns [96, 112) (after
+// P(g) is written, S columns 96..127 are consumed), so the softmax warps add no FADDs per
+// element and the two half-row warps need no sum exchange.
+constexpr bool kMmaRowSum = SORT_ATTN_MMA_ROWSUM != 0;
+constexpr int kPolyEvery = SORT_ATTN_POLY_EVERY;  // exp2 offload ratio in fully visible chunks
 
 template <int DK>
 struct AttnSmem {
@@ -60,7 +68,8 @@ struct AttnSmem {
   static constexpr uint32_t oQ = 0;
   static constexpr uint32_t oK = oQ + 2 * kStride;
   static constexpr uint32_t oV = oK + kKvStages * kStride;
-  static constexpr uint32_t oBar = oV + kKvStages * kStride;
+  static constexpr uint32_t oOnes = oV + kKvStages * kStride;  // 16 x 16 bf16 ones, K-major SW32
+  static constexpr uint32_t oBar = oOnes + 1024;
   static constexpr uint32_t oRed = oBar + 32 * 8;      // softmax cross-warp reduction scratch
   static constexpr uint32_t oGate = oRed + 3 * 1024;   // [2 items][2 halves][128 rows][DK/2] bf16
   static constexpr uint32_t oTiles = oGate + 2 * 128 * DK * 2;  // int32 tile tables follow
@@ -128,6 +137,11 @@ __global__ void __launch_bounds__(kAttnThreads, AttnTmem<DK>::kCtasPerSm)
   for (int i = threadIdx.x; i <= a.n_qtiles; i += kAttnThreads) s_off[i] = a.tile_off[i];
   for (int i = threadIdx.x; i < a.n_qtiles; i += kAttnThreads) s_order[i] = a.qtile_order[i];
   for (int i = threadIdx.x; i < a.n_codes; i += kAttnThreads) s_code[i] = a.tile_code[i];
+  if (kMmaRowSum) {
+    for (int i = threadIdx.x; i < 128; i += kAttnThreads)
+      reinterpret_cast<uint32_t*>(smem + S::oOnes)[i] = 0x3F803F80u;  // bf16 pair (1, 1)
+    fence_proxy_async_smem();  // generic-proxy stores -> tcgen05.mma operand reads
+  }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmQ);
     tma_prefetch_desc(&tmK);
@@ -186,6 +200,7 @@ __global__ void __launch_bounds__(kAttnThreads, AttnTmem<DK>::kCtasPerSm)
     if (lane == 0) {
       const uint32_t id_s = umma_idesc_bf16(128, 64);
       const uint32_t id_o = umma_idesc_bf16(128, DK) | (1u << 16);  // B = V, MN-major
+      const uint32_t id_l = umma_idesc_bf16(128, 16);                  // B = ones, K-major
       constexpr uint32_t sw = DK * 2;  // Q/K/V rows are DK*2 bytes = the swizzle span
       struct Cur {
         int it, li, j, n_t, g;
@@ -239,6 +254,14 @@ __global__ void __launch_bounds__(kAttnThreads, AttnTmem<DK>::kCtasPerSm)
           const uint32_t va = sv + kk * 16 * (DK * 2);           // V rows, MN-major, SBO = 8 rows
           mma_bf16_ts(tmem + AttnTmem<DK>::o_col(buf), pa, umma_sdesc_kmajor(va, sw), id_o, kk != 0 ? 1u : 0u);
         }
+        if (kMmaRowSum) {  // row sums of P(g): D[m][n] = sum_k P[m][k] for all 16 n
+          const uint64_t ones = umma_sdesc_kmajor(smem_u32(smem + S::oOnes), 32);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t pa = tb + (kk >> 2) * 64 + (kk & 3) * 8;
+            mma_bf16_ts(tb + 96, pa, ones, id_l, kk != 0 ? 1u : 0u);
+          }
+        }
         mma_commit(&pv_done[buf]);
         mma_commit(&kv_empty[st]);
         cur = nx;
@@ -257,7 +280,8 @@ __global__ void __launch_bounds__(kAttnThreads, AttnTmem<DK>::kCtasPerSm)
     float* s_red = reinterpret_cast<float*>(smem + S::oRed);  // [2][2][128] maxima, [2][128] sums
     int g = 0, li = 0;
     float m = NEG_INF, alpha_prev = 1.f, alpha_prev_fold = 1.f;  // online mode only
-    float2 lsum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+    float2 lsum[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};  // FMA-pipe row sums
+    float lacc = 0.f;                                                   // MMA row sums (folded)
     float acc[DH];
 #pragma unroll
     for (int i = 0; i < DH; ++i) acc[i] = 0.f;
@@ -271,20 +295,31 @@ __global__ void __launch_bounds__(kAttnThreads, AttnTmem<DK>::kCtasPerSm)
       mbar_wait_sleep(&pv_done[pb], (t >> 1) & 1);
       tc_fence_after();
       float o[DH];
+      uint32_t ls = 0;
+      if (kMmaRowSum)
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
+                     : "=r"(ls) : "r"(tmem + pb * 128 + 96 + lane_off));
       tmem_row_chunk<DH>(tmem + AttnTmem<DK>::o_col(pb) + hf * DH + lane_off, o);
       tc_fence_before();
       mbar_arrive(&o_read[pb]);
 #pragma unroll
       for (int i = 0; i < DH; ++i) acc[i] = kFixed ? acc[i] + o[i] : fmaf(acc[i], alpha, o[i]);
+      if (kMmaRowSum) lacc = kFixed ? lacc + __uint_as_float(ls) : fmaf(lacc, alpha, __uint_as_float(ls));
     };
     // fold the item's last O (tile t), combine the half-row sums, gate, store, clear acc
     auto finish_item = [&](int t, float alpha, int pli, bool gate_pending) {
       fold_o(t, alpha);
-      float* sl = s_red + 512;  // [2][128] partial row sums
-      sl[hf * 128 + r] = p_lsum;
-      named_bar_sync(1 + quarter, 64);
-      const float l = sl[r] + sl[128 + r];
-      named_bar_sync(1 + quarter, 64);  // both partners read before the next item overwrites
+      float l;
+      if constexpr (kMmaRowSum) {
+        l = lacc;  // both half-row warps fold the same full-row sums
+        lacc = 0.f;
+      } else {
+        float* sl = s_red + 512;  // [2][128] partial row sums
+        sl[hf * 128 + r] = p_lsum;
+        named_bar_sync(1 + quarter, 64);
+        l = sl[r] + sl[128 + r];
+        named_bar_sync(1 + quarter, 64);  // both partners read before the next item overwrites
+      }
       if (gate_pending) cp_async_wait_1(); else cp_async_wait_all();
       if (p_valid) {
         const uint8_t* gs = smem + S::oGate + ((pli & 1) * 256 + hf * 128 + r) * (DH * 2);
@@ -380,7 +415,8 @@ __global__ void __launch_bounds__(kAttnThreads, AttnTmem<DK>::kCtasPerSm)
           ref = m_new == NEG_INF ? 0.f : m_new * sl2;
           const float alpha = ex2_approx(m * sl2 - ref);  // m = -inf -> 0
 #pragma unroll
-          for (int u = 0; u < 2; ++u) lsum[u] = make_float2(lsum[u].x * alpha, lsum[u].y * alpha);
+          for (int u = 0; u < 2; ++u)
+            if (!kMmaRowSum) lsum[u] = make_float2(lsum[u].x * alpha, lsum[u].y * alpha);
           alpha_prev_fold = alpha_prev;  // alpha of tile g-1, used by the fold inside this tile
           alpha_prev = alpha;  // applied to acc when O of this tile is folded in (next tile / end)
           m = m_new;
@@ -416,7 +452,7 @@ __global__ void __launch_bounds__(kAttnThreads, AttnTmem<DK>::kCtasPerSm)
                 const float2 p = (kPolyEvery > 0 && i % kPolyEvery == kPolyEvery - 1)
                                      ? ex2_poly2(x)
                                      : make_float2(ex2_approx(x.x), ex2_approx(x.y));
-                lsum[i & 1] = fadd2(lsum[i & 1], p);
+                if (!kMmaRowSum) lsum[i & 1] = fadd2(lsum[i & 1], p);
                 w[i] = pack_bf16x2(p.x, p.y);
               }
             } else {
@@ -428,7 +464,7 @@ __global__ void __launch_bounds__(kAttnThreads, AttnTmem<DK>::kCtasPerSm)
                 x.x = (bits >> (2 * i)) & 1u ? x.x : NEG_INF;
                 x.y = (bits >> (2 * i + 1)) & 1u ? x.y : NEG_INF;
                 const float2 p = make_float2(ex2_approx(x.x), ex2_approx(x.y));
-                lsum[i & 1] = fadd2(lsum[i & 1], p);
+                if (!kMmaRowSum) lsum[i & 1] = fadd2(lsum[i & 1], p);
                 w[i] = pack_bf16x2(p.x, p.y);
               }
             }
