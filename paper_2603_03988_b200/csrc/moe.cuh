@@ -254,8 +254,12 @@ __global__ void __launch_bounds__(256) k_moe_route8(const __nv_bfloat16* __restr
 // segment positions with one warp-aggregated atomic per (slot, expert) on the per-expert
 // cursors (which end as the expert loads), then writes each token's normalised bf16 row into
 // its K (+ shared) segments, re-reading the row from L2.
+// The router columns sit in shared memory as [q][expert quad][lane] float4s (conflict-free
+// LDS.128, 8 KB) rather than in 64 registers per lane: 4 CTAs per SM instead of 2 hide the
+// per-token shuffle chains (the kernel is latency-bound on them).
+constexpr int kRouteCtasPerSm = 4;
 template <int K>
-__global__ void __launch_bounds__(256) k_moe_route_scatter8(
+__global__ void __launch_bounds__(256, kRouteCtasPerSm) k_moe_route_scatter8(
     const __nv_bfloat16* __restrict__ x, int T, int d, const float* __restrict__ gain,
     const float* __restrict__ router, const float* __restrict__ bias, int E, int shared, int Tcap,
     int32_t* __restrict__ sel, float* __restrict__ wgt, int32_t* __restrict__ cursor,
@@ -265,13 +269,16 @@ __global__ void __launch_bounds__(256) k_moe_route_scatter8(
   const int c0 = lane * 8;
   const bool act = c0 < d;
   const int S = K + shared;
-  float g[8], w[8][8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    g[i] = act ? gain[c0 + i] : 0.f;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) w[e][i] = act && e < E ? router[static_cast<size_t>(c0 + i) * E + e] : 0.f;
+  __shared__ float4 sw4[8][2][32];  // router[c0 + q][4 * quad + comp] of lane l at [q][quad][l]
+  for (int i = threadIdx.x; i < 32 * 8 * 8; i += blockDim.x) {
+    const int l = i >> 6, q = (i >> 3) & 7, e = i & 7;
+    const int c = l * 8 + q;
+    reinterpret_cast<float*>(&sw4[q][e >> 2][l])[e & 3] = c < d && e < E ? router[static_cast<size_t>(c) * E + e] : 0.f;
   }
+  float g[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) g[i] = act ? gain[c0 + i] : 0.f;
+  __syncthreads();
   const int my_e = lane >> 2;
   const bool owner = (lane & 3) == 0 && my_e < E;
   const float my_b = owner ? bias[my_e] : 0.f;
@@ -313,11 +320,19 @@ __global__ void __launch_bounds__(256) k_moe_route_scatter8(
       const float inv = rsqrtf(warp_sum(ss) / static_cast<float>(d) + 1e-6f);  // norm.hpp:23-24
       float p[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        float z = 0.f;
+      for (int e = 0; e < 8; ++e) p[e] = 0.f;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) z = fmaf(v[q] * inv * g[q], w[e][q], z);
-        p[e] = z;
+      for (int q = 0; q < 8; ++q) {  // same per-expert summation order as before (q ascending)
+        const float xq = v[q] * inv * g[q];
+        const float4 wa = sw4[q][0][lane], wb = sw4[q][1][lane];
+        p[0] = fmaf(xq, wa.x, p[0]);
+        p[1] = fmaf(xq, wa.y, p[1]);
+        p[2] = fmaf(xq, wa.z, p[2]);
+        p[3] = fmaf(xq, wa.w, p[3]);
+        p[4] = fmaf(xq, wb.x, p[4]);
+        p[5] = fmaf(xq, wb.y, p[5]);
+        p[6] = fmaf(xq, wb.z, p[6]);
+        p[7] = fmaf(xq, wb.w, p[7]);
       }
       float qq[4], rr[2];
 #pragma unroll
@@ -388,26 +403,37 @@ __global__ void __launch_bounds__(256) k_moe_route_scatter8(
         slot_pos[static_cast<size_t>(t) * S + j] = pos[j];
       }
     }
-    // rows: token by token, the whole warp moves one normalised row (16 B per lane)
-    for (int i = 0; i < n; ++i) {
-      int pj[K + 1];
+    // rows: the whole warp moves one normalised row per token (16 B per lane), kScatterBatch
+    // row re-reads (L2) in flight before the first store
+    constexpr int kScatterBatch = 4;
+    for (int i0 = 0; i0 < n; i0 += kScatterBatch) {
+      int4 raw[kScatterBatch];
 #pragma unroll
-      for (int j = 0; j <= K; ++j) pj[j] = __shfl_sync(0xffffffffu, pos[j], i);
-      const float iv = __shfl_sync(0xffffffffu, tinv, i);
-      if (!act) continue;
-      const int4 raw = *reinterpret_cast<const int4*>(x + static_cast<size_t>(base + i) * d + c0);
-      const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
-      uint32_t o[4];
+      for (int u = 0; u < kScatterBatch; ++u)
+        raw[u] = act && i0 + u < n ? *reinterpret_cast<const int4*>(x + static_cast<size_t>(base + i0 + u) * d + c0)
+                                   : make_int4(0, 0, 0, 0);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float2 f = __bfloat1622float2(p2[q]);
-        o[q] = pack_bf16x2(f.x * iv * g[2 * q], f.y * iv * g[2 * q + 1]);
-      }
-      const int4 ov = make_int4(o[0], o[1], o[2], o[3]);
+      for (int u = 0; u < kScatterBatch; ++u) {
+        const int i = i0 + u;
+        if (i >= n) break;
+        int pj[K + 1];
 #pragma unroll
-      for (int j = 0; j <= K; ++j) {
-        if (j == K && !shared) break;
-        *reinterpret_cast<int4*>(xs + static_cast<size_t>(pj[j]) * d + c0) = ov;
+        for (int j = 0; j <= K; ++j) pj[j] = __shfl_sync(0xffffffffu, pos[j], i);
+        const float iv = __shfl_sync(0xffffffffu, tinv, i);
+        if (!act) continue;
+        const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&raw[u]);
+        uint32_t o[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 f = __bfloat1622float2(p2[q]);
+          o[q] = pack_bf16x2(f.x * iv * g[2 * q], f.y * iv * g[2 * q + 1]);
+        }
+        const int4 ov = make_int4(o[0], o[1], o[2], o[3]);
+#pragma unroll
+        for (int j = 0; j <= K; ++j) {
+          if (j == K && !shared) break;
+          *reinterpret_cast<int4*>(xs + static_cast<size_t>(pj[j]) * d + c0) = ov;
+        }
       }
     }
   }
