@@ -69,7 +69,7 @@ struct AttnSmem {
   static constexpr uint32_t oK = oQ + 2 * kStride;
   static constexpr uint32_t oV = oK + kKvStages * kStride;
   static constexpr uint32_t oOnes = oV + kKvStages * kStride;  // 16 x 16 bf16 ones, K-major SW32
-  static constexpr uint32_t oBar = oOnes + 1024;
+  static constexpr uint32_t oBar = oOnes + (kMmaRowSum ? 1024 : 0);
   static constexpr uint32_t oRed = oBar + 32 * 8;      // softmax cross-warp reduction scratch
   static constexpr uint32_t oGate = oRed + 3 * 1024;   // [2 items][2 halves][128 rows][DK/2] bf16
   static constexpr uint32_t oTiles = oGate + 2 * 128 * DK * 2;  // int32 tile tables follow
