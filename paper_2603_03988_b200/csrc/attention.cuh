@@ -47,6 +47,15 @@ constexpr int kKvStages = 4;
 #ifndef SORT_ATTN_POLY_EVERY
 #define SORT_ATTN_POLY_EVERY 3
 #endif
+#ifndef SORT_ATTN_SPIN
+#define SORT_ATTN_SPIN 0
+#endif
+// softmax-warp waits on S / PV completion: suspend-hint try_wait (default) or a plain spin
+#if SORT_ATTN_SPIN
+#define SOFTMAX_WAIT mbar_wait
+#else
+#define SOFTMAX_WAIT mbar_wait_sleep
+#endif
 #ifndef SORT_ATTN_FOLD_AT
 #define SORT_ATTN_FOLD_AT 1
 #endif
@@ -292,7 +301,7 @@ __global__ void __launch_bounds__(kAttnThreads, AttnTmem<DK>::kCtasPerSm)
     // acc <- acc * alpha + O_t  (this warp's DK/2 columns of tile t's PV result)
     auto fold_o = [&](int t, float alpha) {
       const int pb = t & 1;
-      mbar_wait_sleep(&pv_done[pb], (t >> 1) & 1);
+      SOFTMAX_WAIT(&pv_done[pb], (t >> 1) & 1);
       tc_fence_after();
       float o[DH];
       uint32_t ls = 0;
@@ -388,7 +397,7 @@ __global__ void __launch_bounds__(kAttnThreads, AttnTmem<DK>::kCtasPerSm)
         const uint32_t cls = static_cast<uint32_t>(code.y) >> (2 * (4 * quarter + 2 * hf));
         const uint32_t full_mask = (cls & 1u) | ((cls >> 1) & 2u);
         const uint32_t none_mask = ((cls >> 1) & 1u) | ((cls >> 2) & 2u);
-        mbar_wait_sleep(&s_full[buf * 2 + hf], (g >> 1) & 1);
+        SOFTMAX_WAIT(&s_full[buf * 2 + hf], (g >> 1) & 1);
         tc_fence_after();
         float ref;  // exp2 reference in the scaled domain
         if constexpr (kFixed) {
