@@ -953,12 +953,14 @@ static void run_moe(Handle& h, int l, __nv_bfloat16* X, float4* SS, int T) {
   CK(cudaMemsetAsync(counts, 0, static_cast<size_t>(E) * 4, h.stream));
   if (E <= 8 && k <= 2) {  // routing and scatter in one pass; the cursors end as the loads
     const int grid = std::max(1, std::min((T + 255) / 256, kRouteCtasPerSm * h.num_sms));
+    ensure_smem(k_moe_route_scatter8<1>, kRouteSmem);
+    ensure_smem(k_moe_route_scatter8<2>, kRouteSmem);
     if (k == 1)
-      k_moe_route_scatter8<1><<<grid, 256, 0, h.stream>>>(X, T, d, gain, L.router, L.router_bias, E, S, Tcap,
+      k_moe_route_scatter8<1><<<grid, 256, kRouteSmem, h.stream>>>(X, T, d, gain, L.router, L.router_bias, E, S, Tcap,
                                                           L.moe_sel, L.moe_w, counts, h.moe_xs, h.moe_tok, h.moe_wof,
                                                           h.moe_slot, h.err);
     else
-      k_moe_route_scatter8<2><<<grid, 256, 0, h.stream>>>(X, T, d, gain, L.router, L.router_bias, E, S, Tcap,
+      k_moe_route_scatter8<2><<<grid, 256, kRouteSmem, h.stream>>>(X, T, d, gain, L.router, L.router_bias, E, S, Tcap,
                                                           L.moe_sel, L.moe_w, counts, h.moe_xs, h.moe_tok, h.moe_wof,
                                                           h.moe_slot, h.err);
     k_moe_plan<<<1, 256, 0, h.stream>>>(counts, E, S, T, Tcap, h.moe_off, h.moe_cursor, h.moe_tile_group,
