@@ -47,6 +47,27 @@ def workload_desc(cfg):
             f"L={cfg.seq_len}, W={cfg.local_window}, F={cfg.full_suffix}, keep={cfg.keep_schedule()}")
 
 
+def bench_config(cfg, world, B):
+    """The `config` object of BOTH arms (ours and --impl reference): it names the workload
+    only, so the driver can compare the two lines key for key."""
+    return {"workload": workload_desc(cfg), "global_batch": world * B, "requests_per_gpu": B,
+            "seq_len": cfg.seq_len, "parallelism": f"dp{world} (request-sharded replicas, no forward collective)",
+            "l2": "flushed (256 MB write) before every timed step",
+            "weights": "random init (synth.make_params, fan-in), bf16-rounded"}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -149,14 +170,16 @@ def run_reference(args, cfg, rank, world):
         total_r += n
     value = total_c / total_t
     sample = (f"{total_r} SORT-base requests over {args.steps} steps ({int(total_c)} candidates, "
-              f"{total_t:.1f} s), fp64 oracle port, one request per thread")
+              f"{total_t:.1f} s), fp64 oracle port, one request per thread, {threads} threads on "
+              f"{cpu_model()}")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_t / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": workload_desc(cfg), "parallelism": "host threads"},
+        "data": "synthetic", "config": bench_config(cfg, world, args.requests),
+        "execution": f"CPU: {threads} host threads ({cpu_model()}), one request per thread",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -256,11 +279,6 @@ def run_embed(args, cfg, rank, world, local, dist):
     lse_t = torch.empty((B, cfg.n_hist), dtype=torch.float32, device=dev)
     tgt_t = torch.empty((B, cfg.n_hist), dtype=torch.float32, device=dev)
 
-    def step():
-        if pretrain:
-            model.pretrain_forward_device(dbatch, lse_t.data_ptr(), tgt_t.data_ptr())
-        else:
-            model.forward_device(dbatch, scores.data_ptr())
     n_unique = []
 
     def step():
@@ -387,6 +405,46 @@ def run_large(args, rank, world, local, dist, moe=False, pretrain=False):
         dist.destroy_process_group()
 
 
+def launch_ranks(n):
+    """Re-run this command under torch.distributed.run with n ranks on 127.0.0.1 (the
+    driver's own multi-GPU form); rank 0 prints the JSON line."""
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
+def run_dry(args, cfg, rank, world, dist):
+    """--dry-run: the launcher, barrier and max-over-ranks plumbing of the real run on gloo
+    (CPU), with a trivial host step. Used by tests/test_bench_launch.py."""
+    t0 = time.perf_counter()
+    acc = 0.0
+    for i in range(args.warmup + args.steps):
+        acc += float(np.sum(np.arange(1000 * (rank + 1), dtype=np.float64)))
+    ms = (time.perf_counter() - t0) * 1e3 / max(1, args.steps)
+    t = [ms]
+    if dist:
+        import torch
+        tt = torch.tensor(t, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = tt.tolist()
+        ranks = torch.tensor([1.0])
+        dist.all_reduce(ranks)
+        n_ranks = int(ranks.item())
+    else:
+        n_ranks = 1
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": t[0], "dry_run": True, "ranks_seen": n_ranks,
+                          "config": bench_config(cfg, world, args.requests)}), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -405,21 +463,39 @@ def main():
     ap.add_argument("--table-rows", type=int, default=100_000_000)
     ap.add_argument("--profile-launches", action="store_true",
                     help="short run for ncu launch lists (no CPU leg, no e2e)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher check without a GPU: N gloo ranks, barrier + max-over-ranks "
+                         "timing of a trivial host step, one JSON line from rank 0")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if not args.profile_launches else args.warmup
+
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        # `python bench.py --gpus N` launches its own N ranks (one process per GPU) exactly as
+        # the driver's torchrun form does; this process only waits for them
+        launch_ranks(args.gpus)
+        return
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if "WORLD_SIZE" not in os.environ and args.impl == "reference":
+        world = args.gpus  # CPU arm: rank 0's work only, reported for the N-GPU run it sits beside
+    elif world != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world} overrides --gpus {args.gpus}", file=sys.stderr)
     cfg = base_config(batch=args.requests)
 
     import torch
     dist = None
-    if world > 1:
+    if "WORLD_SIZE" in os.environ and world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        torch.cuda.set_device(local) if args.impl == "ours" else None
-        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+        use_nccl = args.impl == "ours" and not args.dry_run
+        torch.cuda.set_device(local) if use_nccl else None
+        dist.init_process_group("nccl" if use_nccl else "gloo")
+
+    if args.dry_run:
+        run_dry(args, cfg, rank, world, dist)
+        return
 
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
@@ -450,14 +526,6 @@ def main():
     dev_batch = {k: torch.from_numpy(v).to(dev) for k, v in batch.items()}
     dbatch = R._DevBatch(dev_batch)
     scores = torch.empty((B, max(cfg.n_cand, 1), 3), dtype=torch.float32, device=dev)
-    lse_t = torch.empty((B, cfg.n_hist), dtype=torch.float32, device=dev)
-    tgt_t = torch.empty((B, cfg.n_hist), dtype=torch.float32, device=dev)
-
-    def step():
-        if pretrain:
-            model.pretrain_forward_device(dbatch, lse_t.data_ptr(), tgt_t.data_ptr())
-        else:
-            model.forward_device(dbatch, scores.data_ptr())
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
 
     def barrier():
@@ -619,19 +687,16 @@ def main():
         threads = os.cpu_count() or 1
         ref = CpuReference(cfg, params, threads)
         rate, dt, n_req = ref.sample(args.cpu_seconds, 32)
-        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port", "cpu_model": cpu_model(),
                "sample": f"{n_req} SORT-base requests ({n_req * cfg.n_cand} candidates) in "
-                         f"{dt:.1f} s, fp64 oracle port of the reference, one request per thread"}
+                         f"{dt:.1f} s, fp64 oracle port of the reference, one request per thread, "
+                         f"{threads} threads on {cpu_model()}"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": workload_desc(cfg), "global_batch": world * B,
-                   "requests_per_gpu": B, "seq_len": cfg.seq_len,
-                   "parallelism": f"dp{world} (request-sharded replicas, no forward collective)",
-                   "l2": "flushed (256 MB write) before every timed step",
-                   "weights": "random init (synth.make_params, fan-in), bf16-rounded"},
+        "config": bench_config(cfg, world, B),
         "mfu": mfu, "mfu_peak": f"{peaks['bf16_tflops']} TFLOP/s bf16 ({peak_kind})",
         "algorithmic_tflop_per_step": step_flops * world / 1e12,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,

@@ -271,8 +271,11 @@ int sort_pretrain_forward(SortHandle h, const SortBatch* batch, int inputs_on_de
  * Routing of layer `layer` in the last forward: sel/weights [rows, moe_topk] host buffers
  * (either may be NULL), rows = batch * l_q(layer) in the forward's row order; selection in
  * descending biased score, weights = renormalised raw sigmoid scores (route_topk,
- * SPEC.md:305-315). */
-int sort_moe_routing(SortHandle h, int layer, int32_t* sel, float* weights);
+ * SPEC.md:305-315). `capacity_rows` is the row capacity of sel/weights: ConfigError when the
+ * last forward routed more rows. `rows_out` (may be NULL) receives the routed row count, so a
+ * caller can size its buffers with a first call passing sel = weights = NULL. */
+int sort_moe_routing(SortHandle h, int layer, int32_t capacity_rows, int32_t* rows_out, int32_t* sel,
+                     float* weights);
 /* Expert-load histogram [moe_experts] of layer `layer` in the last forward (update_balance
  * input). */
 int sort_moe_load(SortHandle h, int layer, int64_t* load);

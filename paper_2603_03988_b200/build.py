@@ -11,9 +11,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libsort_b200.so")
 SOURCES = ["runtime.cu", "plan.cpp", "dataset.cpp"]
-HEADERS = ["ptx.cuh", "gemm.cuh", "epilogues.cuh", "attention.cuh", "tokenizer.cuh", "misc.cuh",
-           "block_tail.cuh", "train.cuh",
-           "plan.hpp", "tma_host.hpp"]
+# every header in csrc/ is a dependency (a stale list once missed moe.cuh / pretrain.cuh edits)
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp", ".h")))
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall", "--expt-relaxed-constexpr", "-shared"]

@@ -10,6 +10,7 @@
 // "dataset line N, field 'F': what" (DatasetFormatError, dataset_io.hpp:12-25), status 1.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cerrno>
 #include <cmath>
 #include <cstdlib>
@@ -294,7 +295,7 @@ static void parse_dataset(const std::string& path, Dataset& ds) {
       s.click.push_back(click);
       s.cart.push_back(cart);
       s.purchase.push_back(purchase);
-      s.n_side = static_cast<int>(cj.a[4].a.size());
+      s.n_side = std::max(s.n_side, static_cast<int>(cj.a[4].a.size()));
     }
     ds.recs.push_back(std::move(s));
   }
@@ -372,6 +373,11 @@ int sort_dataset_batch(SortDataset d, int64_t first, int32_t count, int32_t n_hi
                           " does not match the batch geometry (history " + std::to_string(r.item.size()) +
                           ", candidates " + std::to_string(r.cand.size()) + ", profile " +
                           std::to_string(r.profile.size()) + "): one handle serves one geometry");
+      // candidate side groups are not configured on this path (side_width() == 0): the
+      // reference tokenizer rejects any other width (tokenizer.cpp:116-120), so do we
+      if (r.n_side != 0)
+        throw ConfigError("tokenizer: candidate side feature width " + std::to_string(r.n_side) +
+                          " != configured 0 (dataset record " + std::to_string(first + static_cast<int64_t>(b)) + ")");
       std::memcpy(ds->p_item + b * n_hist, r.item.data(), n_hist * 4);
       std::memcpy(ds->p_action + b * n_hist, r.action.data(), n_hist * 4);
       std::memcpy(ds->p_scene + b * n_hist, r.scene.data(), n_hist * 4);

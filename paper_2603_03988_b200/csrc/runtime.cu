@@ -423,6 +423,7 @@ static void finalize(Handle& h) {
   h.probs = h.dalloc<float>(static_cast<size_t>(h.Bmax) * c.n_cand * 3);
   h.logits = h.dalloc<float>(static_cast<size_t>(h.Bmax) * c.n_cand * 3);
   h.err = h.dalloc<int32_t>(4);
+  CK(cudaMemset(h.err, 0, 4 * sizeof(int32_t)));
   h.hist_time = h.dalloc<int32_t>(static_cast<size_t>(h.Bmax) * std::max(c.n_hist, 1));
   const size_t BH_ = static_cast<size_t>(h.Bmax) * std::max(c.n_hist, 1);
   h.in_item = h.dalloc<int32_t>(BH_);
@@ -743,7 +744,9 @@ static void launch_attention_dk(Handle& h, const LayerDev& L, const LayerPlan& l
   a.n_qtiles = lp.n_qtiles;
   a.n_codes = n_codes;
   a.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(DK)));
-  a.ref_log2 = L.logit_bound * a.scale_log2;
+  // fixed softmax reference in log2 units: the exponent is s * log2e with s = S / sqrt(dk) the
+  // scaled logit, |s| <= logit_bound, so the reference is logit_bound * log2e (every P <= 1)
+  a.ref_log2 = L.logit_bound * 1.4426950408889634f;
   const int n_items = lp.n_qtiles * B * h.H;
   const int tile_ints = 2 * lp.n_qtiles + 2 + 2 * n_codes;
   if constexpr (kFixed) {
@@ -1681,7 +1684,6 @@ static void forward_generic(Handle& h, int B) {
   CK(cublasSetStream(h.cublas, h.stream) == CUBLAS_STATUS_SUCCESS ? cudaSuccess : cudaErrorUnknown);
   const SortConfig& c = h.cfg;
   const int d = h.d, m = h.m, H = h.H, dk = h.dk, N = c.n_cand;
-  CK(cudaMemsetAsync(h.err, 0, 4 * sizeof(int32_t), h.stream));
   // ---- tokenizer: gather -> projection -> bias + RMSNorm (tokenizer.cpp:144-238)
   const TokParams tp = tok_params(h, B);
   float* X = h.gX[0];
@@ -1861,7 +1863,9 @@ static void forward_device(Handle& h, int B) {
     forward_generic(h, B);
     return;
   }
-  CK(cudaMemsetAsync(h.err, 0, 4 * sizeof(int32_t), h.stream));
+  // h.err is NOT cleared here: several sort_forward_async calls may be queued before one
+  // sort_sync, and each batch's device checks (OOV ids, MoE non-finite router scores) must
+  // survive until that sync reads them. collect_status() clears the word after reading it.
   run_tokenizer(h, B);
   stage_mark(h, "tokenizer");
   for (int l = 0; l < h.cfg.layers; ++l) run_layer(h, l, B);
@@ -1946,6 +1950,8 @@ static void collect_status(Handle& h) {
   int32_t err[4];
   CK(cudaMemcpyAsync(err, h.err, sizeof(err), cudaMemcpyDeviceToHost, h.stream));
   CK(cudaStreamSynchronize(h.stream));
+  // the sync point: everything enqueued so far has been checked, start a fresh error word
+  if (err[0] | err[1] | err[2] | err[3]) CK(cudaMemsetAsync(h.err, 0, 4 * sizeof(int32_t), h.stream));
   if (h.timing && h.events.size() > 1) {
     h.stage_ms.clear();
     for (size_t i = 1; i < h.events.size(); ++i) {
@@ -2176,7 +2182,6 @@ int sort_tokenize(SortHandle p, const SortBatch* batch, float* tokens, int32_t* 
     if (!batch) throw ConfigError("null argument");
     begin_timing(*h);
     upload_batch(*h, batch, false);
-    CK(cudaMemsetAsync(h->err, 0, 4 * sizeof(int32_t), h->stream));
     const int B = batch->batch;
     std::vector<__nv_bfloat16> xb(static_cast<size_t>(B) * h->L0 * h->d);
     if (h->generic) {
@@ -2374,7 +2379,7 @@ int sort_train_step(SortHandle p, const SortBatch* batch, const float* dlogits, 
     h->training = false;
     const size_t nz = static_cast<size_t>(B) * h->cfg.n_cand * 3;
     float*& dzb = h->dz_dev;
-    if (!dzb) dzb = h->dalloc<float>(static_cast<size_t>(h->Bmax) * h->cfg.n_cand * 3);
+    if (!dzb) dzb = h->dalloc<float>(static_cast<size_t>(h->Bmax) * h->cfg.n_cand * 3 + 1);  // + loss slot
     CK(cudaMemcpyAsync(dzb, dlogits, nz * 4, cudaMemcpyHostToDevice, h->stream));
     CK(cublasSetStream(h->cublas, h->stream) == CUBLAS_STATUS_SUCCESS ? cudaSuccess : cudaErrorUnknown);
     backward_device(*h, B, dzb);
@@ -2560,12 +2565,17 @@ int sort_pretrain_forward(SortHandle p, const SortBatch* batch, int inputs_on_de
   });
 }
 
-int sort_moe_routing(SortHandle p, int layer, int32_t* sel, float* weights) {
+int sort_moe_routing(SortHandle p, int layer, int32_t capacity_rows, int32_t* rows_out, int32_t* sel,
+                     float* weights) {
   return api([&] {
     Handle* h = ready(p);
     if (!h->moe) throw ConfigError("moe: the model has no MoE FFN");
     if (layer < 0 || layer >= h->cfg.layers) throw ConfigError("moe: layer out of range");
     const LayerDev& L = h->layers[layer];
+    if (rows_out) *rows_out = h->moe_rows[layer];
+    if ((sel || weights) && capacity_rows < h->moe_rows[layer])
+      throw ConfigError("moe: routing buffers hold " + std::to_string(capacity_rows) + " rows, the last forward routed " +
+                        std::to_string(h->moe_rows[layer]));
     const size_t n = static_cast<size_t>(h->moe_rows[layer]) * h->moe_k;
     if (sel) CK(cudaMemcpyAsync(sel, L.moe_sel, n * 4, cudaMemcpyDeviceToHost, h->stream));
     if (weights) CK(cudaMemcpyAsync(weights, L.moe_w, n * 4, cudaMemcpyDeviceToHost, h->stream));
@@ -2610,7 +2620,6 @@ int sort_moe_forward(SortHandle p, int layer, const float* x, int rows, float* o
     for (size_t i = 0; i < xb.size(); ++i) xb[i] = f2bf(x[i]);
     __nv_bfloat16* X = h->X[0];
     CK(cudaMemcpyAsync(X, xb.data(), xb.size() * 2, cudaMemcpyHostToDevice, h->stream));
-    CK(cudaMemsetAsync(h->err, 0, 4 * sizeof(int32_t), h->stream));
     if (rows > 0) run_moe(*h, layer, X, h->SS[0], rows);
     CK(cudaMemcpyAsync(xb.data(), X, xb.size() * 2, cudaMemcpyDeviceToHost, h->stream));
     collect_status(*h);

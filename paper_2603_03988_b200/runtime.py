@@ -105,7 +105,7 @@ def lib():
         L.sort_train_step_bce.argtypes = [C.c_void_p, C.c_void_p, f32p, f32p, f32p]
         L.sort_adamw_step.argtypes = [C.c_void_p, C.c_float, C.c_float, C.c_float, C.c_float, C.c_float]
         L.sort_get_param.argtypes = [C.c_void_p, C.c_char_p, f32p]
-        L.sort_moe_routing.argtypes = [C.c_void_p, C.c_int, i32p, f32p]
+        L.sort_moe_routing.argtypes = [C.c_void_p, C.c_int, C.c_int32, i32p, i32p, f32p]
         L.sort_moe_load.argtypes = [C.c_void_p, C.c_int, i64p]
         L.sort_moe_update_bias.argtypes = [C.c_void_p, C.c_double]
         L.sort_moe_forward.argtypes = [C.c_void_p, C.c_int, f32p, C.c_int, f32p]
@@ -300,13 +300,18 @@ class SortModel:
                                            C.c_void_p(tgt_ptr), 1))
 
     # -- MoE FFN ----------------------------------------------
-    def moe_routing(self, layer: int, rows: int):
-        """(sel [rows, k] int32, weights [rows, k]) of `layer` in the last forward."""
+    def moe_routing(self, layer: int, rows: int | None = None):
+        """(sel [rows, k] int32, weights [rows, k]) of `layer` in the last forward. `rows` is
+        checked against the routed row count (ConfigError if the buffers would be too small);
+        None sizes the buffers from the library's own count."""
         k = self.cfg.moe_topk
+        n = C.c_int32(0)
+        _check(lib().sort_moe_routing(self.h, layer, 0, C.byref(n), None, None))
+        rows = n.value if rows is None else rows
         sel = np.zeros((rows, k), np.int32)
         w = np.zeros((rows, k), np.float32)
-        _check(lib().sort_moe_routing(self.h, layer, _p(sel, i32p), _p(w, f32p)))
-        return sel, w
+        _check(lib().sort_moe_routing(self.h, layer, rows, None, _p(sel, i32p), _p(w, f32p)))
+        return sel[:n.value], w[:n.value]
 
     def moe_load(self, layer: int) -> np.ndarray:
         out = np.zeros(self.cfg.moe_experts, np.int64)

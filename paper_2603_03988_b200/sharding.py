@@ -112,6 +112,19 @@ class ShardedItemTable:
         hist, cand = batch["hist_item"], batch["cand_item"]
         ids = torch.cat([hist.reshape(-1), cand.reshape(-1)]).to(torch.int64)
         uniq, inv = torch.unique(ids, sorted=True, return_inverse=True)
+        # range check BEFORE any collective, agreed over the ranks: a rank that raised alone
+        # would leave its peers blocked inside the all-to-all (reference: check_id,
+        # tokenizer.cpp:14-19 -> ConfigError)
+        bad = torch.zeros(1, dtype=torch.int32, device=ids.device)
+        if uniq.numel():
+            bad[0] = ((uniq[0] < 0) | (uniq[-1] >= self.world * self.R)).to(torch.int32)
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(bad, op=dist.ReduceOp.MAX, group=self.group)
+        if int(bad.item()):
+            from .config import ConfigError
+            raise ConfigError(f"tokenizer: item id outside vocabulary of size {self.world * self.R} "
+                              f"(sharded table, detected on at least one rank)")
         owner = torch.div(uniq, self.R, rounding_mode="floor")
         if self.world == 1:
             rows = self.gather(self.shard, uniq)

@@ -95,3 +95,15 @@ def test_reference_validation_rules(tmp_path, header, rec, field, what):
 def test_good_record_parses(tmp_path):
     ds = R.Dataset(_write(tmp_path, HDR, [GOOD, ""]))  # blank lines are skipped
     assert len(ds) == 1
+
+
+def test_side_features_rejected_at_batch(tmp_path):
+    """A record with candidate side features parses (dataset_io.cpp:142 reads them) but the
+    configured side width is 0, so packing it for the tokenizer is a ConfigError with the
+    reference tokenizer's text (tokenizer.cpp:116-120)."""
+    rec = dict(GOOD, candidates=[[7, 1, 0, 0, [0.5, 1.5]]])
+    ds = R.Dataset(_write(tmp_path, HDR, [rec]))
+    cfg = tiny_config(n_hist=2, n_cand=1)
+    with pytest.raises(R.ConfigError) as ei:
+        ds.batch(0, 1, cfg)
+    assert "candidate side feature width 2 != configured 0" in str(ei.value)

@@ -150,6 +150,18 @@ def _table_worker(rank, world, port, out_q):
     ok = all(torch.equal(rows[mapped[k].long()], full[batch[k].long()]) for k in ("hist_item", "cand_item"))
     uniq = int(torch.unique(torch.cat([batch["hist_item"].reshape(-1), batch["cand_item"].reshape(-1)])).numel())
     ok = ok and rows.shape[0] == uniq
+    # an out-of-vocabulary id on ONE rank must raise on EVERY rank before any all-to-all
+    # (otherwise the clean rank would block in the collective)
+    bad = dict(batch)
+    if rank == 1:
+        bad["cand_item"] = batch["cand_item"].clone()
+        bad["cand_item"][0, 0] = n_items + 5
+    from paper_2603_03988_b200.config import ConfigError
+    try:
+        tab.lookup(bad)
+        ok = False
+    except ConfigError:
+        pass
     oks = [None] * world
     dist.all_gather_object(oks, ok)
     if rank == 0:
