@@ -97,6 +97,9 @@ def lib():
         L.oracle_moe_update_bias.argtypes = [i64p, C.c_int, C.c_double, f64p]
         L.oracle_pretrain_forward.argtypes = [C.c_void_p, C.POINTER(OrSample), f64p, f64p, f64p]
         L.oracle_tokenize_clicks.argtypes = [C.c_void_p, C.POINTER(OrSample), f64p, i32p]
+        L.oracle_attention_backward.argtypes = [C.c_void_p, C.c_int, f64p, C.c_int, i32p, C.c_int, u8p, i32p,
+                                                f64p, f64p, C.POINTER(C.c_void_p)]
+        L.oracle_tokenizer_backward.argtypes = [C.c_void_p, C.POINTER(OrSample), f64p, C.POINTER(C.c_void_p)]
         _lib = L
     return _lib
 
@@ -267,26 +270,32 @@ class _SampleHold:
                           len(a["cand_item"]), _p(a["cand_item"], i32p))
 
 
+def or_cfg(cfg) -> OrModelCfg:
+    """SortConfig -> the C struct both liboracle.so and oracle/_ref/libref.so take."""
+    c = OrModelCfg()
+    c.model_dim, c.item_dim, c.action_dim = cfg.model_dim, cfg.item_dim, cfg.action_dim
+    c.scene_dim, c.time_dim, c.profile_dim = cfg.scene_dim, cfg.time_dim, cfg.profile_dim
+    c.n_items, c.n_actions, c.n_scenes = cfg.n_items, cfg.n_actions, cfg.n_scenes
+    c.n_time_buckets, c.n_profile_fields = cfg.n_time_buckets, len(cfg.profile_vocab)
+    for i, v in enumerate(cfg.profile_vocab):
+        c.profile_vocab[i] = v
+    c.special_tokens = int(cfg.special_tokens)
+    c.layers, c.heads, c.ffn_dim = cfg.layers, cfg.heads, cfg.ffn_dim
+    c.qknorm, c.gate, c.rope_theta = int(cfg.qknorm), int(cfg.gate), cfg.rope_theta
+    c.local_window, c.full_suffix = cfg.local_window, cfg.full_suffix
+    for i, k in enumerate(cfg.keep_schedule()):
+        c.keep[i] = k
+    c.keep_specials, c.head_hidden = int(cfg.keep_specials), cfg.head_hidden
+    c.moe_experts = getattr(cfg, "moe_experts", 0)
+    c.moe_topk = getattr(cfg, "moe_topk", 1)
+    c.moe_shared = getattr(cfg, "moe_shared", 0)
+    c.moe_ffn_dim = getattr(cfg, "moe_ffn_dim", 0)
+    return c
+
+
 class OracleModel:
     def __init__(self, cfg, params: Dict[str, np.ndarray]):
-        c = OrModelCfg()
-        c.model_dim, c.item_dim, c.action_dim = cfg.model_dim, cfg.item_dim, cfg.action_dim
-        c.scene_dim, c.time_dim, c.profile_dim = cfg.scene_dim, cfg.time_dim, cfg.profile_dim
-        c.n_items, c.n_actions, c.n_scenes = cfg.n_items, cfg.n_actions, cfg.n_scenes
-        c.n_time_buckets, c.n_profile_fields = cfg.n_time_buckets, len(cfg.profile_vocab)
-        for i, v in enumerate(cfg.profile_vocab):
-            c.profile_vocab[i] = v
-        c.special_tokens = int(cfg.special_tokens)
-        c.layers, c.heads, c.ffn_dim = cfg.layers, cfg.heads, cfg.ffn_dim
-        c.qknorm, c.gate, c.rope_theta = int(cfg.qknorm), int(cfg.gate), cfg.rope_theta
-        c.local_window, c.full_suffix = cfg.local_window, cfg.full_suffix
-        for i, k in enumerate(cfg.keep_schedule()):
-            c.keep[i] = k
-        c.keep_specials, c.head_hidden = int(cfg.keep_specials), cfg.head_hidden
-        c.moe_experts = getattr(cfg, "moe_experts", 0)
-        c.moe_topk = getattr(cfg, "moe_topk", 1)
-        c.moe_shared = getattr(cfg, "moe_shared", 0)
-        c.moe_ffn_dim = getattr(cfg, "moe_ffn_dim", 0)
+        c = or_cfg(cfg)
         self.cfg = cfg
         h = C.c_void_p()
         _check(lib().oracle_model_create(C.byref(c), C.byref(h)))
@@ -401,6 +410,43 @@ class OracleModel:
                                               _p(qr, i32p), len(qr), _p(vis, u8p), _p(p, i32p),
                                               _p(out, f64p)))
         return out
+
+    def _grads(self, g, names):
+        out = {}
+        try:
+            for name in names:
+                r, c = C.c_int32(0), C.c_int32(0)
+                _check(lib().oracle_grads_get(g, name.encode(), None, C.byref(r), C.byref(c)))
+                a = np.zeros((max(r.value, 1), max(c.value, 1)))
+                if r.value:
+                    _check(lib().oracle_grads_get(g, name.encode(), _p(a, f64p), None, None))
+                    out[name] = a
+                else:
+                    out[name] = None
+        finally:
+            lib().oracle_grads_destroy(g)
+        return out
+
+    def attention_backward(self, layer, xn, query_rows, visible, pos, dout, names):
+        """(dxn, {name: grad}) of the restated AttentionLayer::backward for layer alone."""
+        xn = np.ascontiguousarray(xn, dtype=np.float64)
+        dout = np.ascontiguousarray(dout, dtype=np.float64)
+        qr = np.ascontiguousarray(query_rows, dtype=np.int32)
+        vis = np.ascontiguousarray(visible, dtype=np.uint8)
+        p = np.ascontiguousarray(pos, dtype=np.int32)
+        dxn = np.zeros_like(xn)
+        g = C.c_void_p()
+        _check(lib().oracle_attention_backward(self.h, layer, _p(xn, f64p), xn.shape[0], _p(qr, i32p), len(qr),
+                                               _p(vis, u8p), _p(p, i32p), _p(dout, f64p), _p(dxn, f64p),
+                                               C.byref(g)))
+        return dxn, self._grads(g, names)
+
+    def tokenizer_backward(self, batch, b: int, dtokens, names):
+        hold = _SampleHold(batch, b)
+        dt = np.ascontiguousarray(dtokens, dtype=np.float64)
+        g = C.c_void_p()
+        _check(lib().oracle_tokenizer_backward(self.h, C.byref(hold.s), _p(dt, f64p), C.byref(g)))
+        return self._grads(g, names)
 
     def backward(self, batch, b: int, dlogits: np.ndarray, names):
         """fp64 backward of forward(batch, b) given dL/dlogits [n_cand, 3]: returns

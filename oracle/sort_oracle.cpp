@@ -1503,4 +1503,42 @@ int oracle_grads_get(const OrGrads* g, const char* name, double* out, int* rows,
 }
 
 void oracle_grads_destroy(OrGrads* g) { delete g; }
+
+int oracle_attention_backward(const OrModel* m, int layer, const double* xn, int l_in, const int* query_rows,
+                              int l_q, const uint8_t* visible, const int* position_ids, const double* dout,
+                              double* dxn, OrGrads** out) {
+  return guarded([&] {
+    if (layer < 0 || layer >= m->cfg.layers) throw ConfigError("attention: layer out of range");
+    M x(l_in, m->d);
+    std::memcpy(x.a.data(), xn, sizeof(double) * x.a.size());
+    M dy(l_q, m->d);
+    std::memcpy(dy.a.data(), dout, sizeof(double) * dy.a.size());
+    auto* G = new OrGrads;
+    try {
+      M dx = attention_backward(*m, layer, x, std::vector<int>(query_rows, query_rows + l_q), visible,
+                                std::vector<int>(position_ids, position_ids + l_in), dy, G->g);
+      std::memcpy(dxn, dx.a.data(), sizeof(double) * dx.a.size());
+    } catch (...) {
+      delete G;
+      throw;
+    }
+    *out = G;
+  });
+}
+
+int oracle_tokenizer_backward(const OrModel* m, const OrSample* s, const double* dtokens, OrGrads** out) {
+  return guarded([&] {
+    const int L = (m->cfg.special_tokens ? 3 : 0) + s->n_hist + s->n_prof + s->n_cand;
+    M dt(L, m->d);
+    std::memcpy(dt.a.data(), dtokens, sizeof(double) * dt.a.size());
+    auto* G = new OrGrads;
+    try {
+      tokenizer_backward(*m, *s, dt, G->g);
+    } catch (...) {
+      delete G;
+      throw;
+    }
+    *out = G;
+  });
+}
 }  // extern "C"

@@ -8,12 +8,16 @@
  * can CHECK the CUDA path and time the reference algorithm on host cores.
  * Nothing in the product (paper_2603_03988_b200/) links, loads or calls it.
  *
- * Parity status: the reference cannot be built here (Eigen3 absent, its
- * src/tools/tests CMake dirs missing, attention.cpp:152,180-183,194 do not
- * compile), so this restatement is pinned against every known-answer example
- * in SPEC.md plus the derived counts in SURVEY.md section 8 -- the reference ships
- * no tests or golden vectors. Bit-level claims are made for the integer
- * artifacts (time buckets, positions, roles, masks, schedules, retained rows).
+ * Parity status: PINNED TO THE REFERENCE'S OWN CODE. The reference cannot be built with
+ * its own CMake (Eigen3 absent, its src/tools/tests CMake dirs missing,
+ * attention.cpp:152,180-183,194 do not compile), but oracle/Makefile compiles its
+ * mask.cpp / tokenizer.cpp / attention.cpp unmodified against a small Eigen-subset shim
+ * (oracle/ref_shim) into oracle/_ref/libref.so, and tests/test_ref_pinning.py checks this
+ * restatement against it: integer artifacts bit-identical, fp64 values to 1e-9 (tokenizer
+ * forward/backward, masks, schedules, retained rows, rmsnorm, rope, dense/blockwise
+ * attention, AttentionLayer forward/backward, and the whole-model forward composed from
+ * the reference's calls plus the spec-only FFN/block/head). It is additionally pinned
+ * against every known-answer example in SPEC.md (tests/test_oracle_kat.py).
  *
  * All functions return 0 on success, 1 for a ConfigError (common.hpp:17-21)
  * and 2 for a RuntimeFailure (common.hpp:23-27); oracle_last_error() gives
@@ -179,6 +183,13 @@ int oracle_model_backward(const OrModel* m, const OrSample* s, const double* dlo
                           double* dtokens, OrGrads** out);
 int oracle_grads_get(const OrGrads* g, const char* name, double* out, int* rows, int* cols);
 void oracle_grads_destroy(OrGrads* g);
+/* AttentionLayer::backward of layer `layer` alone (attention.cpp:134-202): d(xn) [l_in, d]
+ * and the layer's gradients (attn.<l>.wq|wk|wv|wo|wg|qk_gain_q|qk_gain_k). */
+int oracle_attention_backward(const OrModel* m, int layer, const double* xn, int l_in, const int* query_rows,
+                              int l_q, const uint8_t* visible, const int* position_ids, const double* dout,
+                              double* dxn, OrGrads** out);
+/* Tokenizer::backward (tokenizer.cpp:286-354) for dL/dtokens [L, d], item table frozen. */
+int oracle_tokenizer_backward(const OrModel* m, const OrSample* s, const double* dtokens, OrGrads** out);
 
 #ifdef __cplusplus
 }
