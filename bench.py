@@ -194,7 +194,7 @@ def run_train(args, cfg, rank, world, local, dist):
     fp32 masters and the bf16 inference weights rebuilt on the device every step."""
     import torch
     from paper_2603_03988_b200 import runtime as R
-    from paper_2603_03988_b200.sharding import allreduce_grads, shard_range
+    from paper_2603_03988_b200.sharding import shard_range
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     b0, b1 = shard_range(args.requests, world, rank)
@@ -205,6 +205,7 @@ def run_train(args, cfg, rank, world, local, dist):
     batch = {k: np.ascontiguousarray(v[b0:b1]) for k, v in full.items()}
     labels = (np.random.default_rng(7).random((args.requests, cfg.n_cand, 3)) < 0.2).astype(np.float32)[b0:b1]
     gbuf = torch.zeros(model.grad_layout()[3], dtype=torch.float32, device=dev)
+    exchange = R.Exchange.nccl(rank, world, local) if dist else None  # gradient sum in the C++ host (NCCL)
     # per-rank mean BCE scaled by 1/world: the all-reduced sum is the global-batch mean
     w_obj = np.array([1.0, 0.5, 0.5], np.float32) / world
     losses = []
@@ -213,7 +214,7 @@ def run_train(args, cfg, rank, world, local, dist):
         losses.append(model.train_step_bce(batch, labels, w_obj))  # fwd + loss + bwd on device
         if dist:
             model.grads_to_device(gbuf.data_ptr())
-            allreduce_grads(gbuf, world)
+            exchange.allreduce(gbuf.data_ptr(), gbuf.numel())
             model.grads_to_device(gbuf.data_ptr(), to_handle=True)
         model.adamw_step(lr=2e-4)  # PAPER.md:4.1.3 base lr, beta (0.9, 0.99), wd 0.01
         torch.cuda.synchronize(dev)
@@ -251,9 +252,10 @@ def run_train(args, cfg, rank, world, local, dist):
 
 def run_embed(args, cfg, rank, world, local, dist):
     """BASELINE configs[4]: SORT-base scoring whose item table (--table-rows x item_dim bf16,
-    6.4 GB at 100M rows) is row-sharded over the ranks. Per step and rank: dedupe the shard's
-    256 requests' item ids, all-to-all ids to their owners, owner-side CUDA gather, all-to-all
-    rows back, batch-local table -> sort_set_item_table -> SORT-base forward."""
+    6.4 GB at 100M rows) is row-sharded over the ranks. Per step and rank, inside the C++
+    library (sort_exchange_lookup over NCCL): group the shard's 256 requests' item ids by
+    owner, all-to-all ids to their owners, owner-side CUDA gather, all-to-all rows back,
+    batch-order scatter -> batch-local table -> sort_set_item_table -> SORT-base forward."""
     import torch
     from paper_2603_03988_b200 import runtime as R
     from paper_2603_03988_b200.sharding import ShardedItemTable
@@ -274,17 +276,13 @@ def run_embed(args, cfg, rank, world, local, dist):
     batch["cand_item"] = np.stack([rng.choice(args.table_rows, size=cfg.n_cand, replace=False)
                                    for _ in range(B)]).astype(np.int32)
     tb = {k: torch.from_numpy(v).to(dev) for k, v in batch.items()}
-    table = ShardedItemTable(shard, rows_per_rank, rank, world, stream_ptr=stream.cuda_stream)
+    exchange = R.Exchange.nccl(rank, world, local)
+    table = ShardedItemTable(shard, rows_per_rank, rank, world, exchange, stream_ptr=stream.cuda_stream)
     scores = torch.empty((B, max(cfg.n_cand, 1), 3), dtype=torch.float32, device=dev)
-    lse_t = torch.empty((B, cfg.n_hist), dtype=torch.float32, device=dev)
-    tgt_t = torch.empty((B, cfg.n_hist), dtype=torch.float32, device=dev)
-
-    n_unique = []
 
     def step():
         with torch.cuda.stream(stream):
             rows, mapped = table.lookup(tb)
-            n_unique.append(rows.shape[0])
             model.set_item_table(rows.data_ptr(), rows.shape[0])
             model.forward_device(R._DevBatch(mapped), scores.data_ptr())
             model.sync()
@@ -310,10 +308,11 @@ def run_embed(args, cfg, rank, world, local, dist):
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": workload_desc(cfg) + f" -- item table {args.table_rows} x "
                                                         f"{cfg.item_dim} bf16 row-sharded over {world} rank(s)",
-                       "requests_per_gpu": B, "unique_items_per_step": int(np.mean(n_unique)),
-                       "parallelism": f"dp{world} + row-sharded table, NCCL all-to-all of ids/rows"},
-            "timing": "wall clock per synchronized step (lookup has host-visible sizes), max over ranks",
+                       "requests_per_gpu": B, "ids_per_step": int(B * (cfg.n_hist + cfg.n_cand)),
+                       "parallelism": f"dp{world} + row-sharded table, C++ exchange (NCCL all-to-all of ids/rows)"},
+            "timing": "wall clock per synchronized step (the exchange needs host-visible counts), max over ranks",
         }))
+    exchange.close()
     if dist:
         dist.destroy_process_group()
 

@@ -175,6 +175,11 @@ int sort_mask_intervals(int32_t l_q, int32_t l_kv, int32_t local_window, int32_t
                         const int32_t* roles, const int32_t* position_ids,
                         const int32_t* query_rows, int32_t* lo, int32_t* hi, int32_t* self_idx);
 
+/* Op-level streaming tcgen05 GEMM (the generic path's engine, gemm_stream.cuh), for tests and
+ * op-level callers: C[M, N] = A[M, K] x Bt[N, K]^T with host fp32 buffers, bf16 operands,
+ * fp32 accumulation. N must be a multiple of 32. */
+int sort_op_gemm_bf16(int32_t M, int32_t N, int32_t K, const float* A, const float* Bt, float* C);
+
 /* ---------------------------------------------------------------- instrumentation */
 /* Number of CUDA kernels one sort_forward launches, and per-stage device times (ms) of
  * the last sort_forward when timing was enabled with sort_enable_stage_timing(h, 1).
@@ -226,6 +231,34 @@ int sort_set_item_table(SortHandle h, const void* rows, int64_t n_rows);
  * if an id is outside [0, n_rows). */
 int sort_gather_rows(const void* table, int64_t n_rows, int32_t row_bytes, const int64_t* ids,
                      int64_t n, void* out, void* stream);
+
+/* ---- the exchange itself, in the library (replaces a host-side dedupe + torch all-to-all).
+ * One SortExchange per rank. Transports: NCCL (sort_nccl_unique_id on rank 0, the 128 bytes
+ * broadcast by the caller's own channel, then sort_exchange_create_nccl on every rank;
+ * libnccl.so.2 is resolved from the process at run time) or a host callback (payloads staged
+ * through host memory; any host collective, several ranks may share one GPU). */
+typedef struct SortExchange_* SortExchange;
+/* all-to-all-v of bytes between the `world` ranks: send holds world consecutive blocks of
+ * send_bytes[p] bytes (block p goes to rank p), recv receives recv_bytes[p] from rank p. */
+typedef int (*sort_alltoallv_fn)(void* ctx, const void* send, const int64_t* send_bytes, void* recv,
+                                 const int64_t* recv_bytes, int world);
+/* in-place sum over the ranks of n floats */
+typedef int (*sort_allreduce_fn)(void* ctx, float* buf, int64_t n);
+int sort_nccl_unique_id(void* out_128_bytes);
+int sort_exchange_create_nccl(const void* unique_id_128_bytes, int rank, int world, int device, SortExchange* out);
+int sort_exchange_create_host(sort_alltoallv_fn fn, sort_allreduce_fn reduce_fn, void* ctx, int rank, int world,
+                              int device, SortExchange* out);
+int sort_exchange_destroy(SortExchange x);
+/* Row-sharded lookup: rank r owns table rows [r R, (r+1) R) as `shard` (device, row_bytes per
+ * row, R = rows_per_rank); ids (device int32 [n], global row ids) -> out_rows (device
+ * [n, row_bytes]) with out_rows[i] = table[ids[i]], through two all-to-all exchanges on
+ * `stream`. Every rank calls it (collective). An id outside [0, world R) on ANY rank makes
+ * every rank return status 1 (ConfigError) before any payload moves (tokenizer.cpp:14-19).
+ * Feed out_rows to sort_set_item_table with ids replaced by their positions. */
+int sort_exchange_lookup(SortExchange x, const void* shard, int64_t rows_per_rank, int32_t row_bytes,
+                         const int32_t* ids, int64_t n, void* out_rows, void* stream);
+/* Data-parallel gradient sum: buf (device fp32 [n]) summed over the ranks in place (training). */
+int sort_exchange_allreduce_f32(SortExchange x, float* buf, int64_t n, void* stream);
 
 /* ---------------------------------------------------------------- request ingest */
 /* The reference's JSONL dataset (schema "rankformer.dataset" v1, read_dataset,

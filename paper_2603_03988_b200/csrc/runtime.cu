@@ -15,7 +15,7 @@
 
 #include "../../include/sort_b200.h"
 #include "attention.cuh"
-#include "attention_fixed.cuh"
+#include "attention_fx.cuh"
 #include "block_tail.cuh"
 #include "epilogues.cuh"
 #include "gemm.cuh"
@@ -25,6 +25,7 @@
 #include "tokenizer.cuh"
 #include "train.cuh"
 #include "generic.cuh"
+#include "gemm_stream.cuh"
 #include "moe.cuh"
 #include "pretrain.cuh"
 
@@ -59,7 +60,6 @@ struct LayerDev {
   float logit_bound = 0.f;  // QKNorm logit bound (0 = unknown -> online-max softmax)
   CUtensorMap tmA_in, tmA_q, tmB_all, tmB_qg, tmB_kv, tmA_hg, tmB_o, tmB_up, tmA_hid, tmB_down;
   CUtensorMap tmQ, tmK, tmV;
-  CUtensorMap tmK64, tmV64;  // 64-row K/V boxes (k_attention_f subtiles)
   CUtensorMap tmRopeKV, tmRopeQ;  // per-row RoPE side tables for the K/V rows and the Q rows
   CUtensorMap tmWo_t, tmWup_t, tmWdown_t;  // k_block_tail weight stages
   CUtensorMap tmWo_p, tmWup_p, tmWdown_p;  // ... as a CTA pair (each CTA loads half the rows)
@@ -89,7 +89,7 @@ struct Handle {
   bool tail_pair = false;  // sort_set_option("tail_pair"): block tail as CTA pairs (cta_group::2)
   bool attn_bwd_mma = true; // sort_set_option("attn_bwd_mma"): tensor-core attention backward
   bool qkvg_pair = false;   // sort_set_option("qkvg_pair"): QKVG projection as CTA pairs
-  bool attn_sub = false;    // sort_set_option("attn_subtiles"): k_attention_f in fixed-reference mode
+  bool attn_fx = false;     // sort_set_option("attn_fx"): fixed-reference layers run k_attn_fx (0: k_attention)
   bool generic = false;    // d > 256 (SORT-large): projections through the generic path
   // ---- MoE FFN: routed + shared experts as grouped tcgen05 GEMMs
   bool moe = false;
@@ -115,6 +115,9 @@ struct Handle {
   // a flat fp32 gradient buffer, saved forward activations per layer, workspace
   std::map<std::string, float*> w32;
   std::map<std::string, __nv_bfloat16*> w16;  // bf16 copies for the generic path's GEMMs
+  std::map<std::string, __nv_bfloat16*> wT;   // bf16 K-major (transposed) weights of the streaming GEMMs
+  std::map<std::tuple<const void*, uint64_t, uint64_t, uint64_t, uint32_t>, CUtensorMap> gs_maps;
+  bool stream_gemm = true;  // sort_set_option("stream_gemm"): generic path on k_gemm_stream (0: cuBLAS)
   std::map<std::string, std::pair<__nv_bfloat16*, size_t>> tw16;  // training: bf16 weights of the FFN backward
   std::map<std::string, std::pair<size_t, std::pair<int64_t, int64_t>>> grad_index;  // offset, shape
   float* grads = nullptr;
@@ -558,9 +561,6 @@ static void finalize(Handle& h) {
       uint64_t skd[2] = {static_cast<uint64_t>(dk) * 2, static_cast<uint64_t>(L.Rkv) * dk * 2};
       L.tmK = make_tmap_bf16(h.Kb, 3, dkd, skd, bq, dk * 2);
       L.tmV = make_tmap_bf16(h.Vb, 3, dkd, skd, bq, dk * 2);
-      uint32_t b64[3] = {static_cast<uint32_t>(dk), 64, 1};
-      L.tmK64 = make_tmap_bf16(h.Kb, 3, dkd, skd, b64, dk * 2);
-      L.tmV64 = make_tmap_bf16(h.Vb, 3, dkd, skd, b64, dk * 2);
     }
   }
   // ---- head (fp32)
@@ -749,13 +749,16 @@ static void launch_attention_dk(Handle& h, const LayerDev& L, const LayerPlan& l
   a.ref_log2 = L.logit_bound * 1.4426950408889634f;
   const int n_items = lp.n_qtiles * B * h.H;
   const int tile_ints = 2 * lp.n_qtiles + 2 + 2 * n_codes;
+  const CUtensorMap& tq = h.save_to ? h.save_to->tmQ : L.tmQ;
+  const CUtensorMap& tk = h.save_to ? h.save_to->tmK : L.tmK;
+  const CUtensorMap& tv = h.save_to ? h.save_to->tmV : L.tmV;
   if constexpr (kFixed) {
-    if (h.attn_sub && !h.save_to) {  // fixed reference: 64-column subtiles, O accumulated in TMEM
-      const size_t smem_f = AttnFLayout<DK>::bytes(tile_ints);
-      ensure_smem(k_attention_f<DK>, smem_f);
-      const int grid_f = std::min(n_items, 2 * h.num_sms);
-      k_attention_f<DK><<<grid_f, kAttnThreads, smem_f, h.stream>>>(L.tmQ, L.tmK64, L.tmV64, a);
-      check_launch("attention (subtiles)");
+    if (h.attn_fx) {  // fixed reference: O accumulated in TMEM (attention_fx.cuh)
+      const size_t smem_f = AttnSmem<DK>::bytes(tile_ints);
+      ensure_smem(k_attn_fx<DK>, smem_f);
+      const int grid_f = std::min(n_items, FxTmem<DK>::kCtasPerSm * h.num_sms);
+      k_attn_fx<DK><<<grid_f, kAttnThreads, smem_f, h.stream>>>(tq, tk, tv, a);
+      check_launch("attention");
       ++h.launches;
       return;
     }
@@ -763,9 +766,6 @@ static void launch_attention_dk(Handle& h, const LayerDev& L, const LayerPlan& l
   const size_t smem = AttnSmem<DK>::bytes(tile_ints);
   ensure_smem(k_attention<DK, kFixed>, smem);
   const int grid = std::min(n_items, AttnTmem<DK>::kCtasPerSm * h.num_sms);
-  const CUtensorMap& tq = h.save_to ? h.save_to->tmQ : L.tmQ;
-  const CUtensorMap& tk = h.save_to ? h.save_to->tmK : L.tmK;
-  const CUtensorMap& tv = h.save_to ? h.save_to->tmV : L.tmV;
   k_attention<DK, kFixed><<<grid, kAttnThreads, smem, h.stream>>>(tq, tk, tv, a);
   check_launch("attention");
   ++h.launches;
@@ -1679,6 +1679,56 @@ static const __nv_bfloat16* w16_cat(Handle& h, const std::string& key, const std
   return h.w16[key] = dst;
 }
 
+// ---- streaming tcgen05 GEMM (gemm_stream.cuh) for the generic path
+static const CUtensorMap& gs_map(Handle& h, const void* p, uint64_t rows, uint64_t cols, uint64_t ld,
+                                 uint32_t box_rows) {
+  const auto key = std::make_tuple(p, rows, cols, ld, box_rows);
+  auto it = h.gs_maps.find(key);
+  if (it != h.gs_maps.end()) return it->second;
+  return h.gs_maps[key] = make_tmap_2d(p, rows, cols, ld, box_rows, kGsBK, 128);
+}
+
+// C[M, N] = A[M, K] (row pitch lda) x Bt[N, K]^T (row pitch ldb), epilogue functor epi
+template <class Epi>
+static void gemm_stream(Handle& h, const __nv_bfloat16* A, int lda, int M, int K, const __nv_bfloat16* Bt, int ldb,
+                        int N, const Epi& epi) {
+  if (M <= 0 || N <= 0) return;
+  if (N % Epi::kChunk != 0) throw ConfigError("stream gemm: N must be a multiple of the epilogue chunk");
+  const CUtensorMap& ta = gs_map(h, A, M, K, lda, kGsBM);
+  const CUtensorMap& tb = gs_map(h, Bt, N, K, ldb, kGsBN);
+  ensure_smem(k_gemm_stream<Epi>, kGsSmem);
+  const int tiles = ((M + kGsBM - 1) / kGsBM) * ((N + kGsBN - 1) / kGsBN);
+  k_gemm_stream<Epi><<<std::min(tiles, h.num_sms), kGsThreads, kGsSmem, h.stream>>>(ta, tb, M, N, K, epi);
+  check_launch("stream gemm");
+  ++h.launches;
+}
+
+// bf16 K-major B operand [sum N_i, ldk] of the column-concatenated [K, N_i] fp32 weights
+// `parts` (reference [in, out] layout); swiglu: the two parts (w_gate, w_up) are interleaved in
+// 32-row blocks [gate_j | up_j] for EpiSwiGLU. ldk = K rounded up to 8 (16-byte TMA pitch).
+static const __nv_bfloat16* wT16(Handle& h, const std::string& key, const std::vector<std::string>& parts,
+                                 bool swiglu = false) {
+  auto it = h.wT.find(key);
+  if (it != h.wT.end()) return it->second;
+  const auto& g0 = h.grad_index.at(parts[0]).second;
+  const int K = static_cast<int>(g0.first), ldk = (K + 7) & ~7;
+  int Ntot = 0;
+  for (const auto& p : parts) Ntot += static_cast<int>(h.grad_index.at(p).second.second);
+  __nv_bfloat16* dst = h.dalloc<__nv_bfloat16>(static_cast<size_t>(Ntot) * ldk);
+  int row0 = 0;
+  for (size_t i = 0; i < parts.size(); ++i) {
+    const auto& gi = h.grad_index.at(parts[i]).second;
+    if (gi.first != K) throw ConfigError("wT16: parts with different input widths");
+    const int N = static_cast<int>(gi.second);
+    const dim3 grid((ldk + 31) / 32, (N + 31) / 32);
+    k_transpose_bf16<<<grid, 256, 0, h.stream>>>(h.w32.at(parts[i]), K, N, ldk, row0, swiglu ? 32 : 0,
+                                                 swiglu ? static_cast<int>(i) * 32 : 0, dst);
+    row0 += N;
+  }
+  check_launch("weight transpose");
+  return h.wT[key] = dst;
+}
+
 static void forward_generic(Handle& h, int B) {
   ensure_generic_buffers(h);
   CK(cublasSetStream(h.cublas, h.stream) == CUBLAS_STATUS_SUCCESS ? cudaSuccess : cudaErrorUnknown);
@@ -1694,7 +1744,13 @@ static void forward_generic(Handle& h, int B) {
     if (gcount[g] == 0) continue;
     __nv_bfloat16* cat = reinterpret_cast<__nv_bfloat16*>(h.gw[8]);
     k_tok_concat<<<warp_rows_grid(gcount[g]), 256, 0, h.stream>>>(tp, g, gK[g], cat, h.g_rows);
-    gemm_rm_bf16(h, gcount[g], d, gK[g], cat, gK[g], w16(h, std::string("tok.w_") + gname[g]), d, h.gw[0], d);
+    if (h.stream_gemm) {
+      const std::string wn = std::string("tok.w_") + gname[g];
+      gemm_stream(h, cat, gK[g], gcount[g], gK[g], wT16(h, wn + "^T", {wn}), (gK[g] + 7) & ~7, d,
+                  GsStore<float>{h.gw[0], d});
+    } else {
+      gemm_rm_bf16(h, gcount[g], d, gK[g], cat, gK[g], w16(h, std::string("tok.w_") + gname[g]), d, h.gw[0], d);
+    }
     k_tok_finish<<<warp_rows_grid(gcount[g]), 256, 0, h.stream>>>(h.gw[0], w32(h, std::string("tok.b_") + gname[g]),
                                                                 w32(h, std::string("tok.g_") + gname[g]), h.g_rows,
                                                                 gcount[g], d, X);
@@ -1725,27 +1781,48 @@ static void forward_generic(Handle& h, int B) {
     }
     // bf16 projection outputs (fp32 accumulation), consumed by the per-head prep: two GEMMs
     // with column-concatenated weights, [Wq | Wg] on the query rows and [Wk | Wv] on all rows
-    __nv_bfloat16* pqg = reinterpret_cast<__nv_bfloat16*>(h.gw[2]);  // [M, 2d]
-    __nv_bfloat16* pkv = reinterpret_cast<__nv_bfloat16*>(h.gw[3]);  // [Mkv, 2d]
-    gemm_rm_bf16(h, M, 2 * d, d, xqp, d, w16_cat(h, A + "wq|wg", {A + "wq", A + "wg"}), 2 * d, pqg, 2 * d, 0.f, true);
-    gemm_rm_bf16(h, Mkv, 2 * d, d, xn, d, w16_cat(h, A + "wk|wv", {A + "wk", A + "wv"}), 2 * d, pkv, 2 * d, 0.f, true);
-    qkv_prep(h, pqg, 2 * d, M, L.Rq, H, dk, 0, L.pos_q, L.gain_q, h.Qb);
-    qkv_prep(h, pkv, 2 * d, Mkv, L.Rkv, H, dk, 1, L.pos_kv, L.gain_k, h.Kb);
-    qkv_prep(h, pkv + d, 2 * d, Mkv, L.Rkv, H, dk, 2, nullptr, nullptr, h.Vb);
-    qkv_prep(h, pqg + d, 2 * d, M, L.Rq, H, dk, 3, nullptr, nullptr, h.Gb);
+    const bool sg = h.stream_gemm && dk == 64;
+    if (sg) {
+      // [Wq | Wg] on the query rows, [Wk | Wv] on all rows; QKNorm + RoPE + head-major layout
+      // (and the sigmoid gate) in the epilogue, straight from the fp32 accumulators
+      gemm_stream(h, xqp, d, M, d, wT16(h, A + "wq|wg^T", {A + "wq", A + "wg"}), d, 2 * d,
+                  GsQKVG{d, H, L.Rq, L.pos_q, h.rope, L.gain_q, h.Qb, h.Gb, true});
+      gemm_stream(h, xn, d, Mkv, d, wT16(h, A + "wk|wv^T", {A + "wk", A + "wv"}), d, 2 * d,
+                  GsQKVG{d, H, L.Rkv, L.pos_kv, h.rope, L.gain_k, h.Kb, h.Vb, false});
+    } else {
+      __nv_bfloat16* pqg = reinterpret_cast<__nv_bfloat16*>(h.gw[2]);  // [M, 2d]
+      __nv_bfloat16* pkv = reinterpret_cast<__nv_bfloat16*>(h.gw[3]);  // [Mkv, 2d]
+      gemm_rm_bf16(h, M, 2 * d, d, xqp, d, w16_cat(h, A + "wq|wg", {A + "wq", A + "wg"}), 2 * d, pqg, 2 * d, 0.f, true);
+      gemm_rm_bf16(h, Mkv, 2 * d, d, xn, d, w16_cat(h, A + "wk|wv", {A + "wk", A + "wv"}), 2 * d, pkv, 2 * d, 0.f, true);
+      qkv_prep(h, pqg, 2 * d, M, L.Rq, H, dk, 0, L.pos_q, L.gain_q, h.Qb);
+      qkv_prep(h, pkv, 2 * d, Mkv, L.Rkv, H, dk, 1, L.pos_kv, L.gain_k, h.Kb);
+      qkv_prep(h, pkv + d, 2 * d, Mkv, L.Rkv, H, dk, 2, nullptr, nullptr, h.Vb);
+      qkv_prep(h, pqg + d, 2 * d, M, L.Rq, H, dk, 3, nullptr, nullptr, h.Gb);
+    }
     check_launch("generic projections");
     stage_mark(h, "L" + sl + ".qkvg");
     launch_attention(h, L, lp, B);  // tcgen05 core; writes the gated output to h.Hg
     stage_mark(h, "L" + sl + ".attention");
-    gemm_rm_bf16(h, M, d, d, h.Hg, d, w16(h, A + "wo"), d, h.gw[2], d);
-    // x1 = P(x) + attn (kept fp32 in xo), then RMSN(x1) -> bf16 FFN input, in one pass
     __nv_bfloat16* xf = reinterpret_cast<__nv_bfloat16*>(h.gw[1]);
-    resid_rmsnorm(h, x, L.query_rows, L.Rq, L.Rkv, h.gw[2], w32(h, Bk + "ffn_norm"), M, d, xo, xf);
-    __nv_bfloat16* gu = reinterpret_cast<__nv_bfloat16*>(h.gw[6]);  // bf16 [gate | up] pre-activations
-    gemm_rm_bf16(h, M, 2 * m, d, xf, d, w16(h, F + "w_gu"), 2 * m, gu, 2 * m, 0.f, true);
     __nv_bfloat16* z = reinterpret_cast<__nv_bfloat16*>(h.gw[7]);
-    k_swiglu_z<__nv_bfloat16, __nv_bfloat16><<<ew_grid(static_cast<size_t>(M) * m / 8), 256, 0, h.stream>>>(gu, M, m, z);
-    gemm_rm_bf16(h, M, d, m, z, m, w16(h, F + "w_down"), d, xo, d, 1.f);
+    if (h.stream_gemm) {
+      // x1 = P(x) + attn Wo (fp32, in xo) in the epilogue; RMSN(x1) -> bf16 FFN input; up
+      // projection with SwishGLU in the epilogue -> z; down projection accumulating into x1
+      gemm_stream(h, h.Hg, d, M, d, wT16(h, A + "wo^T", {A + "wo"}), d, d,
+                  GsResidF32{x, L.query_rows, L.Rq, L.Rkv, d, xo});
+      resid_rmsnorm(h, xo, nullptr, 1, 1, nullptr, w32(h, Bk + "ffn_norm"), M, d, nullptr, xf);
+      gemm_stream(h, xf, d, M, d, wT16(h, F + "w_gate|w_up^T", {F + "w_gate", F + "w_up"}, true), d, 2 * m,
+                  GsSwiGLU{z, m});
+      gemm_stream(h, z, m, M, m, wT16(h, F + "w_down^T", {F + "w_down"}), m, d, GsAccF32{xo, d});
+    } else {
+      gemm_rm_bf16(h, M, d, d, h.Hg, d, w16(h, A + "wo"), d, h.gw[2], d);
+      // x1 = P(x) + attn (kept fp32 in xo), then RMSN(x1) -> bf16 FFN input, in one pass
+      resid_rmsnorm(h, x, L.query_rows, L.Rq, L.Rkv, h.gw[2], w32(h, Bk + "ffn_norm"), M, d, xo, xf);
+      __nv_bfloat16* gu = reinterpret_cast<__nv_bfloat16*>(h.gw[6]);  // bf16 [gate | up] pre-activations
+      gemm_rm_bf16(h, M, 2 * m, d, xf, d, w16(h, F + "w_gu"), 2 * m, gu, 2 * m, 0.f, true);
+      k_swiglu_z<__nv_bfloat16, __nv_bfloat16><<<ew_grid(static_cast<size_t>(M) * m / 8), 256, 0, h.stream>>>(gu, M, m, z);
+      gemm_rm_bf16(h, M, d, m, z, m, w16(h, F + "w_down"), d, xo, d, 1.f);
+    }
     check_launch("generic block tail");
     stage_mark(h, "L" + sl + ".tail");
     cur = 1 - cur;
@@ -2004,6 +2081,8 @@ static std::vector<float> bf16_to_f32(const std::vector<__nv_bfloat16>& v) {
 
 using namespace sortk;
 
+#include "exchange.cuh"
+
 // ======================================================================= C ABI
 extern "C" {
 
@@ -2250,6 +2329,30 @@ int sort_attention_forward(SortHandle p, int layer, int32_t batch, const float* 
   });
 }
 
+int sort_op_gemm_bf16(int32_t M, int32_t N, int32_t K, const float* A, const float* Bt, float* C) {
+  return api([&] {
+    if (M < 0 || N < 0 || K < 1 || (M && (!A || !C)) || (N && !Bt)) throw ConfigError("op gemm: bad arguments");
+    if (N % 32) throw ConfigError("op gemm: N must be a multiple of 32");
+    if (M == 0 || N == 0) return;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    Handle h;  // a bare context: default stream, no plan
+    h.device = dev;
+    CK(cudaDeviceGetAttribute(&h.num_sms, cudaDevAttrMultiProcessorCount, dev));
+    const int ldk = (K + 7) & ~7;
+    std::vector<__nv_bfloat16> a(static_cast<size_t>(M) * ldk, f2bf(0.f)), b(static_cast<size_t>(N) * ldk, f2bf(0.f));
+    for (int i = 0; i < M; ++i)
+      for (int k = 0; k < K; ++k) a[static_cast<size_t>(i) * ldk + k] = f2bf(A[static_cast<size_t>(i) * K + k]);
+    for (int i = 0; i < N; ++i)
+      for (int k = 0; k < K; ++k) b[static_cast<size_t>(i) * ldk + k] = f2bf(Bt[static_cast<size_t>(i) * K + k]);
+    const __nv_bfloat16* da = h.upload(a);
+    const __nv_bfloat16* db = h.upload(b);
+    float* dc = h.dalloc<float>(static_cast<size_t>(M) * N);
+    gemm_stream(h, da, ldk, M, K, db, ldk, N, GsStore<float>{dc, N});
+    CK(cudaMemcpy(C, dc, sizeof(float) * M * N, cudaMemcpyDeviceToHost));
+  });
+}
+
 int sort_block_attention(int32_t nh, int32_t l_q, int32_t l_kv, int32_t dk, const float* q,
                          const float* k, const float* v, const int32_t* lo, const int32_t* hi,
                          const int32_t* self_idx, float* out, int64_t* skipped, int64_t* total) {
@@ -2303,9 +2406,6 @@ int sort_block_attention(int32_t nh, int32_t l_q, int32_t l_kv, int32_t dk, cons
     uint64_t skd[2] = {static_cast<uint64_t>(dk) * 2, static_cast<uint64_t>(l_kv) * dk * 2};
     L.tmK = make_tmap_bf16(h.Kb, 3, dkd, skd, bq, dk * 2);
     L.tmV = make_tmap_bf16(h.Vb, 3, dkd, skd, bq, dk * 2);
-    uint32_t b64[3] = {static_cast<uint32_t>(dk), 64, 1};
-    L.tmK64 = make_tmap_bf16(h.Kb, 3, dkd, skd, b64, dk * 2);
-    L.tmV64 = make_tmap_bf16(h.Vb, 3, dkd, skd, b64, dk * 2);
     launch_attention(h, L, lp, nh);
     std::vector<__nv_bfloat16> ob(static_cast<size_t>(nh) * l_q * dk);
     CK(cudaMemcpyAsync(ob.data(), h.Hg, ob.size() * 2, cudaMemcpyDeviceToHost, h.stream));
@@ -2642,8 +2742,10 @@ int sort_set_option(SortHandle p, const char* name, int32_t value) {
       h->attn_bwd_mma = value != 0;
     } else if (std::strcmp(name, "qkvg_pair") == 0) {
       h->qkvg_pair = value != 0;
-    } else if (std::strcmp(name, "attn_subtiles") == 0) {
-      h->attn_sub = value != 0;
+    } else if (std::strcmp(name, "attn_fx") == 0) {
+      h->attn_fx = value != 0;
+    } else if (std::strcmp(name, "stream_gemm") == 0) {
+      h->stream_gemm = value != 0;
     } else if (std::strcmp(name, "moe_fused") == 0) {
       h->moe_fused = value != 0;
     } else {

@@ -62,9 +62,16 @@ EXPORTS = [
     "sort_get_param", "sort_dataset_open", "sort_dataset_close", "sort_dataset_size",
     "sort_dataset_batch", "sort_moe_routing", "sort_moe_load", "sort_moe_update_bias",
     "sort_moe_forward", "sort_pretrain_forward", "sort_forward_async",
+    "sort_nccl_unique_id", "sort_exchange_create_nccl", "sort_exchange_create_host",
+    "sort_exchange_destroy", "sort_exchange_lookup", "sort_exchange_allreduce_f32", "sort_op_gemm_bf16",
 ]
 
 _lib = None
+
+# host-transport callbacks of the exchange (sort_alltoallv_fn / sort_allreduce_fn)
+ALLTOALLV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.c_void_p,
+                           C.POINTER(C.c_int64), C.c_int)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_float), C.c_int64)
 
 
 def lib():
@@ -120,6 +127,15 @@ def lib():
         L.sort_gather_rows.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int64,
                                        C.c_void_p, C.c_void_p]
         L.sort_stage_times.argtypes = [C.c_void_p, f32p, C.c_int32, i32p, C.c_char_p, C.c_int32]
+        L.sort_nccl_unique_id.argtypes = [C.c_void_p]
+        L.sort_exchange_create_nccl.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+        L.sort_exchange_create_host.argtypes = [ALLTOALLV_FN, ALLREDUCE_FN, C.c_void_p, C.c_int, C.c_int, C.c_int,
+                                                C.POINTER(C.c_void_p)]
+        L.sort_exchange_destroy.argtypes = [C.c_void_p]
+        L.sort_exchange_lookup.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int64,
+                                           C.c_void_p, C.c_void_p]
+        L.sort_exchange_allreduce_f32.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
+        L.sort_op_gemm_bf16.argtypes = [C.c_int32, C.c_int32, C.c_int32, f32p, f32p, f32p]
         _lib = L
     return _lib
 
@@ -243,6 +259,10 @@ class SortModel:
             _check(lib().sort_load_param(self.h, name.encode(), _p(a32, f32p), a32.shape[0],
                                          a32.shape[1]))
         _check(lib().sort_finalize_params(self.h))
+        # experiments only: SORT_OPTIONS="attn_fx=0,graphs=1" sets library options (A/B runs)
+        for kv in filter(None, os.environ.get("SORT_OPTIONS", "").split(",")):
+            k, v = kv.split("=")
+            self.set_option(k.strip(), int(v))
 
     def close(self):
         if getattr(self, "h", None) is not None and _lib is not None:
@@ -445,12 +465,109 @@ class SortModel:
         return dict(zip(keys, ms[: n.value].tolist()))
 
 
+def op_gemm(A: np.ndarray, Bt: np.ndarray) -> np.ndarray:
+    """C = A Bt^T on the streaming tcgen05 GEMM (bf16 operands, fp32 accumulation)."""
+    A = np.ascontiguousarray(A, np.float32)
+    Bt = np.ascontiguousarray(Bt, np.float32)
+    C_ = np.zeros((A.shape[0], Bt.shape[0]), np.float32)
+    _check(lib().sort_op_gemm_bf16(A.shape[0], Bt.shape[0], A.shape[1], _p(A, f32p), _p(Bt, f32p), _p(C_, f32p)))
+    return C_
+
+
 def gather_rows(table_ptr: int, n_rows: int, row_bytes: int, ids_ptr: int, n: int, out_ptr: int,
                 stream_ptr: int = 0) -> None:
     """out[i] = table[ids[i]] on the device (the owner-local step of a sharded lookup)."""
     _check(lib().sort_gather_rows(C.c_void_p(table_ptr), int(n_rows), int(row_bytes),
                                   C.c_void_p(ids_ptr), int(n), C.c_void_p(out_ptr),
                                   C.c_void_p(stream_ptr) if stream_ptr else None))
+
+
+class Exchange:
+    """One rank's end of the library's cross-rank exchange (csrc/exchange.cuh): the
+    row-sharded item lookup and the data-parallel gradient sum, run by the C++ host.
+
+    Exchange.nccl(rank, world, device): NCCL communicator (the 128-byte unique id is made on
+    rank 0 and broadcast over the torch.distributed group). Exchange.host(rank, world,
+    device): payloads staged through host memory and moved by torch.distributed collectives
+    of the current (e.g. gloo) group -- several ranks may share one GPU (tests)."""
+
+    def __init__(self, handle, keep=()):
+        self.h = handle
+        self._keep = keep  # the ctypes callbacks must outlive the handle
+
+    @classmethod
+    def nccl(cls, rank: int, world: int, device: int = 0, group=None):
+        uid = (C.c_uint8 * 128)()
+        if rank == 0:
+            _check(lib().sort_nccl_unique_id(uid))
+        if world > 1:
+            import torch.distributed as dist
+            obj = [bytes(uid)]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            C.memmove(uid, obj[0], 128)
+        h = C.c_void_p()
+        _check(lib().sort_exchange_create_nccl(uid, rank, world, device, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def host(cls, rank: int, world: int, device: int = 0, group=None):
+        fa, fr = host_transport(group)
+        h = C.c_void_p()
+        _check(lib().sort_exchange_create_host(fa, fr, None, rank, world, device, C.byref(h)))
+        return cls(h, (fa, fr))
+
+    def close(self):
+        if getattr(self, "h", None) is not None and _lib is not None:
+            _lib.sort_exchange_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def lookup(self, shard_ptr: int, rows_per_rank: int, row_bytes: int, ids_ptr: int, n: int, out_ptr: int,
+               stream_ptr: int = 0):
+        """out[i] = table[ids[i]] for global ids against the row-sharded table (collective)."""
+        _check(lib().sort_exchange_lookup(self.h, C.c_void_p(shard_ptr), int(rows_per_rank), int(row_bytes),
+                                          C.c_void_p(ids_ptr), int(n), C.c_void_p(out_ptr),
+                                          C.c_void_p(stream_ptr) if stream_ptr else None))
+
+    def allreduce(self, buf_ptr: int, n: int, stream_ptr: int = 0):
+        _check(lib().sort_exchange_allreduce_f32(self.h, C.c_void_p(buf_ptr), int(n),
+                                                 C.c_void_p(stream_ptr) if stream_ptr else None))
+
+
+def host_transport(group=None):
+    """The (alltoallv, allreduce) host callbacks over torch.distributed CPU collectives."""
+    import torch
+    import torch.distributed as dist
+
+    def a2a(ctx, send, send_bytes, recv, recv_bytes, world):
+        try:
+            sb = [int(send_bytes[i]) for i in range(world)]
+            rb = [int(recv_bytes[i]) for i in range(world)]
+            src = (torch.frombuffer((C.c_uint8 * sum(sb)).from_address(send), dtype=torch.uint8)
+                   if sum(sb) else torch.empty(0, dtype=torch.uint8))
+            out = torch.empty(sum(rb), dtype=torch.uint8)
+            dist.all_to_all_single(out, src.clone(), rb, sb, group=group)
+            if sum(rb):
+                C.memmove(recv, out.data_ptr(), sum(rb))
+            return 0
+        except Exception:  # noqa: BLE001 -- reported to the library as a failed callback
+            return 1
+
+    def red(ctx, buf, n):
+        try:
+            if int(n) == 0:
+                return 0
+            t = torch.frombuffer((C.c_float * int(n)).from_address(C.addressof(buf.contents)), dtype=torch.float32)
+            tmp = t.clone()
+            dist.all_reduce(tmp, group=group)
+            t.copy_(tmp)
+            return 0
+        except Exception:  # noqa: BLE001
+            return 1
+
+    return ALLTOALLV_FN(a2a), ALLREDUCE_FN(red)
 
 
 class Dataset:

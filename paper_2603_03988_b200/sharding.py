@@ -76,71 +76,33 @@ class ShardedItemTable:
     """Row-sharded item embedding table ("embedding-heavy": a
     100M-row table split over the GPUs of one node). Rank r owns global rows
     [r * rows_per_rank, (r + 1) * rows_per_rank) in `shard` (a torch tensor [rows, dim] on
-    this rank's device). lookup() serves one batch:
+    this rank's device). lookup() serves one batch through the library's C++ exchange
+    (runtime.Exchange -> sort_exchange_lookup, csrc/exchange.cuh): ids grouped by owner on
+    the device, ids to the owners and rows back by two all-to-all exchanges (NCCL, or the
+    host transport), the owner gather and the batch-order scatter as CUDA kernels. It
+    returns the batch-local table (row i = item row of the batch's i-th id, history ids first,
+    then candidate ids) and the batch with ids replaced by those positions, ready for
+    SortModel.set_item_table() (the reference reads item_table_.value.row(id) from its own
+    table, tokenizer.cpp:95-127)."""
 
-      1. dedupe the batch's item ids (history + candidates)          torch.unique
-      2. exchange per-owner counts, then the ids                      all_to_all (NCCL)
-      3. each owner gathers its rows                                  sort_gather_rows
-      4. rows travel back in the requester's unique-id order          all_to_all (NCCL)
-
-    and returns the batch-local table plus the batch with ids remapped into it, ready for
-    SortModel.set_item_table(). `gather(shard, local_ids) -> rows` defaults to the CUDA
-    kernel; the CPU gloo tests pass torch.index_select to exercise the exchange logic."""
-
-    def __init__(self, shard, rows_per_rank: int, rank: int, world: int, group=None, gather=None,
-                 stream_ptr: int = 0):
-        self.shard, self.R, self.rank, self.world, self.group = shard, rows_per_rank, rank, world, group
-        self.stream_ptr = stream_ptr
-        self.gather = gather or self._cuda_gather
-
-    def _cuda_gather(self, shard, local_ids):
-        import torch
-        from . import runtime as R
-        out = torch.empty((local_ids.numel(), shard.shape[1]), dtype=shard.dtype, device=shard.device)
-        R.gather_rows(shard.data_ptr(), shard.shape[0], shard.shape[1] * shard.element_size(),
-                      local_ids.data_ptr(), local_ids.numel(), out.data_ptr(), self.stream_ptr)
-        return out
-
-    def _a2a(self, out, inp, out_splits, in_splits):
-        import torch.distributed as dist
-        dist.all_to_all_single(out, inp, out_splits, in_splits, group=self.group)
+    def __init__(self, shard, rows_per_rank: int, rank: int, world: int, exchange, stream_ptr: int = 0):
+        self.shard, self.R, self.rank, self.world = shard, rows_per_rank, rank, world
+        self.x, self.stream_ptr = exchange, stream_ptr
+        self._iota = {}
 
     def lookup(self, batch: Dict):
-        """batch: dict of torch tensors with "hist_item" [B, H] and "cand_item" [B, N] on this
-        rank's device. Returns (table [n_unique, dim], batch with remapped int32 item ids)."""
         import torch
         hist, cand = batch["hist_item"], batch["cand_item"]
-        ids = torch.cat([hist.reshape(-1), cand.reshape(-1)]).to(torch.int64)
-        uniq, inv = torch.unique(ids, sorted=True, return_inverse=True)
-        # range check BEFORE any collective, agreed over the ranks: a rank that raised alone
-        # would leave its peers blocked inside the all-to-all (reference: check_id,
-        # tokenizer.cpp:14-19 -> ConfigError)
-        bad = torch.zeros(1, dtype=torch.int32, device=ids.device)
-        if uniq.numel():
-            bad[0] = ((uniq[0] < 0) | (uniq[-1] >= self.world * self.R)).to(torch.int32)
-        if self.world > 1:
-            import torch.distributed as dist
-            dist.all_reduce(bad, op=dist.ReduceOp.MAX, group=self.group)
-        if int(bad.item()):
-            from .config import ConfigError
-            raise ConfigError(f"tokenizer: item id outside vocabulary of size {self.world * self.R} "
-                              f"(sharded table, detected on at least one rank)")
-        owner = torch.div(uniq, self.R, rounding_mode="floor")
-        if self.world == 1:
-            rows = self.gather(self.shard, uniq)
-        else:
-            send = torch.bincount(owner, minlength=self.world)
-            recv = torch.empty_like(send)
-            self._a2a(recv, send, [1] * self.world, [1] * self.world)
-            send_l, recv_l = send.tolist(), recv.tolist()
-            req = torch.empty(sum(recv_l), dtype=torch.int64, device=ids.device)
-            self._a2a(req, uniq, recv_l, send_l)
-            local = self.gather(self.shard, req - self.rank * self.R)
-            dim = self.shard.shape[1]
-            rows = torch.empty((uniq.numel(), dim), dtype=self.shard.dtype, device=ids.device)
-            self._a2a(rows.view(-1), local.reshape(-1), [n * dim for n in send_l], [n * dim for n in recv_l])
+        ids = torch.cat([hist.reshape(-1), cand.reshape(-1)]).to(torch.int32).contiguous()
+        n, dim = ids.numel(), self.shard.shape[1]
+        rows = torch.empty((n, dim), dtype=self.shard.dtype, device=ids.device)
+        self.x.lookup(self.shard.data_ptr(), self.R, dim * self.shard.element_size(), ids.data_ptr(), n,
+                      rows.data_ptr(), self.stream_ptr)
+        key = (tuple(hist.shape), tuple(cand.shape), ids.device)
+        if key not in self._iota:
+            nh = hist.numel()
+            pos = torch.arange(n, dtype=torch.int32, device=ids.device)
+            self._iota[key] = (pos[:nh].reshape(hist.shape).contiguous(), pos[nh:].reshape(cand.shape).contiguous())
         out = dict(batch)
-        nh = hist.numel()
-        out["hist_item"] = inv[:nh].reshape(hist.shape).to(torch.int32).contiguous()
-        out["cand_item"] = inv[nh:].reshape(cand.shape).to(torch.int32).contiguous()
+        out["hist_item"], out["cand_item"] = self._iota[key]
         return rows, out

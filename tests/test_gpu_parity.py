@@ -16,6 +16,7 @@ import numpy as np
 import pytest
 
 import oracle as O
+import ref as RF
 from paper_2603_03988_b200 import runtime as R
 from paper_2603_03988_b200 import synth
 from paper_2603_03988_b200.config import (ROLE_CAND, ROLE_HIST, base_config, tiny_config)
@@ -24,7 +25,7 @@ pytestmark = pytest.mark.gpu
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 TOKEN_TOL = 1.0 / 64        # bf16 half-ulp at |x| < 4 is <= 1/128; tokens are O(1)
-LOGIT_MAX_ABS = 5e-2        # bf16 block stack vs fp64 oracle, max over all logits
+LOGIT_MAX_ABS = 2e-2        # bf16 block stack vs fp64 oracle, max over all logits
 LOGIT_REL_L2 = 1e-2         # ||z_gpu - z_ref|| / ||z_ref||
 ATTN_REL_L2 = 1e-2
 
@@ -411,19 +412,20 @@ def test_forward_async_pipeline_matches_sync(tiny):
 
 
 @pytest.mark.parametrize("which", ["tiny", "base"])
-def test_subtile_attention_option_matches_default(which, tiny, base):
-    """k_attention_f (64-column subtiles, O accumulated in TMEM; sort_set_option
-    "attn_subtiles") computes the same P = exp2(s - B) in bf16 as k_attention and only sums
-    the P V products in another order; through 4 layers of bf16 activations those fp32
-    differences flip bf16 roundings, so the bar is the bf16 one (LOGIT_REL_L2)."""
+def test_tmem_accumulating_attention_matches_register_fold(which, tiny, base):
+    """k_attn_fx (fixed reference, O accumulated in TMEM across kv tiles; the default) and
+    k_attention (O of each kv tile folded through registers; sort_set_option("attn_fx", 0))
+    compute the same P = exp2(s - B) in bf16 and only sum the P V products in another order;
+    through 4 layers of bf16 activations those fp32 differences flip bf16 roundings, so the
+    bar is the bf16 one (LOGIT_REL_L2)."""
     cfg, P, gm, _ = tiny if which == "tiny" else base
     b = synth.make_batch(cfg, 2, seed=77)
     _, z0 = gm.forward_logits(b)
-    gm.set_option("attn_subtiles", 1)
+    gm.set_option("attn_fx", 0)
     try:
         _, z1 = gm.forward_logits(b)
     finally:
-        gm.set_option("attn_subtiles", 0)
+        gm.set_option("attn_fx", 1)
     assert np.max(np.abs(z1 - z0)) < LOGIT_MAX_ABS
     assert rel_l2(z1, z0) < LOGIT_REL_L2
 
@@ -465,3 +467,117 @@ def test_two_handles_two_threads(tiny):
     for slot in range(2):
         for o, r in zip(out[slot], ref):
             np.testing.assert_array_equal(o, r)
+
+
+# ----------------------------------------------------------------------- full-config coverage
+def test_sort_base_geometric_schedule_vs_oracle():
+    """SORT-base with the reference's DEFAULT pruning, make_geometric_schedule(1030, 4, 128) =
+    [1030, 514, 256, 128] (mask.cpp:97-117): every layer's mask bit-exact and the
+    logits within the bf16 bars."""
+    from paper_2603_03988_b200.config import geometric_schedule
+    cfg = base_config()
+    cfg.keep = geometric_schedule(cfg.prefix_len, cfg.layers, 128)
+    assert cfg.keep == [1030, 514, 256, 128]
+    P = synth.make_params(cfg, seed=5)
+    gm, om = R.SortModel(cfg, P, max_batch=4), O.OracleModel(cfg, P)
+    b = synth.make_batch(cfg, 4, seed=51)
+    probs, logits = gm.forward_logits(b)
+    meta = om.layer_meta(b, 0)
+    for l in range(cfg.layers):
+        pl = gm.layer_plan(l)
+        assert pl["l_q"] == meta["l_q"][l] and pl["visible"] == meta["visible"][l]
+        assert list(pl["query_rows"]) == meta["query_rows"][l]
+    ref = np.stack([om.forward(b, i)[1] for i in (0, 3)])
+    got = logits[[0, 3]]
+    assert np.max(np.abs(got - ref)) < LOGIT_MAX_ABS
+    assert rel_l2(got, ref) < LOGIT_REL_L2
+
+
+def test_bench_batch_sampled_requests_vs_oracle():
+    """The bench workload itself (bench.py: SORT-base, params seed 5, rank 0's 256 requests,
+    seed 100): one 256-request GPU forward, requests 0, 127 and 255 scored by the oracle."""
+    cfg = base_config(batch=256)
+    P = synth.make_params(cfg, seed=5)
+    gm, om = R.SortModel(cfg, P, max_batch=256), O.OracleModel(cfg, P)
+    b = synth.make_batch(cfg, 256, seed=100)
+    probs, logits = gm.forward_logits(b)
+    idx = [0, 127, 255]
+    ref = np.stack([om.forward(b, i)[1] for i in idx])
+    got = logits[idx]
+    err = float(np.max(np.abs(got - ref)))
+    assert err < LOGIT_MAX_ABS, err
+    assert rel_l2(got, ref) < LOGIT_REL_L2
+    assert np.all(np.isfinite(logits))
+
+
+def test_sort_large_full_geometry_vs_oracle():
+    """BASELINE configs[3] at its full geometry (12 layers, d=1024, 16 heads, H=4096, N=128,
+    W=256, geometric schedule): GPU logits of two requests vs the fp64 oracle's, frozen in
+    tests/golden/large_fixture.npz (tests/golden/make_large_golden.py; same weights and
+    requests, checked by SHA-256)."""
+    import sys as _s
+    _s.path.insert(0, os.path.join(HERE, "golden"))
+    from make_golden import params_digest
+    import make_large_golden as MG
+    fx = np.load(os.path.join(HERE, "golden", "large_fixture.npz"))
+    cfg, P, b = MG.make()
+    assert str(fx["params_sha256"]) == params_digest(P), "synthetic generator drifted"
+    assert str(fx["batch_sha256"]) == MG.batch_digest(b)
+    gm = R.SortModel(cfg, P, max_batch=MG.BATCH)
+    for l in range(cfg.layers):
+        pl = gm.layer_plan(l)
+        assert pl["l_q"] == int(fx["l_q"][l]) and pl["visible"] == int(fx["visible"][l])
+    probs, logits = gm.forward_logits(b)
+    err = float(np.max(np.abs(logits - fx["logits"])))
+    assert err < LOGIT_MAX_ABS, err
+    assert rel_l2(logits, fx["logits"]) < LOGIT_REL_L2
+
+
+# ----------------------------------------------------------------------- against the reference's own code
+needs_ref = pytest.mark.skipif(not RF.available(), reason="oracle/_ref/libref.so not built")
+
+
+@needs_ref
+def test_tiny_vs_reference_code(tiny):
+    """The CUDA path against oracle/_ref (the reference's tokenizer.cpp / mask.cpp /
+    attention.cpp compiled unmodified): token-index artifact bit-exact, tokens within bf16,
+    whole-model logits within the bf16 bars."""
+    cfg, P, gm, _ = tiny
+    rm = RF.RefModel(cfg, P)
+    b = synth.make_batch(cfg, 2, seed=77)
+    tk = gm.tokenize(b)
+    probs, logits = gm.forward_logits(b)
+    for i in range(2):
+        t = rm.tokenize(b, i)
+        assert np.array_equal(tk["hist_time"][i], t["hist_time"])
+        assert np.array_equal(tk["position_ids"], t["position_ids"])
+        assert np.array_equal(tk["roles"], t["roles"])
+        assert np.array_equal(tk["candidate_index"], t["candidate_index"])
+        assert np.max(np.abs(tk["tokens"][i] - t["tokens"])) < TOKEN_TOL
+        _, lr = rm.forward(b, i)
+        assert np.max(np.abs(logits[i] - lr)) < LOGIT_MAX_ABS
+        assert rel_l2(logits[i], lr) < LOGIT_REL_L2
+
+
+@needs_ref
+def test_layer_masks_vs_reference_code(base):
+    """Every SORT-base layer's mask from the device planner == rankformer::build_mask's."""
+    cfg, P, gm, om = base
+    b = synth.make_batch(cfg, 1, seed=2)
+    t = om.tokenize(b, 0)
+    roles, pos = t["roles"].tolist(), t["position_ids"].tolist()
+    for l in range(cfg.layers):
+        pl = gm.layer_plan(l)
+        qr = list(pl["query_rows"])
+        assert qr == RF.retained_rows(roles, cfg.keep_schedule()[l], cfg.keep_specials)
+        vis, cnt = RF.build_mask(len(qr), roles, pos, cfg.local_window, cfg.full_suffix, qr)
+        assert cnt == pl["visible"]
+        lo, hi, se = pl["lo"], pl["hi"], pl["self"]
+        c = np.arange(len(roles))
+        for i in range(0, len(qr), 37):
+            row = (c >= lo[i]) & (c <= hi[i])
+            if se[i] >= 0:
+                row[se[i]] = True
+            assert np.array_equal(row.astype(np.uint8), vis[i])
+        roles = [roles[i] for i in qr]
+        pos = [pos[i] for i in qr]

@@ -128,40 +128,29 @@ def test_two_rank_gloo_gradient_allreduce_equals_full_batch():
     assert err < 1e-12
 
 
-def _table_worker(rank, world, port, out_q):
+def _transport_worker(rank, world, port, out_q):
+    import ctypes as C
     import sys
     here = os.path.dirname(os.path.abspath(__file__))
     sys.path[:0] = [os.path.dirname(here)]
-    import torch
     import torch.distributed as dist
-    from paper_2603_03988_b200 import sharding as S2
+    from paper_2603_03988_b200 import runtime as R
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    n_items, dim = 1000, 32
-    full = torch.from_numpy(np.random.default_rng(0).normal(size=(n_items, dim)).astype(np.float32))
-    R = n_items // world
-    shard = full[rank * R:(rank + 1) * R].clone()
-    rng = np.random.default_rng(10 + rank)  # each rank serves a different batch
-    batch = {"hist_item": torch.from_numpy(rng.integers(0, n_items, (3, 50)).astype(np.int32)),
-             "cand_item": torch.from_numpy(rng.integers(0, n_items, (3, 7)).astype(np.int32))}
-    tab = S2.ShardedItemTable(shard, R, rank, world, gather=lambda t, i: torch.index_select(t, 0, i))
-    rows, mapped = tab.lookup(batch)
-    ok = all(torch.equal(rows[mapped[k].long()], full[batch[k].long()]) for k in ("hist_item", "cand_item"))
-    uniq = int(torch.unique(torch.cat([batch["hist_item"].reshape(-1), batch["cand_item"].reshape(-1)])).numel())
-    ok = ok and rows.shape[0] == uniq
-    # an out-of-vocabulary id on ONE rank must raise on EVERY rank before any all-to-all
-    # (otherwise the clean rank would block in the collective)
-    bad = dict(batch)
-    if rank == 1:
-        bad["cand_item"] = batch["cand_item"].clone()
-        bad["cand_item"][0, 0] = n_items + 5
-    from paper_2603_03988_b200.config import ConfigError
-    try:
-        tab.lookup(bad)
-        ok = False
-    except ConfigError:
-        pass
+    a2a, red = R.host_transport()
+    # rank r sends (r + 1) * (p + 1) bytes of value 10 r + p to rank p
+    send_b = (C.c_int64 * world)(*[(rank + 1) * (p + 1) for p in range(world)])
+    recv_b = (C.c_int64 * world)(*[(p + 1) * (rank + 1) for p in range(world)])
+    payload = bytes(b for p in range(world) for b in [10 * rank + p] * ((rank + 1) * (p + 1)))
+    send = (C.c_uint8 * len(payload)).from_buffer_copy(payload)
+    recv = (C.c_uint8 * sum(recv_b))()
+    ok = a2a(None, C.addressof(send), send_b, C.addressof(recv), recv_b, world) == 0
+    want = bytes(b for p in range(world) for b in [10 * p + rank] * ((p + 1) * (rank + 1)))
+    ok = ok and bytes(recv) == want
+    buf = (C.c_float * 5)(*[float(rank + i) for i in range(5)])
+    ok = ok and red(None, buf, 5) == 0
+    ok = ok and list(buf) == [float(sum(r + i for r in range(world))) for i in range(5)]
     oks = [None] * world
     dist.all_gather_object(oks, ok)
     if rank == 0:
@@ -169,14 +158,15 @@ def _table_worker(rank, world, port, out_q):
     dist.destroy_process_group()
 
 
-def test_two_rank_gloo_row_sharded_item_table_lookup():
-    """Embedding-heavy path (configs[4]): a row-sharded item table served by dedupe +
-    all-to-all of ids + owner gather + all-to-all of rows reproduces the full-table lookup
-    bit-exactly on every rank, with one row per unique id."""
+def test_two_rank_gloo_exchange_host_transport():
+    """Embedding-heavy path (configs[4]) / data-parallel gradient sum: the host transport the
+    library's C++ exchange (csrc/exchange.cuh) calls back into -- all-to-all-v of byte blocks
+    and the in-place float sum -- moves exactly the right bytes between 2 gloo ranks. (The
+    device side of the exchange runs in tests/test_gpu_exchange.py.)"""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_table_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_transport_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
     ok = q.get(timeout=240)
