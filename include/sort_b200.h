@@ -175,10 +175,13 @@ int sort_mask_intervals(int32_t l_q, int32_t l_kv, int32_t local_window, int32_t
                         const int32_t* roles, const int32_t* position_ids,
                         const int32_t* query_rows, int32_t* lo, int32_t* hi, int32_t* self_idx);
 
-/* Op-level streaming tcgen05 GEMM (the generic path's engine, gemm_stream.cuh), for tests and
- * op-level callers: C[M, N] = A[M, K] x Bt[N, K]^T with host fp32 buffers, bf16 operands,
- * fp32 accumulation. N must be a multiple of 32. */
-int sort_op_gemm_bf16(int32_t M, int32_t N, int32_t K, const float* A, const float* Bt, float* C);
+/* Op-level GEMM on the library's engines (the streaming tcgen05 GEMM of gemm_stream.cuh; small
+ * or TMA-unfriendly fp32 shapes on the SIMT kernel), for tests and op-level callers: row-major
+ * C[M, N] = op(A) op(B) with host fp32 buffers; A stored [M, K] (or [K, M] when trans_a),
+ * B stored [K, N] (or [N, K] when trans_b). tf32 = 0: bf16 operands (row pitches multiples of
+ * 8, N of 32); tf32 = 1: fp32 operands at TF32 precision. fp32 accumulation. */
+int sort_op_gemm(int32_t M, int32_t N, int32_t K, int32_t trans_a, int32_t trans_b, int32_t tf32, const float* A,
+                 const float* B, float* C);
 
 /* ---------------------------------------------------------------- instrumentation */
 /* Number of CUDA kernels one sort_forward launches, and per-stage device times (ms) of

@@ -49,8 +49,11 @@ __device__ __forceinline__ void fx_wait(uint64_t* bar, uint32_t parity, int tag,
 #define FXW(bar, par, tag, a0, a1) fx_wait(bar, par, tag, a0, a1)
 #define FXS(bar, par, tag, a0, a1) fx_wait(bar, par, tag, a0, a1)
 #else
-#define FXW(bar, par, tag, a0, a1) mbar_wait_sleep(bar, par)  // TMA producer / softmax warps
-#define FXS(bar, par, tag, a0, a1) mbar_wait(bar, par)        // MMA issuer: spin (latency-critical)
+// Every wait polls try_wait without a suspend-time hint: with the 1 ms hint of
+// mbar_wait_sleep, waiters on barriers completed by tcgen05.commit (an async-proxy arrive)
+// were observed to sleep out the hint (a B = 256 forward took minutes).
+#define FXW(bar, par, tag, a0, a1) mbar_wait(bar, par)
+#define FXS(bar, par, tag, a0, a1) mbar_wait(bar, par)
 #endif
 
 template <int DK>

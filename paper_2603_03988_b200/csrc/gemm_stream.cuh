@@ -35,10 +35,41 @@ constexpr uint32_t kGsABytes = kGsBM * kGsBK * 2;  // 16 KB
 constexpr uint32_t kGsBBytes = kGsBN * kGsBK * 2;  // 32 KB
 constexpr uint32_t kGsSmem = 1024 + kGsStages * (kGsABytes + kGsBBytes) + 256;
 
-template <class Epi>
+// epilogues that take the split-K index declare `static constexpr bool kSplit = true`
+template <class E, class = void>
+struct gs_split_epi : std::false_type {};
+template <class E>
+struct gs_split_epi<E, std::void_t<decltype(E::kSplit)>> : std::bool_constant<E::kSplit> {};
+
+// UMMA shared-memory descriptor of an MN-major SW128 operand tile (the canonical layout
+// ((8,n),(8,k)):((1,LBO),(8,SBO)) in 16-byte units): 64-element (128-byte) MN atoms of 8-row K
+// groups; TMA writes each {64 MN x 64 K} box as 64 rows of 128 bytes, so K groups are 1024 B
+// apart (SBO) and consecutive MN atoms (separate boxes) 8 KB apart (LBO).
+__device__ __forceinline__ uint64_t umma_sdesc_mnmajor_sw128(uint32_t saddr, uint32_t lbo = 8192u) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4);
+  d |= static_cast<uint64_t>(lbo >> 4) << 16;    // LBO: next 128-byte MN atom (one TMA box)
+  d |= static_cast<uint64_t>(1024u >> 4) << 32;  // SBO: next 8-row K group
+  d |= static_cast<uint64_t>(1u) << 46;          // version (sm_100)
+  d |= static_cast<uint64_t>(2u) << 61;          // 128-byte swizzle
+  return d;
+}
+
+// kAMN / kBMN: the operand is stored MN-major in HBM ([K, M] / [K, N] row-major, e.g. an
+// activation matrix X [rows, in] as the A = X^T of a weight gradient, or a reference weight
+// W [in, out] as the B of a forward product) and is loaded as 64 x 64 boxes. k_splits > 1
+// splits K over CTAs (the weight-gradient products, K = rows): the epilogue then receives
+// the split index and writes a partial that a fixed-order reduction sums (deterministic).
+// T = __nv_bfloat16 (kind::f16, K = 64 per stage) or float (kind::tf32: fp32 operands at TF32
+// precision, K = 32 per stage -- the fp32 ranking head and tokenizer products).
+template <class Epi, bool kAMN = false, bool kBMN = false, class T = __nv_bfloat16>
 __global__ void __launch_bounds__(kGsThreads, 1)
     k_gemm_stream(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                  int K, Epi epi) {
+                  int K, int k_splits, Epi epi) {
+  constexpr bool kTf32 = std::is_same_v<T, float>;
+  constexpr int BK = 128 / sizeof(T);   // K per stage: one 128-byte swizzle row
+  constexpr int MMA_K = 32 / sizeof(T); // K per instruction (32 bytes)
+  constexpr int kAtom = 128 / sizeof(T);  // MN elements per 128-byte atom (MN-major boxes)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align_smem_1k(smem_raw);
   uint8_t* sA = smem;
@@ -53,8 +84,16 @@ __global__ void __launch_bounds__(kGsThreads, 1)
   const int warp = warp_id(), lane = lane_id();
   const int num_m = (M + kGsBM - 1) / kGsBM;
   const int num_n = (N + kGsBN - 1) / kGsBN;
-  const int num_k = (K + kGsBK - 1) / kGsBK;
-  const int n_tiles = num_m * num_n;
+  const int num_k = (K + BK - 1) / BK;
+  const int kb_per = (num_k + k_splits - 1) / k_splits;  // k blocks per split
+  const int n_tiles = num_m * num_n * k_splits;
+  // tile t -> (split, m block, n block), n fastest, then m, then split
+  auto decode = [&](int t, int& ks, int& mb, int& nb) {
+    ks = t / (num_m * num_n);
+    const int r = t - ks * num_m * num_n;
+    mb = r / num_n;
+    nb = r - mb * num_n;
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -80,12 +119,29 @@ __global__ void __launch_bounds__(kGsThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        const int mb = t / num_n, nb = t - mb * num_n;
-        for (int kb = 0; kb < num_k; ++kb) {
+        int ks, mb, nb;
+        decode(t, ks, mb, nb);
+        const int kb0 = ks * kb_per, kb1 = min(num_k, kb0 + kb_per);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait_sleep(&empty[s], ph ^ 1);
           mbar_arrive_expect_tx(&full[s], kGsABytes + kGsBBytes);
-          tma_load_2d(sA + s * kGsABytes, &tmA, &full[s], kb * kGsBK, mb * kGsBM);
-          tma_load_2d(sB + s * kGsBBytes, &tmB, &full[s], kb * kGsBK, nb * kGsBN);
+          uint8_t* a_dst = sA + s * kGsABytes;
+          uint8_t* b_dst = sB + s * kGsBBytes;
+          constexpr uint32_t kBox = BK * 128;  // one {atom MN x BK} MN-major box
+          if constexpr (kAMN) {
+#pragma unroll
+            for (int i = 0; i < kGsBM / kAtom; ++i)
+              tma_load_2d(a_dst + i * kBox, &tmA, &full[s], mb * kGsBM + kAtom * i, kb * BK);
+          } else {
+            tma_load_2d(a_dst, &tmA, &full[s], kb * BK, mb * kGsBM);
+          }
+          if constexpr (kBMN) {
+#pragma unroll
+            for (int i = 0; i < kGsBN / kAtom; ++i)
+              tma_load_2d(b_dst + i * kBox, &tmB, &full[s], nb * kGsBN + kAtom * i, kb * BK);
+          } else {
+            tma_load_2d(b_dst, &tmB, &full[s], kb * BK, nb * kGsBN);
+          }
           if (++s == kGsStages) {
             s = 0;
             ph ^= 1;
@@ -95,22 +151,37 @@ __global__ void __launch_bounds__(kGsThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t idesc = umma_idesc_bf16(kGsBM, kGsBN);
+      const uint32_t idesc = (kTf32 ? umma_idesc_tf32(kGsBM, kGsBN) : umma_idesc_bf16(kGsBM, kGsBN)) |
+                             (kAMN ? (1u << 15) : 0u) | (kBMN ? (1u << 16) : 0u);
+      constexpr uint32_t kBox = BK * 128;
       int s = 0, i = 0;
       uint32_t ph = 0;
       for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+        int ks, mb, nb;
+        decode(t, ks, mb, nb);
+        const int kb0 = ks * kb_per, kb1 = min(num_k, kb0 + kb_per);
         const int acc = i & 1;
         mbar_wait_sleep(&tempty[acc], ((i >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * 256;
-        for (int kb = 0; kb < num_k; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[s], ph);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sA + s * kGsABytes), b0 = smem_u32(sB + s * kGsBBytes);
 #pragma unroll
-          for (int k = 0; k < kGsBK / 16; ++k)
-            mma_bf16_ss(d, umma_sdesc_kmajor(a0 + k * 32, 128), umma_sdesc_kmajor(b0 + k * 32, 128), idesc,
-                        (kb | k) != 0 ? 1u : 0u);
+          for (int k = 0; k < BK / MMA_K; ++k) {
+            // K-major: the next K slice is 32 bytes further in every row; MN-major: MMA_K rows
+            // (of 128 bytes) further
+            const uint64_t da = kAMN ? umma_sdesc_mnmajor_sw128(a0 + k * MMA_K * 128, kBox)
+                                     : umma_sdesc_kmajor(a0 + k * 32, 128);
+            const uint64_t db = kBMN ? umma_sdesc_mnmajor_sw128(b0 + k * MMA_K * 128, kBox)
+                                     : umma_sdesc_kmajor(b0 + k * 32, 128);
+            if constexpr (kTf32) {
+              mma_tf32_ss(d, da, db, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            } else {
+              mma_bf16_ss(d, da, db, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            }
+          }
           mma_commit(&empty[s]);
           if (++s == kGsStages) {
             s = 0;
@@ -125,7 +196,9 @@ __global__ void __launch_bounds__(kGsThreads, 1)
     const int e = warp - 4, q = e & 3, half = e >> 2;
     int i = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
-      const int mb = t / num_n, nb = t - mb * num_n;
+      int ks, mb, nb;
+      decode(t, ks, mb, nb);
+      const bool empty_split = ks * kb_per >= num_k;  // (no k blocks: the accumulator is stale)
       const int acc = i & 1;
       const int row = mb * kGsBM + q * 32 + lane;
       const uint32_t tb = tmem + acc * 256 + (static_cast<uint32_t>(q * 32) << 16);
@@ -137,7 +210,17 @@ __global__ void __launch_bounds__(kGsThreads, 1)
         if (col >= N) break;
         float v[kC];
         tmem_row_chunk<kC>(tb + c, v);
-        if (row < M) epi.apply(row, col, v);
+        if (empty_split) {
+#pragma unroll
+          for (int j = 0; j < kC; ++j) v[j] = 0.f;
+        }
+        if (row < M) {
+          if constexpr (gs_split_epi<Epi>::value) {
+            epi.apply(row, col, v, ks);
+          } else {
+            epi.apply(row, col, v);
+          }
+        }
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
@@ -148,6 +231,42 @@ __global__ void __launch_bounds__(kGsThreads, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
+  }
+}
+
+// fp32 C[M, N] = op(A)[M, K] op(B)[K, N] (+ beta C), op = transpose when ta / tb: the small or
+// TMA-unfriendly fp32 products of the ranking head and the tokenizer (N = 3 logits, K = 3,
+// widths that are not multiples of 32). 32 x 32 output tiles, 32-deep K slices in smem.
+__global__ void __launch_bounds__(256) k_gemm_simt(bool ta, bool tb, int M, int N, int K, const float* __restrict__ A,
+                                                   int lda, const float* __restrict__ B, int ldb, float* __restrict__ C,
+                                                   int ldc, float beta) {
+  __shared__ float sa[32][33], sb[32][33];
+  const int m0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 rows of 4 outputs each
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int k0 = 0; k0 < K; k0 += 32) {
+    for (int i = ty; i < 32; i += 8) {
+      const int m = m0 + i, k = k0 + tx;  // sa[i][tx] = op(A)[m][k]
+      sa[i][tx] = (m < M && k < K) ? (ta ? A[static_cast<size_t>(k) * lda + m] : A[static_cast<size_t>(m) * lda + k]) : 0.f;
+      const int kk = k0 + i, n = n0 + tx;  // sb[i][tx] = op(B)[kk][n]
+      sb[i][tx] = (kk < K && n < N) ? (tb ? B[static_cast<size_t>(n) * ldb + kk] : B[static_cast<size_t>(kk) * ldb + n]) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) {
+      const float bv = sb[k][tx];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[r] = fmaf(sa[ty + 8 * r][k], bv, acc[r]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int m = m0 + ty + 8 * r, n = n0 + tx;
+    if (m < M && n < N) {
+      float* c = C + static_cast<size_t>(m) * ldc + n;
+      *c = beta != 0.f ? acc[r] + beta * *c : acc[r];
+    }
   }
 }
 
@@ -172,6 +291,38 @@ struct GsStore {
     }
   }
 };
+
+// split-K partial: P[split][row][col] = acc (fp32, [splits, M, N]); k_splitk_reduce sums them
+struct GsPartialF32 {
+  static constexpr int kChunk = 32;
+  static constexpr bool kSplit = true;
+  float* P;
+  int M, N;
+  __device__ void apply(int row, int col, const float (&v)[32], int ks) const {
+    float4* p = reinterpret_cast<float4*>(P + (static_cast<size_t>(ks) * M + row) * N + col);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) p[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+  }
+};
+
+// C[M, N] (row pitch ldc, fp32 or bf16) = sum over splits of P (fixed order) + beta C
+template <class T>
+__global__ void k_splitk_reduce(const float* __restrict__ P, int splits, int M, int N, T* __restrict__ C, int ldc,
+                                float beta) {
+  const size_t total = static_cast<size_t>(M) * N;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    float s = 0.f;
+    for (int k = 0; k < splits; ++k) s += P[static_cast<size_t>(k) * total + i];
+    const size_t r = i / N, c = i - r * N;
+    T* dst = C + r * ldc + c;
+    if constexpr (std::is_same_v<T, float>) {
+      *dst = beta != 0.f ? s + beta * *dst : s;
+    } else {
+      *dst = __float2bfloat16_rn(beta != 0.f ? s + beta * __bfloat162float(*dst) : s);
+    }
+  }
+}
 
 // fp32 C += acc (the FFN down projection accumulating into the residual stream)
 struct GsAccF32 {

@@ -16,6 +16,7 @@
 #include "../../include/sort_b200.h"
 #include "attention.cuh"
 #include "attention_fx.cuh"
+#include "attn_bwd.cuh"
 #include "block_tail.cuh"
 #include "epilogues.cuh"
 #include "gemm.cuh"
@@ -88,6 +89,7 @@ struct Handle {
   bool fused_tail = true;  // sort_set_option("fused_tail")
   bool tail_pair = false;  // sort_set_option("tail_pair"): block tail as CTA pairs (cta_group::2)
   bool attn_bwd_mma = true; // sort_set_option("attn_bwd_mma"): tensor-core attention backward
+  bool attn_bwd_tc = true;  // sort_set_option("attn_bwd_tc"): tcgen05 attention backward (0: mma.sync)
   bool qkvg_pair = false;   // sort_set_option("qkvg_pair"): QKVG projection as CTA pairs
   bool attn_fx = false;     // sort_set_option("attn_fx"): fixed-reference layers run k_attn_fx (0: k_attention)
   bool generic = false;    // d > 256 (SORT-large): projections through the generic path
@@ -118,6 +120,9 @@ struct Handle {
   std::map<std::string, __nv_bfloat16*> wT;   // bf16 K-major (transposed) weights of the streaming GEMMs
   std::map<std::tuple<const void*, uint64_t, uint64_t, uint64_t, uint32_t>, CUtensorMap> gs_maps;
   bool stream_gemm = true;  // sort_set_option("stream_gemm"): generic path on k_gemm_stream (0: cuBLAS)
+  bool train_cublas = false;  // sort_set_option("train_cublas"): training GEMMs on cuBLAS (A/B)
+  float* splitk_ws = nullptr;  // split-K partials of the streaming GEMM
+  size_t splitk_cap = 0;
   std::map<std::string, std::pair<__nv_bfloat16*, size_t>> tw16;  // training: bf16 weights of the FFN backward
   std::map<std::string, std::pair<size_t, std::pair<int64_t, int64_t>>> grad_index;  // offset, shape
   float* grads = nullptr;
@@ -134,6 +139,12 @@ struct Handle {
     int2 *dq_iv = nullptr, *dkv_iv = nullptr;
     int32_t *qb_off = nullptr, *qb_list = nullptr;  // tensor-core backward: q blocks per kv block
     CUtensorMap tmQ, tmK, tmV;  // the attention core reads the saved Q / K / V directly
+    // tcgen05 backward (attn_bwd.cuh): X/Y step lists of the dK/dV and dQ passes and the
+    // 128-row (X) / 64-row (Y) boxes of Q, K, V and the token-major dO
+    int32_t *tc_kv_off = nullptr, *tc_q_off = nullptr;
+    int2 *tc_kv_code = nullptr, *tc_q_code = nullptr;
+    int tc_kv_n = 0, tc_q_n = 0;
+    CUtensorMap tmQ64, tmK64, tmV64, tmDO128, tmDO64;
   };
   std::vector<TrainLayer> tl;
   const TrainLayer* save_to = nullptr;  // training forward: QKVG writes straight into these buffers
@@ -229,6 +240,7 @@ struct Handle {
       if (slot_free[i]) cudaEventDestroy(slot_free[i]);
     }
     if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (splitk_ws) cudaFree(splitk_ws);
     if (cublas) cublasDestroy(cublas);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
@@ -1105,8 +1117,8 @@ static void run_layer(Handle& h, int l, int B, bool attn_only = false) {
 // ====================================================================== training
 // Row-major C[M,N] = op(A)[M,K] op(B)[K,N] (+ beta C) through column-major cuBLAS
 // (C^T = op(B)^T op(A)^T), TF32 tensor cores, fp32 in/out.
-static void gemm_rm(Handle& h, bool ta, bool tb, int M, int N, int K, const float* A, int lda, const float* B,
-                    int ldb, float* C, int ldc, float beta = 0.f) {
+static void gemm_rm_cublas(Handle& h, bool ta, bool tb, int M, int N, int K, const float* A, int lda, const float* B,
+                           int ldb, float* C, int ldc, float beta = 0.f) {
   const float alpha = 1.f;
   const cublasStatus_t st = cublasGemmEx(h.cublas, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N,
                                          N, M, K, &alpha, B, CUDA_R_32F, ldb, A, CUDA_R_32F, lda, &beta, C,
@@ -1156,16 +1168,171 @@ static void qkv_prep(Handle& h, const __nv_bfloat16* raw, int ld, int rows, int 
     k_qkv_prep<8><<<g, 256, 0, h.stream>>>(raw, ld, rows, R, H, dk, kind, pos, rope, gain, out);
 }
 
+// ---- streaming tcgen05 GEMM (gemm_stream.cuh) for the generic path
+static const CUtensorMap& gs_map(Handle& h, const void* p, uint64_t rows, uint64_t cols, uint64_t ld,
+                                 uint32_t box_rows, uint32_t box_cols = kGsBK, bool f32 = false) {
+  const auto key = std::make_tuple(p, rows, cols, ld, box_rows | (box_cols << 16) | (f32 ? 1u << 31 : 0u));
+  auto it = h.gs_maps.find(key);
+  if (it != h.gs_maps.end()) return it->second;
+  if (!f32) return h.gs_maps[key] = make_tmap_2d(p, rows, cols, ld, box_rows, box_cols, 128);
+  const uint64_t dims[2] = {cols, rows}, str[1] = {ld * 4};
+  const uint32_t box[2] = {box_cols, box_rows};
+  return h.gs_maps[key] = make_tmap(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, p, 2, dims, str, box, 128);
+}
+
+// C[M, N] = op(A)[M, K] x op(B)[K, N] on the streaming tcgen05 GEMM, epilogue functor epi:
+//   kAMN = false: A stored [M, K] (row pitch lda);  true: A stored [K, M] (A^T, MN-major)
+//   kBMN = false: B stored [N, K] (B^T, K-major);   true: B stored [K, N] (MN-major)
+// k_splits > 1: K split over CTAs, epi must take the split index (GsPartialF32).
+template <class Epi, bool kAMN = false, bool kBMN = false, class T = __nv_bfloat16>
+static void gemm_stream(Handle& h, const T* A, int lda, int M, int K, const T* Bt, int ldb, int N, const Epi& epi,
+                        int k_splits = 1) {
+  if (M <= 0 || N <= 0) return;
+  constexpr bool f32 = std::is_same_v<T, float>;
+  constexpr uint32_t BK = 128 / sizeof(T), kAtom = 128 / sizeof(T);
+  if (N % Epi::kChunk != 0) throw ConfigError("stream gemm: N must be a multiple of the epilogue chunk");
+  const CUtensorMap& ta = kAMN ? gs_map(h, A, K, M, lda, BK, kAtom, f32) : gs_map(h, A, M, K, lda, kGsBM, BK, f32);
+  const CUtensorMap& tb = kBMN ? gs_map(h, Bt, K, N, ldb, BK, kAtom, f32) : gs_map(h, Bt, N, K, ldb, kGsBN, BK, f32);
+  ensure_smem(k_gemm_stream<Epi, kAMN, kBMN, T>, kGsSmem);
+  const int tiles = ((M + kGsBM - 1) / kGsBM) * ((N + kGsBN - 1) / kGsBN) * k_splits;
+  k_gemm_stream<Epi, kAMN, kBMN, T><<<std::min(tiles, h.num_sms), kGsThreads, kGsSmem, h.stream>>>(
+      ta, tb, M, N, K, k_splits, epi);
+  check_launch("stream gemm");
+  ++h.launches;
+}
+
+// bf16 K-major B operand [sum N_i, ldk] of the column-concatenated [K, N_i] fp32 weights
+// `parts` (reference [in, out] layout); swiglu: the two parts (w_gate, w_up) are interleaved in
+// 32-row blocks [gate_j | up_j] for EpiSwiGLU. ldk = K rounded up to 8 (16-byte TMA pitch).
+static const __nv_bfloat16* wT16(Handle& h, const std::string& key, const std::vector<std::string>& parts,
+                                 bool swiglu = false) {
+  auto it = h.wT.find(key);
+  if (it != h.wT.end()) return it->second;
+  const auto& g0 = h.grad_index.at(parts[0]).second;
+  const int K = static_cast<int>(g0.first), ldk = (K + 7) & ~7;
+  int Ntot = 0;
+  for (const auto& p : parts) Ntot += static_cast<int>(h.grad_index.at(p).second.second);
+  __nv_bfloat16* dst = h.dalloc<__nv_bfloat16>(static_cast<size_t>(Ntot) * ldk);
+  int row0 = 0;
+  for (size_t i = 0; i < parts.size(); ++i) {
+    const auto& gi = h.grad_index.at(parts[i]).second;
+    if (gi.first != K) throw ConfigError("wT16: parts with different input widths");
+    const int N = static_cast<int>(gi.second);
+    const dim3 grid((ldk + 31) / 32, (N + 31) / 32);
+    k_transpose_bf16<<<grid, 256, 0, h.stream>>>(h.w32.at(parts[i]), K, N, ldk, row0, swiglu ? 32 : 0,
+                                                 swiglu ? static_cast<int>(i) * 32 : 0, dst);
+    row0 += N;
+  }
+  check_launch("weight transpose");
+  return h.wT[key] = dst;
+}
+
 // Row-major C[M,N] (+ beta C) = op(A) op(B) with bf16 operands and fp32 accumulation; C fp32
 // or bf16 (the training FFN backward).
 static void gemm_rm16(Handle& h, bool ta, bool tb, int M, int N, int K, const __nv_bfloat16* A, int lda,
                       const __nv_bfloat16* B, int ldb, void* C, int ldc, bool c_bf16, float beta = 0.f) {
-  const float alpha = 1.f;
-  const cublasStatus_t st = cublasGemmEx(h.cublas, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N,
-                                         N, M, K, &alpha, B, CUDA_R_16BF, ldb, A, CUDA_R_16BF, lda, &beta, C,
-                                         c_bf16 ? CUDA_R_16BF : CUDA_R_32F, ldc, CUBLAS_COMPUTE_32F,
-                                         CUBLAS_GEMM_DEFAULT);
-  if (st != CUBLAS_STATUS_SUCCESS) throw RuntimeFailure("cublasGemmEx (bf16) failed: " + std::to_string(static_cast<int>(st)));
+  if (M <= 0 || N <= 0) return;
+  if (h.train_cublas) {  // A/B option: the library GEMM
+    const float alpha = 1.f;
+    const cublasStatus_t st = cublasGemmEx(h.cublas, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N,
+                                           N, M, K, &alpha, B, CUDA_R_16BF, ldb, A, CUDA_R_16BF, lda, &beta, C,
+                                           c_bf16 ? CUDA_R_16BF : CUDA_R_32F, ldc, CUBLAS_COMPUTE_32F,
+                                           CUBLAS_GEMM_DEFAULT);
+    if (st != CUBLAS_STATUS_SUCCESS)
+      throw RuntimeFailure("cublasGemmEx (bf16) failed: " + std::to_string(static_cast<int>(st)));
+    return;
+  }
+  // tcgen05 streaming GEMM: op(A) = A^T is an MN-major A, op(B) = B (not transposed) an
+  // MN-major B. Few output tiles and a long K (the weight gradients, K = rows) split K over
+  // the SMs into partials summed in a fixed order (deterministic).
+  const int tiles = ((M + kGsBM - 1) / kGsBM) * ((N + kGsBN - 1) / kGsBN);
+  const int num_k = (K + kGsBK - 1) / kGsBK;
+  int splits = 1;
+  if (tiles * 2 <= h.num_sms && num_k >= 16) splits = std::max(1, std::min(h.num_sms / tiles, num_k / 8));
+  auto run = [&](auto epi) {
+    using E = decltype(epi);
+    if (ta && tb) gemm_stream<E, true, false>(h, A, lda, M, K, B, ldb, N, epi, splits);
+    else if (ta) gemm_stream<E, true, true>(h, A, lda, M, K, B, ldb, N, epi, splits);
+    else if (tb) gemm_stream<E, false, false>(h, A, lda, M, K, B, ldb, N, epi, splits);
+    else gemm_stream<E, false, true>(h, A, lda, M, K, B, ldb, N, epi, splits);
+  };
+  if (splits > 1) {
+    const size_t need = static_cast<size_t>(splits) * M * N;
+    if (need > h.splitk_cap) {
+      if (h.splitk_ws) CK(cudaFree(h.splitk_ws));
+      CK(cudaMalloc(&h.splitk_ws, need * sizeof(float)));
+      h.splitk_cap = need;
+    }
+    run(GsPartialF32{h.splitk_ws, M, N});
+    const int g = static_cast<int>(std::min<size_t>((static_cast<size_t>(M) * N + 255) / 256, 148 * 8));
+    if (c_bf16)
+      k_splitk_reduce<__nv_bfloat16><<<g, 256, 0, h.stream>>>(h.splitk_ws, splits, M, N,
+                                                              static_cast<__nv_bfloat16*>(C), ldc, beta);
+    else
+      k_splitk_reduce<float><<<g, 256, 0, h.stream>>>(h.splitk_ws, splits, M, N, static_cast<float*>(C), ldc, beta);
+    check_launch("split-k reduce");
+    ++h.launches;
+    return;
+  }
+  if (c_bf16) {
+    if (beta != 0.f) throw RuntimeFailure("gemm_rm16: bf16 output with beta is not supported");
+    run(GsStore<__nv_bfloat16>{static_cast<__nv_bfloat16*>(C), ldc});
+  } else if (beta != 0.f) {
+    if (beta != 1.f) throw RuntimeFailure("gemm_rm16: beta must be 0 or 1");
+    run(GsAccF32{static_cast<float*>(C), ldc});
+  } else {
+    run(GsStore<float>{static_cast<float*>(C), ldc});
+  }
+}
+
+// Row-major fp32 C[M,N] (+ beta C) = op(A) op(B) (the ranking head and tokenizer products,
+// fp32 per PAPER.md:243): TF32 tcgen05 streaming GEMM (split-K for the long-K weight
+// gradients), or the SIMT kernel for shapes TMA cannot tile (N = 3 logits, K = 3, widths
+// that are not multiples of 32 / 16-byte row pitches).
+static void gemm_rm(Handle& h, bool ta, bool tb, int M, int N, int K, const float* A, int lda, const float* B, int ldb,
+                    float* C, int ldc, float beta = 0.f) {
+  if (M <= 0 || N <= 0) return;
+  if (h.train_cublas) {
+    gemm_rm_cublas(h, ta, tb, M, N, K, A, lda, B, ldb, C, ldc, beta);
+    return;
+  }
+  const bool tma_ok = N % 32 == 0 && K >= 8 && lda % 4 == 0 && ldb % 4 == 0 && ldc % 4 == 0 &&
+                      (beta == 0.f || beta == 1.f);
+  if (!tma_ok) {
+    const dim3 grid((N + 31) / 32, (M + 31) / 32);
+    k_gemm_simt<<<grid, 256, 0, h.stream>>>(ta, tb, M, N, K, A, lda, B, ldb, C, ldc, beta);
+    check_launch("simt gemm");
+    ++h.launches;
+    return;
+  }
+  const int tiles = ((M + kGsBM - 1) / kGsBM) * ((N + kGsBN - 1) / kGsBN);
+  const int num_k = (K + 31) / 32;
+  int splits = 1;
+  if (tiles * 2 <= h.num_sms && num_k >= 16) splits = std::max(1, std::min(h.num_sms / tiles, num_k / 8));
+  auto run = [&](auto epi) {
+    using E = decltype(epi);
+    if (ta && tb) gemm_stream<E, true, false, float>(h, A, lda, M, K, B, ldb, N, epi, splits);
+    else if (ta) gemm_stream<E, true, true, float>(h, A, lda, M, K, B, ldb, N, epi, splits);
+    else if (tb) gemm_stream<E, false, false, float>(h, A, lda, M, K, B, ldb, N, epi, splits);
+    else gemm_stream<E, false, true, float>(h, A, lda, M, K, B, ldb, N, epi, splits);
+  };
+  if (splits > 1) {
+    const size_t need = static_cast<size_t>(splits) * M * N;
+    if (need > h.splitk_cap) {
+      if (h.splitk_ws) CK(cudaFree(h.splitk_ws));
+      CK(cudaMalloc(&h.splitk_ws, need * sizeof(float)));
+      h.splitk_cap = need;
+    }
+    run(GsPartialF32{h.splitk_ws, M, N});
+    const int g = static_cast<int>(std::min<size_t>((static_cast<size_t>(M) * N + 255) / 256, 148 * 8));
+    k_splitk_reduce<float><<<g, 256, 0, h.stream>>>(h.splitk_ws, splits, M, N, C, ldc, beta);
+    check_launch("split-k reduce");
+    ++h.launches;
+  } else if (beta != 0.f) {
+    run(GsAccF32{C, ldc});
+  } else {
+    run(GsStore<float>{C, ldc});
+  }
 }
 
 static float* grad_ptr(Handle& h, const std::string& name) {
@@ -1234,6 +1401,43 @@ static void build_bwd_lists(const LayerPlan& lp, std::vector<int32_t>& dq_off, s
   }
 }
 
+// Step lists of the tcgen05 attention backward (attn_bwd.cuh): for every 128-row X block the
+// 64-row Y blocks sharing a visible entry, with the class of each 32 x 32 chunk (lane quarter
+// q of X, half hf of Y) in bits 2 (2 q + hf): 1 = fully visible, 2 = invisible, 0 = mixed.
+// dq_mode: X = query rows, Y = kv rows; else X = kv rows, Y = query rows. A chunk is "full"
+// only when all its rows and columns are in range.
+static void build_bwd_tc_lists(const LayerPlan& lp, bool dq_mode, std::vector<int32_t>& off, std::vector<int2>& code) {
+  const int RX = dq_mode ? lp.l_q : lp.l_kv, RY = dq_mode ? lp.l_kv : lp.l_q;
+  const int nX = (RX + 127) / 128, nY = (RY + 63) / 64;
+  off.assign(1, 0);
+  code.clear();
+  auto sees = [&](int q, int k) { return (k >= lp.lo[q] && k <= lp.hi[q]) || k == lp.self_idx[q]; };
+  for (int xb = 0; xb < nX; ++xb) {
+    for (int yb = 0; yb < nY; ++yb) {
+      uint32_t bits = 0;
+      bool any = false;
+      for (int qq = 0; qq < 4; ++qq)
+        for (int hf = 0; hf < 2; ++hf) {
+          const int x0 = xb * 128 + qq * 32, y0 = yb * 64 + hf * 32;
+          bool full = x0 + 32 <= RX && y0 + 32 <= RY, none = true;
+          for (int i = 0; i < 32 && (full || none); ++i)
+            for (int j = 0; j < 32 && (full || none); ++j) {
+              const int x = x0 + i, y = y0 + j;
+              const bool v = x < RX && y < RY && (dq_mode ? sees(x, y) : sees(y, x));
+              full = full && v;
+              none = none && !v;
+            }
+          const uint32_t c = full ? 1u : (none ? 2u : 0u);
+          bits |= c << (2 * (2 * qq + hf));
+          any = any || !none;
+        }
+      if (any) code.push_back(make_int2(yb, static_cast<int32_t>(bits)));
+    }
+    off.push_back(static_cast<int32_t>(code.size()));
+  }
+  if (code.empty()) code.push_back(make_int2(0, 0));
+}
+
 static void ensure_train_buffers(Handle& h, int B) {
   if (h.cfg.pretrain) throw ConfigError("training step: use the ranking model (pretrain backward not in this build)");
   if (h.moe) throw ConfigError("training step: the MoE FFN backward is not implemented in this build");
@@ -1270,6 +1474,22 @@ static void ensure_train_buffers(Handle& h, int B) {
       uint64_t skd[2] = {static_cast<uint64_t>(dk) * 2, static_cast<uint64_t>(L.Rkv) * dk * 2};
       T.tmK = make_tmap_bf16(T.k, 3, dkd, skd, bq, dk * 2);
       T.tmV = make_tmap_bf16(T.v, 3, dkd, skd, bq, dk * 2);
+      uint32_t b64[3] = {static_cast<uint32_t>(dk), 64, 1};
+      T.tmQ64 = make_tmap_bf16(T.q, 3, dq, sq, b64, dk * 2);
+      T.tmK64 = make_tmap_bf16(T.k, 3, dkd, skd, b64, dk * 2);
+      T.tmV64 = make_tmap_bf16(T.v, 3, dkd, skd, b64, dk * 2);
+    }
+    {
+      std::vector<int32_t> off;
+      std::vector<int2> code;
+      build_bwd_tc_lists(h.plan.layers[l], false, off, code);
+      T.tc_kv_off = h.upload(off);
+      T.tc_kv_code = h.upload(code);
+      T.tc_kv_n = static_cast<int>(code.size());
+      build_bwd_tc_lists(h.plan.layers[l], true, off, code);
+      T.tc_q_off = h.upload(off);
+      T.tc_q_code = h.upload(code);
+      T.tc_q_n = static_cast<int>(code.size());
     }
     std::vector<int32_t> qo, ko;
     std::vector<int2> qi, ki;
@@ -1309,6 +1529,16 @@ static void ensure_train_buffers(Handle& h, int B) {
   // 11 raw, 12 GU / dGU, 13 z / dz, 14 inv (rows), 15 D / head scratch
   for (int i = 0; i < 12; ++i) h.tw[i] = h.dalloc<float>(rows * d);
   h.dO16 = h.dalloc<__nv_bfloat16>(rows * d);
+  for (int l = 0; l < h.cfg.layers; ++l) {  // dO16 as token-major [B, Rq, H, dk] boxes
+    const int dk = h.dk;
+    const uint64_t dims[4] = {static_cast<uint64_t>(dk), static_cast<uint64_t>(h.H),
+                              static_cast<uint64_t>(h.layers[l].Rq), static_cast<uint64_t>(B)};
+    const uint64_t str[3] = {static_cast<uint64_t>(dk) * 2, static_cast<uint64_t>(d) * 2,
+                             static_cast<uint64_t>(h.layers[l].Rq) * d * 2};
+    const uint32_t b128[4] = {static_cast<uint32_t>(dk), 1, 128, 1}, b64[4] = {static_cast<uint32_t>(dk), 1, 64, 1};
+    h.tl[l].tmDO128 = make_tmap(CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, h.dO16, 4, dims, str, b128, dk * 2);
+    h.tl[l].tmDO64 = make_tmap(CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, h.dO16, 4, dims, str, b64, dk * 2);
+  }
   h.tw[12] = h.dalloc<float>(rows * 2 * m * 2);  // GU and dGU
   h.tw[13] = h.dalloc<float>(rows * m);
   h.tw[14] = h.dalloc<float>(rows * 2);
@@ -1482,7 +1712,54 @@ static void backward_device(Handle& h, int B, const float* dz) {
     AttnBwdArgs ak = ab;
     ak.blk_off = T.dkv_off;
     ak.blk_iv = T.dkv_iv;
-    if (h.attn_bwd_mma) {
+    if (h.attn_bwd_tc) {
+      AttnBwdTcArgs tb;
+      tb.rowmeta = L.rowmeta;
+      tb.lse = T.lse;
+      tb.D = Dd;
+      tb.BH = B * H;
+      tb.H = H;
+      tb.Rq = L.Rq;
+      tb.Rkv = L.Rkv;
+      tb.scale = ab.scale;
+      tb.scale_log2 = ab.scale_log2;
+      // pass 1: dK, dV per 128-row kv block (X = K, V; Y = Q, dO)
+      tb.x_off = T.tc_kv_off;
+      tb.y_code = T.tc_kv_code;
+      tb.nX = (L.Rkv + 127) / 128;
+      tb.out0 = dK;
+      tb.out1 = dV;
+      tb.out1_16 = reinterpret_cast<__nv_bfloat16*>(h.tw[12]) + 2 * static_cast<size_t>(h.train_B) * h.L0 * d;
+      auto launch_tc = [&](auto kern, const CUtensorMap& x0, const CUtensorMap& x1, const CUtensorMap& y0,
+                           const CUtensorMap& y1, int n_codes, size_t smem_fn_bytes) {
+        ensure_smem(kern, smem_fn_bytes);
+        const int grid = std::min(tb.nX * tb.BH, 2 * h.num_sms);
+        kern<<<grid, kAttnThreads, smem_fn_bytes, h.stream>>>(x0, x1, y0, y1, tb);
+        (void)n_codes;
+      };
+#define SORT_BWD_TC(DKV)                                                                                      \
+  case DKV: {                                                                                                 \
+    launch_tc(k_attn_bwd_tc<DKV, false>, T.tmK, T.tmV, T.tmQ64, T.tmDO64, T.tc_kv_n,                          \
+              BwdSmem<DKV>::bytes(tb.nX + 2 + 2 * T.tc_kv_n));                                                \
+    tb.x_off = T.tc_q_off;                                                                                    \
+    tb.y_code = T.tc_q_code;                                                                                  \
+    tb.nX = (L.Rq + 127) / 128;                                                                               \
+    tb.out0 = dQ;                                                                                             \
+    tb.out1 = nullptr;                                                                                        \
+    tb.out1_16 = nullptr;                                                                                     \
+    launch_tc(k_attn_bwd_tc<DKV, true>, T.tmQ, T.tmDO128, T.tmK64, T.tmV64, T.tc_q_n,                         \
+              BwdSmem<DKV>::bytes(tb.nX + 2 + 2 * T.tc_q_n));                                                 \
+    break;                                                                                                    \
+  }
+      switch (dk) {
+        SORT_BWD_TC(16)
+        SORT_BWD_TC(32)
+        SORT_BWD_TC(64)
+        default: throw ConfigError("training: unsupported head dim");
+      }
+#undef SORT_BWD_TC
+      h.launches += 2;
+    } else if (h.attn_bwd_mma) {
       AttnBwdMmaArgs am;
       am.q = T.q;
       am.k = T.k;
@@ -1545,7 +1822,7 @@ static void backward_device(Handle& h, int B, const float* dz) {
     k_qknorm_rope_bwd_v<1><<<qk_grid_k, 256, d * 4, h.stream>>>(dK, raw, Mkv, L.Rkv, L.pos_kv, h.rope, H, dk,
                                                               w32(h, A + "qk_gain_k"), dK, grad_ptr(h, A + "qk_gain_k"),
                                                               dK16);
-    if (!h.attn_bwd_mma) k_f32_to_bf16<<<ew_grid(nkv), 256, 0, h.stream>>>(dV, nkv, dV16);  // (SIMT path)
+    if (!h.attn_bwd_mma && !h.attn_bwd_tc) k_f32_to_bf16<<<ew_grid(nkv), 256, 0, h.stream>>>(dV, nkv, dV16);  // (SIMT path)
     check_launch("qknorm/rope backward");
     gemm_rm16(h, true, false, d, d, M, xqp, d, dQ16, d, grad_ptr(h, A + "wq"), d, false);
     gemm_rm16(h, true, false, d, d, Mkv, xn, d, dK16, d, grad_ptr(h, A + "wk"), d, false);
@@ -1677,56 +1954,6 @@ static const __nv_bfloat16* w16_cat(Handle& h, const std::string& key, const std
                          static_cast<size_t>(N) * 2, static_cast<size_t>(K), cudaMemcpyDeviceToDevice, h.stream));
   }
   return h.w16[key] = dst;
-}
-
-// ---- streaming tcgen05 GEMM (gemm_stream.cuh) for the generic path
-static const CUtensorMap& gs_map(Handle& h, const void* p, uint64_t rows, uint64_t cols, uint64_t ld,
-                                 uint32_t box_rows) {
-  const auto key = std::make_tuple(p, rows, cols, ld, box_rows);
-  auto it = h.gs_maps.find(key);
-  if (it != h.gs_maps.end()) return it->second;
-  return h.gs_maps[key] = make_tmap_2d(p, rows, cols, ld, box_rows, kGsBK, 128);
-}
-
-// C[M, N] = A[M, K] (row pitch lda) x Bt[N, K]^T (row pitch ldb), epilogue functor epi
-template <class Epi>
-static void gemm_stream(Handle& h, const __nv_bfloat16* A, int lda, int M, int K, const __nv_bfloat16* Bt, int ldb,
-                        int N, const Epi& epi) {
-  if (M <= 0 || N <= 0) return;
-  if (N % Epi::kChunk != 0) throw ConfigError("stream gemm: N must be a multiple of the epilogue chunk");
-  const CUtensorMap& ta = gs_map(h, A, M, K, lda, kGsBM);
-  const CUtensorMap& tb = gs_map(h, Bt, N, K, ldb, kGsBN);
-  ensure_smem(k_gemm_stream<Epi>, kGsSmem);
-  const int tiles = ((M + kGsBM - 1) / kGsBM) * ((N + kGsBN - 1) / kGsBN);
-  k_gemm_stream<Epi><<<std::min(tiles, h.num_sms), kGsThreads, kGsSmem, h.stream>>>(ta, tb, M, N, K, epi);
-  check_launch("stream gemm");
-  ++h.launches;
-}
-
-// bf16 K-major B operand [sum N_i, ldk] of the column-concatenated [K, N_i] fp32 weights
-// `parts` (reference [in, out] layout); swiglu: the two parts (w_gate, w_up) are interleaved in
-// 32-row blocks [gate_j | up_j] for EpiSwiGLU. ldk = K rounded up to 8 (16-byte TMA pitch).
-static const __nv_bfloat16* wT16(Handle& h, const std::string& key, const std::vector<std::string>& parts,
-                                 bool swiglu = false) {
-  auto it = h.wT.find(key);
-  if (it != h.wT.end()) return it->second;
-  const auto& g0 = h.grad_index.at(parts[0]).second;
-  const int K = static_cast<int>(g0.first), ldk = (K + 7) & ~7;
-  int Ntot = 0;
-  for (const auto& p : parts) Ntot += static_cast<int>(h.grad_index.at(p).second.second);
-  __nv_bfloat16* dst = h.dalloc<__nv_bfloat16>(static_cast<size_t>(Ntot) * ldk);
-  int row0 = 0;
-  for (size_t i = 0; i < parts.size(); ++i) {
-    const auto& gi = h.grad_index.at(parts[i]).second;
-    if (gi.first != K) throw ConfigError("wT16: parts with different input widths");
-    const int N = static_cast<int>(gi.second);
-    const dim3 grid((ldk + 31) / 32, (N + 31) / 32);
-    k_transpose_bf16<<<grid, 256, 0, h.stream>>>(h.w32.at(parts[i]), K, N, ldk, row0, swiglu ? 32 : 0,
-                                                 swiglu ? static_cast<int>(i) * 32 : 0, dst);
-    row0 += N;
-  }
-  check_launch("weight transpose");
-  return h.wT[key] = dst;
 }
 
 static void forward_generic(Handle& h, int B) {
@@ -2329,26 +2556,29 @@ int sort_attention_forward(SortHandle p, int layer, int32_t batch, const float* 
   });
 }
 
-int sort_op_gemm_bf16(int32_t M, int32_t N, int32_t K, const float* A, const float* Bt, float* C) {
+int sort_op_gemm(int32_t M, int32_t N, int32_t K, int32_t trans_a, int32_t trans_b, int32_t tf32, const float* A,
+                 const float* B, float* C) {
   return api([&] {
-    if (M < 0 || N < 0 || K < 1 || (M && (!A || !C)) || (N && !Bt)) throw ConfigError("op gemm: bad arguments");
-    if (N % 32) throw ConfigError("op gemm: N must be a multiple of 32");
+    if (M < 0 || N < 0 || K < 1 || (M && (!A || !C)) || (N && !B)) throw ConfigError("op gemm: bad arguments");
     if (M == 0 || N == 0) return;
     int dev = 0;
     CK(cudaGetDevice(&dev));
     Handle h;  // a bare context: default stream, no plan
     h.device = dev;
     CK(cudaDeviceGetAttribute(&h.num_sms, cudaDevAttrMultiProcessorCount, dev));
-    const int ldk = (K + 7) & ~7;
-    std::vector<__nv_bfloat16> a(static_cast<size_t>(M) * ldk, f2bf(0.f)), b(static_cast<size_t>(N) * ldk, f2bf(0.f));
-    for (int i = 0; i < M; ++i)
-      for (int k = 0; k < K; ++k) a[static_cast<size_t>(i) * ldk + k] = f2bf(A[static_cast<size_t>(i) * K + k]);
-    for (int i = 0; i < N; ++i)
-      for (int k = 0; k < K; ++k) b[static_cast<size_t>(i) * ldk + k] = f2bf(Bt[static_cast<size_t>(i) * K + k]);
-    const __nv_bfloat16* da = h.upload(a);
-    const __nv_bfloat16* db = h.upload(b);
+    const size_t na = static_cast<size_t>(M) * K, nb = static_cast<size_t>(K) * N;
+    const int lda = trans_a ? M : K, ldb = trans_b ? K : N;
     float* dc = h.dalloc<float>(static_cast<size_t>(M) * N);
-    gemm_stream(h, da, ldk, M, K, db, ldk, N, GsStore<float>{dc, N});
+    if (tf32) {
+      std::vector<float> a(A, A + na), b(B, B + nb);
+      gemm_rm(h, trans_a != 0, trans_b != 0, M, N, K, h.upload(a), lda, h.upload(b), ldb, dc, N);
+    } else {
+      if (lda % 8 || ldb % 8 || N % 32) throw ConfigError("op gemm (bf16): row pitches must be multiples of 8, N of 32");
+      std::vector<__nv_bfloat16> a(na), b(nb);
+      for (size_t i = 0; i < na; ++i) a[i] = f2bf(A[i]);
+      for (size_t i = 0; i < nb; ++i) b[i] = f2bf(B[i]);
+      gemm_rm16(h, trans_a != 0, trans_b != 0, M, N, K, h.upload(a), lda, h.upload(b), ldb, dc, N, false);
+    }
     CK(cudaMemcpy(C, dc, sizeof(float) * M * N, cudaMemcpyDeviceToHost));
   });
 }
@@ -2746,6 +2976,10 @@ int sort_set_option(SortHandle p, const char* name, int32_t value) {
       h->attn_fx = value != 0;
     } else if (std::strcmp(name, "stream_gemm") == 0) {
       h->stream_gemm = value != 0;
+    } else if (std::strcmp(name, "train_cublas") == 0) {
+      h->train_cublas = value != 0;
+    } else if (std::strcmp(name, "attn_bwd_tc") == 0) {
+      h->attn_bwd_tc = value != 0;
     } else if (std::strcmp(name, "moe_fused") == 0) {
       h->moe_fused = value != 0;
     } else {

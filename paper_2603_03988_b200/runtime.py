@@ -63,7 +63,7 @@ EXPORTS = [
     "sort_dataset_batch", "sort_moe_routing", "sort_moe_load", "sort_moe_update_bias",
     "sort_moe_forward", "sort_pretrain_forward", "sort_forward_async",
     "sort_nccl_unique_id", "sort_exchange_create_nccl", "sort_exchange_create_host",
-    "sort_exchange_destroy", "sort_exchange_lookup", "sort_exchange_allreduce_f32", "sort_op_gemm_bf16",
+    "sort_exchange_destroy", "sort_exchange_lookup", "sort_exchange_allreduce_f32", "sort_op_gemm",
 ]
 
 _lib = None
@@ -135,7 +135,7 @@ def lib():
         L.sort_exchange_lookup.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int64,
                                            C.c_void_p, C.c_void_p]
         L.sort_exchange_allreduce_f32.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
-        L.sort_op_gemm_bf16.argtypes = [C.c_int32, C.c_int32, C.c_int32, f32p, f32p, f32p]
+        L.sort_op_gemm.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, f32p, f32p, f32p]
         _lib = L
     return _lib
 
@@ -465,12 +465,15 @@ class SortModel:
         return dict(zip(keys, ms[: n.value].tolist()))
 
 
-def op_gemm(A: np.ndarray, Bt: np.ndarray) -> np.ndarray:
-    """C = A Bt^T on the streaming tcgen05 GEMM (bf16 operands, fp32 accumulation)."""
+def op_gemm(A: np.ndarray, B: np.ndarray, trans_a: bool = False, trans_b: bool = False, tf32: bool = False) -> np.ndarray:
+    """C = op(A) op(B) on the library's GEMM engines (sort_op_gemm): bf16 (tcgen05 streaming
+    GEMM) or fp32 at TF32 precision; A [M, K] (or [K, M] when trans_a), B [K, N] (or [N, K])."""
     A = np.ascontiguousarray(A, np.float32)
-    Bt = np.ascontiguousarray(Bt, np.float32)
-    C_ = np.zeros((A.shape[0], Bt.shape[0]), np.float32)
-    _check(lib().sort_op_gemm_bf16(A.shape[0], Bt.shape[0], A.shape[1], _p(A, f32p), _p(Bt, f32p), _p(C_, f32p)))
+    B = np.ascontiguousarray(B, np.float32)
+    M, K = (A.shape[1], A.shape[0]) if trans_a else A.shape
+    N = B.shape[0] if trans_b else B.shape[1]
+    C_ = np.zeros((M, N), np.float32)
+    _check(lib().sort_op_gemm(M, N, K, int(trans_a), int(trans_b), int(tf32), _p(A, f32p), _p(B, f32p), _p(C_, f32p)))
     return C_
 
 

@@ -2,14 +2,18 @@
 """GPU training step (sort_train_step: forward + backward of the whole scoring path) against
 the fp64 oracle backward (tests/test_oracle_backward.py pins that by finite differences).
 
-The GPU forward is bf16 (the inference kernels), the backward fp32 with TF32 GEMMs; the
+The GPU forward is bf16 (the inference kernels), the backward bf16 tcgen05 GEMMs and attention
+core with fp32 accumulation and gradients (the ranking head and tokenizer in fp32); the
 oracle is fed the same bf16-rounded weights. The bar is self-calibrated, because these
 gradients are intrinsically sensitive at bf16 resolution (ReLU / softmax decisions flip):
 the oracle's own gradients move by `noise[n]` (relative L2, the larger of NOISE_SAMPLES
 draws) when every trainable weight is perturbed by a relative N(0, 2^-8) -- one bf16 ulp,
 the resolution the GPU forward computes its activations at. Each GPU gradient must be
 within NOISE_FACTOR * noise[n] (floor GRAD_FLOOR) of the oracle's and point the same way
-(cosine > COS_MIN); dtokens likewise. Measured on B200: GPU error ~= 0.5-1.5x noise."""
+(cosine > COS_MIN, or above 1 - NOISE_FACTOR (1 - the oracle's own noise cosine) for
+gradients whose direction the perturbation already turns, e.g. a profile table with one
+contributing row per request); dtokens likewise. Measured on B200: GPU error ~= 0.5-1.5x
+noise."""
 import numpy as np
 import pytest
 
@@ -28,6 +32,10 @@ COS_MIN = 0.99
 
 def rel_l2(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def cosine(a, b):
+    return float((a * b).sum() / max(np.linalg.norm(a) * np.linalg.norm(b), 1e-30))
 
 
 def _oracle_grads(cfg, P, b, dz, names, B):
@@ -55,6 +63,7 @@ def _check_step(cfg, seed, B):
     assert np.max(np.abs(logits - zref)) < 5e-2
     rng = np.random.default_rng(seed + 2)
     noise = {n: 0.0 for n in names}
+    noise_cos = {n: 1.0 for n in names}
     dtok_noise = 0.0
     for _ in range(NOISE_SAMPLES):
         Pn = {k: (v * (1 + rng.normal(size=v.shape) * 2.0 ** -8) if k != "tok.item_table" else v)
@@ -62,15 +71,19 @@ def _check_step(cfg, seed, B):
         refn, dtokn, _ = _oracle_grads(cfg, Pn, b, dz, names, B)
         for n in names:
             noise[n] = max(noise[n], rel_l2(refn[n], ref[n]))
+            noise_cos[n] = min(noise_cos[n], cosine(refn[n], ref[n]))
         dtok_noise = max(dtok_noise, rel_l2(dtokn, dtok_ref))
     report = {}
     for n in names:
         g = gm.grad(n).astype(np.float64)
         err = rel_l2(g, ref[n])
-        cos = float((g * ref[n]).sum() / max(np.linalg.norm(g) * np.linalg.norm(ref[n]), 1e-30))
-        report[n] = (err, noise[n], cos)
+        cos = cosine(g, ref[n])
+        # the direction bar is calibrated like the magnitude bar: a gradient with few
+        # contributing rows (a profile table row per request) turns by bf16 noise alone
+        cos_min = min(COS_MIN, 1.0 - NOISE_FACTOR * (1.0 - noise_cos[n]))
+        report[n] = (err, noise[n], cos, cos_min)
     bad = {n: r for n, r in report.items()
-           if r[0] > max(NOISE_FACTOR * r[1], GRAD_FLOOR) or r[2] < COS_MIN}
+           if r[0] > max(NOISE_FACTOR * r[1], GRAD_FLOOR) or r[2] < r[3]}
     assert not bad, bad
     dtok = gm.dtokens(B)
     assert rel_l2(dtok, dtok_ref) < max(NOISE_FACTOR * dtok_noise, GRAD_FLOOR)
@@ -135,21 +148,36 @@ def test_bce_adamw_step_and_weight_repack():
     assert np.array_equal(p_dev, p_host)
 
 
-def test_tensor_core_and_simt_attention_backward_agree():
-    """k_attn_bwd_mma (bf16 mma.sync, dS/P rounded to bf16) against the fp32 SIMT kernels
-    (k_attn_bwd_dq / k_attn_bwd_dkv) on the same saved activations: every gradient within
-    bf16 resolution."""
-    cfg = tiny_config(keep=[262, 128])
+@pytest.mark.parametrize("mk", ["tiny", "base_shape"])
+def test_attention_backward_variants_agree(mk):
+    """The tcgen05 attention backward (k_attn_bwd_tc: dK/dV and dQ passes, default), the
+    mma.sync kernel (attn_bwd_tc = 0) and the fp32 SIMT kernels (attn_bwd_tc = attn_bwd_mma = 0)
+    on the same saved activations: every gradient within bf16 resolution. The tcgen05 passes
+    use no atomics: two runs are bit-identical."""
+    if mk == "tiny":
+        cfg = tiny_config(keep=[262, 128])
+        B = 2
+    else:
+        cfg = base_config(n_hist=300, n_cand=16, n_items=20000)
+        cfg.keep = [cfg.prefix_len, cfg.prefix_len, 128, 128]
+        B = 4
     P = synth.make_params(cfg, seed=12)
-    gm = R.SortModel(cfg, P, max_batch=2)
-    b = synth.make_batch(cfg, 2, seed=13)
-    dz = np.random.default_rng(4).normal(size=(2, cfg.n_cand, 3)).astype(np.float32)
+    gm = R.SortModel(cfg, P, max_batch=B)
+    b = synth.make_batch(cfg, B, seed=13)
+    dz = np.random.default_rng(4).normal(size=(B, cfg.n_cand, 3)).astype(np.float32)
     gm.train_step(b, dz)
-    g_mma = gm.grads_flat()
-    gm.set_option("attn_bwd_mma", 0)
+    g_tc = gm.grads_flat()
+    gm.train_step(b, dz)
+    assert np.array_equal(gm.grads_flat(), g_tc)
     try:
+        gm.set_option("attn_bwd_tc", 0)
+        gm.train_step(b, dz)
+        g_mma = gm.grads_flat()
+        gm.set_option("attn_bwd_mma", 0)
         gm.train_step(b, dz)
         g_simt = gm.grads_flat()
     finally:
+        gm.set_option("attn_bwd_tc", 1)
         gm.set_option("attn_bwd_mma", 1)
     assert rel_l2(g_mma, g_simt) < 1e-2
+    assert rel_l2(g_tc, g_simt) < 1e-2
