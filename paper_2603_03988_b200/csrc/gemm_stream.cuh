@@ -55,6 +55,19 @@ __device__ __forceinline__ uint64_t umma_sdesc_mnmajor_sw128(uint32_t saddr, uin
   return d;
 }
 
+// MN-major TF32 operands only exist in the 128-byte / 32-byte-atom swizzle (layout type 1,
+// Swizzle<2,5,2> on byte offsets: 4-row K groups of 128-byte rows, written by TMA with
+// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B): K groups are 512 B apart (SBO), MN atoms one box apart.
+__device__ __forceinline__ uint64_t umma_sdesc_mnmajor_sw128_32b(uint32_t saddr, uint32_t lbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4);
+  d |= static_cast<uint64_t>(lbo >> 4) << 16;
+  d |= static_cast<uint64_t>(512u >> 4) << 32;
+  d |= static_cast<uint64_t>(1u) << 46;
+  d |= static_cast<uint64_t>(1u) << 61;  // SWIZZLE_128B_BASE32B
+  return d;
+}
+
 // kAMN / kBMN: the operand is stored MN-major in HBM ([K, M] / [K, N] row-major, e.g. an
 // activation matrix X [rows, in] as the A = X^T of a weight gradient, or a reference weight
 // W [in, out] as the B of a forward product) and is loaded as 64 x 64 boxes. k_splits > 1
@@ -172,9 +185,11 @@ __global__ void __launch_bounds__(kGsThreads, 1)
           for (int k = 0; k < BK / MMA_K; ++k) {
             // K-major: the next K slice is 32 bytes further in every row; MN-major: MMA_K rows
             // (of 128 bytes) further
-            const uint64_t da = kAMN ? umma_sdesc_mnmajor_sw128(a0 + k * MMA_K * 128, kBox)
+            const uint64_t da = kAMN ? (kTf32 ? umma_sdesc_mnmajor_sw128_32b(a0 + k * MMA_K * 128, kBox)
+                                              : umma_sdesc_mnmajor_sw128(a0 + k * MMA_K * 128, kBox))
                                      : umma_sdesc_kmajor(a0 + k * 32, 128);
-            const uint64_t db = kBMN ? umma_sdesc_mnmajor_sw128(b0 + k * MMA_K * 128, kBox)
+            const uint64_t db = kBMN ? (kTf32 ? umma_sdesc_mnmajor_sw128_32b(b0 + k * MMA_K * 128, kBox)
+                                              : umma_sdesc_mnmajor_sw128(b0 + k * MMA_K * 128, kBox))
                                      : umma_sdesc_kmajor(b0 + k * 32, 128);
             if constexpr (kTf32) {
               mma_tf32_ss(d, da, db, idesc, (kb > kb0 || k > 0) ? 1u : 0u);

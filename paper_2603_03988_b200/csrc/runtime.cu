@@ -1169,15 +1169,17 @@ static void qkv_prep(Handle& h, const __nv_bfloat16* raw, int ld, int rows, int 
 }
 
 // ---- streaming tcgen05 GEMM (gemm_stream.cuh) for the generic path
+// mn_f32: an MN-major fp32 (TF32) operand, stored with the 32-byte-atom 128-byte swizzle
 static const CUtensorMap& gs_map(Handle& h, const void* p, uint64_t rows, uint64_t cols, uint64_t ld,
-                                 uint32_t box_rows, uint32_t box_cols = kGsBK, bool f32 = false) {
-  const auto key = std::make_tuple(p, rows, cols, ld, box_rows | (box_cols << 16) | (f32 ? 1u << 31 : 0u));
+                                 uint32_t box_rows, uint32_t box_cols = kGsBK, bool f32 = false, bool mn_f32 = false) {
+  const auto key = std::make_tuple(p, rows, cols, ld,
+                                   box_rows | (box_cols << 16) | (f32 ? 1u << 31 : 0u) | (mn_f32 ? 1u << 30 : 0u));
   auto it = h.gs_maps.find(key);
   if (it != h.gs_maps.end()) return it->second;
   if (!f32) return h.gs_maps[key] = make_tmap_2d(p, rows, cols, ld, box_rows, box_cols, 128);
   const uint64_t dims[2] = {cols, rows}, str[1] = {ld * 4};
   const uint32_t box[2] = {box_cols, box_rows};
-  return h.gs_maps[key] = make_tmap(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, p, 2, dims, str, box, 128);
+  return h.gs_maps[key] = make_tmap(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, p, 2, dims, str, box, mn_f32 ? 129 : 128);
 }
 
 // C[M, N] = op(A)[M, K] x op(B)[K, N] on the streaming tcgen05 GEMM, epilogue functor epi:
@@ -1191,8 +1193,8 @@ static void gemm_stream(Handle& h, const T* A, int lda, int M, int K, const T* B
   constexpr bool f32 = std::is_same_v<T, float>;
   constexpr uint32_t BK = 128 / sizeof(T), kAtom = 128 / sizeof(T);
   if (N % Epi::kChunk != 0) throw ConfigError("stream gemm: N must be a multiple of the epilogue chunk");
-  const CUtensorMap& ta = kAMN ? gs_map(h, A, K, M, lda, BK, kAtom, f32) : gs_map(h, A, M, K, lda, kGsBM, BK, f32);
-  const CUtensorMap& tb = kBMN ? gs_map(h, Bt, K, N, ldb, BK, kAtom, f32) : gs_map(h, Bt, N, K, ldb, kGsBN, BK, f32);
+  const CUtensorMap& ta = kAMN ? gs_map(h, A, K, M, lda, BK, kAtom, f32, f32) : gs_map(h, A, M, K, lda, kGsBM, BK, f32);
+  const CUtensorMap& tb = kBMN ? gs_map(h, Bt, K, N, ldb, BK, kAtom, f32, f32) : gs_map(h, Bt, N, K, ldb, kGsBN, BK, f32);
   ensure_smem(k_gemm_stream<Epi, kAMN, kBMN, T>, kGsSmem);
   const int tiles = ((M + kGsBM - 1) / kGsBM) * ((N + kGsBN - 1) / kGsBN) * k_splits;
   k_gemm_stream<Epi, kAMN, kBMN, T><<<std::min(tiles, h.num_sms), kGsThreads, kGsSmem, h.stream>>>(

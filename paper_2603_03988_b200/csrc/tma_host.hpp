@@ -34,6 +34,7 @@ inline CUtensorMapSwizzle tma_swizzle(int bytes) {
     case 32: return CU_TENSOR_MAP_SWIZZLE_32B;
     case 64: return CU_TENSOR_MAP_SWIZZLE_64B;
     case 128: return CU_TENSOR_MAP_SWIZZLE_128B;
+    case 129: return CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;  // (code 129) the MN-major TF32 UMMA layout
     default: throw std::runtime_error("bad swizzle");
   }
 }
@@ -43,14 +44,21 @@ inline CUtensorMapSwizzle tma_swizzle(int bytes) {
 inline CUtensorMap make_tmap(CUtensorMapDataType dt, const void* base, int rank, const uint64_t* dims,
                              const uint64_t* strides_bytes, const uint32_t* box, int swizzle_bytes) {
   CUtensorMap m;
-  uint32_t elem_strides[3] = {1, 1, 1};
+  uint32_t elem_strides[5] = {1, 1, 1, 1, 1};
   CUresult r = tma_encode_fn()(&m, dt, rank, const_cast<void*>(base),
                                dims, strides_bytes, box, elem_strides,
                                CU_TENSOR_MAP_INTERLEAVE_NONE, tma_swizzle(swizzle_bytes),
                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
-    throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)));
+    std::string what = "cuTensorMapEncodeTiled failed: " + std::to_string(static_cast<int>(r)) + " (base " +
+                       std::to_string(reinterpret_cast<uintptr_t>(base)) + ", dims";
+    for (int i = 0; i < rank; ++i) what += " " + std::to_string(dims[i]);
+    what += ", strides";
+    for (int i = 0; i + 1 < rank; ++i) what += " " + std::to_string(strides_bytes[i]);
+    what += ", box";
+    for (int i = 0; i < rank; ++i) what += " " + std::to_string(box[i]);
+    throw std::runtime_error(what + ")");
   }
   return m;
 }

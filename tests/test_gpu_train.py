@@ -10,7 +10,7 @@ the oracle's own gradients move by `noise[n]` (relative L2, the larger of NOISE_
 draws) when every trainable weight is perturbed by a relative N(0, 2^-8) -- one bf16 ulp,
 the resolution the GPU forward computes its activations at. Each GPU gradient must be
 within NOISE_FACTOR * noise[n] (floor GRAD_FLOOR) of the oracle's and point the same way
-(cosine > COS_MIN, or above 1 - NOISE_FACTOR (1 - the oracle's own noise cosine) for
+(cosine > COS_MIN, or above 1 - NOISE_FACTOR^2 (1 - the oracle's own noise cosine) for
 gradients whose direction the perturbation already turns, e.g. a profile table with one
 contributing row per request); dtokens likewise. Measured on B200: GPU error ~= 0.5-1.5x
 noise."""
@@ -80,7 +80,9 @@ def _check_step(cfg, seed, B):
         cos = cosine(g, ref[n])
         # the direction bar is calibrated like the magnitude bar: a gradient with few
         # contributing rows (a profile table row per request) turns by bf16 noise alone
-        cos_min = min(COS_MIN, 1.0 - NOISE_FACTOR * (1.0 - noise_cos[n]))
+        # (1 - cos) grows with the square of the angle, so a NOISE_FACTOR x larger angle than
+        # the perturbation's own is NOISE_FACTOR^2 x its (1 - cos))
+        cos_min = min(COS_MIN, 1.0 - NOISE_FACTOR ** 2 * (1.0 - noise_cos[n]))
         report[n] = (err, noise[n], cos, cos_min)
     bad = {n: r for n, r in report.items()
            if r[0] > max(NOISE_FACTOR * r[1], GRAD_FLOOR) or r[2] < r[3]}
@@ -153,7 +155,7 @@ def test_attention_backward_variants_agree(mk):
     """The tcgen05 attention backward (k_attn_bwd_tc: dK/dV and dQ passes, default), the
     mma.sync kernel (attn_bwd_tc = 0) and the fp32 SIMT kernels (attn_bwd_tc = attn_bwd_mma = 0)
     on the same saved activations: every gradient within bf16 resolution. The tcgen05 passes
-    use no atomics: two runs are bit-identical."""
+    use no atomics: the weight-matrix gradients of two runs are bit-identical."""
     if mk == "tiny":
         cfg = tiny_config(keep=[262, 128])
         B = 2
@@ -167,8 +169,13 @@ def test_attention_backward_variants_agree(mk):
     dz = np.random.default_rng(4).normal(size=(B, cfg.n_cand, 3)).astype(np.float32)
     gm.train_step(b, dz)
     g_tc = gm.grads_flat()
+    det = [n for n in P if n.split(".")[-1] in ("wq", "wk", "wv", "wo", "wg", "w_gate", "w_up", "w_down")]
+    g_det = {n: gm.grad(n) for n in det}
     gm.train_step(b, dz)
-    assert np.array_equal(gm.grads_flat(), g_tc)
+    # every weight-matrix gradient (GEMMs over the attention-core adjoints) is bit-identical
+    # across runs; gain / bias / feature-table sums use float atomics across CTAs
+    for n in det:
+        assert np.array_equal(gm.grad(n), g_det[n]), n
     try:
         gm.set_option("attn_bwd_tc", 0)
         gm.train_step(b, dz)
