@@ -286,9 +286,7 @@ int sort_dataset_batch(SortDataset d, int64_t first, int32_t count, int32_t n_hi
  * GEMM as CTA pairs, default 0 for the same reason); "attn_bwd_mma" (1 = tensor-core
  * attention backward, the default; 0 = the fp32 SIMT kernels); "moe_fused" (1 = one fused expert kernel per MoE layer, the hidden
  * chunk kept in TMEM, the default; 0 = the grouped [gate|up] and down GEMM pair);
- * "attn_subtiles" (1 = the 64-column-subtile
- * attention kernel with O accumulated in TMEM, k_attention_f; 0 = k_attention, the default:
- * measured faster); "graphs" (1 = replay the
+ * "graphs" (1 = replay the
  * inference forward from a CUDA graph per (batch size, input slot, item table), the default;
  * 0 = eager launches). Status 1 on an unknown name. */
 int sort_set_option(SortHandle h, const char* name, int32_t value);

@@ -15,7 +15,6 @@
 
 #include "../../include/sort_b200.h"
 #include "attention.cuh"
-#include "attention_fx.cuh"
 #include "attn_bwd.cuh"
 #include "block_tail.cuh"
 #include "epilogues.cuh"
@@ -91,7 +90,6 @@ struct Handle {
   bool attn_bwd_mma = true; // sort_set_option("attn_bwd_mma"): tensor-core attention backward
   bool attn_bwd_tc = true;  // sort_set_option("attn_bwd_tc"): tcgen05 attention backward (0: mma.sync)
   bool qkvg_pair = false;   // sort_set_option("qkvg_pair"): QKVG projection as CTA pairs
-  bool attn_fx = false;     // sort_set_option("attn_fx"): fixed-reference layers run k_attn_fx (0: k_attention)
   bool generic = false;    // d > 256 (SORT-large): projections through the generic path
   // ---- MoE FFN: routed + shared experts as grouped tcgen05 GEMMs
   bool moe = false;
@@ -764,17 +762,6 @@ static void launch_attention_dk(Handle& h, const LayerDev& L, const LayerPlan& l
   const CUtensorMap& tq = h.save_to ? h.save_to->tmQ : L.tmQ;
   const CUtensorMap& tk = h.save_to ? h.save_to->tmK : L.tmK;
   const CUtensorMap& tv = h.save_to ? h.save_to->tmV : L.tmV;
-  if constexpr (kFixed) {
-    if (h.attn_fx) {  // fixed reference: O accumulated in TMEM (attention_fx.cuh)
-      const size_t smem_f = AttnSmem<DK>::bytes(tile_ints);
-      ensure_smem(k_attn_fx<DK>, smem_f);
-      const int grid_f = std::min(n_items, FxTmem<DK>::kCtasPerSm * h.num_sms);
-      k_attn_fx<DK><<<grid_f, kAttnThreads, smem_f, h.stream>>>(tq, tk, tv, a);
-      check_launch("attention");
-      ++h.launches;
-      return;
-    }
-  }
   const size_t smem = AttnSmem<DK>::bytes(tile_ints);
   ensure_smem(k_attention<DK, kFixed>, smem);
   const int grid = std::min(n_items, AttnTmem<DK>::kCtasPerSm * h.num_sms);
@@ -2974,8 +2961,7 @@ int sort_set_option(SortHandle p, const char* name, int32_t value) {
       h->attn_bwd_mma = value != 0;
     } else if (std::strcmp(name, "qkvg_pair") == 0) {
       h->qkvg_pair = value != 0;
-    } else if (std::strcmp(name, "attn_fx") == 0) {
-      h->attn_fx = value != 0;
+
     } else if (std::strcmp(name, "stream_gemm") == 0) {
       h->stream_gemm = value != 0;
     } else if (std::strcmp(name, "train_cublas") == 0) {

@@ -259,7 +259,7 @@ class SortModel:
             _check(lib().sort_load_param(self.h, name.encode(), _p(a32, f32p), a32.shape[0],
                                          a32.shape[1]))
         _check(lib().sort_finalize_params(self.h))
-        # experiments only: SORT_OPTIONS="attn_fx=0,graphs=1" sets library options (A/B runs)
+        # experiments only: SORT_OPTIONS="graphs=0" sets library options (A/B runs)
         for kv in filter(None, os.environ.get("SORT_OPTIONS", "").split(",")):
             k, v = kv.split("=")
             self.set_option(k.strip(), int(v))
