@@ -86,7 +86,7 @@ class MatT {
 using Mat = MatT<double>;
 
 struct TokenSequence {
-  MatT<float> tokens;  // L x d (bf16 values widened to fp32)
+  Mat tokens;  // L x d (the device's bf16 token rows, widened)
   std::vector<int> position_ids;
   std::vector<Role> roles;
   std::vector<int> candidate_index;
@@ -275,9 +275,11 @@ class Model {
     Packed p = pack(one, 0, 1);
     const int L = seq_len();
     TokenSequence t;
-    t.tokens = MatT<float>(L, cfg_.model_dim);
+    t.tokens = Mat(L, cfg_.model_dim);
+    std::vector<float> tok(static_cast<size_t>(L) * static_cast<size_t>(cfg_.model_dim));
     std::vector<int32_t> pos(L), roles(L), cidx(L), ht(static_cast<size_t>(cfg_.n_hist > 0 ? cfg_.n_hist : 1));
-    check(sort_tokenize(h_, &p.batch, t.tokens.data(), ht.data(), pos.data(), roles.data(), cidx.data()));
+    check(sort_tokenize(h_, &p.batch, tok.data(), ht.data(), pos.data(), roles.data(), cidx.data()));
+    for (size_t i = 0; i < tok.size(); ++i) t.tokens.data()[i] = tok[i];
     t.position_ids.assign(pos.begin(), pos.end());
     for (int32_t r : roles) t.roles.push_back(static_cast<Role>(r));
     t.candidate_index.assign(cidx.begin(), cidx.end());

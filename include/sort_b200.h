@@ -163,6 +163,31 @@ int sort_block_attention(int32_t nh, int32_t l_q, int32_t l_kv, int32_t dk, cons
                          const float* k, const float* v, const int32_t* lo, const int32_t* hi,
                          const int32_t* self_idx, float* out, int64_t* skipped, int64_t* total);
 
+/* ---------------------------------------------------------------- operator-level entries */
+/* The reference's free functions / AttentionLayer as standalone device ops (no handle; host fp32
+ * buffers in and out). include/rankformer/reference_api.hpp binds them with the reference's
+ * signatures.
+ * rmsnorm_forward (norm.hpp:17-29): y [rows, cols] = x / rms(x) * gain, inv_rms [rows]. */
+int sort_op_rmsnorm(int32_t rows, int32_t cols, const float* x, const float* gain, float* y, float* inv_rms);
+/* rmsnorm_backward (norm.hpp:32-45): dx written, dgain [cols] ACCUMULATED (+=) like the reference. */
+int sort_op_rmsnorm_backward(int32_t rows, int32_t cols, const float* dy, const float* x, const float* inv_rms,
+                             const float* gain, float* dx, float* dgain);
+/* rope_apply (rope.hpp:13-40): out [rows, dim], dim even (else status 1), inverse = exact adjoint. */
+int sort_op_rope(int32_t rows, int32_t dim, const float* x, const int32_t* position_ids, double theta_base,
+                 int32_t inverse, float* out);
+/* AttentionLayer::forward (attention.hpp:58-59, attention.cpp:71-132) and, with dout != NULL,
+ * AttentionLayer::backward (attention.hpp:62-63, attention.cpp:134-202) of one layer on one
+ * request: xn [l_in, d] (normalised input), query_rows [l_q] strictly increasing into xn, the mask
+ * as build_mask rows in compact form (visible = [lo, hi] U {self}; self -1 = none), position_ids
+ * [l_in]. weights[7] = wq, wk, wv, wg, wo ([d, d], [in, out]) and qk_gain_q, qk_gain_k ([heads, dk]).
+ * out [l_q, d]. Backward: dxn [l_in, d] written; dweights[i] ACCUMULATED (+=), NULL entry = frozen
+ * parameter (params.hpp:15-25). dk in {16, 32, 64}; backward needs d <= 256; qknorm = gate = 1. */
+int sort_op_attention_layer(int32_t model_dim, int32_t heads, double rope_theta, int32_t qknorm, int32_t gate,
+                            int32_t l_in, int32_t l_q, const float* xn, const int32_t* query_rows, const int32_t* lo,
+                            const int32_t* hi, const int32_t* self_idx, const int32_t* position_ids,
+                            const float* const* weights, float* out, const float* dout, float* dxn,
+                            float* const* dweights);
+
 /* ---------------------------------------------------------------- host planner */
 /* Host-only integer rules (no GPU needed): time_bucket (tokenizer.cpp:36-40),
  * make_geometric_schedule (mask.cpp:97-117), retained_rows (mask.cpp:132-154) and the

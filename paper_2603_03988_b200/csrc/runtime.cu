@@ -149,6 +149,8 @@ struct Handle {
   float *tw[16] = {nullptr};  // backward workspace
   __nv_bfloat16* dO16 = nullptr;  // bf16 copy of dL/d(attention output) for the tensor-core backward
   float* dtokens = nullptr;
+  float* wpad = nullptr;  // tokenizer backward: zero-padded projection weight
+  size_t wpad_cap = 0;
   float* dz_dev = nullptr;                 // dL/dlogits of the current step
   int32_t* t_rows = nullptr;               // tokenizer backward: token row of each group row
   // generic (d > 256) forward: fp32 residual stream and workspace
@@ -1427,6 +1429,91 @@ static void build_bwd_tc_lists(const LayerPlan& lp, bool dq_mode, std::vector<in
   if (code.empty()) code.push_back(make_int2(0, 0));
 }
 
+// Saved-activation buffers, TMA boxes and backward work lists of one training layer
+// (B requests of plan lp); the dO16 boxes are added by the caller once dO16 exists.
+static void train_layer_buffers(Handle& h, const LayerPlan& lp, const LayerDev& L, int B, Handle::TrainLayer& T) {
+  const int d = h.d;
+  const size_t nq = static_cast<size_t>(B) * L.Rq * d, nkv = static_cast<size_t>(B) * L.Rkv * d;
+  T.x_in = h.dalloc<__nv_bfloat16>(nkv);
+  T.q = h.dalloc<__nv_bfloat16>(nq);
+  T.k = h.dalloc<__nv_bfloat16>(nkv);
+  T.v = h.dalloc<__nv_bfloat16>(nkv);
+  T.g = h.dalloc<__nv_bfloat16>(nq);
+  T.o_pre = h.dalloc<__nv_bfloat16>(nq);
+  T.x1 = h.dalloc<__nv_bfloat16>(nq);
+  T.lse = h.dalloc<float>(static_cast<size_t>(B) * h.H * L.Rq);
+  {
+    const int dk = h.dk;
+    const uint64_t BH = static_cast<uint64_t>(B) * h.H;
+    uint64_t dq[3] = {static_cast<uint64_t>(dk), static_cast<uint64_t>(L.Rq), BH};
+    uint64_t sq[2] = {static_cast<uint64_t>(dk) * 2, static_cast<uint64_t>(L.Rq) * dk * 2};
+    uint32_t bq[3] = {static_cast<uint32_t>(dk), 128, 1};
+    T.tmQ = make_tmap_bf16(T.q, 3, dq, sq, bq, dk * 2);
+    uint64_t dkd[3] = {static_cast<uint64_t>(dk), static_cast<uint64_t>(L.Rkv), BH};
+    uint64_t skd[2] = {static_cast<uint64_t>(dk) * 2, static_cast<uint64_t>(L.Rkv) * dk * 2};
+    T.tmK = make_tmap_bf16(T.k, 3, dkd, skd, bq, dk * 2);
+    T.tmV = make_tmap_bf16(T.v, 3, dkd, skd, bq, dk * 2);
+    uint32_t b64[3] = {static_cast<uint32_t>(dk), 64, 1};
+    T.tmQ64 = make_tmap_bf16(T.q, 3, dq, sq, b64, dk * 2);
+    T.tmK64 = make_tmap_bf16(T.k, 3, dkd, skd, b64, dk * 2);
+    T.tmV64 = make_tmap_bf16(T.v, 3, dkd, skd, b64, dk * 2);
+  }
+  {
+    std::vector<int32_t> off;
+    std::vector<int2> code;
+    build_bwd_tc_lists(lp, false, off, code);
+    T.tc_kv_off = h.upload(off);
+    T.tc_kv_code = h.upload(code);
+    T.tc_kv_n = static_cast<int>(code.size());
+    build_bwd_tc_lists(lp, true, off, code);
+    T.tc_q_off = h.upload(off);
+    T.tc_q_code = h.upload(code);
+    T.tc_q_n = static_cast<int>(code.size());
+  }
+  std::vector<int32_t> qo, ko;
+  std::vector<int2> qi, ki;
+  build_bwd_lists(lp, qo, qi, ko, ki);
+  if (qi.empty()) qi.push_back(make_int2(0, 0));
+  if (ki.empty()) ki.push_back(make_int2(0, 0));
+  T.dq_off = h.upload(qo);
+  T.dq_iv = h.upload(qi);
+  T.dkv_off = h.upload(ko);
+  T.dkv_iv = h.upload(ki);
+  {  // 64-row q blocks that see each 64-column kv block (k_attn_bwd_mma)
+    std::vector<int32_t> off(1, 0), lst;
+    for (int c0 = 0; c0 < lp.l_kv; c0 += 64) {
+      const int c1 = std::min(lp.l_kv, c0 + 64) - 1;
+      for (int qb = 0; qb * 64 < lp.l_q; ++qb) {
+        bool any = false;
+        for (int r = qb * 64; r < std::min(lp.l_q, qb * 64 + 64) && !any; ++r)
+          any = (lp.hi[r] >= lp.lo[r] && lp.lo[r] <= c1 && lp.hi[r] >= c0) ||
+                (lp.self_idx[r] >= c0 && lp.self_idx[r] <= c1);
+        if (!any) continue;
+        // every (q, kv) of the 64 x 64 block visible and in range: no per-element mask
+        bool full = qb * 64 + 64 <= lp.l_q && c0 + 64 <= lp.l_kv;
+        for (int r = qb * 64; r < qb * 64 + 64 && full; ++r) full = lp.lo[r] <= c0 && lp.hi[r] >= c1;
+        lst.push_back(full ? (qb | static_cast<int32_t>(0x40000000)) : qb);
+      }
+      off.push_back(static_cast<int32_t>(lst.size()));
+    }
+    if (lst.empty()) lst.push_back(0);
+    T.qb_off = h.upload(off);
+    T.qb_list = h.upload(lst);
+  }
+}
+
+// dO16 as token-major [B, Rq, H, dk] boxes (128- and 64-row) for the tcgen05 backward
+static void train_do_boxes(Handle& h, int Rq, int B, Handle::TrainLayer& T) {
+  const int dk = h.dk, d = h.d;
+  const uint64_t dims[4] = {static_cast<uint64_t>(dk), static_cast<uint64_t>(h.H), static_cast<uint64_t>(Rq),
+                            static_cast<uint64_t>(B)};
+  const uint64_t str[3] = {static_cast<uint64_t>(dk) * 2, static_cast<uint64_t>(d) * 2,
+                           static_cast<uint64_t>(Rq) * d * 2};
+  const uint32_t b128[4] = {static_cast<uint32_t>(dk), 1, 128, 1}, b64[4] = {static_cast<uint32_t>(dk), 1, 64, 1};
+  T.tmDO128 = make_tmap(CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, h.dO16, 4, dims, str, b128, dk * 2);
+  T.tmDO64 = make_tmap(CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, h.dO16, 4, dims, str, b64, dk * 2);
+}
+
 static void ensure_train_buffers(Handle& h, int B) {
   if (h.cfg.pretrain) throw ConfigError("training step: use the ranking model (pretrain backward not in this build)");
   if (h.moe) throw ConfigError("training step: the MoE FFN backward is not implemented in this build");
@@ -1442,75 +1529,7 @@ static void ensure_train_buffers(Handle& h, int B) {
   size_t mkv_max = 0;
   for (int l = 0; l < h.cfg.layers; ++l) {
     const LayerDev& L = h.layers[l];
-    auto& T = h.tl[l];
-    const size_t nq = static_cast<size_t>(B) * L.Rq * d, nkv = static_cast<size_t>(B) * L.Rkv * d;
-    T.x_in = h.dalloc<__nv_bfloat16>(nkv);
-    T.q = h.dalloc<__nv_bfloat16>(nq);
-    T.k = h.dalloc<__nv_bfloat16>(nkv);
-    T.v = h.dalloc<__nv_bfloat16>(nkv);
-    T.g = h.dalloc<__nv_bfloat16>(nq);
-    T.o_pre = h.dalloc<__nv_bfloat16>(nq);
-    T.x1 = h.dalloc<__nv_bfloat16>(nq);
-    T.lse = h.dalloc<float>(static_cast<size_t>(B) * h.H * L.Rq);
-    {
-      const int dk = h.dk;
-      const uint64_t BH = static_cast<uint64_t>(B) * h.H;
-      uint64_t dq[3] = {static_cast<uint64_t>(dk), static_cast<uint64_t>(L.Rq), BH};
-      uint64_t sq[2] = {static_cast<uint64_t>(dk) * 2, static_cast<uint64_t>(L.Rq) * dk * 2};
-      uint32_t bq[3] = {static_cast<uint32_t>(dk), 128, 1};
-      T.tmQ = make_tmap_bf16(T.q, 3, dq, sq, bq, dk * 2);
-      uint64_t dkd[3] = {static_cast<uint64_t>(dk), static_cast<uint64_t>(L.Rkv), BH};
-      uint64_t skd[2] = {static_cast<uint64_t>(dk) * 2, static_cast<uint64_t>(L.Rkv) * dk * 2};
-      T.tmK = make_tmap_bf16(T.k, 3, dkd, skd, bq, dk * 2);
-      T.tmV = make_tmap_bf16(T.v, 3, dkd, skd, bq, dk * 2);
-      uint32_t b64[3] = {static_cast<uint32_t>(dk), 64, 1};
-      T.tmQ64 = make_tmap_bf16(T.q, 3, dq, sq, b64, dk * 2);
-      T.tmK64 = make_tmap_bf16(T.k, 3, dkd, skd, b64, dk * 2);
-      T.tmV64 = make_tmap_bf16(T.v, 3, dkd, skd, b64, dk * 2);
-    }
-    {
-      std::vector<int32_t> off;
-      std::vector<int2> code;
-      build_bwd_tc_lists(h.plan.layers[l], false, off, code);
-      T.tc_kv_off = h.upload(off);
-      T.tc_kv_code = h.upload(code);
-      T.tc_kv_n = static_cast<int>(code.size());
-      build_bwd_tc_lists(h.plan.layers[l], true, off, code);
-      T.tc_q_off = h.upload(off);
-      T.tc_q_code = h.upload(code);
-      T.tc_q_n = static_cast<int>(code.size());
-    }
-    std::vector<int32_t> qo, ko;
-    std::vector<int2> qi, ki;
-    build_bwd_lists(h.plan.layers[l], qo, qi, ko, ki);
-    if (qi.empty()) qi.push_back(make_int2(0, 0));
-    if (ki.empty()) ki.push_back(make_int2(0, 0));
-    T.dq_off = h.upload(qo);
-    T.dq_iv = h.upload(qi);
-    T.dkv_off = h.upload(ko);
-    T.dkv_iv = h.upload(ki);
-    {  // 64-row q blocks that see each 64-column kv block (k_attn_bwd_mma)
-      const LayerPlan& lp = h.plan.layers[l];
-      std::vector<int32_t> off(1, 0), lst;
-      for (int c0 = 0; c0 < lp.l_kv; c0 += 64) {
-        const int c1 = std::min(lp.l_kv, c0 + 64) - 1;
-        for (int qb = 0; qb * 64 < lp.l_q; ++qb) {
-          bool any = false;
-          for (int r = qb * 64; r < std::min(lp.l_q, qb * 64 + 64) && !any; ++r)
-            any = (lp.hi[r] >= lp.lo[r] && lp.lo[r] <= c1 && lp.hi[r] >= c0) ||
-                  (lp.self_idx[r] >= c0 && lp.self_idx[r] <= c1);
-          if (!any) continue;
-          // every (q, kv) of the 64 x 64 block visible and in range: no per-element mask
-          bool full = qb * 64 + 64 <= lp.l_q && c0 + 64 <= lp.l_kv;
-          for (int r = qb * 64; r < qb * 64 + 64 && full; ++r) full = lp.lo[r] <= c0 && lp.hi[r] >= c1;
-          lst.push_back(full ? (qb | static_cast<int32_t>(0x40000000)) : qb);
-        }
-        off.push_back(static_cast<int32_t>(lst.size()));
-      }
-      if (lst.empty()) lst.push_back(0);
-      T.qb_off = h.upload(off);
-      T.qb_list = h.upload(lst);
-    }
+    train_layer_buffers(h, h.plan.layers[l], L, B, h.tl[l]);
     mkv_max = std::max(mkv_max, static_cast<size_t>(B) * L.Rkv);
   }
   const size_t rows = std::max(mkv_max, static_cast<size_t>(B) * h.L0);
@@ -1518,16 +1537,7 @@ static void ensure_train_buffers(Handle& h, int B) {
   // 11 raw, 12 GU / dGU, 13 z / dz, 14 inv (rows), 15 D / head scratch
   for (int i = 0; i < 12; ++i) h.tw[i] = h.dalloc<float>(rows * d);
   h.dO16 = h.dalloc<__nv_bfloat16>(rows * d);
-  for (int l = 0; l < h.cfg.layers; ++l) {  // dO16 as token-major [B, Rq, H, dk] boxes
-    const int dk = h.dk;
-    const uint64_t dims[4] = {static_cast<uint64_t>(dk), static_cast<uint64_t>(h.H),
-                              static_cast<uint64_t>(h.layers[l].Rq), static_cast<uint64_t>(B)};
-    const uint64_t str[3] = {static_cast<uint64_t>(dk) * 2, static_cast<uint64_t>(d) * 2,
-                             static_cast<uint64_t>(h.layers[l].Rq) * d * 2};
-    const uint32_t b128[4] = {static_cast<uint32_t>(dk), 1, 128, 1}, b64[4] = {static_cast<uint32_t>(dk), 1, 64, 1};
-    h.tl[l].tmDO128 = make_tmap(CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, h.dO16, 4, dims, str, b128, dk * 2);
-    h.tl[l].tmDO64 = make_tmap(CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, h.dO16, 4, dims, str, b64, dk * 2);
-  }
+  for (int l = 0; l < h.cfg.layers; ++l) train_do_boxes(h, h.layers[l].Rq, B, h.tl[l]);
   h.tw[12] = h.dalloc<float>(rows * 2 * m * 2);  // GU and dGU
   h.tw[13] = h.dalloc<float>(rows * m);
   h.tw[14] = h.dalloc<float>(rows * 2);
@@ -1558,6 +1568,59 @@ static void rms_bwd(Handle& h, const float* dy, const T* x, const float* inv, co
 }
 
 // Backward of one training forward; dz = dL/dlogits [B*N, 3] on the device.
+// tcgen05 attention-core backward (attn_bwd.cuh) of one layer, B requests: pass 1 dK / dV per
+// 128-row kv block (X = K, V; Y = Q, dO), pass 2 dQ per 128-row q block (X = Q, dO; Y = K, V).
+// D = rowsum(dO * O) per (bh, query row); dV is also written as bf16 (dV16).
+static void attn_core_backward_tc(Handle& h, const LayerDev& L, const Handle::TrainLayer& T, int B, const float* Dd,
+                                  float* dQ, float* dK, float* dV, __nv_bfloat16* dV16) {
+  const int H = h.H, dk = h.dk;
+  AttnBwdTcArgs tb;
+  tb.rowmeta = L.rowmeta;
+  tb.lse = T.lse;
+  tb.D = Dd;
+  tb.BH = B * H;
+  tb.H = H;
+  tb.Rq = L.Rq;
+  tb.Rkv = L.Rkv;
+  tb.scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(dk)));
+  tb.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(dk)));
+  tb.x_off = T.tc_kv_off;
+  tb.y_code = T.tc_kv_code;
+  tb.nX = (L.Rkv + 127) / 128;
+  tb.out0 = dK;
+  tb.out1 = dV;
+  tb.out1_16 = dV16;
+  auto launch_tc = [&](auto kern, const CUtensorMap& x0, const CUtensorMap& x1, const CUtensorMap& y0,
+                       const CUtensorMap& y1, size_t smem_fn_bytes) {
+    ensure_smem(kern, smem_fn_bytes);
+    const int grid = std::min(tb.nX * tb.BH, 2 * h.num_sms);
+    kern<<<grid, kAttnThreads, smem_fn_bytes, h.stream>>>(x0, x1, y0, y1, tb);
+  };
+#define SORT_BWD_TC(DKV)                                                                               \
+  case DKV: {                                                                                          \
+    launch_tc(k_attn_bwd_tc<DKV, false>, T.tmK, T.tmV, T.tmQ64, T.tmDO64,                              \
+              BwdSmem<DKV>::bytes(tb.nX + 2 + 2 * T.tc_kv_n));                                         \
+    tb.x_off = T.tc_q_off;                                                                             \
+    tb.y_code = T.tc_q_code;                                                                           \
+    tb.nX = (L.Rq + 127) / 128;                                                                        \
+    tb.out0 = dQ;                                                                                      \
+    tb.out1 = nullptr;                                                                                 \
+    tb.out1_16 = nullptr;                                                                              \
+    launch_tc(k_attn_bwd_tc<DKV, true>, T.tmQ, T.tmDO128, T.tmK64, T.tmV64,                            \
+              BwdSmem<DKV>::bytes(tb.nX + 2 + 2 * T.tc_q_n));                                          \
+    break;                                                                                             \
+  }
+  switch (dk) {
+    SORT_BWD_TC(16)
+    SORT_BWD_TC(32)
+    SORT_BWD_TC(64)
+    default: throw ConfigError("training: unsupported head dim");
+  }
+#undef SORT_BWD_TC
+  check_launch("tcgen05 attention backward");
+  h.launches += 2;
+}
+
 static void backward_device(Handle& h, int B, const float* dz) {
   const SortConfig& c = h.cfg;
   const int d = h.d, m = h.m, H = h.H, dk = h.dk, N = c.n_cand, dh = h.dh;
@@ -1702,52 +1765,8 @@ static void backward_device(Handle& h, int B, const float* dz) {
     ak.blk_off = T.dkv_off;
     ak.blk_iv = T.dkv_iv;
     if (h.attn_bwd_tc) {
-      AttnBwdTcArgs tb;
-      tb.rowmeta = L.rowmeta;
-      tb.lse = T.lse;
-      tb.D = Dd;
-      tb.BH = B * H;
-      tb.H = H;
-      tb.Rq = L.Rq;
-      tb.Rkv = L.Rkv;
-      tb.scale = ab.scale;
-      tb.scale_log2 = ab.scale_log2;
-      // pass 1: dK, dV per 128-row kv block (X = K, V; Y = Q, dO)
-      tb.x_off = T.tc_kv_off;
-      tb.y_code = T.tc_kv_code;
-      tb.nX = (L.Rkv + 127) / 128;
-      tb.out0 = dK;
-      tb.out1 = dV;
-      tb.out1_16 = reinterpret_cast<__nv_bfloat16*>(h.tw[12]) + 2 * static_cast<size_t>(h.train_B) * h.L0 * d;
-      auto launch_tc = [&](auto kern, const CUtensorMap& x0, const CUtensorMap& x1, const CUtensorMap& y0,
-                           const CUtensorMap& y1, int n_codes, size_t smem_fn_bytes) {
-        ensure_smem(kern, smem_fn_bytes);
-        const int grid = std::min(tb.nX * tb.BH, 2 * h.num_sms);
-        kern<<<grid, kAttnThreads, smem_fn_bytes, h.stream>>>(x0, x1, y0, y1, tb);
-        (void)n_codes;
-      };
-#define SORT_BWD_TC(DKV)                                                                                      \
-  case DKV: {                                                                                                 \
-    launch_tc(k_attn_bwd_tc<DKV, false>, T.tmK, T.tmV, T.tmQ64, T.tmDO64, T.tc_kv_n,                          \
-              BwdSmem<DKV>::bytes(tb.nX + 2 + 2 * T.tc_kv_n));                                                \
-    tb.x_off = T.tc_q_off;                                                                                    \
-    tb.y_code = T.tc_q_code;                                                                                  \
-    tb.nX = (L.Rq + 127) / 128;                                                                               \
-    tb.out0 = dQ;                                                                                             \
-    tb.out1 = nullptr;                                                                                        \
-    tb.out1_16 = nullptr;                                                                                     \
-    launch_tc(k_attn_bwd_tc<DKV, true>, T.tmQ, T.tmDO128, T.tmK64, T.tmV64, T.tc_q_n,                         \
-              BwdSmem<DKV>::bytes(tb.nX + 2 + 2 * T.tc_q_n));                                                 \
-    break;                                                                                                    \
-  }
-      switch (dk) {
-        SORT_BWD_TC(16)
-        SORT_BWD_TC(32)
-        SORT_BWD_TC(64)
-        default: throw ConfigError("training: unsupported head dim");
-      }
-#undef SORT_BWD_TC
-      h.launches += 2;
+      attn_core_backward_tc(h, L, T, B, Dd, dQ, dK, dV,
+                            reinterpret_cast<__nv_bfloat16*>(h.tw[12]) + 2 * static_cast<size_t>(h.train_B) * h.L0 * d);
     } else if (h.attn_bwd_mma) {
       AttnBwdMmaArgs am;
       am.q = T.q;
@@ -1857,7 +1876,17 @@ static void backward_device(Handle& h, int B, const float* dz) {
     k_colsum<<<dim3((d + 31) / 32, std::min(148, (n + 255) / 256)), dim3(32, 8), 0, h.stream>>>(
         dproj, n, d, grad_ptr(h, std::string("tok.b_") + gname[g]));
     if (g == 1) continue;  // candidates gather only the frozen item table
-    gemm_rm(h, false, true, n, K, d, dproj, d, w32(h, W), d, dcat, K);
+    // d(concat) = dproj W^T with W zero-padded to Kp rows, so N = Kp is a multiple of 32 and the
+    // product runs on the TF32 tcgen05 GEMM (N = 56 would fall back to the SIMT kernel)
+    const int Kp = (K + 31) & ~31;
+    const size_t wp_n = static_cast<size_t>(Kp) * d;
+    if (wp_n > h.wpad_cap) {
+      h.wpad = h.dalloc<float>(wp_n);
+      h.wpad_cap = wp_n;
+    }
+    CK(cudaMemsetAsync(h.wpad, 0, wp_n * 4, h.stream));
+    CK(cudaMemcpyAsync(h.wpad, w32(h, W), static_cast<size_t>(K) * d * 4, cudaMemcpyDeviceToDevice, h.stream));
+    gemm_rm(h, false, true, n, Kp, d, dproj, d, h.wpad, d, dcat, Kp);
     TokTableGrads tg{};
     int tsize = 0;
     if (g == 0) {
@@ -1881,7 +1910,7 @@ static void backward_device(Handle& h, int B, const float* dz) {
     if (tsize * 4 > 48 * 1024)
       CK(cudaFuncSetAttribute(k_tok_table_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, tsize * 4));
     k_tok_table_scatter<<<std::min(148 * 2, (n + 7) / 8), 256, tsize * 4, h.stream>>>(
-        dcat, g == 0 ? 0 : 1, n, K, h.in_action, h.in_scene, h.hist_time, h.in_prof, c.n_profile_fields, c.item_dim,
+        dcat, g == 0 ? 0 : 1, n, Kp, h.in_action, h.in_scene, h.hist_time, h.in_prof, c.n_profile_fields, c.item_dim,
         c.action_dim, c.scene_dim, c.time_dim, c.n_actions, c.n_scenes, c.n_time_buckets, pvd, c.profile_dim, tg);
   }
   if (c.special_tokens)
@@ -2993,3 +3022,5 @@ int sort_stage_times(SortHandle p, float* ms, int32_t cap, int32_t* n, char* nam
 }
 
 }  // extern "C"
+
+#include "layer_op.cuh"  // operator-level entries (rmsnorm / rope / attention layer)

@@ -940,6 +940,7 @@ struct TokTableGrads {
   float* time;    // [n_tb, time_dim]
   float* prof[SORT_MAX_PROFILE_FIELDS];  // per field [vocab_f, prof_dim]
 };
+// K: the row stride of dcat (>= the concat width)
 __global__ void __launch_bounds__(256) k_tok_table_scatter(const float* __restrict__ dcat, int group, int n, int K,
                                                            const int32_t* __restrict__ hist_action,
                                                            const int32_t* __restrict__ hist_scene,

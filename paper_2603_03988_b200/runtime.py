@@ -64,6 +64,7 @@ EXPORTS = [
     "sort_moe_forward", "sort_pretrain_forward", "sort_forward_async",
     "sort_nccl_unique_id", "sort_exchange_create_nccl", "sort_exchange_create_host",
     "sort_exchange_destroy", "sort_exchange_lookup", "sort_exchange_allreduce_f32", "sort_op_gemm",
+    "sort_op_rmsnorm", "sort_op_rmsnorm_backward", "sort_op_rope", "sort_op_attention_layer",
 ]
 
 _lib = None
@@ -136,6 +137,12 @@ def lib():
                                            C.c_void_p, C.c_void_p]
         L.sort_exchange_allreduce_f32.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
         L.sort_op_gemm.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, f32p, f32p, f32p]
+        L.sort_op_rmsnorm.argtypes = [C.c_int32, C.c_int32, f32p, f32p, f32p, f32p]
+        L.sort_op_rmsnorm_backward.argtypes = [C.c_int32, C.c_int32, f32p, f32p, f32p, f32p, f32p, f32p]
+        L.sort_op_rope.argtypes = [C.c_int32, C.c_int32, f32p, i32p, C.c_double, C.c_int32, f32p]
+        L.sort_op_attention_layer.argtypes = [C.c_int32, C.c_int32, C.c_double, C.c_int32, C.c_int32, C.c_int32,
+                                              C.c_int32, f32p, i32p, i32p, i32p, i32p, i32p,
+                                              C.POINTER(f32p), f32p, f32p, f32p, C.POINTER(f32p)]
         _lib = L
     return _lib
 

@@ -1,0 +1,18 @@
+#!/usr/bin/env bash
+# Round-2 state check on one B200: GPU tests, smoke, every bench mode, the reference arm,
+# launch lists of the forward and training steps.
+set -u
+O=gpurun_out/r02a
+mkdir -p $O
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/gpu_tests.txt 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1
+timeout 600 python bench.py > $O/bench_forward.json 2>$O/bench_forward.err
+for m in train embed large moe pretrain; do
+  timeout 600 python bench.py --mode $m --no-cpu-baseline > $O/bench_$m.json 2>$O/bench_$m.err
+done
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_reference.json 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file $O/fwd_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/train_launches.csv python bench.py --mode train --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv --log-file $O/large_launches.csv python bench.py --mode large --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+tail -3 $O/gpu_tests.txt; cat $O/smoke.txt | tail -2
+for f in $O/bench_*.json; do tail -1 $f | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d.get('impl','ours'), d['metric'][:40], d.get('value'), d.get('ms_per_step'), d.get('roofline',{}).get('frac'), d.get('clocks',{}).get('sm_mhz'))" 2>&1; done
