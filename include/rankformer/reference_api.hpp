@@ -22,6 +22,7 @@
 //     ::backward(dout, cache, grads, index)  (attention.hpp:58-63)     (tcgen05 attention backward)
 //   TokenizerCache / Tokenizer::tokenize_sample(sample, cache)         GPU: k_tokenize (sort_tokenize)
 //     (tokenizer.hpp:60-84)
+//   transfer_item_table(from, to, freeze) (tokenizer.hpp:107)          sort_transfer_item_table
 //
 // Numbers: the reference computes in fp64; here the ops run on the device in fp32 (row ops) or
 // bf16 operands with fp32 accumulation (attention), so results agree within the tolerances the
@@ -386,6 +387,8 @@ class Tokenizer {
  public:
   explicit Tokenizer(gpu::Model& model) : m_(&model) {}
 
+  gpu::Model& model() const { return *m_; }
+
   TokenSequence tokenize_sample(const RequestSample& sample, TokenizerCache& cache) const {
     TokenSequence t = m_->tokenize_sample(sample);
     cache = TokenizerCache{};
@@ -418,5 +421,11 @@ class Tokenizer {
  private:
   gpu::Model* m_;
 };
+
+// tokenizer.cpp:376-383: copy the item table between tokenizers with identical item
+// vocabularies and set the destination's frozen flag (sort_transfer_item_table).
+inline void transfer_item_table(const Tokenizer& from, Tokenizer& to, bool freeze) {
+  gpu::check(sort_transfer_item_table(from.model().handle(), to.model().handle(), freeze ? 1 : 0));
+}
 
 }  // namespace rankformer

@@ -230,12 +230,25 @@ int sort_train_step(SortHandle h, const SortBatch* batch, const float* dlogits, 
  * SPEC.md:416); dL/dlogits never leaves the GPU. *loss receives L. */
 int sort_train_step_bce(SortHandle h, const SortBatch* batch, const float* labels,
                         const float* obj_weights, float* loss);
-/* adamw_step over every trainable parameter (the item table is frozen), then
- * the bf16 inference weights are rebuilt from the fp32 masters on the device. Status 2 names
- * the parameter on a non-finite gradient. */
+/* adamw_step over every parameter not frozen (sort_set_frozen), then the bf16
+ * inference weights are rebuilt from the fp32 masters on the device. Status 2 names the
+ * parameter on a non-finite gradient. */
 int sort_adamw_step(SortHandle h, float lr, float beta1, float beta2, float eps, float weight_decay);
-/* Current fp32 master value of a trainable parameter (host copy, reference shape). */
+/* Current fp32 master value of a trainable parameter (host copy, reference shape); for
+ * "tok.item_table" the fp32 master when it is trained, else the device's bf16 table widened. */
 int sort_get_param(SortHandle h, const char* name, float* out);
+/* Gradient of one parameter from the last training step (host copy, reference shape),
+ * "tok.item_table" included when it is not frozen. */
+int sort_get_grad(SortHandle h, const char* name, float* out);
+/* Parameter::frozen (params.hpp:15-25; tokenizer.cpp:289-346): a frozen parameter receives zero
+ * gradient and no optimizer update (bytes unchanged). Every parameter starts
+ * trainable except "tok.item_table", which starts frozen (SORT's transfer + freeze setting);
+ * unfreezing it allocates its fp32 master (from the bf16 device table), gradient and moments. */
+int sort_set_frozen(SortHandle h, const char* name, int32_t frozen);
+/* transfer_item_table (tokenizer.cpp:376-383; transfer_sparse): copies the item
+ * table of `from` (e.g. a pre-training handle) into `to` (same n_items / item_dim) and sets its
+ * frozen flag. */
+int sort_transfer_item_table(SortHandle from, SortHandle to, int32_t freeze);
 /* Offset / shape of one parameter's gradient in the flat buffer, and its total length. */
 int sort_grad_info(SortHandle h, const char* name, int64_t* offset, int64_t* rows, int64_t* cols,
                    int64_t* total);

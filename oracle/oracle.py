@@ -305,6 +305,9 @@ class OracleModel:
             _check(lib().oracle_model_set_param(self.h, name.encode(), _p(a64, f64p),
                                                 a64.shape[0], a64.shape[1]))
 
+    def set_item_trainable(self, trainable: bool = True) -> None:
+        _check(lib().oracle_model_set_item_trainable(self.h, int(trainable)))
+
     def __del__(self):
         if getattr(self, "h", None) and _lib is not None:
             _lib.oracle_model_destroy(self.h)

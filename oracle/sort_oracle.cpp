@@ -353,6 +353,7 @@ struct OrModel {
   OrModelCfg cfg;
   int d = 0, dk = 0, m = 0, dh = 0;
   std::map<std::string, M> p;
+  bool item_trainable = false;  // Parameter::frozen of the item table (params.hpp:18), inverted
 
   const M& P(const std::string& name) const {
     auto it = p.find(name);
@@ -979,8 +980,9 @@ M attention_backward(const OrModel& mdl, int layer, const M& xn, const std::vect
 // Tokenizer::backward (tokenizer.cpp:286-352) for one request: per group
 // dproj = rmsnorm_backward(dtokens[group rows]) -> dW = concat^T dproj, db = colsum(dproj),
 // d(concat) = dproj W^T scattered into the feature tables; special rows take dtokens raw.
-// The item table is treated as frozen (SPEC.md transfer+freeze; tokenizer.cpp:315-317,
-// 346-352 skip frozen tables), so no item-table gradient is produced.
+// The item table is frozen by default (SPEC.md transfer+freeze; tokenizer.cpp:315-317,
+// 346-352 skip frozen tables); with item_trainable its rows take the item columns of d(concat)
+// of the history and candidate groups.
 void tokenizer_backward(const OrModel& mdl, const OrSample& s, const M& dtok, Grads& G) {
   const OrModelCfg& c = mdl.cfg;
   const bool st = c.special_tokens != 0;
@@ -1024,6 +1026,10 @@ void tokenizer_backward(const OrModel& mdl, const OrSample& s, const M& dtok, Gr
     M& gt = grad_of(G, mdl, "tok.time_table");
     for (int i = 0; i < nh; ++i) {
       const int tb = time_bucket(s.timestamp - s.hist_ts[i], c.n_time_buckets);
+      if (mdl.item_trainable) {  // tokenizer.cpp:315-317
+        M& gi = grad_of(G, mdl, "tok.item_table");
+        for (int j = 0; j < c.item_dim; ++j) gi(s.hist_item[i], j) += dc(i, j);
+      }
       for (int j = 0; j < c.action_dim; ++j) ga(s.hist_action[i], j) += dc(i, c.item_dim + j);
       for (int j = 0; j < c.scene_dim; ++j) gsn(s.hist_scene[i], j) += dc(i, c.item_dim + c.action_dim + j);
       for (int j = 0; j < c.time_dim; ++j) gt(tb, j) += dc(i, c.item_dim + c.action_dim + c.scene_dim + j);
@@ -1042,7 +1048,12 @@ void tokenizer_backward(const OrModel& mdl, const OrSample& s, const M& dtok, Gr
   }
   M ccat(nc, c.item_dim);
   for (int j = 0; j < nc; ++j) std::memcpy(ccat.row(j), it.row(s.cand_item[j]), sizeof(double) * c.item_dim);
-  group(ccat, (st ? 3 : 0) + nh + np, "tok.w_cand", "tok.b_cand", "tok.g_cand");
+  M dcc = group(ccat, (st ? 3 : 0) + nh + np, "tok.w_cand", "tok.b_cand", "tok.g_cand");
+  if (mdl.item_trainable) {  // tokenizer.cpp:346-352
+    M& gi = grad_of(G, mdl, "tok.item_table");
+    for (int j = 0; j < nc; ++j)
+      for (int k = 0; k < c.item_dim; ++k) gi(s.cand_item[j], k) += dcc(j, k);
+  }
 }
 
 // Backward of model_forward for one request given dL/dlogits [n_cand, 3]; returns dtokens.
@@ -1378,6 +1389,12 @@ int oracle_model_create(const OrModelCfg* cfg, OrModel** out) {
 }
 
 void oracle_model_destroy(OrModel* m) { delete m; }
+
+int oracle_model_set_item_trainable(OrModel* m, int trainable) {
+  if (!m) return 1;
+  m->item_trainable = trainable != 0;
+  return 0;
+}
 
 int oracle_model_set_param(OrModel* m, const char* name, const double* data, int rows, int cols) {
   return guarded([&] {

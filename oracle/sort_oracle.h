@@ -117,6 +117,9 @@ void oracle_model_destroy(OrModel* m);
  * plus spec-named block.<l>.attn_norm / block.<l>.ffn_norm / ffn.<l>.w_gate|w_up|w_down /
  * final_norm.gain / head.w1|b1|w2|b2. Row-major [rows, cols]. */
 int oracle_model_set_param(OrModel* m, const char* name, const double* data, int rows, int cols);
+/* Parameter::frozen of the item table (params.hpp:18): trainable = 1 makes the backward produce
+ * the "tok.item_table" gradient (tokenizer.cpp:315-317, 346-352). Default: frozen. */
+int oracle_model_set_item_trainable(OrModel* m, int trainable);
 
 /* Tokenize one request (Tokenizer::tokenize_sample, tokenizer.cpp:144-238). */
 int oracle_tokenize(const OrModel* m, const OrSample* s, double* tokens /* L*d */,

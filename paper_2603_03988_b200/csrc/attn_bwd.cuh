@@ -237,6 +237,19 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
         const int2 code = s_code[j];
         const int c0 = code.x * 64 + hf * 32;  // first Y row (column of S) of this warp's half
         const uint32_t cls = (static_cast<uint32_t>(code.y) >> (2 * (2 * quarter + hf))) & 3u;
+        // kDQ = false: the half's 32 columns are query rows; lane i fetches column c0 + i's lse, D
+        // (and mask row for a mixed chunk) BEFORE the wait, so the loads overlap the MMAs; the
+        // column loop broadcasts them with shuffles. Out-of-range columns: lse = +inf -> P = 0.
+        float lse_l = __int_as_float(0x7f800000), D_l = 0.f;
+        int4 m_l = make_int4(0, -1, -1, 0);
+        if constexpr (!kDQ) {
+          const int c = c0 + lane;
+          if (cls != 2u && c < a.Rq) {
+            lse_l = __ldg(lse_bh + c);
+            D_l = __ldg(D_bh + c);
+            if (cls != 1u) m_l = __ldg(a.rowmeta + c);
+          }
+        }
         mbar_wait(s_full, g & 1);
         tc_fence_after();
         uint32_t sv[32], pv[32];
@@ -267,14 +280,13 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
             float pp[2], dd[2];
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-              const int c = c0 + i + e;
-              const bool in = c < a.Rq;
-              const float l = in ? __ldg(lse_bh + c) : 0.f;
-              const float dq = in ? __ldg(D_bh + c) : 0.f;
+              const float l = __shfl_sync(0xffffffffu, lse_l, i + e);
+              const float dq = __shfl_sync(0xffffffffu, D_l, i + e);
               float p = ex2_approx(fmaf(__uint_as_float(sv[i + e]), sl2, -l));
               if (cls != 1u) {
-                const int4 m = in ? __ldg(a.rowmeta + c) : make_int4(0, -1, -1, 0);
-                const bool vis = (x >= m.x && x <= m.y) || x == m.z;
+                const int mx = __shfl_sync(0xffffffffu, m_l.x, i + e), my = __shfl_sync(0xffffffffu, m_l.y, i + e),
+                          mz = __shfl_sync(0xffffffffu, m_l.z, i + e);
+                const bool vis = (x >= mx && x <= my) || x == mz;
                 p = vis ? p : 0.f;
               }
               pp[e] = p;

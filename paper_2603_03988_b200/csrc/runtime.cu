@@ -4,11 +4,13 @@
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <map>
 #include <memory>
 #include <mutex>
+#include <set>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -150,6 +152,11 @@ struct Handle {
   __nv_bfloat16* dO16 = nullptr;  // bf16 copy of dL/d(attention output) for the tensor-core backward
   float* dtokens = nullptr;
   float* wpad = nullptr;  // tokenizer backward: zero-padded projection weight
+  // Parameter::frozen (params.hpp:15-25): frozen tensors get no gradient and no optimizer
+  // update. The item table starts frozen (SORT's transfer + freeze setting);
+  // unfreezing it allocates an fp32 master / gradient / AdamW moments for it.
+  std::set<std::string> frozen{"tok.item_table"};
+  float *item_master = nullptr, *item_grad = nullptr, *item_m = nullptr, *item_v = nullptr;
   size_t wpad_cap = 0;
   float* dz_dev = nullptr;                 // dL/dlogits of the current step
   int32_t* t_rows = nullptr;               // tokenizer backward: token row of each group row
@@ -1541,7 +1548,9 @@ static void ensure_train_buffers(Handle& h, int B) {
   h.tw[12] = h.dalloc<float>(rows * 2 * m * 2);  // GU and dGU
   h.tw[13] = h.dalloc<float>(rows * m);
   h.tw[14] = h.dalloc<float>(rows * 2);
-  h.tw[15] = h.dalloc<float>(std::max(rows * h.H, static_cast<size_t>(B) * h.cfg.n_cand * (h.dh * 4 + 3)));
+  // head scratch: hid, dhid [BN, dh], the 32-column padded dz [BN, 32] and dW2 [dh, 32]
+  h.tw[15] = h.dalloc<float>(std::max(rows * h.H, static_cast<size_t>(B) * h.cfg.n_cand * (h.dh * 2 + 32) +
+                                                      static_cast<size_t>(h.dh) * 32));
   h.train_B = h.Bmax;
 }
 
@@ -1625,6 +1634,9 @@ static void backward_device(Handle& h, int B, const float* dz) {
   const SortConfig& c = h.cfg;
   const int d = h.d, m = h.m, H = h.H, dk = h.dk, N = c.n_cand, dh = h.dh;
   CK(cudaMemsetAsync(h.grads, 0, h.grad_count * sizeof(float), h.stream));
+  const bool item_train = !h.frozen.count("tok.item_table");
+  const size_t n_item_el = static_cast<size_t>(c.n_items) * c.item_dim;
+  if (item_train) CK(cudaMemsetAsync(h.item_grad, 0, n_item_el * sizeof(float), h.stream));
   float* dX = h.tw[0];
   float* dXn = h.tw[1];
   float* inv = h.tw[14];
@@ -1645,7 +1657,15 @@ static void backward_device(Handle& h, int B, const float* dz) {
   check_launch("head rows");
   gemm_rm(h, false, false, BN, dh, d, xh, d, w32(h, "head.w1"), dh, hid, dh);
   k_bias_relu<<<ew_grid(static_cast<size_t>(BN) * dh), 256, 0, h.stream>>>(hid, w32(h, "head.b1"), BN, dh);
-  gemm_rm(h, true, false, dh, 3, BN, hid, dh, dz, 3, grad_ptr(h, "head.w2"), 3);
+  {  // dW2 = hid^T dz: N = 3 would leave the SIMT kernel 8 CTAs over K = B*N rows; dz is
+     // zero-padded to 32 columns so the TF32 tcgen05 GEMM splits K over the SMs
+    float* dz32 = hid + 2 * static_cast<size_t>(BN) * dh;
+    float* gw2 = dz32 + static_cast<size_t>(BN) * 32;
+    CK(cudaMemsetAsync(dz32, 0, static_cast<size_t>(BN) * 32 * 4, h.stream));
+    CK(cudaMemcpy2DAsync(dz32, 32 * 4, dz, 3 * 4, 3 * 4, BN, cudaMemcpyDeviceToDevice, h.stream));
+    gemm_rm(h, true, false, dh, 32, BN, hid, dh, dz32, 32, gw2, 32);
+    CK(cudaMemcpy2DAsync(grad_ptr(h, "head.w2"), 3 * 4, gw2, 32 * 4, 3 * 4, dh, cudaMemcpyDeviceToDevice, h.stream));
+  }
   k_colsum<<<dim3(1, 64), dim3(32, 8), 0, h.stream>>>(dz, BN, 3, grad_ptr(h, "head.b2"));
   gemm_rm(h, false, true, BN, dh, 3, dz, 3, w32(h, "head.w2"), 3, dhid, dh);
   k_relu_mask<<<ew_grid(static_cast<size_t>(BN) * dh), 256, 0, h.stream>>>(dhid, hid, static_cast<size_t>(BN) * dh);
@@ -1875,7 +1895,7 @@ static void backward_device(Handle& h, int B, const float* dz) {
     gemm_rm(h, true, false, K, d, n, catf, K, dproj, d, grad_ptr(h, W), d);
     k_colsum<<<dim3((d + 31) / 32, std::min(148, (n + 255) / 256)), dim3(32, 8), 0, h.stream>>>(
         dproj, n, d, grad_ptr(h, std::string("tok.b_") + gname[g]));
-    if (g == 1) continue;  // candidates gather only the frozen item table
+    if (g == 1 && !item_train) continue;  // the candidate concat is the item row only
     // d(concat) = dproj W^T with W zero-padded to Kp rows, so N = Kp is a multiple of 32 and the
     // product runs on the TF32 tcgen05 GEMM (N = 56 would fall back to the SIMT kernel)
     const int Kp = (K + 31) & ~31;
@@ -1887,6 +1907,10 @@ static void backward_device(Handle& h, int B, const float* dz) {
     CK(cudaMemsetAsync(h.wpad, 0, wp_n * 4, h.stream));
     CK(cudaMemcpyAsync(h.wpad, w32(h, W), static_cast<size_t>(K) * d * 4, cudaMemcpyDeviceToDevice, h.stream));
     gemm_rm(h, false, true, n, Kp, d, dproj, d, h.wpad, d, dcat, Kp);
+    if (item_train && g != 2)  // tokenizer.cpp:315-317, 346-352: the item columns of d(concat)
+      k_item_grad_scatter<<<std::min(148 * 4, (n + 7) / 8), 256, 0, h.stream>>>(
+          dcat, Kp, n, g == 0 ? tp.hist_item : tp.cand_item, c.n_items, c.item_dim, h.item_grad);
+    if (g == 1) continue;
     TokTableGrads tg{};
     int tsize = 0;
     if (g == 0) {
@@ -1917,6 +1941,12 @@ static void backward_device(Handle& h, int B, const float* dz) {
     k_special_grad<<<(3 * d + 255) / 256, 256, 0, h.stream>>>(dX, B, h.L0, c.n_hist, c.n_profile_fields, d,
                                                               grad_ptr(h, "tok.special"));
   check_launch("tokenizer backward");
+  for (const std::string& name : h.frozen) {  // frozen tensors receive zero gradient
+    auto it = h.grad_index.find(name);
+    if (it == h.grad_index.end()) continue;
+    const size_t n = static_cast<size_t>(it->second.second.first) * it->second.second.second;
+    CK(cudaMemsetAsync(h.grads + it->second.first, 0, n * sizeof(float), h.stream));
+  }
 }
 
 
@@ -2762,7 +2792,7 @@ int sort_train_step_bce(SortHandle p, const SortBatch* batch, const float* label
     const float w0 = obj_weights ? obj_weights[0] : 1.f, w1 = obj_weights ? obj_weights[1] : 0.5f,
                 w2 = obj_weights ? obj_weights[2] : 0.5f;  // SPEC.md:416 defaults
     float* dloss = dzb + static_cast<size_t>(h->Bmax) * h->cfg.n_cand * 3;
-    k_bce<<<1, 256, 0, h->stream>>>(h->logits, lab, n, w0, w1, w2, dzb, dloss);
+    k_bce<<<1, 1024, 0, h->stream>>>(h->logits, lab, n, w0, w1, w2, dzb, dloss);
     check_launch("bce");
     float hl = 0.f;
     CK(cudaMemcpyAsync(&hl, dloss, 4, cudaMemcpyDeviceToHost, h->stream));
@@ -2792,15 +2822,44 @@ int sort_adamw_step(SortHandle p, float lr, float beta1, float beta2, float eps,
     if (!bad) throw ConfigError("no gradients yet (call sort_train_step)");
     const unsigned long long none = ~0ull;
     CK(cudaMemcpyAsync(bad, &none, 8, cudaMemcpyHostToDevice, h->stream));
-    k_adamw<<<static_cast<int>(std::min<size_t>((h->grad_count + 255) / 256, 148 * 32)), 256, 0, h->stream>>>(
-        h->master, h->grads, h->adam_m, h->adam_v, h->grad_count, lr, beta1, beta2, eps, weight_decay, bc1, bc2, bad);
+    // one launch per run of trainable tensors (frozen ones are skipped: no update, no decay)
+    std::vector<std::pair<size_t, size_t>> runs;  // [begin, end) in the flat buffer
+    {
+      std::vector<std::pair<size_t, size_t>> fz;
+      for (const std::string& name : h->frozen) {
+        auto it = h->grad_index.find(name);
+        if (it != h->grad_index.end())
+          fz.emplace_back(it->second.first,
+                          it->second.first + static_cast<size_t>(it->second.second.first) * it->second.second.second);
+      }
+      std::sort(fz.begin(), fz.end());
+      size_t at = 0;
+      for (const auto& f : fz) {
+        if (f.first > at) runs.emplace_back(at, f.first);
+        at = std::max(at, f.second);
+      }
+      if (at < h->grad_count) runs.emplace_back(at, h->grad_count);
+    }
+    auto adam = [&](float* p, float* g, float* m, float* v, size_t n, size_t base) {
+      k_adamw<<<static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 32)), 256, 0, h->stream>>>(
+          p, g, m, v, n, lr, beta1, beta2, eps, weight_decay, bc1, bc2, bad, base);
+    };
+    for (const auto& r : runs)
+      adam(h->master + r.first, h->grads + r.first, h->adam_m + r.first, h->adam_v + r.first, r.second - r.first,
+           r.first);
+    const size_t n_item = static_cast<size_t>(h->cfg.n_items) * h->cfg.item_dim;
+    if (!h->frozen.count("tok.item_table")) {
+      adam(h->item_master, h->item_grad, h->item_m, h->item_v, n_item, h->grad_count);
+      k_cast_bf16<<<static_cast<int>(std::min<size_t>((n_item + 255) / 256, 148 * 32)), 256, 0, h->stream>>>(
+          h->item_master, n_item, h->item);
+    }
     check_launch("adamw");
     unsigned long long hb = 0;
     CK(cudaMemcpyAsync(&hb, bad, 8, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
     if (hb != none) {
       const size_t idx = static_cast<size_t>(hb - 1);
-      std::string name = "?";
+      std::string name = idx >= h->grad_count ? "tok.item_table" : "?";
       for (auto& kv : h->grad_index)
         if (idx >= kv.second.first &&
             idx < kv.second.first + static_cast<size_t>(kv.second.second.first) * kv.second.second.second)
@@ -2815,11 +2874,112 @@ int sort_get_param(SortHandle p, const char* name, float* out) {
   return api([&] {
     Handle* h = ready(p);
     if (!name || !out) throw ConfigError("null argument");
+    if (std::strcmp(name, "tok.item_table") == 0) {  // fp32 master when trained, else the bf16 table widened
+      const size_t n = static_cast<size_t>(h->cfg.n_items) * h->cfg.item_dim;
+      if (h->item_master) {
+        CK(cudaMemcpyAsync(out, h->item_master, n * 4, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        return;
+      }
+      std::vector<__nv_bfloat16> b(n);
+      CK(cudaMemcpyAsync(b.data(), h->item, n * 2, cudaMemcpyDeviceToHost, h->stream));
+      CK(cudaStreamSynchronize(h->stream));
+      for (size_t i = 0; i < n; ++i) out[i] = __bfloat162float(b[i]);
+      return;
+    }
     auto it = h->grad_index.find(name);
     if (it == h->grad_index.end()) throw ConfigError(std::string("no trainable parameter ") + name);
     const size_t n = static_cast<size_t>(it->second.second.first) * it->second.second.second;
     CK(cudaMemcpyAsync(out, h->master + it->second.first, n * 4, cudaMemcpyDeviceToHost, h->stream));
     CK(cudaStreamSynchronize(h->stream));
+  });
+}
+
+int sort_get_grad(SortHandle p, const char* name, float* out) {
+  return api([&] {
+    Handle* h = ready(p);
+    if (!name || !out) throw ConfigError("null argument");
+    if (!h->grads) throw ConfigError("no gradients yet (call sort_train_step)");
+    if (std::strcmp(name, "tok.item_table") == 0) {
+      if (h->frozen.count(name) || !h->item_grad) throw ConfigError("tok.item_table is frozen: no gradient");
+      const size_t n = static_cast<size_t>(h->cfg.n_items) * h->cfg.item_dim;
+      CK(cudaMemcpyAsync(out, h->item_grad, n * 4, cudaMemcpyDeviceToHost, h->stream));
+    } else {
+      auto it = h->grad_index.find(name);
+      if (it == h->grad_index.end()) throw ConfigError(std::string("no trainable parameter ") + name);
+      const size_t n = static_cast<size_t>(it->second.second.first) * it->second.second.second;
+      CK(cudaMemcpyAsync(out, h->grads + it->second.first, n * 4, cudaMemcpyDeviceToHost, h->stream));
+    }
+    CK(cudaStreamSynchronize(h->stream));
+  });
+}
+
+static void unfreeze_item_table(Handle& h) {
+  if (h.item_master) return;
+  if (h.cfg.pretrain) throw ConfigError("item-table training: use the ranking model");
+  const size_t n = static_cast<size_t>(h.cfg.n_items) * h.cfg.item_dim;
+  h.item_master = h.dalloc<float>(n);
+  h.item_grad = h.dalloc<float>(n);
+  h.item_m = h.dalloc<float>(n);
+  h.item_v = h.dalloc<float>(n);
+  k_bf16_to_f32<<<ew_grid(n), 256, 0, h.stream>>>(h.item, n, h.item_master);  // master from the device table
+  CK(cudaMemsetAsync(h.item_m, 0, n * 4, h.stream));
+  CK(cudaMemsetAsync(h.item_v, 0, n * 4, h.stream));
+  check_launch("item table master");
+}
+
+int sort_set_frozen(SortHandle p, const char* name, int32_t frozen) {
+  return api([&] {
+    Handle* h = ready(p);
+    if (!name) throw ConfigError("null argument");
+    const std::string n(name);
+    if (n != "tok.item_table" && !h->grad_index.count(n)) throw ConfigError("no parameter " + n);
+    if (frozen) {
+      h->frozen.insert(n);
+      return;
+    }
+    if (n == "tok.item_table") {
+      if (h->item_ext) throw ConfigError("the row-sharded item table (sort_set_item_table) is not trained here");
+      unfreeze_item_table(*h);
+    }
+    h->frozen.erase(n);
+  });
+}
+
+int sort_transfer_item_table(SortHandle from, SortHandle to, int32_t freeze) {
+  return api([&] {
+    Handle* a = ready(from);
+    Handle* b = ready(to);
+    if (a->cfg.n_items != b->cfg.n_items || a->cfg.item_dim != b->cfg.item_dim)
+      throw ConfigError("transfer_item_table: item vocabularies differ");
+    const size_t n = static_cast<size_t>(a->cfg.n_items) * a->cfg.item_dim;
+    std::vector<float> t(n);
+    CK(cudaSetDevice(a->device));
+    if (a->item_master) {
+      CK(cudaMemcpyAsync(t.data(), a->item_master, n * 4, cudaMemcpyDeviceToHost, a->stream));
+      CK(cudaStreamSynchronize(a->stream));
+    } else {
+      std::vector<__nv_bfloat16> hb(n);
+      CK(cudaMemcpyAsync(hb.data(), a->item, n * 2, cudaMemcpyDeviceToHost, a->stream));
+      CK(cudaStreamSynchronize(a->stream));
+      for (size_t i = 0; i < n; ++i) t[i] = __bfloat162float(hb[i]);
+    }
+    CK(cudaSetDevice(b->device));
+    const std::vector<__nv_bfloat16> tb = to_bf16(t);
+    CK(cudaMemcpyAsync(b->item, tb.data(), n * 2, cudaMemcpyHostToDevice, b->stream));
+    if (b->item_master) {
+      CK(cudaMemcpyAsync(b->item_master, t.data(), n * 4, cudaMemcpyHostToDevice, b->stream));
+      CK(cudaMemsetAsync(b->item_m, 0, n * 4, b->stream));
+      CK(cudaMemsetAsync(b->item_v, 0, n * 4, b->stream));
+    }
+    CK(cudaStreamSynchronize(b->stream));
+    b->drop_graphs();
+    if (freeze) {
+      b->frozen.insert("tok.item_table");
+    } else {
+      unfreeze_item_table(*b);
+      b->frozen.erase("tok.item_table");
+    }
   });
 }
 

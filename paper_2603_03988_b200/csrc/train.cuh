@@ -1019,12 +1019,12 @@ __global__ void k_bias_add(float* __restrict__ x, const float* __restrict__ b, i
 // Non-finite gradients set *bad to (index + 1) of the first one seen (host names it).
 __global__ void k_adamw(float* __restrict__ p, const float* __restrict__ g, float* __restrict__ m,
                         float* __restrict__ v, size_t n, float lr, float b1, float b2, float eps, float wd,
-                        float bc1, float bc2, unsigned long long* bad) {
+                        float bc1, float bc2, unsigned long long* bad, size_t base) {
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
     const float gi = g[i];
     if (!isfinite(gi)) {
-      atomicMin(bad, static_cast<unsigned long long>(i) + 1ull);
+      atomicMin(bad, static_cast<unsigned long long>(base + i) + 1ull);
       continue;
     }
     const float mi = b1 * m[i] + (1.f - b1) * gi;
@@ -1036,11 +1036,25 @@ __global__ void k_adamw(float* __restrict__ p, const float* __restrict__ g, floa
   }
 }
 
+// Item-table gradient (tokenizer.cpp:315-317, 346-352) when the table is not frozen: row r of
+// d(concat) (row stride ld) adds its first item_dim columns into ditem[ids[r]]. Warp per row;
+// fp32 atomics (rows sharing an item add in arbitrary order: last-ulp nondeterminism).
+__global__ void k_item_grad_scatter(const float* __restrict__ dcat, int ld, int n, const int32_t* __restrict__ ids,
+                                    int n_items, int item_dim, float* __restrict__ ditem) {
+  const int lane = threadIdx.x & 31;
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += gridDim.x * (blockDim.x >> 5)) {
+    const int id = ids[r];
+    if (static_cast<unsigned>(id) >= static_cast<unsigned>(n_items)) continue;  // OOV is reported by the forward
+    for (int j = lane; j < item_dim; j += 32)
+      atomicAdd(ditem + static_cast<size_t>(id) * item_dim + j, dcat[static_cast<size_t>(r) * ld + j]);
+  }
+}
+
 // Ranking loss: L = sum_obj w_obj * mean over candidates of BCE(p, y) with
-// eps-clamped logs; dL/dz = w_obj (p - y) / n. One block, fixed-order reduction.
-__global__ void k_bce(const float* __restrict__ logits, const float* __restrict__ labels, int n,
+// eps-clamped logs; dL/dz = w_obj (p - y) / n. One block of 1024 threads, fixed-order reduction.
+__global__ void __launch_bounds__(1024) k_bce(const float* __restrict__ logits, const float* __restrict__ labels, int n,
                       float w0, float w1, float w2, float* __restrict__ dz, float* __restrict__ loss) {
-  __shared__ float red[256];
+  __shared__ float red[1024];
   float acc = 0.f;
   const float w[3] = {w0, w1, w2};
   for (int i = threadIdx.x; i < n * 3; i += blockDim.x) {

@@ -65,6 +65,7 @@ EXPORTS = [
     "sort_nccl_unique_id", "sort_exchange_create_nccl", "sort_exchange_create_host",
     "sort_exchange_destroy", "sort_exchange_lookup", "sort_exchange_allreduce_f32", "sort_op_gemm",
     "sort_op_rmsnorm", "sort_op_rmsnorm_backward", "sort_op_rope", "sort_op_attention_layer",
+    "sort_get_grad", "sort_set_frozen", "sort_transfer_item_table",
 ]
 
 _lib = None
@@ -113,6 +114,9 @@ def lib():
         L.sort_train_step_bce.argtypes = [C.c_void_p, C.c_void_p, f32p, f32p, f32p]
         L.sort_adamw_step.argtypes = [C.c_void_p, C.c_float, C.c_float, C.c_float, C.c_float, C.c_float]
         L.sort_get_param.argtypes = [C.c_void_p, C.c_char_p, f32p]
+        L.sort_get_grad.argtypes = [C.c_void_p, C.c_char_p, f32p]
+        L.sort_set_frozen.argtypes = [C.c_void_p, C.c_char_p, C.c_int32]
+        L.sort_transfer_item_table.argtypes = [C.c_void_p, C.c_void_p, C.c_int32]
         L.sort_moe_routing.argtypes = [C.c_void_p, C.c_int, C.c_int32, i32p, i32p, f32p]
         L.sort_moe_load.argtypes = [C.c_void_p, C.c_int, i64p]
         L.sort_moe_update_bias.argtypes = [C.c_void_p, C.c_double]
@@ -384,11 +388,29 @@ class SortModel:
         masters, then the bf16 inference weights are rebuilt on the device."""
         _check(lib().sort_adamw_step(self.h, lr, beta1, beta2, eps, weight_decay))
 
+    def _shape(self, name: str):
+        if name == "tok.item_table":
+            return self.cfg.n_items, self.cfg.item_dim
+        return self.grad_layout(name)[1:3]
+
     def get_param(self, name: str) -> np.ndarray:
-        _, r, c, _ = self.grad_layout(name)
-        out = np.zeros((r, c), np.float32)
+        out = np.zeros(self._shape(name), np.float32)
         _check(lib().sort_get_param(self.h, name.encode(), _p(out, f32p)))
         return out
+
+    def get_grad(self, name: str) -> np.ndarray:
+        """Gradient of `name` from the last training step (tok.item_table when not frozen)."""
+        out = np.zeros(self._shape(name), np.float32)
+        _check(lib().sort_get_grad(self.h, name.encode(), _p(out, f32p)))
+        return out
+
+    def set_frozen(self, name: str, frozen: bool = True) -> None:
+        """Parameter::frozen (params.hpp:15-25): no gradient, no optimizer update."""
+        _check(lib().sort_set_frozen(self.h, name.encode(), int(frozen)))
+
+    def transfer_item_table(self, source: "SortModel", freeze: bool = True) -> None:
+        """transfer_item_table(source -> self, freeze) (tokenizer.cpp:376-383, SPEC.md:399-406)."""
+        _check(lib().sort_transfer_item_table(source.h, self.h, int(freeze)))
 
     def grad_layout(self, name: Optional[str] = None):
         off, r, c, tot = (C.c_int64(0) for _ in range(4))
