@@ -250,6 +250,62 @@ def run_train(args, cfg, rank, world, local, dist):
         dist.destroy_process_group()
 
 
+def run_pretrain_train(args, rank, world, local, dist):
+    """SURVEY 8(f) "next 4" training: pre-training step (sort_pretrain_train_step: forward of 64
+    click sequences x 1024 clicks, mean full-softmax next-item CE over a 65,536-item vocabulary,
+    backward of every parameter incl. the tied item table) + AdamW, per rank; gradients summed
+    over the ranks by the C++ exchange (NCCL) when N > 1."""
+    import torch
+    from paper_2603_03988_b200 import runtime as R
+    from paper_2603_03988_b200.config import pretrain_config
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = pretrain_config()
+    B = cfg.batch
+    model = R.SortModel(cfg, synth.make_params(cfg, seed=5), device=local, max_batch=B)
+    batch = synth.make_batch(cfg, B, seed=100 + rank)
+    gbuf = torch.zeros(model.grad_layout()[3], dtype=torch.float32, device=dev)
+    exchange = R.Exchange.nccl(rank, world, local) if dist else None
+    losses = []
+
+    def step():
+        losses.append(model.pretrain_train_step(batch))
+        if dist:  # dense gradients (the item-table gradient stays per rank in this build)
+            model.grads_to_device(gbuf.data_ptr())
+            exchange.allreduce(gbuf.data_ptr(), gbuf.numel())
+            model.grads_to_device(gbuf.data_ptr(), to_handle=True)
+        model.adamw_step(lr=2e-4)
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0])
+    if rank == 0:
+        print(json.dumps({
+            "metric": "next-item positions trained/sec (pre-training forward+backward+AdamW)",
+            "value": world * B * cfg.n_hist / (ms / 1e3), "unit": "positions/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16/fp32 (bf16 dL/dlogits)", "data": "synthetic",
+            "loss_first_last": [losses[0], losses[-1]],
+            "config": {"workload": f"pre-training step: {cfg.layers} layers, d={cfg.model_dim}, {cfg.heads} heads, "
+                                   f"m={cfg.ffn_dim}, {B} sequences/GPU x {cfg.n_hist} clicks, vocab {cfg.n_items}, "
+                                   "tied full-softmax CE, item table trained",
+                       "requests_per_gpu": B, "parallelism": f"dp{world}"},
+            "timing": "wall clock per synchronized step (host-driven), max over ranks",
+        }))
+    if dist:
+        dist.destroy_process_group()
+
+
 def run_embed(args, cfg, rank, world, local, dist):
     """BASELINE configs[4]: SORT-base scoring whose item table (--table-rows x item_dim bf16,
     6.4 GB at 100M rows) is row-sharded over the ranks. Per step and rank, inside the C++
@@ -454,7 +510,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="minimum length of the CPU-baseline sample (>= 32 requests)")
-    ap.add_argument("--mode", default="forward", choices=["forward", "train", "embed", "large", "moe", "pretrain"],
+    ap.add_argument("--mode", default="forward", choices=["forward", "train", "embed", "large", "moe", "pretrain", "pretrain_train"],
                     help="train: SORT-base training step (BASELINE configs[2]), global batch "
                          "--requests sharded over the ranks, gradient all-reduce over NCCL; "
                          "embed: BASELINE configs[4], 100M-row item table row-sharded over the "
@@ -506,6 +562,8 @@ def main():
     if args.mode == "train":
         run_train(args, cfg, rank, world, local, dist)
         return
+    if args.mode == "pretrain_train":
+        return run_pretrain_train(args, rank, world, local, dist)
     if args.mode == "embed":
         run_embed(args, cfg, rank, world, local, dist)
         return

@@ -230,6 +230,11 @@ int sort_train_step(SortHandle h, const SortBatch* batch, const float* dlogits, 
  * SPEC.md:416); dL/dlogits never leaves the GPU. *loss receives L. */
 int sort_train_step_bce(SortHandle h, const SortBatch* batch, const float* labels,
                         const float* obj_weights, float* loss);
+/* Pre-training step (cfg.pretrain = 1): forward of the click sequences, loss =
+ * mean over the B * n_hist predicted positions of the full-softmax next-item CE (*loss), and the
+ * backward of every parameter, the item table (tied head + input embedding) included unless
+ * frozen. Follow with sort_adamw_step. Needs n_items % 32 == 0. */
+int sort_pretrain_train_step(SortHandle h, const SortBatch* batch, float* loss);
 /* adamw_step over every parameter not frozen (sort_set_frozen), then the bf16
  * inference weights are rebuilt from the fp32 masters on the device. Status 2 names the
  * parameter on a non-finite gradient. */

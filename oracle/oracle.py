@@ -353,6 +353,17 @@ class OracleModel:
                                              _p(hp, f64p)))
         return lse, tgt, hp
 
+    def pretrain_backward(self, batch, b: int, scale: float, names):
+        """fp64 pre-training backward of sequence b: gradients of scale * sum_t CE_t for the
+        requested names (None if off the path) and sum_t CE_t."""
+        hold = _SampleHold(batch, b)
+        ce = C.c_double(0.0)
+        g = C.c_void_p()
+        lib().oracle_pretrain_backward.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.POINTER(C.c_double),
+                                                   C.POINTER(C.c_void_p)]
+        _check(lib().oracle_pretrain_backward(self.h, C.byref(hold.s), scale, C.byref(ce), C.byref(g)))
+        return self._grads(g, names), ce.value
+
     def forward_moe(self, batch, b: int = 0, forced=None):
         """Forward with MoE routing control: forced = list (per layer) of [l_q, k] expert ids or
         None. Returns (probs, logits, sel per layer, margin per layer)."""

@@ -1057,22 +1057,21 @@ void tokenizer_backward(const OrModel& mdl, const OrSample& s, const M& dtok, Gr
 }
 
 // Backward of model_forward for one request given dL/dlogits [n_cand, 3]; returns dtokens.
-M model_backward(const OrModel& mdl, const OrSample& s, const double* dlogits, Grads& G) {
-  if (mdl.cfg.moe_experts > 0) throw ConfigError("oracle: backward of the MoE FFN is not implemented");
-  Seq q = tokenize(mdl, s);
+// Saved activations of one block for the backward.
+struct BlockSaved {
+  M x, xr;
+  std::vector<int> qrows, roles, pos;
+  std::vector<uint8_t> vis;
+};
+
+// blocks_forward with every block's input, residual and plan kept (x, roles, pos advance).
+std::vector<BlockSaved> blocks_forward_saved(const OrModel& mdl, M& x, std::vector<int>& roles, std::vector<int>& pos) {
   const OrModelCfg& c = mdl.cfg;
   const int d = mdl.d;
-  struct Saved {
-    M x, xr;
-    std::vector<int> qrows, roles, pos;
-    std::vector<uint8_t> vis;
-  };
-  std::vector<Saved> sv(c.layers);
-  M x = q.tokens;
-  std::vector<int> roles = q.roles, pos = q.pos;
+  std::vector<BlockSaved> sv(c.layers);
   for (int l = 0; l < c.layers; ++l) {
     const std::string L = std::to_string(l);
-    Saved& S = sv[l];
+    BlockSaved& S = sv[l];
     S.x = x;
     S.roles = roles;
     S.pos = pos;
@@ -1097,40 +1096,16 @@ M model_backward(const OrModel& mdl, const OrSample& s, const double* dlogits, G
     roles = std::move(nroles);
     pos = std::move(npos);
   }
-  // ---- head backward (SPEC.md:362-365)
-  std::vector<int> crows;
-  for (int i = 0; i < x.r; ++i)
-    if (roles[i] == OR_ROLE_CAND) crows.push_back(i);
-  const int nc = static_cast<int>(crows.size());
-  M xc(nc, d);
-  for (int i = 0; i < nc; ++i) std::memcpy(xc.row(i), x.row(crows[i]), sizeof(double) * d);
-  const double* gfin = mdl.P("final_norm.gain").row(0);
-  M xh = rmsnorm(xc, gfin);
-  M hid = matmul(xh, mdl.P("head.w1"));
-  const M& b1 = mdl.P("head.b1");
-  for (int i = 0; i < hid.r; ++i)
-    for (int j = 0; j < hid.c; ++j) hid(i, j) = std::max(0.0, hid(i, j) + b1(0, j));
-  M dz(nc, 3);
-  std::memcpy(dz.a.data(), dlogits, sizeof(double) * nc * 3);
-  add_into(grad_of(G, mdl, "head.w2"), matmul_tn(hid, dz));
-  M& gb2 = grad_of(G, mdl, "head.b2");
-  for (int i = 0; i < nc; ++i)
-    for (int j = 0; j < 3; ++j) gb2(0, j) += dz(i, j);
-  M dhid = matmul_nt(dz, mdl.P("head.w2"));
-  for (size_t t = 0; t < dhid.a.size(); ++t)
-    if (hid.a[t] <= 0.0) dhid.a[t] = 0.0;  // ReLU (the subgradient 0 at 0)
-  add_into(grad_of(G, mdl, "head.w1"), matmul_tn(xh, dhid));
-  M& gb1 = grad_of(G, mdl, "head.b1");
-  for (int i = 0; i < nc; ++i)
-    for (int j = 0; j < dhid.c; ++j) gb1(0, j) += dhid(i, j);
-  M dxh = matmul_nt(dhid, mdl.P("head.w1"));
-  M dxc = rmsnorm_backward(dxh, xc, gfin, grad_of(G, mdl, "final_norm.gain").row(0));
-  M dx(x.r, d);
-  for (int i = 0; i < nc; ++i) std::memcpy(dx.row(crows[i]), dxc.row(i), sizeof(double) * d);
-  // ---- blocks in reverse
+  return sv;
+}
+
+// The blocks in reverse given d(final residual stream); returns d(tokens).
+M blocks_backward(const OrModel& mdl, const std::vector<BlockSaved>& sv, M dx, Grads& G) {
+  const OrModelCfg& c = mdl.cfg;
+  const int d = mdl.d;
   for (int l = c.layers - 1; l >= 0; --l) {
     const std::string L = std::to_string(l);
-    const Saved& S = sv[l];
+    const BlockSaved& S = sv[l];
     const int lq = static_cast<int>(S.qrows.size());
     // FFN: x_out = xr + down(swish(xf Wg) * (xf Wu)), xf = RMSN(xr)
     const double* gf = mdl.P("block." + L + ".ffn_norm").row(0);
@@ -1162,8 +1137,137 @@ M model_backward(const OrModel& mdl, const OrSample& s, const double* dlogits, G
       for (int j = 0; j < d; ++j) dxin(S.qrows[i], j) += dxr(i, j);
     dx = std::move(dxin);
   }
+  return dx;
+}
+
+// Backward of model_forward for one request given dL/dlogits [n_cand, 3]; returns dtokens.
+M model_backward(const OrModel& mdl, const OrSample& s, const double* dlogits, Grads& G) {
+  if (mdl.cfg.moe_experts > 0) throw ConfigError("oracle: backward of the MoE FFN is not implemented");
+  Seq q = tokenize(mdl, s);
+  const int d = mdl.d;
+  M x = q.tokens;
+  std::vector<int> roles = q.roles, pos = q.pos;
+  std::vector<BlockSaved> sv = blocks_forward_saved(mdl, x, roles, pos);
+  // ---- head backward (SPEC.md:362-365)
+  std::vector<int> crows;
+  for (int i = 0; i < x.r; ++i)
+    if (roles[i] == OR_ROLE_CAND) crows.push_back(i);
+  const int nc = static_cast<int>(crows.size());
+  M xc(nc, d);
+  for (int i = 0; i < nc; ++i) std::memcpy(xc.row(i), x.row(crows[i]), sizeof(double) * d);
+  const double* gfin = mdl.P("final_norm.gain").row(0);
+  M xh = rmsnorm(xc, gfin);
+  M hid = matmul(xh, mdl.P("head.w1"));
+  const M& b1 = mdl.P("head.b1");
+  for (int i = 0; i < hid.r; ++i)
+    for (int j = 0; j < hid.c; ++j) hid(i, j) = std::max(0.0, hid(i, j) + b1(0, j));
+  M dz(nc, 3);
+  std::memcpy(dz.a.data(), dlogits, sizeof(double) * nc * 3);
+  add_into(grad_of(G, mdl, "head.w2"), matmul_tn(hid, dz));
+  M& gb2 = grad_of(G, mdl, "head.b2");
+  for (int i = 0; i < nc; ++i)
+    for (int j = 0; j < 3; ++j) gb2(0, j) += dz(i, j);
+  M dhid = matmul_nt(dz, mdl.P("head.w2"));
+  for (size_t t = 0; t < dhid.a.size(); ++t)
+    if (hid.a[t] <= 0.0) dhid.a[t] = 0.0;  // ReLU (the subgradient 0 at 0)
+  add_into(grad_of(G, mdl, "head.w1"), matmul_tn(xh, dhid));
+  M& gb1 = grad_of(G, mdl, "head.b1");
+  for (int i = 0; i < nc; ++i)
+    for (int j = 0; j < dhid.c; ++j) gb1(0, j) += dhid(i, j);
+  M dxh = matmul_nt(dhid, mdl.P("head.w1"));
+  M dxc = rmsnorm_backward(dxh, xc, gfin, grad_of(G, mdl, "final_norm.gain").row(0));
+  M dx(x.r, d);
+  for (int i = 0; i < nc; ++i) std::memcpy(dx.row(crows[i]), dxc.row(i), sizeof(double) * d);
+  dx = blocks_backward(mdl, sv, std::move(dx), G);
   tokenizer_backward(mdl, s, dx, G);
   return dx;
+}
+
+// Backward of the pre-training loss for one click sequence: loss contribution
+// scale * sum_t CE_t (t < n, position t predicting click t) -> every gradient, the item table
+// included twice (tied head: dE += dz^T h; input embedding: tokenize_click_sequence's history
+// projection, tokenizer.cpp:240-284 / 315-317). Returns sum_t CE_t.
+double pretrain_backward(const OrModel& mdl, const OrSample& s, double scale, Grads& G) {
+  if (s.n_hist < 2) throw ConfigError("pretrain: sequences shorter than 2 clicks are skipped");
+  const OrModelCfg& c = mdl.cfg;
+  const int d = mdl.d, n = s.n_hist;
+  Seq q = tokenize_clicks(mdl, s);
+  M x = q.tokens;
+  std::vector<int> roles = q.roles, pos = q.pos;
+  std::vector<BlockSaved> sv = blocks_forward_saved(mdl, x, roles, pos);
+  if (x.r != n + 1) throw ConfigError("pretrain: query pruning must be off");
+  const double* gfin = mdl.P("final_norm.gain").row(0);
+  M xh = rmsnorm(x, gfin);
+  const M& W = mdl.P("pretrain.proj");
+  M h = matmul(xh, W);
+  const M& E = mdl.P("tok.item_table");
+  const int V = E.r, k = E.c;
+  M dh(h.r, k);
+  M& gE = grad_of(G, mdl, "tok.item_table");
+  double loss = 0.0;
+  std::vector<double> z(V);
+  for (int t = 0; t < n; ++t) {
+    double mx = -std::numeric_limits<double>::infinity();
+    for (int v = 0; v < V; ++v) {
+      double a = 0.0;
+      for (int j = 0; j < k; ++j) a += h(t, j) * E(v, j);
+      z[v] = a;
+      mx = std::max(mx, a);
+    }
+    double se = 0.0;
+    for (int v = 0; v < V; ++v) se += std::exp(z[v] - mx);
+    const double lse = mx + std::log(se);
+    const int tg = s.hist_item[t];
+    loss += lse - z[tg];
+    for (int v = 0; v < V; ++v) {
+      const double g = scale * (std::exp(z[v] - lse) - (v == tg ? 1.0 : 0.0));
+      for (int j = 0; j < k; ++j) {
+        dh(t, j) += g * E(v, j);
+        gE(v, j) += g * h(t, j);
+      }
+    }
+  }
+  add_into(grad_of(G, mdl, "pretrain.proj"), matmul_tn(xh, dh));
+  M dxh = matmul_nt(dh, W);
+  M dx = rmsnorm_backward(dxh, x, gfin, grad_of(G, mdl, "final_norm.gain").row(0));
+  dx = blocks_backward(mdl, sv, std::move(dx), G);
+  // tokenize_click_sequence backward: BOS = special row 0, clicks = the history projection
+  M& gs = grad_of(G, mdl, "tok.special");
+  for (int j = 0; j < d; ++j) gs(0, j) += dx(0, j);
+  M cat(n, mdl.hist_width());
+  std::vector<int> tbs(n);
+  for (int i = 0; i < n; ++i) {
+    const int64_t gap = i == 0 ? std::numeric_limits<int64_t>::max() / 4 : s.hist_ts[i] - s.hist_ts[i - 1];
+    tbs[i] = time_bucket(gap, c.n_time_buckets);
+    double* o = cat.row(i);
+    std::memcpy(o, E.row(s.hist_item[i]), sizeof(double) * c.item_dim);
+    std::memcpy(o + c.item_dim, mdl.P("tok.action_table").row(s.hist_action[i]), sizeof(double) * c.action_dim);
+    std::memcpy(o + c.item_dim + c.action_dim, mdl.P("tok.scene_table").row(s.hist_scene[i]),
+                sizeof(double) * c.scene_dim);
+    std::memcpy(o + c.item_dim + c.action_dim + c.scene_dim, mdl.P("tok.time_table").row(tbs[i]),
+                sizeof(double) * c.time_dim);
+  }
+  M dy(n, d);
+  for (int i = 0; i < n; ++i) std::memcpy(dy.row(i), dx.row(1 + i), sizeof(double) * d);
+  M proj = matmul(cat, mdl.P("tok.w_hist"));
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < d; ++j) proj(i, j) += mdl.P("tok.b_hist")(0, j);
+  M dproj = rmsnorm_backward(dy, proj, mdl.P("tok.g_hist").row(0), grad_of(G, mdl, "tok.g_hist").row(0));
+  add_into(grad_of(G, mdl, "tok.w_hist"), matmul_tn(cat, dproj));
+  M& gb = grad_of(G, mdl, "tok.b_hist");
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < d; ++j) gb(0, j) += dproj(i, j);
+  M dc = matmul_nt(dproj, mdl.P("tok.w_hist"));
+  M& ga = grad_of(G, mdl, "tok.action_table");
+  M& gsn = grad_of(G, mdl, "tok.scene_table");
+  M& gt = grad_of(G, mdl, "tok.time_table");
+  for (int i = 0; i < n; ++i) {
+    for (int j = 0; j < c.item_dim; ++j) gE(s.hist_item[i], j) += dc(i, j);
+    for (int j = 0; j < c.action_dim; ++j) ga(s.hist_action[i], j) += dc(i, c.item_dim + j);
+    for (int j = 0; j < c.scene_dim; ++j) gsn(s.hist_scene[i], j) += dc(i, c.item_dim + c.action_dim + j);
+    for (int j = 0; j < c.time_dim; ++j) gt(tbs[i], j) += dc(i, c.item_dim + c.action_dim + c.scene_dim + j);
+  }
+  return loss;
 }
 
 }  // namespace
@@ -1497,6 +1601,20 @@ int oracle_model_backward(const OrModel* m, const OrSample* s, const double* dlo
     try {
       M dx = model_backward(*m, *s, dlogits, G->g);
       if (dtokens) std::memcpy(dtokens, dx.a.data(), sizeof(double) * dx.a.size());
+    } catch (...) {
+      delete G;
+      throw;
+    }
+    *out = G;
+  });
+}
+
+int oracle_pretrain_backward(const OrModel* m, const OrSample* s, double scale, double* ce_sum, OrGrads** out) {
+  return guarded([&] {
+    auto* G = new OrGrads;
+    try {
+      const double l = pretrain_backward(*m, *s, scale, G->g);
+      if (ce_sum) *ce_sum = l;
     } catch (...) {
       delete G;
       throw;

@@ -184,6 +184,10 @@ int oracle_model_forward_batch(const OrModel* m, const OrSample* samples, int B,
 typedef struct OrGrads OrGrads;
 int oracle_model_backward(const OrModel* m, const OrSample* s, const double* dlogits,
                           double* dtokens, OrGrads** out);
+/* Pre-training backward of one click sequence: gradients of
+ * scale * sum_t CE_t over every parameter (item table: tied head + input embedding);
+ * *ce_sum = sum_t CE_t. */
+int oracle_pretrain_backward(const OrModel* m, const OrSample* s, double scale, double* ce_sum, OrGrads** out);
 int oracle_grads_get(const OrGrads* g, const char* name, double* out, int* rows, int* cols);
 void oracle_grads_destroy(OrGrads* g);
 /* AttentionLayer::backward of layer `layer` alone (attention.cpp:134-202): d(xn) [l_in, d]

@@ -24,7 +24,7 @@ __global__ void k_tok_concat(const TokParams p, int group, int K, __nv_bfloat16*
   const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   const int count = group == 0 ? p.B * p.H : (group == 1 ? p.B * p.N : p.B * p.P);
   if (w >= count) return;
-  const int st = p.special_tokens ? 1 : 0;
+  const int st = p.special_tokens || p.click_seq ? 1 : 0;  // click sequences: [BOS; clicks]
   const int off_hist = st, off_prof = st + p.H + st, off_cand = off_prof + p.P + st;
   const __nv_bfloat16* src[4] = {nullptr, nullptr, nullptr, nullptr};
   int len[4] = {0, 0, 0, 0};
@@ -32,7 +32,10 @@ __global__ void k_tok_concat(const TokParams p, int group, int K, __nv_bfloat16*
   if (group == 0) {
     const int b = w / p.H, i = w - b * p.H;
     int item = p.hist_item[w], act = p.hist_action[w], sc = p.hist_scene[w];
-    const int tb = tok_time_bucket(p.req_ts[b] - p.hist_ts[w], p.n_tb);
+    // click sequences: the gap to the previous click (first click: INT64_MAX / 4), as k_tokenize
+    const int64_t delta = p.click_seq ? (i == 0 ? 0x1FFFFFFFFFFFFFFFll : p.hist_ts[w] - p.hist_ts[w - 1])
+                                      : p.req_ts[b] - p.hist_ts[w];
+    const int tb = tok_time_bucket(delta, p.n_tb);
     if (static_cast<unsigned>(item) >= static_cast<unsigned>(p.n_items) ||
         static_cast<unsigned>(act) >= static_cast<unsigned>(p.n_actions) ||
         static_cast<unsigned>(sc) >= static_cast<unsigned>(p.n_scenes)) {

@@ -249,4 +249,57 @@ __global__ void __launch_bounds__(kCeThreads) k_ce_tied(const __nv_bfloat16* __r
   }
 }
 
+// ---------------------------------------------------------------- backward
+// Epilogue of the recomputed logit GEMM z = hp E^T (k_gemm_stream, 32-column chunks): the
+// pre-training loss gradient dL/dz_t[v] = scale * (softmax_t[v] - [v == click_t]) with the
+// forward's natural-log lse (position t < n predicts click t; the last position predicts
+// nothing), as bf16 P [T, V] -- the operand of dh = P E and dE += P^T hp.
+struct GsCeGrad {
+  static constexpr int kChunk = 32;
+  __nv_bfloat16* P;
+  int ldp;
+  const float* lse;       // [B, n]
+  const int32_t* click;   // [B, n]
+  int L, n;
+  float scale;            // 1 / (B n): the loss is the mean CE over predicted positions
+  __device__ void apply(int row, int col, const float (&v)[32]) const {
+    const int b = row / L, t = row - b * L;
+    uint32_t w[16];
+    if (t >= n) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) w[i] = 0u;
+    } else {
+      const float l = lse[static_cast<size_t>(b) * n + t];
+      const int tg = click[static_cast<size_t>(b) * n + t] - col;
+      constexpr float kLog2e = 1.4426950408889634f;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        float p0 = ex2_approx((v[2 * i] - l) * kLog2e) * scale;
+        float p1 = ex2_approx((v[2 * i + 1] - l) * kLog2e) * scale;
+        if (tg == 2 * i) p0 -= scale;
+        if (tg == 2 * i + 1) p1 -= scale;
+        w[i] = pack_bf16x2(p0, p1);
+      }
+    }
+    __nv_bfloat16* p = P + static_cast<size_t>(row) * ldp + col;
+    stg256(p, *reinterpret_cast<const uint32_t(*)[8]>(w));
+    stg256(p + 16, *reinterpret_cast<const uint32_t(*)[8]>(w + 8));
+  }
+};
+
+// loss = mean over the B n predicted positions of lse - target (one block, fixed order).
+__global__ void __launch_bounds__(1024) k_ce_loss(const float* __restrict__ lse, const float* __restrict__ tgt, int n,
+                                                  float* __restrict__ loss) {
+  __shared__ float red[1024];
+  float acc = 0.f;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += lse[i] - tgt[i];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = blockDim.x / 2; s; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *loss = red[0] / static_cast<float>(n);
+}
+
 }  // namespace sortk

@@ -109,6 +109,8 @@ struct Handle {
   const float* pre_proj = nullptr;  // pretrain.proj [d, item_dim] in the master buffer
   __nv_bfloat16* pre_hp = nullptr;  // projected rows [B * L, item_dim]
   float *pre_lse = nullptr, *pre_tgt = nullptr;  // [B, n_hist]
+  __nv_bfloat16* pre_P = nullptr;   // training: dL/dz [B * L, V] bf16 (recomputed logits' gradient)
+  float *pre_dh = nullptr, *pre_loss = nullptr;  // dL/d(hp) [B * L, item_dim], the step's loss
   // row-sharded item table (sort_set_item_table): the batch's item rows, gathered from the
   // owning ranks, replace the handle's table for the following calls
   const __nv_bfloat16* item_ext = nullptr;
@@ -129,6 +131,7 @@ struct Handle {
   float* master = nullptr;                 // fp32 master parameters (grad_index layout)
   float *adam_m = nullptr, *adam_v = nullptr;
   int adam_t = 0;
+  unsigned long long* adam_bad = nullptr;  // first non-finite gradient index + 1
   size_t grad_count = 0;
   bool training = false;  // forward currently saving activations
   struct TrainLayer {
@@ -585,6 +588,7 @@ static void finalize(Handle& h) {
   // ---- head (fp32)
   need_param(h, "final_norm.gain", 1, d);
   if (c.pretrain) {
+    h.frozen.clear();  // pre-training learns the item table (the tables transfer_sparse copies)
     if (c.item_dim != kPreK) throw ConfigError("pretrain: the tied head needs item_dim == 32 in this build");
     need_param(h, "pretrain.proj", d, c.item_dim);
     h.pre_hp = h.dalloc<__nv_bfloat16>(static_cast<size_t>(h.Bmax) * h.L0 * kPreK);
@@ -1521,10 +1525,30 @@ static void train_do_boxes(Handle& h, int Rq, int B, Handle::TrainLayer& T) {
   T.tmDO64 = make_tmap(CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, h.dO16, 4, dims, str, b64, dk * 2);
 }
 
+// Unfreezing the item table: its fp32 master (from the bf16 device table), gradient, moments.
+static void unfreeze_item_table(Handle& h) {
+  if (h.item_master) return;
+  const size_t n = static_cast<size_t>(h.cfg.n_items) * h.cfg.item_dim;
+  h.item_master = h.dalloc<float>(n);
+  h.item_grad = h.dalloc<float>(n);
+  h.item_m = h.dalloc<float>(n);
+  h.item_v = h.dalloc<float>(n);
+  k_bf16_to_f32<<<ew_grid(n), 256, 0, h.stream>>>(h.item, n, h.item_master);  // master from the device table
+  CK(cudaMemsetAsync(h.item_m, 0, n * 4, h.stream));
+  CK(cudaMemsetAsync(h.item_v, 0, n * 4, h.stream));
+  check_launch("item table master");
+}
+
 static void ensure_train_buffers(Handle& h, int B) {
-  if (h.cfg.pretrain) throw ConfigError("training step: use the ranking model (pretrain backward not in this build)");
   if (h.moe) throw ConfigError("training step: the MoE FFN backward is not implemented in this build");
+  if (!h.frozen.count("tok.item_table")) unfreeze_item_table(h);  // (pre-training trains it by default)
   if (h.train_B >= B) return;
+  if (h.cfg.pretrain) {
+    if (h.cfg.n_items % 32 != 0) throw ConfigError("pre-training step: n_items must be a multiple of 32");
+    h.pre_P = h.dalloc<__nv_bfloat16>(static_cast<size_t>(h.Bmax) * h.L0 * h.cfg.n_items);
+    h.pre_dh = h.dalloc<float>(static_cast<size_t>(h.Bmax) * h.L0 * h.cfg.item_dim);
+    h.pre_loss = h.dalloc<float>(1);
+  }
   if (!h.cublas) {
     if (cublasCreate(&h.cublas) != CUBLAS_STATUS_SUCCESS) throw RuntimeFailure("cublasCreate failed");
   }
@@ -1574,6 +1598,31 @@ static void rms_bwd(Handle& h, const float* dy, const T* x, const float* inv, co
     k_rmsnorm_bwd<T><<<(rows + 63) / 64, 256, d * 4, h.stream>>>(dy, x, inv, gain, rows, d, dx, accum, dgain);
     if (dx16) k_f32_to_bf16<<<ew_grid(static_cast<size_t>(rows) * d), 256, 0, h.stream>>>(dx, static_cast<size_t>(rows) * d, dx16);
   }
+}
+
+// Pre-training head backward: loss = mean over the B n predicted positions of
+// lse_t - z_t[click_t], z_t = hp_t E^T. The logits are recomputed by the tcgen05 GEMM whose
+// epilogue writes dL/dz as bf16 (GsCeGrad); dh = dz E and dE += dz^T hp (the tied head's share
+// of the item-table gradient) are two more tcgen05 GEMMs; then hp = RMSN(x) proj backward
+// writes d(final stream) for every position into dX.
+static void pretrain_head_backward(Handle& h, int B, float* dX) {
+  const SortConfig& c = h.cfg;
+  const int d = h.d, L = h.L0, n = L - 1, T = B * L, V = c.n_items, K = c.item_dim;
+  if (h.item_ext) throw ConfigError("pre-training step: the row-sharded item table is not trained here");
+  const __nv_bfloat16* Xf = h.X[h.layers.back().q_buf];
+  gemm_stream(h, h.pre_hp, K, T, K, h.item, K, V,
+              GsCeGrad{h.pre_P, V, h.pre_lse, h.in_item, L, n, 1.f / static_cast<float>(B * n)});
+  gemm_rm16(h, false, false, T, K, V, h.pre_P, V, h.item, K, h.pre_dh, K, false);           // dh = dz E
+  if (!h.frozen.count("tok.item_table"))
+    gemm_rm16(h, true, false, V, K, T, h.pre_P, V, h.pre_hp, K, h.item_grad, K, false, 1.f);  // dE += dz^T hp
+  float* xh = h.tw[2];
+  float* inv = h.tw[14];
+  rms_rows<__nv_bfloat16>(h, Xf, w32(h, "final_norm.gain"), T, d, xh, inv);
+  gemm_rm(h, true, false, d, K, T, xh, d, h.pre_dh, K, grad_ptr(h, "pretrain.proj"), K);
+  float* dxh = h.tw[3];
+  gemm_rm(h, false, true, T, d, K, h.pre_dh, K, w32(h, "pretrain.proj"), K, dxh, d);
+  rms_bwd<__nv_bfloat16>(h, dxh, Xf, inv, w32(h, "final_norm.gain"), T, d, dX, 0, grad_ptr(h, "final_norm.gain"));
+  check_launch("pretrain head backward");
 }
 
 // Backward of one training forward; dz = dL/dlogits [B*N, 3] on the device.
@@ -1640,6 +1689,9 @@ static void backward_device(Handle& h, int B, const float* dz) {
   float* dX = h.tw[0];
   float* dXn = h.tw[1];
   float* inv = h.tw[14];
+  if (c.pretrain) {
+    pretrain_head_backward(h, B, dX);
+  } else {
   // ---- head: xc = final candidate rows, xh = RMSN(xc), hid = relu(xh W1 + b1)
   const LayerDev& last = h.layers.back();
   const int R = last.Rq, BN = B * N;
@@ -1679,6 +1731,7 @@ static void backward_device(Handle& h, int B, const float* dz) {
   CK(cudaMemsetAsync(dX, 0, static_cast<size_t>(B) * R * d * 4, h.stream));
   k_scatter_add_rows<<<(BN + 7) / 8, 256, 0, h.stream>>>(dxc, cmap, B, N, R, d, dX);
   check_launch("head backward");
+  }
   // ---- blocks in reverse
   for (int l = c.layers - 1; l >= 0; --l) {
     const LayerDev& L = h.layers[l];
@@ -1939,7 +1992,7 @@ static void backward_device(Handle& h, int B, const float* dz) {
   }
   if (c.special_tokens)
     k_special_grad<<<(3 * d + 255) / 256, 256, 0, h.stream>>>(dX, B, h.L0, c.n_hist, c.n_profile_fields, d,
-                                                              grad_ptr(h, "tok.special"));
+                                                              c.pretrain ? 1 : 3, grad_ptr(h, "tok.special"));
   check_launch("tokenizer backward");
   for (const std::string& name : h.frozen) {  // frozen tensors receive zero gradient
     auto it = h.grad_index.find(name);
@@ -2766,6 +2819,34 @@ int sort_train_step(SortHandle p, const SortBatch* batch, const float* dlogits, 
   });
 }
 
+int sort_pretrain_train_step(SortHandle p, const SortBatch* batch, float* loss) {
+  return api([&] {
+    Handle* h = ready(p);
+    if (!batch) throw ConfigError("null argument");
+    if (!h->cfg.pretrain) throw ConfigError("sort_pretrain_train_step needs a pre-training model (pretrain = 1)");
+    if (h->cfg.n_hist < 2) throw ConfigError("pretrain: sequences shorter than 2 clicks are skipped");
+    const int B = batch->batch;
+    begin_timing(*h);
+    upload_batch(*h, batch, false);
+    ensure_train_buffers(*h, B);
+    h->training = true;
+    try {
+      forward_device(*h, B);
+    } catch (...) {
+      h->training = false;
+      throw;
+    }
+    h->training = false;
+    k_ce_loss<<<1, 1024, 0, h->stream>>>(h->pre_lse, h->pre_tgt, B * h->cfg.n_hist, h->pre_loss);
+    check_launch("pretrain loss");
+    backward_device(*h, B, nullptr);
+    float hl = 0.f;
+    CK(cudaMemcpyAsync(&hl, h->pre_loss, 4, cudaMemcpyDeviceToHost, h->stream));
+    collect_status(*h);
+    if (loss) *loss = hl;
+  });
+}
+
 int sort_train_step_bce(SortHandle p, const SortBatch* batch, const float* labels, const float* obj_weights,
                         float* loss) {
   return api([&] {
@@ -2818,8 +2899,8 @@ int sort_adamw_step(SortHandle p, float lr, float beta1, float beta2, float eps,
     ++h->adam_t;
     const float bc1 = 1.f - std::pow(beta1, static_cast<float>(h->adam_t));
     const float bc2 = 1.f - std::pow(beta2, static_cast<float>(h->adam_t));
-    unsigned long long* bad = reinterpret_cast<unsigned long long*>(h->dz_dev ? h->tw[14] : nullptr);
-    if (!bad) throw ConfigError("no gradients yet (call sort_train_step)");
+    if (!h->adam_bad) h->adam_bad = h->dalloc<unsigned long long>(1);
+    unsigned long long* bad = h->adam_bad;
     const unsigned long long none = ~0ull;
     CK(cudaMemcpyAsync(bad, &none, 8, cudaMemcpyHostToDevice, h->stream));
     // one launch per run of trainable tensors (frozen ones are skipped: no update, no decay)
@@ -2914,19 +2995,6 @@ int sort_get_grad(SortHandle p, const char* name, float* out) {
   });
 }
 
-static void unfreeze_item_table(Handle& h) {
-  if (h.item_master) return;
-  if (h.cfg.pretrain) throw ConfigError("item-table training: use the ranking model");
-  const size_t n = static_cast<size_t>(h.cfg.n_items) * h.cfg.item_dim;
-  h.item_master = h.dalloc<float>(n);
-  h.item_grad = h.dalloc<float>(n);
-  h.item_m = h.dalloc<float>(n);
-  h.item_v = h.dalloc<float>(n);
-  k_bf16_to_f32<<<ew_grid(n), 256, 0, h.stream>>>(h.item, n, h.item_master);  // master from the device table
-  CK(cudaMemsetAsync(h.item_m, 0, n * 4, h.stream));
-  CK(cudaMemsetAsync(h.item_v, 0, n * 4, h.stream));
-  check_launch("item table master");
-}
 
 int sort_set_frozen(SortHandle p, const char* name, int32_t frozen) {
   return api([&] {

@@ -995,10 +995,10 @@ __global__ void __launch_bounds__(256) k_tok_table_scatter(const float* __restri
 }
 
 // d(special table) rows: BOS = row 0, SEPs = rows 1 + H and 2 + H + P of every request.
-__global__ void k_special_grad(const float* __restrict__ dX, int B, int L, int H, int P, int d,
+__global__ void k_special_grad(const float* __restrict__ dX, int B, int L, int H, int P, int d, int n_special,
                                float* __restrict__ gspecial) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= 3 * d) return;
+  if (i >= n_special * d) return;  // click sequences carry BOS only
   const int k = i / d, c = i - k * d;
   const int row = k == 0 ? 0 : (k == 1 ? 1 + H : 2 + H + P);
   float s = 0.f;

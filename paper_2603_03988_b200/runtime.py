@@ -65,7 +65,7 @@ EXPORTS = [
     "sort_nccl_unique_id", "sort_exchange_create_nccl", "sort_exchange_create_host",
     "sort_exchange_destroy", "sort_exchange_lookup", "sort_exchange_allreduce_f32", "sort_op_gemm",
     "sort_op_rmsnorm", "sort_op_rmsnorm_backward", "sort_op_rope", "sort_op_attention_layer",
-    "sort_get_grad", "sort_set_frozen", "sort_transfer_item_table",
+    "sort_get_grad", "sort_set_frozen", "sort_transfer_item_table", "sort_pretrain_train_step",
 ]
 
 _lib = None
@@ -115,6 +115,7 @@ def lib():
         L.sort_adamw_step.argtypes = [C.c_void_p, C.c_float, C.c_float, C.c_float, C.c_float, C.c_float]
         L.sort_get_param.argtypes = [C.c_void_p, C.c_char_p, f32p]
         L.sort_get_grad.argtypes = [C.c_void_p, C.c_char_p, f32p]
+        L.sort_pretrain_train_step.argtypes = [C.c_void_p, C.c_void_p, f32p]
         L.sort_set_frozen.argtypes = [C.c_void_p, C.c_char_p, C.c_int32]
         L.sort_transfer_item_table.argtypes = [C.c_void_p, C.c_void_p, C.c_int32]
         L.sort_moe_routing.argtypes = [C.c_void_p, C.c_int, C.c_int32, i32p, i32p, f32p]
@@ -381,6 +382,14 @@ class SortModel:
         _check(lib().sort_train_step_bce(self.h, C.byref(hold.c), _p(lab, f32p), _p(w, f32p),
                                          C.byref(loss)))
         return float(loss.value)
+
+    def pretrain_train_step(self, batch: Dict[str, np.ndarray]) -> float:
+        """Pre-training step: mean next-item CE over the predicted positions,
+        gradients of every parameter (item table included unless frozen) on the device."""
+        hold = _BatchHold(batch)
+        loss = np.zeros(1, np.float32)
+        _check(lib().sort_pretrain_train_step(self.h, C.byref(hold.c), _p(loss, f32p)))
+        return float(loss[0])
 
     def adamw_step(self, lr: float, beta1: float = 0.9, beta2: float = 0.99, eps: float = 1e-8,
                    weight_decay: float = 0.01):

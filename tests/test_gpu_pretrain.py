@@ -75,3 +75,69 @@ def test_pretrain_uniform_vocab_ce_is_ln_v():
     gm = R.SortModel(cfg, P, max_batch=1)
     lse, tgt = gm.pretrain_forward(synth.make_batch(cfg, 1, seed=46))
     np.testing.assert_allclose(lse - tgt, np.log(100.0), atol=2e-3)
+
+
+# ---- pre-training backward (sort_pretrain_train_step) vs the fp64 oracle's pretrain_backward.
+# Bars: the GPU forward is bf16 and dL/dz is stored as bf16, so gradients carry ~1e-2 relative
+# noise; each gradient must be within GRAD_REL (rel-L2) of the oracle's and point the same way
+# (cosine >= GRAD_COS); the loss within LOSS_REL. Measured values are printed on failure.
+GRAD_REL = 6e-2
+GRAD_COS = 0.995
+LOSS_REL = 1e-2
+
+
+def test_pretrain_backward_vs_oracle():
+    cfg = small(n_items=2048, n_hist=96)
+    B = 2
+    P = synth.make_params(cfg, seed=51)
+    Pr = {k: synth.bf16_round(v).astype(np.float64) for k, v in P.items()}
+    gm = R.SortModel(cfg, P, max_batch=B)
+    batch = synth.make_batch(cfg, B, seed=52)
+    loss = gm.pretrain_train_step(batch)
+    names = list(P.keys())
+    om = O.OracleModel(cfg, Pr)
+    scale = 1.0 / (B * cfg.n_hist)
+    ref = {n: None for n in names}
+    ce = 0.0
+    for b in range(B):
+        g, c = om.pretrain_backward(batch, b, scale, names)
+        ce += c
+        for n in names:
+            if g[n] is not None:
+                ref[n] = g[n] if ref[n] is None else ref[n] + g[n]
+    assert abs(loss - ce * scale) <= LOSS_REL * abs(ce * scale), (loss, ce * scale)
+    bad = {}
+    for n in names:
+        got = gm.get_grad(n).astype(np.float64)
+        if ref[n] is None:
+            assert not np.any(got), n
+            continue
+        r = ref[n].reshape(got.shape)
+        err = rel_l2(got, r)
+        cos = float((got * r).sum() / max(np.linalg.norm(got) * np.linalg.norm(r), 1e-30))
+        if err > GRAD_REL or cos < GRAD_COS:
+            bad[n] = (err, cos)
+    assert not bad, bad
+    # an optimizer step moves the (trainable) item table and lowers nothing else unexpectedly
+    t0 = gm.get_param("tok.item_table").copy()
+    gm.adamw_step(1e-3)
+    assert np.linalg.norm(gm.get_param("tok.item_table") - t0) > 0
+
+
+def test_pretrain_steps_reduce_loss_and_transfer():
+    """A few AdamW steps on a fixed batch lower the CE; the learned table then transfers into a
+    ranking handle with freeze."""
+    from paper_2603_03988_b200.config import tiny_config
+    cfg = small(n_items=2048, n_hist=96)
+    gm = R.SortModel(cfg, synth.make_params(cfg, seed=53), max_batch=2)
+    batch = synth.make_batch(cfg, 2, seed=54)
+    losses = []
+    for _ in range(6):
+        losses.append(gm.pretrain_train_step(batch))
+        gm.adamw_step(3e-3)
+    assert losses[-1] < losses[0], losses
+    rc = tiny_config(n_items=2048)
+    rank = R.SortModel(rc, synth.make_params(rc, seed=55), max_batch=2)
+    rank.transfer_item_table(gm, freeze=True)
+    # the frozen destination holds the table as bf16 (round to nearest even of the fp32 master)
+    assert np.array_equal(rank.get_param("tok.item_table"), synth.bf16_round(gm.get_param("tok.item_table")))
