@@ -118,7 +118,11 @@ struct AttnTmem {
   __device__ static constexpr uint32_t o_col(int buf) { return DK <= 32 ? buf * 128 + 32 : 256 + buf * DK; }
 };
 
-template <int DK, bool kFixed>
+// kPre (inference, bounded logits only): Q arrives pre-multiplied by log2(e) / sqrt(dk) (folded
+// into the QKNorm gain of the QKVG epilogue), so S is already the base-2 exponent and the
+// reference is 0: |S| <= B log2 e < 58 keeps every 2^S a normal fp32 / bf16 number, P = 2^S
+// needs no FFMA per element and the polynomial exp2 no clamp.
+template <int DK, bool kFixed, bool kPre = false>
 __global__ void __launch_bounds__(kAttnThreads, AttnTmem<DK>::kCtasPerSm)
     k_attention(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const AttnArgs a) {
@@ -384,7 +388,7 @@ __global__ void __launch_bounds__(kAttnThreads, AttnTmem<DK>::kCtasPerSm)
       const bool has_prev = li > 0;
       if (has_prev) {  // this item's row sums start from zero; keep the previous item's
         p_lsum = (lsum[0].x + lsum[0].y) + (lsum[1].x + lsum[1].y);
-        p_ref = kFixed ? a.ref_log2 : (m == NEG_INF ? 0.f : m * sl2);
+        p_ref = kPre ? 0.f : (kFixed ? a.ref_log2 : (m == NEG_INF ? 0.f : m * sl2));
         lsum[0] = lsum[1] = make_float2(0.f, 0.f);
       }
       m = NEG_INF;
@@ -400,7 +404,9 @@ __global__ void __launch_bounds__(kAttnThreads, AttnTmem<DK>::kCtasPerSm)
         SOFTMAX_WAIT(&s_full[buf * 2 + hf], (g >> 1) & 1);
         tc_fence_after();
         float ref;  // exp2 reference in the scaled domain
-        if constexpr (kFixed) {
+        if constexpr (kPre) {
+          ref = 0.f;
+        } else if constexpr (kFixed) {
           ref = a.ref_log2;
         } else {
           float mx4[4] = {NEG_INF, NEG_INF, NEG_INF, NEG_INF};
@@ -455,11 +461,11 @@ __global__ void __launch_bounds__(kAttnThreads, AttnTmem<DK>::kCtasPerSm)
             if (full_mask & (1u << cb)) {
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
-                const float2 x = ffma2(make_float2(__uint_as_float(rr[2 * i]), __uint_as_float(rr[2 * i + 1])),
-                                       sl2v, nref);
+                const float2 s2 = make_float2(__uint_as_float(rr[2 * i]), __uint_as_float(rr[2 * i + 1]));
+                const float2 x = kPre ? s2 : ffma2(s2, sl2v, nref);
                 // every kPolyEvery-th pair on the FMA pipe, the rest on MUFU
                 const float2 p = (kPolyEvery > 0 && i % kPolyEvery == kPolyEvery - 1)
-                                     ? ex2_poly2(x)
+                                     ? (kPre ? ex2_poly2_nc(x) : ex2_poly2(x))
                                      : make_float2(ex2_approx(x.x), ex2_approx(x.y));
                 if (!kMmaRowSum) lsum[i & 1] = fadd2(lsum[i & 1], p);
                 w[i] = pack_bf16x2(p.x, p.y);
@@ -468,8 +474,8 @@ __global__ void __launch_bounds__(kAttnThreads, AttnTmem<DK>::kCtasPerSm)
               const uint32_t bits = chunk_vis_bits(c0 + cb * 32, meta.x, meta.y, meta.z);
 #pragma unroll
               for (int i = 0; i < 16; ++i) {
-                float2 x = ffma2(make_float2(__uint_as_float(rr[2 * i]), __uint_as_float(rr[2 * i + 1])),
-                                 sl2v, nref);
+                const float2 s2 = make_float2(__uint_as_float(rr[2 * i]), __uint_as_float(rr[2 * i + 1]));
+                float2 x = kPre ? s2 : ffma2(s2, sl2v, nref);
                 x.x = (bits >> (2 * i)) & 1u ? x.x : NEG_INF;
                 x.y = (bits >> (2 * i + 1)) & 1u ? x.y : NEG_INF;
                 const float2 p = make_float2(ex2_approx(x.x), ex2_approx(x.y));
@@ -495,7 +501,7 @@ __global__ void __launch_bounds__(kAttnThreads, AttnTmem<DK>::kCtasPerSm)
     }  // item loop
     if (li > 0) {  // the last item
       p_lsum = (lsum[0].x + lsum[0].y) + (lsum[1].x + lsum[1].y);
-      p_ref = kFixed ? a.ref_log2 : (m == NEG_INF ? 0.f : m * sl2);
+      p_ref = kPre ? 0.f : (kFixed ? a.ref_log2 : (m == NEG_INF ? 0.f : m * sl2));
       finish_item(g - 1, alpha_prev, li - 1, false);
     }
   }

@@ -401,6 +401,19 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
                      __int_as_float(__float_as_int(p.y) + (jy << 23)));
 }
 
+// ex2_poly2 without the clamp, for arguments already inside [-126, 127] (pre-scaled logits).
+__device__ __forceinline__ float2 ex2_poly2_nc(float2 x) {
+  const float2 t = fadd2(x, make_float2(12582912.f, 12582912.f));
+  const float2 j = fadd2(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = fadd2(x, make_float2(-j.x, -j.y));
+  float2 p = ffma2(make_float2(5.5171616e-2f, 5.5171616e-2f), f, make_float2(2.4261117e-1f, 2.4261117e-1f));
+  p = ffma2(p, f, make_float2(6.9326103e-1f, 6.9326103e-1f));
+  p = ffma2(p, f, make_float2(9.9992806e-1f, 9.9992806e-1f));
+  const int jx = __float_as_int(t.x) - 0x4B400000, jy = __float_as_int(t.y) - 0x4B400000;
+  return make_float2(__int_as_float(__float_as_int(p.x) + (jx << 23)),
+                     __int_as_float(__float_as_int(p.y) + (jy << 23)));
+}
+
 __device__ __forceinline__ float tanh_approx(float x) {
   float y;
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));

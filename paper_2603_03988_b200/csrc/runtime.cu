@@ -56,6 +56,7 @@ struct LayerDev {
   __nv_bfloat16 *w_all = nullptr, *w_kv = nullptr, *w_qg = nullptr, *w_o = nullptr,
                 *w_up = nullptr, *w_down = nullptr;
   float *gain_q = nullptr, *gain_k = nullptr;
+  float* gain_q_s = nullptr;  // gain_q * log2(e) / sqrt(dk): the pre-scaled Q of inference attention
   int in_buf = 0, q_buf = 0;
   int Rq = 0, Rkv = 0;
   int bn_full = 0, bn_half = 0, bn_up = 0, bn_o = 0, bn_down = 0;
@@ -92,6 +93,7 @@ struct Handle {
   bool attn_bwd_mma = true; // sort_set_option("attn_bwd_mma"): tensor-core attention backward
   bool attn_bwd_tc = true;  // sort_set_option("attn_bwd_tc"): tcgen05 attention backward (0: mma.sync)
   bool qkvg_pair = false;   // sort_set_option("qkvg_pair"): QKVG projection as CTA pairs
+  bool attn_prescale = true;  // sort_set_option("attn_prescale"): inference Q pre-scaled into the exp2 domain
   bool generic = false;    // d > 256 (SORT-large): projections through the generic path
   // ---- MoE FFN: routed + shared experts as grouped tcgen05 GEMMs
   bool moe = false;
@@ -516,6 +518,10 @@ static void finalize(Handle& h) {
       for (float v : gq.v) mq = std::max(mq, std::fabs(v));
       for (float v : gk.v) mk = std::max(mk, std::fabs(v));
       L.logit_bound = 1.02f * std::sqrt(static_cast<float>(dk)) * mq * mk + 1e-3f;
+      std::vector<float> gs(gq.v);
+      const float sl2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(dk)));
+      for (float& v : gs) v *= sl2;
+      L.gain_q_s = h.upload(gs);
     }
     // plan arrays
     std::vector<int4> meta(static_cast<size_t>(lp.n_qtiles) * 128, make_int4(0, -1, -1, 0));
@@ -743,7 +749,14 @@ static void launch_gemm_pair(Handle& h, const CUtensorMap& A, const CUtensorMap&
   ++h.launches;
 }
 
-template <int DK, bool kFixed>
+// Inference with bounded logits: Q leaves the QKVG epilogue multiplied by log2(e)/sqrt(dk)
+// (gain_q_s) and k_attention<.., kPre> exponentiates S directly. Training keeps the unscaled Q
+// (the backward recomputes S from it).
+static bool attn_prescaled(const Handle& h, const LayerDev& L) {
+  return h.attn_prescale && !h.training && L.gain_q_s && L.logit_bound > 0.f && L.logit_bound < kFixedRefMax;
+}
+
+template <int DK, bool kFixed, bool kPre = false>
 static void launch_attention_dk(Handle& h, const LayerDev& L, const LayerPlan& lp, int B) {
   const int n_codes = static_cast<int>(lp.tile_code.size()) / 2;  // {kv_tile, classes} pairs
   AttnArgs a;
@@ -776,15 +789,23 @@ static void launch_attention_dk(Handle& h, const LayerDev& L, const LayerPlan& l
   const CUtensorMap& tk = h.save_to ? h.save_to->tmK : L.tmK;
   const CUtensorMap& tv = h.save_to ? h.save_to->tmV : L.tmV;
   const size_t smem = AttnSmem<DK>::bytes(tile_ints);
-  ensure_smem(k_attention<DK, kFixed>, smem);
+  ensure_smem(k_attention<DK, kFixed, kPre>, smem);
   const int grid = std::min(n_items, AttnTmem<DK>::kCtasPerSm * h.num_sms);
-  k_attention<DK, kFixed><<<grid, kAttnThreads, smem, h.stream>>>(tq, tk, tv, a);
+  k_attention<DK, kFixed, kPre><<<grid, kAttnThreads, smem, h.stream>>>(tq, tk, tv, a);
   check_launch("attention");
   ++h.launches;
 }
 
 static void launch_attention(Handle& h, const LayerDev& L, const LayerPlan& lp, int B) {
   const bool fixed = L.logit_bound > 0.f && L.logit_bound < kFixedRefMax;
+  if (attn_prescaled(h, L)) {
+    switch (h.dk) {
+      case 16: launch_attention_dk<16, true, true>(h, L, lp, B); return;
+      case 32: launch_attention_dk<32, true, true>(h, L, lp, B); return;
+      case 64: launch_attention_dk<64, true, true>(h, L, lp, B); return;
+      default: throw ConfigError("unsupported head dim");
+    }
+  }
   switch (h.dk * 2 + (fixed ? 1 : 0)) {
     case 32: launch_attention_dk<16, false>(h, L, lp, B); break;
     case 33: launch_attention_dk<16, true>(h, L, lp, B); break;
@@ -810,7 +831,7 @@ static void launch_qkvg_dk(Handle& h, const LayerDev& L, const CUtensorMap& A, c
     e.chead[ci] = static_cast<uint8_t>(ci / ns);
   }
   e.inv_d = 1.f / static_cast<float>(h.d);
-  e.gain_q = L.gain_q;
+  e.gain_q = attn_prescaled(h, L) ? L.gain_q_s : L.gain_q;
   e.gain_k = L.gain_k;
   e.q = h.save_to ? h.save_to->q : h.Qb;
   e.k = h.save_to ? h.save_to->k : h.Kb;
@@ -2114,7 +2135,7 @@ static void forward_generic(Handle& h, int B) {
       // [Wq | Wg] on the query rows, [Wk | Wv] on all rows; QKNorm + RoPE + head-major layout
       // (and the sigmoid gate) in the epilogue, straight from the fp32 accumulators
       gemm_stream(h, xqp, d, M, d, wT16(h, A + "wq|wg^T", {A + "wq", A + "wg"}), d, 2 * d,
-                  GsQKVG{d, H, L.Rq, L.pos_q, h.rope, L.gain_q, h.Qb, h.Gb, true});
+                  GsQKVG{d, H, L.Rq, L.pos_q, h.rope, attn_prescaled(h, L) ? L.gain_q_s : L.gain_q, h.Qb, h.Gb, true});
       gemm_stream(h, xn, d, Mkv, d, wT16(h, A + "wk|wv^T", {A + "wk", A + "wv"}), d, 2 * d,
                   GsQKVG{d, H, L.Rkv, L.pos_kv, h.rope, L.gain_k, h.Kb, h.Vb, false});
     } else {
@@ -2122,7 +2143,7 @@ static void forward_generic(Handle& h, int B) {
       __nv_bfloat16* pkv = reinterpret_cast<__nv_bfloat16*>(h.gw[3]);  // [Mkv, 2d]
       gemm_rm_bf16(h, M, 2 * d, d, xqp, d, w16_cat(h, A + "wq|wg", {A + "wq", A + "wg"}), 2 * d, pqg, 2 * d, 0.f, true);
       gemm_rm_bf16(h, Mkv, 2 * d, d, xn, d, w16_cat(h, A + "wk|wv", {A + "wk", A + "wv"}), 2 * d, pkv, 2 * d, 0.f, true);
-      qkv_prep(h, pqg, 2 * d, M, L.Rq, H, dk, 0, L.pos_q, L.gain_q, h.Qb);
+      qkv_prep(h, pqg, 2 * d, M, L.Rq, H, dk, 0, L.pos_q, attn_prescaled(h, L) ? L.gain_q_s : L.gain_q, h.Qb);
       qkv_prep(h, pkv, 2 * d, Mkv, L.Rkv, H, dk, 1, L.pos_kv, L.gain_k, h.Kb);
       qkv_prep(h, pkv + d, 2 * d, Mkv, L.Rkv, H, dk, 2, nullptr, nullptr, h.Vb);
       qkv_prep(h, pqg + d, 2 * d, M, L.Rq, H, dk, 3, nullptr, nullptr, h.Gb);
@@ -2226,6 +2247,12 @@ static void repack_weights(Handle& h) {
     for (float v : gq) mq = std::max(mq, std::fabs(v));
     for (float v : gkv) mk = std::max(mk, std::fabs(v));
     L.logit_bound = 1.02f * std::sqrt(static_cast<float>(dk)) * mq * mk + 1e-3f;
+    if (L.gain_q_s) {
+      const float sl2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(dk)));
+      for (float& v : gq) v *= sl2;
+      CK(cudaMemcpyAsync(L.gain_q_s, gq.data(), gq.size() * 4, cudaMemcpyHostToDevice, h.stream));
+      CK(cudaStreamSynchronize(h.stream));
+    }
   }
   for (auto& kv : h.tw16)  // bf16 copies the training backward reads
     k_f32_to_bf16<<<ew_grid(kv.second.second), 256, 0, h.stream>>>(w32(h, kv.first), kv.second.second,
@@ -3216,6 +3243,8 @@ int sort_set_option(SortHandle p, const char* name, int32_t value) {
       h->tail_pair = value != 0;
     } else if (std::strcmp(name, "attn_bwd_mma") == 0) {
       h->attn_bwd_mma = value != 0;
+    } else if (std::strcmp(name, "attn_prescale") == 0) {
+      h->attn_prescale = value != 0;
     } else if (std::strcmp(name, "qkvg_pair") == 0) {
       h->qkvg_pair = value != 0;
 
