@@ -108,13 +108,25 @@ __global__ void k_xchg_count(const int32_t* __restrict__ ids, int64_t n, int64_t
 __global__ void k_xchg_scatter(const int32_t* __restrict__ ids, int64_t n, int64_t rows_per_rank,
                                const int64_t* __restrict__ offsets, unsigned long long* __restrict__ cursor,
                                int32_t* __restrict__ send_ids, int64_t* __restrict__ src) {
-  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t id = ids[i];
-    const int owner = static_cast<int>(id / rows_per_rank);
-    const int64_t pos = offsets[owner] + static_cast<int64_t>(atomicAdd(cursor + owner, 1ull));
-    send_ids[pos] = static_cast<int32_t>(id - owner * rows_per_rank);
-    src[pos] = i;
+  // warp-aggregated slots: the lanes of a warp with the same owner take one atomicAdd (a
+  // single global counter per owner would otherwise serialise every id, e.g. at world 1)
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t base = blockIdx.x * static_cast<int64_t>(blockDim.x); base < n; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    const bool act = i < n;
+    const int64_t id = act ? ids[i] : 0;
+    const int owner = act ? static_cast<int>(id / rows_per_rank) : -1;
+    const unsigned peers = __match_any_sync(0xffffffffu, owner);
+    const int leader = __ffs(peers) - 1;
+    unsigned long long first = 0;
+    if (act && lane == leader) first = atomicAdd(cursor + owner, static_cast<unsigned long long>(__popc(peers)));
+    first = __shfl_sync(0xffffffffu, first, leader);
+    if (act) {
+      const int64_t pos = offsets[owner] + static_cast<int64_t>(first) + __popc(peers & ((1u << lane) - 1u));
+      send_ids[pos] = static_cast<int32_t>(id - owner * rows_per_rank);
+      src[pos] = i;
+    }
   }
 }
 
@@ -174,6 +186,8 @@ struct SortExchange_ {
   void* rows_in = nullptr;   // requester side received rows
   size_t cap_ids = 0, cap_src = 0, cap_recv = 0, cap_rows_out = 0, cap_rows_in = 0;
   std::vector<uint8_t> h_send, h_recv;  // host transport staging
+  int64_t* h_pin = nullptr;  // pinned [4 world + 1]: own counts, peer counts, offsets, error flag
+  int64_t* d_xc = nullptr;   // device [2 world]: counts message out / in (NCCL transport)
 
   template <class T>
   void grow(T*& p, size_t& cap, size_t n) {
@@ -215,14 +229,15 @@ struct SortExchange_ {
     std::vector<int64_t> send(world), recv(world);
     for (int p = 0; p < world; ++p) send[p] = bad ? -1 : mine[p];
     std::vector<int64_t> b8(world, 8);
-    if (comm) {
-      int64_t* d = nullptr;
-      xck(cudaMallocAsync(reinterpret_cast<void**>(&d), 16 * world, st), "counts buffer");
-      xck(cudaMemcpyAsync(d, send.data(), 8 * world, cudaMemcpyHostToDevice, st), "counts h2d");
-      alltoallv(d, b8, d + world, b8, st);
-      xck(cudaMemcpyAsync(recv.data(), d + world, 8 * world, cudaMemcpyDeviceToHost, st), "counts d2h");
-      xck(cudaFreeAsync(d, st), "counts free");
+    if (comm) {  // through a persistent device buffer and pinned host memory (no pageable staging)
+      if (!d_xc) xck(cudaMalloc(reinterpret_cast<void**>(&d_xc), 16 * world), "counts buffer");
+      int64_t* hp = h_pin + world;
+      std::memcpy(hp, send.data(), 8 * world);
+      xck(cudaMemcpyAsync(d_xc, hp, 8 * world, cudaMemcpyHostToDevice, st), "counts h2d");
+      alltoallv(d_xc, b8, d_xc + world, b8, st);
+      xck(cudaMemcpyAsync(hp, d_xc + world, 8 * world, cudaMemcpyDeviceToHost, st), "counts d2h");
       xck(cudaStreamSynchronize(st), "counts sync");
+      std::memcpy(recv.data(), hp, 8 * world);
     } else {
       if (host_fn(host_ctx, send.data(), b8.data(), recv.data(), b8.data(), world) != 0)
         throw std::runtime_error("exchange: host all-to-all callback failed");
@@ -237,6 +252,8 @@ struct SortExchange_ {
                     static_cast<void*>(send_ids), static_cast<void*>(src), static_cast<void*>(recv_ids), rows_out,
                     rows_in})
       if (p) cudaFree(p);
+    if (d_xc) cudaFree(d_xc);
+    if (h_pin) cudaFreeHost(h_pin);
     if (comm) nccl().CommDestroy(comm);
   }
 };
@@ -315,6 +332,8 @@ int sort_exchange_lookup(SortExchange x, const void* shard, int64_t rows_per_ran
       x->grow(x->d_counts, c0, sizeof(int64_t) * 2 * W);
       x->grow(x->d_cursor, c1, sizeof(unsigned long long) * W);
       x->grow(x->d_err, c2, sizeof(int32_t));
+      xck(cudaHostAlloc(reinterpret_cast<void**>(&x->h_pin), sizeof(int64_t) * (4 * W + 1), cudaHostAllocDefault),
+          "pinned counts");
     }
     // ---- 1. count ids per owner (+ range flag)
     xck(cudaMemsetAsync(x->d_counts, 0, sizeof(int64_t) * W, st), "memset");
@@ -322,11 +341,13 @@ int sort_exchange_lookup(SortExchange x, const void* shard, int64_t rows_per_ran
     xck(cudaMemsetAsync(x->d_err, 0, sizeof(int32_t), st), "memset");
     if (n) k_xchg_count<<<grid_for(n), 256, 0, st>>>(ids, n, rows_per_rank, W, x->d_counts, x->d_err);
     xck(cudaGetLastError(), "exchange count");
-    std::vector<int64_t> sc_ids(W);
-    int32_t herr = 0;
-    xck(cudaMemcpyAsync(sc_ids.data(), x->d_counts, sizeof(int64_t) * W, cudaMemcpyDeviceToHost, st), "d2h");
-    xck(cudaMemcpyAsync(&herr, x->d_err, sizeof(int32_t), cudaMemcpyDeviceToHost, st), "d2h");
+    int64_t* hp = x->h_pin;  // [0, W): own counts; [4W]: error flag (pinned: truly async copies)
+    hp[4 * W] = 0;
+    xck(cudaMemcpyAsync(hp, x->d_counts, sizeof(int64_t) * W, cudaMemcpyDeviceToHost, st), "d2h");
+    xck(cudaMemcpyAsync(hp + 4 * W, x->d_err, sizeof(int32_t), cudaMemcpyDeviceToHost, st), "d2h");
     xck(cudaStreamSynchronize(st), "sync");
+    const std::vector<int64_t> sc_ids(hp, hp + W);
+    const int32_t herr = static_cast<int32_t>(hp[4 * W] & 0xffffffff);
     // ---- 2. agree on the error flag, learn how many ids every peer will ask this rank for
     bool any_bad = false;
     const std::vector<int64_t> rc_ids = x->exchange_counts(sc_ids, herr != 0, any_bad, st);
@@ -340,7 +361,8 @@ int sort_exchange_lookup(SortExchange x, const void* shard, int64_t rows_per_ran
     for (int p = 0; p < W; ++p) n_recv += rc_ids[p];
     x->grow(x->send_ids, x->cap_ids, sizeof(int32_t) * std::max<int64_t>(n, 1));
     x->grow(x->src, x->cap_src, sizeof(int64_t) * std::max<int64_t>(n, 1));
-    xck(cudaMemcpyAsync(x->d_counts + W, off.data(), sizeof(int64_t) * W, cudaMemcpyHostToDevice, st), "h2d");
+    std::memcpy(hp + 2 * W, off.data(), sizeof(int64_t) * W);
+    xck(cudaMemcpyAsync(x->d_counts + W, hp + 2 * W, sizeof(int64_t) * W, cudaMemcpyHostToDevice, st), "h2d");
     if (n)
       k_xchg_scatter<<<grid_for(n), 256, 0, st>>>(ids, n, rows_per_rank, x->d_counts + W, x->d_cursor, x->send_ids,
                                                    x->src);
