@@ -43,12 +43,15 @@ struct BwdSmem {
   static constexpr uint32_t oX = 0;                          // [2 items][2 tiles]
   static constexpr uint32_t oY = oX + 4 * kXs;               // [kBwdStages][2 tiles]
   static constexpr uint32_t oBar = oY + 2 * kBwdStages * kYs;
-  static constexpr uint32_t oTiles = oBar + 32 * 8;
+  static constexpr uint32_t oStat = oBar + 32 * 8;    // [8 warps][lse 32 | D 32] fp32 (pass 1)
+  static constexpr uint32_t oTiles = oStat + 8 * 256;
   static constexpr uint32_t bytes(int n_tile_ints) { return oTiles + 4u * n_tile_ints + 1024; }
 };
 
 struct AttnBwdTcArgs {
   const int4* rowmeta;       // [Rq] compact mask rows of the query rows (kv index space)
+  const int4* kvmeta;        // pass 1 (optional): per kv row the query rows that see it, as two
+                             // intervals {lo1, hi1, lo2, hi2} (the transposed compact mask)
   const int32_t* x_off;      // [nX + 1] CSR: X block -> its Y steps
   const int2* y_code;        // {Y block (64 rows), chunk classes (2 bits per (quarter, half))}
   const float* lse;          // [BH, Rq] log2-domain
@@ -230,6 +233,10 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
           D_r = a.D[static_cast<size_t>(bh) * a.Rq + x];
         }
       }
+      int4 kvm = make_int4(0, -1, 0, -1);  // pass 1: query rows seeing this thread's kv row x
+      if constexpr (!kDQ) {
+        if (a.kvmeta && x < a.Rkv) kvm = a.kvmeta[x];
+      }
       const float* lse_bh = a.lse + static_cast<size_t>(bh) * a.Rq;
       const float* D_bh = a.D + static_cast<size_t>(bh) * a.Rq;
       const int j0 = s_off[xb], j1 = s_off[xb + 1];
@@ -247,7 +254,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
           if (cls != 2u && c < a.Rq) {
             lse_l = __ldg(lse_bh + c);
             D_l = __ldg(D_bh + c);
-            if (cls != 1u) m_l = __ldg(a.rowmeta + c);
+            if (cls != 1u && !a.kvmeta) m_l = __ldg(a.rowmeta + c);
           }
         }
         mbar_wait(s_full, g & 1);
@@ -273,6 +280,34 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
             p1 = (bits >> (2 * i + 1)) & 1u ? p1 : 0.f;
             wp[i] = pack_bf16x2(p0 * (__uint_as_float(pv[2 * i]) - D_r), p1 * (__uint_as_float(pv[2 * i + 1]) - D_r));
           }
+        } else if (a.kvmeta) {
+          // column c = query row: its lse / D are warp-uniform; broadcast from this warp's shared
+          // slot four columns per LDS.128, the mask from the thread's own transposed rows
+          float* st = reinterpret_cast<float*>(smem + S::oStat) + (warp - 2) * 64;
+          st[lane] = lse_l;
+          st[32 + lane] = D_l;
+          __syncwarp();
+          const uint32_t bits = cls == 1u ? 0xffffffffu
+                                          : (chunk_vis_bits(c0, kvm.x, kvm.y, -1) | chunk_vis_bits(c0, kvm.z, kvm.w, -1));
+          const uint32_t sl_a = smem_u32(st), sd_a = sl_a + 128;
+#pragma unroll
+          for (int i = 0; i < 32; i += 4) {
+            const float4 l4 = lds_f32x4(sl_a + 4 * i), d4 = lds_f32x4(sd_a + 4 * i);
+            const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv[4] = {d4.x, d4.y, d4.z, d4.w};
+            float pp[4], dd[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              float p = ex2_approx(fmaf(__uint_as_float(sv[i + e]), sl2, -lv[e]));
+              p = (bits >> (i + e)) & 1u ? p : 0.f;
+              pp[e] = p;
+              dd[e] = p * (__uint_as_float(pv[i + e]) - dv[e]);
+            }
+            wp[i >> 1] = pack_bf16x2(pp[0], pp[1]);
+            wp[(i >> 1) + 1] = pack_bf16x2(pp[2], pp[3]);
+            wd[i >> 1] = pack_bf16x2(dd[0], dd[1]);
+            wd[(i >> 1) + 1] = pack_bf16x2(dd[2], dd[3]);
+          }
+          __syncwarp();  // the slot is rewritten at the next step
         } else {
           // column c = query row: lse, D (and for mixed chunks its mask row) are warp-uniform
 #pragma unroll

@@ -150,6 +150,7 @@ struct Handle {
     int2 *tc_kv_code = nullptr, *tc_q_code = nullptr;
     int tc_kv_n = 0, tc_q_n = 0;
     CUtensorMap tmQ64, tmK64, tmV64, tmDO128, tmDO64;
+    int4* kvmeta = nullptr;  // transposed compact mask (pass 1), null if not two-interval
   };
   std::vector<TrainLayer> tl;
   const TrainLayer* save_to = nullptr;  // training forward: QKVG writes straight into these buffers
@@ -1502,6 +1503,35 @@ static void train_layer_buffers(Handle& h, const LayerPlan& lp, const LayerDev& 
     T.tc_q_code = h.upload(code);
     T.tc_q_n = static_cast<int>(code.size());
   }
+  {  // per kv row x the query rows that see it; kept when every row's set is <= 2 intervals
+    std::vector<std::vector<int32_t>> seen(static_cast<size_t>(lp.l_kv));
+    for (int r = 0; r < lp.l_q; ++r) {
+      for (int c = std::max(lp.lo[r], 0); c <= lp.hi[r] && c < lp.l_kv; ++c) seen[c].push_back(r);
+      if (lp.self_idx[r] >= 0 && (lp.self_idx[r] < lp.lo[r] || lp.self_idx[r] > lp.hi[r]))
+        seen[lp.self_idx[r]].push_back(r);
+    }
+    std::vector<int4> km(static_cast<size_t>(lp.l_kv), make_int4(0, -1, 0, -1));
+    bool ok = true;
+    for (int x = 0; x < lp.l_kv && ok; ++x) {
+      auto& v = seen[x];
+      std::sort(v.begin(), v.end());
+      int runs = 0;
+      for (size_t i = 0; i < v.size() && ok; ++i) {
+        if (i > 0 && v[i] == v[i - 1] + 1) {
+          (runs == 1 ? km[x].y : km[x].w) = v[i];
+          continue;
+        }
+        if (++runs > 2) {
+          ok = false;
+        } else if (runs == 1) {
+          km[x].x = km[x].y = v[i];
+        } else {
+          km[x].z = km[x].w = v[i];
+        }
+      }
+    }
+    if (ok) T.kvmeta = h.upload(km);
+  }
   std::vector<int32_t> qo, ko;
   std::vector<int2> qi, ki;
   build_bwd_lists(lp, qo, qi, ko, ki);
@@ -1655,6 +1685,7 @@ static void attn_core_backward_tc(Handle& h, const LayerDev& L, const Handle::Tr
   const int H = h.H, dk = h.dk;
   AttnBwdTcArgs tb;
   tb.rowmeta = L.rowmeta;
+  tb.kvmeta = T.kvmeta;
   tb.lse = T.lse;
   tb.D = Dd;
   tb.BH = B * H;
@@ -1683,6 +1714,7 @@ static void attn_core_backward_tc(Handle& h, const LayerDev& L, const Handle::Tr
     tb.y_code = T.tc_q_code;                                                                           \
     tb.nX = (L.Rq + 127) / 128;                                                                        \
     tb.out0 = dQ;                                                                                      \
+    tb.kvmeta = nullptr;                                                                               \
     tb.out1 = nullptr;                                                                                 \
     tb.out1_16 = nullptr;                                                                              \
     launch_tc(k_attn_bwd_tc<DKV, true>, T.tmQ, T.tmDO128, T.tmK64, T.tmV64,                            \
