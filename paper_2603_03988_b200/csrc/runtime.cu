@@ -128,6 +128,9 @@ struct Handle {
   float* splitk_ws = nullptr;  // split-K partials of the streaming GEMM
   size_t splitk_cap = 0;
   std::map<std::string, std::pair<__nv_bfloat16*, size_t>> tw16;  // training: bf16 weights of the FFN backward
+  CastSeg* tw16_segs = nullptr;  // device list of the tw16 casts (k_cast_segs)
+  int tw16_nseg = 0;
+  size_t tw16_nmax = 0;
   std::map<std::string, std::pair<size_t, std::pair<int64_t, int64_t>>> grad_index;  // offset, shape
   float* grads = nullptr;
   float* master = nullptr;                 // fp32 master parameters (grad_index layout)
@@ -2286,9 +2289,21 @@ static void repack_weights(Handle& h) {
       CK(cudaStreamSynchronize(h.stream));
     }
   }
-  for (auto& kv : h.tw16)  // bf16 copies the training backward reads
-    k_f32_to_bf16<<<ew_grid(kv.second.second), 256, 0, h.stream>>>(w32(h, kv.first), kv.second.second,
-                                                                   kv.second.first);
+  if (!h.tw16.empty()) {  // bf16 copies the training backward reads, one launch for all
+    if (h.tw16_nseg != static_cast<int>(h.tw16.size())) {
+      std::vector<CastSeg> segs;
+      size_t nmax = 0;
+      for (auto& kv : h.tw16) {
+        segs.push_back(CastSeg{w32(h, kv.first), kv.second.first, kv.second.second});
+        nmax = std::max(nmax, kv.second.second);
+      }
+      h.tw16_segs = h.upload(segs);
+      h.tw16_nseg = static_cast<int>(segs.size());
+      h.tw16_nmax = nmax;
+    }
+    k_cast_segs<<<dim3(static_cast<unsigned>(std::min<size_t>((h.tw16_nmax + 255) / 256, 64)), h.tw16_nseg), 256, 0,
+                  h.stream>>>(h.tw16_segs);
+  }
   check_launch("weight repack");
   h.w16.clear();  // generic-path bf16 copies are rebuilt on next use
 }

@@ -1126,6 +1126,20 @@ __global__ void k_concat_gu(const float* __restrict__ wg, const float* __restric
     out[i] = c < m ? wg[r * m + c] : wu[r * m + c - m];
   }
 }
+// Many fp32 -> bf16 casts in one launch (the training GEMMs' bf16 weight copies refreshed after
+// every optimizer step: ~30 tensors that were one launch each). blockIdx.y = segment.
+struct CastSeg {
+  const float* src;
+  __nv_bfloat16* dst;
+  size_t n;
+};
+__global__ void k_cast_segs(const CastSeg* __restrict__ segs) {
+  const CastSeg sg = segs[blockIdx.y];
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < sg.n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    sg.dst[i] = __float2bfloat16_rn(sg.src[i]);
+}
+
 __global__ void k_cast_bf16(const float* __restrict__ x, size_t n, __nv_bfloat16* __restrict__ y) {
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x)
