@@ -164,8 +164,14 @@ __global__ void __launch_bounds__(kGsThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t idesc = (kTf32 ? umma_idesc_tf32(kGsBM, kGsBN) : umma_idesc_bf16(kGsBM, kGsBN)) |
-                             (kAMN ? (1u << 15) : 0u) | (kBMN ? (1u << 16) : 0u);
+      // the last n block of a narrow product (N - (num_n - 1) kGsBN < kGsBN, e.g. the N = 32
+      // item-width GEMMs of the pre-training backward) runs MMAs of just its width
+      const uint32_t major = (kAMN ? (1u << 15) : 0u) | (kBMN ? (1u << 16) : 0u);
+      const int n_last = N - (num_n - 1) * kGsBN;  // a multiple of 32 (epilogue chunk)
+      const uint32_t idesc_full = (kTf32 ? umma_idesc_tf32(kGsBM, kGsBN) : umma_idesc_bf16(kGsBM, kGsBN)) | major;
+      const uint32_t idesc_last =
+          (kTf32 ? umma_idesc_tf32(kGsBM, static_cast<uint32_t>(n_last)) : umma_idesc_bf16(kGsBM, static_cast<uint32_t>(n_last))) |
+          major;
       constexpr uint32_t kBox = BK * 128;
       int s = 0, i = 0;
       uint32_t ph = 0;
@@ -174,6 +180,7 @@ __global__ void __launch_bounds__(kGsThreads, 1)
         decode(t, ks, mb, nb);
         const int kb0 = ks * kb_per, kb1 = min(num_k, kb0 + kb_per);
         const int acc = i & 1;
+        const uint32_t idesc = nb == num_n - 1 ? idesc_last : idesc_full;
         mbar_wait_sleep(&tempty[acc], ((i >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * 256;
