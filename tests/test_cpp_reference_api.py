@@ -97,13 +97,17 @@ def _rel(a, b):
 
 
 @pytest.mark.gpu
-def test_reference_caller_vs_oracle(tmp_path):
+@pytest.mark.parametrize("which", ["tiny", "base_widths"])
+def test_reference_caller_vs_oracle(tmp_path, which):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
-    cfg = tiny_config()
+    from paper_2603_03988_b200.config import base_config
+    # tiny: d = 64, 4 heads (dk 16); base_widths: SORT-base's d = 256, 8 heads (dk 32), W = 256,
+    # F = 128 with a 300-event history so the fp64 oracle stays fast
+    cfg = tiny_config() if which == "tiny" else base_config(n_hist=300, n_cand=16, n_items=20000)
     P = synth.make_params(cfg, seed=11)
     b = synth.make_batch(cfg, 1, seed=12)
-    keep = 100
+    keep = 100 if which == "tiny" else 160
     om = O.OracleModel(cfg, P)
     tk = om.tokenize(b, 0)
     roles, pos = tk["roles"], tk["position_ids"]

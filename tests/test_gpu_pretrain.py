@@ -86,8 +86,11 @@ GRAD_COS = 0.995
 LOSS_REL = 1e-2
 
 
-def test_pretrain_backward_vs_oracle():
-    cfg = small(n_items=2048, n_hist=96)
+@pytest.mark.parametrize("which", ["small", "base_widths"])
+def test_pretrain_backward_vs_oracle(which):
+    # base_widths: the SORT-base block stack (d = 256, 8 heads, m = 640) over 128 clicks with a
+    # 16,384-item tied head
+    cfg = small(n_items=2048, n_hist=96) if which == "small" else pretrain_config(batch=2, n_hist=128, n_items=16384)
     B = 2
     P = synth.make_params(cfg, seed=51)
     Pr = {k: synth.bf16_round(v).astype(np.float64) for k, v in P.items()}
