@@ -13,6 +13,7 @@
 //   way attention folds QK^T without materialising it.
 #pragma once
 
+#include "attention.cuh"
 #include "train.cuh"
 
 namespace sortk {
@@ -247,6 +248,187 @@ __global__ void __launch_bounds__(kCeThreads) k_ce_tied(const __nv_bfloat16* __r
       if (t < n) lse[static_cast<size_t>(b) * n + t] = m[i] + log2f(s[i]) * 0.6931471805599453f;
     }
   }
+}
+
+// ---------------------------------------------------------------- tcgen05 log-sum-exp
+// lse_t over the full vocabulary on tcgen05 (the k_attention skeleton without P V): a work item
+// = (128-row block of hp, vocabulary chunk of kCeChunk items); per 128-item tile the MMA warp
+// computes Z = hp_blk E_tile^T (two N = 64 halves, K = 32) into one of two TMEM buffers while
+// the 8 softmax warps fold the other buffer into a per-(row, half) online (max, sum) in the
+// log2 domain (no P is written back and nothing else is read from TMEM). Each (row, chunk,
+// half) leaves a partial; k_ce_combine merges them in a fixed order.
+constexpr int kCeChunk = 8192;
+constexpr int kCeStages = 4;
+struct CeTcSmem {
+  static constexpr uint32_t kTile = 128 * kPreK * 2;  // 8 KB: 128 rows x 32 bf16
+  static constexpr uint32_t oH = 0;                    // [2] hp tiles
+  static constexpr uint32_t oE = oH + 2 * kTile;       // [kCeStages] item tiles
+  static constexpr uint32_t oBar = oE + kCeStages * kTile;
+  static constexpr uint32_t bytes = oBar + 32 * 8 + 1024;
+};
+struct CeTcArgs {
+  int T, V, n_chunks, n_items;
+  float2* part;  // [T][n_chunks][2] (max, sum) in the log2 domain
+};
+
+__global__ void __launch_bounds__(kAttnThreads, 2) k_ce_tc(const __grid_constant__ CUtensorMap tmH,
+                                                            const __grid_constant__ CUtensorMap tmE,
+                                                            const CeTcArgs a) {
+  using S = CeTcSmem;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align_smem_1k(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S::oBar);
+  uint64_t* h_full = bars + 0;   // [2]
+  uint64_t* h_empty = bars + 2;  // [2]
+  uint64_t* s_full = bars + 4;   // [2 buffers][2 halves]
+  uint64_t* s_free = bars + 8;   // [2 buffers] (256: every softmax thread has loaded its half)
+  uint64_t* e_full = bars + 10;  // [kCeStages]
+  uint64_t* e_empty = e_full + kCeStages;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(e_empty + kCeStages);
+  const int warp = warp_id(), lane = lane_id();
+  const int tiles_per_chunk = kCeChunk / 128;
+  auto n_tiles_of = [&](int it) {
+    const int ch = it % a.n_chunks;
+    const int items = min(kCeChunk, a.V - ch * kCeChunk);
+    return (items + 127) / 128;
+  };
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmH);
+    tma_prefetch_desc(&tmE);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&h_full[i], 1);
+      mbar_init(&h_empty[i], 1);
+      mbar_init(&s_full[2 * i], 1);
+      mbar_init(&s_full[2 * i + 1], 1);
+      mbar_init(&s_free[i], 256);
+    }
+    for (int i = 0; i < kCeStages; ++i) {
+      mbar_init(&e_full[i], 1);
+      mbar_init(&e_empty[i], 1);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 1) tmem_alloc(tslot, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer
+      int g = 0, li = 0;
+      for (int it = blockIdx.x; it < a.n_items; it += gridDim.x, ++li) {
+        const int rb = it / a.n_chunks, ch = it % a.n_chunks, n_t = n_tiles_of(it);
+        const int hs = li & 1;
+        mbar_wait_sleep(&h_empty[hs], ((li >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&h_full[hs], S::kTile);
+        tma_load_2d(smem + S::oH + hs * S::kTile, &tmH, &h_full[hs], 0, rb * 128);
+        for (int j = 0; j < n_t; ++j, ++g) {
+          const int st = g % kCeStages;
+          mbar_wait_sleep(&e_empty[st], ((g / kCeStages) & 1) ^ 1);
+          mbar_arrive_expect_tx(&e_full[st], S::kTile);
+          tma_load_2d(smem + S::oE + st * S::kTile, &tmE, &e_full[st], 0, ch * kCeChunk + j * 128);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      const uint32_t id_s = umma_idesc_bf16(128, 64);
+      constexpr uint32_t sw = kPreK * 2;  // 64-byte rows
+      int g = 0, li = 0;
+      for (int it = blockIdx.x; it < a.n_items; it += gridDim.x, ++li) {
+        const int n_t = n_tiles_of(it), hs = li & 1;
+        mbar_wait(&h_full[hs], (li >> 1) & 1);
+        const uint32_t sh = smem_u32(smem + S::oH + hs * S::kTile);
+        for (int j = 0; j < n_t; ++j, ++g) {
+          const int buf = g & 1, st = g % kCeStages;
+          if (g >= 2) mbar_wait(&s_free[buf], ((g >> 1) - 1) & 1);
+          mbar_wait(&e_full[st], (g / kCeStages) & 1);
+          tc_fence_after();
+          const uint32_t se = smem_u32(smem + S::oE + st * S::kTile);
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+#pragma unroll
+            for (int k = 0; k < kPreK / 16; ++k)
+              mma_bf16_ss(tmem + buf * 128 + hf * 64, umma_sdesc_kmajor(sh + k * 32, sw),
+                          umma_sdesc_kmajor(se + hf * 64 * kPreK * 2 + k * 32, sw), id_s, k > 0 ? 1u : 0u);
+            mma_commit(&s_full[buf * 2 + hf]);
+          }
+          mma_commit(&e_empty[st]);
+          if (j == n_t - 1) mma_commit(&h_empty[hs]);
+        }
+      }
+    }
+  } else {  // softmax warps: warp pair (w, w + 4) shares lane quarter w % 4, half = which pair
+    const int quarter = warp & 3, hf = (warp - 2) >> 2;
+    const int r = quarter * 32 + lane;
+    const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+    constexpr float kLog2e = 1.4426950408889634f;
+    const float NEG_INF = -__int_as_float(0x7f800000);
+    int g = 0;
+    (void)tiles_per_chunk;
+    for (int it = blockIdx.x; it < a.n_items; it += gridDim.x) {
+      const int rb = it / a.n_chunks, ch = it % a.n_chunks, n_t = n_tiles_of(it);
+      float m2 = NEG_INF;  // running max (log2 units) of this row's half
+      float2 sacc = make_float2(0.f, 0.f);
+      for (int j = 0; j < n_t; ++j, ++g) {
+        const int buf = g & 1;
+        const int c0 = ch * kCeChunk + j * 128 + hf * 64;  // first item of this half
+        mbar_wait_sleep(&s_full[buf * 2 + hf], (g >> 1) & 1);
+        tc_fence_after();
+        uint32_t z[64];
+        tmem_ld_32x32b_x32(tmem + buf * 128 + hf * 64 + lane_off, *reinterpret_cast<uint32_t(*)[32]>(z));
+        tmem_ld_32x32b_x32(tmem + buf * 128 + hf * 64 + 32 + lane_off, *reinterpret_cast<uint32_t(*)[32]>(z + 32));
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&s_free[buf]);
+        if (c0 + 64 > a.V) {  // vocabulary tail
+#pragma unroll
+          for (int i = 0; i < 64; ++i)
+            if (c0 + i >= a.V) z[i] = __float_as_uint(NEG_INF);
+        }
+        float mx[4] = {NEG_INF, NEG_INF, NEG_INF, NEG_INF};
+#pragma unroll
+        for (int i = 0; i < 64; ++i) mx[i & 3] = fmaxf(mx[i & 3], __uint_as_float(z[i]));
+        const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * kLog2e;
+        const float mn = fmaxf(m2, mt);
+        if (mn == NEG_INF) continue;
+        const float alpha = ex2_approx(m2 - mn);  // m2 = -inf -> 0
+        sacc = make_float2(sacc.x * alpha, sacc.y * alpha);
+        const float2 l2 = make_float2(kLog2e, kLog2e), nm = make_float2(-mn, -mn);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float2 x = ffma2(make_float2(__uint_as_float(z[2 * i]), __uint_as_float(z[2 * i + 1])), l2, nm);
+          const float2 e = (i % 3 == 2) ? ex2_poly2(x) : make_float2(ex2_approx(x.x), ex2_approx(x.y));
+          sacc = fadd2(sacc, e);
+        }
+        m2 = mn;
+      }
+      const int row = rb * 128 + r;
+      if (row < a.T) a.part[(static_cast<size_t>(row) * a.n_chunks + ch) * 2 + hf] = make_float2(m2, sacc.x + sacc.y);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 256);
+  }
+}
+
+// lse[b, t] (natural log) of row r = b * L + t, t < n, from its 2 n_chunks partials (fixed order).
+__global__ void k_ce_combine(const float2* __restrict__ part, int T, int L, int n_parts, float* __restrict__ lse) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= T) return;
+  const int b = r / L, t = r - b * L, n = L - 1;
+  if (t >= n) return;
+  const float2* p = part + static_cast<size_t>(r) * n_parts;
+  float m = -__int_as_float(0x7f800000);
+  for (int i = 0; i < n_parts; ++i) m = fmaxf(m, p[i].x);
+  float s = 0.f;
+  for (int i = 0; i < n_parts; ++i)
+    if (p[i].x != -__int_as_float(0x7f800000)) s += p[i].y * exp2f(p[i].x - m);
+  lse[static_cast<size_t>(b) * n + t] = (m + log2f(s)) * 0.6931471805599453f;
 }
 
 // ---------------------------------------------------------------- backward

@@ -110,6 +110,9 @@ struct Handle {
   // ---- pre-training head
   const float* pre_proj = nullptr;  // pretrain.proj [d, item_dim] in the master buffer
   __nv_bfloat16* pre_hp = nullptr;  // projected rows [B * L, item_dim]
+  bool ce_tc = true;  // sort_set_option("ce_tc"): tied-head log-sum-exp on tcgen05 (0: mma.sync k_ce_tied)
+  float2* ce_part = nullptr;  // k_ce_tc partials
+  size_t ce_part_cap = 0;
   float *pre_lse = nullptr, *pre_tgt = nullptr;  // [B, n_hist]
   __nv_bfloat16* pre_P = nullptr;   // training: dL/dz [B * L, V] bf16 (recomputed logits' gradient)
   float *pre_dh = nullptr, *pre_loss = nullptr;  // dL/d(hp) [B * L, item_dim], the step's loss
@@ -2357,7 +2360,28 @@ static void forward_device(Handle& h, int B) {
     const int V = h.item_ext ? static_cast<int>(h.item_ext_rows) : h.cfg.n_items;
     k_pretrain_proj<<<std::max(1, std::min((T + 7) / 8, 8 * h.num_sms)), 256, psmem, h.stream>>>(
         h.X[last.q_buf], T, h.L0, h.d, h.head_gain, h.pre_proj, items, h.in_item, h.pre_hp, h.pre_tgt);
-    k_ce_tied<<<(T + kCeRows - 1) / kCeRows, kCeThreads, 0, h.stream>>>(h.pre_hp, T, h.L0, items, V, h.pre_lse);
+    if (h.ce_tc) {  // tcgen05 logits + online log-sum-exp, partials per vocabulary chunk
+      const int n_chunks = (V + kCeChunk - 1) / kCeChunk;
+      const size_t need = static_cast<size_t>(h.Bmax) * h.L0 * n_chunks * 2;
+      if (need > h.ce_part_cap) {
+        h.ce_part = h.dalloc<float2>(need);
+        h.ce_part_cap = need;
+      }
+      CeTcArgs ca;
+      ca.T = T;
+      ca.V = V;
+      ca.n_chunks = n_chunks;
+      ca.n_items = ((T + 127) / 128) * n_chunks;
+      ca.part = h.ce_part;
+      const CUtensorMap tmH = make_tmap_2d(h.pre_hp, static_cast<uint64_t>(T), kPreK, kPreK, 128, kPreK, kPreK * 2);
+      const CUtensorMap tmE = make_tmap_2d(items, static_cast<uint64_t>(V), kPreK, kPreK, 128, kPreK, kPreK * 2);
+      ensure_smem(k_ce_tc, CeTcSmem::bytes);
+      k_ce_tc<<<std::min(ca.n_items, 2 * h.num_sms), kAttnThreads, CeTcSmem::bytes, h.stream>>>(tmH, tmE, ca);
+      k_ce_combine<<<(T + 255) / 256, 256, 0, h.stream>>>(h.ce_part, T, h.L0, 2 * n_chunks, h.pre_lse);
+      h.launches += 1;
+    } else {
+      k_ce_tied<<<(T + kCeRows - 1) / kCeRows, kCeThreads, 0, h.stream>>>(h.pre_hp, T, h.L0, items, V, h.pre_lse);
+    }
     check_launch("pretrain head");
     h.launches += 2;
     stage_mark(h, "head");
@@ -3290,6 +3314,8 @@ int sort_set_option(SortHandle p, const char* name, int32_t value) {
       h->tail_pair = value != 0;
     } else if (std::strcmp(name, "attn_bwd_mma") == 0) {
       h->attn_bwd_mma = value != 0;
+    } else if (std::strcmp(name, "ce_tc") == 0) {
+      h->ce_tc = value != 0;
     } else if (std::strcmp(name, "attn_prescale") == 0) {
       h->attn_prescale = value != 0;
     } else if (std::strcmp(name, "qkvg_pair") == 0) {
