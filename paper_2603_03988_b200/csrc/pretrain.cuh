@@ -250,6 +250,65 @@ __global__ void __launch_bounds__(kCeThreads) k_ce_tied(const __nv_bfloat16* __r
   }
 }
 
+// ---------------------------------------------------------------- tcgen05 projection
+// hp = RMSN(x; final_norm.gain) . proj on the streaming tcgen05 GEMM: the gain folds into the
+// weight (W' = diag(g) proj, bf16 [K-major: 32 x d]) and 1/rms comes from the row statistics the
+// last block tail wrote (sum of squares of the bf16 row), as everywhere else in the forward.
+// The epilogue (one 32-column chunk = the whole row) writes hp in bf16 and the target logit
+// from the bf16 hp and the target's item row (k_pretrain_proj's rounding points).
+__global__ void k_pretrain_wfold(const float* __restrict__ proj, const float* __restrict__ gain, int d,
+                                 __nv_bfloat16* __restrict__ wt) {  // wt[j][c] = g[c] proj[c][j]
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < kPreK * d; i += gridDim.x * blockDim.x) {
+    const int j = i / d, c = i - j * d;
+    wt[i] = __float2bfloat16_rn(gain[c] * proj[static_cast<size_t>(c) * kPreK + j]);
+  }
+}
+
+struct GsPretrainHead {
+  static constexpr int kChunk = 32;
+  const float4* ss;  // [T] row sum-of-squares partials of x
+  float inv_d;
+  __nv_bfloat16* hp;              // [T, 32]
+  const __nv_bfloat16* items;     // [V, 32]
+  const int32_t* click;           // [B, n]
+  float* tgt;                     // [B, n]
+  int L, n;
+  __device__ void apply(int row, int col, const float (&v)[32]) const {
+    (void)col;
+    const float4 sp = ss[row];
+    const float inv = rsqrtf(((sp.x + sp.y) + (sp.z + sp.w)) * inv_d + 1e-6f);  // norm.hpp:23-24
+    uint32_t w[16];
+    float hb[32];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      w[i] = pack_bf16x2(v[2 * i] * inv, v[2 * i + 1] * inv);
+      const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
+      hb[2 * i] = f.x;
+      hb[2 * i + 1] = f.y;
+    }
+    __nv_bfloat16* dst = hp + static_cast<size_t>(row) * kPreK;
+    stg256(dst, *reinterpret_cast<const uint32_t(*)[8]>(w));
+    stg256(dst + 16, *reinterpret_cast<const uint32_t(*)[8]>(w + 8));
+    const int b = row / L, t = row - b * L;
+    if (t < n) {  // position t predicts click t
+      const int item = click[static_cast<size_t>(b) * n + t];
+      const int4* er = reinterpret_cast<const int4*>(items + static_cast<size_t>(item) * kPreK);
+      float z = 0.f;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int4 e4 = er[q];
+        const __nv_bfloat162* e2 = reinterpret_cast<const __nv_bfloat162*>(&e4);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 f = __bfloat1622float2(e2[k]);
+          z = fmaf(hb[8 * q + 2 * k], f.x, fmaf(hb[8 * q + 2 * k + 1], f.y, z));
+        }
+      }
+      tgt[static_cast<size_t>(b) * n + t] = z;
+    }
+  }
+};
+
 // ---------------------------------------------------------------- tcgen05 log-sum-exp
 // lse_t over the full vocabulary on tcgen05 (the k_attention skeleton without P V): a work item
 // = (128-row block of hp, vocabulary chunk of kCeChunk items); per 128-item tile the MMA warp

@@ -110,6 +110,8 @@ struct Handle {
   // ---- pre-training head
   const float* pre_proj = nullptr;  // pretrain.proj [d, item_dim] in the master buffer
   __nv_bfloat16* pre_hp = nullptr;  // projected rows [B * L, item_dim]
+  bool pre_proj_tc = true;  // sort_set_option("pre_proj_tc"): pre-training projection on tcgen05
+  __nv_bfloat16* pre_wt = nullptr;  // diag(final_norm.gain) . pretrain.proj, K-major bf16 [32, d]
   bool ce_tc = true;  // sort_set_option("ce_tc"): tied-head log-sum-exp on tcgen05 (0: mma.sync k_ce_tied)
   float2* ce_part = nullptr;  // k_ce_tc partials
   size_t ce_part_cap = 0;
@@ -2358,8 +2360,17 @@ static void forward_device(Handle& h, int B) {
     ensure_smem(k_pretrain_proj, psmem);
     const __nv_bfloat16* items = h.item_ext ? h.item_ext : h.item;
     const int V = h.item_ext ? static_cast<int>(h.item_ext_rows) : h.cfg.n_items;
-    k_pretrain_proj<<<std::max(1, std::min((T + 7) / 8, 8 * h.num_sms)), 256, psmem, h.stream>>>(
-        h.X[last.q_buf], T, h.L0, h.d, h.head_gain, h.pre_proj, items, h.in_item, h.pre_hp, h.pre_tgt);
+    if (h.pre_proj_tc && h.d % 32 == 0) {  // projection + target logit on the streaming tcgen05 GEMM
+      if (!h.pre_wt) h.pre_wt = h.dalloc<__nv_bfloat16>(static_cast<size_t>(kPreK) * h.d);
+      k_pretrain_wfold<<<ew_grid(static_cast<size_t>(kPreK) * h.d), 256, 0, h.stream>>>(h.pre_proj, h.head_gain, h.d,
+                                                                                         h.pre_wt);
+      gemm_stream(h, h.X[last.q_buf], h.d, T, h.d, h.pre_wt, h.d, kPreK,
+                  GsPretrainHead{h.SS[last.q_buf], 1.f / static_cast<float>(h.d), h.pre_hp, items, h.in_item,
+                                 h.pre_tgt, h.L0, h.L0 - 1});
+    } else {
+      k_pretrain_proj<<<std::max(1, std::min((T + 7) / 8, 8 * h.num_sms)), 256, psmem, h.stream>>>(
+          h.X[last.q_buf], T, h.L0, h.d, h.head_gain, h.pre_proj, items, h.in_item, h.pre_hp, h.pre_tgt);
+    }
     if (h.ce_tc) {  // tcgen05 logits + online log-sum-exp, partials per vocabulary chunk
       const int n_chunks = (V + kCeChunk - 1) / kCeChunk;
       const size_t need = static_cast<size_t>(h.Bmax) * h.L0 * n_chunks * 2;
@@ -3314,6 +3325,8 @@ int sort_set_option(SortHandle p, const char* name, int32_t value) {
       h->tail_pair = value != 0;
     } else if (std::strcmp(name, "attn_bwd_mma") == 0) {
       h->attn_bwd_mma = value != 0;
+    } else if (std::strcmp(name, "pre_proj_tc") == 0) {
+      h->pre_proj_tc = value != 0;
     } else if (std::strcmp(name, "ce_tc") == 0) {
       h->ce_tc = value != 0;
     } else if (std::strcmp(name, "attn_prescale") == 0) {
