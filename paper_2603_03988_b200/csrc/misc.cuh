@@ -53,9 +53,9 @@ __global__ void k_gather_table_rows(const int4* __restrict__ table, int64_t n_ro
 // memory in 16-row slices (cp.async, double-buffered) that all 16 warps share, so each CTA
 // reads W1 from L2 once.
 // The 3 logits are reduced across the 32 lanes with shuffles in a fixed order.
-constexpr int kHeadRows = 128;
+constexpr int kHeadRows = 112;  // 147 CTAs for the 16,384 SORT-base candidate rows on 148 SMs (128 left 20 SMs idle)
 constexpr int kHeadPitch = kHeadRows + 4;  // xs row pitch: 4-way (not 32-way) conflicts on the transposed store
-constexpr int kHeadThreads = 512;
+constexpr int kHeadThreads = 448;  // 14 warps x 8 rows
 constexpr int kHeadKSlice = 16;  // W1 rows staged per cp.async slice (double-buffered)
 
 template <int CPT>
