@@ -40,6 +40,14 @@ template <class E, class = void>
 struct gs_split_epi : std::false_type {};
 template <class E>
 struct gs_split_epi<E, std::void_t<decltype(E::kSplit)>> : std::bool_constant<E::kSplit> {};
+// epilogues that finish a row once both column halves of its tile are drained declare
+// `static constexpr bool kRowEnd = true` and `void row_end(int row) const`, called by the
+// half-0 thread of the row after a barrier over the 256 epilogue threads (their global
+// writes to the tile's rows are visible to it)
+template <class E, class = void>
+struct gs_rowend_epi : std::false_type {};
+template <class E>
+struct gs_rowend_epi<E, std::void_t<decltype(E::kRowEnd)>> : std::bool_constant<E::kRowEnd> {};
 
 // UMMA shared-memory descriptor of an MN-major SW128 operand tile (the canonical layout
 // ((8,n),(8,k)):((1,LBO),(8,SBO)) in 16-byte units): 64-element (128-byte) MN atoms of 8-row K
@@ -75,10 +83,14 @@ __device__ __forceinline__ uint64_t umma_sdesc_mnmajor_sw128_32b(uint32_t saddr,
 // the split index and writes a partial that a fixed-order reduction sums (deterministic).
 // T = __nv_bfloat16 (kind::f16, K = 64 per stage) or float (kind::tf32: fp32 operands at TF32
 // precision, K = 32 per stage -- the fp32 ranking head and tokenizer products).
+// a_kwrap > 0: A's K coordinate wraps every a_kwrap k blocks, so A [M, a_kwrap BK] meets a B of
+// K = r a_kwrap BK as [A | A | ...] (the ranking head's split-precision weight pieces, GsHead).
+// a_req_rows > 0: tmA is a 3D view {K, a_req_rows, requests} of rows strided inside a larger
+// activation (the candidate rows of each request); an M block is 128 / a_req_rows requests.
 template <class Epi, bool kAMN = false, bool kBMN = false, class T = __nv_bfloat16>
 __global__ void __launch_bounds__(kGsThreads, 1)
     k_gemm_stream(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                  int K, int k_splits, Epi epi) {
+                  int K, int k_splits, Epi epi, int a_kwrap = 0, int a_req_rows = 0) {
   constexpr bool kTf32 = std::is_same_v<T, float>;
   constexpr int BK = 128 / sizeof(T);   // K per stage: one 128-byte swizzle row
   constexpr int MMA_K = 32 / sizeof(T); // K per instruction (32 bytes)
@@ -141,12 +153,15 @@ __global__ void __launch_bounds__(kGsThreads, 1)
           uint8_t* a_dst = sA + s * kGsABytes;
           uint8_t* b_dst = sB + s * kGsBBytes;
           constexpr uint32_t kBox = BK * 128;  // one {atom MN x BK} MN-major box
+          const int ka = a_kwrap > 0 ? kb % a_kwrap : kb;
           if constexpr (kAMN) {
 #pragma unroll
             for (int i = 0; i < kGsBM / kAtom; ++i)
-              tma_load_2d(a_dst + i * kBox, &tmA, &full[s], mb * kGsBM + kAtom * i, kb * BK);
+              tma_load_2d(a_dst + i * kBox, &tmA, &full[s], mb * kGsBM + kAtom * i, ka * BK);
+          } else if (a_req_rows > 0) {
+            tma_load_3d(a_dst, &tmA, &full[s], ka * BK, 0, mb * (kGsBM / a_req_rows));
           } else {
-            tma_load_2d(a_dst, &tmA, &full[s], kb * BK, mb * kGsBM);
+            tma_load_2d(a_dst, &tmA, &full[s], ka * BK, mb * kGsBM);
           }
           if constexpr (kBMN) {
 #pragma unroll
@@ -246,6 +261,11 @@ __global__ void __launch_bounds__(kGsThreads, 1)
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
+      if constexpr (gs_rowend_epi<Epi>::value) {
+        named_bar_sync(1, 256);
+        if (half == 0 && row < M) epi.row_end(row);
+        named_bar_sync(1, 256);  // the partials are rewritten by the next tile
+      }
     }
   }
   tc_fence_before();

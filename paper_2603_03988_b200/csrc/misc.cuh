@@ -169,4 +169,101 @@ __global__ void __launch_bounds__(kHeadThreads)
   }
 }
 
+
+// ---- The ranking head on the tensor cores (default; `sort_set_option("head_tc", 0)` runs
+// k_head above). Same math: h = relu(x / rms(x) (g . W1) + b1), z = h W2 + b2.
+//   k_gather_cand  candidate rows x[b, R - N + j] (bf16, exact) and their row statistics
+//   k_head_wsplit  Wg = g . W1 (fp32) split into three bf16 pieces hi + mid + lo, which carry all
+//                  24 mantissa bits; stored as B = [hi | mid | lo]^T, [dh, 3d] K-major
+//   k_gemm_stream<GsHead> with A's K coordinate wrapping every d: acc = x hi + x mid + x lo
+//                  = x Wg with every product exact in the fp32 TMEM accumulator -- an fp32
+//                  product up to summation order (the SIMT kernel's xn rounding differs by an ulp)
+//   GsHead         epilogue per 32-column chunk: h = relu(acc inv + b1), z += h W2 in column
+//                  order per 128-column half; row_end: z = half 0 + half 1 + b2, sigmoid
+// A is read in place through a 3D tensor map {d, N, B} (row strides d and R d) when N divides
+// 128; otherwise k_gather_cand first copies the candidate rows.
+__global__ void k_gather_cand(const __nv_bfloat16* __restrict__ src, const float4* __restrict__ ss_src, int R, int N,
+                              int total, int d, __nv_bfloat16* __restrict__ dst, float4* __restrict__ ss_dst) {
+  const int chunks = d >> 3;  // 16-byte vectors per row
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total * chunks; t += gridDim.x * blockDim.x) {
+    const int e = t / chunks, c = t - e * chunks;
+    const int b = e / N, j = e - b * N;
+    const size_t row = static_cast<size_t>(b) * R + (R - N) + j;
+    reinterpret_cast<int4*>(dst)[static_cast<size_t>(e) * chunks + c] =
+        __ldg(reinterpret_cast<const int4*>(src + row * d) + c);
+    if (c == 0) ss_dst[e] = ss_src[row];
+  }
+}
+
+__global__ void k_head_wsplit(const float* __restrict__ w1, const float* __restrict__ gain, int d, int dh,
+                              __nv_bfloat16* __restrict__ wt) {  // wt[n][p d + k] = piece p of g[k] w1[k][n]
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d * dh; i += gridDim.x * blockDim.x) {
+    const int n = i / d, k = i - n * d;
+    const float w = gain[k] * w1[static_cast<size_t>(k) * dh + n];
+    const __nv_bfloat16 hi = __float2bfloat16_rn(w);
+    const float r1 = w - __bfloat162float(hi);  // exact (Sterbenz)
+    const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+    const __nv_bfloat16 lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+    __nv_bfloat16* row = wt + static_cast<size_t>(n) * 3 * d;
+    row[k] = hi;
+    row[d + k] = mid;
+    row[2 * d + k] = lo;
+  }
+}
+
+struct GsHead {
+  static constexpr int kChunk = 32;
+  static constexpr bool kRowEnd = true;
+  const float4* ss;  // row sum-of-squares partials: of the last layer's rows (R > 0) or gathered rows
+  int R, N;          // R > 0: row e is candidate e % N of request e / N, at b R + R - N + j in ss
+  float inv_d;
+  const float* b1;  // [dh]
+  const float* w2;  // [dh, 3]
+  const float* b2;  // [3]
+  float* zp;        // [2 column halves][3][M] partial logits
+  float* probs;     // [M, 3]
+  float* logits;    // [M, 3] or null
+  int M, dh;
+  __device__ void apply(int row, int col, const float (&v)[32]) const {
+    size_t sr = static_cast<size_t>(row);
+    if (R > 0) {
+      const int b = row / N;
+      sr = static_cast<size_t>(b) * R + (R - N) + (row - b * N);
+    }
+    const float4 sp = ss[sr];
+    const float inv = rsqrtf(((sp.x + sp.y) + (sp.z + sp.w)) * inv_d + 1e-6f);  // norm.hpp:23-24
+    const float4* bb = reinterpret_cast<const float4*>(b1 + col);
+    const float4* ww = reinterpret_cast<const float4*>(w2 + static_cast<size_t>(col) * 3);
+    // the half's chunks accumulate in order into its partial (written and re-read by this thread)
+    float* dst = zp + static_cast<size_t>(col >= 128 ? 3 : 0) * M + row;
+    const bool first = (col & 127) == 0;
+    float z0 = first ? 0.f : dst[0], z1 = first ? 0.f : dst[M], z2 = first ? 0.f : dst[2 * M];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {  // columns 4q .. 4q + 3 of the chunk
+      const float4 b = __ldg(bb + q);
+      const float4 wa = __ldg(ww + 3 * q), wb = __ldg(ww + 3 * q + 1), wc = __ldg(ww + 3 * q + 2);
+      const float h0 = fmaxf(fmaf(v[4 * q], inv, b.x), 0.f), h1 = fmaxf(fmaf(v[4 * q + 1], inv, b.y), 0.f);
+      const float h2 = fmaxf(fmaf(v[4 * q + 2], inv, b.z), 0.f), h3 = fmaxf(fmaf(v[4 * q + 3], inv, b.w), 0.f);
+      // w2 rows (c, o) for c = 4q .. 4q+3: wa = (c0o0 c0o1 c0o2 c1o0), wb = (c1o1 c1o2 c2o0 c2o1),
+      // wc = (c2o2 c3o0 c3o1 c3o2)
+      z0 = fmaf(h3, wc.y, fmaf(h2, wb.z, fmaf(h1, wa.w, fmaf(h0, wa.x, z0))));
+      z1 = fmaf(h3, wc.z, fmaf(h2, wb.w, fmaf(h1, wb.x, fmaf(h0, wa.y, z1))));
+      z2 = fmaf(h3, wc.w, fmaf(h2, wc.x, fmaf(h1, wb.y, fmaf(h0, wa.z, z2))));
+    }
+    dst[0] = z0;
+    dst[M] = z1;
+    dst[2 * M] = z2;
+  }
+  __device__ void row_end(int row) const {
+#pragma unroll
+    for (int o = 0; o < 3; ++o) {
+      const float* z = zp + static_cast<size_t>(o) * M + row;
+      const float v = (dh > 128 ? z[0] + z[3 * static_cast<size_t>(M)] : z[0]) + b2[o];
+      if (logits) logits[row * 3 + o] = v;
+      // rankformer::sigmoid branch structure (common.hpp:29-35) in fp32
+      probs[row * 3 + o] = v >= 0.f ? 1.f / (1.f + expf(-v)) : expf(v) / (1.f + expf(v));
+    }
+  }
+};
+
 }  // namespace sortk

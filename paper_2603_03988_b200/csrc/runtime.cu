@@ -192,6 +192,12 @@ struct Handle {
   float2* rope = nullptr;
   float *head_gain = nullptr, *head_w1 = nullptr, *head_b1 = nullptr, *head_w2 = nullptr,
         *head_b2 = nullptr;
+  // tensor-core head (misc.cuh GsHead): g . W1 as three bf16 pieces [dh, 3d], gathered candidate
+  // rows + statistics, per-chunk partial logits
+  bool head_tc = true;  // sort_set_option("head_tc"): 0 runs the SIMT k_head
+  __nv_bfloat16 *head_wt = nullptr, *head_xc = nullptr;
+  float4* head_ssc = nullptr;
+  float* head_zp = nullptr;
   std::vector<LayerDev> layers;
   // workspace
   __nv_bfloat16* X[2] = {nullptr, nullptr};
@@ -399,6 +405,15 @@ static void ensure_moe_buffers(Handle& h) {
   h.tmA_moe_xs = make_tmap_2d(h.moe_xs, P, h.d, h.d, 128, 64, 128);
   h.tmA_moe_hs = make_tmap_2d(h.moe_hs, P, h.moe_m, h.moe_m, 128, 64, 128);
   h.tmY_moe = make_tmap_2d(h.moe_ys, P, h.d, h.d, 128, 64, 128);
+}
+
+// g . W1 of the ranking head as three bf16 pieces for the tensor-core head (misc.cuh GsHead);
+// rebuilt whenever the weights change (finalize, repack_weights)
+static void head_wsplit(Handle& h) {
+  const int n = h.d * h.dh;
+  k_head_wsplit<<<std::min((n + 255) / 256, 148 * 8), 256, 0, h.stream>>>(h.head_w1, h.head_gain, h.d, h.dh, h.head_wt);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw RuntimeFailure(std::string("head weight split launch failed: ") + cudaGetErrorString(e));
 }
 
 static void finalize(Handle& h) {
@@ -668,6 +683,14 @@ static void finalize(Handle& h) {
     }
   }
   if (h.moe) ensure_moe_buffers(h);
+  if (!c.pretrain && h.d % 64 == 0 && h.dh % 32 == 0) {
+    const size_t rows = static_cast<size_t>(h.Bmax) * c.n_cand;
+    h.head_wt = h.dalloc<__nv_bfloat16>(static_cast<size_t>(h.dh) * 3 * h.d);
+    h.head_xc = h.dalloc<__nv_bfloat16>(rows * h.d);
+    h.head_ssc = h.dalloc<float4>(rows);
+    h.head_zp = h.dalloc<float>(static_cast<size_t>(6) * rows);  // [2 halves][3][rows]
+    head_wsplit(h);
+  }
   h.host.clear();  // device copies are authoritative from here on
   h.finalized = true;
 }
@@ -2309,6 +2332,7 @@ static void repack_weights(Handle& h) {
     k_cast_segs<<<dim3(static_cast<unsigned>(std::min<size_t>((h.tw16_nmax + 255) / 256, 64)), h.tw16_nseg), 256, 0,
                   h.stream>>>(h.tw16_segs);
   }
+  if (h.head_wt) head_wsplit(h);
   check_launch("weight repack");
   h.w16.clear();  // generic-path bf16 copies are rebuilt on next use
 }
@@ -2399,6 +2423,41 @@ static void forward_device(Handle& h, int B) {
     return;
   }
   const int total = B * h.cfg.n_cand;
+  if (h.head_tc && h.head_wt) {
+    const LayerDev& lst = last;
+    const int N = h.cfg.n_cand, Rq = lst.Rq;
+    GsHead epi{nullptr, 0, 0, 1.f / static_cast<float>(h.d), h.head_b1, h.head_w2, h.head_b2, h.head_zp,
+               h.probs, h.logits, total, h.dh};
+    const __nv_bfloat16* wt = h.head_wt;
+    const int K = 3 * h.d, a_kwrap = h.d / 64;
+    ensure_smem(k_gemm_stream<GsHead, false, false, __nv_bfloat16>, kGsSmem);
+    const CUtensorMap& tb = gs_map(h, wt, h.dh, K, K, kGsBN, 64, false);
+    const int grid = std::min((total + kGsBM - 1) / kGsBM, h.num_sms);
+    if (N <= kGsBM && kGsBM % N == 0) {  // candidate rows read in place: 3D view {d, N, B}
+      const uint64_t dims[3] = {static_cast<uint64_t>(h.d), static_cast<uint64_t>(N), static_cast<uint64_t>(B)};
+      const uint64_t strides[2] = {static_cast<uint64_t>(h.d) * 2, static_cast<uint64_t>(Rq) * h.d * 2};
+      const uint32_t box[3] = {64, static_cast<uint32_t>(N), static_cast<uint32_t>(kGsBM / N)};
+      const CUtensorMap ta =
+          make_tmap_bf16(h.X[lst.q_buf] + static_cast<size_t>(Rq - N) * h.d, 3, dims, strides, box, 128);
+      epi.ss = h.SS[lst.q_buf];
+      epi.R = Rq;
+      epi.N = N;
+      k_gemm_stream<GsHead, false, false, __nv_bfloat16><<<grid, kGsThreads, kGsSmem, h.stream>>>(
+          ta, tb, total, h.dh, K, 1, epi, a_kwrap, N);
+    } else {  // gathered copy of the candidate rows
+      k_gather_cand<<<std::min((total * (h.d / 8) + 255) / 256, 148 * 16), 256, 0, h.stream>>>(
+          h.X[lst.q_buf], h.SS[lst.q_buf], Rq, N, total, h.d, h.head_xc, h.head_ssc);
+      ++h.launches;
+      epi.ss = h.head_ssc;
+      const CUtensorMap& ta = gs_map(h, h.head_xc, total, h.d, h.d, kGsBM, 64, false);
+      k_gemm_stream<GsHead, false, false, __nv_bfloat16><<<grid, kGsThreads, kGsSmem, h.stream>>>(
+          ta, tb, total, h.dh, K, 1, epi, a_kwrap, 0);
+    }
+    check_launch("head");
+    ++h.launches;
+    stage_mark(h, "head");
+    return;
+  }
   const size_t hsmem = (static_cast<size_t>(kHeadPitch) * h.d + 2 * kHeadKSlice * h.dh) * sizeof(float);
   const int hgrid = (total + kHeadRows - 1) / kHeadRows;
   const LayerDev& lst = last;
@@ -3329,6 +3388,8 @@ int sort_set_option(SortHandle p, const char* name, int32_t value) {
       h->pre_proj_tc = value != 0;
     } else if (std::strcmp(name, "ce_tc") == 0) {
       h->ce_tc = value != 0;
+    } else if (std::strcmp(name, "head_tc") == 0) {
+      h->head_tc = value != 0;
     } else if (std::strcmp(name, "attn_prescale") == 0) {
       h->attn_prescale = value != 0;
     } else if (std::strcmp(name, "qkvg_pair") == 0) {

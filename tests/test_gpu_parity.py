@@ -293,6 +293,41 @@ def gm_qkvg_default(gm):
     return 0  # sort_set_option("qkvg_pair") default (runtime.cu)
 
 
+HEAD_F32_TOL = 1e-4  # two fp32 evaluations of the same head: different rounding points / sum order
+
+
+@pytest.mark.parametrize("which", ["tiny", "base", "n20"])
+def test_tensor_core_head_matches_fp32_simt_head(which, tiny, base):
+    """The default head (misc.cuh GsHead: g . W1 split into three bf16 pieces, every product exact
+    in the fp32 TMEM accumulator) is an fp32 evaluation of SPEC.md:362-365 up to summation order:
+    it agrees with the fp32 SIMT head (sort_set_option("head_tc", 0)) to fp32 rounding, and
+    keeps batch-position independence (the property behind bit-identical request sharding).
+    tiny / base read the candidate rows in place (N divides 128); n20 (N = 20, dh = 128, d = 128)
+    takes the gathered path."""
+    if which == "n20":
+        cfg = base_config(model_dim=128, heads=4, ffn_dim=320, head_hidden=128, n_hist=300, n_cand=20,
+                          n_items=5000)
+        cfg.keep = [cfg.prefix_len, 128, 128, 64]
+        P = synth.make_params(cfg, seed=19)
+        gm, om = R.SortModel(cfg, P, max_batch=3), O.OracleModel(cfg, P)
+    else:
+        cfg, P, gm, om = tiny if which == "tiny" else base
+    b = synth.make_batch(cfg, 3, seed=52)
+    p_t, z_t = gm.forward_logits(b)
+    gm.set_option("head_tc", 0)
+    try:
+        p_s, z_s = gm.forward_logits(b)
+    finally:
+        gm.set_option("head_tc", 1)
+    scale = max(1.0, float(np.max(np.abs(z_s))))
+    assert np.max(np.abs(z_t - z_s)) < HEAD_F32_TOL * scale, np.max(np.abs(z_t - z_s))
+    assert np.max(np.abs(p_t - p_s)) < HEAD_F32_TOL
+    one_p, one_z = gm.forward_logits({k: v[2:3] for k, v in b.items()})
+    assert np.array_equal(one_z[0], z_t[2]) and np.array_equal(one_p[0], p_t[2])
+    ref = np.stack([om.forward(b, i)[1] for i in range(3)])
+    assert np.max(np.abs(z_t - ref)) < LOGIT_MAX_ABS
+
+
 def test_fused_tail_d128_vs_oracle():
     cfg = base_config(model_dim=128, heads=4, ffn_dim=320, n_hist=300, n_cand=20,
                       n_items=5000)
