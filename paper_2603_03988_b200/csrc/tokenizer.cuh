@@ -121,13 +121,39 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
     return static_cast<int>(kGroupProf);
   };
   // ---- gather of one token row into registers: up to 8 16-byte chunks of the concatenated
-  // embedding rows (K padded to 64 with zeros). Issued one tile ahead, so the dependent
-  // id -> row loads of tile i+1 are in flight while tile i's MMA and epilogue run.
+  // embedding rows (K padded to 64 with zeros). Two stages so no thread waits on a load:
+  // the row's ids (and timestamps) are fetched TWO tiles ahead, the embedding chunks they
+  // address ONE tile ahead -- both in flight while the current tile's MMA and epilogue run.
+  struct Ids {
+    int a, b, c;      // hist: item, action, scene; cand: item; prof: value
+    int64_t t0, t1;   // hist: event time and the request time (clicks: the previous click)
+  };
   struct Row {
     int4 c[4];  // chunks [4 hh, 4 hh + 4) of the row
     int out_row;
   };
-  auto gather = [&](int tile, Row& g) {
+  auto fetch_ids = [&](int tile, Ids& q) {
+    q.a = q.b = q.c = 0;
+    q.t0 = q.t1 = 0;
+    if (tile >= n_tiles) return;
+    int e0, count;
+    const int group = group_of(tile, e0, count);
+    const int e = e0 + rt;
+    if (e >= count) return;
+    if (group == kGroupHist) {
+      const int b = e / p.H, i = e - b * p.H;
+      q.a = p.hist_item[e];
+      q.b = p.hist_action[e];
+      q.c = p.hist_scene[e];
+      q.t0 = p.hist_ts[e];
+      q.t1 = p.click_seq ? (i == 0 ? 0 : p.hist_ts[e - 1]) : p.req_ts[b];
+    } else if (group == kGroupCand) {
+      q.a = p.cand_item[e];
+    } else {
+      q.a = p.profile[e];
+    }
+  };
+  auto gather = [&](int tile, const Ids& q, Row& g) {
     g.out_row = -1;
     const __nv_bfloat16* src[4] = {nullptr, nullptr, nullptr, nullptr};
     int n8[4] = {0, 0, 0, 0};
@@ -138,11 +164,10 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
       if (e < count) {
         if (group == kGroupHist) {
           const int b = e / p.H, i = e - b * p.H;
-          int item = p.hist_item[e], act = p.hist_action[e], sc = p.hist_scene[e];
+          int item = q.a, act = q.b, sc = q.c;
           // click sequences: the gap to the previous click, the first click at INT64_MAX / 4
           // (tokenizer.cpp:262-270); requests: request time - event time (:95-112)
-          const int64_t delta = p.click_seq ? (i == 0 ? 0x1FFFFFFFFFFFFFFFll : p.hist_ts[e] - p.hist_ts[e - 1])
-                                            : p.req_ts[b] - p.hist_ts[e];
+          const int64_t delta = p.click_seq ? (i == 0 ? 0x1FFFFFFFFFFFFFFFll : q.t0 - q.t1) : q.t1 - q.t0;
           const int tb = tok_time_bucket(delta, p.n_tb);
           if (static_cast<unsigned>(item) >= static_cast<unsigned>(p.n_items) ||
               static_cast<unsigned>(act) >= static_cast<unsigned>(p.n_actions) ||
@@ -164,7 +189,7 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
           g.out_row = b * p.L + off_hist + i;
         } else if (group == kGroupCand) {
           const int b = e / p.N, j = e - b * p.N;
-          int item = p.cand_item[e];
+          int item = q.a;
           if (static_cast<unsigned>(item) >= static_cast<unsigned>(p.n_items)) {
             atomicOr(p.err, kErrOOV);
             item = 0;
@@ -174,7 +199,7 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
           g.out_row = b * p.L + off_cand + j;
         } else {
           const int b = e / p.P, f = e - b * p.P;
-          int v = p.profile[e];
+          int v = q.a;
           if (static_cast<unsigned>(v) >= static_cast<unsigned>(p.prof_vocab[f])) {
             atomicOr(p.err, kErrOOV);
             v = 0;
@@ -198,7 +223,10 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
   int cur_group = -1;
   uint32_t phase = 0;
   Row g;
-  gather(blockIdx.x, g);
+  Ids ids;
+  fetch_ids(blockIdx.x, ids);
+  gather(blockIdx.x, ids, g);
+  fetch_ids(blockIdx.x + gridDim.x, ids);
   for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     int e0, count;
     const int group = group_of(tile, e0, count);
@@ -236,7 +264,8 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
                     idesc, k > 0 ? 1u : 0u);
       mma_commit(bar);
     }
-    gather(tile + gridDim.x, g);  // next tile's rows in flight during this tile's epilogue
+    gather(tile + gridDim.x, ids, g);       // next tile's rows in flight during this tile's epilogue
+    fetch_ids(tile + 2 * gridDim.x, ids);  // and the ids of the tile after
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_fence_after();
@@ -255,9 +284,10 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
 #pragma unroll
       for (int i = 0; i < 32; i += 4) {
         const float4 bv = lds_f32x4(sb + (c + i) * 4);
-        const float v0 = __uint_as_float(rv[i]) + bv.x, v1 = __uint_as_float(rv[i + 1]) + bv.y;
-        const float v2 = __uint_as_float(rv[i + 2]) + bv.z, v3 = __uint_as_float(rv[i + 3]) + bv.w;
-        ss += v0 * v0 + v1 * v1 + v2 * v2 + v3 * v3;
+        const float2 v01 = fadd2(make_float2(__uint_as_float(rv[i]), __uint_as_float(rv[i + 1])), make_float2(bv.x, bv.y));
+        const float2 v23 =
+            fadd2(make_float2(__uint_as_float(rv[i + 2]), __uint_as_float(rv[i + 3])), make_float2(bv.z, bv.w));
+        ss += v01.x * v01.x + v01.y * v01.y + v23.x * v23.x + v23.y * v23.y;
       }
     }
     sSS[hh * 128 + r] = ss;
@@ -265,6 +295,7 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
     const float inv = rsqrtf((sSS[r] + sSS[128 + r]) / static_cast<float>(d) + 1e-6f);
     named_bar_sync(1 + q, 64);  // both halves have read before the sums are overwritten
     // (thread t gathered tile row t & 127 == q * 32 + lane: out_row / valid are this lane's row)
+    const float2 inv2 = make_float2(inv, inv);
     float ss_out = 0.f;
     for (int c = cb; c < ce; c += 32) {
       uint32_t rv[32];
@@ -277,15 +308,18 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
         for (int i = 0; i < 16; i += 4) {
           const int k = q16 * 16 + i;
           const float4 bv = lds_f32x4(sb + (c + k) * 4), gv = lds_f32x4(sgn + (c + k) * 4);
-          const float y0 = (__uint_as_float(rv[k]) + bv.x) * inv * gv.x;
-          const float y1 = (__uint_as_float(rv[k + 1]) + bv.y) * inv * gv.y;
-          const float y2 = (__uint_as_float(rv[k + 2]) + bv.z) * inv * gv.z;
-          const float y3 = (__uint_as_float(rv[k + 3]) + bv.w) * inv * gv.w;
-          packed[i / 2] = pack_bf16x2(y0, y1);
-          packed[i / 2 + 1] = pack_bf16x2(y2, y3);
-          const float2 q0 = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&packed[i / 2]));
-          const float2 q1 = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&packed[i / 2 + 1]));
-          ss_out += q0.x * q0.x + q0.y * q0.y + q1.x * q1.x + q1.y * q1.y;
+          // ((acc + b) / rms) g on packed fp32x2 ops: the same IEEE operations in the same
+          // order as the scalar form, so the rows are bit-identical to it
+          const float2 y01 = fmul2(fmul2(fadd2(make_float2(__uint_as_float(rv[k]), __uint_as_float(rv[k + 1])),
+                                               make_float2(bv.x, bv.y)), inv2), make_float2(gv.x, gv.y));
+          const float2 y23 = fmul2(fmul2(fadd2(make_float2(__uint_as_float(rv[k + 2]), __uint_as_float(rv[k + 3])),
+                                               make_float2(bv.z, bv.w)), inv2), make_float2(gv.z, gv.w));
+          const uint32_t w01 = pack_bf16x2(y01.x, y01.y), w23 = pack_bf16x2(y23.x, y23.y);
+          packed[i / 2] = w01;
+          packed[i / 2 + 1] = w23;
+          const float q0x = __uint_as_float(w01 << 16), q0y = __uint_as_float(w01 & 0xFFFF0000u);
+          const float q1x = __uint_as_float(w23 << 16), q1y = __uint_as_float(w23 & 0xFFFF0000u);
+          ss_out += q0x * q0x + q0y * q0y + q1x * q1x + q1y * q1y;
         }
         if (valid) stg256(p.x + static_cast<size_t>(out_row) * d + c + q16 * 16, packed);
       }
