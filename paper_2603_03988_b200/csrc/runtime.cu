@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <numeric>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -715,6 +716,19 @@ static void ensure_smem(F* fn, size_t bytes) {
 }
 
 // ------------------------------------------------------------------ launches
+// Grid of a persistent kernel that walks work items `it = blockIdx.x + k * grid` laid out
+// (request, head)-major with `period` tiles of unequal cost per (request, head) (the q-tiles
+// of an attention layer, heaviest first): with gcd(grid, period) > 1 a CTA would only ever
+// see some of the ranks -- at a pruned layer (period 2: the 128 retained rows and the
+// candidate tile) and 2 x 148 CTAs, every even CTA got only the heavy candidate tiles. The
+// largest grid <= want coprime to the period makes every CTA cycle through all ranks.
+static int coprime_grid(int want, int period) {
+  if (period <= 1) return std::max(1, want);
+  for (int g = want; g > 1; --g)
+    if (std::gcd(g, period) == 1) return g;
+  return 1;
+}
+
 static void check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw RuntimeFailure(std::string(what) + " launch failed: " + cudaGetErrorString(e));
@@ -822,7 +836,7 @@ static void launch_attention_dk(Handle& h, const LayerDev& L, const LayerPlan& l
   const CUtensorMap& tv = h.save_to ? h.save_to->tmV : L.tmV;
   const size_t smem = AttnSmem<DK>::bytes(tile_ints);
   ensure_smem(k_attention<DK, kFixed, kPre>, smem);
-  const int grid = std::min(n_items, AttnTmem<DK>::kCtasPerSm * h.num_sms);
+  const int grid = coprime_grid(std::min(n_items, AttnTmem<DK>::kCtasPerSm * h.num_sms), lp.n_qtiles);
   k_attention<DK, kFixed, kPre><<<grid, kAttnThreads, smem, h.stream>>>(tq, tk, tv, a);
   check_launch("attention");
   ++h.launches;
@@ -1734,7 +1748,7 @@ static void attn_core_backward_tc(Handle& h, const LayerDev& L, const Handle::Tr
   auto launch_tc = [&](auto kern, const CUtensorMap& x0, const CUtensorMap& x1, const CUtensorMap& y0,
                        const CUtensorMap& y1, size_t smem_fn_bytes) {
     ensure_smem(kern, smem_fn_bytes);
-    const int grid = std::min(tb.nX * tb.BH, 2 * h.num_sms);
+    const int grid = coprime_grid(std::min(tb.nX * tb.BH, 2 * h.num_sms), tb.nX);
     kern<<<grid, kAttnThreads, smem_fn_bytes, h.stream>>>(x0, x1, y0, y1, tb);
   };
 #define SORT_BWD_TC(DKV)                                                                               \
