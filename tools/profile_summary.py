@@ -27,7 +27,7 @@ def stage_of(name, index_in_step, pruned_seen):
     name = name[5:] if name.startswith("void ") else name
     if name.startswith("k_tokenize"):
         return "tokenizer"
-    if name.startswith("k_head"):
+    if name.startswith("k_head") or "GsHead" in name:
         return "head"
     if name.startswith("k_gather_rows"):
         return "gather"
