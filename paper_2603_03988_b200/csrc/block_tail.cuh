@@ -459,15 +459,17 @@ __global__ void __launch_bounds__(kTailThreads, 1)
         float v[64];
         tmem_row_chunk<64>(tu, v);
         uint32_t hw[16];
+        const float2 inv2 = make_float2(inv, inv), half2 = make_float2(0.5f, 0.5f);
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          float hh[2];
-#pragma unroll
-          for (int k = 0; k < 2; ++k) {
-            const float gt = v[2 * i + k] * inv, up = v[32 + 2 * i + k] * inv;
-            hh[k] = gt * up * fast_sigmoid(gt);  // swish(x) = x * sigmoid(x) (common.hpp:37)
-          }
-          hw[i] = pack_bf16x2(hh[0], hh[1]);
+          // swish(g) u = (g u) sigmoid(g), sigmoid(g) = 0.5 tanh(0.5 g) + 0.5 (common.hpp:37,
+          // fast_sigmoid) on packed fp32x2 ops: the scalar form's IEEE operations in its order
+          const float2 gt = fmul2(make_float2(v[2 * i], v[2 * i + 1]), inv2);
+          const float2 up = fmul2(make_float2(v[32 + 2 * i], v[32 + 2 * i + 1]), inv2);
+          const float2 hg = fmul2(half2, gt);
+          const float2 sg = ffma2(half2, make_float2(tanh_approx(hg.x), tanh_approx(hg.y)), half2);
+          const float2 hh = fmul2(fmul2(gt, up), sg);
+          hw[i] = pack_bf16x2(hh.x, hh.y);
         }
         tmem_st_32x32b_x16(tu, hw);
         tmem_st_wait();
