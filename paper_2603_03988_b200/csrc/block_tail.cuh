@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(kTailThreads, 1)
       for (int p = 0; p < static_cast<int>(kKB) / 2; ++p) {
         const int kb = 2 * p + hf;
         mbar_wait(&res_full[kb], t & 1);
-        float ss = 0.f;
+        float2 ss = make_float2(0.f, 0.f);  // even / odd columns (row_ss_pair_add order)
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
           float v[32];
@@ -414,22 +414,17 @@ __global__ void __launch_bounds__(kTailThreads, 1)
           for (int qd = 0; qd < 4; ++qd) {
             const uint32_t adr = xs + sw128_off(r, kb * 8 + cc * 4 + qd);
             const int4 r4 = lds_v4(adr);
-            const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&r4);
             uint32_t w[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const float2 f = __bfloat1622float2(r2[k]);
-              w[k] = pack_bf16x2(f.x + v[qd * 8 + 2 * k], f.y + v[qd * 8 + 2 * k + 1]);
-              const float2 y = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&w[k]));
-              ss = fmaf(y.x, y.x, fmaf(y.y, y.y, ss));
-            }
+            for (int k = 0; k < 4; ++k) w[k] = resid_add_ss(reinterpret_cast<const uint32_t*>(&r4)[k],
+                                                              v[qd * 8 + 2 * k], v[qd * 8 + 2 * k + 1], ss);
             sts_v4(adr, make_int4(w[0], w[1], w[2], w[3]));
             if (a.x1_out && row < a.M)
               *reinterpret_cast<int4*>(a.x1_out + static_cast<size_t>(row) * D + kb * 64 + cc * 32 + qd * 8) =
                   make_int4(w[0], w[1], w[2], w[3]);
           }
         }
-        ssb[p] = ss;
+        ssb[p] = ss.x + ss.y;
         fence_proxy_async_smem();
         tc_fence_before();
         arrive_leader(&x1_kb[kb]);
@@ -481,9 +476,9 @@ __global__ void __launch_bounds__(kTailThreads, 1)
       tc_fence_after();
       // one partial per 64 columns, each summed in column order: the partition the unfused
       // down-projection epilogue (BN = 128, two halves) writes, so row statistics match it bitwise
-      float ss2[kCols / 64];
+      float2 ss2[kCols / 64];
 #pragma unroll
-      for (int i = 0; i < kCols / 64; ++i) ss2[i] = 0.f;
+      for (int i = 0; i < kCols / 64; ++i) ss2[i] = make_float2(0.f, 0.f);
 #pragma unroll
       for (int cc = 0; cc < kCols / 32; ++cc) {
         float v[32];
@@ -492,15 +487,10 @@ __global__ void __launch_bounds__(kTailThreads, 1)
         for (int qd = 0; qd < 4; ++qd) {
           const uint32_t adr = xs + sw128_off(r, (hf * kCols + cc * 32) / 8 + qd);
           const int4 x4 = lds_v4(adr);
-          const __nv_bfloat162* x2p = reinterpret_cast<const __nv_bfloat162*>(&x4);
           uint32_t w[4];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const float2 f = __bfloat1622float2(x2p[k]);
-            w[k] = pack_bf16x2(f.x + v[qd * 8 + 2 * k], f.y + v[qd * 8 + 2 * k + 1]);
-            const float2 y = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&w[k]));
-            ss2[cc >> 1] = fmaf(y.x, y.x, fmaf(y.y, y.y, ss2[cc >> 1]));
-          }
+          for (int k = 0; k < 4; ++k) w[k] = resid_add_ss(reinterpret_cast<const uint32_t*>(&x4)[k],
+                                                            v[qd * 8 + 2 * k], v[qd * 8 + 2 * k + 1], ss2[cc >> 1]);
           sts_v4(adr, make_int4(w[0], w[1], w[2], w[3]));
         }
       }
@@ -511,9 +501,9 @@ __global__ void __launch_bounds__(kTailThreads, 1)
       if (row < a.M) {
         float* so = a.ss_out + static_cast<size_t>(row) * 4;
         if constexpr (D == 256) {
-          *reinterpret_cast<float2*>(so + 2 * hf) = make_float2(ss2[0], ss2[1]);
+          *reinterpret_cast<float2*>(so + 2 * hf) = make_float2(ss2[0].x + ss2[0].y, ss2[1].x + ss2[1].y);
         } else {
-          so[hf] = ss2[0];
+          so[hf] = ss2[0].x + ss2[0].y;
           if (hf == 0) so[2] = so[3] = 0.f;
         }
       }

@@ -50,6 +50,19 @@ __device__ __forceinline__ float row_inv_rms(float ss, float inv_d) {
   return rsqrtf(ss * inv_d + 1e-6f);  // norm.hpp:23-24 (eps = kRmsEps, norm.hpp:8)
 }
 
+// bf16 pair of (residual + accumulator) and its sum of squares: the residual pair r (bf16x2)
+// widened, added to (a0, a1) on one fp32x2 add, rounded to bf16, and the rounded values'
+// squares accumulated into ss on one fp32x2 FMA (even / odd columns in ss.x / ss.y, combined
+// once per 64 columns). Every residual epilogue (fused block tail E1 / E3, EpiResid) uses it, so
+// their row statistics stay bitwise equal.
+__device__ __forceinline__ uint32_t resid_add_ss(uint32_t r, float a0, float a1, float2& ss) {
+  const float2 y = fadd2(make_float2(__uint_as_float(r << 16), __uint_as_float(r & 0xFFFF0000u)), make_float2(a0, a1));
+  const uint32_t w = pack_bf16x2(y.x, y.y);
+  const float2 q = make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+  ss = ffma2(q, q, ss);
+  return w;
+}
+
 __device__ __forceinline__ void store_bf16_row(__nv_bfloat16* dst, const float* v, int n) {
   // n multiple of 16 -> 32-byte sector stores (dst 32-byte aligned); else 16-byte stores
   if (n % 16 == 0) {
@@ -219,7 +232,7 @@ struct EpiResid {
     wait();
     // sum of squares per 64-column block of the row (slot = block index), each summed in
     // column order; spans narrower than 64 columns (d = 64) fall back to one slot per part
-    float ssb[2] = {0.f, 0.f};
+    float2 ssb2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
     for (int cc = 0; cc < 4; ++cc) {
       const int c = c0 + cc * 32;
@@ -231,15 +244,11 @@ struct EpiResid {
 #pragma unroll
       for (int qd = 0; qd < 4; ++qd) {
         const int4 r4 = rv[cc * 4 + qd];
-        const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&r4);
         uint32_t w[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 f = __bfloat1622float2(r2[e]);
-          w[e] = pack_bf16x2(f.x + v[qd * 8 + 2 * e], f.y + v[qd * 8 + 2 * e + 1]);
-          const float2 y = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&w[e]));
-          ssb[cc >> 1] = fmaf(y.x, y.x, fmaf(y.y, y.y, ssb[cc >> 1]));
-        }
+        for (int e = 0; e < 4; ++e)
+          w[e] = resid_add_ss(reinterpret_cast<const uint32_t*>(&r4)[e], v[qd * 8 + 2 * e], v[qd * 8 + 2 * e + 1],
+                              ssb2[cc >> 1]);
         o[qd] = make_int4(w[0], w[1], w[2], w[3]);
       }
       uint8_t* op = reinterpret_cast<uint8_t*>(out + static_cast<size_t>(row) * d + n0 + c);
@@ -252,6 +261,7 @@ struct EpiResid {
         stg256(op + 32 * h2, w8);
       }
     }
+    const float ssb[2] = {ssb2[0].x + ssb2[0].y, ssb2[1].x + ssb2[1].y};
     if (valid) {
       float* o = ss_out + static_cast<size_t>(row) * 4;
       if (c1 - c0 >= 64) {
