@@ -288,8 +288,16 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
         const float2 v23 =
             fadd2(make_float2(__uint_as_float(rv[i + 2]), __uint_as_float(rv[i + 3])), make_float2(bv.z, bv.w));
         ss += v01.x * v01.x + v01.y * v01.y + v23.x * v23.x + v23.y * v23.y;
+        rv[i] = __float_as_uint(v01.x);
+        rv[i + 1] = __float_as_uint(v01.y);
+        rv[i + 2] = __float_as_uint(v23.x);
+        rv[i + 3] = __float_as_uint(v23.y);
       }
+      // acc + b back over the accumulator: pass 2 reads it without reloading the bias
+      tmem_st_32x32b_x16(trow + c, *reinterpret_cast<const uint32_t(*)[16]>(rv));
+      tmem_st_32x32b_x16(trow + c + 16, *reinterpret_cast<const uint32_t(*)[16]>(rv + 16));
     }
+    tmem_st_wait();
     sSS[hh * 128 + r] = ss;
     named_bar_sync(1 + q, 64);
     const float inv = rsqrtf((sSS[r] + sSS[128 + r]) / static_cast<float>(d) + 1e-6f);
@@ -307,13 +315,13 @@ __global__ void __launch_bounds__(kTokThreads) k_tokenize(const TokParams p) {
 #pragma unroll
         for (int i = 0; i < 16; i += 4) {
           const int k = q16 * 16 + i;
-          const float4 bv = lds_f32x4(sb + (c + k) * 4), gv = lds_f32x4(sgn + (c + k) * 4);
-          // ((acc + b) / rms) g on packed fp32x2 ops: the same IEEE operations in the same
-          // order as the scalar form, so the rows are bit-identical to it
-          const float2 y01 = fmul2(fmul2(fadd2(make_float2(__uint_as_float(rv[k]), __uint_as_float(rv[k + 1])),
-                                               make_float2(bv.x, bv.y)), inv2), make_float2(gv.x, gv.y));
-          const float2 y23 = fmul2(fmul2(fadd2(make_float2(__uint_as_float(rv[k + 2]), __uint_as_float(rv[k + 3])),
-                                               make_float2(bv.z, bv.w)), inv2), make_float2(gv.z, gv.w));
+          const float4 gv = lds_f32x4(sgn + (c + k) * 4);
+          // ((acc + b) / rms) g on packed fp32x2 ops (acc + b stored by pass 1): the same IEEE
+          // operations in the same order as the scalar form, so the rows are bit-identical to it
+          const float2 y01 =
+              fmul2(fmul2(make_float2(__uint_as_float(rv[k]), __uint_as_float(rv[k + 1])), inv2), make_float2(gv.x, gv.y));
+          const float2 y23 = fmul2(fmul2(make_float2(__uint_as_float(rv[k + 2]), __uint_as_float(rv[k + 3])), inv2),
+                                   make_float2(gv.z, gv.w));
           const uint32_t w01 = pack_bf16x2(y01.x, y01.y), w23 = pack_bf16x2(y23.x, y23.y);
           packed[i / 2] = w01;
           packed[i / 2 + 1] = w23;
