@@ -331,7 +331,10 @@ int sort_dataset_batch(SortDataset d, int64_t first, int32_t count, int32_t n_hi
  * chunk kept in TMEM, the default; 0 = the grouped [gate|up] and down GEMM pair);
  * "graphs" (1 = replay the
  * inference forward from a CUDA graph per (batch size, input slot, item table), the default;
- * 0 = eager launches). Status 1 on an unknown name. */
+ * 0 = eager launches); "head_tc" (1 = the ranking head on tcgen05 with the fp32 weights split
+ * into three exact bf16 pieces, the default; 0 = the fp32 SIMT head); "attn_prescale",
+ * "ce_tc", "pre_proj_tc", "stream_gemm", "train_cublas". Status 1 on an
+ * unknown name. */
 int sort_set_option(SortHandle h, const char* name, int32_t value);
 
 /* ---- pre-training (config field pretrain = 1) ---------------------------------------------
