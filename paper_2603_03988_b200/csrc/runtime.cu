@@ -684,7 +684,7 @@ static void finalize(Handle& h) {
     }
   }
   if (h.moe) ensure_moe_buffers(h);
-  if (!c.pretrain && h.d % 64 == 0 && h.dh % 32 == 0) {
+  if (!c.pretrain && !h.generic && h.d % 64 == 0 && h.dh % 32 == 0 && h.dh <= 256) {  // the SORT-base head path
     const size_t rows = static_cast<size_t>(h.Bmax) * c.n_cand;
     h.head_wt = h.dalloc<__nv_bfloat16>(static_cast<size_t>(h.dh) * 3 * h.d);
     h.head_xc = h.dalloc<__nv_bfloat16>(rows * h.d);
