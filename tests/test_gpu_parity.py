@@ -296,19 +296,23 @@ def gm_qkvg_default(gm):
 HEAD_F32_TOL = 1e-4  # two fp32 evaluations of the same head: different rounding points / sum order
 
 
-@pytest.mark.parametrize("which", ["tiny", "base", "n20"])
+@pytest.mark.parametrize("which", ["tiny", "base", "n20", "dh32"])
 def test_tensor_core_head_matches_fp32_simt_head(which, tiny, base):
     """The default head (misc.cuh GsHead: g . W1 split into three bf16 pieces, every product exact
     in the fp32 TMEM accumulator) is an fp32 evaluation of SPEC.md:362-365 up to summation order:
     it agrees with the fp32 SIMT head (sort_set_option("head_tc", 0)) to fp32 rounding, and
     keeps batch-position independence (the property behind bit-identical request sharding).
-    tiny / base read the candidate rows in place (N divides 128); n20 (N = 20, dh = 128, d = 128)
-    takes the gathered path."""
+    tiny / base / dh32 read the candidate rows in place (N divides 128); n20 (N = 20, dh = 128,
+    d = 128) takes the gathered path; dh32 is the narrowest hidden width (one 32-column MMA)."""
     if which == "n20":
         cfg = base_config(model_dim=128, heads=4, ffn_dim=320, head_hidden=128, n_hist=300, n_cand=20,
                           n_items=5000)
         cfg.keep = [cfg.prefix_len, 128, 128, 64]
         P = synth.make_params(cfg, seed=19)
+        gm, om = R.SortModel(cfg, P, max_batch=3), O.OracleModel(cfg, P)
+    elif which == "dh32":  # the narrowest head: one 32-column MMA width, one column half
+        cfg = tiny_config(head_hidden=32)
+        P = synth.make_params(cfg, seed=23)
         gm, om = R.SortModel(cfg, P, max_batch=3), O.OracleModel(cfg, P)
     else:
         cfg, P, gm, om = tiny if which == "tiny" else base
