@@ -817,23 +817,43 @@ __global__ void __launch_bounds__(256) k_qknorm_rope_bwd_v(const float* drot, co
     }
   }
   const int warps = gridDim.x * (blockDim.x >> 5);
-  for (int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < rows; w += warps) {
-    float cs[8];  // (cos, sin) of the lane's 4 pairs
-    {
-      const float4* t = reinterpret_cast<const float4*>(rope_tab + static_cast<size_t>(pos[w % R]) * (dk / 2) + e / 2);
-      const float4 a = t[0], b = t[1];
-      cs[0] = a.x; cs[1] = a.y; cs[2] = a.z; cs[3] = a.w;
-      cs[4] = b.x; cs[5] = b.y; cs[6] = b.z; cs[7] = b.w;
+  // one row ahead: the next row's dQ / raw / (cos, sin) loads are in flight while this row is
+  // computed and stored (rows are distinct, so the in-place draw == drot stores cannot alias them)
+  struct RowIn {
+    float4 g[kV][2], x[kV][2], cs[2];
+  };
+  auto load_row = [&](int w, RowIn& in) {
+    const float4* t = reinterpret_cast<const float4*>(rope_tab + static_cast<size_t>(pos[w % R]) * (dk / 2) + e / 2);
+    in.cs[0] = t[0];
+    in.cs[1] = t[1];
+#pragma unroll
+    for (int i = 0; i < kV; ++i) {
+      const int c = lane + 32 * i;
+      if (c < d8) {
+        const float4* gp = reinterpret_cast<const float4*>(drot + static_cast<size_t>(w) * d + c * 8);
+        const float4* xp = reinterpret_cast<const float4*>(raw + static_cast<size_t>(w) * d + c * 8);
+        in.g[i][0] = gp[0];
+        in.g[i][1] = gp[1];
+        in.x[i][0] = xp[0];
+        in.x[i][1] = xp[1];
+      }
     }
+  };
+  int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  RowIn cur;
+  if (w < rows) load_row(w, cur);
+  for (; w < rows; w += warps) {
+    RowIn nxt;
+    if (w + warps < rows) load_row(w + warps, nxt);
+    const float cs[8] = {cur.cs[0].x, cur.cs[0].y, cur.cs[0].z, cur.cs[0].w,
+                         cur.cs[1].x, cur.cs[1].y, cur.cs[1].z, cur.cs[1].w};  // (cos, sin) of 4 pairs
 #pragma unroll
     for (int i = 0; i < kV; ++i) {
       const int c = lane + 32 * i;
       const bool act = c < d8;
       float dq[8], x[8];
       if (act) {
-        const float4* gp = reinterpret_cast<const float4*>(drot + static_cast<size_t>(w) * d + c * 8);
-        const float4* xp = reinterpret_cast<const float4*>(raw + static_cast<size_t>(w) * d + c * 8);
-        const float4 g0 = gp[0], g1 = gp[1], x0 = xp[0], x1 = xp[1];
+        const float4 g0 = cur.g[i][0], g1 = cur.g[i][1], x0 = cur.x[i][0], x1 = cur.x[i][1];
         const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
         x[0] = x0.x; x[1] = x0.y; x[2] = x0.z; x[3] = x0.w;
         x[4] = x1.x; x[5] = x1.y; x[6] = x1.z; x[7] = x1.w;
@@ -871,6 +891,7 @@ __global__ void __launch_bounds__(256) k_qknorm_rope_bwd_v(const float* drot, co
         if (draw16) store8(draw16 + static_cast<size_t>(w) * d + c * 8, out);
       }
     }
+    cur = nxt;
   }
 #pragma unroll
   for (int i = 0; i < kV; ++i) {
