@@ -150,9 +150,15 @@ __global__ void __launch_bounds__(256) k_rmsnorm_rows_v(const T* __restrict__ x,
 #pragma unroll
   for (int k = 0; k < 8; ++k) g[k] = act && gain ? gain[c0 + k] : 1.f;
   const int warps = gridDim.x * (blockDim.x >> 5);
-  for (int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < rows; w += warps) {
-    float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    if (act) load8(x + static_cast<size_t>(w) * d + c0, v);
+  // one row ahead: the next row's load is in flight while this row is reduced and stored
+  int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  float nx[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (act && w < rows) load8(x + static_cast<size_t>(w) * d + c0, nx);
+  for (; w < rows; w += warps) {
+    float v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = nx[k];
+    if (act && w + warps < rows) load8(x + static_cast<size_t>(w + warps) * d + c0, nx);
     float ss = 0.f;
 #pragma unroll
     for (int k = 0; k < 8; ++k) ss = fmaf(v[k], v[k], ss);
