@@ -1831,6 +1831,7 @@ static void backward_device(Handle& h, int B, const float* dz) {
   check_launch("head backward");
   }
   // ---- blocks in reverse
+  bool dX16_ready = false;  // tw[3] already holds dX in bf16 (written by the layer above)
   for (int l = c.layers - 1; l >= 0; --l) {
     const LayerDev& L = h.layers[l];
     const LayerPlan& lp = h.plan.layers[l];
@@ -1857,7 +1858,8 @@ static void backward_device(Handle& h, int B, const float* dz) {
     }
     gemm_rm16(h, false, false, M, 2 * m, d, xf, d, Wgu, 2 * m, GU, 2 * m, true);
     k_swiglu_z<__nv_bfloat16, __nv_bfloat16><<<ew_grid(static_cast<size_t>(M) * m / 8), 256, 0, h.stream>>>(GU, M, m, z);
-    k_f32_to_bf16<<<ew_grid(nq), 256, 0, h.stream>>>(dX, nq, dX16);
+    if (!dX16_ready) k_f32_to_bf16<<<ew_grid(nq), 256, 0, h.stream>>>(dX, nq, dX16);
+    dX16_ready = false;
     gemm_rm16(h, true, false, m, d, M, z, m, dX16, d, grad_ptr(h, F + "w_down"), d, false);
     gemm_rm16(h, false, true, M, m, d, dX16, d, Wdn, d, z, m, true);  // z <- dz
     k_swiglu_bwd16<<<ew_grid(static_cast<size_t>(M) * m / 8), 256, 0, h.stream>>>(z, GU, M, m, dGU);
@@ -1907,7 +1909,11 @@ static void backward_device(Handle& h, int B, const float* dz) {
     }
     check_launch("attention rows");
     gemm_rm16(h, true, false, d, d, M, xqp, d, dgraw, d, grad_ptr(h, A + "wg"), d, false);
-    float* dxq = h.tw[4];  // (the gated output is no longer needed) -- fp32 [M, d]
+    // d(xq) = dgraw Wg^T + dQ Wq^T. When the query rows are all kv rows in order (unpruned
+    // layers) d(xq) is accumulated straight into d(xn) (tw[5]: dH is dead after the gate
+    // backward), so no separate [M, d] buffer is written and scattered back.
+    float* dxn = h.tw[5];
+    float* dxq = lp.q_identity ? dxn : h.tw[4];  // (the gated output is no longer needed) -- fp32 [M, d]
     gemm_rm16(h, false, true, M, d, d, dgraw, d, Wg16, d, dxq, d, false);
     // attention core
     AttnBwdArgs ab;
@@ -2007,7 +2013,20 @@ static void backward_device(Handle& h, int B, const float* dz) {
     gemm_rm16(h, true, false, d, d, Mkv, xn, d, dK16, d, grad_ptr(h, A + "wk"), d, false);
     gemm_rm16(h, true, false, d, d, Mkv, xn, d, dV16, d, grad_ptr(h, A + "wv"), d, false);
     gemm_rm16(h, false, true, M, d, d, dQ16, d, Wq16, d, dxq, d, false, 1.f);
-    float* dxn = h.tw[5];
+    if (lp.q_identity) {
+      // d(xn) already holds d(xq); d(x_in) = d(xr) + RMSN_bwd(d(xn)) accumulated in place into dX
+      // (the same fp32 sum as the scatter below, operands swapped)
+      gemm_rm16(h, false, true, Mkv, d, d, dK16, d, Wk16, d, dxn, d, false, 1.f);
+      gemm_rm16(h, false, true, Mkv, d, d, dV16, d, Wv16, d, dxn, d, false, 1.f);
+      // ... and, below the first layer, its bf16 copy for the next layer's FFN GEMMs (tw[3]: the
+      // FFN's d(xf) is dead), so that layer skips its own conversion pass
+      rms_bwd<__nv_bfloat16>(h, dxn, T.x_in, inv_a, w32(h, Bk + "attn_norm"), Mkv, d, dX, 1,
+                             grad_ptr(h, Bk + "attn_norm"),
+                             l > 0 ? reinterpret_cast<__nv_bfloat16*>(h.tw[3]) : nullptr);
+      dX16_ready = l > 0;
+      check_launch("attention backward");
+      continue;
+    }
     gemm_rm16(h, false, true, Mkv, d, d, dK16, d, Wk16, d, dxn, d, false);
     gemm_rm16(h, false, true, Mkv, d, d, dV16, d, Wv16, d, dxn, d, false, 1.f);
     k_scatter_add_rows<<<(M + 7) / 8, 256, 0, h.stream>>>(dxq, L.query_rows, B, L.Rq, L.Rkv, d, dxn);
