@@ -57,7 +57,7 @@ struct AttnBwdTcArgs {
   const float* lse;          // [BH, Rq] log2-domain
   const float* D;            // [BH, Rq]
   float* out0;               // kDQ: dq; else dk   (token-major fp32 [B*R, H*DK])
-  float* out1;               // dv (kDQ: unused)
+  float* out1;               // dv (kDQ: unused; may be null when only out1_16 is wanted)
   __nv_bfloat16* out1_16;    // optional bf16 copy of dv
   int BH, H, Rq, Rkv, nX;
   float scale_log2, scale;
@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(kAttnThreads, 2)
           for (int i = 0; i < DH; i += 4) {
             *reinterpret_cast<float4*>(a.out0 + o + i) =
                 make_float4(o1[i] * a.scale, o1[i + 1] * a.scale, o1[i + 2] * a.scale, o1[i + 3] * a.scale);
-            *reinterpret_cast<float4*>(a.out1 + o + i) = make_float4(o0[i], o0[i + 1], o0[i + 2], o0[i + 3]);
+            if (a.out1) *reinterpret_cast<float4*>(a.out1 + o + i) = make_float4(o0[i], o0[i + 1], o0[i + 2], o0[i + 3]);
           }
           if (a.out1_16) {
 #pragma unroll

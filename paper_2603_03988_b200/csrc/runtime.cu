@@ -1888,7 +1888,9 @@ static void backward_device(Handle& h, int B, const float* dz) {
     gemm_rm16(h, true, false, d, d, M, Hm, d, dXr16, d, grad_ptr(h, A + "wo"), d, false);
     gemm_rm16(h, false, true, M, d, d, dXr16, d, Wo16, d, dH, d, false);
     float* Dd = h.tw[15];
-    k_gate_bwd_rows<<<warp_rows_grid(M), 256, 0, h.stream>>>(dH, T.g, T.o_pre, M, L.Rq, H, dk, dO, h.dO16, dgraw,
+    // fp32 dO only for the SIMT attention backward; the tcgen05 / mma.sync kernels read dO16
+    k_gate_bwd_rows<<<warp_rows_grid(M), 256, 0, h.stream>>>(dH, T.g, T.o_pre, M, L.Rq, H, dk,
+                                                             (h.attn_bwd_tc || h.attn_bwd_mma) ? nullptr : dO, h.dO16, dgraw,
                                                              Dd);
     __nv_bfloat16* xn = reinterpret_cast<__nv_bfloat16*>(h.tw[2]);
     __nv_bfloat16* xq = reinterpret_cast<__nv_bfloat16*>(h.tw[3]);
@@ -1942,7 +1944,8 @@ static void backward_device(Handle& h, int B, const float* dz) {
     ak.blk_off = T.dkv_off;
     ak.blk_iv = T.dkv_iv;
     if (h.attn_bwd_tc) {
-      attn_core_backward_tc(h, L, T, B, Dd, dQ, dK, dV,
+      // (only the bf16 dV feeds the GEMMs below: no fp32 copy)
+      attn_core_backward_tc(h, L, T, B, Dd, dQ, dK, nullptr,
                             reinterpret_cast<__nv_bfloat16*>(h.tw[12]) + 2 * static_cast<size_t>(h.train_B) * h.L0 * d);
     } else if (h.attn_bwd_mma) {
       AttnBwdMmaArgs am;
@@ -1997,15 +2000,16 @@ static void backward_device(Handle& h, int B, const float* dz) {
     __nv_bfloat16* dK16 = dQ16 + static_cast<size_t>(h.train_B) * h.L0 * d;
     __nv_bfloat16* dV16 = dK16 + static_cast<size_t>(h.train_B) * h.L0 * d;
     gemm_rm16(h, false, false, M, d, d, xqp, d, Wq16, d, raw, d, false);
-    // persistent grid (register-held gain partials per warp, one smem reduction per CTA)
+    // persistent grid (register-held gain partials per warp, one smem reduction per CTA); only
+    // the bf16 d(raw) feeds the GEMMs below, so the fp32 copy is not written
     const int qk_grid_q = std::max(1, std::min((M + 7) / 8, 4 * h.num_sms));
     k_qknorm_rope_bwd_v<1><<<qk_grid_q, 256, d * 4, h.stream>>>(dQ, raw, M, L.Rq, L.pos_q, h.rope, H, dk,
-                                                              w32(h, A + "qk_gain_q"), dQ, grad_ptr(h, A + "qk_gain_q"),
+                                                              w32(h, A + "qk_gain_q"), nullptr, grad_ptr(h, A + "qk_gain_q"),
                                                               dQ16);
     gemm_rm16(h, false, false, Mkv, d, d, xn, d, Wk16, d, raw, d, false);
     const int qk_grid_k = std::max(1, std::min((Mkv + 7) / 8, 4 * h.num_sms));
     k_qknorm_rope_bwd_v<1><<<qk_grid_k, 256, d * 4, h.stream>>>(dK, raw, Mkv, L.Rkv, L.pos_kv, h.rope, H, dk,
-                                                              w32(h, A + "qk_gain_k"), dK, grad_ptr(h, A + "qk_gain_k"),
+                                                              w32(h, A + "qk_gain_k"), nullptr, grad_ptr(h, A + "qk_gain_k"),
                                                               dK16);
     if (!h.attn_bwd_mma && !h.attn_bwd_tc) k_f32_to_bf16<<<ew_grid(nkv), 256, 0, h.stream>>>(dV, nkv, dV16);  // (SIMT path)
     check_launch("qknorm/rope backward");

@@ -361,8 +361,10 @@ __global__ void __launch_bounds__(256) k_gate_bwd_rows(const float* __restrict__
       dot = fmaf(dov[2 * q], ob.x, fmaf(dov[2 * q + 1], ob.y, dot));
       pk[q] = pack_bf16x2(dov[2 * q], dov[2 * q + 1]);
     }
-    reinterpret_cast<float4*>(dO + o)[0] = make_float4(dov[0], dov[1], dov[2], dov[3]);
-    reinterpret_cast<float4*>(dO + o)[1] = make_float4(dov[4], dov[5], dov[6], dov[7]);
+    if (dO) {  // (null: the tensor-core attention backward reads only dO16)
+      reinterpret_cast<float4*>(dO + o)[0] = make_float4(dov[0], dov[1], dov[2], dov[3]);
+      reinterpret_cast<float4*>(dO + o)[1] = make_float4(dov[4], dov[5], dov[6], dov[7]);
+    }
     *reinterpret_cast<int4*>(dgraw + o) = make_int4(pack_bf16x2(dgr[0], dgr[1]), pack_bf16x2(dgr[2], dgr[3]),
                                                     pack_bf16x2(dgr[4], dgr[5]), pack_bf16x2(dgr[6], dgr[7]));
     *reinterpret_cast<int4*>(dO16 + o) = make_int4(pk[0], pk[1], pk[2], pk[3]);
@@ -795,7 +797,7 @@ __global__ void __launch_bounds__(128, 4) k_attn_bwd_mma(const AttnBwdMmaArgs a)
 // QKNorm + RoPE backward (attention.cpp:177-183): dx_rot -> inverse RoPE at the row's position
 // (rope.hpp:13-40, angle -> -angle) -> per-head RMSNorm backward against the raw projection
 // `raw` with gain g[h]; drot and draw may alias (each lane reads its elements before writing
-// them). One warp per row, lane owns 8 contiguous
+// them); draw may be null when only the bf16 copy draw16 is wanted. One warp per row, lane owns 8 contiguous
 // elements (4 rotation pairs) of chunk c = lane + 32 i, so a head spans dk / 8 aligned lanes and
 // both per-head reductions are 1-3 shuffle steps; 32-byte loads and stores. Gain-gradient
 // partials stay in registers across the warp's rows (grid-stride), then one shared-memory
@@ -891,9 +893,11 @@ __global__ void __launch_bounds__(256) k_qknorm_rope_bwd_v(const float* drot, co
           gacc[i][k] = fmaf(dq[k], xh, gacc[i][k]);
           out[k] = (dq[k] * g[i][k] - proj * xh) * inv;
         }
-        float4* op = reinterpret_cast<float4*>(draw + static_cast<size_t>(w) * d + c * 8);
-        op[0] = make_float4(out[0], out[1], out[2], out[3]);
-        op[1] = make_float4(out[4], out[5], out[6], out[7]);
+        if (draw) {  // (null: only the bf16 copy is consumed -- the training GEMMs)
+          float4* op = reinterpret_cast<float4*>(draw + static_cast<size_t>(w) * d + c * 8);
+          op[0] = make_float4(out[0], out[1], out[2], out[3]);
+          op[1] = make_float4(out[4], out[5], out[6], out[7]);
+        }
         if (draw16) store8(draw16 + static_cast<size_t>(w) * d + c * 8, out);
       }
     }
